@@ -1,0 +1,193 @@
+/*
+ * traj.h -- C-ABI of libtraj.so: the quantum-trajectory time step of a monitored
+ * U(1) Gaussian (Slater-determinant) state on B200 (sm_100a).
+ *
+ * Paper: B. Fan, C. Yin, A. M. Garcia-Garcia, "Entanglement dynamics of monitored
+ * non-interacting fermions on GPUs", arXiv 2508.18468.  "P:NNN" cites a line of
+ * that paper's LaTeX source together with the section / equation.
+ * Q-numbers are the readings of ambiguous passages listed in DESIGN.md.
+ *
+ * State of one trajectory (App. A): |psi> = prod_k [sum_j U_jk c_j^dag] |vac>,
+ * U an L x N complex matrix with U^dag U = 1, N = L/2 (half filling).
+ * One step (north star; P:203-209 QSD, P:171-196 PM):
+ *   (a) U <- K U with K = exp(-i H~ dt), H~_ij = J delta_{i+-1,j}, dense;
+ *   (b) n_i = sum_k |U_ik|^2, then the monitor: homodyne Eq. (A3) in split form, or
+ *       projective clicks with Born outcomes, Eq. (A1)/(A2) (sign-corrected A2, Q15);
+ *   (c) CholeskyQR2: G = U^dag U, R^dag R = G, U <- U R^-1, twice ("QR ... after each step").
+ * At sampled times: C_A = U_A U_A^dag, S_A = -sum[l ln l + (1-l) ln(1-l)],
+ * I_2 = S_A + S_B - S_{AuB}.
+ *
+ * Conventions (all calls):
+ *   - Every call returns a traj_status; nothing aborts.  After TRAJ_EINVAL,
+ *     TRAJ_ECONFIG or TRAJ_EDOMAIN the handle stays usable.
+ *   - Calls are ordered on cfg.stream and asynchronous, except those returning host
+ *     values (traj_entropy, traj_mutual_info, traj_failed, traj_get_step), which
+ *     synchronise the stream.
+ *   - Complex numbers are complex128 stored as interleaved (re, im) doubles; matrices
+ *     are row-major.  The library copies traj_config; the caller owns every pointer it
+ *     passes and the workspace, which must outlive the handle.
+ *   - The library owns its cuSOLVER handle and events and frees them in traj_destroy.
+ *   - There is no CPU fallback: without a CUDA device, traj_init returns TRAJ_ECUDA.
+ *   - One handle per host thread.
+ */
+#ifndef TRAJ_H
+#define TRAJ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct traj_ctx* traj_handle;      /* opaque; owned by the library */
+
+typedef enum {
+  TRAJ_OK = 0,
+  TRAJ_EINVAL = 1,    /* bad argument to a call (null pointer, out-of-range index)        */
+  TRAJ_ECONFIG = 2,   /* invalid traj_config (mirrors SPEC's "config error = 2")           */
+  TRAJ_ENUMERIC = 3,  /* Cholesky breakdown / spectrum outside [-1e-8, 1+1e-8]; the
+                         trajectory is marked failed and excluded (never reseeded)        */
+  TRAJ_ECUDA = 4,     /* CUDA / cuSOLVER error, or no device                              */
+  TRAJ_ENCCL = 5,     /* reserved: NCCL error (row sharding, not in this build)           */
+  TRAJ_EDOMAIN = 6    /* overlapping regions, site index outside the lattice              */
+} traj_status;
+
+enum { TRAJ_PROJECTIVE = 0, TRAJ_HOMODYNE = 1 };
+/* Initial state (Q1, Q2): sites with (x + y) even occupied -- the Neel state
+ * |1010...> of P:173/P:198 (0-based even sites) in 1d, the checkerboard in 2d. */
+enum { TRAJ_INIT_NEEL = 0 };
+
+typedef struct {
+  int32_t dim;              /* 1 or 2 (P:42 ring; P:123 square torus)                         */
+  int64_t Lx, Ly;           /* extents; Ly = 1 in 1d; L = Lx*Ly even (then exactly L/2 sites
+                               have x+y even); 2d needs Lx, Ly >= 3; site = y*Lx + x (Q2)     */
+  int64_t N;                /* particle number, must equal L/2                         */
+  double J, dt;             /* hopping J (J = 1) and time step dt > 0 (0.05)     */
+  int32_t protocol;         /* TRAJ_PROJECTIVE or TRAJ_HOMODYNE       */
+  int32_t init;             /* TRAJ_INIT_NEEL                                                  */
+  uint64_t seed;            /* Philox4x32-10 key (lo, hi words), Q9                            */
+  int64_t n_traj;           /* trajectories held by this handle, >= 1                          */
+  int64_t traj_base;        /* global id of the first one (Philox counter word 2)              */
+  const double* gamma;      /* host[n_traj]: per-site monitoring rate, gamma >= 0 (Q11);
+                               projective needs gamma*dt <= 1 (Q10)                            */
+  int32_t shard_rank;       /* row sharding is not built yet: must be 0                        */
+  int32_t shard_size;       /* must be 1                                                       */
+  const void* nccl_id;      /* must be NULL in this build                                       */
+  void* stream;             /* cudaStream_t the handle runs on (e.g. torch's current stream)   */
+  void* workspace;          /* device memory, >= traj_workspace_bytes, 256-byte aligned        */
+  size_t workspace_bytes;
+} traj_config;
+
+/* Device bytes the handle needs for cfg (the caller allocates them, e.g. with torch).
+ * Validates cfg; TRAJ_ECONFIG if invalid.  Needs a CUDA device (cuSOLVER query). */
+int traj_workspace_bytes(const traj_config* cfg, size_t* out);
+
+/* Validate cfg, build K = exp(-i H~ dt) on the device (1d: Bessel series of the
+ * circulant; 2d: K_y (x) K_x), set U0 = Neel / checkerboard for every trajectory,
+ * step counter = 0.  *out receives the handle. */
+int traj_init(const traj_config* cfg, traj_handle* out);
+
+/* Advance every trajectory by n_steps >= 0 steps (P:203-209 / P:171-196).  Step s
+ * draws Philox counters (site, s, traj_base + t, 0).  Asynchronous for the homodyne
+ * protocol; the projective protocol synchronises once per step to size its click
+ * list.  A trajectory whose Cholesky breaks down is marked failed (traj_failed). */
+int traj_step(traj_handle h, int64_t n_steps);
+
+/* Re-orthonormalise every trajectory with CholeskyQR2 (step (c) alone). */
+int traj_orthonormalize(traj_handle h);
+
+/* Entanglement entropy of region A (host array of nA distinct site indices in
+ * [0, L)) for every trajectory: S_out = host[n_traj].  eigvalsh of
+ * C_A = U_A U_A^dag (or U_A^dag U_A when nA > N) by cuSOLVER.  Returns TRAJ_ENUMERIC
+ * if some eigenvalue is outside [-1e-8, 1+1e-8] (that trajectory's S_out is NaN and
+ * it is marked failed); failed trajectories give NaN. */
+int traj_entropy(traj_handle h, const int64_t* A, int64_t nA, double* S_out);
+
+/* I_2 = S_A + S_B - S_{AuB} for every trajectory; A and B must be disjoint
+ * (TRAJ_EDOMAIN otherwise). */
+int traj_mutual_info(traj_handle h, const int64_t* A, int64_t nA,
+                     const int64_t* B, int64_t nB, double* I_out);
+
+/* n_out = device[n_traj][L] doubles: n_i = sum_k |U_ik|^2 of the current state. */
+int traj_occupations(traj_handle h, double* n_out);
+
+/* Rows [row0, row0+nrows) of C = U U^dag for trajectory traj into C_out =
+ * device complex128 [nrows][L]. */
+int traj_correlation_rows(traj_handle h, int64_t traj, int64_t row0, int64_t nrows, void* C_out);
+
+/* Copy U (L x N, complex128 row-major, ld = N) of trajectory traj out of / into the
+ * handle.  The pointer may be host or device (UVA copy).  traj_set_state does not
+ * orthonormalise: call traj_orthonormalize (or traj_step) afterwards. */
+int traj_get_state(traj_handle h, int64_t traj, void* U_out);
+int traj_set_state(traj_handle h, int64_t traj, const void* U_in);
+
+/* Step counter (the Philox step word of the next step); set for checkpoint/resume. */
+int traj_get_step(traj_handle h, int64_t* step);
+int traj_set_step(traj_handle h, int64_t step);
+
+/* *flag = 1 if trajectory traj failed (Cholesky breakdown or bad spectrum). */
+int traj_failed(traj_handle h, int64_t traj, int32_t* flag);
+
+/* Clicks of the last projective step of trajectory traj: |S| and the number of
+ * "occupied" outcomes. */
+int traj_last_clicks(traj_handle h, int64_t traj, int64_t* n_clicks, int64_t* n_occupied);
+
+/* Per-phase device timing with CUDA events on the handle's stream.  enable != 0
+ * starts recording (and zeroes the totals).  traj_phase_times fills ms[TRAJ_NPHASES]
+ * with accumulated milliseconds and launches[TRAJ_NPHASES] with kernel-launch counts
+ * (synchronises).  Phases: */
+enum { TRAJ_PH_PROPAGATE = 0,  /* U <- K U                                   */
+       TRAJ_PH_MONITOR = 1,    /* occupations + homodyne factor / click draw */
+       TRAJ_PH_PROJECT = 2,    /* click list, D_SS, sampling, rank-k update  */
+       TRAJ_PH_GRAM = 3,       /* G = U^dag U (both CQR passes)              */
+       TRAJ_PH_CHOL = 4,       /* Cholesky + triangular inverse of G         */
+       TRAJ_PH_TRMM = 5,       /* U <- U R^-1                                */
+       TRAJ_NPHASES = 6 };
+int traj_profile(traj_handle h, int enable);
+int traj_phase_times(traj_handle h, double* ms, int64_t* launches);
+
+/* Kernels launched by the library in this process so far (every launch site counts). */
+long long traj_kernel_launches(void);
+
+int traj_destroy(traj_handle h);
+/* Message of the last failure on h (h = NULL: the last failure of a handle-less call
+ * on this thread, e.g. traj_init). */
+const char* traj_last_error(traj_handle h);
+const char* traj_strerror(int status);
+
+/* ---------------------------------------------------------------------------
+ * Building blocks, exported for kernel-level tests.  Device pointers; all
+ * matrices complex128 row-major with leading dimension ld (in complex elements,
+ * ld >= columns, ld*16 a multiple of 16 bytes).
+ *
+ * traj_zgemm: C_b = alpha * op(A_b) op(B_b) + beta * C_b for b in [0, batch),
+ *   op(X) = X (op = 0) or X^dag (op = 1); op(A) is M x K, op(B) is K x N.
+ *   X_b = X + b*strideX (strideX in complex elements; 0 shares X across the batch).
+ *   flags: TRAJ_TRI_* declare a triangular operand whose other triangle is
+ *   stored as zeros (k-blocks that are all zero are skipped); TRAJ_C_UPPER writes
+ *   only entries with row <= col (and skips tiles below the diagonal).
+ *   The FP64 tensor pipe (DMMA) does the arithmetic; 8mnk flops. */
+enum { TRAJ_TRI_A_UPPER = 1, TRAJ_TRI_A_LOWER = 2, TRAJ_TRI_B_UPPER = 4,
+       TRAJ_TRI_B_LOWER = 8, TRAJ_C_UPPER = 16 };
+int traj_zgemm(void* stream, int opA, int opB, int64_t M, int64_t N, int64_t K,
+               double alpha_re, double alpha_im,
+               const void* A, int64_t lda, int64_t strideA,
+               const void* B, int64_t ldb, int64_t strideB,
+               double beta, void* C, int64_t ldc, int64_t strideC,
+               int64_t batch, int flags);
+
+/* traj_chol_inverse: for each b, G_b (n x n Hermitian positive definite; only the
+ * upper triangle is read) = R^dag R with R upper triangular; writes X_b = R^-1
+ * (upper triangle; the strict lower triangle is set to zero).  G_b's strict lower
+ * triangle is used as scratch.  scratch: device, >= traj_chol_scratch_bytes(n, batch).
+ * failed: device int32[batch]; set to 1 where a pivot is not positive/finite. */
+size_t traj_chol_scratch_bytes(int64_t n, int64_t batch);
+int traj_chol_inverse(void* stream, int64_t n, void* G, int64_t ldg, int64_t strideG,
+                      void* X, int64_t ldx, int64_t strideX, int64_t batch,
+                      void* scratch, int32_t* failed);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TRAJ_H */

@@ -1,0 +1,402 @@
+// Monitoring kernels of the trajectory step and small helpers.
+//
+// Homodyne / QSD (Eq. A3, split form, readings Q5-Q8): one CTA per row i of
+// one trajectory reads the row once into registers, reduces n_i = sum_k |U_ik|^2
+// (warp shuffles + one smem pass), draws Philox4x32-10 at counter
+// (i, step, traj_global, 0), forms a_i = sqrt(gamma dt) z_i + (2 n_i - 1) gamma dt with
+// z_i = sqrt(-2 ln(1-u0)) cos(2 pi u1) and writes exp(a_i) * row back: one HBM read and
+// one write of U (32 L N bytes per trajectory-step, the HBM roofline of this phase).
+//
+// Projective / PM (readings Q10, Q13, Q16, Q17): sites click iff
+// u0 < gamma dt; the click list S (ascending) is sampled sequentially on
+// C_SS = U_S U_S^dag with the Schur-complement update of Eq. (A1) / sign-corrected (A2):
+//     C <- C - C[:,t] C[t,:] / pivot,  pivot = C_tt (occupied) or C_tt - 1 (empty).
+#include <math.h>
+#include "common.cuh"
+#include "monitor.h"
+
+namespace traj {
+
+namespace {
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+template <int BS>
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (BS == 32) return v;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < BS / 32 ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) red[0] = s;
+  }
+  __syncthreads();
+  return red[0];
+}
+
+// mode 0: occupations only; mode 1: homodyne scaling (and occupations)
+template <int BS, int VPT>
+__global__ void __launch_bounds__(BS) row_monitor_kernel(cplx* U, long long ld, long long sU, int L, int N, int mode,
+                                                         long long step, long long traj_base, uint32_t k0, uint32_t k1,
+                                                         const double* gamma, double dt, double* n_out) {
+  __shared__ double red[32];
+  __shared__ double fac;
+  const int i = blockIdx.x, t = blockIdx.y;
+  cplx* row = U + t * sU + (long long)i * ld;
+  double s = 0.0;
+  double2 v[VPT > 0 ? VPT : 1];
+  if (VPT > 0) {
+#pragma unroll
+    for (int q = 0; q < VPT; ++q) {
+      const int k = threadIdx.x + q * BS;
+      v[q] = k < N ? row[k] : make_double2(0.0, 0.0);
+      s += v[q].x * v[q].x + v[q].y * v[q].y;
+    }
+  } else {
+    for (int k = threadIdx.x; k < N; k += BS) {
+      const double2 w = row[k];
+      s += w.x * w.x + w.y * w.y;
+    }
+  }
+  const double n = block_sum<BS>(s, red);
+  if (threadIdx.x == 0) {
+    if (n_out) n_out[(long long)t * L + i] = n;
+    if (mode == 1) {
+      const u32x4 x = philox4x32_10(u32x4{(uint32_t)i, (uint32_t)step, (uint32_t)(traj_base + t), 0u}, k0, k1);
+      const double u0 = u53(x.x, x.y), u1 = u53(x.z, x.w);
+      const double z = sqrt(-2.0 * log(1.0 - u0)) * cos(2.0 * M_PI * u1);
+      const double gdt = gamma[t] * dt;
+      fac = exp(sqrt(gdt) * z + (2.0 * n - 1.0) * gdt);
+    }
+  }
+  if (mode != 1) return;
+  __syncthreads();
+  const double f = fac;
+  if (VPT > 0) {
+#pragma unroll
+    for (int q = 0; q < VPT; ++q) {
+      const int k = threadIdx.x + q * BS;
+      if (k < N) row[k] = make_double2(f * v[q].x, f * v[q].y);
+    }
+  } else {
+    for (int k = threadIdx.x; k < N; k += BS) {
+      const double2 w = row[k];
+      row[k] = make_double2(f * w.x, f * w.y);
+    }
+  }
+}
+
+__global__ void click_draw_kernel(int L, long long step, long long traj_base, uint32_t k0, uint32_t k1,
+                                  const double* gamma, double dt, int32_t* flags) {
+  const int t = blockIdx.y;
+  const double p = gamma[t] * dt;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x) {
+    const u32x4 x = philox4x32_10(u32x4{(uint32_t)i, (uint32_t)step, (uint32_t)(traj_base + t), 0u}, k0, k1);
+    flags[(long long)t * L + i] = u53(x.x, x.y) < p ? 1 : 0;
+  }
+}
+
+// one CTA (1024 threads) per trajectory: ascending list of flagged sites
+__global__ void __launch_bounds__(1024) compact_kernel(const int32_t* flags, int L, int32_t* list, int cap,
+                                                       int32_t* count) {
+  __shared__ int wsum[32];
+  __shared__ int base;
+  const int t = blockIdx.x;
+  const int32_t* f = flags + (long long)t * L;
+  int32_t* out = list + (long long)t * cap;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < L; c0 += 1024) {
+    const int i = c0 + threadIdx.x;
+    const int fl = i < L ? f[i] : 0;
+    const unsigned b = __ballot_sync(0xffffffffu, fl);
+    const int before = __popc(b & ((1u << l) - 1u));
+    if (l == 0) wsum[w] = __popc(b);
+    __syncthreads();
+    int off = 0;
+    for (int q = 0; q < w; ++q) off += wsum[q];
+    const int pos = base + off + before;
+    if (fl && pos < cap) out[pos] = i;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int q = 0; q < 32; ++q) tot += wsum[q];
+      base += tot;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) count[t] = base;
+}
+
+// dst[t][r][:] = src[t][idx[t][r]][:] for r < count[t]
+__global__ void gather_rows_kernel(const cplx* src, long long lds, long long sS, const int32_t* idx, long long sIdx,
+                                   const int32_t* count, int fixed_count, cplx* dst, long long ldd, long long sD,
+                                   int ncols) {
+  const int t = blockIdx.z;
+  const int r = blockIdx.y;
+  const int cnt = count ? count[t] : fixed_count;
+  if (r >= cnt) return;
+  const long long srow = idx[t * sIdx + r];
+  const cplx* s = src + t * sS + srow * lds;
+  cplx* d = dst + t * sD + (long long)r * ldd;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ncols; k += gridDim.x * blockDim.x) d[k] = s[k];
+}
+
+__device__ __forceinline__ bool decide(double p, double u1) {
+  p = fmin(fmax(p, 0.0), 1.0);
+  bool occ = u1 < p;
+  if (occ && p < 1e-12) occ = false;
+  else if (!occ && (1.0 - p) < 1e-12) occ = true;
+  return occ;
+}
+
+// Sequential conditional Born sampling on C_SS (one CTA per trajectory).  D0: the GEMM
+// output (kept), Dw: work copy.  Outputs occ[t][r], pos1 (indices r with occ), S1/S0 site
+// lists and counts (k1, k0).
+__global__ void __launch_bounds__(1024) sample_kernel(const cplx* D0, cplx* Dw, long long ldd, long long sD,
+                                                      const int32_t* S, int cap, const int32_t* count,
+                                                      long long step, long long traj_base, uint32_t key0,
+                                                      uint32_t key1, int32_t* occ, int32_t* pos1, int32_t* S1,
+                                                      int32_t* S0, int32_t* k1_out, int32_t* k0_out) {
+  __shared__ double2 piv_inv;
+  const int t = blockIdx.x;
+  const int m = count[t] < cap ? count[t] : cap;
+  const cplx* d0 = D0 + t * sD;
+  cplx* D = Dw + t * sD;
+  const int32_t* s = S + (long long)t * cap;
+  int32_t* oc = occ + (long long)t * cap;
+  for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
+    const int i = idx / m, k = idx % m;
+    D[(long long)i * ldd + k] = d0[(long long)i * ldd + k];
+  }
+  __syncthreads();
+  for (int r = 0; r < m; ++r) {
+    if (threadIdx.x == 0) {
+      const int site = s[r];
+      const u32x4 x = philox4x32_10(u32x4{(uint32_t)site, (uint32_t)step, (uint32_t)(traj_base + t), 0u}, key0, key1);
+      const double u1 = u53(x.z, x.w);
+      const double p = D[(long long)r * ldd + r].x;
+      const bool o = decide(p, u1);
+      oc[r] = o ? 1 : 0;
+      const double pv = o ? p : p - 1.0;
+      piv_inv = make_double2(1.0 / pv, 0.0);
+    }
+    __syncthreads();
+    const int mm = m - r - 1;
+    const double inv = piv_inv.x;
+    for (int idx = threadIdx.x; idx < mm * mm; idx += blockDim.x) {
+      const int i = r + 1 + idx / mm, k = r + 1 + idx % mm;
+      const double2 a = D[(long long)i * ldd + r], b = D[(long long)r * ldd + k];
+      const double2 p = cmul(a, b);
+      double2& dst = D[(long long)i * ldd + k];
+      dst.x -= p.x * inv;
+      dst.y -= p.y * inv;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int n1 = 0, n0 = 0;
+    for (int r = 0; r < m; ++r) {
+      if (oc[r]) {
+        pos1[(long long)t * cap + n1] = r;
+        S1[(long long)t * cap + n1] = s[r];
+        ++n1;
+      } else {
+        S0[(long long)t * cap + n0] = s[r];
+        ++n0;
+      }
+    }
+    k1_out[t] = n1;
+    k0_out[t] = n0;
+  }
+}
+
+// D11[a][b] = D0[pos[a]][pos[b]]
+__global__ void gather_sub_kernel(const cplx* D0, long long ld0, const int32_t* pos, int k, cplx* D11, long long ld1) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < k * k; idx += gridDim.x * blockDim.x) {
+    const int a = idx / k, b = idx % k;
+    D11[(long long)a * ld1 + b] = D0[(long long)pos[a] * ld0 + pos[b]];
+  }
+}
+
+// T[S1[c]][c] -= 1
+__global__ void sub_identity_kernel(cplx* T, long long ld, const int32_t* S1, int k) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < k) T[(long long)S1[c] * ld + c].x -= 1.0;
+}
+
+__global__ void zero_rows_kernel(cplx* U, long long ld, const int32_t* rows, int nrows, int ncols) {
+  const int r = blockIdx.y;
+  if (r >= nrows) return;
+  cplx* p = U + (long long)rows[r] * ld;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ncols; k += gridDim.x * blockDim.x)
+    p[k] = make_double2(0.0, 0.0);
+}
+
+// S = -sum[l ln l + (1-l) ln(1-l)] over n eigenvalues, l clamped to [0, 1];
+// bad = 1 if some l is outside [-1e-8, 1+1e-8] or not finite.
+__global__ void __launch_bounds__(256) entropy_kernel(const double* lam, int n, double* S_out, int32_t* bad) {
+  __shared__ double red[32];
+  __shared__ int badf;
+  if (threadIdx.x == 0) badf = 0;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += 256) {
+    double l = lam[i];
+    if (!(l >= -1e-8 && l <= 1.0 + 1e-8)) badf = 1;
+    l = fmin(fmax(l, 0.0), 1.0);
+    if (l > 0.0 && l < 1.0) s -= l * log(l) + (1.0 - l) * log(1.0 - l);
+  }
+  const double tot = block_sum<256>(s, red);
+  if (threadIdx.x == 0) {
+    *S_out = badf ? nan("") : tot;
+    if (badf) *bad = 1;
+  }
+}
+
+__global__ void build_k_kernel(cplx* K, long long ld, int Lx, int Ly, const cplx* kx, const cplx* ky) {
+  const long long L = (long long)Lx * Ly;
+  const long long total = L * L;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long i = idx / L, j = idx % L;
+    const int ix = (int)(i % Lx), iy = (int)(i / Lx), jx = (int)(j % Lx), jy = (int)(j / Lx);
+    const int dx = ((jx - ix) % Lx + Lx) % Lx, dy = ((jy - iy) % Ly + Ly) % Ly;
+    K[i * ld + j] = cmul(kx[dx], ky[dy]);
+  }
+}
+
+__global__ void init_state_kernel(cplx* U, long long ld, long long sU, const int32_t* sites, int N) {
+  const int t = blockIdx.y;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < N) U[t * sU + (long long)sites[k] * ld + k] = make_double2(1.0, 0.0);
+}
+
+cudaError_t last(std::string* err, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && err) *err = std::string(what) + ": " + cudaGetErrorString(e);
+  return e;
+}
+
+template <int BS, int VPT>
+void launch_row(cudaStream_t st, dim3 grid, cplx* U, long long ld, long long sU, int L, int N, int mode,
+                long long step, long long traj_base, uint32_t k0, uint32_t k1, const double* gamma, double dt,
+                double* n_out) {
+  row_monitor_kernel<BS, VPT><<<grid, BS, 0, st>>>(U, ld, sU, L, N, mode, step, traj_base, k0, k1, gamma, dt, n_out);
+}
+
+}  // namespace
+
+int row_monitor(cudaStream_t st, cplx* U, long long ld, long long sU, int L, int N, int T, int mode, long long step,
+                long long traj_base, uint64_t seed, const double* gamma_dev, double dt, double* n_out,
+                std::string* err) {
+  dim3 grid(L, T);
+  const uint32_t k0 = (uint32_t)(seed & 0xffffffffu), k1 = (uint32_t)(seed >> 32);
+#define ROW(BS, VPT) launch_row<BS, VPT>(st, grid, U, ld, sU, L, N, mode, step, traj_base, k0, k1, gamma_dev, dt, n_out)
+  if (N <= 32) ROW(32, 1);
+  else if (N <= 64) ROW(32, 2);
+  else if (N <= 128) ROW(32, 4);
+  else if (N <= 256) ROW(256, 1);
+  else if (N <= 512) ROW(256, 2);
+  else if (N <= 1024) ROW(256, 4);
+  else if (N <= 2048) ROW(256, 8);
+  else if (N <= 4096) ROW(256, 16);
+  else if (N <= 8192) ROW(256, 32);
+  else if (N <= 16384) ROW(256, 64);
+  else ROW(256, 0);
+#undef ROW
+  count_launch();
+  return last(err, "row_monitor") == cudaSuccess ? 0 : 4;
+}
+
+int click_draw(cudaStream_t st, int L, int T, long long step, long long traj_base, uint64_t seed,
+               const double* gamma_dev, double dt, int32_t* flags, std::string* err) {
+  dim3 grid((unsigned)std::min<long long>(ceil_div(L, 256), 4096), T);
+  click_draw_kernel<<<grid, 256, 0, st>>>(L, step, traj_base, (uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32),
+                                          gamma_dev, dt, flags);
+  count_launch();
+  return last(err, "click_draw") == cudaSuccess ? 0 : 4;
+}
+
+int compact(cudaStream_t st, const int32_t* flags, int L, int T, int32_t* list, int cap, int32_t* count,
+            std::string* err) {
+  compact_kernel<<<T, 1024, 0, st>>>(flags, L, list, cap, count);
+  count_launch();
+  return last(err, "compact") == cudaSuccess ? 0 : 4;
+}
+
+int gather_rows(cudaStream_t st, const cplx* src, long long lds, long long sS, const int32_t* idx, long long sIdx,
+                const int32_t* count_dev, int rows, int T, cplx* dst, long long ldd, long long sD, int ncols,
+                std::string* err) {
+  if (rows <= 0 || T <= 0) return 0;
+  dim3 grid((unsigned)std::min<long long>(ceil_div(ncols, 256), 64), rows, T);
+  gather_rows_kernel<<<grid, 256, 0, st>>>(src, lds, sS, idx, sIdx, count_dev, rows, dst, ldd, sD, ncols);
+  count_launch();
+  return last(err, "gather_rows") == cudaSuccess ? 0 : 4;
+}
+
+int sample_outcomes(cudaStream_t st, const cplx* D0, cplx* Dw, long long ldd, long long sD, const int32_t* S, int cap,
+                    const int32_t* count, int T, long long step, long long traj_base, uint64_t seed, int32_t* occ,
+                    int32_t* pos1, int32_t* S1, int32_t* S0, int32_t* k1, int32_t* k0, std::string* err) {
+  sample_kernel<<<T, 1024, 0, st>>>(D0, Dw, ldd, sD, S, cap, count, step, traj_base, (uint32_t)(seed & 0xffffffffu),
+                                    (uint32_t)(seed >> 32), occ, pos1, S1, S0, k1, k0);
+  count_launch();
+  return last(err, "sample") == cudaSuccess ? 0 : 4;
+}
+
+int gather_sub(cudaStream_t st, const cplx* D0, long long ld0, const int32_t* pos, int k, cplx* D11, long long ld1,
+               std::string* err) {
+  if (k <= 0) return 0;
+  gather_sub_kernel<<<(unsigned)std::min<long long>(ceil_div((long long)k * k, 256), 4096), 256, 0, st>>>(D0, ld0, pos,
+                                                                                                       k, D11, ld1);
+  count_launch();
+  return last(err, "gather_sub") == cudaSuccess ? 0 : 4;
+}
+
+int sub_identity(cudaStream_t st, cplx* T, long long ld, const int32_t* S1, int k, std::string* err) {
+  if (k <= 0) return 0;
+  sub_identity_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(T, ld, S1, k);
+  count_launch();
+  return last(err, "sub_identity") == cudaSuccess ? 0 : 4;
+}
+
+int zero_rows(cudaStream_t st, cplx* U, long long ld, const int32_t* rows, int nrows, int ncols, std::string* err) {
+  if (nrows <= 0) return 0;
+  dim3 grid((unsigned)std::min<long long>(ceil_div(ncols, 256), 64), nrows);
+  zero_rows_kernel<<<grid, 256, 0, st>>>(U, ld, rows, nrows, ncols);
+  count_launch();
+  return last(err, "zero_rows") == cudaSuccess ? 0 : 4;
+}
+
+int entropy_reduce(cudaStream_t st, const double* lam, int n, double* S_out, int32_t* bad, std::string* err) {
+  entropy_kernel<<<1, 256, 0, st>>>(lam, n, S_out, bad);
+  count_launch();
+  return last(err, "entropy") == cudaSuccess ? 0 : 4;
+}
+
+int build_k(cudaStream_t st, cplx* K, long long ld, int Lx, int Ly, const cplx* kx, const cplx* ky, std::string* err) {
+  const long long L = (long long)Lx * Ly;
+  build_k_kernel<<<(unsigned)std::min<long long>(ceil_div(L * L, 256), 148 * 64), 256, 0, st>>>(K, ld, Lx, Ly, kx, ky);
+  count_launch();
+  return last(err, "build_k") == cudaSuccess ? 0 : 4;
+}
+
+int init_state(cudaStream_t st, cplx* U, long long ld, long long sU, const int32_t* sites, int N, int T,
+               std::string* err) {
+  dim3 grid((unsigned)ceil_div(N, 256), T);
+  init_state_kernel<<<grid, 256, 0, st>>>(U, ld, sU, sites, N);
+  count_launch();
+  return last(err, "init_state") == cudaSuccess ? 0 : 4;
+}
+
+}  // namespace traj

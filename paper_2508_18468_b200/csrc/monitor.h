@@ -1,0 +1,31 @@
+// Internal interface of the monitoring kernels and helpers (monitor.cu).
+#pragma once
+#include <string>
+#include "common.cuh"
+
+namespace traj {
+
+// mode 0: n_out[t][i] = sum_k |U_ik|^2; mode 1: also U_i. *= exp(a_i) (homodyne, Eq. A3).
+int row_monitor(cudaStream_t st, cplx* U, long long ld, long long sU, int L, int N, int T, int mode, long long step,
+                long long traj_base, uint64_t seed, const double* gamma_dev, double dt, double* n_out,
+                std::string* err);
+int click_draw(cudaStream_t st, int L, int T, long long step, long long traj_base, uint64_t seed,
+               const double* gamma_dev, double dt, int32_t* flags, std::string* err);
+int compact(cudaStream_t st, const int32_t* flags, int L, int T, int32_t* list, int cap, int32_t* count,
+            std::string* err);
+int gather_rows(cudaStream_t st, const cplx* src, long long lds, long long sS, const int32_t* idx, long long sIdx,
+                const int32_t* count_dev, int rows, int T, cplx* dst, long long ldd, long long sD, int ncols,
+                std::string* err);
+int sample_outcomes(cudaStream_t st, const cplx* D0, cplx* Dw, long long ldd, long long sD, const int32_t* S, int cap,
+                    const int32_t* count, int T, long long step, long long traj_base, uint64_t seed, int32_t* occ,
+                    int32_t* pos1, int32_t* S1, int32_t* S0, int32_t* k1, int32_t* k0, std::string* err);
+int gather_sub(cudaStream_t st, const cplx* D0, long long ld0, const int32_t* pos, int k, cplx* D11, long long ld1,
+               std::string* err);
+int sub_identity(cudaStream_t st, cplx* T, long long ld, const int32_t* S1, int k, std::string* err);
+int zero_rows(cudaStream_t st, cplx* U, long long ld, const int32_t* rows, int nrows, int ncols, std::string* err);
+int entropy_reduce(cudaStream_t st, const double* lam, int n, double* S_out, int32_t* bad, std::string* err);
+int build_k(cudaStream_t st, cplx* K, long long ld, int Lx, int Ly, const cplx* kx, const cplx* ky, std::string* err);
+int init_state(cudaStream_t st, cplx* U, long long ld, long long sU, const int32_t* sites, int N, int T,
+               std::string* err);
+
+}  // namespace traj

@@ -1,0 +1,712 @@
+// C-ABI of libtraj.so (include/traj.h): handle, workspace, K construction, the
+// trajectory step and the sampled observables.  Host code only orchestrates; every
+// arithmetic step of the path runs in the kernels of zgemm.cu, cholinv.cu, monitor.cu
+// and (eigvalsh, the one vendor call allowed by the north star) cuSOLVER.
+#include <cusolverDn.h>
+#include <math.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <complex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/traj.h"
+#include "cholinv.h"
+#include "common.cuh"
+#include "monitor.h"
+#include "zgemm.h"
+
+namespace traj {
+std::atomic<long long> g_kernel_launches{0};
+}
+
+using namespace traj;
+
+struct traj_ctx {
+  traj_config cfg;
+  std::vector<double> gamma;
+  int L = 0, N = 0, Lx = 0, Ly = 0, T = 0, cap = 0;
+  long long ldN = 0, ldL = 0, ldcap = 0, sU = 0, sG = 0;
+  cudaStream_t st = nullptr;
+  cplx* K = nullptr;
+  cplx* U[2] = {nullptr, nullptr};
+  int cur = 0;
+  cplx* G = nullptr;
+  cplx* X = nullptr;
+  void* chol_scratch = nullptr;
+  double* gamma_dev = nullptr;
+  double* nbuf = nullptr;
+  int32_t* failed_dev = nullptr;
+  // projective
+  int32_t *flags = nullptr, *S = nullptr, *count = nullptr, *occ = nullptr, *pos1 = nullptr, *S1 = nullptr,
+          *S0 = nullptr, *k1 = nullptr, *k0 = nullptr;
+  cplx *US = nullptr, *D0 = nullptr, *Dw = nullptr, *D11 = nullptr, *X11 = nullptr, *W = nullptr, *Tm = nullptr;
+  void* chol_scratch_small = nullptr;
+  long long sUS = 0, sD = 0;
+  // observables
+  double* eig_w = nullptr;
+  cplx* eig_work = nullptr;
+  int lwork = 0;
+  int* eig_info = nullptr;
+  double* S_dev = nullptr;
+  int32_t* bad_dev = nullptr;
+  int32_t* region = nullptr;
+  cplx* kcoef = nullptr;
+  int32_t* sites = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  long long step = 0;
+  int32_t* h_small = nullptr;     // pinned host scratch
+  std::vector<int64_t> last_nS, last_n1;
+  std::string err;
+  // profiling
+  bool prof = false;
+  std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> evs;
+  std::vector<cudaEvent_t> pool;
+  double ms[TRAJ_NPHASES] = {0};
+  long long launches[TRAJ_NPHASES] = {0};
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(traj_ctx* h, int status, const std::string& msg) {
+  if (h) h->err = msg;
+  g_err = msg;
+  return status;
+}
+
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess) return fail(h, TRAJ_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+#define TRY(x)                        \
+  do {                                \
+    std::string m_;                   \
+    int s_ = (x);                     \
+    (void)m_;                         \
+    if (s_) return fail(h, s_, h->err); \
+  } while (0)
+
+struct Layout {
+  size_t off = 0;
+  char* base = nullptr;
+  template <typename P>
+  void take(P*& p, size_t bytes) {
+    off = (off + 255) & ~size_t(255);
+    p = base ? reinterpret_cast<P*>(base + off) : nullptr;
+    off += bytes;
+  }
+};
+
+int validate(const traj_config* c, std::string* why) {
+  auto bad = [&](const char* m) {
+    *why = m;
+    return TRAJ_ECONFIG;
+  };
+  if (!c) return bad("null config");
+  if (c->dim != 1 && c->dim != 2) return bad("dim must be 1 or 2");
+  if (c->dim == 1 && c->Ly != 1) return bad("1d needs Ly = 1");
+  if (c->dim == 1 && c->Lx < 2) return bad("1d needs Lx >= 2");
+  if (c->dim == 2 && (c->Lx < 3 || c->Ly < 3)) return bad("2d needs Lx, Ly >= 3");
+  const long long L = c->Lx * c->Ly;
+  if (L % 2) return bad("L = Lx*Ly must be even (half filling)");
+  if (L > (1ll << 20)) return bad("L too large");
+  if (c->N != L / 2) return bad("N must equal L/2 (P:43)");
+  if (!(c->dt > 0) || !isfinite(c->dt)) return bad("dt must be > 0");
+  if (!isfinite(c->J)) return bad("J must be finite");
+  if (c->protocol != TRAJ_PROJECTIVE && c->protocol != TRAJ_HOMODYNE) return bad("unknown protocol");
+  if (c->init != TRAJ_INIT_NEEL) return bad("unknown init");
+  if (c->n_traj < 1 || c->n_traj > 65535) return bad("n_traj must be in [1, 65535]");
+  if (c->traj_base < 0 || c->traj_base + c->n_traj > (1ll << 32)) return bad("trajectory ids must fit 32 bits");
+  if (!c->gamma) return bad("gamma is null");
+  for (long long t = 0; t < c->n_traj; ++t) {
+    const double g = c->gamma[t];
+    if (!(g >= 0) || !isfinite(g)) return bad("gamma must be >= 0 and finite");
+    if (c->protocol == TRAJ_PROJECTIVE && g * c->dt > 1.0) return bad("projective needs gamma*dt <= 1 (Q10)");
+  }
+  if (c->shard_rank != 0 || c->shard_size != 1) return bad("row sharding is not available in this build");
+  if (c->nccl_id) return bad("nccl_id must be NULL in this build");
+  return 0;
+}
+
+// click-list capacity: mean + 12 sigma + 64 of Binomial(L, p), at most L
+int click_capacity(long long L, const traj_config* c) {
+  if (c->protocol != TRAJ_PROJECTIVE) return 0;
+  double pmax = 0;
+  for (long long t = 0; t < c->n_traj; ++t) pmax = std::max(pmax, c->gamma[t] * c->dt);
+  const double m = L * pmax, sd = sqrt(L * pmax * (1 - pmax));
+  return (int)std::min<long long>(L, (long long)ceil(m + 12 * sd + 64));
+}
+
+size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
+  Layout lay;
+  lay.base = base;
+  const long long Lx = c->Lx, Ly = c->Ly, L = Lx * Ly, N = c->N, T = c->n_traj;
+  const long long ldN = round_up(N, 8), ldL = round_up(L, 8);
+  const int cap = click_capacity(L, c);
+  const long long ldcap = round_up(std::max(cap, 1), 8);
+  h->L = (int)L;
+  h->N = (int)N;
+  h->Lx = (int)Lx;
+  h->Ly = (int)Ly;
+  h->T = (int)T;
+  h->cap = cap;
+  h->ldN = ldN;
+  h->ldL = ldL;
+  h->ldcap = ldcap;
+  h->sU = L * ldN;
+  h->sG = N * ldN;
+  lay.take(h->K, (size_t)L * ldL * 16);
+  lay.take(h->U[0], (size_t)T * L * ldN * 16);
+  lay.take(h->U[1], (size_t)T * L * ldN * 16);
+  lay.take(h->G, (size_t)T * N * ldN * 16);
+  lay.take(h->X, (size_t)T * N * ldN * 16);
+  lay.take(h->chol_scratch, chol_scratch_bytes(N, T));
+  lay.take(h->gamma_dev, (size_t)T * 8);
+  lay.take(h->nbuf, (size_t)T * L * 8);
+  lay.take(h->failed_dev, (size_t)T * 4);
+  lay.take(h->eig_w, (size_t)N * 8);
+  lay.take(h->eig_work, (size_t)std::max(lwork, 1) * 16);
+  lay.take(h->eig_info, 16);
+  lay.take(h->S_dev, (size_t)T * 8);
+  lay.take(h->bad_dev, (size_t)T * 4);
+  lay.take(h->region, (size_t)L * 4);
+  lay.take(h->kcoef, (size_t)(Lx + Ly) * 16);
+  lay.take(h->sites, (size_t)N * 4);
+  if (cap > 0) {
+    h->sUS = (long long)cap * ldN;
+    h->sD = (long long)cap * ldcap;
+    lay.take(h->flags, (size_t)T * L * 4);
+    lay.take(h->S, (size_t)T * cap * 4);
+    lay.take(h->count, (size_t)T * 4);
+    lay.take(h->occ, (size_t)T * cap * 4);
+    lay.take(h->pos1, (size_t)T * cap * 4);
+    lay.take(h->S1, (size_t)T * cap * 4);
+    lay.take(h->S0, (size_t)T * cap * 4);
+    lay.take(h->k1, (size_t)T * 4);
+    lay.take(h->k0, (size_t)T * 4);
+    lay.take(h->US, (size_t)T * cap * ldN * 16);
+    lay.take(h->D0, (size_t)T * cap * ldcap * 16);
+    lay.take(h->Dw, (size_t)T * cap * ldcap * 16);
+    lay.take(h->D11, (size_t)cap * ldcap * 16);
+    lay.take(h->X11, (size_t)cap * ldcap * 16);
+    lay.take(h->chol_scratch_small, chol_scratch_bytes(cap, 1));
+    lay.take(h->W, (size_t)N * ldcap * 16);
+    lay.take(h->Tm, (size_t)L * ldcap * 16);
+  }
+  return lay.off + 256;
+}
+
+int eig_lwork(int N, int* lwork, std::string* why) {
+  cusolverDnHandle_t s;
+  if (cusolverDnCreate(&s) != CUSOLVER_STATUS_SUCCESS) {
+    *why = "cusolverDnCreate failed (no CUDA device?)";
+    return TRAJ_ECUDA;
+  }
+  int lw = 0;
+  cusolverStatus_t r = cusolverDnZheevd_bufferSize(s, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER, N, nullptr,
+                                                   N, nullptr, &lw);
+  cusolverDnDestroy(s);
+  if (r != CUSOLVER_STATUS_SUCCESS) {
+    *why = "cusolverDnZheevd_bufferSize failed";
+    return TRAJ_ECUDA;
+  }
+  *lwork = lw;
+  return 0;
+}
+
+// 1d coefficient row of K = exp(-i H~ dt) on a ring of n sites:
+//   K_{ij} = c[(j - i) mod n],  c_d = sum_{m in Z, m = d mod n} (-i)^|m| J_|m|(2 J dt)
+// (Jacobi-Anger generating function of the Bessel functions; H~ = J (T + T^-1)).
+std::vector<std::complex<double>> ring_coefficients(int n, double J, double dt) {
+  std::vector<std::complex<double>> c(n, 0.0);
+  const double x = 2.0 * J * dt;
+  const int mmax = (int)ceil(fabs(x)) + 80;
+  const std::complex<double> ph[4] = {{1, 0}, {0, -1}, {-1, 0}, {0, 1}};
+  for (int m = -mmax; m <= mmax; ++m) {
+    const int a = m < 0 ? -m : m;
+    const double jv = jn(a, x);
+    if (jv == 0.0) continue;
+    c[((m % n) + n) % n] += ph[a & 3] * jv;
+  }
+  return c;
+}
+
+struct Phase {
+  traj_ctx* h;
+  int ph;
+  cudaEvent_t a = nullptr, b = nullptr;
+  long long l0;
+  Phase(traj_ctx* h_, int p) : h(h_), ph(p), l0(g_kernel_launches.load()) {
+    if (!h->prof) return;
+    a = get();
+    cudaEventRecord(a, h->st);
+  }
+  cudaEvent_t get() {
+    if (!h->pool.empty()) {
+      cudaEvent_t e = h->pool.back();
+      h->pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  ~Phase() {
+    h->launches[ph] += g_kernel_launches.load() - l0;
+    if (!h->prof) return;
+    b = get();
+    cudaEventRecord(b, h->st);
+    h->evs.emplace_back(ph, a, b);
+  }
+};
+
+// CholeskyQR2 on U (state), tmp another buffer of the same shape; result in U.
+int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
+  cplx* src = U;
+  cplx* dst = tmp;
+  for (int pass = 0; pass < 2; ++pass) {
+    {
+      Phase p(h, TRAJ_PH_GRAM);
+      TRY(zgemm(h->st, 1, 0, h->N, h->N, h->L, 1.0, 0.0, src, h->ldN, h->sU, src, h->ldN, h->sU, 0.0, h->G, h->ldN,
+                h->sG, h->T, TRAJ_C_UPPER_F, &h->err));
+    }
+    {
+      Phase p(h, TRAJ_PH_CHOL);
+      TRY(chol_inverse(h->st, h->N, h->G, h->ldN, h->sG, h->X, h->ldN, h->sG, h->T, h->chol_scratch, h->failed_dev,
+                       &h->err));
+    }
+    {
+      Phase p(h, TRAJ_PH_TRMM);
+      TRY(zgemm(h->st, 0, 0, h->L, h->N, h->N, 1.0, 0.0, src, h->ldN, h->sU, h->X, h->ldN, h->sG, 0.0, dst, h->ldN,
+                h->sU, h->T, TRAJ_TRI_B_UPPER_F, &h->err));
+    }
+    std::swap(src, dst);
+  }
+  return 0;   // two passes: result back in U
+}
+
+int projective(traj_ctx* h, cplx* U) {
+  Phase p(h, TRAJ_PH_PROJECT);
+  const int T = h->T, cap = h->cap;
+  TRY(compact(h->st, h->flags, h->L, T, h->S, cap, h->count, &h->err));
+  CK(cudaMemcpyAsync(h->h_small, h->count, T * 4, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  int maxc = 0;
+  for (int t = 0; t < T; ++t) {
+    h->last_nS[t] = h->h_small[t];
+    h->last_n1[t] = 0;
+    if (h->h_small[t] > cap)
+      return fail(h, TRAJ_ENUMERIC, "click list overflow: " + std::to_string(h->h_small[t]) + " > capacity " +
+                                        std::to_string(cap));
+    maxc = std::max(maxc, h->h_small[t]);
+  }
+  if (maxc == 0) return 0;
+  TRY(gather_rows(h->st, U, h->ldN, h->sU, h->S, cap, h->count, maxc, T, h->US, h->ldN, h->sUS, h->N, &h->err));
+  // C_SS = U_S U_S^dag (all trajectories padded to maxc rows; rows beyond a trajectory's
+  // count are never read by the sampler)
+  TRY(zgemm(h->st, 0, 1, maxc, maxc, h->N, 1.0, 0.0, h->US, h->ldN, h->sUS, h->US, h->ldN, h->sUS, 0.0, h->D0,
+            h->ldcap, h->sD, T, 0, &h->err));
+  TRY(sample_outcomes(h->st, h->D0, h->Dw, h->ldcap, h->sD, h->S, cap, h->count, T, h->step, h->cfg.traj_base,
+                      h->cfg.seed, h->occ, h->pos1, h->S1, h->S0, h->k1, h->k0, &h->err));
+  CK(cudaMemcpyAsync(h->h_small, h->k1, T * 4, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaMemcpyAsync(h->h_small + T, h->k0, T * 4, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  for (int t = 0; t < T; ++t) {
+    const int k1 = h->h_small[t], k0 = h->h_small[T + t];
+    h->last_n1[t] = k1;
+    cplx* Ut = U + t * h->sU;
+    if (k1 > 0) {
+      const int32_t* pos1 = h->pos1 + (long long)t * cap;
+      const int32_t* S1 = h->S1 + (long long)t * cap;
+      TRY(gather_sub(h->st, h->D0 + t * h->sD, h->ldcap, pos1, k1, h->D11, h->ldcap, &h->err));
+      // R^dag R = C_{S1 S1},  X11 = R^-1
+      TRY(chol_inverse(h->st, k1, h->D11, h->ldcap, 0, h->X11, h->ldcap, 0, 1, h->chol_scratch_small,
+                       h->failed_dev + t, &h->err));
+      // U_{S1} rows -> US[t] (C_SS is already formed)
+      TRY(gather_rows(h->st, Ut, h->ldN, 0, S1, 0, nullptr, k1, 1, h->US + t * h->sUS, h->ldN, 0, h->N, &h->err));
+      // W = U_{S1}^dag R^-1   (N x k1)
+      TRY(zgemm(h->st, 1, 0, h->N, k1, k1, 1.0, 0.0, h->US + t * h->sUS, h->ldN, 0, h->X11, h->ldcap, 0, 0.0, h->W,
+                h->ldcap, 0, 1, TRAJ_TRI_B_UPPER_F, &h->err));
+      // Tm = U W - E_{S1}   (L x k1)
+      TRY(zgemm(h->st, 0, 0, h->L, k1, h->N, 1.0, 0.0, Ut, h->ldN, 0, h->W, h->ldcap, 0, 0.0, h->Tm, h->ldcap, 0, 1, 0,
+                &h->err));
+      TRY(sub_identity(h->st, h->Tm, h->ldcap, S1, k1, &h->err));
+      // U <- U - Tm W^dag
+      TRY(zgemm(h->st, 0, 1, h->L, h->N, k1, -1.0, 0.0, h->Tm, h->ldcap, 0, h->W, h->ldcap, 0, 1.0, Ut, h->ldN, 0, 1,
+                0, &h->err));
+    }
+    if (k0 > 0) TRY(zero_rows(h->st, Ut, h->ldN, h->S0 + (long long)t * cap, k0, h->N, &h->err));
+  }
+  return 0;
+}
+
+int one_step(traj_ctx* h) {
+  cplx* Uc = h->U[h->cur];
+  cplx* Un = h->U[1 - h->cur];
+  {
+    Phase p(h, TRAJ_PH_PROPAGATE);
+    // U <- K U  (K shared across the batch: stride 0)
+    TRY(zgemm(h->st, 0, 0, h->L, h->N, h->L, 1.0, 0.0, h->K, h->ldL, 0, Uc, h->ldN, h->sU, 0.0, Un, h->ldN, h->sU,
+              h->T, 0, &h->err));
+  }
+  if (h->cfg.protocol == TRAJ_HOMODYNE) {
+    Phase p(h, TRAJ_PH_MONITOR);
+    TRY(row_monitor(h->st, Un, h->ldN, h->sU, h->L, h->N, h->T, 1, h->step, h->cfg.traj_base, h->cfg.seed,
+                    h->gamma_dev, h->cfg.dt, nullptr, &h->err));
+  } else {
+    {
+      Phase p(h, TRAJ_PH_MONITOR);
+      TRY(click_draw(h->st, h->L, h->T, h->step, h->cfg.traj_base, h->cfg.seed, h->gamma_dev, h->cfg.dt, h->flags,
+                     &h->err));
+    }
+    int s = projective(h, Un);
+    if (s) return s;
+  }
+  int s = cqr2(h, Un, Uc);
+  if (s) return s;
+  h->cur = 1 - h->cur;
+  h->step += 1;
+  return 0;
+}
+
+int check_traj(traj_ctx* h, int64_t t) {
+  if (!h) return TRAJ_EINVAL;
+  if (t < 0 || t >= h->T) return fail(h, TRAJ_EINVAL, "trajectory index out of range");
+  return 0;
+}
+
+int entropy_impl(traj_ctx* h, const int64_t* A, int64_t nA, double* S_out) {
+  if (nA < 0 || (nA > 0 && !A) || !S_out) return fail(h, TRAJ_EINVAL, "bad region arguments");
+  std::vector<int32_t> idx(nA);
+  std::vector<char> seen(h->L, 0);
+  for (int64_t q = 0; q < nA; ++q) {
+    if (A[q] < 0 || A[q] >= h->L) return fail(h, TRAJ_EDOMAIN, "site index outside the lattice");
+    if (seen[A[q]]) return fail(h, TRAJ_EDOMAIN, "duplicate site in region");
+    seen[A[q]] = 1;
+    idx[q] = (int32_t)A[q];
+  }
+  if (nA == 0) {
+    for (int t = 0; t < h->T; ++t) S_out[t] = 0.0;
+    return 0;
+  }
+  CK(cudaMemcpyAsync(h->region, idx.data(), nA * 4, cudaMemcpyHostToDevice, h->st));
+  CK(cudaMemsetAsync(h->bad_dev, 0, h->T * 4, h->st));
+  const int n = (int)std::min<int64_t>(nA, h->N);
+  for (int t = 0; t < h->T; ++t) {
+    cplx* Ut = h->U[h->cur] + t * h->sU;
+    cplx* UA = h->U[1 - h->cur] + t * h->sU;    // scratch: the other state buffer
+    cplx* C = h->G + t * h->sG;
+    TRY(gather_rows(h->st, Ut, h->ldN, 0, h->region, 0, nullptr, (int)nA, 1, UA, h->ldN, 0, h->N, &h->err));
+    if (nA <= h->N)   // C_A = U_A U_A^dag
+      TRY(zgemm(h->st, 0, 1, nA, nA, h->N, 1.0, 0.0, UA, h->ldN, 0, UA, h->ldN, 0, 0.0, C, h->ldN, 0, 1, 0, &h->err));
+    else              // same non-zero spectrum: U_A^dag U_A (N x N)
+      TRY(zgemm(h->st, 1, 0, h->N, h->N, nA, 1.0, 0.0, UA, h->ldN, 0, UA, h->ldN, 0, 0.0, C, h->ldN, 0, 1, 0, &h->err));
+    cusolverStatus_t r = cusolverDnZheevd(h->solver, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER, n,
+                                          reinterpret_cast<cuDoubleComplex*>(C), (int)h->ldN, h->eig_w,
+                                          reinterpret_cast<cuDoubleComplex*>(h->eig_work), h->lwork, h->eig_info);
+    if (r != CUSOLVER_STATUS_SUCCESS) return fail(h, TRAJ_ECUDA, "cusolverDnZheevd failed: " + std::to_string(r));
+    TRY(entropy_reduce(h->st, h->eig_w, n, h->S_dev + t, h->bad_dev + t, &h->err));
+  }
+  std::vector<int32_t> bad(h->T), failed(h->T);
+  CK(cudaMemcpyAsync(S_out, h->S_dev, h->T * 8, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaMemcpyAsync(bad.data(), h->bad_dev, h->T * 4, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaMemcpyAsync(failed.data(), h->failed_dev, h->T * 4, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  bool newbad = false;
+  for (int t = 0; t < h->T; ++t) {
+    if (failed[t]) S_out[t] = nan("");
+    if (bad[t] && !failed[t]) {
+      newbad = true;
+      int32_t one = 1;
+      CK(cudaMemcpy(h->failed_dev + t, &one, 4, cudaMemcpyHostToDevice));
+    }
+  }
+  if (newbad) return fail(h, TRAJ_ENUMERIC, "spectrum of C_A outside [-1e-8, 1+1e-8]");
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* traj_strerror(int s) {
+  switch (s) {
+    case TRAJ_OK: return "ok";
+    case TRAJ_EINVAL: return "invalid argument";
+    case TRAJ_ECONFIG: return "invalid configuration";
+    case TRAJ_ENUMERIC: return "numerical failure (trajectory marked failed)";
+    case TRAJ_ECUDA: return "CUDA / cuSOLVER error";
+    case TRAJ_ENCCL: return "NCCL error";
+    case TRAJ_EDOMAIN: return "domain error";
+    default: return "unknown status";
+  }
+}
+
+const char* traj_last_error(traj_handle h) { return h ? h->err.c_str() : g_err.c_str(); }
+
+long long traj_kernel_launches(void) { return g_kernel_launches.load(); }
+
+int traj_workspace_bytes(const traj_config* cfg, size_t* out) {
+  traj_ctx* h = nullptr;
+  std::string why;
+  if (!out) return fail(h, TRAJ_EINVAL, "null out");
+  int s = validate(cfg, &why);
+  if (s) return fail(h, s, why);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(h, TRAJ_ECUDA, "no CUDA device");
+  int lw = 0;
+  if ((s = eig_lwork((int)cfg->N, &lw, &why))) return fail(h, s, why);
+  traj_ctx tmp;
+  *out = carve(&tmp, cfg, nullptr, lw);
+  return 0;
+}
+
+int traj_init(const traj_config* cfg, traj_handle* out) {
+  traj_ctx* h = nullptr;
+  std::string why;
+  if (!out) return fail(h, TRAJ_EINVAL, "null out");
+  *out = nullptr;
+  int s = validate(cfg, &why);
+  if (s) return fail(h, s, why);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(h, TRAJ_ECUDA, "no CUDA device");
+  int lw = 0;
+  if ((s = eig_lwork((int)cfg->N, &lw, &why))) return fail(h, s, why);
+  {
+    traj_ctx tmp;
+    const size_t need = carve(&tmp, cfg, nullptr, lw);
+    if (!cfg->workspace || cfg->workspace_bytes < need)
+      return fail(h, TRAJ_ECONFIG, "workspace missing or smaller than traj_workspace_bytes");
+    if (reinterpret_cast<uintptr_t>(cfg->workspace) & 255) return fail(h, TRAJ_ECONFIG, "workspace not 256-B aligned");
+  }
+  h = new traj_ctx();
+  h->cfg = *cfg;
+  h->gamma.assign(cfg->gamma, cfg->gamma + cfg->n_traj);
+  h->cfg.gamma = h->gamma.data();
+  h->st = reinterpret_cast<cudaStream_t>(cfg->stream);
+  h->lwork = lw;
+  carve(h, cfg, reinterpret_cast<char*>(cfg->workspace), lw);
+  h->last_nS.assign(h->T, 0);
+  h->last_n1.assign(h->T, 0);
+  auto bail = [&](int st, const std::string& m) {
+    std::string msg = m;
+    traj_destroy(h);
+    g_err = msg;
+    return st;
+  };
+  if (cudaMallocHost(&h->h_small, std::max(2 * h->T, 16) * 4) != cudaSuccess) return bail(TRAJ_ECUDA, "cudaMallocHost");
+  if (cusolverDnCreate(&h->solver) != CUSOLVER_STATUS_SUCCESS) return bail(TRAJ_ECUDA, "cusolverDnCreate");
+  cusolverDnSetStream(h->solver, h->st);
+  // zero the whole workspace: padded columns (ld > N) must read as zeros
+  if (cudaMemsetAsync(cfg->workspace, 0, cfg->workspace_bytes, h->st) != cudaSuccess) return bail(TRAJ_ECUDA, "memset");
+  // K = K_y (x) K_x from the ring coefficient rows (Ly = 1: K_y = [1])
+  std::vector<std::complex<double>> kc = ring_coefficients(h->Lx, cfg->J, cfg->dt);
+  if (h->Ly > 1) {
+    std::vector<std::complex<double>> ky = ring_coefficients(h->Ly, cfg->J, cfg->dt);
+    kc.insert(kc.end(), ky.begin(), ky.end());
+  } else {
+    kc.push_back(1.0);
+  }
+  std::vector<int32_t> sites;
+  for (int i = 0; i < h->L; ++i)
+    if (((i % h->Lx) + (i / h->Lx)) % 2 == 0) sites.push_back(i);
+  if ((int)sites.size() != h->N) return bail(TRAJ_ECONFIG, "initial state does not have N particles");
+  std::string e;
+  if (cudaMemcpyAsync(h->kcoef, kc.data(), kc.size() * 16, cudaMemcpyHostToDevice, h->st) != cudaSuccess ||
+      cudaMemcpyAsync(h->sites, sites.data(), sites.size() * 4, cudaMemcpyHostToDevice, h->st) != cudaSuccess ||
+      cudaMemcpyAsync(h->gamma_dev, h->gamma.data(), h->T * 8, cudaMemcpyHostToDevice, h->st) != cudaSuccess)
+    return bail(TRAJ_ECUDA, "upload");
+  if (build_k(h->st, h->K, h->ldL, h->Lx, h->Ly, h->kcoef, h->kcoef + h->Lx, &e)) return bail(TRAJ_ECUDA, e);
+  if (init_state(h->st, h->U[0], h->ldN, h->sU, h->sites, h->N, h->T, &e)) return bail(TRAJ_ECUDA, e);
+  if (cudaStreamSynchronize(h->st) != cudaSuccess) return bail(TRAJ_ECUDA, "init sync");
+  *out = h;
+  return 0;
+}
+
+int traj_step(traj_handle h, int64_t n_steps) {
+  if (!h) return TRAJ_EINVAL;
+  if (n_steps < 0) return fail(h, TRAJ_EINVAL, "n_steps < 0");
+  for (int64_t s = 0; s < n_steps; ++s) {
+    int r = one_step(h);
+    if (r) return r;
+  }
+  return 0;
+}
+
+int traj_orthonormalize(traj_handle h) {
+  if (!h) return TRAJ_EINVAL;
+  return cqr2(h, h->U[h->cur], h->U[1 - h->cur]);
+}
+
+int traj_entropy(traj_handle h, const int64_t* A, int64_t nA, double* S_out) {
+  if (!h) return TRAJ_EINVAL;
+  return entropy_impl(h, A, nA, S_out);
+}
+
+int traj_mutual_info(traj_handle h, const int64_t* A, int64_t nA, const int64_t* B, int64_t nB, double* I_out) {
+  if (!h) return TRAJ_EINVAL;
+  if (!I_out || nA < 0 || nB < 0 || (nA && !A) || (nB && !B)) return fail(h, TRAJ_EINVAL, "bad region arguments");
+  std::vector<char> inA(h->L, 0);
+  for (int64_t q = 0; q < nA; ++q)
+    if (A[q] >= 0 && A[q] < h->L) inA[A[q]] = 1;
+  for (int64_t q = 0; q < nB; ++q)
+    if (B[q] >= 0 && B[q] < h->L && inA[B[q]]) return fail(h, TRAJ_EDOMAIN, "regions overlap");
+  std::vector<int64_t> AB(A, A + nA);
+  AB.insert(AB.end(), B, B + nB);
+  std::vector<double> sa(h->T), sb(h->T), sab(h->T);
+  int s;
+  if ((s = entropy_impl(h, A, nA, sa.data()))) return s;
+  if ((s = entropy_impl(h, B, nB, sb.data()))) return s;
+  if ((s = entropy_impl(h, AB.data(), (int64_t)AB.size(), sab.data()))) return s;
+  for (int t = 0; t < h->T; ++t) I_out[t] = sa[t] + sb[t] - sab[t];
+  return 0;
+}
+
+int traj_occupations(traj_handle h, double* n_out) {
+  if (!h) return TRAJ_EINVAL;
+  if (!n_out) return fail(h, TRAJ_EINVAL, "null n_out");
+  TRY(row_monitor(h->st, h->U[h->cur], h->ldN, h->sU, h->L, h->N, h->T, 0, h->step, h->cfg.traj_base, h->cfg.seed,
+                  h->gamma_dev, h->cfg.dt, n_out, &h->err));
+  return 0;
+}
+
+int traj_correlation_rows(traj_handle h, int64_t traj, int64_t row0, int64_t nrows, void* C_out) {
+  int s = check_traj(h, traj);
+  if (s) return s;
+  if (row0 < 0 || nrows < 0 || row0 + nrows > h->L || !C_out) return fail(h, TRAJ_EINVAL, "bad row range");
+  if (nrows == 0) return 0;
+  cplx* Ut = h->U[h->cur] + traj * h->sU;
+  TRY(zgemm(h->st, 0, 1, nrows, h->L, h->N, 1.0, 0.0, Ut + row0 * h->ldN, h->ldN, 0, Ut, h->ldN, 0, 0.0,
+            reinterpret_cast<cplx*>(C_out), h->L, 0, 1, 0, &h->err));
+  return 0;
+}
+
+int traj_get_state(traj_handle h, int64_t traj, void* U_out) {
+  int s = check_traj(h, traj);
+  if (s) return s;
+  if (!U_out) return fail(h, TRAJ_EINVAL, "null U_out");
+  CK(cudaMemcpy2DAsync(U_out, (size_t)h->N * 16, h->U[h->cur] + traj * h->sU, (size_t)h->ldN * 16, (size_t)h->N * 16,
+                       h->L, cudaMemcpyDefault, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return 0;
+}
+
+int traj_set_state(traj_handle h, int64_t traj, const void* U_in) {
+  int s = check_traj(h, traj);
+  if (s) return s;
+  if (!U_in) return fail(h, TRAJ_EINVAL, "null U_in");
+  CK(cudaMemcpy2DAsync(h->U[h->cur] + traj * h->sU, (size_t)h->ldN * 16, U_in, (size_t)h->N * 16, (size_t)h->N * 16,
+                       h->L, cudaMemcpyDefault, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return 0;
+}
+
+int traj_get_step(traj_handle h, int64_t* step) {
+  if (!h || !step) return TRAJ_EINVAL;
+  *step = h->step;
+  return 0;
+}
+
+int traj_set_step(traj_handle h, int64_t step) {
+  if (!h) return TRAJ_EINVAL;
+  if (step < 0 || step >= (1ll << 32)) return fail(h, TRAJ_EINVAL, "step out of range");
+  h->step = step;
+  return 0;
+}
+
+int traj_failed(traj_handle h, int64_t traj, int32_t* flag) {
+  int s = check_traj(h, traj);
+  if (s) return s;
+  if (!flag) return fail(h, TRAJ_EINVAL, "null flag");
+  CK(cudaMemcpyAsync(h->h_small, h->failed_dev + traj, 4, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  *flag = h->h_small[0];
+  return 0;
+}
+
+int traj_last_clicks(traj_handle h, int64_t traj, int64_t* n_clicks, int64_t* n_occupied) {
+  int s = check_traj(h, traj);
+  if (s) return s;
+  if (n_clicks) *n_clicks = h->last_nS[traj];
+  if (n_occupied) *n_occupied = h->last_n1[traj];
+  return 0;
+}
+
+int traj_profile(traj_handle h, int enable) {
+  if (!h) return TRAJ_EINVAL;
+  CK(cudaStreamSynchronize(h->st));
+  for (auto& e : h->evs) {
+    h->pool.push_back(std::get<1>(e));
+    h->pool.push_back(std::get<2>(e));
+  }
+  h->evs.clear();
+  for (int p = 0; p < TRAJ_NPHASES; ++p) {
+    h->ms[p] = 0;
+    h->launches[p] = 0;
+  }
+  h->prof = enable != 0;
+  return 0;
+}
+
+int traj_phase_times(traj_handle h, double* ms, int64_t* launches) {
+  if (!h) return TRAJ_EINVAL;
+  CK(cudaStreamSynchronize(h->st));
+  for (auto& e : h->evs) {
+    float t = 0;
+    cudaEventElapsedTime(&t, std::get<1>(e), std::get<2>(e));
+    h->ms[std::get<0>(e)] += t;
+    h->pool.push_back(std::get<1>(e));
+    h->pool.push_back(std::get<2>(e));
+  }
+  h->evs.clear();
+  for (int p = 0; p < TRAJ_NPHASES; ++p) {
+    if (ms) ms[p] = h->ms[p];
+    if (launches) launches[p] = h->launches[p];
+  }
+  return 0;
+}
+
+int traj_destroy(traj_handle h) {
+  if (!h) return TRAJ_EINVAL;
+  if (h->st) cudaStreamSynchronize(h->st);
+  for (auto& e : h->evs) {
+    cudaEventDestroy(std::get<1>(e));
+    cudaEventDestroy(std::get<2>(e));
+  }
+  for (auto e : h->pool) cudaEventDestroy(e);
+  if (h->solver) cusolverDnDestroy(h->solver);
+  if (h->h_small) cudaFreeHost(h->h_small);
+  delete h;
+  return 0;
+}
+
+int traj_zgemm(void* stream, int opA, int opB, int64_t M, int64_t N, int64_t K, double alpha_re, double alpha_im,
+               const void* A, int64_t lda, int64_t strideA, const void* B, int64_t ldb, int64_t strideB, double beta,
+               void* C, int64_t ldc, int64_t strideC, int64_t batch, int flags) {
+  if ((opA != 0 && opA != 1) || (opB != 0 && opB != 1) || M < 0 || N < 0 || K < 0 || batch < 0 || !C ||
+      (K > 0 && (!A || !B)))
+    return fail(nullptr, TRAJ_EINVAL, "traj_zgemm: bad arguments");
+  std::string e;
+  int s = zgemm(reinterpret_cast<cudaStream_t>(stream), opA, opB, M, N, K, alpha_re, alpha_im,
+                reinterpret_cast<const cplx*>(A), lda, strideA, reinterpret_cast<const cplx*>(B), ldb, strideB, beta,
+                reinterpret_cast<cplx*>(C), ldc, strideC, batch, flags, &e);
+  return s ? fail(nullptr, s, e) : 0;
+}
+
+size_t traj_chol_scratch_bytes(int64_t n, int64_t batch) { return chol_scratch_bytes(n, batch); }
+
+int traj_chol_inverse(void* stream, int64_t n, void* G, int64_t ldg, int64_t strideG, void* X, int64_t ldx,
+                      int64_t strideX, int64_t batch, void* scratch, int32_t* failed) {
+  if (n < 0 || batch < 0 || (n > 0 && (!G || !X || !scratch))) return fail(nullptr, TRAJ_EINVAL, "bad arguments");
+  std::string e;
+  int s = chol_inverse(reinterpret_cast<cudaStream_t>(stream), n, reinterpret_cast<cplx*>(G), ldg, strideG,
+                       reinterpret_cast<cplx*>(X), ldx, strideX, batch, scratch, failed, &e);
+  return s ? fail(nullptr, s, e) : 0;
+}
+
+}  // extern "C"

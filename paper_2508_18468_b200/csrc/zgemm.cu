@@ -1,0 +1,321 @@
+// Complex-FP64 GEMM on the B200 FP64 tensor pipe (DMMA.8x8x4), TMA-fed.
+//
+//   C_b = alpha * op(A_b) * op(B_b) + beta * C_b,  op in {N, C(onjugate transpose)}
+//
+// Used for every contraction of the step: U <- K U (a1),
+// G = U^dag U and U <- U R^-1 (a3, CholeskyQR2 for the QR of P:209), the Cholesky /
+// triangular-inverse recursion, the projective rank-k update (a2) and C_A = U_A U_A^dag (a4).
+//
+// Design (sm_100a):
+//  * tcgen05 has no f64 kind; the FP64 tensor path is mma.sync.m8n8k4.f64 -> DMMA.8x8x4
+//    (measured 37.1 TF/s chip peak, profiles/r01_fp64_microbench.txt).
+//  * Complex product as 4 real products folded into 2 real MMAs over an interleaved
+//    k axis: k_real = (complex k, component c).  The A fragment is the raw interleaved
+//    double; the B fragment is built in registers from one 16-byte complex load:
+//        Cr += [a_r a_i] . [b_r, -sa*sb*b_i]      Ci += [a_r a_i] . [sb*b_i, sa*b_r]
+//    (sa, sb = -1 for a conjugated operand), so conjugation costs nothing.
+//  * CTA tile 128 x 64 complex, 8 warps of 32 x 32 complex (64 accumulator doubles
+//    each, up to 255 registers: 2 warps per SM sub-partition).  Lane 0 of warp 0 also
+//    issues the TMA loads (cp.async.bulk.tensor) STAGES-1 stages ahead into a 6-stage
+//    mbarrier ring of 24 KB stages (8 complex k per stage); a separate producer warp
+//    would put 3 warps on one sub-partition and cap registers at 168.
+//  * Every smem tile is made of 128-byte lines with the TMA 128B swizzle; each MMA
+//    k-step pairs complex k with k+4, which makes all four operand layouts
+//    (k-contiguous or m/n-contiguous) bank-conflict free.
+//  * Out-of-range rows / k are zero-filled by TMA, so ragged M, N, K need no masks
+//    except in the epilogue.
+#include "common.cuh"
+#include "zgemm.h"
+
+namespace traj {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 64;
+constexpr int BKC = 8;                 // complex k per stage
+constexpr int STAGES = 6;
+constexpr int CONSUMER_WARPS = 8;
+constexpr int THREADS = CONSUMER_WARPS * 32;
+constexpr int A_BYTES = BM * 128;
+constexpr int B_BYTES = BN * 128;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8;
+constexpr int GROUP_M = 8;
+
+struct Args {
+  int M, N, K;
+  int tiles_m, tiles_n;
+  int flags;
+  int a_batched, b_batched;
+  double alpha_re, alpha_im, beta;
+  cplx* C;
+  long long ldc, strideC;
+};
+
+// byte offset of complex element (r, k) in a k-contiguous tile: line r, chunk k (swizzled)
+__device__ __forceinline__ uint32_t off_kc(int r, int k) { return r * 128 + ((k ^ (r & 7)) << 4); }
+// byte offset in an m/n-contiguous tile made of [8 k-lines][8 complex] 1 KB sub-boxes
+__device__ __forceinline__ uint32_t off_mn(int r, int k) {
+  return (r >> 3) * 1024 + k * 128 + (((r & 7) ^ k) << 4);
+}
+
+template <bool CONJ_A, bool CONJ_B>
+__global__ void __launch_bounds__(THREADS, 1)
+    zgemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const Args args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+
+  // ---- tile coordinates (grouped raster for L2 reuse of the A row-panel)
+  const int t = blockIdx.x;
+  const int group = GROUP_M * args.tiles_n;
+  const int first_m = (t / group) * GROUP_M;
+  const int gm = min(GROUP_M, args.tiles_m - first_m);
+  const int pid_m = first_m + (t % group) % gm;
+  const int pid_n = (t % group) / gm;
+  const int m0 = pid_m * BM, n0 = pid_n * BN;
+  const int z = blockIdx.z;
+  if ((args.flags & TRAJ_C_UPPER_F) && m0 > n0 + BN - 1) return;   // tile entirely below the diagonal
+
+  int kb = 0, ke = args.K;
+  if (args.flags & TRAJ_TRI_A_UPPER_F) kb = max(kb, m0);
+  if (args.flags & TRAJ_TRI_A_LOWER_F) ke = min(ke, m0 + BM);
+  if (args.flags & TRAJ_TRI_B_UPPER_F) ke = min(ke, n0 + BN);
+  if (args.flags & TRAJ_TRI_B_LOWER_F) kb = max(kb, n0);
+  const int nk = ke > kb ? (ke - kb + BKC - 1) / BKC : 0;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CONSUMER_WARPS);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // ================= TMA issue (warp 0, lane 0), STAGES-1 stages ahead
+  const bool issuer = (warp == 0 && lane == 0);
+  const int za = args.a_batched ? z : 0, zb = args.b_batched ? z : 0;
+  auto issue = [&](int it) {
+    const int s = it % STAGES;
+    mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+    const int k0 = kb + it * BKC;
+    uint8_t* sA = smem + s * STAGE_BYTES;
+    uint8_t* sB = sA + A_BYTES;
+    if (!CONJ_A) {
+      tma_load_3d(sA, &tmA, 2 * k0, m0, za, &full[s]);                 // [BM rows][8 k]
+    } else {
+#pragma unroll
+      for (int c = 0; c < BM / 8; ++c) tma_load_3d(sA + c * 1024, &tmA, 2 * (m0 + 8 * c), k0, za, &full[s]);
+    }
+    if (CONJ_B) {
+      tma_load_3d(sB, &tmB, 2 * k0, n0, zb, &full[s]);                 // [BN rows][8 k]
+    } else {
+#pragma unroll
+      for (int c = 0; c < BN / 8; ++c) tma_load_3d(sB + c * 1024, &tmB, 2 * (n0 + 8 * c), k0, zb, &full[s]);
+    }
+  };
+  if (issuer) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int it = 0; it < min(nk, STAGES - 1); ++it) issue(it);
+  }
+
+  // ================= DMMA consumers
+  const int warp_m = warp & 3, warp_n = warp >> 2;
+  const int g = lane >> 2;          // fragment row (A) / column (B)
+  const int slot = lane & 3;        // k slot of the 8x8x4 MMA
+  const int c = slot & 1;           // component of the interleaved complex k
+  const int khalf = (slot >> 1) * 4;
+  constexpr double sa = CONJ_A ? -1.0 : 1.0;
+  constexpr double sb = CONJ_B ? -1.0 : 1.0;
+  constexpr double s_b1 = -sa * sb;
+
+  double acc[4][4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int p = 0; p < 2; ++p) acc[i][j][p][0] = acc[i][j][p][1] = 0.0;
+
+  for (int it = 0; it < nk; ++it) {
+    const int s = it % STAGES;
+    if (issuer) {
+      // refill the slot consumed in iteration it-1 (all warps must have released it)
+      const int nx = it + STAGES - 1;
+      if (nx < nk) {
+        if (nx >= STAGES) mbar_wait(&empty[nx % STAGES], ((nx / STAGES) + 1) & 1);
+        issue(nx);
+      }
+    }
+    mbar_wait(&full[s], (it / STAGES) & 1);
+    const uint8_t* sA = smem + s * STAGE_BYTES;
+    const uint8_t* sB = sA + A_BYTES;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = q + khalf;
+      double a[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = warp_m * 32 + 8 * i + g;
+        const uint32_t o = (CONJ_A ? off_mn(r, k) : off_kc(r, k)) + 8 * c;
+        a[i] = *reinterpret_cast<const double*>(sA + o);
+      }
+      double b1[4], b2[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = warp_n * 32 + 8 * j + g;
+        const uint32_t o = CONJ_B ? off_kc(r, k) : off_mn(r, k);
+        const double2 b = *reinterpret_cast<const double2*>(sB + o);
+        b1[j] = c ? s_b1 * b.y : b.x;
+        b2[j] = c ? sa * b.x : sb * b.y;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          dmma_8x8x4(acc[i][j][0][0], acc[i][j][0][1], a[i], b1[j]);
+          dmma_8x8x4(acc[i][j][1][0], acc[i][j][1][1], a[i], b2[j]);
+        }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // ---- epilogue: thread holds C(row g, cols 2*slot, 2*slot+1) of each 8x8 block
+  cplx* C = args.C + (long long)z * args.strideC;
+  const bool upper = args.flags & TRAJ_C_UPPER_F;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = m0 + warp_m * 32 + 8 * i + g;
+    if (row >= args.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = n0 + warp_n * 32 + 8 * j + 2 * slot + e;
+        if (col >= args.N || (upper && row > col)) continue;
+        const double vr = acc[i][j][0][e], vi = acc[i][j][1][e];
+        double2 out;
+        out.x = args.alpha_re * vr - args.alpha_im * vi;
+        out.y = args.alpha_re * vi + args.alpha_im * vr;
+        cplx* p = C + (long long)row * args.ldc + col;
+        if (args.beta != 0.0) {
+          const double2 old = *p;
+          out.x += args.beta * old.x;
+          out.y += args.beta * old.y;
+        }
+        *p = out;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled_t get_encode() {
+  static PFN_encodeTiled_t fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+  }
+  return fn;
+}
+
+// Map a batch of row-major complex matrices [rows][cols] (ld, batch stride in complex
+// elements) as a 3D FP64 tensor {2*cols, rows, batch} with boxes {16, box_rows, 1}.
+bool make_map(CUtensorMap* map, const void* base, long long rows, long long cols, long long ld, long long stride,
+              long long batch, int box_rows) {
+  PFN_encodeTiled_t enc = get_encode();
+  if (!enc) return false;
+  const bool batched = stride != 0 && batch > 1;
+  cuuint64_t dims[3] = {(cuuint64_t)(2 * cols), (cuuint64_t)rows, (cuuint64_t)(batched ? batch : 1)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 16), (cuuint64_t)((batched ? stride : ld * rows) * 16)};
+  cuuint32_t box[3] = {16, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <bool CA, bool CB>
+cudaError_t launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const Args& args, int batch) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(zgemm_dmma_kernel<CA, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid(args.tiles_m * args.tiles_n, 1, batch);
+  zgemm_dmma_kernel<CA, CB><<<grid, THREADS, SMEM_BYTES, st>>>(a, b, args);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int zgemm(cudaStream_t st, int opA, int opB, long long M, long long N, long long K, double alpha_re,
+          double alpha_im, const cplx* A, long long lda, long long strideA, const cplx* B, long long ldb,
+          long long strideB, double beta, cplx* C, long long ldc, long long strideC, long long batch, int flags,
+          std::string* err) {
+  if (M <= 0 || N <= 0 || batch <= 0) return 0;
+  if (M > (1ll << 30) || N > (1ll << 30) || K > (1ll << 30) || batch > 65535) {
+    if (err) *err = "zgemm: dimension too large";
+    return 1;
+  }
+  if (K > 0 && (lda <= 0 || ldb <= 0 || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15))) {
+    if (err) *err = "zgemm: bad lda/ldb or misaligned operand";
+    return 1;
+  }
+  CUtensorMap ma, mb;
+  const long long Ka = K > 0 ? K : 1;
+  // op(A) = A: stored [M][K], k-contiguous tile [BM rows][8 k]; op(A) = A^dag: stored [K][M].
+  bool ok = opA == 0 ? make_map(&ma, A, M, Ka, lda, strideA, batch, BM)
+                     : make_map(&ma, A, Ka, M, lda, strideA, batch, 8);
+  ok = ok && (opB == 0 ? make_map(&mb, B, Ka, N, ldb, strideB, batch, 8)
+                       : make_map(&mb, B, N, Ka, ldb, strideB, batch, BN));
+  if (!ok) {
+    if (err) *err = "zgemm: cuTensorMapEncodeTiled failed";
+    return 4;
+  }
+  Args args;
+  args.M = (int)M;
+  args.N = (int)N;
+  args.K = (int)K;
+  args.tiles_m = (int)ceil_div(M, BM);
+  args.tiles_n = (int)ceil_div(N, BN);
+  args.flags = flags;
+  args.a_batched = strideA != 0 && batch > 1;
+  args.b_batched = strideB != 0 && batch > 1;
+  args.alpha_re = alpha_re;
+  args.alpha_im = alpha_im;
+  args.beta = beta;
+  args.C = C;
+  args.ldc = ldc;
+  args.strideC = strideC;
+  cudaError_t e;
+  if (opA == 0 && opB == 0) e = launch<false, false>(st, ma, mb, args, (int)batch);
+  else if (opA == 0) e = launch<false, true>(st, ma, mb, args, (int)batch);
+  else if (opB == 0) e = launch<true, false>(st, ma, mb, args, (int)batch);
+  else e = launch<true, true>(st, ma, mb, args, (int)batch);
+  if (e != cudaSuccess) {
+    if (err) *err = std::string("zgemm launch: ") + cudaGetErrorString(e);
+    return 4;
+  }
+  return 0;
+}
+
+}  // namespace traj

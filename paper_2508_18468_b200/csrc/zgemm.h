@@ -1,0 +1,22 @@
+// Internal interface of the DMMA complex GEMM (zgemm.cu).
+#pragma once
+#include <string>
+#include "common.cuh"
+
+namespace traj {
+
+enum {
+  TRAJ_TRI_A_UPPER_F = 1,
+  TRAJ_TRI_A_LOWER_F = 2,
+  TRAJ_TRI_B_UPPER_F = 4,
+  TRAJ_TRI_B_LOWER_F = 8,
+  TRAJ_C_UPPER_F = 16
+};
+
+// C_b = alpha op(A_b) op(B_b) + beta C_b.  Returns 0, or a traj_status with *err set.
+int zgemm(cudaStream_t st, int opA, int opB, long long M, long long N, long long K, double alpha_re,
+          double alpha_im, const cplx* A, long long lda, long long strideA, const cplx* B, long long ldb,
+          long long strideB, double beta, cplx* C, long long ldc, long long strideC, long long batch, int flags,
+          std::string* err);
+
+}  // namespace traj

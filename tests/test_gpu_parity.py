@@ -1,0 +1,171 @@
+"""GPU path (through the C-ABI) vs the oracle on the same seeded Philox streams.
+
+Bar (north star): C = U U^dag within 1e-10 absolute and S_A within 1e-8 over short runs;
+projective click lists and outcomes identical.  Sizes span several 128 x 64 GEMM tiles
+with ragged tails; configs c1 (full) and reduced c2/c4-shaped cases; full-size c3 checks
+via closed forms and invariants that hold at any size."""
+import numpy as np
+import pytest
+
+import workloads
+from oracle import gaussian, lattice
+from oracle.trajectory import OracleTrajectory
+
+pytestmark = pytest.mark.gpu
+
+C_TOL = 1e-10
+S_TOL = 1e-8
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2508_18468_b200 import build
+    build.build()
+    import paper_2508_18468_b200 as P
+    P.load_library()
+    return P
+
+
+def lockstep(P, Lx, Ly, protocol, gammas, steps, sample_every, regions, seed=0, traj_base=0, dt=0.05,
+             mi=None, check_clicks=True):
+    gpu = P.Trajectories(Lx, Ly, protocol, gammas, dt=dt, seed=seed, traj_base=traj_base)
+    K = lattice.propagator_lattice(Lx, Ly, 1.0, dt)
+    orc = [OracleTrajectory(Lx, Ly, protocol, g, dt, seed=seed, traj=traj_base + t, K=K)
+           for t, g in enumerate(gammas)]
+    worst_c = worst_s = 0.0
+    clicks = 0
+    for s in range(steps + 1):
+        if s % sample_every == 0:
+            for t, o in enumerate(orc):
+                C = gpu.correlation(t).cpu().numpy()
+                worst_c = max(worst_c, np.abs(C - o.correlation()).max())
+            for A in regions:
+                S = gpu.entropy(A)
+                for t, o in enumerate(orc):
+                    worst_s = max(worst_s, abs(S[t] - o.entropy(A)))
+            if mi is not None:
+                I = gpu.mutual_info(*mi)
+                for t, o in enumerate(orc):
+                    worst_s = max(worst_s, abs(I[t] - o.mutual_info(*mi)))
+        if s == steps:
+            break
+        gpu.step(1)
+        for t, o in enumerate(orc):
+            o.step(1)
+            if protocol == "projective" and check_clicks:
+                nS, n1 = gpu.last_clicks(t)
+                S_, occ = o.last_clicks
+                assert (nS, n1) == (S_.size, int(occ.sum())), (s, t)
+                clicks += nS
+    for t in range(len(gammas)):
+        assert not gpu.failed(t)
+    assert worst_c < C_TOL, worst_c
+    assert worst_s < S_TOL, worst_s
+    return gpu, orc, clicks
+
+
+def test_c1_projective_full(P):
+    """configs[0]: L = 64, projective gamma = 0.5, 16 trajectories, 200 steps, S(half) every 10."""
+    w = workloads.c1()
+    _, _, clicks = lockstep(P, w.Lx, w.Ly, w.protocol, [w.gamma_of(t) for t in range(w.n_traj)], w.steps,
+                            w.sample_every, [w.regions["half"]], seed=w.seed)
+    assert clicks > 100
+
+
+def test_projective_ragged_many_clicks(P):
+    """L = 300 (N = 150: 3 ragged 64-wide tiles), p = gamma dt = 0.1: ~30 clicks per step."""
+    lockstep(P, 300, 1, "projective", [2.0, 0.6], 30, 5, [np.arange(150), np.arange(37, 211)], seed=7)
+
+
+def test_homodyne_1d_ragged(P):
+    """c2-shaped (homodyne, gamma sweep) at L = 200."""
+    lockstep(P, 200, 1, "homodyne", [0.1, 1.0, 3.0], 100, 20, [np.arange(100), np.arange(13)], seed=3,
+             traj_base=5)
+
+
+def test_homodyne_2d_mutual_information(P):
+    """c4-shaped (2d torus, checkerboard, homodyne, MI between strips) at 12 x 8."""
+    A, B = workloads.strips_2d(12, 8)
+    lockstep(P, 12, 8, "homodyne", [0.5, 3.0], 60, 20, [workloads.columns(12, 8, 0, 6)], seed=11, mi=(A, B))
+
+
+def test_projective_2d(P):
+    """c5-shaped (2d, projective near the per-site critical rate) at 10 x 10."""
+    A, B = workloads.strips_2d(10, 10)
+    lockstep(P, 10, 10, "projective", [2.86, 5.72], 40, 10, [workloads.columns(10, 10, 0, 5)], seed=5, mi=(A, B))
+
+
+def test_every_site_measured(P):
+    """gamma dt = 1: N occupied outcomes, C diagonal 0/1, S = 0 after the step."""
+    L = 96
+    g = P.Trajectories(L, 1, "projective", [20.0, 20.0], dt=0.05, seed=2)
+    g.step(3)
+    for t in range(2):
+        nS, n1 = g.last_clicks(t)
+        assert nS == L and n1 == L // 2
+        C = g.correlation(t).cpu().numpy()
+        assert np.abs(C - np.diag(np.diag(C))).max() < 1e-12
+        d = np.diag(C).real
+        assert np.all((np.abs(d) < 1e-12) | (np.abs(d - 1) < 1e-12))
+    assert np.all(np.abs(g.entropy(np.arange(L // 2))) < 1e-9)
+
+
+def test_set_state_orthonormalize_matches_householder(P):
+    """CholeskyQR2 of an arbitrary full-rank U spans the same subspace as Householder QR."""
+    import torch
+    L, N = 200, 100
+    g = P.Trajectories(L, 1, "homodyne", [0.0], seed=0)
+    U = workloads.random_matrix(L, N, 21)
+    g.set_state(0, torch.from_numpy(U).cuda())
+    g.orthonormalize()
+    Ug = g.get_state(0).cpu().numpy()
+    assert np.abs(Ug.conj().T @ Ug - np.eye(N)).max() < 1e-13
+    Q = gaussian.orthonormalize(U)
+    assert np.abs(g.correlation(0).cpu().numpy() - gaussian.correlation(Q)).max() < 1e-12
+
+
+def test_free_evolution_closed_form_full_c3(P):
+    """configs[2] size (L = 16384, N = 8192), gamma = 0: n_i(t) = 1/2 + (-1)^i/(2L) sum_m cos(4t cos(2 pi m/L))
+    after 10 steps; Tr C = N; the step keeps U^dag U = 1."""
+    L, steps, dt = 16384, 10, 0.05
+    g = P.Trajectories(L, 1, "projective", [0.0], dt=dt, seed=0)
+    g.step(steps)
+    n = g.occupations()[0].cpu().numpy()
+    m = np.arange(L)
+    want = 0.5 + 0.5 * (-1.0) ** m * np.mean(np.cos(4 * steps * dt * np.cos(2 * np.pi * m / L)))
+    assert np.abs(n - want).max() < 1e-12
+    assert abs(n.sum() - L // 2) < 1e-8
+
+
+def test_projective_full_c3_invariants(P):
+    """configs[2] (L = 16384, gamma = 0.3): after a step every clicked site has n in {0, 1},
+    the particle number is N, U stays orthonormal, and S_A = S_complement."""
+    import torch
+    from paper_2508_18468_b200 import traj_zgemm
+    w = workloads.c3()
+    g = P.Trajectories(w.Lx, 1, "projective", list(w.gammas), dt=w.dt, seed=w.seed)
+    g.step(2)
+    nS, n1 = g.last_clicks(0)
+    assert 150 < nS < 350
+    from oracle.philox import site_uniforms
+    u0, _ = site_uniforms(w.L, 1, 0, w.seed)
+    S = np.nonzero(u0 < w.gammas[0] * w.dt)[0]
+    assert S.size == nS
+    n = g.occupations()[0].cpu().numpy()
+    ns = n[S]
+    assert np.all((np.abs(ns) < 1e-10) | (np.abs(ns - 1) < 1e-10))
+    assert int(np.round(ns.sum())) == n1
+    assert abs(n.sum() - w.N) < 1e-7
+    U = g.get_state(0)
+    G = torch.zeros((w.N, w.N), dtype=torch.complex128, device="cuda")
+    traj_zgemm(1, 0, U, U, G)
+    G -= torch.eye(w.N, dtype=torch.complex128, device="cuda")
+    assert G.abs().max().item() < 1e-12
+    del G, U
+    A = np.arange(w.L // 8)
+    Ac = np.arange(w.L // 8, w.L)
+    sa, sc = g.entropy(A)[0], g.entropy(Ac)[0]
+    assert abs(sa - sc) < 1e-8
