@@ -1,0 +1,307 @@
+#!/usr/bin/env python
+"""Benchmark of the trajectory step -- one JSON line on rank 0.
+
+Default workload: BASELINE.json configs[2] ("c3"): 1d ring L = 16384, N = 8192, Neel
+start, projective protocol gamma = 0.3, dt = 0.05, complex128, one trajectory per GPU
+(weak scaling: ranks run independent trajectories with global ids = rank; no data-path
+collective).  A "step" is one full pass of the hot path: U <- K U (dense), Philox
+clicks + conditional Born sampling + rank-k projective update, CholeskyQR2.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3|c5|c2|c4]
+
+N > 1 is launched by the driver with torch.distributed.run (one process per GPU).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads  # noqa: E402
+
+FP64_PEAK_TFLOPS = 37.1        # measured DMMA.8x8x4 issue-rate peak, profiles/r01_fp64_microbench.txt
+FP64_PEAK_SOURCE = ("measured on this pool's B200: DMMA.8x8x4 microbenchmark 37.1 TF/s (cuBLAS ZGEMM 37.0 TF/s), "
+                    "profiles/r01_fp64_microbench.txt; MEASURED_PEAKS.json has no FP64 entry "
+                    "(bf16 x 40/2250 nominal ratio would give 29.4)")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", default="c3")
+    p.add_argument("--traj-per-gpu", type=int, default=0, help="0: the config's natural batch (1 for c3/c5)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-budget", type=float, default=150.0, help="seconds of oracle work (reference arm)")
+    return p.parse_args()
+
+
+def workload(args):
+    w = workloads.CONFIGS[args.config]()
+    tpg = args.traj_per_gpu or (1 if args.config in ("c3", "c5") else 8)
+    return w, tpg
+
+
+def describe(w, tpg):
+    proto = f"{w.protocol} gamma={','.join(f'{g:g}' for g in w.gammas)}"
+    lat = f"1d ring L={w.L}" if w.Ly == 1 else f"2d torus {w.Lx}x{w.Ly} (L={w.L})"
+    return {"workload": f"{w.name}: {lat}, N={w.N}, {proto}, dt={w.dt}, Neel/checkerboard start, "
+                        f"{tpg} trajectory(ies) per GPU, complex128",
+            "L": w.L, "N": w.N, "protocol": w.protocol, "dt": w.dt, "traj_per_gpu": tpg,
+            "l2": "inputs larger than L2 (K is %.2f GB, U %.2f GB per trajectory; L2 = 126 MB)"
+                  % (16 * w.L * w.L / 1e9, 16 * w.L * w.N / 1e9)}
+
+
+# ----------------------------------------------------------------------------- clocks
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-i", str(self.index), "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [l.split(",") for l in open(self.f.name).read().strip().splitlines() if l.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 8 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 8 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in rows if len(r) >= 8 for j in range(4) if "Active" == r[4 + j].strip()})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle (CPU)
+def cpu_cores() -> int:
+    return len(os.sched_getaffinity(0))
+
+
+def oracle_steps(w, budget_s: float, max_steps: int):
+    """Time the oracle (as it stands) on the same workload: one trajectory from the
+    Neel state, whole steps, until max_steps or the time budget is used."""
+    from threadpoolctl import threadpool_info
+    from oracle import lattice
+    from oracle.trajectory import OracleTrajectory
+    K = lattice.propagator_lattice(w.Lx, w.Ly, w.J, w.dt)
+    tr = OracleTrajectory(w.Lx, w.Ly, w.protocol, w.gammas[0], w.dt, w.J, seed=w.seed, traj=0, K=K)
+    times = []
+    t_all = time.perf_counter()
+    while len(times) < max_steps:
+        t0 = time.perf_counter()
+        tr.step(1)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all > budget_s:
+            break
+    blas = [f"{i.get('internal_api')} {i.get('version')} x{i.get('num_threads')}" for i in threadpool_info()]
+    return times, blas
+
+
+def cpu_baseline_record(w, budget_s: float, max_steps: int, unit: str):
+    times, blas = oracle_steps(w, budget_s, max_steps)
+    v = len(times) / sum(times)
+    return {"value": v, "unit": unit, "cores": cpu_cores(), "kind": "oracle",
+            "sample": f"{len(times)} full oracle step(s) of one {w.name} trajectory from the Neel start "
+                      f"(NumPy/SciPy, {'; '.join(blas)}), {sum(times):.1f} s; K construction not timed"}
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2508_18468_b200 as P
+
+    w, tpg = workload(args)
+    gam = [w.gammas[(rank * tpg + t) % len(w.gammas)] for t in range(tpg)]
+    base = rank * tpg
+    tr = P.Trajectories(w.Lx, w.Ly, w.protocol, gam, dt=w.dt, J=w.J, seed=w.seed, traj_base=base)
+    st = tr.stream
+    for _ in range(args.warmup):
+        tr.step(1)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    tr.profile(True)
+    clocks = Clocks(local)
+    clocks.start()
+    l0 = P.traj_kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(args.steps):
+        tr.step(1)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    launches = P.traj_kernel_launches() - l0
+    clk = clocks.stop()
+    phases = tr.phase_times()
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    else:
+        ms_max = ms
+    value = world * tpg * args.steps / (ms_max / 1e3)
+    # ---- roofline of the dominant kernel: the dense K.U contraction (one launch per step)
+    prop_ms = phases["propagate"][0] / args.steps
+    flops_launch = 8.0 * w.L * w.L * w.N * tpg
+    achieved = flops_launch / (prop_ms / 1e3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(w.name, {}).get("propagate_dram_bytes")
+        except Exception:
+            traffic = None
+    step_flops = {"propagate": flops_launch, "gram": 2 * 4.0 * w.L * w.N * w.N * tpg,
+                  "trmm": 2 * 4.0 * w.L * w.N * w.N * tpg, "chol": 2 * (8.0 / 3.0) * w.N ** 3 * tpg}
+    dense_tflops = sum(step_flops.values()) * args.steps / (ms / 1e3) / 1e12
+    tr.close()
+    del tr
+    torch.cuda.empty_cache()
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, w, tpg, gam, base, world, P)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    out = {
+        "metric": "trajectory steps/s (configs[2]: 1d L=16384 projective; metric also quoted at 2d 160x160)",
+        "value": value, "unit": "trajectory-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128 (f64 arithmetic)", "data": "synthetic (Neel start, Philox randoms, seed 0)",
+        "config": describe(w, tpg),
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                     "kernel": "zgemm_dmma_kernel<N,N> (U <- K U, 8 L^2 N flops per trajectory)",
+                     "kernel_ms": prop_ms, "peak_source": FP64_PEAK_SOURCE},
+        "step_dense_tflops": dense_tflops,
+        "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
+        "phase_launches_per_step": {k: v[1] / args.steps for k, v in phases.items()},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline_record(w, budget_s=20.0, max_steps=1, unit="trajectory-steps/s")
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, w, tpg, gam, base, world, P):
+    """Same metric through the public API from host buffers: the initial orbital matrix
+    comes from pinned host memory (traj_set_state), every step ends with a device->host
+    read of the occupations n_i, and the run ends with S_A (host output)."""
+    import torch
+    import torch.distributed as dist
+    from oracle import lattice as _unused  # noqa: F401  (keeps import cost out of the timed region)
+    U0 = torch.zeros((w.L, w.N), dtype=torch.complex128).pin_memory()
+    occ = np.arange(0, w.L, 2) if w.Ly == 1 else None
+    if occ is None:
+        ys, xs = np.divmod(np.arange(w.L), w.Lx)
+        occ = np.nonzero((xs + ys) % 2 == 0)[0]
+    U0[torch.from_numpy(occ), torch.arange(w.N)] = 1.0
+    n_host = torch.empty((tpg, w.L), dtype=torch.float64).pin_memory()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    tr = P.Trajectories(w.Lx, w.Ly, w.protocol, gam, dt=w.dt, J=w.J, seed=w.seed, traj_base=base, stream=stream)
+    for t in range(tpg):
+        tr.set_state(t, U0)                       # H2D from pinned host memory
+    h2d = tpg * U0.numel() * 16
+    d2h = 0
+    for _ in range(args.steps):
+        tr.step(1)
+        n_host.copy_(tr.occupations(), non_blocking=True)   # D2H of the step's result
+        d2h += n_host.numel() * 8
+    S = tr.entropy(np.arange(w.L // 2))
+    d2h += S.size * 8
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    tr.close()
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"value": world * tpg * args.steps / (ms / 1e3), "unit": "trajectory-steps/s",
+            "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+            "includes": "handle init (K build), U0 upload from pinned host, K steps, per-step D2H of n_i, "
+                        "final S_A(half) eigvalsh + D2H"}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w, tpg = workload(args)
+    times, blas = oracle_steps(w, budget_s=args.cpu_budget, max_steps=max(1, args.steps))
+    v = len(times) / sum(times)
+    unit = "trajectory-steps/s"
+    rec = {"metric": "trajectory steps/s (configs[2]: 1d L=16384 projective; metric also quoted at 2d 160x160)",
+           "value": v, "unit": unit, "impl": "reference", "n_gpus": world, "steps": len(times), "warmup": 0,
+           "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "c128 (f64 arithmetic)", "data": "synthetic (Neel start, Philox randoms, seed 0)",
+           "config": describe(w, 1),
+           "cpu_baseline": {"value": v, "unit": unit, "cores": cpu_cores(), "kind": "oracle",
+                            "sample": f"{len(times)} oracle step(s) of one {w.name} trajectory (budget "
+                                      f"{args.cpu_budget:.0f} s; no warm-up: NumPy has no JIT), {'; '.join(blas)}"},
+           "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(rec), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -10,10 +10,13 @@
 //  * tcgen05 has no f64 kind; the FP64 tensor path is mma.sync.m8n8k4.f64 -> DMMA.8x8x4
 //    (measured 37.1 TF/s chip peak, profiles/r01_fp64_microbench.txt).
 //  * Complex product as 4 real products folded into 2 real MMAs over an interleaved
-//    k axis: k_real = (complex k, component c).  The A fragment is the raw interleaved
-//    double; the B fragment is built in registers from one 16-byte complex load:
-//        Cr += [a_r a_i] . [b_r, -sa*sb*b_i]      Ci += [a_r a_i] . [sb*b_i, sa*b_r]
-//    (sa, sb = -1 for a conjugated operand), so conjugation costs nothing.
+//    k axis: k_real = (complex k, component c).  With op(A) = a_r + i sa a_i and
+//    op(B) = b_r + i sb b_i (sa, sb = -1 for a conjugated operand):
+//        Cr += [a_r, -sa*sb*a_i] . [b_r, b_i]      (B fragment: the raw interleaved double)
+//        Ci += [sb*a_r,  sa*a_i] . [b_i, b_r]      (B fragment: the swapped double)
+//    so every B fragment is a plain 64-bit shared load and the signs are sign-bit XORs
+//    on the A fragment (ALU pipe; a DADD negation would sit on the FP64 pipe and stall
+//    the dependent DMMA).
 //  * CTA tile 128 x 64 complex, 8 warps of 32 x 32 complex (64 accumulator doubles
 //    each, up to 255 registers: 2 warps per SM sub-partition).  Lane 0 of warp 0 also
 //    issues the TMA loads (cp.async.bulk.tensor) STAGES-1 stages ahead into a 6-stage
@@ -26,6 +29,7 @@
 //    except in the epilogue.
 #include "common.cuh"
 #include "zgemm.h"
+#include <stdlib.h>
 
 namespace traj {
 
@@ -48,6 +52,7 @@ struct Args {
   int tiles_m, tiles_n;
   int flags;
   int a_batched, b_batched;
+  int a_4d, b_4d;          // m/n-contiguous operand mapped as one 4D box per stage
   double alpha_re, alpha_im, beta;
   cplx* C;
   long long ldc, strideC;
@@ -65,7 +70,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     zgemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const Args args) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B alignment for the 128B swizzle, by pointer arithmetic so loads stay LDS
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
 
@@ -108,21 +114,40 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint8_t* sB = sA + A_BYTES;
     if (!CONJ_A) {
       tma_load_3d(sA, &tmA, 2 * k0, m0, za, &full[s]);                 // [BM rows][8 k]
+    } else if (args.a_4d) {
+      tma_load_4d(sA, &tmA, 0, k0, m0 / 8, za, &full[s]);              // [BM/8 chunks][8 k][8 m]
     } else {
 #pragma unroll
       for (int c = 0; c < BM / 8; ++c) tma_load_3d(sA + c * 1024, &tmA, 2 * (m0 + 8 * c), k0, za, &full[s]);
     }
     if (CONJ_B) {
       tma_load_3d(sB, &tmB, 2 * k0, n0, zb, &full[s]);                 // [BN rows][8 k]
+    } else if (args.b_4d) {
+      tma_load_4d(sB, &tmB, 0, k0, n0 / 8, zb, &full[s]);              // [BN/8 chunks][8 k][8 n]
     } else {
 #pragma unroll
       for (int c = 0; c < BN / 8; ++c) tma_load_3d(sB + c * 1024, &tmB, 2 * (n0 + 8 * c), k0, zb, &full[s]);
     }
   };
+  // Stage x reuses the slot of stage x-STAGES, free once all 8 warps released it.  The
+  // issuer polls (test_wait) instead of blocking so that warp 0 is not held back by the
+  // slowest warp; it blocks only if the stage it is about to consume is not in flight.
+  int issued = 0;
+  auto try_issue = [&](int it, bool must) {
+    while (issued < nk && issued <= it + STAGES - 1) {
+      if (issued >= STAGES) {
+        const uint32_t par = ((issued / STAGES) + 1) & 1;
+        if (must && issued <= it) mbar_wait(&empty[issued % STAGES], par);
+        else if (!mbar_test(&empty[issued % STAGES], par)) break;
+      }
+      issue(issued);
+      ++issued;
+    }
+  };
   if (issuer) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
-    for (int it = 0; it < min(nk, STAGES - 1); ++it) issue(it);
+    try_issue(0, true);
   }
 
   // ================= DMMA consumers
@@ -131,9 +156,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int slot = lane & 3;        // k slot of the 8x8x4 MMA
   const int c = slot & 1;           // component of the interleaved complex k
   const int khalf = (slot >> 1) * 4;
-  constexpr double sa = CONJ_A ? -1.0 : 1.0;
-  constexpr double sb = CONJ_B ? -1.0 : 1.0;
-  constexpr double s_b1 = -sa * sb;
+  constexpr unsigned long long SIGN = 0x8000000000000000ull;
+  // A1 = [a_r, -sa*sb*a_i]: flip the imaginary lane when sa*sb = +1
+  const unsigned long long mask1 = (c == 1 && CONJ_A == CONJ_B) ? SIGN : 0ull;
+  // A2 = [sb*a_r, sa*a_i]
+  const unsigned long long mask2 = ((c == 0 && CONJ_B) || (c == 1 && CONJ_A)) ? SIGN : 0ull;
 
   double acc[4][4][2][2];
 #pragma unroll
@@ -145,43 +172,39 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   for (int it = 0; it < nk; ++it) {
     const int s = it % STAGES;
-    if (issuer) {
-      // refill the slot consumed in iteration it-1 (all warps must have released it)
-      const int nx = it + STAGES - 1;
-      if (nx < nk) {
-        if (nx >= STAGES) mbar_wait(&empty[nx % STAGES], ((nx / STAGES) + 1) & 1);
-        issue(nx);
-      }
-    }
+    if (issuer) try_issue(it, true);
     mbar_wait(&full[s], (it / STAGES) & 1);
     const uint8_t* sA = smem + s * STAGE_BYTES;
     const uint8_t* sB = sA + A_BYTES;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int k = q + khalf;
-      double a[4];
+      unsigned long long a[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int r = warp_m * 32 + 8 * i + g;
         const uint32_t o = (CONJ_A ? off_mn(r, k) : off_kc(r, k)) + 8 * c;
-        a[i] = *reinterpret_cast<const double*>(sA + o);
+        a[i] = *reinterpret_cast<const unsigned long long*>(sA + o);
       }
       double b1[4], b2[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int r = warp_n * 32 + 8 * j + g;
         const uint32_t o = CONJ_B ? off_kc(r, k) : off_mn(r, k);
-        const double2 b = *reinterpret_cast<const double2*>(sB + o);
-        b1[j] = c ? s_b1 * b.y : b.x;
-        b2[j] = c ? sa * b.x : sb * b.y;
+        b1[j] = *reinterpret_cast<const double*>(sB + o + 8 * c);
+        b2[j] = *reinterpret_cast<const double*>(sB + o + 8 * (1 - c));
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4; ++i) {
+        const double a1 = __longlong_as_double((long long)(a[i] ^ mask1));
+        const double a2 = __longlong_as_double((long long)(a[i] ^ mask2));
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          dmma_8x8x4(acc[i][j][0][0], acc[i][j][0][1], a[i], b1[j]);
-          dmma_8x8x4(acc[i][j][1][0], acc[i][j][1][1], a[i], b2[j]);
+          dmma_8x8x4(acc[i][j][0][0], acc[i][j][0][1], a1, b1[j]);
+          dmma_8x8x4(acc[i][j][1][0], acc[i][j][1][1], a2, b2[j]);
         }
+      }
+      if (q == 1 && issuer) try_issue(it, false);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -250,6 +273,25 @@ bool make_map(CUtensorMap* map, const void* base, long long rows, long long cols
   return r == CUDA_SUCCESS;
 }
 
+// m/n-contiguous operand [rows = k][cols] as a 4D tensor {16 doubles, rows, chunks of 8
+// complex (stride 128 B), batch}; one box {16, 8, box_chunks, 1} fills a whole stage tile.
+// Column chunks are read whole, so this is used only when round_up(cols, 8) <= ld (the
+// extra columns then stay inside each row and only feed discarded outputs).
+bool make_map_4d(CUtensorMap* map, const void* base, long long rows, long long cols, long long ld, long long stride,
+                 long long batch, int box_chunks) {
+  PFN_encodeTiled_t enc = get_encode();
+  if (!enc) return false;
+  const bool batched = stride != 0 && batch > 1;
+  cuuint64_t dims[4] = {16, (cuuint64_t)rows, (cuuint64_t)ceil_div(cols, 8), (cuuint64_t)(batched ? batch : 1)};
+  cuuint64_t strides[3] = {(cuuint64_t)(ld * 16), 128, (cuuint64_t)((batched ? stride : ld * rows) * 16)};
+  cuuint32_t box[4] = {16, 8, (cuuint32_t)box_chunks, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 template <bool CA, bool CB>
 cudaError_t launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const Args& args, int batch) {
   static bool attr = false;
@@ -283,9 +325,13 @@ int zgemm(cudaStream_t st, int opA, int opB, long long M, long long N, long long
   CUtensorMap ma, mb;
   const long long Ka = K > 0 ? K : 1;
   // op(A) = A: stored [M][K], k-contiguous tile [BM rows][8 k]; op(A) = A^dag: stored [K][M].
+  const bool a4 = opA == 1 && round_up(M, 8) <= lda && !getenv("TRAJ_NO_TMA4D");
+  const bool b4 = opB == 0 && round_up(N, 8) <= ldb && !getenv("TRAJ_NO_TMA4D");
   bool ok = opA == 0 ? make_map(&ma, A, M, Ka, lda, strideA, batch, BM)
-                     : make_map(&ma, A, Ka, M, lda, strideA, batch, 8);
-  ok = ok && (opB == 0 ? make_map(&mb, B, Ka, N, ldb, strideB, batch, 8)
+                     : (a4 ? make_map_4d(&ma, A, Ka, M, lda, strideA, batch, BM / 8)
+                           : make_map(&ma, A, Ka, M, lda, strideA, batch, 8));
+  ok = ok && (opB == 0 ? (b4 ? make_map_4d(&mb, B, Ka, N, ldb, strideB, batch, BN / 8)
+                             : make_map(&mb, B, Ka, N, ldb, strideB, batch, 8))
                        : make_map(&mb, B, N, Ka, ldb, strideB, batch, BN));
   if (!ok) {
     if (err) *err = "zgemm: cuTensorMapEncodeTiled failed";
@@ -300,6 +346,8 @@ int zgemm(cudaStream_t st, int opA, int opB, long long M, long long N, long long
   args.flags = flags;
   args.a_batched = strideA != 0 && batch > 1;
   args.b_batched = strideB != 0 && batch > 1;
+  args.a_4d = a4;
+  args.b_4d = b4;
   args.alpha_re = alpha_re;
   args.alpha_im = alpha_im;
   args.beta = beta;
