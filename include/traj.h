@@ -133,6 +133,11 @@ int traj_failed(traj_handle h, int64_t traj, int32_t* flag);
  * "occupied" outcomes. */
 int traj_last_clicks(traj_handle h, int64_t traj, int64_t* n_clicks, int64_t* n_occupied);
 
+/* Number of CholeskyQR2 second passes that needed the full Cholesky because
+ * N max|G2 - I|^2 >= 1e-18 (otherwise the first-order factor, exact to rounding, is used;
+ * environment TRAJ_CQR2_FULL=1 forces the full factorisation every time). */
+int traj_cqr2_fallbacks(traj_handle h, int64_t* n);
+
 /* Per-phase device timing with CUDA events on the handle's stream.  enable != 0
  * starts recording (and zeroes the totals).  traj_phase_times fills ms[TRAJ_NPHASES]
  * with accumulated milliseconds and launches[TRAJ_NPHASES] with kernel-launch counts

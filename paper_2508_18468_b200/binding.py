@@ -71,6 +71,7 @@ _SIGS = {
     "traj_set_step": (ctypes.c_int, [_P, _I64]),
     "traj_failed": (ctypes.c_int, [_P, _I64, ctypes.POINTER(ctypes.c_int32)]),
     "traj_last_clicks": (ctypes.c_int, [_P, _I64, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
+    "traj_cqr2_fallbacks": (ctypes.c_int, [_P, ctypes.POINTER(_I64)]),
     "traj_profile": (ctypes.c_int, [_P, ctypes.c_int]),
     "traj_phase_times": (ctypes.c_int, [_P, ctypes.POINTER(_D), ctypes.POINTER(_I64)]),
     "traj_kernel_launches": (ctypes.c_longlong, []),
@@ -293,6 +294,11 @@ class Trajectories:
     @step_index.setter
     def step_index(self, v: int):
         self._c(lib().traj_set_step(self._h, int(v)))
+
+    def cqr2_fallbacks(self) -> int:
+        n = ctypes.c_int64(0)
+        self._c(lib().traj_cqr2_fallbacks(self._h, ctypes.byref(n)))
+        return n.value
 
     # -- profiling
     def profile(self, enable: bool = True):

@@ -24,21 +24,20 @@ constexpr int NB = 64;            // leaf size
 constexpr int LD = NB + 1;        // padded smem row (complex)
 constexpr int LEAF_THREADS = 256;
 
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
 __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {   // conj(a) * b
   return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
 }
 
 // One CTA per batch entry: n <= 64 diagonal block.  Reads the upper triangle of G,
-// writes X = R^-1 (upper) and zeros below the diagonal.
+// writes X = R^-1 (upper) and zeros below the diagonal.  Right-looking elimination with
+// G = L L^dag (L = R^dag): step j scales row j of the working matrix A (its final row of
+// R) and row j of W, then eliminates rows i > j in A (upper part) and applies the same
+// row operation to W; W ends as L^-1, so X = R^-1 = W^dag.  Two barriers per column.
 __global__ void __launch_bounds__(LEAF_THREADS) chol_leaf_kernel(int n, cplx* G, long long ldg, long long sG, cplx* X,
                                                                   long long ldx, long long sX, int32_t* failed) {
   extern __shared__ double2 sm[];
-  double2* R = sm;               // [NB][LD]
-  double2* Xs = sm + NB * LD;    // [NB][LD]
-  __shared__ double inv_piv;
+  double2* R = sm;               // [NB][LD]  working matrix -> R (upper)
+  double2* Ws = sm + NB * LD;    // [NB][LD]  -> L^-1 (lower)
   __shared__ int bad;
   const int b = blockIdx.x, tid = threadIdx.x;
   const cplx* g = G + b * sG;
@@ -47,74 +46,52 @@ __global__ void __launch_bounds__(LEAF_THREADS) chol_leaf_kernel(int n, cplx* G,
   for (int idx = tid; idx < n * n; idx += LEAF_THREADS) {
     const int i = idx / n, j = idx % n;
     if (i <= j) R[i * LD + j] = g[(long long)i * ldg + j];
+    Ws[i * LD + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
   }
   __syncthreads();
-  // right-looking Cholesky, upper: after step j, row j of R is final.
   for (int j = 0; j < n; ++j) {
-    if (tid == 0) {
-      const double d = R[j * LD + j].x;
-      if (!(d > 0.0) || !isfinite(d)) bad = 1;
-      const double r = sqrt(d);
-      R[j * LD + j] = make_double2(r, 0.0);
-      inv_piv = 1.0 / r;
+    // (1) pivot and scaling of row j (every thread reads the pivot itself: no extra barrier)
+    const double d = R[j * LD + j].x;
+    const double r = sqrt(d);
+    const double ip = 1.0 / r;
+    if (tid == 0 && (!(d > 0.0) || !isfinite(d))) bad = 1;
+    __syncthreads();     // all threads have read R[j][j] before it is overwritten
+    for (int k = j + tid; k < n; k += LEAF_THREADS) {
+      const double2 v = R[j * LD + k];
+      R[j * LD + k] = k == j ? make_double2(r, 0.0) : make_double2(v.x * ip, v.y * ip);
+    }
+    for (int k = tid; k <= j; k += LEAF_THREADS) {
+      const double2 v = Ws[j * LD + k];
+      Ws[j * LD + k] = make_double2(v.x * ip, v.y * ip);
     }
     __syncthreads();
-    for (int k = j + 1 + tid; k < n; k += LEAF_THREADS) {
-      double2 v = R[j * LD + k];
-      R[j * LD + k] = make_double2(v.x * inv_piv, v.y * inv_piv);
-    }
-    __syncthreads();
-    const int m = n - j - 1;                       // trailing block (j+1..n-1)^2, upper part
-    for (int idx = tid; idx < m * m; idx += LEAF_THREADS) {
-      const int i = j + 1 + idx / m, k = j + 1 + idx % m;
-      if (i <= k) {
-        const double2 p = cmulc(R[j * LD + i], R[j * LD + k]);
-        R[i * LD + k].x -= p.x;
-        R[i * LD + k].y -= p.y;
-      }
-    }
-    __syncthreads();
-  }
-  // X = R^-1 by back substitution, 4 threads per column (column k = tid / 4).
-  {
-    const int k = tid >> 2, part = tid & 3;
-    for (int i = n - 1; i >= 0; --i) {
-      double2 s = make_double2(0.0, 0.0);
-      if (k < n && i < k) {
-        for (int l = i + 1 + part; l <= k; l += 4) {
-          const double2 p = cmul(R[i * LD + l], Xs[l * LD + k]);
-          s.x += p.x;
-          s.y += p.y;
+    // (2) eliminate rows i > j: l_ij = conj(R_ji)
+    const int m = n - j - 1;
+    const int wA = m * m, wW = m * (j + 1);
+    for (int idx = tid; idx < wA + wW; idx += LEAF_THREADS) {
+      if (idx < wA) {
+        const int i = j + 1 + idx / m, k = j + 1 + idx % m;
+        if (i <= k) {
+          const double2 p = cmulc(R[j * LD + i], R[j * LD + k]);
+          R[i * LD + k].x -= p.x;
+          R[i * LD + k].y -= p.y;
         }
+      } else {
+        const int q = idx - wA;
+        const int i = j + 1 + q / (j + 1), k = q % (j + 1);
+        const double2 p = cmulc(R[j * LD + i], Ws[j * LD + k]);
+        Ws[i * LD + k].x -= p.x;
+        Ws[i * LD + k].y -= p.y;
       }
-      s.x += __shfl_xor_sync(0xffffffffu, s.x, 1);
-      s.y += __shfl_xor_sync(0xffffffffu, s.y, 1);
-      s.x += __shfl_xor_sync(0xffffffffu, s.x, 2);
-      s.y += __shfl_xor_sync(0xffffffffu, s.y, 2);
-      if (k < n && part == 0) {
-        const double rii = R[i * LD + i].x;
-        if (i == k) Xs[i * LD + k] = make_double2(1.0 / rii, 0.0);
-        else if (i < k) Xs[i * LD + k] = make_double2(-s.x / rii, -s.y / rii);
-      }
-      __syncthreads();
     }
+    __syncthreads();
   }
   for (int idx = tid; idx < n * n; idx += LEAF_THREADS) {
-    const int i = idx / n, j = idx % n;
-    x[(long long)i * ldx + j] = i <= j ? Xs[i * LD + j] : make_double2(0.0, 0.0);
+    const int i = idx / n, j = idx % n;     // X_ij = conj(W_ji), upper
+    const double2 w = Ws[j * LD + i];
+    x[(long long)i * ldx + j] = i <= j ? make_double2(w.x, -w.y) : make_double2(0.0, 0.0);
   }
   if (tid == 0 && bad && failed) failed[b] = 1;
-}
-
-// zero a rows x cols block in each batch entry
-__global__ void zero_block_kernel(cplx* P, long long ld, long long stride, int rows, int cols) {
-  const long long total = (long long)rows * cols;
-  cplx* p = P + blockIdx.y * stride;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const long long i = idx / cols, j = idx % cols;
-    p[i * ld + j] = make_double2(0.0, 0.0);
-  }
 }
 
 int split(long long n) { return (int)(NB * ceil_div(ceil_div(n, NB), 2)); }
@@ -157,7 +134,6 @@ int rec(Ctx& c, long long o, long long n) {
   cplx* XA = c.X + o * c.ldx + o;
   cplx* XB = c.X + o * c.ldx + (o + h);
   cplx* XC = c.X + (o + h) * c.ldx + (o + h);
-  cplx* XL = c.X + (o + h) * c.ldx + o;
   int s;
   if ((s = rec(c, o, h))) return s;
   // R_B^dag = B^dag X_A : (r x h) = op_C(B: h x r) * X_A (h x h, upper)
@@ -177,14 +153,6 @@ int rec(Ctx& c, long long o, long long n) {
   if ((s = zgemm(c.st, 0, 0, h, r, h, -1.0, 0.0, XA, c.ldx, c.sX, c.tmp, c.ldt, c.sT, 0.0, XB, c.ldx, c.sX, c.batch,
                  TRAJ_TRI_A_UPPER_F, c.err)))
     return s;
-  dim3 grid((unsigned)std::min<long long>(ceil_div(r * h, 256), 1024), (unsigned)c.batch);
-  zero_block_kernel<<<grid, 256, 0, c.st>>>(XL, c.ldx, c.sX, (int)r, (int)h);
-  count_launch();
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    if (c.err) *c.err = std::string("zero block: ") + cudaGetErrorString(e);
-    return 4;
-  }
   return 0;
 }
 
@@ -217,6 +185,20 @@ int chol_inverse(cudaStream_t st, long long n, cplx* G, long long ldg, long long
   c.sT = n <= NB ? 0 : split(n) * c.ldt;
   c.failed = failed;
   c.err = err;
+  if (n > NB) {
+    // the strict lower triangle of X must read as zeros (triangular GEMM tiles cross it)
+    cudaError_t e = cudaSuccess;
+    if (batch == 1 || sX == n * ldx) {
+      e = cudaMemset2DAsync(X, (size_t)ldx * 16, 0, (size_t)n * 16, (size_t)(n * batch), st);
+    } else {
+      for (long long b = 0; b < batch && e == cudaSuccess; ++b)
+        e = cudaMemset2DAsync(X + b * sX, (size_t)ldx * 16, 0, (size_t)n * 16, (size_t)n, st);
+    }
+    if (e != cudaSuccess) {
+      if (err) *err = std::string("chol_inverse memset: ") + cudaGetErrorString(e);
+      return 4;
+    }
+  }
   return rec(c, 0, n);
 }
 

@@ -282,6 +282,55 @@ __global__ void init_state_kernel(cplx* U, long long ld, long long sU, const int
   if (k < N) U[t * sU + (long long)sites[k] * ld + k] = make_double2(1.0, 0.0);
 }
 
+// max over the upper triangle of |G_ij - delta_ij| (component-wise), per batch entry;
+// out[t] must be zeroed (non-negative doubles order like their bit patterns).
+__global__ void gram_deviation_kernel(const cplx* G, long long ld, long long sG, int n, unsigned long long* out) {
+  __shared__ double red[32];
+  const int t = blockIdx.y;
+  const cplx* g = G + t * sG;
+  const long long total = (long long)n * n;
+  double m = 0.0;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / n), j = (int)(idx % n);
+    if (i > j) continue;
+    const double2 v = g[(long long)i * ld + j];
+    const double e = fmax(fabs(v.x - (i == j ? 1.0 : 0.0)), fabs(v.y));
+    m = (e > m || e != e) ? e : m;      // NaN propagates
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b = fmax(b, red[w]);
+    atomicMax(out + t, (unsigned long long)__double_as_longlong(b));
+  }
+}
+
+// CholeskyQR2 second pass: G = I + E with |E| ~ kappa^2 eps, so R = I + F + O(E^2) with
+// F = triu(E, 1) + diag(E)/2 and R^-1 = I - F + O(E^2).  X = I - F (upper, zeros below).
+__global__ void first_order_inverse_kernel(const cplx* G, long long ldg, long long sG, cplx* X, long long ldx,
+                                           long long sX, int n) {
+  const int t = blockIdx.y;
+  const cplx* g = G + t * sG;
+  cplx* x = X + t * sX;
+  const long long total = (long long)n * n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / n), j = (int)(idx % n);
+    double2 out = make_double2(0.0, 0.0);
+    if (i == j) {
+      out.x = 1.0 - 0.5 * (g[(long long)i * ldg + j].x - 1.0);
+    } else if (i < j) {
+      const double2 v = g[(long long)i * ldg + j];
+      out = make_double2(-v.x, -v.y);
+    }
+    x[(long long)i * ldx + j] = out;
+  }
+}
+
 cudaError_t last(std::string* err, const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess && err) *err = std::string(what) + ": " + cudaGetErrorString(e);
@@ -389,6 +438,23 @@ int build_k(cudaStream_t st, cplx* K, long long ld, int Lx, int Ly, const cplx* 
   build_k_kernel<<<(unsigned)std::min<long long>(ceil_div(L * L, 256), 148 * 64), 256, 0, st>>>(K, ld, Lx, Ly, kx, ky);
   count_launch();
   return last(err, "build_k") == cudaSuccess ? 0 : 4;
+}
+
+int gram_deviation(cudaStream_t st, const cplx* G, long long ld, long long sG, int n, int T, unsigned long long* out,
+                   std::string* err) {
+  if (cudaMemsetAsync(out, 0, (size_t)T * 8, st) != cudaSuccess) return 4;
+  dim3 grid((unsigned)std::min<long long>(ceil_div((long long)n * n, 256), 2048), T);
+  gram_deviation_kernel<<<grid, 256, 0, st>>>(G, ld, sG, n, out);
+  count_launch();
+  return last(err, "gram_deviation") == cudaSuccess ? 0 : 4;
+}
+
+int first_order_inverse(cudaStream_t st, const cplx* G, long long ldg, long long sG, cplx* X, long long ldx,
+                        long long sX, int n, int T, std::string* err) {
+  dim3 grid((unsigned)std::min<long long>(ceil_div((long long)n * n, 256), 8192), T);
+  first_order_inverse_kernel<<<grid, 256, 0, st>>>(G, ldg, sG, X, ldx, sX, n);
+  count_launch();
+  return last(err, "first_order_inverse") == cudaSuccess ? 0 : 4;
 }
 
 int init_state(cudaStream_t st, cplx* U, long long ld, long long sU, const int32_t* sites, int N, int T,

@@ -25,6 +25,12 @@ int sub_identity(cudaStream_t st, cplx* T, long long ld, const int32_t* S1, int 
 int zero_rows(cudaStream_t st, cplx* U, long long ld, const int32_t* rows, int nrows, int ncols, std::string* err);
 int entropy_reduce(cudaStream_t st, const double* lam, int n, double* S_out, int32_t* bad, std::string* err);
 int build_k(cudaStream_t st, cplx* K, long long ld, int Lx, int Ly, const cplx* kx, const cplx* ky, std::string* err);
+// out[t] = max_{i<=j} |G_ij - delta_ij| (as the bit pattern of a non-negative double)
+int gram_deviation(cudaStream_t st, const cplx* G, long long ld, long long sG, int n, int T, unsigned long long* out,
+                   std::string* err);
+// X = I - triu(E,1) - diag(E)/2 with E = G - I: R^-1 of G = R^dag R to O(|E|^2)
+int first_order_inverse(cudaStream_t st, const cplx* G, long long ldg, long long sG, cplx* X, long long ldx,
+                        long long sX, int n, int T, std::string* err);
 int init_state(cudaStream_t st, cplx* U, long long ld, long long sU, const int32_t* sites, int N, int T,
                std::string* err);
 

@@ -5,6 +5,7 @@
 #include <cusolverDn.h>
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <complex>
@@ -52,12 +53,16 @@ struct traj_ctx {
   int* eig_info = nullptr;
   double* S_dev = nullptr;
   int32_t* bad_dev = nullptr;
+  unsigned long long* gdev = nullptr;   // per-trajectory max |G2 - I| of the second CQR pass
   int32_t* region = nullptr;
+  bool full_cqr2 = false;                // TRAJ_CQR2_FULL=1: always factor G2 by chol_inverse
+  long long cqr2_fallbacks = 0;
   cplx* kcoef = nullptr;
   int32_t* sites = nullptr;
   cusolverDnHandle_t solver = nullptr;
   long long step = 0;
   int32_t* h_small = nullptr;     // pinned host scratch
+  double* h_dev = nullptr;        // pinned host copy of gdev
   std::vector<int64_t> last_nS, last_n1;
   std::string err;
   // profiling
@@ -174,6 +179,7 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
   lay.take(h->eig_info, 16);
   lay.take(h->S_dev, (size_t)T * 8);
   lay.take(h->bad_dev, (size_t)T * 4);
+  lay.take(h->gdev, (size_t)T * 8);
   lay.take(h->region, (size_t)L * 4);
   lay.take(h->kcoef, (size_t)(Lx + Ly) * 16);
   lay.take(h->sites, (size_t)N * 4);
@@ -266,6 +272,9 @@ struct Phase {
 };
 
 // CholeskyQR2 on U (state), tmp another buffer of the same shape; result in U.
+// Pass 2 sees G2 = I + E with |E| ~ kappa(U)^2 eps: its Cholesky inverse is taken from the
+// first-order closed form (exact up to N |E|^2, below rounding when N max|E|^2 < 1e-18,
+// checked on the device per step); otherwise, or with TRAJ_CQR2_FULL=1, chol_inverse.
 int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
   cplx* src = U;
   cplx* dst = tmp;
@@ -277,8 +286,24 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
     }
     {
       Phase p(h, TRAJ_PH_CHOL);
-      TRY(chol_inverse(h->st, h->N, h->G, h->ldN, h->sG, h->X, h->ldN, h->sG, h->T, h->chol_scratch, h->failed_dev,
-                       &h->err));
+      bool full = pass == 0 || h->full_cqr2;
+      if (!full) {
+        TRY(gram_deviation(h->st, h->G, h->ldN, h->sG, h->N, h->T, h->gdev, &h->err));
+        CK(cudaMemcpyAsync(h->h_dev, h->gdev, h->T * 8, cudaMemcpyDeviceToHost, h->st));
+        CK(cudaStreamSynchronize(h->st));
+        const double thr = 1e-9 / sqrt((double)h->N);
+        for (int t = 0; t < h->T; ++t) {
+          const double m = h->h_dev[t];
+          if (m > thr) full = true;           // NaN (failed trajectory) does not force the fallback
+        }
+        if (full) ++h->cqr2_fallbacks;
+      }
+      if (full) {
+        TRY(chol_inverse(h->st, h->N, h->G, h->ldN, h->sG, h->X, h->ldN, h->sG, h->T, h->chol_scratch,
+                         h->failed_dev, &h->err));
+      } else {
+        TRY(first_order_inverse(h->st, h->G, h->ldN, h->sG, h->X, h->ldN, h->sG, h->N, h->T, &h->err));
+      }
     }
     {
       Phase p(h, TRAJ_PH_TRMM);
@@ -499,7 +524,13 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
     g_err = msg;
     return st;
   };
-  if (cudaMallocHost(&h->h_small, std::max(2 * h->T, 16) * 4) != cudaSuccess) return bail(TRAJ_ECUDA, "cudaMallocHost");
+  if (cudaMallocHost(&h->h_small, std::max(2 * h->T, 16) * 4) != cudaSuccess ||
+      cudaMallocHost(&h->h_dev, std::max(h->T, 16) * 8) != cudaSuccess)
+    return bail(TRAJ_ECUDA, "cudaMallocHost");
+  {
+    const char* e = getenv("TRAJ_CQR2_FULL");
+    h->full_cqr2 = e && e[0] == '1';
+  }
   if (cusolverDnCreate(&h->solver) != CUSOLVER_STATUS_SUCCESS) return bail(TRAJ_ECUDA, "cusolverDnCreate");
   cusolverDnSetStream(h->solver, h->st);
   // zero the whole workspace: padded columns (ld > N) must read as zeros
@@ -637,6 +668,12 @@ int traj_last_clicks(traj_handle h, int64_t traj, int64_t* n_clicks, int64_t* n_
   return 0;
 }
 
+int traj_cqr2_fallbacks(traj_handle h, int64_t* n) {
+  if (!h || !n) return TRAJ_EINVAL;
+  *n = h->cqr2_fallbacks;
+  return 0;
+}
+
 int traj_profile(traj_handle h, int enable) {
   if (!h) return TRAJ_EINVAL;
   CK(cudaStreamSynchronize(h->st));
@@ -681,6 +718,7 @@ int traj_destroy(traj_handle h) {
   for (auto e : h->pool) cudaEventDestroy(e);
   if (h->solver) cusolverDnDestroy(h->solver);
   if (h->h_small) cudaFreeHost(h->h_small);
+  if (h->h_dev) cudaFreeHost(h->h_dev);
   delete h;
   return 0;
 }

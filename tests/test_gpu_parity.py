@@ -169,3 +169,33 @@ def test_projective_full_c3_invariants(P):
     Ac = np.arange(w.L // 8, w.L)
     sa, sc = g.entropy(A)[0], g.entropy(Ac)[0]
     assert abs(sa - sc) < 1e-8
+
+
+def test_cqr2_first_order_second_pass_matches_full(P):
+    """The second CQR pass uses R2^-1 = I - triu(E,1) - diag(E)/2 (exact to O(N|E|^2));
+    the result equals the full Cholesky second pass, and an ill-conditioned state falls back."""
+    import os
+    import torch
+    args = (200, 1, "homodyne", [1.0, 3.0])
+    a = P.Trajectories(*args, seed=4)
+    os.environ["TRAJ_CQR2_FULL"] = "1"
+    try:
+        b = P.Trajectories(*args, seed=4)
+    finally:
+        del os.environ["TRAJ_CQR2_FULL"]
+    a.step(40)
+    b.step(40)
+    assert a.cqr2_fallbacks() == 0
+    for t in range(2):
+        assert np.abs(a.correlation(t).cpu().numpy() - b.correlation(t).cpu().numpy()).max() < 1e-12
+    # kappa ~ 1e5: pass 1 leaves |E| ~ 1e-6, so the second pass must factor G2 fully
+    L, N = 200, 100
+    U = workloads.random_matrix(L, N, 3)
+    U[:, 1] = U[:, 0] + 1e-5 * U[:, 1]
+    c = P.Trajectories(L, 1, "homodyne", [0.0])
+    c.set_state(0, torch.from_numpy(U).cuda())
+    c.orthonormalize()
+    assert c.cqr2_fallbacks() == 1
+    Ug = c.get_state(0).cpu().numpy()
+    assert np.abs(Ug.conj().T @ Ug - np.eye(N)).max() < 1e-12
+    assert np.abs(c.correlation(0).cpu().numpy() - gaussian.correlation(gaussian.orthonormalize(U))).max() < 1e-9
