@@ -14,6 +14,7 @@
 #include <math.h>
 #include "common.cuh"
 #include "monitor.h"
+#include "zgemm.h"
 
 namespace traj {
 
@@ -160,65 +161,112 @@ __device__ __forceinline__ bool decide(double p, double u1) {
   return occ;
 }
 
-// Sequential conditional Born sampling on C_SS (one CTA per trajectory).  D0: the GEMM
-// output (kept), Dw: work copy.  Outputs occ[t][r], pos1 (indices r with occ), S1/S0 site
-// lists and counts (k1, k0).
-__global__ void __launch_bounds__(1024) sample_kernel(const cplx* D0, cplx* Dw, long long ldd, long long sD,
-                                                      const int32_t* S, int cap, const int32_t* count,
-                                                      long long step, long long traj_base, uint32_t key0,
-                                                      uint32_t key1, int32_t* occ, int32_t* pos1, int32_t* S1,
-                                                      int32_t* S0, int32_t* k1_out, int32_t* k0_out) {
-  __shared__ double2 piv_inv;
+// Blocked sequential conditional Born sampling on C_SS (readings Q13, Q16, Q17).
+// Sites are visited in ascending order in panels of PB.  For a panel [s0, s0+nb) the
+// kernel below runs the sequential decisions on the nb x nb diagonal block in shared memory:
+//   p = Re C_tt, occupied iff u1 < p (Q17 guard), piv_t = p (occupied) or p - 1 (empty),
+//   C <- C - C[:,t] C[t,:] / piv_t inside the block (Eq. A1 / sign-corrected A2),
+// and returns the unit-lower multipliers as Linv = L^-1 and Dinv_Linv = diag(1/piv) L^-1.
+// The trailing block then takes the same rank-nb Schur update on the GEMM:
+//   Y = L^-1 C12, Z = diag(1/piv) Y, C22 <- C22 - Y^dag Z.
+constexpr int PB = 64;
+constexpr int PLD = PB + 1;
+
+__global__ void __launch_bounds__(256) panel_sample_kernel(const cplx* Dw, long long ldd, long long sD,
+                                                           const int32_t* S, int cap, const int32_t* count, int s0,
+                                                           long long step, long long traj_base, uint32_t key0,
+                                                           uint32_t key1, int32_t* occ, cplx* Linv, cplx* DLinv) {
+  extern __shared__ double2 psm[];
+  double2* A = psm;               // [PB][PLD] panel block, then multipliers below the diagonal
+  double2* Li = psm + PB * PLD;   // [PB][PLD] L^-1
+  __shared__ double inv_s;
+  __shared__ double piv_s[PB];
   const int t = blockIdx.x;
   const int m = count[t] < cap ? count[t] : cap;
-  const cplx* d0 = D0 + t * sD;
-  cplx* D = Dw + t * sD;
-  const int32_t* s = S + (long long)t * cap;
-  int32_t* oc = occ + (long long)t * cap;
-  for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
-    const int i = idx / m, k = idx % m;
-    D[(long long)i * ldd + k] = d0[(long long)i * ldd + k];
+  if (s0 >= m) return;
+  const int nb = min(PB, m - s0);
+  const cplx* D = Dw + t * sD + (long long)s0 * ldd + s0;
+  for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
+    const int i = idx / nb, k = idx % nb;
+    A[i * PLD + k] = D[(long long)i * ldd + k];
   }
   __syncthreads();
-  for (int r = 0; r < m; ++r) {
+  for (int r = 0; r < nb; ++r) {
     if (threadIdx.x == 0) {
-      const int site = s[r];
+      const int site = S[(long long)t * cap + s0 + r];
       const u32x4 x = philox4x32_10(u32x4{(uint32_t)site, (uint32_t)step, (uint32_t)(traj_base + t), 0u}, key0, key1);
       const double u1 = u53(x.z, x.w);
-      const double p = D[(long long)r * ldd + r].x;
+      const double p = A[r * PLD + r].x;
       const bool o = decide(p, u1);
-      oc[r] = o ? 1 : 0;
+      occ[(long long)t * cap + s0 + r] = o ? 1 : 0;
       const double pv = o ? p : p - 1.0;
-      piv_inv = make_double2(1.0 / pv, 0.0);
+      piv_s[r] = pv;
+      inv_s = 1.0 / pv;
     }
     __syncthreads();
-    const int mm = m - r - 1;
-    const double inv = piv_inv.x;
+    const double inv = inv_s;
+    for (int i = r + 1 + threadIdx.x; i < nb; i += blockDim.x) {     // multipliers l_ir
+      const double2 v = A[i * PLD + r];
+      A[i * PLD + r] = make_double2(v.x * inv, v.y * inv);
+    }
+    __syncthreads();
+    const int mm = nb - r - 1;
     for (int idx = threadIdx.x; idx < mm * mm; idx += blockDim.x) {
       const int i = r + 1 + idx / mm, k = r + 1 + idx % mm;
-      const double2 a = D[(long long)i * ldd + r], b = D[(long long)r * ldd + k];
-      const double2 p = cmul(a, b);
-      double2& dst = D[(long long)i * ldd + k];
-      dst.x -= p.x * inv;
-      dst.y -= p.y * inv;
+      const double2 p = cmul(A[i * PLD + r], A[r * PLD + k]);
+      A[i * PLD + k].x -= p.x;
+      A[i * PLD + k].y -= p.y;
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    int n1 = 0, n0 = 0;
-    for (int r = 0; r < m; ++r) {
-      if (oc[r]) {
-        pos1[(long long)t * cap + n1] = r;
-        S1[(long long)t * cap + n1] = s[r];
-        ++n1;
-      } else {
-        S0[(long long)t * cap + n0] = s[r];
-        ++n0;
+  // L^-1 by forward substitution, one thread per column (L unit lower, multipliers in A)
+  for (int k = threadIdx.x; k < PB; k += blockDim.x) {
+    for (int i = 0; i < PB; ++i) {
+      double2 v = make_double2(i == k ? 1.0 : 0.0, 0.0);
+      if (i > k && i < nb) {
+        for (int j = k; j < i; ++j) {
+          const double2 p = cmul(A[i * PLD + j], Li[j * PLD + k]);
+          v.x -= p.x;
+          v.y -= p.y;
+        }
+      } else if (i >= nb) {
+        v = make_double2(0.0, 0.0);
       }
+      Li[i * PLD + k] = v;
     }
-    k1_out[t] = n1;
-    k0_out[t] = n0;
   }
+  __syncthreads();
+  cplx* lo = Linv + (long long)t * PB * PB;
+  cplx* dl = DLinv + (long long)t * PB * PB;
+  for (int idx = threadIdx.x; idx < PB * PB; idx += blockDim.x) {
+    const int i = idx / PB, k = idx % PB;
+    const double2 v = Li[i * PLD + k];
+    lo[idx] = v;
+    const double ip = i < nb ? 1.0 / piv_s[i] : 0.0;
+    dl[idx] = make_double2(v.x * ip, v.y * ip);
+  }
+}
+
+// occupied / empty site lists from the outcome flags (one thread per trajectory)
+__global__ void finalize_outcomes_kernel(const int32_t* S, int cap, const int32_t* count, const int32_t* occ, int T,
+                                         int32_t* pos1, int32_t* S1, int32_t* S0, int32_t* k1_out, int32_t* k0_out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int m = count[t] < cap ? count[t] : cap;
+  const long long b = (long long)t * cap;
+  int n1 = 0, n0 = 0;
+  for (int r = 0; r < m; ++r) {
+    if (occ[b + r]) {
+      pos1[b + n1] = r;
+      S1[b + n1] = S[b + r];
+      ++n1;
+    } else {
+      S0[b + n0] = S[b + r];
+      ++n0;
+    }
+  }
+  k1_out[t] = n1;
+  k0_out[t] = n0;
 }
 
 // D11[a][b] = D0[pos[a]][pos[b]]
@@ -395,12 +443,45 @@ int gather_rows(cudaStream_t st, const cplx* src, long long lds, long long sS, c
 }
 
 int sample_outcomes(cudaStream_t st, const cplx* D0, cplx* Dw, long long ldd, long long sD, const int32_t* S, int cap,
-                    const int32_t* count, int T, long long step, long long traj_base, uint64_t seed, int32_t* occ,
-                    int32_t* pos1, int32_t* S1, int32_t* S0, int32_t* k1, int32_t* k0, std::string* err) {
-  sample_kernel<<<T, 1024, 0, st>>>(D0, Dw, ldd, sD, S, cap, count, step, traj_base, (uint32_t)(seed & 0xffffffffu),
-                                    (uint32_t)(seed >> 32), occ, pos1, S1, S0, k1, k0);
+                    const int32_t* count, int maxc, int T, long long step, long long traj_base, uint64_t seed,
+                    int32_t* occ, cplx* Linv, cplx* DLinv, cplx* Ybuf, cplx* Zbuf, long long ldy, int32_t* pos1,
+                    int32_t* S1, int32_t* S0, int32_t* k1, int32_t* k0, std::string* err) {
+  const uint32_t key0 = (uint32_t)(seed & 0xffffffffu), key1 = (uint32_t)(seed >> 32);
+  if (cudaMemcpyAsync(Dw, D0, (size_t)T * sD * 16, cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
+    if (err) *err = "sample: copy";
+    return 4;
+  }
+  static bool attr = false;
+  const int smem = 2 * PB * PLD * (int)sizeof(double2);
+  if (!attr) {
+    cudaFuncSetAttribute(panel_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  for (int s0 = 0; s0 < maxc; s0 += PB) {
+    panel_sample_kernel<<<T, 256, smem, st>>>(Dw, ldd, sD, S, cap, count, s0, step, traj_base, key0, key1, occ, Linv,
+                                              DLinv);
+    count_launch();
+    if (last(err, "panel_sample") != cudaSuccess) return 4;
+    const int rest = maxc - s0 - PB;
+    if (rest <= 0) break;
+    const cplx* C12 = Dw + (long long)s0 * ldd + s0 + PB;
+    int r;
+    // Y = L^-1 C12, Z = diag(1/piv) L^-1 C12  (PB x rest)
+    if ((r = zgemm(st, 0, 0, PB, rest, PB, 1.0, 0.0, Linv, PB, PB * PB, C12, ldd, sD, 0.0, Ybuf, ldy, PB * ldy, T,
+                   TRAJ_TRI_A_LOWER_F, err)))
+      return r;
+    if ((r = zgemm(st, 0, 0, PB, rest, PB, 1.0, 0.0, DLinv, PB, PB * PB, C12, ldd, sD, 0.0, Zbuf, ldy, PB * ldy, T,
+                   TRAJ_TRI_A_LOWER_F, err)))
+      return r;
+    // C22 -= Y^dag Z
+    cplx* C22 = Dw + (long long)(s0 + PB) * ldd + s0 + PB;
+    if ((r = zgemm(st, 1, 0, rest, rest, PB, -1.0, 0.0, Ybuf, ldy, PB * ldy, Zbuf, ldy, PB * ldy, 1.0, C22, ldd, sD,
+                   T, 0, err)))
+      return r;
+  }
+  finalize_outcomes_kernel<<<(unsigned)ceil_div(T, 128), 128, 0, st>>>(S, cap, count, occ, T, pos1, S1, S0, k1, k0);
   count_launch();
-  return last(err, "sample") == cudaSuccess ? 0 : 4;
+  return last(err, "finalize_outcomes") == cudaSuccess ? 0 : 4;
 }
 
 int gather_sub(cudaStream_t st, const cplx* D0, long long ld0, const int32_t* pos, int k, cplx* D11, long long ld1,

@@ -16,9 +16,12 @@ int compact(cudaStream_t st, const int32_t* flags, int L, int T, int32_t* list, 
 int gather_rows(cudaStream_t st, const cplx* src, long long lds, long long sS, const int32_t* idx, long long sIdx,
                 const int32_t* count_dev, int rows, int T, cplx* dst, long long ldd, long long sD, int ncols,
                 std::string* err);
+// Blocked conditional Born sampling of every trajectory's click list on C_SS (D0, kept);
+// Dw: work copy; Linv/DLinv: [T][64][64]; Ybuf/Zbuf: [T][64][ldy] with ldy >= maxc.
 int sample_outcomes(cudaStream_t st, const cplx* D0, cplx* Dw, long long ldd, long long sD, const int32_t* S, int cap,
-                    const int32_t* count, int T, long long step, long long traj_base, uint64_t seed, int32_t* occ,
-                    int32_t* pos1, int32_t* S1, int32_t* S0, int32_t* k1, int32_t* k0, std::string* err);
+                    const int32_t* count, int maxc, int T, long long step, long long traj_base, uint64_t seed,
+                    int32_t* occ, cplx* Linv, cplx* DLinv, cplx* Ybuf, cplx* Zbuf, long long ldy, int32_t* pos1,
+                    int32_t* S1, int32_t* S0, int32_t* k1, int32_t* k0, std::string* err);
 int gather_sub(cudaStream_t st, const cplx* D0, long long ld0, const int32_t* pos, int k, cplx* D11, long long ld1,
                std::string* err);
 int sub_identity(cudaStream_t st, cplx* T, long long ld, const int32_t* S1, int k, std::string* err);

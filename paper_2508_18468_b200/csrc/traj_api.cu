@@ -44,6 +44,7 @@ struct traj_ctx {
   int32_t *flags = nullptr, *S = nullptr, *count = nullptr, *occ = nullptr, *pos1 = nullptr, *S1 = nullptr,
           *S0 = nullptr, *k1 = nullptr, *k0 = nullptr;
   cplx *US = nullptr, *D0 = nullptr, *Dw = nullptr, *D11 = nullptr, *X11 = nullptr, *W = nullptr, *Tm = nullptr;
+  cplx *Linv = nullptr, *DLinv = nullptr, *Ybuf = nullptr, *Zbuf = nullptr;
   void* chol_scratch_small = nullptr;
   long long sUS = 0, sD = 0;
   // observables
@@ -198,6 +199,10 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     lay.take(h->US, (size_t)T * cap * ldN * 16);
     lay.take(h->D0, (size_t)T * cap * ldcap * 16);
     lay.take(h->Dw, (size_t)T * cap * ldcap * 16);
+    lay.take(h->Linv, (size_t)T * 64 * 64 * 16);
+    lay.take(h->DLinv, (size_t)T * 64 * 64 * 16);
+    lay.take(h->Ybuf, (size_t)T * 64 * ldcap * 16);
+    lay.take(h->Zbuf, (size_t)T * 64 * ldcap * 16);
     lay.take(h->D11, (size_t)cap * ldcap * 16);
     lay.take(h->X11, (size_t)cap * ldcap * 16);
     lay.take(h->chol_scratch_small, chol_scratch_bytes(cap, 1));
@@ -336,8 +341,9 @@ int projective(traj_ctx* h, cplx* U) {
   // count are never read by the sampler)
   TRY(zgemm(h->st, 0, 1, maxc, maxc, h->N, 1.0, 0.0, h->US, h->ldN, h->sUS, h->US, h->ldN, h->sUS, 0.0, h->D0,
             h->ldcap, h->sD, T, 0, &h->err));
-  TRY(sample_outcomes(h->st, h->D0, h->Dw, h->ldcap, h->sD, h->S, cap, h->count, T, h->step, h->cfg.traj_base,
-                      h->cfg.seed, h->occ, h->pos1, h->S1, h->S0, h->k1, h->k0, &h->err));
+  TRY(sample_outcomes(h->st, h->D0, h->Dw, h->ldcap, h->sD, h->S, cap, h->count, maxc, T, h->step,
+                      h->cfg.traj_base, h->cfg.seed, h->occ, h->Linv, h->DLinv, h->Ybuf, h->Zbuf, h->ldcap, h->pos1,
+                      h->S1, h->S0, h->k1, h->k0, &h->err));
   CK(cudaMemcpyAsync(h->h_small, h->k1, T * 4, cudaMemcpyDeviceToHost, h->st));
   CK(cudaMemcpyAsync(h->h_small + T, h->k0, T * 4, cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));

@@ -199,3 +199,10 @@ def test_cqr2_first_order_second_pass_matches_full(P):
     Ug = c.get_state(0).cpu().numpy()
     assert np.abs(Ug.conj().T @ Ug - np.eye(N)).max() < 1e-12
     assert np.abs(c.correlation(0).cpu().numpy() - gaussian.correlation(gaussian.orthonormalize(U))).max() < 1e-9
+
+
+def test_projective_blocked_sampler_many_panels(P):
+    """gamma dt = 0.5 at L = 400: ~200 clicks per step, i.e. 4 panels of the blocked sampler
+    (in-panel sequential decisions + GEMM trailing updates) against the oracle's Eq. (A1)/(A2)."""
+    _, _, clicks = lockstep(P, 400, 1, "projective", [10.0, 6.0], 12, 3, [np.arange(200)], seed=9)
+    assert clicks > 12 * 250
