@@ -206,3 +206,24 @@ def test_projective_blocked_sampler_many_panels(P):
     (in-panel sequential decisions + GEMM trailing updates) against the oracle's Eq. (A1)/(A2)."""
     _, _, clicks = lockstep(P, 400, 1, "projective", [10.0, 6.0], 12, 3, [np.arange(200)], seed=9)
     assert clicks > 12 * 250
+
+
+def test_trajectory_parallel_ensemble_matches_oracle_average(P):
+    """a5: ensemble statistics of a gamma sweep (ids folded with gamma), run in batches with
+    traj_base offsets, equal the oracle's per-trajectory values averaged the same way."""
+    from paper_2508_18468_b200.ensemble import run_ensemble
+    w = workloads.Workload("mini", 32, 1, "projective", (0.5, 3.0), n_traj_per_gamma=3, steps=30,
+                           sample_every=10, regions={"half": np.arange(16)})
+    res = run_ensemble(w, 30, 10, {"half": ("entropy", np.arange(16))}, max_batch=4)
+    K = lattice.propagator_lattice(32, 1, 1.0, 0.05)
+    vals = np.zeros((w.n_traj, 4))
+    for tau in range(w.n_traj):
+        o = OracleTrajectory(32, 1, "projective", w.gamma_of(tau), 0.05, seed=0, traj=tau, K=K)
+        for k in range(4):
+            vals[tau, k] = o.entropy(np.arange(16))
+            if k < 3:
+                o.step(10)
+    for g in range(2):
+        x = vals[g * 3:(g + 1) * 3]
+        assert np.all(res.count["half"][g] == 3)
+        assert np.abs(res.mean["half"][g] - x.mean(axis=0)).max() < 1e-8
