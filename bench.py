@@ -45,7 +45,7 @@ def parse():
     p.add_argument("--traj-per-gpu", type=int, default=0, help="0: the config's natural batch (1 for c3/c5)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--cpu-budget", type=float, default=150.0, help="seconds of oracle work (reference arm)")
+    p.add_argument("--cpu-budget", type=float, default=120.0, help="seconds of oracle work (reference arm)")
     return p.parse_args()
 
 
