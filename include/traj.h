@@ -49,7 +49,7 @@ typedef enum {
   TRAJ_ENUMERIC = 3,  /* Cholesky breakdown / spectrum outside [-1e-8, 1+1e-8]; the
                          trajectory is marked failed and excluded (never reseeded)        */
   TRAJ_ECUDA = 4,     /* CUDA / cuSOLVER error, or no device                              */
-  TRAJ_ENCCL = 5,     /* reserved: NCCL error (row sharding, not in this build)           */
+  TRAJ_ENCCL = 5,     /* NCCL error (row-sharded mode)                                     */
   TRAJ_EDOMAIN = 6    /* overlapping regions, site index outside the lattice              */
 } traj_status;
 
@@ -71,9 +71,16 @@ typedef struct {
   int64_t traj_base;        /* global id of the first one (Philox counter word 2)              */
   const double* gamma;      /* host[n_traj]: per-site monitoring rate, gamma >= 0 (Q11);
                                projective needs gamma*dt <= 1 (Q10)                            */
-  int32_t shard_rank;       /* row sharding is not built yet: must be 0                        */
-  int32_t shard_size;       /* must be 1                                                       */
-  const void* nccl_id;      /* must be NULL in this build                                       */
+  /* Row sharding of K and U, n_traj must be 1 and L % shard_size == 0.
+   * shard_size = 1, nccl_id = NULL: no sharding.
+   * nccl_id != NULL: this handle is rank shard_rank of shard_size processes (one per GPU);
+   *   nccl_id is a 128-byte ncclUniqueId (traj_nccl_unique_id on rank 0, broadcast by the
+   *   caller, e.g. over torch.distributed).  Rank r owns rows [r L/P, (r+1) L/P).
+   * nccl_id = NULL, shard_size = P > 1, shard_rank = 0: single-GPU emulation -- the handle
+   *   holds all P shards and performs the collectives as device copies / sums.          */
+  int32_t shard_rank;
+  int32_t shard_size;
+  const void* nccl_id;
   void* stream;             /* cudaStream_t the handle runs on (e.g. torch's current stream)   */
   void* workspace;          /* device memory, >= traj_workspace_bytes, 256-byte aligned        */
   size_t workspace_bytes;
@@ -109,7 +116,8 @@ int traj_entropy(traj_handle h, const int64_t* A, int64_t nA, double* S_out);
 int traj_mutual_info(traj_handle h, const int64_t* A, int64_t nA,
                      const int64_t* B, int64_t nB, double* I_out);
 
-/* n_out = device[n_traj][L] doubles: n_i = sum_k |U_ik|^2 of the current state. */
+/* n_out = device[n_traj][L] doubles: n_i = sum_k |U_ik|^2 of the current state
+ * (row-sharded: the rows this handle holds, see traj_shard_info). */
 int traj_occupations(traj_handle h, double* n_out);
 
 /* Rows [row0, row0+nrows) of C = U U^dag for trajectory traj into C_out =
@@ -117,8 +125,9 @@ int traj_occupations(traj_handle h, double* n_out);
 int traj_correlation_rows(traj_handle h, int64_t traj, int64_t row0, int64_t nrows, void* C_out);
 
 /* Copy U (L x N, complex128 row-major, ld = N) of trajectory traj out of / into the
- * handle.  The pointer may be host or device (UVA copy).  traj_set_state does not
- * orthonormalise: call traj_orthonormalize (or traj_step) afterwards. */
+ * handle (row-sharded: the rows this handle holds).  The pointer may be host or device
+ * (UVA copy).  traj_set_state does not orthonormalise: call traj_orthonormalize (or
+ * traj_step) afterwards. */
 int traj_get_state(traj_handle h, int64_t traj, void* U_out);
 int traj_set_state(traj_handle h, int64_t traj, const void* U_in);
 
@@ -151,6 +160,13 @@ enum { TRAJ_PH_PROPAGATE = 0,  /* U <- K U                                   */
        TRAJ_NPHASES = 6 };
 int traj_profile(traj_handle h, int enable);
 int traj_phase_times(traj_handle h, double* ms, int64_t* launches);
+
+/* Row sharding: *shard_size = P, *local_shards = shards held by this handle (1, or P in
+ * the single-GPU emulation), rows [*row0, *row0 + *rows) of U / n are held here. */
+int traj_shard_info(traj_handle h, int32_t* shard_size, int32_t* local_shards, int64_t* row0, int64_t* rows);
+
+/* out128 <- a fresh ncclUniqueId (128 bytes) for traj_config.nccl_id. */
+int traj_nccl_unique_id(void* out128);
 
 /* Kernels launched by the library in this process so far (every launch site counts). */
 long long traj_kernel_launches(void);

@@ -13,5 +13,6 @@ from .binding import (  # noqa: F401
     load_library,
     traj_chol_inverse,
     traj_kernel_launches,
+    traj_nccl_unique_id,
     traj_zgemm,
 )

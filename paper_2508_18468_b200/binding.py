@@ -80,6 +80,9 @@ _SIGS = {
     "traj_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "traj_zgemm": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _I64, _I64, _I64, _D, _D, _P, _I64, _I64, _P, _I64,
                                   _I64, _D, _P, _I64, _I64, _I64, ctypes.c_int]),
+    "traj_shard_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                       ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
+    "traj_nccl_unique_id": (ctypes.c_int, [_P]),
     "traj_chol_scratch_bytes": (ctypes.c_size_t, [_I64, _I64]),
     "traj_chol_inverse": (ctypes.c_int, [_P, _I64, _P, _I64, _I64, _P, _I64, _I64, _I64, _P, _P]),
 }
@@ -118,6 +121,13 @@ def traj_kernel_launches() -> int:
 
 def _ptr(t) -> int:
     return int(t.data_ptr())
+
+
+def traj_nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (rank 0 creates it; the caller broadcasts it)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().traj_nccl_unique_id(buf))
+    return buf.raw
 
 
 def traj_zgemm(opA, opB, A, B, C, *, alpha=1.0, beta=0.0, flags=0, M=None, N=None, K=None, stream=None):
@@ -168,7 +178,8 @@ class Trajectories:
     global id of the first trajectory (reading Q9)."""
 
     def __init__(self, Lx: int, Ly: int = 1, protocol: str = "projective", gammas=(0.5,), dt: float = 0.05,
-                 J: float = 1.0, seed: int = 0, traj_base: int = 0, device=None, stream=None):
+                 J: float = 1.0, seed: int = 0, traj_base: int = 0, device=None, stream=None,
+                 shard_size: int = 1, shard_rank: int = 0, nccl_id: bytes | None = None):
         import torch
         self._torch = torch
         lib_ = lib()
@@ -190,8 +201,9 @@ class Trajectories:
         cfg.n_traj = self.n_traj
         cfg.traj_base = int(traj_base)
         cfg.gamma = self.gammas.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
-        cfg.shard_rank, cfg.shard_size = 0, 1
-        cfg.nccl_id = None
+        cfg.shard_rank, cfg.shard_size = int(shard_rank), int(shard_size)
+        self._nccl_id = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        cfg.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p) if nccl_id is not None else None
         cfg.stream = self.stream.cuda_stream
         nbytes = ctypes.c_size_t(0)
         _check(lib_.traj_workspace_bytes(ctypes.byref(cfg), ctypes.byref(nbytes)))
@@ -202,6 +214,9 @@ class Trajectories:
         h = ctypes.c_void_p()
         _check(lib_.traj_init(ctypes.byref(cfg), ctypes.byref(h)))
         self._h = h
+        P, nloc, r0, rows = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
+        _check(lib_.traj_shard_info(h, ctypes.byref(P), ctypes.byref(nloc), ctypes.byref(r0), ctypes.byref(rows)))
+        self.shard_size, self.local_shards, self.row0, self.rows = P.value, nloc.value, r0.value, rows.value
 
     # -- lifecycle
     def close(self):
@@ -252,7 +267,8 @@ class Trajectories:
         return out
 
     def occupations(self):
-        n = self._torch.empty((self.n_traj, self.L), dtype=self._torch.float64, device=self.device)
+        """n_i of the rows this handle holds: [n_traj][rows] (rows = L unless row-sharded)."""
+        n = self._torch.empty((self.n_traj, self.rows), dtype=self._torch.float64, device=self.device)
         self._c(lib().traj_occupations(self._h, _ptr(n)))
         return n
 
@@ -266,13 +282,13 @@ class Trajectories:
 
     def get_state(self, traj: int = 0, out=None):
         if out is None:
-            out = self._torch.empty((self.L, self.N), dtype=self._torch.complex128, device=self.device)
+            out = self._torch.empty((self.rows, self.N), dtype=self._torch.complex128, device=self.device)
         self._c(lib().traj_get_state(self._h, traj, _ptr(out)))
         return out
 
     def set_state(self, traj: int, U):
         U = U.contiguous()
-        assert U.dtype == self._torch.complex128 and tuple(U.shape) == (self.L, self.N)
+        assert U.dtype == self._torch.complex128 and tuple(U.shape) == (self.rows, self.N)
         self._c(lib().traj_set_state(self._h, traj, _ptr(U)))
 
     def failed(self, traj: int) -> bool:

@@ -9,11 +9,21 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libtraj.so")
-SOURCES = ["zgemm.cu", "cholinv.cu", "monitor.cu", "traj_api.cu"]
+SOURCES = ["zgemm.cu", "cholinv.cu", "monitor.cu", "shard.cu", "traj_api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_dir():
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    base = list(spec.submodule_search_locations)[0] if spec else "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia"
+    return os.path.join(base, "nccl")
+
+
+NCCL = _nccl_dir()
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
-         "-I" + os.path.join(ROOT, "include")]
+         "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(NCCL, "include")]
 
 
 def _deps():
@@ -46,7 +56,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(r.stderr)
         objs.append(obj)
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp", *objs,
-           "-L/usr/local/cuda/lib64", "-lcusolver", "-lcudart", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
+           "-L/usr/local/cuda/lib64", "-lcusolver", "-lcudart", "-Xlinker", "-rpath=/usr/local/cuda/lib64",
+           "-L" + os.path.join(NCCL, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(NCCL, "lib")]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -48,7 +48,7 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 template <int BS, int VPT>
 __global__ void __launch_bounds__(BS) row_monitor_kernel(cplx* U, long long ld, long long sU, int L, int N, int mode,
                                                          long long step, long long traj_base, uint32_t k0, uint32_t k1,
-                                                         const double* gamma, double dt, double* n_out) {
+                                                         const double* gamma, double dt, double* n_out, int site0) {
   __shared__ double red[32];
   __shared__ double fac;
   const int i = blockIdx.x, t = blockIdx.y;
@@ -72,7 +72,8 @@ __global__ void __launch_bounds__(BS) row_monitor_kernel(cplx* U, long long ld, 
   if (threadIdx.x == 0) {
     if (n_out) n_out[(long long)t * L + i] = n;
     if (mode == 1) {
-      const u32x4 x = philox4x32_10(u32x4{(uint32_t)i, (uint32_t)step, (uint32_t)(traj_base + t), 0u}, k0, k1);
+      const u32x4 x =
+          philox4x32_10(u32x4{(uint32_t)(site0 + i), (uint32_t)step, (uint32_t)(traj_base + t), 0u}, k0, k1);
       const double u0 = u53(x.x, x.y), u1 = u53(x.z, x.w);
       const double z = sqrt(-2.0 * log(1.0 - u0)) * cos(2.0 * M_PI * u1);
       const double gdt = gamma[t] * dt;
@@ -97,18 +98,19 @@ __global__ void __launch_bounds__(BS) row_monitor_kernel(cplx* U, long long ld, 
 }
 
 __global__ void click_draw_kernel(int L, long long step, long long traj_base, uint32_t k0, uint32_t k1,
-                                  const double* gamma, double dt, int32_t* flags) {
+                                  const double* gamma, double dt, int32_t* flags, int site0) {
   const int t = blockIdx.y;
   const double p = gamma[t] * dt;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x) {
-    const u32x4 x = philox4x32_10(u32x4{(uint32_t)i, (uint32_t)step, (uint32_t)(traj_base + t), 0u}, k0, k1);
+    const u32x4 x =
+        philox4x32_10(u32x4{(uint32_t)(site0 + i), (uint32_t)step, (uint32_t)(traj_base + t), 0u}, k0, k1);
     flags[(long long)t * L + i] = u53(x.x, x.y) < p ? 1 : 0;
   }
 }
 
 // one CTA (1024 threads) per trajectory: ascending list of flagged sites
 __global__ void __launch_bounds__(1024) compact_kernel(const int32_t* flags, int L, int32_t* list, int cap,
-                                                       int32_t* count) {
+                                                       int32_t* count, int site0) {
   __shared__ int wsum[32];
   __shared__ int base;
   const int t = blockIdx.x;
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(1024) compact_kernel(const int32_t* flags, int
     int off = 0;
     for (int q = 0; q < w; ++q) off += wsum[q];
     const int pos = base + off + before;
-    if (fl && pos < cap) out[pos] = i;
+    if (fl && pos < cap) out[pos] = site0 + i;
     __syncthreads();
     if (threadIdx.x == 0) {
       int tot = 0;
@@ -142,12 +144,12 @@ __global__ void __launch_bounds__(1024) compact_kernel(const int32_t* flags, int
 // dst[t][r][:] = src[t][idx[t][r]][:] for r < count[t]
 __global__ void gather_rows_kernel(const cplx* src, long long lds, long long sS, const int32_t* idx, long long sIdx,
                                    const int32_t* count, int fixed_count, cplx* dst, long long ldd, long long sD,
-                                   int ncols) {
+                                   int ncols, int row_offset) {
   const int t = blockIdx.z;
   const int r = blockIdx.y;
   const int cnt = count ? count[t] : fixed_count;
   if (r >= cnt) return;
-  const long long srow = idx[t * sIdx + r];
+  const long long srow = idx[t * sIdx + r] - row_offset;
   const cplx* s = src + t * sS + srow * lds;
   cplx* d = dst + t * sD + (long long)r * ldd;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ncols; k += gridDim.x * blockDim.x) d[k] = s[k];
@@ -278,15 +280,20 @@ __global__ void gather_sub_kernel(const cplx* D0, long long ld0, const int32_t* 
 }
 
 // T[S1[c]][c] -= 1
-__global__ void sub_identity_kernel(cplx* T, long long ld, const int32_t* S1, int k) {
+__global__ void sub_identity_kernel(cplx* T, long long ld, const int32_t* S1, int k, int row0, int nrows) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < k) T[(long long)S1[c] * ld + c].x -= 1.0;
+  if (c >= k) return;
+  const int r = S1[c] - row0;
+  if (r >= 0 && r < nrows) T[(long long)r * ld + c].x -= 1.0;
 }
 
-__global__ void zero_rows_kernel(cplx* U, long long ld, const int32_t* rows, int nrows, int ncols) {
+__global__ void zero_rows_kernel(cplx* U, long long ld, const int32_t* rows, int nrows, int ncols, int row0,
+                                 int nlocal) {
   const int r = blockIdx.y;
   if (r >= nrows) return;
-  cplx* p = U + (long long)rows[r] * ld;
+  const int lr = rows[r] - row0;
+  if (lr < 0 || lr >= nlocal) return;
+  cplx* p = U + (long long)lr * ld;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ncols; k += gridDim.x * blockDim.x)
     p[k] = make_double2(0.0, 0.0);
 }
@@ -312,22 +319,29 @@ __global__ void __launch_bounds__(256) entropy_kernel(const double* lam, int n, 
   }
 }
 
-__global__ void build_k_kernel(cplx* K, long long ld, int Lx, int Ly, const cplx* kx, const cplx* ky) {
+// rows [row0, row0 + nrows) of K = K_y (x) K_x (row-major sites), into K[0..nrows)
+__global__ void build_k_kernel(cplx* K, long long ld, int Lx, int Ly, const cplx* kx, const cplx* ky, long long row0,
+                               long long nrows) {
   const long long L = (long long)Lx * Ly;
-  const long long total = L * L;
+  const long long total = nrows * L;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
-    const long long i = idx / L, j = idx % L;
+    const long long r = idx / L, j = idx % L;
+    const long long i = row0 + r;
     const int ix = (int)(i % Lx), iy = (int)(i / Lx), jx = (int)(j % Lx), jy = (int)(j / Lx);
     const int dx = ((jx - ix) % Lx + Lx) % Lx, dy = ((jy - iy) % Ly + Ly) % Ly;
-    K[i * ld + j] = cmul(kx[dx], ky[dy]);
+    K[r * ld + j] = cmul(kx[dx], ky[dy]);
   }
 }
 
-__global__ void init_state_kernel(cplx* U, long long ld, long long sU, const int32_t* sites, int N) {
+// U[t][site_k - row0][k] = 1 for the occupied sites inside [row0, row0 + nrows)
+__global__ void init_state_kernel(cplx* U, long long ld, long long sU, const int32_t* sites, int N, int row0,
+                                  int nrows) {
   const int t = blockIdx.y;
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < N) U[t * sU + (long long)sites[k] * ld + k] = make_double2(1.0, 0.0);
+  if (k >= N) return;
+  const int r = sites[k] - row0;
+  if (r >= 0 && r < nrows) U[t * sU + (long long)r * ld + k] = make_double2(1.0, 0.0);
 }
 
 // max over the upper triangle of |G_ij - delta_ij| (component-wise), per batch entry;
@@ -388,18 +402,20 @@ cudaError_t last(std::string* err, const char* what) {
 template <int BS, int VPT>
 void launch_row(cudaStream_t st, dim3 grid, cplx* U, long long ld, long long sU, int L, int N, int mode,
                 long long step, long long traj_base, uint32_t k0, uint32_t k1, const double* gamma, double dt,
-                double* n_out) {
-  row_monitor_kernel<BS, VPT><<<grid, BS, 0, st>>>(U, ld, sU, L, N, mode, step, traj_base, k0, k1, gamma, dt, n_out);
+                double* n_out, int site0) {
+  row_monitor_kernel<BS, VPT><<<grid, BS, 0, st>>>(U, ld, sU, L, N, mode, step, traj_base, k0, k1, gamma, dt, n_out,
+                                                   site0);
 }
 
 }  // namespace
 
 int row_monitor(cudaStream_t st, cplx* U, long long ld, long long sU, int L, int N, int T, int mode, long long step,
                 long long traj_base, uint64_t seed, const double* gamma_dev, double dt, double* n_out,
-                std::string* err) {
+                std::string* err, int site0) {
   dim3 grid(L, T);
   const uint32_t k0 = (uint32_t)(seed & 0xffffffffu), k1 = (uint32_t)(seed >> 32);
-#define ROW(BS, VPT) launch_row<BS, VPT>(st, grid, U, ld, sU, L, N, mode, step, traj_base, k0, k1, gamma_dev, dt, n_out)
+#define ROW(BS, VPT) \
+  launch_row<BS, VPT>(st, grid, U, ld, sU, L, N, mode, step, traj_base, k0, k1, gamma_dev, dt, n_out, site0)
   if (N <= 32) ROW(32, 1);
   else if (N <= 64) ROW(32, 2);
   else if (N <= 128) ROW(32, 4);
@@ -417,27 +433,28 @@ int row_monitor(cudaStream_t st, cplx* U, long long ld, long long sU, int L, int
 }
 
 int click_draw(cudaStream_t st, int L, int T, long long step, long long traj_base, uint64_t seed,
-               const double* gamma_dev, double dt, int32_t* flags, std::string* err) {
+               const double* gamma_dev, double dt, int32_t* flags, std::string* err, int site0) {
   dim3 grid((unsigned)std::min<long long>(ceil_div(L, 256), 4096), T);
   click_draw_kernel<<<grid, 256, 0, st>>>(L, step, traj_base, (uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32),
-                                          gamma_dev, dt, flags);
+                                          gamma_dev, dt, flags, site0);
   count_launch();
   return last(err, "click_draw") == cudaSuccess ? 0 : 4;
 }
 
 int compact(cudaStream_t st, const int32_t* flags, int L, int T, int32_t* list, int cap, int32_t* count,
-            std::string* err) {
-  compact_kernel<<<T, 1024, 0, st>>>(flags, L, list, cap, count);
+            std::string* err, int site0) {
+  compact_kernel<<<T, 1024, 0, st>>>(flags, L, list, cap, count, site0);
   count_launch();
   return last(err, "compact") == cudaSuccess ? 0 : 4;
 }
 
 int gather_rows(cudaStream_t st, const cplx* src, long long lds, long long sS, const int32_t* idx, long long sIdx,
                 const int32_t* count_dev, int rows, int T, cplx* dst, long long ldd, long long sD, int ncols,
-                std::string* err) {
+                std::string* err, int row_offset) {
   if (rows <= 0 || T <= 0) return 0;
   dim3 grid((unsigned)std::min<long long>(ceil_div(ncols, 256), 64), rows, T);
-  gather_rows_kernel<<<grid, 256, 0, st>>>(src, lds, sS, idx, sIdx, count_dev, rows, dst, ldd, sD, ncols);
+  gather_rows_kernel<<<grid, 256, 0, st>>>(src, lds, sS, idx, sIdx, count_dev, rows, dst, ldd, sD, ncols,
+                                           row_offset);
   count_launch();
   return last(err, "gather_rows") == cudaSuccess ? 0 : 4;
 }
@@ -447,7 +464,9 @@ int sample_outcomes(cudaStream_t st, const cplx* D0, cplx* Dw, long long ldd, lo
                     int32_t* occ, cplx* Linv, cplx* DLinv, cplx* Ybuf, cplx* Zbuf, long long ldy, int32_t* pos1,
                     int32_t* S1, int32_t* S0, int32_t* k1, int32_t* k0, std::string* err) {
   const uint32_t key0 = (uint32_t)(seed & 0xffffffffu), key1 = (uint32_t)(seed >> 32);
-  if (cudaMemcpyAsync(Dw, D0, (size_t)T * sD * 16, cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
+  // work copy of C_SS: every batch entry's leading maxc rows (sD = 0 when unbatched)
+  const size_t bytes = (size_t)((T - 1) * sD + (long long)maxc * ldd) * 16;
+  if (cudaMemcpyAsync(Dw, D0, bytes, cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
     if (err) *err = "sample: copy";
     return 4;
   }
@@ -493,19 +512,33 @@ int gather_sub(cudaStream_t st, const cplx* D0, long long ld0, const int32_t* po
   return last(err, "gather_sub") == cudaSuccess ? 0 : 4;
 }
 
-int sub_identity(cudaStream_t st, cplx* T, long long ld, const int32_t* S1, int k, std::string* err) {
+int sub_identity(cudaStream_t st, cplx* T, long long ld, const int32_t* S1, int k, std::string* err, int row0,
+                 int nrows) {
   if (k <= 0) return 0;
-  sub_identity_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(T, ld, S1, k);
+  sub_identity_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(T, ld, S1, k, row0, nrows);
   count_launch();
   return last(err, "sub_identity") == cudaSuccess ? 0 : 4;
 }
 
-int zero_rows(cudaStream_t st, cplx* U, long long ld, const int32_t* rows, int nrows, int ncols, std::string* err) {
+int zero_rows(cudaStream_t st, cplx* U, long long ld, const int32_t* rows, int nrows, int ncols, std::string* err,
+              int row0, int nlocal) {
   if (nrows <= 0) return 0;
   dim3 grid((unsigned)std::min<long long>(ceil_div(ncols, 256), 64), nrows);
-  zero_rows_kernel<<<grid, 256, 0, st>>>(U, ld, rows, nrows, ncols);
+  zero_rows_kernel<<<grid, 256, 0, st>>>(U, ld, rows, nrows, ncols, row0, nlocal);
   count_launch();
   return last(err, "zero_rows") == cudaSuccess ? 0 : 4;
+}
+
+// out += in (n doubles): the single-GPU emulation of an all-reduce
+__global__ void add_kernel(double* out, const double* in, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] += in[i];
+}
+
+int add_inplace(cudaStream_t st, double* out, const double* in, long long n, std::string* err) {
+  add_kernel<<<(unsigned)std::min<long long>(ceil_div(n, 256), 148 * 32), 256, 0, st>>>(out, in, n);
+  count_launch();
+  return last(err, "add") == cudaSuccess ? 0 : 4;
 }
 
 int entropy_reduce(cudaStream_t st, const double* lam, int n, double* S_out, int32_t* bad, std::string* err) {
@@ -514,9 +547,12 @@ int entropy_reduce(cudaStream_t st, const double* lam, int n, double* S_out, int
   return last(err, "entropy") == cudaSuccess ? 0 : 4;
 }
 
-int build_k(cudaStream_t st, cplx* K, long long ld, int Lx, int Ly, const cplx* kx, const cplx* ky, std::string* err) {
+int build_k(cudaStream_t st, cplx* K, long long ld, int Lx, int Ly, const cplx* kx, const cplx* ky, std::string* err,
+            long long row0, long long nrows) {
   const long long L = (long long)Lx * Ly;
-  build_k_kernel<<<(unsigned)std::min<long long>(ceil_div(L * L, 256), 148 * 64), 256, 0, st>>>(K, ld, Lx, Ly, kx, ky);
+  if (nrows < 0) nrows = L;
+  build_k_kernel<<<(unsigned)std::min<long long>(ceil_div(nrows * L, 256), 148 * 64), 256, 0, st>>>(K, ld, Lx, Ly, kx,
+                                                                                                   ky, row0, nrows);
   count_launch();
   return last(err, "build_k") == cudaSuccess ? 0 : 4;
 }
@@ -539,9 +575,9 @@ int first_order_inverse(cudaStream_t st, const cplx* G, long long ldg, long long
 }
 
 int init_state(cudaStream_t st, cplx* U, long long ld, long long sU, const int32_t* sites, int N, int T,
-               std::string* err) {
+               std::string* err, int row0, int nrows) {
   dim3 grid((unsigned)ceil_div(N, 256), T);
-  init_state_kernel<<<grid, 256, 0, st>>>(U, ld, sU, sites, N);
+  init_state_kernel<<<grid, 256, 0, st>>>(U, ld, sU, sites, N, row0, nrows);
   count_launch();
   return last(err, "init_state") == cudaSuccess ? 0 : 4;
 }

@@ -8,14 +8,17 @@ namespace traj {
 // mode 0: n_out[t][i] = sum_k |U_ik|^2; mode 1: also U_i. *= exp(a_i) (homodyne, Eq. A3).
 int row_monitor(cudaStream_t st, cplx* U, long long ld, long long sU, int L, int N, int T, int mode, long long step,
                 long long traj_base, uint64_t seed, const double* gamma_dev, double dt, double* n_out,
-                std::string* err);
+                std::string* err, int site0 = 0);
+// flags[t][i] = (u0 of site site0+i < gamma_t dt)
 int click_draw(cudaStream_t st, int L, int T, long long step, long long traj_base, uint64_t seed,
-               const double* gamma_dev, double dt, int32_t* flags, std::string* err);
+               const double* gamma_dev, double dt, int32_t* flags, std::string* err, int site0 = 0);
+// list[t] = site0 + (ascending flagged indices), count[t]
 int compact(cudaStream_t st, const int32_t* flags, int L, int T, int32_t* list, int cap, int32_t* count,
-            std::string* err);
+            std::string* err, int site0 = 0);
+// dst[t][r] = src[t][idx[t][r] - row_offset] for r < count[t] (or rows if count_dev is null)
 int gather_rows(cudaStream_t st, const cplx* src, long long lds, long long sS, const int32_t* idx, long long sIdx,
                 const int32_t* count_dev, int rows, int T, cplx* dst, long long ldd, long long sD, int ncols,
-                std::string* err);
+                std::string* err, int row_offset = 0);
 // Blocked conditional Born sampling of every trajectory's click list on C_SS (D0, kept);
 // Dw: work copy; Linv/DLinv: [T][64][64]; Ybuf/Zbuf: [T][64][ldy] with ldy >= maxc.
 int sample_outcomes(cudaStream_t st, const cplx* D0, cplx* Dw, long long ldd, long long sD, const int32_t* S, int cap,
@@ -24,10 +27,18 @@ int sample_outcomes(cudaStream_t st, const cplx* D0, cplx* Dw, long long ldd, lo
                     int32_t* S1, int32_t* S0, int32_t* k1, int32_t* k0, std::string* err);
 int gather_sub(cudaStream_t st, const cplx* D0, long long ld0, const int32_t* pos, int k, cplx* D11, long long ld1,
                std::string* err);
-int sub_identity(cudaStream_t st, cplx* T, long long ld, const int32_t* S1, int k, std::string* err);
-int zero_rows(cudaStream_t st, cplx* U, long long ld, const int32_t* rows, int nrows, int ncols, std::string* err);
+// T[S1[c] - row0][c] -= 1 for the S1 entries inside [row0, row0 + nrows)
+int sub_identity(cudaStream_t st, cplx* T, long long ld, const int32_t* S1, int k, std::string* err, int row0 = 0,
+                 int nrows = 1 << 30);
+// zero the rows (global ids) inside [row0, row0 + nlocal) of the local block U
+int zero_rows(cudaStream_t st, cplx* U, long long ld, const int32_t* rows, int nrows, int ncols, std::string* err,
+              int row0 = 0, int nlocal = 1 << 30);
 int entropy_reduce(cudaStream_t st, const double* lam, int n, double* S_out, int32_t* bad, std::string* err);
-int build_k(cudaStream_t st, cplx* K, long long ld, int Lx, int Ly, const cplx* kx, const cplx* ky, std::string* err);
+// rows [row0, row0+nrows) of K (nrows < 0: all L rows)
+int build_k(cudaStream_t st, cplx* K, long long ld, int Lx, int Ly, const cplx* kx, const cplx* ky, std::string* err,
+            long long row0 = 0, long long nrows = -1);
+// out[i] += in[i]
+int add_inplace(cudaStream_t st, double* out, const double* in, long long n, std::string* err);
 // out[t] = max_{i<=j} |G_ij - delta_ij| (as the bit pattern of a non-negative double)
 int gram_deviation(cudaStream_t st, const cplx* G, long long ld, long long sG, int n, int T, unsigned long long* out,
                    std::string* err);
@@ -35,6 +46,6 @@ int gram_deviation(cudaStream_t st, const cplx* G, long long ld, long long sG, i
 int first_order_inverse(cudaStream_t st, const cplx* G, long long ldg, long long sG, cplx* X, long long ldx,
                         long long sX, int n, int T, std::string* err);
 int init_state(cudaStream_t st, cplx* U, long long ld, long long sU, const int32_t* sites, int N, int T,
-               std::string* err);
+               std::string* err, int row0 = 0, int nrows = 1 << 30);
 
 }  // namespace traj

@@ -1,0 +1,535 @@
+// Row-sharded trajectory step (north star: "K and U are row-sharded,
+// with an NCCL allgather of U over NVLink each step and an allreduce of the Gram matrix").
+//
+// Shard g owns rows [g Lp, (g+1) Lp) of K and U (Lp = L / P).  One step:
+//   allgather U rows -> U_full;  U_g <- K_g U_full                           (a1)
+//   homodyne: local rows, Philox at global site ids                          (a2)
+//   projective: local clicks -> allgather (counts, sites, U_S rows) -> the replicated,
+//     deterministic C_SS / sampling / W on every shard -> local rank-k update  (a2)
+//   CholeskyQR2: G_g = U_g^dag U_g -> allreduce -> replicated factor -> U_g X  (a3)
+// Replicated decisions are bitwise identical on every shard: the all-reduced / gathered
+// inputs are identical and the kernels are deterministic.
+#include <cusolverDn.h>
+#include <math.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <complex>
+
+#include "cholinv.h"
+#include "monitor.h"
+#include "shard.h"
+#include "zgemm.h"
+
+namespace traj {
+
+namespace {
+
+struct Lay {
+  size_t off = 0;
+  char* base = nullptr;
+  template <typename P>
+  void take(P*& p, size_t bytes) {
+    off = (off + 255) & ~size_t(255);
+    p = base ? reinterpret_cast<P*>(base + off) : nullptr;
+    off += bytes;
+  }
+};
+
+std::string cuerr(const char* what, cudaError_t e) { return std::string(what) + ": " + cudaGetErrorString(e); }
+
+#define SCK(x)                            \
+  do {                                    \
+    cudaError_t e_ = (x);                 \
+    if (e_ != cudaSuccess) {              \
+      if (err) *err = cuerr(#x, e_);      \
+      return TRAJ_ECUDA;                  \
+    }                                     \
+  } while (0)
+#define STRY(x)             \
+  do {                      \
+    int s_ = (x);           \
+    if (s_) return s_;      \
+  } while (0)
+
+int capacity(long long n, double p) {
+  const double m = n * p, sd = sqrt(n * p * (1 - p));
+  return (int)std::min<long long>(n, (long long)ceil(m + 12 * sd + 64));
+}
+
+}  // namespace
+
+int ShardComm::allgather(cudaStream_t st, void* const* send, void* recv, size_t bytes, std::string* err) {
+  if (comm) {
+    ncclResult_t r = ncclAllGather(send[0], recv, bytes, ncclUint8, comm, st);
+    if (r != ncclSuccess) {
+      if (err) *err = std::string("ncclAllGather: ") + ncclGetErrorString(r);
+      return TRAJ_ENCCL;
+    }
+    return 0;
+  }
+  for (int s = 0; s < P_local; ++s) {
+    char* dst = reinterpret_cast<char*>(recv) + (size_t)(rank0 + s) * bytes;
+    if (dst == send[s]) continue;
+    cudaError_t e = cudaMemcpyAsync(dst, send[s], bytes, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) {
+      if (err) *err = cuerr("allgather (emulated)", e);
+      return TRAJ_ECUDA;
+    }
+  }
+  return 0;
+}
+
+int ShardComm::allreduce(cudaStream_t st, double* const* part, double* out, size_t n, std::string* err) {
+  if (comm) {
+    ncclResult_t r = ncclAllReduce(part[0], out, n, ncclFloat64, ncclSum, comm, st);
+    if (r != ncclSuccess) {
+      if (err) *err = std::string("ncclAllReduce: ") + ncclGetErrorString(r);
+      return TRAJ_ENCCL;
+    }
+    return 0;
+  }
+  if (out != part[0]) {
+    cudaError_t e = cudaMemcpyAsync(out, part[0], n * 8, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) {
+      if (err) *err = cuerr("allreduce (emulated)", e);
+      return TRAJ_ECUDA;
+    }
+  }
+  for (int s = 1; s < P_local; ++s) STRY(add_inplace(st, out, part[s], (long long)n, err));
+  return 0;
+}
+
+int nccl_unique_id(void* out128, std::string* err) {
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) {
+    if (err) *err = std::string("ncclGetUniqueId: ") + ncclGetErrorString(r);
+    return TRAJ_ENCCL;
+  }
+  memcpy(out128, &id, sizeof(id));
+  return 0;
+}
+
+int shard_validate(const traj_config* c, std::string* why) {
+  const long long L = c->Lx * c->Ly;
+  if (c->shard_size < 1 || c->shard_size > 1024) {
+    *why = "shard_size must be in [1, 1024]";
+    return TRAJ_ECONFIG;
+  }
+  if (L % c->shard_size) {
+    *why = "L must be divisible by shard_size";
+    return TRAJ_ECONFIG;
+  }
+  if (c->n_traj != 1) {
+    *why = "row sharding holds a single trajectory (n_traj = 1)";
+    return TRAJ_ECONFIG;
+  }
+  if (c->nccl_id) {
+    if (c->shard_rank < 0 || c->shard_rank >= c->shard_size) {
+      *why = "shard_rank outside [0, shard_size)";
+      return TRAJ_ECONFIG;
+    }
+  } else if (c->shard_rank != 0) {
+    *why = "single-GPU shard emulation (nccl_id = NULL) needs shard_rank = 0";
+    return TRAJ_ECONFIG;
+  }
+  return 0;
+}
+
+size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork) {
+  Lay lay;
+  lay.base = base;
+  const long long L = c->Lx * c->Ly, N = c->N;
+  const int P = c->shard_size;
+  const bool emulate = c->nccl_id == nullptr;
+  sh->comm.P = P;
+  sh->comm.P_local = emulate ? P : 1;
+  sh->comm.rank0 = emulate ? 0 : c->shard_rank;
+  sh->L = (int)L;
+  sh->N = (int)N;
+  sh->Lx = (int)c->Lx;
+  sh->Ly = (int)c->Ly;
+  sh->P = P;
+  sh->Lp = (int)(L / P);
+  sh->ldN = round_up(N, 8);
+  sh->ldL = round_up(L, 8);
+  const double p = c->protocol == TRAJ_PROJECTIVE ? c->gamma[0] * c->dt : 0.0;
+  sh->capr = c->protocol == TRAJ_PROJECTIVE ? capacity(sh->Lp, p) : 0;
+  sh->cap = sh->capr * P;
+  sh->ldcap = round_up(std::max(sh->cap, 1), 8);
+  sh->lwork = lwork;
+  const long long Lp = sh->Lp, ldN = sh->ldN, ldL = sh->ldL, ldcap = sh->ldcap;
+  const int capr = sh->capr, cap = sh->cap;
+  sh->loc.assign(sh->comm.P_local, ShardLocal());
+  lay.take(sh->Ufull, (size_t)L * ldN * 16);
+  lay.take(sh->G, (size_t)N * ldN * 16);
+  lay.take(sh->X, (size_t)N * ldN * 16);
+  lay.take(sh->chol_scratch, chol_scratch_bytes(N, 1));
+  for (int s = 0; s < sh->comm.P_local; ++s) {
+    ShardLocal& l = sh->loc[s];
+    l.g = sh->comm.rank0 + s;
+    l.row0 = (int)(l.g * Lp);
+    lay.take(l.K, (size_t)Lp * ldL * 16);
+    lay.take(l.U[0], (size_t)Lp * ldN * 16);
+    lay.take(l.U[1], (size_t)Lp * ldN * 16);
+    if (emulate) lay.take(l.Gpart, (size_t)N * ldN * 16);
+    else l.Gpart = sh->G;
+    if (cap > 0) {
+      lay.take(l.flags, (size_t)Lp * 4);
+      lay.take(l.Sloc, (size_t)capr * 4);
+      lay.take(l.cnt, 16);
+      lay.take(l.USloc, (size_t)capr * ldN * 16);
+      lay.take(l.Tm, (size_t)Lp * ldcap * 16);
+    }
+  }
+  lay.take(sh->gamma_dev, 16);
+  lay.take(sh->failed_dev, 16);
+  lay.take(sh->eig_w, (size_t)N * 8);
+  lay.take(sh->eig_work, (size_t)std::max(lwork, 1) * 16);
+  lay.take(sh->eig_info, 16);
+  lay.take(sh->S_dev, 16);
+  lay.take(sh->bad_dev, 16);
+  lay.take(sh->gdev, 16);
+  lay.take(sh->region, (size_t)L * 4);
+  lay.take(sh->kcoef, (size_t)(c->Lx + c->Ly) * 16);
+  lay.take(sh->sites, (size_t)N * 4);
+  if (cap > 0) {
+    lay.take(sh->Srecv, (size_t)cap * 4);
+    lay.take(sh->cntrecv, (size_t)P * 4);
+    lay.take(sh->USrecv, (size_t)cap * ldN * 16);
+    lay.take(sh->S, (size_t)cap * 4);
+    lay.take(sh->count, 16);
+    lay.take(sh->US, (size_t)cap * ldN * 16);
+    lay.take(sh->D0, (size_t)cap * ldcap * 16);
+    lay.take(sh->Dw, (size_t)cap * ldcap * 16);
+    lay.take(sh->Linv, 64 * 64 * 16);
+    lay.take(sh->DLinv, 64 * 64 * 16);
+    lay.take(sh->Ybuf, (size_t)64 * ldcap * 16);
+    lay.take(sh->Zbuf, (size_t)64 * ldcap * 16);
+    lay.take(sh->occ, (size_t)cap * 4);
+    lay.take(sh->pos1, (size_t)cap * 4);
+    lay.take(sh->S1, (size_t)cap * 4);
+    lay.take(sh->S0, (size_t)cap * 4);
+    lay.take(sh->k1, 16);
+    lay.take(sh->k0, 16);
+    lay.take(sh->D11, (size_t)cap * ldcap * 16);
+    lay.take(sh->X11, (size_t)cap * ldcap * 16);
+    lay.take(sh->chol_scratch_small, chol_scratch_bytes(cap, 1));
+    lay.take(sh->W, (size_t)N * ldcap * 16);
+  }
+  return lay.off + 256;
+}
+
+int shard_init(ShardedCtx* sh, const traj_config* c, std::string* err) {
+  sh->protocol = c->protocol;
+  sh->dt = c->dt;
+  sh->J = c->J;
+  sh->gamma = c->gamma[0];
+  sh->seed = c->seed;
+  sh->traj_base = c->traj_base;
+  sh->st = reinterpret_cast<cudaStream_t>(c->stream);
+  if (c->nccl_id) {
+    ncclUniqueId id;
+    memcpy(&id, c->nccl_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&sh->comm.comm, c->shard_size, id, c->shard_rank);
+    if (r != ncclSuccess) {
+      if (err) *err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+      return TRAJ_ENCCL;
+    }
+  }
+  SCK(cudaMallocHost(&sh->h_small, std::max(sh->P + 8, 64) * 4));
+  SCK(cudaMallocHost(&sh->h_dev, 64 * 8));
+  return 0;
+}
+
+// upload the K coefficient rows and the initial occupied sites, build K blocks and U0
+int shard_build(ShardedCtx* sh, const std::vector<std::complex<double>>& kc, const std::vector<int32_t>& sites,
+                std::string* err) {
+  cudaStream_t st = sh->st;
+  SCK(cudaMemcpyAsync(sh->kcoef, kc.data(), kc.size() * 16, cudaMemcpyHostToDevice, st));
+  SCK(cudaMemcpyAsync(sh->sites, sites.data(), sites.size() * 4, cudaMemcpyHostToDevice, st));
+  SCK(cudaMemcpyAsync(sh->gamma_dev, &sh->gamma, 8, cudaMemcpyHostToDevice, st));
+  for (auto& l : sh->loc) {
+    if (build_k(st, l.K, sh->ldL, sh->Lx, sh->Ly, sh->kcoef, sh->kcoef + sh->Lx, err, l.row0, sh->Lp)) return 4;
+    if (init_state(st, l.U[0], sh->ldN, 0, sh->sites, sh->N, 1, err, l.row0, sh->Lp)) return 4;
+  }
+  SCK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+namespace {
+
+int gather_full(ShardedCtx* sh, int which, std::string* err) {
+  std::vector<void*> send;
+  for (auto& l : sh->loc) send.push_back(l.U[which]);
+  return sh->comm.allgather(sh->st, send.data(), sh->Ufull, (size_t)sh->Lp * sh->ldN * 16, err);
+}
+
+int allreduce_gram(ShardedCtx* sh, std::string* err) {
+  std::vector<double*> part;
+  for (auto& l : sh->loc) part.push_back(reinterpret_cast<double*>(l.Gpart));
+  return sh->comm.allreduce(sh->st, part.data(), reinterpret_cast<double*>(sh->G), (size_t)sh->N * sh->ldN * 2, err);
+}
+
+// CholeskyQR2 of the distributed U (local blocks src[s]); tmp[s] the other buffers.
+int cqr2(ShardedCtx* sh, int src_which, std::string* err) {
+  int src = src_which;
+  for (int pass = 0; pass < 2; ++pass) {
+    {
+      Phase p(sh->prof, sh->st, TRAJ_PH_GRAM);
+      for (auto& l : sh->loc)
+        STRY(zgemm(sh->st, 1, 0, sh->N, sh->N, sh->Lp, 1.0, 0.0, l.U[src], sh->ldN, 0, l.U[src], sh->ldN, 0, 0.0,
+                   l.Gpart, sh->ldN, 0, 1, TRAJ_C_UPPER_F, err));
+      STRY(allreduce_gram(sh, err));
+    }
+    {
+      Phase p(sh->prof, sh->st, TRAJ_PH_CHOL);
+      bool full = pass == 0 || sh->full_cqr2;
+      if (!full) {
+        STRY(gram_deviation(sh->st, sh->G, sh->ldN, 0, sh->N, 1, sh->gdev, err));
+        SCK(cudaMemcpyAsync(sh->h_dev, sh->gdev, 8, cudaMemcpyDeviceToHost, sh->st));
+        SCK(cudaStreamSynchronize(sh->st));
+        if (sh->h_dev[0] > 1e-9 / sqrt((double)sh->N)) full = true;
+        if (full) ++sh->cqr2_fallbacks;
+      }
+      if (full)
+        STRY(chol_inverse(sh->st, sh->N, sh->G, sh->ldN, 0, sh->X, sh->ldN, 0, 1, sh->chol_scratch, sh->failed_dev,
+                          err));
+      else
+        STRY(first_order_inverse(sh->st, sh->G, sh->ldN, 0, sh->X, sh->ldN, 0, sh->N, 1, err));
+    }
+    {
+      Phase p(sh->prof, sh->st, TRAJ_PH_TRMM);
+      for (auto& l : sh->loc)
+        STRY(zgemm(sh->st, 0, 0, sh->Lp, sh->N, sh->N, 1.0, 0.0, l.U[src], sh->ldN, 0, sh->X, sh->ldN, 0, 0.0,
+                   l.U[1 - src], sh->ldN, 0, 1, TRAJ_TRI_B_UPPER_F, err));
+    }
+    src = 1 - src;
+  }
+  return 0;   // two passes: back in src_which
+}
+
+int projective(ShardedCtx* sh, int which, long long step, std::string* err) {
+  Phase p(sh->prof, sh->st, TRAJ_PH_PROJECT);
+  cudaStream_t st = sh->st;
+  const int capr = sh->capr, P = sh->P;
+  for (auto& l : sh->loc) {
+    STRY(compact(st, l.flags, sh->Lp, 1, l.Sloc, capr, l.cnt, err, l.row0));
+    STRY(gather_rows(st, l.U[which], sh->ldN, 0, l.Sloc, 0, l.cnt, capr, 1, l.USloc, sh->ldN, 0, sh->N, err, l.row0));
+  }
+  {
+    std::vector<void*> a, b, c;
+    for (auto& l : sh->loc) {
+      a.push_back(l.cnt);
+      b.push_back(l.Sloc);
+      c.push_back(l.USloc);
+    }
+    STRY(sh->comm.allgather(st, a.data(), sh->cntrecv, 4, err));
+    STRY(sh->comm.allgather(st, b.data(), sh->Srecv, (size_t)capr * 4, err));
+    STRY(sh->comm.allgather(st, c.data(), sh->USrecv, (size_t)capr * sh->ldN * 16, err));
+  }
+  SCK(cudaMemcpyAsync(sh->h_small, sh->cntrecv, P * 4, cudaMemcpyDeviceToHost, st));
+  SCK(cudaStreamSynchronize(st));
+  std::vector<int> cnt(sh->h_small, sh->h_small + P);
+  int total = 0;
+  for (int q = 0; q < P; ++q) {
+    if (cnt[q] > capr) {
+      if (err) *err = "click list overflow on shard " + std::to_string(q);
+      return TRAJ_ENUMERIC;
+    }
+    total += cnt[q];
+  }
+  sh->last_nS = total;
+  sh->last_n1 = 0;
+  if (total == 0) return 0;
+  // pack the per-shard blocks (shard order = ascending sites) into S and U_S
+  int off = 0;
+  for (int q = 0; q < P; ++q) {
+    if (cnt[q] == 0) continue;
+    SCK(cudaMemcpyAsync(sh->S + off, sh->Srecv + (size_t)q * capr, cnt[q] * 4, cudaMemcpyDeviceToDevice, st));
+    SCK(cudaMemcpyAsync(sh->US + (size_t)off * sh->ldN, sh->USrecv + (size_t)q * capr * sh->ldN,
+                        (size_t)cnt[q] * sh->ldN * 16, cudaMemcpyDeviceToDevice, st));
+    off += cnt[q];
+  }
+  sh->h_small[P] = total;
+  SCK(cudaMemcpyAsync(sh->count, sh->h_small + P, 4, cudaMemcpyHostToDevice, st));
+  // replicated: C_SS, sampling, W
+  STRY(zgemm(st, 0, 1, total, total, sh->N, 1.0, 0.0, sh->US, sh->ldN, 0, sh->US, sh->ldN, 0, 0.0, sh->D0, sh->ldcap,
+             0, 1, 0, err));
+  STRY(sample_outcomes(st, sh->D0, sh->Dw, sh->ldcap, 0, sh->S, sh->cap, sh->count, total, 1, step, sh->traj_base,
+                       sh->seed, sh->occ, sh->Linv, sh->DLinv, sh->Ybuf, sh->Zbuf, sh->ldcap, sh->pos1, sh->S1, sh->S0,
+                       sh->k1, sh->k0, err));
+  SCK(cudaMemcpyAsync(sh->h_small, sh->k1, 4, cudaMemcpyDeviceToHost, st));
+  SCK(cudaMemcpyAsync(sh->h_small + 1, sh->k0, 4, cudaMemcpyDeviceToHost, st));
+  SCK(cudaStreamSynchronize(st));
+  const int k1 = sh->h_small[0], k0 = sh->h_small[1];
+  sh->last_n1 = k1;
+  if (k1 > 0) {
+    STRY(gather_sub(st, sh->D0, sh->ldcap, sh->pos1, k1, sh->D11, sh->ldcap, err));
+    STRY(chol_inverse(st, k1, sh->D11, sh->ldcap, 0, sh->X11, sh->ldcap, 0, 1, sh->chol_scratch_small, sh->failed_dev,
+                      err));
+    // U_{S1} = rows pos1 of U_S (into USrecv, free now)
+    STRY(gather_rows(st, sh->US, sh->ldN, 0, sh->pos1, 0, nullptr, k1, 1, sh->USrecv, sh->ldN, 0, sh->N, err));
+    STRY(zgemm(st, 1, 0, sh->N, k1, k1, 1.0, 0.0, sh->USrecv, sh->ldN, 0, sh->X11, sh->ldcap, 0, 0.0, sh->W,
+               sh->ldcap, 0, 1, TRAJ_TRI_B_UPPER_F, err));
+    for (auto& l : sh->loc) {
+      STRY(zgemm(st, 0, 0, sh->Lp, k1, sh->N, 1.0, 0.0, l.U[which], sh->ldN, 0, sh->W, sh->ldcap, 0, 0.0, l.Tm,
+                 sh->ldcap, 0, 1, 0, err));
+      STRY(sub_identity(st, l.Tm, sh->ldcap, sh->S1, k1, err, l.row0, sh->Lp));
+      STRY(zgemm(st, 0, 1, sh->Lp, sh->N, k1, -1.0, 0.0, l.Tm, sh->ldcap, 0, sh->W, sh->ldcap, 0, 1.0, l.U[which],
+                 sh->ldN, 0, 1, 0, err));
+    }
+  }
+  if (k0 > 0)
+    for (auto& l : sh->loc) STRY(zero_rows(st, l.U[which], sh->ldN, sh->S0, k0, sh->N, err, l.row0, sh->Lp));
+  return 0;
+}
+
+}  // namespace
+
+int shard_step(ShardedCtx* sh, long long* step, std::string* err) {
+  const int cur = sh->cur, nxt = 1 - sh->cur;
+  {
+    Phase p(sh->prof, sh->st, TRAJ_PH_PROPAGATE);
+    STRY(gather_full(sh, cur, err));
+    for (auto& l : sh->loc)
+      STRY(zgemm(sh->st, 0, 0, sh->Lp, sh->N, sh->L, 1.0, 0.0, l.K, sh->ldL, 0, sh->Ufull, sh->ldN, 0, 0.0, l.U[nxt],
+                 sh->ldN, 0, 1, 0, err));
+  }
+  {
+    Phase p(sh->prof, sh->st, TRAJ_PH_MONITOR);
+    for (auto& l : sh->loc) {
+      if (sh->protocol == TRAJ_HOMODYNE)
+        STRY(row_monitor(sh->st, l.U[nxt], sh->ldN, 0, sh->Lp, sh->N, 1, 1, *step, sh->traj_base, sh->seed,
+                         sh->gamma_dev, sh->dt, nullptr, err, l.row0));
+      else
+        STRY(click_draw(sh->st, sh->Lp, 1, *step, sh->traj_base, sh->seed, sh->gamma_dev, sh->dt, l.flags, err,
+                        l.row0));
+    }
+  }
+  if (sh->protocol == TRAJ_PROJECTIVE) STRY(projective(sh, nxt, *step, err));
+  STRY(cqr2(sh, nxt, err));
+  sh->cur = nxt;
+  *step += 1;
+  return 0;
+}
+
+int shard_orthonormalize(ShardedCtx* sh, std::string* err) { return cqr2(sh, sh->cur, err); }
+
+int shard_entropy(ShardedCtx* sh, const int64_t* A, int64_t nA, double* S_out, std::string* err) {
+  cudaStream_t st = sh->st;
+  // split A by owning shard (order within a shard preserved; the spectrum is order-free)
+  std::vector<std::vector<int32_t>> part(sh->P);
+  for (int64_t q = 0; q < nA; ++q) part[A[q] / sh->Lp].push_back((int32_t)A[q]);
+  std::vector<int32_t> flat;
+  std::vector<size_t> offs(sh->P + 1, 0);
+  for (int q = 0; q < sh->P; ++q) {
+    offs[q] = flat.size();
+    flat.insert(flat.end(), part[q].begin(), part[q].end());
+  }
+  offs[sh->P] = flat.size();
+  SCK(cudaMemcpyAsync(sh->region, flat.data(), flat.size() * 4, cudaMemcpyHostToDevice, st));
+  SCK(cudaMemsetAsync(sh->bad_dev, 0, 4, st));
+  const int other = 1 - sh->cur;
+  int n;
+  if (nA > sh->N) {
+    // distributed Gram of U_A: sum over shards of U_{A,g}^dag U_{A,g}
+    for (auto& l : sh->loc) {
+      const int c = (int)part[l.g].size();
+      if (c) STRY(gather_rows(st, l.U[sh->cur], sh->ldN, 0, sh->region + offs[l.g], 0, nullptr, c, 1, l.U[other],
+                              sh->ldN, 0, sh->N, err, l.row0));
+      STRY(zgemm(st, 1, 0, sh->N, sh->N, c, 1.0, 0.0, l.U[other], sh->ldN, 0, l.U[other], sh->ldN, 0, 0.0, l.Gpart,
+                 sh->ldN, 0, 1, 0, err));
+    }
+    STRY(allreduce_gram(sh, err));
+    n = sh->N;
+  } else {
+    // gather the rows of A from every shard, then C_A = U_A U_A^dag
+    size_t capA = 0;
+    for (int q = 0; q < sh->P; ++q) capA = std::max(capA, part[q].size());
+    std::vector<void*> send;
+    for (auto& l : sh->loc) {
+      const int c = (int)part[l.g].size();
+      if (c) STRY(gather_rows(st, l.U[sh->cur], sh->ldN, 0, sh->region + offs[l.g], 0, nullptr, c, 1, l.U[other],
+                              sh->ldN, 0, sh->N, err, l.row0));
+      send.push_back(l.U[other]);
+    }
+    STRY(sh->comm.allgather(st, send.data(), sh->Ufull, capA * sh->ldN * 16, err));
+    for (int q = 0; q < sh->P; ++q)
+      if (!part[q].empty())
+        SCK(cudaMemcpyAsync(sh->X + offs[q] * sh->ldN, sh->Ufull + (size_t)q * capA * sh->ldN,
+                            part[q].size() * sh->ldN * 16, cudaMemcpyDeviceToDevice, st));
+    STRY(zgemm(st, 0, 1, nA, nA, sh->N, 1.0, 0.0, sh->X, sh->ldN, 0, sh->X, sh->ldN, 0, 0.0, sh->G, sh->ldN, 0, 1, 0,
+               err));
+    n = (int)nA;
+  }
+  cusolverStatus_t r = cusolverDnZheevd(sh->solver, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER, n,
+                                        reinterpret_cast<cuDoubleComplex*>(sh->G), (int)sh->ldN, sh->eig_w,
+                                        reinterpret_cast<cuDoubleComplex*>(sh->eig_work), sh->lwork, sh->eig_info);
+  if (r != CUSOLVER_STATUS_SUCCESS) {
+    if (err) *err = "cusolverDnZheevd failed: " + std::to_string(r);
+    return TRAJ_ECUDA;
+  }
+  STRY(entropy_reduce(st, sh->eig_w, n, sh->S_dev, sh->bad_dev, err));
+  int32_t flags[2];
+  SCK(cudaMemcpyAsync(S_out, sh->S_dev, 8, cudaMemcpyDeviceToHost, st));
+  SCK(cudaMemcpyAsync(&flags[0], sh->bad_dev, 4, cudaMemcpyDeviceToHost, st));
+  SCK(cudaMemcpyAsync(&flags[1], sh->failed_dev, 4, cudaMemcpyDeviceToHost, st));
+  SCK(cudaStreamSynchronize(st));
+  if (flags[1]) S_out[0] = nan("");
+  if (flags[0] && !flags[1]) {
+    int32_t one = 1;
+    SCK(cudaMemcpy(sh->failed_dev, &one, 4, cudaMemcpyHostToDevice));
+    if (err) *err = "spectrum of C_A outside [-1e-8, 1+1e-8]";
+    return TRAJ_ENUMERIC;
+  }
+  return 0;
+}
+
+int shard_occupations(ShardedCtx* sh, double* n_out, long long step, std::string* err) {
+  for (size_t s = 0; s < sh->loc.size(); ++s)
+    STRY(row_monitor(sh->st, sh->loc[s].U[sh->cur], sh->ldN, 0, sh->Lp, sh->N, 1, 0, step, sh->traj_base, sh->seed,
+                     sh->gamma_dev, sh->dt, n_out + s * sh->Lp, err, sh->loc[s].row0));
+  return 0;
+}
+
+int shard_correlation_rows(ShardedCtx* sh, int64_t row0, int64_t nrows, void* C_out, std::string* err) {
+  STRY(gather_full(sh, sh->cur, err));
+  return zgemm(sh->st, 0, 1, nrows, sh->L, sh->N, 1.0, 0.0, sh->Ufull + row0 * sh->ldN, sh->ldN, 0, sh->Ufull,
+               sh->ldN, 0, 0.0, reinterpret_cast<cplx*>(C_out), sh->L, 0, 1, 0, err);
+}
+
+int shard_get_state(ShardedCtx* sh, void* U_out, std::string* err) {
+  for (size_t s = 0; s < sh->loc.size(); ++s)
+    SCK(cudaMemcpy2DAsync(reinterpret_cast<char*>(U_out) + s * (size_t)sh->Lp * sh->N * 16, (size_t)sh->N * 16,
+                          sh->loc[s].U[sh->cur], (size_t)sh->ldN * 16, (size_t)sh->N * 16, sh->Lp, cudaMemcpyDefault,
+                          sh->st));
+  SCK(cudaStreamSynchronize(sh->st));
+  return 0;
+}
+
+int shard_set_state(ShardedCtx* sh, const void* U_in, std::string* err) {
+  for (size_t s = 0; s < sh->loc.size(); ++s)
+    SCK(cudaMemcpy2DAsync(sh->loc[s].U[sh->cur], (size_t)sh->ldN * 16,
+                          reinterpret_cast<const char*>(U_in) + s * (size_t)sh->Lp * sh->N * 16, (size_t)sh->N * 16,
+                          (size_t)sh->N * 16, sh->Lp, cudaMemcpyDefault, sh->st));
+  SCK(cudaStreamSynchronize(sh->st));
+  return 0;
+}
+
+int shard_failed(ShardedCtx* sh, int32_t* flag, std::string* err) {
+  SCK(cudaMemcpyAsync(sh->h_small, sh->failed_dev, 4, cudaMemcpyDeviceToHost, sh->st));
+  SCK(cudaStreamSynchronize(sh->st));
+  *flag = sh->h_small[0];
+  return 0;
+}
+
+void shard_destroy(ShardedCtx* sh) {
+  if (sh->st) cudaStreamSynchronize(sh->st);
+  if (sh->comm.comm) ncclCommDestroy(sh->comm.comm);
+  if (sh->h_small) cudaFreeHost(sh->h_small);
+  if (sh->h_dev) cudaFreeHost(sh->h_dev);
+}
+
+}  // namespace traj

@@ -1,0 +1,94 @@
+// Row-sharded trajectory step: K and U split by rows across P shards.
+#pragma once
+#include <complex>
+#include <string>
+#include <vector>
+
+#include "../../include/traj.h"
+#include "common.cuh"
+#include "profiler.h"
+
+typedef struct ncclComm* ncclComm_t;
+typedef struct cusolverDnContext* cusolverDnHandle_t;
+
+namespace traj {
+
+// Collectives over the P shards.  NCCL mode: one shard per process (rank = shard_rank).
+// Emulation mode (nccl_id == NULL): all P shards live in this handle on one GPU and the
+// collectives are device copies / sums in rank order -- the same data movement, used to
+// validate the sharded algorithm on a single GPU.
+struct ShardComm {
+  int P = 1, P_local = 1, rank0 = 0;
+  ncclComm_t comm = nullptr;
+  int allgather(cudaStream_t st, void* const* send, void* recv, size_t bytes, std::string* err);
+  int allreduce(cudaStream_t st, double* const* part, double* out, size_t n, std::string* err);
+};
+
+struct ShardLocal {
+  int g = 0, row0 = 0;
+  cplx* K = nullptr;       // Lp x ldL: rows [row0, row0 + Lp) of K
+  cplx* U[2] = {nullptr, nullptr};   // Lp x ldN
+  cplx* Gpart = nullptr;   // N x ldN partial Gram (aliases G in NCCL mode)
+  int32_t* flags = nullptr;
+  int32_t* Sloc = nullptr;
+  int32_t* cnt = nullptr;
+  cplx* USloc = nullptr;   // capr x ldN
+  cplx* Tm = nullptr;      // Lp x ldcap
+};
+
+struct ShardedCtx {
+  ShardComm comm;
+  int L = 0, N = 0, Lx = 0, Ly = 0, P = 1, Lp = 0, capr = 0, cap = 0, lwork = 0;
+  long long ldN = 0, ldL = 0, ldcap = 0;
+  int protocol = 0;
+  double dt = 0, J = 0, gamma = 0;
+  uint64_t seed = 0;
+  long long traj_base = 0;
+  std::vector<ShardLocal> loc;
+  int cur = 0;
+  cplx *Ufull = nullptr, *G = nullptr, *X = nullptr;
+  void* chol_scratch = nullptr;
+  int32_t *Srecv = nullptr, *cntrecv = nullptr, *S = nullptr, *count = nullptr;
+  cplx *USrecv = nullptr, *US = nullptr;
+  cplx *D0 = nullptr, *Dw = nullptr, *Linv = nullptr, *DLinv = nullptr, *Ybuf = nullptr, *Zbuf = nullptr;
+  int32_t *occ = nullptr, *pos1 = nullptr, *S1 = nullptr, *S0 = nullptr, *k1 = nullptr, *k0 = nullptr;
+  cplx *D11 = nullptr, *X11 = nullptr, *W = nullptr;
+  void* chol_scratch_small = nullptr;
+  double* gamma_dev = nullptr;
+  int32_t* failed_dev = nullptr;
+  double* eig_w = nullptr;
+  cplx* eig_work = nullptr;
+  int* eig_info = nullptr;
+  double* S_dev = nullptr;
+  int32_t* bad_dev = nullptr;
+  unsigned long long* gdev = nullptr;
+  int32_t* region = nullptr;
+  cplx* kcoef = nullptr;
+  int32_t* sites = nullptr;
+  int32_t* h_small = nullptr;
+  double* h_dev = nullptr;
+  long long last_nS = 0, last_n1 = 0, cqr2_fallbacks = 0;
+  bool full_cqr2 = false;
+  cudaStream_t st = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  Profiler* prof = nullptr;
+};
+
+// Validates the sharding fields; fills the geometry of sh.
+int shard_validate(const traj_config* c, std::string* why);
+size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork);
+int shard_init(ShardedCtx* sh, const traj_config* c, std::string* err);
+int shard_build(ShardedCtx* sh, const std::vector<std::complex<double>>& kc, const std::vector<int32_t>& sites,
+                std::string* err);
+int shard_step(ShardedCtx* sh, long long* step, std::string* err);
+int shard_orthonormalize(ShardedCtx* sh, std::string* err);
+int shard_entropy(ShardedCtx* sh, const int64_t* A, int64_t nA, double* S_out, std::string* err);
+int shard_occupations(ShardedCtx* sh, double* n_out, long long step, std::string* err);
+int shard_correlation_rows(ShardedCtx* sh, int64_t row0, int64_t nrows, void* C_out, std::string* err);
+int shard_get_state(ShardedCtx* sh, void* U_out, std::string* err);
+int shard_set_state(ShardedCtx* sh, const void* U_in, std::string* err);
+int shard_failed(ShardedCtx* sh, int32_t* flag, std::string* err);
+void shard_destroy(ShardedCtx* sh);
+int nccl_unique_id(void* out128, std::string* err);
+
+}  // namespace traj

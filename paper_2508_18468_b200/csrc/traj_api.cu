@@ -18,6 +18,8 @@
 #include "common.cuh"
 #include "monitor.h"
 #include "zgemm.h"
+#include "profiler.h"
+#include "shard.h"
 
 namespace traj {
 std::atomic<long long> g_kernel_launches{0};
@@ -27,6 +29,7 @@ using namespace traj;
 
 struct traj_ctx {
   traj_config cfg;
+  ShardedCtx* sh = nullptr;        // row-sharded mode (shard_size > 1 or an NCCL communicator)
   std::vector<double> gamma;
   int L = 0, N = 0, Lx = 0, Ly = 0, T = 0, cap = 0;
   long long ldN = 0, ldL = 0, ldcap = 0, sU = 0, sG = 0;
@@ -66,12 +69,7 @@ struct traj_ctx {
   double* h_dev = nullptr;        // pinned host copy of gdev
   std::vector<int64_t> last_nS, last_n1;
   std::string err;
-  // profiling
-  bool prof = false;
-  std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> evs;
-  std::vector<cudaEvent_t> pool;
-  double ms[TRAJ_NPHASES] = {0};
-  long long launches[TRAJ_NPHASES] = {0};
+  Profiler prof;
 };
 
 namespace {
@@ -134,8 +132,8 @@ int validate(const traj_config* c, std::string* why) {
     if (!(g >= 0) || !isfinite(g)) return bad("gamma must be >= 0 and finite");
     if (c->protocol == TRAJ_PROJECTIVE && g * c->dt > 1.0) return bad("projective needs gamma*dt <= 1 (Q10)");
   }
-  if (c->shard_rank != 0 || c->shard_size != 1) return bad("row sharding is not available in this build");
-  if (c->nccl_id) return bad("nccl_id must be NULL in this build");
+  if (c->shard_size != 1 || c->nccl_id) return shard_validate(c, why);
+  if (c->shard_rank != 0) return bad("shard_rank must be 0 without sharding");
   return 0;
 }
 
@@ -247,35 +245,6 @@ std::vector<std::complex<double>> ring_coefficients(int n, double J, double dt) 
   return c;
 }
 
-struct Phase {
-  traj_ctx* h;
-  int ph;
-  cudaEvent_t a = nullptr, b = nullptr;
-  long long l0;
-  Phase(traj_ctx* h_, int p) : h(h_), ph(p), l0(g_kernel_launches.load()) {
-    if (!h->prof) return;
-    a = get();
-    cudaEventRecord(a, h->st);
-  }
-  cudaEvent_t get() {
-    if (!h->pool.empty()) {
-      cudaEvent_t e = h->pool.back();
-      h->pool.pop_back();
-      return e;
-    }
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    return e;
-  }
-  ~Phase() {
-    h->launches[ph] += g_kernel_launches.load() - l0;
-    if (!h->prof) return;
-    b = get();
-    cudaEventRecord(b, h->st);
-    h->evs.emplace_back(ph, a, b);
-  }
-};
-
 // CholeskyQR2 on U (state), tmp another buffer of the same shape; result in U.
 // Pass 2 sees G2 = I + E with |E| ~ kappa(U)^2 eps: its Cholesky inverse is taken from the
 // first-order closed form (exact up to N |E|^2, below rounding when N max|E|^2 < 1e-18,
@@ -285,12 +254,12 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
   cplx* dst = tmp;
   for (int pass = 0; pass < 2; ++pass) {
     {
-      Phase p(h, TRAJ_PH_GRAM);
+      Phase p(&h->prof, h->st, TRAJ_PH_GRAM);
       TRY(zgemm(h->st, 1, 0, h->N, h->N, h->L, 1.0, 0.0, src, h->ldN, h->sU, src, h->ldN, h->sU, 0.0, h->G, h->ldN,
                 h->sG, h->T, TRAJ_C_UPPER_F, &h->err));
     }
     {
-      Phase p(h, TRAJ_PH_CHOL);
+      Phase p(&h->prof, h->st, TRAJ_PH_CHOL);
       bool full = pass == 0 || h->full_cqr2;
       if (!full) {
         TRY(gram_deviation(h->st, h->G, h->ldN, h->sG, h->N, h->T, h->gdev, &h->err));
@@ -311,7 +280,7 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
       }
     }
     {
-      Phase p(h, TRAJ_PH_TRMM);
+      Phase p(&h->prof, h->st, TRAJ_PH_TRMM);
       TRY(zgemm(h->st, 0, 0, h->L, h->N, h->N, 1.0, 0.0, src, h->ldN, h->sU, h->X, h->ldN, h->sG, 0.0, dst, h->ldN,
                 h->sU, h->T, TRAJ_TRI_B_UPPER_F, &h->err));
     }
@@ -321,7 +290,7 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
 }
 
 int projective(traj_ctx* h, cplx* U) {
-  Phase p(h, TRAJ_PH_PROJECT);
+  Phase p(&h->prof, h->st, TRAJ_PH_PROJECT);
   const int T = h->T, cap = h->cap;
   TRY(compact(h->st, h->flags, h->L, T, h->S, cap, h->count, &h->err));
   CK(cudaMemcpyAsync(h->h_small, h->count, T * 4, cudaMemcpyDeviceToHost, h->st));
@@ -380,18 +349,18 @@ int one_step(traj_ctx* h) {
   cplx* Uc = h->U[h->cur];
   cplx* Un = h->U[1 - h->cur];
   {
-    Phase p(h, TRAJ_PH_PROPAGATE);
+    Phase p(&h->prof, h->st, TRAJ_PH_PROPAGATE);
     // U <- K U  (K shared across the batch: stride 0)
     TRY(zgemm(h->st, 0, 0, h->L, h->N, h->L, 1.0, 0.0, h->K, h->ldL, 0, Uc, h->ldN, h->sU, 0.0, Un, h->ldN, h->sU,
               h->T, 0, &h->err));
   }
   if (h->cfg.protocol == TRAJ_HOMODYNE) {
-    Phase p(h, TRAJ_PH_MONITOR);
+    Phase p(&h->prof, h->st, TRAJ_PH_MONITOR);
     TRY(row_monitor(h->st, Un, h->ldN, h->sU, h->L, h->N, h->T, 1, h->step, h->cfg.traj_base, h->cfg.seed,
                     h->gamma_dev, h->cfg.dt, nullptr, &h->err));
   } else {
     {
-      Phase p(h, TRAJ_PH_MONITOR);
+      Phase p(&h->prof, h->st, TRAJ_PH_MONITOR);
       TRY(click_draw(h->st, h->L, h->T, h->step, h->cfg.traj_base, h->cfg.seed, h->gamma_dev, h->cfg.dt, h->flags,
                      &h->err));
     }
@@ -404,6 +373,8 @@ int one_step(traj_ctx* h) {
   h->step += 1;
   return 0;
 }
+
+bool is_sharded(const traj_config* c) { return c->shard_size != 1 || c->nccl_id != nullptr; }
 
 int check_traj(traj_ctx* h, int64_t t) {
   if (!h) return TRAJ_EINVAL;
@@ -424,6 +395,10 @@ int entropy_impl(traj_ctx* h, const int64_t* A, int64_t nA, double* S_out) {
   if (nA == 0) {
     for (int t = 0; t < h->T; ++t) S_out[t] = 0.0;
     return 0;
+  }
+  if (h->sh) {
+    int r = shard_entropy(h->sh, A, nA, S_out, &h->err);
+    return r ? fail(h, r, h->err) : 0;
   }
   CK(cudaMemcpyAsync(h->region, idx.data(), nA * 4, cudaMemcpyHostToDevice, h->st));
   CK(cudaMemsetAsync(h->bad_dev, 0, h->T * 4, h->st));
@@ -492,8 +467,13 @@ int traj_workspace_bytes(const traj_config* cfg, size_t* out) {
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(h, TRAJ_ECUDA, "no CUDA device");
   int lw = 0;
   if ((s = eig_lwork((int)cfg->N, &lw, &why))) return fail(h, s, why);
-  traj_ctx tmp;
-  *out = carve(&tmp, cfg, nullptr, lw);
+  if (is_sharded(cfg)) {
+    ShardedCtx sh;
+    *out = shard_carve(&sh, cfg, nullptr, lw);
+  } else {
+    traj_ctx tmp;
+    *out = carve(&tmp, cfg, nullptr, lw);
+  }
   return 0;
 }
 
@@ -509,8 +489,14 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
   int lw = 0;
   if ((s = eig_lwork((int)cfg->N, &lw, &why))) return fail(h, s, why);
   {
-    traj_ctx tmp;
-    const size_t need = carve(&tmp, cfg, nullptr, lw);
+    size_t need;
+    if (is_sharded(cfg)) {
+      ShardedCtx sh;
+      need = shard_carve(&sh, cfg, nullptr, lw);
+    } else {
+      traj_ctx tmp;
+      need = carve(&tmp, cfg, nullptr, lw);
+    }
     if (!cfg->workspace || cfg->workspace_bytes < need)
       return fail(h, TRAJ_ECONFIG, "workspace missing or smaller than traj_workspace_bytes");
     if (reinterpret_cast<uintptr_t>(cfg->workspace) & 255) return fail(h, TRAJ_ECONFIG, "workspace not 256-B aligned");
@@ -521,7 +507,18 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
   h->cfg.gamma = h->gamma.data();
   h->st = reinterpret_cast<cudaStream_t>(cfg->stream);
   h->lwork = lw;
-  carve(h, cfg, reinterpret_cast<char*>(cfg->workspace), lw);
+  if (is_sharded(cfg)) {
+    h->sh = new ShardedCtx();
+    shard_carve(h->sh, cfg, reinterpret_cast<char*>(cfg->workspace), lw);
+    h->L = h->sh->L;
+    h->N = h->sh->N;
+    h->Lx = h->sh->Lx;
+    h->Ly = h->sh->Ly;
+    h->T = 1;
+    h->sh->prof = &h->prof;
+  } else {
+    carve(h, cfg, reinterpret_cast<char*>(cfg->workspace), lw);
+  }
   h->last_nS.assign(h->T, 0);
   h->last_n1.assign(h->T, 0);
   auto bail = [&](int st, const std::string& m) {
@@ -541,6 +538,13 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
   cusolverDnSetStream(h->solver, h->st);
   // zero the whole workspace: padded columns (ld > N) must read as zeros
   if (cudaMemsetAsync(cfg->workspace, 0, cfg->workspace_bytes, h->st) != cudaSuccess) return bail(TRAJ_ECUDA, "memset");
+  if (h->sh) {
+    h->sh->solver = h->solver;
+    h->sh->full_cqr2 = h->full_cqr2;
+    std::string e;
+    int s2 = shard_init(h->sh, cfg, &e);
+    if (s2) return bail(s2, e);
+  }
   // K = K_y (x) K_x from the ring coefficient rows (Ly = 1: K_y = [1])
   std::vector<std::complex<double>> kc = ring_coefficients(h->Lx, cfg->J, cfg->dt);
   if (h->Ly > 1) {
@@ -554,6 +558,12 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
     if (((i % h->Lx) + (i / h->Lx)) % 2 == 0) sites.push_back(i);
   if ((int)sites.size() != h->N) return bail(TRAJ_ECONFIG, "initial state does not have N particles");
   std::string e;
+  if (h->sh) {
+    int s2 = shard_build(h->sh, kc, sites, &e);
+    if (s2) return bail(s2, e);
+    *out = h;
+    return 0;
+  }
   if (cudaMemcpyAsync(h->kcoef, kc.data(), kc.size() * 16, cudaMemcpyHostToDevice, h->st) != cudaSuccess ||
       cudaMemcpyAsync(h->sites, sites.data(), sites.size() * 4, cudaMemcpyHostToDevice, h->st) != cudaSuccess ||
       cudaMemcpyAsync(h->gamma_dev, h->gamma.data(), h->T * 8, cudaMemcpyHostToDevice, h->st) != cudaSuccess)
@@ -569,14 +579,18 @@ int traj_step(traj_handle h, int64_t n_steps) {
   if (!h) return TRAJ_EINVAL;
   if (n_steps < 0) return fail(h, TRAJ_EINVAL, "n_steps < 0");
   for (int64_t s = 0; s < n_steps; ++s) {
-    int r = one_step(h);
-    if (r) return r;
+    int r = h->sh ? shard_step(h->sh, &h->step, &h->err) : one_step(h);
+    if (r) return fail(h, r, h->err);
   }
   return 0;
 }
 
 int traj_orthonormalize(traj_handle h) {
   if (!h) return TRAJ_EINVAL;
+  if (h->sh) {
+    int r = shard_orthonormalize(h->sh, &h->err);
+    return r ? fail(h, r, h->err) : 0;
+  }
   return cqr2(h, h->U[h->cur], h->U[1 - h->cur]);
 }
 
@@ -607,7 +621,8 @@ int traj_mutual_info(traj_handle h, const int64_t* A, int64_t nA, const int64_t*
 int traj_occupations(traj_handle h, double* n_out) {
   if (!h) return TRAJ_EINVAL;
   if (!n_out) return fail(h, TRAJ_EINVAL, "null n_out");
-  TRY(row_monitor(h->st, h->U[h->cur], h->ldN, h->sU, h->L, h->N, h->T, 0, h->step, h->cfg.traj_base, h->cfg.seed,
+  if (h->sh) TRY(shard_occupations(h->sh, n_out, h->step, &h->err));
+  else TRY(row_monitor(h->st, h->U[h->cur], h->ldN, h->sU, h->L, h->N, h->T, 0, h->step, h->cfg.traj_base, h->cfg.seed,
                   h->gamma_dev, h->cfg.dt, n_out, &h->err));
   return 0;
 }
@@ -617,6 +632,10 @@ int traj_correlation_rows(traj_handle h, int64_t traj, int64_t row0, int64_t nro
   if (s) return s;
   if (row0 < 0 || nrows < 0 || row0 + nrows > h->L || !C_out) return fail(h, TRAJ_EINVAL, "bad row range");
   if (nrows == 0) return 0;
+  if (h->sh) {
+    TRY(shard_correlation_rows(h->sh, row0, nrows, C_out, &h->err));
+    return 0;
+  }
   cplx* Ut = h->U[h->cur] + traj * h->sU;
   TRY(zgemm(h->st, 0, 1, nrows, h->L, h->N, 1.0, 0.0, Ut + row0 * h->ldN, h->ldN, 0, Ut, h->ldN, 0, 0.0,
             reinterpret_cast<cplx*>(C_out), h->L, 0, 1, 0, &h->err));
@@ -627,6 +646,10 @@ int traj_get_state(traj_handle h, int64_t traj, void* U_out) {
   int s = check_traj(h, traj);
   if (s) return s;
   if (!U_out) return fail(h, TRAJ_EINVAL, "null U_out");
+  if (h->sh) {
+    TRY(shard_get_state(h->sh, U_out, &h->err));
+    return 0;
+  }
   CK(cudaMemcpy2DAsync(U_out, (size_t)h->N * 16, h->U[h->cur] + traj * h->sU, (size_t)h->ldN * 16, (size_t)h->N * 16,
                        h->L, cudaMemcpyDefault, h->st));
   CK(cudaStreamSynchronize(h->st));
@@ -637,6 +660,10 @@ int traj_set_state(traj_handle h, int64_t traj, const void* U_in) {
   int s = check_traj(h, traj);
   if (s) return s;
   if (!U_in) return fail(h, TRAJ_EINVAL, "null U_in");
+  if (h->sh) {
+    TRY(shard_set_state(h->sh, U_in, &h->err));
+    return 0;
+  }
   CK(cudaMemcpy2DAsync(h->U[h->cur] + traj * h->sU, (size_t)h->ldN * 16, U_in, (size_t)h->N * 16, (size_t)h->N * 16,
                        h->L, cudaMemcpyDefault, h->st));
   CK(cudaStreamSynchronize(h->st));
@@ -660,6 +687,10 @@ int traj_failed(traj_handle h, int64_t traj, int32_t* flag) {
   int s = check_traj(h, traj);
   if (s) return s;
   if (!flag) return fail(h, TRAJ_EINVAL, "null flag");
+  if (h->sh) {
+    TRY(shard_failed(h->sh, flag, &h->err));
+    return 0;
+  }
   CK(cudaMemcpyAsync(h->h_small, h->failed_dev + traj, 4, cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
   *flag = h->h_small[0];
@@ -669,6 +700,11 @@ int traj_failed(traj_handle h, int64_t traj, int32_t* flag) {
 int traj_last_clicks(traj_handle h, int64_t traj, int64_t* n_clicks, int64_t* n_occupied) {
   int s = check_traj(h, traj);
   if (s) return s;
+  if (h->sh) {
+    if (n_clicks) *n_clicks = h->sh->last_nS;
+    if (n_occupied) *n_occupied = h->sh->last_n1;
+    return 0;
+  }
   if (n_clicks) *n_clicks = h->last_nS[traj];
   if (n_occupied) *n_occupied = h->last_n1[traj];
   return 0;
@@ -676,40 +712,24 @@ int traj_last_clicks(traj_handle h, int64_t traj, int64_t* n_clicks, int64_t* n_
 
 int traj_cqr2_fallbacks(traj_handle h, int64_t* n) {
   if (!h || !n) return TRAJ_EINVAL;
-  *n = h->cqr2_fallbacks;
+  *n = h->sh ? h->sh->cqr2_fallbacks : h->cqr2_fallbacks;
   return 0;
 }
 
 int traj_profile(traj_handle h, int enable) {
   if (!h) return TRAJ_EINVAL;
   CK(cudaStreamSynchronize(h->st));
-  for (auto& e : h->evs) {
-    h->pool.push_back(std::get<1>(e));
-    h->pool.push_back(std::get<2>(e));
-  }
-  h->evs.clear();
-  for (int p = 0; p < TRAJ_NPHASES; ++p) {
-    h->ms[p] = 0;
-    h->launches[p] = 0;
-  }
-  h->prof = enable != 0;
+  h->prof.reset(enable != 0);
   return 0;
 }
 
 int traj_phase_times(traj_handle h, double* ms, int64_t* launches) {
   if (!h) return TRAJ_EINVAL;
   CK(cudaStreamSynchronize(h->st));
-  for (auto& e : h->evs) {
-    float t = 0;
-    cudaEventElapsedTime(&t, std::get<1>(e), std::get<2>(e));
-    h->ms[std::get<0>(e)] += t;
-    h->pool.push_back(std::get<1>(e));
-    h->pool.push_back(std::get<2>(e));
-  }
-  h->evs.clear();
+  h->prof.collect();
   for (int p = 0; p < TRAJ_NPHASES; ++p) {
-    if (ms) ms[p] = h->ms[p];
-    if (launches) launches[p] = h->launches[p];
+    if (ms) ms[p] = h->prof.ms[p];
+    if (launches) launches[p] = h->prof.launches[p];
   }
   return 0;
 }
@@ -717,11 +737,11 @@ int traj_phase_times(traj_handle h, double* ms, int64_t* launches) {
 int traj_destroy(traj_handle h) {
   if (!h) return TRAJ_EINVAL;
   if (h->st) cudaStreamSynchronize(h->st);
-  for (auto& e : h->evs) {
-    cudaEventDestroy(std::get<1>(e));
-    cudaEventDestroy(std::get<2>(e));
+  if (h->sh) {
+    shard_destroy(h->sh);
+    delete h->sh;
   }
-  for (auto e : h->pool) cudaEventDestroy(e);
+  h->prof.destroy();
   if (h->solver) cusolverDnDestroy(h->solver);
   if (h->h_small) cudaFreeHost(h->h_small);
   if (h->h_dev) cudaFreeHost(h->h_dev);
@@ -740,6 +760,29 @@ int traj_zgemm(void* stream, int opA, int opB, int64_t M, int64_t N, int64_t K, 
                 reinterpret_cast<const cplx*>(A), lda, strideA, reinterpret_cast<const cplx*>(B), ldb, strideB, beta,
                 reinterpret_cast<cplx*>(C), ldc, strideC, batch, flags, &e);
   return s ? fail(nullptr, s, e) : 0;
+}
+
+int traj_nccl_unique_id(void* out128) {
+  if (!out128) return fail(nullptr, TRAJ_EINVAL, "null out");
+  std::string e;
+  int s = nccl_unique_id(out128, &e);
+  return s ? fail(nullptr, s, e) : 0;
+}
+
+int traj_shard_info(traj_handle h, int32_t* shard_size, int32_t* local_shards, int64_t* row0, int64_t* rows) {
+  if (!h) return TRAJ_EINVAL;
+  if (h->sh) {
+    if (shard_size) *shard_size = h->sh->P;
+    if (local_shards) *local_shards = h->sh->comm.P_local;
+    if (row0) *row0 = (int64_t)h->sh->comm.rank0 * h->sh->Lp;
+    if (rows) *rows = (int64_t)h->sh->comm.P_local * h->sh->Lp;
+  } else {
+    if (shard_size) *shard_size = 1;
+    if (local_shards) *local_shards = 1;
+    if (row0) *row0 = 0;
+    if (rows) *rows = h->L;
+  }
+  return 0;
 }
 
 size_t traj_chol_scratch_bytes(int64_t n, int64_t batch) { return chol_scratch_bytes(n, batch); }

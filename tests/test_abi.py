@@ -64,7 +64,7 @@ def _cfg(**kw):
 
 
 @pytest.mark.parametrize("field,value", [("N", 31), ("Lx", 63), ("dt", 0.0), ("protocol", 7), ("dim", 3),
-                                         ("n_traj", 0), ("shard_size", 2)])
+                                         ("n_traj", 0), ("shard_size", 3), ("shard_rank", 1)])
 def test_config_validation(lib, field, value):
     c, _keep = _cfg(**{field: value})
     if field == "Lx":
@@ -89,3 +89,12 @@ def test_no_cpu_fallback(lib):
     h = ctypes.c_void_p()
     assert lib.traj_init(ctypes.byref(c), ctypes.byref(h)) == 4      # TRAJ_ECUDA
     assert h.value is None
+
+
+def test_sharding_needs_single_trajectory(lib):
+    c, g = _cfg(shard_size=2)
+    g2 = np.array([0.5, 0.5])
+    c.gamma = g2.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    c.n_traj = 2
+    out = ctypes.c_size_t(0)
+    assert lib.traj_workspace_bytes(ctypes.byref(c), ctypes.byref(out)) == 2

@@ -227,3 +227,46 @@ def test_trajectory_parallel_ensemble_matches_oracle_average(P):
         x = vals[g * 3:(g + 1) * 3]
         assert np.all(res.count["half"][g] == 3)
         assert np.abs(res.mean["half"][g] - x.mean(axis=0)).max() < 1e-8
+
+
+@pytest.mark.parametrize("P_shards,protocol,gamma", [(2, "projective", 4.0), (4, "homodyne", 1.0),
+                                                     (4, "projective", 1.0)])
+def test_row_sharded_step_matches_oracle(P, P_shards, protocol, gamma):
+    """Row-sharded K and U, single-GPU emulation of P shards: allgather of U,
+    local K_g U, global-site Philox, gathered clicks with replicated sampling, all-reduced Gram.
+    Same trajectory as the oracle; entropies through both the gathered-rows (|A| <= N) and the
+    all-reduced-Gram (|A| > N) paths."""
+    L = 256
+    g = P.Trajectories(L, 1, protocol, [gamma], seed=13, traj_base=2, shard_size=P_shards)
+    assert (g.shard_size, g.local_shards, g.rows) == (P_shards, P_shards, L)
+    K = lattice.propagator_lattice(L, 1, 1.0, 0.05)
+    o = OracleTrajectory(L, 1, protocol, gamma, 0.05, seed=13, traj=2, K=K)
+    regions = [np.arange(L // 2), np.arange(37, 77), np.arange(0, L, 3)[:150], np.arange(200)]
+    for s in range(16):
+        g.step(1)
+        o.step(1)
+        if protocol == "projective":
+            assert g.last_clicks(0) == (o.last_clicks[0].size, int(o.last_clicks[1].sum()))
+        if s % 5 == 4:
+            assert np.abs(g.correlation(0).cpu().numpy() - o.correlation()).max() < C_TOL
+            for A in regions:
+                assert abs(g.entropy(A)[0] - o.entropy(A)) < S_TOL
+    n = g.occupations()[0].cpu().numpy()
+    assert np.abs(n - gaussian.occupations(o.U)).max() < 1e-12
+    U = g.get_state(0).cpu().numpy()
+    assert np.abs(U.conj().T @ U - np.eye(L // 2)).max() < 1e-12
+    assert not g.failed(0)
+
+
+def test_row_sharded_nccl_single_rank(P):
+    """The NCCL code path of the sharded step with a one-rank communicator (the only
+    configuration one GPU allows): same result as the unsharded handle."""
+    uid = P.traj_nccl_unique_id()
+    a = P.Trajectories(128, 1, "projective", [3.0], seed=5, shard_size=1, shard_rank=0, nccl_id=uid)
+    b = P.Trajectories(128, 1, "projective", [3.0], seed=5)
+    a.step(10)
+    b.step(10)
+    assert a.last_clicks(0) == b.last_clicks(0)
+    assert np.abs(a.correlation(0).cpu().numpy() - b.correlation(0).cpu().numpy()).max() < 1e-12
+    assert abs(a.entropy(np.arange(64))[0] - b.entropy(np.arange(64))[0]) < 1e-10
+    a.close()
