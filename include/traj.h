@@ -116,6 +116,18 @@ int traj_entropy(traj_handle h, const int64_t* A, int64_t nA, double* S_out);
 int traj_mutual_info(traj_handle h, const int64_t* A, int64_t nA,
                      const int64_t* B, int64_t nB, double* I_out);
 
+/* Density correlator of Eq. (2) for the 1d chain: C_out = host[L],
+ * C_out[r] = mean over the L - r pairs i < j = i + r of C_ij = -D_ij D_ji = -|(U U^dag)_ij|^2,
+ * r = 1..L-1 (C_out[0] = NaN).  Rows of U U^dag are formed in blocks on the DMMA GEMM and
+ * binned by a deterministic kernel (8 L^2 N flops).  TRAJ_EDOMAIN in 2d. */
+int traj_density_correlation(traj_handle h, int64_t traj, double* C_out);
+
+/* Particle-number covariance of Eq. (5) between disjoint regions A and B:
+ * G_out = host[n_traj], G_AB = -sum_{i in A, j in B} C_ij = sum |(U U^dag)_ij|^2 >= 0.
+ * The paper compares I_2 with (2 pi^2 / 3) G_AB. */
+int traj_particle_covariance(traj_handle h, const int64_t* A, int64_t nA, const int64_t* B, int64_t nB,
+                             double* G_out);
+
 /* n_out = device[n_traj][L] doubles: n_i = sum_k |U_ik|^2 of the current state
  * (row-sharded: the rows this handle holds, see traj_shard_info). */
 int traj_occupations(traj_handle h, double* n_out);

@@ -76,3 +76,27 @@ def mutual_information(U: np.ndarray, A, B) -> float:
 def occupations(U: np.ndarray) -> np.ndarray:
     """n_i = sum_k |U_ik|^2 (<n_i>_t = sum_j U_ij U_ij^*)."""
     return np.sum(np.abs(U) ** 2, axis=1)
+
+
+def density_correlation(U: np.ndarray) -> np.ndarray:
+    """C(r) of Eq. (2) for a 1d chain: C_ij = -D_ij D_ji = -|C_ij|^2 (i != j),
+    averaged over the pairs with |i - j| = r (i < j: L - r pairs), r = 1..L-1.
+    Returns an array of length L with entry 0 unused (NaN)."""
+    C = correlation(U)
+    L = C.shape[0]
+    out = np.full(L, np.nan)
+    w = np.abs(C) ** 2
+    for r in range(1, L):
+        out[r] = -np.mean(np.diagonal(w, offset=r))
+    return out
+
+
+def particle_covariance(U: np.ndarray, A, B) -> float:
+    """G_AB of Eq. (5): -sum_{i in A, j in B} C_ij with C_ij = -|D_ij|^2,
+    i.e. sum |(U U^dag)_ij|^2 over i in A, j in B (A, B disjoint)."""
+    A = np.asarray(A, dtype=np.int64)
+    B = np.asarray(B, dtype=np.int64)
+    if np.intersect1d(A, B).size:
+        raise ValueError("regions overlap")
+    CAB = U[A] @ U[B].conj().T
+    return float(np.sum(np.abs(CAB) ** 2))

@@ -63,6 +63,9 @@ _SIGS = {
     "traj_entropy": (ctypes.c_int, [_P, ctypes.POINTER(_I64), _I64, ctypes.POINTER(_D)]),
     "traj_mutual_info": (ctypes.c_int, [_P, ctypes.POINTER(_I64), _I64, ctypes.POINTER(_I64), _I64,
                                         ctypes.POINTER(_D)]),
+    "traj_density_correlation": (ctypes.c_int, [_P, _I64, ctypes.POINTER(_D)]),
+    "traj_particle_covariance": (ctypes.c_int, [_P, ctypes.POINTER(_I64), _I64, ctypes.POINTER(_I64), _I64,
+                                                ctypes.POINTER(_D)]),
     "traj_occupations": (ctypes.c_int, [_P, _P]),
     "traj_correlation_rows": (ctypes.c_int, [_P, _I64, _I64, _I64, _P]),
     "traj_get_state": (ctypes.c_int, [_P, _I64, _P]),
@@ -264,6 +267,21 @@ class Trajectories:
         out = np.zeros(self.n_traj)
         self._c(lib().traj_mutual_info(self._h, pa, a.size, pb, b.size,
                                        out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return out
+
+    def density_correlation(self, traj: int = 0) -> np.ndarray:
+        """C(r), Eq. (2), r = 0..L-1 (entry 0 is NaN); 1d only."""
+        out = np.zeros(self.L)
+        self._c(lib().traj_density_correlation(self._h, traj, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return out
+
+    def particle_covariance(self, A, B) -> np.ndarray:
+        """G_AB, Eq. (5), for every trajectory."""
+        a, pa = self._sites(A)
+        b, pb = self._sites(B)
+        out = np.zeros(self.n_traj)
+        self._c(lib().traj_particle_covariance(self._h, pa, a.size, pb, b.size,
+                                               out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
         return out
 
     def occupations(self):

@@ -529,10 +529,65 @@ int zero_rows(cudaStream_t st, cplx* U, long long ld, const int32_t* rows, int n
   return last(err, "zero_rows") == cudaSuccess ? 0 : 4;
 }
 
+// bins[r] += sum_{i < R, row0 + i + r < L} |C[i][row0 + i + r]|^2 for r = 1..L-1: one thread
+// per distance r, rows visited in order (deterministic).  Eq. (2).
+__global__ void bin_abs2_kernel(const cplx* C, long long ld, int R, int row0, int L, double* bins) {
+  for (int r = 1 + blockIdx.x * blockDim.x + threadIdx.x; r < L; r += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    const int imax = min(R, L - r - row0);
+    for (int i = 0; i < imax; ++i) {
+      const double2 v = C[(long long)i * ld + row0 + i + r];
+      s += v.x * v.x + v.y * v.y;
+    }
+    bins[r] += s;
+  }
+}
+
+// part[block] = sum over rows < R, columns j with mask[j], of |C[i][j]|^2 (Eq. 5)
+__global__ void masked_abs2_kernel(const cplx* C, long long ld, int R, int ncols, const int32_t* mask, double* part) {
+  __shared__ double red[32];
+  double s = 0.0;
+  const long long total = (long long)R * ncols;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / ncols), j = (int)(idx % ncols);
+    if (mask[j]) {
+      const double2 v = C[(long long)i * ld + j];
+      s += v.x * v.x + v.y * v.y;
+    }
+  }
+  s = block_sum<256>(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// out[0] += sum of part[0..n) (one thread, fixed order: deterministic)
+__global__ void accumulate_kernel(const double* part, int n, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += part[i];
+    out[0] += s;
+  }
+}
+
 // out += in (n doubles): the single-GPU emulation of an all-reduce
 __global__ void add_kernel(double* out, const double* in, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     out[i] += in[i];
+}
+
+int bin_abs2(cudaStream_t st, const cplx* C, long long ld, int R, int row0, int L, double* bins, std::string* err) {
+  bin_abs2_kernel<<<(unsigned)ceil_div(L, 256), 256, 0, st>>>(C, ld, R, row0, L, bins);
+  count_launch();
+  return last(err, "bin_abs2") == cudaSuccess ? 0 : 4;
+}
+
+int masked_abs2(cudaStream_t st, const cplx* C, long long ld, int R, int ncols, const int32_t* mask, double* part,
+                double* out, std::string* err) {
+  const int blocks = (int)std::min<long long>(ceil_div((long long)R * ncols, 256), 1024);
+  masked_abs2_kernel<<<blocks, 256, 0, st>>>(C, ld, R, ncols, mask, part);
+  accumulate_kernel<<<1, 32, 0, st>>>(part, blocks, out);
+  count_launch(2);
+  return last(err, "masked_abs2") == cudaSuccess ? 0 : 4;
 }
 
 int add_inplace(cudaStream_t st, double* out, const double* in, long long n, std::string* err) {

@@ -37,6 +37,11 @@ int entropy_reduce(cudaStream_t st, const double* lam, int n, double* S_out, int
 // rows [row0, row0+nrows) of K (nrows < 0: all L rows)
 int build_k(cudaStream_t st, cplx* K, long long ld, int Lx, int Ly, const cplx* kx, const cplx* ky, std::string* err,
             long long row0 = 0, long long nrows = -1);
+// bins[r] += sum_i |C[i][row0+i+r]|^2 over the R rows of the block C (rows row0.. of U U^dag)
+int bin_abs2(cudaStream_t st, const cplx* C, long long ld, int R, int row0, int L, double* bins, std::string* err);
+// out[0] += sum_{i<R, mask[j]} |C[i][j]|^2 (part: >= 1024 doubles of scratch)
+int masked_abs2(cudaStream_t st, const cplx* C, long long ld, int R, int ncols, const int32_t* mask, double* part,
+                double* out, std::string* err);
 // out[i] += in[i]
 int add_inplace(cudaStream_t st, double* out, const double* in, long long n, std::string* err);
 // out[t] = max_{i<=j} |G_ij - delta_ij| (as the bit pattern of a non-negative double)

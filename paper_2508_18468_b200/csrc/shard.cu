@@ -194,6 +194,10 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork) 
   lay.take(sh->region, (size_t)L * 4);
   lay.take(sh->kcoef, (size_t)(c->Lx + c->Ly) * 16);
   lay.take(sh->sites, (size_t)N * 4);
+  lay.take(sh->obs_bins, (size_t)L * 8);
+  lay.take(sh->obs_part, 1024 * 8);
+  lay.take(sh->obs_out, 16);
+  lay.take(sh->obs_mask, (size_t)L * 4);
   if (cap > 0) {
     lay.take(sh->Srecv, (size_t)cap * 4);
     lay.take(sh->cntrecv, (size_t)P * 4);
@@ -493,6 +497,8 @@ int shard_occupations(ShardedCtx* sh, double* n_out, long long step, std::string
                      sh->gamma_dev, sh->dt, n_out + s * sh->Lp, err, sh->loc[s].row0));
   return 0;
 }
+
+int shard_full_state(ShardedCtx* sh, std::string* err) { return gather_full(sh, sh->cur, err); }
 
 int shard_correlation_rows(ShardedCtx* sh, int64_t row0, int64_t nrows, void* C_out, std::string* err) {
   STRY(gather_full(sh, sh->cur, err));

@@ -72,6 +72,8 @@ struct ShardedCtx {
   cudaStream_t st = nullptr;
   cusolverDnHandle_t solver = nullptr;
   Profiler* prof = nullptr;
+  double *obs_bins = nullptr, *obs_part = nullptr, *obs_out = nullptr;
+  int32_t* obs_mask = nullptr;
 };
 
 // Validates the sharding fields; fills the geometry of sh.
@@ -88,6 +90,8 @@ int shard_correlation_rows(ShardedCtx* sh, int64_t row0, int64_t nrows, void* C_
 int shard_get_state(ShardedCtx* sh, void* U_out, std::string* err);
 int shard_set_state(ShardedCtx* sh, const void* U_in, std::string* err);
 int shard_failed(ShardedCtx* sh, int32_t* flag, std::string* err);
+// allgather the current U into sh->Ufull (L x ldN, row-major)
+int shard_full_state(ShardedCtx* sh, std::string* err);
 void shard_destroy(ShardedCtx* sh);
 int nccl_unique_id(void* out128, std::string* err);
 

@@ -60,6 +60,10 @@ struct traj_ctx {
   unsigned long long* gdev = nullptr;   // per-trajectory max |G2 - I| of the second CQR pass
   int32_t* region = nullptr;
   bool full_cqr2 = false;                // TRAJ_CQR2_FULL=1: always factor G2 by chol_inverse
+  double* obs_bins = nullptr;            // C(r) accumulators [L]
+  double* obs_part = nullptr;            // reduction partials [1024]
+  double* obs_out = nullptr;             // [n_traj]
+  int32_t* obs_mask = nullptr;           // region indicator [L]
   long long cqr2_fallbacks = 0;
   cplx* kcoef = nullptr;
   int32_t* sites = nullptr;
@@ -179,6 +183,10 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
   lay.take(h->S_dev, (size_t)T * 8);
   lay.take(h->bad_dev, (size_t)T * 4);
   lay.take(h->gdev, (size_t)T * 8);
+  lay.take(h->obs_bins, (size_t)L * 8);
+  lay.take(h->obs_part, 1024 * 8);
+  lay.take(h->obs_out, (size_t)T * 8);
+  lay.take(h->obs_mask, (size_t)L * 4);
   lay.take(h->region, (size_t)L * 4);
   lay.take(h->kcoef, (size_t)(Lx + Ly) * 16);
   lay.take(h->sites, (size_t)N * 4);
@@ -436,6 +444,76 @@ int entropy_impl(traj_ctx* h, const int64_t* A, int64_t nA, double* S_out) {
   return 0;
 }
 
+// Row-major source of the full U of trajectory t (sharded: gathered) and a scratch area
+// of `cap` complex elements for blocks of C = U U^dag.
+int full_state(traj_ctx* h, int t, const cplx** U, cplx** scratch, long long* cap) {
+  if (h->sh) {
+    TRY(shard_full_state(h->sh, &h->err));
+    *U = h->sh->Ufull;
+    *scratch = h->sh->X;
+    *cap = (long long)h->N * h->ldN;
+  } else {
+    *U = h->U[h->cur] + t * h->sU;
+    *scratch = h->X;
+    *cap = (long long)h->T * h->N * h->ldN;
+  }
+  return 0;
+}
+
+// C(r), Eq. (2): rows of C = U U^dag in blocks of R, binned by distance
+int density_correlation_impl(traj_ctx* h, int t, double* C_out) {
+  const cplx* U;
+  cplx* scr;
+  long long cap;
+  int s = full_state(h, t, &U, &scr, &cap);
+  if (s) return s;
+  const long long ldc = round_up(h->L, 8);
+  const int R = (int)std::max<long long>(1, std::min<long long>(h->L, cap / ldc));
+  CK(cudaMemsetAsync(h->obs_bins, 0, (size_t)h->L * 8, h->st));
+  for (int r0 = 0; r0 < h->L; r0 += R) {
+    const int rows = std::min(R, h->L - r0);
+    TRY(zgemm(h->st, 0, 1, rows, h->L, h->N, 1.0, 0.0, U + (long long)r0 * h->ldN, h->ldN, 0, U, h->ldN, 0, 0.0, scr,
+              ldc, 0, 1, 0, &h->err));
+    TRY(bin_abs2(h->st, scr, ldc, rows, r0, h->L, h->obs_bins, &h->err));
+  }
+  std::vector<double> bins(h->L);
+  CK(cudaMemcpyAsync(bins.data(), h->obs_bins, (size_t)h->L * 8, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  C_out[0] = nan("");
+  for (int r = 1; r < h->L; ++r) C_out[r] = -bins[r] / (double)(h->L - r);
+  return 0;
+}
+
+// G_AB, Eq. (5): sum over i in A (rows of C in blocks), j in B (mask) of |C_ij|^2
+int particle_covariance_impl(traj_ctx* h, const std::vector<int32_t>& A, const std::vector<int32_t>& maskB,
+                             double* G_out) {
+  const long long ldc = round_up(h->L, 8);
+  CK(cudaMemcpyAsync(h->obs_mask, maskB.data(), (size_t)h->L * 4, cudaMemcpyHostToDevice, h->st));
+  CK(cudaMemcpyAsync(h->region, A.data(), A.size() * 4, cudaMemcpyHostToDevice, h->st));
+  CK(cudaMemsetAsync(h->obs_out, 0, (size_t)h->T * 8, h->st));
+  for (int t = 0; t < h->T; ++t) {
+    const cplx* U;
+    cplx* scr;
+    long long cap;
+    int s = full_state(h, t, &U, &scr, &cap);
+    if (s) return s;
+    // rows of A gathered into the front of the scratch, the C block after them
+    const long long R = std::max<long long>(1, std::min<long long>((long long)A.size(), cap / (ldc + h->ldN)));
+    cplx* UA = scr;
+    cplx* Cb = scr + R * h->ldN;
+    for (long long a0 = 0; a0 < (long long)A.size(); a0 += R) {
+      const int rows = (int)std::min<long long>(R, (long long)A.size() - a0);
+      TRY(gather_rows(h->st, U, h->ldN, 0, h->region + a0, 0, nullptr, rows, 1, UA, h->ldN, 0, h->N, &h->err));
+      TRY(zgemm(h->st, 0, 1, rows, h->L, h->N, 1.0, 0.0, UA, h->ldN, 0, U, h->ldN, 0, 0.0, Cb, ldc, 0, 1, 0,
+                &h->err));
+      TRY(masked_abs2(h->st, Cb, ldc, rows, h->L, h->obs_mask, h->obs_part, h->obs_out + t, &h->err));
+    }
+  }
+  CK(cudaMemcpyAsync(G_out, h->obs_out, (size_t)h->T * 8, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -510,11 +588,18 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
   if (is_sharded(cfg)) {
     h->sh = new ShardedCtx();
     shard_carve(h->sh, cfg, reinterpret_cast<char*>(cfg->workspace), lw);
+    h->obs_bins = h->sh->obs_bins;
+    h->obs_part = h->sh->obs_part;
+    h->obs_out = h->sh->obs_out;
+    h->obs_mask = h->sh->obs_mask;
+    h->region = h->sh->region;
     h->L = h->sh->L;
     h->N = h->sh->N;
     h->Lx = h->sh->Lx;
     h->Ly = h->sh->Ly;
     h->T = 1;
+    h->ldN = h->sh->ldN;
+    h->ldL = h->sh->ldL;
     h->sh->prof = &h->prof;
   } else {
     carve(h, cfg, reinterpret_cast<char*>(cfg->workspace), lw);
@@ -616,6 +701,39 @@ int traj_mutual_info(traj_handle h, const int64_t* A, int64_t nA, const int64_t*
   if ((s = entropy_impl(h, AB.data(), (int64_t)AB.size(), sab.data()))) return s;
   for (int t = 0; t < h->T; ++t) I_out[t] = sa[t] + sb[t] - sab[t];
   return 0;
+}
+
+int traj_density_correlation(traj_handle h, int64_t traj, double* C_out) {
+  int s = check_traj(h, traj);
+  if (s) return s;
+  if (!C_out) return fail(h, TRAJ_EINVAL, "null C_out");
+  if (h->cfg.dim != 1) return fail(h, TRAJ_EDOMAIN, "C(r) binned by |i - j| is defined for the 1d chain");
+  return density_correlation_impl(h, (int)traj, C_out);
+}
+
+int traj_particle_covariance(traj_handle h, const int64_t* A, int64_t nA, const int64_t* B, int64_t nB,
+                             double* G_out) {
+  if (!h) return TRAJ_EINVAL;
+  if (!G_out || nA < 0 || nB < 0 || (nA && !A) || (nB && !B)) return fail(h, TRAJ_EINVAL, "bad region arguments");
+  std::vector<int32_t> a(nA), mask(h->L, 0);
+  for (int64_t q = 0; q < nB; ++q) {
+    if (B[q] < 0 || B[q] >= h->L) return fail(h, TRAJ_EDOMAIN, "site index outside the lattice");
+    if (mask[B[q]]) return fail(h, TRAJ_EDOMAIN, "duplicate site in region");
+    mask[B[q]] = 1;
+  }
+  std::vector<char> seen(h->L, 0);
+  for (int64_t q = 0; q < nA; ++q) {
+    if (A[q] < 0 || A[q] >= h->L) return fail(h, TRAJ_EDOMAIN, "site index outside the lattice");
+    if (mask[A[q]]) return fail(h, TRAJ_EDOMAIN, "regions overlap");
+    if (seen[A[q]]) return fail(h, TRAJ_EDOMAIN, "duplicate site in region");
+    seen[A[q]] = 1;
+    a[q] = (int32_t)A[q];
+  }
+  if (nA == 0 || nB == 0) {
+    for (int t = 0; t < h->T; ++t) G_out[t] = 0.0;
+    return 0;
+  }
+  return particle_covariance_impl(h, a, mask, G_out);
 }
 
 int traj_occupations(traj_handle h, double* n_out) {

@@ -270,3 +270,36 @@ def test_row_sharded_nccl_single_rank(P):
     assert np.abs(a.correlation(0).cpu().numpy() - b.correlation(0).cpu().numpy()).max() < 1e-12
     assert abs(a.entropy(np.arange(64))[0] - b.entropy(np.arange(64))[0]) < 1e-10
     a.close()
+
+
+@pytest.mark.parametrize("shards", [1, 4])
+def test_density_correlation_and_particle_covariance(P, shards):
+    """NEXT-3: C(r) of Eq. (2) and G_AB of Eq. (5) against the oracle (blocks of U U^dag on the
+    GEMM, deterministic binning); also through the row-sharded handle."""
+    L = 320
+    g = P.Trajectories(L, 1, "homodyne", [0.7], seed=2, shard_size=shards)
+    K = lattice.propagator_lattice(L, 1, 1.0, 0.05)
+    o = OracleTrajectory(L, 1, "homodyne", 0.7, 0.05, seed=2, traj=0, K=K)
+    g.step(25)
+    o.step(25)
+    Cr = g.density_correlation(0)
+    want = gaussian.density_correlation(o.U)
+    assert np.isnan(Cr[0])
+    assert np.abs(Cr[1:] - want[1:]).max() < 1e-13
+    A, B = np.arange(0, 80), np.arange(160, 240)
+    G = g.particle_covariance(A, B)[0]
+    assert G == pytest.approx(gaussian.particle_covariance(o.U, A, B), rel=1e-11, abs=1e-13)
+
+
+def test_particle_covariance_2d_batch(P):
+    """G_AB between the c4/c5 strips on a 2d torus, batched trajectories."""
+    A, B = workloads.strips_2d(12, 12)
+    g = P.Trajectories(12, 12, "projective", [2.86, 5.72], seed=1)
+    K = lattice.propagator_lattice(12, 12, 1.0, 0.05)
+    orc = [OracleTrajectory(12, 12, "projective", gm, 0.05, seed=1, traj=t, K=K) for t, gm in enumerate([2.86, 5.72])]
+    g.step(15)
+    for o in orc:
+        o.step(15)
+    G = g.particle_covariance(A, B)
+    for t, o in enumerate(orc):
+        assert G[t] == pytest.approx(gaussian.particle_covariance(o.U, A, B), rel=1e-11, abs=1e-13)

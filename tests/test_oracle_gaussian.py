@@ -89,3 +89,50 @@ def test_entropy_vs_fock_schmidt(A):
     U = rand_state(L, N, 7)
     F = FockSector(L, N)
     assert gaussian.entanglement_entropy(U, A) == pytest.approx(F.entropy(F.slater(U), A), abs=1e-12)
+
+
+def _fock_nn(F, psi):
+    """Connected density-density correlator <n_i n_j> - <n_i><n_j> by brute force."""
+    L = F.L
+    n = F.occupations(psi)
+    nn = np.zeros((L, L))
+    for k, b in enumerate(F.states):
+        occ = np.array([(b >> i) & 1 for i in range(L)], dtype=float)
+        nn += abs(psi[k]) ** 2 * np.outer(occ, occ)
+    return nn - np.outer(n, n)
+
+
+def test_density_correlation_vs_fock():
+    """Eq. (2): C_ij = -D_ij D_ji is the connected <n_i n_j> (Wick), checked on the many-body state."""
+    L, N = 8, 4
+    U = rand_state(L, N, 30)
+    F = FockSector(L, N)
+    nn = _fock_nn(F, F.slater(U))
+    Cr = gaussian.density_correlation(U)
+    for r in range(1, L):
+        want = np.mean([nn[i, i + r] for i in range(L - r)])
+        assert Cr[r] == pytest.approx(want, abs=1e-13)
+
+
+def test_particle_covariance_vs_fock():
+    """Eq. (5): G_AB = -Cov(N_A, N_B) on the many-body state."""
+    L, N = 8, 4
+    U = rand_state(L, N, 31)
+    F = FockSector(L, N)
+    nn = _fock_nn(F, F.slater(U))
+    A, B = [0, 1, 5], [3, 6, 7]
+    assert gaussian.particle_covariance(U, A, B) == pytest.approx(-nn[np.ix_(A, B)].sum(), abs=1e-13)
+    assert gaussian.particle_covariance(U, A, B) >= 0.0
+
+
+def test_density_correlation_product_state_and_sum_rule():
+    """Neel product state: C(r) = 0.  Sum rule of a pure Gaussian state with N particles:
+    sum_j |C_ij|^2 = n_i, so summing -C(r)(L-r) over r (both orders) gives N - sum n_i^2."""
+    U = lattice.initial_state(16)
+    assert np.all(gaussian.density_correlation(U)[1:] == 0.0)
+    U = rand_state(20, 10, 32)
+    Cr = gaussian.density_correlation(U)
+    L = 20
+    tot = -2 * sum(Cr[r] * (L - r) for r in range(1, L))
+    n = gaussian.occupations(U)
+    assert tot == pytest.approx(10 - np.sum(n ** 2), abs=1e-12)
