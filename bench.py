@@ -46,6 +46,8 @@ def parse():
     p.add_argument("--mode", choices=["traj", "shard"], default="traj",
                    help="traj: independent trajectories per GPU (weak scaling); shard: one trajectory with K and U "
                         "row-sharded over the GPUs (NCCL allgather + Gram allreduce, strong scaling)")
+    p.add_argument("--propagator", choices=["dense", "banded"], default="dense",
+                   help="dense: the north star's dense K U (default); banded: NEXT-1 stencil passes")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-budget", type=float, default=120.0, help="seconds of oracle work (reference arm)")
@@ -160,7 +162,8 @@ def run_ours(args):
     else:
         gam = [w.gammas[(rank * tpg + t) % len(w.gammas)] for t in range(tpg)]
         base = rank * tpg
-        tr = P.Trajectories(w.Lx, w.Ly, w.protocol, gam, dt=w.dt, J=w.J, seed=w.seed, traj_base=base)
+        tr = P.Trajectories(w.Lx, w.Ly, w.protocol, gam, dt=w.dt, J=w.J, seed=w.seed, traj_base=base,
+                            propagator=args.propagator)
     st = tr.stream
     for _ in range(args.warmup):
         tr.step(1)
@@ -190,20 +193,32 @@ def run_ours(args):
     else:
         ms_max = ms
     value = (1 if shard else world) * tpg * args.steps / (ms_max / 1e3)
-    # ---- roofline of the dominant kernel: the dense K.U contraction (one launch per step)
-    prop_ms = phases["propagate"][0] / args.steps
+    # ---- roofline of the dominant kernel (the phase with the largest device time):
+    #   propagate (dense K U): 8 (L/P) L N flops, 1 launch per step
+    #   gram (G = U^dag U, upper tiles): 4 (L/P) N^2 per launch, 2 per step
+    #   trmm (U <- U R^-1): 4 (L/P) N^2 per launch, 2 per step
     rows = w.L // world if shard else w.L
-    flops_launch = 8.0 * rows * w.L * w.N * tpg
-    achieved = flops_launch / (prop_ms / 1e3) / 1e12
+    kern = {"propagate": (8.0 * rows * w.L * w.N * tpg, "zgemm_dmma_kernel<N,N>: U <- K U (8 L^2 N flops)"),
+            "gram": (4.0 * rows * w.N * w.N * tpg, "zgemm_dmma_kernel<C,N>: G = U^dag U upper tiles (4 L N^2)"),
+            "trmm": (4.0 * rows * w.N * w.N * tpg, "zgemm_dmma_kernel<N,N> triangular: U <- U R^-1 (4 L N^2)")}
+    if args.propagator == "banded":
+        kern.pop("propagate")
+    dom = max(kern, key=lambda k: phases[k][0])
+    launches_per_step = max(1.0, phases[dom][1] / args.steps)
+    kern_ms = phases[dom][0] / args.steps / launches_per_step
+    flops_launch = kern[dom][0]
+    achieved = flops_launch / (kern_ms / 1e3) / 1e12
+    prop_ms = phases["propagate"][0] / args.steps
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and dom == "propagate" and not shard:
         try:
             traffic = json.load(open(tp)).get(w.name, {}).get("propagate_dram_bytes")
         except Exception:
             traffic = None
-    step_flops = {"propagate": flops_launch, "gram": 2 * 4.0 * w.L * w.N * w.N * tpg,
-                  "trmm": 2 * 4.0 * w.L * w.N * w.N * tpg, "chol": 2 * (8.0 / 3.0) * w.N ** 3 * tpg}
+    step_flops = {"propagate": 8.0 * rows * w.L * w.N * tpg if args.propagator == "dense" else 0.0,
+                  "gram": 2 * 4.0 * rows * w.N * w.N * tpg, "trmm": 2 * 4.0 * rows * w.N * w.N * tpg,
+                  "chol": (8.0 / 3.0) * w.N ** 3 * tpg}
     dense_tflops = sum(step_flops.values()) * args.steps / (ms / 1e3) / 1e12
     tr.close()
     del tr
@@ -225,12 +240,12 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "c128 (f64 arithmetic)", "data": "synthetic (Neel start, Philox randoms, seed 0)",
         "config": dict(describe(w, tpg), parallelism=(f"row-sharded K,U over {world} GPU(s) (NCCL)" if shard
-                                                      else f"trajectory-parallel dp{world}")),
+                                                      else f"trajectory-parallel dp{world}"),
+                       propagator=args.propagator),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-                     "kernel": "zgemm_dmma_kernel<N,N> (U <- K U, 8 L^2 N flops per trajectory; "
-                               "8 (L/P) L N per shard when row-sharded; phase time includes the U allgather)",
-                     "kernel_ms": prop_ms, "peak_source": FP64_PEAK_SOURCE},
+                     "kernel": kern[dom][1] + ("; per shard (L/P rows) when row-sharded" if shard else ""),
+                     "kernel_ms": kern_ms, "peak_source": FP64_PEAK_SOURCE},
         "step_dense_tflops": dense_tflops,
         "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
         "phase_launches_per_step": {k: v[1] / args.steps for k, v in phases.items()},

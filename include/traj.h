@@ -84,7 +84,16 @@ typedef struct {
   void* stream;             /* cudaStream_t the handle runs on (e.g. torch's current stream)   */
   void* workspace;          /* device memory, >= traj_workspace_bytes, 256-byte aligned        */
   size_t workspace_bytes;
+  int32_t propagator;       /* TRAJ_PROP_DENSE (the north star's dense K U) or TRAJ_PROP_BANDED */
 } traj_config;
+
+/* Propagator of step (a).  DENSE: U <- K U with the dense L x L K on the FP64 tensor pipe
+ * (8 L^2 N flops).  BANDED: K is a circulant per lattice axis whose
+ * coefficients fall below 1e-18 after a few neighbours (Bessel tail); U <- K U becomes one
+ * (1d) or two (2d, K = K_y (x) K_x) banded stencil passes of half-width W (W chosen so the
+ * dropped tail is < 1e-18; the dense path is used if 2W+1 exceeds an extent).  No L x L
+ * matrix is stored.  Not combined with row sharding in this build. */
+enum { TRAJ_PROP_DENSE = 0, TRAJ_PROP_BANDED = 1 };
 
 /* Device bytes the handle needs for cfg (the caller allocates them, e.g. with torch).
  * Validates cfg; TRAJ_ECONFIG if invalid.  Needs a CUDA device (cuSOLVER query). */

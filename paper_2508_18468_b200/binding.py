@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libtraj.so")
 TRAJ_PROJECTIVE = 0
 TRAJ_HOMODYNE = 1
 TRAJ_INIT_NEEL = 0
+TRAJ_PROP_DENSE, TRAJ_PROP_BANDED = 0, 1
 TRAJ_TRI_A_UPPER, TRAJ_TRI_A_LOWER, TRAJ_TRI_B_UPPER, TRAJ_TRI_B_LOWER, TRAJ_C_UPPER = 1, 2, 4, 8, 16
 PHASES = ("propagate", "monitor", "project", "gram", "chol", "trmm")
 STATUS = {0: "TRAJ_OK", 1: "TRAJ_EINVAL", 2: "TRAJ_ECONFIG", 3: "TRAJ_ENUMERIC", 4: "TRAJ_ECUDA",
@@ -42,6 +43,7 @@ class TrajConfig(ctypes.Structure):
         ("stream", ctypes.c_void_p),
         ("workspace", ctypes.c_void_p),
         ("workspace_bytes", ctypes.c_size_t),
+        ("propagator", ctypes.c_int32),
     ]
 
 
@@ -182,7 +184,8 @@ class Trajectories:
 
     def __init__(self, Lx: int, Ly: int = 1, protocol: str = "projective", gammas=(0.5,), dt: float = 0.05,
                  J: float = 1.0, seed: int = 0, traj_base: int = 0, device=None, stream=None,
-                 shard_size: int = 1, shard_rank: int = 0, nccl_id: bytes | None = None):
+                 shard_size: int = 1, shard_rank: int = 0, nccl_id: bytes | None = None,
+                 propagator: str = "dense"):
         import torch
         self._torch = torch
         lib_ = lib()
@@ -208,6 +211,7 @@ class Trajectories:
         self._nccl_id = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         cfg.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p) if nccl_id is not None else None
         cfg.stream = self.stream.cuda_stream
+        cfg.propagator = {"dense": TRAJ_PROP_DENSE, "banded": TRAJ_PROP_BANDED}[propagator]
         nbytes = ctypes.c_size_t(0)
         _check(lib_.traj_workspace_bytes(ctypes.byref(cfg), ctypes.byref(nbytes)))
         self.workspace = torch.empty(nbytes.value + 256, dtype=torch.uint8, device=self.device)

@@ -20,6 +20,7 @@
 #include "zgemm.h"
 #include "profiler.h"
 #include "shard.h"
+#include "banded.h"
 
 namespace traj {
 std::atomic<long long> g_kernel_launches{0};
@@ -30,6 +31,9 @@ using namespace traj;
 struct traj_ctx {
   traj_config cfg;
   ShardedCtx* sh = nullptr;        // row-sharded mode (shard_size > 1 or an NCCL communicator)
+  bool banded = false;             // TRAJ_PROP_BANDED with a band narrower than the lattice
+  int Wx = 0, Wy = 0;              // compiled half-bandwidths per axis
+  cplx* bcoef = nullptr;           // [2Wx+1 | 2Wy+1] stencil coefficients
   std::vector<double> gamma;
   int L = 0, N = 0, Lx = 0, Ly = 0, T = 0, cap = 0;
   long long ldN = 0, ldL = 0, ldcap = 0, sU = 0, sG = 0;
@@ -136,7 +140,11 @@ int validate(const traj_config* c, std::string* why) {
     if (!(g >= 0) || !isfinite(g)) return bad("gamma must be >= 0 and finite");
     if (c->protocol == TRAJ_PROJECTIVE && g * c->dt > 1.0) return bad("projective needs gamma*dt <= 1 (Q10)");
   }
-  if (c->shard_size != 1 || c->nccl_id) return shard_validate(c, why);
+  if (c->propagator != TRAJ_PROP_DENSE && c->propagator != TRAJ_PROP_BANDED) return bad("unknown propagator");
+  if (c->shard_size != 1 || c->nccl_id) {
+    if (c->propagator == TRAJ_PROP_BANDED) return bad("the banded propagator is not combined with row sharding");
+    return shard_validate(c, why);
+  }
   if (c->shard_rank != 0) return bad("shard_rank must be 0 without sharding");
   return 0;
 }
@@ -148,6 +156,30 @@ int click_capacity(long long L, const traj_config* c) {
   for (long long t = 0; t < c->n_traj; ++t) pmax = std::max(pmax, c->gamma[t] * c->dt);
   const double m = L * pmax, sd = sqrt(L * pmax * (1 - pmax));
   return (int)std::min<long long>(L, (long long)ceil(m + 12 * sd + 64));
+}
+
+std::vector<std::complex<double>> ring_coefficients(int n, double J, double dt);
+
+// half-bandwidth of a ring propagator: smallest w with sum_{w < |d| <= n/2} |c_d| < 1e-18
+int band_width(const std::vector<std::complex<double>>& c) {
+  const int n = (int)c.size();
+  double tail = 0.0;
+  for (int d = n / 2; d >= 1; --d) {
+    tail += std::abs(c[d]) + (n - d != d ? std::abs(c[n - d]) : 0.0);
+    if (tail >= 1e-18) return d;
+  }
+  return 0;
+}
+
+// compiled widths (Wx, Wy) for the banded propagator, or false if it does not fit
+bool banded_widths(const traj_config* c, int* Wx, int* Wy) {
+  if (c->propagator != TRAJ_PROP_BANDED) return false;
+  const int wx = banded_template_width(band_width(ring_coefficients((int)c->Lx, c->J, c->dt)));
+  const int wy = c->Ly > 1 ? banded_template_width(band_width(ring_coefficients((int)c->Ly, c->J, c->dt))) : 0;
+  if (wx < 0 || wy < 0 || 2 * wx + 1 > c->Lx || (c->Ly > 1 && 2 * wy + 1 > c->Ly)) return false;
+  *Wx = wx;
+  *Wy = wy;
+  return true;
 }
 
 size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
@@ -168,7 +200,9 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
   h->ldcap = ldcap;
   h->sU = L * ldN;
   h->sG = N * ldN;
-  lay.take(h->K, (size_t)L * ldL * 16);
+  h->banded = banded_widths(c, &h->Wx, &h->Wy);
+  if (h->banded) lay.take(h->bcoef, (size_t)(2 * h->Wx + 2 * h->Wy + 2) * 16);
+  else lay.take(h->K, (size_t)L * ldL * 16);
   lay.take(h->U[0], (size_t)T * L * ldN * 16);
   lay.take(h->U[1], (size_t)T * L * ldN * 16);
   lay.take(h->G, (size_t)T * N * ldN * 16);
@@ -356,15 +390,27 @@ int projective(traj_ctx* h, cplx* U) {
 int one_step(traj_ctx* h) {
   cplx* Uc = h->U[h->cur];
   cplx* Un = h->U[1 - h->cur];
+  cplx* Us = Un;      // where the propagated state lands
   {
     Phase p(&h->prof, h->st, TRAJ_PH_PROPAGATE);
-    // U <- K U  (K shared across the batch: stride 0)
-    TRY(zgemm(h->st, 0, 0, h->L, h->N, h->L, 1.0, 0.0, h->K, h->ldL, 0, Uc, h->ldN, h->sU, 0.0, Un, h->ldN, h->sU,
-              h->T, 0, &h->err));
+    if (h->banded) {
+      // 1d: one pass along the ring; 2d: x pass (lines = rows y) then y pass (lines = columns x)
+      TRY(banded_pass(h->st, Uc, Un, h->ldN, h->sU, h->N, h->T, h->Lx, h->Ly, h->Lx, 1, h->bcoef, h->Wx, &h->err));
+      if (h->Ly > 1) {
+        TRY(banded_pass(h->st, Un, Uc, h->ldN, h->sU, h->N, h->T, h->Ly, h->Lx, 1, h->Lx, h->bcoef + 2 * h->Wx + 1,
+                        h->Wy, &h->err));
+        Us = Uc;
+      }
+    } else {
+      // U <- K U  (K shared across the batch: stride 0)
+      TRY(zgemm(h->st, 0, 0, h->L, h->N, h->L, 1.0, 0.0, h->K, h->ldL, 0, Uc, h->ldN, h->sU, 0.0, Un, h->ldN, h->sU,
+                h->T, 0, &h->err));
+    }
   }
+  cplx* Ut = Us == Un ? Uc : Un;
   if (h->cfg.protocol == TRAJ_HOMODYNE) {
     Phase p(&h->prof, h->st, TRAJ_PH_MONITOR);
-    TRY(row_monitor(h->st, Un, h->ldN, h->sU, h->L, h->N, h->T, 1, h->step, h->cfg.traj_base, h->cfg.seed,
+    TRY(row_monitor(h->st, Us, h->ldN, h->sU, h->L, h->N, h->T, 1, h->step, h->cfg.traj_base, h->cfg.seed,
                     h->gamma_dev, h->cfg.dt, nullptr, &h->err));
   } else {
     {
@@ -372,12 +418,12 @@ int one_step(traj_ctx* h) {
       TRY(click_draw(h->st, h->L, h->T, h->step, h->cfg.traj_base, h->cfg.seed, h->gamma_dev, h->cfg.dt, h->flags,
                      &h->err));
     }
-    int s = projective(h, Un);
+    int s = projective(h, Us);
     if (s) return s;
   }
-  int s = cqr2(h, Un, Uc);
+  int s = cqr2(h, Us, Ut);
   if (s) return s;
-  h->cur = 1 - h->cur;
+  h->cur = Us == h->U[0] ? 0 : 1;
   h->step += 1;
   return 0;
 }
@@ -653,7 +699,20 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
       cudaMemcpyAsync(h->sites, sites.data(), sites.size() * 4, cudaMemcpyHostToDevice, h->st) != cudaSuccess ||
       cudaMemcpyAsync(h->gamma_dev, h->gamma.data(), h->T * 8, cudaMemcpyHostToDevice, h->st) != cudaSuccess)
     return bail(TRAJ_ECUDA, "upload");
-  if (build_k(h->st, h->K, h->ldL, h->Lx, h->Ly, h->kcoef, h->kcoef + h->Lx, &e)) return bail(TRAJ_ECUDA, e);
+  if (h->banded) {
+    std::vector<std::complex<double>> bc;
+    auto axis = [&](int n, int W) {
+      std::vector<std::complex<double>> c = ring_coefficients(n, cfg->J, cfg->dt);
+      for (int d = -W; d <= W; ++d) bc.push_back(c[((d % n) + n) % n]);
+    };
+    axis(h->Lx, h->Wx);
+    if (h->Ly > 1) axis(h->Ly, h->Wy);
+    else bc.push_back(1.0);
+    if (cudaMemcpyAsync(h->bcoef, bc.data(), bc.size() * 16, cudaMemcpyHostToDevice, h->st) != cudaSuccess)
+      return bail(TRAJ_ECUDA, "upload band");
+  } else if (build_k(h->st, h->K, h->ldL, h->Lx, h->Ly, h->kcoef, h->kcoef + h->Lx, &e)) {
+    return bail(TRAJ_ECUDA, e);
+  }
   if (init_state(h->st, h->U[0], h->ldN, h->sU, h->sites, h->N, h->T, &e)) return bail(TRAJ_ECUDA, e);
   if (cudaStreamSynchronize(h->st) != cudaSuccess) return bail(TRAJ_ECUDA, "init sync");
   *out = h;

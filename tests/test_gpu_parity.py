@@ -303,3 +303,34 @@ def test_particle_covariance_2d_batch(P):
     G = g.particle_covariance(A, B)
     for t, o in enumerate(orc):
         assert G[t] == pytest.approx(gaussian.particle_covariance(o.U, A, B), rel=1e-11, abs=1e-13)
+
+
+@pytest.mark.parametrize("Lx,Ly,protocol,gam", [(240, 1, "homodyne", 1.0), (200, 1, "projective", 3.0),
+                                                (14, 10, "homodyne", 2.0), (12, 12, "projective", 2.86)])
+def test_banded_propagator_matches_dense_oracle(P, Lx, Ly, protocol, gam):
+    """NEXT-1: banded circulant passes (1d) / K_y (x) K_x as two passes (2d) against the oracle's
+    dense exact K: the dropped Bessel tail is below 1e-18, so the lockstep bar is unchanged."""
+    lockstep_kw = dict(seed=6)
+    gpu = P.Trajectories(Lx, Ly, protocol, [gam, gam / 2], propagator="banded", **lockstep_kw)
+    K = lattice.propagator_lattice(Lx, Ly, 1.0, 0.05)
+    orc = [OracleTrajectory(Lx, Ly, protocol, g, 0.05, seed=6, traj=t, K=K) for t, g in enumerate([gam, gam / 2])]
+    A = np.arange(Lx * Ly // 2)
+    for s in range(30):
+        gpu.step(1)
+        for o in orc:
+            o.step(1)
+    S = gpu.entropy(A)
+    for t, o in enumerate(orc):
+        assert np.abs(gpu.correlation(t).cpu().numpy() - o.correlation()).max() < C_TOL
+        assert abs(S[t] - o.entropy(A)) < S_TOL
+
+
+def test_banded_free_evolution_closed_form_full_c3(P):
+    """configs[2] size with the banded propagator: finite-L closed form after 40 steps."""
+    L, steps, dt = 16384, 40, 0.05
+    g = P.Trajectories(L, 1, "projective", [0.0], dt=dt, propagator="banded")
+    g.step(steps)
+    n = g.occupations()[0].cpu().numpy()
+    m = np.arange(L)
+    want = 0.5 + 0.5 * (-1.0) ** m * np.mean(np.cos(4 * steps * dt * np.cos(2 * np.pi * m / L)))
+    assert np.abs(n - want).max() < 1e-12
