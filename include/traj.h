@@ -219,6 +219,14 @@ int traj_zgemm(void* stream, int opA, int opB, int64_t M, int64_t N, int64_t K,
                double beta, void* C, int64_t ldc, int64_t strideC,
                int64_t batch, int flags);
 
+/* Complex multiplication scheme of every contraction (process-wide): 1 = 3M (Gauss, the
+ * default): A_r B_r, A_i B_i and (A_r + A_i)(B_r + B_i) as three real DMMA products, 6mnk
+ * tensor-pipe flops per 8mnk algorithmic, FP64 throughout, the usual ZGEMM3M error bound for
+ * the imaginary part; 0 = 4M: two real DMMA products over an interleaved (re, im) k axis,
+ * 8mnk tensor flops.  Initial value from the environment: TRAJ_ZGEMM_3M=0 selects 4M. */
+int traj_set_zgemm_algorithm(int algo);
+int traj_get_zgemm_algorithm(void);
+
 /* traj_chol_inverse: for each b, G_b (n x n Hermitian positive definite; only the
  * upper triangle is read) = R^dag R with R upper triangular; writes X_b = R^-1
  * (upper triangle; the strict lower triangle is set to zero).  G_b's strict lower

@@ -13,6 +13,8 @@ from .binding import (  # noqa: F401
     load_library,
     traj_chol_inverse,
     traj_kernel_launches,
+    traj_get_zgemm_algorithm,
     traj_nccl_unique_id,
+    traj_set_zgemm_algorithm,
     traj_zgemm,
 )

@@ -88,6 +88,8 @@ _SIGS = {
     "traj_shard_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                        ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "traj_nccl_unique_id": (ctypes.c_int, [_P]),
+    "traj_set_zgemm_algorithm": (ctypes.c_int, [ctypes.c_int]),
+    "traj_get_zgemm_algorithm": (ctypes.c_int, []),
     "traj_chol_scratch_bytes": (ctypes.c_size_t, [_I64, _I64]),
     "traj_chol_inverse": (ctypes.c_int, [_P, _I64, _P, _I64, _I64, _P, _I64, _I64, _I64, _P, _P]),
 }
@@ -126,6 +128,16 @@ def traj_kernel_launches() -> int:
 
 def _ptr(t) -> int:
     return int(t.data_ptr())
+
+
+def traj_set_zgemm_algorithm(algo: str | int):
+    """"4m" (0, default) or "3m" (1) complex multiplication in every contraction (process-wide)."""
+    a = {"4m": 0, "3m": 1}.get(algo, algo) if isinstance(algo, str) else int(algo)
+    _check(lib().traj_set_zgemm_algorithm(a))
+
+
+def traj_get_zgemm_algorithm() -> str:
+    return "3m" if lib().traj_get_zgemm_algorithm() == 1 else "4m"
 
 
 def traj_nccl_unique_id() -> bytes:

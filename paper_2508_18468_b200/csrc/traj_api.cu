@@ -939,6 +939,14 @@ int traj_zgemm(void* stream, int opA, int opB, int64_t M, int64_t N, int64_t K, 
   return s ? fail(nullptr, s, e) : 0;
 }
 
+int traj_set_zgemm_algorithm(int algo) {
+  if (algo != 0 && algo != 1) return fail(nullptr, TRAJ_EINVAL, "algorithm must be 0 (4M) or 1 (3M)");
+  set_zgemm_algorithm(algo);
+  return 0;
+}
+
+int traj_get_zgemm_algorithm(void) { return zgemm_algorithm(); }
+
 int traj_nccl_unique_id(void* out128) {
   if (!out128) return fail(nullptr, TRAJ_EINVAL, "null out");
   std::string e;

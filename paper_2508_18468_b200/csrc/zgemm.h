@@ -19,4 +19,9 @@ int zgemm(cudaStream_t st, int opA, int opB, long long M, long long N, long long
           long long strideB, double beta, cplx* C, long long ldc, long long strideC, long long batch, int flags,
           std::string* err);
 
+// 0: 4M (two real MMAs over an interleaved k axis, default); 1: 3M (Gauss, three real MMAs).
+// Initialised from the environment (TRAJ_ZGEMM_3M=1); process-wide.
+int zgemm_algorithm();
+void set_zgemm_algorithm(int algo);
+
 }  // namespace traj
