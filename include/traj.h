@@ -53,7 +53,11 @@ typedef enum {
   TRAJ_EDOMAIN = 6    /* overlapping regions, site index outside the lattice              */
 } traj_status;
 
-enum { TRAJ_PROJECTIVE = 0, TRAJ_HOMODYNE = 1 };
+/* Protocols.  TRAJ_HOMODYNE: Eq. (A3) in exact split form (K, then the diagonal factor).
+ * TRAJ_HOMODYNE_RK4: the paper-literal integrator of P:209 -- classical RK4 on
+ * dU/dt = M U, M = -i H~ + diag(dW/dt) + gamma diag(2 <n>_t - 1) held fixed over the step
+ * (dW and <n>_t at time t), H~ applied as a nearest-neighbour stencil, then CholeskyQR2. */
+enum { TRAJ_PROJECTIVE = 0, TRAJ_HOMODYNE = 1, TRAJ_HOMODYNE_RK4 = 2 };
 /* Initial state (Q1, Q2): sites with (x + y) even occupied -- the Neel state
  * |1010...> of P:173/P:198 (0-based even sites) in 1d, the checkerboard in 2d. */
 enum { TRAJ_INIT_NEEL = 0 };
@@ -64,7 +68,8 @@ typedef struct {
                                have x+y even); 2d needs Lx, Ly >= 3; site = y*Lx + x (Q2)     */
   int64_t N;                /* particle number, must equal L/2                         */
   double J, dt;             /* hopping J (J = 1) and time step dt > 0 (0.05)     */
-  int32_t protocol;         /* TRAJ_PROJECTIVE or TRAJ_HOMODYNE       */
+  int32_t protocol;         /* TRAJ_PROJECTIVE, TRAJ_HOMODYNE or TRAJ_HOMODYNE_RK4
+                                                                                  */
   int32_t init;             /* TRAJ_INIT_NEEL                                                  */
   uint64_t seed;            /* Philox4x32-10 key (lo, hi words), Q9                            */
   int64_t n_traj;           /* trajectories held by this handle, >= 1                          */

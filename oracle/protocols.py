@@ -152,3 +152,26 @@ def projective_step(U, K, gamma: float, dt: float, step: int, traj: int, seed: i
     occ = sample_outcomes_paper(D_SS, u1[S])
     U = project_block(U, S[occ], S[~occ])
     return U, S, occ
+
+
+# ----------------------------------------------------------------------------- NEXT-2: RK4 QSD
+def qsd_generator(H, n, dW, gamma: float, dt: float):
+    """M of Eq. (A3) divided by dt: dU/dt = M U with
+    M = -i H~ + diag(dW/dt) + gamma diag(2 <n>_t - 1), held fixed over the step
+    (dW and <n>_t taken at time t)."""
+    return -1j * H + np.diag(dW / dt + gamma * (2.0 * n - 1.0))
+
+
+def homodyne_step_rk4(U, H, gamma: float, dt: float, step: int, traj: int, seed: int):
+    """Paper-literal QSD step: classical fourth-order Runge-Kutta on dU/dt = M U over dt
+    with the Gaussian noise dW_i = sqrt(gamma dt) z_i held across the four stages, then QR."""
+    n = gaussian.occupations(U)
+    u0, u1 = site_uniforms(U.shape[0], step, traj, seed)
+    dW = np.sqrt(gamma * dt) * gaussian_from_uniforms(u0, u1)
+    M = qsd_generator(H, n, dW, gamma, dt)
+    k1 = M @ U
+    k2 = M @ (U + 0.5 * dt * k1)
+    k3 = M @ (U + 0.5 * dt * k2)
+    k4 = M @ (U + dt * k3)
+    U = U + (dt / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
+    return gaussian.orthonormalize(U)

@@ -14,6 +14,7 @@ import numpy as np
 from . import gaussian, lattice, protocols
 
 HOMODYNE = "homodyne"
+HOMODYNE_RK4 = "homodyne_rk4"      # NEXT-2: the paper's RK4 integrator
 PROJECTIVE = "projective"
 
 
@@ -33,7 +34,9 @@ class OracleTrajectory:
     last_clicks: tuple = field(init=False, default=())
 
     def __post_init__(self):
-        if self.K is None:
+        if self.protocol == HOMODYNE_RK4:
+            self.H = lattice.hopping_matrix(self.Lx, self.Ly, self.J)
+        elif self.K is None:
             self.K = lattice.propagator_lattice(self.Lx, self.Ly, self.J, self.dt)
         self.U = lattice.initial_state(self.Lx, self.Ly)
 
@@ -46,6 +49,8 @@ class OracleTrajectory:
             s = self.step_index
             if self.protocol == HOMODYNE:
                 self.U = protocols.homodyne_step(self.U, self.K, self.gamma, self.dt, s, self.traj, self.seed)
+            elif self.protocol == HOMODYNE_RK4:
+                self.U = protocols.homodyne_step_rk4(self.U, self.H, self.gamma, self.dt, s, self.traj, self.seed)
             else:
                 self.U, S, occ = protocols.projective_step(self.U, self.K, self.gamma, self.dt, s,
                                                            self.traj, self.seed, form=form)

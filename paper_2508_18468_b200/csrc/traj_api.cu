@@ -21,6 +21,7 @@
 #include "profiler.h"
 #include "shard.h"
 #include "banded.h"
+#include "qsd_rk4.h"
 
 namespace traj {
 std::atomic<long long> g_kernel_launches{0};
@@ -34,6 +35,8 @@ struct traj_ctx {
   bool banded = false;             // TRAJ_PROP_BANDED with a band narrower than the lattice
   int Wx = 0, Wy = 0;              // compiled half-bandwidths per axis
   cplx* bcoef = nullptr;           // [2Wx+1 | 2Wy+1] stencil coefficients
+  cplx* Wrk = nullptr;             // RK4 QSD scratch, shaped like U
+  double* dbuf = nullptr;          // RK4 QSD diagonal generator [T][L]
   std::vector<double> gamma;
   int L = 0, N = 0, Lx = 0, Ly = 0, T = 0, cap = 0;
   long long ldN = 0, ldL = 0, ldcap = 0, sU = 0, sG = 0;
@@ -130,7 +133,8 @@ int validate(const traj_config* c, std::string* why) {
   if (c->N != L / 2) return bad("N must equal L/2 (P:43)");
   if (!(c->dt > 0) || !isfinite(c->dt)) return bad("dt must be > 0");
   if (!isfinite(c->J)) return bad("J must be finite");
-  if (c->protocol != TRAJ_PROJECTIVE && c->protocol != TRAJ_HOMODYNE) return bad("unknown protocol");
+  if (c->protocol != TRAJ_PROJECTIVE && c->protocol != TRAJ_HOMODYNE && c->protocol != TRAJ_HOMODYNE_RK4)
+    return bad("unknown protocol");
   if (c->init != TRAJ_INIT_NEEL) return bad("unknown init");
   if (c->n_traj < 1 || c->n_traj > 65535) return bad("n_traj must be in [1, 65535]");
   if (c->traj_base < 0 || c->traj_base + c->n_traj > (1ll << 32)) return bad("trajectory ids must fit 32 bits");
@@ -143,6 +147,7 @@ int validate(const traj_config* c, std::string* why) {
   if (c->propagator != TRAJ_PROP_DENSE && c->propagator != TRAJ_PROP_BANDED) return bad("unknown propagator");
   if (c->shard_size != 1 || c->nccl_id) {
     if (c->propagator == TRAJ_PROP_BANDED) return bad("the banded propagator is not combined with row sharding");
+    if (c->protocol == TRAJ_HOMODYNE_RK4) return bad("the RK4 QSD protocol is not combined with row sharding");
     return shard_validate(c, why);
   }
   if (c->shard_rank != 0) return bad("shard_rank must be 0 without sharding");
@@ -201,8 +206,15 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
   h->sU = L * ldN;
   h->sG = N * ldN;
   h->banded = banded_widths(c, &h->Wx, &h->Wy);
-  if (h->banded) lay.take(h->bcoef, (size_t)(2 * h->Wx + 2 * h->Wy + 2) * 16);
-  else lay.take(h->K, (size_t)L * ldL * 16);
+  if (c->protocol == TRAJ_HOMODYNE_RK4) {     // stencil generator: no K
+    h->banded = false;
+    lay.take(h->Wrk, (size_t)T * L * ldN * 16);
+    lay.take(h->dbuf, (size_t)T * L * 8);
+  } else if (h->banded) {
+    lay.take(h->bcoef, (size_t)(2 * h->Wx + 2 * h->Wy + 2) * 16);
+  } else {
+    lay.take(h->K, (size_t)L * ldL * 16);
+  }
   lay.take(h->U[0], (size_t)T * L * ldN * 16);
   lay.take(h->U[1], (size_t)T * L * ldN * 16);
   lay.take(h->G, (size_t)T * N * ldN * 16);
@@ -391,6 +403,24 @@ int one_step(traj_ctx* h) {
   cplx* Uc = h->U[h->cur];
   cplx* Un = h->U[1 - h->cur];
   cplx* Us = Un;      // where the propagated state lands
+  if (h->cfg.protocol == TRAJ_HOMODYNE_RK4) {
+    // NEXT-2: <n>_t from U(t), then RK4 (= Taylor-4 of exp(dt M)) on the Eq. (A3) generator
+    {
+      Phase p(&h->prof, h->st, TRAJ_PH_MONITOR);
+      TRY(row_monitor(h->st, Uc, h->ldN, h->sU, h->L, h->N, h->T, 0, h->step, h->cfg.traj_base, h->cfg.seed,
+                      h->gamma_dev, h->cfg.dt, h->nbuf, &h->err));
+    }
+    {
+      Phase p(&h->prof, h->st, TRAJ_PH_PROPAGATE);
+      TRY(qsd_rk4_propagate(h->st, Uc, h->Wrk, Un, h->ldN, h->sU, h->Lx, h->Ly, h->N, h->T, h->nbuf, h->dbuf,
+                            h->step, h->cfg.traj_base, h->cfg.seed, h->gamma_dev, h->cfg.J, h->cfg.dt, &h->err));
+    }
+    int s = cqr2(h, Un, Uc);
+    if (s) return s;
+    h->cur = 1 - h->cur;
+    h->step += 1;
+    return 0;
+  }
   {
     Phase p(&h->prof, h->st, TRAJ_PH_PROPAGATE);
     if (h->banded) {
@@ -710,7 +740,8 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
     else bc.push_back(1.0);
     if (cudaMemcpyAsync(h->bcoef, bc.data(), bc.size() * 16, cudaMemcpyHostToDevice, h->st) != cudaSuccess)
       return bail(TRAJ_ECUDA, "upload band");
-  } else if (build_k(h->st, h->K, h->ldL, h->Lx, h->Ly, h->kcoef, h->kcoef + h->Lx, &e)) {
+  } else if (cfg->protocol != TRAJ_HOMODYNE_RK4 &&
+             build_k(h->st, h->K, h->ldL, h->Lx, h->Ly, h->kcoef, h->kcoef + h->Lx, &e)) {
     return bail(TRAJ_ECUDA, e);
   }
   if (init_state(h->st, h->U[0], h->ldN, h->sU, h->sites, h->N, h->T, &e)) return bail(TRAJ_ECUDA, e);

@@ -334,3 +334,11 @@ def test_banded_free_evolution_closed_form_full_c3(P):
     m = np.arange(L)
     want = 0.5 + 0.5 * (-1.0) ** m * np.mean(np.cos(4 * steps * dt * np.cos(2 * np.pi * m / L)))
     assert np.abs(n - want).max() < 1e-12
+
+
+@pytest.mark.parametrize("Lx,Ly", [(200, 1), (10, 8)])
+def test_rk4_qsd_protocol_matches_oracle(P, Lx, Ly):
+    """NEXT-2: the paper-literal QSD integrator (RK4 on the Eq. A3 generator) in lockstep
+    with the oracle's literal RK4 stages (the GPU evaluates the same polynomial in Horner form)."""
+    A = np.arange(Lx * Ly // 2)
+    lockstep(P, Lx, Ly, "homodyne_rk4", [0.3, 2.0], 60, 20, [A], seed=12)

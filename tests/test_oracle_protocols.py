@@ -193,3 +193,67 @@ def test_zeno_pinning():
     weak = OracleTrajectory(24, 1, "homodyne", 0.1, 0.05, seed=4)
     weak.step(40)
     assert tr.entropy(np.arange(12)) < 0.2 < weak.entropy(np.arange(12))
+
+
+# ---------------------------------------------------------------- NEXT-2: RK4 QSD
+def test_rk4_step_is_fourth_order_taylor_of_expm():
+    """One RK4 step of the linear ODE dU/dt = M U equals exp(dt M) U up to the Taylor remainder
+    |dt M|^5 / 5! (classical RK4 on a linear autonomous system), with M the Eq. (A3) generator."""
+    import scipy.linalg
+    L, gamma, dt = 12, 1.5, 0.05
+    H = lattice.hopping_matrix(L)
+    U = rand_state(L, 6, 40)
+    n = gaussian.occupations(U)
+    u0, u1 = site_uniforms(L, 3, 0, 1)
+    dW = np.sqrt(gamma * dt) * gaussian_from_uniforms(u0, u1)
+    M = protocols.qsd_generator(H, n, dW, gamma, dt)
+    k1 = M @ U
+    k2 = M @ (U + 0.5 * dt * k1)
+    k3 = M @ (U + 0.5 * dt * k2)
+    k4 = M @ (U + dt * k3)
+    rk = U + dt / 6 * (k1 + 2 * k2 + 2 * k3 + k4)
+    ex = scipy.linalg.expm(dt * M) @ U
+    nrm = np.linalg.norm(dt * M, 2)
+    bound = nrm ** 5 / 120 * np.exp(nrm) * np.linalg.norm(U, 2)
+    assert np.linalg.norm(rk - ex, 2) <= bound
+    # and the 4th-order Taylor polynomial is the same map (RK4 == Taylor-4 for linear M)
+    X = dt * M
+    tay = U + X @ U + X @ X @ U / 2 + X @ X @ X @ U / 6 + X @ X @ X @ X @ U / 24
+    assert np.abs(rk - tay).max() < 1e-14
+
+
+def test_rk4_free_evolution_converges_at_fourth_order():
+    """gamma = 0: RK4 + QR against the finite-L closed form; halving dt cuts the error ~16x."""
+    L, T = 32, 2.0
+    m = np.arange(L)
+    want = 0.5 + 0.5 * (-1.0) ** m * np.mean(np.cos(4 * T * np.cos(2 * np.pi * m / L)))
+    errs = []
+    for dt in (0.1, 0.05):
+        tr = OracleTrajectory(L, 1, "homodyne_rk4", 0.0, dt, seed=0)
+        tr.step(int(round(T / dt)))
+        errs.append(np.abs(gaussian.occupations(tr.U) - want).max())
+    assert errs[1] < 1e-5
+    assert 10 < errs[0] / errs[1] < 24
+
+
+def test_rk4_qsd_step_vs_fock_exponential():
+    """Eq. (A3) on the many-body state: exp(sum_ij X_ij c_i^dag c_j)|psi> (X = dt M) is the Slater
+    state of exp(X) U exactly; the RK4 step approximates it within the Taylor remainder
+    |X|^5 e^|X| / 5! (the O(sqrt(dt)) noise term makes |X| ~ 0.5 at dt = 0.05)."""
+    import scipy.linalg
+    L, N, gamma, dt = 8, 4, 1.0, 0.05
+    H = lattice.hopping_matrix(L)
+    U = rand_state(L, N, 41)
+    F = FockSector(L, N)
+    n = gaussian.occupations(U)
+    u0, u1 = site_uniforms(L, 0, 0, 9)
+    dW = np.sqrt(gamma * dt) * gaussian_from_uniforms(u0, u1)
+    X = dt * protocols.qsd_generator(H, n, dW, gamma, dt)
+    psi = scipy.linalg.expm(F.hamiltonian(X)) @ F.slater(U)      # sum_ij X_ij c_i^dag c_j
+    psi /= np.linalg.norm(psi)
+    Ue = gaussian.orthonormalize(scipy.linalg.expm(X) @ U)
+    assert np.abs(F.correlation(psi) - gaussian.correlation_paper(Ue)).max() < 1e-12
+    U2 = protocols.homodyne_step_rk4(U, H, gamma, dt, 0, 0, 9)
+    x = np.linalg.norm(X, 2)
+    drift = np.linalg.norm(gaussian.correlation(U2) - gaussian.correlation(Ue), 2)
+    assert drift < 4 * x ** 5 * np.exp(x) / 120 * np.linalg.cond(scipy.linalg.expm(X))
