@@ -48,6 +48,9 @@ def parse():
                         "row-sharded over the GPUs (NCCL allgather + Gram allreduce, strong scaling)")
     p.add_argument("--propagator", choices=["dense", "banded"], default="dense",
                    help="dense: the north star's dense K U (default); banded: NEXT-1 stencil passes")
+    p.add_argument("--protocol", default=None,
+                   help="override the config's protocol: projective | homodyne | homodyne_rk4 (NEXT-2) | "
+                        "projective_events (NEXT-4)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-budget", type=float, default=120.0, help="seconds of oracle work (reference arm)")
@@ -56,6 +59,9 @@ def parse():
 
 def workload(args):
     w = workloads.CONFIGS[args.config]()
+    if args.protocol:
+        import dataclasses
+        w = dataclasses.replace(w, protocol=args.protocol)
     tpg = args.traj_per_gpu or (1 if args.config in ("c3", "c5") else 8)
     return w, tpg
 

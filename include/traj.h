@@ -57,7 +57,13 @@ typedef enum {
  * TRAJ_HOMODYNE_RK4: the paper-literal integrator of P:209 -- classical RK4 on
  * dU/dt = M U, M = -i H~ + diag(dW/dt) + gamma diag(2 <n>_t - 1) held fixed over the step
  * (dW and <n>_t at time t), H~ applied as a nearest-neighbour stencil, then CholeskyQR2. */
-enum { TRAJ_PROJECTIVE = 0, TRAJ_HOMODYNE = 1, TRAJ_HOMODYNE_RK4 = 2 };
+/* TRAJ_PROJECTIVE_EVENTS: the paper-literal event-driven PM of P:173-195 --
+ * Poisson waiting times -ln(eta)/(gamma N), one uniformly chosen site per event, Born outcome
+ * against p_c, the exact rank-1 update of Eq. (A1)/(A2) in orbital form; traj_step advances the
+ * time by dt per step, processing every event inside the window, then CholeskyQR2.  Event e of
+ * trajectory tau draws Philox counters (e_lo, e_hi, tau, 1) and (e_lo, e_hi, tau, 2).
+ * traj_last_clicks reports the events of the last window and how many were "occupied". */
+enum { TRAJ_PROJECTIVE = 0, TRAJ_HOMODYNE = 1, TRAJ_HOMODYNE_RK4 = 2, TRAJ_PROJECTIVE_EVENTS = 3 };
 /* Initial state (Q1, Q2): sites with (x + y) even occupied -- the Neel state
  * |1010...> of P:173/P:198 (0-based even sites) in 1d, the checkerboard in 2d. */
 enum { TRAJ_INIT_NEEL = 0 };

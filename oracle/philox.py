@@ -69,3 +69,15 @@ def site_uniforms(L: int, step: int, traj: int, seed: int):
 def gaussian_from_uniforms(u0, u1):
     """Box-Muller (reading Q8): z = sqrt(-2 ln(1-u0)) cos(2 pi u1), one z per site."""
     return np.sqrt(-2.0 * np.log(1.0 - u0)) * np.cos(2.0 * np.pi * u1)
+
+
+def event_uniforms(event: int, traj: int, seed: int):
+    """The three uniforms of measurement event number `event` of the event-driven PM protocol
+    (NEXT-4, P:173-174): counter (event_lo, event_hi, traj, 1) -> (u_eta, u_site),
+    counter (event_lo, event_hi, traj, 2) -> u_pc (53-bit each, same mapping as site_uniforms)."""
+    key = (seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF)
+    c = np.array([[event & 0xFFFFFFFF, (event >> 32) & 0xFFFFFFFF, traj, 1],
+                  [event & 0xFFFFFFFF, (event >> 32) & 0xFFFFFFFF, traj, 2]], dtype=np.uint64)
+    x = philox4x32_10(c, key)
+    return float(_u53(x[0:1, 0], x[0:1, 1])[0]), float(_u53(x[0:1, 2], x[0:1, 3])[0]), \
+        float(_u53(x[1:2, 0], x[1:2, 1])[0])

@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libtraj.so")
 TRAJ_PROJECTIVE = 0
 TRAJ_HOMODYNE = 1
 TRAJ_HOMODYNE_RK4 = 2
+TRAJ_PROJECTIVE_EVENTS = 3
 TRAJ_INIT_NEEL = 0
 TRAJ_PROP_DENSE, TRAJ_PROP_BANDED = 0, 1
 TRAJ_TRI_A_UPPER, TRAJ_TRI_A_LOWER, TRAJ_TRI_B_UPPER, TRAJ_TRI_B_LOWER, TRAJ_C_UPPER = 1, 2, 4, 8, 16
@@ -215,7 +216,7 @@ class Trajectories:
         cfg.Lx, cfg.Ly, cfg.N = self.Lx, self.Ly, self.N
         cfg.J, cfg.dt = float(J), float(dt)
         cfg.protocol = {"projective": TRAJ_PROJECTIVE, "homodyne": TRAJ_HOMODYNE,
-                        "homodyne_rk4": TRAJ_HOMODYNE_RK4}[protocol]
+                        "homodyne_rk4": TRAJ_HOMODYNE_RK4, "projective_events": TRAJ_PROJECTIVE_EVENTS}[protocol]
         cfg.init = TRAJ_INIT_NEEL
         cfg.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
         cfg.n_traj = self.n_traj

@@ -22,6 +22,7 @@
 #include "shard.h"
 #include "banded.h"
 #include "qsd_rk4.h"
+#include "pm_events.h"
 
 namespace traj {
 std::atomic<long long> g_kernel_launches{0};
@@ -36,6 +37,14 @@ struct traj_ctx {
   int Wx = 0, Wy = 0;              // compiled half-bandwidths per axis
   cplx* bcoef = nullptr;           // [2Wx+1 | 2Wy+1] stencil coefficients
   cplx* Wrk = nullptr;             // RK4 QSD scratch, shaped like U
+  // event-driven PM (NEXT-4)
+  std::vector<long long> ev_count;
+  std::vector<double> ev_tnext, ev_tcur;
+  cplx* yhat = nullptr;
+  double* ev_coef = nullptr;
+  int32_t* occ_count = nullptr;
+  cplx* taps_dev = nullptr;
+  std::complex<double>* taps_host = nullptr;   // pinned staging
   double* dbuf = nullptr;          // RK4 QSD diagonal generator [T][L]
   std::vector<double> gamma;
   int L = 0, N = 0, Lx = 0, Ly = 0, T = 0, cap = 0;
@@ -133,7 +142,8 @@ int validate(const traj_config* c, std::string* why) {
   if (c->N != L / 2) return bad("N must equal L/2 (P:43)");
   if (!(c->dt > 0) || !isfinite(c->dt)) return bad("dt must be > 0");
   if (!isfinite(c->J)) return bad("J must be finite");
-  if (c->protocol != TRAJ_PROJECTIVE && c->protocol != TRAJ_HOMODYNE && c->protocol != TRAJ_HOMODYNE_RK4)
+  if (c->protocol != TRAJ_PROJECTIVE && c->protocol != TRAJ_HOMODYNE && c->protocol != TRAJ_HOMODYNE_RK4 &&
+      c->protocol != TRAJ_PROJECTIVE_EVENTS)
     return bad("unknown protocol");
   if (c->init != TRAJ_INIT_NEEL) return bad("unknown init");
   if (c->n_traj < 1 || c->n_traj > 65535) return bad("n_traj must be in [1, 65535]");
@@ -148,6 +158,7 @@ int validate(const traj_config* c, std::string* why) {
   if (c->shard_size != 1 || c->nccl_id) {
     if (c->propagator == TRAJ_PROP_BANDED) return bad("the banded propagator is not combined with row sharding");
     if (c->protocol == TRAJ_HOMODYNE_RK4) return bad("the RK4 QSD protocol is not combined with row sharding");
+    if (c->protocol == TRAJ_PROJECTIVE_EVENTS) return bad("the event-driven protocol is not combined with row sharding");
     return shard_validate(c, why);
   }
   if (c->shard_rank != 0) return bad("shard_rank must be 0 without sharding");
@@ -164,6 +175,7 @@ int click_capacity(long long L, const traj_config* c) {
 }
 
 std::vector<std::complex<double>> ring_coefficients(int n, double J, double dt);
+constexpr long long EV_TAPCAP = 1 << 20;     // complex taps staged per upload (event-driven PM)
 
 // half-bandwidth of a ring propagator: smallest w with sum_{w < |d| <= n/2} |c_d| < 1e-18
 int band_width(const std::vector<std::complex<double>>& c) {
@@ -210,6 +222,12 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     h->banded = false;
     lay.take(h->Wrk, (size_t)T * L * ldN * 16);
     lay.take(h->dbuf, (size_t)T * L * 8);
+  } else if (c->protocol == TRAJ_PROJECTIVE_EVENTS) {   // per-event stencils: no K
+    h->banded = false;
+    lay.take(h->yhat, (size_t)N * 16);
+    lay.take(h->ev_coef, 64);
+    lay.take(h->occ_count, (size_t)T * 4);
+    lay.take(h->taps_dev, (size_t)EV_TAPCAP * 16);
   } else if (h->banded) {
     lay.take(h->bcoef, (size_t)(2 * h->Wx + 2 * h->Wy + 2) * 16);
   } else {
@@ -399,10 +417,157 @@ int projective(traj_ctx* h, cplx* U) {
   return 0;
 }
 
+// ---- NEXT-4: event-driven PM -------------------------------------------------------------
+// uniforms of event e of trajectory t: counter (e_lo, e_hi, traj, 1) -> (u_eta, u_site),
+// (e_lo, e_hi, traj, 2) -> u_pc (the oracle's philox.event_uniforms)
+void event_uniforms_host(traj_ctx* h, int t, long long e, double* u_eta, double* u_site, double* u_pc) {
+  const uint32_t k0 = (uint32_t)(h->cfg.seed & 0xffffffffu), k1 = (uint32_t)(h->cfg.seed >> 32);
+  const uint32_t tr = (uint32_t)(h->cfg.traj_base + t);
+  const u32x4 a = philox4x32_10(u32x4{(uint32_t)(e & 0xffffffff), (uint32_t)(e >> 32), tr, 1u}, k0, k1);
+  const u32x4 b = philox4x32_10(u32x4{(uint32_t)(e & 0xffffffff), (uint32_t)(e >> 32), tr, 2u}, k0, k1);
+  if (u_eta) *u_eta = u53(a.x, a.y);
+  if (u_site) *u_site = u53(a.z, a.w);
+  if (u_pc) *u_pc = u53(b.x, b.y);
+}
+
+// waiting time before event e: tau = -ln(eta) / (gamma N), eta = 1 - u in (0, 1]  (Q12)
+double event_wait(traj_ctx* h, int t, long long e) {
+  double u;
+  event_uniforms_host(h, t, e, &u, nullptr, nullptr);
+  const double rate = h->gamma[t] * h->N;
+  return rate > 0 ? -log(1.0 - u) / rate : INFINITY;
+}
+
+// taps of K(tau) along a ring of n sites: the band [-W, W] where the Bessel tail is < 1e-18,
+// or the whole circulant when the band does not fit
+struct AxisTaps {
+  int lo = 0, n = 1;
+  std::vector<std::complex<double>> c{1.0};
+};
+
+AxisTaps axis_taps(int n, double J, double tau) {
+  const double x = 2.0 * J * tau;
+  std::vector<double> jm;
+  for (int m = 0; m < 100000; ++m) {
+    const double v = jn(m, x);
+    jm.push_back(v);
+    if (m > fabs(x) + 4 && fabs(v) < 1e-30) break;
+  }
+  int W = (int)jm.size() - 1;
+  double tail = 0.0;
+  while (W > 0 && tail + 2 * fabs(jm[W]) < 1e-18) tail += 2 * fabs(jm[W--]);
+  const std::complex<double> ph[4] = {{1, 0}, {0, -1}, {-1, 0}, {0, 1}};
+  AxisTaps a;
+  a.c.clear();
+  if (2 * W + 1 <= n) {
+    a.lo = -W;
+    a.n = 2 * W + 1;
+    for (int d = -W; d <= W; ++d) a.c.push_back(ph[std::abs(d) & 3] * jm[std::abs(d)]);
+  } else {
+    a.lo = 0;
+    a.n = n;
+    a.c.assign(n, 0.0);
+    const int M = (int)jm.size() - 1;
+    for (int m = -M; m <= M; ++m) a.c[((m % n) + n) % n] += ph[std::abs(m) & 3] * jm[std::abs(m)];
+  }
+  return a;
+}
+
+struct EvPass {
+  int j;            // measured site, or -1 for propagation only
+  double pc;
+  long long off;    // taps offset in the staged buffer
+  AxisTaps x, y;
+};
+
+int event_window(traj_ctx* h) {
+  const double t_end = (h->step + 1) * h->cfg.dt;
+  CK(cudaMemsetAsync(h->occ_count, 0, (size_t)h->T * 4, h->st));
+  for (int t = 0; t < h->T; ++t) {
+    std::vector<EvPass> passes;
+    auto taps = [&](double tau, EvPass& p) {
+      p.x = axis_taps(h->Lx, h->cfg.J, tau);
+      if (h->Ly > 1) p.y = axis_taps(h->Ly, h->cfg.J, tau);
+    };
+    while (h->ev_tnext[t] < t_end) {
+      EvPass p;
+      double u_site, u_pc;
+      event_uniforms_host(h, t, h->ev_count[t], nullptr, &u_site, &u_pc);
+      p.j = std::min((int)(u_site * h->L), h->L - 1);
+      p.pc = u_pc;
+      taps(h->ev_tnext[t] - h->ev_tcur[t], p);
+      passes.push_back(p);
+      h->ev_tcur[t] = h->ev_tnext[t];
+      h->ev_count[t] += 1;
+      h->ev_tnext[t] = h->ev_tcur[t] + event_wait(h, t, h->ev_count[t]);
+    }
+    // propagate to the window end; an odd number of passes leaves the state in the other buffer
+    const double rest = t_end - h->ev_tcur[t];
+    h->ev_tcur[t] = t_end;
+    const int nend = (passes.size() + 1) % 2 == 1 ? 1 : 2;
+    for (int q = 0; q < nend; ++q) {
+      EvPass p;
+      p.j = -1;
+      p.pc = 0;
+      taps(rest / nend, p);
+      passes.push_back(p);
+    }
+    h->last_nS[t] = (int64_t)passes.size() - nend;
+    // stage the taps
+    long long used = 0;
+    size_t first = 0;
+    cplx* src = h->U[h->cur] + t * h->sU;
+    cplx* dst = h->U[1 - h->cur] + t * h->sU;
+    auto flush = [&](size_t upto) -> int {
+      if (used) CK(cudaMemcpyAsync(h->taps_dev, h->taps_host, (size_t)used * 16, cudaMemcpyHostToDevice, h->st));
+      for (size_t q = first; q < upto; ++q) {
+        EvPass& p = passes[q];
+        const cplx* cx = h->taps_dev + p.off;
+        const cplx* cy = cx + p.x.n;
+        if (p.j >= 0) {
+          TRY(event_prep(h->st, src, h->ldN, h->N, h->Lx, h->Ly, p.j, cx, p.x.lo, p.x.n, cy, p.y.lo, p.y.n, p.pc,
+                         h->yhat, h->ev_coef, h->occ_count + t, &h->err));
+          TRY(event_update(h->st, src, dst, h->ldN, h->N, h->Lx, h->Ly, cx, p.x.lo, p.x.n, cy, p.y.lo, p.y.n,
+                           h->yhat, h->ev_coef, p.j, &h->err));
+        } else {
+          TRY(event_update(h->st, src, dst, h->ldN, h->N, h->Lx, h->Ly, cx, p.x.lo, p.x.n, cy, p.y.lo, p.y.n,
+                           nullptr, nullptr, -1, &h->err));
+        }
+        std::swap(src, dst);
+      }
+      CK(cudaStreamSynchronize(h->st));    // the staging buffer is reused
+      used = 0;
+      first = upto;
+      return 0;
+    };
+    for (size_t q = 0; q < passes.size(); ++q) {
+      const long long need = passes[q].x.n + passes[q].y.n;
+      if (used + need > EV_TAPCAP) TRY(flush(q));
+      passes[q].off = used;
+      for (int r = 0; r < passes[q].x.n; ++r) h->taps_host[used++] = passes[q].x.c[r];
+      for (int r = 0; r < passes[q].y.n; ++r) h->taps_host[used++] = passes[q].y.c[r];
+    }
+    TRY(flush(passes.size()));
+  }
+  return 0;
+}
+
 int one_step(traj_ctx* h) {
   cplx* Uc = h->U[h->cur];
   cplx* Un = h->U[1 - h->cur];
   cplx* Us = Un;      // where the propagated state lands
+  if (h->cfg.protocol == TRAJ_PROJECTIVE_EVENTS) {
+    {
+      Phase p(&h->prof, h->st, TRAJ_PH_PROJECT);
+      int s = event_window(h);
+      if (s) return s;
+    }
+    int s = cqr2(h, Un, Uc);
+    if (s) return s;
+    h->cur = 1 - h->cur;
+    h->step += 1;
+    return 0;
+  }
   if (h->cfg.protocol == TRAJ_HOMODYNE_RK4) {
     // NEXT-2: <n>_t from U(t), then RK4 (= Taylor-4 of exp(dt M)) on the Eq. (A3) generator
     {
@@ -740,11 +905,18 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
     else bc.push_back(1.0);
     if (cudaMemcpyAsync(h->bcoef, bc.data(), bc.size() * 16, cudaMemcpyHostToDevice, h->st) != cudaSuccess)
       return bail(TRAJ_ECUDA, "upload band");
-  } else if (cfg->protocol != TRAJ_HOMODYNE_RK4 &&
+  } else if (cfg->protocol != TRAJ_HOMODYNE_RK4 && cfg->protocol != TRAJ_PROJECTIVE_EVENTS &&
              build_k(h->st, h->K, h->ldL, h->Lx, h->Ly, h->kcoef, h->kcoef + h->Lx, &e)) {
     return bail(TRAJ_ECUDA, e);
   }
   if (init_state(h->st, h->U[0], h->ldN, h->sU, h->sites, h->N, h->T, &e)) return bail(TRAJ_ECUDA, e);
+  if (cfg->protocol == TRAJ_PROJECTIVE_EVENTS) {
+    if (cudaMallocHost(&h->taps_host, (size_t)EV_TAPCAP * 16) != cudaSuccess) return bail(TRAJ_ECUDA, "cudaMallocHost");
+    h->ev_count.assign(h->T, 0);
+    h->ev_tcur.assign(h->T, 0.0);
+    h->ev_tnext.assign(h->T, 0.0);
+    for (int t = 0; t < h->T; ++t) h->ev_tnext[t] = event_wait(h, t, 0);
+  }
   if (cudaStreamSynchronize(h->st) != cudaSuccess) return bail(TRAJ_ECUDA, "init sync");
   *out = h;
   return 0;
@@ -913,6 +1085,12 @@ int traj_last_clicks(traj_handle h, int64_t traj, int64_t* n_clicks, int64_t* n_
     if (n_occupied) *n_occupied = h->sh->last_n1;
     return 0;
   }
+  if (h->cfg.protocol == TRAJ_PROJECTIVE_EVENTS && n_occupied) {
+    int32_t v = 0;
+    CK(cudaMemcpyAsync(&v, h->occ_count + traj, 4, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    h->last_n1[traj] = v;
+  }
   if (n_clicks) *n_clicks = h->last_nS[traj];
   if (n_occupied) *n_occupied = h->last_n1[traj];
   return 0;
@@ -953,6 +1131,7 @@ int traj_destroy(traj_handle h) {
   if (h->solver) cusolverDnDestroy(h->solver);
   if (h->h_small) cudaFreeHost(h->h_small);
   if (h->h_dev) cudaFreeHost(h->h_dev);
+  if (h->taps_host) cudaFreeHost(h->taps_host);
   delete h;
   return 0;
 }

@@ -342,3 +342,30 @@ def test_rk4_qsd_protocol_matches_oracle(P, Lx, Ly):
     with the oracle's literal RK4 stages (the GPU evaluates the same polynomial in Horner form)."""
     A = np.arange(Lx * Ly // 2)
     lockstep(P, Lx, Ly, "homodyne_rk4", [0.3, 2.0], 60, 20, [A], seed=12)
+
+
+@pytest.mark.parametrize("Lx,Ly,gam", [(64, 1, 3.0), (96, 1, 0.5), (8, 6, 4.0)])
+def test_event_driven_pm_matches_oracle(P, Lx, Ly, gam):
+    """NEXT-4: the paper-literal event-driven PM (Poisson waiting times, one site per event,
+    Eq. A1/A2 on the L x L matrix in the oracle) against the GPU's orbital form (banded K(tau)
+    stencils and exact rank-1 updates), with the same Philox event stream."""
+    from oracle.pm_events import EventPM
+    g = P.Trajectories(Lx, Ly, "projective_events", [gam, gam * 1.5], seed=3)
+    orc = [EventPM(Lx, Ly, gm, 0.05, seed=3, traj=t) for t, gm in enumerate([gam, gam * 1.5])]
+    A = np.arange(Lx * Ly // 2)
+    events = 0
+    for s in range(1, 41):
+        g.step(1)
+        for t, o in enumerate(orc):
+            n0 = len(o.log)
+            o.step(1)
+            nev, nocc = g.last_clicks(t)
+            assert nev == len(o.log) - n0
+            assert nocc == sum(1 for e in o.log[n0:] if e[3])
+            events += nev
+        if s % 10 == 0:
+            S = g.entropy(A)
+            for t, o in enumerate(orc):
+                assert np.abs(g.correlation(t).cpu().numpy() - o.correlation()).max() < C_TOL
+                assert abs(S[t] - o.entropy(A)) < S_TOL
+    assert events > 50

@@ -257,3 +257,47 @@ def test_rk4_qsd_step_vs_fock_exponential():
     x = np.linalg.norm(X, 2)
     drift = np.linalg.norm(gaussian.correlation(U2) - gaussian.correlation(Ue), 2)
     assert drift < 4 * x ** 5 * np.exp(x) / 120 * np.linalg.cond(scipy.linalg.expm(X))
+
+
+# ---------------------------------------------------------------- NEXT-4: event-driven PM
+def test_event_pm_vs_fock():
+    """The literal D-matrix PM against the Fock space with the same events:
+    propagate by exp(-iH tau), project site j with Born p_j (the same p_c)."""
+    from oracle.pm_events import EventPM
+    from oracle.philox import event_uniforms
+    L, gamma, dt = 8, 3.0, 0.05
+    pm = EventPM(L, 1, gamma, dt, seed=4, traj=2)
+    pm.step(40)
+    assert len(pm.log) > 20
+    F = FockSector(L, L // 2)
+    H = lattice.hopping_matrix(L)
+    import scipy.linalg
+    Hm = F.hamiltonian(H)
+    psi = F.slater(lattice.initial_state(L).astype(complex))
+    t = 0.0
+    for e, te, j, occ in pm.log:
+        psi = scipy.linalg.expm(-1j * Hm * (te - t)) @ psi
+        t = te
+        _, u_site, u_pc = event_uniforms(e, 2, 4)
+        assert j == int(u_site * L)
+        p = F.occupations(psi)[j]
+        assert protocols.decide(float(p), u_pc) == occ
+        psi, _ = F.project(psi, j, occ)
+    psi = scipy.linalg.expm(-1j * Hm * (40 * dt - t)) @ psi
+    # C = U U^dag = conj(<c^dag c>) (reading Q19)
+    assert np.abs(np.conj(F.correlation(psi)) - pm.correlation()).max() < 1e-11
+
+
+def test_event_pm_rates_and_invariants():
+    """Events arrive at rate gamma N, sites uniformly; D stays a rank-N projector."""
+    from oracle.pm_events import EventPM
+    L, gamma, dt = 40, 2.0, 0.05
+    pm = EventPM(L, 1, gamma, dt, seed=1)
+    pm.step(100)
+    T = 100 * dt
+    n_ev = len(pm.log)
+    lam = gamma * (L // 2) * T
+    assert abs(n_ev - lam) < 5 * np.sqrt(lam)
+    C = pm.correlation()
+    assert np.abs(C @ C - C).max() < 1e-10
+    assert abs(np.trace(C).real - L // 2) < 1e-10
