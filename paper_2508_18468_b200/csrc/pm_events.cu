@@ -103,13 +103,60 @@ __global__ void __launch_bounds__(256) event_prep_kernel(const cplx* U, long lon
   }
 }
 
-// one CTA per row: out_i = r_i + (alpha <r_i, yhat> + beta delta_ij) yhat  (coef == nullptr: r_i)
+// one CTA per row: out_i = r_i + (alpha <r_i, yhat> + beta delta_ij) yhat  (coef == nullptr: r_i).
+// The tap rows of row i and their product coefficients are resolved once per CTA in shared
+// memory; the second pass re-reads the freshly written row (L1/L2).
+constexpr int MAXTAPS = 128;
+
 __global__ void __launch_bounds__(256) event_update_kernel(const cplx* U, cplx* out, long long ld, int N, int Lx,
                                                            int Ly, Taps tx, Taps ty, const cplx* yhat,
                                                            const double* coef, int j) {
   __shared__ double red[8];
+  __shared__ long long trow[MAXTAPS];
+  __shared__ double2 tcoef[MAXTAPS];
   const int i = blockIdx.x;
+  const int nt = tx.n * ty.n;
   cplx* o = out + (long long)i * ld;
+  const bool fast = nt <= MAXTAPS;
+  if (fast) {
+    const int x = i % Lx, y = i / Lx;
+    for (int q = threadIdx.x; q < nt; q += 256) {
+      const int qy = q / tx.n, qx = q % tx.n;
+      const int yy = ((y + ty.lo + qy) % Ly + Ly) % Ly, xx = ((x + tx.lo + qx) % Lx + Lx) % Lx;
+      trow[q] = (long long)(yy * Lx + xx) * ld;
+      const double2 a = tx.c[qx], b = ty.c[qy];
+      tcoef[q] = make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+    }
+    __syncthreads();
+    double vr = 0.0, vi = 0.0;
+    for (int k = threadIdx.x; k < N; k += 256) {
+      double re = 0.0, im = 0.0;
+      for (int q = 0; q < nt; ++q) {
+        const double2 c = tcoef[q];
+        const double2 u = U[trow[q] + k];
+        re += c.x * u.x - c.y * u.y;
+        im += c.x * u.y + c.y * u.x;
+      }
+      o[k] = make_double2(re, im);
+      if (coef) {
+        const double2 yk = yhat[k];
+        vr += re * yk.x + im * yk.y;
+        vi += im * yk.x - re * yk.y;
+      }
+    }
+    if (!coef) return;
+    vr = block_sum256(vr, red);
+    vi = block_sum256(vi, red);
+    const double xr = coef[0] * vr + (i == j ? coef[1] : 0.0), xi = coef[0] * vi;
+    for (int k = threadIdx.x; k < N; k += 256) {
+      const double2 yk = yhat[k];
+      double2 r = o[k];
+      r.x += xr * yk.x - xi * yk.y;
+      r.y += xr * yk.y + xi * yk.x;
+      o[k] = r;
+    }
+    return;
+  }
   double vr = 0.0, vi = 0.0;
   for (int k = threadIdx.x; k < N; k += 256) {
     const double2 r = stencil(U, ld, Lx, Ly, i, k, tx, ty);
