@@ -451,6 +451,198 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// Wide variant: CTA 128 x 64, 8 warps of 32 x 32 (three accumulator sets = 192 registers, the
+// fragments loaded per k-step without a prefetch buffer), 4 stages of 48 KB.
+namespace g3w {
+constexpr int BM = 128, BN = 64, STAGES = 4, KSUB = 2;
+constexpr int A_SUB = BM * 128, B_SUB = BN * 128;
+constexpr int A_BYTES = KSUB * A_SUB, B_BYTES = KSUB * B_SUB, STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8;
+}  // namespace g3w
+
+template <bool CONJ_A, bool CONJ_B>
+__global__ void __launch_bounds__(THREADS, 1)
+    zgemm3mw_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        const Args args) {
+  constexpr int BM3 = g3w::BM, BN3 = g3w::BN, ST3 = g3w::STAGES, SB3 = g3w::STAGE_BYTES;
+  constexpr int KS = BKC * g3w::KSUB;     // complex k per stage
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST3 * SB3);
+  uint64_t* empty = full + ST3;
+  const int t = blockIdx.x;
+  const int group = GROUP_M * args.tiles_n;
+  const int first_m = (t / group) * GROUP_M;
+  const int gm = min(GROUP_M, args.tiles_m - first_m);
+  const int pid_m = first_m + (t % group) % gm;
+  const int pid_n = (t % group) / gm;
+  const int m0 = pid_m * BM3, n0 = pid_n * BN3;
+  const int z = blockIdx.z;
+  if ((args.flags & TRAJ_C_UPPER_F) && m0 > n0 + BN3 - 1) return;
+  int kb = 0, ke = args.K;
+  if (args.flags & TRAJ_TRI_A_UPPER_F) kb = max(kb, m0);
+  if (args.flags & TRAJ_TRI_A_LOWER_F) ke = min(ke, m0 + BM3);
+  if (args.flags & TRAJ_TRI_B_UPPER_F) ke = min(ke, n0 + BN3);
+  if (args.flags & TRAJ_TRI_B_LOWER_F) kb = max(kb, n0);
+  const int nk = ke > kb ? (ke - kb + KS - 1) / KS : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST3; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CONSUMER_WARPS);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const bool issuer = (warp == 0 && lane == 0);
+  const int za = args.a_batched ? z : 0, zb = args.b_batched ? z : 0;
+  auto issue = [&](int it) {
+    const int s = it % ST3;
+    mbar_arrive_expect_tx(&full[s], SB3);
+#pragma unroll
+    for (int h = 0; h < g3w::KSUB; ++h) {
+      const int k0 = kb + it * KS + h * BKC;
+      uint8_t* sA = smem + s * SB3 + h * g3w::A_SUB;
+      uint8_t* sB = smem + s * SB3 + g3w::A_BYTES + h * g3w::B_SUB;
+      if (!CONJ_A) {
+        tma_load_3d(sA, &tmA, 2 * k0, m0, za, &full[s]);
+      } else if (args.a_4d) {
+        tma_load_4d(sA, &tmA, 0, k0, m0 / 8, za, &full[s]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < BM3 / 8; ++c) tma_load_3d(sA + c * 1024, &tmA, 2 * (m0 + 8 * c), k0, za, &full[s]);
+      }
+      if (CONJ_B) {
+        tma_load_3d(sB, &tmB, 2 * k0, n0, zb, &full[s]);
+      } else if (args.b_4d) {
+        tma_load_4d(sB, &tmB, 0, k0, n0 / 8, zb, &full[s]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < BN3 / 8; ++c) tma_load_3d(sB + c * 1024, &tmB, 2 * (n0 + 8 * c), k0, zb, &full[s]);
+      }
+    }
+  };
+  int issued = 0;
+  auto try_issue = [&](int it, bool must) {
+    while (issued < nk && issued <= it + ST3 - 1) {
+      if (issued >= ST3) {
+        const uint32_t par = ((issued / ST3) + 1) & 1;
+        if (must && issued <= it) mbar_wait(&empty[issued % ST3], par);
+        else if (!mbar_test(&empty[issued % ST3], par)) break;
+      }
+      issue(issued);
+      ++issued;
+    }
+  };
+  if (issuer) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    try_issue(0, true);
+  }
+  const int warp_m = warp & 3, warp_n = warp >> 2;    // 4 x 2 warps of 32 x 32
+  const int g = lane >> 2, slot = lane & 3;
+  constexpr unsigned long long SIGN = 0x8000000000000000ull;
+  constexpr unsigned long long ma = CONJ_A ? SIGN : 0ull, mb = CONJ_B ? SIGN : 0ull;
+  uint32_t offA[4], offB[4];   // per-lane offsets of (row, k = 2*slot) inside an 8-k sub-tile
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = warp_m * 32 + 8 * i + g;
+    offA[i] = CONJ_A ? off_mn(r, 2 * slot) : off_kc(r, 2 * slot);
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int r = warp_n * 32 + 8 * j + g;
+    offB[j] = CONJ_B ? off_kc(r, 2 * slot) : off_mn(r, 2 * slot);
+  }
+  double acc[4][4][3][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int p = 0; p < 3; ++p) acc[i][j][p][0] = acc[i][j][p][1] = 0.0;
+  // fragment address for k-step q: k = (q & 1) + 2*slot in sub-tile q >> 1.  The swizzle
+  // XORs the chunk with (row & 7) for k-contiguous tiles and (k) for m/n-contiguous ones;
+  // (q & 1) flips bit 0 of k, handled by recomputing the offset.
+  auto addrA = [&](const uint8_t* base, int q, int i) -> const double2* {
+    const int r = warp_m * 32 + 8 * i + g, k = (q & 1) + 2 * slot;
+    return reinterpret_cast<const double2*>(base + (q >> 1) * g3w::A_SUB +
+                                            (CONJ_A ? off_mn(r, k) : off_kc(r, k)));
+  };
+  auto addrB = [&](const uint8_t* base, int q, int j) -> const double2* {
+    const int r = warp_n * 32 + 8 * j + g, k = (q & 1) + 2 * slot;
+    return reinterpret_cast<const double2*>(base + g3w::A_BYTES + (q >> 1) * g3w::B_SUB +
+                                            (CONJ_B ? off_kc(r, k) : off_mn(r, k)));
+  };
+  (void)offA;
+  (void)offB;
+  for (int it = 0; it < nk; ++it) {
+    const int s = it % ST3;
+    if (issuer) try_issue(it, true);
+    mbar_wait(&full[s], (it / ST3) & 1);
+    const uint8_t* base = smem + s * SB3;
+#pragma unroll
+    for (int q = 0; q < 2 * g3w::KSUB; ++q) {
+      double2 va[4], vb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) va[i] = *addrA(base, q, i);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) vb[j] = *addrB(base, q, j);
+      if (CONJ_A) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) va[i].y = -va[i].y;
+      }
+      if (CONJ_B) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) vb[j].y = -vb[j].y;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          dmma_8x8x4(acc[i][j][0][0], acc[i][j][0][1], va[i].x, vb[j].x);
+          dmma_8x8x4(acc[i][j][1][0], acc[i][j][1][1], va[i].y, vb[j].y);
+        }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double a3 = va[i].x + va[i].y;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][2][0], acc[i][j][2][1], a3, vb[j].x + vb[j].y);
+      }
+      if (q == 1 && issuer) try_issue(it, false);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  cplx* C = args.C + (long long)z * args.strideC;
+  const bool upper = args.flags & TRAJ_C_UPPER_F;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = m0 + warp_m * 32 + 8 * i + g;
+    if (row >= args.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = n0 + warp_n * 32 + 8 * j + 2 * slot + e;
+        if (col >= args.N || (upper && row > col)) continue;
+        const double p1 = acc[i][j][0][e], p2 = acc[i][j][1][e], p3 = acc[i][j][2][e];
+        const double vr = p1 - p2, vi = p3 - p1 - p2;
+        double2 out;
+        out.x = args.alpha_re * vr - args.alpha_im * vi;
+        out.y = args.alpha_re * vi + args.alpha_im * vr;
+        cplx* pc = C + (long long)row * args.ldc + col;
+        if (args.beta != 0.0) {
+          const double2 old = *pc;
+          out.x += args.beta * old.x;
+          out.y += args.beta * old.y;
+        }
+        *pc = out;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ host side
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -534,6 +726,21 @@ cudaError_t launch3m(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b
   return cudaGetLastError();
 }
 
+template <bool CA, bool CB>
+cudaError_t launch3mw(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const Args& args, int batch) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(zgemm3mw_dmma_kernel<CA, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         g3w::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid(args.tiles_m * args.tiles_n, 1, batch);
+  zgemm3mw_dmma_kernel<CA, CB><<<grid, THREADS, g3w::SMEM_BYTES, st>>>(a, b, args);
+  count_launch();
+  return cudaGetLastError();
+}
+
 std::atomic<int> g_algo{-1};
 
 }  // namespace
@@ -565,8 +772,13 @@ int zgemm(cudaStream_t st, int opA, int opB, long long M, long long N, long long
   }
   CUtensorMap ma, mb;
   const long long Ka = K > 0 ? K : 1;
-  const bool m3 = zgemm_algorithm() == 1;
-  const int bm = m3 ? g3::BM : BM, bn = m3 ? g3::BN : BN;
+  int algo = zgemm_algorithm();
+  // 3M shape policy: the 128 x 64 (32 x 32 warp tiles) variant for large N x N products
+  // (better fragment reuse; K.U +3%), the 64 x 64 one otherwise (Gram upper tiles, skinny and
+  // small GEMMs of the Cholesky recursion get more CTAs and less diagonal waste)
+  if (algo == 1 && opA == 0 && opB == 0 && ceil_div(M, g3w::BM) * ceil_div(N, g3w::BN) * batch >= 4 * 148) algo = 2;
+  const bool m3 = algo >= 1;
+  const int bm = algo == 2 ? g3w::BM : (m3 ? g3::BM : BM), bn = algo == 2 ? g3w::BN : (m3 ? g3::BN : BN);
   // op(A) = A: stored [M][K], k-contiguous tile [BM rows][8 k]; op(A) = A^dag: stored [K][M].
   const bool a4 = opA == 1 && round_up(M, 8) <= lda && !getenv("TRAJ_NO_TMA4D");
   const bool b4 = opB == 0 && round_up(N, 8) <= ldb && !getenv("TRAJ_NO_TMA4D");
@@ -598,7 +810,12 @@ int zgemm(cudaStream_t st, int opA, int opB, long long M, long long N, long long
   args.ldc = ldc;
   args.strideC = strideC;
   cudaError_t e;
-  if (m3) {
+  if (algo == 2) {
+    if (opA == 0 && opB == 0) e = launch3mw<false, false>(st, ma, mb, args, (int)batch);
+    else if (opA == 0) e = launch3mw<false, true>(st, ma, mb, args, (int)batch);
+    else if (opB == 0) e = launch3mw<true, false>(st, ma, mb, args, (int)batch);
+    else e = launch3mw<true, true>(st, ma, mb, args, (int)batch);
+  } else if (m3) {
     if (opA == 0 && opB == 0) e = launch3m<false, false>(st, ma, mb, args, (int)batch);
     else if (opA == 0) e = launch3m<false, true>(st, ma, mb, args, (int)batch);
     else if (opB == 0) e = launch3m<true, false>(st, ma, mb, args, (int)batch);
