@@ -21,76 +21,91 @@ namespace traj {
 namespace {
 
 constexpr int NB = 64;            // leaf size
-constexpr int LD = NB + 1;        // padded smem row (complex)
-constexpr int LEAF_THREADS = 256;
 
-__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {   // conj(a) * b
-  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
-}
 
-// One CTA per batch entry: n <= 64 diagonal block.  Reads the upper triangle of G,
-// writes X = R^-1 (upper) and zeros below the diagonal.  Right-looking elimination with
-// G = L L^dag (L = R^dag): step j scales row j of the working matrix A (its final row of
-// R) and row j of W, then eliminates rows i > j in A (upper part) and applies the same
-// row operation to W; W ends as L^-1, so X = R^-1 = W^dag.  Two barriers per column.
-__global__ void __launch_bounds__(LEAF_THREADS) chol_leaf_kernel(int n, cplx* G, long long ldg, long long sG, cplx* X,
-                                                                  long long ldx, long long sX, int32_t* failed) {
-  extern __shared__ double2 sm[];
-  double2* R = sm;               // [NB][LD]  working matrix -> R (upper)
-  double2* Ws = sm + NB * LD;    // [NB][LD]  -> L^-1 (lower)
+// One CTA (1024 threads) per batch entry: n <= 64 diagonal block.  Reads the upper
+// triangle of G, writes X = R^-1 (upper) and zeros below the diagonal.  Each thread owns a
+// 2 x 2 block of the (identity-padded, full Hermitian) working matrix A and of W in registers.
+// Step j of the right-looking elimination (G = L L^dag, L = R^dag): the owners publish row j
+// of A and W and column j of A through shared memory; every thread then applies
+//   l_i = A_ij / r_jj (= conj R_ji),  A_ik -= l_i A_jk / r_jj (i, k > j),  W_ik -= l_i W_jk / r_jj (i > j),
+// W ends as L^-1 (rows scaled by 1/r_jj at their step), so X = R^-1 = W^dag.
+__global__ void __launch_bounds__(1024) chol_leaf_kernel(int n, cplx* G, long long ldg, long long sG, cplx* X,
+                                                         long long ldx, long long sX, int32_t* failed) {
+  __shared__ double2 rowA[NB], rowW[NB], colA[NB];
   __shared__ int bad;
   const int b = blockIdx.x, tid = threadIdx.x;
   const cplx* g = G + b * sG;
   cplx* x = X + b * sX;
-  if (tid == 0) bad = 0;
-  for (int idx = tid; idx < n * n; idx += LEAF_THREADS) {
-    const int i = idx / n, j = idx % n;
-    if (i <= j) R[i * LD + j] = g[(long long)i * ldg + j];
-    Ws[i * LD + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
-  }
-  __syncthreads();
-  for (int j = 0; j < n; ++j) {
-    // (1) pivot and scaling of row j (every thread reads the pivot itself: no extra barrier)
-    const double d = R[j * LD + j].x;
-    const double r = sqrt(d);
-    const double ip = 1.0 / r;
-    if (tid == 0 && (!(d > 0.0) || !isfinite(d))) bad = 1;
-    __syncthreads();     // all threads have read R[j][j] before it is overwritten
-    for (int k = j + tid; k < n; k += LEAF_THREADS) {
-      const double2 v = R[j * LD + k];
-      R[j * LD + k] = k == j ? make_double2(r, 0.0) : make_double2(v.x * ip, v.y * ip);
+  const int i0 = 2 * (tid >> 5), k0 = 2 * (tid & 31);
+  double2 A[2][2], W[2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int i = i0 + a, k = k0 + c;
+      double2 v = make_double2(i == k ? 1.0 : 0.0, 0.0);
+      if (i < n && k < n) {
+        if (i <= k) v = g[(long long)i * ldg + k];
+        else {
+          const double2 u = g[(long long)k * ldg + i];
+          v = make_double2(u.x, -u.y);
+        }
+      }
+      A[a][c] = v;
+      W[a][c] = make_double2(i == k ? 1.0 : 0.0, 0.0);
     }
-    for (int k = tid; k <= j; k += LEAF_THREADS) {
-      const double2 v = Ws[j * LD + k];
-      Ws[j * LD + k] = make_double2(v.x * ip, v.y * ip);
+  if (tid == 0) bad = 0;
+  for (int j = 0; j < n; ++j) {     // padded identity rows/columns need no elimination
+    if ((j >> 1) == (i0 >> 1)) {
+      const int a = j & 1;
+      rowA[k0] = A[a][0];
+      rowA[k0 + 1] = A[a][1];
+      rowW[k0] = W[a][0];
+      rowW[k0 + 1] = W[a][1];
+    }
+    if ((j >> 1) == (k0 >> 1)) {
+      const int c = j & 1;
+      colA[i0] = A[0][c];
+      colA[i0 + 1] = A[1][c];
     }
     __syncthreads();
-    // (2) eliminate rows i > j: l_ij = conj(R_ji)
-    const int m = n - j - 1;
-    const int wA = m * m, wW = m * (j + 1);
-    for (int idx = tid; idx < wA + wW; idx += LEAF_THREADS) {
-      if (idx < wA) {
-        const int i = j + 1 + idx / m, k = j + 1 + idx % m;
-        if (i <= k) {
-          const double2 p = cmulc(R[j * LD + i], R[j * LD + k]);
-          R[i * LD + k].x -= p.x;
-          R[i * LD + k].y -= p.y;
+    const double d = rowA[j].x;
+    if (tid == 0 && j < n && (!(d > 0.0) || !isfinite(d))) bad = 1;
+    const double ip = 1.0 / d;            // l_i * A_jk / r_jj = (A_ij / r)(A_jk / r) = A_ij A_jk / d
+    const double ir = 1.0 / sqrt(d);
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const int i = i0 + a;
+      if (i == j) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) W[a][c] = make_double2(W[a][c].x * ir, W[a][c].y * ir);
+      } else if (i > j) {
+        const double2 l = colA[i];        // A_ij
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int k = k0 + c;
+          if (k > j) {
+            const double2 r = rowA[k];    // A_jk
+            A[a][c].x -= (l.x * r.x - l.y * r.y) * ip;
+            A[a][c].y -= (l.x * r.y + l.y * r.x) * ip;
+          }
+          const double2 w = rowW[k];      // W_jk (unscaled): l/r * W_jk/r
+          W[a][c].x -= (l.x * w.x - l.y * w.y) * ip;
+          W[a][c].y -= (l.x * w.y + l.y * w.x) * ip;
         }
-      } else {
-        const int q = idx - wA;
-        const int i = j + 1 + q / (j + 1), k = q % (j + 1);
-        const double2 p = cmulc(R[j * LD + i], Ws[j * LD + k]);
-        Ws[i * LD + k].x -= p.x;
-        Ws[i * LD + k].y -= p.y;
       }
     }
     __syncthreads();
   }
-  for (int idx = tid; idx < n * n; idx += LEAF_THREADS) {
-    const int i = idx / n, j = idx % n;     // X_ij = conj(W_ji), upper
-    const double2 w = Ws[j * LD + i];
-    x[(long long)i * ldx + j] = i <= j ? make_double2(w.x, -w.y) : make_double2(0.0, 0.0);
-  }
+  // X = W^dag: X_ki = conj(W_ik) for k <= i; zeros below the diagonal
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int i = i0 + a, k = k0 + c;    // element W_ik  ->  X_ki
+      if (i < n && k < n) x[(long long)k * ldx + i] = k <= i ? make_double2(W[a][c].x, -W[a][c].y) : make_double2(0.0, 0.0);
+    }
   if (tid == 0 && bad && failed) failed[b] = 1;
 }
 
@@ -111,13 +126,7 @@ struct Ctx {
 
 int rec(Ctx& c, long long o, long long n) {
   if (n <= NB) {
-    static bool attr = false;
-    const int smem = 2 * NB * LD * sizeof(double2);
-    if (!attr) {
-      cudaFuncSetAttribute(chol_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      attr = true;
-    }
-    chol_leaf_kernel<<<(unsigned)c.batch, LEAF_THREADS, smem, c.st>>>((int)n, c.G + o * c.ldg + o, c.ldg, c.sG,
+    chol_leaf_kernel<<<(unsigned)c.batch, 1024, 0, c.st>>>((int)n, c.G + o * c.ldg + o, c.ldg, c.sG,
                                                                       c.X + o * c.ldx + o, c.ldx, c.sX, c.failed);
     count_launch();
     cudaError_t e = cudaGetLastError();

@@ -144,11 +144,18 @@ __global__ void __launch_bounds__(1024) compact_kernel(const int32_t* flags, int
 // dst[t][r][:] = src[t][idx[t][r]][:] for r < count[t]
 __global__ void gather_rows_kernel(const cplx* src, long long lds, long long sS, const int32_t* idx, long long sIdx,
                                    const int32_t* count, int fixed_count, cplx* dst, long long ldd, long long sD,
-                                   int ncols, int row_offset) {
+                                   int ncols, int row_offset, int zero_fill) {
   const int t = blockIdx.z;
   const int r = blockIdx.y;
   const int cnt = count ? count[t] : fixed_count;
-  if (r >= cnt) return;
+  if (r >= cnt) {
+    if (zero_fill) {
+      cplx* d = dst + t * sD + (long long)r * ldd;
+      for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ncols; k += gridDim.x * blockDim.x)
+        d[k] = make_double2(0.0, 0.0);
+    }
+    return;
+  }
   const long long srow = idx[t * sIdx + r] - row_offset;
   const cplx* s = src + t * sS + srow * lds;
   cplx* d = dst + t * sD + (long long)r * ldd;
@@ -277,6 +284,36 @@ __global__ void gather_sub_kernel(const cplx* D0, long long ld0, const int32_t* 
     const int a = idx / k, b = idx % k;
     D11[(long long)a * ld1 + b] = D0[(long long)pos[a] * ld0 + pos[b]];
   }
+}
+
+// D11[t][a][b] = D0[t][pos[t][a]][pos[t][b]] for a, b < k[t]; identity padding up to kmax
+__global__ void gather_sub_batched_kernel(const cplx* D0, long long ld0, long long s0, const int32_t* pos, int cap,
+                                          const int32_t* k, int kmax, cplx* D11, long long ld1, long long s1) {
+  const int t = blockIdx.y;
+  const int kt = k[t];
+  const int32_t* p = pos + (long long)t * cap;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < kmax * kmax; idx += gridDim.x * blockDim.x) {
+    const int a = idx / kmax, b = idx % kmax;
+    double2 v = make_double2(a == b ? 1.0 : 0.0, 0.0);
+    if (a < kt && b < kt) v = D0[t * s0 + (long long)p[a] * ld0 + p[b]];
+    D11[t * s1 + (long long)a * ld1 + b] = v;
+  }
+}
+
+__global__ void sub_identity_batched_kernel(cplx* T, long long ld, long long sT, const int32_t* S1, int cap,
+                                            const int32_t* k) {
+  const int t = blockIdx.y;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < k[t]) T[t * sT + (long long)S1[(long long)t * cap + c] * ld + c].x -= 1.0;
+}
+
+__global__ void zero_rows_batched_kernel(cplx* U, long long ld, long long sU, const int32_t* rows, int cap,
+                                         const int32_t* k, int ncols) {
+  const int t = blockIdx.z, r = blockIdx.y;
+  if (r >= k[t]) return;
+  cplx* p = U + t * sU + (long long)rows[(long long)t * cap + r] * ld;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += gridDim.x * blockDim.x)
+    p[c] = make_double2(0.0, 0.0);
 }
 
 // T[S1[c]][c] -= 1
@@ -450,11 +487,11 @@ int compact(cudaStream_t st, const int32_t* flags, int L, int T, int32_t* list, 
 
 int gather_rows(cudaStream_t st, const cplx* src, long long lds, long long sS, const int32_t* idx, long long sIdx,
                 const int32_t* count_dev, int rows, int T, cplx* dst, long long ldd, long long sD, int ncols,
-                std::string* err, int row_offset) {
+                std::string* err, int row_offset, int zero_fill) {
   if (rows <= 0 || T <= 0) return 0;
   dim3 grid((unsigned)std::min<long long>(ceil_div(ncols, 256), 64), rows, T);
   gather_rows_kernel<<<grid, 256, 0, st>>>(src, lds, sS, idx, sIdx, count_dev, rows, dst, ldd, sD, ncols,
-                                           row_offset);
+                                           row_offset, zero_fill);
   count_launch();
   return last(err, "gather_rows") == cudaSuccess ? 0 : 4;
 }
@@ -510,6 +547,34 @@ int gather_sub(cudaStream_t st, const cplx* D0, long long ld0, const int32_t* po
                                                                                                        k, D11, ld1);
   count_launch();
   return last(err, "gather_sub") == cudaSuccess ? 0 : 4;
+}
+
+int gather_sub_batched(cudaStream_t st, const cplx* D0, long long ld0, long long s0, const int32_t* pos, int cap,
+                       const int32_t* k_dev, int kmax, int T, cplx* D11, long long ld1, long long s1,
+                       std::string* err) {
+  if (kmax <= 0) return 0;
+  dim3 grid((unsigned)std::min<long long>(ceil_div((long long)kmax * kmax, 256), 1024), T);
+  gather_sub_batched_kernel<<<grid, 256, 0, st>>>(D0, ld0, s0, pos, cap, k_dev, kmax, D11, ld1, s1);
+  count_launch();
+  return last(err, "gather_sub_batched") == cudaSuccess ? 0 : 4;
+}
+
+int sub_identity_batched(cudaStream_t st, cplx* T, long long ld, long long sT, const int32_t* S1, int cap,
+                         const int32_t* k_dev, int kmax, int nT, std::string* err) {
+  if (kmax <= 0) return 0;
+  dim3 grid((unsigned)ceil_div(kmax, 256), nT);
+  sub_identity_batched_kernel<<<grid, 256, 0, st>>>(T, ld, sT, S1, cap, k_dev);
+  count_launch();
+  return last(err, "sub_identity_batched") == cudaSuccess ? 0 : 4;
+}
+
+int zero_rows_batched(cudaStream_t st, cplx* U, long long ld, long long sU, const int32_t* rows, int cap,
+                      const int32_t* k_dev, int kmax, int T, int ncols, std::string* err) {
+  if (kmax <= 0) return 0;
+  dim3 grid((unsigned)std::min<long long>(ceil_div(ncols, 256), 64), kmax, T);
+  zero_rows_batched_kernel<<<grid, 256, 0, st>>>(U, ld, sU, rows, cap, k_dev, ncols);
+  count_launch();
+  return last(err, "zero_rows_batched") == cudaSuccess ? 0 : 4;
 }
 
 int sub_identity(cudaStream_t st, cplx* T, long long ld, const int32_t* S1, int k, std::string* err, int row0,

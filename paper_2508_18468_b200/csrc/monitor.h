@@ -18,7 +18,15 @@ int compact(cudaStream_t st, const int32_t* flags, int L, int T, int32_t* list, 
 // dst[t][r] = src[t][idx[t][r] - row_offset] for r < count[t] (or rows if count_dev is null)
 int gather_rows(cudaStream_t st, const cplx* src, long long lds, long long sS, const int32_t* idx, long long sIdx,
                 const int32_t* count_dev, int rows, int T, cplx* dst, long long ldd, long long sD, int ncols,
-                std::string* err, int row_offset = 0);
+                std::string* err, int row_offset = 0, int zero_fill = 0);
+// batched helpers of the projective rank-k update (k_dev: per-trajectory counts, padded to kmax)
+int gather_sub_batched(cudaStream_t st, const cplx* D0, long long ld0, long long s0, const int32_t* pos, int cap,
+                       const int32_t* k_dev, int kmax, int T, cplx* D11, long long ld1, long long s1,
+                       std::string* err);
+int sub_identity_batched(cudaStream_t st, cplx* T, long long ld, long long sT, const int32_t* S1, int cap,
+                         const int32_t* k_dev, int kmax, int nT, std::string* err);
+int zero_rows_batched(cudaStream_t st, cplx* U, long long ld, long long sU, const int32_t* rows, int cap,
+                      const int32_t* k_dev, int kmax, int T, int ncols, std::string* err);
 // Blocked conditional Born sampling of every trajectory's click list on C_SS (D0, kept);
 // Dw: work copy; Linv/DLinv: [T][64][64]; Ybuf/Zbuf: [T][64][ldy] with ldy >= maxc.
 int sample_outcomes(cudaStream_t st, const cplx* D0, cplx* Dw, long long ldd, long long sD, const int32_t* S, int cap,

@@ -273,11 +273,11 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     lay.take(h->DLinv, (size_t)T * 64 * 64 * 16);
     lay.take(h->Ybuf, (size_t)T * 64 * ldcap * 16);
     lay.take(h->Zbuf, (size_t)T * 64 * ldcap * 16);
-    lay.take(h->D11, (size_t)cap * ldcap * 16);
-    lay.take(h->X11, (size_t)cap * ldcap * 16);
-    lay.take(h->chol_scratch_small, chol_scratch_bytes(cap, 1));
-    lay.take(h->W, (size_t)N * ldcap * 16);
-    lay.take(h->Tm, (size_t)L * ldcap * 16);
+    lay.take(h->D11, (size_t)T * cap * ldcap * 16);
+    lay.take(h->X11, (size_t)T * cap * ldcap * 16);
+    lay.take(h->chol_scratch_small, chol_scratch_bytes(cap, T));
+    lay.take(h->W, (size_t)T * N * ldcap * 16);
+    lay.take(h->Tm, (size_t)T * L * ldcap * 16);
   }
   return lay.off + 256;
 }
@@ -388,32 +388,36 @@ int projective(traj_ctx* h, cplx* U) {
   CK(cudaMemcpyAsync(h->h_small, h->k1, T * 4, cudaMemcpyDeviceToHost, h->st));
   CK(cudaMemcpyAsync(h->h_small + T, h->k0, T * 4, cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
+  // rank-k update of every trajectory at once, padded to k1max (identity block in C_{S1S1},
+  // zero rows of U_{S1}: the padded columns of W and Tm vanish)
+  int k1max = 0, k0max = 0;
   for (int t = 0; t < T; ++t) {
-    const int k1 = h->h_small[t], k0 = h->h_small[T + t];
-    h->last_n1[t] = k1;
-    cplx* Ut = U + t * h->sU;
-    if (k1 > 0) {
-      const int32_t* pos1 = h->pos1 + (long long)t * cap;
-      const int32_t* S1 = h->S1 + (long long)t * cap;
-      TRY(gather_sub(h->st, h->D0 + t * h->sD, h->ldcap, pos1, k1, h->D11, h->ldcap, &h->err));
-      // R^dag R = C_{S1 S1},  X11 = R^-1
-      TRY(chol_inverse(h->st, k1, h->D11, h->ldcap, 0, h->X11, h->ldcap, 0, 1, h->chol_scratch_small,
-                       h->failed_dev + t, &h->err));
-      // U_{S1} rows -> US[t] (C_SS is already formed)
-      TRY(gather_rows(h->st, Ut, h->ldN, 0, S1, 0, nullptr, k1, 1, h->US + t * h->sUS, h->ldN, 0, h->N, &h->err));
-      // W = U_{S1}^dag R^-1   (N x k1)
-      TRY(zgemm(h->st, 1, 0, h->N, k1, k1, 1.0, 0.0, h->US + t * h->sUS, h->ldN, 0, h->X11, h->ldcap, 0, 0.0, h->W,
-                h->ldcap, 0, 1, TRAJ_TRI_B_UPPER_F, &h->err));
-      // Tm = U W - E_{S1}   (L x k1)
-      TRY(zgemm(h->st, 0, 0, h->L, k1, h->N, 1.0, 0.0, Ut, h->ldN, 0, h->W, h->ldcap, 0, 0.0, h->Tm, h->ldcap, 0, 1, 0,
-                &h->err));
-      TRY(sub_identity(h->st, h->Tm, h->ldcap, S1, k1, &h->err));
-      // U <- U - Tm W^dag
-      TRY(zgemm(h->st, 0, 1, h->L, h->N, k1, -1.0, 0.0, h->Tm, h->ldcap, 0, h->W, h->ldcap, 0, 1.0, Ut, h->ldN, 0, 1,
-                0, &h->err));
-    }
-    if (k0 > 0) TRY(zero_rows(h->st, Ut, h->ldN, h->S0 + (long long)t * cap, k0, h->N, &h->err));
+    h->last_n1[t] = h->h_small[t];
+    k1max = std::max(k1max, h->h_small[t]);
+    k0max = std::max(k0max, h->h_small[T + t]);
   }
+  const long long sX = (long long)cap * h->ldcap, sW = (long long)h->N * h->ldcap, sT = (long long)h->L * h->ldcap;
+  if (k1max > 0) {
+    TRY(gather_sub_batched(h->st, h->D0, h->ldcap, h->sD, h->pos1, cap, h->k1, k1max, T, h->D11, h->ldcap, sX,
+                           &h->err));
+    // R^dag R = C_{S1 S1},  X11 = R^-1
+    TRY(chol_inverse(h->st, k1max, h->D11, h->ldcap, sX, h->X11, h->ldcap, sX, T, h->chol_scratch_small,
+                     h->failed_dev, &h->err));
+    // U_{S1} rows (zero beyond k1[t]) -> US
+    TRY(gather_rows(h->st, U, h->ldN, h->sU, h->S1, cap, h->k1, k1max, T, h->US, h->ldN, h->sUS, h->N, &h->err, 0,
+                    1));
+    // W = U_{S1}^dag R^-1   (N x k1)
+    TRY(zgemm(h->st, 1, 0, h->N, k1max, k1max, 1.0, 0.0, h->US, h->ldN, h->sUS, h->X11, h->ldcap, sX, 0.0, h->W,
+              h->ldcap, sW, T, TRAJ_TRI_B_UPPER_F, &h->err));
+    // Tm = U W - E_{S1}   (L x k1)
+    TRY(zgemm(h->st, 0, 0, h->L, k1max, h->N, 1.0, 0.0, U, h->ldN, h->sU, h->W, h->ldcap, sW, 0.0, h->Tm, h->ldcap,
+              sT, T, 0, &h->err));
+    TRY(sub_identity_batched(h->st, h->Tm, h->ldcap, sT, h->S1, cap, h->k1, k1max, T, &h->err));
+    // U <- U - Tm W^dag
+    TRY(zgemm(h->st, 0, 1, h->L, h->N, k1max, -1.0, 0.0, h->Tm, h->ldcap, sT, h->W, h->ldcap, sW, 1.0, U, h->ldN,
+              h->sU, T, 0, &h->err));
+  }
+  if (k0max > 0) TRY(zero_rows_batched(h->st, U, h->ldN, h->sU, h->S0, cap, h->k0, k0max, T, h->N, &h->err));
   return 0;
 }
 

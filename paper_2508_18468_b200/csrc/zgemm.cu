@@ -588,13 +588,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int i = 0; i < 4; ++i) va[i] = *addrA(base, q, i);
 #pragma unroll
       for (int j = 0; j < 4; ++j) vb[j] = *addrB(base, q, j);
-      if (CONJ_A) {
+      if (CONJ_A) {   // sign-bit XOR (ALU), not a DADD negation on the FP64 pipe
 #pragma unroll
-        for (int i = 0; i < 4; ++i) va[i].y = -va[i].y;
+        for (int i = 0; i < 4; ++i)
+          va[i].y = __longlong_as_double((long long)((unsigned long long)__double_as_longlong(va[i].y) ^ ma));
       }
       if (CONJ_B) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) vb[j].y = -vb[j].y;
+        for (int j = 0; j < 4; ++j)
+          vb[j].y = __longlong_as_double((long long)((unsigned long long)__double_as_longlong(vb[j].y) ^ mb));
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
