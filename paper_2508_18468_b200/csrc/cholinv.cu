@@ -30,14 +30,15 @@ constexpr int NB = 64;            // leaf size
 // of A and W and column j of A through shared memory; every thread then applies
 //   l_i = A_ij / r_jj (= conj R_ji),  A_ik -= l_i A_jk / r_jj (i, k > j),  W_ik -= l_i W_jk / r_jj (i > j),
 // W ends as L^-1 (rows scaled by 1/r_jj at their step), so X = R^-1 = W^dag.
-__global__ void __launch_bounds__(1024) chol_leaf_kernel(int n, cplx* G, long long ldg, long long sG, cplx* X,
-                                                         long long ldx, long long sX, int32_t* failed) {
+template <int TW>   // TW x TW threads, each owning a 2 x 2 block (n <= 2 TW)
+__global__ void __launch_bounds__(TW * TW) chol_leaf_kernel(int n, cplx* G, long long ldg, long long sG, cplx* X,
+                                                            long long ldx, long long sX, int32_t* failed) {
   __shared__ double2 rowA[NB], rowW[NB], colA[NB];
   __shared__ int bad;
   const int b = blockIdx.x, tid = threadIdx.x;
   const cplx* g = G + b * sG;
   cplx* x = X + b * sX;
-  const int i0 = 2 * (tid >> 5), k0 = 2 * (tid & 31);
+  const int i0 = 2 * (tid / TW), k0 = 2 * (tid % TW);
   double2 A[2][2], W[2][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
@@ -126,7 +127,9 @@ struct Ctx {
 
 int rec(Ctx& c, long long o, long long n) {
   if (n <= NB) {
-    chol_leaf_kernel<<<(unsigned)c.batch, 1024, 0, c.st>>>((int)n, c.G + o * c.ldg + o, c.ldg, c.sG,
+    auto leaf = n <= 16 ? chol_leaf_kernel<8> : (n <= 32 ? chol_leaf_kernel<16> : chol_leaf_kernel<32>);
+    const int tw = n <= 16 ? 8 : (n <= 32 ? 16 : 32);
+    leaf<<<(unsigned)c.batch, tw * tw, 0, c.st>>>((int)n, c.G + o * c.ldg + o, c.ldg, c.sG,
                                                                       c.X + o * c.ldx + o, c.ldx, c.sX, c.failed);
     count_launch();
     cudaError_t e = cudaGetLastError();
