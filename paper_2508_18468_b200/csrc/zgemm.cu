@@ -605,11 +605,14 @@ __global__ void __launch_bounds__(THREADS, 1)
           dmma_8x8x4(acc[i][j][0][0], acc[i][j][0][1], va[i].x, vb[j].x);
           dmma_8x8x4(acc[i][j][1][0], acc[i][j][1][1], va[i].y, vb[j].y);
         }
+      double b3[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b3[j] = vb[j].x + vb[j].y;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const double a3 = va[i].x + va[i].y;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][2][0], acc[i][j][2][1], a3, vb[j].x + vb[j].y);
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][2][0], acc[i][j][2][1], a3, b3[j]);
       }
       if (q == 1 && issuer) try_issue(it, false);
     }
