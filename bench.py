@@ -164,7 +164,7 @@ def run_ours(args):
         if world > 1:
             dist.broadcast_object_list(uid, src=0)
         tr = P.Trajectories(w.Lx, w.Ly, w.protocol, gam, dt=w.dt, J=w.J, seed=w.seed, traj_base=0,
-                            shard_size=world, shard_rank=rank, nccl_id=uid[0])
+                            shard_size=world, shard_rank=rank, nccl_id=uid[0], propagator=args.propagator)
     else:
         gam = [w.gammas[(rank * tpg + t) % len(w.gammas)] for t in range(tpg)]
         base = rank * tpg

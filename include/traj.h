@@ -103,7 +103,8 @@ typedef struct {
  * coefficients fall below 1e-18 after a few neighbours (Bessel tail); U <- K U becomes one
  * (1d) or two (2d, K = K_y (x) K_x) banded stencil passes of half-width W (W chosen so the
  * dropped tail is < 1e-18; the dense path is used if 2W+1 exceeds an extent).  No L x L
- * matrix is stored.  Not combined with row sharding in this build. */
+ * matrix is stored.  With row sharding the U allgather is replaced by a halo exchange of W rows
+ * (1d) or W*Lx rows (2d, whole lattice rows per shard required) with the neighbouring shards. */
 enum { TRAJ_PROP_DENSE = 0, TRAJ_PROP_BANDED = 1 };
 
 /* Device bytes the handle needs for cfg (the caller allocates them, e.g. with torch).

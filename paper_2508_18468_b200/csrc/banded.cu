@@ -29,7 +29,7 @@ template <int W, int RPT = Rpt<W>::value>
 __global__ void __launch_bounds__(TC * RG) banded_kernel(const cplx* __restrict__ U, cplx* __restrict__ V,
                                                          long long ld, long long sU, int N, int len, int lines,
                                                          long long line_stride, long long pos_stride,
-                                                         const cplx* __restrict__ coef) {
+                                                         const cplx* __restrict__ coef, int periodic) {
   __shared__ double2 c[2 * W + 1];
   for (int i = threadIdx.x; i < 2 * W + 1; i += blockDim.x) c[i] = coef[i];
   __syncthreads();
@@ -44,7 +44,8 @@ __global__ void __launch_bounds__(TC * RG) banded_kernel(const cplx* __restrict_
 #pragma unroll
   for (int q = 0; q < RPT + 2 * W; ++q) {
     int p = p0 - W + q;
-    p = ((p % len) + len) % len;
+    if (periodic) p = ((p % len) + len) % len;
+    else p = p0 + q;      // halo mode: the input carries W extra positions on each side
     in[q] = u[(long long)p * pos_stride * ld];
   }
 #pragma unroll
@@ -65,11 +66,11 @@ __global__ void __launch_bounds__(TC * RG) banded_kernel(const cplx* __restrict_
 
 template <int W>
 cudaError_t launch(cudaStream_t st, const cplx* U, cplx* V, long long ld, long long sU, int N, int len, int lines,
-                   long long ls, long long ps, const cplx* coef, int T) {
+                   long long ls, long long ps, const cplx* coef, int T, int periodic) {
   constexpr int RPT = Rpt<W>::value;
   const int tiles = (len + RPT * RG - 1) / (RPT * RG);
   dim3 grid((unsigned)(tiles * lines), (unsigned)ceil_div(N, TC), (unsigned)T);
-  banded_kernel<W><<<grid, TC * RG, 0, st>>>(U, V, ld, sU, N, len, lines, ls, ps, coef);
+  banded_kernel<W><<<grid, TC * RG, 0, st>>>(U, V, ld, sU, N, len, lines, ls, ps, coef, periodic);
   count_launch();
   return cudaGetLastError();
 }
@@ -83,16 +84,17 @@ int banded_template_width(int w) {
 }
 
 int banded_pass(cudaStream_t st, const cplx* U, cplx* V, long long ld, long long sU, int N, int T, int len, int lines,
-                long long line_stride, long long pos_stride, const cplx* coef, int W, std::string* err) {
+                long long line_stride, long long pos_stride, const cplx* coef, int W, std::string* err,
+                int periodic) {
   cudaError_t e;
   switch (W) {
-    case 2: e = launch<2>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T); break;
-    case 4: e = launch<4>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T); break;
-    case 8: e = launch<8>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T); break;
-    case 12: e = launch<12>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T); break;
-    case 16: e = launch<16>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T); break;
-    case 24: e = launch<24>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T); break;
-    case 32: e = launch<32>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T); break;
+    case 2: e = launch<2>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T, periodic); break;
+    case 4: e = launch<4>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T, periodic); break;
+    case 8: e = launch<8>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T, periodic); break;
+    case 12: e = launch<12>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T, periodic); break;
+    case 16: e = launch<16>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T, periodic); break;
+    case 24: e = launch<24>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T, periodic); break;
+    case 32: e = launch<32>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T, periodic); break;
     default:
       if (err) *err = "banded_pass: unsupported template width";
       return 1;

@@ -20,6 +20,7 @@
 #include "monitor.h"
 #include "shard.h"
 #include "zgemm.h"
+#include "banded.h"
 
 namespace traj {
 
@@ -100,6 +101,51 @@ int ShardComm::allreduce(cudaStream_t st, double* const* part, double* out, size
   return 0;
 }
 
+int ShardComm::halo(cudaStream_t st, void* const* send_lo, void* const* send_hi, void* const* recv_lo,
+                    void* const* recv_hi, size_t bytes, std::string* err) {
+  if (comm) {
+    const int me = rank0, left = (me + P - 1) % P, right = (me + 1) % P;
+    // NCCL pairs operations to the same peer in FIFO order; with P <= 2 left == right, so the
+    // sends go (high block -> right, low block -> left) to meet the receives (low halo from the
+    // left, high halo from the right) in the same order on the partner.
+    ncclGroupStart();
+    ncclSend(send_hi[0], bytes, ncclUint8, right, comm, st);
+    ncclSend(send_lo[0], bytes, ncclUint8, left, comm, st);
+    ncclRecv(recv_lo[0], bytes, ncclUint8, left, comm, st);
+    ncclRecv(recv_hi[0], bytes, ncclUint8, right, comm, st);
+    ncclResult_t r = ncclGroupEnd();
+    if (r != ncclSuccess) {
+      if (err) *err = std::string("nccl halo exchange: ") + ncclGetErrorString(r);
+      return TRAJ_ENCCL;
+    }
+    return 0;
+  }
+  for (int s = 0; s < P_local; ++s) {
+    const int left = (s + P - 1) % P, right = (s + 1) % P;
+    cudaError_t e = cudaMemcpyAsync(recv_lo[s], send_hi[left], bytes, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(recv_hi[s], send_lo[right], bytes, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) {
+      if (err) *err = cuerr("halo (emulated)", e);
+      return TRAJ_ECUDA;
+    }
+  }
+  return 0;
+}
+
+bool shard_banded_fits(const traj_config* c, int Wx, int Wy, std::string* why) {
+  const long long L = c->Lx * c->Ly, Lp = L / c->shard_size;
+  const long long H = c->Ly > 1 ? (long long)Wy * c->Lx : Wx;
+  if (c->Ly > 1 && Lp % c->Lx) {
+    *why = "banded + sharded 2d needs whole lattice rows per shard (Ly divisible by shard_size)";
+    return false;
+  }
+  if (H > Lp) {
+    *why = "banded + sharded needs the halo (W rows in 1d, W*Lx in 2d) within one neighbouring shard";
+    return false;
+  }
+  return true;
+}
+
 int nccl_unique_id(void* out128, std::string* err) {
   ncclUniqueId id;
   ncclResult_t r = ncclGetUniqueId(&id);
@@ -137,7 +183,7 @@ int shard_validate(const traj_config* c, std::string* why) {
   return 0;
 }
 
-size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork) {
+size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, bool banded, int Wx, int Wy) {
   Lay lay;
   lay.base = base;
   const long long L = c->Lx * c->Ly, N = c->N;
@@ -159,6 +205,10 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork) 
   sh->cap = sh->capr * P;
   sh->ldcap = round_up(std::max(sh->cap, 1), 8);
   sh->lwork = lwork;
+  sh->banded = banded;
+  sh->Wx = Wx;
+  sh->Wy = Wy;
+  sh->H = banded ? (c->Ly > 1 ? Wy * (int)c->Lx : Wx) : 0;
   const long long Lp = sh->Lp, ldN = sh->ldN, ldL = sh->ldL, ldcap = sh->ldcap;
   const int capr = sh->capr, cap = sh->cap;
   sh->loc.assign(sh->comm.P_local, ShardLocal());
@@ -170,7 +220,8 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork) 
     ShardLocal& l = sh->loc[s];
     l.g = sh->comm.rank0 + s;
     l.row0 = (int)(l.g * Lp);
-    lay.take(l.K, (size_t)Lp * ldL * 16);
+    if (banded) lay.take(l.Uext, (size_t)(Lp + 2 * sh->H) * ldN * 16);
+    else lay.take(l.K, (size_t)Lp * ldL * 16);
     lay.take(l.U[0], (size_t)Lp * ldN * 16);
     lay.take(l.U[1], (size_t)Lp * ldN * 16);
     if (emulate) lay.take(l.Gpart, (size_t)N * ldN * 16);
@@ -183,6 +234,7 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork) 
       lay.take(l.Tm, (size_t)Lp * ldcap * 16);
     }
   }
+  if (banded) lay.take(sh->bcoef, (size_t)(2 * Wx + 2 * Wy + 2) * 16);
   lay.take(sh->gamma_dev, 16);
   lay.take(sh->failed_dev, 16);
   lay.take(sh->eig_w, (size_t)N * 8);
@@ -249,13 +301,15 @@ int shard_init(ShardedCtx* sh, const traj_config* c, std::string* err) {
 
 // upload the K coefficient rows and the initial occupied sites, build K blocks and U0
 int shard_build(ShardedCtx* sh, const std::vector<std::complex<double>>& kc, const std::vector<int32_t>& sites,
-                std::string* err) {
+                std::string* err, const std::vector<std::complex<double>>* band) {
   cudaStream_t st = sh->st;
+  if (sh->banded) SCK(cudaMemcpyAsync(sh->bcoef, band->data(), band->size() * 16, cudaMemcpyHostToDevice, st));
   SCK(cudaMemcpyAsync(sh->kcoef, kc.data(), kc.size() * 16, cudaMemcpyHostToDevice, st));
   SCK(cudaMemcpyAsync(sh->sites, sites.data(), sites.size() * 4, cudaMemcpyHostToDevice, st));
   SCK(cudaMemcpyAsync(sh->gamma_dev, &sh->gamma, 8, cudaMemcpyHostToDevice, st));
   for (auto& l : sh->loc) {
-    if (build_k(st, l.K, sh->ldL, sh->Lx, sh->Ly, sh->kcoef, sh->kcoef + sh->Lx, err, l.row0, sh->Lp)) return 4;
+    if (!sh->banded && build_k(st, l.K, sh->ldL, sh->Lx, sh->Ly, sh->kcoef, sh->kcoef + sh->Lx, err, l.row0, sh->Lp))
+      return 4;
     if (init_state(st, l.U[0], sh->ldN, 0, sh->sites, sh->N, 1, err, l.row0, sh->Lp)) return 4;
   }
   SCK(cudaStreamSynchronize(st));
@@ -390,11 +444,46 @@ int projective(ShardedCtx* sh, int which, long long step, std::string* err) {
   return 0;
 }
 
+// NEXT-1 with sharding: 1d -- halo of W rows from each neighbour, one non-periodic pass;
+// 2d -- the x pass is local (whole lattice rows per shard), then a halo of W*Lx rows for the
+// y pass.  Uext = [H halo rows | Lp local rows | H halo rows].
+int propagate_banded(ShardedCtx* sh, int cur, int nxt, std::string* err) {
+  cudaStream_t st = sh->st;
+  const long long H = sh->H, Lp = sh->Lp, ld = sh->ldN;
+  const bool twod = sh->Ly > 1;
+  std::vector<void*> slo, shi, rlo, rhi;
+  for (auto& l : sh->loc) {
+    cplx* mid = l.Uext + H * ld;
+    if (twod) {
+      STRY(banded_pass(st, l.U[cur], mid, ld, 0, sh->N, 1, sh->Lx, (int)(Lp / sh->Lx), sh->Lx, 1, sh->bcoef, sh->Wx,
+                       err));
+    } else {
+      SCK(cudaMemcpyAsync(mid, l.U[cur], (size_t)Lp * ld * 16, cudaMemcpyDeviceToDevice, st));
+    }
+    slo.push_back(mid);
+    shi.push_back(mid + (Lp - H) * ld);
+    rlo.push_back(l.Uext);
+    rhi.push_back(mid + Lp * ld);
+  }
+  STRY(sh->comm.halo(st, slo.data(), shi.data(), rlo.data(), rhi.data(), (size_t)H * ld * 16, err));
+  for (auto& l : sh->loc) {
+    if (twod)
+      STRY(banded_pass(st, l.Uext, l.U[nxt], ld, 0, sh->N, 1, (int)(Lp / sh->Lx), sh->Lx, 1, sh->Lx,
+                       sh->bcoef + 2 * sh->Wx + 1, sh->Wy, err, 0));
+    else
+      STRY(banded_pass(st, l.Uext, l.U[nxt], ld, 0, sh->N, 1, (int)Lp, 1, 0, 1, sh->bcoef, sh->Wx, err, 0));
+  }
+  return 0;
+}
+
 }  // namespace
 
 int shard_step(ShardedCtx* sh, long long* step, std::string* err) {
   const int cur = sh->cur, nxt = 1 - sh->cur;
-  {
+  if (sh->banded) {
+    Phase p(sh->prof, sh->st, TRAJ_PH_PROPAGATE);
+    STRY(propagate_banded(sh, cur, nxt, err));
+  } else {
     Phase p(sh->prof, sh->st, TRAJ_PH_PROPAGATE);
     STRY(gather_full(sh, cur, err));
     for (auto& l : sh->loc)

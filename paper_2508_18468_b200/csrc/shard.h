@@ -22,6 +22,9 @@ struct ShardComm {
   ncclComm_t comm = nullptr;
   int allgather(cudaStream_t st, void* const* send, void* recv, size_t bytes, std::string* err);
   int allreduce(cudaStream_t st, double* const* part, double* out, size_t n, std::string* err);
+  // halo exchange on the ring of shards: recv_lo[s] <- send_hi of shard g-1, recv_hi[s] <- send_lo of g+1
+  int halo(cudaStream_t st, void* const* send_lo, void* const* send_hi, void* const* recv_lo, void* const* recv_hi,
+           size_t bytes, std::string* err);
 };
 
 struct ShardLocal {
@@ -34,6 +37,7 @@ struct ShardLocal {
   int32_t* cnt = nullptr;
   cplx* USloc = nullptr;   // capr x ldN
   cplx* Tm = nullptr;      // Lp x ldcap
+  cplx* Uext = nullptr;    // banded: (H + Lp + H) x ldN, halo rows around the local block
 };
 
 struct ShardedCtx {
@@ -41,6 +45,9 @@ struct ShardedCtx {
   int L = 0, N = 0, Lx = 0, Ly = 0, P = 1, Lp = 0, capr = 0, cap = 0, lwork = 0;
   long long ldN = 0, ldL = 0, ldcap = 0;
   int protocol = 0;
+  bool banded = false;     // NEXT-1 with sharding: halo exchange instead of the allgather
+  int Wx = 0, Wy = 0, H = 0;
+  cplx* bcoef = nullptr;
   double dt = 0, J = 0, gamma = 0;
   uint64_t seed = 0;
   long long traj_base = 0;
@@ -78,10 +85,14 @@ struct ShardedCtx {
 
 // Validates the sharding fields; fills the geometry of sh.
 int shard_validate(const traj_config* c, std::string* why);
-size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork);
+// banded: the compiled half-widths (Wx, Wy) of the banded propagator, or false for the dense K
+size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, bool banded = false, int Wx = 0,
+                   int Wy = 0);
+// halo rows of the banded sharded propagator and whether they fit the shard geometry
+bool shard_banded_fits(const traj_config* c, int Wx, int Wy, std::string* why);
 int shard_init(ShardedCtx* sh, const traj_config* c, std::string* err);
 int shard_build(ShardedCtx* sh, const std::vector<std::complex<double>>& kc, const std::vector<int32_t>& sites,
-                std::string* err);
+                std::string* err, const std::vector<std::complex<double>>* band = nullptr);
 int shard_step(ShardedCtx* sh, long long* step, std::string* err);
 int shard_orthonormalize(ShardedCtx* sh, std::string* err);
 int shard_entropy(ShardedCtx* sh, const int64_t* A, int64_t nA, double* S_out, std::string* err);

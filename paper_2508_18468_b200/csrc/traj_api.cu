@@ -156,7 +156,6 @@ int validate(const traj_config* c, std::string* why) {
   }
   if (c->propagator != TRAJ_PROP_DENSE && c->propagator != TRAJ_PROP_BANDED) return bad("unknown propagator");
   if (c->shard_size != 1 || c->nccl_id) {
-    if (c->propagator == TRAJ_PROP_BANDED) return bad("the banded propagator is not combined with row sharding");
     if (c->protocol == TRAJ_HOMODYNE_RK4) return bad("the RK4 QSD protocol is not combined with row sharding");
     if (c->protocol == TRAJ_PROJECTIVE_EVENTS) return bad("the event-driven protocol is not combined with row sharding");
     return shard_validate(c, why);
@@ -792,7 +791,10 @@ int traj_workspace_bytes(const traj_config* cfg, size_t* out) {
   if ((s = eig_lwork((int)cfg->N, &lw, &why))) return fail(h, s, why);
   if (is_sharded(cfg)) {
     ShardedCtx sh;
-    *out = shard_carve(&sh, cfg, nullptr, lw);
+    int Wx = 0, Wy = 0;
+    const bool bd = banded_widths(cfg, &Wx, &Wy);
+    if (bd && !shard_banded_fits(cfg, Wx, Wy, &why)) return fail(h, TRAJ_ECONFIG, why);
+    *out = shard_carve(&sh, cfg, nullptr, lw, bd, Wx, Wy);
   } else {
     traj_ctx tmp;
     *out = carve(&tmp, cfg, nullptr, lw);
@@ -815,7 +817,10 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
     size_t need;
     if (is_sharded(cfg)) {
       ShardedCtx sh;
-      need = shard_carve(&sh, cfg, nullptr, lw);
+      int Wx = 0, Wy = 0;
+      const bool bd = banded_widths(cfg, &Wx, &Wy);
+      if (bd && !shard_banded_fits(cfg, Wx, Wy, &why)) return fail(h, TRAJ_ECONFIG, why);
+      need = shard_carve(&sh, cfg, nullptr, lw, bd, Wx, Wy);
     } else {
       traj_ctx tmp;
       need = carve(&tmp, cfg, nullptr, lw);
@@ -832,7 +837,14 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
   h->lwork = lw;
   if (is_sharded(cfg)) {
     h->sh = new ShardedCtx();
-    shard_carve(h->sh, cfg, reinterpret_cast<char*>(cfg->workspace), lw);
+    {
+      int Wx = 0, Wy = 0;
+      const bool bd = banded_widths(cfg, &Wx, &Wy);
+      shard_carve(h->sh, cfg, reinterpret_cast<char*>(cfg->workspace), lw, bd, Wx, Wy);
+      h->banded = bd;
+      h->Wx = Wx;
+      h->Wy = Wy;
+    }
     h->obs_bins = h->sh->obs_bins;
     h->obs_part = h->sh->obs_part;
     h->obs_out = h->sh->obs_out;
@@ -888,8 +900,18 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
     if (((i % h->Lx) + (i / h->Lx)) % 2 == 0) sites.push_back(i);
   if ((int)sites.size() != h->N) return bail(TRAJ_ECONFIG, "initial state does not have N particles");
   std::string e;
+  std::vector<std::complex<double>> band;
+  if (h->banded) {
+    auto axis = [&](int n, int W) {
+      std::vector<std::complex<double>> c = ring_coefficients(n, cfg->J, cfg->dt);
+      for (int d = -W; d <= W; ++d) band.push_back(c[((d % n) + n) % n]);
+    };
+    axis(h->Lx, h->Wx);
+    if (h->Ly > 1) axis(h->Ly, h->Wy);
+    else band.push_back(1.0);
+  }
   if (h->sh) {
-    int s2 = shard_build(h->sh, kc, sites, &e);
+    int s2 = shard_build(h->sh, kc, sites, &e, &band);
     if (s2) return bail(s2, e);
     *out = h;
     return 0;
@@ -899,15 +921,7 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
       cudaMemcpyAsync(h->gamma_dev, h->gamma.data(), h->T * 8, cudaMemcpyHostToDevice, h->st) != cudaSuccess)
     return bail(TRAJ_ECUDA, "upload");
   if (h->banded) {
-    std::vector<std::complex<double>> bc;
-    auto axis = [&](int n, int W) {
-      std::vector<std::complex<double>> c = ring_coefficients(n, cfg->J, cfg->dt);
-      for (int d = -W; d <= W; ++d) bc.push_back(c[((d % n) + n) % n]);
-    };
-    axis(h->Lx, h->Wx);
-    if (h->Ly > 1) axis(h->Ly, h->Wy);
-    else bc.push_back(1.0);
-    if (cudaMemcpyAsync(h->bcoef, bc.data(), bc.size() * 16, cudaMemcpyHostToDevice, h->st) != cudaSuccess)
+    if (cudaMemcpyAsync(h->bcoef, band.data(), band.size() * 16, cudaMemcpyHostToDevice, h->st) != cudaSuccess)
       return bail(TRAJ_ECUDA, "upload band");
   } else if (cfg->protocol != TRAJ_HOMODYNE_RK4 && cfg->protocol != TRAJ_PROJECTIVE_EVENTS &&
              build_k(h->st, h->K, h->ldL, h->Lx, h->Ly, h->kcoef, h->kcoef + h->Lx, &e)) {

@@ -369,3 +369,31 @@ def test_event_driven_pm_matches_oracle(P, Lx, Ly, gam):
                 assert np.abs(g.correlation(t).cpu().numpy() - o.correlation()).max() < C_TOL
                 assert abs(S[t] - o.entropy(A)) < S_TOL
     assert events > 50
+
+
+@pytest.mark.parametrize("Lx,Ly,P_shards,protocol", [(256, 1, 4, "projective"), (240, 1, 2, "homodyne"),
+                                                     (12, 12, 3, "projective"), (10, 8, 2, "homodyne")])
+def test_row_sharded_banded_halo_matches_oracle(P, Lx, Ly, P_shards, protocol):
+    """NEXT-1 with sharding: the halo exchange (W rows in 1d, W*Lx rows for the 2d y pass)
+    replaces the allgather; lockstep with the oracle's dense K."""
+    gam = 3.0 if protocol == "projective" else 1.0
+    g = P.Trajectories(Lx, Ly, protocol, [gam], seed=21, shard_size=P_shards, propagator="banded")
+    K = lattice.propagator_lattice(Lx, Ly, 1.0, 0.05)
+    o = OracleTrajectory(Lx, Ly, protocol, gam, 0.05, seed=21, traj=0, K=K)
+    A = np.arange(Lx * Ly // 2)
+    for s in range(20):
+        g.step(1)
+        o.step(1)
+    assert np.abs(g.correlation(0).cpu().numpy() - o.correlation()).max() < C_TOL
+    assert abs(g.entropy(A)[0] - o.entropy(A)) < S_TOL
+
+
+def test_row_sharded_banded_nccl_single_rank(P):
+    """Halo exchange through NCCL send/recv with a one-rank communicator (neighbours = self)."""
+    uid = P.traj_nccl_unique_id()
+    a = P.Trajectories(128, 1, "homodyne", [1.0], seed=5, shard_size=1, nccl_id=uid, propagator="banded")
+    b = P.Trajectories(128, 1, "homodyne", [1.0], seed=5)
+    a.step(10)
+    b.step(10)
+    assert np.abs(a.correlation(0).cpu().numpy() - b.correlation(0).cpu().numpy()).max() < 1e-12
+    a.close()
