@@ -342,17 +342,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int g = lane >> 2, slot = lane & 3;
   constexpr unsigned long long SIGN = 0x8000000000000000ull;
   constexpr unsigned long long ma = CONJ_A ? SIGN : 0ull, mb = CONJ_B ? SIGN : 0ull;
-  uint32_t offA[4], offB[2];   // per-lane offsets of (row, k = 2*slot) inside an 8-k sub-tile
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int r = warp_m * 32 + 8 * i + g;
-    offA[i] = CONJ_A ? off_mn(r, 2 * slot) : off_kc(r, 2 * slot);
-  }
-#pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const int r = warp_n * 16 + 8 * j + g;
-    offB[j] = CONJ_B ? off_kc(r, 2 * slot) : off_mn(r, 2 * slot);
-  }
   double acc[4][2][3][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -373,8 +362,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     return reinterpret_cast<const double2*>(base + g3::A_BYTES + (q >> 1) * g3::B_SUB +
                                             (CONJ_B ? off_kc(r, k) : off_mn(r, k)));
   };
-  (void)offA;
-  (void)offB;
   for (int it = 0; it < nk; ++it) {
     const int s = it % ST3;
     if (issuer) try_issue(it, true);
@@ -543,17 +530,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int g = lane >> 2, slot = lane & 3;
   constexpr unsigned long long SIGN = 0x8000000000000000ull;
   constexpr unsigned long long ma = CONJ_A ? SIGN : 0ull, mb = CONJ_B ? SIGN : 0ull;
-  uint32_t offA[4], offB[4];   // per-lane offsets of (row, k = 2*slot) inside an 8-k sub-tile
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int r = warp_m * 32 + 8 * i + g;
-    offA[i] = CONJ_A ? off_mn(r, 2 * slot) : off_kc(r, 2 * slot);
-  }
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int r = warp_n * 32 + 8 * j + g;
-    offB[j] = CONJ_B ? off_kc(r, 2 * slot) : off_mn(r, 2 * slot);
-  }
   double acc[4][4][3][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -574,8 +550,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     return reinterpret_cast<const double2*>(base + g3w::A_BYTES + (q >> 1) * g3w::B_SUB +
                                             (CONJ_B ? off_kc(r, k) : off_mn(r, k)));
   };
-  (void)offA;
-  (void)offB;
   for (int it = 0; it < nk; ++it) {
     const int s = it % ST3;
     if (issuer) try_issue(it, true);
