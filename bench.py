@@ -53,6 +53,7 @@ def parse():
                         "projective_events (NEXT-4)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-observables", action="store_true")
     p.add_argument("--cpu-budget", type=float, default=120.0, help="seconds of oracle work (reference arm)")
     return p.parse_args()
 
@@ -228,6 +229,21 @@ def run_ours(args):
                   "gram": 2 * 4.0 * rows * w.N * w.N * tpg, "trmm": 2 * 4.0 * rows * w.N * w.N * tpg,
                   "chol": (8.0 / 3.0) * w.N ** 3 * tpg}
     dense_tflops = sum(step_flops.values()) * args.steps / (ms / 1e3) / 1e12
+    # ---- row a4, timed separately (north star: "eigvalsh on C_A at sampled times, timed
+    # separately"): the config's sampled observables once, after the timed steps
+    obs = None
+    if not args.no_observables and not shard:
+        obs = {}
+        for name, region in w.regions.items():
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            if isinstance(region, tuple):
+                tr.mutual_info(*region)
+                kind = "I2"
+            else:
+                tr.entropy(region)
+                kind = "S_A"
+            obs[f"{kind}:{name}"] = 1e3 * (time.perf_counter() - t0)
     tr.close()
     del tr
     torch.cuda.empty_cache()
@@ -263,6 +279,7 @@ def run_ours(args):
         "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
         "phase_launches_per_step": {k: v[1] / args.steps for k, v in phases.items()},
         "gpu_launches": launches,
+        "sampled_observables_ms": obs,
         "clocks": clk,
         "e2e": e2e,
     }
