@@ -397,3 +397,25 @@ def test_row_sharded_banded_nccl_single_rank(P):
     b.step(10)
     assert np.abs(a.correlation(0).cpu().numpy() - b.correlation(0).cpu().numpy()).max() < 1e-12
     a.close()
+
+
+@pytest.mark.parametrize("protocol,gam", [("homodyne", 0.5), ("projective", 1.0)])
+def test_long_run_trajectory_averaged_entropy(P, protocol, gam):
+    """North star: trajectory-averaged S_A within statistical error over long runs (here 600
+    steps, t = 30, 24 trajectories at L = 128): Welch-type |mean_gpu - mean_oracle| < 3 sigma at
+    every sample time.  The trajectories also stay individually close (contraction of
+    perturbations), which the looser ensemble bound does not rely on."""
+    L, T, steps, every = 128, 24, 600, 100
+    A = np.arange(L // 2)
+    g = P.Trajectories(L, 1, protocol, [gam] * T, seed=31)
+    K = lattice.propagator_lattice(L, 1, 1.0, 0.05)
+    orc = [OracleTrajectory(L, 1, protocol, gam, 0.05, seed=31, traj=t, K=K) for t in range(T)]
+    for s in range(every, steps + 1, every):
+        g.step(every)
+        for o in orc:
+            o.step(every)
+        sg = g.entropy(A)
+        so = np.array([o.entropy(A) for o in orc])
+        sigma = np.sqrt(sg.var(ddof=1) / T + so.var(ddof=1) / T)
+        assert abs(sg.mean() - so.mean()) < 3 * sigma + 1e-12
+        assert np.abs(sg - so).max() < 1e-6
