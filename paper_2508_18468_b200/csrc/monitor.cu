@@ -634,6 +634,17 @@ __global__ void accumulate_kernel(const double* part, int n, double* out) {
   }
 }
 
+// upper triangle of each n x n batch entry set to the identity
+__global__ void set_identity_kernel(cplx* G, long long ld, long long sG, int n) {
+  const int t = blockIdx.y;
+  const long long total = (long long)n * n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / n), j = (int)(idx % n);
+    if (i <= j) G[t * sG + (long long)i * ld + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+  }
+}
+
 // out += in (n doubles): the single-GPU emulation of an all-reduce
 __global__ void add_kernel(double* out, const double* in, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -653,6 +664,13 @@ int masked_abs2(cudaStream_t st, const cplx* C, long long ld, int R, int ncols, 
   accumulate_kernel<<<1, 32, 0, st>>>(part, blocks, out);
   count_launch(2);
   return last(err, "masked_abs2") == cudaSuccess ? 0 : 4;
+}
+
+int set_identity(cudaStream_t st, cplx* G, long long ld, long long sG, int n, int T, std::string* err) {
+  dim3 grid((unsigned)std::min<long long>(ceil_div((long long)n * n, 256), 8192), T);
+  set_identity_kernel<<<grid, 256, 0, st>>>(G, ld, sG, n);
+  count_launch();
+  return last(err, "set_identity") == cudaSuccess ? 0 : 4;
 }
 
 int add_inplace(cudaStream_t st, double* out, const double* in, long long n, std::string* err) {

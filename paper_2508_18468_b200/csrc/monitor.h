@@ -50,6 +50,8 @@ int bin_abs2(cudaStream_t st, const cplx* C, long long ld, int R, int row0, int 
 // out[0] += sum_{i<R, mask[j]} |C[i][j]|^2 (part: >= 1024 doubles of scratch)
 int masked_abs2(cudaStream_t st, const cplx* C, long long ld, int R, int ncols, const int32_t* mask, double* part,
                 double* out, std::string* err);
+// upper triangle of every n x n batch entry := identity
+int set_identity(cudaStream_t st, cplx* G, long long ld, long long sG, int n, int T, std::string* err);
 // out[i] += in[i]
 int add_inplace(cudaStream_t st, double* out, const double* in, long long n, std::string* err);
 // out[t] = max_{i<=j} |G_ij - delta_ij| (as the bit pattern of a non-negative double)

@@ -76,6 +76,8 @@ struct traj_ctx {
   unsigned long long* gdev = nullptr;   // per-trajectory max |G2 - I| of the second CQR pass
   int32_t* region = nullptr;
   bool full_cqr2 = false;                // TRAJ_CQR2_FULL=1: always factor G2 by chol_inverse
+  bool lowrank_gram = true;              // TRAJ_LOWRANK_GRAM=0: always measure the first Gram
+  int lr_k0 = -1;                        // >= 0: pass-1 Gram of this step = I - V^dag V, V (k0 rows) in US
   double* obs_bins = nullptr;            // C(r) accumulators [L]
   double* obs_part = nullptr;            // reduction partials [1024]
   double* obs_out = nullptr;             // [n_traj]
@@ -323,11 +325,21 @@ std::vector<std::complex<double>> ring_coefficients(int n, double J, double dt) 
 int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
   cplx* src = U;
   cplx* dst = tmp;
+  const int lr = h->lr_k0;
+  h->lr_k0 = -1;
   for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 0 && lr == 0) continue;     // no row zeroed: U is orthonormal, pass 1 has R = I
     {
       Phase p(&h->prof, h->st, TRAJ_PH_GRAM);
-      TRY(zgemm(h->st, 1, 0, h->N, h->N, h->L, 1.0, 0.0, src, h->ldN, h->sU, src, h->ldN, h->sU, 0.0, h->G, h->ldN,
-                h->sG, h->T, TRAJ_C_UPPER_F, &h->err));
+      if (pass == 0 && lr > 0) {
+        // G = U'^dag U' = I - V^dag V (upper tiles): 4 N^2 k0 instead of 4 L N^2 flops
+        TRY(set_identity(h->st, h->G, h->ldN, h->sG, h->N, h->T, &h->err));
+        TRY(zgemm(h->st, 1, 0, h->N, h->N, lr, -1.0, 0.0, h->US, h->ldN, h->sUS, h->US, h->ldN, h->sUS, 1.0, h->G,
+                  h->ldN, h->sG, h->T, TRAJ_C_UPPER_F, &h->err));
+      } else {
+        TRY(zgemm(h->st, 1, 0, h->N, h->N, h->L, 1.0, 0.0, src, h->ldN, h->sU, src, h->ldN, h->sU, 0.0, h->G,
+                  h->ldN, h->sG, h->T, TRAJ_C_UPPER_F, &h->err));
+      }
     }
     {
       Phase p(&h->prof, h->st, TRAJ_PH_CHOL);
@@ -357,6 +369,9 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
     }
     std::swap(src, dst);
   }
+  if (lr == 0) {   // one pass ran: the result is in tmp
+    CK(cudaMemcpyAsync(U, tmp, (size_t)h->T * h->sU * 16, cudaMemcpyDeviceToDevice, h->st));
+  }
   return 0;   // two passes: result back in U
 }
 
@@ -375,7 +390,10 @@ int projective(traj_ctx* h, cplx* U) {
                                         std::to_string(cap));
     maxc = std::max(maxc, h->h_small[t]);
   }
-  if (maxc == 0) return 0;
+  if (maxc == 0) {            // no click: U = K U is orthonormal, pass 1 of CQR2 has R = I
+    if (h->lowrank_gram) h->lr_k0 = 0;
+    return 0;
+  }
   TRY(gather_rows(h->st, U, h->ldN, h->sU, h->S, cap, h->count, maxc, T, h->US, h->ldN, h->sUS, h->N, &h->err));
   // C_SS = U_S U_S^dag (all trajectories padded to maxc rows; rows beyond a trajectory's
   // count are never read by the sampler)
@@ -415,6 +433,14 @@ int projective(traj_ctx* h, cplx* U) {
     // U <- U - Tm W^dag
     TRY(zgemm(h->st, 0, 1, h->L, h->N, k1max, -1.0, 0.0, h->Tm, h->ldcap, sT, h->W, h->ldcap, sW, 1.0, U, h->ldN,
               h->sU, T, 0, &h->err));
+  }
+  // U is orthonormal here (K unitary, the rank-k update exact), so after zeroing rows S0 the
+  // first CholeskyQR Gram is I - V^dag V with V the k0 zeroed rows: keep V (zero-padded).
+  if (h->lowrank_gram) {
+    if (k0max > 0)
+      TRY(gather_rows(h->st, U, h->ldN, h->sU, h->S0, cap, h->k0, k0max, T, h->US, h->ldN, h->sUS, h->N, &h->err, 0,
+                      1));
+    h->lr_k0 = k0max;
   }
   if (k0max > 0) TRY(zero_rows_batched(h->st, U, h->ldN, h->sU, h->S0, cap, h->k0, k0max, T, h->N, &h->err));
   return 0;
@@ -875,6 +901,8 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
   {
     const char* e = getenv("TRAJ_CQR2_FULL");
     h->full_cqr2 = e && e[0] == '1';
+    const char* g = getenv("TRAJ_LOWRANK_GRAM");
+    h->lowrank_gram = !(g && g[0] == '0');
   }
   if (cusolverDnCreate(&h->solver) != CUSOLVER_STATUS_SUCCESS) return bail(TRAJ_ECUDA, "cusolverDnCreate");
   cusolverDnSetStream(h->solver, h->st);

@@ -419,3 +419,24 @@ def test_long_run_trajectory_averaged_entropy(P, protocol, gam):
         sigma = np.sqrt(sg.var(ddof=1) / T + so.var(ddof=1) / T)
         assert abs(sg.mean() - so.mean()) < 3 * sigma + 1e-12
         assert np.abs(sg - so).max() < 1e-6
+
+
+def test_projective_lowrank_first_gram_matches_measured(P):
+    """The projective step forms CholeskyQR2's first Gram as I - V^dag V (V: the rows zeroed by
+    the empty outcomes; U is orthonormal before zeroing) instead of U'^dag U'; the second pass
+    measures the Gram.  Same state as with the measured first Gram (TRAJ_LOWRANK_GRAM=0)."""
+    import os
+    args = (300, 1, "projective", [3.0, 0.5])
+    a = P.Trajectories(*args, seed=17)
+    os.environ["TRAJ_LOWRANK_GRAM"] = "0"
+    try:
+        b = P.Trajectories(*args, seed=17)
+    finally:
+        del os.environ["TRAJ_LOWRANK_GRAM"]
+    a.step(40)
+    b.step(40)
+    for t in range(2):
+        assert a.last_clicks(t) == b.last_clicks(t)
+        assert np.abs(a.correlation(t).cpu().numpy() - b.correlation(t).cpu().numpy()).max() < 1e-12
+        U = a.get_state(t).cpu().numpy()
+        assert np.abs(U.conj().T @ U - np.eye(150)).max() < 1e-13
