@@ -48,6 +48,8 @@ def parse():
                         "row-sharded over the GPUs (NCCL allgather + Gram allreduce, strong scaling)")
     p.add_argument("--propagator", choices=["dense", "banded"], default="dense",
                    help="dense: the north star's dense K U (default); banded: NEXT-1 stencil passes")
+    p.add_argument("--orthonormalizer", choices=["cqr2", "lowrank"], default="cqr2",
+                   help="cqr2: CholeskyQR2 (north star); lowrank: NEXT-1 low-rank first pass for the projective step")
     p.add_argument("--protocol", default=None,
                    help="override the config's protocol: projective | homodyne | homodyne_rk4 (NEXT-2) | "
                         "projective_events (NEXT-4)")
@@ -170,7 +172,7 @@ def run_ours(args):
         gam = [w.gammas[(rank * tpg + t) % len(w.gammas)] for t in range(tpg)]
         base = rank * tpg
         tr = P.Trajectories(w.Lx, w.Ly, w.protocol, gam, dt=w.dt, J=w.J, seed=w.seed, traj_base=base,
-                            propagator=args.propagator)
+                            propagator=args.propagator, orthonormalizer=args.orthonormalizer)
     st = tr.stream
     for _ in range(args.warmup):
         tr.step(1)
@@ -265,7 +267,7 @@ def run_ours(args):
         "dtype": "c128 (f64 arithmetic)", "data": "synthetic (Neel start, Philox randoms, seed 0)",
         "config": dict(describe(w, tpg), parallelism=(f"row-sharded K,U over {world} GPU(s) (NCCL)" if shard
                                                       else f"trajectory-parallel dp{world}"),
-                       propagator=args.propagator),
+                       propagator=args.propagator, orthonormalizer=args.orthonormalizer),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                      "kernel": kern[dom][1] + ("; per shard (L/P rows) when row-sharded" if shard else ""),

@@ -96,7 +96,17 @@ typedef struct {
   void* workspace;          /* device memory, >= traj_workspace_bytes, 256-byte aligned        */
   size_t workspace_bytes;
   int32_t propagator;       /* TRAJ_PROP_DENSE (the north star's dense K U) or TRAJ_PROP_BANDED */
+  int32_t orthonormalizer;  /* TRAJ_ORTH_CQR2 (default) or TRAJ_ORTH_LOWRANK (projective only)   */
 } traj_config;
+
+/* Orthonormalisation of the projective step.  CQR2: CholeskyQR2 (its first Gram formed from the
+ * rows zeroed by the empty outcomes).  LOWRANK ("orthonormalise the projective
+ * step at low rank"): U is orthonormal before k0 rows V are zeroed, so U' (I + V^dag F V) with
+ * F = Z^2 (Z + I)^-1, Z = (I - V V^dag)^(-1/2) (coupled Newton-Schulz on the k0 x k0 block) is
+ * orthonormal -- two O(L N k0) GEMMs instead of pass 1's Cholesky and triangular multiply; the
+ * second CholeskyQR pass (measured Gram) follows.  Falls back to CQR2 if the iteration does not
+ * converge in 100 steps. */
+enum { TRAJ_ORTH_CQR2 = 0, TRAJ_ORTH_LOWRANK = 1 };
 
 /* Propagator of step (a).  DENSE: U <- K U with the dense L x L K on the FP64 tensor pipe
  * (8 L^2 N flops).  BANDED: K is a circulant per lattice axis whose

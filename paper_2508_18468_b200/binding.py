@@ -46,6 +46,7 @@ class TrajConfig(ctypes.Structure):
         ("workspace", ctypes.c_void_p),
         ("workspace_bytes", ctypes.c_size_t),
         ("propagator", ctypes.c_int32),
+        ("orthonormalizer", ctypes.c_int32),
     ]
 
 
@@ -199,7 +200,7 @@ class Trajectories:
     def __init__(self, Lx: int, Ly: int = 1, protocol: str = "projective", gammas=(0.5,), dt: float = 0.05,
                  J: float = 1.0, seed: int = 0, traj_base: int = 0, device=None, stream=None,
                  shard_size: int = 1, shard_rank: int = 0, nccl_id: bytes | None = None,
-                 propagator: str = "dense"):
+                 propagator: str = "dense", orthonormalizer: str = "cqr2"):
         import torch
         self._torch = torch
         lib_ = lib()
@@ -227,6 +228,7 @@ class Trajectories:
         cfg.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p) if nccl_id is not None else None
         cfg.stream = self.stream.cuda_stream
         cfg.propagator = {"dense": TRAJ_PROP_DENSE, "banded": TRAJ_PROP_BANDED}[propagator]
+        cfg.orthonormalizer = {"cqr2": 0, "lowrank": 1}[orthonormalizer]
         nbytes = ctypes.c_size_t(0)
         _check(lib_.traj_workspace_bytes(ctypes.byref(cfg), ctypes.byref(nbytes)))
         self.workspace = torch.empty(nbytes.value + 256, dtype=torch.uint8, device=self.device)

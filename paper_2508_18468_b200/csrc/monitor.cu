@@ -645,6 +645,19 @@ __global__ void set_identity_kernel(cplx* G, long long ld, long long sG, int n) 
   }
 }
 
+// X = a X + b I on every n x n batch entry (full matrix)
+__global__ void axpby_identity_kernel(cplx* X, long long ld, long long sX, int n, double a, double b) {
+  const int t = blockIdx.y;
+  const long long total = (long long)n * n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / n), j = (int)(idx % n);
+    cplx* p = X + t * sX + (long long)i * ld + j;
+    const double2 v = *p;
+    *p = make_double2(a * v.x + (i == j ? b : 0.0), a * v.y);
+  }
+}
+
 // out += in (n doubles): the single-GPU emulation of an all-reduce
 __global__ void add_kernel(double* out, const double* in, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -664,6 +677,14 @@ int masked_abs2(cudaStream_t st, const cplx* C, long long ld, int R, int ncols, 
   accumulate_kernel<<<1, 32, 0, st>>>(part, blocks, out);
   count_launch(2);
   return last(err, "masked_abs2") == cudaSuccess ? 0 : 4;
+}
+
+int axpby_identity(cudaStream_t st, cplx* X, long long ld, long long sX, int n, int T, double a, double b,
+                   std::string* err) {
+  dim3 grid((unsigned)std::min<long long>(ceil_div((long long)n * n, 256), 8192), T);
+  axpby_identity_kernel<<<grid, 256, 0, st>>>(X, ld, sX, n, a, b);
+  count_launch();
+  return last(err, "axpby_identity") == cudaSuccess ? 0 : 4;
 }
 
 int set_identity(cudaStream_t st, cplx* G, long long ld, long long sG, int n, int T, std::string* err) {

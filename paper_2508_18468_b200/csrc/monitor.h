@@ -50,6 +50,9 @@ int bin_abs2(cudaStream_t st, const cplx* C, long long ld, int R, int row0, int 
 // out[0] += sum_{i<R, mask[j]} |C[i][j]|^2 (part: >= 1024 doubles of scratch)
 int masked_abs2(cudaStream_t st, const cplx* C, long long ld, int R, int ncols, const int32_t* mask, double* part,
                 double* out, std::string* err);
+// X = a X + b I (full n x n batch entries)
+int axpby_identity(cudaStream_t st, cplx* X, long long ld, long long sX, int n, int T, double a, double b,
+                   std::string* err);
 // upper triangle of every n x n batch entry := identity
 int set_identity(cudaStream_t st, cplx* G, long long ld, long long sG, int n, int T, std::string* err);
 // out[i] += in[i]

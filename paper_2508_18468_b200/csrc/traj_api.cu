@@ -77,6 +77,9 @@ struct traj_ctx {
   int32_t* region = nullptr;
   bool full_cqr2 = false;                // TRAJ_CQR2_FULL=1: always factor G2 by chol_inverse
   bool lowrank_gram = true;              // TRAJ_LOWRANK_GRAM=0: always measure the first Gram
+  bool lowrank_orth = false;             // TRAJ_ORTH_LOWRANK
+  cplx *Mb = nullptr, *Yb = nullptr, *Zb = nullptr, *Tb = nullptr, *Pb = nullptr, *Qb = nullptr, *FV = nullptr;
+  long long lowrank_iters = 0, lowrank_fallbacks = 0;
   int lr_k0 = -1;                        // >= 0: pass-1 Gram of this step = I - V^dag V, V (k0 rows) in US
   double* obs_bins = nullptr;            // C(r) accumulators [L]
   double* obs_part = nullptr;            // reduction partials [1024]
@@ -157,9 +160,12 @@ int validate(const traj_config* c, std::string* why) {
     if (c->protocol == TRAJ_PROJECTIVE && g * c->dt > 1.0) return bad("projective needs gamma*dt <= 1 (Q10)");
   }
   if (c->propagator != TRAJ_PROP_DENSE && c->propagator != TRAJ_PROP_BANDED) return bad("unknown propagator");
+  if (c->orthonormalizer != TRAJ_ORTH_CQR2 && c->orthonormalizer != TRAJ_ORTH_LOWRANK)
+    return bad("unknown orthonormalizer");
   if (c->shard_size != 1 || c->nccl_id) {
     if (c->protocol == TRAJ_HOMODYNE_RK4) return bad("the RK4 QSD protocol is not combined with row sharding");
     if (c->protocol == TRAJ_PROJECTIVE_EVENTS) return bad("the event-driven protocol is not combined with row sharding");
+    if (c->orthonormalizer == TRAJ_ORTH_LOWRANK) return bad("the low-rank orthonormaliser is not combined with row sharding");
     return shard_validate(c, why);
   }
   if (c->shard_rank != 0) return bad("shard_rank must be 0 without sharding");
@@ -279,6 +285,10 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     lay.take(h->chol_scratch_small, chol_scratch_bytes(cap, T));
     lay.take(h->W, (size_t)T * N * ldcap * 16);
     lay.take(h->Tm, (size_t)T * L * ldcap * 16);
+    if (c->orthonormalizer == TRAJ_ORTH_LOWRANK) {
+      for (cplx** b : {&h->Mb, &h->Yb, &h->Zb, &h->Tb, &h->Pb, &h->Qb}) lay.take(*b, (size_t)T * cap * ldcap * 16);
+      lay.take(h->FV, (size_t)T * cap * ldN * 16);
+    }
   }
   return lay.off + 256;
 }
@@ -375,6 +385,67 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
   return 0;   // two passes: result back in U
 }
 
+// NEXT-1 option: orthonormalise U' (rows S0 of the orthonormal U zeroed; V = those rows, in US)
+// at low rank: U' <- U' + (U' V^dag) F V, F = Z^2 (Z + I)^-1, Z = (I - M)^(-1/2), M = V V^dag.
+// Z by the coupled Newton-Schulz iteration Y <- Y T, Z <- T Z, T = (3I - Z Y)/2 from Y = I - M,
+// Z = I (converges for spec(M) in [0, 1)).  On success CQR2 skips its first pass (lr_k0 = 0).
+int lowrank_orthonormalize(traj_ctx* h, cplx* U, int k) {
+  const int T = h->T;
+  const long long ld = h->ldcap, s2 = (long long)h->cap * h->ldcap;
+  // M = V V^dag, Y = I - M, Z = I
+  TRY(zgemm(h->st, 0, 1, k, k, h->N, 1.0, 0.0, h->US, h->ldN, h->sUS, h->US, h->ldN, h->sUS, 0.0, h->Mb, ld, s2, T, 0,
+            &h->err));
+  CK(cudaMemcpyAsync(h->Yb, h->Mb, (size_t)T * s2 * 16, cudaMemcpyDeviceToDevice, h->st));
+  TRY(axpby_identity(h->st, h->Yb, ld, s2, k, T, -1.0, 1.0, &h->err));
+  CK(cudaMemsetAsync(h->Zb, 0, (size_t)T * s2 * 16, h->st));
+  TRY(axpby_identity(h->st, h->Zb, ld, s2, k, T, 1.0, 1.0, &h->err));
+  bool converged = false;
+  for (int it = 0; it < 100; ++it) {
+    // Tb = Z Y; residual max|Z Y - I| decides convergence
+    TRY(zgemm(h->st, 0, 0, k, k, k, 1.0, 0.0, h->Zb, ld, s2, h->Yb, ld, s2, 0.0, h->Tb, ld, s2, T, 0, &h->err));
+    TRY(gram_deviation(h->st, h->Tb, ld, s2, k, T, h->gdev, &h->err));
+    CK(cudaMemcpyAsync(h->h_dev, h->gdev, (size_t)T * 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    double worst = 0.0;
+    for (int t = 0; t < T; ++t)
+      if (!std::isnan(h->h_dev[t])) worst = std::max(worst, h->h_dev[t]);   // a failed trajectory stays NaN
+    ++h->lowrank_iters;
+    if (worst < 1e-14) {
+      converged = true;
+      break;
+    }
+    // T = 1.5 I - 0.5 Z Y;  Y <- Y T,  Z <- T Z
+    TRY(axpby_identity(h->st, h->Tb, ld, s2, k, T, -0.5, 1.5, &h->err));
+    TRY(zgemm(h->st, 0, 0, k, k, k, 1.0, 0.0, h->Yb, ld, s2, h->Tb, ld, s2, 0.0, h->Pb, ld, s2, T, 0, &h->err));
+    TRY(zgemm(h->st, 0, 0, k, k, k, 1.0, 0.0, h->Tb, ld, s2, h->Zb, ld, s2, 0.0, h->Qb, ld, s2, T, 0, &h->err));
+    std::swap(h->Yb, h->Pb);
+    std::swap(h->Zb, h->Qb);
+  }
+  if (!converged) {          // keep CholeskyQR2 (its first Gram from the zeroed rows)
+    ++h->lowrank_fallbacks;
+    return 0;
+  }
+  // F = Z^2 (Z + I)^-1 with (Z + I)^-1 = X X^dag, R^dag R = Z + I, X = R^-1
+  CK(cudaMemcpyAsync(h->Mb, h->Zb, (size_t)T * s2 * 16, cudaMemcpyDeviceToDevice, h->st));
+  TRY(axpby_identity(h->st, h->Mb, ld, s2, k, T, 1.0, 1.0, &h->err));
+  TRY(chol_inverse(h->st, k, h->Mb, ld, s2, h->Yb, ld, s2, T, h->chol_scratch_small, h->failed_dev, &h->err));
+  TRY(zgemm(h->st, 0, 0, k, k, k, 1.0, 0.0, h->Zb, ld, s2, h->Zb, ld, s2, 0.0, h->Tb, ld, s2, T, 0, &h->err));
+  TRY(zgemm(h->st, 0, 0, k, k, k, 1.0, 0.0, h->Tb, ld, s2, h->Yb, ld, s2, 0.0, h->Pb, ld, s2, T, TRAJ_TRI_B_UPPER_F,
+            &h->err));
+  TRY(zgemm(h->st, 0, 1, k, k, k, 1.0, 0.0, h->Pb, ld, s2, h->Yb, ld, s2, 0.0, h->Qb, ld, s2, T, TRAJ_TRI_B_LOWER_F,
+            &h->err));
+  // FV = F V (k x N);  P = U' V^dag (L x k);  U' += P FV
+  TRY(zgemm(h->st, 0, 0, k, h->N, k, 1.0, 0.0, h->Qb, ld, s2, h->US, h->ldN, h->sUS, 0.0, h->FV, h->ldN, h->sUS, T, 0,
+            &h->err));
+  const long long sT = (long long)h->L * h->ldcap;
+  TRY(zgemm(h->st, 0, 1, h->L, k, h->N, 1.0, 0.0, U, h->ldN, h->sU, h->US, h->ldN, h->sUS, 0.0, h->Tm, h->ldcap, sT, T,
+            0, &h->err));
+  TRY(zgemm(h->st, 0, 0, h->L, h->N, k, 1.0, 0.0, h->Tm, h->ldcap, sT, h->FV, h->ldN, h->sUS, 1.0, U, h->ldN, h->sU, T,
+            0, &h->err));
+  h->lr_k0 = 0;              // U is orthonormal: CholeskyQR2's first pass has R = I
+  return 0;
+}
+
 int projective(traj_ctx* h, cplx* U) {
   Phase p(&h->prof, h->st, TRAJ_PH_PROJECT);
   const int T = h->T, cap = h->cap;
@@ -443,6 +514,10 @@ int projective(traj_ctx* h, cplx* U) {
     h->lr_k0 = k0max;
   }
   if (k0max > 0) TRY(zero_rows_batched(h->st, U, h->ldN, h->sU, h->S0, cap, h->k0, k0max, T, h->N, &h->err));
+  if (h->lowrank_orth && k0max > 0) {
+    int s = lowrank_orthonormalize(h, U, k0max);
+    if (s) return s;
+  }
   return 0;
 }
 
@@ -902,7 +977,8 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
     const char* e = getenv("TRAJ_CQR2_FULL");
     h->full_cqr2 = e && e[0] == '1';
     const char* g = getenv("TRAJ_LOWRANK_GRAM");
-    h->lowrank_gram = !(g && g[0] == '0');
+    h->lowrank_gram = !(g && g[0] == '0') || cfg->orthonormalizer == TRAJ_ORTH_LOWRANK;
+    h->lowrank_orth = cfg->orthonormalizer == TRAJ_ORTH_LOWRANK && cfg->protocol == TRAJ_PROJECTIVE;
   }
   if (cusolverDnCreate(&h->solver) != CUSOLVER_STATUS_SUCCESS) return bail(TRAJ_ECUDA, "cusolverDnCreate");
   cusolverDnSetStream(h->solver, h->st);

@@ -440,3 +440,25 @@ def test_projective_lowrank_first_gram_matches_measured(P):
         assert np.abs(a.correlation(t).cpu().numpy() - b.correlation(t).cpu().numpy()).max() < 1e-12
         U = a.get_state(t).cpu().numpy()
         assert np.abs(U.conj().T @ U - np.eye(150)).max() < 1e-13
+
+
+@pytest.mark.parametrize("Lx,Ly,gams", [(300, 1, [3.0, 0.5]), (10, 10, [2.86, 5.72]), (400, 1, [10.0])])
+def test_lowrank_projective_orthonormalizer_matches_oracle(P, Lx, Ly, gams):
+    """NEXT-1 option: the projective step orthonormalised at low rank (Newton-Schulz on the
+    k0 x k0 block, two O(L N k0) GEMMs) plus the measured second CholeskyQR pass, in lockstep
+    with the oracle (Householder QR)."""
+    g = P.Trajectories(Lx, Ly, "projective", gams, seed=23, orthonormalizer="lowrank")
+    K = lattice.propagator_lattice(Lx, Ly, 1.0, 0.05)
+    orc = [OracleTrajectory(Lx, Ly, "projective", gm, 0.05, seed=23, traj=t, K=K) for t, gm in enumerate(gams)]
+    A = np.arange(Lx * Ly // 2)
+    for s in range(25):
+        g.step(1)
+        for t, o in enumerate(orc):
+            o.step(1)
+            assert g.last_clicks(t) == (o.last_clicks[0].size, int(o.last_clicks[1].sum()))
+    S = g.entropy(A)
+    for t, o in enumerate(orc):
+        assert np.abs(g.correlation(t).cpu().numpy() - o.correlation()).max() < C_TOL
+        assert abs(S[t] - o.entropy(A)) < S_TOL
+        U = g.get_state(t).cpu().numpy()
+        assert np.abs(U.conj().T @ U - np.eye(U.shape[1])).max() < 1e-13
