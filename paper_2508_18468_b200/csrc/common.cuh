@@ -18,11 +18,6 @@ typedef double2 cplx;   // (re, im), interleaved complex128
 extern std::atomic<long long> g_kernel_launches;
 inline void count_launch(long long n = 1) { g_kernel_launches.fetch_add(n, std::memory_order_relaxed); }
 
-struct Error {
-  int status;
-  std::string msg;
-};
-
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -112,11 +112,9 @@ int fail(traj_ctx* h, int status, const std::string& msg) {
     cudaError_t e_ = (x);                                                                      \
     if (e_ != cudaSuccess) return fail(h, TRAJ_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
-#define TRY(x)                        \
-  do {                                \
-    std::string m_;                   \
-    int s_ = (x);                     \
-    (void)m_;                         \
+#define TRY(x)                          \
+  do {                                  \
+    int s_ = (x);                       \
     if (s_) return fail(h, s_, h->err); \
   } while (0)
 
