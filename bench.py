@@ -56,6 +56,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-observables", action="store_true")
+    p.add_argument("--secondary", default="c5",
+                   help="also time this config (the metric is quoted at 1d L=16384 and 2d 160x160); '' to skip")
     p.add_argument("--cpu-budget", type=float, default=120.0, help="seconds of oracle work (reference arm)")
     return p.parse_args()
 
@@ -250,6 +252,11 @@ def run_ours(args):
     del tr
     torch.cuda.empty_cache()
 
+    # ---- the metric's second lattice (2d 160x160), same step, same timing rules
+    secondary = None
+    if args.secondary and args.secondary != args.config and not shard:
+        secondary = run_secondary(args, world, rank, P)
+
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e and not shard:
@@ -282,6 +289,7 @@ def run_ours(args):
         "phase_launches_per_step": {k: v[1] / args.steps for k, v in phases.items()},
         "gpu_launches": launches,
         "sampled_observables_ms": obs,
+        "secondary": secondary,
         "clocks": clk,
         "e2e": e2e,
     }
@@ -290,6 +298,49 @@ def run_ours(args):
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_secondary(args, world, rank, P, steps=2, warmup=2):
+    """Time the secondary config (default c5: 2d 160x160 projective) with the same step, the
+    same propagator/orthonormaliser and CUDA events; max over ranks."""
+    import torch
+    import torch.distributed as dist
+    import dataclasses
+    w = workloads.CONFIGS[args.secondary]()
+    if args.protocol:
+        w = dataclasses.replace(w, protocol=args.protocol)
+    tr = P.Trajectories(w.Lx, w.Ly, w.protocol, [w.gammas[0]], dt=w.dt, J=w.J, seed=w.seed, traj_base=rank,
+                        propagator=args.propagator, orthonormalizer=args.orthonormalizer)
+    for _ in range(warmup):
+        tr.step(1)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    tr.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(tr.stream)
+    for _ in range(steps):
+        tr.step(1)
+    e1.record(tr.stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    ph = tr.phase_times()
+    tr.close()
+    del tr
+    torch.cuda.empty_cache()
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    prop = ph["propagate"][0] / steps
+    out = {"config": describe(w, 1), "value": world * steps / (ms / 1e3), "unit": "trajectory-steps/s",
+           "ms_per_step": ms / steps, "steps": steps, "warmup": warmup,
+           "phases_ms_per_step": {k: v[0] / steps for k, v in ph.items()}}
+    if args.propagator == "dense":
+        ach = 8.0 * w.L * w.L * w.N / (prop / 1e3) / 1e12
+        out["roofline_propagate"] = {"bound": "tensor", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                                     "frac": ach / FP64_PEAK_TFLOPS}
+    return out
 
 
 def run_e2e(args, w, tpg, gam, base, world, P):
