@@ -57,7 +57,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-observables", action="store_true")
     p.add_argument("--secondary", default="c5",
-                   help="also time this config (the metric is quoted at 1d L=16384 and 2d 160x160); '' to skip")
+                   help="also time this config (the metric is quoted at 1d L=16384 and 2d 160x160); 'none' skips")
     p.add_argument("--cpu-budget", type=float, default=120.0, help="seconds of oracle work (reference arm)")
     return p.parse_args()
 
@@ -254,7 +254,8 @@ def run_ours(args):
 
     # ---- the metric's second lattice (2d 160x160), same step, same timing rules
     secondary = None
-    if args.secondary and args.secondary != args.config and not shard:
+    if args.secondary and args.secondary not in ("none", '""', "''") and args.secondary != args.config \
+            and not shard:
         secondary = run_secondary(args, world, rank, P)
 
     # ---- end to end through the public API with host buffers
