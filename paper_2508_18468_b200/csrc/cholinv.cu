@@ -23,90 +23,95 @@ namespace {
 constexpr int NB = 64;            // leaf size
 
 
-// One CTA (1024 threads) per batch entry: n <= 64 diagonal block.  Reads the upper
-// triangle of G, writes X = R^-1 (upper) and zeros below the diagonal.  Each thread owns a
-// 2 x 2 block of the (identity-padded, full Hermitian) working matrix A and of W in registers.
-// Step j of the right-looking elimination (G = L L^dag, L = R^dag): the owners publish row j
-// of A and W and column j of A through shared memory; every thread then applies
-//   l_i = A_ij / r_jj (= conj R_ji),  A_ik -= l_i A_jk / r_jj (i, k > j),  W_ik -= l_i W_jk / r_jj (i > j),
-// W ends as L^-1 (rows scaled by 1/r_jj at their step), so X = R^-1 = W^dag.
-template <int TW>   // TW x TW threads, each owning a 2 x 2 block (n <= 2 TW)
+// One CTA per batch entry: n <= 64 diagonal block.  Reads the upper triangle of G, writes
+// X = R^-1 (upper) and zeros below the diagonal.  Each of the TW x TW threads owns a BS x BS
+// block of the (identity-padded) working matrix A (upper triangle kept) and of W in registers.
+// Step j of the right-looking elimination (G = L L^dag, L = R^dag): the owners of row j publish
+// row j of A and W and the pivot scalars 1/d, 1/sqrt(d) (double-buffered, so one barrier per
+// step; only the diagonal owner evaluates the rsqrt); A is Hermitian, so the column entry A_ij
+// is conj(A_ji) and needs no second broadcast.  Every thread then applies
+//   A_ik -= A_ij A_jk / d  (j < i <= k),   W_ik -= A_ij W_jk / d  (i > j, k <= j),   d = A_jj,
+// and the owners of row j scale it by 1/sqrt(d).  W ends as L^-1, so X = R^-1 = W^dag.
+template <int TW, int BS>
 __global__ void __launch_bounds__(TW * TW) chol_leaf_kernel(int n, cplx* G, long long ldg, long long sG, cplx* X,
                                                             long long ldx, long long sX, int32_t* failed) {
-  __shared__ double2 rowA[NB], rowW[NB], colA[NB];
+  __shared__ double2 rowA[2][TW * BS], rowW[2][TW * BS], piv[2];
   __shared__ int bad;
   const int b = blockIdx.x, tid = threadIdx.x;
   const cplx* g = G + b * sG;
   cplx* x = X + b * sX;
-  const int i0 = 2 * (tid / TW), k0 = 2 * (tid % TW);
-  double2 A[2][2], W[2][2];
+  const int i0 = BS * (tid / TW), k0 = BS * (tid % TW);
+  double2 A[BS][BS], W[BS][BS];
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < BS; ++a)
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
+    for (int c = 0; c < BS; ++c) {
       const int i = i0 + a, k = k0 + c;
       double2 v = make_double2(i == k ? 1.0 : 0.0, 0.0);
-      if (i < n && k < n) {
-        if (i <= k) v = g[(long long)i * ldg + k];
-        else {
-          const double2 u = g[(long long)k * ldg + i];
-          v = make_double2(u.x, -u.y);
-        }
-      }
+      if (i <= k && k < n) v = g[(long long)i * ldg + k];
       A[a][c] = v;
       W[a][c] = make_double2(i == k ? 1.0 : 0.0, 0.0);
     }
   if (tid == 0) bad = 0;
   for (int j = 0; j < n; ++j) {     // padded identity rows/columns need no elimination
-    if ((j >> 1) == (i0 >> 1)) {
-      const int a = j & 1;
-      rowA[k0] = A[a][0];
-      rowA[k0 + 1] = A[a][1];
-      rowW[k0] = W[a][0];
-      rowW[k0 + 1] = W[a][1];
-    }
-    if ((j >> 1) == (k0 >> 1)) {
-      const int c = j & 1;
-      colA[i0] = A[0][c];
-      colA[i0 + 1] = A[1][c];
+    const int buf = j & 1;
+    if (j >= i0 && j < i0 + BS) {
+#pragma unroll
+      for (int a = 0; a < BS; ++a)
+        if (i0 + a == j) {
+#pragma unroll
+          for (int c = 0; c < BS; ++c) {
+            rowA[buf][k0 + c] = A[a][c];
+            rowW[buf][k0 + c] = W[a][c];
+            if (k0 + c == j) {              // the diagonal owner publishes the pivot scalars
+              const double d = A[a][c].x;
+              if (!(d > 0.0) || !isfinite(d)) bad = 1;
+              const double ir = rsqrt(d);
+              piv[buf] = make_double2(ir * ir, ir);
+            }
+          }
+        }
     }
     __syncthreads();
-    const double d = rowA[j].x;
-    if (tid == 0 && j < n && (!(d > 0.0) || !isfinite(d))) bad = 1;
-    const double ip = 1.0 / d;            // l_i * A_jk / r_jj = (A_ij / r)(A_jk / r) = A_ij A_jk / d
-    const double ir = 1.0 / sqrt(d);
+    const double ip = piv[buf].x;           // 1 / d
+    const double ir = piv[buf].y;           // 1 / sqrt(d)
+    if (i0 + BS - 1 < j) continue;          // rows all eliminated
 #pragma unroll
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < BS; ++a) {
       const int i = i0 + a;
       if (i == j) {
 #pragma unroll
-        for (int c = 0; c < 2; ++c) W[a][c] = make_double2(W[a][c].x * ir, W[a][c].y * ir);
+        for (int c = 0; c < BS; ++c) W[a][c] = make_double2(W[a][c].x * ir, W[a][c].y * ir);
       } else if (i > j) {
-        const double2 l = colA[i];        // A_ij
+        const double2 u = rowA[buf][i];     // A_ji;  A_ij = conj(u)
+        const double lx = u.x * ip, ly = -u.y * ip;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
+        for (int c = 0; c < BS; ++c) {
           const int k = k0 + c;
           if (k > j) {
-            const double2 r = rowA[k];    // A_jk
-            A[a][c].x -= (l.x * r.x - l.y * r.y) * ip;
-            A[a][c].y -= (l.x * r.y + l.y * r.x) * ip;
+            if (k >= i) {
+              const double2 r = rowA[buf][k];   // A_jk
+              A[a][c].x -= lx * r.x - ly * r.y;
+              A[a][c].y -= lx * r.y + ly * r.x;
+            }
+          } else {
+            const double2 w = rowW[buf][k];     // W_jk (unscaled)
+            W[a][c].x -= lx * w.x - ly * w.y;
+            W[a][c].y -= lx * w.y + ly * w.x;
           }
-          const double2 w = rowW[k];      // W_jk (unscaled): l/r * W_jk/r
-          W[a][c].x -= (l.x * w.x - l.y * w.y) * ip;
-          W[a][c].y -= (l.x * w.y + l.y * w.x) * ip;
         }
       }
     }
-    __syncthreads();
   }
   // X = W^dag: X_ki = conj(W_ik) for k <= i; zeros below the diagonal
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < BS; ++a)
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
+    for (int c = 0; c < BS; ++c) {
       const int i = i0 + a, k = k0 + c;    // element W_ik  ->  X_ki
       if (i < n && k < n) x[(long long)k * ldx + i] = k <= i ? make_double2(W[a][c].x, -W[a][c].y) : make_double2(0.0, 0.0);
     }
+  __syncthreads();
   if (tid == 0 && bad && failed) failed[b] = 1;
 }
 
@@ -127,9 +132,9 @@ struct Ctx {
 
 int rec(Ctx& c, long long o, long long n) {
   if (n <= NB) {
-    auto leaf = n <= 16 ? chol_leaf_kernel<8> : (n <= 32 ? chol_leaf_kernel<16> : chol_leaf_kernel<32>);
-    const int tw = n <= 16 ? 8 : (n <= 32 ? 16 : 32);
-    leaf<<<(unsigned)c.batch, tw * tw, 0, c.st>>>((int)n, c.G + o * c.ldg + o, c.ldg, c.sG,
+    auto leaf = n <= 16 ? chol_leaf_kernel<8, 2> : (n <= 32 ? chol_leaf_kernel<16, 2> : chol_leaf_kernel<32, 2>);
+    const int threads = n <= 16 ? 64 : (n <= 32 ? 256 : 1024);
+    leaf<<<(unsigned)c.batch, threads, 0, c.st>>>((int)n, c.G + o * c.ldg + o, c.ldg, c.sG,
                                                                       c.X + o * c.ldx + o, c.ldx, c.sX, c.failed);
     count_launch();
     cudaError_t e = cudaGetLastError();
