@@ -229,6 +229,19 @@ def run_ours(args):
             traffic = json.load(open(tp)).get(w.name, {}).get("propagate_dram_bytes")
         except Exception:
             traffic = None
+    # same-shape library denominators (tools/library_compare.py, committed under profiles/):
+    # cublasZgemm / cublasZgemm3m for K U, cuSOLVER potrf + trtri for the Cholesky inverse
+    library = None
+    lp = os.path.join(ROOT, "profiles", "r01", f"library_compare_{w.name}.json")
+    if os.path.exists(lp) and not shard and args.propagator == "dense":
+        try:
+            lc = json.load(open(lp))
+            library = {"source": os.path.relpath(lp, ROOT) + " (tools/library_compare.py, same shapes, same box type)",
+                       "K_U_ms": {k: round(v["ms"], 2) for k, v in lc["K_U"].items()},
+                       "chol_inverse_ms": {k: round(v["ms"], 2) for k, v in lc["chol_inverse"].items()
+                                           if isinstance(v, dict)}}
+        except Exception:
+            library = None
     step_flops = {"propagate": 8.0 * rows * w.L * w.N * tpg if args.propagator == "dense" else 0.0,
                   "gram": 2 * 4.0 * rows * w.N * w.N * tpg, "trmm": 2 * 4.0 * rows * w.N * w.N * tpg,
                   "chol": (8.0 / 3.0) * w.N ** 3 * tpg}
@@ -285,6 +298,7 @@ def run_ours(args):
                      "note": ("achieved counts the conventional 8mnk complex flops; the 3M (Gauss) kernels issue "
                               "6mnk flops on the DMMA pipe, reported as pipe_tflops / pipe_frac")
                      if algo == "3m" else "4M: 8mnk flops on the DMMA pipe"},
+        "library_same_shape": library,
         "step_dense_tflops": dense_tflops,
         "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
         "phase_launches_per_step": {k: v[1] / args.steps for k, v in phases.items()},
