@@ -190,6 +190,24 @@ int traj_last_clicks(traj_handle h, int64_t traj, int64_t* n_clicks, int64_t* n_
  * environment TRAJ_CQR2_FULL=1 forces the full factorisation every time). */
 int traj_cqr2_fallbacks(traj_handle h, int64_t* n);
 
+/* Counters of the low-rank projective orthonormaliser (TRAJ_ORTH_LOWRANK, NEXT-1 option; SURVEY
+ * §8(f) 1 "orthonormalise the projective step at low rank"), cumulative since traj_init:
+ *   newton_iters  coupled Newton-Schulz iterations for (I - V V^dag)^(-1/2);
+ *   fallbacks     steps where the iteration did not converge and CholeskyQR2 ran instead;
+ *   probes        orthonormality certificates: ||U^dag U - I||_F estimated with 4 unit-modulus
+ *                 random probes (Hutchinson) after a low-rank step, two HBM passes over U;
+ *   refinements   probes above the tolerance (environment TRAJ_LOWRANK_TOL, default 5e-13;
+ *                 0 = refine every step), each followed by one measured CholeskyQR pass.
+ * Any pointer may be NULL.  TRAJ_EINVAL on a NULL handle.  Zeros for other orthonormalisers. */
+int traj_lowrank_stats(traj_handle h, int64_t* newton_iters, int64_t* fallbacks, int64_t* probes,
+                       int64_t* refinements);
+
+/* The orthonormality certificate used by the low-rank orthonormaliser, on the current state:
+ * est_out[t] (host, n_traj doubles) = sqrt((1/4) sum_j ||U_t^dag (U_t x_j) - x_j||^2), an unbiased
+ * (in the square) estimate of ||U_t^dag U_t - I||_F from 4 probes x_j with entries (+-1 +- i)/sqrt 2
+ * drawn by Philox (k, step, traj, 3).  Synchronises the stream.  TRAJ_EINVAL with row sharding. */
+int traj_probe_orthonormality(traj_handle h, double* est_out);
+
 /* Per-phase device timing with CUDA events on the handle's stream.  enable != 0
  * starts recording (and zeroes the totals).  traj_phase_times fills ms[TRAJ_NPHASES]
  * with accumulated milliseconds and launches[TRAJ_NPHASES] with kernel-launch counts

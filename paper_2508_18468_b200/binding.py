@@ -80,6 +80,9 @@ _SIGS = {
     "traj_failed": (ctypes.c_int, [_P, _I64, ctypes.POINTER(ctypes.c_int32)]),
     "traj_last_clicks": (ctypes.c_int, [_P, _I64, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "traj_cqr2_fallbacks": (ctypes.c_int, [_P, ctypes.POINTER(_I64)]),
+    "traj_probe_orthonormality": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_double)]),
+    "traj_lowrank_stats": (ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64),
+                                          ctypes.POINTER(_I64)]),
     "traj_profile": (ctypes.c_int, [_P, ctypes.c_int]),
     "traj_phase_times": (ctypes.c_int, [_P, ctypes.POINTER(_D), ctypes.POINTER(_I64)]),
     "traj_kernel_launches": (ctypes.c_longlong, []),
@@ -354,6 +357,20 @@ class Trajectories:
         n = ctypes.c_int64(0)
         self._c(lib().traj_cqr2_fallbacks(self._h, ctypes.byref(n)))
         return n.value
+
+    def probe_orthonormality(self):
+        """Estimated ||U_t^dag U_t - I||_F per trajectory (4 random unit-modulus probes)."""
+        import numpy as np
+        out = np.zeros(self.n_traj, dtype=np.float64)
+        self._c(lib().traj_probe_orthonormality(self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return out
+
+    def lowrank_stats(self) -> dict:
+        """Counters of the low-rank orthonormaliser: Newton-Schulz iterations, fallbacks to
+        CholeskyQR2, orthonormality probes and the refinements they triggered."""
+        v = [ctypes.c_int64(0) for _ in range(4)]
+        self._c(lib().traj_lowrank_stats(self._h, *[ctypes.byref(x) for x in v]))
+        return dict(zip(("newton_iters", "fallbacks", "probes", "refinements"), (x.value for x in v)))
 
     # -- profiling
     def profile(self, enable: bool = True):

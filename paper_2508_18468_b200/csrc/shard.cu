@@ -12,6 +12,7 @@
 #include <cusolverDn.h>
 #include <math.h>
 #include <nccl.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <complex>
@@ -296,6 +297,14 @@ int shard_init(ShardedCtx* sh, const traj_config* c, std::string* err) {
   }
   SCK(cudaMallocHost(&sh->h_small, std::max(sh->P + 8, 64) * 4));
   SCK(cudaMallocHost(&sh->h_dev, 64 * 8));
+  const char* ov = getenv("TRAJ_SHARD_OVERLAP");
+  sh->overlap = !(ov && ov[0] == '0');
+  if (sh->comm.comm && sh->overlap && sh->P > 1) {
+    SCK(cudaStreamCreateWithFlags(&sh->cst, cudaStreamNonBlocking));
+    SCK(cudaEventCreateWithFlags(&sh->ev_start, cudaEventDisableTiming));
+    sh->ev_chunk.assign(sh->P, nullptr);
+    for (auto& e : sh->ev_chunk) SCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   return 0;
 }
 
@@ -476,6 +485,64 @@ int propagate_banded(ShardedCtx* sh, int cur, int nxt, std::string* err) {
   return 0;
 }
 
+// a1 with sharding, SURVEY §8(e) "fusion with the collective": U_g' = sum_s K_g[:, s] U_s over
+// the P row blocks s of U, in ring-distance order d = 0..P-1 (s = g - d mod P).  d = 0 is the
+// local block and starts at once; in NCCL mode block d arrives by a send/recv pair on the comm
+// stream (send U_g to g + d, receive U_{g-d}) and its GEMM waits only for that transfer, so
+// the exchange of block d+1 runs under the GEMM of block d.  The emulation (one GPU) gathers
+// first and then runs the same chunk GEMMs in the same order (the same arithmetic).
+// TRAJ_SHARD_OVERLAP=0: one allgather, then one L-deep GEMM.
+int propagate_dense(ShardedCtx* sh, int cur, int nxt, std::string* err) {
+  cudaStream_t st = sh->st;
+  const long long Lp = sh->Lp, ld = sh->ldN;
+  const size_t bytes = (size_t)Lp * ld * 16;
+  if (!sh->overlap || sh->P == 1) {
+    STRY(gather_full(sh, cur, err));
+    for (auto& l : sh->loc)
+      STRY(zgemm(st, 0, 0, Lp, sh->N, sh->L, 1.0, 0.0, l.K, sh->ldL, 0, sh->Ufull, ld, 0, 0.0, l.U[nxt], ld, 0, 1, 0,
+                 err));
+    return 0;
+  }
+  const int P = sh->P;
+  if (sh->comm.comm) {
+    ShardLocal& l = sh->loc[0];
+    const int g = l.g;
+    SCK(cudaEventRecord(sh->ev_start, st));
+    SCK(cudaStreamWaitEvent(sh->cst, sh->ev_start, 0));
+    for (int d = 1; d < P; ++d) {
+      const int to = (g + d) % P, from = (g - d + P) % P;
+      ncclGroupStart();
+      ncclSend(l.U[cur], bytes, ncclUint8, to, sh->comm.comm, sh->cst);
+      ncclRecv(sh->Ufull + (size_t)from * Lp * ld, bytes, ncclUint8, from, sh->comm.comm, sh->cst);
+      ncclResult_t r = ncclGroupEnd();
+      if (r != ncclSuccess) {
+        if (err) *err = std::string("nccl send/recv (propagate): ") + ncclGetErrorString(r);
+        return TRAJ_ENCCL;
+      }
+      SCK(cudaEventRecord(sh->ev_chunk[d], sh->cst));
+    }
+    for (int d = 0; d < P; ++d) {
+      const int s = (g - d + P) % P;
+      const cplx* Us = l.U[cur];
+      if (d > 0) {
+        SCK(cudaStreamWaitEvent(st, sh->ev_chunk[d], 0));
+        Us = sh->Ufull + (size_t)s * Lp * ld;
+      }
+      STRY(zgemm(st, 0, 0, Lp, sh->N, Lp, 1.0, 0.0, l.K + (size_t)s * Lp, sh->ldL, 0, Us, ld, 0, d ? 1.0 : 0.0,
+                 l.U[nxt], ld, 0, 1, 0, err));
+    }
+    return 0;
+  }
+  STRY(gather_full(sh, cur, err));
+  for (auto& l : sh->loc)
+    for (int d = 0; d < P; ++d) {
+      const int s = (l.g - d + P) % P;
+      STRY(zgemm(st, 0, 0, Lp, sh->N, Lp, 1.0, 0.0, l.K + (size_t)s * Lp, sh->ldL, 0, sh->Ufull + (size_t)s * Lp * ld,
+                 ld, 0, d ? 1.0 : 0.0, l.U[nxt], ld, 0, 1, 0, err));
+    }
+  return 0;
+}
+
 }  // namespace
 
 int shard_step(ShardedCtx* sh, long long* step, std::string* err) {
@@ -485,10 +552,7 @@ int shard_step(ShardedCtx* sh, long long* step, std::string* err) {
     STRY(propagate_banded(sh, cur, nxt, err));
   } else {
     Phase p(sh->prof, sh->st, TRAJ_PH_PROPAGATE);
-    STRY(gather_full(sh, cur, err));
-    for (auto& l : sh->loc)
-      STRY(zgemm(sh->st, 0, 0, sh->Lp, sh->N, sh->L, 1.0, 0.0, l.K, sh->ldL, 0, sh->Ufull, sh->ldN, 0, 0.0, l.U[nxt],
-                 sh->ldN, 0, 1, 0, err));
+    STRY(propagate_dense(sh, cur, nxt, err));
   }
   {
     Phase p(sh->prof, sh->st, TRAJ_PH_MONITOR);
@@ -622,6 +686,13 @@ int shard_failed(ShardedCtx* sh, int32_t* flag, std::string* err) {
 
 void shard_destroy(ShardedCtx* sh) {
   if (sh->st) cudaStreamSynchronize(sh->st);
+  if (sh->cst) {
+    cudaStreamSynchronize(sh->cst);
+    cudaStreamDestroy(sh->cst);
+  }
+  if (sh->ev_start) cudaEventDestroy(sh->ev_start);
+  for (auto e : sh->ev_chunk)
+    if (e) cudaEventDestroy(e);
   if (sh->comm.comm) ncclCommDestroy(sh->comm.comm);
   if (sh->h_small) cudaFreeHost(sh->h_small);
   if (sh->h_dev) cudaFreeHost(sh->h_dev);

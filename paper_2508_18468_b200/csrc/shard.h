@@ -77,6 +77,12 @@ struct ShardedCtx {
   long long last_nS = 0, last_n1 = 0, cqr2_fallbacks = 0;
   bool full_cqr2 = false;
   cudaStream_t st = nullptr;
+  // dense propagate with the allgather overlapped (NCCL mode): per-distance send/recv on cst,
+  // chunk d of K_g U_full on st waits only for ev_chunk[d]
+  bool overlap = true;
+  cudaStream_t cst = nullptr;
+  cudaEvent_t ev_start = nullptr;
+  std::vector<cudaEvent_t> ev_chunk;
   cusolverDnHandle_t solver = nullptr;
   Profiler* prof = nullptr;
   double *obs_bins = nullptr, *obs_part = nullptr, *obs_out = nullptr;

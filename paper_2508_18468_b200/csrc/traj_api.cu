@@ -23,6 +23,7 @@
 #include "banded.h"
 #include "qsd_rk4.h"
 #include "pm_events.h"
+#include "probe.h"
 
 namespace traj {
 std::atomic<long long> g_kernel_launches{0};
@@ -78,6 +79,11 @@ struct traj_ctx {
   bool full_cqr2 = false;                // TRAJ_CQR2_FULL=1: always factor G2 by chol_inverse
   bool lowrank_gram = true;              // TRAJ_LOWRANK_GRAM=0: always measure the first Gram
   bool lowrank_orth = false;             // TRAJ_ORTH_LOWRANK
+  bool lowrank_refine = true;            // TRAJ_LOWRANK_REFINE=0: never refine (drift studies only)
+  double lowrank_tol = 5e-13;            // TRAJ_LOWRANK_TOL: refine when the probed ||U^dag U - I||_F exceeds it
+  cplx *PX = nullptr, *PY = nullptr, *Ppart = nullptr;
+  double* pest = nullptr;
+  long long lowrank_probes = 0, lowrank_refinements = 0;
   cplx *Mb = nullptr, *Yb = nullptr, *Zb = nullptr, *Tb = nullptr, *Pb = nullptr, *Qb = nullptr, *FV = nullptr;
   long long lowrank_iters = 0, lowrank_fallbacks = 0;
   int lr_k0 = -1;                        // >= 0: pass-1 Gram of this step = I - V^dag V, V (k0 rows) in US
@@ -259,6 +265,10 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
   lay.take(h->region, (size_t)L * 4);
   lay.take(h->kcoef, (size_t)(Lx + Ly) * 16);
   lay.take(h->sites, (size_t)N * 4);
+  lay.take(h->PX, probe_x_bytes(N, T));
+  lay.take(h->PY, probe_y_bytes(L, T));
+  lay.take(h->Ppart, probe_partial_bytes(N, T));
+  lay.take(h->pest, (size_t)T * 8);
   if (cap > 0) {
     h->sUS = (long long)cap * ldN;
     h->sD = (long long)cap * ldcap;
@@ -335,6 +345,25 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
   cplx* dst = tmp;
   const int lr = h->lr_k0;
   h->lr_k0 = -1;
+  if (lr == 0 && h->lowrank_orth) {
+    // NEXT-1 low-rank mode: U is orthonormal up to the rounding drift the low-rank updates
+    // accumulate; certify that with the probe (probe.cu) and refine with one measured
+    // CholeskyQR pass only above the tolerance (TRAJ_LOWRANK_TOL=0: every step)
+    if (!h->lowrank_refine) return 0;
+    if (h->lowrank_tol > 0) {
+      Phase p(&h->prof, h->st, TRAJ_PH_GRAM);
+      TRY(probe_orthonormality(h->st, U, h->ldN, h->sU, h->L, h->N, h->T, h->step, h->cfg.traj_base, h->cfg.seed,
+                               h->PX, h->PY, h->Ppart, h->pest, &h->err));
+      CK(cudaMemcpyAsync(h->h_dev, h->pest, h->T * 8, cudaMemcpyDeviceToHost, h->st));
+      CK(cudaStreamSynchronize(h->st));
+      ++h->lowrank_probes;
+      bool need = false;
+      for (int t = 0; t < h->T; ++t)
+        if (h->h_dev[t] > h->lowrank_tol) need = true;   // NaN (failed trajectory) does not force it
+      if (!need) return 0;
+      ++h->lowrank_refinements;
+    }
+  }
   for (int pass = 0; pass < 2; ++pass) {
     if (pass == 0 && lr == 0) continue;     // no row zeroed: U is orthonormal, pass 1 has R = I
     {
@@ -977,6 +1006,10 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
     const char* g = getenv("TRAJ_LOWRANK_GRAM");
     h->lowrank_gram = !(g && g[0] == '0') || cfg->orthonormalizer == TRAJ_ORTH_LOWRANK;
     h->lowrank_orth = cfg->orthonormalizer == TRAJ_ORTH_LOWRANK && cfg->protocol == TRAJ_PROJECTIVE;
+    const char* rf = getenv("TRAJ_LOWRANK_REFINE");
+    h->lowrank_refine = !(rf && rf[0] == '0');
+    const char* tl = getenv("TRAJ_LOWRANK_TOL");
+    if (tl) h->lowrank_tol = atof(tl);
   }
   if (cusolverDnCreate(&h->solver) != CUSOLVER_STATUS_SUCCESS) return bail(TRAJ_ECUDA, "cusolverDnCreate");
   cusolverDnSetStream(h->solver, h->st);
@@ -1219,6 +1252,26 @@ int traj_last_clicks(traj_handle h, int64_t traj, int64_t* n_clicks, int64_t* n_
 int traj_cqr2_fallbacks(traj_handle h, int64_t* n) {
   if (!h || !n) return TRAJ_EINVAL;
   *n = h->sh ? h->sh->cqr2_fallbacks : h->cqr2_fallbacks;
+  return 0;
+}
+
+int traj_probe_orthonormality(traj_handle h, double* est_out) {
+  if (!h || !est_out) return TRAJ_EINVAL;
+  if (h->sh) return fail(h, TRAJ_EINVAL, "traj_probe_orthonormality: not available with row sharding");
+  TRY(probe_orthonormality(h->st, h->U[h->cur], h->ldN, h->sU, h->L, h->N, h->T, h->step, h->cfg.traj_base,
+                           h->cfg.seed, h->PX, h->PY, h->Ppart, h->pest, &h->err));
+  CK(cudaMemcpyAsync(est_out, h->pest, h->T * 8, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return 0;
+}
+
+int traj_lowrank_stats(traj_handle h, int64_t* newton_iters, int64_t* fallbacks, int64_t* probes,
+                       int64_t* refinements) {
+  if (!h) return TRAJ_EINVAL;
+  if (newton_iters) *newton_iters = h->lowrank_iters;
+  if (fallbacks) *fallbacks = h->lowrank_fallbacks;
+  if (probes) *probes = h->lowrank_probes;
+  if (refinements) *refinements = h->lowrank_refinements;
   return 0;
 }
 

@@ -258,6 +258,31 @@ def test_row_sharded_step_matches_oracle(P, P_shards, protocol, gamma):
     assert not g.failed(0)
 
 
+@pytest.mark.parametrize("P_shards", [2, 4, 8])
+def test_row_sharded_chunked_propagate_matches_single_gemm(P, P_shards, monkeypatch):
+    """The sharded dense propagate as P ring-ordered K-chunk GEMMs (the schedule that overlaps
+    the per-distance exchange with compute in NCCL mode, SURVEY §8(e) "fusion with the
+    collective") equals the allgather + one L-deep GEMM (TRAJ_SHARD_OVERLAP=0) to rounding,
+    and both equal the oracle."""
+    L = 512
+    monkeypatch.setenv("TRAJ_SHARD_OVERLAP", "0")
+    a = P.Trajectories(L, 1, "projective", [2.0], seed=21, shard_size=P_shards)
+    monkeypatch.setenv("TRAJ_SHARD_OVERLAP", "1")
+    b = P.Trajectories(L, 1, "projective", [2.0], seed=21, shard_size=P_shards)
+    K = lattice.propagator_lattice(L, 1, 1.0, 0.05)
+    o = OracleTrajectory(L, 1, "projective", 2.0, 0.05, seed=21, traj=0, K=K)
+    for s in range(6):
+        a.step(1)
+        b.step(1)
+        o.step(1)
+        assert a.last_clicks(0) == b.last_clicks(0)
+    ca, cb = a.correlation(0).cpu().numpy(), b.correlation(0).cpu().numpy()
+    assert np.abs(ca - cb).max() < 1e-13
+    assert np.abs(cb - o.correlation()).max() < C_TOL
+    a.close()
+    b.close()
+
+
 def test_row_sharded_nccl_single_rank(P):
     """The NCCL code path of the sharded step with a one-rank communicator (the only
     configuration one GPU allows): same result as the unsharded handle."""
@@ -445,8 +470,9 @@ def test_projective_lowrank_first_gram_matches_measured(P):
 @pytest.mark.parametrize("Lx,Ly,gams", [(300, 1, [3.0, 0.5]), (10, 10, [2.86, 5.72]), (400, 1, [10.0])])
 def test_lowrank_projective_orthonormalizer_matches_oracle(P, Lx, Ly, gams):
     """NEXT-1 option: the projective step orthonormalised at low rank (Newton-Schulz on the
-    k0 x k0 block, two O(L N k0) GEMMs) plus the measured second CholeskyQR pass, in lockstep
-    with the oracle (Householder QR)."""
+    k0 x k0 block, two O(L N k0) GEMMs), certified each step by the orthonormality probe with a
+    measured CholeskyQR refinement above its tolerance, in lockstep with the oracle
+    (Householder QR)."""
     g = P.Trajectories(Lx, Ly, "projective", gams, seed=23, orthonormalizer="lowrank")
     K = lattice.propagator_lattice(Lx, Ly, 1.0, 0.05)
     orc = [OracleTrajectory(Lx, Ly, "projective", gm, 0.05, seed=23, traj=t, K=K) for t, gm in enumerate(gams)]
@@ -462,3 +488,63 @@ def test_lowrank_projective_orthonormalizer_matches_oracle(P, Lx, Ly, gams):
         assert abs(S[t] - o.entropy(A)) < S_TOL
         U = g.get_state(t).cpu().numpy()
         assert np.abs(U.conj().T @ U - np.eye(U.shape[1])).max() < 1e-13
+
+
+def _random_orthonormal(L, N, seed):
+    rng = np.random.default_rng(seed)
+    Q, _ = np.linalg.qr(rng.standard_normal((L, N)) + 1j * rng.standard_normal((L, N)))
+    return Q
+
+
+def test_probe_orthonormality_estimates_gram_deviation(P):
+    """The orthonormality certificate (probe.cu): est = sqrt(mean_j ||U^dag U x_j - x_j||^2) for 4
+    unit-modulus random probes estimates ||E||_F, E = U^dag U - I (Hutchinson, E[x x^dag] = I).
+    Pinned against the exact E from NumPy: an orthonormal U reads at rounding level; a diffuse
+    E = 2 eps H + eps^2 H^2 within the estimator's spread (relative std ~ sqrt(2/(4N)) ~ 6%);
+    an error confined to one entry pair exactly (|x_k| = 1)."""
+    import torch
+    L, N = 256, 128
+    g = P.Trajectories(L, 1, "homodyne", [0.5, 0.5, 0.5], seed=3)
+    Q = _random_orthonormal(L, N, 1)
+    rng = np.random.default_rng(2)
+    H = rng.standard_normal((N, N)) + 1j * rng.standard_normal((N, N))
+    H = (H + H.conj().T) / 2
+    U1 = Q @ (np.eye(N) + 1e-7 * H)
+    B = np.eye(N, dtype=complex)
+    B[5, 77] += 3e-7 - 2e-7j
+    U2 = Q @ B
+    for t, U in enumerate((Q, U1, U2)):
+        g.set_state(t, torch.from_numpy(np.ascontiguousarray(U)).cuda())
+    est = g.probe_orthonormality()
+    exact = [np.linalg.norm(U.conj().T @ U - np.eye(N)) for U in (Q, U1, U2)]
+    assert est[0] < 1e-13
+    assert 0.7 < est[1] / exact[1] < 1.3
+    assert abs(est[2] / exact[2] - 1) < 1e-4
+    g.close()
+
+
+def test_lowrank_probe_gates_refinement(P, monkeypatch):
+    """With the low-rank orthonormaliser the measured CholeskyQR pass runs only when the probe
+    sees ||U^dag U - I||_F above TRAJ_LOWRANK_TOL: over 300 steps the state stays orthonormal to
+    the tolerance, the oracle-lockstep C agrees, a tight tolerance refines more often than a
+    loose one, and TRAJ_LOWRANK_TOL=0 refines every step without probing."""
+    L, gam, steps = 400, 2.0, 300
+    K = lattice.propagator_lattice(L, 1, 1.0, 0.05)
+    o = OracleTrajectory(L, 1, "projective", gam, 0.05, seed=31, traj=0, K=K)
+    res = {}
+    for tol in ("5e-13", "5e-14", "0"):
+        monkeypatch.setenv("TRAJ_LOWRANK_TOL", tol)
+        g = P.Trajectories(L, 1, "projective", [gam], seed=31, orthonormalizer="lowrank")
+        g.step(steps)
+        U = g.get_state(0).cpu().numpy()
+        E = U.conj().T @ U - np.eye(L // 2)
+        res[tol] = (g.lowrank_stats(), np.linalg.norm(E), g.correlation(0).cpu().numpy())
+        g.close()
+    o.step(steps)
+    for tol, (st, nE, C) in res.items():
+        assert nE < max(float(tol), 5e-14) * 3, (tol, nE)
+        assert np.abs(C - o.correlation()).max() < C_TOL
+        assert st["fallbacks"] == 0
+    assert res["0"][0]["probes"] == 0
+    assert res["5e-13"][0]["probes"] >= steps // 2
+    assert res["5e-13"][0]["refinements"] < res["5e-14"][0]["refinements"]
