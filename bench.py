@@ -123,20 +123,23 @@ def cpu_cores() -> int:
 def oracle_steps(w, budget_s: float, max_steps: int):
     """Time the oracle (as it stands) on the same workload: one trajectory from the
     Neel state, whole steps, until max_steps or the time budget is used."""
-    from threadpoolctl import threadpool_info
+    from threadpoolctl import threadpool_info, threadpool_limits
     from oracle import lattice
     from oracle.trajectory import OracleTrajectory
-    K = lattice.propagator_lattice(w.Lx, w.Ly, w.J, w.dt)
-    tr = OracleTrajectory(w.Lx, w.Ly, w.protocol, w.gammas[0], w.dt, w.J, seed=w.seed, traj=0, K=K)
-    times = []
-    t_all = time.perf_counter()
-    while len(times) < max_steps:
-        t0 = time.perf_counter()
-        tr.step(1)
-        times.append(time.perf_counter() - t0)
-        if time.perf_counter() - t_all > budget_s:
-            break
-    blas = [f"{i.get('internal_api')} {i.get('version')} x{i.get('num_threads')}" for i in threadpool_info()]
+    # torchrun exports OMP_NUM_THREADS=1; the oracle leg runs alone on rank 0 and gets every core
+    # of this process's affinity set
+    with threadpool_limits(limits=cpu_cores()):
+        K = lattice.propagator_lattice(w.Lx, w.Ly, w.J, w.dt)
+        tr = OracleTrajectory(w.Lx, w.Ly, w.protocol, w.gammas[0], w.dt, w.J, seed=w.seed, traj=0, K=K)
+        times = []
+        t_all = time.perf_counter()
+        while len(times) < max_steps:
+            t0 = time.perf_counter()
+            tr.step(1)
+            times.append(time.perf_counter() - t0)
+            if time.perf_counter() - t_all > budget_s:
+                break
+        blas = [f"{i.get('internal_api')} {i.get('version')} x{i.get('num_threads')}" for i in threadpool_info()]
     return times, blas
 
 
@@ -155,9 +158,16 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BENCH_SMOKE_ONE_DEVICE=1: launch-logic smoke test of the N > 1 path on a one-GPU box (every
+    # rank on cuda:0, gloo for the barrier / max-over-ranks); its numbers are not measurements
+    if os.environ.get("BENCH_SMOKE_ONE_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("BENCH_SMOKE_ONE_DEVICE") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2508_18468_b200 as P
 
     w, tpg = workload(args)
