@@ -219,12 +219,14 @@ def run_ours(args):
     #   gram (G = U^dag U, upper tiles): 4 (L/P) N^2 per launch, 2 per step
     #   trmm (U <- U R^-1): 4 (L/P) N^2 per launch, 2 per step
     rows = w.L // world if shard else w.L
-    kern = {"propagate": (8.0 * rows * w.L * w.N * tpg, "zgemm_dmma_kernel<N,N>: U <- K U (8 L^2 N flops)"),
-            "gram": (4.0 * rows * w.N * w.N * tpg, "zgemm_dmma_kernel<C,N>: G = U^dag U upper tiles (4 L N^2)"),
-            "trmm": (4.0 * rows * w.N * w.N * tpg, "zgemm_dmma_kernel<N,N> triangular: U <- U R^-1 (4 L N^2)")}
+    algo = P.traj_get_zgemm_algorithm()
+    kn = {"3m": ("zgemm3mw_dmma_kernel<0,0> (3M, 128x64 CTA)", "zgemm3m_dmma_kernel<1,0> (3M, 64x64 CTA)"),
+          "4m": ("zgemm_dmma_kernel<0,0> (4M)", "zgemm_dmma_kernel<1,0> (4M)")}[algo]
+    kern = {"propagate": (8.0 * rows * w.L * w.N * tpg, f"{kn[0]}: U <- K U (8 L^2 N flops)"),
+            "gram": (4.0 * rows * w.N * w.N * tpg, f"{kn[1]}: G = U^dag U upper tiles (4 L N^2)"),
+            "trmm": (4.0 * rows * w.N * w.N * tpg, f"{kn[0]} triangular: U <- U R^-1 (4 L N^2)")}
     if args.propagator == "banded":
         kern.pop("propagate")
-    algo = P.traj_get_zgemm_algorithm()
     pipe_per_alg = 0.75 if algo == "3m" else 1.0      # DMMA flops per algorithmic 8mnk flop
     dom = max(kern, key=lambda k: phases[k][0])
     launches_per_step = max(1.0, phases[dom][1] / args.steps)

@@ -19,7 +19,9 @@ namespace traj {
 
 size_t probe_x_bytes(long long N, int T) { return (size_t)T * N * PROBE_M * 16; }
 size_t probe_y_bytes(long long L, int T) { return (size_t)T * L * PROBE_M * 16; }
-size_t probe_partial_bytes(long long N, int T) { return (size_t)T * PROBE_RS_MAX * N * PROBE_M * 16; }
+size_t probe_partial_bytes(long long N, int T) {
+  return (size_t)T * PROBE_RS_MAX * N * PROBE_M * 16 + (size_t)T * 256 * 8;
+}
 
 namespace {
 
@@ -41,7 +43,7 @@ __global__ void probe_gen_kernel(int N, long long step, long long traj_base, uin
 // Y[t][i][j] = sum_k U[t][i][k] X[t][k][j].  CTA: 8 warps x 4 rows, k in chunks of KC staged in
 // shared memory; lane-strided k (coalesced 512-byte row segments).
 constexpr int PR_ROWS = 32, PR_KC = 256;
-__global__ void __launch_bounds__(256) probe_rows_kernel(const cplx* __restrict__ U, long long ld, long long sU, int L,
+__global__ void __launch_bounds__(256, 2) probe_rows_kernel(const cplx* __restrict__ U, long long ld, long long sU, int L,
                                                          int N, const cplx* __restrict__ X, cplx* __restrict__ Y) {
   __shared__ double2 xs[PR_KC][PROBE_M];
   const int t = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -60,6 +62,7 @@ __global__ void __launch_bounds__(256) probe_rows_kernel(const cplx* __restrict_
       xs[kk][j] = kc + kk < N ? x[(long long)(kc + kk) * PROBE_M + j] : make_double2(0.0, 0.0);
     }
     __syncthreads();
+#pragma unroll 2
     for (int kk = lane; kk < PR_KC && kc + kk < N; kk += 32) {
       double2 v[4];
 #pragma unroll
@@ -130,20 +133,22 @@ __global__ void __launch_bounds__(PC_COLS) probe_cols_kernel(const cplx* __restr
   }
 }
 
-// est[t] = sqrt((1/m) sum_{k,j} |sum_s partial[t][s][k][j] - X[t][k][j]|^2)
-__global__ void probe_finish_kernel(int N, int splits, const cplx* __restrict__ partial, const cplx* __restrict__ X,
-                                    double* est) {
+// part2[t][b] = sum over this block's (k, j) of |sum_s partial[t][s][k][j] - X[t][k][j]|^2
+constexpr int PF_BLOCKS = 256;
+__global__ void probe_reduce_kernel(int N, int splits, const cplx* __restrict__ partial, const cplx* __restrict__ X,
+                                    double* part2) {
   __shared__ double red[32];
-  const int t = blockIdx.x;
+  const int t = blockIdx.y;
+  const long long n = (long long)N * PROBE_M;
   double acc = 0.0;
-  for (long long idx = threadIdx.x; idx < (long long)N * PROBE_M; idx += blockDim.x) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n; idx += (long long)gridDim.x * blockDim.x) {
     double2 z = make_double2(0.0, 0.0);
     for (int s = 0; s < splits; ++s) {
-      const double2 p = partial[((long long)t * PROBE_RS_MAX + s) * N * PROBE_M + idx];
+      const double2 p = partial[((long long)t * PROBE_RS_MAX + s) * n + idx];
       z.x += p.x;
       z.y += p.y;
     }
-    const double2 x = X[(long long)t * N * PROBE_M + idx];
+    const double2 x = X[(long long)t * n + idx];
     const double a = z.x - x.x, b = z.y - x.y;
     acc += a * a + b * b;
   }
@@ -154,6 +159,16 @@ __global__ void probe_finish_kernel(int N, int splits, const cplx* __restrict__ 
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    part2[(long long)t * PF_BLOCKS + blockIdx.x] = s;
+  }
+}
+
+// est[t] = sqrt((1/m) sum_b part2[t][b]), fixed order
+__global__ void probe_finish_kernel(int nblocks, const double* part2, double* est) {
+  const int t = blockIdx.x;
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int b = 0; b < nblocks; ++b) s += part2[(long long)t * PF_BLOCKS + b];
     est[t] = sqrt(s / PROBE_M);
   }
 }
@@ -174,8 +189,12 @@ int probe_orthonormality(cudaStream_t st, const cplx* U, long long ld, long long
   splits = ceil_div(L, rows_per_split);
   probe_cols_kernel<<<dim3((unsigned)cblocks, (unsigned)splits, T), PC_COLS, 0, st>>>(U, ld, sU, L, N, rows_per_split,
                                                                                      Y, partial);
-  probe_finish_kernel<<<T, 256, 0, st>>>(N, (int)splits, partial, X, est);
-  count_launch(4);
+  // the reduction partials live after the split partials of the last trajectory's slot
+  double* part2 = reinterpret_cast<double*>(partial + (size_t)T * PROBE_RS_MAX * N * PROBE_M);
+  const int nb = (int)std::min<long long>(PF_BLOCKS, ceil_div((long long)N * PROBE_M, 256));
+  probe_reduce_kernel<<<dim3((unsigned)nb, T), 256, 0, st>>>(N, (int)splits, partial, X, part2);
+  probe_finish_kernel<<<T, 32, 0, st>>>(nb, part2, est);
+  count_launch(5);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     if (err) *err = std::string("probe_orthonormality: ") + cudaGetErrorString(e);
