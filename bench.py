@@ -29,6 +29,7 @@ import numpy as np  # noqa: E402
 
 import workloads  # noqa: E402
 
+HBM_PEAK_GBS = 6536.7         # MEASURED_PEAKS.json hbm_gbs (copy bandwidth on this pool's B200)
 FP64_PEAK_TFLOPS = 37.1        # measured DMMA.8x8x4 issue-rate peak, profiles/r01_fp64_microbench.txt
 FP64_PEAK_SOURCE = ("measured on this pool's B200: DMMA.8x8x4 microbenchmark 37.1 TF/s (cuBLAS ZGEMM 37.0 TF/s), "
                     "profiles/r01_fp64_microbench.txt; MEASURED_PEAKS.json has no FP64 entry "
@@ -254,6 +255,22 @@ def run_ours(args):
                                            if isinstance(v, dict)}}
         except Exception:
             library = None
+    # HBM-bound kernels of the step (a2 homodyne "32 L N bytes"; NEXT-1 banded stencil
+    # 32 L N bytes per 1d pass, two passes in 2d): algorithmic bytes / event-timed phase time
+    hbm = {}
+    if w.protocol == "homodyne" and phases["monitor"][0] > 0:
+        b = 32.0 * rows * w.N * tpg * args.steps
+        g = b / (phases["monitor"][0] / 1e3) / 1e9
+        hbm["row_monitor_kernel (homodyne, 32 L N B/step)"] = {"achieved_gbs": g, "peak_gbs": HBM_PEAK_GBS,
+                                                               "frac": g / HBM_PEAK_GBS,
+                                                               "ms_per_step": phases["monitor"][0] / args.steps}
+    if args.propagator == "banded" and phases["propagate"][0] > 0:
+        passes = 1 if w.Ly == 1 else 2
+        b = 32.0 * passes * rows * w.N * tpg * args.steps
+        g = b / (phases["propagate"][0] / 1e3) / 1e9
+        hbm[f"banded_kernel ({passes} pass(es), 32 L N B each)"] = {"achieved_gbs": g, "peak_gbs": HBM_PEAK_GBS,
+                                                                   "frac": g / HBM_PEAK_GBS,
+                                                                   "ms_per_step": phases["propagate"][0] / args.steps}
     step_flops = {"propagate": 8.0 * rows * w.L * w.N * tpg if args.propagator == "dense" else 0.0,
                   "gram": 2 * 4.0 * rows * w.N * w.N * tpg, "trmm": 2 * 4.0 * rows * w.N * w.N * tpg,
                   "chol": (8.0 / 3.0) * w.N ** 3 * tpg}
@@ -311,6 +328,7 @@ def run_ours(args):
                               "6mnk flops on the DMMA pipe, reported as pipe_tflops / pipe_frac")
                      if algo == "3m" else "4M: 8mnk flops on the DMMA pipe"},
         "library_same_shape": library,
+        "hbm_kernels": hbm or None,
         "step_dense_tflops": dense_tflops,
         "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
         "phase_launches_per_step": {k: v[1] / args.steps for k, v in phases.items()},

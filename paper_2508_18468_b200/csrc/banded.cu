@@ -21,18 +21,21 @@ constexpr int RG = 4;       // row groups per CTA
 // output positions per thread: the register window is RPT + 2W complex values
 template <int W>
 struct Rpt {
-  static constexpr int value = W <= 12 ? 16 : (W <= 16 ? 12 : 8);
+  static constexpr int value = 8;
+};
+
+// the 2W+1 taps travel as a kernel parameter: constant-bank operands of the DFMAs
+template <int W>
+struct Taps {
+  double2 c[2 * W + 1];
 };
 
 // one thread: column k, positions [p0, p0 + RPT) of one line
 template <int W, int RPT = Rpt<W>::value>
-__global__ void __launch_bounds__(TC * RG) banded_kernel(const cplx* __restrict__ U, cplx* __restrict__ V,
+__global__ void __launch_bounds__(TC * RG, W <= 10 ? 2 : 1) banded_kernel(const cplx* __restrict__ U, cplx* __restrict__ V,
                                                          long long ld, long long sU, int N, int len, int lines,
                                                          long long line_stride, long long pos_stride,
-                                                         const cplx* __restrict__ coef, int periodic) {
-  __shared__ double2 c[2 * W + 1];
-  for (int i = threadIdx.x; i < 2 * W + 1; i += blockDim.x) c[i] = coef[i];
-  __syncthreads();
+                                                         const __grid_constant__ Taps<W> taps, int periodic) {
   const int col = blockIdx.y * TC + (threadIdx.x % TC);
   const int tiles_per_line = (len + RPT * RG - 1) / (RPT * RG);
   const int line = blockIdx.x / tiles_per_line;
@@ -40,13 +43,18 @@ __global__ void __launch_bounds__(TC * RG) banded_kernel(const cplx* __restrict_
   if (col >= N || line >= lines || p0 >= len) return;
   const cplx* u = U + (long long)blockIdx.z * sU + line * line_stride * ld + col;
   cplx* v = V + (long long)blockIdx.z * sU + line * line_stride * ld + col;
+  const long long step = pos_stride * ld;
   double2 in[RPT + 2 * W];
 #pragma unroll
   for (int q = 0; q < RPT + 2 * W; ++q) {
-    int p = p0 - W + q;
-    if (periodic) p = ((p % len) + len) % len;
-    else p = p0 + q;      // halo mode: the input carries W extra positions on each side
-    in[q] = u[(long long)p * pos_stride * ld];
+    int p;
+    if (periodic) {              // p0 - W + q lies in [-W, len + W): one conditional wrap
+      p = p0 - W + q;
+      p = p < 0 ? p + len : (p >= len ? p - len : p);
+    } else {
+      p = p0 + q;                // halo mode: the input carries W extra positions on each side
+    }
+    in[q] = u[(long long)p * step];
   }
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
@@ -54,23 +62,25 @@ __global__ void __launch_bounds__(TC * RG) banded_kernel(const cplx* __restrict_
     double re = 0.0, im = 0.0;
 #pragma unroll
     for (int d = 0; d < 2 * W + 1; ++d) {
-      const double2 a = c[d], b = in[r + d];
+      const double2 a = taps.c[d], b = in[r + d];
       re = fma(a.x, b.x, re);
       re = fma(-a.y, b.y, re);
       im = fma(a.x, b.y, im);
       im = fma(a.y, b.x, im);
     }
-    v[(long long)(p0 + r) * pos_stride * ld] = make_double2(re, im);
+    v[(long long)(p0 + r) * step] = make_double2(re, im);
   }
 }
 
 template <int W>
 cudaError_t launch(cudaStream_t st, const cplx* U, cplx* V, long long ld, long long sU, int N, int len, int lines,
-                   long long ls, long long ps, const cplx* coef, int T, int periodic) {
+                   long long ls, long long ps, const cplx* coef_host, int T, int periodic) {
   constexpr int RPT = Rpt<W>::value;
+  Taps<W> taps;
+  for (int i = 0; i < 2 * W + 1; ++i) taps.c[i] = coef_host[i];
   const int tiles = (len + RPT * RG - 1) / (RPT * RG);
   dim3 grid((unsigned)(tiles * lines), (unsigned)ceil_div(N, TC), (unsigned)T);
-  banded_kernel<W><<<grid, TC * RG, 0, st>>>(U, V, ld, sU, N, len, lines, ls, ps, coef, periodic);
+  banded_kernel<W><<<grid, TC * RG, 0, st>>>(U, V, ld, sU, N, len, lines, ls, ps, taps, periodic);
   count_launch();
   return cudaGetLastError();
 }
@@ -78,19 +88,23 @@ cudaError_t launch(cudaStream_t st, const cplx* U, cplx* V, long long ld, long l
 }  // namespace
 
 int banded_template_width(int w) {
-  for (int W : {2, 4, 8, 12, 16, 24, 32})
+  for (int W : {2, 4, 8, 9, 10, 11, 12, 16, 24, 32})
     if (w <= W) return W;
   return -1;
 }
 
 int banded_pass(cudaStream_t st, const cplx* U, cplx* V, long long ld, long long sU, int N, int T, int len, int lines,
-                long long line_stride, long long pos_stride, const cplx* coef, int W, std::string* err,
+                long long line_stride, long long pos_stride, const cplx* coef_host, int W, std::string* err,
                 int periodic) {
+  const cplx* coef = coef_host;
   cudaError_t e;
   switch (W) {
     case 2: e = launch<2>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T, periodic); break;
     case 4: e = launch<4>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T, periodic); break;
     case 8: e = launch<8>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T, periodic); break;
+    case 9: e = launch<9>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T, periodic); break;
+    case 10: e = launch<10>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T, periodic); break;
+    case 11: e = launch<11>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T, periodic); break;
     case 12: e = launch<12>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T, periodic); break;
     case 16: e = launch<16>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T, periodic); break;
     case 24: e = launch<24>(st, U, V, ld, sU, N, len, lines, line_stride, pos_stride, coef, T, periodic); break;

@@ -312,7 +312,11 @@ int shard_init(ShardedCtx* sh, const traj_config* c, std::string* err) {
 int shard_build(ShardedCtx* sh, const std::vector<std::complex<double>>& kc, const std::vector<int32_t>& sites,
                 std::string* err, const std::vector<std::complex<double>>* band) {
   cudaStream_t st = sh->st;
-  if (sh->banded) SCK(cudaMemcpyAsync(sh->bcoef, band->data(), band->size() * 16, cudaMemcpyHostToDevice, st));
+  if (sh->banded) {
+    SCK(cudaMemcpyAsync(sh->bcoef, band->data(), band->size() * 16, cudaMemcpyHostToDevice, st));
+    sh->band_host.resize(band->size());
+    for (size_t i = 0; i < band->size(); ++i) sh->band_host[i] = make_double2((*band)[i].real(), (*band)[i].imag());
+  }
   SCK(cudaMemcpyAsync(sh->kcoef, kc.data(), kc.size() * 16, cudaMemcpyHostToDevice, st));
   SCK(cudaMemcpyAsync(sh->sites, sites.data(), sites.size() * 4, cudaMemcpyHostToDevice, st));
   SCK(cudaMemcpyAsync(sh->gamma_dev, &sh->gamma, 8, cudaMemcpyHostToDevice, st));
@@ -464,7 +468,7 @@ int propagate_banded(ShardedCtx* sh, int cur, int nxt, std::string* err) {
   for (auto& l : sh->loc) {
     cplx* mid = l.Uext + H * ld;
     if (twod) {
-      STRY(banded_pass(st, l.U[cur], mid, ld, 0, sh->N, 1, sh->Lx, (int)(Lp / sh->Lx), sh->Lx, 1, sh->bcoef, sh->Wx,
+      STRY(banded_pass(st, l.U[cur], mid, ld, 0, sh->N, 1, sh->Lx, (int)(Lp / sh->Lx), sh->Lx, 1, sh->band_host.data(), sh->Wx,
                        err));
     } else {
       SCK(cudaMemcpyAsync(mid, l.U[cur], (size_t)Lp * ld * 16, cudaMemcpyDeviceToDevice, st));
@@ -478,9 +482,9 @@ int propagate_banded(ShardedCtx* sh, int cur, int nxt, std::string* err) {
   for (auto& l : sh->loc) {
     if (twod)
       STRY(banded_pass(st, l.Uext, l.U[nxt], ld, 0, sh->N, 1, (int)(Lp / sh->Lx), sh->Lx, 1, sh->Lx,
-                       sh->bcoef + 2 * sh->Wx + 1, sh->Wy, err, 0));
+                       sh->band_host.data() + 2 * sh->Wx + 1, sh->Wy, err, 0));
     else
-      STRY(banded_pass(st, l.Uext, l.U[nxt], ld, 0, sh->N, 1, (int)Lp, 1, 0, 1, sh->bcoef, sh->Wx, err, 0));
+      STRY(banded_pass(st, l.Uext, l.U[nxt], ld, 0, sh->N, 1, (int)Lp, 1, 0, 1, sh->band_host.data(), sh->Wx, err, 0));
   }
   return 0;
 }

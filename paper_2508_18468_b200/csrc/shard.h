@@ -48,6 +48,7 @@ struct ShardedCtx {
   bool banded = false;     // NEXT-1 with sharding: halo exchange instead of the allgather
   int Wx = 0, Wy = 0, H = 0;
   cplx* bcoef = nullptr;
+  std::vector<cplx> band_host;   // host copy of the stencil taps (launch parameters)
   double dt = 0, J = 0, gamma = 0;
   uint64_t seed = 0;
   long long traj_base = 0;

@@ -36,7 +36,8 @@ struct traj_ctx {
   ShardedCtx* sh = nullptr;        // row-sharded mode (shard_size > 1 or an NCCL communicator)
   bool banded = false;             // TRAJ_PROP_BANDED with a band narrower than the lattice
   int Wx = 0, Wy = 0;              // compiled half-bandwidths per axis
-  cplx* bcoef = nullptr;           // [2Wx+1 | 2Wy+1] stencil coefficients
+  cplx* bcoef = nullptr;           // [2Wx+1 | 2Wy+1] stencil coefficients (device copy)
+  std::vector<cplx> band_host;     // the same on the host: passed by value to the stencil launches
   cplx* Wrk = nullptr;             // RK4 QSD scratch, shaped like U
   // event-driven PM (NEXT-4)
   std::vector<long long> ev_count;
@@ -721,9 +722,10 @@ int one_step(traj_ctx* h) {
     Phase p(&h->prof, h->st, TRAJ_PH_PROPAGATE);
     if (h->banded) {
       // 1d: one pass along the ring; 2d: x pass (lines = rows y) then y pass (lines = columns x)
-      TRY(banded_pass(h->st, Uc, Un, h->ldN, h->sU, h->N, h->T, h->Lx, h->Ly, h->Lx, 1, h->bcoef, h->Wx, &h->err));
+      TRY(banded_pass(h->st, Uc, Un, h->ldN, h->sU, h->N, h->T, h->Lx, h->Ly, h->Lx, 1, h->band_host.data(), h->Wx,
+                      &h->err));
       if (h->Ly > 1) {
-        TRY(banded_pass(h->st, Un, Uc, h->ldN, h->sU, h->N, h->T, h->Ly, h->Lx, 1, h->Lx, h->bcoef + 2 * h->Wx + 1,
+        TRY(banded_pass(h->st, Un, Uc, h->ldN, h->sU, h->N, h->T, h->Ly, h->Lx, 1, h->Lx, h->band_host.data() + 2 * h->Wx + 1,
                         h->Wy, &h->err));
         Us = Uc;
       }
@@ -1045,6 +1047,8 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
     if (h->Ly > 1) axis(h->Ly, h->Wy);
     else band.push_back(1.0);
   }
+  h->band_host.resize(band.size());
+  for (size_t i = 0; i < band.size(); ++i) h->band_host[i] = make_double2(band[i].real(), band[i].imag());
   if (h->sh) {
     int s2 = shard_build(h->sh, kc, sites, &e, &band);
     if (s2) return bail(s2, e);
