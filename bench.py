@@ -271,6 +271,12 @@ def run_ours(args):
         hbm[f"banded_kernel ({passes} pass(es), 32 L N B each)"] = {"achieved_gbs": g, "peak_gbs": HBM_PEAK_GBS,
                                                                    "frac": g / HBM_PEAK_GBS,
                                                                    "ms_per_step": phases["propagate"][0] / args.steps}
+    if w.protocol == "homodyne_rk4" and phases["propagate"][0] > 0:
+        b = 4 * 48.0 * rows * w.N * tpg * args.steps
+        g = b / (phases["propagate"][0] / 1e3) / 1e9
+        hbm["horner_pass_kernel (RK4 as 4 Horner passes, 48 L N B each)"] = {
+            "achieved_gbs": g, "peak_gbs": HBM_PEAK_GBS, "frac": g / HBM_PEAK_GBS,
+            "ms_per_step": phases["propagate"][0] / args.steps}
     step_flops = {"propagate": 8.0 * rows * w.L * w.N * tpg if args.propagator == "dense" else 0.0,
                   "gram": 2 * 4.0 * rows * w.N * w.N * tpg, "trmm": 2 * 4.0 * rows * w.N * w.N * tpg,
                   "chol": (8.0 / 3.0) * w.N ** 3 * tpg}

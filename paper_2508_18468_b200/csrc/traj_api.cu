@@ -659,12 +659,9 @@ int event_window(traj_ctx* h) {
         if (p.j >= 0) {
           TRY(event_prep(h->st, src, h->ldN, h->N, h->Lx, h->Ly, p.j, cx, p.x.lo, p.x.n, cy, p.y.lo, p.y.n, p.pc,
                          h->yhat, h->ev_coef, h->occ_count + t, &h->err));
-          TRY(event_update(h->st, src, dst, h->ldN, h->N, h->Lx, h->Ly, cx, p.x.lo, p.x.n, cy, p.y.lo, p.y.n,
-                           h->yhat, h->ev_coef, p.j, &h->err));
-        } else {
-          TRY(event_update(h->st, src, dst, h->ldN, h->N, h->Lx, h->Ly, cx, p.x.lo, p.x.n, cy, p.y.lo, p.y.n,
-                           nullptr, nullptr, -1, &h->err));
         }
+        TRY(event_update(h->st, src, dst, h->ldN, h->N, h->Lx, h->Ly, cx, p.x.lo, p.x.n, cy, p.y.lo, p.y.n,
+                         p.j >= 0 ? h->yhat : nullptr, p.j >= 0 ? h->ev_coef : nullptr, p.j, &h->err));
         std::swap(src, dst);
       }
       CK(cudaStreamSynchronize(h->st));    // the staging buffer is reused
@@ -694,6 +691,9 @@ int one_step(traj_ctx* h) {
       int s = event_window(h);
       if (s) return s;
     }
+    // the per-event updates are exact rank-1 maps of an orthonormal U: with the low-rank
+    // orthonormaliser the window's CholeskyQR runs only when the probe sees drift
+    if (h->lowrank_orth) h->lr_k0 = 0;
     int s = cqr2(h, Un, Uc);
     if (s) return s;
     h->cur = 1 - h->cur;
@@ -1007,7 +1007,8 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
     h->full_cqr2 = e && e[0] == '1';
     const char* g = getenv("TRAJ_LOWRANK_GRAM");
     h->lowrank_gram = !(g && g[0] == '0') || cfg->orthonormalizer == TRAJ_ORTH_LOWRANK;
-    h->lowrank_orth = cfg->orthonormalizer == TRAJ_ORTH_LOWRANK && cfg->protocol == TRAJ_PROJECTIVE;
+    h->lowrank_orth = cfg->orthonormalizer == TRAJ_ORTH_LOWRANK &&
+                      (cfg->protocol == TRAJ_PROJECTIVE || cfg->protocol == TRAJ_PROJECTIVE_EVENTS);
     const char* rf = getenv("TRAJ_LOWRANK_REFINE");
     h->lowrank_refine = !(rf && rf[0] == '0');
     const char* tl = getenv("TRAJ_LOWRANK_TOL");

@@ -369,13 +369,16 @@ def test_rk4_qsd_protocol_matches_oracle(P, Lx, Ly):
     lockstep(P, Lx, Ly, "homodyne_rk4", [0.3, 2.0], 60, 20, [A], seed=12)
 
 
-@pytest.mark.parametrize("Lx,Ly,gam", [(64, 1, 3.0), (96, 1, 0.5), (8, 6, 4.0)])
-def test_event_driven_pm_matches_oracle(P, Lx, Ly, gam):
+@pytest.mark.parametrize("Lx,Ly,gam,orth", [(64, 1, 3.0, "cqr2"), (96, 1, 0.5, "cqr2"), (8, 6, 4.0, "cqr2"),
+                                             (100, 1, 2.0, "lowrank"), (8, 6, 4.0, "lowrank")])
+def test_event_driven_pm_matches_oracle(P, Lx, Ly, gam, orth):
     """NEXT-4: the paper-literal event-driven PM (Poisson waiting times, one site per event,
     Eq. A1/A2 on the L x L matrix in the oracle) against the GPU's orbital form (banded K(tau)
-    stencils and exact rank-1 updates), with the same Philox event stream."""
+    stencils and exact rank-1 updates; 1d: the row-blocked kernel, L = 100 leaves a ragged last
+    block), with the same Philox event stream.  orth = "lowrank": the window's CholeskyQR runs
+    only when the orthonormality probe sees drift."""
     from oracle.pm_events import EventPM
-    g = P.Trajectories(Lx, Ly, "projective_events", [gam, gam * 1.5], seed=3)
+    g = P.Trajectories(Lx, Ly, "projective_events", [gam, gam * 1.5], seed=3, orthonormalizer=orth)
     orc = [EventPM(Lx, Ly, gm, 0.05, seed=3, traj=t) for t, gm in enumerate([gam, gam * 1.5])]
     A = np.arange(Lx * Ly // 2)
     events = 0
