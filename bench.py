@@ -330,6 +330,11 @@ def run_ours(args):
                      "kernel_ms": kern_ms, "peak_source": FP64_PEAK_SOURCE,
                      "complex_mult": algo,
                      "pipe_tflops": achieved * pipe_per_alg, "pipe_frac": achieved * pipe_per_alg / FP64_PEAK_TFLOPS,
+                     "traffic_note": ("ncu dram bytes of one K U launch (profiles/ncu_traffic.json) vs 8.6 GB "
+                                      "algorithmic: each wave of 148 output-stationary 128x64 tiles streams its K "
+                                      "panels (~580 MB per wave at K = 16384, > L2), so >= ~64 GB is inherent to "
+                                      "this tiling; 154 GB in 390 ms is ~0.4 TB/s, 6% of HBM, not a bound")
+                     if traffic else None,
                      "note": ("achieved counts the conventional 8mnk complex flops; the 3M (Gauss) kernels issue "
                               "6mnk flops on the DMMA pipe, reported as pipe_tflops / pipe_frac")
                      if algo == "3m" else "4M: 8mnk flops on the DMMA pipe"},
