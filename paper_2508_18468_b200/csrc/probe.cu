@@ -40,10 +40,10 @@ __global__ void probe_gen_kernel(int N, long long step, long long traj_base, uin
   }
 }
 
-// Y[t][i][j] = sum_k U[t][i][k] X[t][k][j].  CTA: 8 warps x 4 rows, k in chunks of KC staged in
+// Y[t][i][j] = sum_k U[t][i][k] X[t][k][j].  CTA: 4 warps x 4 rows, k in chunks of KC staged in
 // shared memory; lane-strided k (coalesced 512-byte row segments).
-constexpr int PR_ROWS = 32, PR_KC = 256;
-__global__ void __launch_bounds__(256, 2) probe_rows_kernel(const cplx* __restrict__ U, long long ld, long long sU, int L,
+constexpr int PR_ROWS = 16, PR_KC = 256, PR_THREADS = 128;
+__global__ void __launch_bounds__(PR_THREADS, 4) probe_rows_kernel(const cplx* __restrict__ U, long long ld, long long sU, int L,
                                                          int N, const cplx* __restrict__ X, cplx* __restrict__ Y) {
   __shared__ double2 xs[PR_KC][PROBE_M];
   const int t = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256, 2) probe_rows_kernel(const cplx* __restri
       xs[kk][j] = kc + kk < N ? x[(long long)(kc + kk) * PROBE_M + j] : make_double2(0.0, 0.0);
     }
     __syncthreads();
-#pragma unroll 2
+#pragma unroll 4
     for (int kk = lane; kk < PR_KC && kc + kk < N; kk += 32) {
       double2 v[4];
 #pragma unroll
@@ -180,7 +180,7 @@ int probe_orthonormality(cudaStream_t st, const cplx* U, long long ld, long long
                          double* est, std::string* err) {
   const uint32_t k0 = (uint32_t)(seed & 0xffffffffu), k1 = (uint32_t)(seed >> 32);
   probe_gen_kernel<<<dim3((unsigned)ceil_div(N, 256), T), 256, 0, st>>>(N, step, traj_base, k0, k1, X);
-  probe_rows_kernel<<<dim3((unsigned)ceil_div(L, PR_ROWS), T), 256, 0, st>>>(U, ld, sU, L, N, X, Y);
+  probe_rows_kernel<<<dim3((unsigned)ceil_div(L, PR_ROWS), T), PR_THREADS, 0, st>>>(U, ld, sU, L, N, X, Y);
   // row splits: about 4 CTAs per SM over (column blocks x splits x T), at least 64 rows per split
   const long long cblocks = ceil_div(N, PC_COLS);
   long long splits = ceil_div(4 * 148, cblocks * T);
