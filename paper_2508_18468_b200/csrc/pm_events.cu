@@ -12,6 +12,9 @@
 // and (alpha, beta); one fused pass per event then propagates each row by the stencil, forms
 // v_i = <r_i, yhat> and writes r_i + (alpha v_i + beta delta_ij) yhat: O(L N) per event.
 #include <math.h>
+
+#include <algorithm>
+
 #include "common.cuh"
 #include "pm_events.h"
 
@@ -202,6 +205,402 @@ int event_update(cudaStream_t st, const cplx* U, cplx* out, long long ld, int N,
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess && err) *err = std::string("event_update: ") + cudaGetErrorString(e);
+  return e == cudaSuccess ? 0 : 4;
+}
+
+
+
+// ---------------------------------------------------------------------------------------------
+// One-pass event updates.  With g = U yhat^dag (an L-vector) the rank-1 coefficient of every row
+// is known before the pass: <r_i, yhat> = (K(tau) g)_i, r = K(tau) U.  The pass for event q then
+// reads U once, writes r_i + (alpha (K g)_i + beta delta_ij) yhat once, and accumulates
+// g' = out yhat'^dag for the NEXT event q+1, whose yhat' (row j' of K(tau') out) was prepared
+// before the pass: the K(tau) commute, so row j' of K(tau') out = row j' of K(tau + tau') U plus
+// (K(tau') x)_j' yhat with x_m = alpha (K(tau) g)_m + beta delta_mj -- one row stencil and a
+// scalar.  yhat is kept unnormalised (r) with its scale s = 1/|r| in coef[4].
+namespace {
+
+struct DevTaps {
+  const cplx* c;
+  int lo, n;
+};
+
+__device__ __forceinline__ int nb_site(int m, int Lx, int Ly, int ox, int oy) {
+  const int x = m % Lx, y = m / Lx;
+  int xx = x + ox, yy = y + oy;
+  xx %= Lx;
+  if (xx < 0) xx += Lx;
+  yy %= Ly;
+  if (yy < 0) yy += Ly;
+  return yy * Lx + xx;
+}
+
+// (K g)_m for the product taps (tx, ty), g an L-vector
+__device__ __forceinline__ double2 stencil_vec(const double2* g, int Lx, int Ly, int m, DevTaps tx, DevTaps ty) {
+  double re = 0.0, im = 0.0;
+  for (int qy = 0; qy < ty.n; ++qy)
+    for (int qx = 0; qx < tx.n; ++qx) {
+      const double2 a = tx.c[qx], b = ty.c[qy];
+      const double cr = a.x * b.x - a.y * b.y, ci = a.x * b.y + a.y * b.x;
+      const double2 v = g[nb_site(m, Lx, Ly, tx.lo + qx, ty.lo + qy)];
+      re += cr * v.x - ci * v.y;
+      im += cr * v.y + ci * v.x;
+    }
+  return make_double2(re, im);
+}
+
+// r_k = (K(tau + tau') U)_{j', k} + X yprev_k sprev,  X = sum_{q'} c'_{q'} x_{m_q'} (prev event);
+// part[b] = sum over this block's k of |r_k|^2.  Without a previous event: r = (K(tau') U)_{j'}.
+constexpr int EVP_THREADS = 256;
+__global__ void __launch_bounds__(EVP_THREADS) ev_prep_kernel(const cplx* U, long long ld, int N, int Lx, int Ly, int j,
+                                                             DevTaps cx, DevTaps cy, DevTaps ox, DevTaps oy,
+                                                             DevTaps ix, DevTaps iy, const double* coef_prev,
+                                                             const double2* g_prev, const cplx* y_prev, int j_prev,
+                                                             cplx* y_out, double* part) {
+  __shared__ double red[EVP_THREADS / 32];
+  __shared__ double2 Xs;
+  if (threadIdx.x == 0) {
+    double2 X = make_double2(0.0, 0.0);
+    if (coef_prev) {
+      const double alpha = coef_prev[0], beta = coef_prev[1], s = coef_prev[4];
+      for (int qy = 0; qy < oy.n; ++qy)
+        for (int qx = 0; qx < ox.n; ++qx) {
+          const int m = nb_site(j, Lx, Ly, ox.lo + qx, oy.lo + qy);
+          const double2 v = stencil_vec(g_prev, Lx, Ly, m, ix, iy);
+          double xr = alpha * v.x + (m == j_prev ? beta : 0.0), xi = alpha * v.y;
+          const double2 a = ox.c[qx], b = oy.c[qy];
+          const double cr = a.x * b.x - a.y * b.y, ci = a.x * b.y + a.y * b.x;
+          X.x += cr * xr - ci * xi;
+          X.y += cr * xi + ci * xr;
+        }
+      X.x *= s;
+      X.y *= s;
+    }
+    Xs = X;
+  }
+  __syncthreads();
+  const double2 X = Xs;
+  double p = 0.0;
+  for (int k = blockIdx.x * EVP_THREADS + threadIdx.x; k < N; k += gridDim.x * EVP_THREADS) {
+    double2 r = stencil(U, ld, Lx, Ly, j, k, Taps{cx.c, cx.lo, cx.n}, Taps{cy.c, cy.lo, cy.n});
+    if (coef_prev) {
+      const double2 y = y_prev[k];
+      r.x += X.x * y.x - X.y * y.y;
+      r.y += X.x * y.y + X.y * y.x;
+    }
+    y_out[k] = r;
+    p += r.x * r.x + r.y * r.y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = p;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < EVP_THREADS / 32; ++w) s += red[w];
+    part[blockIdx.x] = s;
+  }
+}
+
+// coef = [alpha, beta, occ, p, s]: the Born decision of P:174 on p = |r_j|^2 (readings Q13, Q17)
+__global__ void ev_decide_kernel(const double* part, int nparts, double pc, double* coef, int32_t* occ_count) {
+  if (threadIdx.x != 0) return;
+  double p = 0.0;
+  for (int b = 0; b < nparts; ++b) p += part[b];
+  const double pcl = fmin(fmax(p, 0.0), 1.0);
+  bool occ = pc <= pcl;
+  if (occ && pcl < 1e-12) occ = false;
+  else if (!occ && 1.0 - pcl < 1e-12) occ = true;
+  double alpha = 0.0, beta = 0.0, s = 0.0;
+  if (p > 1e-300) {
+    s = 1.0 / sqrt(p);
+    if (occ) {
+      alpha = -1.0;
+      beta = 1.0;
+    } else {
+      const double c = 1.0 / sqrt(fmax(1.0 - p, 1e-300)) - 1.0;
+      alpha = c;
+      beta = -(1.0 + c) * sqrt(p);
+    }
+  }
+  coef[0] = alpha;
+  coef[1] = beta;
+  coef[2] = occ ? 1.0 : 0.0;
+  coef[3] = p;
+  coef[4] = s;
+  if (occ) ++*occ_count;
+}
+
+// g_i = s sum_k U_ik conj(y_k): one warp per row
+__global__ void __launch_bounds__(256) ev_gemv_kernel(const cplx* U, long long ld, int N, int L, const cplx* y,
+                                                      const double* coef, double2* g) {
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (i >= L) return;
+  const cplx* u = U + (long long)i * ld;
+  double re = 0.0, im = 0.0;
+#pragma unroll 4
+  for (int k = lane; k < N; k += 32) {
+    const double2 a = u[k], b = y[k];
+    re += a.x * b.x + a.y * b.y;
+    im += a.y * b.x - a.x * b.y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    re += __shfl_xor_sync(0xffffffffu, re, o);
+    im += __shfl_xor_sync(0xffffffffu, im, o);
+  }
+  if (lane == 0) {
+    const double s = coef[4];
+    g[i] = make_double2(s * re, s * im);
+  }
+}
+
+// taps by value for the 1d row-blocked pass: (re, im, -im) so no negation is formed per thread
+template <int W>
+struct EvTaps {
+  double c[2 * W + 1][3];
+};
+
+// 1d ring: EV_R (8 for W <= 4, else 4: registers) consecutive rows per CTA, each input row loaded once per column into a register
+// window.  out_i = sum_d c_d U_{i+d} + x_i yhat (x_i from g), gn_i = <out_i, yhat_next>.
+template <int W, int EV_R>
+__global__ void __launch_bounds__(256) ev_pass_1d_kernel(const cplx* __restrict__ U, cplx* __restrict__ out,
+                                                         long long ld, int N, int L,
+                                                         const __grid_constant__ EvTaps<W> taps,
+                                                         const cplx* __restrict__ y, const double* __restrict__ coef,
+                                                         const double2* __restrict__ g, int j,
+                                                         const cplx* __restrict__ yn, const double* __restrict__ coefn,
+                                                         double2* __restrict__ gn) {
+  __shared__ double2 xs[EV_R];
+  __shared__ double red[8][2 * EV_R];
+  const int i0 = blockIdx.x * EV_R;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < EV_R) {
+    double2 x = make_double2(0.0, 0.0);
+    const int i = i0 + threadIdx.x;
+    if (coef && i < L) {
+      double vr = 0.0, vi = 0.0;
+      for (int d = 0; d < 2 * W + 1; ++d) {
+        int p = i - W + d;
+        p = p < 0 ? p + L : (p >= L ? p - L : p);
+        const double2 v = g[p];
+        vr += taps.c[d][0] * v.x - taps.c[d][1] * v.y;
+        vi += taps.c[d][0] * v.y + taps.c[d][1] * v.x;
+      }
+      const double s = coef[4];
+      x = make_double2(s * (coef[0] * vr + (i == j ? coef[1] : 0.0)), s * coef[0] * vi);
+    }
+    xs[threadIdx.x] = x;
+  }
+  __syncthreads();
+  double2 x[EV_R];
+#pragma unroll
+  for (int r = 0; r < EV_R; ++r) x[r] = xs[r];
+  const double sn = coefn ? coefn[4] : 0.0;
+  double ar[EV_R], ai[EV_R];
+#pragma unroll
+  for (int r = 0; r < EV_R; ++r) ar[r] = ai[r] = 0.0;
+  const bool wraps = i0 - W < 0 || i0 + EV_R + W > L;
+#pragma unroll 1
+  for (int k = threadIdx.x; k < N; k += 256) {
+    double2 in[EV_R + 2 * W];
+#pragma unroll
+    for (int q = 0; q < EV_R + 2 * W; ++q) {
+      int p = i0 - W + q;
+      if (wraps) p = p < 0 ? p + L : (p >= L ? p - L : p);
+      in[q] = U[(long long)p * ld + k];
+    }
+    const double2 yk = coef ? y[k] : make_double2(0.0, 0.0);
+    const double2 ynk = yn ? yn[k] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int r = 0; r < EV_R; ++r) {
+      double re = x[r].x * yk.x - x[r].y * yk.y, im = x[r].x * yk.y + x[r].y * yk.x;
+#pragma unroll
+      for (int d = 0; d < 2 * W + 1; ++d) {
+        const double2 b = in[r + d];
+        re = fma(taps.c[d][0], b.x, re);
+        re = fma(taps.c[d][2], b.y, re);
+        im = fma(taps.c[d][0], b.y, im);
+        im = fma(taps.c[d][1], b.x, im);
+      }
+      if (i0 + r < L) out[(long long)(i0 + r) * ld + k] = make_double2(re, im);
+      ar[r] += re * ynk.x + im * ynk.y;
+      ai[r] += im * ynk.x - re * ynk.y;
+    }
+  }
+  if (!yn) return;
+#pragma unroll
+  for (int r = 0; r < EV_R; ++r) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ar[r] += __shfl_xor_sync(0xffffffffu, ar[r], o);
+      ai[r] += __shfl_xor_sync(0xffffffffu, ai[r], o);
+    }
+    if (lane == 0) {
+      red[warp][2 * r] = ar[r];
+      red[warp][2 * r + 1] = ai[r];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < EV_R && i0 + threadIdx.x < L) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      a += red[w][2 * threadIdx.x];
+      b += red[w][2 * threadIdx.x + 1];
+    }
+    gn[i0 + threadIdx.x] = make_double2(sn * a, sn * b);
+  }
+}
+
+// any lattice / any taps: one CTA per row with the resolved tap table in shared memory
+constexpr int EVG_MAXTAPS = 1024;
+__global__ void __launch_bounds__(256) ev_pass_generic_kernel(const cplx* __restrict__ U, cplx* __restrict__ out,
+                                                              long long ld, int N, int Lx, int Ly, DevTaps tx,
+                                                              DevTaps ty, const cplx* __restrict__ y,
+                                                              const double* __restrict__ coef,
+                                                              const double2* __restrict__ g, int j,
+                                                              const cplx* __restrict__ yn,
+                                                              const double* __restrict__ coefn,
+                                                              double2* __restrict__ gn) {
+  __shared__ int trow[EVG_MAXTAPS];
+  __shared__ double2 tcoef[EVG_MAXTAPS];
+  __shared__ double red[16];
+  __shared__ double2 xs;
+  const int i = blockIdx.x;
+  const int nt = tx.n * ty.n;
+  for (int q = threadIdx.x; q < nt; q += 256) {
+    const int qy = q / tx.n, qx = q % tx.n;
+    trow[q] = nb_site(i, Lx, Ly, tx.lo + qx, ty.lo + qy);
+    const double2 a = tx.c[qx], b = ty.c[qy];
+    tcoef[q] = make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 x = make_double2(0.0, 0.0);
+    if (coef) {
+      double vr = 0.0, vi = 0.0;
+      for (int q = 0; q < nt; ++q) {
+        const double2 c = tcoef[q], v = g[trow[q]];
+        vr += c.x * v.x - c.y * v.y;
+        vi += c.x * v.y + c.y * v.x;
+      }
+      const double s = coef[4];
+      x = make_double2(s * (coef[0] * vr + (i == j ? coef[1] : 0.0)), s * coef[0] * vi);
+    }
+    xs = x;
+  }
+  __syncthreads();
+  const double2 x = xs;
+  const double sn = coefn ? coefn[4] : 0.0;
+  double ar = 0.0, ai = 0.0;
+  cplx* o = out + (long long)i * ld;
+  for (int k = threadIdx.x; k < N; k += 256) {
+    const double2 yk = coef ? y[k] : make_double2(0.0, 0.0);
+    double re = x.x * yk.x - x.y * yk.y, im = x.x * yk.y + x.y * yk.x;
+    for (int q = 0; q < nt; ++q) {
+      const double2 c = tcoef[q];
+      const double2 u = U[(long long)trow[q] * ld + k];
+      re += c.x * u.x - c.y * u.y;
+      im += c.x * u.y + c.y * u.x;
+    }
+    o[k] = make_double2(re, im);
+    if (yn) {
+      const double2 b = yn[k];
+      ar += re * b.x + im * b.y;
+      ai += im * b.x - re * b.y;
+    }
+  }
+  if (!yn) return;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    ar += __shfl_xor_sync(0xffffffffu, ar, off);
+    ai += __shfl_xor_sync(0xffffffffu, ai, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[2 * (threadIdx.x >> 5)] = ar;
+    red[2 * (threadIdx.x >> 5) + 1] = ai;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      a += red[2 * w];
+      b += red[2 * w + 1];
+    }
+    gn[i] = make_double2(sn * a, sn * b);
+  }
+}
+
+template <int W>
+cudaError_t launch_pass_1d(cudaStream_t st, const cplx* U, cplx* out, long long ld, int N, int L,
+                           const cplx* taps_host, int w, const cplx* y, const double* coef, const double2* g, int j,
+                           const cplx* yn, const double* coefn, double2* gn) {
+  constexpr int R = W <= 4 ? 8 : 4;
+  EvTaps<W> t;
+  for (int d = 0; d < 2 * W + 1; ++d) t.c[d][0] = t.c[d][1] = t.c[d][2] = 0.0;
+  for (int d = 0; d < 2 * w + 1; ++d) {
+    t.c[W - w + d][0] = taps_host[d].x;
+    t.c[W - w + d][1] = taps_host[d].y;
+    t.c[W - w + d][2] = -taps_host[d].y;
+  }
+  ev_pass_1d_kernel<W, R><<<(unsigned)ceil_div(L, R), 256, 0, st>>>(U, out, ld, N, L, t, y, coef, g, j, yn, coefn, gn);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int ev_prep(cudaStream_t st, const cplx* U, long long ld, int N, int Lx, int Ly, int j, const cplx* cxc, int cxlo,
+            int cxn, const cplx* cyc, int cylo, int cyn, const cplx* oxc, int oxlo, int oxn, const cplx* oyc, int oylo,
+            int oyn, const cplx* ixc, int ixlo, int ixn, const cplx* iyc, int iylo, int iyn, const double* coef_prev,
+            const double2* g_prev, const cplx* y_prev, int j_prev, double pc, cplx* y_out, double* part,
+            double* coef_out, int32_t* occ_count, std::string* err) {
+  const int nb = (int)std::min<long long>(ceil_div(N, EVP_THREADS), 64);
+  ev_prep_kernel<<<nb, EVP_THREADS, 0, st>>>(U, ld, N, Lx, Ly, j, DevTaps{cxc, cxlo, cxn}, DevTaps{cyc, cylo, cyn},
+                                             DevTaps{oxc, oxlo, oxn}, DevTaps{oyc, oylo, oyn},
+                                             DevTaps{ixc, ixlo, ixn}, DevTaps{iyc, iylo, iyn}, coef_prev, g_prev,
+                                             y_prev, j_prev, y_out, part);
+  ev_decide_kernel<<<1, 32, 0, st>>>(part, nb, pc, coef_out, occ_count);
+  count_launch(2);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && err) *err = std::string("ev_prep: ") + cudaGetErrorString(e);
+  return e == cudaSuccess ? 0 : 4;
+}
+
+int ev_gemv(cudaStream_t st, const cplx* U, long long ld, int N, int L, const cplx* y, const double* coef, double2* g,
+            std::string* err) {
+  ev_gemv_kernel<<<(unsigned)ceil_div(L, 8), 256, 0, st>>>(U, ld, N, L, y, coef, g);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && err) *err = std::string("ev_gemv: ") + cudaGetErrorString(e);
+  return e == cudaSuccess ? 0 : 4;
+}
+
+int ev_pass(cudaStream_t st, const cplx* U, cplx* out, long long ld, int N, int Lx, int Ly, const cplx* cx_dev,
+            const cplx* cx_host, int xlo, int xn, const cplx* cy_dev, int ylo, int yn_taps, const cplx* y,
+            const double* coef, const double2* g, int j, const cplx* yn, const double* coefn, double2* gn,
+            std::string* err) {
+  const int w = (xn - 1) / 2;
+  cudaError_t e;
+  if (Ly == 1 && xlo == -w && w <= 9 && xn + 16 <= Lx && cx_host) {
+    if (w <= 2)
+      e = launch_pass_1d<2>(st, U, out, ld, N, Lx, cx_host, w, y, coef, g, j, yn, coefn, gn);
+    else if (w <= 4)
+      e = launch_pass_1d<4>(st, U, out, ld, N, Lx, cx_host, w, y, coef, g, j, yn, coefn, gn);
+    else if (w <= 6)
+      e = launch_pass_1d<6>(st, U, out, ld, N, Lx, cx_host, w, y, coef, g, j, yn, coefn, gn);
+    else
+      e = launch_pass_1d<9>(st, U, out, ld, N, Lx, cx_host, w, y, coef, g, j, yn, coefn, gn);
+  } else {
+    if (xn * yn_taps > EVG_MAXTAPS) {
+      if (err) *err = "ev_pass: more than 1024 taps";
+      return 1;
+    }
+    ev_pass_generic_kernel<<<Lx * Ly, 256, 0, st>>>(U, out, ld, N, Lx, Ly, DevTaps{cx_dev, xlo, xn},
+                                                    DevTaps{cy_dev, ylo, yn_taps}, y, coef, g, j, yn, coefn, gn);
+    e = cudaGetLastError();
+  }
+  count_launch();
+  if (e != cudaSuccess && err) *err = std::string("ev_pass: ") + cudaGetErrorString(e);
   return e == cudaSuccess ? 0 : 4;
 }
 

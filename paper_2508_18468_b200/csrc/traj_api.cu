@@ -44,6 +44,11 @@ struct traj_ctx {
   std::vector<double> ev_tnext, ev_tcur;
   cplx* yhat = nullptr;
   double* ev_coef = nullptr;
+  cplx* ev_y2 = nullptr;           // one-pass events: [2][N] unnormalised yhat
+  double* ev_c2 = nullptr;         // [2][8] coef
+  double2* ev_g2 = nullptr;        // [2][L] g = U yhat^dag
+  double* ev_part = nullptr;       // [64] prep partials
+  bool ev_onepass = true;          // TRAJ_EVENTS_ONEPASS=0: two-pass event updates
   int32_t* occ_count = nullptr;
   cplx* taps_dev = nullptr;
   std::complex<double>* taps_host = nullptr;   // pinned staging
@@ -238,6 +243,10 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     h->banded = false;
     lay.take(h->yhat, (size_t)N * 16);
     lay.take(h->ev_coef, 64);
+    lay.take(h->ev_y2, (size_t)2 * N * 16);
+    lay.take(h->ev_c2, 2 * 8 * 8);
+    lay.take(h->ev_g2, (size_t)2 * L * 16);
+    lay.take(h->ev_part, 64 * 8);
     lay.take(h->occ_count, (size_t)T * 4);
     lay.take(h->taps_dev, (size_t)EV_TAPCAP * 16);
   } else if (h->banded) {
@@ -610,6 +619,9 @@ struct EvPass {
   double pc;
   long long off;    // taps offset in the staged buffer
   AxisTaps x, y;
+  double tau = 0.0;
+  long long offc = 0;   // one-pass: taps of tau_prev + tau (the prep stencil)
+  AxisTaps cx, cy;
 };
 
 int event_window(traj_ctx* h) {
@@ -681,6 +693,123 @@ int event_window(traj_ctx* h) {
   return 0;
 }
 
+// NEXT-4, one-pass form (pm_events.cu): per event one read and one write of U.  Events come first
+// in a window, then one or two propagation-only passes; yhat / coef / g are double-buffered by
+// event parity.  The first event of a window is prepared from U and its g = U yhat^dag taken by
+// a GEMV; every later event q+1 is prepared before pass q (row j' of K(tau_q + tau_q+1) U plus the
+// rank-1 term's scalar), and pass q accumulates its g.
+int event_window_onepass(traj_ctx* h) {
+  const double t_end = (h->step + 1) * h->cfg.dt;
+  CK(cudaMemsetAsync(h->occ_count, 0, (size_t)h->T * 4, h->st));
+  const long long N = h->N;
+  for (int t = 0; t < h->T; ++t) {
+    std::vector<EvPass> passes;
+    auto taps = [&](double tau, AxisTaps& x, AxisTaps& y) {
+      x = axis_taps(h->Lx, h->cfg.J, tau);
+      if (h->Ly > 1) y = axis_taps(h->Ly, h->cfg.J, tau);
+    };
+    while (h->ev_tnext[t] < t_end) {
+      EvPass p;
+      double u_site, u_pc;
+      event_uniforms_host(h, t, h->ev_count[t], nullptr, &u_site, &u_pc);
+      p.j = std::min((int)(u_site * h->L), h->L - 1);
+      p.pc = u_pc;
+      p.tau = h->ev_tnext[t] - h->ev_tcur[t];
+      taps(p.tau, p.x, p.y);
+      passes.push_back(p);
+      h->ev_tcur[t] = h->ev_tnext[t];
+      h->ev_count[t] += 1;
+      h->ev_tnext[t] = h->ev_tcur[t] + event_wait(h, t, h->ev_count[t]);
+    }
+    const double rest = t_end - h->ev_tcur[t];
+    h->ev_tcur[t] = t_end;
+    const int nend = (passes.size() + 1) % 2 == 1 ? 1 : 2;
+    for (int q = 0; q < nend; ++q) {
+      EvPass p;
+      p.j = -1;
+      p.pc = 0;
+      p.tau = rest / nend;
+      taps(p.tau, p.x, p.y);
+      passes.push_back(p);
+    }
+    h->last_nS[t] = (int64_t)passes.size() - nend;
+    for (size_t q = 1; q < passes.size(); ++q)
+      if (passes[q].j >= 0) taps(passes[q - 1].tau + passes[q].tau, passes[q].cx, passes[q].cy);
+    long long used = 0;
+    size_t first = 0;
+    int cur = 0;
+    cplx* src = h->U[h->cur] + t * h->sU;
+    cplx* dst = h->U[1 - h->cur] + t * h->sU;
+    cplx* Y[2] = {h->ev_y2, h->ev_y2 + N};
+    double* C[2] = {h->ev_c2, h->ev_c2 + 8};
+    double2* G[2] = {h->ev_g2, h->ev_g2 + h->L};
+    auto flush = [&](size_t upto) -> int {
+      if (used) CK(cudaMemcpyAsync(h->taps_dev, h->taps_host, (size_t)used * 16, cudaMemcpyHostToDevice, h->st));
+      for (size_t q = first; q < upto; ++q) {
+        EvPass& p = passes[q];
+        const cplx* cx = h->taps_dev + p.off;
+        const cplx* cy = cx + p.x.n;
+        const bool ev = p.j >= 0;
+        if (ev && q == 0) {
+          TRY(ev_prep(h->st, src, h->ldN, h->N, h->Lx, h->Ly, p.j, cx, p.x.lo, p.x.n, cy, p.y.lo, p.y.n, nullptr, 0, 0,
+                      nullptr, 0, 0, nullptr, 0, 0, nullptr, 0, 0, nullptr, nullptr, nullptr, -1, p.pc, Y[cur],
+                      h->ev_part, C[cur], h->occ_count + t, &h->err));
+          TRY(ev_gemv(h->st, src, h->ldN, h->N, h->L, Y[cur], C[cur], G[cur], &h->err));
+        }
+        const bool next_ev = ev && q + 1 < passes.size() && passes[q + 1].j >= 0;
+        if (next_ev) {
+          EvPass& pn = passes[q + 1];
+          const cplx* ncx = h->taps_dev + pn.off;
+          const cplx* ncy = ncx + pn.x.n;
+          const cplx* ccx = h->taps_dev + pn.offc;
+          const cplx* ccy = ccx + pn.cx.n;
+          TRY(ev_prep(h->st, src, h->ldN, h->N, h->Lx, h->Ly, pn.j, ccx, pn.cx.lo, pn.cx.n, ccy, pn.cy.lo, pn.cy.n, ncx,
+                      pn.x.lo, pn.x.n, ncy, pn.y.lo, pn.y.n, cx, p.x.lo, p.x.n, cy, p.y.lo, p.y.n, C[cur], G[cur],
+                      Y[cur], p.j, pn.pc, Y[1 - cur], h->ev_part, C[1 - cur], h->occ_count + t, &h->err));
+        }
+        TRY(ev_pass(h->st, src, dst, h->ldN, h->N, h->Lx, h->Ly, cx, reinterpret_cast<const cplx*>(p.x.c.data()),
+                    p.x.lo, p.x.n, cy, p.y.lo, p.y.n, ev ? Y[cur] : nullptr, ev ? C[cur] : nullptr, G[cur], p.j,
+                    next_ev ? Y[1 - cur] : nullptr, next_ev ? C[1 - cur] : nullptr, G[1 - cur], &h->err));
+        std::swap(src, dst);
+        if (ev) cur = 1 - cur;
+      }
+      CK(cudaStreamSynchronize(h->st));    // the staging buffer is reused
+      used = 0;
+      first = upto;
+      return 0;
+    };
+    // pass q needs its own taps and, when pass q+1 is an event, that pass's own and combined taps
+    // in the same staged buffer: both are (re)staged after a flush
+    int gen = 0;
+    std::vector<int> sgen(passes.size(), -1);
+    auto need_of = [&](size_t i) -> long long {
+      return passes[i].x.n + passes[i].y.n + passes[i].cx.n + passes[i].cy.n;
+    };
+    auto stage = [&](size_t i) {
+      EvPass& p = passes[i];
+      p.off = used;
+      for (int r = 0; r < p.x.n; ++r) h->taps_host[used++] = p.x.c[r];
+      for (int r = 0; r < p.y.n; ++r) h->taps_host[used++] = p.y.c[r];
+      p.offc = used;
+      for (int r = 0; r < p.cx.n; ++r) h->taps_host[used++] = p.cx.c[r];
+      for (int r = 0; r < p.cy.n; ++r) h->taps_host[used++] = p.cy.c[r];
+      sgen[i] = gen;
+    };
+    for (size_t q = 0; q < passes.size(); ++q) {
+      const bool nx = passes[q].j >= 0 && q + 1 < passes.size() && passes[q + 1].j >= 0;
+      const long long need = (sgen[q] == gen ? 0 : need_of(q)) + (nx && sgen[q + 1] != gen ? need_of(q + 1) : 0);
+      if (used + need > EV_TAPCAP) {
+        TRY(flush(q));
+        ++gen;
+      }
+      if (sgen[q] != gen) stage(q);
+      if (nx && sgen[q + 1] != gen) stage(q + 1);
+    }
+    TRY(flush(passes.size()));
+  }
+  return 0;
+}
+
 int one_step(traj_ctx* h) {
   cplx* Uc = h->U[h->cur];
   cplx* Un = h->U[1 - h->cur];
@@ -688,7 +817,7 @@ int one_step(traj_ctx* h) {
   if (h->cfg.protocol == TRAJ_PROJECTIVE_EVENTS) {
     {
       Phase p(&h->prof, h->st, TRAJ_PH_PROJECT);
-      int s = event_window(h);
+      int s = h->ev_onepass ? event_window_onepass(h) : event_window(h);
       if (s) return s;
     }
     // the per-event updates are exact rank-1 maps of an orthonormal U: with the low-rank
@@ -1011,6 +1140,8 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
                       (cfg->protocol == TRAJ_PROJECTIVE || cfg->protocol == TRAJ_PROJECTIVE_EVENTS);
     const char* rf = getenv("TRAJ_LOWRANK_REFINE");
     h->lowrank_refine = !(rf && rf[0] == '0');
+    const char* op = getenv("TRAJ_EVENTS_ONEPASS");
+    h->ev_onepass = !(op && op[0] == '0');
     const char* tl = getenv("TRAJ_LOWRANK_TOL");
     if (tl) h->lowrank_tol = atof(tl);
   }
