@@ -361,7 +361,7 @@ struct EvTaps {
   double c[2 * W + 1][3];
 };
 
-// 1d ring: EV_R (8 for W <= 4, else 4: registers) consecutive rows per CTA, each input row loaded once per column into a register
+// 1d ring: EV_R (8 for W <= 6, else 4: registers) consecutive rows per CTA, each input row loaded once per column into a register
 // window.  out_i = sum_d c_d U_{i+d} + x_i yhat (x_i from g), gn_i = <out_i, yhat_next>.
 template <int W, int EV_R>
 __global__ void __launch_bounds__(256) ev_pass_1d_kernel(const cplx* __restrict__ U, cplx* __restrict__ out,
@@ -535,7 +535,7 @@ template <int W>
 cudaError_t launch_pass_1d(cudaStream_t st, const cplx* U, cplx* out, long long ld, int N, int L,
                            const cplx* taps_host, int w, const cplx* y, const double* coef, const double2* g, int j,
                            const cplx* yn, const double* coefn, double2* gn) {
-  constexpr int R = W <= 4 ? 8 : 4;
+  constexpr int R = W <= 6 ? 8 : 4;
   EvTaps<W> t;
   for (int d = 0; d < 2 * W + 1; ++d) t.c[d][0] = t.c[d][1] = t.c[d][2] = 0.0;
   for (int d = 0; d < 2 * w + 1; ++d) {
