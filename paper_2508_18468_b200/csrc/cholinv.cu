@@ -12,6 +12,10 @@
 // the 64 x 64 diagonal leaves run in a small shared-memory kernel.  R_B^dag is kept in
 // G's (unused) strict lower triangle, so the only scratch is the h x (n-h) product.
 #include <math.h>
+
+#include <algorithm>
+#include <vector>
+
 #include "common.cuh"
 #include "zgemm.h"
 #include "cholinv.h"
@@ -128,7 +132,40 @@ struct Ctx {
   long long ldt, sT;
   int32_t* failed;
   std::string* err;
+  const CholDist* dist;
 };
+
+// row slice boundaries of M rows over P ranks, 128-aligned; tri: equal area of an upper triangle
+std::vector<long long> slices(long long M, int P, bool tri) {
+  std::vector<long long> b(P + 1, 0);
+  for (int i = 1; i < P; ++i) {
+    const double f = (double)i / P;
+    const double x = tri ? M * (1.0 - sqrt(1.0 - f)) : M * f;
+    b[i] = std::min(M, std::max(b[i - 1], (long long)(x / 128.0 + 0.5) * 128));
+  }
+  b[P] = M;
+  return b;
+}
+
+// C rows [0, M) of op(A) op(B) split over the ranks (see CholDist); A's rows (opA = 0) or columns
+// (opA = 1) follow the slice
+int dist_gemm(Ctx& c, bool tri_c, int opA, int opB, long long M, long long N, long long K, double alpha,
+              const cplx* A, long long lda, const cplx* B, long long ldb, double beta, cplx* C, long long ldc,
+              int flags) {
+  const CholDist* d = c.dist;
+  const std::vector<long long> b = slices(M, d->P, tri_c);
+  for (int i = 0; i < d->P; ++i) {
+    if (d->rank >= 0 && d->rank != i) continue;
+    const long long m = b[i + 1] - b[i];
+    if (m <= 0) continue;
+    const cplx* Ai = opA == 0 ? A + b[i] * lda : A + b[i];
+    int s = zgemm(c.st, opA, opB, m, N, K, alpha, 0.0, Ai, lda, 0, B, ldb, 0, beta, C + b[i] * ldc, ldc, 0, 1, flags,
+                  c.err, b[i], 0);
+    if (s) return s;
+  }
+  if (d->rank < 0) return 0;
+  return d->share_rows(d->user, C, ldc, N, b.data(), d->P, c.st, c.err);
+}
 
 int rec(Ctx& c, long long o, long long n) {
   if (n <= NB) {
@@ -153,6 +190,19 @@ int rec(Ctx& c, long long o, long long n) {
   cplx* XC = c.X + (o + h) * c.ldx + (o + h);
   int s;
   if ((s = rec(c, o, h))) return s;
+  if (c.dist && c.dist->P > 1 && n >= c.dist->min_n && c.batch == 1) {
+    // the same four products, each split into row slices over the ranks
+    if ((s = dist_gemm(c, false, 1, 0, r, h, h, 1.0, B_blk, c.ldg, XA, c.ldx, 0.0, L_blk, c.ldg, TRAJ_TRI_B_UPPER_F)))
+      return s;
+    if ((s = dist_gemm(c, true, 0, 1, r, r, h, -1.0, L_blk, c.ldg, L_blk, c.ldg, 1.0, C_blk, c.ldg, TRAJ_C_UPPER_F)))
+      return s;
+    if ((s = rec(c, o + h, r))) return s;
+    if ((s = dist_gemm(c, false, 1, 0, h, r, r, 1.0, L_blk, c.ldg, XC, c.ldx, 0.0, c.tmp, c.ldt, TRAJ_TRI_B_UPPER_F)))
+      return s;
+    if ((s = dist_gemm(c, false, 0, 0, h, r, h, -1.0, XA, c.ldx, c.tmp, c.ldt, 0.0, XB, c.ldx, TRAJ_TRI_A_UPPER_F)))
+      return s;
+    return 0;
+  }
   // R_B^dag = B^dag X_A : (r x h) = op_C(B: h x r) * X_A (h x h, upper)
   if ((s = zgemm(c.st, 1, 0, r, h, h, 1.0, 0.0, B_blk, c.ldg, c.sG, XA, c.ldx, c.sX, 0.0, L_blk, c.ldg, c.sG, c.batch,
                  TRAJ_TRI_B_UPPER_F, c.err)))
@@ -182,7 +232,8 @@ size_t chol_scratch_bytes(long long n, long long batch) {
 }
 
 int chol_inverse(cudaStream_t st, long long n, cplx* G, long long ldg, long long sG, cplx* X, long long ldx,
-                 long long sX, long long batch, void* scratch, int32_t* failed, std::string* err) {
+                 long long sX, long long batch, void* scratch, int32_t* failed, std::string* err,
+                 const CholDist* dist) {
   if (n <= 0 || batch <= 0) return 0;
   if (batch > 65535) {
     if (err) *err = "chol_inverse: batch too large";
@@ -202,6 +253,7 @@ int chol_inverse(cudaStream_t st, long long n, cplx* G, long long ldg, long long
   c.sT = n <= NB ? 0 : split(n) * c.ldt;
   c.failed = failed;
   c.err = err;
+  c.dist = dist;
   if (n > NB) {
     // the strict lower triangle of X must read as zeros (triangular GEMM tiles cross it)
     cudaError_t e = cudaSuccess;

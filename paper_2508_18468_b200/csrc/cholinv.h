@@ -7,10 +7,27 @@ namespace traj {
 
 size_t chol_scratch_bytes(long long n, long long batch);
 
+// Distribution of the large recursion levels over the P ranks of a row-sharded trajectory (SURVEY
+// §8(e): the replicated N x N factorisation bounds the sharded speed-up).  At every level with
+// n >= min_n the four GEMMs are split into P row slices (128-row aligned; equal triangle area for
+// the Hermitian update): rank r computes slice r, then share_rows() makes every slice visible on
+// every rank.  rank < 0: a single-process emulation that computes every slice itself (share_rows
+// is not called).  Only batch == 1.
+struct CholDist {
+  int P = 1, rank = 0;
+  long long min_n = 2048;
+  void* user = nullptr;
+  // the block of ncols columns at base (row-major, leading dimension ld): rows [bounds[i],
+  // bounds[i+1]) were computed by rank i
+  int (*share_rows)(void* user, cplx* base, long long ld, long long ncols, const long long* bounds, int P,
+                    cudaStream_t st, std::string* err) = nullptr;
+};
+
 // G_b = R^dag R (upper triangle of G_b read; strict lower triangle used as scratch),
 // X_b = R^-1 (upper; strict lower set to zero).  failed[b] = 1 on a non-positive or
 // non-finite pivot.
 int chol_inverse(cudaStream_t st, long long n, cplx* G, long long ldg, long long sG, cplx* X, long long ldx,
-                 long long sX, long long batch, void* scratch, int32_t* failed, std::string* err);
+                 long long sX, long long batch, void* scratch, int32_t* failed, std::string* err,
+                 const CholDist* dist = nullptr);
 
 }  // namespace traj

@@ -236,6 +236,11 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
     }
   }
   if (banded) lay.take(sh->bcoef, (size_t)(2 * Wx + 2 * Wy + 2) * 16);
+  if (c->nccl_id && sh->P > 1) {   // distributed Cholesky: the largest shared block, (N/2 + 128)^2
+    const long long hb = (long long)sh->N / 2 + 128;
+    sh->dist_scratch_bytes = (size_t)(hb * hb * 16);
+    lay.take(sh->dist_scratch, sh->dist_scratch_bytes);
+  }
   lay.take(sh->gamma_dev, 16);
   lay.take(sh->failed_dev, 16);
   lay.take(sh->eig_w, (size_t)N * 8);
@@ -278,6 +283,45 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
   return lay.off + 256;
 }
 
+namespace {
+
+// make the row slices of a (ld-strided, ncols-wide) block computed by each rank visible everywhere:
+// the owner packs its slice into the contiguous scratch, one grouped broadcast per owner, every
+// other rank unpacks (only the block's columns travel)
+int dist_share_rows(void* user, cplx* base, long long ld, long long ncols, const long long* bounds, int P,
+                    cudaStream_t st, std::string* err) {
+  ShardedCtx* sh = reinterpret_cast<ShardedCtx*>(user);
+  const int me = sh->cdist.rank;
+  cplx* scr = sh->dist_scratch;
+  if ((bounds[P]) * ncols * 16 > (long long)sh->dist_scratch_bytes) {
+    if (err) *err = "distributed Cholesky: share scratch too small";
+    return TRAJ_ECUDA;
+  }
+  const size_t w = (size_t)ncols * 16;
+  if (bounds[me + 1] > bounds[me])
+    SCK(cudaMemcpy2DAsync(scr + bounds[me] * ncols, w, base + bounds[me] * ld, (size_t)ld * 16, w,
+                          (size_t)(bounds[me + 1] - bounds[me]), cudaMemcpyDeviceToDevice, st));
+  ncclGroupStart();
+  for (int i = 0; i < P; ++i) {
+    if (bounds[i + 1] <= bounds[i]) continue;
+    cplx* p = scr + bounds[i] * ncols;
+    ncclBroadcast(p, p, (size_t)(bounds[i + 1] - bounds[i]) * w, ncclUint8, i, sh->comm.comm, st);
+  }
+  ncclResult_t r = ncclGroupEnd();
+  if (r != ncclSuccess) {
+    if (err) *err = std::string("ncclBroadcast (distributed Cholesky): ") + ncclGetErrorString(r);
+    return TRAJ_ENCCL;
+  }
+  for (int i = 0; i < P; ++i) {
+    if (i == me || bounds[i + 1] <= bounds[i]) continue;
+    SCK(cudaMemcpy2DAsync(base + bounds[i] * ld, (size_t)ld * 16, scr + bounds[i] * ncols, w, w,
+                          (size_t)(bounds[i + 1] - bounds[i]), cudaMemcpyDeviceToDevice, st));
+  }
+  return 0;
+}
+
+}  // namespace
+
 int shard_init(ShardedCtx* sh, const traj_config* c, std::string* err) {
   sh->protocol = c->protocol;
   sh->dt = c->dt;
@@ -297,6 +341,15 @@ int shard_init(ShardedCtx* sh, const traj_config* c, std::string* err) {
   }
   SCK(cudaMallocHost(&sh->h_small, std::max(sh->P + 8, 64) * 4));
   SCK(cudaMallocHost(&sh->h_dev, 64 * 8));
+  {
+    const char* dm = getenv("TRAJ_DIST_CHOL_MIN");
+    const long long mn = dm ? atoll(dm) : 2048;
+    sh->cdist.P = mn > 0 ? sh->P : 1;
+    sh->cdist.rank = sh->comm.comm ? c->shard_rank : -1;
+    sh->cdist.min_n = mn > 0 ? mn : (1ll << 40);
+    sh->cdist.user = sh;
+    sh->cdist.share_rows = dist_share_rows;
+  }
   const char* ov = getenv("TRAJ_SHARD_OVERLAP");
   sh->overlap = !(ov && ov[0] == '0');
   if (sh->comm.comm && sh->overlap && sh->P > 1) {
@@ -366,7 +419,7 @@ int cqr2(ShardedCtx* sh, int src_which, std::string* err) {
       }
       if (full)
         STRY(chol_inverse(sh->st, sh->N, sh->G, sh->ldN, 0, sh->X, sh->ldN, 0, 1, sh->chol_scratch, sh->failed_dev,
-                          err));
+                          err, &sh->cdist));
       else
         STRY(first_order_inverse(sh->st, sh->G, sh->ldN, 0, sh->X, sh->ldN, 0, sh->N, 1, err));
     }

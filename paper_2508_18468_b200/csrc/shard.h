@@ -7,6 +7,7 @@
 #include "../../include/traj.h"
 #include "common.cuh"
 #include "profiler.h"
+#include "cholinv.h"
 
 typedef struct ncclComm* ncclComm_t;
 typedef struct cusolverDnContext* cusolverDnHandle_t;
@@ -81,6 +82,9 @@ struct ShardedCtx {
   // dense propagate with the allgather overlapped (NCCL mode): per-distance send/recv on cst,
   // chunk d of K_g U_full on st waits only for ev_chunk[d]
   bool overlap = true;
+  CholDist cdist;          // the N x N Cholesky's large levels split over the ranks
+  cplx* dist_scratch = nullptr;
+  size_t dist_scratch_bytes = 0;
   cudaStream_t cst = nullptr;
   cudaEvent_t ev_start = nullptr;
   std::vector<cudaEvent_t> ev_chunk;

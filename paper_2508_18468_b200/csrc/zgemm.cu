@@ -56,6 +56,7 @@ struct Args {
   double alpha_re, alpha_im, beta;
   cplx* C;
   long long ldc, strideC;
+  int m_off, n_off;        // global row / column of this call's (0, 0): triangle and upper-tile tests
 };
 
 // byte offset of complex element (r, k) in a k-contiguous tile: line r, chunk k (swizzled)
@@ -84,13 +85,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int pid_n = (t % group) / gm;
   const int m0 = pid_m * BM, n0 = pid_n * BN;
   const int z = blockIdx.z;
-  if ((args.flags & TRAJ_C_UPPER_F) && m0 > n0 + BN - 1) return;   // tile entirely below the diagonal
+  if ((args.flags & TRAJ_C_UPPER_F) && m0 + args.m_off > n0 + args.n_off + BN - 1) return;   // tile entirely below the diagonal
 
   int kb = 0, ke = args.K;
-  if (args.flags & TRAJ_TRI_A_UPPER_F) kb = max(kb, m0);
-  if (args.flags & TRAJ_TRI_A_LOWER_F) ke = min(ke, m0 + BM);
-  if (args.flags & TRAJ_TRI_B_UPPER_F) ke = min(ke, n0 + BN);
-  if (args.flags & TRAJ_TRI_B_LOWER_F) kb = max(kb, n0);
+  if (args.flags & TRAJ_TRI_A_UPPER_F) kb = max(kb, m0 + args.m_off);
+  if (args.flags & TRAJ_TRI_A_LOWER_F) ke = min(ke, m0 + args.m_off + BM);
+  if (args.flags & TRAJ_TRI_B_UPPER_F) ke = min(ke, n0 + args.n_off + BN);
+  if (args.flags & TRAJ_TRI_B_LOWER_F) kb = max(kb, n0 + args.n_off);
   const int nk = ke > kb ? (ke - kb + BKC - 1) / BKC : 0;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = n0 + warp_n * 32 + 8 * j + 2 * slot + e;
-        if (col >= args.N || (upper && row > col)) continue;
+        if (col >= args.N || (upper && row + args.m_off > col + args.n_off)) continue;
         const double vr = acc[i][j][0][e], vi = acc[i][j][1][e];
         double2 out;
         out.x = args.alpha_re * vr - args.alpha_im * vi;
@@ -277,12 +278,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int pid_n = (t % group) / gm;
   const int m0 = pid_m * BM3, n0 = pid_n * BN3;
   const int z = blockIdx.z;
-  if ((args.flags & TRAJ_C_UPPER_F) && m0 > n0 + BN3 - 1) return;
+  if ((args.flags & TRAJ_C_UPPER_F) && m0 + args.m_off > n0 + args.n_off + BN3 - 1) return;
   int kb = 0, ke = args.K;
-  if (args.flags & TRAJ_TRI_A_UPPER_F) kb = max(kb, m0);
-  if (args.flags & TRAJ_TRI_A_LOWER_F) ke = min(ke, m0 + BM3);
-  if (args.flags & TRAJ_TRI_B_UPPER_F) ke = min(ke, n0 + BN3);
-  if (args.flags & TRAJ_TRI_B_LOWER_F) kb = max(kb, n0);
+  if (args.flags & TRAJ_TRI_A_UPPER_F) kb = max(kb, m0 + args.m_off);
+  if (args.flags & TRAJ_TRI_A_LOWER_F) ke = min(ke, m0 + args.m_off + BM3);
+  if (args.flags & TRAJ_TRI_B_UPPER_F) ke = min(ke, n0 + args.n_off + BN3);
+  if (args.flags & TRAJ_TRI_B_LOWER_F) kb = max(kb, n0 + args.n_off);
   const int nk = ke > kb ? (ke - kb + KS - 1) / KS : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -420,7 +421,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = n0 + warp_n * 16 + 8 * j + 2 * slot + e;
-        if (col >= args.N || (upper && row > col)) continue;
+        if (col >= args.N || (upper && row + args.m_off > col + args.n_off)) continue;
         const double p1 = acc[i][j][0][e], p2 = acc[i][j][1][e], p3 = acc[i][j][2][e];
         const double vr = p1 - p2, vi = p3 - p1 - p2;
         double2 out;
@@ -465,12 +466,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int pid_n = (t % group) / gm;
   const int m0 = pid_m * BM3, n0 = pid_n * BN3;
   const int z = blockIdx.z;
-  if ((args.flags & TRAJ_C_UPPER_F) && m0 > n0 + BN3 - 1) return;
+  if ((args.flags & TRAJ_C_UPPER_F) && m0 + args.m_off > n0 + args.n_off + BN3 - 1) return;
   int kb = 0, ke = args.K;
-  if (args.flags & TRAJ_TRI_A_UPPER_F) kb = max(kb, m0);
-  if (args.flags & TRAJ_TRI_A_LOWER_F) ke = min(ke, m0 + BM3);
-  if (args.flags & TRAJ_TRI_B_UPPER_F) ke = min(ke, n0 + BN3);
-  if (args.flags & TRAJ_TRI_B_LOWER_F) kb = max(kb, n0);
+  if (args.flags & TRAJ_TRI_A_UPPER_F) kb = max(kb, m0 + args.m_off);
+  if (args.flags & TRAJ_TRI_A_LOWER_F) ke = min(ke, m0 + args.m_off + BM3);
+  if (args.flags & TRAJ_TRI_B_UPPER_F) ke = min(ke, n0 + args.n_off + BN3);
+  if (args.flags & TRAJ_TRI_B_LOWER_F) kb = max(kb, n0 + args.n_off);
   const int nk = ke > kb ? (ke - kb + KS - 1) / KS : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -604,7 +605,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = n0 + warp_n * 32 + 8 * j + 2 * slot + e;
-        if (col >= args.N || (upper && row > col)) continue;
+        if (col >= args.N || (upper && row + args.m_off > col + args.n_off)) continue;
         const double p1 = acc[i][j][0][e], p2 = acc[i][j][1][e], p3 = acc[i][j][2][e];
         const double vr = p1 - p2, vi = p3 - p1 - p2;
         double2 out;
@@ -739,7 +740,7 @@ void set_zgemm_algorithm(int algo) { g_algo.store(algo ? 1 : 0); }
 int zgemm(cudaStream_t st, int opA, int opB, long long M, long long N, long long K, double alpha_re,
           double alpha_im, const cplx* A, long long lda, long long strideA, const cplx* B, long long ldb,
           long long strideB, double beta, cplx* C, long long ldc, long long strideC, long long batch, int flags,
-          std::string* err) {
+          std::string* err, long long m_off, long long n_off) {
   if (M <= 0 || N <= 0 || batch <= 0) return 0;
   if (M > (1ll << 30) || N > (1ll << 30) || K > (1ll << 30) || batch > 65535) {
     if (err) *err = "zgemm: dimension too large";
@@ -788,6 +789,8 @@ int zgemm(cudaStream_t st, int opA, int opB, long long M, long long N, long long
   args.C = C;
   args.ldc = ldc;
   args.strideC = strideC;
+  args.m_off = (int)m_off;
+  args.n_off = (int)n_off;
   cudaError_t e;
   if (algo == 2) {
     if (opA == 0 && opB == 0) e = launch3mw<false, false>(st, ma, mb, args, (int)batch);

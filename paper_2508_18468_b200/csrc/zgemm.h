@@ -17,7 +17,7 @@ enum {
 int zgemm(cudaStream_t st, int opA, int opB, long long M, long long N, long long K, double alpha_re,
           double alpha_im, const cplx* A, long long lda, long long strideA, const cplx* B, long long ldb,
           long long strideB, double beta, cplx* C, long long ldc, long long strideC, long long batch, int flags,
-          std::string* err);
+          std::string* err, long long m_off = 0, long long n_off = 0);
 
 // 0: 4M (two real MMAs over an interleaved k axis, default); 1: 3M (Gauss, three real MMAs).
 // Initialised from the environment (TRAJ_ZGEMM_3M=1); process-wide.

@@ -283,6 +283,33 @@ def test_row_sharded_chunked_propagate_matches_single_gemm(P, P_shards, monkeypa
     b.close()
 
 
+@pytest.mark.parametrize("P_shards", [2, 4, 8])
+def test_row_sharded_distributed_cholesky_matches_replicated(P, P_shards, monkeypatch):
+    """The N x N Cholesky of the row-sharded CholeskyQR with its recursion levels split into row
+    slices over the ranks (every level >= 64 here; the emulation computes each rank's slice in
+    turn, exercising the slice offsets of the triangular / upper-tile GEMMs; at P = 8 some slices
+    round to empty): the same state as the replicated factorisation, and the oracle's."""
+    L = 512
+    monkeypatch.setenv("TRAJ_DIST_CHOL_MIN", "0")
+    a = P.Trajectories(L, 1, "projective", [1.5], seed=33, shard_size=P_shards)
+    monkeypatch.setenv("TRAJ_DIST_CHOL_MIN", "64")
+    b = P.Trajectories(L, 1, "projective", [1.5], seed=33, shard_size=P_shards)
+    K = lattice.propagator_lattice(L, 1, 1.0, 0.05)
+    o = OracleTrajectory(L, 1, "projective", 1.5, 0.05, seed=33, traj=0, K=K)
+    for s in range(8):
+        a.step(1)
+        b.step(1)
+        o.step(1)
+        assert a.last_clicks(0) == b.last_clicks(0)
+    ca, cb = a.correlation(0).cpu().numpy(), b.correlation(0).cpu().numpy()
+    assert np.abs(ca - cb).max() < 1e-12
+    assert np.abs(cb - o.correlation()).max() < C_TOL
+    U = b.get_state(0).cpu().numpy()
+    assert np.abs(U.conj().T @ U - np.eye(L // 2)).max() < 1e-12
+    a.close()
+    b.close()
+
+
 def test_row_sharded_nccl_single_rank(P):
     """The NCCL code path of the sharded step with a one-rank communicator (the only
     configuration one GPU allows): same result as the unsharded handle."""

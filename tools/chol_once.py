@@ -1,7 +1,7 @@
 import os, sys, torch
 sys.path.insert(0, os.getcwd())
 import paper_2508_18468_b200 as P
-n = 8192
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 U = torch.randn(2 * n, n, dtype=torch.complex128, device="cuda")
 G0 = torch.empty(n, n, dtype=torch.complex128, device="cuda")
 P.traj_zgemm(1, 0, U, U, G0)
