@@ -14,13 +14,15 @@ enum {
 };
 
 // C_b = alpha op(A_b) op(B_b) + beta C_b.  Returns 0, or a traj_status with *err set.
+// m_off, n_off: the global row / column of this call's C(0, 0) when it computes a slice of a larger
+// product; only the triangle (TRI_*) and upper-tile (C_UPPER) tests use them.
 int zgemm(cudaStream_t st, int opA, int opB, long long M, long long N, long long K, double alpha_re,
           double alpha_im, const cplx* A, long long lda, long long strideA, const cplx* B, long long ldb,
           long long strideB, double beta, cplx* C, long long ldc, long long strideC, long long batch, int flags,
           std::string* err, long long m_off = 0, long long n_off = 0);
 
-// 0: 4M (two real MMAs over an interleaved k axis, default); 1: 3M (Gauss, three real MMAs).
-// Initialised from the environment (TRAJ_ZGEMM_3M=1); process-wide.
+// 0: 4M (two real MMAs over an interleaved k axis); 1: 3M (Gauss, three real MMAs; the default).
+// Initialised from the environment (TRAJ_ZGEMM_3M=0 selects 4M); process-wide.
 int zgemm_algorithm();
 void set_zgemm_algorithm(int algo);
 
