@@ -207,6 +207,7 @@ def run_ours(args):
     launches = P.traj_kernel_launches() - l0
     clk = clocks.stop()
     phases = tr.phase_times()
+    tr_clicks = [tr.last_clicks(t)[0] for t in range(tpg)] if w.protocol == "projective" else [0]
     if world > 1:
         dist.barrier()
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -228,9 +229,19 @@ def run_ours(args):
             "trmm": (4.0 * rows * w.N * w.N * tpg, f"{kn[0]} triangular: U <- U R^-1 (4 L N^2)")}
     if args.propagator == "banded":
         kern.pop("propagate")
+    lowrank_proj = args.orthonormalizer == "lowrank" and w.protocol == "projective" and not shard
+    if lowrank_proj:
+        # no N x N Gram / TRMM per step: the work is the four rank-k GEMMs of the projective phase,
+        # 16 L N (k1 + k0) flops per trajectory (U W, U -= T W^dag, U' V^dag, U' += P F V); k from
+        # the last timed step's clicks; the phase time also holds the sampler and Newton-Schulz
+        k_sum = sum(tr_clicks)
+        kern = {"project": (16.0 * w.L * w.N * k_sum,
+                            f"projective rank-k GEMMs ({kn[1].split(' ')[0].split('<')[0]} family): 16 L N (k1 + k0) "
+                            f"flops per step, k1 + k0 = {k_sum} clicks in the last timed step; phase time includes "
+                            "the blocked sampler and the Newton-Schulz iteration")}
     pipe_per_alg = 0.75 if algo == "3m" else 1.0      # DMMA flops per algorithmic 8mnk flop
     dom = max(kern, key=lambda k: phases[k][0])
-    launches_per_step = max(1.0, phases[dom][1] / args.steps)
+    launches_per_step = 1.0 if lowrank_proj else max(1.0, phases[dom][1] / args.steps)
     kern_ms = phases[dom][0] / args.steps / launches_per_step
     flops_launch = kern[dom][0]
     achieved = flops_launch / (kern_ms / 1e3) / 1e12
@@ -324,7 +335,7 @@ def run_ours(args):
         "config": dict(describe(w, tpg), parallelism=(f"row-sharded K,U over {world} GPU(s) (NCCL)" if shard
                                                       else f"trajectory-parallel dp{world}"),
                        propagator=args.propagator, orthonormalizer=args.orthonormalizer),
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+        "roofline": {"bound": "latency" if w.name == "c1" else "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                      "kernel": kern[dom][1] + ("; per shard (L/P rows) when row-sharded" if shard else ""),
                      "kernel_ms": kern_ms, "peak_source": FP64_PEAK_SOURCE,
@@ -335,7 +346,10 @@ def run_ours(args):
                                       "panels (~580 MB per wave at K = 16384, > L2), so >= ~64 GB is inherent to "
                                       "this tiling; 154 GB in 390 ms is ~0.4 TB/s, 6% of HBM, not a bound")
                      if traffic else None,
-                     "note": ("achieved counts the conventional 8mnk complex flops; the 3M (Gauss) kernels issue "
+                     "note": ("c1 is latency-bound (SURVEY §8(d)): L = 64 trajectories, ~20 small launches "
+                              "and two host syncs per step; the fraction is not a kernel-quality figure. "
+                              if w.name == "c1" else "") +
+                             ("achieved counts the conventional 8mnk complex flops; the 3M (Gauss) kernels issue "
                               "6mnk flops on the DMMA pipe, reported as pipe_tflops / pipe_frac")
                      if algo == "3m" else "4M: 8mnk flops on the DMMA pipe"},
         "library_same_shape": library,

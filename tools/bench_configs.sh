@@ -1,0 +1,14 @@
+#!/bin/bash
+# One bench line per BASELINE config at N = 1 (c3 and c5 in dense, banded and banded + low-rank
+# forms), appended to gpurun_out/bench_configs.jsonl.  Usage (on the GPU box): bash tools/bench_configs.sh
+out=gpurun_out/bench_configs.jsonl
+: > $out
+common="--no-cpu-baseline --no-e2e --no-observables --secondary none"
+for c in c1 c2 c4; do
+  python bench.py --config $c --steps 10 --warmup 3 $common >> $out 2>/dev/null
+done
+python bench.py --config c4 --propagator banded --steps 10 --warmup 3 $common >> $out 2>/dev/null
+python bench.py --config c2 --propagator banded --steps 10 --warmup 3 $common >> $out 2>/dev/null
+python bench.py --config c5 --steps 2 --warmup 2 $common >> $out 2>/dev/null
+python bench.py --config c5 --propagator banded --steps 3 --warmup 2 $common >> $out 2>/dev/null
+python bench.py --config c5 --propagator banded --orthonormalizer lowrank --steps 3 --warmup 2 $common >> $out 2>/dev/null
