@@ -133,6 +133,8 @@ struct Ctx {
   int32_t* failed;
   std::string* err;
   const CholDist* dist;
+  const CholHook* hook;
+  long long n_top;
 };
 
 // row slice boundaries of M rows over P ranks, 128-aligned; tri: equal area of an upper triangle
@@ -190,6 +192,7 @@ int rec(Ctx& c, long long o, long long n) {
   cplx* XC = c.X + (o + h) * c.ldx + (o + h);
   int s;
   if ((s = rec(c, o, h))) return s;
+  if (o == 0 && c.hook && c.hook->left_ready) c.hook->left_ready(c.hook->user, h);   // X[:, 0:h] final
   if (c.dist && c.dist->P > 1 && n >= c.dist->min_n && c.batch == 1) {
     // the same four products, each split into row slices over the ranks
     if ((s = dist_gemm(c, false, 1, 0, r, h, h, 1.0, B_blk, c.ldg, XA, c.ldx, 0.0, L_blk, c.ldg, TRAJ_TRI_B_UPPER_F)))
@@ -233,7 +236,7 @@ size_t chol_scratch_bytes(long long n, long long batch) {
 
 int chol_inverse(cudaStream_t st, long long n, cplx* G, long long ldg, long long sG, cplx* X, long long ldx,
                  long long sX, long long batch, void* scratch, int32_t* failed, std::string* err,
-                 const CholDist* dist) {
+                 const CholDist* dist, const CholHook* hook) {
   if (n <= 0 || batch <= 0) return 0;
   if (batch > 65535) {
     if (err) *err = "chol_inverse: batch too large";
@@ -254,6 +257,8 @@ int chol_inverse(cudaStream_t st, long long n, cplx* G, long long ldg, long long
   c.failed = failed;
   c.err = err;
   c.dist = dist;
+  c.hook = hook;
+  c.n_top = n;
   if (n > NB) {
     // the strict lower triangle of X must read as zeros (triangular GEMM tiles cross it)
     cudaError_t e = cudaSuccess;

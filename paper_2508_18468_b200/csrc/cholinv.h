@@ -23,11 +23,19 @@ struct CholDist {
                     cudaStream_t st, std::string* err) = nullptr;
 };
 
+// Called (on the host, in launch order) whenever a left-edge block X[0:h, 0:h] of the recursion has
+// been queued on the stream (h increasing: 64, 128, ..., the top split): columns [0, h) of X are
+// final from that point of the stream on.
+struct CholHook {
+  void (*left_ready)(void* user, long long h) = nullptr;
+  void* user = nullptr;
+};
+
 // G_b = R^dag R (upper triangle of G_b read; strict lower triangle used as scratch),
 // X_b = R^-1 (upper; strict lower set to zero).  failed[b] = 1 on a non-positive or
 // non-finite pivot.
 int chol_inverse(cudaStream_t st, long long n, cplx* G, long long ldg, long long sG, cplx* X, long long ldx,
                  long long sX, long long batch, void* scratch, int32_t* failed, std::string* err,
-                 const CholDist* dist = nullptr);
+                 const CholDist* dist = nullptr, const CholHook* hook = nullptr);
 
 }  // namespace traj

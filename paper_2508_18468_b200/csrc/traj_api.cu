@@ -57,6 +57,11 @@ struct traj_ctx {
   int L = 0, N = 0, Lx = 0, Ly = 0, T = 0, cap = 0;
   long long ldN = 0, ldL = 0, ldcap = 0, sU = 0, sG = 0;
   cudaStream_t st = nullptr;
+  // CholeskyQR pass 1: the factorisation runs on st_hi (high priority) while the TRMM of X's left
+  // block runs on st_lo as soon as that block is final (TRAJ_CHOL_OVERLAP=0: serial)
+  bool chol_overlap = true;
+  cudaStream_t st_hi = nullptr, st_lo = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_left = nullptr, ev_lo_done = nullptr, ev_hi_done = nullptr;
   cplx* K = nullptr;
   cplx* U[2] = {nullptr, nullptr};
   int cur = 0;
@@ -401,6 +406,49 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
           if (m > thr) full = true;           // NaN (failed trajectory) does not force the fallback
         }
         if (full) ++h->cqr2_fallbacks;
+      }
+      if (full && h->chol_overlap && h->st_hi && h->N > 64) {
+        // fork: factorise on st_hi; as each left-edge block X[0:h, 0:h] is queued, st_lo runs the
+        // TRMM of the columns it completes
+        CK(cudaEventRecord(h->ev_fork, h->st));
+        CK(cudaStreamWaitEvent(h->st_hi, h->ev_fork, 0));
+        struct HookUser {
+          traj_ctx* h;
+          const cplx* src;
+          cplx* dst;
+          long long hs;
+          int status;
+        } hu{h, src, dst, 0, 0};
+        CholHook hook;
+        hook.user = &hu;
+        // each left-edge block adds the column piece [previous h, h): dst[:, a:b] = src[:, 0:b] X[0:b, a:b]
+        hook.left_ready = [](void* u, long long hs) {
+          HookUser* q = reinterpret_cast<HookUser*>(u);
+          traj_ctx* hh = q->h;
+          if (q->status || hs <= q->hs) return;
+          const long long a = q->hs;
+          q->hs = hs;
+          if (cudaEventRecord(hh->ev_left, hh->st_hi) != cudaSuccess ||
+              cudaStreamWaitEvent(hh->st_lo, hh->ev_left, 0) != cudaSuccess) {
+            q->status = TRAJ_ECUDA;
+            return;
+          }
+          q->status = zgemm(hh->st_lo, 0, 0, hh->L, hs - a, hs, 1.0, 0.0, q->src, hh->ldN, hh->sU, hh->X + a, hh->ldN,
+                            hh->sG, 0.0, q->dst + a, hh->ldN, hh->sU, hh->T, TRAJ_TRI_B_UPPER_F, &hh->err, 0, a);
+          if (!q->status && cudaEventRecord(hh->ev_lo_done, hh->st_lo) != cudaSuccess) q->status = TRAJ_ECUDA;
+        };
+        TRY(chol_inverse(h->st_hi, h->N, h->G, h->ldN, h->sG, h->X, h->ldN, h->sG, h->T, h->chol_scratch,
+                         h->failed_dev, &h->err, nullptr, &hook));
+        if (hu.status) return fail(h, hu.status, h->err.empty() ? "chol overlap: left TRMM" : h->err);
+        if (hu.hs <= 0) return fail(h, TRAJ_ECUDA, "chol overlap: the left block was not reported");
+        // dst[:, hs:N] = src X[:, hs:N] (triangle offset hs) on st_hi, then join both into st
+        TRY(zgemm(h->st_hi, 0, 0, h->L, h->N - hu.hs, h->N, 1.0, 0.0, src, h->ldN, h->sU, h->X + hu.hs, h->ldN, h->sG,
+                  0.0, dst + hu.hs, h->ldN, h->sU, h->T, TRAJ_TRI_B_UPPER_F, &h->err, 0, hu.hs));
+        CK(cudaEventRecord(h->ev_hi_done, h->st_hi));
+        CK(cudaStreamWaitEvent(h->st, h->ev_hi_done, 0));
+        CK(cudaStreamWaitEvent(h->st, h->ev_lo_done, 0));
+        std::swap(src, dst);
+        continue;   // this pass's TRMM is done (its time is inside the Cholesky phase)
       }
       if (full) {
         TRY(chol_inverse(h->st, h->N, h->G, h->ldN, h->sG, h->X, h->ldN, h->sG, h->T, h->chol_scratch,
@@ -1093,6 +1141,19 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
   h->gamma.assign(cfg->gamma, cfg->gamma + cfg->n_traj);
   h->cfg.gamma = h->gamma.data();
   h->st = reinterpret_cast<cudaStream_t>(cfg->stream);
+  {
+    const char* co = getenv("TRAJ_CHOL_OVERLAP");
+    h->chol_overlap = !(co && co[0] == '0');
+    int least = 0, greatest = 0;
+    if (h->chol_overlap && cudaDeviceGetStreamPriorityRange(&least, &greatest) == cudaSuccess &&
+        cudaStreamCreateWithPriority(&h->st_hi, cudaStreamNonBlocking, greatest) == cudaSuccess &&
+        cudaStreamCreateWithPriority(&h->st_lo, cudaStreamNonBlocking, least) == cudaSuccess) {
+      for (cudaEvent_t* e : {&h->ev_fork, &h->ev_left, &h->ev_lo_done, &h->ev_hi_done})
+        if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) h->chol_overlap = false;
+    } else {
+      h->chol_overlap = false;
+    }
+  }
   h->lwork = lw;
   if (is_sharded(cfg)) {
     h->sh = new ShardedCtx();
@@ -1437,6 +1498,13 @@ int traj_destroy(traj_handle h) {
     delete h->sh;
   }
   h->prof.destroy();
+  for (cudaStream_t q : {h->st_hi, h->st_lo})
+    if (q) {
+      cudaStreamSynchronize(q);
+      cudaStreamDestroy(q);
+    }
+  for (cudaEvent_t e : {h->ev_fork, h->ev_left, h->ev_lo_done, h->ev_hi_done})
+    if (e) cudaEventDestroy(e);
   if (h->solver) cusolverDnDestroy(h->solver);
   if (h->h_small) cudaFreeHost(h->h_small);
   if (h->h_dev) cudaFreeHost(h->h_dev);
