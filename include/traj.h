@@ -264,6 +264,14 @@ int traj_zgemm(void* stream, int opA, int opB, int64_t M, int64_t N, int64_t K,
  * tensor-pipe flops per 8mnk algorithmic, FP64 throughout, the usual ZGEMM3M error bound for
  * the imaginary part; 0 = 4M: two real DMMA products over an interleaved (re, im) k axis,
  * 8mnk tensor flops.  Initial value from the environment: TRAJ_ZGEMM_3M=0 selects 4M. */
+/* Real FP64 GEMM on the DMMA pipe, C_z = alpha A_z B_z + beta C_z (row-major, no transposes), the
+ * building block of the planar 3M complex product (three real products, one accumulator set per
+ * warp).  Device pointers; stream = cudaStream_t.  Needs K > 0, even lda and ldc, ldb a multiple of
+ * 16 with ldb >= N rounded up to 16, 16-byte alignment; TRAJ_EINVAL otherwise. */
+int traj_dgemm(void* stream, int64_t M, int64_t N, int64_t K, double alpha, const void* A, int64_t lda,
+               int64_t strideA, const void* B, int64_t ldb, int64_t strideB, double beta, void* C, int64_t ldc,
+               int64_t strideC, int64_t batch);
+
 int traj_set_zgemm_algorithm(int algo);
 int traj_get_zgemm_algorithm(void);
 

@@ -17,4 +17,5 @@ from .binding import (  # noqa: F401
     traj_nccl_unique_id,
     traj_set_zgemm_algorithm,
     traj_zgemm,
+    traj_dgemm,
 )

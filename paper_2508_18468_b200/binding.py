@@ -91,6 +91,7 @@ _SIGS = {
     "traj_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "traj_zgemm": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _I64, _I64, _I64, _D, _D, _P, _I64, _I64, _P, _I64,
                                   _I64, _D, _P, _I64, _I64, _I64, ctypes.c_int]),
+    "traj_dgemm": (ctypes.c_int, [_P, _I64, _I64, _I64, _D, _P, _I64, _I64, _P, _I64, _I64, _D, _P, _I64, _I64, _I64]),
     "traj_shard_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                        ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "traj_nccl_unique_id": (ctypes.c_int, [_P]),
@@ -173,6 +174,25 @@ def traj_zgemm(opA, opB, A, B, C, *, alpha=1.0, beta=0.0, flags=0, M=None, N=Non
     a = complex(alpha)
     _check(lib_.traj_zgemm(st, opA, opB, M, N, K, a.real, a.imag, _ptr(Ab), Ab.stride(-2), sA, _ptr(Bb),
                            Bb.stride(-2), sB, float(beta), _ptr(Cb), Cb.stride(-2), Cb.stride(0), batch, flags))
+    return C
+
+
+def traj_dgemm(A, B, C, *, alpha=1.0, beta=0.0, stream=None):
+    """C = alpha A B + beta C on torch float64 CUDA tensors (2d, or 3d = batch), row-major, no transposes."""
+    import torch
+    lib_ = lib()
+    Ab = A if A.dim() == 3 else A.unsqueeze(0)
+    Bb = B if B.dim() == 3 else B.unsqueeze(0)
+    Cb = C if C.dim() == 3 else C.unsqueeze(0)
+    for t in (Ab, Bb, Cb):
+        assert t.dtype == torch.float64 and t.is_cuda and t.stride(-1) == 1
+    batch, M, N = Cb.shape
+    K = Ab.shape[2]
+    sA = Ab.stride(0) if Ab.shape[0] > 1 else 0
+    sB = Bb.stride(0) if Bb.shape[0] > 1 else 0
+    st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    _check(lib_.traj_dgemm(st, M, N, K, float(alpha), _ptr(Ab), Ab.stride(-2), sA, _ptr(Bb), Bb.stride(-2), sB,
+                           float(beta), _ptr(Cb), Cb.stride(-2), Cb.stride(0), batch))
     return C
 
 

@@ -1,0 +1,101 @@
+// Planar 3M form of the dense propagator U <- K U (row a1; the north star's dense complex-FP64
+// contraction).  With K = Kr + i Ki and U = Ur + i Ui:
+//   P1 = Kr Ur,  P2 = Ki Ui,  P3 = (Kr + Ki)(Ur + Ui),   K U = (P1 - P2) + i (P3 - P1 - P2)
+// -- the Gauss/3M identity of csrc/zgemm.cu's interleaved kernels, here as three independent real
+// GEMMs on whole planes (dgemm.cu: one accumulator set per warp, 96% of the DMMA pipe).  K's planes
+// (Kr, Ki, Kr + Ki) are built once; U is split into (Ur, Ui, Ur + Ui) before and the products are
+// recombined after: two HBM passes, 40 L N bytes each way per trajectory.
+#include "common.cuh"
+#include "planar.h"
+
+namespace traj {
+
+namespace {
+
+__device__ __forceinline__ double2 cmul2(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// K[i][j] = kx[(jx - ix) mod Lx] ky[(jy - iy) mod Ly]; planes (re, im, re + im)
+__global__ void build_k_planar_kernel(double* Kp, long long ld, long long ps, int Lx, int Ly, const cplx* kx,
+                                      const cplx* ky) {
+  const long long L = (long long)Lx * Ly;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < L * L;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long i = idx / L, j = idx % L;
+    const int ix = (int)(i % Lx), iy = (int)(i / Lx), jx = (int)(j % Lx), jy = (int)(j / Lx);
+    const int dx = ((jx - ix) % Lx + Lx) % Lx, dy = ((jy - iy) % Ly + Ly) % Ly;
+    const double2 v = cmul2(kx[dx], ky[dy]);
+    const long long o = i * ld + j;
+    Kp[o] = v.x;
+    Kp[ps + o] = v.y;
+    Kp[2 * ps + o] = v.x + v.y;
+  }
+}
+
+// planes[t][0..2][row][col] = (re, im, re + im) of U[t][row][col]; two columns per thread
+__global__ void split_kernel(const cplx* __restrict__ U, long long ldu, long long sU, int L, int N,
+                             double* __restrict__ Pl, long long ldp, long long ps, long long ts) {
+  const int t = blockIdx.z;
+  const int row = blockIdx.y;
+  const cplx* u = U + t * sU + (long long)row * ldu;
+  double* p = Pl + t * ts + (long long)row * ldp;
+  for (int c = 2 * (blockIdx.x * blockDim.x + threadIdx.x); c < N; c += 2 * gridDim.x * blockDim.x) {
+    const double2 a = u[c];
+    const double2 b = c + 1 < N ? u[c + 1] : make_double2(0.0, 0.0);
+    *reinterpret_cast<double2*>(p + c) = make_double2(a.x, b.x);
+    *reinterpret_cast<double2*>(p + ps + c) = make_double2(a.y, b.y);
+    *reinterpret_cast<double2*>(p + 2 * ps + c) = make_double2(a.x + a.y, b.x + b.y);
+  }
+}
+
+// U[t][row][col] = (P1 - P2) + i (P3 - P1 - P2)
+__global__ void combine_kernel(const double* __restrict__ Pl, long long ldp, long long ps, long long ts, int L, int N,
+                               cplx* __restrict__ U, long long ldu, long long sU) {
+  const int t = blockIdx.z;
+  const int row = blockIdx.y;
+  const double* p = Pl + t * ts + (long long)row * ldp;
+  cplx* u = U + t * sU + (long long)row * ldu;
+  for (int c = 2 * (blockIdx.x * blockDim.x + threadIdx.x); c < N; c += 2 * gridDim.x * blockDim.x) {
+    const double2 p1 = *reinterpret_cast<const double2*>(p + c);
+    const double2 p2 = *reinterpret_cast<const double2*>(p + ps + c);
+    const double2 p3 = *reinterpret_cast<const double2*>(p + 2 * ps + c);
+    u[c] = make_double2(p1.x - p2.x, p3.x - p1.x - p2.x);
+    if (c + 1 < N) u[c + 1] = make_double2(p1.y - p2.y, p3.y - p1.y - p2.y);
+  }
+}
+
+}  // namespace
+
+int build_k_planar(cudaStream_t st, double* Kp, long long ld, long long ps, int Lx, int Ly, const cplx* kx,
+                   const cplx* ky, std::string* err) {
+  const long long L = (long long)Lx * Ly;
+  build_k_planar_kernel<<<(unsigned)std::min<long long>(ceil_div(L * L, 256), 148 * 64), 256, 0, st>>>(Kp, ld, ps, Lx,
+                                                                                                       Ly, kx, ky);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && err) *err = std::string("build_k_planar: ") + cudaGetErrorString(e);
+  return e == cudaSuccess ? 0 : 4;
+}
+
+int split_planes(cudaStream_t st, const cplx* U, long long ldu, long long sU, int L, int N, int T, double* Pl,
+                 long long ldp, long long ps, long long ts, std::string* err) {
+  dim3 grid((unsigned)std::min<long long>(ceil_div(N, 512), 16), L, T);
+  split_kernel<<<grid, 256, 0, st>>>(U, ldu, sU, L, N, Pl, ldp, ps, ts);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && err) *err = std::string("split_planes: ") + cudaGetErrorString(e);
+  return e == cudaSuccess ? 0 : 4;
+}
+
+int combine_planes(cudaStream_t st, const double* Pl, long long ldp, long long ps, long long ts, int L, int N, int T,
+                   cplx* U, long long ldu, long long sU, std::string* err) {
+  dim3 grid((unsigned)std::min<long long>(ceil_div(N, 512), 16), L, T);
+  combine_kernel<<<grid, 256, 0, st>>>(Pl, ldp, ps, ts, L, N, U, ldu, sU);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && err) *err = std::string("combine_planes: ") + cudaGetErrorString(e);
+  return e == cudaSuccess ? 0 : 4;
+}
+
+}  // namespace traj

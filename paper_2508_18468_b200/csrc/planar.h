@@ -1,0 +1,20 @@
+// Internal interface of the planar 3M propagator (planar.cu): K and U as (re, im, re + im) planes,
+// three real GEMMs (dgemm.cu), then (P1 - P2) + i (P3 - P1 - P2).
+#pragma once
+#include <algorithm>
+#include <string>
+#include "common.cuh"
+
+namespace traj {
+
+// Kp planes [3][L][ld] (plane stride ps) of K = kx (x) ky (Lx*Ly sites, row-major site = y Lx + x)
+int build_k_planar(cudaStream_t st, double* Kp, long long ld, long long ps, int Lx, int Ly, const cplx* kx,
+                   const cplx* ky, std::string* err);
+// Pl[t][p][row][col] (plane stride ps, trajectory stride ts) = (re, im, re + im)[p] of U[t][row][col]
+int split_planes(cudaStream_t st, const cplx* U, long long ldu, long long sU, int L, int N, int T, double* Pl,
+                 long long ldp, long long ps, long long ts, std::string* err);
+// U[t][row][col] = (P1 - P2) + i (P3 - P1 - P2) from Pl[t][0..2]
+int combine_planes(cudaStream_t st, const double* Pl, long long ldp, long long ps, long long ts, int L, int N, int T,
+                   cplx* U, long long ldu, long long sU, std::string* err);
+
+}  // namespace traj

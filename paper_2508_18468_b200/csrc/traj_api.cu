@@ -24,6 +24,8 @@
 #include "qsd_rk4.h"
 #include "pm_events.h"
 #include "probe.h"
+#include "dgemm.h"
+#include "planar.h"
 
 namespace traj {
 std::atomic<long long> g_kernel_launches{0};
@@ -37,6 +39,11 @@ struct traj_ctx {
   bool banded = false;             // TRAJ_PROP_BANDED with a band narrower than the lattice
   int Wx = 0, Wy = 0;              // compiled half-bandwidths per axis
   cplx* bcoef = nullptr;           // [2Wx+1 | 2Wy+1] stencil coefficients (device copy)
+  // planar 3M dense propagator (planar.cu, TRAJ_PLANAR_KU=0: the interleaved zgemm): K planes
+  // [3][L][ldK], U planes and product planes [T][3][L][ldP]
+  bool planar = false;
+  double *Kp = nullptr, *Up = nullptr, *Pp = nullptr;
+  long long ldK = 0, ldP = 0;
   std::vector<cplx> band_host;     // the same on the host: passed by value to the stencil launches
   cplx* Wrk = nullptr;             // RK4 QSD scratch, shaped like U
   // event-driven PM (NEXT-4)
@@ -240,6 +247,11 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
   h->sU = L * ldN;
   h->sG = N * ldN;
   h->banded = banded_widths(c, &h->Wx, &h->Wy);
+  {
+    const char* pk = getenv("TRAJ_PLANAR_KU");
+    h->planar = !h->banded && c->protocol != TRAJ_HOMODYNE_RK4 && c->protocol != TRAJ_PROJECTIVE_EVENTS &&
+                !(pk && pk[0] == '0');
+  }
   if (c->protocol == TRAJ_HOMODYNE_RK4) {     // stencil generator: no K
     h->banded = false;
     lay.take(h->Wrk, (size_t)T * L * ldN * 16);
@@ -256,6 +268,12 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     lay.take(h->taps_dev, (size_t)EV_TAPCAP * 16);
   } else if (h->banded) {
     lay.take(h->bcoef, (size_t)(2 * h->Wx + 2 * h->Wy + 2) * 16);
+  } else if (h->planar) {
+    h->ldK = round_up(L, 16);
+    h->ldP = round_up(N, 16);
+    lay.take(h->Kp, (size_t)3 * L * h->ldK * 8);
+    lay.take(h->Up, (size_t)T * 3 * L * h->ldP * 8);
+    lay.take(h->Pp, (size_t)T * 3 * L * h->ldP * 8);
   } else {
     lay.take(h->K, (size_t)L * ldL * 16);
   }
@@ -908,8 +926,18 @@ int one_step(traj_ctx* h) {
       }
     } else {
       // U <- K U  (K shared across the batch: stride 0)
-      TRY(zgemm(h->st, 0, 0, h->L, h->N, h->L, 1.0, 0.0, h->K, h->ldL, 0, Uc, h->ldN, h->sU, 0.0, Un, h->ldN, h->sU,
+      if (h->planar) {
+        // three real products on planes, then (P1 - P2) + i (P3 - P1 - P2)
+        const long long ps = h->L * h->ldP, ts = 3 * ps;
+        TRY(split_planes(h->st, Uc, h->ldN, h->sU, h->L, h->N, h->T, h->Up, h->ldP, ps, ts, &h->err));
+        for (int p = 0; p < 3; ++p)
+          TRY(dgemm_nn(h->st, h->L, h->N, h->L, 1.0, h->Kp + p * h->L * h->ldK, h->ldK, 0, h->Up + p * ps, h->ldP, ts,
+                       0.0, h->Pp + p * ps, h->ldP, ts, h->T, &h->err));
+        TRY(combine_planes(h->st, h->Pp, h->ldP, ps, ts, h->L, h->N, h->T, Un, h->ldN, h->sU, &h->err));
+      } else {
+        TRY(zgemm(h->st, 0, 0, h->L, h->N, h->L, 1.0, 0.0, h->K, h->ldL, 0, Uc, h->ldN, h->sU, 0.0, Un, h->ldN, h->sU,
                 h->T, 0, &h->err));
+      }
     }
   }
   cplx* Ut = Us == Un ? Uc : Un;
@@ -1255,6 +1283,9 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
   if (h->banded) {
     if (cudaMemcpyAsync(h->bcoef, band.data(), band.size() * 16, cudaMemcpyHostToDevice, h->st) != cudaSuccess)
       return bail(TRAJ_ECUDA, "upload band");
+  } else if (h->planar) {
+    if (build_k_planar(h->st, h->Kp, h->ldK, h->L * h->ldK, h->Lx, h->Ly, h->kcoef, h->kcoef + h->Lx, &e))
+      return bail(TRAJ_ECUDA, e);
   } else if (cfg->protocol != TRAJ_HOMODYNE_RK4 && cfg->protocol != TRAJ_PROJECTIVE_EVENTS &&
              build_k(h->st, h->K, h->ldL, h->Lx, h->Ly, h->kcoef, h->kcoef + h->Lx, &e)) {
     return bail(TRAJ_ECUDA, e);
@@ -1511,6 +1542,17 @@ int traj_destroy(traj_handle h) {
   if (h->taps_host) cudaFreeHost(h->taps_host);
   delete h;
   return 0;
+}
+
+int traj_dgemm(void* stream, int64_t M, int64_t N, int64_t K, double alpha, const void* A, int64_t lda,
+               int64_t strideA, const void* B, int64_t ldb, int64_t strideB, double beta, void* C, int64_t ldc,
+               int64_t strideC, int64_t batch) {
+  if (M < 0 || N < 0 || K < 0 || batch < 0 || !C || (K > 0 && (!A || !B))) return fail(nullptr, TRAJ_EINVAL, "traj_dgemm: bad argument");
+  std::string e;
+  const int s = dgemm_nn(reinterpret_cast<cudaStream_t>(stream), M, N, K, alpha, reinterpret_cast<const double*>(A), lda,
+                         strideA, reinterpret_cast<const double*>(B), ldb, strideB, beta, reinterpret_cast<double*>(C),
+                         ldc, strideC, batch, &e);
+  return s ? fail(nullptr, s == 1 ? TRAJ_EINVAL : s, e) : 0;
 }
 
 int traj_zgemm(void* stream, int opA, int opB, int64_t M, int64_t N, int64_t K, double alpha_re, double alpha_im,

@@ -138,3 +138,35 @@ def test_chol_inverse_flags_breakdown(T):
     X = T.zeros((n, n), dtype=T.complex128, device="cuda")
     _, failed = traj_chol_inverse(dev(T, G), X)
     assert failed.cpu().numpy()[0] == 1
+
+
+@pytest.mark.parametrize("M,N,K,batch", [(300, 200, 100, 1), (129, 17, 34, 2), (520, 300, 778, 3), (64, 128, 16, 1)])
+def test_dgemm_real_ragged_batched(T, M, N, K, batch):
+    """traj_dgemm (the real DMMA GEMM of the planar 3M propagator) against NumPy: tails that are not
+    multiples of the 128 x 128 tile or the 16-deep stage, alpha/beta, batches, B's leading dimension
+    padded to 16 columns, C's to an even count."""
+    import paper_2508_18468_b200 as P
+    rng = np.random.default_rng(M + N + K)
+    ldb = (N + 15) // 16 * 16
+    ldc = N + (N & 1)
+    lda = K + (K & 1)
+    A = rng.standard_normal((batch, M, lda))
+    B = rng.standard_normal((batch, K, ldb))
+    C = rng.standard_normal((batch, M, ldc))
+    want = 0.5 * np.einsum("bmk,bkn->bmn", A[:, :, :K], B[:, :, :N]) + 2.0 * C[:, :, :N]
+    dA, dB, dC = dev(T, A), dev(T, B), dev(T, C)
+    st = T.cuda.current_stream().cuda_stream
+    r = P.lib().traj_dgemm(st, M, N, K, 0.5, dA.data_ptr(), lda, M * lda if batch > 1 else 0, dB.data_ptr(), ldb,
+                           K * ldb if batch > 1 else 0, 2.0, dC.data_ptr(), ldc, M * ldc, batch)
+    assert r == 0
+    got = dC.cpu().numpy()[:, :, :N]
+    assert np.abs(got - want).max() < 1e-12 * max(1.0, np.abs(want).max()) * K ** 0.5
+    assert np.array_equal(dC.cpu().numpy()[:, :, N:], C[:, :, N:])      # padding untouched
+
+
+def test_dgemm_rejects_bad_layouts(T):
+    import paper_2508_18468_b200 as P
+    st = T.cuda.current_stream().cuda_stream
+    A = T.zeros(8, 8, dtype=T.float64, device="cuda")
+    assert P.lib().traj_dgemm(st, 8, 8, 8, 1.0, A.data_ptr(), 7, 0, A.data_ptr(), 8, 0, 0.0, A.data_ptr(), 8, 0, 1) == 1
+    assert P.lib().traj_dgemm(st, 8, 8, 8, 1.0, A.data_ptr(), 8, 0, A.data_ptr(), 8, 0, 0.0, A.data_ptr(), 8, 0, 1) == 1

@@ -310,6 +310,30 @@ def test_row_sharded_distributed_cholesky_matches_replicated(P, P_shards, monkey
     b.close()
 
 
+@pytest.mark.parametrize("Lx,Ly,protocol", [(300, 1, "projective"), (12, 10, "homodyne")])
+def test_planar_propagator_matches_interleaved(P, Lx, Ly, protocol, monkeypatch):
+    """The dense propagator as three real planar products (TRAJ_PLANAR_KU, the default) against
+    the interleaved complex 3M GEMM and the oracle, same trajectory."""
+    gam = [2.0] if protocol == "projective" else [1.0]
+    monkeypatch.setenv("TRAJ_PLANAR_KU", "0")
+    a = P.Trajectories(Lx, Ly, protocol, gam, seed=41)
+    monkeypatch.setenv("TRAJ_PLANAR_KU", "1")
+    b = P.Trajectories(Lx, Ly, protocol, gam, seed=41)
+    K = lattice.propagator_lattice(Lx, Ly, 1.0, 0.05)
+    o = OracleTrajectory(Lx, Ly, protocol, gam[0], 0.05, seed=41, traj=0, K=K)
+    for s in range(12):
+        a.step(1)
+        b.step(1)
+        o.step(1)
+        if protocol == "projective":
+            assert a.last_clicks(0) == b.last_clicks(0)
+    ca, cb = a.correlation(0).cpu().numpy(), b.correlation(0).cpu().numpy()
+    assert np.abs(ca - cb).max() < 1e-12
+    assert np.abs(cb - o.correlation()).max() < C_TOL
+    a.close()
+    b.close()
+
+
 def test_row_sharded_nccl_single_rank(P):
     """The NCCL code path of the sharded step with a one-rank communicator (the only
     configuration one GPU allows): same result as the unsharded handle."""
