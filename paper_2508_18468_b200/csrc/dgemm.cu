@@ -28,6 +28,8 @@ struct DArgs {
   int M, N, K;
   int tiles_m, tiles_n;
   int a_batched, b_batched;
+  int flags;               // DG_TRI_B_UPPER, DG_C_UPPER (dgemm.h)
+  int m_off, n_off;        // global row / column of C(0, 0) for the triangle tests
   double alpha, beta;
   double* C;
   long long ldc, strideC;
@@ -40,6 +42,8 @@ __device__ __forceinline__ uint32_t doff_b(int k, int n) {
   return ((n >> 4) * 16 + k) * 128 + (((((n & 15) >> 1) ^ (k & 7))) << 4) + (n & 1) * 8;
 }
 
+// TA: op(A) = A^T with A stored [K][M] (m-contiguous tiles, the same 4D box as B)
+template <bool TA>
 __global__ void __launch_bounds__(DTHREADS, 1)
     dgemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const DArgs args) {
@@ -53,7 +57,10 @@ __global__ void __launch_bounds__(DTHREADS, 1)
   const int gm = min(DGROUP_M, args.tiles_m - first_m);
   const int m0 = (first_m + (t % group) % gm) * DBM, n0 = ((t % group) / gm) * DBN;
   const int z = blockIdx.z;
-  const int nk = (args.K + DBK - 1) / DBK;
+  if ((args.flags & DG_C_UPPER) && m0 + args.m_off > n0 + args.n_off + DBN - 1) return;   // below the diagonal
+  int ke = args.K;
+  if (args.flags & DG_TRI_B_UPPER) ke = min(ke, n0 + args.n_off + DBN);
+  const int nk = (ke + DBK - 1) / DBK;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < DSTAGES; ++s) {
@@ -69,7 +76,8 @@ __global__ void __launch_bounds__(DTHREADS, 1)
     const int s = it % DSTAGES;
     mbar_arrive_expect_tx(&full[s], DSTAGE);
     uint8_t* sA = smem + s * DSTAGE;
-    tma_load_3d(sA, &tmA, it * DBK, m0, za, &full[s]);
+    if (TA) tma_load_4d(sA, &tmA, 0, it * DBK, m0 / 16, za, &full[s]);
+    else tma_load_3d(sA, &tmA, it * DBK, m0, za, &full[s]);
     tma_load_4d(sA + DA_BYTES, &tmB, 0, it * DBK, n0 / 16, zb, &full[s]);
   };
   int issued = 0;
@@ -107,7 +115,9 @@ __global__ void __launch_bounds__(DTHREADS, 1)
       const int k = 4 * q + slot;
       double a[4], b[8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = *reinterpret_cast<const double*>(sA + doff_a(warp_m * 32 + 8 * i + g, k));
+      for (int i = 0; i < 4; ++i)
+        a[i] = *reinterpret_cast<const double*>(sA + (TA ? doff_b(k, warp_m * 32 + 8 * i + g)
+                                                          : doff_a(warp_m * 32 + 8 * i + g, k)));
 #pragma unroll
       for (int j = 0; j < 8; ++j) b[j] = *reinterpret_cast<const double*>(sB + doff_b(k, warp_n * 64 + 8 * j + g));
 #pragma unroll
@@ -120,6 +130,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
     if (lane == 0) mbar_arrive(&empty[s]);
   }
   double* C = args.C + (long long)z * args.strideC;
+  const bool upper = args.flags & DG_C_UPPER;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int row = m0 + warp_m * 32 + 8 * i + g;
@@ -128,6 +139,14 @@ __global__ void __launch_bounds__(DTHREADS, 1)
     for (int j = 0; j < 8; ++j) {
       const int col = n0 + warp_n * 64 + 8 * j + 2 * slot;
       double* p = C + (long long)row * args.ldc + col;
+      if (upper && row + args.m_off > col + args.n_off) {   // one of the pair may still be on/above
+        if (row + args.m_off <= col + 1 + args.n_off && col + 1 < args.N) {
+          double v = args.alpha * acc[i][j][1];
+          if (args.beta != 0.0) v += args.beta * p[1];
+          p[1] = v;
+        }
+        continue;
+      }
       if (col + 1 < args.N) {
         double2 v = make_double2(args.alpha * acc[i][j][0], args.alpha * acc[i][j][1]);
         if (args.beta != 0.0) {
@@ -163,24 +182,26 @@ PFN_encode_t encode_fn() {
 
 }  // namespace
 
-int dgemm_nn(cudaStream_t st, long long M, long long N, long long K, double alpha, const double* A, long long lda,
-             long long strideA, const double* B, long long ldb, long long strideB, double beta, double* C,
-             long long ldc, long long strideC, long long batch, std::string* err) {
+int dgemm(cudaStream_t st, int opA, long long M, long long N, long long K, double alpha, const double* A,
+          long long lda, long long strideA, const double* B, long long ldb, long long strideB, double beta, double* C,
+          long long ldc, long long strideC, long long batch, int flags, std::string* err, long long m_off,
+          long long n_off) {
   if (M <= 0 || N <= 0 || batch <= 0) return 0;
   if (K <= 0 || (lda & 1) || (ldb & 15) || round_up(N, 16) > ldb || (ldc & 1) ||
+      (opA == 1 && ((lda & 15) || round_up(M, 16) > lda)) || (opA != 0 && opA != 1) ||
       (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15) ||
       (reinterpret_cast<uintptr_t>(C) & 15) || batch > 65535) {
-    if (err) *err = "dgemm_nn: needs K > 0, even lda/ldc, ldb a multiple of 16 >= round_up(N, 16), 16-B alignment";
+    if (err) *err = "dgemm: needs K > 0, even lda/ldc, ldb (and lda for op(A) = A^T) a multiple of 16 >= N (M) rounded up to 16, 16-B alignment";
     return 1;
   }
   PFN_encode_t enc = encode_fn();
   if (!enc) {
-    if (err) *err = "dgemm_nn: cuTensorMapEncodeTiled unavailable";
+    if (err) *err = "dgemm: cuTensorMapEncodeTiled unavailable";
     return 4;
   }
   const bool ab = strideA != 0 && batch > 1, bb = strideB != 0 && batch > 1;
   CUtensorMap ma, mb;
-  {
+  if (opA == 0) {
     cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)M, (cuuint64_t)(ab ? batch : 1)};
     cuuint64_t strides[2] = {(cuuint64_t)(lda * 8), (cuuint64_t)((ab ? strideA : lda * M) * 8)};
     cuuint32_t box[3] = {DBK, DBM, 1};
@@ -188,7 +209,18 @@ int dgemm_nn(cudaStream_t st, long long M, long long N, long long K, double alph
     if (enc(&ma, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(A), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
-      if (err) *err = "dgemm_nn: A tensor map";
+      if (err) *err = "dgemm: A tensor map";
+      return 4;
+    }
+  } else {   // A stored [K][M]: 16-column chunks of m, like B
+    cuuint64_t dims[4] = {16, (cuuint64_t)K, (cuuint64_t)ceil_div(M, 16), (cuuint64_t)(ab ? batch : 1)};
+    cuuint64_t strides[3] = {(cuuint64_t)(lda * 8), 128, (cuuint64_t)((ab ? strideA : lda * K) * 8)};
+    cuuint32_t box[4] = {16, DBK, DBM / 16, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    if (enc(&ma, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(A), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      if (err) *err = "dgemm: A^T tensor map";
       return 4;
     }
   }
@@ -200,7 +232,7 @@ int dgemm_nn(cudaStream_t st, long long M, long long N, long long K, double alph
     if (enc(&mb, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(B), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
-      if (err) *err = "dgemm_nn: B tensor map";
+      if (err) *err = "dgemm: B tensor map";
       return 4;
     }
   }
@@ -212,25 +244,31 @@ int dgemm_nn(cudaStream_t st, long long M, long long N, long long K, double alph
   args.tiles_n = (int)ceil_div(N, DBN);
   args.a_batched = ab;
   args.b_batched = bb;
+  args.flags = flags;
+  args.m_off = (int)m_off;
+  args.n_off = (int)n_off;
   args.alpha = alpha;
   args.beta = beta;
   args.C = C;
   args.ldc = ldc;
   args.strideC = strideC;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(dgemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DSMEM) != cudaSuccess) {
-      if (err) *err = "dgemm_nn: shared memory attribute";
+  static bool attr[2] = {false, false};
+  if (!attr[opA]) {
+    cudaError_t e = opA ? cudaFuncSetAttribute(dgemm_dmma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DSMEM)
+                        : cudaFuncSetAttribute(dgemm_dmma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DSMEM);
+    if (e != cudaSuccess) {
+      if (err) *err = "dgemm: shared memory attribute";
       return 4;
     }
-    attr = true;
+    attr[opA] = true;
   }
   dim3 grid((unsigned)(args.tiles_m * args.tiles_n), 1, (unsigned)batch);
-  dgemm_dmma_kernel<<<grid, DTHREADS, DSMEM, st>>>(ma, mb, args);
+  if (opA) dgemm_dmma_kernel<true><<<grid, DTHREADS, DSMEM, st>>>(ma, mb, args);
+  else dgemm_dmma_kernel<false><<<grid, DTHREADS, DSMEM, st>>>(ma, mb, args);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
-    if (err) *err = std::string("dgemm_nn: ") + cudaGetErrorString(e);
+    if (err) *err = std::string("dgemm: ") + cudaGetErrorString(e);
     return 4;
   }
   return 0;

@@ -65,7 +65,61 @@ __global__ void combine_kernel(const double* __restrict__ Pl, long long ldp, lon
   }
 }
 
+// planes (re, im, re - im, re, im, re + im) of U: the Gram's A operands (Ur, Ui, Ur - Ui; U^dag =
+// Ur^T - i Ui^T) followed by its B operands (Ur, Ui, Ur + Ui), each triple a constant-stride batch
+__global__ void split6_kernel(const cplx* __restrict__ U, long long ldu, long long sU, int L, int N,
+                              double* __restrict__ Pl, long long ldp, long long ps, long long ts) {
+  const int t = blockIdx.z;
+  const int row = blockIdx.y;
+  const cplx* u = U + t * sU + (long long)row * ldu;
+  double* p = Pl + t * ts + (long long)row * ldp;
+  for (int c = 2 * (blockIdx.x * blockDim.x + threadIdx.x); c < N; c += 2 * gridDim.x * blockDim.x) {
+    const double2 a = u[c];
+    const double2 b = c + 1 < N ? u[c + 1] : make_double2(0.0, 0.0);
+    *reinterpret_cast<double2*>(p + c) = make_double2(a.x, b.x);
+    *reinterpret_cast<double2*>(p + ps + c) = make_double2(a.y, b.y);
+    *reinterpret_cast<double2*>(p + 2 * ps + c) = make_double2(a.x - a.y, b.x - b.y);
+    *reinterpret_cast<double2*>(p + 3 * ps + c) = make_double2(a.x, b.x);
+    *reinterpret_cast<double2*>(p + 4 * ps + c) = make_double2(a.y, b.y);
+    *reinterpret_cast<double2*>(p + 5 * ps + c) = make_double2(a.x + a.y, b.x + b.y);
+  }
+}
+
+// G = U^dag U from P1 = Ur^T Ur, Q2 = Ui^T Ui, P3 = (Ur - Ui)^T (Ur + Ui): Re = P1 + Q2,
+// Im = P3 - P1 + Q2; upper triangle only
+__global__ void combine_gram_kernel(const double* __restrict__ Pl, long long ldp, long long ps, long long ts, int n,
+                                    cplx* __restrict__ G, long long ldg, long long sG) {
+  const int t = blockIdx.z;
+  const int row = blockIdx.y;
+  const double* p = Pl + t * ts + (long long)row * ldp;
+  cplx* g = G + t * sG + (long long)row * ldg;
+  for (int c = row + blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+    const double p1 = p[c], q2 = p[ps + c], p3 = p[2 * ps + c];
+    g[c] = make_double2(p1 + q2, p3 - p1 + q2);
+  }
+}
+
 }  // namespace
+
+int split6_planes(cudaStream_t st, const cplx* U, long long ldu, long long sU, int L, int N, int T, double* Pl,
+                  long long ldp, long long ps, long long ts, std::string* err) {
+  dim3 grid((unsigned)std::min<long long>(ceil_div(N, 512), 16), L, T);
+  split6_kernel<<<grid, 256, 0, st>>>(U, ldu, sU, L, N, Pl, ldp, ps, ts);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && err) *err = std::string("split6_planes: ") + cudaGetErrorString(e);
+  return e == cudaSuccess ? 0 : 4;
+}
+
+int combine_gram(cudaStream_t st, const double* Pl, long long ldp, long long ps, long long ts, int n, int T, cplx* G,
+                 long long ldg, long long sG, std::string* err) {
+  dim3 grid((unsigned)std::min<long long>(ceil_div(n, 256), 32), n, T);
+  combine_gram_kernel<<<grid, 256, 0, st>>>(Pl, ldp, ps, ts, n, G, ldg, sG);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && err) *err = std::string("combine_gram: ") + cudaGetErrorString(e);
+  return e == cudaSuccess ? 0 : 4;
+}
 
 int build_k_planar(cudaStream_t st, double* Kp, long long ld, long long ps, int Lx, int Ly, const cplx* kx,
                    const cplx* ky, std::string* err) {

@@ -17,4 +17,11 @@ int split_planes(cudaStream_t st, const cplx* U, long long ldu, long long sU, in
 int combine_planes(cudaStream_t st, const double* Pl, long long ldp, long long ps, long long ts, int L, int N, int T,
                    cplx* U, long long ldu, long long sU, std::string* err);
 
+// Pl[t][0..5] = (re, im, re - im, re, im, re + im) of U[t]
+int split6_planes(cudaStream_t st, const cplx* U, long long ldu, long long sU, int L, int N, int T, double* Pl,
+                  long long ldp, long long ps, long long ts, std::string* err);
+// upper triangle of G[t] (n x n) = (P1 + Q2) + i (P3 - P1 + Q2) from Pl[t][0..2]
+int combine_gram(cudaStream_t st, const double* Pl, long long ldp, long long ps, long long ts, int n, int T, cplx* G,
+                 long long ldg, long long sG, std::string* err);
+
 }  // namespace traj

@@ -44,6 +44,12 @@ struct traj_ctx {
   bool planar = false;
   double *Kp = nullptr, *Up = nullptr, *Pp = nullptr;
   long long ldK = 0, ldP = 0;
+  // planar CholeskyQR (TRAJ_PLANAR_CQR=0: interleaved): measured Grams as three real U^T U-type
+  // products, TRMMs as three real products against X's planes (Xp).  Up holds 6 planes per
+  // trajectory, (re, im, re - im, re, im, re + im): planes 0..2 and 3..5 are constant-stride
+  // triples, so with one trajectory each group of three products is a single batched launch
+  bool planar_cqr = false;
+  double* Xp = nullptr;
   std::vector<cplx> band_host;     // the same on the host: passed by value to the stencil launches
   cplx* Wrk = nullptr;             // RK4 QSD scratch, shaped like U
   // event-driven PM (NEXT-4)
@@ -251,6 +257,8 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     const char* pk = getenv("TRAJ_PLANAR_KU");
     h->planar = !h->banded && c->protocol != TRAJ_HOMODYNE_RK4 && c->protocol != TRAJ_PROJECTIVE_EVENTS &&
                 !(pk && pk[0] == '0');
+    const char* pc = getenv("TRAJ_PLANAR_CQR");
+    h->planar_cqr = !(pc && pc[0] == '0');
   }
   if (c->protocol == TRAJ_HOMODYNE_RK4) {     // stencil generator: no K
     h->banded = false;
@@ -270,12 +278,15 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     lay.take(h->bcoef, (size_t)(2 * h->Wx + 2 * h->Wy + 2) * 16);
   } else if (h->planar) {
     h->ldK = round_up(L, 16);
-    h->ldP = round_up(N, 16);
     lay.take(h->Kp, (size_t)3 * L * h->ldK * 8);
-    lay.take(h->Up, (size_t)T * 3 * L * h->ldP * 8);
-    lay.take(h->Pp, (size_t)T * 3 * L * h->ldP * 8);
   } else {
     lay.take(h->K, (size_t)L * ldL * 16);
+  }
+  if (h->planar || h->planar_cqr) {
+    h->ldP = round_up(N, 16);
+    lay.take(h->Up, (size_t)T * 6 * L * h->ldP * 8);
+    lay.take(h->Pp, (size_t)T * 3 * L * h->ldP * 8);
+    if (h->planar_cqr) lay.take(h->Xp, (size_t)T * 3 * N * h->ldP * 8);
   }
   lay.take(h->U[0], (size_t)T * L * ldN * 16);
   lay.take(h->U[1], (size_t)T * L * ldN * 16);
@@ -373,9 +384,25 @@ std::vector<std::complex<double>> ring_coefficients(int n, double J, double dt) 
 // Pass 2 sees G2 = I + E with |E| ~ kappa(U)^2 eps: its Cholesky inverse is taken from the
 // first-order closed form (exact up to N |E|^2, below rounding when N max|E|^2 < 1e-18,
 // checked on the device per step); otherwise, or with TRAJ_CQR2_FULL=1, chol_inverse.
+// Three real products C_q = op(A_q) B_q (q = 0, 1, 2) whose operands are plane triples at constant
+// strides (pa, pb, pc) within each trajectory (strides ta, tb, tc between trajectories): one
+// batch-3 launch for a single trajectory (fewer partial waves), else one launch per product.
+int prod3(traj_ctx* h, int opA, long long M, long long N, long long K, const double* A, long long lda, long long pa,
+          long long ta, const double* B, long long ldb, long long pb, long long tb, double* C, long long pc,
+          long long tc, int flags) {
+  if (h->T == 1) return dgemm(h->st, opA, M, N, K, 1.0, A, lda, pa, B, ldb, pb, 0.0, C, h->ldP, pc, 3, flags, &h->err);
+  for (int q = 0; q < 3; ++q) {
+    int s = dgemm(h->st, opA, M, N, K, 1.0, A + q * pa, lda, ta, B + q * pb, ldb, tb, 0.0, C + q * pc, h->ldP, tc, h->T,
+                  flags, &h->err);
+    if (s) return s;
+  }
+  return 0;
+}
+
 int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
   cplx* src = U;
   cplx* dst = tmp;
+  const cplx* planes_of = nullptr;   // the state whose planes Up holds (set by a planar Gram)
   const int lr = h->lr_k0;
   h->lr_k0 = -1;
   if (lr == 0 && h->lowrank_orth) {
@@ -406,6 +433,15 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
         TRY(set_identity(h->st, h->G, h->ldN, h->sG, h->N, h->T, &h->err));
         TRY(zgemm(h->st, 1, 0, h->N, h->N, lr, -1.0, 0.0, h->US, h->ldN, h->sUS, h->US, h->ldN, h->sUS, 1.0, h->G,
                   h->ldN, h->sG, h->T, TRAJ_C_UPPER_F, &h->err));
+      } else if (h->planar_cqr) {
+        // G = U^dag U = (P1 + Q2) + i (P3 - P1 + Q2): P1 = Ur^T Ur, Q2 = Ui^T Ui, P3 = (Ur - Ui)^T (Ur + Ui),
+        // A triple = planes 0..2, B triple = planes 3..5
+        const long long ps = h->L * h->ldP, tsu = 6 * ps, tsp = 3 * ps;
+        TRY(split6_planes(h->st, src, h->ldN, h->sU, h->L, h->N, h->T, h->Up, h->ldP, ps, tsu, &h->err));
+        TRY(prod3(h, 1, h->N, h->N, h->L, h->Up, h->ldP, ps, tsu, h->Up + 3 * ps, h->ldP, ps, tsu, h->Pp, ps, tsp,
+                  DG_C_UPPER));
+        TRY(combine_gram(h->st, h->Pp, h->ldP, ps, tsp, h->N, h->T, h->G, h->ldN, h->sG, &h->err));
+        planes_of = src;
       } else {
         TRY(zgemm(h->st, 1, 0, h->N, h->N, h->L, 1.0, 0.0, src, h->ldN, h->sU, src, h->ldN, h->sU, 0.0, h->G,
                   h->ldN, h->sG, h->T, TRAJ_C_UPPER_F, &h->err));
@@ -477,8 +513,18 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
     }
     {
       Phase p(&h->prof, h->st, TRAJ_PH_TRMM);
-      TRY(zgemm(h->st, 0, 0, h->L, h->N, h->N, 1.0, 0.0, src, h->ldN, h->sU, h->X, h->ldN, h->sG, 0.0, dst, h->ldN,
-                h->sU, h->T, TRAJ_TRI_B_UPPER_F, &h->err));
+      if (h->planar_cqr && planes_of == src) {
+        // U X = (P1 - P2) + i (P3 - P1 - P2): P1 = Ur Xr, P2 = Ui Xi, P3 = (Ur + Ui)(Xr + Xi) on the
+        // Gram's planes of U and X's planes (X upper triangular: k-blocks past the diagonal skipped)
+        const long long ps = h->L * h->ldP, tsu = 6 * ps, tsp = 3 * ps, psx = (long long)h->N * h->ldP, tsx = 3 * psx;
+        TRY(split_planes(h->st, h->X, h->ldN, h->sG, h->N, h->N, h->T, h->Xp, h->ldP, psx, tsx, &h->err));
+        TRY(prod3(h, 0, h->L, h->N, h->N, h->Up + 3 * ps, h->ldP, ps, tsu, h->Xp, h->ldP, psx, tsx, h->Pp, ps, tsp,
+                  DG_TRI_B_UPPER));
+        TRY(combine_planes(h->st, h->Pp, h->ldP, ps, tsp, h->L, h->N, h->T, dst, h->ldN, h->sU, &h->err));
+      } else {
+        TRY(zgemm(h->st, 0, 0, h->L, h->N, h->N, 1.0, 0.0, src, h->ldN, h->sU, h->X, h->ldN, h->sG, 0.0, dst, h->ldN,
+                  h->sU, h->T, TRAJ_TRI_B_UPPER_F, &h->err));
+      }
     }
     std::swap(src, dst);
   }
@@ -928,12 +974,11 @@ int one_step(traj_ctx* h) {
       // U <- K U  (K shared across the batch: stride 0)
       if (h->planar) {
         // three real products on planes, then (P1 - P2) + i (P3 - P1 - P2)
-        const long long ps = h->L * h->ldP, ts = 3 * ps;
-        TRY(split_planes(h->st, Uc, h->ldN, h->sU, h->L, h->N, h->T, h->Up, h->ldP, ps, ts, &h->err));
-        for (int p = 0; p < 3; ++p)
-          TRY(dgemm_nn(h->st, h->L, h->N, h->L, 1.0, h->Kp + p * h->L * h->ldK, h->ldK, 0, h->Up + p * ps, h->ldP, ts,
-                       0.0, h->Pp + p * ps, h->ldP, ts, h->T, &h->err));
-        TRY(combine_planes(h->st, h->Pp, h->ldP, ps, ts, h->L, h->N, h->T, Un, h->ldN, h->sU, &h->err));
+        const long long ps = h->L * h->ldP, tsu = 6 * ps, tsp = 3 * ps;
+        TRY(split_planes(h->st, Uc, h->ldN, h->sU, h->L, h->N, h->T, h->Up + 3 * ps, h->ldP, ps, tsu, &h->err));
+        TRY(prod3(h, 0, h->L, h->N, h->L, h->Kp, h->ldK, h->L * h->ldK, 0, h->Up + 3 * ps, h->ldP, ps, tsu, h->Pp, ps,
+                  tsp, 0));
+        TRY(combine_planes(h->st, h->Pp, h->ldP, ps, tsp, h->L, h->N, h->T, Un, h->ldN, h->sU, &h->err));
       } else {
         TRY(zgemm(h->st, 0, 0, h->L, h->N, h->L, 1.0, 0.0, h->K, h->ldL, 0, Uc, h->ldN, h->sU, 0.0, Un, h->ldN, h->sU,
                 h->T, 0, &h->err));
