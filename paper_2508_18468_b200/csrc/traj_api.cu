@@ -74,7 +74,7 @@ struct traj_ctx {
   // block runs on st_lo as soon as that block is final (TRAJ_CHOL_OVERLAP=0: serial)
   bool chol_overlap = true;
   cudaStream_t st_hi = nullptr, st_lo = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_left = nullptr, ev_lo_done = nullptr, ev_hi_done = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_left = nullptr, ev_lo_done = nullptr, ev_hi_done = nullptr, ev_split = nullptr;
   cplx* K = nullptr;
   cplx* U[2] = {nullptr, nullptr};
   int cur = 0;
@@ -389,11 +389,13 @@ std::vector<std::complex<double>> ring_coefficients(int n, double J, double dt) 
 // batch-3 launch for a single trajectory (fewer partial waves), else one launch per product.
 int prod3(traj_ctx* h, int opA, long long M, long long N, long long K, const double* A, long long lda, long long pa,
           long long ta, const double* B, long long ldb, long long pb, long long tb, double* C, long long pc,
-          long long tc, int flags) {
-  if (h->T == 1) return dgemm(h->st, opA, M, N, K, 1.0, A, lda, pa, B, ldb, pb, 0.0, C, h->ldP, pc, 3, flags, &h->err);
+          long long tc, int flags, cudaStream_t st = nullptr, long long n_off = 0) {
+  if (!st) st = h->st;
+  if (h->T == 1)
+    return dgemm(st, opA, M, N, K, 1.0, A, lda, pa, B, ldb, pb, 0.0, C, h->ldP, pc, 3, flags, &h->err, 0, n_off);
   for (int q = 0; q < 3; ++q) {
-    int s = dgemm(h->st, opA, M, N, K, 1.0, A + q * pa, lda, ta, B + q * pb, ldb, tb, 0.0, C + q * pc, h->ldP, tc, h->T,
-                  flags, &h->err);
+    int s = dgemm(st, opA, M, N, K, 1.0, A + q * pa, lda, ta, B + q * pb, ldb, tb, 0.0, C + q * pc, h->ldP, tc, h->T,
+                  flags, &h->err, 0, n_off);
     if (s) return s;
   }
   return 0;
@@ -473,6 +475,13 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
           long long hs;
           int status;
         } hu{h, src, dst, 0, 0};
+        const bool pl = h->planar_cqr;
+        const long long ps = h->L * h->ldP, tsu = 6 * ps, tsp = 3 * ps, psx = (long long)h->N * h->ldP, tsx = 3 * psx;
+        if (pl) {   // U's (re, im, re + im) planes for the planar pieces, on the low-priority stream
+          CK(cudaStreamWaitEvent(h->st_lo, h->ev_fork, 0));
+          TRY(split_planes(h->st_lo, src, h->ldN, h->sU, h->L, h->N, h->T, h->Up + 3 * ps, h->ldP, ps, tsu, &h->err));
+          CK(cudaEventRecord(h->ev_split, h->st_lo));
+        }
         CholHook hook;
         hook.user = &hu;
         // each left-edge block adds the column piece [previous h, h): dst[:, a:b] = src[:, 0:b] X[0:b, a:b]
@@ -487,8 +496,18 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
             q->status = TRAJ_ECUDA;
             return;
           }
-          q->status = zgemm(hh->st_lo, 0, 0, hh->L, hs - a, hs, 1.0, 0.0, q->src, hh->ldN, hh->sU, hh->X + a, hh->ldN,
-                            hh->sG, 0.0, q->dst + a, hh->ldN, hh->sU, hh->T, TRAJ_TRI_B_UPPER_F, &hh->err, 0, a);
+          if (hh->planar_cqr) {
+            // planes of X[0:hs, a:hs], then the three real products into the same columns of Pp
+            const long long ps = hh->L * hh->ldP, tsu = 6 * ps, tsp = 3 * ps, psx = (long long)hh->N * hh->ldP;
+            q->status = split_planes(hh->st_lo, hh->X + a, hh->ldN, hh->sG, (int)hs, (int)(hs - a), hh->T, hh->Xp + a,
+                                     hh->ldP, psx, 3 * psx, &hh->err);
+            if (!q->status)
+              q->status = prod3(hh, 0, hh->L, hs - a, hs, hh->Up + 3 * ps, hh->ldP, ps, tsu, hh->Xp + a, hh->ldP, psx,
+                                3 * psx, hh->Pp + a, ps, tsp, DG_TRI_B_UPPER, hh->st_lo, a);
+          } else {
+            q->status = zgemm(hh->st_lo, 0, 0, hh->L, hs - a, hs, 1.0, 0.0, q->src, hh->ldN, hh->sU, hh->X + a, hh->ldN,
+                              hh->sG, 0.0, q->dst + a, hh->ldN, hh->sU, hh->T, TRAJ_TRI_B_UPPER_F, &hh->err, 0, a);
+          }
           if (!q->status && cudaEventRecord(hh->ev_lo_done, hh->st_lo) != cudaSuccess) q->status = TRAJ_ECUDA;
         };
         TRY(chol_inverse(h->st_hi, h->N, h->G, h->ldN, h->sG, h->X, h->ldN, h->sG, h->T, h->chol_scratch,
@@ -496,11 +515,20 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
         if (hu.status) return fail(h, hu.status, h->err.empty() ? "chol overlap: left TRMM" : h->err);
         if (hu.hs <= 0) return fail(h, TRAJ_ECUDA, "chol overlap: the left block was not reported");
         // dst[:, hs:N] = src X[:, hs:N] (triangle offset hs) on st_hi, then join both into st
-        TRY(zgemm(h->st_hi, 0, 0, h->L, h->N - hu.hs, h->N, 1.0, 0.0, src, h->ldN, h->sU, h->X + hu.hs, h->ldN, h->sG,
-                  0.0, dst + hu.hs, h->ldN, h->sU, h->T, TRAJ_TRI_B_UPPER_F, &h->err, 0, hu.hs));
+        if (pl) {
+          CK(cudaStreamWaitEvent(h->st_hi, h->ev_split, 0));   // U's planes (split on st_lo) are ready
+          TRY(split_planes(h->st_hi, h->X + hu.hs, h->ldN, h->sG, h->N, (int)(h->N - hu.hs), h->T, h->Xp + hu.hs,
+                           h->ldP, psx, tsx, &h->err));
+          TRY(prod3(h, 0, h->L, h->N - hu.hs, h->N, h->Up + 3 * ps, h->ldP, ps, tsu, h->Xp + hu.hs, h->ldP, psx, tsx,
+                    h->Pp + hu.hs, ps, tsp, DG_TRI_B_UPPER, h->st_hi, hu.hs));
+        } else {
+          TRY(zgemm(h->st_hi, 0, 0, h->L, h->N - hu.hs, h->N, 1.0, 0.0, src, h->ldN, h->sU, h->X + hu.hs, h->ldN, h->sG,
+                    0.0, dst + hu.hs, h->ldN, h->sU, h->T, TRAJ_TRI_B_UPPER_F, &h->err, 0, hu.hs));
+        }
         CK(cudaEventRecord(h->ev_hi_done, h->st_hi));
         CK(cudaStreamWaitEvent(h->st, h->ev_hi_done, 0));
         CK(cudaStreamWaitEvent(h->st, h->ev_lo_done, 0));
+        if (pl) TRY(combine_planes(h->st, h->Pp, h->ldP, ps, tsp, h->L, h->N, h->T, dst, h->ldN, h->sU, &h->err));
         std::swap(src, dst);
         continue;   // this pass's TRMM is done (its time is inside the Cholesky phase)
       }
@@ -1221,7 +1249,7 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
     if (h->chol_overlap && cudaDeviceGetStreamPriorityRange(&least, &greatest) == cudaSuccess &&
         cudaStreamCreateWithPriority(&h->st_hi, cudaStreamNonBlocking, greatest) == cudaSuccess &&
         cudaStreamCreateWithPriority(&h->st_lo, cudaStreamNonBlocking, least) == cudaSuccess) {
-      for (cudaEvent_t* e : {&h->ev_fork, &h->ev_left, &h->ev_lo_done, &h->ev_hi_done})
+      for (cudaEvent_t* e : {&h->ev_fork, &h->ev_left, &h->ev_lo_done, &h->ev_hi_done, &h->ev_split})
         if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) h->chol_overlap = false;
     } else {
       h->chol_overlap = false;
@@ -1579,7 +1607,7 @@ int traj_destroy(traj_handle h) {
       cudaStreamSynchronize(q);
       cudaStreamDestroy(q);
     }
-  for (cudaEvent_t e : {h->ev_fork, h->ev_left, h->ev_lo_done, h->ev_hi_done})
+  for (cudaEvent_t e : {h->ev_fork, h->ev_left, h->ev_lo_done, h->ev_hi_done, h->ev_split})
     if (e) cudaEventDestroy(e);
   if (h->solver) cusolverDnDestroy(h->solver);
   if (h->h_small) cudaFreeHost(h->h_small);
