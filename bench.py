@@ -216,21 +216,32 @@ def run_ours(args):
     else:
         ms_max = ms
     value = (1 if shard else world) * tpg * args.steps / (ms_max / 1e3)
-    # ---- roofline of the dominant kernel (the phase with the largest device time):
-    #   propagate (dense K U): 8 (L/P) L N flops, 1 launch per step
-    #   gram (G = U^dag U, upper tiles): 4 (L/P) N^2 per launch, 2 per step
-    #   trmm (U <- U R^-1): 4 (L/P) N^2 per launch, 2 per step
+    # ---- roofline of the dominant phase (the largest device time), per step:
+    #   propagate (dense K U): 8 (L/P) L N flops
+    #   gram (G = U^dag U, upper tiles): 4 (L/P) N^2 per measured Gram -- one per step for the
+    #     projective protocol (pass 1's Gram comes from the zeroed rows), two otherwise
+    #   trmm (U <- U R^-1): 4 (L/P) N^2 per TRMM counted in this phase -- the second pass only when
+    #     the first is overlapped with the Cholesky (its time is then in the chol phase)
     rows = w.L // world if shard else w.L
     algo = P.traj_get_zgemm_algorithm()
     kn = {"3m": ("zgemm3mw_dmma_kernel<0,0> (3M, 128x64 CTA)", "zgemm3m_dmma_kernel<1,0> (3M, 64x64 CTA)"),
           "4m": ("zgemm_dmma_kernel<0,0> (4M)", "zgemm_dmma_kernel<1,0> (4M)")}[algo]
     planar = (args.propagator == "dense" and not shard and os.environ.get("TRAJ_PLANAR_KU", "1") != "0"
               and w.protocol in ("projective", "homodyne"))
+    planar_cqr = not shard and os.environ.get("TRAJ_PLANAR_CQR", "1") != "0"
     ku_name = ("dgemm_dmma_kernel x3 (planar 3M: Kr Ur, Ki Ui, (Kr+Ki)(Ur+Ui); 128x128 CTA) + split/combine passes"
                if planar else kn[0])
-    kern = {"propagate": (8.0 * rows * w.L * w.N * tpg, f"{ku_name}: U <- K U (8 L^2 N flops)"),
-            "gram": (4.0 * rows * w.N * w.N * tpg, f"{kn[1]}: G = U^dag U upper tiles (4 L N^2)"),
-            "trmm": (4.0 * rows * w.N * w.N * tpg, f"{kn[0]} triangular: U <- U R^-1 (4 L N^2)")}
+    gram_name = ("dgemm_dmma_kernel<1> x3 (planar 3M: Ur^T Ur, Ui^T Ui, (Ur-Ui)^T (Ur+Ui); upper tiles) + split/combine"
+                 if planar_cqr else f"{kn[1]}: G = U^dag U upper tiles")
+    trmm_name = ("dgemm_dmma_kernel<0> x3 (planar 3M against X's planes, triangle skipped) + split/combine"
+                 if planar_cqr else f"{kn[0]} triangular")
+    n_gram = 1 if (w.protocol == "projective" and os.environ.get("TRAJ_LOWRANK_GRAM", "1") != "0") else 2
+    n_trmm = 1 if (not shard and os.environ.get("TRAJ_CHOL_OVERLAP", "1") != "0") else 2
+    kern = {"propagate": (8.0 * rows * w.L * w.N * tpg, f"{ku_name}: U <- K U (8 L^2 N flops per step)"),
+            "gram": (n_gram * 4.0 * rows * w.N * w.N * tpg,
+                     f"{gram_name}: {n_gram} measured Gram(s) per step, 4 L N^2 each"),
+            "trmm": (n_trmm * 4.0 * rows * w.N * w.N * tpg,
+                     f"{trmm_name}: U <- U R^-1, {n_trmm} TRMM(s) in this phase per step, 4 L N^2 each")}
     if args.propagator == "banded":
         kern.pop("propagate")
     lowrank_proj = args.orthonormalizer == "lowrank" and w.protocol == "projective" and not shard
@@ -243,10 +254,10 @@ def run_ours(args):
                             f"projective rank-k GEMMs ({kn[1].split(' ')[0].split('<')[0]} family): 16 L N (k1 + k0) "
                             f"flops per step, k1 + k0 = {k_sum} clicks in the last timed step; phase time includes "
                             "the blocked sampler and the Newton-Schulz iteration")}
-    pipe_per_alg = 0.75 if (algo == "3m" or planar) else 1.0      # DMMA flops per algorithmic 8mnk flop
+    pipe_per_alg = 0.75 if (algo == "3m" or planar or planar_cqr) else 1.0   # DMMA flops per 8mnk flop
     dom = max(kern, key=lambda k: phases[k][0])
-    launches_per_step = 1.0 if lowrank_proj or (planar and dom == "propagate") else max(1.0, phases[dom][1] / args.steps)
-    kern_ms = phases[dom][0] / args.steps / launches_per_step
+    launches_per_step = 1.0
+    kern_ms = phases[dom][0] / args.steps
     flops_launch = kern[dom][0]
     achieved = flops_launch / (kern_ms / 1e3) / 1e12
     prop_ms = phases["propagate"][0] / args.steps
@@ -343,8 +354,10 @@ def run_ours(args):
         "roofline": {"bound": "latency" if w.name == "c1" else "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                      "kernel": kern[dom][1] + ("; per shard (L/P rows) when row-sharded" if shard else ""),
-                     "kernel_ms": kern_ms, "peak_source": FP64_PEAK_SOURCE,
-                     "complex_mult": "planar 3m" if (planar and dom == "propagate") else algo,
+                     "kernel_ms": kern_ms, "timed": "device time of that phase per step (CUDA events around it on "
+                                                   "the handle's stream)", "peak_source": FP64_PEAK_SOURCE,
+                     "complex_mult": ("planar 3m" if (planar and dom == "propagate") or
+                                      (planar_cqr and dom in ("gram", "trmm")) else algo),
                      "pipe_tflops": achieved * pipe_per_alg, "pipe_frac": achieved * pipe_per_alg / FP64_PEAK_TFLOPS,
                      "traffic_note": ("ncu dram bytes of the propagate phase (profiles/ncu_traffic.json: split, three "
                                       "real 16384x8192x16384 products, combine) vs 8.6 GB algorithmic: each wave of "
