@@ -278,6 +278,8 @@ def run_ours(args):
             lc = json.load(open(lp))
             library = {"source": os.path.relpath(lp, ROOT) + " (tools/library_compare.py, same shapes, same box type)",
                        "K_U_ms": {k: round(v["ms"], 2) for k, v in lc["K_U"].items()},
+                       "K_U_note": "ours_planar_3x_dgemm is the three real products the propagator launches "
+                                   "(its split/combine passes add about 1.5 ms)",
                        "chol_inverse_ms": {k: round(v["ms"], 2) for k, v in lc["chol_inverse"].items()
                                            if isinstance(v, dict)}}
         except Exception:

@@ -2,7 +2,9 @@
 (iii) cuBLAS ZGEMM on the same shape").
 
 Times, with CUDA events on one stream after warm-up:
-  K U        (L x L) (L x N), row-major      : traj_zgemm  vs cublasZgemm / cublasZgemm3m
+  K U        (L x L) (L x N), row-major      : traj_zgemm (interleaved 3M) and traj_dgemm x3 (planar 3M,
+                                               the propagator's path) vs cublasZgemm / cublasZgemm3m /
+                                               cuBLAS Dgemm on the same three real products
   U^dag U    (N x L) (L x N) (full, no tri)  : traj_zgemm  vs cublasZgemm / cublasZgemm3m
   G = R^dag R, X = R^-1 (n = N)              : traj_chol_inverse vs cusolverDnZpotrf + cusolverDnXtrtri
 cuBLAS / cuSOLVER are column-major: a row-major C = A B is the column-major C^T = B^T A^T.
@@ -73,7 +75,7 @@ def main():
     # K U: column-major V^T (N x L) = U^T (N x L) K^T (L x L)
     f_ku = 8.0 * L * L * N
     ku = {
-        "ours": lambda: P.traj_zgemm(0, 0, K, U, V),
+        "ours_interleaved_zgemm3m": lambda: P.traj_zgemm(0, 0, K, U, V),
         "cublasZgemm": lambda: cub(cublas.cublasZgemm_v2, CUBLAS_OP_N, CUBLAS_OP_N, N, L, L, U, N, K, L, V, N),
         "cublasZgemm3m": lambda: cub(cublas.cublasZgemm3m, CUBLAS_OP_N, CUBLAS_OP_N, N, L, L, U, N, K, L, V, N),
     }
@@ -86,6 +88,31 @@ def main():
             ref = V.clone()
         err = (V - ref).abs().max().item() / ref.abs().max().item()
         res[name] = {"ms": ms, "tflops_8mnk": f_ku / ms / 1e9, "rel_diff_vs_ours": err}
+    # planar 3M: the three real products (Kr Ur, Ki Ui, (Kr+Ki)(Ur+Ui)) as one batch-3 traj_dgemm,
+    # the path the library's propagator takes; split/combine (2 x 0.8 ms at c3) timed with ours
+    Kp = torch.stack([K.real, K.imag, K.real + K.imag]).contiguous()
+    ldp = (N + 15) // 16 * 16
+    Up = torch.zeros(3, L, ldp, dtype=torch.float64, device=dev)
+    Up[0, :, :N], Up[1, :, :N], Up[2, :, :N] = U.real, U.imag, U.real + U.imag
+    Pp = torch.empty(3, L, ldp, dtype=torch.float64, device=dev)
+
+    def planar():
+        r = lib.traj_dgemm(st, L, N, L, 1.0, Kp.data_ptr(), L, L * L, Up.data_ptr(), ldp, L * ldp, 0.0,
+                           Pp.data_ptr(), ldp, L * ldp, 3)
+        assert r == 0, r
+
+    lib = P.lib()
+    ms = timed(planar, reps)
+    Vp = torch.complex(Pp[0, :, :N] - Pp[1, :, :N], Pp[2, :, :N] - Pp[0, :, :N] - Pp[1, :, :N])
+    err = (Vp - ref).abs().max().item() / ref.abs().max().item()
+    res["ours_planar_3x_dgemm"] = {"ms": ms, "tflops_8mnk": f_ku / ms / 1e9, "rel_diff_vs_ours": err,
+                                   "note": "three real 16384x8192x16384 products in one batch-3 launch; the "
+                                           "propagator adds a split and a combine pass (about 1.5 ms at c3)"}
+    Kr, Ur = Kp, Up[:, :, :N].contiguous()
+    Pr = torch.empty(3, L, N, dtype=torch.float64, device=dev)
+    ms = timed(lambda: torch.bmm(Kr, Ur, out=Pr), reps)
+    res["cublasDgemm_3_real_products"] = {"ms": ms, "tflops_8mnk": f_ku / ms / 1e9}
+    del Kp, Up, Pp, Vp, Kr, Ur, Pr
     out["K_U"] = res
     del ref
     # U^dag U (full N x N): column-major G^T (N x N) = U^T (N x L) conj(U) (L x N)
