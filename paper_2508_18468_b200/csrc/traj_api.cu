@@ -45,9 +45,9 @@ struct traj_ctx {
   double *Kp = nullptr, *Up = nullptr, *Pp = nullptr;
   long long ldK = 0, ldP = 0;
   // planar CholeskyQR (TRAJ_PLANAR_CQR=0: interleaved): measured Grams as three real U^T U-type
-  // products, TRMMs as three real products against X's planes (Xp).  Up holds 6 planes per
-  // trajectory, (re, im, re - im, re, im, re + im): planes 0..2 and 3..5 are constant-stride
-  // triples, so with one trajectory each group of three products is a single batched launch
+  // products, TRMMs as three real products against X's planes (Xp).  Up holds 6 planes, (re, im,
+  // re - im, re, im, re + im), plane-major [plane][T][L][ldP]: planes 0..2 and 3..5 are
+  // constant-stride triples over all trajectories, so each group of three products is one launch
   bool planar_cqr = false;
   double* Xp = nullptr;
   std::vector<cplx> band_host;     // the same on the host: passed by value to the stencil launches
@@ -255,10 +255,11 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
   h->banded = banded_widths(c, &h->Wx, &h->Wy);
   {
     const char* pk = getenv("TRAJ_PLANAR_KU");
+    // below N = 512 the split / combine passes and the 128 x 128 tiles cost more than they save
     h->planar = !h->banded && c->protocol != TRAJ_HOMODYNE_RK4 && c->protocol != TRAJ_PROJECTIVE_EVENTS &&
-                !(pk && pk[0] == '0');
+                !(pk && pk[0] == '0') && N >= 512;
     const char* pc = getenv("TRAJ_PLANAR_CQR");
-    h->planar_cqr = !(pc && pc[0] == '0');
+    h->planar_cqr = !(pc && pc[0] == '0') && N >= 512;
   }
   if (c->protocol == TRAJ_HOMODYNE_RK4) {     // stencil generator: no K
     h->banded = false;
@@ -384,21 +385,14 @@ std::vector<std::complex<double>> ring_coefficients(int n, double J, double dt) 
 // Pass 2 sees G2 = I + E with |E| ~ kappa(U)^2 eps: its Cholesky inverse is taken from the
 // first-order closed form (exact up to N |E|^2, below rounding when N max|E|^2 < 1e-18,
 // checked on the device per step); otherwise, or with TRAJ_CQR2_FULL=1, chol_inverse.
-// Three real products C_q = op(A_q) B_q (q = 0, 1, 2) whose operands are plane triples at constant
-// strides (pa, pb, pc) within each trajectory (strides ta, tb, tc between trajectories): one
-// batch-3 launch for a single trajectory (fewer partial waves), else one launch per product.
-int prod3(traj_ctx* h, int opA, long long M, long long N, long long K, const double* A, long long lda, long long pa,
-          long long ta, const double* B, long long ldb, long long pb, long long tb, double* C, long long pc,
-          long long tc, int flags, cudaStream_t st = nullptr, long long n_off = 0) {
-  if (!st) st = h->st;
-  if (h->T == 1)
-    return dgemm(st, opA, M, N, K, 1.0, A, lda, pa, B, ldb, pb, 0.0, C, h->ldP, pc, 3, flags, &h->err, 0, n_off);
-  for (int q = 0; q < 3; ++q) {
-    int s = dgemm(st, opA, M, N, K, 1.0, A + q * pa, lda, ta, B + q * pb, ldb, tb, 0.0, C + q * pc, h->ldP, tc, h->T,
-                  flags, &h->err, 0, n_off);
-    if (s) return s;
-  }
-  return 0;
+// Planes are stored plane-major, [plane][trajectory][rows][ldP], so a triple of planes over all
+// trajectories sits at one constant stride: three real products C_q = op(A_q) B_q for every
+// trajectory are a single batched launch of 3T entries (entry z = q T + t at z * stride).
+int prod3(traj_ctx* h, int opA, long long M, long long N, long long K, const double* A, long long lda, long long sA,
+          const double* B, long long ldb, long long sB, double* C, long long sC, int flags, cudaStream_t st = nullptr,
+          long long n_off = 0) {
+  return dgemm(st ? st : h->st, opA, M, N, K, 1.0, A, lda, sA, B, ldb, sB, 0.0, C, h->ldP, sC, 3LL * h->T, flags,
+               &h->err, 0, n_off);
 }
 
 int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
@@ -438,11 +432,10 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
       } else if (h->planar_cqr) {
         // G = U^dag U = (P1 + Q2) + i (P3 - P1 + Q2): P1 = Ur^T Ur, Q2 = Ui^T Ui, P3 = (Ur - Ui)^T (Ur + Ui),
         // A triple = planes 0..2, B triple = planes 3..5
-        const long long ps = h->L * h->ldP, tsu = 6 * ps, tsp = 3 * ps;
-        TRY(split6_planes(h->st, src, h->ldN, h->sU, h->L, h->N, h->T, h->Up, h->ldP, ps, tsu, &h->err));
-        TRY(prod3(h, 1, h->N, h->N, h->L, h->Up, h->ldP, ps, tsu, h->Up + 3 * ps, h->ldP, ps, tsu, h->Pp, ps, tsp,
-                  DG_C_UPPER));
-        TRY(combine_gram(h->st, h->Pp, h->ldP, ps, tsp, h->N, h->T, h->G, h->ldN, h->sG, &h->err));
+        const long long tU = h->L * h->ldP, pU = h->T * tU;
+        TRY(split6_planes(h->st, src, h->ldN, h->sU, h->L, h->N, h->T, h->Up, h->ldP, pU, tU, &h->err));
+        TRY(prod3(h, 1, h->N, h->N, h->L, h->Up, h->ldP, tU, h->Up + 3 * pU, h->ldP, tU, h->Pp, tU, DG_C_UPPER));
+        TRY(combine_gram(h->st, h->Pp, h->ldP, pU, tU, h->N, h->T, h->G, h->ldN, h->sG, &h->err));
         planes_of = src;
       } else {
         TRY(zgemm(h->st, 1, 0, h->N, h->N, h->L, 1.0, 0.0, src, h->ldN, h->sU, src, h->ldN, h->sU, 0.0, h->G,
@@ -476,10 +469,10 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
           int status;
         } hu{h, src, dst, 0, 0};
         const bool pl = h->planar_cqr;
-        const long long ps = h->L * h->ldP, tsu = 6 * ps, tsp = 3 * ps, psx = (long long)h->N * h->ldP, tsx = 3 * psx;
+        const long long tU = h->L * h->ldP, pU = h->T * tU, tX = (long long)h->N * h->ldP, pX = h->T * tX;
         if (pl) {   // U's (re, im, re + im) planes for the planar pieces, on the low-priority stream
           CK(cudaStreamWaitEvent(h->st_lo, h->ev_fork, 0));
-          TRY(split_planes(h->st_lo, src, h->ldN, h->sU, h->L, h->N, h->T, h->Up + 3 * ps, h->ldP, ps, tsu, &h->err));
+          TRY(split_planes(h->st_lo, src, h->ldN, h->sU, h->L, h->N, h->T, h->Up + 3 * pU, h->ldP, pU, tU, &h->err));
           CK(cudaEventRecord(h->ev_split, h->st_lo));
         }
         CholHook hook;
@@ -498,12 +491,12 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
           }
           if (hh->planar_cqr) {
             // planes of X[0:hs, a:hs], then the three real products into the same columns of Pp
-            const long long ps = hh->L * hh->ldP, tsu = 6 * ps, tsp = 3 * ps, psx = (long long)hh->N * hh->ldP;
+            const long long tU = hh->L * hh->ldP, pU = hh->T * tU, tX = (long long)hh->N * hh->ldP, pX = hh->T * tX;
             q->status = split_planes(hh->st_lo, hh->X + a, hh->ldN, hh->sG, (int)hs, (int)(hs - a), hh->T, hh->Xp + a,
-                                     hh->ldP, psx, 3 * psx, &hh->err);
+                                     hh->ldP, pX, tX, &hh->err);
             if (!q->status)
-              q->status = prod3(hh, 0, hh->L, hs - a, hs, hh->Up + 3 * ps, hh->ldP, ps, tsu, hh->Xp + a, hh->ldP, psx,
-                                3 * psx, hh->Pp + a, ps, tsp, DG_TRI_B_UPPER, hh->st_lo, a);
+              q->status = prod3(hh, 0, hh->L, hs - a, hs, hh->Up + 3 * pU, hh->ldP, tU, hh->Xp + a, hh->ldP, tX,
+                                hh->Pp + a, tU, DG_TRI_B_UPPER, hh->st_lo, a);
           } else {
             q->status = zgemm(hh->st_lo, 0, 0, hh->L, hs - a, hs, 1.0, 0.0, q->src, hh->ldN, hh->sU, hh->X + a, hh->ldN,
                               hh->sG, 0.0, q->dst + a, hh->ldN, hh->sU, hh->T, TRAJ_TRI_B_UPPER_F, &hh->err, 0, a);
@@ -518,9 +511,9 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
         if (pl) {
           CK(cudaStreamWaitEvent(h->st_hi, h->ev_split, 0));   // U's planes (split on st_lo) are ready
           TRY(split_planes(h->st_hi, h->X + hu.hs, h->ldN, h->sG, h->N, (int)(h->N - hu.hs), h->T, h->Xp + hu.hs,
-                           h->ldP, psx, tsx, &h->err));
-          TRY(prod3(h, 0, h->L, h->N - hu.hs, h->N, h->Up + 3 * ps, h->ldP, ps, tsu, h->Xp + hu.hs, h->ldP, psx, tsx,
-                    h->Pp + hu.hs, ps, tsp, DG_TRI_B_UPPER, h->st_hi, hu.hs));
+                           h->ldP, pX, tX, &h->err));
+          TRY(prod3(h, 0, h->L, h->N - hu.hs, h->N, h->Up + 3 * pU, h->ldP, tU, h->Xp + hu.hs, h->ldP, tX,
+                    h->Pp + hu.hs, tU, DG_TRI_B_UPPER, h->st_hi, hu.hs));
         } else {
           TRY(zgemm(h->st_hi, 0, 0, h->L, h->N - hu.hs, h->N, 1.0, 0.0, src, h->ldN, h->sU, h->X + hu.hs, h->ldN, h->sG,
                     0.0, dst + hu.hs, h->ldN, h->sU, h->T, TRAJ_TRI_B_UPPER_F, &h->err, 0, hu.hs));
@@ -528,7 +521,7 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
         CK(cudaEventRecord(h->ev_hi_done, h->st_hi));
         CK(cudaStreamWaitEvent(h->st, h->ev_hi_done, 0));
         CK(cudaStreamWaitEvent(h->st, h->ev_lo_done, 0));
-        if (pl) TRY(combine_planes(h->st, h->Pp, h->ldP, ps, tsp, h->L, h->N, h->T, dst, h->ldN, h->sU, &h->err));
+        if (pl) TRY(combine_planes(h->st, h->Pp, h->ldP, pU, tU, h->L, h->N, h->T, dst, h->ldN, h->sU, &h->err));
         std::swap(src, dst);
         continue;   // this pass's TRMM is done (its time is inside the Cholesky phase)
       }
@@ -544,11 +537,10 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
       if (h->planar_cqr && planes_of == src) {
         // U X = (P1 - P2) + i (P3 - P1 - P2): P1 = Ur Xr, P2 = Ui Xi, P3 = (Ur + Ui)(Xr + Xi) on the
         // Gram's planes of U and X's planes (X upper triangular: k-blocks past the diagonal skipped)
-        const long long ps = h->L * h->ldP, tsu = 6 * ps, tsp = 3 * ps, psx = (long long)h->N * h->ldP, tsx = 3 * psx;
-        TRY(split_planes(h->st, h->X, h->ldN, h->sG, h->N, h->N, h->T, h->Xp, h->ldP, psx, tsx, &h->err));
-        TRY(prod3(h, 0, h->L, h->N, h->N, h->Up + 3 * ps, h->ldP, ps, tsu, h->Xp, h->ldP, psx, tsx, h->Pp, ps, tsp,
-                  DG_TRI_B_UPPER));
-        TRY(combine_planes(h->st, h->Pp, h->ldP, ps, tsp, h->L, h->N, h->T, dst, h->ldN, h->sU, &h->err));
+        const long long tU = h->L * h->ldP, pU = h->T * tU, tX = (long long)h->N * h->ldP, pX = h->T * tX;
+        TRY(split_planes(h->st, h->X, h->ldN, h->sG, h->N, h->N, h->T, h->Xp, h->ldP, pX, tX, &h->err));
+        TRY(prod3(h, 0, h->L, h->N, h->N, h->Up + 3 * pU, h->ldP, tU, h->Xp, h->ldP, tX, h->Pp, tU, DG_TRI_B_UPPER));
+        TRY(combine_planes(h->st, h->Pp, h->ldP, pU, tU, h->L, h->N, h->T, dst, h->ldN, h->sU, &h->err));
       } else {
         TRY(zgemm(h->st, 0, 0, h->L, h->N, h->N, 1.0, 0.0, src, h->ldN, h->sU, h->X, h->ldN, h->sG, 0.0, dst, h->ldN,
                   h->sU, h->T, TRAJ_TRI_B_UPPER_F, &h->err));
@@ -1002,11 +994,17 @@ int one_step(traj_ctx* h) {
       // U <- K U  (K shared across the batch: stride 0)
       if (h->planar) {
         // three real products on planes, then (P1 - P2) + i (P3 - P1 - P2)
-        const long long ps = h->L * h->ldP, tsu = 6 * ps, tsp = 3 * ps;
-        TRY(split_planes(h->st, Uc, h->ldN, h->sU, h->L, h->N, h->T, h->Up + 3 * ps, h->ldP, ps, tsu, &h->err));
-        TRY(prod3(h, 0, h->L, h->N, h->L, h->Kp, h->ldK, h->L * h->ldK, 0, h->Up + 3 * ps, h->ldP, ps, tsu, h->Pp, ps,
-                  tsp, 0));
-        TRY(combine_planes(h->st, h->Pp, h->ldP, ps, tsp, h->L, h->N, h->T, Un, h->ldN, h->sU, &h->err));
+        const long long tU = h->L * h->ldP, pU = h->T * tU, pK = h->L * h->ldK;
+        TRY(split_planes(h->st, Uc, h->ldN, h->sU, h->L, h->N, h->T, h->Up + 3 * pU, h->ldP, pU, tU, &h->err));
+        if (h->T == 1) {   // one batch-3 launch: A = K's planes, B = U's
+          TRY(dgemm(h->st, 0, h->L, h->N, h->L, 1.0, h->Kp, h->ldK, pK, h->Up + 3 * pU, h->ldP, tU, 0.0, h->Pp,
+                    h->ldP, tU, 3, 0, &h->err));
+        } else {           // K's plane q is shared by the T trajectories of product q
+          for (int q = 0; q < 3; ++q)
+            TRY(dgemm(h->st, 0, h->L, h->N, h->L, 1.0, h->Kp + q * pK, h->ldK, 0, h->Up + (3 + q) * pU, h->ldP, tU, 0.0,
+                      h->Pp + q * pU, h->ldP, tU, h->T, 0, &h->err));
+        }
+        TRY(combine_planes(h->st, h->Pp, h->ldP, pU, tU, h->L, h->N, h->T, Un, h->ldN, h->sU, &h->err));
       } else {
         TRY(zgemm(h->st, 0, 0, h->L, h->N, h->L, 1.0, 0.0, h->K, h->ldL, 0, Uc, h->ldN, h->sU, 0.0, Un, h->ldN, h->sU,
                 h->T, 0, &h->err));
