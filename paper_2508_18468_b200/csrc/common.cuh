@@ -5,6 +5,9 @@
 #include <stdint.h>
 #include <string>
 #include <atomic>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "libtraj targets sm_100a only"
@@ -17,6 +20,20 @@ typedef double2 cplx;   // (re, im), interleaved complex128
 // Every kernel launch of the library increments this (the bench's gpu_launches claim).
 extern std::atomic<long long> g_kernel_launches;
 inline void count_launch(long long n = 1) { g_kernel_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// The dynamic shared-memory limit of a kernel, raised once per (kernel, device); thread-safe.
+inline cudaError_t ensure_smem(const void* kernel, int bytes) {
+  static std::mutex m;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(m);
+  if (done.count({kernel, dev})) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({kernel, dev});
+  return e;
+}
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -252,15 +252,12 @@ int dgemm(cudaStream_t st, int opA, long long M, long long N, long long K, doubl
   args.C = C;
   args.ldc = ldc;
   args.strideC = strideC;
-  static bool attr[2] = {false, false};
-  if (!attr[opA]) {
-    cudaError_t e = opA ? cudaFuncSetAttribute(dgemm_dmma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DSMEM)
-                        : cudaFuncSetAttribute(dgemm_dmma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DSMEM);
-    if (e != cudaSuccess) {
+  {
+    const void* kern = opA ? (const void*)dgemm_dmma_kernel<true> : (const void*)dgemm_dmma_kernel<false>;
+    if (ensure_smem(kern, DSMEM) != cudaSuccess) {
       if (err) *err = "dgemm: shared memory attribute";
       return 4;
     }
-    attr[opA] = true;
   }
   dim3 grid((unsigned)(args.tiles_m * args.tiles_n), 1, (unsigned)batch);
   if (opA) dgemm_dmma_kernel<true><<<grid, DTHREADS, DSMEM, st>>>(ma, mb, args);

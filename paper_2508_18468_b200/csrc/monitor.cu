@@ -507,12 +507,8 @@ int sample_outcomes(cudaStream_t st, const cplx* D0, cplx* Dw, long long ldd, lo
     if (err) *err = "sample: copy";
     return 4;
   }
-  static bool attr = false;
   const int smem = 2 * PB * PLD * (int)sizeof(double2);
-  if (!attr) {
-    cudaFuncSetAttribute(panel_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  ensure_smem((const void*)panel_sample_kernel, smem);
   for (int s0 = 0; s0 < maxc; s0 += PB) {
     panel_sample_kernel<<<T, 256, smem, st>>>(Dw, ldd, sD, S, cap, count, s0, step, traj_base, key0, key1, occ, Linv,
                                               DLinv);

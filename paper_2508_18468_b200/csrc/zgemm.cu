@@ -678,12 +678,9 @@ bool make_map_4d(CUtensorMap* map, const void* base, long long rows, long long c
 
 template <bool CA, bool CB>
 cudaError_t launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const Args& args, int batch) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(zgemm_dmma_kernel<CA, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         SMEM_BYTES);
+  {
+    cudaError_t e = ensure_smem((const void*)zgemm_dmma_kernel<CA, CB>, SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   dim3 grid(args.tiles_m * args.tiles_n, 1, batch);
   zgemm_dmma_kernel<CA, CB><<<grid, THREADS, SMEM_BYTES, st>>>(a, b, args);
@@ -693,12 +690,9 @@ cudaError_t launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, 
 
 template <bool CA, bool CB>
 cudaError_t launch3m(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const Args& args, int batch) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(zgemm3m_dmma_kernel<CA, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         g3::SMEM_BYTES);
+  {
+    cudaError_t e = ensure_smem((const void*)zgemm3m_dmma_kernel<CA, CB>, g3::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   dim3 grid(args.tiles_m * args.tiles_n, 1, batch);
   zgemm3m_dmma_kernel<CA, CB><<<grid, THREADS, g3::SMEM_BYTES, st>>>(a, b, args);
@@ -708,12 +702,9 @@ cudaError_t launch3m(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b
 
 template <bool CA, bool CB>
 cudaError_t launch3mw(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const Args& args, int batch) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(zgemm3mw_dmma_kernel<CA, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         g3w::SMEM_BYTES);
+  {
+    cudaError_t e = ensure_smem((const void*)zgemm3mw_dmma_kernel<CA, CB>, g3w::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   dim3 grid(args.tiles_m * args.tiles_n, 1, batch);
   zgemm3mw_dmma_kernel<CA, CB><<<grid, THREADS, g3w::SMEM_BYTES, st>>>(a, b, args);
