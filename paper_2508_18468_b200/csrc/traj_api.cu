@@ -256,10 +256,13 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
   {
     const char* pk = getenv("TRAJ_PLANAR_KU");
     // below N = 512 the split / combine passes and the 128 x 128 tiles cost more than they save
+    // (TRAJ_PLANAR_MIN_N overrides the threshold, e.g. for small parity tests)
+    const char* mn = getenv("TRAJ_PLANAR_MIN_N");
+    const long long min_n = mn ? atoll(mn) : 512;
     h->planar = !h->banded && c->protocol != TRAJ_HOMODYNE_RK4 && c->protocol != TRAJ_PROJECTIVE_EVENTS &&
-                !(pk && pk[0] == '0') && N >= 512;
+                !(pk && pk[0] == '0') && N >= min_n;
     const char* pc = getenv("TRAJ_PLANAR_CQR");
-    h->planar_cqr = !(pc && pc[0] == '0') && N >= 512;
+    h->planar_cqr = !(pc && pc[0] == '0') && N >= min_n;
   }
   if (c->protocol == TRAJ_HOMODYNE_RK4) {     // stencil generator: no K
     h->banded = false;

@@ -310,26 +310,33 @@ def test_row_sharded_distributed_cholesky_matches_replicated(P, P_shards, monkey
     b.close()
 
 
-@pytest.mark.parametrize("Lx,Ly,protocol", [(300, 1, "projective"), (12, 10, "homodyne")])
-def test_planar_propagator_matches_interleaved(P, Lx, Ly, protocol, monkeypatch):
-    """The dense propagator as three real planar products (TRAJ_PLANAR_KU, the default) against
-    the interleaved complex 3M GEMM and the oracle, same trajectory."""
-    gam = [2.0] if protocol == "projective" else [1.0]
+@pytest.mark.parametrize("Lx,Ly,protocol,gams", [(300, 1, "projective", [2.0]), (12, 10, "homodyne", [1.0, 3.0]),
+                                                  (260, 1, "projective", [1.0, 2.5, 0.3])])
+def test_planar_propagator_matches_interleaved(P, Lx, Ly, protocol, gams, monkeypatch):
+    """The planar 3M paths (K U as three real products; CholeskyQR's Grams and TRMMs likewise, with
+    the plane-major batching of several trajectories) against the interleaved complex 3M kernels
+    and the oracle, same trajectories.  TRAJ_PLANAR_MIN_N=0 turns the planar paths on at these
+    small sizes."""
+    monkeypatch.setenv("TRAJ_PLANAR_MIN_N", "0")
     monkeypatch.setenv("TRAJ_PLANAR_KU", "0")
-    a = P.Trajectories(Lx, Ly, protocol, gam, seed=41)
+    monkeypatch.setenv("TRAJ_PLANAR_CQR", "0")
+    a = P.Trajectories(Lx, Ly, protocol, gams, seed=41)
     monkeypatch.setenv("TRAJ_PLANAR_KU", "1")
-    b = P.Trajectories(Lx, Ly, protocol, gam, seed=41)
+    monkeypatch.setenv("TRAJ_PLANAR_CQR", "1")
+    b = P.Trajectories(Lx, Ly, protocol, gams, seed=41)
     K = lattice.propagator_lattice(Lx, Ly, 1.0, 0.05)
-    o = OracleTrajectory(Lx, Ly, protocol, gam[0], 0.05, seed=41, traj=0, K=K)
+    orc = [OracleTrajectory(Lx, Ly, protocol, g, 0.05, seed=41, traj=t, K=K) for t, g in enumerate(gams)]
     for s in range(12):
         a.step(1)
         b.step(1)
-        o.step(1)
-        if protocol == "projective":
-            assert a.last_clicks(0) == b.last_clicks(0)
-    ca, cb = a.correlation(0).cpu().numpy(), b.correlation(0).cpu().numpy()
-    assert np.abs(ca - cb).max() < 1e-12
-    assert np.abs(cb - o.correlation()).max() < C_TOL
+        for t, o in enumerate(orc):
+            o.step(1)
+            if protocol == "projective":
+                assert a.last_clicks(t) == b.last_clicks(t)
+    for t, o in enumerate(orc):
+        ca, cb = a.correlation(t).cpu().numpy(), b.correlation(t).cpu().numpy()
+        assert np.abs(ca - cb).max() < 1e-12
+        assert np.abs(cb - o.correlation()).max() < C_TOL
     a.close()
     b.close()
 
