@@ -18,15 +18,15 @@ __device__ __forceinline__ double2 cmul2(double2 a, double2 b) {
 
 // K[i][j] = kx[(jx - ix) mod Lx] ky[(jy - iy) mod Ly]; planes (re, im, re + im)
 __global__ void build_k_planar_kernel(double* Kp, long long ld, long long ps, int Lx, int Ly, const cplx* kx,
-                                      const cplx* ky) {
+                                      const cplx* ky, long long row0, long long nrows) {
   const long long L = (long long)Lx * Ly;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < L * L;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < nrows * L;
        idx += (long long)gridDim.x * blockDim.x) {
-    const long long i = idx / L, j = idx % L;
+    const long long r = idx / L, j = idx % L, i = row0 + r;
     const int ix = (int)(i % Lx), iy = (int)(i / Lx), jx = (int)(j % Lx), jy = (int)(j / Lx);
     const int dx = ((jx - ix) % Lx + Lx) % Lx, dy = ((jy - iy) % Ly + Ly) % Ly;
     const double2 v = cmul2(kx[dx], ky[dy]);
-    const long long o = i * ld + j;
+    const long long o = r * ld + j;
     Kp[o] = v.x;
     Kp[ps + o] = v.y;
     Kp[2 * ps + o] = v.x + v.y;
@@ -122,10 +122,11 @@ int combine_gram(cudaStream_t st, const double* Pl, long long ldp, long long ps,
 }
 
 int build_k_planar(cudaStream_t st, double* Kp, long long ld, long long ps, int Lx, int Ly, const cplx* kx,
-                   const cplx* ky, std::string* err) {
+                   const cplx* ky, std::string* err, long long row0, long long nrows) {
   const long long L = (long long)Lx * Ly;
-  build_k_planar_kernel<<<(unsigned)std::min<long long>(ceil_div(L * L, 256), 148 * 64), 256, 0, st>>>(Kp, ld, ps, Lx,
-                                                                                                       Ly, kx, ky);
+  if (nrows < 0) nrows = L;
+  build_k_planar_kernel<<<(unsigned)std::min<long long>(ceil_div(nrows * L, 256), 148 * 64), 256, 0, st>>>(
+      Kp, ld, ps, Lx, Ly, kx, ky, row0, nrows);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess && err) *err = std::string("build_k_planar: ") + cudaGetErrorString(e);

@@ -7,9 +7,10 @@
 
 namespace traj {
 
-// Kp planes [3][L][ld] (plane stride ps) of K = kx (x) ky (Lx*Ly sites, row-major site = y Lx + x)
+// Kp planes [3][nrows][ld] (plane stride ps) of rows [row0, row0 + nrows) of K = kx (x) ky (Lx*Ly
+// sites, row-major site = y Lx + x); nrows < 0: all L rows
 int build_k_planar(cudaStream_t st, double* Kp, long long ld, long long ps, int Lx, int Ly, const cplx* kx,
-                   const cplx* ky, std::string* err);
+                   const cplx* ky, std::string* err, long long row0 = 0, long long nrows = -1);
 // Pl[t][p][row][col] (plane stride ps, trajectory stride ts) = (re, im, re + im)[p] of U[t][row][col]
 int split_planes(cudaStream_t st, const cplx* U, long long ldu, long long sU, int L, int N, int T, double* Pl,
                  long long ldp, long long ps, long long ts, std::string* err);

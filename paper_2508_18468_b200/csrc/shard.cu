@@ -22,6 +22,8 @@
 #include "shard.h"
 #include "zgemm.h"
 #include "banded.h"
+#include "dgemm.h"
+#include "planar.h"
 
 namespace traj {
 
@@ -212,6 +214,15 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
   sh->H = banded ? (c->Ly > 1 ? Wy * (int)c->Lx : Wx) : 0;
   const long long Lp = sh->Lp, ldN = sh->ldN, ldL = sh->ldL, ldcap = sh->ldcap;
   const int capr = sh->capr, cap = sh->cap;
+  {
+    const char* pk = getenv("TRAJ_PLANAR_KU");
+    const char* pc = getenv("TRAJ_PLANAR_CQR");
+    const char* mn = getenv("TRAJ_PLANAR_MIN_N");
+    const long long min_n = mn ? atoll(mn) : 512;
+    sh->planar = !banded && !(pk && pk[0] == '0') && !(pc && pc[0] == '0') && N >= min_n;
+    sh->ldKs = round_up(L, 16);
+    sh->ldPs = round_up(N, 16);
+  }
   sh->loc.assign(sh->comm.P_local, ShardLocal());
   lay.take(sh->Ufull, (size_t)L * ldN * 16);
   lay.take(sh->G, (size_t)N * ldN * 16);
@@ -221,8 +232,15 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
     ShardLocal& l = sh->loc[s];
     l.g = sh->comm.rank0 + s;
     l.row0 = (int)(l.g * Lp);
-    if (banded) lay.take(l.Uext, (size_t)(Lp + 2 * sh->H) * ldN * 16);
-    else lay.take(l.K, (size_t)Lp * ldL * 16);
+    if (banded) {
+      lay.take(l.Uext, (size_t)(Lp + 2 * sh->H) * ldN * 16);
+    } else if (sh->planar) {
+      lay.take(l.Kp, (size_t)3 * Lp * sh->ldKs * 8);
+      lay.take(l.Pp, (size_t)3 * Lp * sh->ldPs * 8);
+      lay.take(l.Up6, (size_t)6 * Lp * sh->ldPs * 8);
+    } else {
+      lay.take(l.K, (size_t)Lp * ldL * 16);
+    }
     lay.take(l.U[0], (size_t)Lp * ldN * 16);
     lay.take(l.U[1], (size_t)Lp * ldN * 16);
     if (emulate) lay.take(l.Gpart, (size_t)N * ldN * 16);
@@ -236,6 +254,11 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
     }
   }
   if (banded) lay.take(sh->bcoef, (size_t)(2 * Wx + 2 * Wy + 2) * 16);
+  if (sh->planar) {
+    lay.take(sh->Cp, (size_t)3 * Lp * sh->ldPs * 8);
+    lay.take(sh->Gp, (size_t)3 * N * sh->ldPs * 8);
+    lay.take(sh->Xp, (size_t)3 * N * sh->ldPs * 8);
+  }
   if (c->nccl_id && sh->P > 1) {   // distributed Cholesky: the largest shared block, (N/2 + 128)^2
     const long long hb = (long long)sh->N / 2 + 128;
     sh->dist_scratch_bytes = (size_t)(hb * hb * 16);
@@ -374,8 +397,14 @@ int shard_build(ShardedCtx* sh, const std::vector<std::complex<double>>& kc, con
   SCK(cudaMemcpyAsync(sh->sites, sites.data(), sites.size() * 4, cudaMemcpyHostToDevice, st));
   SCK(cudaMemcpyAsync(sh->gamma_dev, &sh->gamma, 8, cudaMemcpyHostToDevice, st));
   for (auto& l : sh->loc) {
-    if (!sh->banded && build_k(st, l.K, sh->ldL, sh->Lx, sh->Ly, sh->kcoef, sh->kcoef + sh->Lx, err, l.row0, sh->Lp))
+    if (sh->planar) {
+      if (build_k_planar(st, l.Kp, sh->ldKs, (long long)sh->Lp * sh->ldKs, sh->Lx, sh->Ly, sh->kcoef,
+                         sh->kcoef + sh->Lx, err, l.row0, sh->Lp))
+        return 4;
+    } else if (!sh->banded &&
+               build_k(st, l.K, sh->ldL, sh->Lx, sh->Ly, sh->kcoef, sh->kcoef + sh->Lx, err, l.row0, sh->Lp)) {
       return 4;
+    }
     if (init_state(st, l.U[0], sh->ldN, 0, sh->sites, sh->N, 1, err, l.row0, sh->Lp)) return 4;
   }
   SCK(cudaStreamSynchronize(st));
@@ -402,9 +431,19 @@ int cqr2(ShardedCtx* sh, int src_which, std::string* err) {
   for (int pass = 0; pass < 2; ++pass) {
     {
       Phase p(sh->prof, sh->st, TRAJ_PH_GRAM);
-      for (auto& l : sh->loc)
-        STRY(zgemm(sh->st, 1, 0, sh->N, sh->N, sh->Lp, 1.0, 0.0, l.U[src], sh->ldN, 0, l.U[src], sh->ldN, 0, 0.0,
-                   l.Gpart, sh->ldN, 0, 1, TRAJ_C_UPPER_F, err));
+      for (auto& l : sh->loc) {
+        if (sh->planar) {
+          // local G_g = U_g^dag U_g as three real products (planes re, im, re - im | re, im, re + im)
+          const long long psU = (long long)sh->Lp * sh->ldPs, psG = (long long)sh->N * sh->ldPs;
+          STRY(split6_planes(sh->st, l.U[src], sh->ldN, 0, sh->Lp, sh->N, 1, l.Up6, sh->ldPs, psU, 0, err));
+          STRY(dgemm(sh->st, 1, sh->N, sh->N, sh->Lp, 1.0, l.Up6, sh->ldPs, psU, l.Up6 + 3 * psU, sh->ldPs, psU, 0.0,
+                     sh->Gp, sh->ldPs, psG, 3, DG_C_UPPER, err));
+          STRY(combine_gram(sh->st, sh->Gp, sh->ldPs, psG, 0, sh->N, 1, l.Gpart, sh->ldN, 0, err));
+        } else {
+          STRY(zgemm(sh->st, 1, 0, sh->N, sh->N, sh->Lp, 1.0, 0.0, l.U[src], sh->ldN, 0, l.U[src], sh->ldN, 0, 0.0,
+                     l.Gpart, sh->ldN, 0, 1, TRAJ_C_UPPER_F, err));
+        }
+      }
       STRY(allreduce_gram(sh, err));
     }
     {
@@ -425,9 +464,20 @@ int cqr2(ShardedCtx* sh, int src_which, std::string* err) {
     }
     {
       Phase p(sh->prof, sh->st, TRAJ_PH_TRMM);
-      for (auto& l : sh->loc)
-        STRY(zgemm(sh->st, 0, 0, sh->Lp, sh->N, sh->N, 1.0, 0.0, l.U[src], sh->ldN, 0, sh->X, sh->ldN, 0, 0.0,
-                   l.U[1 - src], sh->ldN, 0, 1, TRAJ_TRI_B_UPPER_F, err));
+      if (sh->planar) {
+        // U_g X as three real products on the Gram's planes of U_g and X's planes
+        const long long psU = (long long)sh->Lp * sh->ldPs, psX = (long long)sh->N * sh->ldPs;
+        STRY(split_planes(sh->st, sh->X, sh->ldN, 0, sh->N, sh->N, 1, sh->Xp, sh->ldPs, psX, 0, err));
+        for (auto& l : sh->loc) {
+          STRY(dgemm(sh->st, 0, sh->Lp, sh->N, sh->N, 1.0, l.Up6 + 3 * psU, sh->ldPs, psU, sh->Xp, sh->ldPs, psX, 0.0,
+                     l.Pp, sh->ldPs, psU, 3, DG_TRI_B_UPPER, err));
+          STRY(combine_planes(sh->st, l.Pp, sh->ldPs, psU, 0, sh->Lp, sh->N, 1, l.U[1 - src], sh->ldN, 0, err));
+        }
+      } else {
+        for (auto& l : sh->loc)
+          STRY(zgemm(sh->st, 0, 0, sh->Lp, sh->N, sh->N, 1.0, 0.0, l.U[src], sh->ldN, 0, sh->X, sh->ldN, 0, 0.0,
+                     l.U[1 - src], sh->ldN, 0, 1, TRAJ_TRI_B_UPPER_F, err));
+      }
     }
     src = 1 - src;
   }
@@ -549,10 +599,37 @@ int propagate_banded(ShardedCtx* sh, int cur, int nxt, std::string* err) {
 // the exchange of block d+1 runs under the GEMM of block d.  The emulation (one GPU) gathers
 // first and then runs the same chunk GEMMs in the same order (the same arithmetic).
 // TRAJ_SHARD_OVERLAP=0: one allgather, then one L-deep GEMM.
+// planar 3M chunk: P_q (+)= K_g[:, s]_q U_s,q for the three products (one batch-3 launch), U_s split
+// into (re, im, re + im) planes first
+int planar_chunk(ShardedCtx* sh, ShardLocal& l, const cplx* Us, int s, bool accumulate, std::string* err) {
+  const long long Lp = sh->Lp, psC = Lp * sh->ldPs;
+  STRY(split_planes(sh->st, Us, sh->ldN, 0, (int)Lp, sh->N, 1, sh->Cp, sh->ldPs, psC, 0, err));
+  return dgemm(sh->st, 0, Lp, sh->N, Lp, 1.0, l.Kp + (long long)s * Lp, sh->ldKs, Lp * sh->ldKs, sh->Cp, sh->ldPs, psC,
+               accumulate ? 1.0 : 0.0, l.Pp, sh->ldPs, psC, 3, 0, err);
+}
+
+int planar_finish(ShardedCtx* sh, ShardLocal& l, int nxt, std::string* err) {
+  const long long psC = (long long)sh->Lp * sh->ldPs;
+  return combine_planes(sh->st, l.Pp, sh->ldPs, psC, 0, sh->Lp, sh->N, 1, l.U[nxt], sh->ldN, 0, err);
+}
+
 int propagate_dense(ShardedCtx* sh, int cur, int nxt, std::string* err) {
   cudaStream_t st = sh->st;
   const long long Lp = sh->Lp, ld = sh->ldN;
   const size_t bytes = (size_t)Lp * ld * 16;
+  if (sh->planar && !(sh->comm.comm && sh->overlap && sh->P > 1)) {
+    // gathered first (emulation, one shard, or TRAJ_SHARD_OVERLAP=0), then the chunk products
+    if (sh->P > 1) STRY(gather_full(sh, cur, err));
+    for (auto& l : sh->loc) {
+      for (int d = 0; d < sh->P; ++d) {
+        const int s = (l.g - d + sh->P) % sh->P;
+        const cplx* Us = sh->P > 1 ? sh->Ufull + (size_t)s * Lp * ld : l.U[cur];
+        STRY(planar_chunk(sh, l, Us, s, d > 0, err));
+      }
+      STRY(planar_finish(sh, l, nxt, err));
+    }
+    return 0;
+  }
   if (!sh->overlap || sh->P == 1) {
     STRY(gather_full(sh, cur, err));
     for (auto& l : sh->loc)
@@ -585,9 +662,12 @@ int propagate_dense(ShardedCtx* sh, int cur, int nxt, std::string* err) {
         SCK(cudaStreamWaitEvent(st, sh->ev_chunk[d], 0));
         Us = sh->Ufull + (size_t)s * Lp * ld;
       }
-      STRY(zgemm(st, 0, 0, Lp, sh->N, Lp, 1.0, 0.0, l.K + (size_t)s * Lp, sh->ldL, 0, Us, ld, 0, d ? 1.0 : 0.0,
-                 l.U[nxt], ld, 0, 1, 0, err));
+      if (sh->planar) STRY(planar_chunk(sh, l, Us, s, d > 0, err));
+      else
+        STRY(zgemm(st, 0, 0, Lp, sh->N, Lp, 1.0, 0.0, l.K + (size_t)s * Lp, sh->ldL, 0, Us, ld, 0, d ? 1.0 : 0.0,
+                   l.U[nxt], ld, 0, 1, 0, err));
     }
+    if (sh->planar) STRY(planar_finish(sh, l, nxt, err));
     return 0;
   }
   STRY(gather_full(sh, cur, err));

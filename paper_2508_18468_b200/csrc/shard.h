@@ -39,6 +39,8 @@ struct ShardLocal {
   cplx* USloc = nullptr;   // capr x ldN
   cplx* Tm = nullptr;      // Lp x ldcap
   cplx* Uext = nullptr;    // banded: (H + Lp + H) x ldN, halo rows around the local block
+  // planar 3M (dense K): K_g's planes [3][Lp][ldKs], product planes [3][Lp][ldPs], U's six planes
+  double *Kp = nullptr, *Pp = nullptr, *Up6 = nullptr;
 };
 
 struct ShardedCtx {
@@ -83,6 +85,10 @@ struct ShardedCtx {
   // chunk d of K_g U_full on st waits only for ev_chunk[d]
   bool overlap = true;
   CholDist cdist;          // the N x N Cholesky's large levels split over the ranks
+  // planar 3M for K_g U and the local Gram / TRMM (TRAJ_PLANAR_KU / TRAJ_PLANAR_CQR, N >= TRAJ_PLANAR_MIN_N)
+  bool planar = false;
+  long long ldKs = 0, ldPs = 0;
+  double *Cp = nullptr, *Gp = nullptr, *Xp = nullptr;   // chunk planes [3][Lp], Gram / X planes [3][N]
   cplx* dist_scratch = nullptr;
   size_t dist_scratch_bytes = 0;
   cudaStream_t cst = nullptr;
