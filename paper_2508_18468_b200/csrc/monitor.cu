@@ -258,7 +258,8 @@ __global__ void __launch_bounds__(256) panel_sample_kernel(const cplx* Dw, long 
 
 // occupied / empty site lists from the outcome flags (one thread per trajectory)
 __global__ void finalize_outcomes_kernel(const int32_t* S, int cap, const int32_t* count, const int32_t* occ, int T,
-                                         int32_t* pos1, int32_t* S1, int32_t* S0, int32_t* k1_out, int32_t* k0_out) {
+                                         int32_t* pos1, int32_t* S1, int32_t* S0, int32_t* k1_out, int32_t* k0_out,
+                                         int32_t* pos0) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
   const int m = count[t] < cap ? count[t] : cap;
@@ -270,6 +271,7 @@ __global__ void finalize_outcomes_kernel(const int32_t* S, int cap, const int32_
       S1[b + n1] = S[b + r];
       ++n1;
     } else {
+      if (pos0) pos0[b + n0] = r;
       S0[b + n0] = S[b + r];
       ++n0;
     }
@@ -499,7 +501,7 @@ int gather_rows(cudaStream_t st, const cplx* src, long long lds, long long sS, c
 int sample_outcomes(cudaStream_t st, const cplx* D0, cplx* Dw, long long ldd, long long sD, const int32_t* S, int cap,
                     const int32_t* count, int maxc, int T, long long step, long long traj_base, uint64_t seed,
                     int32_t* occ, cplx* Linv, cplx* DLinv, cplx* Ybuf, cplx* Zbuf, long long ldy, int32_t* pos1,
-                    int32_t* S1, int32_t* S0, int32_t* k1, int32_t* k0, std::string* err) {
+                    int32_t* S1, int32_t* S0, int32_t* k1, int32_t* k0, std::string* err, int32_t* pos0) {
   const uint32_t key0 = (uint32_t)(seed & 0xffffffffu), key1 = (uint32_t)(seed >> 32);
   // work copy of C_SS: every batch entry's leading maxc rows (sD = 0 when unbatched)
   const size_t bytes = (size_t)((T - 1) * sD + (long long)maxc * ldd) * 16;
@@ -531,7 +533,8 @@ int sample_outcomes(cudaStream_t st, const cplx* D0, cplx* Dw, long long ldd, lo
                    T, 0, err)))
       return r;
   }
-  finalize_outcomes_kernel<<<(unsigned)ceil_div(T, 128), 128, 0, st>>>(S, cap, count, occ, T, pos1, S1, S0, k1, k0);
+  finalize_outcomes_kernel<<<(unsigned)ceil_div(T, 128), 128, 0, st>>>(S, cap, count, occ, T, pos1, S1, S0, k1, k0,
+                                                                        pos0);
   count_launch();
   return last(err, "finalize_outcomes") == cudaSuccess ? 0 : 4;
 }

@@ -28,11 +28,12 @@ int sub_identity_batched(cudaStream_t st, cplx* T, long long ld, long long sT, c
 int zero_rows_batched(cudaStream_t st, cplx* U, long long ld, long long sU, const int32_t* rows, int cap,
                       const int32_t* k_dev, int kmax, int T, int ncols, std::string* err);
 // Blocked conditional Born sampling of every trajectory's click list on C_SS (D0, kept);
+// pos0 (optional): positions within S of the empty outcomes;
 // Dw: work copy; Linv/DLinv: [T][64][64]; Ybuf/Zbuf: [T][64][ldy] with ldy >= maxc.
 int sample_outcomes(cudaStream_t st, const cplx* D0, cplx* Dw, long long ldd, long long sD, const int32_t* S, int cap,
                     const int32_t* count, int maxc, int T, long long step, long long traj_base, uint64_t seed,
                     int32_t* occ, cplx* Linv, cplx* DLinv, cplx* Ybuf, cplx* Zbuf, long long ldy, int32_t* pos1,
-                    int32_t* S1, int32_t* S0, int32_t* k1, int32_t* k0, std::string* err);
+                    int32_t* S1, int32_t* S0, int32_t* k1, int32_t* k0, std::string* err, int32_t* pos0 = nullptr);
 int gather_sub(cudaStream_t st, const cplx* D0, long long ld0, const int32_t* pos, int k, cplx* D11, long long ld1,
                std::string* err);
 // T[S1[c] - row0][c] -= 1 for the S1 entries inside [row0, row0 + nrows)

@@ -296,6 +296,7 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
     lay.take(sh->pos1, (size_t)cap * 4);
     lay.take(sh->S1, (size_t)cap * 4);
     lay.take(sh->S0, (size_t)cap * 4);
+    lay.take(sh->pos0, (size_t)cap * 4);
     lay.take(sh->k1, 16);
     lay.take(sh->k0, 16);
     lay.take(sh->D11, (size_t)cap * ldcap * 16);
@@ -373,6 +374,10 @@ int shard_init(ShardedCtx* sh, const traj_config* c, std::string* err) {
     sh->cdist.user = sh;
     sh->cdist.share_rows = dist_share_rows;
   }
+  {
+    const char* lg = getenv("TRAJ_LOWRANK_GRAM");
+    sh->lowrank_gram = !(lg && lg[0] == '0');
+  }
   const char* ov = getenv("TRAJ_SHARD_OVERLAP");
   sh->overlap = !(ov && ov[0] == '0');
   if (sh->comm.comm && sh->overlap && sh->P > 1) {
@@ -428,8 +433,11 @@ int allreduce_gram(ShardedCtx* sh, std::string* err) {
 // CholeskyQR2 of the distributed U (local blocks src[s]); tmp[s] the other buffers.
 int cqr2(ShardedCtx* sh, int src_which, std::string* err) {
   int src = src_which;
+  const int lr = sh->lr_k0;
+  sh->lr_k0 = -1;
   for (int pass = 0; pass < 2; ++pass) {
-    {
+    if (pass == 0 && lr == 0) continue;     // no row zeroed: pass 1 has R = I
+    if (!(pass == 0 && lr > 0)) {            // else pass 1's G = I - V^dag V is already set, replicated
       Phase p(sh->prof, sh->st, TRAJ_PH_GRAM);
       for (auto& l : sh->loc) {
         if (sh->planar) {
@@ -469,6 +477,8 @@ int cqr2(ShardedCtx* sh, int src_which, std::string* err) {
         const long long psU = (long long)sh->Lp * sh->ldPs, psX = (long long)sh->N * sh->ldPs;
         STRY(split_planes(sh->st, sh->X, sh->ldN, 0, sh->N, sh->N, 1, sh->Xp, sh->ldPs, psX, 0, err));
         for (auto& l : sh->loc) {
+          if (pass == 0 && lr > 0)   // no measured Gram split U this pass: its (re, im, re + im) planes
+            STRY(split_planes(sh->st, l.U[src], sh->ldN, 0, sh->Lp, sh->N, 1, l.Up6 + 3 * psU, sh->ldPs, psU, 0, err));
           STRY(dgemm(sh->st, 0, sh->Lp, sh->N, sh->N, 1.0, l.Up6 + 3 * psU, sh->ldPs, psU, sh->Xp, sh->ldPs, psX, 0.0,
                      l.Pp, sh->ldPs, psU, 3, DG_TRI_B_UPPER, err));
           STRY(combine_planes(sh->st, l.Pp, sh->ldPs, psU, 0, sh->Lp, sh->N, 1, l.U[1 - src], sh->ldN, 0, err));
@@ -481,7 +491,10 @@ int cqr2(ShardedCtx* sh, int src_which, std::string* err) {
     }
     src = 1 - src;
   }
-  return 0;   // two passes: back in src_which
+  if (src != src_which)   // one pass ran: move the result back into src_which
+    for (auto& l : sh->loc)
+      SCK(cudaMemcpyAsync(l.U[src_which], l.U[src], (size_t)sh->Lp * sh->ldN * 16, cudaMemcpyDeviceToDevice, sh->st));
+  return 0;   // the result is in src_which
 }
 
 int projective(ShardedCtx* sh, int which, long long step, std::string* err) {
@@ -516,7 +529,10 @@ int projective(ShardedCtx* sh, int which, long long step, std::string* err) {
   }
   sh->last_nS = total;
   sh->last_n1 = 0;
-  if (total == 0) return 0;
+  if (total == 0) {
+    if (sh->lowrank_gram) sh->lr_k0 = 0;     // U = K U is orthonormal: pass 1 has R = I
+    return 0;
+  }
   // pack the per-shard blocks (shard order = ascending sites) into S and U_S
   int off = 0;
   for (int q = 0; q < P; ++q) {
@@ -533,7 +549,7 @@ int projective(ShardedCtx* sh, int which, long long step, std::string* err) {
              0, 1, 0, err));
   STRY(sample_outcomes(st, sh->D0, sh->Dw, sh->ldcap, 0, sh->S, sh->cap, sh->count, total, 1, step, sh->traj_base,
                        sh->seed, sh->occ, sh->Linv, sh->DLinv, sh->Ybuf, sh->Zbuf, sh->ldcap, sh->pos1, sh->S1, sh->S0,
-                       sh->k1, sh->k0, err));
+                       sh->k1, sh->k0, err, sh->pos0));
   SCK(cudaMemcpyAsync(sh->h_small, sh->k1, 4, cudaMemcpyDeviceToHost, st));
   SCK(cudaMemcpyAsync(sh->h_small + 1, sh->k0, 4, cudaMemcpyDeviceToHost, st));
   SCK(cudaStreamSynchronize(st));
@@ -557,6 +573,23 @@ int projective(ShardedCtx* sh, int which, long long step, std::string* err) {
   }
   if (k0 > 0)
     for (auto& l : sh->loc) STRY(zero_rows(st, l.U[which], sh->ldN, sh->S0, k0, sh->N, err, l.row0, sh->Lp));
+  if (sh->lowrank_gram) {
+    // U was orthonormal before the rows S0 were zeroed, so pass 1's Gram is I - V^dag V with V the
+    // zeroed rows after the rank-k1 update: V = U_S0 - (U_S0 W) W^dag from the gathered rows (replicated)
+    if (k0 > 0) {
+      STRY(gather_rows(st, sh->US, sh->ldN, 0, sh->pos0, 0, nullptr, k0, 1, sh->USrecv, sh->ldN, 0, sh->N, err));
+      if (k1 > 0) {
+        STRY(zgemm(st, 0, 0, k0, k1, sh->N, 1.0, 0.0, sh->USrecv, sh->ldN, 0, sh->W, sh->ldcap, 0, 0.0, sh->D11,
+                   sh->ldcap, 0, 1, 0, err));
+        STRY(zgemm(st, 0, 1, k0, sh->N, k1, -1.0, 0.0, sh->D11, sh->ldcap, 0, sh->W, sh->ldcap, 0, 1.0, sh->USrecv,
+                   sh->ldN, 0, 1, 0, err));
+      }
+      STRY(set_identity(st, sh->G, sh->ldN, 0, sh->N, 1, err));
+      STRY(zgemm(st, 1, 0, sh->N, sh->N, k0, -1.0, 0.0, sh->USrecv, sh->ldN, 0, sh->USrecv, sh->ldN, 0, 1.0, sh->G,
+                 sh->ldN, 0, 1, TRAJ_C_UPPER_F, err));
+    }
+    sh->lr_k0 = k0;
+  }
   return 0;
 }
 

@@ -80,6 +80,11 @@ struct ShardedCtx {
   double* h_dev = nullptr;
   long long last_nS = 0, last_n1 = 0, cqr2_fallbacks = 0;
   bool full_cqr2 = false;
+  // pass 1 of CholeskyQR after a projective step: G = I - V^dag V from the zeroed rows V, formed
+  // from the gathered (replicated) U_S rows -- no Gram, no allreduce (TRAJ_LOWRANK_GRAM=0: measured)
+  bool lowrank_gram = true;
+  int lr_k0 = -1;          // >= 0: pass 1's G is set (0: no row zeroed, pass 1 has R = I)
+  int32_t* pos0 = nullptr;
   cudaStream_t st = nullptr;
   // dense propagate with the allgather overlapped (NCCL mode): per-distance send/recv on cst,
   // chunk d of K_g U_full on st waits only for ev_chunk[d]
