@@ -377,6 +377,14 @@ int shard_init(ShardedCtx* sh, const traj_config* c, std::string* err) {
   {
     const char* lg = getenv("TRAJ_LOWRANK_GRAM");
     sh->lowrank_gram = !(lg && lg[0] == '0');
+    const char* co = getenv("TRAJ_CHOL_OVERLAP");
+    int least = 0, greatest = 0;
+    sh->chol_overlap = !(co && co[0] == '0') && cudaDeviceGetStreamPriorityRange(&least, &greatest) == cudaSuccess &&
+                       cudaStreamCreateWithPriority(&sh->st_hi, cudaStreamNonBlocking, greatest) == cudaSuccess &&
+                       cudaStreamCreateWithPriority(&sh->st_lo, cudaStreamNonBlocking, least) == cudaSuccess;
+    for (cudaEvent_t* e : {&sh->ev_fork, &sh->ev_left, &sh->ev_lo_done, &sh->ev_hi_done})
+      if (sh->chol_overlap && cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess)
+        sh->chol_overlap = false;
   }
   const char* ov = getenv("TRAJ_SHARD_OVERLAP");
   sh->overlap = !(ov && ov[0] == '0');
@@ -430,6 +438,24 @@ int allreduce_gram(ShardedCtx* sh, std::string* err) {
   return sh->comm.allreduce(sh->st, part.data(), reinterpret_cast<double*>(sh->G), (size_t)sh->N * sh->ldN * 2, err);
 }
 
+// dst[:, a:b] = src[:, 0:b] X[0:b, a:b] for every local shard (X upper triangular) on stream q;
+// planar: into the product planes (combined later), U's planes 3..5 already split
+int trmm_cols(ShardedCtx* sh, int src, long long a, long long b, cudaStream_t q, std::string* err) {
+  if (b <= a) return 0;
+  if (sh->planar) {
+    const long long psU = (long long)sh->Lp * sh->ldPs, psX = (long long)sh->N * sh->ldPs;
+    STRY(split_planes(q, sh->X + a, sh->ldN, 0, (int)b, (int)(b - a), 1, sh->Xp + a, sh->ldPs, psX, 0, err));
+    for (auto& l : sh->loc)
+      STRY(dgemm(q, 0, sh->Lp, b - a, b, 1.0, l.Up6 + 3 * psU, sh->ldPs, psU, sh->Xp + a, sh->ldPs, psX, 0.0, l.Pp + a,
+                 sh->ldPs, psU, 3, DG_TRI_B_UPPER, err, 0, a));
+    return 0;
+  }
+  for (auto& l : sh->loc)
+    STRY(zgemm(q, 0, 0, sh->Lp, b - a, b, 1.0, 0.0, l.U[src], sh->ldN, 0, sh->X + a, sh->ldN, 0, 0.0, l.U[1 - src] + a,
+               sh->ldN, 0, 1, TRAJ_TRI_B_UPPER_F, err, 0, a));
+  return 0;
+}
+
 // CholeskyQR2 of the distributed U (local blocks src[s]); tmp[s] the other buffers.
 int cqr2(ShardedCtx* sh, int src_which, std::string* err) {
   int src = src_which;
@@ -463,6 +489,52 @@ int cqr2(ShardedCtx* sh, int src_which, std::string* err) {
         SCK(cudaStreamSynchronize(sh->st));
         if (sh->h_dev[0] > 1e-9 / sqrt((double)sh->N)) full = true;
         if (full) ++sh->cqr2_fallbacks;
+      }
+      if (full && pass == 0 && sh->chol_overlap && sh->N > 64) {
+        // factorise on st_hi; each newly final left column block's TRMM runs on st_lo
+        SCK(cudaEventRecord(sh->ev_fork, sh->st));
+        SCK(cudaStreamWaitEvent(sh->st_hi, sh->ev_fork, 0));
+        SCK(cudaStreamWaitEvent(sh->st_lo, sh->ev_fork, 0));
+        const long long psU = (long long)sh->Lp * sh->ldPs;
+        if (sh->planar && lr > 0)   // pass 1's Gram was not measured: U's (re, im, re + im) planes
+          for (auto& l : sh->loc)
+            STRY(split_planes(sh->st_lo, l.U[src], sh->ldN, 0, sh->Lp, sh->N, 1, l.Up6 + 3 * psU, sh->ldPs, psU, 0,
+                              err));
+        struct HookUser {
+          ShardedCtx* sh;
+          int src;
+          long long hs;
+          int status;
+          std::string* err;
+        } hu{sh, src, 0, 0, err};
+        CholHook hook;
+        hook.user = &hu;
+        hook.left_ready = [](void* u, long long hs) {
+          HookUser* q = reinterpret_cast<HookUser*>(u);
+          ShardedCtx* s2 = q->sh;
+          if (q->status || hs <= q->hs) return;
+          const long long a = q->hs;
+          q->hs = hs;
+          if (cudaEventRecord(s2->ev_left, s2->st_hi) != cudaSuccess ||
+              cudaStreamWaitEvent(s2->st_lo, s2->ev_left, 0) != cudaSuccess) {
+            q->status = TRAJ_ECUDA;
+            return;
+          }
+          q->status = trmm_cols(s2, q->src, a, hs, s2->st_lo, q->err);
+        };
+        STRY(chol_inverse(sh->st_hi, sh->N, sh->G, sh->ldN, 0, sh->X, sh->ldN, 0, 1, sh->chol_scratch, sh->failed_dev,
+                          err, &sh->cdist, &hook));
+        if (hu.status) return hu.status;
+        SCK(cudaEventRecord(sh->ev_lo_done, sh->st_lo));
+        SCK(cudaStreamWaitEvent(sh->st_hi, sh->ev_lo_done, 0));   // the U planes / pieces before the right part
+        STRY(trmm_cols(sh, src, hu.hs, sh->N, sh->st_hi, err));
+        SCK(cudaEventRecord(sh->ev_hi_done, sh->st_hi));
+        SCK(cudaStreamWaitEvent(sh->st, sh->ev_hi_done, 0));
+        if (sh->planar)
+          for (auto& l : sh->loc)
+            STRY(combine_planes(sh->st, l.Pp, sh->ldPs, psU, 0, sh->Lp, sh->N, 1, l.U[1 - src], sh->ldN, 0, err));
+        src = 1 - src;
+        continue;   // this pass's TRMM is done (inside the Cholesky phase)
       }
       if (full)
         STRY(chol_inverse(sh->st, sh->N, sh->G, sh->ldN, 0, sh->X, sh->ldN, 0, 1, sh->chol_scratch, sh->failed_dev,
@@ -861,6 +933,13 @@ void shard_destroy(ShardedCtx* sh) {
     cudaStreamDestroy(sh->cst);
   }
   if (sh->ev_start) cudaEventDestroy(sh->ev_start);
+  for (cudaStream_t q : {sh->st_hi, sh->st_lo})
+    if (q) {
+      cudaStreamSynchronize(q);
+      cudaStreamDestroy(q);
+    }
+  for (cudaEvent_t e : {sh->ev_fork, sh->ev_left, sh->ev_lo_done, sh->ev_hi_done})
+    if (e) cudaEventDestroy(e);
   for (auto e : sh->ev_chunk)
     if (e) cudaEventDestroy(e);
   if (sh->comm.comm) ncclCommDestroy(sh->comm.comm);

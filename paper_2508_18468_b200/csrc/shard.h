@@ -83,6 +83,11 @@ struct ShardedCtx {
   // pass 1 of CholeskyQR after a projective step: G = I - V^dag V from the zeroed rows V, formed
   // from the gathered (replicated) U_S rows -- no Gram, no allreduce (TRAJ_LOWRANK_GRAM=0: measured)
   bool lowrank_gram = true;
+  // CholeskyQR pass 1: factorisation on st_hi, TRMM of each newly final column block on st_lo
+  // (TRAJ_CHOL_OVERLAP=0: serial)
+  bool chol_overlap = false;
+  cudaStream_t st_hi = nullptr, st_lo = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_left = nullptr, ev_lo_done = nullptr, ev_hi_done = nullptr;
   int lr_k0 = -1;          // >= 0: pass 1's G is set (0: no row zeroed, pass 1 has R = I)
   int32_t* pos0 = nullptr;
   cudaStream_t st = nullptr;
