@@ -219,7 +219,8 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
     const char* pc = getenv("TRAJ_PLANAR_CQR");
     const char* mn = getenv("TRAJ_PLANAR_MIN_N");
     const long long min_n = mn ? atoll(mn) : 512;
-    sh->planar = !banded && !(pk && pk[0] == '0') && !(pc && pc[0] == '0') && N >= min_n;
+    // (K_g's chunk columns start at s Lp doubles: TMA needs them 16-byte aligned, so Lp even)
+    sh->planar = !banded && !(pk && pk[0] == '0') && !(pc && pc[0] == '0') && N >= min_n && (L / P) % 2 == 0;
     sh->ldKs = round_up(L, 16);
     sh->ldPs = round_up(N, 16);
   }
