@@ -89,6 +89,7 @@ struct traj_ctx {
           *S0 = nullptr, *k1 = nullptr, *k0 = nullptr;
   cplx *US = nullptr, *D0 = nullptr, *Dw = nullptr, *D11 = nullptr, *X11 = nullptr, *W = nullptr, *Tm = nullptr;
   cplx *Linv = nullptr, *DLinv = nullptr, *Ybuf = nullptr, *Zbuf = nullptr;
+  cplx* Tm2 = nullptr;             // split-K partner of Tm (one trajectory)
   void* chol_scratch_small = nullptr;
   long long sUS = 0, sD = 0;
   // observables
@@ -341,6 +342,7 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     lay.take(h->chol_scratch_small, chol_scratch_bytes(cap, T));
     lay.take(h->W, (size_t)T * N * ldcap * 16);
     lay.take(h->Tm, (size_t)T * L * ldcap * 16);
+    if (T == 1) lay.take(h->Tm2, (size_t)L * ldcap * 16);
     if (c->orthonormalizer == TRAJ_ORTH_LOWRANK) {
       for (cplx** b : {&h->Mb, &h->Yb, &h->Zb, &h->Tb, &h->Pb, &h->Qb}) lay.take(*b, (size_t)T * cap * ldcap * 16);
       lay.take(h->FV, (size_t)T * cap * ldN * 16);
@@ -388,6 +390,24 @@ std::vector<std::complex<double>> ring_coefficients(int n, double J, double dt) 
 // Pass 2 sees G2 = I + E with |E| ~ kappa(U)^2 eps: its Cholesky inverse is taken from the
 // first-order closed form (exact up to N |E|^2, below rounding when N max|E|^2 < 1e-18,
 // checked on the device per step); otherwise, or with TRAJ_CQR2_FULL=1, chol_inverse.
+// C (M x Nc, ld h->ldcap) = A (M x K, ld lda) op(B) for a skinny output (Nc = a click count, K = N):
+// with one trajectory the K range is split in two halves run as one batch-2 launch (twice the CTAs
+// for the few output tiles), the second half into Tm2, then added; otherwise one launch.
+int skinny_gemm(traj_ctx* h, int opB, long long M, long long Nc, long long K, const cplx* A, long long lda, long long sA,
+                const cplx* B, long long ldb, long long sB, cplx* C, long long sC) {
+  const long long tiles = ceil_div(M, 64) * ceil_div(Nc, 64);
+  if (h->T != 1 || !h->Tm2 || C != h->Tm || K < 2048 || K % 32 || tiles >= 8 * 148)
+    return zgemm(h->st, 0, opB, M, Nc, K, 1.0, 0.0, A, lda, sA, B, ldb, sB, 0.0, C, h->ldcap, sC, h->T, 0, &h->err);
+  // batch entry z in {0, 1} takes k in [z K/2, (z + 1) K/2): A's columns and B's rows (opB = 0) or
+  // columns (opB = 1) at a batch stride of K/2, the outputs at Tm and Tm2 (stride Tm2 - Tm)
+  const long long k2 = K / 2;
+  int s = zgemm(h->st, 0, opB, M, Nc, k2, 1.0, 0.0, A, lda, k2, B, ldb, opB == 0 ? k2 * ldb : k2, 0.0, C, h->ldcap,
+                h->Tm2 - C, 2, 0, &h->err);
+  if (!s) s = add_inplace(h->st, reinterpret_cast<double*>(C), reinterpret_cast<const double*>(h->Tm2),
+                          M * h->ldcap * 2, &h->err);
+  return s;
+}
+
 // Planes are stored plane-major, [plane][trajectory][rows][ldP], so a triple of planes over all
 // trajectories sits at one constant stride: three real products C_q = op(A_q) B_q for every
 // trajectory are a single batched launch of 3T entries (entry z = q T + t at z * stride).
@@ -610,8 +630,7 @@ int lowrank_orthonormalize(traj_ctx* h, cplx* U, int k) {
   TRY(zgemm(h->st, 0, 0, k, h->N, k, 1.0, 0.0, h->Qb, ld, s2, h->US, h->ldN, h->sUS, 0.0, h->FV, h->ldN, h->sUS, T, 0,
             &h->err));
   const long long sT = (long long)h->L * h->ldcap;
-  TRY(zgemm(h->st, 0, 1, h->L, k, h->N, 1.0, 0.0, U, h->ldN, h->sU, h->US, h->ldN, h->sUS, 0.0, h->Tm, h->ldcap, sT, T,
-            0, &h->err));
+  TRY(skinny_gemm(h, 1, h->L, k, h->N, U, h->ldN, h->sU, h->US, h->ldN, h->sUS, h->Tm, sT));
   TRY(zgemm(h->st, 0, 0, h->L, h->N, k, 1.0, 0.0, h->Tm, h->ldcap, sT, h->FV, h->ldN, h->sUS, 1.0, U, h->ldN, h->sU, T,
             0, &h->err));
   h->lr_k0 = 0;              // U is orthonormal: CholeskyQR2's first pass has R = I
@@ -670,8 +689,7 @@ int projective(traj_ctx* h, cplx* U) {
     TRY(zgemm(h->st, 1, 0, h->N, k1max, k1max, 1.0, 0.0, h->US, h->ldN, h->sUS, h->X11, h->ldcap, sX, 0.0, h->W,
               h->ldcap, sW, T, TRAJ_TRI_B_UPPER_F, &h->err));
     // Tm = U W - E_{S1}   (L x k1)
-    TRY(zgemm(h->st, 0, 0, h->L, k1max, h->N, 1.0, 0.0, U, h->ldN, h->sU, h->W, h->ldcap, sW, 0.0, h->Tm, h->ldcap,
-              sT, T, 0, &h->err));
+    TRY(skinny_gemm(h, 0, h->L, k1max, h->N, U, h->ldN, h->sU, h->W, h->ldcap, sW, h->Tm, sT));
     TRY(sub_identity_batched(h->st, h->Tm, h->ldcap, sT, h->S1, cap, h->k1, k1max, T, &h->err));
     // U <- U - Tm W^dag
     TRY(zgemm(h->st, 0, 1, h->L, h->N, k1max, -1.0, 0.0, h->Tm, h->ldcap, sT, h->W, h->ldcap, sW, 1.0, U, h->ldN,

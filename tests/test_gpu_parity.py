@@ -609,3 +609,21 @@ def test_lowrank_probe_gates_refinement(P, monkeypatch):
     assert res["0"][0]["probes"] == 0
     assert res["5e-13"][0]["probes"] >= steps // 2
     assert res["5e-13"][0]["refinements"] < res["5e-14"][0]["refinements"]
+
+
+@pytest.mark.parametrize("orth", ["cqr2", "lowrank"])
+def test_projective_l4096_lockstep(P, orth):
+    """L = 4096 (N = 2048): large enough for the split-K skinny products of the projective step
+    (U W, and U' V^dag in the low-rank mode, K = N as one batch-2 launch) and for the planar
+    paths at their default threshold; three steps in lockstep with the oracle."""
+    L, gam = 4096, 0.5
+    g = P.Trajectories(L, 1, "projective", [gam], seed=17, orthonormalizer=orth)
+    K = lattice.propagator_lattice(L, 1, 1.0, 0.05)
+    o = OracleTrajectory(L, 1, "projective", gam, 0.05, seed=17, traj=0, K=K)
+    for s in range(3):
+        g.step(1)
+        o.step(1)
+        assert g.last_clicks(0) == (o.last_clicks[0].size, int(o.last_clicks[1].sum()))
+    assert np.abs(g.correlation(0).cpu().numpy() - o.correlation()).max() < C_TOL
+    A = np.arange(L // 2)
+    assert abs(g.entropy(A)[0] - o.entropy(A)) < S_TOL
