@@ -207,7 +207,8 @@ def run_ours(args):
     launches = P.traj_kernel_launches() - l0
     clk = clocks.stop()
     phases = tr.phase_times()
-    tr_clicks = [tr.last_clicks(t)[0] for t in range(tpg)] if w.protocol == "projective" else [0]
+    tr_clicks = ([tr.last_clicks(t)[0] for t in range(tpg)]
+                 if w.protocol in ("projective", "projective_events") else [0])
     if world > 1:
         dist.barrier()
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -254,6 +255,7 @@ def run_ours(args):
                             f"projective rank-k GEMMs ({kn[1].split(' ')[0].split('<')[0]} family): 16 L N (k1 + k0) "
                             f"flops per step, k1 + k0 = {k_sum} clicks in the last timed step; phase time includes "
                             "the blocked sampler and the Newton-Schulz iteration")}
+    events_hbm = w.protocol == "projective_events" and args.orthonormalizer == "lowrank"
     pipe_per_alg = 0.75 if (algo == "3m" or planar or planar_cqr) else 1.0   # DMMA flops per 8mnk flop
     dom = max(kern, key=lambda k: phases[k][0])
     launches_per_step = 1.0
@@ -300,6 +302,13 @@ def run_ours(args):
         hbm[f"banded_kernel ({passes} pass(es), 32 L N B each)"] = {"achieved_gbs": g, "peak_gbs": HBM_PEAK_GBS,
                                                                    "frac": g / HBM_PEAK_GBS,
                                                                    "ms_per_step": phases["propagate"][0] / args.steps}
+    if w.protocol == "projective_events" and phases["project"][0] > 0:
+        # one pass per event reads U once and writes it once (32 L N bytes); events of the last window
+        b = 32.0 * w.L * w.N * sum(tr_clicks) * args.steps
+        g = b / (phases["project"][0] / 1e3) / 1e9
+        hbm["ev_pass_1d_kernel (one pass per event, 32 L N B; events in the last window)"] = {
+            "achieved_gbs": g, "peak_gbs": HBM_PEAK_GBS, "frac": g / HBM_PEAK_GBS,
+            "ms_per_step": phases["project"][0] / args.steps}
     if w.protocol == "homodyne_rk4" and phases["propagate"][0] > 0:
         b = 4 * 48.0 * rows * w.N * tpg * args.steps
         g = b / (phases["propagate"][0] / 1e3) / 1e9
@@ -344,6 +353,38 @@ def run_ours(args):
         if world > 1:
             dist.destroy_process_group()
         return
+    ev_key = next((k for k in hbm if k.startswith("ev_pass")), None)
+    if events_hbm and ev_key:
+        # the event-driven step with the probe certificate is one HBM read + write of U per event
+        roof = {"bound": "hbm", "achieved": hbm[ev_key]["achieved_gbs"], "peak": HBM_PEAK_GBS, "unit": "GB/s",
+                "frac": hbm[ev_key]["frac"], "traffic": None, "kernel": ev_key,
+                "kernel_ms": hbm[ev_key]["ms_per_step"], "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    else:
+        roof = {"bound": "latency" if w.name == "c1" else "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                "kernel": kern[dom][1] + ("; per shard (L/P rows) when row-sharded" if shard else ""),
+                "kernel_ms": kern_ms, "timed": "device time of that phase per step (CUDA events around it on "
+                                              "the handle's stream)", "peak_source": FP64_PEAK_SOURCE,
+                "complex_mult": ("planar 3m" if (planar and dom == "propagate") or
+                                 (planar_cqr and dom in ("gram", "trmm")) else algo),
+                "pipe_tflops": achieved * pipe_per_alg, "pipe_frac": achieved * pipe_per_alg / FP64_PEAK_TFLOPS,
+                "traffic_note": ("ncu dram bytes of the propagate phase (profiles/ncu_traffic.json: split, three "
+                                 "real 16384x8192x16384 products, combine) vs 8.6 GB algorithmic: each wave of "
+                                 "148 output-stationary 128x128 tiles streams its K panels (> L2 at K = 16384), so "
+                                 "tens of GB are inherent to output-stationary tiling; 96 GB in 374 ms is "
+                                 "~0.26 TB/s, 4% of HBM, not a bound (the interleaved 128x64 kernel moved 154 GB)")
+                if planar else
+                ("ncu dram bytes of one K U launch (profiles/ncu_traffic.json) vs 8.6 GB "
+                                 "algorithmic: each wave of 148 output-stationary 128x64 tiles streams its K "
+                                 "panels (~580 MB per wave at K = 16384, > L2), so >= ~64 GB is inherent to "
+                                 "this tiling; 154 GB in 390 ms is ~0.4 TB/s, 6% of HBM, not a bound")
+                if traffic else None,
+                "note": ("c1 is latency-bound (SURVEY §8(d)): L = 64 trajectories, ~20 small launches "
+                         "and two host syncs per step; the fraction is not a kernel-quality figure. "
+                         if w.name == "c1" else "") +
+                        ("achieved counts the conventional 8mnk complex flops; the 3M (Gauss) kernels issue "
+                         "6mnk flops on the DMMA pipe, reported as pipe_tflops / pipe_frac")
+                if algo == "3m" else "4M: 8mnk flops on the DMMA pipe"}
     out = {
         "metric": "trajectory steps/s (configs[2]: 1d L=16384 projective; metric also quoted at 2d 160x160)",
         "value": value, "unit": "trajectory-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -353,31 +394,7 @@ def run_ours(args):
         "config": dict(describe(w, tpg), parallelism=(f"row-sharded K,U over {world} GPU(s) (NCCL)" if shard
                                                       else f"trajectory-parallel dp{world}"),
                        propagator=args.propagator, orthonormalizer=args.orthonormalizer),
-        "roofline": {"bound": "latency" if w.name == "c1" else "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-                     "kernel": kern[dom][1] + ("; per shard (L/P rows) when row-sharded" if shard else ""),
-                     "kernel_ms": kern_ms, "timed": "device time of that phase per step (CUDA events around it on "
-                                                   "the handle's stream)", "peak_source": FP64_PEAK_SOURCE,
-                     "complex_mult": ("planar 3m" if (planar and dom == "propagate") or
-                                      (planar_cqr and dom in ("gram", "trmm")) else algo),
-                     "pipe_tflops": achieved * pipe_per_alg, "pipe_frac": achieved * pipe_per_alg / FP64_PEAK_TFLOPS,
-                     "traffic_note": ("ncu dram bytes of the propagate phase (profiles/ncu_traffic.json: split, three "
-                                      "real 16384x8192x16384 products, combine) vs 8.6 GB algorithmic: each wave of "
-                                      "148 output-stationary 128x128 tiles streams its K panels (> L2 at K = 16384), so "
-                                      "tens of GB are inherent to output-stationary tiling; 96 GB in 374 ms is "
-                                      "~0.26 TB/s, 4% of HBM, not a bound (the interleaved 128x64 kernel moved 154 GB)")
-                     if planar else
-                     ("ncu dram bytes of one K U launch (profiles/ncu_traffic.json) vs 8.6 GB "
-                                      "algorithmic: each wave of 148 output-stationary 128x64 tiles streams its K "
-                                      "panels (~580 MB per wave at K = 16384, > L2), so >= ~64 GB is inherent to "
-                                      "this tiling; 154 GB in 390 ms is ~0.4 TB/s, 6% of HBM, not a bound")
-                     if traffic else None,
-                     "note": ("c1 is latency-bound (SURVEY §8(d)): L = 64 trajectories, ~20 small launches "
-                              "and two host syncs per step; the fraction is not a kernel-quality figure. "
-                              if w.name == "c1" else "") +
-                             ("achieved counts the conventional 8mnk complex flops; the 3M (Gauss) kernels issue "
-                              "6mnk flops on the DMMA pipe, reported as pipe_tflops / pipe_frac")
-                     if algo == "3m" else "4M: 8mnk flops on the DMMA pipe"},
+        "roofline": roof,
         "library_same_shape": library,
         "hbm_kernels": hbm or None,
         "step_dense_tflops": dense_tflops,
