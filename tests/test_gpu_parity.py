@@ -171,6 +171,56 @@ def test_projective_full_c3_invariants(P):
     assert abs(sa - sc) < 1e-8
 
 
+def test_free_evolution_closed_form_full_c5(P):
+    """configs[4] size (2d 160 x 160, N = 12800), gamma = 0, checkerboard start: after 5 steps
+    n = 1/2 + (-1)^(x+y)/2 s(t)^2 with s(t) = (1/160) sum_m cos(4t cos(2 pi m/160)) -- the 2d
+    Kronecker K as planar products and CholeskyQR at full size.  Tr C = N."""
+    Lx = Ly = 160
+    steps, dt = 5, 0.05
+    g = P.Trajectories(Lx, Ly, "projective", [0.0], dt=dt, seed=0)
+    g.step(steps)
+    n = g.occupations()[0].cpu().numpy()
+    m = np.arange(Lx)
+    s_t = np.mean(np.cos(4 * steps * dt * np.cos(2 * np.pi * m / Lx)))
+    ys, xs = np.divmod(np.arange(Lx * Ly), Lx)
+    want = 0.5 + 0.5 * (-1.0) ** (xs + ys) * s_t ** 2
+    assert np.abs(n - want).max() < 1e-12
+    assert abs(n.sum() - Lx * Ly // 2) < 1e-7
+    g.close()
+
+
+def test_projective_full_c5_invariants(P):
+    """configs[4] (160 x 160, projective gamma = 2.86, ~3660 clicks per step): after two steps every
+    clicked site has n in {0, 1} and the occupied count matches, the particle number is N, U stays
+    orthonormal, and S_A = S_complement for the strip A = x in [0, 40)."""
+    import torch
+    from paper_2508_18468_b200 import traj_zgemm
+    w = workloads.c5()
+    g = P.Trajectories(w.Lx, w.Ly, "projective", list(w.gammas), dt=w.dt, seed=w.seed)
+    g.step(2)
+    nS, n1 = g.last_clicks(0)
+    assert 3200 < nS < 4200
+    from oracle.philox import site_uniforms
+    u0, _ = site_uniforms(w.L, 1, 0, w.seed)
+    S = np.nonzero(u0 < w.gammas[0] * w.dt)[0]
+    assert S.size == nS
+    n = g.occupations()[0].cpu().numpy()
+    ns = n[S]
+    assert np.all((np.abs(ns) < 1e-10) | (np.abs(ns - 1) < 1e-10))
+    assert int(np.round(ns.sum())) == n1
+    assert abs(n.sum() - w.N) < 1e-7
+    U = g.get_state(0)
+    G = torch.zeros((w.N, w.N), dtype=torch.complex128, device="cuda")
+    traj_zgemm(1, 0, U, U, G)
+    G -= torch.eye(w.N, dtype=torch.complex128, device="cuda")
+    assert G.abs().max().item() < 1e-12
+    del G, U
+    A = workloads.columns(w.Lx, w.Ly, 0, w.Lx // 4)
+    Ac = np.setdiff1d(np.arange(w.L), A)
+    assert abs(g.entropy(A)[0] - g.entropy(Ac)[0]) < 1e-8
+    g.close()
+
+
 def test_cqr2_first_order_second_pass_matches_full(P):
     """The second CQR pass uses R2^-1 = I - triu(E,1) - diag(E)/2 (exact to O(N|E|^2));
     the result equals the full Cholesky second pass, and an ill-conditioned state falls back."""
