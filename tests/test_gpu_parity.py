@@ -221,6 +221,24 @@ def test_projective_full_c5_invariants(P):
     g.close()
 
 
+def test_c2_full_size_homodyne_lockstep(P):
+    """configs[1] at full size (1d L = 2048, N = 1024, homodyne, gamma in {0.1, 0.3, 1.0} as one
+    batch of three trajectories): the planar defaults with trajectory batching, 8 steps in lockstep
+    with the oracle; C, S(half) and n."""
+    w = workloads.c2()
+    gams = list(w.gammas)
+    lockstep(P, w.Lx, w.Ly, w.protocol, gams, 8, 4, [w.regions["half"]], seed=w.seed)
+
+
+def test_c4_full_size_homodyne_mutual_information(P):
+    """configs[3] at full size (2d 64 x 64, N = 2048, homodyne, two gammas of the sweep): 4 steps in
+    lockstep with the oracle including I2 between the 16 x 64 strips."""
+    w = workloads.c4()
+    gams = [w.gammas[0], w.gammas[-1]]
+    A, B = w.regions["mi"]
+    lockstep(P, w.Lx, w.Ly, w.protocol, gams, 4, 4, [A], seed=w.seed, mi=(A, B))
+
+
 def test_cqr2_first_order_second_pass_matches_full(P):
     """The second CQR pass uses R2^-1 = I - triu(E,1) - diag(E)/2 (exact to O(N|E|^2));
     the result equals the full Cholesky second pass, and an ill-conditioned state falls back."""
