@@ -3,10 +3,11 @@
 // planar form runs the three real products P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi) as one
 // batched real GEMM with a single accumulator set per warp).
 //
-// C_z = alpha A_z B_z + beta C_z, row-major real matrices, z < batch.  CTA 128 x 128, 8 warps of
-// 32 x 64 (64 accumulator doubles), 16 real k per stage, STAGES-deep TMA ring (lane 0 of warp 0
-// issues), 128B-swizzled tiles: A [128 m][16 k] (one 3D box), B [8 chunks of 16 n][16 k][16 n]
-// (one 4D box).  DMMA m8n8k4: A fragment A[g][k], B fragment B[k][g], k = 4 q + slot.
+// C_z = alpha op(A_z) B_z + beta C_z, row-major real matrices, z < batch.  CTA 128 x 128, 8 warps of
+// 32 x 64 (64 accumulator doubles), 16 real k per stage, a 4-deep TMA ring (3, 5 and 6 stages and
+// other refill points measured no better, tools/dgemm_bench.py) whose lane 0 of warp 0 issues;
+// 128B-swizzled tiles: A [128 m][16 k] (one 3D box; op(A) = A^T: the 4D box of B), B [8 chunks of
+// 16 n][16 k][16 n] (one 4D box).  DMMA m8n8k4: A fragment A[g][k], B fragment B[k][g], k = 4 q + slot.
 #include <cuda.h>
 #include <stdlib.h>
 
@@ -19,7 +20,7 @@ namespace traj {
 
 namespace {
 
-constexpr int DBM = 128, DBN = 128, DBK = 16, DSTAGES = 5, DWARPS = 8, DTHREADS = DWARPS * 32;
+constexpr int DBM = 128, DBN = 128, DBK = 16, DSTAGES = 4, DWARPS = 8, DTHREADS = DWARPS * 32;
 constexpr int DA_BYTES = DBM * DBK * 8, DB_BYTES = DBK * DBN * 8, DSTAGE = DA_BYTES + DB_BYTES;
 constexpr int DSMEM = DSTAGES * DSTAGE + 1024 + 2 * DSTAGES * 8;
 constexpr int DGROUP_M = 8;
