@@ -255,6 +255,12 @@ def run_ours(args):
                             f"projective rank-k GEMMs ({kn[1].split(' ')[0].split('<')[0]} family): 16 L N (k1 + k0) "
                             f"flops per step, k1 + k0 = {k_sum} clicks in the last timed step; phase time includes "
                             "the blocked sampler and the Newton-Schulz iteration")}
+    if phases.get("fused", (0.0,))[0] > 0:
+        # the fused small-lattice step (small_step.cu): the whole step in one CTA per trajectory;
+        # algorithmic flops per trajectory-step 8 L^2 N (K U) + 2 x (4 L N^2 Gram + 4 L N^2 solve)
+        kern = {"fused": ((8.0 * w.L * w.L * w.N + 16.0 * w.L * w.N * w.N) * tpg,
+                          "small_step_kernel: the whole step (K U, monitor, CholeskyQR2) with U in shared "
+                          "memory, one CTA per trajectory; 8 L^2 N + 16 L N^2 flops per trajectory-step")}
     events_hbm = w.protocol == "projective_events" and args.orthonormalizer == "lowrank"
     pipe_per_alg = 0.75 if (algo == "3m" or planar or planar_cqr) else 1.0   # DMMA flops per 8mnk flop
     dom = max(kern, key=lambda k: phases[k][0])
@@ -379,12 +385,17 @@ def run_ours(args):
                                  "panels (~580 MB per wave at K = 16384, > L2), so >= ~64 GB is inherent to "
                                  "this tiling; 154 GB in 390 ms is ~0.4 TB/s, 6% of HBM, not a bound")
                 if traffic else None,
-                "note": ("c1 is latency-bound (SURVEY §8(d)): L = 64 trajectories, ~20 small launches "
-                         "and two host syncs per step; the fraction is not a kernel-quality figure. "
+                "note": ("c1 is latency-bound (SURVEY §8(d)): L = 64, one fused launch per step with one CTA "
+                         "per trajectory, whose ~140 barriers and dependent pivots set the time; the fraction "
+                         "is not a kernel-quality figure. "
                          if w.name == "c1" else "") +
                         ("achieved counts the conventional 8mnk complex flops; the 3M (Gauss) kernels issue "
                          "6mnk flops on the DMMA pipe, reported as pipe_tflops / pipe_frac")
                 if algo == "3m" else "4M: 8mnk flops on the DMMA pipe"}
+    if dom == "fused":
+        roof.update({"complex_mult": "4m on DFMA (FP64 CUDA cores; the tensor pipe needs 8x8x4 tiles the barrier-"
+                                     "bound step cannot feed)", "pipe_tflops": None, "pipe_frac": None,
+                     "note": roof["note"].split(". ")[0] + "." if w.name == "c1" else None})
     out = {
         "metric": "trajectory steps/s (configs[2]: 1d L=16384 projective; metric also quoted at 2d 160x160)",
         "value": value, "unit": "trajectory-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

@@ -218,7 +218,8 @@ enum { TRAJ_PH_PROPAGATE = 0,  /* U <- K U                                   */
        TRAJ_PH_GRAM = 3,       /* G = U^dag U (both CQR passes)              */
        TRAJ_PH_CHOL = 4,       /* Cholesky + triangular inverse of G         */
        TRAJ_PH_TRMM = 5,       /* U <- U R^-1                                */
-       TRAJ_NPHASES = 6 };
+       TRAJ_PH_FUSED = 6,      /* the fused small-lattice step (all rows)    */
+       TRAJ_NPHASES = 7 };
 int traj_profile(traj_handle h, int enable);
 int traj_phase_times(traj_handle h, double* ms, int64_t* launches);
 

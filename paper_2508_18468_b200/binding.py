@@ -20,7 +20,7 @@ TRAJ_PROJECTIVE_EVENTS = 3
 TRAJ_INIT_NEEL = 0
 TRAJ_PROP_DENSE, TRAJ_PROP_BANDED = 0, 1
 TRAJ_TRI_A_UPPER, TRAJ_TRI_A_LOWER, TRAJ_TRI_B_UPPER, TRAJ_TRI_B_LOWER, TRAJ_C_UPPER = 1, 2, 4, 8, 16
-PHASES = ("propagate", "monitor", "project", "gram", "chol", "trmm")
+PHASES = ("propagate", "monitor", "project", "gram", "chol", "trmm", "fused")
 STATUS = {0: "TRAJ_OK", 1: "TRAJ_EINVAL", 2: "TRAJ_ECONFIG", 3: "TRAJ_ENUMERIC", 4: "TRAJ_ECUDA",
           5: "TRAJ_ENCCL", 6: "TRAJ_EDOMAIN"}
 
@@ -397,7 +397,7 @@ class Trajectories:
         self._c(lib().traj_profile(self._h, 1 if enable else 0))
 
     def phase_times(self):
-        ms = (ctypes.c_double * 6)()
-        ln = (ctypes.c_int64 * 6)()
+        ms = (ctypes.c_double * len(PHASES))()
+        ln = (ctypes.c_int64 * len(PHASES))()
         self._c(lib().traj_phase_times(self._h, ms, ln))
         return {p: (ms[i], ln[i]) for i, p in enumerate(PHASES)}

@@ -7,7 +7,7 @@
 
 namespace traj {
 
-constexpr int NPHASES = 6;
+constexpr int NPHASES = 7;
 
 struct Profiler {
   bool on = false;

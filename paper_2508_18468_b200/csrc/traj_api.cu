@@ -26,6 +26,7 @@
 #include "probe.h"
 #include "dgemm.h"
 #include "planar.h"
+#include "small_step.h"
 
 namespace traj {
 std::atomic<long long> g_kernel_launches{0};
@@ -124,6 +125,12 @@ struct traj_ctx {
   int32_t* h_small = nullptr;     // pinned host scratch
   double* h_dev = nullptr;        // pinned host copy of gdev
   std::vector<int64_t> last_nS, last_n1;
+  // fused small-lattice step (small_step.cu; TRAJ_SMALL_STEP=0: the general path): U, the step's
+  // scratch and the sampler fit one CTA's shared memory, one CTA per trajectory, one launch per
+  // traj_step call; the last step's click counts stay on the device (small_last [T][2])
+  bool small = false;
+  int32_t* small_last = nullptr;
+  bool small_last_dev = false;
   std::string err;
   Profiler prof;
 };
@@ -293,6 +300,7 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     lay.take(h->Pp, (size_t)T * 3 * L * h->ldP * 8);
     if (h->planar_cqr) lay.take(h->Xp, (size_t)T * 3 * N * h->ldP * 8);
   }
+  lay.take(h->small_last, (size_t)T * 2 * 4);
   lay.take(h->U[0], (size_t)T * L * ldN * 16);
   lay.take(h->U[1], (size_t)T * L * ldN * 16);
   lay.take(h->G, (size_t)T * N * ldN * 16);
@@ -1325,6 +1333,10 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
     h->ev_onepass = !(op && op[0] == '0');
     const char* tl = getenv("TRAJ_LOWRANK_TOL");
     if (tl) h->lowrank_tol = atof(tl);
+    const char* sm = getenv("TRAJ_SMALL_STEP");
+    const bool proj = cfg->protocol == TRAJ_PROJECTIVE;
+    h->small = !h->sh && !h->banded && h->K && !(sm && sm[0] == '0') && !h->lowrank_orth &&
+               (proj || cfg->protocol == TRAJ_HOMODYNE) && small_step_fits(h->L, h->N, proj);
   }
   if (cusolverDnCreate(&h->solver) != CUSOLVER_STATUS_SUCCESS) return bail(TRAJ_ECUDA, "cusolverDnCreate");
   cusolverDnSetStream(h->solver, h->st);
@@ -1398,6 +1410,36 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
 int traj_step(traj_handle h, int64_t n_steps) {
   if (!h) return TRAJ_EINVAL;
   if (n_steps < 0) return fail(h, TRAJ_EINVAL, "n_steps < 0");
+  if (h->small && n_steps > 0) {
+    Phase p(&h->prof, h->st, TRAJ_PH_FUSED);
+    SmallStepArgs a;
+    a.U = h->U[h->cur];
+    a.ldU = h->ldN;
+    a.sU = h->sU;
+    a.K = h->K;
+    a.ldK = h->ldL;
+    a.L = h->L;
+    a.N = h->N;
+    a.T = h->T;
+    a.projective = h->cfg.protocol == TRAJ_PROJECTIVE;
+    a.step0 = h->step;
+    a.n_steps = n_steps;
+    a.traj_base = h->cfg.traj_base;
+    a.seed = h->cfg.seed;
+    a.gamma = h->gamma_dev;
+    a.dt = h->cfg.dt;
+    a.failed = h->failed_dev;
+    a.last = h->small_last;
+    a.Dg = h->D0;
+    a.ldDg = h->ldcap;
+    a.sDg = h->sD;
+    a.cap = h->cap;
+    int r = small_steps(h->st, a, &h->err);
+    if (r) return fail(h, r, h->err);
+    h->step += n_steps;
+    h->small_last_dev = a.projective != 0;
+    return 0;
+  }
   for (int64_t s = 0; s < n_steps; ++s) {
     int r = h->sh ? shard_step(h->sh, &h->step, &h->err) : one_step(h);
     if (r) return fail(h, r, h->err);
@@ -1563,6 +1605,12 @@ int traj_last_clicks(traj_handle h, int64_t traj, int64_t* n_clicks, int64_t* n_
     CK(cudaMemcpyAsync(&v, h->occ_count + traj, 4, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
     h->last_n1[traj] = v;
+  }
+  if (h->small_last_dev) {   // fused small-lattice step: counts of the last step on the device
+    CK(cudaMemcpyAsync(h->h_small, h->small_last + 2 * traj, 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    h->last_nS[traj] = h->h_small[0];
+    h->last_n1[traj] = h->h_small[1];
   }
   if (n_clicks) *n_clicks = h->last_nS[traj];
   if (n_occupied) *n_occupied = h->last_n1[traj];

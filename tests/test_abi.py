@@ -98,3 +98,12 @@ def test_sharding_needs_single_trajectory(lib):
     c.n_traj = 2
     out = ctypes.c_size_t(0)
     assert lib.traj_workspace_bytes(ctypes.byref(c), ctypes.byref(out)) == 2
+
+
+def test_phase_names_match_the_header():
+    """binding.PHASES sizes the buffers traj_phase_times fills: one name per TRAJ_PH_* entry."""
+    txt = open(HEADER).read()
+    n = int(re.search(r"TRAJ_NPHASES\s*=\s*(\d+)", txt).group(1))
+    ids = [int(v) for v in re.findall(r"TRAJ_PH_[A-Z]+\s*=\s*(\d+)", txt)]
+    from paper_2508_18468_b200 import binding
+    assert len(binding.PHASES) == n == len(ids) and sorted(ids) == list(range(n))

@@ -695,3 +695,63 @@ def test_projective_l4096_lockstep(P, orth):
     assert np.abs(g.correlation(0).cpu().numpy() - o.correlation()).max() < C_TOL
     A = np.arange(L // 2)
     assert abs(g.entropy(A)[0] - o.entropy(A)) < S_TOL
+
+
+@pytest.mark.parametrize("Lx,Ly,protocol,gams", [(64, 1, "projective", [0.5, 0.3, 2.0]), (8, 8, "projective", [2.86]),
+                                                  (12, 8, "homodyne", [0.5, 3.0]), (50, 1, "homodyne", [1.0]),
+                                                  (10, 1, "projective", [20.0, 20.0]), (2, 1, "projective", [5.0])])
+def test_small_step_matches_general_path_and_oracle(P, Lx, Ly, protocol, gams, monkeypatch):
+    """The fused small-lattice step (small_step.cu: one CTA per trajectory, U in shared memory)
+    against the general multi-kernel path (TRAJ_SMALL_STEP=0) and the oracle on the same Philox
+    streams: identical click lists and outcomes, C within the north-star bar.  gamma dt = 1
+    (every site clicks) puts C_SS in global memory; L = 2 is the smallest lattice."""
+    monkeypatch.setenv("TRAJ_SMALL_STEP", "0")
+    a = P.Trajectories(Lx, Ly, protocol, gams, seed=23, traj_base=3)
+    monkeypatch.setenv("TRAJ_SMALL_STEP", "1")
+    b = P.Trajectories(Lx, Ly, protocol, gams, seed=23, traj_base=3)
+    K = lattice.propagator_lattice(Lx, Ly, 1.0, 0.05)
+    orc = [OracleTrajectory(Lx, Ly, protocol, g, 0.05, seed=23, traj=3 + t, K=K) for t, g in enumerate(gams)]
+    n0 = P.traj_kernel_launches()
+    b.step(1)
+    assert P.traj_kernel_launches() - n0 == 1          # the fused path ran: one launch per call
+    a.step(1)
+    for t, o in enumerate(orc):
+        o.step(1)
+    for s in range(1, 25):
+        if protocol == "projective":
+            for t, o in enumerate(orc):
+                S_, occ = o.last_clicks
+                assert a.last_clicks(t) == b.last_clicks(t) == (S_.size, int(occ.sum())), (s, t)
+        a.step(1)
+        b.step(1)
+        for o in orc:
+            o.step(1)
+    for t, o in enumerate(orc):
+        assert not b.failed(t)
+        ca, cb = a.correlation(t).cpu().numpy(), b.correlation(t).cpu().numpy()
+        assert np.abs(ca - cb).max() < C_TOL
+        assert np.abs(cb - o.correlation()).max() < C_TOL
+        U = b.get_state(t).cpu().numpy()
+        assert np.abs(U.conj().T @ U - np.eye(U.shape[1])).max() < 1e-13
+    A = np.arange(Lx * Ly // 2)
+    assert np.abs(b.entropy(A) - np.array([o.entropy(A) for o in orc])).max() < S_TOL
+    a.close()
+    b.close()
+
+
+def test_small_step_multi_step_launch_is_step_by_step(P):
+    """traj_step(n) runs n steps inside one launch: bit-identical to n calls of one step (same
+    kernel, same counters), and the click counts reported are those of the last step."""
+    a = P.Trajectories(64, 1, "projective", [0.5, 1.5], seed=9)
+    b = P.Trajectories(64, 1, "projective", [0.5, 1.5], seed=9)
+    n0 = P.traj_kernel_launches()
+    a.step(40)
+    assert P.traj_kernel_launches() - n0 == 1
+    for _ in range(40):
+        b.step(1)
+    for t in range(2):
+        assert a.last_clicks(t) == b.last_clicks(t)
+        assert np.array_equal(a.get_state(t).cpu().numpy(), b.get_state(t).cpu().numpy())
+    assert a.step_index == b.step_index == 40
+    a.close()
+    b.close()
