@@ -67,7 +67,7 @@ __device__ __forceinline__ bool decide_born(double p, double u1) {   // readings
 
 struct Carve {
   double2 *A, *B, *G, *uw, *wv;
-  double *piv, *u0, *u1;
+  double *piv, *u0, *u1, *red;
   int *S, *occ, *misc;
 };
 
@@ -88,6 +88,7 @@ __host__ __device__ inline size_t carve_small(int L, int N, bool proj, char* bas
   k.piv = reinterpret_cast<double*>(take(N * 8));
   k.u0 = reinterpret_cast<double*>(take(L * 8));
   k.u1 = reinterpret_cast<double*>(take(L * 8));
+  k.red = reinterpret_cast<double*>(take(NW * 8));
   k.S = reinterpret_cast<int*>(take(L * 4));
   k.occ = reinterpret_cast<int*>(take(L * 4));
   k.misc = reinterpret_cast<int*>(take(8 * 4));
@@ -288,6 +289,7 @@ __global__ void __launch_bounds__(SB, 1) small_step_kernel(SmallStepArgs a) {
     // triangle); B = A X.  N + 3 barriers per pass.
     for (int pass = 0; pass < 2 && !bad; ++pass) {
       double2* W = B;
+      double dev = 0.0;
       for (int p = warp; p < N; p += NW)
         for (int q = lane; q < N; q += 32) W[p * ld + q] = make_double2(p == q ? 1.0 : 0.0, 0.0);
       {   // G = A^dag A, tiles on and above the diagonal (DMMA)
@@ -302,46 +304,79 @@ __global__ void __launch_bounds__(SB, 1) small_step_kernel(SmallStepArgs a) {
                       [&](int k, int n) { return (k < L && q0 + n < N) ? Ad[k * ld + q0 + n] : make_double2(0.0, 0.0); },
                       L, lane >> 2, lane & 3, cr, ci);
           const int r = p0 + (lane >> 2), c0 = q0 + 2 * (lane & 3);
-          if (r < N) {
-            if (c0 < N) G[r * ld + c0] = make_double2(cr[0], ci[0]);
-            if (c0 + 1 < N) G[r * ld + c0 + 1] = make_double2(cr[1], ci[1]);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int cc = c0 + e;
+            if (r < N && cc < N) {
+              G[r * ld + cc] = make_double2(cr[e], ci[e]);
+              if (r <= cc) {   // max |G - I| over the upper triangle (NaN propagates)
+                const double d = fmax(fabs(cr[e] - (r == cc ? 1.0 : 0.0)), fabs(ci[e]));
+                dev = (d > dev || d != d) ? d : dev;
+              }
+            }
           }
         }
       }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double v = __shfl_xor_sync(0xffffffffu, dev, o);
+        dev = (v > dev || v != v) ? v : dev;
+      }
+      if (lane == 0) c.red[warp] = dev;
       __syncthreads();
-      for (int j = 0; j < N; ++j) {
-        const double p = G[j * ld + j].x;
-        if (!(p > 0.0) || !isfinite(p)) {   // the same value in every thread: uniform exit
-          bad = true;
-          break;
-        }
-        const double inv = 1.0 / p;
-        if (tid == 0) c.piv[j] = p;
-        for (int i = j + 1 + warp; i < N; i += NW) {
-          const double2 g = G[j * ld + i];           // l_ij = conj(G_ji) / p_j
-          const double lx = g.x * inv, ly = -g.y * inv;
-          for (int k = i + lane; k < N; k += 32) {   // G row i, upper part
-            const double2 r = G[j * ld + k];
-            G[i * ld + k].x -= lx * r.x - ly * r.y;
-            G[i * ld + k].y -= lx * r.y + ly * r.x;
+      // second pass: G = I + E with |E| ~ kappa^2 eps, R^-1 = I - triu(E, 1) - diag(E) / 2 up to
+      // O(N |E|^2), exact to rounding when N max|E|^2 < 1e-18 (the general path's rule and
+      // threshold, monitor.cu first_order_inverse); otherwise the full factorisation
+      bool first_order = false;
+      if (pass == 1 && !a.full_cqr2) {
+        double mx = 0.0;
+        for (int w = 0; w < NW; ++w) mx = (c.red[w] > mx || c.red[w] != c.red[w]) ? c.red[w] : mx;
+        first_order = mx <= 1e-9 / sqrt((double)N);
+        if (!first_order && tid == 0) atomicAdd(a.fallbacks, 1ull);
+      }
+      if (first_order) {
+        for (int p = warp; p < N; p += NW)
+          for (int q = p + lane; q < N; q += 32) {
+            const double2 v = G[p * ld + q];
+            G[p * ld + q] = q == p ? make_double2(1.0 - 0.5 * (v.x - 1.0), 0.0) : make_double2(-v.x, -v.y);
           }
-          for (int k = lane; k <= j; k += 32) {      // W row i, columns <= j
-            const double2 w = W[j * ld + k];
-            W[i * ld + k].x -= lx * w.x - ly * w.y;
-            W[i * ld + k].y -= lx * w.y + ly * w.x;
+        __syncthreads();
+      }
+      if (!first_order) {
+        for (int j = 0; j < N; ++j) {
+          const double p = G[j * ld + j].x;
+          if (!(p > 0.0) || !isfinite(p)) {   // the same value in every thread: uniform exit
+            bad = true;
+            break;
+          }
+          const double inv = 1.0 / p;
+          if (tid == 0) c.piv[j] = p;
+          for (int i = j + 1 + warp; i < N; i += NW) {
+            const double2 g = G[j * ld + i];           // l_ij = conj(G_ji) / p_j
+            const double lx = g.x * inv, ly = -g.y * inv;
+            for (int k = i + lane; k < N; k += 32) {   // G row i, upper part
+              const double2 r = G[j * ld + k];
+              G[i * ld + k].x -= lx * r.x - ly * r.y;
+              G[i * ld + k].y -= lx * r.y + ly * r.x;
+            }
+            for (int k = lane; k <= j; k += 32) {      // W row i, columns <= j
+              const double2 w = W[j * ld + k];
+              W[i * ld + k].x -= lx * w.x - ly * w.y;
+              W[i * ld + k].y -= lx * w.y + ly * w.x;
+            }
+          }
+          __syncthreads();
+        }
+        if (bad) break;
+        for (int i = warp; i < N; i += NW) {   // X_ki = conj(W_ik) / sqrt(p_i), k <= i
+          const double ir = 1.0 / sqrt(c.piv[i]);
+          for (int k = lane; k <= i; k += 32) {
+            const double2 w = W[i * ld + k];
+            G[k * ld + i] = make_double2(w.x * ir, -w.y * ir);
           }
         }
         __syncthreads();
       }
-      if (bad) break;
-      for (int i = warp; i < N; i += NW) {   // X_ki = conj(W_ik) / sqrt(p_i), k <= i
-        const double ir = 1.0 / sqrt(c.piv[i]);
-        for (int k = lane; k <= i; k += 32) {
-          const double2 w = W[i * ld + k];
-          G[k * ld + i] = make_double2(w.x * ir, -w.y * ir);
-        }
-      }
-      __syncthreads();
       {   // B = A X (DMMA), X upper triangular in G: k-steps past the tile's last column skipped
         const int NT = (N + 7) >> 3, MT = (L + 7) >> 3;
         for (int tile = warp; tile < MT * NT; tile += NW) {

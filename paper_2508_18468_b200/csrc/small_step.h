@@ -24,6 +24,8 @@ struct SmallStepArgs {
   cplx* Dg;                 // [T][cap][ldDg] global C_SS for click lists too long for the scratch
   long long ldDg, sDg;      //   buffer in shared memory (m (m + 1) > L (N + 1), e.g. gamma dt = 1)
   int cap;                  // click-list capacity: more clicks flag the trajectory as failed
+  int full_cqr2;            // 1: always factor the second Gram (TRAJ_CQR2_FULL=1)
+  unsigned long long* fallbacks;   // second passes that needed the full factorisation (atomic count)
 };
 
 // Dynamic shared memory the fused kernel needs for (L, N), in bytes.

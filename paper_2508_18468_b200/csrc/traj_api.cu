@@ -6,6 +6,7 @@
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 #include <complex>
@@ -130,6 +131,7 @@ struct traj_ctx {
   // traj_step call; the last step's click counts stay on the device (small_last [T][2])
   bool small = false;
   int32_t* small_last = nullptr;
+  unsigned long long* small_fallbacks = nullptr;   // full second-pass factorisations in the fused step
   bool small_last_dev = false;
   std::string err;
   Profiler prof;
@@ -301,6 +303,7 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     if (h->planar_cqr) lay.take(h->Xp, (size_t)T * 3 * N * h->ldP * 8);
   }
   lay.take(h->small_last, (size_t)T * 2 * 4);
+  lay.take(h->small_fallbacks, 8);
   lay.take(h->U[0], (size_t)T * L * ldN * 16);
   lay.take(h->U[1], (size_t)T * L * ldN * 16);
   lay.take(h->G, (size_t)T * N * ldN * 16);
@@ -1434,6 +1437,8 @@ int traj_step(traj_handle h, int64_t n_steps) {
     a.ldDg = h->ldcap;
     a.sDg = h->sD;
     a.cap = h->cap;
+    a.full_cqr2 = h->full_cqr2 ? 1 : 0;
+    a.fallbacks = h->small_fallbacks;
     int r = small_steps(h->st, a, &h->err);
     if (r) return fail(h, r, h->err);
     h->step += n_steps;
@@ -1620,6 +1625,13 @@ int traj_last_clicks(traj_handle h, int64_t traj, int64_t* n_clicks, int64_t* n_
 int traj_cqr2_fallbacks(traj_handle h, int64_t* n) {
   if (!h || !n) return TRAJ_EINVAL;
   *n = h->sh ? h->sh->cqr2_fallbacks : h->cqr2_fallbacks;
+  if (h->small) {   // the fused small-lattice step counts on the device
+    unsigned long long v = 0;
+    CK(cudaMemcpyAsync(h->h_dev, h->small_fallbacks, 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    memcpy(&v, h->h_dev, 8);
+    *n += (int64_t)v;
+  }
   return 0;
 }
 

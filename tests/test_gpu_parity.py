@@ -755,3 +755,46 @@ def test_small_step_multi_step_launch_is_step_by_step(P):
     assert a.step_index == b.step_index == 40
     a.close()
     b.close()
+
+
+def test_small_step_first_order_second_pass_and_fallback(P, monkeypatch):
+    """The fused step's CholeskyQR2 second pass uses the first-order R2^-1 (the general path's rule
+    and threshold): strong homodyne reweighting (gamma dt = 5, kappa up to ~3e4) gives the same
+    states as the full second factorisation (TRAJ_CQR2_FULL=1), the general path and the oracle;
+    an ill-conditioned state (kappa ~ 1e5: pass 1 leaves |E| ~ 1e-6) must fall back to the full
+    factorisation, counted by traj_cqr2_fallbacks."""
+    import torch
+    args = (32, 1, "homodyne", [100.0])
+    monkeypatch.setenv("TRAJ_SMALL_STEP", "0")
+    a = P.Trajectories(*args, seed=6)
+    monkeypatch.setenv("TRAJ_SMALL_STEP", "1")
+    b = P.Trajectories(*args, seed=6)
+    monkeypatch.setenv("TRAJ_CQR2_FULL", "1")
+    c = P.Trajectories(*args, seed=6)
+    monkeypatch.delenv("TRAJ_CQR2_FULL")
+    K = lattice.propagator_lattice(32, 1, 1.0, 0.05)
+    o = OracleTrajectory(32, 1, "homodyne", 100.0, 0.05, seed=6, traj=0, K=K)
+    for _ in range(20):
+        a.step(1)
+        b.step(1)
+        c.step(1)
+        o.step(1)
+    cb = b.correlation(0).cpu().numpy()
+    assert np.abs(cb - a.correlation(0).cpu().numpy()).max() < C_TOL
+    assert np.abs(cb - c.correlation(0).cpu().numpy()).max() < 1e-12
+    assert np.abs(cb - o.correlation()).max() < C_TOL
+    # gamma = 0: one step is K U, then CholeskyQR2 of the ill-conditioned K U
+    L, N = 32, 16
+    U = workloads.random_matrix(L, N, 3)
+    U[:, 1] = U[:, 0] + 1e-5 * U[:, 1]
+    d = P.Trajectories(L, 1, "homodyne", [0.0])
+    d.set_state(0, torch.from_numpy(U).cuda())
+    n0 = d.cqr2_fallbacks()
+    d.step(1)
+    assert d.cqr2_fallbacks() - n0 == 1
+    Ud = d.get_state(0).cpu().numpy()
+    assert np.abs(Ud.conj().T @ Ud - np.eye(N)).max() < 1e-12
+    ref = gaussian.correlation(gaussian.orthonormalize(K @ U))
+    assert np.abs(d.correlation(0).cpu().numpy() - ref).max() < 1e-9
+    for h in (a, b, c, d):
+        h.close()
