@@ -72,14 +72,21 @@ def workload(args):
     return w, tpg
 
 
+L2_BYTES = 126e6
+
+
 def describe(w, tpg):
     proto = f"{w.protocol} gamma={','.join(f'{g:g}' for g in w.gammas)}"
     lat = f"1d ring L={w.L}" if w.Ly == 1 else f"2d torus {w.Lx}x{w.Ly} (L={w.L})"
     return {"workload": f"{w.name}: {lat}, N={w.N}, {proto}, dt={w.dt}, Neel/checkerboard start, "
                         f"{tpg} trajectory(ies) per GPU, complex128",
             "L": w.L, "N": w.N, "protocol": w.protocol, "dt": w.dt, "traj_per_gpu": tpg,
-            "l2": "inputs larger than L2 (K is %.2f GB, U %.2f GB per trajectory; L2 = 126 MB)"
-                  % (16 * w.L * w.L / 1e9, 16 * w.L * w.N / 1e9)}
+            "l2": ("inputs larger than L2 (K is %.2f GB, U %.2f GB per trajectory; L2 = 126 MB)"
+                   % (16 * w.L * w.L / 1e9, 16 * w.L * w.N / 1e9)
+                   if 16.0 * w.L * w.L + 32.0 * w.L * w.N * tpg >= L2_BYTES else
+                   "K and U fit the 126 MB L2: L2 flushed (256 MB write) before every timed call of "
+                   f"{w.sample_every} steps (the config's sampling interval), per-call CUDA-event times summed"),
+            "steps_per_call": w.sample_every}
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -187,8 +194,16 @@ def run_ours(args):
         tr = P.Trajectories(w.Lx, w.Ly, w.protocol, gam, dt=w.dt, J=w.J, seed=w.seed, traj_base=base,
                             propagator=args.propagator, orthonormalizer=args.orthonormalizer)
     st = tr.stream
-    for _ in range(args.warmup):
-        tr.step(1)
+    # steps are issued the way a run of the config issues them: one traj_step call per interval
+    # between sampled observables (w.sample_every steps; the fused small-lattice path runs a call
+    # as one launch, the general path as its per-step launches)
+    def run_steps(n):
+        done = 0
+        while done < n:
+            k = min(max(1, w.sample_every), n - done)
+            tr.step(k)
+            done += k
+    run_steps(args.warmup)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -198,12 +213,29 @@ def run_ours(args):
     l0 = P.traj_kernel_launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    e0.record(st)
-    for _ in range(args.steps):
-        tr.step(1)
-    e1.record(st)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
+    fits_l2 = 16.0 * w.L * w.L + 32.0 * w.L * w.N * tpg < L2_BYTES
+    if fits_l2:
+        # K and U fit the L2: flush it (a 256 MB write) before every timed call, outside the
+        # event pair, and sum the per-call device times
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        ms, done = 0.0, 0
+        while done < args.steps:
+            k = min(max(1, w.sample_every), args.steps - done)
+            flush.fill_(done & 0xff)
+            torch.cuda.synchronize()
+            e0.record(st)
+            tr.step(k)
+            e1.record(st)
+            torch.cuda.synchronize()
+            ms += e0.elapsed_time(e1)
+            done += k
+        del flush
+    else:
+        e0.record(st)
+        run_steps(args.steps)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
     launches = P.traj_kernel_launches() - l0
     clk = clocks.stop()
     phases = tr.phase_times()

@@ -46,15 +46,35 @@ __device__ __forceinline__ double2 cmulcb(double2 a, double2 b) {  // a conj(b)
 // fb(k, n) returns B[k][n0 + n] (zero outside the operands); op(A) = conj(A) when CONJ_A.
 template <bool CONJ_A, class FA, class FB>
 __device__ __forceinline__ void ztile(FA fa, FB fb, int K, int g, int slot, double* cr, double* ci) {
-  for (int k0 = 0; k0 < K; k0 += 4) {
+  // two accumulator sets (even / odd k-steps) halve the dependent DMMA chains
+  double r1[2] = {0.0, 0.0}, i1[2] = {0.0, 0.0};
+  int k0 = 0;
+  for (; k0 + 4 < K; k0 += 8) {
+    const double2 av = fa(g, k0 + slot), aw = fa(g, k0 + 4 + slot);
+    const double2 bv = fb(k0 + slot, g), bw = fb(k0 + 4 + slot, g);
+    const double ai = CONJ_A ? -av.y : av.y, aj = CONJ_A ? -aw.y : aw.y;
+    dmma_8x8x4(cr[0], cr[1], av.x, bv.x);
+    dmma_8x8x4(r1[0], r1[1], aw.x, bw.x);
+    dmma_8x8x4(ci[0], ci[1], av.x, bv.y);
+    dmma_8x8x4(i1[0], i1[1], aw.x, bw.y);
+    dmma_8x8x4(cr[0], cr[1], -ai, bv.y);
+    dmma_8x8x4(r1[0], r1[1], -aj, bw.y);
+    dmma_8x8x4(ci[0], ci[1], ai, bv.x);
+    dmma_8x8x4(i1[0], i1[1], aj, bw.x);
+  }
+  if (k0 < K) {
     const double2 av = fa(g, k0 + slot);
     const double2 bv = fb(k0 + slot, g);
     const double ai = CONJ_A ? -av.y : av.y;
     dmma_8x8x4(cr[0], cr[1], av.x, bv.x);
-    dmma_8x8x4(cr[0], cr[1], -ai, bv.y);
     dmma_8x8x4(ci[0], ci[1], av.x, bv.y);
+    dmma_8x8x4(cr[0], cr[1], -ai, bv.y);
     dmma_8x8x4(ci[0], ci[1], ai, bv.x);
   }
+  cr[0] += r1[0];
+  cr[1] += r1[1];
+  ci[0] += i1[0];
+  ci[1] += i1[1];
 }
 
 __device__ __forceinline__ bool decide_born(double p, double u1) {   // readings Q13, Q17
