@@ -298,16 +298,23 @@ __global__ void __launch_bounds__(SB, 1) small_step_kernel(SmallStepArgs a) {
       for (int r = warp; r < m; r += NW)   // empty sites: rows zeroed
         if (!c.occ[r])
           for (int k = lane; k < N; k += 32) A[c.S[r] * ld + k] = make_double2(0.0, 0.0);
-      if (tid == 0 && s == a.n_steps - 1) {
-        a.last[2 * t] = m;
-        a.last[2 * t + 1] = k1;
+      if (tid == 0) {
+        c.misc[1] = m - k1;   // zeroed rows
+        if (s == a.n_steps - 1) {
+          a.last[2 * t] = m;
+          a.last[2 * t + 1] = k1;
+        }
       }
       __syncthreads();
     }
     // ---- (a3) CholeskyQR2.  Per pass: G = A^dag A (upper); Gaussian elimination of [G | I] on
     // unscaled rows, G = L D L^dag, W = L^-1 (in B); X = R^-1 = W^dag D^-1/2 (into G's upper
     // triangle); B = A X.  N + 3 barriers per pass.
-    for (int pass = 0; pass < 2 && !bad; ++pass) {
+    // projective: the occupied-site maps are exact isometries and K is unitary, so with no row
+    // zeroed U is orthonormal to rounding and pass 1 has R = I (the general path's rule with the
+    // low-rank first Gram on; pass 2 still measures the Gram and certifies the result)
+    const bool skip1 = proj && a.skip_orthonormal_pass && c.misc[1] == 0;
+    for (int pass = skip1 ? 1 : 0; pass < 2 && !bad; ++pass) {
       double2* W = B;
       double dev = 0.0;
       for (int p = warp; p < N; p += NW)

@@ -25,6 +25,7 @@ struct SmallStepArgs {
   long long ldDg, sDg;      //   buffer in shared memory (m (m + 1) > L (N + 1), e.g. gamma dt = 1)
   int cap;                  // click-list capacity: more clicks flag the trajectory as failed
   int full_cqr2;            // 1: always factor the second Gram (TRAJ_CQR2_FULL=1)
+  int skip_orthonormal_pass;  // 1: projective step with no zeroed row skips CholeskyQR pass 1
   unsigned long long* fallbacks;   // second passes that needed the full factorisation (atomic count)
 };
 

@@ -1438,6 +1438,7 @@ int traj_step(traj_handle h, int64_t n_steps) {
     a.sDg = h->sD;
     a.cap = h->cap;
     a.full_cqr2 = h->full_cqr2 ? 1 : 0;
+    a.skip_orthonormal_pass = h->lowrank_gram ? 1 : 0;
     a.fallbacks = h->small_fallbacks;
     int r = small_steps(h->st, a, &h->err);
     if (r) return fail(h, r, h->err);
