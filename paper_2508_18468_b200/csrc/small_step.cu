@@ -17,7 +17,7 @@
 // projections are applied one at a time instead of monitor.cu's block rank-k update: both give
 // span(E_S1) + Z_S0 U null(U_S1) (the projectors of distinct sites commute), i.e. the same
 // C = U U^dag after CholeskyQR2.  The Cholesky factor's inverse comes from Gaussian elimination
-// of [G | I] on unscaled rows (one barrier per pivot), U R^-1 is then one product.  The three
+// of [G | I] on unscaled rows (two pivots per barrier), U R^-1 is then one product.  The three
 // GEMM-shaped phases (K U, U^dag U, U X) run on the FP64 tensor pipe (m8n8k4 DMMA, 8 x 8 complex
 // tiles, one per warp at a time); the rest is DFMA with rows on warps and columns on lanes.
 #include <math.h>
@@ -370,26 +370,95 @@ __global__ void __launch_bounds__(SB, 1) small_step_kernel(SmallStepArgs a) {
         __syncthreads();
       }
       if (!first_order) {
-        for (int j = 0; j < N; ++j) {
-          const double p = G[j * ld + j].x;
-          if (!(p > 0.0) || !isfinite(p)) {   // the same value in every thread: uniform exit
+        // two pivots (a, a + 1) per barrier: row a + 1 after pivot a is formed on the fly,
+        //   m = conj(G_a,a+1) / p_a,  G'_a+1,k = G_a+1,k - m G_a,k,  p_a+1 = G'_a+1,a+1,
+        // and each row i > a + 1 takes  row_i -= c_a row_a + c_b row_a+1  (G: k >= i; W: k <= a + 1)
+        // with l_a = conj(G_a,i) / p_a, c_b = conj(G'_a+1,i) / p_a+1, c_a = l_a - c_b m.  W's row
+        // a + 1 itself becomes W_a+1 - m W_a in the next phase (nobody reads it there).
+        int prev = -1;   // first pivot of the previous pair: W row prev + 1 still pending
+        for (int j = 0; j < N; j += 2) {
+          const bool pair = j + 1 < N;
+          const double pa = G[j * ld + j].x;
+          if (!(pa > 0.0) || !isfinite(pa)) {   // the same values in every thread: uniform exit
             bad = true;
             break;
           }
-          const double inv = 1.0 / p;
-          if (tid == 0) c.piv[j] = p;
-          for (int i = j + 1 + warp; i < N; i += NW) {
-            const double2 g = G[j * ld + i];           // l_ij = conj(G_ji) / p_j
-            const double lx = g.x * inv, ly = -g.y * inv;
-            for (int k = i + lane; k < N; k += 32) {   // G row i, upper part
-              const double2 r = G[j * ld + k];
-              G[i * ld + k].x -= lx * r.x - ly * r.y;
-              G[i * ld + k].y -= lx * r.y + ly * r.x;
+          const double ia = 1.0 / pa;
+          double2 mm = make_double2(0.0, 0.0);
+          double ib = 0.0;
+          if (pair) {
+            const double2 gab = G[j * ld + j + 1];
+            mm = make_double2(gab.x * ia, -gab.y * ia);
+            const double pb = G[(j + 1) * ld + j + 1].x - (gab.x * gab.x + gab.y * gab.y) * ia;
+            if (!(pb > 0.0) || !isfinite(pb)) {
+              bad = true;
+              break;
             }
-            for (int k = lane; k <= j; k += 32) {      // W row i, columns <= j
-              const double2 w = W[j * ld + k];
-              W[i * ld + k].x -= lx * w.x - ly * w.y;
-              W[i * ld + k].y -= lx * w.y + ly * w.x;
+            ib = 1.0 / pb;
+            if (tid == 0) c.piv[j + 1] = pb;
+          }
+          if (tid == 0) c.piv[j] = pa;
+          if (prev >= 0 && warp == NW - 1) {   // the previous pair's pending W row
+            const double2 g = G[prev * ld + prev + 1];
+            const double ip = 1.0 / c.piv[prev];
+            const double mx = g.x * ip, my = -g.y * ip;
+            for (int k = lane; k <= prev; k += 32) {
+              const double2 w = W[prev * ld + k];
+              W[(prev + 1) * ld + k].x -= mx * w.x - my * w.y;
+              W[(prev + 1) * ld + k].y -= mx * w.y + my * w.x;
+            }
+          }
+          const int b = pair ? j + 1 : j;
+          for (int i = b + 1 + warp; i < N; i += NW) {
+            const double2 gai = G[j * ld + i];
+            const double lax = gai.x * ia, lay = -gai.y * ia;              // l_a
+            double cax = lax, cay = lay, cbx = 0.0, cby = 0.0;
+            if (pair) {
+              const double2 gbi = G[(j + 1) * ld + i];
+              const double2 gpi = make_double2(gbi.x - (mm.x * gai.x - mm.y * gai.y),
+                                               gbi.y - (mm.x * gai.y + mm.y * gai.x));   // G'_a+1,i
+              cbx = gpi.x * ib;
+              cby = -gpi.y * ib;
+              cax = lax - (cbx * mm.x - cby * mm.y);
+              cay = lay - (cbx * mm.y + cby * mm.x);
+            }
+            for (int k = i + lane; k < N; k += 32) {   // G row i, upper part
+              const double2 ra = G[j * ld + k];
+              double2 v = G[i * ld + k];
+              v.x -= cax * ra.x - cay * ra.y;
+              v.y -= cax * ra.y + cay * ra.x;
+              if (pair) {
+                const double2 rb = G[(j + 1) * ld + k];
+                v.x -= cbx * rb.x - cby * rb.y;
+                v.y -= cbx * rb.y + cby * rb.x;
+              }
+              G[i * ld + k] = v;
+            }
+            for (int k = lane; k <= b; k += 32) {      // W row i, columns <= b
+              const double2 wa = W[j * ld + k];
+              double2 v = W[i * ld + k];
+              v.x -= cax * wa.x - cay * wa.y;
+              v.y -= cax * wa.y + cay * wa.x;
+              if (pair) {
+                const double2 wb = W[(j + 1) * ld + k];
+                v.x -= cbx * wb.x - cby * wb.y;
+                v.y -= cbx * wb.y + cby * wb.x;
+              }
+              W[i * ld + k] = v;
+            }
+          }
+          prev = pair ? j : -1;
+          __syncthreads();
+        }
+        if (!bad && prev >= 0) {   // the last pair's pending W row
+          if (warp == NW - 1) {
+            const double2 g = G[prev * ld + prev + 1];
+            const double ip = 1.0 / c.piv[prev];
+            const double mx = g.x * ip, my = -g.y * ip;
+            for (int k = lane; k <= prev; k += 32) {
+              const double2 w = W[prev * ld + k];
+              W[(prev + 1) * ld + k].x -= mx * w.x - my * w.y;
+              W[(prev + 1) * ld + k].y -= mx * w.y + my * w.x;
             }
           }
           __syncthreads();
