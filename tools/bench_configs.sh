@@ -12,6 +12,7 @@ python bench.py --config c2 --propagator banded --steps 10 --warmup 3 $common >>
 python bench.py --config c5 --steps 2 --warmup 2 $common >> $out 2>/dev/null
 python bench.py --config c5 --propagator banded --steps 3 --warmup 2 $common >> $out 2>/dev/null
 python bench.py --config c5 --propagator banded --orthonormalizer lowrank --steps 3 --warmup 2 $common >> $out 2>/dev/null
+python bench.py --orthonormalizer lowrank --steps 5 --warmup 3 $common >> $out 2>/dev/null
 python bench.py --propagator banded --steps 5 --warmup 3 $common >> $out 2>/dev/null
 python bench.py --propagator banded --orthonormalizer lowrank --steps 10 --warmup 3 $common >> $out 2>/dev/null
 python bench.py --protocol homodyne --steps 5 --warmup 3 $common >> $out 2>/dev/null
