@@ -129,7 +129,11 @@ int traj_init(const traj_config* cfg, traj_handle* out);
 /* Advance every trajectory by n_steps >= 0 steps (P:203-209 / P:171-196).  Step s
  * draws Philox counters (site, s, traj_base + t, 0).  Asynchronous for the homodyne
  * protocol; the projective protocol synchronises once per step to size its click
- * list.  A trajectory whose Cholesky breaks down is marked failed (traj_failed). */
+ * list.  A trajectory whose Cholesky breaks down is marked failed (traj_failed).
+ * Small lattices (dense K, projective or homodyne, unsharded, U and the step's scratch
+ * within one CTA's shared memory: L up to ~110) run all n_steps in one asynchronous launch
+ * of the fused step (one CTA per trajectory); there a failed trajectory stops evolving.
+ * TRAJ_SMALL_STEP=0 in the environment at traj_init selects the general path. */
 int traj_step(traj_handle h, int64_t n_steps);
 
 /* Re-orthonormalise every trajectory with CholeskyQR2 (step (c) alone). */
