@@ -68,7 +68,9 @@ def workload(args):
     if args.protocol:
         import dataclasses
         w = dataclasses.replace(w, protocol=args.protocol)
-    tpg = args.traj_per_gpu or (1 if args.config in ("c3", "c5") else 8)
+    # trajectories per GPU: c3/c5 one (row-shardable); c1 all 16 of the config ("16,
+    # batched on 1 GPU"); c2/c4 8 of their 192/256 (memory and time of a default run)
+    tpg = args.traj_per_gpu or {"c3": 1, "c5": 1, "c1": 16}.get(args.config, 8)
     return w, tpg
 
 

@@ -798,3 +798,25 @@ def test_small_step_first_order_second_pass_and_fallback(P, monkeypatch):
     assert np.abs(d.correlation(0).cpu().numpy() - ref).max() < 1e-9
     for h in (a, b, c, d):
         h.close()
+
+
+def test_small_step_failed_trajectory_is_flagged_and_frozen(P):
+    """A rank-deficient state makes the fused step's Cholesky break down: that trajectory is
+    flagged (traj_failed) and stops evolving, the other trajectories of the batch are unaffected
+    and still match the oracle."""
+    import torch
+    L = 32
+    g = P.Trajectories(L, 1, "homodyne", [0.5, 0.5], seed=8)
+    U = workloads.random_matrix(L, L // 2, 5)
+    U[:, 1] = U[:, 0]                         # exactly rank deficient
+    g.set_state(0, torch.from_numpy(U).cuda())
+    g.step(3)
+    assert g.failed(0) and not g.failed(1)
+    U0 = g.get_state(0).cpu().numpy()
+    g.step(2)
+    assert np.array_equal(g.get_state(0).cpu().numpy(), U0)   # frozen
+    K = lattice.propagator_lattice(L, 1, 1.0, 0.05)
+    o = OracleTrajectory(L, 1, "homodyne", 0.5, 0.05, seed=8, traj=1, K=K)
+    o.step(5)
+    assert np.abs(g.correlation(1).cpu().numpy() - o.correlation()).max() < C_TOL
+    g.close()
