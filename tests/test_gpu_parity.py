@@ -699,12 +699,14 @@ def test_projective_l4096_lockstep(P, orth):
 
 @pytest.mark.parametrize("Lx,Ly,protocol,gams", [(64, 1, "projective", [0.5, 0.3, 2.0]), (8, 8, "projective", [2.86]),
                                                   (12, 8, "homodyne", [0.5, 3.0]), (50, 1, "homodyne", [1.0]),
-                                                  (10, 1, "projective", [20.0, 20.0]), (2, 1, "projective", [5.0])])
+                                                  (10, 1, "projective", [20.0, 20.0]), (2, 1, "projective", [5.0]),
+                                                  (104, 1, "projective", [4.0]), (10, 10, "projective", [5.72])])
 def test_small_step_matches_general_path_and_oracle(P, Lx, Ly, protocol, gams, monkeypatch):
     """The fused small-lattice step (small_step.cu: one CTA per trajectory, U in shared memory)
     against the general multi-kernel path (TRAJ_SMALL_STEP=0) and the oracle on the same Philox
     streams: identical click lists and outcomes, C within the north-star bar.  gamma dt = 1
-    (every site clicks) puts C_SS in global memory; L = 2 is the smallest lattice."""
+    (every site clicks) puts C_SS in global memory; L = 2 is the smallest lattice, L = 104 the largest
+    1d ring whose state fits one CTA's shared memory."""
     monkeypatch.setenv("TRAJ_SMALL_STEP", "0")
     a = P.Trajectories(Lx, Ly, protocol, gams, seed=23, traj_base=3)
     monkeypatch.setenv("TRAJ_SMALL_STEP", "1")
@@ -820,3 +822,18 @@ def test_small_step_failed_trajectory_is_flagged_and_frozen(P):
     o.step(5)
     assert np.abs(g.correlation(1).cpu().numpy() - o.correlation()).max() < C_TOL
     g.close()
+
+
+def test_small_step_size_boundary(P):
+    """L = 104 (N = 52) still fits the fused step (one launch per call); L = 106 does not and runs
+    the general multi-kernel path."""
+    a = P.Trajectories(104, 1, "homodyne", [0.5])
+    b = P.Trajectories(106, 1, "homodyne", [0.5])
+    n0 = P.traj_kernel_launches()
+    a.step(3)
+    n1 = P.traj_kernel_launches()
+    b.step(3)
+    n2 = P.traj_kernel_launches()
+    assert n1 - n0 == 1 and n2 - n1 > 3
+    a.close()
+    b.close()
