@@ -567,7 +567,9 @@ def run_reference(args):
            "value": v, "unit": unit, "impl": "reference", "n_gpus": world, "steps": len(times), "warmup": 0,
            "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "c128 (f64 arithmetic)", "data": "synthetic (Neel start, Philox randoms, seed 0)",
-           "config": describe(w, 1),
+           "config": dict(describe(w, tpg), oracle_note=(
+               f"the oracle steps one trajectory at a time; the {tpg} trajectories of the config are "
+               "independent and cost the same, so the rate of one is the config's per-trajectory rate")),
            "cpu_baseline": {"value": v, "unit": unit, "cores": cpu_cores(), "kind": "oracle",
                             "sample": f"{len(times)} oracle step(s) of one {w.name} trajectory (budget "
                                       f"{args.cpu_budget:.0f} s; no warm-up: NumPy has no JIT), {'; '.join(blas)}"},
