@@ -12,6 +12,7 @@
 // the 64 x 64 diagonal leaves run in a small shared-memory kernel.  R_B^dag is kept in
 // G's (unused) strict lower triangle, so the only scratch is the h x (n-h) product.
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <vector>
@@ -119,6 +120,131 @@ __global__ void __launch_bounds__(TW * TW) chol_leaf_kernel(int n, cplx* G, long
   if (tid == 0 && bad && failed) failed[b] = 1;
 }
 
+// The same leaf by Gaussian elimination of [G | I] in shared memory (the fused small step's
+// scheme, small_step.cu): 16 warps, rows on warps and columns on lanes, two pivots per barrier --
+// row a + 1 after pivot a is formed on the fly (m = conj(G_a,a+1) / p_a, p_a+1 = G_a+1,a+1 -
+// |G_a,a+1|^2 / p_a) and each row i > a + 1 takes row_i -= c_a row_a + c_b row_a+1 with
+// c_b = conj(G_a+1,i - m G_a,i) / p_a+1, c_a = conj(G_a,i) / p_a - c_b m; W's row a + 1 becomes
+// W_a+1 - m W_a one phase later.  W ends as L^-1 of G = L D L^dag on unscaled rows and
+// X = R^-1 = W^dag D^-1/2.  A non-positive pivot flags the batch entry and fills X with NaN.
+constexpr int EW = 16;            // warps of the elimination leaf
+constexpr int ELD = NB + 1;
+
+__device__ __forceinline__ void pending_w_row(double2* Ws, const double2* Gs, const double* piv, int prev, int lane) {
+  const double2 g = Gs[prev * ELD + prev + 1];
+  const double ip = 1.0 / piv[prev];
+  const double mx = g.x * ip, my = -g.y * ip;
+  for (int k = lane; k <= prev; k += 32) {
+    const double2 w = Ws[prev * ELD + k];
+    Ws[(prev + 1) * ELD + k].x -= mx * w.x - my * w.y;
+    Ws[(prev + 1) * ELD + k].y -= mx * w.y + my * w.x;
+  }
+}
+
+__global__ void __launch_bounds__(EW * 32) chol_leaf_elim_kernel(int n, const cplx* G, long long ldg, long long sG,
+                                                                 cplx* X, long long ldx, long long sX, int32_t* failed) {
+  extern __shared__ __align__(16) double2 lsm[];
+  double2* Gs = lsm;                 // [NB][ELD] upper triangle, eliminated in place
+  double2* Ws = lsm + NB * ELD;      // [NB][ELD] W = L^-1 (lower)
+  __shared__ double piv[NB];
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const cplx* g = G + b * sG;
+  cplx* x = X + b * sX;
+  for (int i = warp; i < n; i += EW)
+    for (int k = lane; k < n; k += 32) {
+      if (k >= i) Gs[i * ELD + k] = g[(long long)i * ldg + k];
+      Ws[i * ELD + k] = make_double2(i == k ? 1.0 : 0.0, 0.0);
+    }
+  __syncthreads();
+  bool bad = false;
+  int prev = -1;
+  for (int j = 0; j < n; j += 2) {
+    const bool pair = j + 1 < n;
+    const double pa = Gs[j * ELD + j].x;
+    if (!(pa > 0.0) || !isfinite(pa)) {   // the same value in every thread: uniform exit
+      bad = true;
+      break;
+    }
+    const double ia = 1.0 / pa;
+    double2 mm = make_double2(0.0, 0.0);
+    double ib = 0.0;
+    if (pair) {
+      const double2 gab = Gs[j * ELD + j + 1];
+      mm = make_double2(gab.x * ia, -gab.y * ia);
+      const double pb = Gs[(j + 1) * ELD + j + 1].x - (gab.x * gab.x + gab.y * gab.y) * ia;
+      if (!(pb > 0.0) || !isfinite(pb)) {
+        bad = true;
+        break;
+      }
+      ib = 1.0 / pb;
+      if (tid == 0) piv[j + 1] = pb;
+    }
+    if (tid == 0) piv[j] = pa;
+    if (prev >= 0 && warp == EW - 1) pending_w_row(Ws, Gs, piv, prev, lane);
+    const int bb = pair ? j + 1 : j;
+    for (int i = bb + 1 + warp; i < n; i += EW) {
+      const double2 gai = Gs[j * ELD + i];
+      const double lax = gai.x * ia, lay = -gai.y * ia;
+      double cax = lax, cay = lay, cbx = 0.0, cby = 0.0;
+      if (pair) {
+        const double2 gbi = Gs[(j + 1) * ELD + i];
+        const double px = gbi.x - (mm.x * gai.x - mm.y * gai.y), py = gbi.y - (mm.x * gai.y + mm.y * gai.x);
+        cbx = px * ib;
+        cby = -py * ib;
+        cax = lax - (cbx * mm.x - cby * mm.y);
+        cay = lay - (cbx * mm.y + cby * mm.x);
+      }
+      for (int k = i + lane; k < n; k += 32) {
+        const double2 ra = Gs[j * ELD + k];
+        double2 v = Gs[i * ELD + k];
+        v.x -= cax * ra.x - cay * ra.y;
+        v.y -= cax * ra.y + cay * ra.x;
+        if (pair) {
+          const double2 rb = Gs[(j + 1) * ELD + k];
+          v.x -= cbx * rb.x - cby * rb.y;
+          v.y -= cbx * rb.y + cby * rb.x;
+        }
+        Gs[i * ELD + k] = v;
+      }
+      for (int k = lane; k <= bb; k += 32) {
+        const double2 wa = Ws[j * ELD + k];
+        double2 v = Ws[i * ELD + k];
+        v.x -= cax * wa.x - cay * wa.y;
+        v.y -= cax * wa.y + cay * wa.x;
+        if (pair) {
+          const double2 wb = Ws[(j + 1) * ELD + k];
+          v.x -= cbx * wb.x - cby * wb.y;
+          v.y -= cbx * wb.y + cby * wb.x;
+        }
+        Ws[i * ELD + k] = v;
+      }
+    }
+    prev = pair ? j : -1;
+    __syncthreads();
+  }
+  if (!bad && prev >= 0) {
+    if (warp == EW - 1) pending_w_row(Ws, Gs, piv, prev, lane);
+    __syncthreads();
+  }
+  // X_ki = conj(W_ik) / sqrt(p_i) for k <= i, zero below the diagonal
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
+  for (int k = warp; k < n; k += EW)
+    for (int i = lane; i < n; i += 32) {
+      double2 v = make_double2(0.0, 0.0);
+      if (bad) {
+        v = make_double2(nan, nan);
+      } else if (k <= i) {
+        const double ir = 1.0 / sqrt(piv[i]);
+        const double2 w = Ws[i * ELD + k];
+        v = make_double2(w.x * ir, -w.y * ir);
+      }
+      x[(long long)k * ldx + i] = v;
+    }
+  if (tid == 0 && bad && failed) failed[b] = 1;
+}
+
+constexpr int ELEAF_SMEM = 2 * NB * ELD * 16;
+
 int split(long long n) { return (int)(NB * ceil_div(ceil_div(n, NB), 2)); }
 
 struct Ctx {
@@ -135,6 +261,7 @@ struct Ctx {
   const CholDist* dist;
   const CholHook* hook;
   long long n_top;
+  bool elim_leaf;
 };
 
 // row slice boundaries of M rows over P ranks, 128-aligned; tri: equal area of an upper triangle
@@ -171,12 +298,20 @@ int dist_gemm(Ctx& c, bool tri_c, int opA, int opB, long long M, long long N, lo
 
 int rec(Ctx& c, long long o, long long n) {
   if (n <= NB) {
-    auto leaf = n <= 16 ? chol_leaf_kernel<8, 2> : (n <= 32 ? chol_leaf_kernel<16, 2> : chol_leaf_kernel<32, 2>);
-    const int threads = n <= 16 ? 64 : (n <= 32 ? 256 : 1024);
-    leaf<<<(unsigned)c.batch, threads, 0, c.st>>>((int)n, c.G + o * c.ldg + o, c.ldg, c.sG,
-                                                                      c.X + o * c.ldx + o, c.ldx, c.sX, c.failed);
+    cudaError_t e = cudaSuccess;
+    if (n > 16 && c.elim_leaf) {   // elimination leaf (TRAJ_CHOL_LEAF=regs: the register-blocked one)
+      e = ensure_smem(reinterpret_cast<const void*>(chol_leaf_elim_kernel), ELEAF_SMEM);
+      if (e == cudaSuccess)
+        chol_leaf_elim_kernel<<<(unsigned)c.batch, EW * 32, ELEAF_SMEM, c.st>>>(
+            (int)n, c.G + o * c.ldg + o, c.ldg, c.sG, c.X + o * c.ldx + o, c.ldx, c.sX, c.failed);
+    } else {
+      auto leaf = n <= 16 ? chol_leaf_kernel<8, 2> : (n <= 32 ? chol_leaf_kernel<16, 2> : chol_leaf_kernel<32, 2>);
+      const int threads = n <= 16 ? 64 : (n <= 32 ? 256 : 1024);
+      leaf<<<(unsigned)c.batch, threads, 0, c.st>>>((int)n, c.G + o * c.ldg + o, c.ldg, c.sG, c.X + o * c.ldx + o,
+                                                    c.ldx, c.sX, c.failed);
+    }
     count_launch();
-    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) {
       if (c.err) *c.err = std::string("chol leaf: ") + cudaGetErrorString(e);
       return 4;
@@ -259,6 +394,10 @@ int chol_inverse(cudaStream_t st, long long n, cplx* G, long long ldg, long long
   c.dist = dist;
   c.hook = hook;
   c.n_top = n;
+  {
+    const char* lf = getenv("TRAJ_CHOL_LEAF");
+    c.elim_leaf = !(lf && lf[0] == 'r');
+  }
   if (n > NB) {
     // the strict lower triangle of X must read as zeros (triangular GEMM tiles cross it)
     cudaError_t e = cudaSuccess;
