@@ -4,7 +4,8 @@
 out=gpurun_out/bench_configs.jsonl
 : > $out
 common="--no-cpu-baseline --no-e2e --no-observables --secondary none"
-for c in c1 c2 c4; do
+python bench.py --config c1 --steps 200 --warmup 10 $common >> $out 2>/dev/null
+for c in c2 c4; do
   python bench.py --config $c --steps 10 --warmup 3 $common >> $out 2>/dev/null
 done
 python bench.py --config c4 --propagator banded --steps 10 --warmup 3 $common >> $out 2>/dev/null
