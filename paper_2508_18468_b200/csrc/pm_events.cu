@@ -15,6 +15,7 @@
 
 #include <algorithm>
 
+#include <stdlib.h>
 #include "common.cuh"
 #include "pm_events.h"
 
@@ -363,7 +364,9 @@ struct EvTaps {
 
 // 1d ring: EV_R (8 for W <= 6, else 4: registers) consecutive rows per CTA, each input row loaded once per column into a register
 // window.  out_i = sum_d c_d U_{i+d} + x_i yhat (x_i from g), gn_i = <out_i, yhat_next>.
-template <int W, int EV_R>
+// ALT: the taps of K(tau) on the bipartite ring alternate real / imaginary, c_d = (-i)^|d| J_|d|(2 J tau)
+// (axis_taps builds them in exactly that form), so each tap is two FMAs instead of four.
+template <int W, int EV_R, bool ALT>
 __global__ void __launch_bounds__(256) ev_pass_1d_kernel(const cplx* __restrict__ U, cplx* __restrict__ out,
                                                          long long ld, int N, int L,
                                                          const __grid_constant__ EvTaps<W> taps,
@@ -418,10 +421,18 @@ __global__ void __launch_bounds__(256) ev_pass_1d_kernel(const cplx* __restrict_
 #pragma unroll
       for (int d = 0; d < 2 * W + 1; ++d) {
         const double2 b = in[r + d];
-        re = fma(taps.c[d][0], b.x, re);
-        re = fma(taps.c[d][2], b.y, re);
-        im = fma(taps.c[d][0], b.y, im);
-        im = fma(taps.c[d][1], b.x, im);
+        if (!ALT) {
+          re = fma(taps.c[d][0], b.x, re);
+          re = fma(taps.c[d][2], b.y, re);
+          im = fma(taps.c[d][0], b.y, im);
+          im = fma(taps.c[d][1], b.x, im);
+        } else if (((d - W) & 1) == 0) {   // real tap
+          re = fma(taps.c[d][0], b.x, re);
+          im = fma(taps.c[d][0], b.y, im);
+        } else {                           // imaginary tap i s: (re, im) += (-s b.y, s b.x)
+          re = fma(taps.c[d][2], b.y, re);
+          im = fma(taps.c[d][1], b.x, im);
+        }
       }
       if (i0 + r < L) out[(long long)(i0 + r) * ld + k] = make_double2(re, im);
       ar[r] += re * ynk.x + im * ynk.y;
@@ -531,6 +542,12 @@ __global__ void __launch_bounds__(256) ev_pass_generic_kernel(const cplx* __rest
   }
 }
 
+// TRAJ_EV_ALT_TAPS=0: always the general four-FMA taps
+bool ev_alt_taps() {
+  const char* e = getenv("TRAJ_EV_ALT_TAPS");
+  return !(e && e[0] == '0');
+}
+
 template <int W>
 cudaError_t launch_pass_1d(cudaStream_t st, const cplx* U, cplx* out, long long ld, int N, int L,
                            const cplx* taps_host, int w, const cplx* y, const double* coef, const double2* g, int j,
@@ -538,12 +555,19 @@ cudaError_t launch_pass_1d(cudaStream_t st, const cplx* U, cplx* out, long long 
   constexpr int R = W <= 6 ? 8 : 4;
   EvTaps<W> t;
   for (int d = 0; d < 2 * W + 1; ++d) t.c[d][0] = t.c[d][1] = t.c[d][2] = 0.0;
+  bool alt = true;   // even offsets purely real, odd offsets purely imaginary (exactly)
   for (int d = 0; d < 2 * w + 1; ++d) {
     t.c[W - w + d][0] = taps_host[d].x;
     t.c[W - w + d][1] = taps_host[d].y;
     t.c[W - w + d][2] = -taps_host[d].y;
+    alt = alt && (((d - w) & 1) == 0 ? taps_host[d].y == 0.0 : taps_host[d].x == 0.0);
   }
-  ev_pass_1d_kernel<W, R><<<(unsigned)ceil_div(L, R), 256, 0, st>>>(U, out, ld, N, L, t, y, coef, g, j, yn, coefn, gn);
+  if (alt && ev_alt_taps())
+    ev_pass_1d_kernel<W, R, true><<<(unsigned)ceil_div(L, R), 256, 0, st>>>(U, out, ld, N, L, t, y, coef, g, j, yn,
+                                                                            coefn, gn);
+  else
+    ev_pass_1d_kernel<W, R, false><<<(unsigned)ceil_div(L, R), 256, 0, st>>>(U, out, ld, N, L, t, y, coef, g, j, yn,
+                                                                             coefn, gn);
   return cudaGetLastError();
 }
 

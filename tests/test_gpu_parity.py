@@ -837,3 +837,20 @@ def test_small_step_size_boundary(P):
     assert n1 - n0 == 1 and n2 - n1 > 3
     a.close()
     b.close()
+
+
+def test_event_pass_alternating_taps_match_general(P, monkeypatch):
+    """The 1d event pass with the two-FMA taps (K(tau)'s taps alternate real / imaginary on the
+    bipartite ring) against the general four-FMA taps (TRAJ_EV_ALT_TAPS=0), same event stream:
+    identical event outcomes and states equal to rounding."""
+    a = P.Trajectories(200, 1, "projective_events", [2.0], seed=13)
+    b = P.Trajectories(200, 1, "projective_events", [2.0], seed=13)
+    for _ in range(20):
+        monkeypatch.setenv("TRAJ_EV_ALT_TAPS", "0")
+        a.step(1)
+        monkeypatch.setenv("TRAJ_EV_ALT_TAPS", "1")
+        b.step(1)
+        assert a.last_clicks(0) == b.last_clicks(0)
+    assert np.abs(a.get_state(0).cpu().numpy() - b.get_state(0).cpu().numpy()).max() < 1e-13
+    a.close()
+    b.close()
