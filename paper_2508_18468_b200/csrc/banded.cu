@@ -9,6 +9,8 @@
 // 8 (2w+1) L N flops and 32 L N bytes per pass: an FP64-ALU / HBM-bound stencil instead of
 // the 8 L^2 N-flop dense contraction.  The oracle keeps the dense exact K; the truncation
 // error is below double rounding.
+#include <stdlib.h>
+
 #include "banded.h"
 #include "common.cuh"
 
@@ -30,8 +32,10 @@ struct Taps {
   double2 c[2 * W + 1];
 };
 
-// one thread: column k, positions [p0, p0 + RPT) of one line
-template <int W, int RPT = Rpt<W>::value>
+// one thread: column k, positions [p0, p0 + RPT) of one line.  ALT: on an even-length axis
+// c_d = sum_{m = d mod len} (-i)^|m| J_|m| is purely real for even d and purely imaginary for
+// odd d (every wrap m has d's parity), so each tap is two FMAs instead of four.
+template <int W, bool ALT, int RPT = Rpt<W>::value>
 __global__ void __launch_bounds__(TC * RG, W <= 10 ? 2 : 1) banded_kernel(const cplx* __restrict__ U, cplx* __restrict__ V,
                                                          long long ld, long long sU, int N, int len, int lines,
                                                          long long line_stride, long long pos_stride,
@@ -63,10 +67,18 @@ __global__ void __launch_bounds__(TC * RG, W <= 10 ? 2 : 1) banded_kernel(const 
 #pragma unroll
     for (int d = 0; d < 2 * W + 1; ++d) {
       const double2 a = taps.c[d], b = in[r + d];
-      re = fma(a.x, b.x, re);
-      re = fma(-a.y, b.y, re);
-      im = fma(a.x, b.y, im);
-      im = fma(a.y, b.x, im);
+      if (!ALT) {
+        re = fma(a.x, b.x, re);
+        re = fma(-a.y, b.y, re);
+        im = fma(a.x, b.y, im);
+        im = fma(a.y, b.x, im);
+      } else if (((d - W) & 1) == 0) {   // real tap
+        re = fma(a.x, b.x, re);
+        im = fma(a.x, b.y, im);
+      } else {                           // imaginary tap
+        re = fma(-a.y, b.y, re);
+        im = fma(a.y, b.x, im);
+      }
     }
     v[(long long)(p0 + r) * step] = make_double2(re, im);
   }
@@ -77,10 +89,19 @@ cudaError_t launch(cudaStream_t st, const cplx* U, cplx* V, long long ld, long l
                    long long ls, long long ps, const cplx* coef_host, int T, int periodic) {
   constexpr int RPT = Rpt<W>::value;
   Taps<W> taps;
-  for (int i = 0; i < 2 * W + 1; ++i) taps.c[i] = coef_host[i];
+  bool alt = true;   // exactly real at even offsets, exactly imaginary at odd ones
+  for (int i = 0; i < 2 * W + 1; ++i) {
+    taps.c[i] = coef_host[i];
+    alt = alt && (((i - W) & 1) == 0 ? coef_host[i].y == 0.0 : coef_host[i].x == 0.0);
+  }
+  const char* ev = getenv("TRAJ_BANDED_ALT_TAPS");
+  if (ev && ev[0] == '0') alt = false;
   const int tiles = (len + RPT * RG - 1) / (RPT * RG);
   dim3 grid((unsigned)(tiles * lines), (unsigned)ceil_div(N, TC), (unsigned)T);
-  banded_kernel<W><<<grid, TC * RG, 0, st>>>(U, V, ld, sU, N, len, lines, ls, ps, taps, periodic);
+  if (alt)
+    banded_kernel<W, true><<<grid, TC * RG, 0, st>>>(U, V, ld, sU, N, len, lines, ls, ps, taps, periodic);
+  else
+    banded_kernel<W, false><<<grid, TC * RG, 0, st>>>(U, V, ld, sU, N, len, lines, ls, ps, taps, periodic);
   count_launch();
   return cudaGetLastError();
 }

@@ -457,10 +457,12 @@ def test_particle_covariance_2d_batch(P):
 
 
 @pytest.mark.parametrize("Lx,Ly,protocol,gam", [(240, 1, "homodyne", 1.0), (200, 1, "projective", 3.0),
-                                                (14, 10, "homodyne", 2.0), (12, 12, "projective", 2.86)])
+                                                (14, 10, "homodyne", 2.0), (12, 12, "projective", 2.86),
+                                                (15, 10, "homodyne", 2.0)])
 def test_banded_propagator_matches_dense_oracle(P, Lx, Ly, protocol, gam):
     """NEXT-1: banded circulant passes (1d) / K_y (x) K_x as two passes (2d) against the oracle's
-    dense exact K: the dropped Bessel tail is below 1e-18, so the lockstep bar is unchanged."""
+    dense exact K: the dropped Bessel tail is below 1e-18, so the lockstep bar is unchanged.  An
+    odd axis (15) has taps that are not purely real / imaginary: the four-FMA kernel there."""
     lockstep_kw = dict(seed=6)
     gpu = P.Trajectories(Lx, Ly, protocol, [gam, gam / 2], propagator="banded", **lockstep_kw)
     K = lattice.propagator_lattice(Lx, Ly, 1.0, 0.05)
@@ -851,6 +853,21 @@ def test_event_pass_alternating_taps_match_general(P, monkeypatch):
         monkeypatch.setenv("TRAJ_EV_ALT_TAPS", "1")
         b.step(1)
         assert a.last_clicks(0) == b.last_clicks(0)
+    assert np.abs(a.get_state(0).cpu().numpy() - b.get_state(0).cpu().numpy()).max() < 1e-13
+    a.close()
+    b.close()
+
+
+def test_banded_alternating_taps_match_general(P, monkeypatch):
+    """The banded stencil with two-FMA taps (even ring: taps alternate real / imaginary) against the
+    four-FMA taps (TRAJ_BANDED_ALT_TAPS=0): the same trajectory to rounding."""
+    a = P.Trajectories(256, 1, "homodyne", [1.0], propagator="banded", seed=21)
+    b = P.Trajectories(256, 1, "homodyne", [1.0], propagator="banded", seed=21)
+    for _ in range(10):
+        monkeypatch.setenv("TRAJ_BANDED_ALT_TAPS", "0")
+        a.step(1)
+        monkeypatch.delenv("TRAJ_BANDED_ALT_TAPS")
+        b.step(1)
     assert np.abs(a.get_state(0).cpu().numpy() - b.get_state(0).cpu().numpy()).max() < 1e-13
     a.close()
     b.close()
