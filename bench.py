@@ -411,11 +411,12 @@ def run_ours(args):
                 "complex_mult": ("planar 3m" if (planar and dom == "propagate") or
                                  (planar_cqr and dom in ("gram", "trmm")) else algo),
                 "pipe_tflops": achieved * pipe_per_alg, "pipe_frac": achieved * pipe_per_alg / FP64_PEAK_TFLOPS,
-                "traffic_note": ("ncu dram bytes of the propagate phase (profiles/ncu_traffic.json: split, three "
-                                 "real 16384x8192x16384 products, combine) vs 8.6 GB algorithmic: each wave of "
-                                 "148 output-stationary 128x128 tiles streams its K panels (> L2 at K = 16384), so "
-                                 "tens of GB are inherent to output-stationary tiling; 96 GB in 374 ms is "
-                                 "~0.26 TB/s, 4% of HBM, not a bound (the interleaved 128x64 kernel moved 154 GB)")
+                "traffic_note": ("ncu dram bytes of the propagate phase (profiles/ncu_traffic.json: split, the "
+                                 "three real 16384x8192x16384 products as one batch-3 launch, combine) vs 8.6 GB "
+                                 "algorithmic: each wave of 148 output-stationary 128x128 tiles streams its K "
+                                 "panels (> L2 at K = 16384), so tens of GB are inherent to output-stationary "
+                                 "tiling; 148 GB in 368 ms is ~0.40 TB/s, 6% of HBM, not a bound (three separate "
+                                 "launches moved 96 GB in 372 ms)")
                 if planar else
                 ("ncu dram bytes of one K U launch (profiles/ncu_traffic.json) vs 8.6 GB "
                                  "algorithmic: each wave of 148 output-stationary 128x64 tiles streams its K "
