@@ -68,9 +68,9 @@ def workload(args):
     if args.protocol:
         import dataclasses
         w = dataclasses.replace(w, protocol=args.protocol)
-    # trajectories per GPU: c3/c5 one (row-shardable); c1 all 16 of the config ("16,
-    # batched on 1 GPU"); c2/c4 8 of their 192/256 (memory and time of a default run)
-    tpg = args.traj_per_gpu or {"c3": 1, "c5": 1, "c1": 16}.get(args.config, 8)
+    # trajectories per GPU as SURVEY §8(d) places them: c3/c5 one (row-shardable); c1 all 16 of
+    # the config ("16, batched on 1 GPU"); c2 192 and c4 256 spread over 8 GPUs (24 and 32 each)
+    tpg = args.traj_per_gpu or {"c3": 1, "c5": 1, "c1": 16, "c2": 24, "c4": 32}.get(args.config, 8)
     return w, tpg
 
 
