@@ -871,3 +871,19 @@ def test_banded_alternating_taps_match_general(P, monkeypatch):
     assert np.abs(a.get_state(0).cpu().numpy() - b.get_state(0).cpu().numpy()).max() < 1e-13
     a.close()
     b.close()
+
+
+def test_phase_times_attribute_the_fused_step(P):
+    """traj_phase_times: the fused small-lattice step records its whole time and its one launch per
+    call under "fused"; the general path leaves "fused" at zero."""
+    a = P.Trajectories(64, 1, "projective", [0.5, 0.5], seed=1)
+    b = P.Trajectories(200, 1, "projective", [0.5], seed=1)
+    for h in (a, b):
+        h.profile(True)
+        h.step(5)
+    pa, pb = a.phase_times(), b.phase_times()
+    assert pa["fused"][0] > 0 and pa["fused"][1] == 1
+    assert all(pa[k] == (0.0, 0) for k in pa if k != "fused")
+    assert pb["fused"] == (0.0, 0) and pb["propagate"][0] > 0 and pb["gram"][1] > 0
+    a.close()
+    b.close()
