@@ -22,5 +22,10 @@ trajectory one trajectory driven step by step with sampled observables.
 
 Parity status: every function is pinned by a ``-m "not gpu"`` test in
 ``tests/test_oracle_*.py`` (closed forms, invariants, Fock-space brute force,
-published Philox known-answer vectors).  Nothing here is "parity unpinned".
+published Philox known-answer vectors).  The Eq. (A3) drift and noise
+coefficients of ``protocols.homodyne_factor`` / ``protocols.qsd_generator`` are
+pinned without re-using their formulas by ``tests/test_oracle_drift_pins.py``
+(Born-rule martingale E[n'] = n + O(dt^2) and the Lindblad dephasing rate
+-gamma, both by exact Gauss-Hermite quadrature over the noise; wrong
+coefficients are shown to fail).  Nothing here is "parity unpinned".
 """
