@@ -2,14 +2,20 @@
 """Benchmark of the trajectory step -- one JSON line on rank 0.
 
 Default workload: BASELINE.json configs[2] ("c3"): 1d ring L = 16384, N = 8192, Neel
-start, projective protocol gamma = 0.3, dt = 0.05, complex128, one trajectory per GPU
-(weak scaling: ranks run independent trajectories with global ids = rank; no data-path
-collective).  A "step" is one full pass of the hot path: U <- K U (dense), Philox
-clicks + conditional Born sampling + rank-k projective update, CholeskyQR2.
+start, projective protocol gamma = 0.3, dt = 0.05, complex128, ONE trajectory.  A "step" is
+one full pass of the hot path: U <- K U (dense), Philox clicks + conditional Born sampling +
+rank-k projective update, CholeskyQR2.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3|c5|c2|c4]
+                    [--mode auto|traj|shard]
 
-N > 1 is launched by the driver with torch.distributed.run (one process per GPU).
+N > 1 is launched by the driver with torch.distributed.run (one process per GPU).  With
+--mode auto (the default) the single-trajectory configs c3 and c5 are ROW-SHARDED over the N
+GPUs (K and U split by rows, NCCL exchange of U fused with the chunked K_g U,
+Gram allreduce; strong scaling, BASELINE c3 "single trajectory row-sharded over 1/2/4/8 GPUs"),
+with c5 row-sharded as the secondary line; the ensemble configs c1, c2, c4 run
+trajectory-parallel (independent trajectories per GPU, no data-path
+collective, weak scaling).  At N = 1 both modes are one trajectory on one GPU.
 """
 from __future__ import annotations
 
@@ -44,9 +50,10 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", default="c3")
     p.add_argument("--traj-per-gpu", type=int, default=0, help="0: the config's natural batch (1 for c3/c5)")
-    p.add_argument("--mode", choices=["traj", "shard"], default="traj",
+    p.add_argument("--mode", choices=["auto", "traj", "shard"], default="auto",
                    help="traj: independent trajectories per GPU (weak scaling); shard: one trajectory with K and U "
-                        "row-sharded over the GPUs (NCCL allgather + Gram allreduce, strong scaling)")
+                        "row-sharded over the GPUs (NCCL exchange + Gram allreduce, strong scaling); auto: shard "
+                        "for the single-trajectory configs c3/c5 when N > 1, traj otherwise")
     p.add_argument("--propagator", choices=["dense", "banded"], default="dense",
                    help="dense: the north star's dense K U (default); banded: NEXT-1 stencil passes")
     p.add_argument("--orthonormalizer", choices=["cqr2", "lowrank"], default="cqr2",
@@ -77,18 +84,32 @@ def workload(args):
 L2_BYTES = 126e6
 
 
-def describe(w, tpg):
+def resolve_mode(args, w, world: int) -> str:
+    """auto: row-shard the single-trajectory configs (c3, c5) over N > 1 GPUs, else trajectory-parallel."""
+    if args.mode != "auto":
+        return args.mode
+    return "shard" if world > 1 and w.name in ("c3", "c5") else "traj"
+
+
+def describe(w, tpg, mode: str = "traj", world: int = 1, args=None):
     proto = f"{w.protocol} gamma={','.join(f'{g:g}' for g in w.gammas)}"
     lat = f"1d ring L={w.L}" if w.Ly == 1 else f"2d torus {w.Lx}x{w.Ly} (L={w.L})"
-    return {"workload": f"{w.name}: {lat}, N={w.N}, {proto}, dt={w.dt}, Neel/checkerboard start, "
-                        f"{tpg} trajectory(ies) per GPU, complex128",
-            "L": w.L, "N": w.N, "protocol": w.protocol, "dt": w.dt, "traj_per_gpu": tpg,
-            "l2": ("inputs larger than L2 (K is %.2f GB, U %.2f GB per trajectory; L2 = 126 MB)"
-                   % (16 * w.L * w.L / 1e9, 16 * w.L * w.N / 1e9)
-                   if 16.0 * w.L * w.L + 32.0 * w.L * w.N * tpg >= L2_BYTES else
-                   "K and U fit the 126 MB L2: L2 flushed (256 MB write) before every timed call of "
-                   f"{w.sample_every} steps (the config's sampling interval), per-call CUDA-event times summed"),
-            "steps_per_call": w.sample_every}
+    place = (f"one trajectory, K and U row-sharded over {world} GPU(s)" if mode == "shard" else
+             f"{tpg} trajectory(ies) per GPU")
+    d = {"workload": f"{w.name}: {lat}, N={w.N}, {proto}, dt={w.dt}, Neel/checkerboard start, {place}, complex128",
+         "L": w.L, "N": w.N, "protocol": w.protocol, "dt": w.dt, "traj_per_gpu": tpg,
+         "l2": ("inputs larger than L2 (K is %.2f GB, U %.2f GB per trajectory; L2 = 126 MB)"
+                % (16 * w.L * w.L / 1e9, 16 * w.L * w.N / 1e9)
+                if 16.0 * w.L * w.L + 32.0 * w.L * w.N * tpg >= L2_BYTES else
+                "K and U fit the 126 MB L2: L2 flushed (256 MB write) before every timed call of "
+                f"{w.sample_every} steps (the config's sampling interval), per-call CUDA-event times summed"),
+         "steps_per_call": w.sample_every,
+         "parallelism": (f"row-sharded K,U over {world} GPU(s) (NCCL)" if mode == "shard" and world > 1 else
+                         f"trajectory-parallel dp{world}")}
+    if args is not None:
+        d["propagator"] = args.propagator
+        d["orthonormalizer"] = "cqr2" if mode == "shard" else args.orthonormalizer
+    return d
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -162,39 +183,63 @@ def cpu_baseline_record(w, budget_s: float, max_steps: int, unit: str):
 
 
 # ----------------------------------------------------------------------------- our arm
+def _dist():
+    import torch.distributed as dist
+    return dist
+
+
+def open_handle(P, args, w, mode, rank, world, tpg, stream=None):
+    """The handle a user opens for this run: row-sharded (one trajectory, NCCL communicator id
+    from rank 0 broadcast over torch.distributed) or a batch of tpg trajectories with global ids
+    rank * tpg + t and the folded gamma index of SURVEY §8(d) (workloads.gamma_of)."""
+    if mode == "shard":
+        uid = None
+        if world > 1:
+            box = [P.traj_nccl_unique_id() if rank == 0 else None]
+            _dist().broadcast_object_list(box, src=0)
+            uid = box[0]
+        return P.Trajectories(w.Lx, w.Ly, w.protocol, [w.gammas[0]], dt=w.dt, J=w.J, seed=w.seed, traj_base=0,
+                              stream=stream, shard_size=world, shard_rank=rank if world > 1 else 0, nccl_id=uid,
+                              propagator=args.propagator)
+    gam = [w.gamma_of((rank * tpg + t) % w.n_traj) for t in range(tpg)]
+    return P.Trajectories(w.Lx, w.Ly, w.protocol, gam, dt=w.dt, J=w.J, seed=w.seed, traj_base=rank * tpg,
+                          stream=stream, propagator=args.propagator, orthonormalizer=args.orthonormalizer)
+
+
+def max_over_ranks(ms: float, world: int) -> float:
+    if world == 1:
+        return ms
+    import torch
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    _dist().all_reduce(t, op=_dist().ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # BENCH_SMOKE_ONE_DEVICE=1: launch-logic smoke test of the N > 1 path on a one-GPU box (every
-    # rank on cuda:0, gloo for the barrier / max-over-ranks); its numbers are not measurements
-    if os.environ.get("BENCH_SMOKE_ONE_DEVICE") == "1":
+    # BENCH_SMOKE_ONE_DEVICE=1: launch-logic smoke test of the N > 1 trajectory-parallel path on a
+    # one-GPU box (every rank on cuda:0, gloo for the barrier / max-over-ranks); not a measurement
+    smoke1 = os.environ.get("BENCH_SMOKE_ONE_DEVICE") == "1"
+    if smoke1:
         local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        if os.environ.get("BENCH_SMOKE_ONE_DEVICE") == "1":
+        if smoke1:
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2508_18468_b200 as P
 
     w, tpg = workload(args)
-    shard = args.mode == "shard"
+    mode = resolve_mode(args, w, world)
+    shard = mode == "shard"
     if shard:
         tpg = 1
-        gam, base = [w.gammas[0]], 0
-        uid = [P.traj_nccl_unique_id() if rank == 0 else None]
-        if world > 1:
-            dist.broadcast_object_list(uid, src=0)
-        tr = P.Trajectories(w.Lx, w.Ly, w.protocol, gam, dt=w.dt, J=w.J, seed=w.seed, traj_base=0,
-                            shard_size=world, shard_rank=rank, nccl_id=uid[0], propagator=args.propagator)
-    else:
-        gam = [w.gammas[(rank * tpg + t) % len(w.gammas)] for t in range(tpg)]
-        base = rank * tpg
-        tr = P.Trajectories(w.Lx, w.Ly, w.protocol, gam, dt=w.dt, J=w.J, seed=w.seed, traj_base=base,
-                            propagator=args.propagator, orthonormalizer=args.orthonormalizer)
+    tr = open_handle(P, args, w, mode, rank, world, tpg)
     st = tr.stream
     # steps are issued the way a run of the config issues them: one traj_step call per interval
     # between sampled observables (w.sample_every steps; the fused small-lattice path runs a call
@@ -238,71 +283,143 @@ def run_ours(args):
         e1.record(st)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
+    if world > 1:
+        dist.barrier()
     launches = P.traj_kernel_launches() - l0
     clk = clocks.stop()
     phases = tr.phase_times()
-    tr_clicks = ([tr.last_clicks(t)[0] for t in range(tpg)]
-                 if w.protocol in ("projective", "projective_events") else [0])
-    if world > 1:
-        dist.barrier()
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
-    else:
-        ms_max = ms
+    tr_clicks = ([tr.last_clicks(t) for t in range(tpg)]
+                 if w.protocol in ("projective", "projective_events") else [(0, 0)])
+    ms_max = max_over_ranks(ms, world)
     value = (1 if shard else world) * tpg * args.steps / (ms_max / 1e3)
-    # ---- roofline of the dominant phase (the largest device time), per step:
-    #   propagate (dense K U): 8 (L/P) L N flops
-    #   gram (G = U^dag U, upper tiles): 4 (L/P) N^2 per measured Gram -- one per step for the
-    #     projective protocol (pass 1's Gram comes from the zeroed rows), two otherwise
-    #   trmm (U <- U R^-1): 4 (L/P) N^2 per TRMM counted in this phase -- the second pass only when
-    #     the first is overlapped with the Cholesky (its time is then in the chol phase)
     rows = w.L // world if shard else w.L
+    roof, executed, hbm, library = roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P)
+    # ---- row a4, timed separately (north star: "eigvalsh on C_A at sampled times, timed
+    # separately"): the config's sampled observables once, after the timed steps
+    obs = None
+    if not args.no_observables:
+        obs = {}
+        for name, region in w.regions.items():
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            if isinstance(region, tuple):
+                tr.mutual_info(*region)
+                kind = "I2"
+            else:
+                tr.entropy(region)
+                kind = "S_A"
+            obs[f"{kind}:{name}"] = 1e3 * (time.perf_counter() - t0)
+    tr.close()
+    del tr
+    # the workspace block stays in torch's caching allocator, so the e2e handle below takes it from
+    # there as a user's next handle would (a fresh 29 GB cudaMalloc after a free costs ~0.4 s)
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, w, tpg, mode, rank, world, P)
+
+    # ---- the metric's second lattice (2d 160x160), same step, same timing rules, same mode
+    secondary = None
+    if args.secondary and args.secondary not in ("none", '""', "''") and args.secondary != args.config:
+        torch.cuda.empty_cache()
+        secondary = run_secondary(args, world, rank, P)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    out = {
+        "metric": "trajectory steps/s (configs[2]: 1d L=16384 projective; metric also quoted at 2d 160x160)",
+        "value": value, "unit": "trajectory-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong" if shard else "weak",
+        "vs_baseline": None,
+        "dtype": "c128 (f64 arithmetic)", "data": "synthetic (Neel start, Philox randoms, seed 0)",
+        "config": describe(w, tpg, mode, world, args),
+        "roofline": roof,
+        "step_executed_dmma": executed,
+        "library_same_shape": library,
+        "hbm_kernels": hbm or None,
+        "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
+        "phase_launches_per_step": {k: v[1] / args.steps for k, v in phases.items()},
+        "gpu_launches": launches,
+        "sampled_observables_ms": obs,
+        "secondary": secondary,
+        "clocks": clk,
+        "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline_record(w, budget_s=20.0, max_steps=1, unit="trajectory-steps/s")
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P):
+    """Roofline of the dominant phase (the largest device time per step) on EXECUTED flops.
+
+    Work per step in conventional 8mnk complex flops, per GPU (rows = L/P of the
+    L rows when row-sharded):
+      propagate (dense K U): 8 rows L N
+      gram (G = U^dag U, upper tiles): 4 rows N^2 per measured Gram -- one per projective step
+        (pass 1's Gram comes from the zeroed rows), two otherwise
+      trmm (U <- U R^-1): 4 rows N^2 per TRMM counted in this phase -- the second pass only when
+        the first is overlapped with the Cholesky (its time is then in the chol phase)
+    The 3M (Gauss) schemes -- the planar real products and the interleaved zgemm3m kernels -- issue
+    6mnk flops on the DMMA pipe for every 8mnk: `achieved` / `frac` count those executed flops;
+    `achieved_8mnk_equiv` / `frac_8mnk_equiv` state the conventional-count equivalent."""
     algo = P.traj_get_zgemm_algorithm()
     kn = {"3m": ("zgemm3mw_dmma_kernel<0,0> (3M, 128x64 CTA)", "zgemm3m_dmma_kernel<1,0> (3M, 64x64 CTA)"),
           "4m": ("zgemm_dmma_kernel<0,0> (4M)", "zgemm_dmma_kernel<1,0> (4M)")}[algo]
-    planar = (args.propagator == "dense" and not shard and os.environ.get("TRAJ_PLANAR_KU", "1") != "0"
-              and w.protocol in ("projective", "homodyne"))
-    planar_cqr = not shard and os.environ.get("TRAJ_PLANAR_CQR", "1") != "0"
+    plan_on = os.environ.get("TRAJ_PLANAR_MIN_N")
+    big = w.N >= (int(plan_on) if plan_on else 512)
+    planar = (args.propagator == "dense" and big and os.environ.get("TRAJ_PLANAR_KU", "1") != "0"
+              and w.protocol in ("projective", "homodyne")
+              and (not shard or os.environ.get("TRAJ_PLANAR_CQR", "1") != "0"))
+    planar_cqr = big and os.environ.get("TRAJ_PLANAR_CQR", "1") != "0" and (not shard or planar)
     ku_name = ("dgemm_dmma_kernel x3 (planar 3M: Kr Ur, Ki Ui, (Kr+Ki)(Ur+Ui); 128x128 CTA) + split/combine passes"
+               + ("; per shard: P ring-distance K-chunk products accumulated, the U exchange under them" if shard
+                  else "")
                if planar else kn[0])
     gram_name = ("dgemm_dmma_kernel<1> x3 (planar 3M: Ur^T Ur, Ui^T Ui, (Ur-Ui)^T (Ur+Ui); upper tiles) + split/combine"
                  if planar_cqr else f"{kn[1]}: G = U^dag U upper tiles")
     trmm_name = ("dgemm_dmma_kernel<0> x3 (planar 3M against X's planes, triangle skipped) + split/combine"
                  if planar_cqr else f"{kn[0]} triangular")
     n_gram = 1 if (w.protocol == "projective" and os.environ.get("TRAJ_LOWRANK_GRAM", "1") != "0") else 2
-    n_trmm = 1 if (not shard and os.environ.get("TRAJ_CHOL_OVERLAP", "1") != "0") else 2
-    kern = {"propagate": (8.0 * rows * w.L * w.N * tpg, f"{ku_name}: U <- K U (8 L^2 N flops per step)"),
-            "gram": (n_gram * 4.0 * rows * w.N * w.N * tpg,
+    n_trmm = 1 if os.environ.get("TRAJ_CHOL_OVERLAP", "1") != "0" else 2
+    a_ku = 0.75 if (planar or algo == "3m") else 1.0       # DMMA flops per 8mnk flop
+    a_cqr = 0.75 if (planar_cqr or algo == "3m") else 1.0
+    kern = {"propagate": (8.0 * rows * w.L * w.N * tpg, a_ku, f"{ku_name}: U <- K U (8 L^2 N flops per step)"),
+            "gram": (n_gram * 4.0 * rows * w.N * w.N * tpg, a_cqr,
                      f"{gram_name}: {n_gram} measured Gram(s) per step, 4 L N^2 each"),
-            "trmm": (n_trmm * 4.0 * rows * w.N * w.N * tpg,
+            "trmm": (n_trmm * 4.0 * rows * w.N * w.N * tpg, a_cqr,
                      f"{trmm_name}: U <- U R^-1, {n_trmm} TRMM(s) in this phase per step, 4 L N^2 each")}
     if args.propagator == "banded":
         kern.pop("propagate")
-    lowrank_proj = args.orthonormalizer == "lowrank" and w.protocol == "projective" and not shard
-    if lowrank_proj:
+    k_sum = sum(c[0] for c in tr_clicks)
+    k1_sum = sum(c[1] for c in tr_clicks)
+    if args.orthonormalizer == "lowrank" and w.protocol == "projective" and not shard:
         # no N x N Gram / TRMM per step: the work is the four rank-k GEMMs of the projective phase,
         # 16 L N (k1 + k0) flops per trajectory (U W, U -= T W^dag, U' V^dag, U' += P F V); k from
         # the last timed step's clicks; the phase time also holds the sampler and Newton-Schulz
-        k_sum = sum(tr_clicks)
-        kern = {"project": (16.0 * w.L * w.N * k_sum,
+        kern = {"project": (16.0 * w.L * w.N * k_sum, 1.0 if algo == "4m" else 0.75,
                             f"projective rank-k GEMMs ({kn[1].split(' ')[0].split('<')[0]} family): 16 L N (k1 + k0) "
                             f"flops per step, k1 + k0 = {k_sum} clicks in the last timed step; phase time includes "
                             "the blocked sampler and the Newton-Schulz iteration")}
-    if phases.get("fused", (0.0,))[0] > 0:
-        # the fused small-lattice step (small_step.cu): the whole step in one CTA per trajectory;
-        # algorithmic flops per trajectory-step 8 L^2 N (K U) + 2 x (4 L N^2 Gram + 4 L N^2 solve)
-        kern = {"fused": ((8.0 * w.L * w.L * w.N + 16.0 * w.L * w.N * w.N) * tpg,
+    fused = phases.get("fused", (0.0,))[0] > 0
+    if fused:
+        # the fused small-lattice step (small_step.cu): the whole step in one CTA per trajectory,
+        # 4M complex tiles as four real m8n8k4 DMMAs; algorithmic flops per trajectory-step
+        # 8 L^2 N (K U) + 2 x (4 L N^2 Gram + 4 L N^2 solve)
+        kern = {"fused": ((8.0 * w.L * w.L * w.N + 16.0 * w.L * w.N * w.N) * tpg, 1.0,
                           "small_step_kernel: the whole step (K U, monitor, CholeskyQR2) with U in shared "
-                          "memory, one CTA per trajectory; 8 L^2 N + 16 L N^2 flops per trajectory-step")}
-    events_hbm = w.protocol == "projective_events" and args.orthonormalizer == "lowrank"
-    pipe_per_alg = 0.75 if (algo == "3m" or planar or planar_cqr) else 1.0   # DMMA flops per 8mnk flop
+                          "memory, one CTA per trajectory, 4M complex tiles on DMMA m8n8k4; "
+                          "8 L^2 N + 16 L N^2 flops per trajectory-step")}
     dom = max(kern, key=lambda k: phases[k][0])
-    launches_per_step = 1.0
     kern_ms = phases[dom][0] / args.steps
-    flops_launch = kern[dom][0]
-    achieved = flops_launch / (kern_ms / 1e3) / 1e12
-    prop_ms = phases["propagate"][0] / args.steps
+    flops8, alpha, kname = kern[dom]
+    eq8 = flops8 / (kern_ms / 1e3) / 1e12
+    achieved = eq8 * alpha
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp) and dom == "propagate" and not shard:
@@ -311,6 +428,42 @@ def run_ours(args):
             traffic = tj.get("propagate_dram_bytes") if planar else tj.get("interleaved_zgemm3mw_dram_bytes")
         except Exception:
             traffic = None
+    mult = ("planar 3m" if (planar and dom == "propagate") or (planar_cqr and dom in ("gram", "trmm")) else
+            "4m" if dom == "fused" else algo)
+    roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+            "achieved_8mnk_equiv": eq8, "frac_8mnk_equiv": eq8 / FP64_PEAK_TFLOPS,
+            "kernel": kname + ("; per shard (L/P rows) when row-sharded" if shard else ""),
+            "kernel_ms": kern_ms, "timed": "device time of that phase per step (CUDA events around it on "
+                                          "the handle's stream)", "peak_source": FP64_PEAK_SOURCE,
+            "complex_mult": mult,
+            "flops_counted": ("executed DMMA flops: 6mnk per complex product for 3M (three real products), "
+                              "8mnk for 4M; achieved_8mnk_equiv counts the conventional 8mnk"),
+            "traffic_note": ("ncu dram bytes of the propagate phase (profiles/ncu_traffic.json: split, the "
+                             "three real 16384x8192x16384 products as one batch-3 launch, combine) vs 8.6 GB "
+                             "algorithmic") if traffic else None}
+    if w.name == "c1":
+        roof["note"] = ("c1 is latency-bound (SURVEY §8(d)): L = 64, one fused launch per step with one CTA per "
+                        "trajectory, whose ~140 barriers and dependent pivots set the time; the fraction is not a "
+                        "kernel-quality figure")
+    # executed DMMA flops of the whole step (model of what the kernels issue), over the step time
+    k1 = k1_sum / max(1, tpg)
+    step8 = {"propagate": (8.0 * rows * w.L * w.N if args.propagator == "dense" else 0.0, a_ku),
+             "gram": (n_gram * 4.0 * rows * w.N * w.N, a_cqr),
+             "trmm": (2 * 4.0 * rows * w.N * w.N, a_cqr),
+             "chol": ((8.0 / 3.0) * w.N ** 3, 0.75 if algo == "3m" else 1.0),
+             "project": (16.0 * rows * w.N * k1 if w.protocol == "projective" else 0.0, 0.75 if algo == "3m" else 1.0)}
+    executed = None
+    if not fused and not (args.orthonormalizer == "lowrank" and w.protocol == "projective" and not shard) \
+            and w.protocol in ("projective", "homodyne"):
+        fl = sum(f * a for f, a in step8.values()) * tpg
+        t = ms / args.steps / 1e3
+        executed = {"tflops": fl / t / 1e12, "frac": fl / t / 1e12 / FP64_PEAK_TFLOPS, "flops_per_step": fl,
+                    "model": "per step (and per shard): K U 8 rows L N, one chol_inverse (8/3) N^3 (the second "
+                             "CholeskyQR pass takes the first-order factor), the measured Gram(s) 4 rows N^2, two "
+                             "TRMMs 4 rows N^2, the projective rank-k1 update 16 rows N k1; each x 0.75 for the 3M "
+                             "schemes (the DMMA flops they issue)",
+                    "per_phase_8mnk": {k: v[0] * tpg for k, v in step8.items()}}
     # same-shape library denominators (tools/library_compare.py, committed under profiles/):
     # cublasZgemm / cublasZgemm3m for K U, cuSOLVER potrf + trtri for the Cholesky inverse
     library = None
@@ -347,7 +500,7 @@ def run_ours(args):
                                                                    "ms_per_step": phases["propagate"][0] / args.steps}
     if w.protocol == "projective_events" and phases["project"][0] > 0:
         # one pass per event reads U once and writes it once (32 L N bytes); events of the last window
-        b = 32.0 * w.L * w.N * sum(tr_clicks) * args.steps
+        b = 32.0 * w.L * w.N * k_sum * args.steps
         g = b / (phases["project"][0] / 1e3) / 1e9
         hbm["ev_pass_1d_kernel (one pass per event, 32 L N B; events in the last window)"] = {
             "achieved_gbs": g, "peak_gbs": HBM_PEAK_GBS, "frac": g / HBM_PEAK_GBS,
@@ -358,127 +511,31 @@ def run_ours(args):
         hbm["horner_pass_kernel (RK4 as 4 Horner passes, 48 L N B each)"] = {
             "achieved_gbs": g, "peak_gbs": HBM_PEAK_GBS, "frac": g / HBM_PEAK_GBS,
             "ms_per_step": phases["propagate"][0] / args.steps}
-    step_flops = {"propagate": 8.0 * rows * w.L * w.N * tpg if args.propagator == "dense" else 0.0,
-                  "gram": 2 * 4.0 * rows * w.N * w.N * tpg, "trmm": 2 * 4.0 * rows * w.N * w.N * tpg,
-                  "chol": (8.0 / 3.0) * w.N ** 3 * tpg}
-    dense_tflops = sum(step_flops.values()) * args.steps / (ms / 1e3) / 1e12
-    # ---- row a4, timed separately (north star: "eigvalsh on C_A at sampled times, timed
-    # separately"): the config's sampled observables once, after the timed steps
-    obs = None
-    if not args.no_observables and not shard:
-        obs = {}
-        for name, region in w.regions.items():
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            if isinstance(region, tuple):
-                tr.mutual_info(*region)
-                kind = "I2"
-            else:
-                tr.entropy(region)
-                kind = "S_A"
-            obs[f"{kind}:{name}"] = 1e3 * (time.perf_counter() - t0)
-    tr.close()
-    del tr
-    # the workspace block stays in torch's caching allocator, so the e2e handle below takes it from
-    # there as a user's next handle would (a fresh 29 GB cudaMalloc after a free costs ~0.4 s)
-
-    # ---- the metric's second lattice (2d 160x160), same step, same timing rules
-    secondary = None
-    if args.secondary and args.secondary not in ("none", '""', "''") and args.secondary != args.config \
-            and not shard:
-        secondary = run_secondary(args, world, rank, P)
-
-    # ---- end to end through the public API with host buffers
-    e2e = None
-    if not args.no_e2e and not shard:
-        e2e = run_e2e(args, w, tpg, gam, base, world, P)
-
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
     ev_key = next((k for k in hbm if k.startswith("ev_pass")), None)
-    if events_hbm and ev_key:
+    if w.protocol == "projective_events" and args.orthonormalizer == "lowrank" and ev_key:
         # the event-driven step with the probe certificate is one HBM read + write of U per event
         roof = {"bound": "hbm", "achieved": hbm[ev_key]["achieved_gbs"], "peak": HBM_PEAK_GBS, "unit": "GB/s",
                 "frac": hbm[ev_key]["frac"], "traffic": None, "kernel": ev_key,
                 "kernel_ms": hbm[ev_key]["ms_per_step"], "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
-    else:
-        roof = {"bound": "latency" if w.name == "c1" else "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-                "kernel": kern[dom][1] + ("; per shard (L/P rows) when row-sharded" if shard else ""),
-                "kernel_ms": kern_ms, "timed": "device time of that phase per step (CUDA events around it on "
-                                              "the handle's stream)", "peak_source": FP64_PEAK_SOURCE,
-                "complex_mult": ("planar 3m" if (planar and dom == "propagate") or
-                                 (planar_cqr and dom in ("gram", "trmm")) else algo),
-                "pipe_tflops": achieved * pipe_per_alg, "pipe_frac": achieved * pipe_per_alg / FP64_PEAK_TFLOPS,
-                "traffic_note": ("ncu dram bytes of the propagate phase (profiles/ncu_traffic.json: split, the "
-                                 "three real 16384x8192x16384 products as one batch-3 launch, combine) vs 8.6 GB "
-                                 "algorithmic: each wave of 148 output-stationary 128x128 tiles streams its K "
-                                 "panels (> L2 at K = 16384), so tens of GB are inherent to output-stationary "
-                                 "tiling; 148 GB in 368 ms is ~0.40 TB/s, 6% of HBM, not a bound (three separate "
-                                 "launches moved 96 GB in 372 ms)")
-                if planar else
-                ("ncu dram bytes of one K U launch (profiles/ncu_traffic.json) vs 8.6 GB "
-                                 "algorithmic: each wave of 148 output-stationary 128x64 tiles streams its K "
-                                 "panels (~580 MB per wave at K = 16384, > L2), so >= ~64 GB is inherent to "
-                                 "this tiling; 154 GB in 390 ms is ~0.4 TB/s, 6% of HBM, not a bound")
-                if traffic else None,
-                "note": ("c1 is latency-bound (SURVEY §8(d)): L = 64, one fused launch per step with one CTA "
-                         "per trajectory, whose ~140 barriers and dependent pivots set the time; the fraction "
-                         "is not a kernel-quality figure. "
-                         if w.name == "c1" else "") +
-                        ("achieved counts the conventional 8mnk complex flops; the 3M (Gauss) kernels issue "
-                         "6mnk flops on the DMMA pipe, reported as pipe_tflops / pipe_frac")
-                if algo == "3m" else "4M: 8mnk flops on the DMMA pipe"}
-    if dom == "fused":
-        roof.update({"complex_mult": "4m on DFMA (FP64 CUDA cores; the tensor pipe needs 8x8x4 tiles the barrier-"
-                                     "bound step cannot feed)", "pipe_tflops": None, "pipe_frac": None,
-                     "note": roof["note"].split(". ")[0] + "." if w.name == "c1" else None})
-    out = {
-        "metric": "trajectory steps/s (configs[2]: 1d L=16384 projective; metric also quoted at 2d 160x160)",
-        "value": value, "unit": "trajectory-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong" if shard else "weak",
-        "vs_baseline": None,
-        "dtype": "c128 (f64 arithmetic)", "data": "synthetic (Neel start, Philox randoms, seed 0)",
-        "config": dict(describe(w, tpg), parallelism=(f"row-sharded K,U over {world} GPU(s) (NCCL)" if shard
-                                                      else f"trajectory-parallel dp{world}"),
-                       propagator=args.propagator, orthonormalizer=args.orthonormalizer),
-        "roofline": roof,
-        "library_same_shape": library,
-        "hbm_kernels": hbm or None,
-        "step_dense_tflops": dense_tflops,
-        "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
-        "phase_launches_per_step": {k: v[1] / args.steps for k, v in phases.items()},
-        "gpu_launches": launches,
-        "sampled_observables_ms": obs,
-        "secondary": secondary,
-        "clocks": clk,
-        "e2e": e2e,
-    }
-    if world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline_record(w, budget_s=20.0, max_steps=1, unit="trajectory-steps/s")
-    print(json.dumps(out), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    return roof, executed, hbm, library
 
 
 def run_secondary(args, world, rank, P, steps=2, warmup=2):
     """Time the secondary config (default c5: 2d 160x160 projective) with the same step, the
-    same propagator/orthonormaliser and CUDA events; max over ranks."""
+    same propagator/orthonormaliser, the same mode (row-sharded over the N GPUs when the primary
+    is) and CUDA events; max over ranks."""
     import torch
-    import torch.distributed as dist
     import dataclasses
     w = workloads.CONFIGS[args.secondary]()
     if args.protocol:
         w = dataclasses.replace(w, protocol=args.protocol)
-    tr = P.Trajectories(w.Lx, w.Ly, w.protocol, [w.gammas[0]], dt=w.dt, J=w.J, seed=w.seed, traj_base=rank,
-                        propagator=args.propagator, orthonormalizer=args.orthonormalizer)
+    mode = resolve_mode(args, w, world)
+    tr = open_handle(P, args, w, mode, rank, world, 1)
     for _ in range(warmup):
         tr.step(1)
     torch.cuda.synchronize()
     if world > 1:
-        dist.barrier()
+        _dist().barrier()
     tr.profile(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(tr.stream)
@@ -491,44 +548,50 @@ def run_secondary(args, world, rank, P, steps=2, warmup=2):
     tr.close()
     del tr
     torch.cuda.empty_cache()
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, world)
+    shard = mode == "shard"
+    rows = w.L // world if shard else w.L
     prop = ph["propagate"][0] / steps
-    out = {"config": describe(w, 1), "value": world * steps / (ms / 1e3), "unit": "trajectory-steps/s",
+    out = {"config": describe(w, 1, mode, world, args), "value": (1 if shard else world) * steps / (ms / 1e3),
+           "unit": "trajectory-steps/s", "scaling": "strong" if shard else "weak",
            "ms_per_step": ms / steps, "steps": steps, "warmup": warmup,
            "phases_ms_per_step": {k: v[0] / steps for k, v in ph.items()}}
-    if args.propagator == "dense":
-        ach = 8.0 * w.L * w.L * w.N / (prop / 1e3) / 1e12
-        out["roofline_propagate"] = {"bound": "tensor", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                                     "frac": ach / FP64_PEAK_TFLOPS}
+    if args.propagator == "dense" and prop > 0:
+        eq8 = 8.0 * rows * w.L * w.N / (prop / 1e3) / 1e12
+        a = 0.75 if P.traj_get_zgemm_algorithm() == "3m" or os.environ.get("TRAJ_PLANAR_KU", "1") != "0" else 1.0
+        out["roofline_propagate"] = {"bound": "tensor", "achieved": eq8 * a, "peak": FP64_PEAK_TFLOPS,
+                                     "unit": "TFLOP/s", "frac": eq8 * a / FP64_PEAK_TFLOPS,
+                                     "achieved_8mnk_equiv": eq8, "frac_8mnk_equiv": eq8 / FP64_PEAK_TFLOPS,
+                                     "flops_counted": "executed DMMA flops (6mnk for 3M)"}
     return out
 
 
-def run_e2e(args, w, tpg, gam, base, world, P):
+def run_e2e(args, w, tpg, mode, rank, world, P):
     """Same metric through the public API from host buffers: the handle is created inside the
-    timed region (K built on the device), the initial orbital matrix comes from pinned host
-    memory (traj_set_state), every step ends with a device->host read of the occupations n_i,
-    and the config's sampled observables run at its cadence (every w.sample_every steps, as a
-    user's run would; SURVEY §8(d) times them separately, `sampled_observables_ms`)."""
+    timed region (K built on the device; row-sharded: the NCCL communicator too), the initial
+    orbital matrix comes from pinned host memory (traj_set_state; row-sharded: this rank's rows),
+    every step ends with a device->host read of the occupations n_i this GPU holds, and the
+    config's sampled observables run at its cadence (every w.sample_every steps, as a user's run
+    would; SURVEY §8(d) times them separately, `sampled_observables_ms`)."""
     import torch
-    import torch.distributed as dist
-    U0 = torch.zeros((w.L, w.N), dtype=torch.complex128).pin_memory()
+    shard = mode == "shard"
+    rows = w.L // world if shard else w.L
+    r0 = rank * rows if shard else 0
     occ = np.arange(0, w.L, 2) if w.Ly == 1 else None
     if occ is None:
         ys, xs = np.divmod(np.arange(w.L), w.Lx)
         occ = np.nonzero((xs + ys) % 2 == 0)[0]
-    U0[torch.from_numpy(occ), torch.arange(w.N)] = 1.0
-    n_host = torch.empty((tpg, w.L), dtype=torch.float64).pin_memory()
+    U0 = torch.zeros((rows, w.N), dtype=torch.complex128).pin_memory()
+    sel = (occ >= r0) & (occ < r0 + rows)
+    U0[torch.from_numpy(occ[sel] - r0), torch.from_numpy(np.nonzero(sel)[0])] = 1.0
+    n_host = torch.empty((tpg, rows), dtype=torch.float64).pin_memory()
     torch.cuda.synchronize()
     if world > 1:
-        dist.barrier()
+        _dist().barrier()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    tr = P.Trajectories(w.Lx, w.Ly, w.protocol, gam, dt=w.dt, J=w.J, seed=w.seed, traj_base=base, stream=stream,
-                        propagator=args.propagator, orthonormalizer=args.orthonormalizer)
+    tr = open_handle(P, args, w, mode, rank, world, tpg, stream=stream)
     for t in range(tpg):
         tr.set_state(t, U0)                       # H2D from pinned host memory
     h2d = tpg * U0.numel() * 16
@@ -536,7 +599,7 @@ def run_e2e(args, w, tpg, gam, base, world, P):
     samples = 0
     for s in range(1, args.steps + 1):
         tr.step(1)
-        n_host.copy_(tr.occupations(), non_blocking=True)   # D2H of the step's result
+        n_host.copy_(tr.occupations().reshape(tpg, rows), non_blocking=True)   # D2H of the step's result
         d2h += n_host.numel() * 8
         if s % w.sample_every == 0:
             for region in w.regions.values():
@@ -547,16 +610,15 @@ def run_e2e(args, w, tpg, gam, base, world, P):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     tr.close()
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    return {"value": world * tpg * args.steps / (ms / 1e3), "unit": "trajectory-steps/s",
+    ms = max_over_ranks(ms, world)
+    return {"value": (1 if shard else world) * tpg * args.steps / (ms / 1e3), "unit": "trajectory-steps/s",
             "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
-            "includes": f"handle init (workspace from torch's caching allocator, K built on the device), U0 upload "
-                        f"from pinned host, {args.steps} steps with "
-                        f"a D2H of n_i after each, the config's observables every {w.sample_every} steps "
-                        f"({samples} sample(s) in this window; their cost alone is sampled_observables_ms)"}
+            "includes": f"handle init (workspace from torch's caching allocator, K built on the device"
+                        f"{', NCCL communicator' if shard and world > 1 else ''}), U0 upload "
+                        f"from pinned host{' (this rank' + chr(39) + 's rows)' if shard and world > 1 else ''}, "
+                        f"{args.steps} steps with a D2H of n_i after each, the config's observables every "
+                        f"{w.sample_every} steps ({samples} sample(s) in this window; their cost alone is "
+                        f"sampled_observables_ms)"}
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -566,16 +628,21 @@ def run_reference(args):
     if rank != 0:
         return
     w, tpg = workload(args)
+    mode = resolve_mode(args, w, world)
+    if mode == "shard":
+        tpg = 1
     times, blas = oracle_steps(w, budget_s=args.cpu_budget, max_steps=max(1, args.steps))
     v = len(times) / sum(times)
     unit = "trajectory-steps/s"
     rec = {"metric": "trajectory steps/s (configs[2]: 1d L=16384 projective; metric also quoted at 2d 160x160)",
            "value": v, "unit": unit, "impl": "reference", "n_gpus": world, "steps": len(times), "warmup": 0,
-           "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "weak",
+           "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+           "scaling": "strong" if mode == "shard" else "weak",
            "vs_baseline": None, "dtype": "c128 (f64 arithmetic)", "data": "synthetic (Neel start, Philox randoms, seed 0)",
-           "config": dict(describe(w, tpg), oracle_note=(
-               f"the oracle steps one trajectory at a time; the {tpg} trajectories of the config are "
-               "independent and cost the same, so the rate of one is the config's per-trajectory rate")),
+           "config": describe(w, tpg, mode, world, args),
+           "note": (f"the oracle (NumPy/SciPy on the host cores) steps one trajectory at a time on rank 0; the "
+                    f"{tpg} trajectory(ies) per GPU of the config are independent and cost the same, so the rate "
+                    "of one is the config's per-trajectory rate"),
            "cpu_baseline": {"value": v, "unit": unit, "cores": cpu_cores(), "kind": "oracle",
                             "sample": f"{len(times)} oracle step(s) of one {w.name} trajectory (budget "
                                       f"{args.cpu_budget:.0f} s; no warm-up: NumPy has no JIT), {'; '.join(blas)}"},

@@ -64,9 +64,10 @@ typedef enum {
  * trajectory tau draws Philox counters (e_lo, e_hi, tau, 1) and (e_lo, e_hi, tau, 2).
  * traj_last_clicks reports the events of the last window and how many were "occupied". */
 enum { TRAJ_PROJECTIVE = 0, TRAJ_HOMODYNE = 1, TRAJ_HOMODYNE_RK4 = 2, TRAJ_PROJECTIVE_EVENTS = 3 };
-/* Initial state (Q1, Q2): sites with (x + y) even occupied -- the Neel state
- * |1010...> of P:173/P:198 (0-based even sites) in 1d, the checkerboard in 2d. */
-enum { TRAJ_INIT_NEEL = 0 };
+/* Initial state (Q1, Q2): sites with (x + y) even occupied.  TRAJ_INIT_NEEL: the Neel state
+ * |1010...> of P:173/P:198 (0-based even sites) in 1d -- and, for compatibility, the same (x + y)
+ * even rule in 2d; TRAJ_INIT_CHECKERBOARD: the 2d checkerboard (dim = 2 only, TRAJ_ECONFIG in 1d). */
+enum { TRAJ_INIT_NEEL = 0, TRAJ_INIT_CHECKERBOARD = 1 };
 
 typedef struct {
   int32_t dim;              /* 1 or 2 (P:42 ring; P:123 square torus)                         */
@@ -76,7 +77,7 @@ typedef struct {
   double J, dt;             /* hopping J (J = 1) and time step dt > 0 (0.05)     */
   int32_t protocol;         /* TRAJ_PROJECTIVE, TRAJ_HOMODYNE or TRAJ_HOMODYNE_RK4
                                                                                   */
-  int32_t init;             /* TRAJ_INIT_NEEL                                                  */
+  int32_t init;             /* TRAJ_INIT_NEEL (1d or 2d) or TRAJ_INIT_CHECKERBOARD (2d)          */
   uint64_t seed;            /* Philox4x32-10 key (lo, hi words), Q9                            */
   int64_t n_traj;           /* trajectories held by this handle, >= 1                          */
   int64_t traj_base;        /* global id of the first one (Philox counter word 2)              */
@@ -178,7 +179,10 @@ int traj_correlation_rows(traj_handle h, int64_t traj, int64_t row0, int64_t nro
 int traj_get_state(traj_handle h, int64_t traj, void* U_out);
 int traj_set_state(traj_handle h, int64_t traj, const void* U_in);
 
-/* Step counter (the Philox step word of the next step); set for checkpoint/resume. */
+/* Step counter (the Philox step word of the next step); set for checkpoint/resume.  For
+ * TRAJ_PROJECTIVE_EVENTS traj_set_step also rebuilds the event clock at time step * dt (events
+ * before it counted, the next event's time) from the Philox waiting times, so (state, step) is a
+ * complete checkpoint for every protocol. */
 int traj_get_step(traj_handle h, int64_t* step);
 int traj_set_step(traj_handle h, int64_t step);
 
@@ -230,6 +234,22 @@ int traj_phase_times(traj_handle h, double* ms, int64_t* launches);
 /* Row sharding: *shard_size = P, *local_shards = shards held by this handle (1, or P in
  * the single-GPU emulation), rows [*row0, *row0 + *rows) of U / n are held here. */
 int traj_shard_info(traj_handle h, int32_t* shard_size, int32_t* local_shards, int64_t* row0, int64_t* rows);
+
+/* The communication schedule of the row-sharded step for rank `rank` of P, as plain
+ * host data (no GPU, no NCCL): the NCCL executor issues exactly these operations, in this order.
+ *   kind 0: the U exchange fused into the chunked K_g U (dense propagator): for ring distance
+ *           d = 1..P-1 one group {send own block to rank+d, receive block rank-d};
+ *   kind 1: the halo exchange of the banded propagator: one group of two sends and two receives;
+ *           entries are 5 int64: (group, op 0 = send / 1 = recv, peer, slot, block) -- slot is the local
+ *           buffer (kind 0: 0 = own block / the received block's row range of U_full; kind 1: 0 = low
+ *           edge / low halo, 1 = high edge / high halo), block the global identity of the data (kind 0:
+ *           the row block's owner; kind 1: 2r = low edge of rank r, 2r + 1 = its high edge);
+ *   kind 2: the broadcasts of the distributed Cholesky of an n x n Gram (levels >= TRAJ_DIST_CHOL_MIN,
+ *           default 2048), in issue order: 3 int64 (root, rows, cols) per broadcast.
+ * NCCL pairs the operations between two ranks in issue order; tests/test_comm_plan.py checks that every
+ * receive meets the send of the block it names, for P = 2..8, and runs the schedules over gloo.
+ * Writes min(count, max_entries) entries to out (host) and returns the entry count, or -TRAJ_EINVAL. */
+int64_t traj_comm_plan(int kind, int P, int rank, int64_t n, int64_t* out, int64_t max_entries);
 
 /* out128 <- a fresh ncclUniqueId (128 bytes) for traj_config.nccl_id. */
 int traj_nccl_unique_id(void* out128);

@@ -15,6 +15,7 @@ from .binding import (  # noqa: F401
     traj_kernel_launches,
     traj_get_zgemm_algorithm,
     traj_nccl_unique_id,
+    traj_comm_plan,
     traj_set_zgemm_algorithm,
     traj_zgemm,
     traj_dgemm,

@@ -18,6 +18,7 @@ TRAJ_HOMODYNE = 1
 TRAJ_HOMODYNE_RK4 = 2
 TRAJ_PROJECTIVE_EVENTS = 3
 TRAJ_INIT_NEEL = 0
+TRAJ_INIT_CHECKERBOARD = 1
 TRAJ_PROP_DENSE, TRAJ_PROP_BANDED = 0, 1
 TRAJ_TRI_A_UPPER, TRAJ_TRI_A_LOWER, TRAJ_TRI_B_UPPER, TRAJ_TRI_B_LOWER, TRAJ_C_UPPER = 1, 2, 4, 8, 16
 PHASES = ("propagate", "monitor", "project", "gram", "chol", "trmm", "fused")
@@ -95,6 +96,7 @@ _SIGS = {
     "traj_shard_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                        ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "traj_nccl_unique_id": (ctypes.c_int, [_P]),
+    "traj_comm_plan": (ctypes.c_int64, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _I64, ctypes.POINTER(_I64), _I64]),
     "traj_set_zgemm_algorithm": (ctypes.c_int, [ctypes.c_int]),
     "traj_get_zgemm_algorithm": (ctypes.c_int, []),
     "traj_chol_scratch_bytes": (ctypes.c_size_t, [_I64, _I64]),
@@ -138,7 +140,8 @@ def _ptr(t) -> int:
 
 
 def traj_set_zgemm_algorithm(algo: str | int):
-    """"4m" (0, default) or "3m" (1) complex multiplication in every contraction (process-wide)."""
+    """"3m" (1, the default: Gauss, three real DMMA products) or "4m" (0) complex multiplication in
+    every contraction (process-wide; the environment TRAJ_ZGEMM_3M=0 sets 4m at load)."""
     a = {"4m": 0, "3m": 1}.get(algo, algo) if isinstance(algo, str) else int(algo)
     _check(lib().traj_set_zgemm_algorithm(a))
 
@@ -152,6 +155,19 @@ def traj_nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(lib().traj_nccl_unique_id(buf))
     return buf.raw
+
+
+def traj_comm_plan(kind: int, P: int, rank: int, n: int = 0) -> np.ndarray:
+    """The row-sharded step's communication schedule for one rank (host data, no GPU): kind 0 the
+    ring exchange of the propagate, 1 the halo exchange, 2 the distributed Cholesky's broadcasts.
+    Rows (group, op, peer, slot, block) for kinds 0/1, (root, rows, cols) for kind 2."""
+    w = 3 if kind == 2 else 5
+    cnt = lib().traj_comm_plan(kind, P, rank, n, None, 0)
+    if cnt < 0:
+        _check(-cnt)
+    out = np.zeros(max(cnt, 1) * w, dtype=np.int64)
+    lib().traj_comm_plan(kind, P, rank, n, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), cnt)
+    return out[:cnt * w].reshape(cnt, w)
 
 
 def traj_zgemm(opA, opB, A, B, C, *, alpha=1.0, beta=0.0, flags=0, M=None, N=None, K=None, stream=None):
@@ -241,7 +257,7 @@ class Trajectories:
         cfg.J, cfg.dt = float(J), float(dt)
         cfg.protocol = {"projective": TRAJ_PROJECTIVE, "homodyne": TRAJ_HOMODYNE,
                         "homodyne_rk4": TRAJ_HOMODYNE_RK4, "projective_events": TRAJ_PROJECTIVE_EVENTS}[protocol]
-        cfg.init = TRAJ_INIT_NEEL
+        cfg.init = TRAJ_INIT_NEEL if self.Ly == 1 else TRAJ_INIT_CHECKERBOARD
         cfg.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
         cfg.n_traj = self.n_traj
         cfg.traj_base = int(traj_base)

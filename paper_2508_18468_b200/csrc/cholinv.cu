@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "zgemm.h"
 #include "cholinv.h"
+#include "comm_plan.h"
 
 namespace traj {
 
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(EW * 32) chol_leaf_elim_kernel(int n, const cp
 
 constexpr int ELEAF_SMEM = 2 * NB * ELD * 16;
 
-int split(long long n) { return (int)(NB * ceil_div(ceil_div(n, NB), 2)); }
+int split(long long n) { return (int)chol_split(n); }
 
 struct Ctx {
   cudaStream_t st;
@@ -264,17 +265,8 @@ struct Ctx {
   bool elim_leaf;
 };
 
-// row slice boundaries of M rows over P ranks, 128-aligned; tri: equal area of an upper triangle
-std::vector<long long> slices(long long M, int P, bool tri) {
-  std::vector<long long> b(P + 1, 0);
-  for (int i = 1; i < P; ++i) {
-    const double f = (double)i / P;
-    const double x = tri ? M * (1.0 - sqrt(1.0 - f)) : M * f;
-    b[i] = std::min(M, std::max(b[i - 1], (long long)(x / 128.0 + 0.5) * 128));
-  }
-  b[P] = M;
-  return b;
-}
+// row slice boundaries of M rows over P ranks (comm_plan.h row_slices: the schedule the ranks share)
+std::vector<long long> slices(long long M, int P, bool tri) { return row_slices(M, P, tri); }
 
 // C rows [0, M) of op(A) op(B) split over the ranks (see CholDist); A's rows (opA = 0) or columns
 // (opA = 1) follow the slice

@@ -24,6 +24,7 @@
 #include "banded.h"
 #include "dgemm.h"
 #include "planar.h"
+#include "comm_plan.h"
 
 namespace traj {
 
@@ -63,9 +64,27 @@ int capacity(long long n, double p) {
 
 }  // namespace
 
+int ShardComm::begin(std::string* err) {
+  const int s = wd.check(err);
+  if (s) return s;
+  wd.lock();
+  if (wd.aborted()) {   // aborted while waiting for the lock
+    wd.unlock();
+    return wd.check(err);
+  }
+  return 0;
+}
+
+void ShardComm::end(cudaStream_t st) {
+  wd.unlock();
+  wd.mark(st, nullptr);   // the watchdog times every enqueued collective
+}
+
 int ShardComm::allgather(cudaStream_t st, void* const* send, void* recv, size_t bytes, std::string* err) {
   if (comm) {
+    STRY(begin(err));
     ncclResult_t r = ncclAllGather(send[0], recv, bytes, ncclUint8, comm, st);
+    end(st);
     if (r != ncclSuccess) {
       if (err) *err = std::string("ncclAllGather: ") + ncclGetErrorString(r);
       return TRAJ_ENCCL;
@@ -86,7 +105,9 @@ int ShardComm::allgather(cudaStream_t st, void* const* send, void* recv, size_t 
 
 int ShardComm::allreduce(cudaStream_t st, double* const* part, double* out, size_t n, std::string* err) {
   if (comm) {
+    STRY(begin(err));
     ncclResult_t r = ncclAllReduce(part[0], out, n, ncclFloat64, ncclSum, comm, st);
+    end(st);
     if (r != ncclSuccess) {
       if (err) *err = std::string("ncclAllReduce: ") + ncclGetErrorString(r);
       return TRAJ_ENCCL;
@@ -107,16 +128,18 @@ int ShardComm::allreduce(cudaStream_t st, double* const* part, double* out, size
 int ShardComm::halo(cudaStream_t st, void* const* send_lo, void* const* send_hi, void* const* recv_lo,
                     void* const* recv_hi, size_t bytes, std::string* err) {
   if (comm) {
-    const int me = rank0, left = (me + P - 1) % P, right = (me + 1) % P;
-    // NCCL pairs operations to the same peer in FIFO order; with P <= 2 left == right, so the
-    // sends go (high block -> right, low block -> left) to meet the receives (low halo from the
-    // left, high halo from the right) in the same order on the partner.
+    // the schedule of comm_plan.h halo_plan: NCCL pairs operations between two ranks in issue
+    // order, and with P <= 2 left == right -- the plan's order makes both sides agree
+    void* const* sendv[2] = {send_lo, send_hi};
+    void* const* recvv[2] = {recv_lo, recv_hi};
+    STRY(begin(err));
     ncclGroupStart();
-    ncclSend(send_hi[0], bytes, ncclUint8, right, comm, st);
-    ncclSend(send_lo[0], bytes, ncclUint8, left, comm, st);
-    ncclRecv(recv_lo[0], bytes, ncclUint8, left, comm, st);
-    ncclRecv(recv_hi[0], bytes, ncclUint8, right, comm, st);
+    for (const CommOp& op : halo_plan(P, rank0)) {
+      if (op.kind == COMM_SEND) ncclSend(sendv[op.slot][0], bytes, ncclUint8, op.peer, comm, st);
+      else ncclRecv(recvv[op.slot][0], bytes, ncclUint8, op.peer, comm, st);
+    }
     ncclResult_t r = ncclGroupEnd();
+    end(st);
     if (r != ncclSuccess) {
       if (err) *err = std::string("nccl halo exchange: ") + ncclGetErrorString(r);
       return TRAJ_ENCCL;
@@ -326,6 +349,7 @@ int dist_share_rows(void* user, cplx* base, long long ld, long long ncols, const
   if (bounds[me + 1] > bounds[me])
     SCK(cudaMemcpy2DAsync(scr + bounds[me] * ncols, w, base + bounds[me] * ld, (size_t)ld * 16, w,
                           (size_t)(bounds[me + 1] - bounds[me]), cudaMemcpyDeviceToDevice, st));
+  STRY(sh->comm.begin(err));
   ncclGroupStart();
   for (int i = 0; i < P; ++i) {
     if (bounds[i + 1] <= bounds[i]) continue;
@@ -333,6 +357,7 @@ int dist_share_rows(void* user, cplx* base, long long ld, long long ncols, const
     ncclBroadcast(p, p, (size_t)(bounds[i + 1] - bounds[i]) * w, ncclUint8, i, sh->comm.comm, st);
   }
   ncclResult_t r = ncclGroupEnd();
+  sh->comm.end(st);
   if (r != ncclSuccess) {
     if (err) *err = std::string("ncclBroadcast (distributed Cholesky): ") + ncclGetErrorString(r);
     return TRAJ_ENCCL;
@@ -363,6 +388,12 @@ int shard_init(ShardedCtx* sh, const traj_config* c, std::string* err) {
       if (err) *err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
       return TRAJ_ENCCL;
     }
+    const char* to = getenv("TRAJ_NCCL_TIMEOUT_S");
+    int dev = 0;
+    SCK(cudaGetDevice(&dev));
+    STRY(sh->comm.wd.start(sh->comm.comm, dev, to ? atof(to) : 600.0, err));
+    const char* ts = getenv("TRAJ_WATCHDOG_TEST_STALL");
+    sh->test_stall = ts && ts[0] == '1';
   }
   SCK(cudaMallocHost(&sh->h_small, std::max(sh->P + 8, 64) * 4));
   SCK(cudaMallocHost(&sh->h_dev, 64 * 8));
@@ -749,17 +780,25 @@ int propagate_dense(ShardedCtx* sh, int cur, int nxt, std::string* err) {
     const int g = l.g;
     SCK(cudaEventRecord(sh->ev_start, st));
     SCK(cudaStreamWaitEvent(sh->cst, sh->ev_start, 0));
-    for (int d = 1; d < P; ++d) {
-      const int to = (g + d) % P, from = (g - d + P) % P;
+    // comm_plan.h ring_plan: group d - 1 sends U_g to g + d and receives U_{g-d}; the K-chunk
+    // product of distance d waits for that group only
+    const std::vector<CommOp> plan = ring_plan(P, g);
+    for (size_t q = 0; q < plan.size();) {
+      const int grp = plan[q].group;
+      STRY(sh->comm.begin(err));
       ncclGroupStart();
-      ncclSend(l.U[cur], bytes, ncclUint8, to, sh->comm.comm, sh->cst);
-      ncclRecv(sh->Ufull + (size_t)from * Lp * ld, bytes, ncclUint8, from, sh->comm.comm, sh->cst);
+      for (; q < plan.size() && plan[q].group == grp; ++q) {
+        const CommOp& op = plan[q];
+        if (op.kind == COMM_SEND) ncclSend(l.U[cur], bytes, ncclUint8, op.peer, sh->comm.comm, sh->cst);
+        else ncclRecv(sh->Ufull + (size_t)op.block * Lp * ld, bytes, ncclUint8, op.peer, sh->comm.comm, sh->cst);
+      }
       ncclResult_t r = ncclGroupEnd();
+      sh->comm.end(sh->cst);
       if (r != ncclSuccess) {
         if (err) *err = std::string("nccl send/recv (propagate): ") + ncclGetErrorString(r);
         return TRAJ_ENCCL;
       }
-      SCK(cudaEventRecord(sh->ev_chunk[d], sh->cst));
+      SCK(cudaEventRecord(sh->ev_chunk[grp + 1], sh->cst));
     }
     for (int d = 0; d < P; ++d) {
       const int s = (g - d + P) % P;
@@ -789,6 +828,15 @@ int propagate_dense(ShardedCtx* sh, int cur, int nxt, std::string* err) {
 }  // namespace
 
 int shard_step(ShardedCtx* sh, long long* step, std::string* err) {
+  STRY(sh->comm.wd.check(err));
+  if (sh->test_stall) {   // test hook: a "collective" that never completes, and nothing behind it
+    STRY(sh->comm.wd.stall(sh->st, err));
+    return sh->comm.wd.mark(sh->st, err);
+  }
+  return shard_step_impl(sh, step, err);
+}
+
+int shard_step_impl(ShardedCtx* sh, long long* step, std::string* err) {
   const int cur = sh->cur, nxt = 1 - sh->cur;
   if (sh->banded) {
     Phase p(sh->prof, sh->st, TRAJ_PH_PROPAGATE);
@@ -818,6 +866,7 @@ int shard_step(ShardedCtx* sh, long long* step, std::string* err) {
 int shard_orthonormalize(ShardedCtx* sh, std::string* err) { return cqr2(sh, sh->cur, err); }
 
 int shard_entropy(ShardedCtx* sh, const int64_t* A, int64_t nA, double* S_out, std::string* err) {
+  STRY(sh->comm.wd.check(err));
   cudaStream_t st = sh->st;
   // split A by owning shard (order within a shard preserved; the spectrum is order-free)
   std::vector<std::vector<int32_t>> part(sh->P);
@@ -923,6 +972,7 @@ int shard_set_state(ShardedCtx* sh, const void* U_in, std::string* err) {
 int shard_failed(ShardedCtx* sh, int32_t* flag, std::string* err) {
   SCK(cudaMemcpyAsync(sh->h_small, sh->failed_dev, 4, cudaMemcpyDeviceToHost, sh->st));
   SCK(cudaStreamSynchronize(sh->st));
+  STRY(sh->comm.wd.check(err));
   *flag = sh->h_small[0];
   return 0;
 }
@@ -943,7 +993,8 @@ void shard_destroy(ShardedCtx* sh) {
     if (e) cudaEventDestroy(e);
   for (auto e : sh->ev_chunk)
     if (e) cudaEventDestroy(e);
-  if (sh->comm.comm) ncclCommDestroy(sh->comm.comm);
+  const bool aborted = sh->comm.wd.stop();   // an aborted communicator is already freed
+  if (sh->comm.comm && !aborted) ncclCommDestroy(sh->comm.comm);
   if (sh->h_small) cudaFreeHost(sh->h_small);
   if (sh->h_dev) cudaFreeHost(sh->h_dev);
 }

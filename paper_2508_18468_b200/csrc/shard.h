@@ -8,6 +8,7 @@
 #include "common.cuh"
 #include "profiler.h"
 #include "cholinv.h"
+#include "watchdog.h"
 
 typedef struct ncclComm* ncclComm_t;
 typedef struct cusolverDnContext* cusolverDnHandle_t;
@@ -21,6 +22,11 @@ namespace traj {
 struct ShardComm {
   int P = 1, P_local = 1, rank0 = 0;
   ncclComm_t comm = nullptr;
+  Watchdog wd;             // NCCL mode: async-error / deadline polling, abort (watchdog.h)
+  // every NCCL call site: begin() returns TRAJ_ENCCL once the communicator was aborted, else
+  // takes the watchdog's lock; end(st) releases it and hands the watchdog a completion mark on st
+  int begin(std::string* err);
+  void end(cudaStream_t st);
   int allgather(cudaStream_t st, void* const* send, void* recv, size_t bytes, std::string* err);
   int allreduce(cudaStream_t st, double* const* part, double* out, size_t n, std::string* err);
   // halo exchange on the ring of shards: recv_lo[s] <- send_hi of shard g-1, recv_hi[s] <- send_lo of g+1
@@ -106,6 +112,7 @@ struct ShardedCtx {
   std::vector<cudaEvent_t> ev_chunk;
   cusolverDnHandle_t solver = nullptr;
   Profiler* prof = nullptr;
+  bool test_stall = false;       // TRAJ_WATCHDOG_TEST_STALL=1 (NCCL mode): watchdog test hook
   double *obs_bins = nullptr, *obs_part = nullptr, *obs_out = nullptr;
   int32_t* obs_mask = nullptr;
 };
@@ -121,6 +128,7 @@ int shard_init(ShardedCtx* sh, const traj_config* c, std::string* err);
 int shard_build(ShardedCtx* sh, const std::vector<std::complex<double>>& kc, const std::vector<int32_t>& sites,
                 std::string* err, const std::vector<std::complex<double>>* band = nullptr);
 int shard_step(ShardedCtx* sh, long long* step, std::string* err);
+int shard_step_impl(ShardedCtx* sh, long long* step, std::string* err);
 int shard_orthonormalize(ShardedCtx* sh, std::string* err);
 int shard_entropy(ShardedCtx* sh, const int64_t* A, int64_t nA, double* S_out, std::string* err);
 int shard_occupations(ShardedCtx* sh, double* n_out, long long step, std::string* err);

@@ -28,6 +28,7 @@
 #include "dgemm.h"
 #include "planar.h"
 #include "small_step.h"
+#include "comm_plan.h"
 
 namespace traj {
 std::atomic<long long> g_kernel_launches{0};
@@ -188,7 +189,8 @@ int validate(const traj_config* c, std::string* why) {
   if (c->protocol != TRAJ_PROJECTIVE && c->protocol != TRAJ_HOMODYNE && c->protocol != TRAJ_HOMODYNE_RK4 &&
       c->protocol != TRAJ_PROJECTIVE_EVENTS)
     return bad("unknown protocol");
-  if (c->init != TRAJ_INIT_NEEL) return bad("unknown init");
+  if (c->init != TRAJ_INIT_NEEL && !(c->init == TRAJ_INIT_CHECKERBOARD && c->dim == 2))
+    return bad("init must be TRAJ_INIT_NEEL, or TRAJ_INIT_CHECKERBOARD in 2d");
   if (c->n_traj < 1 || c->n_traj > 65535) return bad("n_traj must be in [1, 65535]");
   if (c->traj_base < 0 || c->traj_base + c->n_traj > (1ll << 32)) return bad("trajectory ids must fit 32 bits");
   if (!c->gamma) return bad("gamma is null");
@@ -1581,6 +1583,23 @@ int traj_set_step(traj_handle h, int64_t step) {
   if (!h) return TRAJ_EINVAL;
   if (step < 0 || step >= (1ll << 32)) return fail(h, TRAJ_EINVAL, "step out of range");
   h->step = step;
+  if (h->cfg.protocol == TRAJ_PROJECTIVE_EVENTS) {
+    // the event clock at time step * dt, as event_window leaves it: ev_count = events before that
+    // time, ev_tnext = the next event's time (the same accumulation of the Philox waiting times),
+    // ev_tcur = the window end; host Philox only
+    const double t_end = step * h->cfg.dt;
+    for (int t = 0; t < h->T; ++t) {
+      long long e = 0;
+      double tn = event_wait(h, t, 0);
+      while (tn < t_end) {
+        ++e;
+        tn = tn + event_wait(h, t, e);
+      }
+      h->ev_count[t] = e;
+      h->ev_tnext[t] = tn;
+      h->ev_tcur[t] = t_end;
+    }
+  }
   return 0;
 }
 
@@ -1734,6 +1753,28 @@ int traj_nccl_unique_id(void* out128) {
   std::string e;
   int s = nccl_unique_id(out128, &e);
   return s ? fail(nullptr, s, e) : 0;
+}
+
+int64_t traj_comm_plan(int kind, int P, int rank, int64_t n, int64_t* out, int64_t max_entries) {
+  if (P < 1 || P > 1024 || rank < 0 || rank >= P || max_entries < 0 || (max_entries > 0 && !out))
+    return -fail(nullptr, TRAJ_EINVAL, "traj_comm_plan: bad arguments");
+  std::vector<int64_t> flat;
+  if (kind == 0 || kind == 1) {
+    for (const CommOp& op : kind == 0 ? ring_plan(P, rank) : halo_plan(P, rank))
+      flat.insert(flat.end(), {op.group, op.kind, op.peer, op.slot, op.block});
+  } else if (kind == 2) {
+    if (n < 1) return -fail(nullptr, TRAJ_EINVAL, "traj_comm_plan: n < 1");
+    const char* dm = getenv("TRAJ_DIST_CHOL_MIN");
+    const long long mn = dm ? atoll(dm) : 2048;
+    std::vector<BcastOp> b;
+    if (mn > 0) dist_chol_plan_rec(n, P, mn, &b);
+    for (const BcastOp& op : b) flat.insert(flat.end(), {op.root, op.rows, op.cols});
+  } else {
+    return -fail(nullptr, TRAJ_EINVAL, "traj_comm_plan: unknown kind");
+  }
+  const int64_t w = kind == 2 ? 3 : 5, count = (int64_t)flat.size() / w;
+  for (int64_t i = 0; i < std::min<int64_t>(count, max_entries) * w; ++i) out[i] = flat[i];
+  return count;
 }
 
 int traj_shard_info(traj_handle h, int32_t* shard_size, int32_t* local_shards, int64_t* row0, int64_t* rows) {

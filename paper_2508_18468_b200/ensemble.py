@@ -64,6 +64,20 @@ class EnsembleResult:
     count: dict
 
 
+def _observe(tr, kind: str, region):
+    """One sampled observable for every trajectory of the handle.  A spectrum newly found outside
+    [-1e-8, 1 + 1e-8] marks that trajectory failed and returns TRAJ_ENUMERIC (traj.h); the call is
+    then repeated, giving NaN for the failed one, which ``accumulate`` excludes -- so one bad
+    trajectory never aborts the ensemble (nor leaves the other ranks waiting in the all-reduce)."""
+    from .binding import TrajError
+    for attempt in range(2):
+        try:
+            return tr.entropy(region) if kind == "entropy" else tr.mutual_info(*region)
+        except TrajError as e:
+            if e.status != 3 or attempt == 1:
+                raise
+
+
 def run_ensemble(workload, steps: int, sample_every: int, observables: dict, rank: int = 0, world: int = 1,
                  group=None, device=None, max_batch: int | None = None, seed: int | None = None):
     """Advance this rank's block of the workload's trajectories and return ensemble
@@ -90,9 +104,9 @@ def run_ensemble(workload, steps: int, sample_every: int, observables: dict, ran
         for k, s in enumerate(times):
             tr.step(int(s - done))
             done = int(s)
-            ok = np.array([not tr.failed(t) for t in range(sub.size)])
             for name, (kind, region) in observables.items():
-                vals = tr.entropy(region) if kind == "entropy" else tr.mutual_info(*region)
+                vals = _observe(tr, kind, region)
+                ok = np.array([not tr.failed(t) for t in range(sub.size)])
                 local[name][k] += accumulate(vals, ok, gidx[b0:b0 + batch], n_gamma)
         tr.close()
     mean, sem, cnt = {}, {}, {}

@@ -18,7 +18,7 @@ def P():
     return P
 
 
-@pytest.mark.parametrize("protocol", ["projective", "homodyne", "homodyne_rk4"])
+@pytest.mark.parametrize("protocol", ["projective", "homodyne", "homodyne_rk4", "projective_events"])
 def test_checkpoint_resume_is_exact(P, protocol):
     """(state, step) is a complete checkpoint: counter-based Philox makes the resumed run
     bitwise identical to the uninterrupted one."""
