@@ -128,9 +128,15 @@ int traj_workspace_bytes(const traj_config* cfg, size_t* out);
 int traj_init(const traj_config* cfg, traj_handle* out);
 
 /* Advance every trajectory by n_steps >= 0 steps (P:203-209 / P:171-196).  Step s
- * draws Philox counters (site, s, traj_base + t, 0).  Asynchronous for the homodyne
- * protocol; the projective protocol synchronises once per step to size its click
- * list.  A trajectory whose Cholesky breaks down is marked failed (traj_failed).
+ * draws Philox counters (site, s, traj_base + t, 0).  Asynchronous (stream-ordered, no host
+ * round trip) for TRAJ_HOMODYNE, TRAJ_HOMODYNE_RK4 and TRAJ_PROJECTIVE with CholeskyQR2, sharded or
+ * not: the projective launches are sized by click counts the host computes from the same
+ * counter-based draws (the device's own draws decide the clicks), the occupied / empty counts of
+ * the Born sampling stay on the device (launches bounded there), and CholeskyQR2's second-pass
+ * fallback is decided on the device.  TRAJ_PROJECTIVE_EVENTS (host-drawn event times and staged
+ * stencil taps) and TRAJ_ORTH_LOWRANK (its k0 x k0 iteration checks convergence on the host)
+ * synchronise within the step.  A trajectory whose Cholesky breaks down is marked failed
+ * (traj_failed).
  * Small lattices (dense K, projective or homodyne, unsharded, U and the step's scratch
  * within one CTA's shared memory: L up to ~110) run all n_steps in one asynchronous launch
  * of the fused step (one CTA per trajectory); there a failed trajectory stops evolving.

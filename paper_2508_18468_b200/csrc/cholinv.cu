@@ -40,7 +40,9 @@ constexpr int NB = 64;            // leaf size
 // and the owners of row j scale it by 1/sqrt(d).  W ends as L^-1, so X = R^-1 = W^dag.
 template <int TW, int BS>
 __global__ void __launch_bounds__(TW * TW) chol_leaf_kernel(int n, cplx* G, long long ldg, long long sG, cplx* X,
-                                                            long long ldx, long long sX, int32_t* failed) {
+                                                            long long ldx, long long sX, int32_t* failed,
+                                                            const int32_t* gate) {
+  if (gate && *gate == 0) return;
   __shared__ double2 rowA[2][TW * BS], rowW[2][TW * BS], piv[2];
   __shared__ int bad;
   const int b = blockIdx.x, tid = threadIdx.x;
@@ -143,7 +145,9 @@ __device__ __forceinline__ void pending_w_row(double2* Ws, const double2* Gs, co
 }
 
 __global__ void __launch_bounds__(EW * 32) chol_leaf_elim_kernel(int n, const cplx* G, long long ldg, long long sG,
-                                                                 cplx* X, long long ldx, long long sX, int32_t* failed) {
+                                                                 cplx* X, long long ldx, long long sX, int32_t* failed,
+                                                                 const int32_t* gate) {
+  if (gate && *gate == 0) return;
   extern __shared__ __align__(16) double2 lsm[];
   double2* Gs = lsm;                 // [NB][ELD] upper triangle, eliminated in place
   double2* Ws = lsm + NB * ELD;      // [NB][ELD] W = L^-1 (lower)
@@ -261,6 +265,7 @@ struct Ctx {
   std::string* err;
   const CholDist* dist;
   const CholHook* hook;
+  DevBounds db;            // gate: every launch of the factorisation runs only if *gate != 0
   long long n_top;
   bool elim_leaf;
 };
@@ -281,7 +286,7 @@ int dist_gemm(Ctx& c, bool tri_c, int opA, int opB, long long M, long long N, lo
     if (m <= 0) continue;
     const cplx* Ai = opA == 0 ? A + b[i] * lda : A + b[i];
     int s = zgemm(c.st, opA, opB, m, N, K, alpha, 0.0, Ai, lda, 0, B, ldb, 0, beta, C + b[i] * ldc, ldc, 0, 1, flags,
-                  c.err, b[i], 0);
+                  c.err, b[i], 0, &c.db);
     if (s) return s;
   }
   if (d->rank < 0) return 0;
@@ -295,12 +300,12 @@ int rec(Ctx& c, long long o, long long n) {
       e = ensure_smem(reinterpret_cast<const void*>(chol_leaf_elim_kernel), ELEAF_SMEM);
       if (e == cudaSuccess)
         chol_leaf_elim_kernel<<<(unsigned)c.batch, EW * 32, ELEAF_SMEM, c.st>>>(
-            (int)n, c.G + o * c.ldg + o, c.ldg, c.sG, c.X + o * c.ldx + o, c.ldx, c.sX, c.failed);
+            (int)n, c.G + o * c.ldg + o, c.ldg, c.sG, c.X + o * c.ldx + o, c.ldx, c.sX, c.failed, c.db.gate);
     } else {
       auto leaf = n <= 16 ? chol_leaf_kernel<8, 2> : (n <= 32 ? chol_leaf_kernel<16, 2> : chol_leaf_kernel<32, 2>);
       const int threads = n <= 16 ? 64 : (n <= 32 ? 256 : 1024);
       leaf<<<(unsigned)c.batch, threads, 0, c.st>>>((int)n, c.G + o * c.ldg + o, c.ldg, c.sG, c.X + o * c.ldx + o,
-                                                    c.ldx, c.sX, c.failed);
+                                                    c.ldx, c.sX, c.failed, c.db.gate);
     }
     count_launch();
     if (e == cudaSuccess) e = cudaGetLastError();
@@ -335,20 +340,20 @@ int rec(Ctx& c, long long o, long long n) {
   }
   // R_B^dag = B^dag X_A : (r x h) = op_C(B: h x r) * X_A (h x h, upper)
   if ((s = zgemm(c.st, 1, 0, r, h, h, 1.0, 0.0, B_blk, c.ldg, c.sG, XA, c.ldx, c.sX, 0.0, L_blk, c.ldg, c.sG, c.batch,
-                 TRAJ_TRI_B_UPPER_F, c.err)))
+                 TRAJ_TRI_B_UPPER_F, c.err, 0, 0, &c.db)))
     return s;
   // C -= R_B^dag R_B (upper tiles)
   if ((s = zgemm(c.st, 0, 1, r, r, h, -1.0, 0.0, L_blk, c.ldg, c.sG, L_blk, c.ldg, c.sG, 1.0, C_blk, c.ldg, c.sG,
-                 c.batch, TRAJ_C_UPPER_F, c.err)))
+                 c.batch, TRAJ_C_UPPER_F, c.err, 0, 0, &c.db)))
     return s;
   if ((s = rec(c, o + h, r))) return s;
   // tmp = R_B X_C : (h x r) = op_C(L_blk: r x h) * X_C (r x r, upper)
   if ((s = zgemm(c.st, 1, 0, h, r, r, 1.0, 0.0, L_blk, c.ldg, c.sG, XC, c.ldx, c.sX, 0.0, c.tmp, c.ldt, c.sT, c.batch,
-                 TRAJ_TRI_B_UPPER_F, c.err)))
+                 TRAJ_TRI_B_UPPER_F, c.err, 0, 0, &c.db)))
     return s;
   // X_B = -X_A tmp
   if ((s = zgemm(c.st, 0, 0, h, r, h, -1.0, 0.0, XA, c.ldx, c.sX, c.tmp, c.ldt, c.sT, 0.0, XB, c.ldx, c.sX, c.batch,
-                 TRAJ_TRI_A_UPPER_F, c.err)))
+                 TRAJ_TRI_A_UPPER_F, c.err, 0, 0, &c.db)))
     return s;
   return 0;
 }
@@ -363,7 +368,7 @@ size_t chol_scratch_bytes(long long n, long long batch) {
 
 int chol_inverse(cudaStream_t st, long long n, cplx* G, long long ldg, long long sG, cplx* X, long long ldx,
                  long long sX, long long batch, void* scratch, int32_t* failed, std::string* err,
-                 const CholDist* dist, const CholHook* hook) {
+                 const CholDist* dist, const CholHook* hook, const int32_t* gate) {
   if (n <= 0 || batch <= 0) return 0;
   if (batch > 65535) {
     if (err) *err = "chol_inverse: batch too large";
@@ -385,6 +390,7 @@ int chol_inverse(cudaStream_t st, long long n, cplx* G, long long ldg, long long
   c.err = err;
   c.dist = dist;
   c.hook = hook;
+  c.db.gate = gate;
   c.n_top = n;
   {
     const char* lf = getenv("TRAJ_CHOL_LEAF");

@@ -319,17 +319,18 @@ __global__ void zero_rows_batched_kernel(cplx* U, long long ld, long long sU, co
 }
 
 // T[S1[c]][c] -= 1
-__global__ void sub_identity_kernel(cplx* T, long long ld, const int32_t* S1, int k, int row0, int nrows) {
+__global__ void sub_identity_kernel(cplx* T, long long ld, const int32_t* S1, int k, int row0, int nrows,
+                                    const int32_t* k_dev) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= k) return;
+  if (c >= k || (k_dev && c >= *k_dev)) return;
   const int r = S1[c] - row0;
   if (r >= 0 && r < nrows) T[(long long)r * ld + c].x -= 1.0;
 }
 
 __global__ void zero_rows_kernel(cplx* U, long long ld, const int32_t* rows, int nrows, int ncols, int row0,
-                                 int nlocal) {
+                                 int nlocal, const int32_t* k_dev) {
   const int r = blockIdx.y;
-  if (r >= nrows) return;
+  if (r >= nrows || (k_dev && r >= *k_dev)) return;
   const int lr = rows[r] - row0;
   if (lr < 0 || lr >= nlocal) return;
   cplx* p = U + (long long)lr * ld;
@@ -432,6 +433,20 @@ __global__ void first_order_inverse_kernel(const cplx* G, long long ldg, long lo
   }
 }
 
+// gate[0] = 1 if some trajectory's max|G2 - I| exceeds thr (a NaN -- failed trajectory -- does not),
+// then the full factorisation runs; counts the fallbacks on the device
+__global__ void cqr2_decide_kernel(const unsigned long long* dev, int T, double thr, int32_t* gate,
+                                   unsigned long long* fallbacks) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int full = 0;
+  for (int t = 0; t < T; ++t) {
+    const double m = __longlong_as_double((long long)dev[t]);
+    if (m > thr) full = 1;
+  }
+  gate[0] = full;
+  if (full && fallbacks) fallbacks[0] += 1ull;
+}
+
 cudaError_t last(std::string* err, const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess && err) *err = std::string(what) + ": " + cudaGetErrorString(e);
@@ -478,6 +493,21 @@ int click_draw(cudaStream_t st, int L, int T, long long step, long long traj_bas
                                           gamma_dev, dt, flags, site0);
   count_launch();
   return last(err, "click_draw") == cudaSuccess ? 0 : 4;
+}
+
+void host_click_counts(int L, int T, long long step, long long traj_base, uint64_t seed, const double* gamma,
+                       double dt, int32_t* counts, int site0) {
+  const uint32_t k0 = (uint32_t)(seed & 0xffffffffu), k1 = (uint32_t)(seed >> 32);
+  for (int t = 0; t < T; ++t) {
+    const double p = gamma[t] * dt;
+    int c = 0;
+    if (p > 0)
+      for (int i = 0; i < L; ++i) {
+        const u32x4 x = philox4x32_10(u32x4{(uint32_t)(site0 + i), (uint32_t)step, (uint32_t)(traj_base + t), 0u}, k0, k1);
+        c += u53(x.x, x.y) < p ? 1 : 0;
+      }
+    counts[t] = c;
+  }
 }
 
 int compact(cudaStream_t st, const int32_t* flags, int L, int T, int32_t* list, int cap, int32_t* count,
@@ -577,18 +607,18 @@ int zero_rows_batched(cudaStream_t st, cplx* U, long long ld, long long sU, cons
 }
 
 int sub_identity(cudaStream_t st, cplx* T, long long ld, const int32_t* S1, int k, std::string* err, int row0,
-                 int nrows) {
+                 int nrows, const int32_t* k_dev) {
   if (k <= 0) return 0;
-  sub_identity_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(T, ld, S1, k, row0, nrows);
+  sub_identity_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(T, ld, S1, k, row0, nrows, k_dev);
   count_launch();
   return last(err, "sub_identity") == cudaSuccess ? 0 : 4;
 }
 
 int zero_rows(cudaStream_t st, cplx* U, long long ld, const int32_t* rows, int nrows, int ncols, std::string* err,
-              int row0, int nlocal) {
+              int row0, int nlocal, const int32_t* k_dev) {
   if (nrows <= 0) return 0;
   dim3 grid((unsigned)std::min<long long>(ceil_div(ncols, 256), 64), nrows);
-  zero_rows_kernel<<<grid, 256, 0, st>>>(U, ld, rows, nrows, ncols, row0, nlocal);
+  zero_rows_kernel<<<grid, 256, 0, st>>>(U, ld, rows, nrows, ncols, row0, nlocal, k_dev);
   count_launch();
   return last(err, "zero_rows") == cudaSuccess ? 0 : 4;
 }
@@ -722,6 +752,27 @@ int gram_deviation(cudaStream_t st, const cplx* G, long long ld, long long sG, i
   gram_deviation_kernel<<<grid, 256, 0, st>>>(G, ld, sG, n, out);
   count_launch();
   return last(err, "gram_deviation") == cudaSuccess ? 0 : 4;
+}
+
+__global__ void sum_i32_kernel(const int32_t* in, int n, int32_t* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    int v = 0;
+    for (int i = 0; i < n; ++i) v += in[i];
+    out[0] = v;
+  }
+}
+
+int sum_i32(cudaStream_t st, const int32_t* in, int n, int32_t* out, std::string* err) {
+  sum_i32_kernel<<<1, 32, 0, st>>>(in, n, out);
+  count_launch();
+  return last(err, "sum_i32") == cudaSuccess ? 0 : 4;
+}
+
+int cqr2_decide(cudaStream_t st, const unsigned long long* dev, int T, double thr, int32_t* gate,
+                unsigned long long* fallbacks, std::string* err) {
+  cqr2_decide_kernel<<<1, 32, 0, st>>>(dev, T, thr, gate, fallbacks);
+  count_launch();
+  return last(err, "cqr2_decide") == cudaSuccess ? 0 : 4;
 }
 
 int first_order_inverse(cudaStream_t st, const cplx* G, long long ldg, long long sG, cplx* X, long long ldx,

@@ -296,6 +296,8 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
   lay.take(sh->S_dev, 16);
   lay.take(sh->bad_dev, 16);
   lay.take(sh->gdev, 16);
+  lay.take(sh->fb_dev, 16);
+  lay.take(sh->gate, 16);
   lay.take(sh->region, (size_t)L * 4);
   lay.take(sh->kcoef, (size_t)(c->Lx + c->Ly) * 16);
   lay.take(sh->sites, (size_t)N * 4);
@@ -514,13 +516,16 @@ int cqr2(ShardedCtx* sh, int src_which, std::string* err) {
     }
     {
       Phase p(sh->prof, sh->st, TRAJ_PH_CHOL);
-      bool full = pass == 0 || sh->full_cqr2;
+      const bool full = pass == 0 || sh->full_cqr2;
       if (!full) {
+        // decided on the device from the all-reduced G2 (the same bits on every rank): the
+        // first-order factor, overwritten by the gated full factorisation when it is needed
+        // (replicated, not distributed: a gated-off step must not move the Cholesky's broadcasts)
         STRY(gram_deviation(sh->st, sh->G, sh->ldN, 0, sh->N, 1, sh->gdev, err));
-        SCK(cudaMemcpyAsync(sh->h_dev, sh->gdev, 8, cudaMemcpyDeviceToHost, sh->st));
-        SCK(cudaStreamSynchronize(sh->st));
-        if (sh->h_dev[0] > 1e-9 / sqrt((double)sh->N)) full = true;
-        if (full) ++sh->cqr2_fallbacks;
+        STRY(cqr2_decide(sh->st, sh->gdev, 1, 1e-9 / sqrt((double)sh->N), sh->gate, sh->fb_dev, err));
+        STRY(first_order_inverse(sh->st, sh->G, sh->ldN, 0, sh->X, sh->ldN, 0, sh->N, 1, err));
+        STRY(chol_inverse(sh->st, sh->N, sh->G, sh->ldN, 0, sh->X, sh->ldN, 0, 1, sh->chol_scratch, sh->failed_dev,
+                          err, nullptr, nullptr, sh->gate));
       }
       if (full && pass == 0 && sh->chol_overlap && sh->N > 64) {
         // factorise on st_hi; each newly final left column block's TRMM runs on st_lo
@@ -571,8 +576,6 @@ int cqr2(ShardedCtx* sh, int src_which, std::string* err) {
       if (full)
         STRY(chol_inverse(sh->st, sh->N, sh->G, sh->ldN, 0, sh->X, sh->ldN, 0, 1, sh->chol_scratch, sh->failed_dev,
                           err, &sh->cdist));
-      else
-        STRY(first_order_inverse(sh->st, sh->G, sh->ldN, 0, sh->X, sh->ldN, 0, sh->N, 1, err));
     }
     {
       Phase p(sh->prof, sh->st, TRAJ_PH_TRMM);
@@ -605,94 +608,101 @@ int projective(ShardedCtx* sh, int which, long long step, std::string* err) {
   Phase p(sh->prof, sh->st, TRAJ_PH_PROJECT);
   cudaStream_t st = sh->st;
   const int capr = sh->capr, P = sh->P;
+  // per-shard click counts on the host (the device's click_draw makes the same counter-based
+  // decisions): they size every launch below, so the step needs no host round trip
+  sh->hcnt.assign(P, 0);
+  for (int q = 0; q < P; ++q)
+    host_click_counts(sh->Lp, 1, step, sh->traj_base, sh->seed, &sh->gamma, sh->dt, &sh->hcnt[q], q * sh->Lp);
+  int total = 0;
+  for (int q = 0; q < P; ++q) {
+    if (sh->hcnt[q] > capr) {
+      if (err) *err = "click list overflow on shard " + std::to_string(q);
+      return TRAJ_ENUMERIC;
+    }
+    total += sh->hcnt[q];
+  }
+  sh->last_nS = total;
+  sh->last_n1 = 0;
+  sh->k1_dev = false;
+  if (total == 0) {
+    if (sh->lowrank_gram) sh->lr_k0 = 0;     // U = K U is orthonormal: pass 1 has R = I
+    return 0;
+  }
   for (auto& l : sh->loc) {
     STRY(compact(st, l.flags, sh->Lp, 1, l.Sloc, capr, l.cnt, err, l.row0));
     STRY(gather_rows(st, l.U[which], sh->ldN, 0, l.Sloc, 0, l.cnt, capr, 1, l.USloc, sh->ldN, 0, sh->N, err, l.row0));
   }
   {
-    std::vector<void*> a, b, c;
+    std::vector<void*> b, c;
     for (auto& l : sh->loc) {
-      a.push_back(l.cnt);
       b.push_back(l.Sloc);
       c.push_back(l.USloc);
     }
-    STRY(sh->comm.allgather(st, a.data(), sh->cntrecv, 4, err));
     STRY(sh->comm.allgather(st, b.data(), sh->Srecv, (size_t)capr * 4, err));
     STRY(sh->comm.allgather(st, c.data(), sh->USrecv, (size_t)capr * sh->ldN * 16, err));
-  }
-  SCK(cudaMemcpyAsync(sh->h_small, sh->cntrecv, P * 4, cudaMemcpyDeviceToHost, st));
-  SCK(cudaStreamSynchronize(st));
-  std::vector<int> cnt(sh->h_small, sh->h_small + P);
-  int total = 0;
-  for (int q = 0; q < P; ++q) {
-    if (cnt[q] > capr) {
-      if (err) *err = "click list overflow on shard " + std::to_string(q);
-      return TRAJ_ENUMERIC;
-    }
-    total += cnt[q];
-  }
-  sh->last_nS = total;
-  sh->last_n1 = 0;
-  if (total == 0) {
-    if (sh->lowrank_gram) sh->lr_k0 = 0;     // U = K U is orthonormal: pass 1 has R = I
-    return 0;
   }
   // pack the per-shard blocks (shard order = ascending sites) into S and U_S
   int off = 0;
   for (int q = 0; q < P; ++q) {
-    if (cnt[q] == 0) continue;
-    SCK(cudaMemcpyAsync(sh->S + off, sh->Srecv + (size_t)q * capr, cnt[q] * 4, cudaMemcpyDeviceToDevice, st));
+    const int cq = sh->hcnt[q];
+    if (cq == 0) continue;
+    SCK(cudaMemcpyAsync(sh->S + off, sh->Srecv + (size_t)q * capr, cq * 4, cudaMemcpyDeviceToDevice, st));
     SCK(cudaMemcpyAsync(sh->US + (size_t)off * sh->ldN, sh->USrecv + (size_t)q * capr * sh->ldN,
-                        (size_t)cnt[q] * sh->ldN * 16, cudaMemcpyDeviceToDevice, st));
-    off += cnt[q];
+                        (size_t)cq * sh->ldN * 16, cudaMemcpyDeviceToDevice, st));
+    off += cq;
   }
-  sh->h_small[P] = total;
-  SCK(cudaMemcpyAsync(sh->count, sh->h_small + P, 4, cudaMemcpyHostToDevice, st));
+  // the total on the device: the local counts of every shard are the host's (same draws)
+  {
+    std::vector<void*> a;
+    for (auto& l : sh->loc) a.push_back(l.cnt);
+    STRY(sh->comm.allgather(st, a.data(), sh->cntrecv, 4, err));
+    STRY(sum_i32(st, sh->cntrecv, P, sh->count, err));
+  }
   // replicated: C_SS, sampling, W
   STRY(zgemm(st, 0, 1, total, total, sh->N, 1.0, 0.0, sh->US, sh->ldN, 0, sh->US, sh->ldN, 0, 0.0, sh->D0, sh->ldcap,
              0, 1, 0, err));
   STRY(sample_outcomes(st, sh->D0, sh->Dw, sh->ldcap, 0, sh->S, sh->cap, sh->count, total, 1, step, sh->traj_base,
                        sh->seed, sh->occ, sh->Linv, sh->DLinv, sh->Ybuf, sh->Zbuf, sh->ldcap, sh->pos1, sh->S1, sh->S0,
                        sh->k1, sh->k0, err, sh->pos0));
-  SCK(cudaMemcpyAsync(sh->h_small, sh->k1, 4, cudaMemcpyDeviceToHost, st));
-  SCK(cudaMemcpyAsync(sh->h_small + 1, sh->k0, 4, cudaMemcpyDeviceToHost, st));
-  SCK(cudaStreamSynchronize(st));
-  const int k1 = sh->h_small[0], k0 = sh->h_small[1];
-  sh->last_n1 = k1;
-  if (k1 > 0) {
-    STRY(gather_sub(st, sh->D0, sh->ldcap, sh->pos1, k1, sh->D11, sh->ldcap, err));
-    STRY(chol_inverse(st, k1, sh->D11, sh->ldcap, 0, sh->X11, sh->ldcap, 0, 1, sh->chol_scratch_small, sh->failed_dev,
-                      err));
-    // U_{S1} = rows pos1 of U_S (into USrecv, free now)
-    STRY(gather_rows(st, sh->US, sh->ldN, 0, sh->pos1, 0, nullptr, k1, 1, sh->USrecv, sh->ldN, 0, sh->N, err));
-    STRY(zgemm(st, 1, 0, sh->N, k1, k1, 1.0, 0.0, sh->USrecv, sh->ldN, 0, sh->X11, sh->ldcap, 0, 0.0, sh->W,
-               sh->ldcap, 0, 1, TRAJ_TRI_B_UPPER_F, err));
-    for (auto& l : sh->loc) {
-      STRY(zgemm(st, 0, 0, sh->Lp, k1, sh->N, 1.0, 0.0, l.U[which], sh->ldN, 0, sh->W, sh->ldcap, 0, 0.0, l.Tm,
-                 sh->ldcap, 0, 1, 0, err));
-      STRY(sub_identity(st, l.Tm, sh->ldcap, sh->S1, k1, err, l.row0, sh->Lp));
-      STRY(zgemm(st, 0, 1, sh->Lp, sh->N, k1, -1.0, 0.0, l.Tm, sh->ldcap, 0, sh->W, sh->ldcap, 0, 1.0, l.U[which],
-                 sh->ldN, 0, 1, 0, err));
-    }
+  sh->k1_dev = true;
+  // k1, k0 stay on the device: launches sized by the click count `total`, bounded there (zgemm.h
+  // DevBounds; identity past k1 in C_{S1 S1}, zero rows past k1 / k0 in the gathered blocks)
+  DevBounds b1, bk, b0;
+  b1.n = sh->k1;
+  b1.k = sh->k1;
+  bk.k = sh->k1;
+  b0.k = sh->k0;
+  STRY(gather_sub_batched(st, sh->D0, sh->ldcap, 0, sh->pos1, sh->cap, sh->k1, total, 1, sh->D11, sh->ldcap, 0, err));
+  STRY(chol_inverse(st, total, sh->D11, sh->ldcap, 0, sh->X11, sh->ldcap, 0, 1, sh->chol_scratch_small, sh->failed_dev,
+                    err));
+  // U_{S1} = rows pos1 of U_S (into USrecv, free now; zero past k1)
+  STRY(gather_rows(st, sh->US, sh->ldN, 0, sh->pos1, 0, sh->k1, total, 1, sh->USrecv, sh->ldN, 0, sh->N, err, 0, 1));
+  STRY(zgemm(st, 1, 0, sh->N, total, total, 1.0, 0.0, sh->USrecv, sh->ldN, 0, sh->X11, sh->ldcap, 0, 0.0, sh->W,
+             sh->ldcap, 0, 1, TRAJ_TRI_B_UPPER_F, err, 0, 0, &b1));
+  for (auto& l : sh->loc) {
+    DevBounds bn;
+    bn.n = sh->k1;
+    STRY(zgemm(st, 0, 0, sh->Lp, total, sh->N, 1.0, 0.0, l.U[which], sh->ldN, 0, sh->W, sh->ldcap, 0, 0.0, l.Tm,
+               sh->ldcap, 0, 1, 0, err, 0, 0, &bn));
+    STRY(sub_identity(st, l.Tm, sh->ldcap, sh->S1, total, err, l.row0, sh->Lp, sh->k1));
+    STRY(zgemm(st, 0, 1, sh->Lp, sh->N, total, -1.0, 0.0, l.Tm, sh->ldcap, 0, sh->W, sh->ldcap, 0, 1.0, l.U[which],
+               sh->ldN, 0, 1, 0, err, 0, 0, &bk));
   }
-  if (k0 > 0)
-    for (auto& l : sh->loc) STRY(zero_rows(st, l.U[which], sh->ldN, sh->S0, k0, sh->N, err, l.row0, sh->Lp));
+  for (auto& l : sh->loc) STRY(zero_rows(st, l.U[which], sh->ldN, sh->S0, total, sh->N, err, l.row0, sh->Lp, sh->k0));
   if (sh->lowrank_gram) {
     // U was orthonormal before the rows S0 were zeroed, so pass 1's Gram is I - V^dag V with V the
     // zeroed rows after the rank-k1 update: V = U_S0 - (U_S0 W) W^dag from the gathered rows (replicated)
-    if (k0 > 0) {
-      STRY(gather_rows(st, sh->US, sh->ldN, 0, sh->pos0, 0, nullptr, k0, 1, sh->USrecv, sh->ldN, 0, sh->N, err));
-      if (k1 > 0) {
-        STRY(zgemm(st, 0, 0, k0, k1, sh->N, 1.0, 0.0, sh->USrecv, sh->ldN, 0, sh->W, sh->ldcap, 0, 0.0, sh->D11,
-                   sh->ldcap, 0, 1, 0, err));
-        STRY(zgemm(st, 0, 1, k0, sh->N, k1, -1.0, 0.0, sh->D11, sh->ldcap, 0, sh->W, sh->ldcap, 0, 1.0, sh->USrecv,
-                   sh->ldN, 0, 1, 0, err));
-      }
-      STRY(set_identity(st, sh->G, sh->ldN, 0, sh->N, 1, err));
-      STRY(zgemm(st, 1, 0, sh->N, sh->N, k0, -1.0, 0.0, sh->USrecv, sh->ldN, 0, sh->USrecv, sh->ldN, 0, 1.0, sh->G,
-                 sh->ldN, 0, 1, TRAJ_C_UPPER_F, err));
-    }
-    sh->lr_k0 = k0;
+    DevBounds bn;
+    bn.n = sh->k1;
+    STRY(gather_rows(st, sh->US, sh->ldN, 0, sh->pos0, 0, sh->k0, total, 1, sh->USrecv, sh->ldN, 0, sh->N, err, 0, 1));
+    STRY(zgemm(st, 0, 0, total, total, sh->N, 1.0, 0.0, sh->USrecv, sh->ldN, 0, sh->W, sh->ldcap, 0, 0.0, sh->D11,
+               sh->ldcap, 0, 1, 0, err, 0, 0, &bn));
+    STRY(zgemm(st, 0, 1, total, sh->N, total, -1.0, 0.0, sh->D11, sh->ldcap, 0, sh->W, sh->ldcap, 0, 1.0, sh->USrecv,
+               sh->ldN, 0, 1, 0, err, 0, 0, &bk));
+    STRY(set_identity(st, sh->G, sh->ldN, 0, sh->N, 1, err));
+    STRY(zgemm(st, 1, 0, sh->N, sh->N, total, -1.0, 0.0, sh->USrecv, sh->ldN, 0, sh->USrecv, sh->ldN, 0, 1.0, sh->G,
+               sh->ldN, 0, 1, TRAJ_C_UPPER_F, err, 0, 0, &b0));
+    sh->lr_k0 = total;
   }
   return 0;
 }

@@ -85,6 +85,10 @@ struct ShardedCtx {
   int32_t* h_small = nullptr;
   double* h_dev = nullptr;
   long long last_nS = 0, last_n1 = 0, cqr2_fallbacks = 0;
+  unsigned long long* fb_dev = nullptr;   // second passes that took the full factorisation (device count)
+  int32_t* gate = nullptr;                // this step's second-pass decision (device)
+  bool k1_dev = false;                    // the last step's occupied count is in k1 (device)
+  std::vector<int32_t> hcnt;              // per-shard click counts of the current step (host Philox)
   bool full_cqr2 = false;
   // pass 1 of CholeskyQR after a projective step: G = I - V^dag V from the zeroed rows V, formed
   // from the gathered (replicated) U_S rows -- no Gram, no allreduce (TRAJ_LOWRANK_GRAM=0: measured)

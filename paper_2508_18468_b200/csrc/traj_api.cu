@@ -120,6 +120,16 @@ struct traj_ctx {
   double* obs_out = nullptr;             // [n_traj]
   int32_t* obs_mask = nullptr;           // region indicator [L]
   long long cqr2_fallbacks = 0;
+  unsigned long long* fb_dev = nullptr;  // CholeskyQR2 second passes that took the full factorisation
+  int32_t* gate = nullptr;               // [1]: this step's second-pass decision (device)
+  std::vector<int32_t> hcount;           // host click counts of the current step (host Philox)
+  bool k1_dev = false;                   // the last projective step's occupied counts are in k1 (device)
+  const int32_t* lr_kdev = nullptr;      // device bound of pass 1's V rows (k0), with lr_k0 its capacity
+  // CholeskyQR pass 1 on the structure G = I - V^dag V (structured_pass1; TRAJ_STRUCT_CHOL=0: dense)
+  bool struct_chol = true;
+  int sb = 128;                          // column block of the structured factorisation
+  cplx *sY = nullptr, *sC = nullptr, *sX = nullptr, *sW = nullptr, *sZ = nullptr;
+  void* s_chol_scratch = nullptr;
   cplx* kcoef = nullptr;
   int32_t* sites = nullptr;
   cusolverDnHandle_t solver = nullptr;
@@ -320,6 +330,8 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
   lay.take(h->S_dev, (size_t)T * 8);
   lay.take(h->bad_dev, (size_t)T * 4);
   lay.take(h->gdev, (size_t)T * 8);
+  lay.take(h->fb_dev, 8);
+  lay.take(h->gate, 16);
   lay.take(h->obs_bins, (size_t)L * 8);
   lay.take(h->obs_part, 1024 * 8);
   lay.take(h->obs_out, (size_t)T * 8);
@@ -359,6 +371,18 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     if (c->orthonormalizer == TRAJ_ORTH_LOWRANK) {
       for (cplx** b : {&h->Mb, &h->Yb, &h->Zb, &h->Tb, &h->Pb, &h->Qb}) lay.take(*b, (size_t)T * cap * ldcap * 16);
       lay.take(h->FV, (size_t)T * cap * ldN * 16);
+    }
+    {   // structured CholeskyQR pass 1 (structured_pass1): Y [cap][sb], C [sb][sb], the blocks' R^-1
+        // [N][sb], W = V X and Z = M W [cap][ldN]
+      const char* sbv = getenv("TRAJ_STRUCT_B");
+      h->sb = sbv ? std::max(16, std::min(1024, atoi(sbv) / 16 * 16)) : 128;
+      const long long b = h->sb;
+      lay.take(h->sY, (size_t)T * cap * b * 16);
+      lay.take(h->sC, (size_t)T * b * b * 16);
+      lay.take(h->sX, (size_t)T * round_up(N, b) * b * 16);
+      lay.take(h->sW, (size_t)T * cap * ldN * 16);
+      lay.take(h->sZ, (size_t)T * cap * ldN * 16);
+      lay.take(h->s_chol_scratch, chol_scratch_bytes(b, T));
     }
   }
   return lay.off + 256;
@@ -407,15 +431,19 @@ std::vector<std::complex<double>> ring_coefficients(int n, double J, double dt) 
 // with one trajectory the K range is split in two halves run as one batch-2 launch (twice the CTAs
 // for the few output tiles), the second half into Tm2, then added; otherwise one launch.
 int skinny_gemm(traj_ctx* h, int opB, long long M, long long Nc, long long K, const cplx* A, long long lda, long long sA,
-                const cplx* B, long long ldb, long long sB, cplx* C, long long sC) {
+                const cplx* B, long long ldb, long long sB, cplx* C, long long sC, const int32_t* nc_dev = nullptr) {
   const long long tiles = ceil_div(M, 64) * ceil_div(Nc, 64);
+  DevBounds db;             // output columns needed per trajectory (device), Nc their capacity
+  db.n = nc_dev;
   if (h->T != 1 || !h->Tm2 || C != h->Tm || K < 2048 || K % 32 || tiles >= 8 * 148)
-    return zgemm(h->st, 0, opB, M, Nc, K, 1.0, 0.0, A, lda, sA, B, ldb, sB, 0.0, C, h->ldcap, sC, h->T, 0, &h->err);
+    return zgemm(h->st, 0, opB, M, Nc, K, 1.0, 0.0, A, lda, sA, B, ldb, sB, 0.0, C, h->ldcap, sC, h->T, 0, &h->err, 0, 0,
+                 &db);
+  db.per_batch = 0;         // the batch of two is the two K halves of the one trajectory
   // batch entry z in {0, 1} takes k in [z K/2, (z + 1) K/2): A's columns and B's rows (opB = 0) or
   // columns (opB = 1) at a batch stride of K/2, the outputs at Tm and Tm2 (stride Tm2 - Tm)
   const long long k2 = K / 2;
   int s = zgemm(h->st, 0, opB, M, Nc, k2, 1.0, 0.0, A, lda, k2, B, ldb, opB == 0 ? k2 * ldb : k2, 0.0, C, h->ldcap,
-                h->Tm2 - C, 2, 0, &h->err);
+                h->Tm2 - C, 2, 0, &h->err, 0, 0, &db);
   if (!s) s = add_inplace(h->st, reinterpret_cast<double*>(C), reinterpret_cast<const double*>(h->Tm2),
                           M * h->ldcap * 2, &h->err);
   return s;
@@ -429,6 +457,75 @@ int prod3(traj_ctx* h, int opA, long long M, long long N, long long K, const dou
           long long n_off = 0) {
   return dgemm(st ? st : h->st, opA, M, N, K, 1.0, A, lda, sA, B, ldb, sB, 0.0, C, h->ldP, sC, 3LL * h->T, flags,
                &h->err, 0, n_off);
+}
+
+// CholeskyQR pass 1 after a projective step, on the structure of its Gram: G = I - V^dag V with V
+// the k0 rows the empty outcomes zeroed (k0 << N), so every Schur complement of G is I - V^dag M V
+// for a k0 x k0 matrix M.  Column blocks c of width b (sequential over c):
+//   Y = M V_c,  C_c = I - V_c^dag Y = R_c^dag R_c,  X_c = R_c^-1,  W_c = V_c X_c,  Z_c = M W_c,
+//   M <- M + Z_c Z_c^dag                                  (the Schur update M + Y C_c^-1 Y^dag)
+// gives the Cholesky factor of G block row by block row: R_cc = R_c, R_{c,d} = -Z_c^dag V_d (d > c).
+// The triangular solve dst = src R^-1 then runs over the column blocks with an L x k0 accumulator
+//   dst_c = src_c X_c + A W_c,   A <- A + dst_c Z_c^dag      (A = sum_{d < c} dst_d Z_d^dag)
+// -- exactly the dense CholeskyQR pass (same R, same U R^-1 to rounding) in O(N k0^2 + L N k0 + L N b)
+// flops instead of O(N^3 + L N^2).  V is in US (capacity lr rows, zero past k0 -- read on the device),
+// M in Dw, A in Tm.
+int structured_pass1(traj_ctx* h, const cplx* src, cplx* dst, int kc) {
+  const int T = h->T, N = h->N, L = h->L, b = h->sb;
+  const long long ldk = h->ldcap, sM = h->sD, sV = h->sUS, sY = (long long)h->cap * b, sC = (long long)b * b;
+  const long long sXb = round_up(N, b) * b, sA = (long long)L * h->ldcap;
+  DevBounds bk;              // reductions over the k0 rows of V
+  bk.k = h->lr_kdev;
+  DevBounds bn;              // outputs with k0 columns
+  bn.n = h->lr_kdev;
+  // M = I
+  CK(cudaMemsetAsync(h->Dw, 0, (size_t)T * sM * 16, h->st));
+  TRY(axpby_identity(h->st, h->Dw, ldk, sM, kc, T, 1.0, 1.0, &h->err));
+  const int nblk = (int)ceil_div(N, b);
+  for (int c = 0; c < nblk; ++c) {
+    const int c0 = c * b, bc = std::min(b, N - c0);
+    const cplx* Vc = h->US + c0;
+    cplx* Xc = h->sX + (long long)c0 * b;
+    // Y = M V_c (kc x bc);  C = I - V_c^dag Y (upper);  X_c = chol_inv(C)
+    TRY(zgemm(h->st, 0, 0, kc, bc, kc, 1.0, 0.0, h->Dw, ldk, sM, Vc, h->ldN, sV, 0.0, h->sY, b, sY, T, 0, &h->err, 0, 0,
+              &bk));
+    TRY(set_identity(h->st, h->sC, b, sC, bc, T, &h->err));
+    TRY(zgemm(h->st, 1, 0, bc, bc, kc, -1.0, 0.0, Vc, h->ldN, sV, h->sY, b, sY, 1.0, h->sC, b, sC, T, TRAJ_C_UPPER_F,
+              &h->err, 0, 0, &bk));
+    TRY(chol_inverse(h->st, bc, h->sC, b, sC, Xc, b, sXb, T, h->s_chol_scratch, h->failed_dev, &h->err));
+    // W_c = V_c X_c,  Z_c = M W_c  (into the block's columns of sW, sZ)
+    TRY(zgemm(h->st, 0, 0, kc, bc, bc, 1.0, 0.0, Vc, h->ldN, sV, Xc, b, sXb, 0.0, h->sW + c0, h->ldN, sV, T,
+              TRAJ_TRI_B_UPPER_F, &h->err));
+    TRY(zgemm(h->st, 0, 0, kc, bc, kc, 1.0, 0.0, h->Dw, ldk, sM, h->sW + c0, h->ldN, sV, 0.0, h->sZ + c0, h->ldN, sV, T,
+              0, &h->err, 0, 0, &bk));
+    // M += Z_c Z_c^dag
+    if (c + 1 < nblk)
+      TRY(zgemm(h->st, 0, 1, kc, kc, bc, 1.0, 0.0, h->sZ + c0, h->ldN, sV, h->sZ + c0, h->ldN, sV, 1.0, h->Dw, ldk, sM,
+                T, 0, &h->err));
+  }
+  // dst = src blockdiag(X_c): the full blocks as one batched launch per trajectory, then the tail
+  const int nfull = N / b;
+  for (int t = 0; t < T; ++t) {
+    if (nfull > 0)
+      TRY(zgemm(h->st, 0, 0, L, b, b, 1.0, 0.0, src + t * h->sU, h->ldN, b, h->sX + t * sXb, b, (long long)b * b, 0.0,
+                dst + t * h->sU, h->ldN, b, nfull, TRAJ_TRI_B_UPPER_F, &h->err));
+    if (nfull < nblk) {
+      const int c0 = nfull * b, bc = N - c0;
+      TRY(zgemm(h->st, 0, 0, L, bc, bc, 1.0, 0.0, src + t * h->sU + c0, h->ldN, 0, h->sX + t * sXb + (long long)c0 * b,
+                b, 0, 0.0, dst + t * h->sU + c0, h->ldN, 0, 1, TRAJ_TRI_B_UPPER_F, &h->err));
+    }
+  }
+  // the sequential part: dst_c += A W_c, A (+)= dst_c Z_c^dag
+  for (int c = 0; c < nblk; ++c) {
+    const int c0 = c * b, bc = std::min(b, N - c0);
+    if (c > 0)
+      TRY(zgemm(h->st, 0, 0, L, bc, kc, 1.0, 0.0, h->Tm, ldk, sA, h->sW + c0, h->ldN, sV, 1.0, dst + c0, h->ldN, h->sU,
+                T, 0, &h->err, 0, 0, &bk));
+    if (c + 1 < nblk)
+      TRY(zgemm(h->st, 0, 1, L, kc, bc, 1.0, 0.0, dst + c0, h->ldN, h->sU, h->sZ + c0, h->ldN, sV, c > 0 ? 1.0 : 0.0,
+                h->Tm, ldk, sA, T, 0, &h->err, 0, 0, &bn));
+  }
+  return 0;
 }
 
 int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
@@ -458,13 +555,23 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
   }
   for (int pass = 0; pass < 2; ++pass) {
     if (pass == 0 && lr == 0) continue;     // no row zeroed: U is orthonormal, pass 1 has R = I
+    if (pass == 0 && lr > 0 && h->struct_chol && h->lr_kdev && 4LL * lr <= h->N) {
+      // pass 1 on the structure of G = I - V^dag V (k0 <= lr << N): no dense Gram / factorisation / TRMM
+      Phase p(&h->prof, h->st, TRAJ_PH_CHOL);
+      TRY(structured_pass1(h, src, dst, lr));
+      std::swap(src, dst);
+      continue;
+    }
     {
       Phase p(&h->prof, h->st, TRAJ_PH_GRAM);
       if (pass == 0 && lr > 0) {
         // G = U'^dag U' = I - V^dag V (upper tiles): 4 N^2 k0 instead of 4 L N^2 flops
+        // (lr = the rows' capacity; their count k0 is read on the device -- rows past it are zero)
+        DevBounds db;
+        db.k = h->lr_kdev;
         TRY(set_identity(h->st, h->G, h->ldN, h->sG, h->N, h->T, &h->err));
         TRY(zgemm(h->st, 1, 0, h->N, h->N, lr, -1.0, 0.0, h->US, h->ldN, h->sUS, h->US, h->ldN, h->sUS, 1.0, h->G,
-                  h->ldN, h->sG, h->T, TRAJ_C_UPPER_F, &h->err));
+                  h->ldN, h->sG, h->T, TRAJ_C_UPPER_F, &h->err, 0, 0, &db));
       } else if (h->planar_cqr) {
         // G = U^dag U = (P1 + Q2) + i (P3 - P1 + Q2): P1 = Ur^T Ur, Q2 = Ui^T Ui, P3 = (Ur - Ui)^T (Ur + Ui),
         // A triple = planes 0..2, B triple = planes 3..5
@@ -480,17 +587,16 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
     }
     {
       Phase p(&h->prof, h->st, TRAJ_PH_CHOL);
-      bool full = pass == 0 || h->full_cqr2;
+      const bool full = pass == 0 || h->full_cqr2;
       if (!full) {
+        // second pass: G2 = I + E; the first-order factor unless N max|E|^2 >= 1e-18 for some
+        // trajectory -- decided on the device (no host round trip): the first-order X is written,
+        // then the full factorisation, gated on that decision, overwrites it when needed
         TRY(gram_deviation(h->st, h->G, h->ldN, h->sG, h->N, h->T, h->gdev, &h->err));
-        CK(cudaMemcpyAsync(h->h_dev, h->gdev, h->T * 8, cudaMemcpyDeviceToHost, h->st));
-        CK(cudaStreamSynchronize(h->st));
-        const double thr = 1e-9 / sqrt((double)h->N);
-        for (int t = 0; t < h->T; ++t) {
-          const double m = h->h_dev[t];
-          if (m > thr) full = true;           // NaN (failed trajectory) does not force the fallback
-        }
-        if (full) ++h->cqr2_fallbacks;
+        TRY(cqr2_decide(h->st, h->gdev, h->T, 1e-9 / sqrt((double)h->N), h->gate, h->fb_dev, &h->err));
+        TRY(first_order_inverse(h->st, h->G, h->ldN, h->sG, h->X, h->ldN, h->sG, h->N, h->T, &h->err));
+        TRY(chol_inverse(h->st, h->N, h->G, h->ldN, h->sG, h->X, h->ldN, h->sG, h->T, h->chol_scratch,
+                         h->failed_dev, &h->err, nullptr, nullptr, h->gate));
       }
       if (full && h->chol_overlap && h->st_hi && h->N > 64) {
         // fork: factorise on st_hi; as each left-edge block X[0:h, 0:h] is queued, st_lo runs the
@@ -564,8 +670,6 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
       if (full) {
         TRY(chol_inverse(h->st, h->N, h->G, h->ldN, h->sG, h->X, h->ldN, h->sG, h->T, h->chol_scratch,
                          h->failed_dev, &h->err));
-      } else {
-        TRY(first_order_inverse(h->st, h->G, h->ldN, h->sG, h->X, h->ldN, h->sG, h->N, h->T, &h->err));
       }
     }
     {
@@ -653,22 +757,24 @@ int lowrank_orthonormalize(traj_ctx* h, cplx* U, int k) {
 int projective(traj_ctx* h, cplx* U) {
   Phase p(&h->prof, h->st, TRAJ_PH_PROJECT);
   const int T = h->T, cap = h->cap;
-  TRY(compact(h->st, h->flags, h->L, T, h->S, cap, h->count, &h->err));
-  CK(cudaMemcpyAsync(h->h_small, h->count, T * 4, cudaMemcpyDeviceToHost, h->st));
-  CK(cudaStreamSynchronize(h->st));
+  // click counts on the host from the same counter-based draws the device makes (click_draw):
+  // they size the launches, so no count is read back from the device (traj_step stays async)
+  host_click_counts(h->L, T, h->step, h->cfg.traj_base, h->cfg.seed, h->gamma.data(), h->cfg.dt, h->hcount.data());
   int maxc = 0;
   for (int t = 0; t < T; ++t) {
-    h->last_nS[t] = h->h_small[t];
+    h->last_nS[t] = h->hcount[t];
     h->last_n1[t] = 0;
-    if (h->h_small[t] > cap)
-      return fail(h, TRAJ_ENUMERIC, "click list overflow: " + std::to_string(h->h_small[t]) + " > capacity " +
+    if (h->hcount[t] > cap)
+      return fail(h, TRAJ_ENUMERIC, "click list overflow: " + std::to_string(h->hcount[t]) + " > capacity " +
                                         std::to_string(cap));
-    maxc = std::max(maxc, h->h_small[t]);
+    maxc = std::max(maxc, h->hcount[t]);
   }
+  h->k1_dev = false;
   if (maxc == 0) {            // no click: U = K U is orthonormal, pass 1 of CQR2 has R = I
     if (h->lowrank_gram) h->lr_k0 = 0;
     return 0;
   }
+  TRY(compact(h->st, h->flags, h->L, T, h->S, cap, h->count, &h->err));
   TRY(gather_rows(h->st, U, h->ldN, h->sU, h->S, cap, h->count, maxc, T, h->US, h->ldN, h->sUS, h->N, &h->err));
   // C_SS = U_S U_S^dag (all trajectories padded to maxc rows; rows beyond a trajectory's
   // count are never read by the sampler)
@@ -677,44 +783,51 @@ int projective(traj_ctx* h, cplx* U) {
   TRY(sample_outcomes(h->st, h->D0, h->Dw, h->ldcap, h->sD, h->S, cap, h->count, maxc, T, h->step,
                       h->cfg.traj_base, h->cfg.seed, h->occ, h->Linv, h->DLinv, h->Ybuf, h->Zbuf, h->ldcap, h->pos1,
                       h->S1, h->S0, h->k1, h->k0, &h->err));
-  CK(cudaMemcpyAsync(h->h_small, h->k1, T * 4, cudaMemcpyDeviceToHost, h->st));
-  CK(cudaMemcpyAsync(h->h_small + T, h->k0, T * 4, cudaMemcpyDeviceToHost, h->st));
-  CK(cudaStreamSynchronize(h->st));
-  // rank-k update of every trajectory at once, padded to k1max (identity block in C_{S1S1},
-  // zero rows of U_{S1}: the padded columns of W and Tm vanish)
-  int k1max = 0, k0max = 0;
-  for (int t = 0; t < T; ++t) {
-    h->last_n1[t] = h->h_small[t];
-    k1max = std::max(k1max, h->h_small[t]);
-    k0max = std::max(k0max, h->h_small[T + t]);
+  h->k1_dev = true;
+  // The occupied / empty counts k1[t], k0[t] stay on the device.  Every launch below is sized by
+  // the click capacity maxc and reads them there (zgemm.h DevBounds: output tiles past k1 exit,
+  // reduction k-blocks past k1 / k0 are skipped); the padded rows / columns are zeros (identity
+  // block in C_{S1 S1}, zero rows of U_{S1}), so the rank-k update is the exact rank-k1 one.
+  int k0max = maxc;
+  if (h->lowrank_orth) {      // the NEXT-1 low-rank orthonormaliser sizes its k0 x k0 iteration on the host
+    CK(cudaMemcpyAsync(h->h_small, h->k0, T * 4, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    k0max = 0;
+    for (int t = 0; t < T; ++t) k0max = std::max(k0max, h->h_small[t]);
   }
   const long long sX = (long long)cap * h->ldcap, sW = (long long)h->N * h->ldcap, sT = (long long)h->L * h->ldcap;
-  if (k1max > 0) {
-    TRY(gather_sub_batched(h->st, h->D0, h->ldcap, h->sD, h->pos1, cap, h->k1, k1max, T, h->D11, h->ldcap, sX,
+  {
+    TRY(gather_sub_batched(h->st, h->D0, h->ldcap, h->sD, h->pos1, cap, h->k1, maxc, T, h->D11, h->ldcap, sX,
                            &h->err));
-    // R^dag R = C_{S1 S1},  X11 = R^-1
-    TRY(chol_inverse(h->st, k1max, h->D11, h->ldcap, sX, h->X11, h->ldcap, sX, T, h->chol_scratch_small,
+    // R^dag R = C_{S1 S1} (identity past k1),  X11 = R^-1
+    TRY(chol_inverse(h->st, maxc, h->D11, h->ldcap, sX, h->X11, h->ldcap, sX, T, h->chol_scratch_small,
                      h->failed_dev, &h->err));
     // U_{S1} rows (zero beyond k1[t]) -> US
-    TRY(gather_rows(h->st, U, h->ldN, h->sU, h->S1, cap, h->k1, k1max, T, h->US, h->ldN, h->sUS, h->N, &h->err, 0,
+    TRY(gather_rows(h->st, U, h->ldN, h->sU, h->S1, cap, h->k1, maxc, T, h->US, h->ldN, h->sUS, h->N, &h->err, 0,
                     1));
+    DevBounds b1;
+    b1.n = h->k1;
+    b1.k = h->k1;
     // W = U_{S1}^dag R^-1   (N x k1)
-    TRY(zgemm(h->st, 1, 0, h->N, k1max, k1max, 1.0, 0.0, h->US, h->ldN, h->sUS, h->X11, h->ldcap, sX, 0.0, h->W,
-              h->ldcap, sW, T, TRAJ_TRI_B_UPPER_F, &h->err));
+    TRY(zgemm(h->st, 1, 0, h->N, maxc, maxc, 1.0, 0.0, h->US, h->ldN, h->sUS, h->X11, h->ldcap, sX, 0.0, h->W,
+              h->ldcap, sW, T, TRAJ_TRI_B_UPPER_F, &h->err, 0, 0, &b1));
     // Tm = U W - E_{S1}   (L x k1)
-    TRY(skinny_gemm(h, 0, h->L, k1max, h->N, U, h->ldN, h->sU, h->W, h->ldcap, sW, h->Tm, sT));
-    TRY(sub_identity_batched(h->st, h->Tm, h->ldcap, sT, h->S1, cap, h->k1, k1max, T, &h->err));
-    // U <- U - Tm W^dag
-    TRY(zgemm(h->st, 0, 1, h->L, h->N, k1max, -1.0, 0.0, h->Tm, h->ldcap, sT, h->W, h->ldcap, sW, 1.0, U, h->ldN,
-              h->sU, T, 0, &h->err));
+    TRY(skinny_gemm(h, 0, h->L, maxc, h->N, U, h->ldN, h->sU, h->W, h->ldcap, sW, h->Tm, sT, h->k1));
+    TRY(sub_identity_batched(h->st, h->Tm, h->ldcap, sT, h->S1, cap, h->k1, maxc, T, &h->err));
+    // U <- U - Tm W^dag  (reduction over the k1 columns)
+    DevBounds bk;
+    bk.k = h->k1;
+    TRY(zgemm(h->st, 0, 1, h->L, h->N, maxc, -1.0, 0.0, h->Tm, h->ldcap, sT, h->W, h->ldcap, sW, 1.0, U, h->ldN,
+              h->sU, T, 0, &h->err, 0, 0, &bk));
   }
   // U is orthonormal here (K unitary, the rank-k update exact), so after zeroing rows S0 the
   // first CholeskyQR Gram is I - V^dag V with V the k0 zeroed rows: keep V (zero-padded).
-  if (h->lowrank_gram) {
-    if (k0max > 0)
-      TRY(gather_rows(h->st, U, h->ldN, h->sU, h->S0, cap, h->k0, k0max, T, h->US, h->ldN, h->sUS, h->N, &h->err, 0,
-                      1));
+  if (h->lowrank_gram && k0max > 0) {
+    TRY(gather_rows(h->st, U, h->ldN, h->sU, h->S0, cap, h->k0, k0max, T, h->US, h->ldN, h->sUS, h->N, &h->err, 0, 1));
     h->lr_k0 = k0max;
+    h->lr_kdev = h->k0;
+  } else if (h->lowrank_gram) {
+    h->lr_k0 = 0;
   }
   if (k0max > 0) TRY(zero_rows_batched(h->st, U, h->ldN, h->sU, h->S0, cap, h->k0, k0max, T, h->N, &h->err));
   if (h->lowrank_orth && k0max > 0) {
@@ -1316,6 +1429,7 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
   }
   h->last_nS.assign(h->T, 0);
   h->last_n1.assign(h->T, 0);
+  h->hcount.assign(h->T, 0);
   auto bail = [&](int st, const std::string& m) {
     std::string msg = m;
     traj_destroy(h);
@@ -1338,6 +1452,8 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
     h->ev_onepass = !(op && op[0] == '0');
     const char* tl = getenv("TRAJ_LOWRANK_TOL");
     if (tl) h->lowrank_tol = atof(tl);
+    const char* sc = getenv("TRAJ_STRUCT_CHOL");
+    h->struct_chol = !(sc && sc[0] == '0');
     const char* sm = getenv("TRAJ_SMALL_STEP");
     const bool proj = cfg->protocol == TRAJ_PROJECTIVE;
     h->small = !h->sh && !h->banded && h->K && !(sm && sm[0] == '0') && !h->lowrank_orth &&
@@ -1621,9 +1737,19 @@ int traj_last_clicks(traj_handle h, int64_t traj, int64_t* n_clicks, int64_t* n_
   int s = check_traj(h, traj);
   if (s) return s;
   if (h->sh) {
+    if (h->sh->k1_dev && n_occupied) {   // the occupied count of the last step is on the device
+      CK(cudaMemcpyAsync(h->h_small, h->sh->k1, 4, cudaMemcpyDeviceToHost, h->st));
+      CK(cudaStreamSynchronize(h->st));
+      h->sh->last_n1 = h->h_small[0];
+    }
     if (n_clicks) *n_clicks = h->sh->last_nS;
     if (n_occupied) *n_occupied = h->sh->last_n1;
     return 0;
+  }
+  if (h->k1_dev && n_occupied) {           // general path: k1 of the last projective step (device)
+    CK(cudaMemcpyAsync(h->h_small, h->k1 + traj, 4, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    h->last_n1[traj] = h->h_small[0];
   }
   if (h->cfg.protocol == TRAJ_PROJECTIVE_EVENTS && n_occupied) {
     int32_t v = 0;
@@ -1645,9 +1771,11 @@ int traj_last_clicks(traj_handle h, int64_t traj, int64_t* n_clicks, int64_t* n_
 int traj_cqr2_fallbacks(traj_handle h, int64_t* n) {
   if (!h || !n) return TRAJ_EINVAL;
   *n = h->sh ? h->sh->cqr2_fallbacks : h->cqr2_fallbacks;
-  if (h->small) {   // the fused small-lattice step counts on the device
+  // the fused small-lattice step and the general path's device-side decision count on the device
+  const unsigned long long* dev = h->sh ? h->sh->fb_dev : (h->small ? h->small_fallbacks : h->fb_dev);
+  if (dev) {
     unsigned long long v = 0;
-    CK(cudaMemcpyAsync(h->h_dev, h->small_fallbacks, 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaMemcpyAsync(h->h_dev, dev, 8, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
     memcpy(&v, h->h_dev, 8);
     *n += (int64_t)v;

@@ -57,7 +57,19 @@ struct Args {
   cplx* C;
   long long ldc, strideC;
   int m_off, n_off;        // global row / column of this call's (0, 0): triangle and upper-tile tests
+  // device-side bounds (zgemm.h DevBounds): read once per CTA
+  const int32_t* gate;     // nullptr, or the launch does nothing unless *gate != 0
+  const int32_t* nbd;      // nullptr, or C's needed columns per batch entry: tiles at n0 >= nbd exit
+  const int32_t* kbd;      // nullptr, or the reduction extent per batch entry (k-blocks past it skipped)
+  int db_per_batch;        // 1: bounds indexed by the batch entry; 0: entry 0 for every batch entry
 };
+
+// the device-side bounds of zgemm.h DevBounds, evaluated uniformly by the whole CTA
+#define TRAJ_DEV_BOUNDS(n0)                                      \
+  if (args.gate && *args.gate == 0) return;                      \
+  const int dbz_ = args.db_per_batch ? z : 0;                    \
+  if (args.nbd && (n0) >= args.nbd[dbz_]) return;                \
+  const int Kz = args.kbd ? min(args.K, args.kbd[dbz_]) : args.K;
 
 // byte offset of complex element (r, k) in a k-contiguous tile: line r, chunk k (swizzled)
 __device__ __forceinline__ uint32_t off_kc(int r, int k) { return r * 128 + ((k ^ (r & 7)) << 4); }
@@ -86,8 +98,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int m0 = pid_m * BM, n0 = pid_n * BN;
   const int z = blockIdx.z;
   if ((args.flags & TRAJ_C_UPPER_F) && m0 + args.m_off > n0 + args.n_off + BN - 1) return;   // tile entirely below the diagonal
+  TRAJ_DEV_BOUNDS(n0)
 
-  int kb = 0, ke = args.K;
+  int kb = 0, ke = Kz;
   if (args.flags & TRAJ_TRI_A_UPPER_F) kb = max(kb, m0 + args.m_off);
   if (args.flags & TRAJ_TRI_A_LOWER_F) ke = min(ke, m0 + args.m_off + BM);
   if (args.flags & TRAJ_TRI_B_UPPER_F) ke = min(ke, n0 + args.n_off + BN);
@@ -279,7 +292,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int m0 = pid_m * BM3, n0 = pid_n * BN3;
   const int z = blockIdx.z;
   if ((args.flags & TRAJ_C_UPPER_F) && m0 + args.m_off > n0 + args.n_off + BN3 - 1) return;
-  int kb = 0, ke = args.K;
+  TRAJ_DEV_BOUNDS(n0)
+  int kb = 0, ke = Kz;
   if (args.flags & TRAJ_TRI_A_UPPER_F) kb = max(kb, m0 + args.m_off);
   if (args.flags & TRAJ_TRI_A_LOWER_F) ke = min(ke, m0 + args.m_off + BM3);
   if (args.flags & TRAJ_TRI_B_UPPER_F) ke = min(ke, n0 + args.n_off + BN3);
@@ -467,7 +481,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int m0 = pid_m * BM3, n0 = pid_n * BN3;
   const int z = blockIdx.z;
   if ((args.flags & TRAJ_C_UPPER_F) && m0 + args.m_off > n0 + args.n_off + BN3 - 1) return;
-  int kb = 0, ke = args.K;
+  TRAJ_DEV_BOUNDS(n0)
+  int kb = 0, ke = Kz;
   if (args.flags & TRAJ_TRI_A_UPPER_F) kb = max(kb, m0 + args.m_off);
   if (args.flags & TRAJ_TRI_A_LOWER_F) ke = min(ke, m0 + args.m_off + BM3);
   if (args.flags & TRAJ_TRI_B_UPPER_F) ke = min(ke, n0 + args.n_off + BN3);
@@ -731,7 +746,7 @@ void set_zgemm_algorithm(int algo) { g_algo.store(algo ? 1 : 0); }
 int zgemm(cudaStream_t st, int opA, int opB, long long M, long long N, long long K, double alpha_re,
           double alpha_im, const cplx* A, long long lda, long long strideA, const cplx* B, long long ldb,
           long long strideB, double beta, cplx* C, long long ldc, long long strideC, long long batch, int flags,
-          std::string* err, long long m_off, long long n_off) {
+          std::string* err, long long m_off, long long n_off, const DevBounds* db) {
   if (M <= 0 || N <= 0 || batch <= 0) return 0;
   if (M > (1ll << 30) || N > (1ll << 30) || K > (1ll << 30) || batch > 65535) {
     if (err) *err = "zgemm: dimension too large";
@@ -782,6 +797,10 @@ int zgemm(cudaStream_t st, int opA, int opB, long long M, long long N, long long
   args.strideC = strideC;
   args.m_off = (int)m_off;
   args.n_off = (int)n_off;
+  args.gate = db ? db->gate : nullptr;
+  args.nbd = db ? db->n : nullptr;
+  args.kbd = db ? db->k : nullptr;
+  args.db_per_batch = db ? db->per_batch : 0;
   cudaError_t e;
   if (algo == 2) {
     if (opA == 0 && opB == 0) e = launch3mw<false, false>(st, ma, mb, args, (int)batch);

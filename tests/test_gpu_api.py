@@ -88,3 +88,33 @@ def test_2d_density_correlation_is_a_domain_error(P):
     with pytest.raises(P.TrajError) as e:
         g.density_correlation(0)
     assert e.value.status == 6
+
+
+@pytest.mark.parametrize("protocol,shards", [("projective", 1), ("homodyne", 1), ("projective", 2),
+                                             ("homodyne_rk4", 1)])
+def test_traj_step_is_asynchronous(P, protocol, shards):
+    """calls are stream-ordered and asynchronous unless they return host values.
+    traj_step sizes the projective launches from the host's own counter-based click counts and
+    decides CholeskyQR2's second pass on the device, so it returns while the GPU is still busy
+    (the stream reports work pending) -- and the result is unchanged (checked against a run that
+    synchronises after every step)."""
+    import time
+    import torch
+    L = 4096
+    a = P.Trajectories(L, 1, protocol, [0.6], seed=11, shard_size=shards)
+    a.step(1)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    a.step(3)
+    host_ms = 1e3 * (time.perf_counter() - t0)
+    pending = not a.stream.query()
+    torch.cuda.synchronize()
+    assert pending, f"traj_step returned after the GPU finished ({host_ms:.2f} ms on the host)"
+    b = P.Trajectories(L, 1, protocol, [0.6], seed=11, shard_size=shards)
+    for _ in range(4):
+        b.step(1)
+        torch.cuda.synchronize()
+    assert a.last_clicks(0) == b.last_clicks(0)
+    assert np.abs(a.get_state(0).cpu().numpy() - b.get_state(0).cpu().numpy()).max() == 0.0
+    a.close()
+    b.close()
