@@ -396,8 +396,9 @@ int chol_inverse(cudaStream_t st, long long n, cplx* G, long long ldg, long long
     const char* lf = getenv("TRAJ_CHOL_LEAF");
     c.elim_leaf = !(lf && lf[0] == 'r');
   }
-  if (n > NB) {
-    // the strict lower triangle of X must read as zeros (triangular GEMM tiles cross it)
+  if (n > NB && !gate) {
+    // the strict lower triangle of X must read as zeros (triangular GEMM tiles cross it); with a
+    // gate the caller's X (the first-order factor) already is, and must stay intact when gated off
     cudaError_t e = cudaSuccess;
     if (batch == 1 || sX == n * ldx) {
       e = cudaMemset2DAsync(X, (size_t)ldx * 16, 0, (size_t)n * 16, (size_t)(n * batch), st);

@@ -34,8 +34,8 @@ struct CholHook {
 // G_b = R^dag R (upper triangle of G_b read; strict lower triangle used as scratch),
 // X_b = R^-1 (upper; strict lower set to zero).  failed[b] = 1 on a non-positive or
 // non-finite pivot.  gate (device, may be null): every kernel of the factorisation does nothing
-// unless *gate != 0 -- the CholeskyQR2 fallback decided on the device, without a host round trip
-// (X's strict lower triangle is still zeroed).
+// unless *gate != 0 -- the CholeskyQR2 fallback decided on the device, without a host round trip.
+// With a gate X is not touched when gated off, and must already be zero below its diagonal.
 int chol_inverse(cudaStream_t st, long long n, cplx* G, long long ldg, long long sG, cplx* X, long long ldx,
                  long long sX, long long batch, void* scratch, int32_t* failed, std::string* err,
                  const CholDist* dist = nullptr, const CholHook* hook = nullptr, const int32_t* gate = nullptr);

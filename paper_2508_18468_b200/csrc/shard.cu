@@ -329,6 +329,22 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
     lay.take(sh->X11, (size_t)cap * ldcap * 16);
     lay.take(sh->chol_scratch_small, chol_scratch_bytes(cap, 1));
     lay.take(sh->W, (size_t)N * ldcap * 16);
+    // structured CholeskyQR pass 1 (structchol.h): Y [cap][b], C [b][b], X blocks [N][b], W, Z [cap][ldN]
+    const char* sbv = getenv("TRAJ_STRUCT_B");
+    const int b = sbv ? std::max(16, std::min(1024, atoi(sbv) / 16 * 16)) : 128;
+    sh->sc.b = b;
+    sh->sc.N = (int)N;
+    sh->sc.T = 1;
+    sh->sc.M = sh->Dw;
+    sh->sc.ldM = ldcap;
+    sh->sc.sM = 0;
+    lay.take(sh->sc.Y, (size_t)cap * b * 16);
+    lay.take(sh->sc.C, (size_t)b * b * 16);
+    lay.take(sh->sc.Xb, (size_t)round_up(N, b) * b * 16);
+    lay.take(sh->sc.W, (size_t)cap * ldN * 16);
+    lay.take(sh->sc.Z, (size_t)cap * ldN * 16);
+    sh->sc.ldWZ = ldN;
+    lay.take(sh->sc.chol_scratch, chol_scratch_bytes(b, 1));
   }
   return lay.off + 256;
 }
@@ -411,6 +427,8 @@ int shard_init(ShardedCtx* sh, const traj_config* c, std::string* err) {
   {
     const char* lg = getenv("TRAJ_LOWRANK_GRAM");
     sh->lowrank_gram = !(lg && lg[0] == '0');
+    const char* scv = getenv("TRAJ_STRUCT_CHOL");
+    sh->struct_chol = !(scv && scv[0] == '0');
     const char* co = getenv("TRAJ_CHOL_OVERLAP");
     int least = 0, greatest = 0;
     sh->chol_overlap = !(co && co[0] == '0') && cudaDeviceGetStreamPriorityRange(&least, &greatest) == cudaSuccess &&
@@ -495,8 +513,21 @@ int cqr2(ShardedCtx* sh, int src_which, std::string* err) {
   int src = src_which;
   const int lr = sh->lr_k0;
   sh->lr_k0 = -1;
+  const bool structured = sh->struct_pending;
+  sh->struct_pending = false;
   for (int pass = 0; pass < 2; ++pass) {
     if (pass == 0 && lr == 0) continue;     // no row zeroed: pass 1 has R = I
+    if (pass == 0 && lr > 0 && structured) {
+      // factor I - V^dag V from the replicated V (no collective), solve on each shard's rows
+      Phase p(sh->prof, sh->st, TRAJ_PH_CHOL);
+      sh->sc.kc = lr;
+      STRY(struct_chol_factor(sh->st, sh->sc, sh->USrecv, sh->ldN, 0, sh->k0, sh->failed_dev, err));
+      for (auto& l : sh->loc)
+        STRY(struct_chol_apply(sh->st, sh->sc, sh->Lp, l.U[src], l.U[1 - src], sh->ldN, 0, l.Tm, sh->ldcap, 0, sh->k0,
+                               err));
+      src = 1 - src;
+      continue;
+    }
     if (!(pass == 0 && lr > 0)) {            // else pass 1's G = I - V^dag V is already set, replicated
       Phase p(sh->prof, sh->st, TRAJ_PH_GRAM);
       for (auto& l : sh->loc) {
@@ -699,6 +730,11 @@ int projective(ShardedCtx* sh, int which, long long step, std::string* err) {
                sh->ldcap, 0, 1, 0, err, 0, 0, &bn));
     STRY(zgemm(st, 0, 1, total, sh->N, total, -1.0, 0.0, sh->D11, sh->ldcap, 0, sh->W, sh->ldcap, 0, 1.0, sh->USrecv,
                sh->ldN, 0, 1, 0, err, 0, 0, &bk));
+    sh->lr_k0 = total;
+    if (sh->struct_chol && 2LL * total <= sh->N) {   // pass 1 on the structure of I - V^dag V (V in USrecv)
+      sh->struct_pending = true;
+      return 0;
+    }
     STRY(set_identity(st, sh->G, sh->ldN, 0, sh->N, 1, err));
     STRY(zgemm(st, 1, 0, sh->N, sh->N, total, -1.0, 0.0, sh->USrecv, sh->ldN, 0, sh->USrecv, sh->ldN, 0, 1.0, sh->G,
                sh->ldN, 0, 1, TRAJ_C_UPPER_F, err, 0, 0, &b0));

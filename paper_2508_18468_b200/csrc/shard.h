@@ -9,6 +9,7 @@
 #include "profiler.h"
 #include "cholinv.h"
 #include "watchdog.h"
+#include "structchol.h"
 
 typedef struct ncclComm* ncclComm_t;
 typedef struct cusolverDnContext* cusolverDnHandle_t;
@@ -89,6 +90,10 @@ struct ShardedCtx {
   int32_t* gate = nullptr;                // this step's second-pass decision (device)
   bool k1_dev = false;                    // the last step's occupied count is in k1 (device)
   std::vector<int32_t> hcnt;              // per-shard click counts of the current step (host Philox)
+  // CholeskyQR pass 1 on the structure G = I - V^dag V (structchol.h; TRAJ_STRUCT_CHOL=0: dense):
+  // factored once from the gathered V (replicated, no collective), applied to each shard's rows
+  bool struct_chol = true, struct_pending = false;
+  StructChol sc;
   bool full_cqr2 = false;
   // pass 1 of CholeskyQR after a projective step: G = I - V^dag V from the zeroed rows V, formed
   // from the gathered (replicated) U_S rows -- no Gram, no allreduce (TRAJ_LOWRANK_GRAM=0: measured)

@@ -1,0 +1,93 @@
+// CholeskyQR pass 1 on the structure G = I - V^dag V (structchol.h).
+//
+// Column blocks c of width b, sequential over c (Schur complement of the leading blocks):
+//   Y = M V_c,  C_c = I - V_c^dag Y = R_c^dag R_c,  X_c = R_c^-1,  W_c = V_c X_c,  Z_c = M W_c,
+//   M <- M + Z_c Z_c^dag                                  (= M + Y C_c^-1 Y^dag)
+// so that R_cc = R_c and R_{c,d} = -Z_c^dag V_d (d > c).  The solve dst = src R^-1 then runs over
+// the column blocks with the accumulator A = sum_{d < c} dst_d Z_d^dag:
+//   dst_c = src_c X_c + A W_c,   A <- A + dst_c Z_c^dag.
+// Rows of V past k0 are zero and every reduction over them is bounded by k0 on the device (zgemm.h
+// DevBounds), so launches are sized by the host's capacity kc and the step stays asynchronous.
+#include <algorithm>
+
+#include "cholinv.h"
+#include "monitor.h"
+#include "structchol.h"
+#include "zgemm.h"
+
+namespace traj {
+
+#define SC_TRY(x)         \
+  do {                    \
+    int s_ = (x);         \
+    if (s_) return s_;    \
+  } while (0)
+
+int struct_chol_factor(cudaStream_t st, StructChol& s, const cplx* V, long long ldV, long long sV,
+                       const int32_t* k_dev, int32_t* failed, std::string* err) {
+  const int b = s.b, N = s.N, kc = s.kc, T = s.T;
+  DevBounds bk;     // reductions over the k0 rows of V
+  bk.k = k_dev;
+  // M = I
+  if (cudaMemsetAsync(s.M, 0, (size_t)T * s.sM * 16, st) != cudaSuccess) {
+    if (err) *err = "struct_chol: memset";
+    return 4;
+  }
+  SC_TRY(axpby_identity(st, s.M, s.ldM, s.sM, kc, T, 1.0, 1.0, err));
+  const int nblk = (int)ceil_div(N, b);
+  for (int c = 0; c < nblk; ++c) {
+    const int c0 = c * b, bc = std::min(b, N - c0);
+    const cplx* Vc = V + c0;
+    cplx* Xc = s.Xb + (long long)c0 * b;
+    // Y = M V_c (kc x bc);  C = I - V_c^dag Y (upper);  X_c = chol_inv(C)
+    SC_TRY(zgemm(st, 0, 0, kc, bc, kc, 1.0, 0.0, s.M, s.ldM, s.sM, Vc, ldV, sV, 0.0, s.Y, b, s.sY, T, 0, err, 0, 0,
+                 &bk));
+    SC_TRY(set_identity(st, s.C, b, s.sC, bc, T, err));
+    SC_TRY(zgemm(st, 1, 0, bc, bc, kc, -1.0, 0.0, Vc, ldV, sV, s.Y, b, s.sY, 1.0, s.C, b, s.sC, T, TRAJ_C_UPPER_F, err,
+                 0, 0, &bk));
+    SC_TRY(chol_inverse(st, bc, s.C, b, s.sC, Xc, b, s.sXb, T, s.chol_scratch, failed, err));
+    // W_c = V_c X_c,  Z_c = M W_c  (the block's columns of W, Z)
+    SC_TRY(zgemm(st, 0, 0, kc, bc, bc, 1.0, 0.0, Vc, ldV, sV, Xc, b, s.sXb, 0.0, s.W + c0, s.ldWZ, s.sWZ, T,
+                 TRAJ_TRI_B_UPPER_F, err));
+    SC_TRY(zgemm(st, 0, 0, kc, bc, kc, 1.0, 0.0, s.M, s.ldM, s.sM, s.W + c0, s.ldWZ, s.sWZ, 0.0, s.Z + c0, s.ldWZ,
+                 s.sWZ, T, 0, err, 0, 0, &bk));
+    // M += Z_c Z_c^dag
+    if (c + 1 < nblk)
+      SC_TRY(zgemm(st, 0, 1, kc, kc, bc, 1.0, 0.0, s.Z + c0, s.ldWZ, s.sWZ, s.Z + c0, s.ldWZ, s.sWZ, 1.0, s.M, s.ldM,
+                   s.sM, T, 0, err));
+  }
+  return 0;
+}
+
+int struct_chol_apply(cudaStream_t st, const StructChol& s, int Lr, const cplx* src, cplx* dst, long long ldU,
+                      long long sU, cplx* A, long long ldA, long long sA, const int32_t* k_dev, std::string* err) {
+  const int b = s.b, N = s.N, kc = s.kc, T = s.T;
+  DevBounds bk, bn;  // reductions over / outputs of the k0 columns of A
+  bk.k = k_dev;
+  bn.n = k_dev;
+  // dst = src blockdiag(X_c): the full blocks as one batched launch per trajectory, then the tail
+  const int nblk = (int)ceil_div(N, b), nfull = N / b;
+  for (int t = 0; t < T; ++t) {
+    if (nfull > 0)
+      SC_TRY(zgemm(st, 0, 0, Lr, b, b, 1.0, 0.0, src + t * sU, ldU, b, s.Xb + t * s.sXb, b, (long long)b * b, 0.0,
+                   dst + t * sU, ldU, b, nfull, TRAJ_TRI_B_UPPER_F, err));
+    if (nfull < nblk) {
+      const int c0 = nfull * b, bc = N - c0;
+      SC_TRY(zgemm(st, 0, 0, Lr, bc, bc, 1.0, 0.0, src + t * sU + c0, ldU, 0, s.Xb + t * s.sXb + (long long)c0 * b, b,
+                   0, 0.0, dst + t * sU + c0, ldU, 0, 1, TRAJ_TRI_B_UPPER_F, err));
+    }
+  }
+  // the sequential part: dst_c += A W_c,  A (+)= dst_c Z_c^dag
+  for (int c = 0; c < nblk; ++c) {
+    const int c0 = c * b, bc = std::min(b, N - c0);
+    if (c > 0)
+      SC_TRY(zgemm(st, 0, 0, Lr, bc, kc, 1.0, 0.0, A, ldA, sA, s.W + c0, s.ldWZ, s.sWZ, 1.0, dst + c0, ldU, sU, T, 0,
+                   err, 0, 0, &bk));
+    if (c + 1 < nblk)
+      SC_TRY(zgemm(st, 0, 1, Lr, kc, bc, 1.0, 0.0, dst + c0, ldU, sU, s.Z + c0, s.ldWZ, s.sWZ, c > 0 ? 1.0 : 0.0, A,
+                   ldA, sA, T, 0, err, 0, 0, &bn));
+  }
+  return 0;
+}
+
+}  // namespace traj

@@ -29,6 +29,7 @@
 #include "planar.h"
 #include "small_step.h"
 #include "comm_plan.h"
+#include "structchol.h"
 
 namespace traj {
 std::atomic<long long> g_kernel_launches{0};
@@ -459,73 +460,31 @@ int prod3(traj_ctx* h, int opA, long long M, long long N, long long K, const dou
                &h->err, 0, n_off);
 }
 
-// CholeskyQR pass 1 after a projective step, on the structure of its Gram: G = I - V^dag V with V
-// the k0 rows the empty outcomes zeroed (k0 << N), so every Schur complement of G is I - V^dag M V
-// for a k0 x k0 matrix M.  Column blocks c of width b (sequential over c):
-//   Y = M V_c,  C_c = I - V_c^dag Y = R_c^dag R_c,  X_c = R_c^-1,  W_c = V_c X_c,  Z_c = M W_c,
-//   M <- M + Z_c Z_c^dag                                  (the Schur update M + Y C_c^-1 Y^dag)
-// gives the Cholesky factor of G block row by block row: R_cc = R_c, R_{c,d} = -Z_c^dag V_d (d > c).
-// The triangular solve dst = src R^-1 then runs over the column blocks with an L x k0 accumulator
-//   dst_c = src_c X_c + A W_c,   A <- A + dst_c Z_c^dag      (A = sum_{d < c} dst_d Z_d^dag)
-// -- exactly the dense CholeskyQR pass (same R, same U R^-1 to rounding) in O(N k0^2 + L N k0 + L N b)
-// flops instead of O(N^3 + L N^2).  V is in US (capacity lr rows, zero past k0 -- read on the device),
-// M in Dw, A in Tm.
+// CholeskyQR pass 1 after a projective step on the structure of its Gram, G = I - V^dag V
+// (structchol.h): V = the k0 zeroed rows in US (capacity kc, zero past k0), M in Dw, A in Tm.
 int structured_pass1(traj_ctx* h, const cplx* src, cplx* dst, int kc) {
-  const int T = h->T, N = h->N, L = h->L, b = h->sb;
-  const long long ldk = h->ldcap, sM = h->sD, sV = h->sUS, sY = (long long)h->cap * b, sC = (long long)b * b;
-  const long long sXb = round_up(N, b) * b, sA = (long long)L * h->ldcap;
-  DevBounds bk;              // reductions over the k0 rows of V
-  bk.k = h->lr_kdev;
-  DevBounds bn;              // outputs with k0 columns
-  bn.n = h->lr_kdev;
-  // M = I
-  CK(cudaMemsetAsync(h->Dw, 0, (size_t)T * sM * 16, h->st));
-  TRY(axpby_identity(h->st, h->Dw, ldk, sM, kc, T, 1.0, 1.0, &h->err));
-  const int nblk = (int)ceil_div(N, b);
-  for (int c = 0; c < nblk; ++c) {
-    const int c0 = c * b, bc = std::min(b, N - c0);
-    const cplx* Vc = h->US + c0;
-    cplx* Xc = h->sX + (long long)c0 * b;
-    // Y = M V_c (kc x bc);  C = I - V_c^dag Y (upper);  X_c = chol_inv(C)
-    TRY(zgemm(h->st, 0, 0, kc, bc, kc, 1.0, 0.0, h->Dw, ldk, sM, Vc, h->ldN, sV, 0.0, h->sY, b, sY, T, 0, &h->err, 0, 0,
-              &bk));
-    TRY(set_identity(h->st, h->sC, b, sC, bc, T, &h->err));
-    TRY(zgemm(h->st, 1, 0, bc, bc, kc, -1.0, 0.0, Vc, h->ldN, sV, h->sY, b, sY, 1.0, h->sC, b, sC, T, TRAJ_C_UPPER_F,
-              &h->err, 0, 0, &bk));
-    TRY(chol_inverse(h->st, bc, h->sC, b, sC, Xc, b, sXb, T, h->s_chol_scratch, h->failed_dev, &h->err));
-    // W_c = V_c X_c,  Z_c = M W_c  (into the block's columns of sW, sZ)
-    TRY(zgemm(h->st, 0, 0, kc, bc, bc, 1.0, 0.0, Vc, h->ldN, sV, Xc, b, sXb, 0.0, h->sW + c0, h->ldN, sV, T,
-              TRAJ_TRI_B_UPPER_F, &h->err));
-    TRY(zgemm(h->st, 0, 0, kc, bc, kc, 1.0, 0.0, h->Dw, ldk, sM, h->sW + c0, h->ldN, sV, 0.0, h->sZ + c0, h->ldN, sV, T,
-              0, &h->err, 0, 0, &bk));
-    // M += Z_c Z_c^dag
-    if (c + 1 < nblk)
-      TRY(zgemm(h->st, 0, 1, kc, kc, bc, 1.0, 0.0, h->sZ + c0, h->ldN, sV, h->sZ + c0, h->ldN, sV, 1.0, h->Dw, ldk, sM,
-                T, 0, &h->err));
-  }
-  // dst = src blockdiag(X_c): the full blocks as one batched launch per trajectory, then the tail
-  const int nfull = N / b;
-  for (int t = 0; t < T; ++t) {
-    if (nfull > 0)
-      TRY(zgemm(h->st, 0, 0, L, b, b, 1.0, 0.0, src + t * h->sU, h->ldN, b, h->sX + t * sXb, b, (long long)b * b, 0.0,
-                dst + t * h->sU, h->ldN, b, nfull, TRAJ_TRI_B_UPPER_F, &h->err));
-    if (nfull < nblk) {
-      const int c0 = nfull * b, bc = N - c0;
-      TRY(zgemm(h->st, 0, 0, L, bc, bc, 1.0, 0.0, src + t * h->sU + c0, h->ldN, 0, h->sX + t * sXb + (long long)c0 * b,
-                b, 0, 0.0, dst + t * h->sU + c0, h->ldN, 0, 1, TRAJ_TRI_B_UPPER_F, &h->err));
-    }
-  }
-  // the sequential part: dst_c += A W_c, A (+)= dst_c Z_c^dag
-  for (int c = 0; c < nblk; ++c) {
-    const int c0 = c * b, bc = std::min(b, N - c0);
-    if (c > 0)
-      TRY(zgemm(h->st, 0, 0, L, bc, kc, 1.0, 0.0, h->Tm, ldk, sA, h->sW + c0, h->ldN, sV, 1.0, dst + c0, h->ldN, h->sU,
-                T, 0, &h->err, 0, 0, &bk));
-    if (c + 1 < nblk)
-      TRY(zgemm(h->st, 0, 1, L, kc, bc, 1.0, 0.0, dst + c0, h->ldN, h->sU, h->sZ + c0, h->ldN, sV, c > 0 ? 1.0 : 0.0,
-                h->Tm, ldk, sA, T, 0, &h->err, 0, 0, &bn));
-  }
-  return 0;
+  StructChol s;
+  s.b = h->sb;
+  s.N = h->N;
+  s.kc = kc;
+  s.T = h->T;
+  s.M = h->Dw;
+  s.ldM = h->ldcap;
+  s.sM = h->sD;
+  s.Y = h->sY;
+  s.sY = (long long)h->cap * h->sb;
+  s.C = h->sC;
+  s.sC = (long long)h->sb * h->sb;
+  s.Xb = h->sX;
+  s.sXb = round_up(h->N, h->sb) * h->sb;
+  s.W = h->sW;
+  s.Z = h->sZ;
+  s.ldWZ = h->ldN;
+  s.sWZ = h->sUS;
+  s.chol_scratch = h->s_chol_scratch;
+  TRY(struct_chol_factor(h->st, s, h->US, h->ldN, h->sUS, h->lr_kdev, h->failed_dev, &h->err));
+  return struct_chol_apply(h->st, s, h->L, src, dst, h->ldN, h->sU, h->Tm, h->ldcap, (long long)h->L * h->ldcap,
+                           h->lr_kdev, &h->err);
 }
 
 int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
@@ -555,7 +514,7 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
   }
   for (int pass = 0; pass < 2; ++pass) {
     if (pass == 0 && lr == 0) continue;     // no row zeroed: U is orthonormal, pass 1 has R = I
-    if (pass == 0 && lr > 0 && h->struct_chol && h->lr_kdev && 4LL * lr <= h->N) {
+    if (pass == 0 && lr > 0 && h->struct_chol && h->lr_kdev && 2LL * lr <= h->N) {
       // pass 1 on the structure of G = I - V^dag V (k0 <= lr << N): no dense Gram / factorisation / TRMM
       Phase p(&h->prof, h->st, TRAJ_PH_CHOL);
       TRY(structured_pass1(h, src, dst, lr));

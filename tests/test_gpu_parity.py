@@ -223,20 +223,49 @@ def test_projective_full_c5_invariants(P):
 
 def test_c2_full_size_homodyne_lockstep(P):
     """configs[1] at full size (1d L = 2048, N = 1024, homodyne, gamma in {0.1, 0.3, 1.0} as one
-    batch of three trajectories): the planar defaults with trajectory batching, 8 steps in lockstep
-    with the oracle; C, S(half) and n."""
+    batch of three trajectories): the planar defaults with trajectory batching, 50 steps in lockstep
+    with the oracle (>= 50-step windows); C and S(half) every 10 steps."""
     w = workloads.c2()
     gams = list(w.gammas)
-    lockstep(P, w.Lx, w.Ly, w.protocol, gams, 8, 4, [w.regions["half"]], seed=w.seed)
+    lockstep(P, w.Lx, w.Ly, w.protocol, gams, 50, 10, [w.regions["half"]], seed=w.seed)
 
 
 def test_c4_full_size_homodyne_mutual_information(P):
-    """configs[3] at full size (2d 64 x 64, N = 2048, homodyne, two gammas of the sweep): 4 steps in
-    lockstep with the oracle including I2 between the 16 x 64 strips."""
+    """configs[3] at full size (2d 64 x 64, N = 2048, homodyne, all 8 gammas of the sweep as one batch
+    of trajectories): 4 steps in lockstep with the oracle including I2 between the 16 x 64 strips."""
     w = workloads.c4()
-    gams = [w.gammas[0], w.gammas[-1]]
+    gams = list(w.gammas)
     A, B = w.regions["mi"]
     lockstep(P, w.Lx, w.Ly, w.protocol, gams, 4, 4, [A], seed=w.seed, mi=(A, B))
+
+
+@pytest.mark.parametrize("block,shards", [(128, 1), (64, 1), (64, 2)])
+def test_structured_pass1_matches_dense_factorisation(P, monkeypatch, block, shards):
+    """CholeskyQR pass 1 of a projective step on the structure of G = I - V^dag V (csrc/structchol.cu):
+    the same orthonormalised state as the dense Gram / Cholesky / TRMM pass (1e-12) and the oracle
+    (1e-10), batched trajectories with different click counts, column blocks with a ragged tail
+    (N = 350), and through the row-sharded emulation."""
+    L, steps = 700, 12
+    gams = [1.5, 0.8] if shards == 1 else [1.5]
+    monkeypatch.setenv("TRAJ_STRUCT_B", str(block))
+    a = P.Trajectories(L, 1, "projective", gams, seed=21, shard_size=shards)
+    monkeypatch.setenv("TRAJ_STRUCT_CHOL", "0")
+    b = P.Trajectories(L, 1, "projective", gams, seed=21, shard_size=shards)
+    K = lattice.propagator_lattice(L, 1, 1.0, 0.05)
+    orc = [OracleTrajectory(L, 1, "projective", g, 0.05, seed=21, traj=t, K=K) for t, g in enumerate(gams)]
+    for s in range(steps):
+        a.step(1)
+        b.step(1)
+        for t, o in enumerate(orc):
+            o.step(1)
+            assert a.last_clicks(t) == b.last_clicks(t) == (o.last_clicks[0].size, int(o.last_clicks[1].sum()))
+    for t, o in enumerate(orc):
+        Ca, Cb = a.correlation(t).cpu().numpy(), b.correlation(t).cpu().numpy()
+        assert np.abs(Ca - Cb).max() < 1e-12
+        assert np.abs(Ca - o.correlation()).max() < C_TOL
+        U = a.get_state(t).cpu().numpy()
+        assert np.abs(U.conj().T @ U - np.eye(L // 2)).max() < 1e-12
+        assert not a.failed(t)
 
 
 def test_cqr2_first_order_second_pass_matches_full(P):
