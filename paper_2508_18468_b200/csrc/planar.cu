@@ -99,7 +99,34 @@ __global__ void combine_gram_kernel(const double* __restrict__ Pl, long long ldp
   }
 }
 
+// buf[row][c - c0] (ld w) = the Gram entry (row, c) combined from the planes for row < c1, c in [c0, c1)
+// with row <= c; zeros below the diagonal
+__global__ void pack_gram_panel_kernel(const double* __restrict__ Pl, long long ldp, long long ps, int c0, int c1,
+                                       cplx* __restrict__ buf, int w) {
+  const int row = blockIdx.y;
+  for (int c = c0 + blockIdx.x * blockDim.x + threadIdx.x; c < c1; c += gridDim.x * blockDim.x) {
+    double2 v = make_double2(0.0, 0.0);
+    if (row <= c) {
+      const double* p = Pl + (long long)row * ldp;
+      const double p1 = p[c], q2 = p[ps + c], p3 = p[2 * ps + c];
+      v = make_double2(p1 + q2, p3 - p1 + q2);
+    }
+    buf[(long long)row * w + (c - c0)] = v;
+  }
+}
+
 }  // namespace
+
+int pack_gram_panel(cudaStream_t st, const double* Pl, long long ldp, long long ps, int c0, int c1, cplx* buf, int w,
+                    std::string* err) {
+  if (c1 <= c0) return 0;
+  dim3 grid((unsigned)ceil_div(c1 - c0, 256), c1);
+  pack_gram_panel_kernel<<<grid, 256, 0, st>>>(Pl, ldp, ps, c0, c1, buf, w);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && err) *err = std::string("pack_gram_panel: ") + cudaGetErrorString(e);
+  return e == cudaSuccess ? 0 : 4;
+}
 
 int split6_planes(cudaStream_t st, const cplx* U, long long ldu, long long sU, int L, int N, int T, double* Pl,
                   long long ldp, long long ps, long long ts, std::string* err) {

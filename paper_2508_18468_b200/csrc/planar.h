@@ -25,4 +25,9 @@ int split6_planes(cudaStream_t st, const cplx* U, long long ldu, long long sU, i
 int combine_gram(cudaStream_t st, const double* Pl, long long ldp, long long ps, long long ts, int n, int T, cplx* G,
                  long long ldg, long long sG, std::string* err);
 
+// the column panel [c0, c1) of the Gram, rows [0, c1), combined from the planes Pl[0..2] into the
+// contiguous buf [c1][w] (upper triangle; zeros below the diagonal) for a packed allreduce
+int pack_gram_panel(cudaStream_t st, const double* Pl, long long ldp, long long ps, int c0, int c1, cplx* buf, int w,
+                    std::string* err);
+
 }  // namespace traj

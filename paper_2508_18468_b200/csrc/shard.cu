@@ -12,6 +12,7 @@
 #include <cusolverDn.h>
 #include <math.h>
 #include <nccl.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -283,6 +284,12 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
     lay.take(sh->Gp, (size_t)3 * N * sh->ldPs * 8);
     lay.take(sh->Xp, (size_t)3 * N * sh->ldPs * 8);
   }
+  if (c->nccl_id && sh->planar) {   // packed, pipelined Gram allreduce: two panel buffers
+    const char* gp = getenv("TRAJ_GRAM_PANEL");
+    const long long pw = gp ? atoll(gp) : 1024;
+    sh->gram_pw = pw > 0 ? (int)std::min<long long>(round_up(pw, 64), round_up(N, 64)) : 0;
+    if (sh->gram_pw) lay.take(sh->gpack, (size_t)2 * N * sh->gram_pw * 16);
+  }
   if (c->nccl_id && sh->P > 1) {   // distributed Cholesky: the largest shared block, (N/2 + 128)^2
     const long long hb = (long long)sh->N / 2 + 128;
     sh->dist_scratch_bytes = (size_t)(hb * hb * 16);
@@ -438,6 +445,11 @@ int shard_init(ShardedCtx* sh, const traj_config* c, std::string* err) {
       if (sh->chol_overlap && cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess)
         sh->chol_overlap = false;
   }
+  if (sh->comm.comm && sh->gpack) {
+    SCK(cudaStreamCreateWithFlags(&sh->gst, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&sh->ev_gpacked[0], &sh->ev_gpacked[1], &sh->ev_gfree[0], &sh->ev_gfree[1], &sh->ev_gdone})
+      SCK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
   const char* ov = getenv("TRAJ_SHARD_OVERLAP");
   sh->overlap = !(ov && ov[0] == '0');
   if (sh->comm.comm && sh->overlap && sh->P > 1) {
@@ -482,6 +494,37 @@ int gather_full(ShardedCtx* sh, int which, std::string* err) {
   std::vector<void*> send;
   for (auto& l : sh->loc) send.push_back(l.U[which]);
   return sh->comm.allgather(sh->st, send.data(), sh->Ufull, (size_t)sh->Lp * sh->ldN * 16, err);
+}
+
+// NCCL mode, planar: G = sum over ranks of U_g^dag U_g by column panels [c0, c1): the panel's Gram
+// (three real products, rows [0, c1), upper tiles) on st, packed with its plane combine into a
+// contiguous buffer, all-reduced in place and unpacked into G on gst while st computes the next
+// panel -- the collective moves the upper part only (N^2/2 + N w/2 instead of N ldN entries) and runs
+// under the Gram GEMMs (SURVEY §8(e) "pipeline the Gram by column panels")
+int gram_panels(ShardedCtx* sh, int src, std::string* err) {
+  ShardLocal& l = sh->loc[0];
+  const long long psU = (long long)sh->Lp * sh->ldPs, psG = (long long)sh->N * sh->ldPs;
+  const int N = sh->N, pw = sh->gram_pw;
+  STRY(split6_planes(sh->st, l.U[src], sh->ldN, 0, sh->Lp, N, 1, l.Up6, sh->ldPs, psU, 0, err));
+  int j = 0;
+  for (int c0 = 0; c0 < N; c0 += pw, ++j) {
+    const int c1 = std::min(N, c0 + pw), w = c1 - c0, q = j & 1;
+    cplx* buf = sh->gpack + (size_t)q * N * pw;
+    STRY(dgemm(sh->st, 1, c1, w, sh->Lp, 1.0, l.Up6, sh->ldPs, psU, l.Up6 + 3 * psU + c0, sh->ldPs, psU, 0.0,
+               sh->Gp + c0, sh->ldPs, psG, 3, DG_C_UPPER, err, 0, c0));
+    if (j >= 2) SCK(cudaStreamWaitEvent(sh->st, sh->ev_gfree[q], 0));   // the buffer's last panel is unpacked
+    STRY(pack_gram_panel(sh->st, sh->Gp, sh->ldPs, psG, c0, c1, buf, w, err));
+    SCK(cudaEventRecord(sh->ev_gpacked[q], sh->st));
+    SCK(cudaStreamWaitEvent(sh->gst, sh->ev_gpacked[q], 0));
+    double* pb = reinterpret_cast<double*>(buf);
+    STRY(sh->comm.allreduce(sh->gst, &pb, pb, (size_t)c1 * w * 2, err));
+    SCK(cudaMemcpy2DAsync(sh->G + c0, (size_t)sh->ldN * 16, buf, (size_t)w * 16, (size_t)w * 16, c1,
+                          cudaMemcpyDeviceToDevice, sh->gst));
+    SCK(cudaEventRecord(sh->ev_gfree[q], sh->gst));
+  }
+  SCK(cudaEventRecord(sh->ev_gdone, sh->gst));
+  SCK(cudaStreamWaitEvent(sh->st, sh->ev_gdone, 0));
+  return 0;
 }
 
 int allreduce_gram(ShardedCtx* sh, std::string* err) {
@@ -530,6 +573,10 @@ int cqr2(ShardedCtx* sh, int src_which, std::string* err) {
     }
     if (!(pass == 0 && lr > 0)) {            // else pass 1's G = I - V^dag V is already set, replicated
       Phase p(sh->prof, sh->st, TRAJ_PH_GRAM);
+      if (sh->comm.comm && sh->gpack && sh->gst) {
+        STRY(gram_panels(sh, src, err));
+        goto gram_done;
+      }
       for (auto& l : sh->loc) {
         if (sh->planar) {
           // local G_g = U_g^dag U_g as three real products (planes re, im, re - im | re, im, re + im)
@@ -545,6 +592,7 @@ int cqr2(ShardedCtx* sh, int src_which, std::string* err) {
       }
       STRY(allreduce_gram(sh, err));
     }
+  gram_done:
     {
       Phase p(sh->prof, sh->st, TRAJ_PH_CHOL);
       const bool full = pass == 0 || sh->full_cqr2;
@@ -689,13 +737,33 @@ int projective(ShardedCtx* sh, int which, long long step, std::string* err) {
     STRY(sh->comm.allgather(st, a.data(), sh->cntrecv, 4, err));
     STRY(sum_i32(st, sh->cntrecv, P, sh->count, err));
   }
-  // replicated: C_SS, sampling, W
-  STRY(zgemm(st, 0, 1, total, total, sh->N, 1.0, 0.0, sh->US, sh->ldN, 0, sh->US, sh->ldN, 0, 0.0, sh->D0, sh->ldcap,
-             0, 1, 0, err));
+  // C_SS = U_S U_S^dag: with an NCCL communicator each rank computes a slice of its rows and one
+  // in-place allgather replicates it (the sampling and W below stay replicated); else replicated
+  const int sr = (total + P - 1) / P;
+  const char* css = getenv("TRAJ_SHARD_CSS_SPLIT");   // =0: replicated C_SS
+  if (sh->comm.comm && P > 1 && (long long)sr * P <= sh->cap && !(css && css[0] == '0')) {
+    const int me = sh->comm.rank0, r0 = me * sr, nr = std::max(0, std::min(sr, total - r0));
+    if (nr > 0)
+      STRY(zgemm(st, 0, 1, nr, total, sh->N, 1.0, 0.0, sh->US + (size_t)r0 * sh->ldN, sh->ldN, 0, sh->US, sh->ldN, 0,
+                 0.0, sh->D0 + (size_t)r0 * sh->ldcap, sh->ldcap, 0, 1, 0, err));
+    void* mine = sh->D0 + (size_t)r0 * sh->ldcap;
+    STRY(sh->comm.allgather(st, &mine, sh->D0, (size_t)sr * sh->ldcap * 16, err));
+  } else {
+    STRY(zgemm(st, 0, 1, total, total, sh->N, 1.0, 0.0, sh->US, sh->ldN, 0, sh->US, sh->ldN, 0, 0.0, sh->D0,
+               sh->ldcap, 0, 1, 0, err));
+  }
   STRY(sample_outcomes(st, sh->D0, sh->Dw, sh->ldcap, 0, sh->S, sh->cap, sh->count, total, 1, step, sh->traj_base,
                        sh->seed, sh->occ, sh->Linv, sh->DLinv, sh->Ybuf, sh->Zbuf, sh->ldcap, sh->pos1, sh->S1, sh->S0,
                        sh->k1, sh->k0, err, sh->pos0));
   sh->k1_dev = true;
+  if (getenv("TRAJ_DEBUG_SHARD")) {   // debugging aid: the device counts of this step
+    int32_t v[4] = {0, 0, 0, 0};
+    cudaMemcpyAsync(v, sh->count, 4, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(v + 1, sh->k1, 4, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(v + 2, sh->k0, 4, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "[shard] step %lld: host total %d, device count %d, k1 %d, k0 %d\n", step, total, v[0], v[1], v[2]);
+  }
   // k1, k0 stay on the device: launches sized by the click count `total`, bounded there (zgemm.h
   // DevBounds; identity past k1 in C_{S1 S1}, zero rows past k1 / k0 in the gathered blocks)
   DevBounds b1, bk, b0;
@@ -1030,6 +1098,12 @@ void shard_destroy(ShardedCtx* sh) {
     cudaStreamDestroy(sh->cst);
   }
   if (sh->ev_start) cudaEventDestroy(sh->ev_start);
+  if (sh->gst) {
+    cudaStreamSynchronize(sh->gst);
+    cudaStreamDestroy(sh->gst);
+  }
+  for (cudaEvent_t e : {sh->ev_gpacked[0], sh->ev_gpacked[1], sh->ev_gfree[0], sh->ev_gfree[1], sh->ev_gdone})
+    if (e) cudaEventDestroy(e);
   for (cudaStream_t q : {sh->st_hi, sh->st_lo})
     if (q) {
       cudaStreamSynchronize(q);

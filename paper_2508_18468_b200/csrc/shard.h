@@ -93,6 +93,12 @@ struct ShardedCtx {
   // CholeskyQR pass 1 on the structure G = I - V^dag V (structchol.h; TRAJ_STRUCT_CHOL=0: dense):
   // factored once from the gathered V (replicated, no collective), applied to each shard's rows
   bool struct_chol = true, struct_pending = false;
+  // NCCL mode, planar Gram: column panels of width gram_pw, each packed (upper part, rows [0, c1))
+  // and all-reduced on gst while the next panel's Gram runs (TRAJ_GRAM_PANEL=0: one full allreduce)
+  int gram_pw = 0;
+  cplx* gpack = nullptr;                  // [2][N][gram_pw]
+  cudaStream_t gst = nullptr;
+  cudaEvent_t ev_gpacked[2] = {nullptr, nullptr}, ev_gfree[2] = {nullptr, nullptr}, ev_gdone = nullptr;
   StructChol sc;
   bool full_cqr2 = false;
   // pass 1 of CholeskyQR after a projective step: G = I - V^dag V from the zeroed rows V, formed

@@ -26,10 +26,16 @@ namespace traj {
 int struct_chol_factor(cudaStream_t st, StructChol& s, const cplx* V, long long ldV, long long sV,
                        const int32_t* k_dev, int32_t* failed, std::string* err) {
   const int b = s.b, N = s.N, kc = s.kc, T = s.T;
-  DevBounds bk;     // reductions over the k0 rows of V
+  DevBounds bk;     // reductions over the k0 rows of V, outputs with k0 rows (the rest is zero)
   bk.k = k_dev;
+  bk.m = k_dev;
+  DevBounds bm;     // outputs with k0 rows
+  bm.m = k_dev;
+  DevBounds bmn;    // k0 x k0 outputs
+  bmn.m = k_dev;
+  bmn.n = k_dev;
   // M = I
-  if (cudaMemsetAsync(s.M, 0, (size_t)T * s.sM * 16, st) != cudaSuccess) {
+  if (cudaMemsetAsync(s.M, 0, (size_t)((T - 1) * s.sM + (long long)kc * s.ldM) * 16, st) != cudaSuccess) {
     if (err) *err = "struct_chol: memset";
     return 4;
   }
@@ -43,18 +49,20 @@ int struct_chol_factor(cudaStream_t st, StructChol& s, const cplx* V, long long 
     SC_TRY(zgemm(st, 0, 0, kc, bc, kc, 1.0, 0.0, s.M, s.ldM, s.sM, Vc, ldV, sV, 0.0, s.Y, b, s.sY, T, 0, err, 0, 0,
                  &bk));
     SC_TRY(set_identity(st, s.C, b, s.sC, bc, T, err));
+    DevBounds bkk;  // the b x b C: reduction over k0 only
+    bkk.k = k_dev;
     SC_TRY(zgemm(st, 1, 0, bc, bc, kc, -1.0, 0.0, Vc, ldV, sV, s.Y, b, s.sY, 1.0, s.C, b, s.sC, T, TRAJ_C_UPPER_F, err,
-                 0, 0, &bk));
+                 0, 0, &bkk));
     SC_TRY(chol_inverse(st, bc, s.C, b, s.sC, Xc, b, s.sXb, T, s.chol_scratch, failed, err));
     // W_c = V_c X_c,  Z_c = M W_c  (the block's columns of W, Z)
     SC_TRY(zgemm(st, 0, 0, kc, bc, bc, 1.0, 0.0, Vc, ldV, sV, Xc, b, s.sXb, 0.0, s.W + c0, s.ldWZ, s.sWZ, T,
-                 TRAJ_TRI_B_UPPER_F, err));
+                 TRAJ_TRI_B_UPPER_F, err, 0, 0, &bm));
     SC_TRY(zgemm(st, 0, 0, kc, bc, kc, 1.0, 0.0, s.M, s.ldM, s.sM, s.W + c0, s.ldWZ, s.sWZ, 0.0, s.Z + c0, s.ldWZ,
                  s.sWZ, T, 0, err, 0, 0, &bk));
     // M += Z_c Z_c^dag
     if (c + 1 < nblk)
       SC_TRY(zgemm(st, 0, 1, kc, kc, bc, 1.0, 0.0, s.Z + c0, s.ldWZ, s.sWZ, s.Z + c0, s.ldWZ, s.sWZ, 1.0, s.M, s.ldM,
-                   s.sM, T, 0, err));
+                   s.sM, T, 0, err, 0, 0, &bmn));
   }
   return 0;
 }

@@ -59,6 +59,7 @@ struct Args {
   int m_off, n_off;        // global row / column of this call's (0, 0): triangle and upper-tile tests
   // device-side bounds (zgemm.h DevBounds): read once per CTA
   const int32_t* gate;     // nullptr, or the launch does nothing unless *gate != 0
+  const int32_t* mbd;      // nullptr, or C's needed rows per batch entry: tiles at m0 >= mbd exit
   const int32_t* nbd;      // nullptr, or C's needed columns per batch entry: tiles at n0 >= nbd exit
   const int32_t* kbd;      // nullptr, or the reduction extent per batch entry (k-blocks past it skipped)
   int db_per_batch;        // 1: bounds indexed by the batch entry; 0: entry 0 for every batch entry
@@ -69,6 +70,7 @@ struct Args {
   if (args.gate && *args.gate == 0) return;                      \
   const int dbz_ = args.db_per_batch ? z : 0;                    \
   if (args.nbd && (n0) >= args.nbd[dbz_]) return;                \
+  if (args.mbd && m0 >= args.mbd[dbz_]) return;                  \
   const int Kz = args.kbd ? min(args.K, args.kbd[dbz_]) : args.K;
 
 // byte offset of complex element (r, k) in a k-contiguous tile: line r, chunk k (swizzled)
@@ -799,6 +801,7 @@ int zgemm(cudaStream_t st, int opA, int opB, long long M, long long N, long long
   args.n_off = (int)n_off;
   args.gate = db ? db->gate : nullptr;
   args.nbd = db ? db->n : nullptr;
+  args.mbd = db ? db->m : nullptr;
   args.kbd = db ? db->k : nullptr;
   args.db_per_batch = db ? db->per_batch : 0;
   cudaError_t e;

@@ -17,13 +17,14 @@ enum {
 // needs no host round trip for a data-dependent size (the projective click counts) or decision (the
 // CholeskyQR2 fallback).  Every pointer may be null.
 //   gate: the launch does nothing unless *gate != 0;
-//   n:    columns of C needed: output tiles starting at or past n exit (columns of a straddling
-//         tile past n are written with values the caller must not use);
+//   m, n: rows / columns of C needed: output tiles starting at or past them exit (the rest of a
+//         straddling tile is written with values the caller must not use);
 //   k:    the reduction extent: k-blocks starting at or past k are skipped -- the operands must hold
 //         zeros in the rest of the last block (zero-padded rows / columns), so the sum is exact.
 //   per_batch: n[b], k[b] for batch entry b (else n[0], k[0] for every entry).
 struct DevBounds {
   const int32_t* gate = nullptr;
+  const int32_t* m = nullptr;
   const int32_t* n = nullptr;
   const int32_t* k = nullptr;
   int per_batch = 1;

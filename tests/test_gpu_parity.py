@@ -438,17 +438,25 @@ def test_planar_propagator_matches_interleaved(P, Lx, Ly, protocol, gams, monkey
     b.close()
 
 
-def test_row_sharded_nccl_single_rank(P):
+@pytest.mark.parametrize("planar", [False, True])
+def test_row_sharded_nccl_single_rank(P, planar, monkeypatch):
     """The NCCL code path of the sharded step with a one-rank communicator (the only
-    configuration one GPU allows): same result as the unsharded handle."""
+    configuration one GPU allows): same result as the unsharded handle.  planar: the planar
+    Gram with its packed, pipelined allreduce by 64-column panels (ragged last panel)."""
+    L = 232 if planar else 128
+    if planar:
+        monkeypatch.setenv("TRAJ_PLANAR_MIN_N", "0")
+        monkeypatch.setenv("TRAJ_GRAM_PANEL", "64")
     uid = P.traj_nccl_unique_id()
-    a = P.Trajectories(128, 1, "projective", [3.0], seed=5, shard_size=1, shard_rank=0, nccl_id=uid)
-    b = P.Trajectories(128, 1, "projective", [3.0], seed=5)
+    a = P.Trajectories(L, 1, "projective", [3.0], seed=5, shard_size=1, shard_rank=0, nccl_id=uid)
+    b = P.Trajectories(L, 1, "projective", [3.0], seed=5)
     a.step(10)
     b.step(10)
     assert a.last_clicks(0) == b.last_clicks(0)
     assert np.abs(a.correlation(0).cpu().numpy() - b.correlation(0).cpu().numpy()).max() < 1e-12
     assert abs(a.entropy(np.arange(64))[0] - b.entropy(np.arange(64))[0]) < 1e-10
+    U = a.get_state(0).cpu().numpy()
+    assert np.abs(U.conj().T @ U - np.eye(L // 2)).max() < 1e-12
     a.close()
 
 
