@@ -386,7 +386,12 @@ def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P):
     trmm_name = ("dgemm_dmma_kernel<0> x3 (planar 3M against X's planes, triangle skipped) + split/combine"
                  if planar_cqr else f"{kn[0]} triangular")
     n_gram = 1 if (w.protocol == "projective" and os.environ.get("TRAJ_LOWRANK_GRAM", "1") != "0") else 2
-    n_trmm = 1 if os.environ.get("TRAJ_CHOL_OVERLAP", "1") != "0" else 2
+    nS0 = sum(c[0] for c in tr_clicks) / max(1, tpg)
+    struct0 = (w.protocol == "projective" and args.orthonormalizer == "cqr2" and 0 < 2 * nS0 <= w.N
+               and os.environ.get("TRAJ_STRUCT_CHOL", "1") != "0")
+    # the TRMMs timed in the trmm phase: pass 2's; pass 1's too unless it ran inside the chol phase
+    # (overlapped with the factorisation, or the structured pass 1)
+    n_trmm = 1 if (struct0 or os.environ.get("TRAJ_CHOL_OVERLAP", "1") != "0") else 2
     a_ku = 0.75 if (planar or algo == "3m") else 1.0       # DMMA flops per 8mnk flop
     a_cqr = 0.75 if (planar_cqr or algo == "3m") else 1.0
     kern = {"propagate": (8.0 * rows * w.L * w.N * tpg, a_ku, f"{ku_name}: U <- K U (8 L^2 N flops per step)"),
@@ -448,21 +453,39 @@ def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P):
                         "kernel-quality figure")
     # executed DMMA flops of the whole step (model of what the kernels issue), over the step time
     k1 = k1_sum / max(1, tpg)
+    nS = k_sum / max(1, tpg)
+    k0 = nS - k1
+    a3 = 0.75 if algo == "3m" else 1.0
+    structured = (w.protocol == "projective" and args.orthonormalizer == "cqr2" and k0 > 0
+                  and os.environ.get("TRAJ_STRUCT_CHOL", "1") != "0" and 2 * nS <= w.N)
+    sb = int(os.environ.get("TRAJ_STRUCT_B", "128"))
     step8 = {"propagate": (8.0 * rows * w.L * w.N if args.propagator == "dense" else 0.0, a_ku),
              "gram": (n_gram * 4.0 * rows * w.N * w.N, a_cqr),
-             "trmm": (2 * 4.0 * rows * w.N * w.N, a_cqr),
-             "chol": ((8.0 / 3.0) * w.N ** 3, 0.75 if algo == "3m" else 1.0),
-             "project": (16.0 * rows * w.N * k1 if w.protocol == "projective" else 0.0, 0.75 if algo == "3m" else 1.0)}
+             "project": (16.0 * rows * w.N * k1 + 8.0 * nS * nS * w.N if w.protocol == "projective" else 0.0, a3)}
+    if structured:
+        # pass 1 on the structure of I - V^dag V (csrc/structchol.cu): the factorisation
+        # 24 k0^2 N + 8 b k0 N + (8/3) b^2 N, the solve 16 L N k0 + 4 L N b; pass 2 measured Gram + TRMM
+        step8["chol"] = (24.0 * k0 * k0 * w.N + 8.0 * sb * k0 * w.N + (8.0 / 3.0) * sb * sb * w.N
+                         + 16.0 * rows * w.N * k0 + 4.0 * rows * w.N * sb, a3)
+        step8["trmm"] = (4.0 * rows * w.N * w.N, a_cqr)
+    else:
+        step8["chol"] = ((8.0 / 3.0) * w.N ** 3, a3)
+        step8["trmm"] = (2 * 4.0 * rows * w.N * w.N, a_cqr)
     executed = None
     if not fused and not (args.orthonormalizer == "lowrank" and w.protocol == "projective" and not shard) \
             and w.protocol in ("projective", "homodyne"):
         fl = sum(f * a for f, a in step8.values()) * tpg
         t = ms / args.steps / 1e3
         executed = {"tflops": fl / t / 1e12, "frac": fl / t / 1e12 / FP64_PEAK_TFLOPS, "flops_per_step": fl,
-                    "model": "per step (and per shard): K U 8 rows L N, one chol_inverse (8/3) N^3 (the second "
-                             "CholeskyQR pass takes the first-order factor), the measured Gram(s) 4 rows N^2, two "
-                             "TRMMs 4 rows N^2, the projective rank-k1 update 16 rows N k1; each x 0.75 for the 3M "
-                             "schemes (the DMMA flops they issue)",
+                    "model": ("per step (and per shard, rows = L/P): K U 8 rows L N; the measured Gram(s) 4 rows N^2; "
+                              "the projective update 16 rows N k1 + C_SS 8 |S|^2 N; " +
+                              ("CholeskyQR pass 1 on the structure of I - V^dag V (k0 = |S| - k1 zeroed rows, "
+                               f"column blocks b = {sb}): 24 k0^2 N + 8 b k0 N + (8/3) b^2 N + 16 rows N k0 + "
+                               "4 rows N b, pass 2's TRMM 4 rows N^2" if structured else
+                               "one chol_inverse (8/3) N^3 (the second CholeskyQR pass takes the first-order "
+                               "factor), two TRMMs 4 rows N^2") +
+                              "; each x 0.75 for the 3M schemes (the DMMA flops they issue)"),
+                    "structured_pass1": structured, "k1": k1, "k0": k0,
                     "per_phase_8mnk": {k: v[0] * tpg for k, v in step8.items()}}
     # same-shape library denominators (tools/library_compare.py, committed under profiles/):
     # cublasZgemm / cublasZgemm3m for K U, cuSOLVER potrf + trtri for the Cholesky inverse

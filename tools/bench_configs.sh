@@ -1,7 +1,7 @@
 #!/bin/bash
 # One bench line per BASELINE config at N = 1 (c3 and c5 in dense, banded and banded + low-rank
 # forms), appended to gpurun_out/bench_configs.jsonl.  Usage (on the GPU box): bash tools/bench_configs.sh
-out=gpurun_out/bench_configs.jsonl
+out=gpurun_out/${BENCH_CONFIGS_OUT:-bench_configs.jsonl}
 : > $out
 common="--no-cpu-baseline --no-e2e --no-observables --secondary none"
 python bench.py --config c1 --steps 200 --warmup 10 $common >> $out 2>/dev/null
