@@ -377,7 +377,13 @@ def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P):
               and w.protocol in ("projective", "homodyne")
               and (not shard or os.environ.get("TRAJ_PLANAR_CQR", "1") != "0"))
     planar_cqr = big and os.environ.get("TRAJ_PLANAR_CQR", "1") != "0" and (not shard or planar)
-    ku_name = ("dgemm_dmma_kernel x3 (planar 3M: Kr Ur, Ki Ui, (Kr+Ki)(Ur+Ui); 128x128 CTA) + split/combine passes"
+    smin = int(os.environ.get("TRAJ_STRASSEN_MIN_N", "2048"))
+    strassen = (planar and not shard and w.L % 4 == 0 and w.N >= smin
+                and os.environ.get("TRAJ_STRASSEN", "1") != "0")
+    ku_name = ("dgemm_dmma_kernel x21 (planar 3M: Kr Ur, Ki Ui, (Kr+Ki)(Ur+Ui), each by one Strassen level: seven "
+               "half-size real products; 128x128 CTA, one batch-21 launch) + operand / recombination passes"
+               if strassen else
+               "dgemm_dmma_kernel x3 (planar 3M: Kr Ur, Ki Ui, (Kr+Ki)(Ur+Ui); 128x128 CTA) + split/combine passes"
                + ("; per shard: P ring-distance K-chunk products accumulated, the U exchange under them" if shard
                   else "")
                if planar else kn[0])
@@ -392,7 +398,8 @@ def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P):
     # the TRMMs timed in the trmm phase: pass 2's; pass 1's too unless it ran inside the chol phase
     # (overlapped with the factorisation, or the structured pass 1)
     n_trmm = 1 if (struct0 or os.environ.get("TRAJ_CHOL_OVERLAP", "1") != "0") else 2
-    a_ku = 0.75 if (planar or algo == "3m") else 1.0       # DMMA flops per 8mnk flop
+    # DMMA flops per 8mnk flop: 3M 6/8; with one Strassen level 7/8 of that (21 half-size products)
+    a_ku = (0.75 * 7 / 8 if strassen else 0.75) if (planar or algo == "3m") else 1.0
     a_cqr = 0.75 if (planar_cqr or algo == "3m") else 1.0
     kern = {"propagate": (8.0 * rows * w.L * w.N * tpg, a_ku, f"{ku_name}: U <- K U (8 L^2 N flops per step)"),
             "gram": (n_gram * 4.0 * rows * w.N * w.N * tpg, a_cqr,
@@ -430,10 +437,12 @@ def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P):
     if os.path.exists(tp) and dom == "propagate" and not shard:
         try:
             tj = json.load(open(tp)).get(w.name, {})
-            traffic = tj.get("propagate_dram_bytes") if planar else tj.get("interleaved_zgemm3mw_dram_bytes")
+            traffic = (tj.get("propagate_strassen_dram_bytes") if strassen else
+                       tj.get("propagate_dram_bytes") if planar else tj.get("interleaved_zgemm3mw_dram_bytes"))
         except Exception:
             traffic = None
-    mult = ("planar 3m" if (planar and dom == "propagate") or (planar_cqr and dom in ("gram", "trmm")) else
+    mult = ("planar 3m + one Strassen level" if (strassen and dom == "propagate") else
+            "planar 3m" if (planar and dom == "propagate") or (planar_cqr and dom in ("gram", "trmm")) else
             "4m" if dom == "fused" else algo)
     roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
             "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
@@ -443,10 +452,14 @@ def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P):
                                           "the handle's stream)", "peak_source": FP64_PEAK_SOURCE,
             "complex_mult": mult,
             "flops_counted": ("executed DMMA flops: 6mnk per complex product for 3M (three real products), "
-                              "8mnk for 4M; achieved_8mnk_equiv counts the conventional 8mnk"),
-            "traffic_note": ("ncu dram bytes of the propagate phase (profiles/ncu_traffic.json: split, the "
-                             "three real 16384x8192x16384 products as one batch-3 launch, combine) vs 8.6 GB "
-                             "algorithmic") if traffic else None}
+                              "21/4 mnk with one Strassen level on each (seven half-size products per real "
+                              "product), 8mnk for 4M; achieved_8mnk_equiv counts the conventional 8mnk"),
+            "traffic_note": (("ncu dram bytes of the propagate phase (profiles/ncu_traffic.json: U's Strassen "
+                              "operands, the 21 half-size real products as one batch-21 launch, the "
+                              "recombination) vs 8.6 GB algorithmic") if strassen else
+                             ("ncu dram bytes of the propagate phase (profiles/ncu_traffic.json: split, the "
+                              "three real 16384x8192x16384 products as one batch-3 launch, combine) vs 8.6 GB "
+                              "algorithmic")) if traffic else None}
     if w.name == "c1":
         roof["note"] = ("c1 is latency-bound (SURVEY §8(d)): L = 64, one fused launch per step with one CTA per "
                         "trajectory, whose ~140 barriers and dependent pivots set the time; the fraction is not a "
@@ -582,10 +595,14 @@ def run_secondary(args, world, rank, P, steps=2, warmup=2):
     if args.propagator == "dense" and prop > 0:
         eq8 = 8.0 * rows * w.L * w.N / (prop / 1e3) / 1e12
         a = 0.75 if P.traj_get_zgemm_algorithm() == "3m" or os.environ.get("TRAJ_PLANAR_KU", "1") != "0" else 1.0
+        if (not shard and w.L % 4 == 0 and w.N >= int(os.environ.get("TRAJ_STRASSEN_MIN_N", "2048"))
+                and os.environ.get("TRAJ_STRASSEN", "1") != "0" and os.environ.get("TRAJ_PLANAR_KU", "1") != "0"):
+            a *= 7 / 8            # one Strassen level on each planar product
         out["roofline_propagate"] = {"bound": "tensor", "achieved": eq8 * a, "peak": FP64_PEAK_TFLOPS,
                                      "unit": "TFLOP/s", "frac": eq8 * a / FP64_PEAK_TFLOPS,
                                      "achieved_8mnk_equiv": eq8, "frac_8mnk_equiv": eq8 / FP64_PEAK_TFLOPS,
-                                     "flops_counted": "executed DMMA flops (6mnk for 3M)"}
+                                     "flops_counted": "executed DMMA flops (6mnk for 3M, x 7/8 with one Strassen "
+                                                      "level)"}
     return out
 
 

@@ -115,7 +115,122 @@ __global__ void pack_gram_panel_kernel(const double* __restrict__ Pl, long long 
   }
 }
 
+// One level of Strassen's algorithm on every real product of the planar 3M propagator.  With
+// A = K's plane q and B = U's plane q in 2 x 2 blocks of (L/2) x (L/2) and (L/2) x (N/2):
+//   M1 = (A11 + A22)(B11 + B22)  M2 = (A21 + A22) B11  M3 = A11 (B12 - B22)  M4 = A22 (B21 - B11)
+//   M5 = (A11 + A12) B22         M6 = (A21 - A11)(B11 + B12)             M7 = (A12 - A22)(B21 + B22)
+//   C11 = M1 + M4 - M5 + M7,  C12 = M3 + M5,  C21 = M2 + M4,  C22 = M1 - M2 + M3 + M6
+// -- seven half-size products instead of eight.  K's seven operands are formed once; U's seven per
+// step (strassen_b), the M's combined with the complex 3M recombination in one pass (strassen_c).
+
+// Ks[q][s][i][j] (s = 0..6, operand of M_{s+1}) from K's planes
+__global__ void strassen_a_kernel(const double* __restrict__ Kp, long long ldk, long long pk, int h,
+                                  double* __restrict__ Ks, long long ldks) {
+  const int q = blockIdx.z, i = blockIdx.y;
+  const double* k = Kp + q * pk;
+  double* o = Ks + (long long)q * 7 * h * ldks + (long long)i * ldks;
+  const long long bs = (long long)h * ldks;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < h; j += gridDim.x * blockDim.x) {
+    const double a11 = k[(long long)i * ldk + j], a12 = k[(long long)i * ldk + h + j];
+    const double a21 = k[(long long)(h + i) * ldk + j], a22 = k[(long long)(h + i) * ldk + h + j];
+    o[j] = a11 + a22;
+    o[bs + j] = a21 + a22;
+    o[2 * bs + j] = a11;
+    o[3 * bs + j] = a22;
+    o[4 * bs + j] = a11 + a12;
+    o[5 * bs + j] = a21 - a11;
+    o[6 * bs + j] = a12 - a22;
+  }
+}
+
+// Bc[q][s][t][i][j]: the B operands of M_{s+1} for the planes (re, im, re + im) of U[t]
+__global__ void strassen_b_kernel(const cplx* __restrict__ U, long long ldu, long long sU, int h, int nh, int T,
+                                  double* __restrict__ Bc, long long ldb) {
+  const int t = blockIdx.z, i = blockIdx.y;
+  const cplx* u = U + t * sU;
+  const long long bs = (long long)T * h * ldb;          // stride between (q, s) entries
+  double* o = Bc + (long long)t * h * ldb + (long long)i * ldb;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nh; j += gridDim.x * blockDim.x) {
+    const double2 b11 = u[(long long)i * ldu + j], b12 = u[(long long)i * ldu + nh + j];
+    const double2 b21 = u[(long long)(h + i) * ldu + j], b22 = u[(long long)(h + i) * ldu + nh + j];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double v11 = q == 0 ? b11.x : (q == 1 ? b11.y : b11.x + b11.y);
+      const double v12 = q == 0 ? b12.x : (q == 1 ? b12.y : b12.x + b12.y);
+      const double v21 = q == 0 ? b21.x : (q == 1 ? b21.y : b21.x + b21.y);
+      const double v22 = q == 0 ? b22.x : (q == 1 ? b22.y : b22.x + b22.y);
+      double* oq = o + (long long)q * 7 * bs;
+      oq[j] = v11 + v22;
+      oq[bs + j] = v11;
+      oq[2 * bs + j] = v12 - v22;
+      oq[3 * bs + j] = v21 - v11;
+      oq[4 * bs + j] = v22;
+      oq[5 * bs + j] = v11 + v12;
+      oq[6 * bs + j] = v21 + v22;
+    }
+  }
+}
+
+// U[t] from the M's: per plane C11..C22, then (P1 - P2) + i (P3 - P1 - P2)
+__global__ void strassen_c_kernel(const double* __restrict__ Mb, long long ldb, int h, int nh, int T,
+                                  cplx* __restrict__ U, long long ldu, long long sU) {
+  const int t = blockIdx.z, i = blockIdx.y;
+  const long long bs = (long long)T * h * ldb;
+  const double* m = Mb + (long long)t * h * ldb + (long long)i * ldb;
+  cplx* u = U + t * sU;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nh; j += gridDim.x * blockDim.x) {
+    double c[3][4];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double* mq = m + (long long)q * 7 * bs;
+      const double m1 = mq[j], m2 = mq[bs + j], m3 = mq[2 * bs + j], m4 = mq[3 * bs + j];
+      const double m5 = mq[4 * bs + j], m6 = mq[5 * bs + j], m7 = mq[6 * bs + j];
+      c[q][0] = m1 + m4 - m5 + m7;
+      c[q][1] = m3 + m5;
+      c[q][2] = m2 + m4;
+      c[q][3] = m1 - m2 + m3 + m6;
+    }
+    const long long off[4] = {(long long)i * ldu + j, (long long)i * ldu + nh + j, (long long)(h + i) * ldu + j,
+                              (long long)(h + i) * ldu + nh + j};
+#pragma unroll
+    for (int b = 0; b < 4; ++b) u[off[b]] = make_double2(c[0][b] - c[1][b], c[2][b] - c[0][b] - c[1][b]);
+  }
+}
+
 }  // namespace
+
+int strassen_k(cudaStream_t st, const double* Kp, long long ldk, long long pk, int L, double* Ks, long long ldks,
+               std::string* err) {
+  const int h = L / 2;
+  dim3 grid((unsigned)std::min<long long>(ceil_div(h, 256), 16), h, 3);
+  strassen_a_kernel<<<grid, 256, 0, st>>>(Kp, ldk, pk, h, Ks, ldks);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && err) *err = std::string("strassen_k: ") + cudaGetErrorString(e);
+  return e == cudaSuccess ? 0 : 4;
+}
+
+int strassen_b(cudaStream_t st, const cplx* U, long long ldu, long long sU, int L, int N, int T, double* Bc,
+               long long ldb, std::string* err) {
+  const int h = L / 2, nh = N / 2;
+  dim3 grid((unsigned)std::min<long long>(ceil_div(nh, 256), 16), h, T);
+  strassen_b_kernel<<<grid, 256, 0, st>>>(U, ldu, sU, h, nh, T, Bc, ldb);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && err) *err = std::string("strassen_b: ") + cudaGetErrorString(e);
+  return e == cudaSuccess ? 0 : 4;
+}
+
+int strassen_c(cudaStream_t st, const double* Mb, long long ldb, int L, int N, int T, cplx* U, long long ldu,
+               long long sU, std::string* err) {
+  const int h = L / 2, nh = N / 2;
+  dim3 grid((unsigned)std::min<long long>(ceil_div(nh, 256), 16), h, T);
+  strassen_c_kernel<<<grid, 256, 0, st>>>(Mb, ldb, h, nh, T, U, ldu, sU);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && err) *err = std::string("strassen_c: ") + cudaGetErrorString(e);
+  return e == cudaSuccess ? 0 : 4;
+}
 
 int pack_gram_panel(cudaStream_t st, const double* Pl, long long ldp, long long ps, int c0, int c1, cplx* buf, int w,
                     std::string* err) {

@@ -25,6 +25,16 @@ int split6_planes(cudaStream_t st, const cplx* U, long long ldu, long long sU, i
 int combine_gram(cudaStream_t st, const double* Pl, long long ldp, long long ps, long long ts, int n, int T, cplx* G,
                  long long ldg, long long sG, std::string* err);
 
+// One Strassen level on each planar product (planar.cu): Ks [3][7][L/2][ldks] = K's seven operands per
+// plane (once); Bc [3][7][T][L/2][ldb] = U's seven operands per plane; U[t] = the recombined product
+// from Mb (same layout as Bc).  L and N even.
+int strassen_k(cudaStream_t st, const double* Kp, long long ldk, long long pk, int L, double* Ks, long long ldks,
+               std::string* err);
+int strassen_b(cudaStream_t st, const cplx* U, long long ldu, long long sU, int L, int N, int T, double* Bc,
+               long long ldb, std::string* err);
+int strassen_c(cudaStream_t st, const double* Mb, long long ldb, int L, int N, int T, cplx* U, long long ldu,
+               long long sU, std::string* err);
+
 // the column panel [c0, c1) of the Gram, rows [0, c1), combined from the planes Pl[0..2] into the
 // contiguous buf [c1][w] (upper triangle; zeros below the diagonal) for a packed allreduce
 int pack_gram_panel(cudaStream_t st, const double* Pl, long long ldp, long long ps, int c0, int c1, cplx* buf, int w,

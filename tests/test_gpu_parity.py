@@ -239,6 +239,33 @@ def test_c4_full_size_homodyne_mutual_information(P):
     lockstep(P, w.Lx, w.Ly, w.protocol, gams, 4, 4, [A], seed=w.seed, mi=(A, B))
 
 
+@pytest.mark.parametrize("Lx,Ly,protocol,gams", [(200, 1, "projective", [2.0]), (200, 1, "homodyne", [1.0, 0.3]),
+                                               (12, 12, "projective", [3.0, 1.0]), (12, 12, "homodyne", [1.5])])
+def test_strassen_propagator_matches_oracle(P, monkeypatch, Lx, Ly, protocol, gams):
+    """One Strassen level on each planar real product of K U (csrc/planar.cu strassen_*): the same
+    state as the plain planar products (1e-12) and the oracle (1e-10) -- 1d and 2d (Kronecker K),
+    one trajectory (one batch-21 launch) and two (21 batched launches)."""
+    L, steps = Lx * Ly, 10
+    monkeypatch.setenv("TRAJ_PLANAR_MIN_N", "0")
+    monkeypatch.setenv("TRAJ_STRASSEN_MIN_N", "0")
+    a = P.Trajectories(Lx, Ly, protocol, gams, seed=17)
+    monkeypatch.setenv("TRAJ_STRASSEN", "0")
+    b = P.Trajectories(Lx, Ly, protocol, gams, seed=17)
+    K = lattice.propagator_lattice(Lx, Ly, 1.0, 0.05)
+    orc = [OracleTrajectory(Lx, Ly, protocol, g, 0.05, seed=17, traj=t, K=K) for t, g in enumerate(gams)]
+    for s in range(steps):
+        a.step(1)
+        b.step(1)
+        for o in orc:
+            o.step(1)
+    for t, o in enumerate(orc):
+        Ca, Cb = a.correlation(t).cpu().numpy(), b.correlation(t).cpu().numpy()
+        assert np.abs(Ca - Cb).max() < 1e-12
+        assert np.abs(Ca - o.correlation()).max() < C_TOL
+        if protocol == "projective":
+            assert a.last_clicks(t) == b.last_clicks(t)
+
+
 @pytest.mark.parametrize("block,shards", [(128, 1), (64, 1), (64, 2)])
 def test_structured_pass1_matches_dense_factorisation(P, monkeypatch, block, shards):
     """CholeskyQR pass 1 of a projective step on the structure of G = I - V^dag V (csrc/structchol.cu):
