@@ -115,117 +115,185 @@ __global__ void pack_gram_panel_kernel(const double* __restrict__ Pl, long long 
   }
 }
 
-// One level of Strassen's algorithm on every real product of the planar 3M propagator.  With
-// A = K's plane q and B = U's plane q in 2 x 2 blocks of (L/2) x (L/2) and (L/2) x (N/2):
+// Strassen's algorithm on every real product of the planar 3M propagator, LV = 1 or 2 levels.  With
+// A = K's plane q and B = U's plane q in 2 x 2 blocks:
 //   M1 = (A11 + A22)(B11 + B22)  M2 = (A21 + A22) B11  M3 = A11 (B12 - B22)  M4 = A22 (B21 - B11)
 //   M5 = (A11 + A12) B22         M6 = (A21 - A11)(B11 + B12)             M7 = (A12 - A22)(B21 + B22)
 //   C11 = M1 + M4 - M5 + M7,  C12 = M3 + M5,  C21 = M2 + M4,  C22 = M1 - M2 + M3 + M6
-// -- seven half-size products instead of eight.  K's seven operands are formed once; U's seven per
-// step (strassen_b), the M's combined with the complex 3M recombination in one pass (strassen_c).
+// -- seven half-size products instead of eight; applied again to each of the seven (LV = 2), 49
+// quarter-size products instead of 64.  The operand / recombination coefficients over the 2 x 2
+// blocks (11, 12, 21, 22) are the tables below; one thread handles one element of the leaf grid and
+// all 2^LV x 2^LV positions it stands for, so each pass reads and writes every matrix once.  K's
+// operands are formed once (strassen_k), U's per step (strassen_b), the leaf products are
+// recombined together with the complex 3M recombination in one pass (strassen_c).
+__constant__ int8_t kSA[7][4] = {{1, 0, 0, 1}, {0, 0, 1, 1}, {1, 0, 0, 0}, {0, 0, 0, 1},
+                                 {1, 1, 0, 0}, {-1, 0, 1, 0}, {0, 1, 0, -1}};
+__constant__ int8_t kSB[7][4] = {{1, 0, 0, 1}, {1, 0, 0, 0}, {0, 1, 0, -1}, {-1, 0, 1, 0},
+                                 {0, 0, 0, 1}, {1, 1, 0, 0}, {0, 0, 1, 1}};
+__constant__ int8_t kSC[4][7] = {{1, 0, 0, 1, -1, 0, 1}, {0, 0, 1, 0, 1, 0, 0},
+                                 {0, 1, 0, 1, 0, 0, 0}, {1, -1, 1, 0, 0, 1, 0}};
 
-// Ks[q][s][i][j] (s = 0..6, operand of M_{s+1}) from K's planes
-__global__ void strassen_a_kernel(const double* __restrict__ Kp, long long ldk, long long pk, int h,
-                                  double* __restrict__ Ks, long long ldks) {
-  const int q = blockIdx.z, i = blockIdx.y;
-  const double* k = Kp + q * pk;
-  double* o = Ks + (long long)q * 7 * h * ldks + (long long)i * ldks;
-  const long long bs = (long long)h * ldks;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < h; j += gridDim.x * blockDim.x) {
-    const double a11 = k[(long long)i * ldk + j], a12 = k[(long long)i * ldk + h + j];
-    const double a21 = k[(long long)(h + i) * ldk + j], a22 = k[(long long)(h + i) * ldk + h + j];
-    o[j] = a11 + a22;
-    o[bs + j] = a21 + a22;
-    o[2 * bs + j] = a11;
-    o[3 * bs + j] = a22;
-    o[4 * bs + j] = a11 + a12;
-    o[5 * bs + j] = a21 - a11;
-    o[6 * bs + j] = a12 - a22;
+// the 7^LV operands of a matrix given on its 2^LV x 2^LV grid of leaf blocks x[R][C] (one element each)
+template <int LV>
+__device__ __forceinline__ void strassen_operands(const double (&x)[1 << LV][1 << LV], const int8_t (&co)[7][4],
+                                                  double* out, long long bs) {
+  if (LV == 1) {
+#pragma unroll
+    for (int s = 0; s < 7; ++s)
+      out[s * bs] = co[s][0] * x[0][0] + co[s][1] * x[0][1] + co[s][2] * x[1][0] + co[s][3] * x[1][1];
+  } else {
+#pragma unroll
+    for (int s1 = 0; s1 < 7; ++s1) {
+      double h[2][2];   // level-1 operand s1 on its 2 x 2 grid of quarter blocks
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          h[r][c] = co[s1][0] * x[r][c] + co[s1][1] * x[r][2 + c] + co[s1][2] * x[2 + r][c] +
+                    co[s1][3] * x[2 + r][2 + c];
+#pragma unroll
+      for (int s2 = 0; s2 < 7; ++s2)
+        out[(s1 * 7 + s2) * bs] = co[s2][0] * h[0][0] + co[s2][1] * h[0][1] + co[s2][2] * h[1][0] +
+                                  co[s2][3] * h[1][1];
+    }
   }
 }
 
-// Bc[q][s][t][i][j]: the B operands of M_{s+1} for the planes (re, im, re + im) of U[t]
+// Ks[q][s][i][j] (s < 7^LV) from K's planes: leaf grid h = L / 2^LV
+template <int LV>
+__global__ void strassen_a_kernel(const double* __restrict__ Kp, long long ldk, long long pk, int h,
+                                  double* __restrict__ Ks, long long ldks) {
+  constexpr int G = 1 << LV, NS = LV == 1 ? 7 : 49;
+  const int q = blockIdx.z, i = blockIdx.y;
+  const double* k = Kp + q * pk;
+  const long long bs = (long long)h * ldks;
+  double* o = Ks + (long long)q * NS * bs + (long long)i * ldks;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < h; j += gridDim.x * blockDim.x) {
+    double x[G][G];
+#pragma unroll
+    for (int R = 0; R < G; ++R)
+#pragma unroll
+      for (int C = 0; C < G; ++C) x[R][C] = k[(long long)(R * h + i) * ldk + C * h + j];
+    strassen_operands<LV>(x, kSA, o + j, bs);
+  }
+}
+
+// Bc[q][s][t][i][j]: the operands of the planes (re, im, re + im) of U[t]; leaf grid h x nh
+template <int LV>
 __global__ void strassen_b_kernel(const cplx* __restrict__ U, long long ldu, long long sU, int h, int nh, int T,
                                   double* __restrict__ Bc, long long ldb) {
+  constexpr int G = 1 << LV, NS = LV == 1 ? 7 : 49;
   const int t = blockIdx.z, i = blockIdx.y;
   const cplx* u = U + t * sU;
   const long long bs = (long long)T * h * ldb;          // stride between (q, s) entries
   double* o = Bc + (long long)t * h * ldb + (long long)i * ldb;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nh; j += gridDim.x * blockDim.x) {
-    const double2 b11 = u[(long long)i * ldu + j], b12 = u[(long long)i * ldu + nh + j];
-    const double2 b21 = u[(long long)(h + i) * ldu + j], b22 = u[(long long)(h + i) * ldu + nh + j];
+    double2 v[G][G];
+#pragma unroll
+    for (int R = 0; R < G; ++R)
+#pragma unroll
+      for (int C = 0; C < G; ++C) v[R][C] = u[(long long)(R * h + i) * ldu + C * nh + j];
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      const double v11 = q == 0 ? b11.x : (q == 1 ? b11.y : b11.x + b11.y);
-      const double v12 = q == 0 ? b12.x : (q == 1 ? b12.y : b12.x + b12.y);
-      const double v21 = q == 0 ? b21.x : (q == 1 ? b21.y : b21.x + b21.y);
-      const double v22 = q == 0 ? b22.x : (q == 1 ? b22.y : b22.x + b22.y);
-      double* oq = o + (long long)q * 7 * bs;
-      oq[j] = v11 + v22;
-      oq[bs + j] = v11;
-      oq[2 * bs + j] = v12 - v22;
-      oq[3 * bs + j] = v21 - v11;
-      oq[4 * bs + j] = v22;
-      oq[5 * bs + j] = v11 + v12;
-      oq[6 * bs + j] = v21 + v22;
+      double x[G][G];
+#pragma unroll
+      for (int R = 0; R < G; ++R)
+#pragma unroll
+        for (int C = 0; C < G; ++C) x[R][C] = q == 0 ? v[R][C].x : (q == 1 ? v[R][C].y : v[R][C].x + v[R][C].y);
+      strassen_operands<LV>(x, kSB, o + (long long)q * NS * bs + j, bs);
     }
   }
 }
 
-// U[t] from the M's: per plane C11..C22, then (P1 - P2) + i (P3 - P1 - P2)
+// U[t] from the leaf products: per plane the 2^LV x 2^LV blocks of the product, then
+// (P1 - P2) + i (P3 - P1 - P2)
+template <int LV>
 __global__ void strassen_c_kernel(const double* __restrict__ Mb, long long ldb, int h, int nh, int T,
                                   cplx* __restrict__ U, long long ldu, long long sU) {
+  constexpr int G = 1 << LV, NS = LV == 1 ? 7 : 49;
   const int t = blockIdx.z, i = blockIdx.y;
   const long long bs = (long long)T * h * ldb;
   const double* m = Mb + (long long)t * h * ldb + (long long)i * ldb;
   cplx* u = U + t * sU;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nh; j += gridDim.x * blockDim.x) {
-    double c[3][4];
+    double c[3][G][G];
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      const double* mq = m + (long long)q * 7 * bs;
-      const double m1 = mq[j], m2 = mq[bs + j], m3 = mq[2 * bs + j], m4 = mq[3 * bs + j];
-      const double m5 = mq[4 * bs + j], m6 = mq[5 * bs + j], m7 = mq[6 * bs + j];
-      c[q][0] = m1 + m4 - m5 + m7;
-      c[q][1] = m3 + m5;
-      c[q][2] = m2 + m4;
-      c[q][3] = m1 - m2 + m3 + m6;
-    }
-    const long long off[4] = {(long long)i * ldu + j, (long long)i * ldu + nh + j, (long long)(h + i) * ldu + j,
-                              (long long)(h + i) * ldu + nh + j};
+      const double* mq = m + (long long)q * NS * bs + j;
+      if (LV == 1) {
+        double mm[7];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) u[off[b]] = make_double2(c[0][b] - c[1][b], c[2][b] - c[0][b] - c[1][b]);
+        for (int s = 0; s < 7; ++s) mm[s] = mq[s * bs];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          double acc = 0.0;
+#pragma unroll
+          for (int s = 0; s < 7; ++s) acc += kSC[b][s] * mm[s];
+          c[q][b >> 1][b & 1] = acc;
+        }
+      } else {
+#pragma unroll
+        for (int R = 0; R < G; ++R)
+#pragma unroll
+          for (int C = 0; C < G; ++C) c[q][R][C] = 0.0;
+#pragma unroll
+        for (int s1 = 0; s1 < 7; ++s1) {
+          double mm[7];
+#pragma unroll
+          for (int s2 = 0; s2 < 7; ++s2) mm[s2] = mq[(s1 * 7 + s2) * bs];
+#pragma unroll
+          for (int b2 = 0; b2 < 4; ++b2) {      // the 2 x 2 blocks of the level-1 product s1
+            double acc = 0.0;
+#pragma unroll
+            for (int s2 = 0; s2 < 7; ++s2) acc += kSC[b2][s2] * mm[s2];
+#pragma unroll
+            for (int b1 = 0; b1 < 4; ++b1)       // its share of the full product's half-blocks
+              if (kSC[b1][s1]) c[q][2 * (b1 >> 1) + (b2 >> 1)][2 * (b1 & 1) + (b2 & 1)] += kSC[b1][s1] * acc;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int R = 0; R < G; ++R)
+#pragma unroll
+      for (int C = 0; C < G; ++C)
+        u[(long long)(R * h + i) * ldu + C * nh + j] =
+            make_double2(c[0][R][C] - c[1][R][C], c[2][R][C] - c[0][R][C] - c[1][R][C]);
   }
 }
 
 }  // namespace
 
-int strassen_k(cudaStream_t st, const double* Kp, long long ldk, long long pk, int L, double* Ks, long long ldks,
-               std::string* err) {
-  const int h = L / 2;
+int strassen_k(cudaStream_t st, int levels, const double* Kp, long long ldk, long long pk, int L, double* Ks,
+               long long ldks, std::string* err) {
+  const int h = L >> levels;
   dim3 grid((unsigned)std::min<long long>(ceil_div(h, 256), 16), h, 3);
-  strassen_a_kernel<<<grid, 256, 0, st>>>(Kp, ldk, pk, h, Ks, ldks);
+  if (levels == 2) strassen_a_kernel<2><<<grid, 256, 0, st>>>(Kp, ldk, pk, h, Ks, ldks);
+  else strassen_a_kernel<1><<<grid, 256, 0, st>>>(Kp, ldk, pk, h, Ks, ldks);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess && err) *err = std::string("strassen_k: ") + cudaGetErrorString(e);
   return e == cudaSuccess ? 0 : 4;
 }
 
-int strassen_b(cudaStream_t st, const cplx* U, long long ldu, long long sU, int L, int N, int T, double* Bc,
-               long long ldb, std::string* err) {
-  const int h = L / 2, nh = N / 2;
+int strassen_b(cudaStream_t st, int levels, const cplx* U, long long ldu, long long sU, int L, int N, int T,
+               double* Bc, long long ldb, std::string* err) {
+  const int h = L >> levels, nh = N >> levels;
   dim3 grid((unsigned)std::min<long long>(ceil_div(nh, 256), 16), h, T);
-  strassen_b_kernel<<<grid, 256, 0, st>>>(U, ldu, sU, h, nh, T, Bc, ldb);
+  if (levels == 2) strassen_b_kernel<2><<<grid, 256, 0, st>>>(U, ldu, sU, h, nh, T, Bc, ldb);
+  else strassen_b_kernel<1><<<grid, 256, 0, st>>>(U, ldu, sU, h, nh, T, Bc, ldb);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess && err) *err = std::string("strassen_b: ") + cudaGetErrorString(e);
   return e == cudaSuccess ? 0 : 4;
 }
 
-int strassen_c(cudaStream_t st, const double* Mb, long long ldb, int L, int N, int T, cplx* U, long long ldu,
-               long long sU, std::string* err) {
-  const int h = L / 2, nh = N / 2;
+int strassen_c(cudaStream_t st, int levels, const double* Mb, long long ldb, int L, int N, int T, cplx* U,
+               long long ldu, long long sU, std::string* err) {
+  const int h = L >> levels, nh = N >> levels;
   dim3 grid((unsigned)std::min<long long>(ceil_div(nh, 256), 16), h, T);
-  strassen_c_kernel<<<grid, 256, 0, st>>>(Mb, ldb, h, nh, T, U, ldu, sU);
+  if (levels == 2) strassen_c_kernel<2><<<grid, 256, 0, st>>>(Mb, ldb, h, nh, T, U, ldu, sU);
+  else strassen_c_kernel<1><<<grid, 256, 0, st>>>(Mb, ldb, h, nh, T, U, ldu, sU);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess && err) *err = std::string("strassen_c: ") + cudaGetErrorString(e);

@@ -25,15 +25,16 @@ int split6_planes(cudaStream_t st, const cplx* U, long long ldu, long long sU, i
 int combine_gram(cudaStream_t st, const double* Pl, long long ldp, long long ps, long long ts, int n, int T, cplx* G,
                  long long ldg, long long sG, std::string* err);
 
-// One Strassen level on each planar product (planar.cu): Ks [3][7][L/2][ldks] = K's seven operands per
-// plane (once); Bc [3][7][T][L/2][ldb] = U's seven operands per plane; U[t] = the recombined product
-// from Mb (same layout as Bc).  L and N even.
-int strassen_k(cudaStream_t st, const double* Kp, long long ldk, long long pk, int L, double* Ks, long long ldks,
-               std::string* err);
-int strassen_b(cudaStream_t st, const cplx* U, long long ldu, long long sU, int L, int N, int T, double* Bc,
-               long long ldb, std::string* err);
-int strassen_c(cudaStream_t st, const double* Mb, long long ldb, int L, int N, int T, cplx* U, long long ldu,
-               long long sU, std::string* err);
+// Strassen on each planar product, `levels` = 1 or 2 (planar.cu), leaf grid h = L / 2^levels,
+// nh = N / 2^levels, NS = 7^levels products per plane: Ks [3][NS][h][ldks] = K's operands (once);
+// Bc [3][NS][T][h][ldb] = U's operands; U[t] = the recombined product from Mb (Bc's layout).
+// L divisible by 2^(levels+1).
+int strassen_k(cudaStream_t st, int levels, const double* Kp, long long ldk, long long pk, int L, double* Ks,
+               long long ldks, std::string* err);
+int strassen_b(cudaStream_t st, int levels, const cplx* U, long long ldu, long long sU, int L, int N, int T,
+               double* Bc, long long ldb, std::string* err);
+int strassen_c(cudaStream_t st, int levels, const double* Mb, long long ldb, int L, int N, int T, cplx* U,
+               long long ldu, long long sU, std::string* err);
 
 // the column panel [c0, c1) of the Gram, rows [0, c1), combined from the planes Pl[0..2] into the
 // contiguous buf [c1][w] (upper triangle; zeros below the diagonal) for a packed allreduce

@@ -54,9 +54,11 @@ struct traj_ctx {
   // constant-stride triples over all trajectories, so each group of three products is one launch
   bool planar_cqr = false;
   double* Xp = nullptr;
-  // one Strassen level on each planar product of K U (planar.cu; TRAJ_STRASSEN=0: off): K's seven
-  // operands per plane Ks [3][7][L/2][ldS], U's Bc (in Up's space) and the products Ms [3][7][T][L/2][ldM]
+  // Strassen (1 or 2 levels) on each planar product of K U (planar.cu; TRAJ_STRASSEN=0: off): K's
+  // 7^lv operands per plane Ks [3][7^lv][L/2^lv][ldS], U's Bc (in Up's space) and the products Ms
+  // [3][7^lv][T][L/2^lv][ldM]
   bool strassen = false;
+  int slv = 0;
   double *Ks = nullptr, *Bc = nullptr, *Ms = nullptr;
   long long ldS = 0, ldM = 0;
   std::vector<cplx> band_host;     // the same on the host: passed by value to the stencil launches
@@ -316,12 +318,16 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     const long long smin = sm ? atoll(sm) : 2048;
     h->strassen = !(sv && sv[0] == '0') && L % 4 == 0 && N >= smin;
     if (h->strassen) {
-      const long long hh = L / 2;
+      // two levels when K's 147 quarter operands fit 24 GB (c3: 19.7 GB) and N >= 4096, else one
+      const char* lv = getenv("TRAJ_STRASSEN_LEVELS");
+      const bool two_ok = L % 8 == 0 && 147.0 * (L / 4) * round_up(L / 4, 16) * 8 <= 24e9;
+      h->slv = lv ? (atoi(lv) >= 2 && two_ok ? 2 : 1) : (two_ok && N >= 4096 ? 2 : 1);
+      const long long hh = L >> h->slv, ns = 3 * (h->slv == 2 ? 49 : 7);
       h->ldS = round_up(hh, 16);
-      h->ldM = round_up(N / 2, 16);
-      lay.take(h->Ks, (size_t)21 * hh * h->ldS * 8);
+      h->ldM = round_up(N >> h->slv, 16);
+      lay.take(h->Ks, (size_t)ns * hh * h->ldS * 8);
       // the products alias K's planes once Ks is built, when they fit (one trajectory)
-      const size_t mb = (size_t)21 * T * hh * h->ldM * 8;
+      const size_t mb = (size_t)ns * T * hh * h->ldM * 8;
       if (mb <= (size_t)3 * L * h->ldK * 8) h->Ms = h->Kp;
       else lay.take(h->Ms, mb);
     }
@@ -330,7 +336,9 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
   }
   if (h->planar || h->planar_cqr) {
     h->ldP = round_up(N, 16);
-    lay.take(h->Up, (size_t)T * std::max<long long>(6 * L * h->ldP, h->strassen ? 21 * (L / 2) * h->ldM : 0) * 8);
+    lay.take(h->Up, (size_t)T * std::max<long long>(6 * L * h->ldP,
+                                                     h->strassen ? 3 * (h->slv == 2 ? 49 : 7) * (L >> h->slv) * h->ldM
+                                                                 : 0) * 8);
     h->Bc = h->Up;   // U's Strassen operands use the plane buffer (free during K U)
     lay.take(h->Pp, (size_t)T * 3 * L * h->ldP * 8);
     if (h->planar_cqr) lay.take(h->Xp, (size_t)T * 3 * N * h->ldP * 8);
@@ -1119,19 +1127,20 @@ int one_step(traj_ctx* h) {
     } else {
       // U <- K U  (K shared across the batch: stride 0)
       if (h->strassen) {
-        // one Strassen level per planar product: U's seven operands per plane, 21 half-size real
-        // products (one batched launch for one trajectory), recombined into K U in one pass
-        const long long hh = h->L / 2, nh = h->N / 2, bK = hh * h->ldS, bM = hh * h->ldM;
-        TRY(strassen_b(h->st, Uc, h->ldN, h->sU, h->L, h->N, h->T, h->Bc, h->ldM, &h->err));
+        // Strassen per planar product: U's 7^lv operands per plane, 3 7^lv leaf-size real products
+        // (one batched launch for one trajectory), recombined into K U in one pass
+        const int np = 3 * (h->slv == 2 ? 49 : 7);
+        const long long hh = h->L >> h->slv, nh = h->N >> h->slv, bK = hh * h->ldS, bM = hh * h->ldM;
+        TRY(strassen_b(h->st, h->slv, Uc, h->ldN, h->sU, h->L, h->N, h->T, h->Bc, h->ldM, &h->err));
         if (h->T == 1) {
-          TRY(dgemm(h->st, 0, hh, nh, hh, 1.0, h->Ks, h->ldS, bK, h->Bc, h->ldM, bM, 0.0, h->Ms, h->ldM, bM, 21, 0,
+          TRY(dgemm(h->st, 0, hh, nh, hh, 1.0, h->Ks, h->ldS, bK, h->Bc, h->ldM, bM, 0.0, h->Ms, h->ldM, bM, np, 0,
                     &h->err));
         } else {
-          for (int qs = 0; qs < 21; ++qs)
+          for (int qs = 0; qs < np; ++qs)
             TRY(dgemm(h->st, 0, hh, nh, hh, 1.0, h->Ks + qs * bK, h->ldS, 0, h->Bc + qs * h->T * bM, h->ldM, bM, 0.0,
                       h->Ms + qs * h->T * bM, h->ldM, bM, h->T, 0, &h->err));
         }
-        TRY(strassen_c(h->st, h->Ms, h->ldM, h->L, h->N, h->T, Un, h->ldN, h->sU, &h->err));
+        TRY(strassen_c(h->st, h->slv, h->Ms, h->ldM, h->L, h->N, h->T, Un, h->ldN, h->sU, &h->err));
       } else if (h->planar) {
         // three real products on planes, then (P1 - P2) + i (P3 - P1 - P2)
         const long long tU = h->L * h->ldP, pU = h->T * tU, pK = h->L * h->ldK;
@@ -1504,7 +1513,7 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
   } else if (h->planar) {
     if (build_k_planar(h->st, h->Kp, h->ldK, h->L * h->ldK, h->Lx, h->Ly, h->kcoef, h->kcoef + h->Lx, &e))
       return bail(TRAJ_ECUDA, e);
-    if (h->strassen && strassen_k(h->st, h->Kp, h->ldK, h->L * h->ldK, h->L, h->Ks, h->ldS, &e))
+    if (h->strassen && strassen_k(h->st, h->slv, h->Kp, h->ldK, h->L * h->ldK, h->L, h->Ks, h->ldS, &e))
       return bail(TRAJ_ECUDA, e);
   } else if (cfg->protocol != TRAJ_HOMODYNE_RK4 && cfg->protocol != TRAJ_PROJECTIVE_EVENTS &&
              build_k(h->st, h->K, h->ldL, h->Lx, h->Ly, h->kcoef, h->kcoef + h->Lx, &e)) {
