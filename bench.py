@@ -631,7 +631,9 @@ def run_e2e(args, w, tpg, mode, rank, world, P):
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    t_init = time.perf_counter()
     tr = open_handle(P, args, w, mode, rank, world, tpg, stream=stream)
+    init_ms = 1e3 * (time.perf_counter() - t_init)      # traj_init returns after its own stream sync
     for t in range(tpg):
         tr.set_state(t, U0)                       # H2D from pinned host memory
     h2d = tpg * U0.numel() * 16
@@ -653,6 +655,7 @@ def run_e2e(args, w, tpg, mode, rank, world, P):
     ms = max_over_ranks(ms, world)
     return {"value": (1 if shard else world) * tpg * args.steps / (ms / 1e3), "unit": "trajectory-steps/s",
             "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+            "handle_init_ms": init_ms,
             "includes": f"handle init (workspace from torch's caching allocator, K built on the device"
                         f"{', NCCL communicator' if shard and world > 1 else ''}), U0 upload "
                         f"from pinned host{' (this rank' + chr(39) + 's rows)' if shard and world > 1 else ''}, "
