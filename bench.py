@@ -355,6 +355,18 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def strassen_levels(w) -> int:
+    """Strassen levels the unsharded planar K U uses (the rule of csrc/traj_api.cu carve())."""
+    if os.environ.get("TRAJ_STRASSEN", "1") == "0" or w.L % 4 or w.N < int(os.environ.get("TRAJ_STRASSEN_MIN_N", "2048")):
+        return 0
+    q = w.L // 4
+    two_ok = w.L % 8 == 0 and 147.0 * q * ((q + 15) // 16 * 16) * 8 <= 24e9
+    lv = os.environ.get("TRAJ_STRASSEN_LEVELS")
+    if lv:
+        return 2 if int(lv) >= 2 and two_ok else 1
+    return 2 if two_ok and w.N >= 4096 else 1
+
+
 def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P):
     """Roofline of the dominant phase (the largest device time per step) on EXECUTED flops.
 
@@ -377,11 +389,11 @@ def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P):
               and w.protocol in ("projective", "homodyne")
               and (not shard or os.environ.get("TRAJ_PLANAR_CQR", "1") != "0"))
     planar_cqr = big and os.environ.get("TRAJ_PLANAR_CQR", "1") != "0" and (not shard or planar)
-    smin = int(os.environ.get("TRAJ_STRASSEN_MIN_N", "2048"))
-    strassen = (planar and not shard and w.L % 4 == 0 and w.N >= smin
-                and os.environ.get("TRAJ_STRASSEN", "1") != "0")
-    ku_name = ("dgemm_dmma_kernel x21 (planar 3M: Kr Ur, Ki Ui, (Kr+Ki)(Ur+Ui), each by one Strassen level: seven "
-               "half-size real products; 128x128 CTA, one batch-21 launch) + operand / recombination passes"
+    slv = strassen_levels(w) if (planar and not shard) else 0
+    strassen = slv > 0
+    ku_name = (f"dgemm_dmma_kernel x{3 * 7 ** slv} (planar 3M: Kr Ur, Ki Ui, (Kr+Ki)(Ur+Ui), each by {slv} "
+               f"Strassen level(s): {7 ** slv} products of 1/{2 ** slv} size; 128x128 CTA, one batched launch) + "
+               "operand / recombination passes"
                if strassen else
                "dgemm_dmma_kernel x3 (planar 3M: Kr Ur, Ki Ui, (Kr+Ki)(Ur+Ui); 128x128 CTA) + split/combine passes"
                + ("; per shard: P ring-distance K-chunk products accumulated, the U exchange under them" if shard
@@ -399,7 +411,7 @@ def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P):
     # (overlapped with the factorisation, or the structured pass 1)
     n_trmm = 1 if (struct0 or os.environ.get("TRAJ_CHOL_OVERLAP", "1") != "0") else 2
     # DMMA flops per 8mnk flop: 3M 6/8; with one Strassen level 7/8 of that (21 half-size products)
-    a_ku = (0.75 * 7 / 8 if strassen else 0.75) if (planar or algo == "3m") else 1.0
+    a_ku = 0.75 * (7 / 8) ** slv if (planar or algo == "3m") else 1.0
     a_cqr = 0.75 if (planar_cqr or algo == "3m") else 1.0
     kern = {"propagate": (8.0 * rows * w.L * w.N * tpg, a_ku, f"{ku_name}: U <- K U (8 L^2 N flops per step)"),
             "gram": (n_gram * 4.0 * rows * w.N * w.N * tpg, a_cqr,
@@ -437,11 +449,11 @@ def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P):
     if os.path.exists(tp) and dom == "propagate" and not shard:
         try:
             tj = json.load(open(tp)).get(w.name, {})
-            traffic = (tj.get("propagate_strassen_dram_bytes") if strassen else
+            traffic = (tj.get(f"propagate_strassen{slv}_dram_bytes") if strassen else
                        tj.get("propagate_dram_bytes") if planar else tj.get("interleaved_zgemm3mw_dram_bytes"))
         except Exception:
             traffic = None
-    mult = ("planar 3m + one Strassen level" if (strassen and dom == "propagate") else
+    mult = (f"planar 3m + {slv} Strassen level(s)" if (strassen and dom == "propagate") else
             "planar 3m" if (planar and dom == "propagate") or (planar_cqr and dom in ("gram", "trmm")) else
             "4m" if dom == "fused" else algo)
     roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
@@ -452,10 +464,10 @@ def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P):
                                           "the handle's stream)", "peak_source": FP64_PEAK_SOURCE,
             "complex_mult": mult,
             "flops_counted": ("executed DMMA flops: 6mnk per complex product for 3M (three real products), "
-                              "21/4 mnk with one Strassen level on each (seven half-size products per real "
-                              "product), 8mnk for 4M; achieved_8mnk_equiv counts the conventional 8mnk"),
+                              "x 7/8 per Strassen level on each real product (seven products of half size), 8mnk "
+                              "for 4M; achieved_8mnk_equiv counts the conventional 8mnk"),
             "traffic_note": (("ncu dram bytes of the propagate phase (profiles/ncu_traffic.json: U's Strassen "
-                              "operands, the 21 half-size real products as one batch-21 launch, the "
+                              f"operands, the {3 * 7 ** slv} real products as one batched launch, the "
                               "recombination) vs 8.6 GB algorithmic") if strassen else
                              ("ncu dram bytes of the propagate phase (profiles/ncu_traffic.json: split, the "
                               "three real 16384x8192x16384 products as one batch-3 launch, combine) vs 8.6 GB "
@@ -595,9 +607,8 @@ def run_secondary(args, world, rank, P, steps=2, warmup=2):
     if args.propagator == "dense" and prop > 0:
         eq8 = 8.0 * rows * w.L * w.N / (prop / 1e3) / 1e12
         a = 0.75 if P.traj_get_zgemm_algorithm() == "3m" or os.environ.get("TRAJ_PLANAR_KU", "1") != "0" else 1.0
-        if (not shard and w.L % 4 == 0 and w.N >= int(os.environ.get("TRAJ_STRASSEN_MIN_N", "2048"))
-                and os.environ.get("TRAJ_STRASSEN", "1") != "0" and os.environ.get("TRAJ_PLANAR_KU", "1") != "0"):
-            a *= 7 / 8            # one Strassen level on each planar product
+        if not shard and os.environ.get("TRAJ_PLANAR_KU", "1") != "0":
+            a *= (7 / 8) ** strassen_levels(w)      # Strassen levels on each planar product
         out["roofline_propagate"] = {"bound": "tensor", "achieved": eq8 * a, "peak": FP64_PEAK_TFLOPS,
                                      "unit": "TFLOP/s", "frac": eq8 * a / FP64_PEAK_TFLOPS,
                                      "achieved_8mnk_equiv": eq8, "frac_8mnk_equiv": eq8 / FP64_PEAK_TFLOPS,

@@ -250,195 +250,6 @@ __global__ void __launch_bounds__(EW * 32) chol_leaf_elim_kernel(int n, const cp
 
 constexpr int ELEAF_SMEM = 2 * NB * ELD * 16;
 
-// The leaf by 16 x 16 blocks (default; TRAJ_CHOL_LEAF=elim / regs select the others).  A (the upper
-// triangle of G, padded with the identity to 64 x 64) and X live in shared memory.  Right-looking over
-// the four block columns: warp 0 factors the diagonal block (16 pivots, warp-synchronous) and inverts
-// its factor; the block row R_kj = R_kk^-dag A_kj and the trailing update A_ij -= R_ki^dag R_kj are
-// 16 x 16 x 16 products, one block per warp; then X = R^-1 by block back-substitution along the
-// superdiagonals, X_ij = -R_ii^-1 sum_{i<k<=j} R_ik X_kj.  Four barriers per block column instead of
-// one per pivot pair: the 64-pivot dependency chain stays inside one warp.
-constexpr int BW = 4;                     // warps of the blocked leaf
-constexpr int BLD = NB + 1;               // padded leading dimension (complex)
-constexpr int BLEAF_SMEM = (2 * NB * BLD + BW * 16 * 17) * 16;
-
-__device__ __forceinline__ double2 cfma_conj(double2 a, double2 b, double2 acc) {   // acc + conj(a) b
-  acc.x += a.x * b.x + a.y * b.y;
-  acc.y += a.x * b.y - a.y * b.x;
-  return acc;
-}
-__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 acc) {        // acc + a b
-  acc.x += a.x * b.x - a.y * b.y;
-  acc.y += a.x * b.y + a.y * b.x;
-  return acc;
-}
-
-// out[r] (rows r0 + r, column c) = sum_k conj(A[k][r0 + r]) B[k][c] over k < 16 (16 x 16 blocks)
-__device__ __forceinline__ void warp_ahb(const double2* A, int lda, const double2* B, int ldb, int r0, int c,
-                                         double2 (&out)[8]) {
-#pragma unroll
-  for (int r = 0; r < 8; ++r) out[r] = make_double2(0.0, 0.0);
-#pragma unroll 4
-  for (int k = 0; k < 16; ++k) {
-    const double2 b = B[k * ldb + c];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) out[r] = cfma_conj(A[k * lda + r0 + r], b, out[r]);
-  }
-}
-
-// out[r] = sum_k A[r0 + r][k] B[k][c]
-__device__ __forceinline__ void warp_ab(const double2* A, int lda, const double2* B, int ldb, int r0, int c,
-                                        double2 (&out)[8]) {
-#pragma unroll
-  for (int r = 0; r < 8; ++r) out[r] = make_double2(0.0, 0.0);
-#pragma unroll 4
-  for (int k = 0; k < 16; ++k) {
-    const double2 b = B[k * ldb + c];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) out[r] = cfma(A[(r0 + r) * lda + k], b, out[r]);
-  }
-}
-
-__global__ void __launch_bounds__(BW * 32) chol_leaf_blk_kernel(int n, const cplx* G, long long ldg, long long sG,
-                                                                cplx* X, long long ldx, long long sX, int32_t* failed,
-                                                                const int32_t* gate) {
-  if (gate && *gate == 0) return;
-  extern __shared__ __align__(16) double2 bsm[];
-  double2* As = bsm;                      // [64][BLD]: A, overwritten by R (upper)
-  double2* Xs = bsm + NB * BLD;           // [64][BLD]: X = R^-1 (upper)
-  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double2* Ts = bsm + 2 * NB * BLD + warp * 16 * 17;   // this warp's 16 x 16 scratch
-  const cplx* g = G + b * sG;
-  cplx* x = X + b * sX;
-  const int nblk = (n + 15) >> 4;
-  for (int idx = tid; idx < NB * NB; idx += BW * 32) {
-    const int i = idx >> 6, k = idx & 63;
-    double2 v = make_double2(i == k ? 1.0 : 0.0, 0.0);
-    if (i < n && k < n && k >= i) v = g[(long long)i * ldg + k];
-    As[i * BLD + k] = v;
-    Xs[i * BLD + k] = make_double2(0.0, 0.0);
-  }
-  __syncthreads();
-  __shared__ int bad;
-  if (tid == 0) bad = 0;
-  const int c = lane & 15, r0 = (lane >> 4) * 8;
-  for (int kb = 0; kb < nblk; ++kb) {
-    const int o = kb * 16;
-    double2* D = As + o * BLD + o;
-    double2* Xd = Xs + o * BLD + o;
-    if (warp == 0) {
-      // unblocked Cholesky of the diagonal block: row p of R = row p of A / sqrt(d_p), then
-      // A_ik -= conj(R_pi) R_pk for p < i <= k
-      for (int p = 0; p < 16; ++p) {
-        const double d = D[p * BLD + p].x;
-        if (!(d > 0.0) || !isfinite(d)) {
-          if (lane == 0) bad = 1;
-        }
-        const double ir = rsqrt(d);
-        __syncwarp();
-        if (lane >= p && lane < 16) {
-          const double2 v = D[p * BLD + lane];
-          D[p * BLD + lane] = make_double2(v.x * ir, v.y * ir);
-        }
-        __syncwarp();
-        for (int e = lane; e < 256; e += 32) {
-          const int i = e >> 4, k = e & 15;
-          if (i > p && k >= i) {
-            const double2 ri = D[p * BLD + i], rk = D[p * BLD + k];
-            double2 v = D[i * BLD + k];
-            v.x -= ri.x * rk.x + ri.y * rk.y;
-            v.y -= ri.x * rk.y - ri.y * rk.x;
-            D[i * BLD + k] = v;
-          }
-        }
-        __syncwarp();
-      }
-      // X_dd = R_dd^-1 (upper): lane c < 16 solves column c by back substitution
-      if (lane < 16) {
-        double2 col[16];
-#pragma unroll
-        for (int i = 15; i >= 0; --i) {
-          double2 acc = make_double2(i == c ? 1.0 : 0.0, 0.0);
-#pragma unroll
-          for (int k = i + 1; k < 16; ++k) {
-            if (k <= c) {
-              const double2 r = D[i * BLD + k];
-              acc.x -= r.x * col[k].x - r.y * col[k].y;
-              acc.y -= r.x * col[k].y + r.y * col[k].x;
-            }
-          }
-          const double rii = D[i * BLD + i].x;
-          col[i] = i <= c ? make_double2(acc.x / rii, acc.y / rii) : make_double2(0.0, 0.0);
-        }
-#pragma unroll
-        for (int i = 0; i < 16; ++i) Xd[i * BLD + c] = col[i];
-      }
-    }
-    __syncthreads();
-    // block row: R_kj = R_kk^-dag A_kj  (X_dd^dag A_kj)
-    for (int j = kb + 1 + warp; j < nblk; j += BW) {
-      double2 out[8];
-      double2* Akj = As + o * BLD + j * 16;
-      warp_ahb(Xd, BLD, Akj, BLD, r0, c, out);
-      __syncwarp();
-#pragma unroll
-      for (int r = 0; r < 8; ++r) Akj[(r0 + r) * BLD + c] = out[r];
-    }
-    __syncthreads();
-    // trailing update A_ij -= R_ki^dag R_kj, kb < i <= j
-    {
-      int t = 0;
-      for (int i = kb + 1; i < nblk; ++i)
-        for (int j = i; j < nblk; ++j, ++t) {
-          if (t % BW != warp) continue;
-          double2 out[8];
-          warp_ahb(As + o * BLD + i * 16, BLD, As + o * BLD + j * 16, BLD, r0, c, out);
-          double2* Aij = As + (i * 16) * BLD + j * 16;
-#pragma unroll
-          for (int r = 0; r < 8; ++r) {
-            double2 v = Aij[(r0 + r) * BLD + c];
-            v.x -= out[r].x;
-            v.y -= out[r].y;
-            Aij[(r0 + r) * BLD + c] = v;
-          }
-        }
-    }
-    __syncthreads();
-  }
-  // X_ij = -X_ii sum_{i<k<=j} R_ik X_kj along the superdiagonals d = j - i
-  for (int d = 1; d < nblk; ++d) {
-    for (int i = warp; i + d < nblk; i += BW) {
-      const int j = i + d;
-      double2 acc[8];
-#pragma unroll
-      for (int r = 0; r < 8; ++r) acc[r] = make_double2(0.0, 0.0);
-      for (int k = i + 1; k <= j; ++k) {
-        double2 out[8];
-        warp_ab(As + (i * 16) * BLD + k * 16, BLD, Xs + (k * 16) * BLD + j * 16, BLD, r0, c, out);
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          acc[r].x += out[r].x;
-          acc[r].y += out[r].y;
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < 8; ++r) Ts[(r0 + r) * 17 + c] = acc[r];
-      __syncwarp();
-      double2 out[8];
-      warp_ab(Xs + (i * 16) * BLD + i * 16, BLD, Ts, 17, r0, c, out);
-#pragma unroll
-      for (int r = 0; r < 8; ++r) Xs[(i * 16 + r0 + r) * BLD + j * 16 + c] = make_double2(-out[r].x, -out[r].y);
-      __syncwarp();
-    }
-    __syncthreads();
-  }
-  const double nan = __longlong_as_double(0x7ff8000000000000ll);
-  for (int idx = tid; idx < n * n; idx += BW * 32) {
-    const int i = idx / n, k = idx % n;
-    x[(long long)i * ldx + k] = bad ? make_double2(nan, nan) : (k >= i ? Xs[i * BLD + k] : make_double2(0.0, 0.0));
-  }
-  if (tid == 0 && bad && failed) failed[b] = 1;
-}
-
 int split(long long n) { return (int)chol_split(n); }
 
 struct Ctx {
@@ -456,7 +267,7 @@ struct Ctx {
   const CholHook* hook;
   DevBounds db;            // gate: every launch of the factorisation runs only if *gate != 0
   long long n_top;
-  int leaf;                // 0: blocked (default), 1: elimination (TRAJ_CHOL_LEAF=elim), 2: registers (=regs)
+  int leaf;                // 1: elimination (default), 2: register-blocked (TRAJ_CHOL_LEAF=regs)
 };
 
 // row slice boundaries of M rows over P ranks (comm_plan.h row_slices: the schedule the ranks share)
@@ -485,12 +296,7 @@ int dist_gemm(Ctx& c, bool tri_c, int opA, int opB, long long M, long long N, lo
 int rec(Ctx& c, long long o, long long n) {
   if (n <= NB) {
     cudaError_t e = cudaSuccess;
-    if (c.leaf == 0) {             // blocked leaf (default)
-      e = ensure_smem(reinterpret_cast<const void*>(chol_leaf_blk_kernel), BLEAF_SMEM);
-      if (e == cudaSuccess)
-        chol_leaf_blk_kernel<<<(unsigned)c.batch, BW * 32, BLEAF_SMEM, c.st>>>(
-            (int)n, c.G + o * c.ldg + o, c.ldg, c.sG, c.X + o * c.ldx + o, c.ldx, c.sX, c.failed, c.db.gate);
-    } else if (n > 16 && c.leaf == 1) {   // elimination leaf (TRAJ_CHOL_LEAF=elim)
+    if (n > 16 && c.leaf == 1) {   // elimination leaf (default; TRAJ_CHOL_LEAF=regs: the register-blocked one)
       e = ensure_smem(reinterpret_cast<const void*>(chol_leaf_elim_kernel), ELEAF_SMEM);
       if (e == cudaSuccess)
         chol_leaf_elim_kernel<<<(unsigned)c.batch, EW * 32, ELEAF_SMEM, c.st>>>(
@@ -588,7 +394,7 @@ int chol_inverse(cudaStream_t st, long long n, cplx* G, long long ldg, long long
   c.n_top = n;
   {
     const char* lf = getenv("TRAJ_CHOL_LEAF");
-    c.leaf = !lf ? 0 : (lf[0] == 'e' ? 1 : (lf[0] == 'r' ? 2 : 0));
+    c.leaf = (lf && lf[0] == 'r') ? 2 : 1;
   }
   if (n > NB && !gate) {
     // the strict lower triangle of X must read as zeros (triangular GEMM tiles cross it); with a

@@ -107,11 +107,11 @@ def test_zgemm_triangular_skips_and_upper_epilogue(T):
     assert np.all(g[il] == 7.0)
 
 
-@pytest.mark.parametrize("leaf", ["blk", "elim", "regs"])
+@pytest.mark.parametrize("leaf", ["elim", "regs"])
 @pytest.mark.parametrize("n", [1, 5, 17, 33, 64, 65, 130, 300, 520])
 def test_chol_inverse(T, n, leaf, monkeypatch):
-    """The three 64 x 64 leaves (the 16 x 16-blocked leaf, default; TRAJ_CHOL_LEAF=elim the elimination
-    leaf, =regs the register-blocked one) under the recursion, against NumPy's Cholesky and inverse."""
+    """Both 64 x 64 leaves (the elimination leaf, default; TRAJ_CHOL_LEAF=regs the register-blocked
+    one) under the recursion, against NumPy's Cholesky and inverse."""
     from paper_2508_18468_b200 import traj_chol_inverse
     monkeypatch.setenv("TRAJ_CHOL_LEAF", leaf)
     nb = 3
@@ -133,7 +133,7 @@ def test_chol_inverse(T, n, leaf, monkeypatch):
         assert np.abs(x[b].conj().T @ Gs[b] @ x[b] - np.eye(n)).max() < 1e-11
 
 
-@pytest.mark.parametrize("leaf", ["blk", "elim", "regs"])
+@pytest.mark.parametrize("leaf", ["elim", "regs"])
 def test_chol_inverse_flags_breakdown(T, leaf, monkeypatch):
     from paper_2508_18468_b200 import traj_chol_inverse
     monkeypatch.setenv("TRAJ_CHOL_LEAF", leaf)
