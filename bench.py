@@ -355,12 +355,15 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def strassen_levels(w) -> int:
-    """Strassen levels the unsharded planar K U uses (the rule of csrc/traj_api.cu carve())."""
-    if os.environ.get("TRAJ_STRASSEN", "1") == "0" or w.L % 4 or w.N < int(os.environ.get("TRAJ_STRASSEN_MIN_N", "2048")):
+def strassen_levels(w, P: int = 1) -> int:
+    """Strassen levels of the planar K U (the rule of csrc/traj_api.cu carve(); row-sharded over P GPUs:
+    csrc/shard.cu's rule on the Lp x Lp chunks K_g[:, s], Lp = L / P)."""
+    Lp = w.L // P
+    if (os.environ.get("TRAJ_STRASSEN", "1") == "0" or Lp % 2 or w.N % 2
+            or w.N < int(os.environ.get("TRAJ_STRASSEN_MIN_N", "2048"))):
         return 0
-    q = w.L // 4
-    two_ok = w.L % 8 == 0 and 147.0 * q * ((q + 15) // 16 * 16) * 8 <= 24e9
+    q = Lp // 4
+    two_ok = Lp % 4 == 0 and w.N % 4 == 0 and 147.0 * P * q * ((q + 15) // 16 * 16) * 8 <= 24e9
     lv = os.environ.get("TRAJ_STRASSEN_LEVELS")
     if lv:
         return 2 if int(lv) >= 2 and two_ok else 1
@@ -389,7 +392,7 @@ def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P):
               and w.protocol in ("projective", "homodyne")
               and (not shard or os.environ.get("TRAJ_PLANAR_CQR", "1") != "0"))
     planar_cqr = big and os.environ.get("TRAJ_PLANAR_CQR", "1") != "0" and (not shard or planar)
-    slv = strassen_levels(w) if (planar and not shard) else 0
+    slv = strassen_levels(w, w.L // rows) if planar else 0
     strassen = slv > 0
     ku_name = (f"dgemm_dmma_kernel x{3 * 7 ** slv} (planar 3M: Kr Ur, Ki Ui, (Kr+Ki)(Ur+Ui), each by {slv} "
                f"Strassen level(s): {7 ** slv} products of 1/{2 ** slv} size; 128x128 CTA, one batched launch) + "
@@ -607,8 +610,8 @@ def run_secondary(args, world, rank, P, steps=2, warmup=2):
     if args.propagator == "dense" and prop > 0:
         eq8 = 8.0 * rows * w.L * w.N / (prop / 1e3) / 1e12
         a = 0.75 if P.traj_get_zgemm_algorithm() == "3m" or os.environ.get("TRAJ_PLANAR_KU", "1") != "0" else 1.0
-        if not shard and os.environ.get("TRAJ_PLANAR_KU", "1") != "0":
-            a *= (7 / 8) ** strassen_levels(w)      # Strassen levels on each planar product
+        if os.environ.get("TRAJ_PLANAR_KU", "1") != "0":
+            a *= (7 / 8) ** strassen_levels(w, world if shard else 1)   # Strassen levels on each planar product
         out["roofline_propagate"] = {"bound": "tensor", "achieved": eq8 * a, "peak": FP64_PEAK_TFLOPS,
                                      "unit": "TFLOP/s", "frac": eq8 * a / FP64_PEAK_TFLOPS,
                                      "achieved_8mnk_equiv": eq8, "frac_8mnk_equiv": eq8 / FP64_PEAK_TFLOPS,

@@ -414,4 +414,85 @@ int chol_inverse(cudaStream_t st, long long n, cplx* G, long long ldg, long long
   return rec(c, 0, n);
 }
 
+namespace {
+
+__global__ void fallback_decide_kernel(const unsigned long long* dev, int T, double thr,
+                                       cudaGraphConditionalHandle cond, unsigned long long* fallbacks) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  unsigned int full = 0;
+  for (int t = 0; t < T; ++t)
+    if (__longlong_as_double((long long)dev[t]) > thr) full = 1;   // a NaN does not force it
+  if (full && fallbacks) fallbacks[0] += 1ull;
+  cudaGraphSetConditional(cond, full);
+}
+
+}  // namespace
+
+int CholFallbackGraph::build(long long n, cplx* G, long long ldg, long long sG, cplx* X, long long ldx, long long sX,
+                             long long batch, void* scratch, int32_t* failed, const unsigned long long* dev, double thr,
+                             unsigned long long* fallbacks, std::string* err) {
+  auto bad = [&](const char* what, cudaError_t e) {
+    if (err) *err = std::string("fallback graph: ") + what + ": " + cudaGetErrorString(e);
+    destroy();
+    return 4;
+  };
+  cudaError_t e = cudaGraphCreate(&graph, 0);
+  if (e != cudaSuccess) return bad("create", e);
+  cudaGraphConditionalHandle cond;
+  if ((e = cudaGraphConditionalHandleCreate(&cond, graph, 0, 0)) != cudaSuccess) return bad("handle", e);
+  int T = (int)batch;
+  void* args[] = {const_cast<unsigned long long**>(&dev), &T, &thr, &cond, &fallbacks};
+  cudaKernelNodeParams kp = {};
+  kp.func = reinterpret_cast<void*>(fallback_decide_kernel);
+  kp.gridDim = dim3(1);
+  kp.blockDim = dim3(32);
+  kp.kernelParams = args;
+  cudaGraphNode_t decide;
+  if ((e = cudaGraphAddKernelNode(&decide, graph, nullptr, 0, &kp)) != cudaSuccess) return bad("decide node", e);
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = cond;
+  cp.conditional.type = cudaGraphCondTypeIf;
+  cp.conditional.size = 1;
+  cudaGraphNode_t ifn;
+  if ((e = cudaGraphAddNode(&ifn, graph, &decide, 1, &cp)) != cudaSuccess) return bad("if node", e);
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  cudaStream_t cs;
+  if ((e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking)) != cudaSuccess) return bad("stream", e);
+  if ((e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)) != cudaSuccess) {
+    cudaStreamDestroy(cs);
+    return bad("capture", e);
+  }
+  std::string cerr;
+  const int r = chol_inverse(cs, n, G, ldg, sG, X, ldx, sX, batch, scratch, failed, &cerr);
+  cudaGraph_t captured = body;
+  e = cudaStreamEndCapture(cs, &captured);
+  cudaStreamDestroy(cs);
+  if (r) {
+    if (err) *err = "fallback graph: " + cerr;
+    destroy();
+    return r;
+  }
+  if (e != cudaSuccess) return bad("end capture", e);
+  if ((e = cudaGraphInstantiate(&exec, graph, 0)) != cudaSuccess) return bad("instantiate", e);
+  return 0;
+}
+
+int CholFallbackGraph::launch(cudaStream_t st, std::string* err) {
+  const cudaError_t e = cudaGraphLaunch(exec, st);
+  count_launch();
+  if (e != cudaSuccess) {
+    if (err) *err = std::string("fallback graph launch: ") + cudaGetErrorString(e);
+    return 4;
+  }
+  return 0;
+}
+
+void CholFallbackGraph::destroy() {
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
+  exec = nullptr;
+  graph = nullptr;
+}
+
 }  // namespace traj

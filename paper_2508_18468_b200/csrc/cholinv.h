@@ -40,4 +40,19 @@ int chol_inverse(cudaStream_t st, long long n, cplx* G, long long ldg, long long
                  long long sX, long long batch, void* scratch, int32_t* failed, std::string* err,
                  const CholDist* dist = nullptr, const CholHook* hook = nullptr, const int32_t* gate = nullptr);
 
+// CholeskyQR2's second-pass fallback as one CUDA graph: a decide node (any trajectory's max|G2 - I|,
+// the bit pattern in dev[t], above thr) sets the condition of an IF node whose body is the captured
+// chol_inverse(n) of these buffers.  One graph launch per step instead of the factorisation's
+// ~640 gated kernel launches; the body runs only when needed.  build() returns non-zero when the
+// runtime cannot build it (the caller keeps the gated launches).
+struct CholFallbackGraph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int build(long long n, cplx* G, long long ldg, long long sG, cplx* X, long long ldx, long long sX, long long batch,
+            void* scratch, int32_t* failed, const unsigned long long* dev, double thr, unsigned long long* fallbacks,
+            std::string* err);
+  int launch(cudaStream_t st, std::string* err);
+  void destroy();
+};
+
 }  // namespace traj

@@ -209,7 +209,7 @@ __global__ void strassen_b_kernel(const cplx* __restrict__ U, long long ldu, lon
 // (P1 - P2) + i (P3 - P1 - P2)
 template <int LV>
 __global__ void strassen_c_kernel(const double* __restrict__ Mb, long long ldb, int h, int nh, int T,
-                                  cplx* __restrict__ U, long long ldu, long long sU) {
+                                  cplx* __restrict__ U, long long ldu, long long sU, int accumulate) {
   constexpr int G = 1 << LV, NS = LV == 1 ? 7 : 49;
   const int t = blockIdx.z, i = blockIdx.y;
   const long long bs = (long long)T * h * ldb;
@@ -256,9 +256,16 @@ __global__ void strassen_c_kernel(const double* __restrict__ Mb, long long ldb, 
 #pragma unroll
     for (int R = 0; R < G; ++R)
 #pragma unroll
-      for (int C = 0; C < G; ++C)
-        u[(long long)(R * h + i) * ldu + C * nh + j] =
-            make_double2(c[0][R][C] - c[1][R][C], c[2][R][C] - c[0][R][C] - c[1][R][C]);
+      for (int C = 0; C < G; ++C) {
+        cplx* p = u + (long long)(R * h + i) * ldu + C * nh + j;
+        double2 v = make_double2(c[0][R][C] - c[1][R][C], c[2][R][C] - c[0][R][C] - c[1][R][C]);
+        if (accumulate) {
+          const double2 o = *p;
+          v.x += o.x;
+          v.y += o.y;
+        }
+        *p = v;
+      }
   }
 }
 
@@ -289,11 +296,11 @@ int strassen_b(cudaStream_t st, int levels, const cplx* U, long long ldu, long l
 }
 
 int strassen_c(cudaStream_t st, int levels, const double* Mb, long long ldb, int L, int N, int T, cplx* U,
-               long long ldu, long long sU, std::string* err) {
+               long long ldu, long long sU, std::string* err, int accumulate) {
   const int h = L >> levels, nh = N >> levels;
   dim3 grid((unsigned)std::min<long long>(ceil_div(nh, 256), 16), h, T);
-  if (levels == 2) strassen_c_kernel<2><<<grid, 256, 0, st>>>(Mb, ldb, h, nh, T, U, ldu, sU);
-  else strassen_c_kernel<1><<<grid, 256, 0, st>>>(Mb, ldb, h, nh, T, U, ldu, sU);
+  if (levels == 2) strassen_c_kernel<2><<<grid, 256, 0, st>>>(Mb, ldb, h, nh, T, U, ldu, sU, accumulate);
+  else strassen_c_kernel<1><<<grid, 256, 0, st>>>(Mb, ldb, h, nh, T, U, ldu, sU, accumulate);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess && err) *err = std::string("strassen_c: ") + cudaGetErrorString(e);

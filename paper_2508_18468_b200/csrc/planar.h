@@ -28,13 +28,13 @@ int combine_gram(cudaStream_t st, const double* Pl, long long ldp, long long ps,
 // Strassen on each planar product, `levels` = 1 or 2 (planar.cu), leaf grid h = L / 2^levels,
 // nh = N / 2^levels, NS = 7^levels products per plane: Ks [3][NS][h][ldks] = K's operands (once);
 // Bc [3][NS][T][h][ldb] = U's operands; U[t] = the recombined product from Mb (Bc's layout).
-// L divisible by 2^(levels+1).
+// K is L x L, U L x N: L and N divisible by 2^levels.
 int strassen_k(cudaStream_t st, int levels, const double* Kp, long long ldk, long long pk, int L, double* Ks,
                long long ldks, std::string* err);
 int strassen_b(cudaStream_t st, int levels, const cplx* U, long long ldu, long long sU, int L, int N, int T,
                double* Bc, long long ldb, std::string* err);
 int strassen_c(cudaStream_t st, int levels, const double* Mb, long long ldb, int L, int N, int T, cplx* U,
-               long long ldu, long long sU, std::string* err);
+               long long ldu, long long sU, std::string* err, int accumulate = 0);   // accumulate: U +=
 
 // the column panel [c0, c1) of the Gram, rows [0, c1), combined from the planes Pl[0..2] into the
 // contiguous buf [c1][w] (upper triangle; zeros below the diagonal) for a packed allreduce

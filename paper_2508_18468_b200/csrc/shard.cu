@@ -247,6 +247,21 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
     sh->planar = !banded && !(pk && pk[0] == '0') && !(pc && pc[0] == '0') && N >= min_n && (L / P) % 2 == 0;
     sh->ldKs = round_up(L, 16);
     sh->ldPs = round_up(N, 16);
+    if (sh->planar) {
+      // the unsharded rule (traj_api.cu carve) on the Lp x Lp chunks
+      const char* sv = getenv("TRAJ_STRASSEN");
+      const char* sm = getenv("TRAJ_STRASSEN_MIN_N");
+      const char* lv = getenv("TRAJ_STRASSEN_LEVELS");
+      const long long smin = sm ? atoll(sm) : 2048, Lp = L / P;
+      const bool one_ok = !(sv && sv[0] == '0') && Lp % 2 == 0 && N % 2 == 0 && N >= smin;
+      const bool two_ok = one_ok && Lp % 4 == 0 && N % 4 == 0 &&
+                          147.0 * P * (Lp / 4) * round_up(Lp / 4, 16) * 8 * sh->comm.P_local <= 24e9;
+      sh->slv = !one_ok ? 0 : (lv ? (atoi(lv) >= 2 && two_ok ? 2 : 1) : (two_ok && N >= 4096 ? 2 : 1));
+      if (sh->slv) {
+        sh->ldS = round_up(Lp >> sh->slv, 16);
+        sh->ldSM = round_up(N >> sh->slv, 16);
+      }
+    }
   }
   sh->loc.assign(sh->comm.P_local, ShardLocal());
   lay.take(sh->Ufull, (size_t)L * ldN * 16);
@@ -261,6 +276,8 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
       lay.take(l.Uext, (size_t)(Lp + 2 * sh->H) * ldN * 16);
     } else if (sh->planar) {
       lay.take(l.Kp, (size_t)3 * Lp * sh->ldKs * 8);
+      if (sh->slv)
+        lay.take(l.Ks, (size_t)P * 3 * (sh->slv == 2 ? 49 : 7) * (Lp >> sh->slv) * sh->ldS * 8);
       lay.take(l.Pp, (size_t)3 * Lp * sh->ldPs * 8);
       lay.take(l.Up6, (size_t)6 * Lp * sh->ldPs * 8);
     } else {
@@ -279,6 +296,11 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
     }
   }
   if (banded) lay.take(sh->bcoef, (size_t)(2 * Wx + 2 * Wy + 2) * 16);
+  if (sh->slv) {
+    const size_t nb = (size_t)3 * (sh->slv == 2 ? 49 : 7) * (Lp >> sh->slv) * sh->ldSM * 8;
+    lay.take(sh->Sb, nb);
+    lay.take(sh->Sm, nb);
+  }
   if (sh->planar) {
     lay.take(sh->Cp, (size_t)3 * Lp * sh->ldPs * 8);
     lay.take(sh->Gp, (size_t)3 * N * sh->ldPs * 8);
@@ -478,6 +500,12 @@ int shard_build(ShardedCtx* sh, const std::vector<std::complex<double>>& kc, con
       if (build_k_planar(st, l.Kp, sh->ldKs, (long long)sh->Lp * sh->ldKs, sh->Lx, sh->Ly, sh->kcoef,
                          sh->kcoef + sh->Lx, err, l.row0, sh->Lp))
         return 4;
+      // the Strassen operands of every chunk K_g[:, s] (Lp x Lp at column s Lp of the planes)
+      const long long ns = 3 * (sh->slv == 2 ? 49 : 7), hh = sh->Lp >> sh->slv;
+      for (int c = 0; sh->slv && c < sh->P; ++c)
+        if (strassen_k(st, sh->slv, l.Kp + (long long)c * sh->Lp, sh->ldKs, (long long)sh->Lp * sh->ldKs, sh->Lp,
+                       l.Ks + c * ns * hh * sh->ldS, sh->ldS, err))
+          return 4;
     } else if (!sh->banded &&
                build_k(st, l.K, sh->ldL, sh->Lx, sh->Ly, sh->kcoef, sh->kcoef + sh->Lx, err, l.row0, sh->Lp)) {
       return 4;
@@ -600,11 +628,23 @@ int cqr2(ShardedCtx* sh, int src_which, std::string* err) {
         // decided on the device from the all-reduced G2 (the same bits on every rank): the
         // first-order factor, overwritten by the gated full factorisation when it is needed
         // (replicated, not distributed: a gated-off step must not move the Cholesky's broadcasts)
+        const double thr = 1e-9 / sqrt((double)sh->N);
         STRY(gram_deviation(sh->st, sh->G, sh->ldN, 0, sh->N, 1, sh->gdev, err));
-        STRY(cqr2_decide(sh->st, sh->gdev, 1, 1e-9 / sqrt((double)sh->N), sh->gate, sh->fb_dev, err));
         STRY(first_order_inverse(sh->st, sh->G, sh->ldN, 0, sh->X, sh->ldN, 0, sh->N, 1, err));
-        STRY(chol_inverse(sh->st, sh->N, sh->G, sh->ldN, 0, sh->X, sh->ldN, 0, 1, sh->chol_scratch, sh->failed_dev,
-                          err, nullptr, nullptr, sh->gate));
+        if (sh->fbg_state == 0) {
+          const char* fg = getenv("TRAJ_FALLBACK_GRAPH");
+          std::string e2;
+          sh->fbg_state = (fg && fg[0] == '0') || sh->fbg.build(sh->N, sh->G, sh->ldN, 0, sh->X, sh->ldN, 0, 1,
+                                                                 sh->chol_scratch, sh->failed_dev, sh->gdev, thr,
+                                                                 sh->fb_dev, &e2) ? -1 : 1;
+        }
+        if (sh->fbg_state == 1) {
+          STRY(sh->fbg.launch(sh->st, err));
+        } else {
+          STRY(cqr2_decide(sh->st, sh->gdev, 1, thr, sh->gate, sh->fb_dev, err));
+          STRY(chol_inverse(sh->st, sh->N, sh->G, sh->ldN, 0, sh->X, sh->ldN, 0, 1, sh->chol_scratch,
+                            sh->failed_dev, err, nullptr, nullptr, sh->gate));
+        }
       }
       if (full && pass == 0 && sh->chol_overlap && sh->N > 64) {
         // factorise on st_hi; each newly final left column block's TRMM runs on st_lo
@@ -852,14 +892,26 @@ int propagate_banded(ShardedCtx* sh, int cur, int nxt, std::string* err) {
 // TRAJ_SHARD_OVERLAP=0: one allgather, then one L-deep GEMM.
 // planar 3M chunk: P_q (+)= K_g[:, s]_q U_s,q for the three products (one batch-3 launch), U_s split
 // into (re, im, re + im) planes first
-int planar_chunk(ShardedCtx* sh, ShardLocal& l, const cplx* Us, int s, bool accumulate, std::string* err) {
+int planar_chunk(ShardedCtx* sh, ShardLocal& l, const cplx* Us, int s, bool accumulate, std::string* err,
+                 int nxt = -1) {
   const long long Lp = sh->Lp, psC = Lp * sh->ldPs;
+  if (sh->slv) {
+    // Strassen on the chunk product K_g[:, s] U_s, accumulated into U_g' directly by the recombination
+    const int np = 3 * (sh->slv == 2 ? 49 : 7);
+    const long long hh = Lp >> sh->slv, nh = sh->N >> sh->slv, bK = hh * sh->ldS, bM = hh * sh->ldSM;
+    STRY(strassen_b(sh->st, sh->slv, Us, sh->ldN, 0, (int)Lp, sh->N, 1, sh->Sb, sh->ldSM, err));
+    STRY(dgemm(sh->st, 0, hh, nh, hh, 1.0, l.Ks + s * np * bK, sh->ldS, bK, sh->Sb, sh->ldSM, bM, 0.0, sh->Sm,
+               sh->ldSM, bM, np, 0, err));
+    return strassen_c(sh->st, sh->slv, sh->Sm, sh->ldSM, (int)Lp, sh->N, 1, l.U[nxt], sh->ldN, 0, err,
+                      accumulate ? 1 : 0);
+  }
   STRY(split_planes(sh->st, Us, sh->ldN, 0, (int)Lp, sh->N, 1, sh->Cp, sh->ldPs, psC, 0, err));
   return dgemm(sh->st, 0, Lp, sh->N, Lp, 1.0, l.Kp + (long long)s * Lp, sh->ldKs, Lp * sh->ldKs, sh->Cp, sh->ldPs, psC,
                accumulate ? 1.0 : 0.0, l.Pp, sh->ldPs, psC, 3, 0, err);
 }
 
 int planar_finish(ShardedCtx* sh, ShardLocal& l, int nxt, std::string* err) {
+  if (sh->slv) return 0;   // the Strassen recombination wrote U_g' already
   const long long psC = (long long)sh->Lp * sh->ldPs;
   return combine_planes(sh->st, l.Pp, sh->ldPs, psC, 0, sh->Lp, sh->N, 1, l.U[nxt], sh->ldN, 0, err);
 }
@@ -875,7 +927,7 @@ int propagate_dense(ShardedCtx* sh, int cur, int nxt, std::string* err) {
       for (int d = 0; d < sh->P; ++d) {
         const int s = (l.g - d + sh->P) % sh->P;
         const cplx* Us = sh->P > 1 ? sh->Ufull + (size_t)s * Lp * ld : l.U[cur];
-        STRY(planar_chunk(sh, l, Us, s, d > 0, err));
+        STRY(planar_chunk(sh, l, Us, s, d > 0, err, nxt));
       }
       STRY(planar_finish(sh, l, nxt, err));
     }
@@ -921,7 +973,7 @@ int propagate_dense(ShardedCtx* sh, int cur, int nxt, std::string* err) {
         SCK(cudaStreamWaitEvent(st, sh->ev_chunk[d], 0));
         Us = sh->Ufull + (size_t)s * Lp * ld;
       }
-      if (sh->planar) STRY(planar_chunk(sh, l, Us, s, d > 0, err));
+      if (sh->planar) STRY(planar_chunk(sh, l, Us, s, d > 0, err, nxt));
       else
         STRY(zgemm(st, 0, 0, Lp, sh->N, Lp, 1.0, 0.0, l.K + (size_t)s * Lp, sh->ldL, 0, Us, ld, 0, d ? 1.0 : 0.0,
                    l.U[nxt], ld, 0, 1, 0, err));
@@ -1113,6 +1165,7 @@ void shard_destroy(ShardedCtx* sh) {
     if (e) cudaEventDestroy(e);
   for (auto e : sh->ev_chunk)
     if (e) cudaEventDestroy(e);
+  sh->fbg.destroy();
   const bool aborted = sh->comm.wd.stop();   // an aborted communicator is already freed
   if (sh->comm.comm && !aborted) ncclCommDestroy(sh->comm.comm);
   if (sh->h_small) cudaFreeHost(sh->h_small);

@@ -48,6 +48,7 @@ struct ShardLocal {
   cplx* Uext = nullptr;    // banded: (H + Lp + H) x ldN, halo rows around the local block
   // planar 3M (dense K): K_g's planes [3][Lp][ldKs], product planes [3][Lp][ldPs], U's six planes
   double *Kp = nullptr, *Pp = nullptr, *Up6 = nullptr;
+  double* Ks = nullptr;    // Strassen: the operands of every K chunk K_g[:, s], [P][3 7^lv][Lp/2^lv][ldS]
 };
 
 struct ShardedCtx {
@@ -88,6 +89,8 @@ struct ShardedCtx {
   long long last_nS = 0, last_n1 = 0, cqr2_fallbacks = 0;
   unsigned long long* fb_dev = nullptr;   // second passes that took the full factorisation (device count)
   int32_t* gate = nullptr;                // this step's second-pass decision (device)
+  CholFallbackGraph fbg;                  // the decision + the conditional factorisation as one graph
+  int fbg_state = 0;                      // 0: not built yet, 1: built, -1: gated launches
   bool k1_dev = false;                    // the last step's occupied count is in k1 (device)
   std::vector<int32_t> hcnt;              // per-shard click counts of the current step (host Philox)
   // CholeskyQR pass 1 on the structure G = I - V^dag V (structchol.h; TRAJ_STRUCT_CHOL=0: dense):
@@ -119,6 +122,11 @@ struct ShardedCtx {
   // planar 3M for K_g U and the local Gram / TRMM (TRAJ_PLANAR_KU / TRAJ_PLANAR_CQR, N >= TRAJ_PLANAR_MIN_N)
   bool planar = false;
   long long ldKs = 0, ldPs = 0;
+  // Strassen (slv levels) on each K-chunk product K_g[:, s] U_s (TRAJ_STRASSEN=0: off): U_s's operands
+  // Sb and the leaf products Sm [3 7^lv][Lp/2^lv][ldSM], shared by the chunks
+  int slv = 0;
+  long long ldS = 0, ldSM = 0;
+  double *Sb = nullptr, *Sm = nullptr;
   double *Cp = nullptr, *Gp = nullptr, *Xp = nullptr;   // chunk planes [3][Lp], Gram / X planes [3][N]
   cplx* dist_scratch = nullptr;
   size_t dist_scratch_bytes = 0;

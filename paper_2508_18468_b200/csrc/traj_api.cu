@@ -130,6 +130,8 @@ struct traj_ctx {
   long long cqr2_fallbacks = 0;
   unsigned long long* fb_dev = nullptr;  // CholeskyQR2 second passes that took the full factorisation
   int32_t* gate = nullptr;               // [1]: this step's second-pass decision (device)
+  CholFallbackGraph fbg;                 // the decision + the conditional factorisation as one graph
+  int fbg_state = 0;                     // 0: not built yet, 1: built, -1: unavailable (gated launches)
   std::vector<int32_t> hcount;           // host click counts of the current step (host Philox)
   bool k1_dev = false;                   // the last projective step's occupied counts are in k1 (device)
   const int32_t* lr_kdev = nullptr;      // device bound of pass 1's V rows (k0), with lr_k0 its capacity
@@ -579,11 +581,23 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
         // second pass: G2 = I + E; the first-order factor unless N max|E|^2 >= 1e-18 for some
         // trajectory -- decided on the device (no host round trip): the first-order X is written,
         // then the full factorisation, gated on that decision, overwrites it when needed
+        const double thr = 1e-9 / sqrt((double)h->N);
         TRY(gram_deviation(h->st, h->G, h->ldN, h->sG, h->N, h->T, h->gdev, &h->err));
-        TRY(cqr2_decide(h->st, h->gdev, h->T, 1e-9 / sqrt((double)h->N), h->gate, h->fb_dev, &h->err));
         TRY(first_order_inverse(h->st, h->G, h->ldN, h->sG, h->X, h->ldN, h->sG, h->N, h->T, &h->err));
-        TRY(chol_inverse(h->st, h->N, h->G, h->ldN, h->sG, h->X, h->ldN, h->sG, h->T, h->chol_scratch,
-                         h->failed_dev, &h->err, nullptr, nullptr, h->gate));
+        if (h->fbg_state == 0) {   // built once: the fallback factorisation as a conditional graph node
+          const char* fg = getenv("TRAJ_FALLBACK_GRAPH");
+          std::string e2;
+          h->fbg_state = (fg && fg[0] == '0') || h->fbg.build(h->N, h->G, h->ldN, h->sG, h->X, h->ldN, h->sG, h->T,
+                                                               h->chol_scratch, h->failed_dev, h->gdev, thr,
+                                                               h->fb_dev, &e2) ? -1 : 1;
+        }
+        if (h->fbg_state == 1) {
+          TRY(h->fbg.launch(h->st, &h->err));
+        } else {   // the same decision, every kernel of the factorisation gated on it
+          TRY(cqr2_decide(h->st, h->gdev, h->T, thr, h->gate, h->fb_dev, &h->err));
+          TRY(chol_inverse(h->st, h->N, h->G, h->ldN, h->sG, h->X, h->ldN, h->sG, h->T, h->chol_scratch,
+                           h->failed_dev, &h->err, nullptr, nullptr, h->gate));
+        }
       }
       if (full && h->chol_overlap && h->st_hi && h->N > 64) {
         // fork: factorise on st_hi; as each left-edge block X[0:h, 0:h] is queued, st_lo runs the
@@ -1833,6 +1847,7 @@ int traj_destroy(traj_handle h) {
     delete h->sh;
   }
   h->prof.destroy();
+  h->fbg.destroy();
   for (cudaStream_t q : {h->st_hi, h->st_lo})
     if (q) {
       cudaStreamSynchronize(q);

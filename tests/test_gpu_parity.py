@@ -269,6 +269,31 @@ def test_strassen_propagator_matches_oracle(P, monkeypatch, Lx, Ly, protocol, ga
             assert a.last_clicks(t) == b.last_clicks(t)
 
 
+@pytest.mark.parametrize("levels,shards,protocol", [(1, 2, "projective"), (2, 2, "homodyne"), (1, 4, "homodyne"),
+                                                   (2, 4, "projective")])
+def test_row_sharded_strassen_chunks_match_oracle(P, monkeypatch, levels, shards, protocol):
+    """Strassen on every K-chunk product K_g[:, s] U_s of the row-sharded propagate (the chunk operands
+    formed once per shard, the recombination accumulating over the ring-ordered chunks): the same state
+    as the plain chunk products (1e-12) and the oracle (1e-10), P = 2 and 4 emulated shards."""
+    L, steps, gam = 256, 8, (3.0 if protocol == "projective" else 1.0)
+    monkeypatch.setenv("TRAJ_PLANAR_MIN_N", "0")
+    monkeypatch.setenv("TRAJ_STRASSEN_MIN_N", "0")
+    monkeypatch.setenv("TRAJ_STRASSEN_LEVELS", str(levels))
+    a = P.Trajectories(L, 1, protocol, [gam], seed=19, shard_size=shards)
+    monkeypatch.setenv("TRAJ_STRASSEN", "0")
+    b = P.Trajectories(L, 1, protocol, [gam], seed=19, shard_size=shards)
+    o = OracleTrajectory(L, 1, protocol, gam, 0.05, seed=19, traj=0, K=lattice.propagator_lattice(L, 1, 1.0, 0.05))
+    for s in range(steps):
+        a.step(1)
+        b.step(1)
+        o.step(1)
+    Ca, Cb = a.correlation(0).cpu().numpy(), b.correlation(0).cpu().numpy()
+    assert np.abs(Ca - Cb).max() < 1e-12
+    assert np.abs(Ca - o.correlation()).max() < C_TOL
+    if protocol == "projective":
+        assert a.last_clicks(0) == b.last_clicks(0) == (o.last_clicks[0].size, int(o.last_clicks[1].sum()))
+
+
 @pytest.mark.parametrize("block,shards", [(128, 1), (64, 1), (64, 2)])
 def test_structured_pass1_matches_dense_factorisation(P, monkeypatch, block, shards):
     """CholeskyQR pass 1 of a projective step on the structure of G = I - V^dag V (csrc/structchol.cu):
