@@ -360,7 +360,7 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
     lay.take(sh->W, (size_t)N * ldcap * 16);
     // structured CholeskyQR pass 1 (structchol.h): Y [cap][b], C [b][b], X blocks [N][b], W, Z [cap][ldN]
     const char* sbv = getenv("TRAJ_STRUCT_B");
-    const int b = sbv ? std::max(16, std::min(1024, atoi(sbv) / 16 * 16)) : 128;
+    const int b = sbv ? std::max(16, std::min(1024, atoi(sbv) / 16 * 16)) : (cap >= 1024 ? 512 : 128);
     sh->sc.b = b;
     sh->sc.N = (int)N;
     sh->sc.T = 1;

@@ -405,8 +405,11 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     }
     {   // structured CholeskyQR pass 1 (structured_pass1): Y [cap][sb], C [sb][sb], the blocks' R^-1
         // [N][sb], W = V X and Z = M W [cap][ldN]
+      // wider blocks when many rows are zeroed (c5: k0 ~ 1800): the solve's L x b x k0 products fill
+      // the GPU better and the factor has fewer sequential blocks (measured: c5 chol phase 399 ms at
+      // b = 128, 306 ms at 512; c3 flat from 128 to 512)
       const char* sbv = getenv("TRAJ_STRUCT_B");
-      h->sb = sbv ? std::max(16, std::min(1024, atoi(sbv) / 16 * 16)) : 128;
+      h->sb = sbv ? std::max(16, std::min(1024, atoi(sbv) / 16 * 16)) : (cap >= 1024 ? 512 : 128);
       const long long b = h->sb;
       lay.take(h->sY, (size_t)T * cap * b * 16);
       lay.take(h->sC, (size_t)T * b * b * 16);
