@@ -367,7 +367,7 @@ def strassen_levels(w, P: int = 1) -> int:
     lv = os.environ.get("TRAJ_STRASSEN_LEVELS")
     if lv:
         return 2 if int(lv) >= 2 and two_ok else 1
-    return 2 if two_ok and w.N >= 4096 else 1
+    return 2 if two_ok else 1
 
 
 def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P):

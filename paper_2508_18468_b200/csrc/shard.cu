@@ -256,7 +256,7 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
       const bool one_ok = !(sv && sv[0] == '0') && Lp % 2 == 0 && N % 2 == 0 && N >= smin;
       const bool two_ok = one_ok && Lp % 4 == 0 && N % 4 == 0 &&
                           147.0 * P * (Lp / 4) * round_up(Lp / 4, 16) * 8 * sh->comm.P_local <= 24e9;
-      sh->slv = !one_ok ? 0 : (lv ? (atoi(lv) >= 2 && two_ok ? 2 : 1) : (two_ok && N >= 4096 ? 2 : 1));
+      sh->slv = !one_ok ? 0 : (lv ? (atoi(lv) >= 2 && two_ok ? 2 : 1) : (two_ok ? 2 : 1));
       if (sh->slv) {
         sh->ldS = round_up(Lp >> sh->slv, 16);
         sh->ldSM = round_up(N >> sh->slv, 16);

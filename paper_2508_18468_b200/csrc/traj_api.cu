@@ -320,10 +320,11 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     const long long smin = sm ? atoll(sm) : 2048;
     h->strassen = !(sv && sv[0] == '0') && L % 4 == 0 && N >= smin;
     if (h->strassen) {
-      // two levels when K's 147 quarter operands fit 24 GB (c3: 19.7 GB) and N >= 4096, else one
+      // two levels when K's 147 quarter operands fit 24 GB (c3: 19.7 GB, c4: 1.2 GB; c4 391 vs 401 ms
+      // per step with one level, c2 (N = 1024) is below TRAJ_STRASSEN_MIN_N), else one (c5)
       const char* lv = getenv("TRAJ_STRASSEN_LEVELS");
       const bool two_ok = L % 8 == 0 && 147.0 * (L / 4) * round_up(L / 4, 16) * 8 <= 24e9;
-      h->slv = lv ? (atoi(lv) >= 2 && two_ok ? 2 : 1) : (two_ok && N >= 4096 ? 2 : 1);
+      h->slv = lv ? (atoi(lv) >= 2 && two_ok ? 2 : 1) : (two_ok ? 2 : 1);
       const long long hh = L >> h->slv, ns = 3 * (h->slv == 2 ? 49 : 7);
       h->ldS = round_up(hh, 16);
       h->ldM = round_up(N >> h->slv, 16);
