@@ -355,19 +355,18 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def strassen_levels(w, P: int = 1) -> int:
+def strassen_levels(w, P: int = 1, T: int = 1) -> int:
     """Strassen levels of the planar K U (the rule of csrc/traj_api.cu carve(); row-sharded over P GPUs:
-    csrc/shard.cu's rule on the Lp x Lp chunks K_g[:, s], Lp = L / P)."""
+    csrc/shard.cu's rule on the Lp x Lp chunks K_g[:, s], Lp = L / P, at most two levels)."""
     Lp = w.L // P
     if (os.environ.get("TRAJ_STRASSEN", "1") == "0" or Lp % 2 or w.N % 2
             or w.N < int(os.environ.get("TRAJ_STRASSEN_MIN_N", "2048"))):
         return 0
-    q = Lp // 4
-    two_ok = Lp % 4 == 0 and w.N % 4 == 0 and 147.0 * P * q * ((q + 15) // 16 * 16) * 8 <= 24e9
-    lv = os.environ.get("TRAJ_STRASSEN_LEVELS")
-    if lv:
-        return 2 if int(lv) >= 2 and two_ok else 1
-    return 2 if two_ok else 1
+    r16 = lambda x: (x + 15) // 16 * 16
+    two_ok = Lp % 4 == 0 and w.N % 4 == 0 and 147.0 * P * (Lp // 4) * r16(Lp // 4) * 8 <= 24e9
+    three_ok = P == 1 and T == 1 and w.L % 16 == 0 and 1029.0 * (w.L // 8) * r16(w.L // 8) * 8 <= 40e9
+    want = int(os.environ.get("TRAJ_STRASSEN_LEVELS", "3"))
+    return 3 if want >= 3 and three_ok else (2 if want >= 2 and two_ok else 1)
 
 
 def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P):
@@ -392,7 +391,7 @@ def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P):
               and w.protocol in ("projective", "homodyne")
               and (not shard or os.environ.get("TRAJ_PLANAR_CQR", "1") != "0"))
     planar_cqr = big and os.environ.get("TRAJ_PLANAR_CQR", "1") != "0" and (not shard or planar)
-    slv = strassen_levels(w, w.L // rows) if planar else 0
+    slv = strassen_levels(w, w.L // rows, tpg) if planar else 0
     strassen = slv > 0
     ku_name = (f"dgemm_dmma_kernel x{3 * 7 ** slv} (planar 3M: Kr Ur, Ki Ui, (Kr+Ki)(Ur+Ui), each by {slv} "
                f"Strassen level(s): {7 ** slv} products of 1/{2 ** slv} size; 128x128 CTA, one batched launch) + "

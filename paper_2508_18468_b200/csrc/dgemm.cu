@@ -29,6 +29,7 @@ struct DArgs {
   int M, N, K;
   int tiles_m, tiles_n;
   int a_batched, b_batched;
+  int a_div;               // batch entries per A entry (A_z = A entry z / a_div)
   int flags;               // DG_TRI_B_UPPER, DG_C_UPPER (dgemm.h)
   int m_off, n_off;        // global row / column of C(0, 0) for the triangle tests
   double alpha, beta;
@@ -72,7 +73,7 @@ __global__ void __launch_bounds__(DTHREADS, 1)
   }
   __syncthreads();
   const bool issuer = warp == 0 && lane == 0;
-  const int za = args.a_batched ? z : 0, zb = args.b_batched ? z : 0;
+  const int za = args.a_batched ? z / args.a_div : 0, zb = args.b_batched ? z : 0;
   auto issue = [&](int it) {
     const int s = it % DSTAGES;
     mbar_arrive_expect_tx(&full[s], DSTAGE);
@@ -186,7 +187,7 @@ PFN_encode_t encode_fn() {
 int dgemm(cudaStream_t st, int opA, long long M, long long N, long long K, double alpha, const double* A,
           long long lda, long long strideA, const double* B, long long ldb, long long strideB, double beta, double* C,
           long long ldc, long long strideC, long long batch, int flags, std::string* err, long long m_off,
-          long long n_off) {
+          long long n_off, int a_div) {
   if (M <= 0 || N <= 0 || batch <= 0) return 0;
   if (K <= 0 || (lda & 1) || (ldb & 15) || round_up(N, 16) > ldb || (ldc & 1) ||
       (opA == 1 && ((lda & 15) || round_up(M, 16) > lda)) || (opA != 0 && opA != 1) ||
@@ -200,10 +201,15 @@ int dgemm(cudaStream_t st, int opA, long long M, long long N, long long K, doubl
     if (err) *err = "dgemm: cuTensorMapEncodeTiled unavailable";
     return 4;
   }
-  const bool ab = strideA != 0 && batch > 1, bb = strideB != 0 && batch > 1;
+  if (a_div < 1 || batch % a_div) {
+    if (err) *err = "dgemm: a_div must divide the batch";
+    return 1;
+  }
+  const long long na = batch / a_div;   // A entries
+  const bool ab = strideA != 0 && na > 1, bb = strideB != 0 && batch > 1;
   CUtensorMap ma, mb;
   if (opA == 0) {
-    cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)M, (cuuint64_t)(ab ? batch : 1)};
+    cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)M, (cuuint64_t)(ab ? na : 1)};
     cuuint64_t strides[2] = {(cuuint64_t)(lda * 8), (cuuint64_t)((ab ? strideA : lda * M) * 8)};
     cuuint32_t box[3] = {DBK, DBM, 1};
     cuuint32_t es[3] = {1, 1, 1};
@@ -214,7 +220,7 @@ int dgemm(cudaStream_t st, int opA, long long M, long long N, long long K, doubl
       return 4;
     }
   } else {   // A stored [K][M]: 16-column chunks of m, like B
-    cuuint64_t dims[4] = {16, (cuuint64_t)K, (cuuint64_t)ceil_div(M, 16), (cuuint64_t)(ab ? batch : 1)};
+    cuuint64_t dims[4] = {16, (cuuint64_t)K, (cuuint64_t)ceil_div(M, 16), (cuuint64_t)(ab ? na : 1)};
     cuuint64_t strides[3] = {(cuuint64_t)(lda * 8), 128, (cuuint64_t)((ab ? strideA : lda * K) * 8)};
     cuuint32_t box[4] = {16, DBK, DBM / 16, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
@@ -244,6 +250,7 @@ int dgemm(cudaStream_t st, int opA, long long M, long long N, long long K, doubl
   args.tiles_m = (int)ceil_div(M, DBM);
   args.tiles_n = (int)ceil_div(N, DBN);
   args.a_batched = ab;
+  args.a_div = a_div;
   args.b_batched = bb;
   args.flags = flags;
   args.m_off = (int)m_off;

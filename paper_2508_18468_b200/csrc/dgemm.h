@@ -17,7 +17,7 @@ enum { DG_TRI_B_UPPER = 4, DG_C_UPPER = 16 };   // the values of zgemm.h's TRAJ_
 int dgemm(cudaStream_t st, int opA, long long M, long long N, long long K, double alpha, const double* A,
           long long lda, long long strideA, const double* B, long long ldb, long long strideB, double beta, double* C,
           long long ldc, long long strideC, long long batch, int flags, std::string* err, long long m_off = 0,
-          long long n_off = 0);
+          long long n_off = 0, int a_div = 1);   // a_div: batch entries per A entry (A_z = A entry z / a_div)
 
 inline int dgemm_nn(cudaStream_t st, long long M, long long N, long long K, double alpha, const double* A,
                     long long lda, long long strideA, const double* B, long long ldb, long long strideB, double beta,

@@ -115,13 +115,13 @@ __global__ void pack_gram_panel_kernel(const double* __restrict__ Pl, long long 
   }
 }
 
-// Strassen's algorithm on every real product of the planar 3M propagator, LV = 1 or 2 levels.  With
+// Strassen's algorithm on every real product of the planar 3M propagator, LV = 1, 2 or 3 levels.  With
 // A = K's plane q and B = U's plane q in 2 x 2 blocks:
 //   M1 = (A11 + A22)(B11 + B22)  M2 = (A21 + A22) B11  M3 = A11 (B12 - B22)  M4 = A22 (B21 - B11)
 //   M5 = (A11 + A12) B22         M6 = (A21 - A11)(B11 + B12)             M7 = (A12 - A22)(B21 + B22)
 //   C11 = M1 + M4 - M5 + M7,  C12 = M3 + M5,  C21 = M2 + M4,  C22 = M1 - M2 + M3 + M6
 // -- seven half-size products instead of eight; applied again to each of the seven (LV = 2), 49
-// quarter-size products instead of 64.  The operand / recombination coefficients over the 2 x 2
+// quarter-size products instead of 64; once more (LV = 3), 343 eighth-size products instead of 512.  The operand / recombination coefficients over the 2 x 2
 // blocks (11, 12, 21, 22) are the tables below; one thread handles one element of the leaf grid and
 // all 2^LV x 2^LV positions it stands for, so each pass reads and writes every matrix once.  K's
 // operands are formed once (strassen_k), U's per step (strassen_b), the leaf products are
@@ -133,37 +133,82 @@ __constant__ int8_t kSB[7][4] = {{1, 0, 0, 1}, {1, 0, 0, 0}, {0, 1, 0, -1}, {-1,
 __constant__ int8_t kSC[4][7] = {{1, 0, 0, 1, -1, 0, 1}, {0, 0, 1, 0, 1, 0, 0},
                                  {0, 1, 0, 1, 0, 0, 0}, {1, -1, 1, 0, 0, 1, 0}};
 
-// the 7^LV operands of a matrix given on its 2^LV x 2^LV grid of leaf blocks x[R][C] (one element each)
 template <int LV>
-__device__ __forceinline__ void strassen_operands(const double (&x)[1 << LV][1 << LV], const int8_t (&co)[7][4],
-                                                  double* out, long long bs) {
-  if (LV == 1) {
+struct P7 {
+  static constexpr int v = 7 * P7<LV - 1>::v;
+};
+template <>
+struct P7<0> {
+  static constexpr int v = 1;
+};
+
+// the 7^LV operands of a matrix given on its 2^LV x 2^LV grid of leaf blocks x[R][C] (one element each):
+// operand s1 of the top split over the four half-blocks, then recursively its 7^(LV-1) operands
+template <int LV>
+struct StrassenOps {
+  static __device__ __forceinline__ void run(const double (&x)[1 << LV][1 << LV], const int8_t (&co)[7][4],
+                                             double* out, long long bs) {
+    constexpr int H = 1 << (LV - 1);
 #pragma unroll
-    for (int s = 0; s < 7; ++s)
-      out[s * bs] = co[s][0] * x[0][0] + co[s][1] * x[0][1] + co[s][2] * x[1][0] + co[s][3] * x[1][1];
-  } else {
+    for (int s = 0; s < 7; ++s) {
+      double h[H][H];
 #pragma unroll
-    for (int s1 = 0; s1 < 7; ++s1) {
-      double h[2][2];   // level-1 operand s1 on its 2 x 2 grid of quarter blocks
+      for (int r = 0; r < H; ++r)
 #pragma unroll
-      for (int r = 0; r < 2; ++r)
-#pragma unroll
-        for (int c = 0; c < 2; ++c)
-          h[r][c] = co[s1][0] * x[r][c] + co[s1][1] * x[r][2 + c] + co[s1][2] * x[2 + r][c] +
-                    co[s1][3] * x[2 + r][2 + c];
-#pragma unroll
-      for (int s2 = 0; s2 < 7; ++s2)
-        out[(s1 * 7 + s2) * bs] = co[s2][0] * h[0][0] + co[s2][1] * h[0][1] + co[s2][2] * h[1][0] +
-                                  co[s2][3] * h[1][1];
+        for (int c = 0; c < H; ++c)
+          h[r][c] = co[s][0] * x[r][c] + co[s][1] * x[r][H + c] + co[s][2] * x[H + r][c] + co[s][3] * x[H + r][H + c];
+      StrassenOps<LV - 1>::run(h, co, out + (long long)s * P7<LV - 1>::v * bs, bs);
     }
   }
-}
+};
+template <>
+struct StrassenOps<0> {
+  static __device__ __forceinline__ void run(const double (&x)[1][1], const int8_t (&)[7][4], double* out,
+                                             long long) {
+    out[0] = x[0][0];
+  }
+};
+
+// c[R][C] = the 2^LV x 2^LV blocks of the product recombined from its 7^LV leaf products m[k * bs]
+template <int LV>
+struct StrassenComb {
+  static __device__ __forceinline__ void run(const double* m, long long bs, double (&c)[1 << LV][1 << LV]) {
+    constexpr int H = 1 << (LV - 1);
+#pragma unroll
+    for (int r = 0; r < 2 * H; ++r)
+#pragma unroll
+      for (int q = 0; q < 2 * H; ++q) c[r][q] = 0.0;
+    auto add = [&](int s) {
+      double ch[H][H];
+      StrassenComb<LV - 1>::run(m + (long long)s * P7<LV - 1>::v * bs, bs, ch);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const double k = kSC[b][s];
+#pragma unroll
+        for (int r = 0; r < H; ++r)
+#pragma unroll
+          for (int q = 0; q < H; ++q) c[(b >> 1) * H + r][(b & 1) * H + q] += k * ch[r][q];
+      }
+    };
+    if constexpr (LV >= 3) {   // one top-level product at a time: 49 loads live, not 343
+#pragma unroll 1
+      for (int s = 0; s < 7; ++s) add(s);
+    } else {
+#pragma unroll
+      for (int s = 0; s < 7; ++s) add(s);
+    }
+  }
+};
+template <>
+struct StrassenComb<0> {
+  static __device__ __forceinline__ void run(const double* m, long long, double (&c)[1][1]) { c[0][0] = m[0]; }
+};
 
 // Ks[q][s][i][j] (s < 7^LV) from K's planes: leaf grid h = L / 2^LV
 template <int LV>
 __global__ void strassen_a_kernel(const double* __restrict__ Kp, long long ldk, long long pk, int h,
                                   double* __restrict__ Ks, long long ldks) {
-  constexpr int G = 1 << LV, NS = LV == 1 ? 7 : 49;
+  constexpr int G = 1 << LV, NS = P7<LV>::v;
   const int q = blockIdx.z, i = blockIdx.y;
   const double* k = Kp + q * pk;
   const long long bs = (long long)h * ldks;
@@ -174,15 +219,17 @@ __global__ void strassen_a_kernel(const double* __restrict__ Kp, long long ldk, 
     for (int R = 0; R < G; ++R)
 #pragma unroll
       for (int C = 0; C < G; ++C) x[R][C] = k[(long long)(R * h + i) * ldk + C * h + j];
-    strassen_operands<LV>(x, kSA, o + j, bs);
+    StrassenOps<LV>::run(x, kSA, o + j, bs);
   }
 }
 
-// Bc[q][s][t][i][j]: the operands of the planes (re, im, re + im) of U[t]; leaf grid h x nh
-template <int LV>
+// Bc[q][s][t][i][j]: the operands of the planes (re, im, re + im) of U[t]; leaf grid h x nh.  PL < 0: all
+// three planes in one pass; PL = q: plane q only (the three-level pass, whose 64 positions per thread
+// leave no registers for three planes)
+template <int LV, int PL>
 __global__ void strassen_b_kernel(const cplx* __restrict__ U, long long ldu, long long sU, int h, int nh, int T,
                                   double* __restrict__ Bc, long long ldb) {
-  constexpr int G = 1 << LV, NS = LV == 1 ? 7 : 49;
+  constexpr int G = 1 << LV, NS = P7<LV>::v;
   const int t = blockIdx.z, i = blockIdx.y;
   const cplx* u = U + t * sU;
   const long long bs = (long long)T * h * ldb;          // stride between (q, s) entries
@@ -195,64 +242,52 @@ __global__ void strassen_b_kernel(const cplx* __restrict__ U, long long ldu, lon
       for (int C = 0; C < G; ++C) v[R][C] = u[(long long)(R * h + i) * ldu + C * nh + j];
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
+      if (PL >= 0 && q != PL) continue;
       double x[G][G];
 #pragma unroll
       for (int R = 0; R < G; ++R)
 #pragma unroll
         for (int C = 0; C < G; ++C) x[R][C] = q == 0 ? v[R][C].x : (q == 1 ? v[R][C].y : v[R][C].x + v[R][C].y);
-      strassen_operands<LV>(x, kSB, o + (long long)q * NS * bs + j, bs);
+      StrassenOps<LV>::run(x, kSB, o + (long long)q * NS * bs + j, bs);
     }
   }
 }
 
-// U[t] from the leaf products: per plane the 2^LV x 2^LV blocks of the product, then
-// (P1 - P2) + i (P3 - P1 - P2)
-template <int LV>
+// U[t] (+)= the product recombined from the leaf products: per plane the 2^LV x 2^LV blocks, then
+// (P1 - P2) + i (P3 - P1 - P2).  PL < 0: all planes; PL = q: plane q's share only, added to U
+// (plane 0 writes or accumulates per `accumulate`, planes 1 and 2 always accumulate)
+template <int LV, int PL>
 __global__ void strassen_c_kernel(const double* __restrict__ Mb, long long ldb, int h, int nh, int T,
                                   cplx* __restrict__ U, long long ldu, long long sU, int accumulate) {
-  constexpr int G = 1 << LV, NS = LV == 1 ? 7 : 49;
+  constexpr int G = 1 << LV, NS = P7<LV>::v;
   const int t = blockIdx.z, i = blockIdx.y;
   const long long bs = (long long)T * h * ldb;
   const double* m = Mb + (long long)t * h * ldb + (long long)i * ldb;
   cplx* u = U + t * sU;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nh; j += gridDim.x * blockDim.x) {
+    if (PL >= 0) {   // plane PL's share: (re, im) += (sr, si) x its product
+      double c[G][G];
+      StrassenComb<LV>::run(m + (long long)PL * NS * bs + j, bs, c);
+      const double sr = PL == 0 ? 1.0 : (PL == 1 ? -1.0 : 0.0), si = PL == 2 ? 1.0 : -1.0;
+      const bool acc = PL > 0 || accumulate;
+#pragma unroll
+      for (int R = 0; R < G; ++R)
+#pragma unroll
+        for (int C = 0; C < G; ++C) {
+          cplx* p = u + (long long)(R * h + i) * ldu + C * nh + j;
+          double2 v = make_double2(sr * c[R][C], si * c[R][C]);
+          if (acc) {
+            const double2 o = *p;
+            v.x += o.x;
+            v.y += o.y;
+          }
+          *p = v;
+        }
+      continue;
+    }
     double c[3][G][G];
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const double* mq = m + (long long)q * NS * bs + j;
-      if (LV == 1) {
-        double mm[7];
-#pragma unroll
-        for (int s = 0; s < 7; ++s) mm[s] = mq[s * bs];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          double acc = 0.0;
-#pragma unroll
-          for (int s = 0; s < 7; ++s) acc += kSC[b][s] * mm[s];
-          c[q][b >> 1][b & 1] = acc;
-        }
-      } else {
-#pragma unroll
-        for (int R = 0; R < G; ++R)
-#pragma unroll
-          for (int C = 0; C < G; ++C) c[q][R][C] = 0.0;
-#pragma unroll
-        for (int s1 = 0; s1 < 7; ++s1) {
-          double mm[7];
-#pragma unroll
-          for (int s2 = 0; s2 < 7; ++s2) mm[s2] = mq[(s1 * 7 + s2) * bs];
-#pragma unroll
-          for (int b2 = 0; b2 < 4; ++b2) {      // the 2 x 2 blocks of the level-1 product s1
-            double acc = 0.0;
-#pragma unroll
-            for (int s2 = 0; s2 < 7; ++s2) acc += kSC[b2][s2] * mm[s2];
-#pragma unroll
-            for (int b1 = 0; b1 < 4; ++b1)       // its share of the full product's half-blocks
-              if (kSC[b1][s1]) c[q][2 * (b1 >> 1) + (b2 >> 1)][2 * (b1 & 1) + (b2 & 1)] += kSC[b1][s1] * acc;
-          }
-        }
-      }
-    }
+    for (int q = 0; q < 3; ++q) StrassenComb<LV>::run(m + (long long)q * NS * bs + j, bs, c[q]);
 #pragma unroll
     for (int R = 0; R < G; ++R)
 #pragma unroll
@@ -275,7 +310,8 @@ int strassen_k(cudaStream_t st, int levels, const double* Kp, long long ldk, lon
                long long ldks, std::string* err) {
   const int h = L >> levels;
   dim3 grid((unsigned)std::min<long long>(ceil_div(h, 256), 16), h, 3);
-  if (levels == 2) strassen_a_kernel<2><<<grid, 256, 0, st>>>(Kp, ldk, pk, h, Ks, ldks);
+  if (levels == 3) strassen_a_kernel<3><<<grid, 256, 0, st>>>(Kp, ldk, pk, h, Ks, ldks);
+  else if (levels == 2) strassen_a_kernel<2><<<grid, 256, 0, st>>>(Kp, ldk, pk, h, Ks, ldks);
   else strassen_a_kernel<1><<<grid, 256, 0, st>>>(Kp, ldk, pk, h, Ks, ldks);
   count_launch();
   cudaError_t e = cudaGetLastError();
@@ -287,8 +323,16 @@ int strassen_b(cudaStream_t st, int levels, const cplx* U, long long ldu, long l
                double* Bc, long long ldb, std::string* err) {
   const int h = L >> levels, nh = N >> levels;
   dim3 grid((unsigned)std::min<long long>(ceil_div(nh, 256), 16), h, T);
-  if (levels == 2) strassen_b_kernel<2><<<grid, 256, 0, st>>>(U, ldu, sU, h, nh, T, Bc, ldb);
-  else strassen_b_kernel<1><<<grid, 256, 0, st>>>(U, ldu, sU, h, nh, T, Bc, ldb);
+  if (levels == 3) {
+    strassen_b_kernel<3, 0><<<grid, 256, 0, st>>>(U, ldu, sU, h, nh, T, Bc, ldb);
+    strassen_b_kernel<3, 1><<<grid, 256, 0, st>>>(U, ldu, sU, h, nh, T, Bc, ldb);
+    strassen_b_kernel<3, 2><<<grid, 256, 0, st>>>(U, ldu, sU, h, nh, T, Bc, ldb);
+    count_launch(2);
+  } else if (levels == 2) {
+    strassen_b_kernel<2, -1><<<grid, 256, 0, st>>>(U, ldu, sU, h, nh, T, Bc, ldb);
+  } else {
+    strassen_b_kernel<1, -1><<<grid, 256, 0, st>>>(U, ldu, sU, h, nh, T, Bc, ldb);
+  }
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess && err) *err = std::string("strassen_b: ") + cudaGetErrorString(e);
@@ -299,8 +343,16 @@ int strassen_c(cudaStream_t st, int levels, const double* Mb, long long ldb, int
                long long ldu, long long sU, std::string* err, int accumulate) {
   const int h = L >> levels, nh = N >> levels;
   dim3 grid((unsigned)std::min<long long>(ceil_div(nh, 256), 16), h, T);
-  if (levels == 2) strassen_c_kernel<2><<<grid, 256, 0, st>>>(Mb, ldb, h, nh, T, U, ldu, sU, accumulate);
-  else strassen_c_kernel<1><<<grid, 256, 0, st>>>(Mb, ldb, h, nh, T, U, ldu, sU, accumulate);
+  if (levels == 3) {
+    strassen_c_kernel<3, 0><<<grid, 256, 0, st>>>(Mb, ldb, h, nh, T, U, ldu, sU, accumulate);
+    strassen_c_kernel<3, 1><<<grid, 256, 0, st>>>(Mb, ldb, h, nh, T, U, ldu, sU, accumulate);
+    strassen_c_kernel<3, 2><<<grid, 256, 0, st>>>(Mb, ldb, h, nh, T, U, ldu, sU, accumulate);
+    count_launch(2);
+  } else if (levels == 2) {
+    strassen_c_kernel<2, -1><<<grid, 256, 0, st>>>(Mb, ldb, h, nh, T, U, ldu, sU, accumulate);
+  } else {
+    strassen_c_kernel<1, -1><<<grid, 256, 0, st>>>(Mb, ldb, h, nh, T, U, ldu, sU, accumulate);
+  }
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess && err) *err = std::string("strassen_c: ") + cudaGetErrorString(e);

@@ -25,7 +25,10 @@ int split6_planes(cudaStream_t st, const cplx* U, long long ldu, long long sU, i
 int combine_gram(cudaStream_t st, const double* Pl, long long ldp, long long ps, long long ts, int n, int T, cplx* G,
                  long long ldg, long long sG, std::string* err);
 
-// Strassen on each planar product, `levels` = 1 or 2 (planar.cu), leaf grid h = L / 2^levels,
+// products per plane x 3 planes for `levels` Strassen levels
+inline int strassen_products(int levels) { return 3 * (levels >= 3 ? 343 : (levels == 2 ? 49 : 7)); }
+
+// Strassen on each planar product, `levels` = 1, 2 or 3 (planar.cu), leaf grid h = L / 2^levels,
 // nh = N / 2^levels, NS = 7^levels products per plane: Ks [3][NS][h][ldks] = K's operands (once);
 // Bc [3][NS][T][h][ldb] = U's operands; U[t] = the recombined product from Mb (Bc's layout).
 // K is L x L, U L x N: L and N divisible by 2^levels.

@@ -277,7 +277,7 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
     } else if (sh->planar) {
       lay.take(l.Kp, (size_t)3 * Lp * sh->ldKs * 8);
       if (sh->slv)
-        lay.take(l.Ks, (size_t)P * 3 * (sh->slv == 2 ? 49 : 7) * (Lp >> sh->slv) * sh->ldS * 8);
+        lay.take(l.Ks, (size_t)P * strassen_products(sh->slv) * (Lp >> sh->slv) * sh->ldS * 8);
       lay.take(l.Pp, (size_t)3 * Lp * sh->ldPs * 8);
       lay.take(l.Up6, (size_t)6 * Lp * sh->ldPs * 8);
     } else {
@@ -297,7 +297,7 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
   }
   if (banded) lay.take(sh->bcoef, (size_t)(2 * Wx + 2 * Wy + 2) * 16);
   if (sh->slv) {
-    const size_t nb = (size_t)3 * (sh->slv == 2 ? 49 : 7) * (Lp >> sh->slv) * sh->ldSM * 8;
+    const size_t nb = (size_t)strassen_products(sh->slv) * (Lp >> sh->slv) * sh->ldSM * 8;
     lay.take(sh->Sb, nb);
     lay.take(sh->Sm, nb);
   }
@@ -501,7 +501,7 @@ int shard_build(ShardedCtx* sh, const std::vector<std::complex<double>>& kc, con
                          sh->kcoef + sh->Lx, err, l.row0, sh->Lp))
         return 4;
       // the Strassen operands of every chunk K_g[:, s] (Lp x Lp at column s Lp of the planes)
-      const long long ns = 3 * (sh->slv == 2 ? 49 : 7), hh = sh->Lp >> sh->slv;
+      const long long ns = strassen_products(sh->slv), hh = sh->Lp >> sh->slv;
       for (int c = 0; sh->slv && c < sh->P; ++c)
         if (strassen_k(st, sh->slv, l.Kp + (long long)c * sh->Lp, sh->ldKs, (long long)sh->Lp * sh->ldKs, sh->Lp,
                        l.Ks + c * ns * hh * sh->ldS, sh->ldS, err))
@@ -897,7 +897,7 @@ int planar_chunk(ShardedCtx* sh, ShardLocal& l, const cplx* Us, int s, bool accu
   const long long Lp = sh->Lp, psC = Lp * sh->ldPs;
   if (sh->slv) {
     // Strassen on the chunk product K_g[:, s] U_s, accumulated into U_g' directly by the recombination
-    const int np = 3 * (sh->slv == 2 ? 49 : 7);
+    const int np = strassen_products(sh->slv);
     const long long hh = Lp >> sh->slv, nh = sh->N >> sh->slv, bK = hh * sh->ldS, bM = hh * sh->ldSM;
     STRY(strassen_b(sh->st, sh->slv, Us, sh->ldN, 0, (int)Lp, sh->N, 1, sh->Sb, sh->ldSM, err));
     STRY(dgemm(sh->st, 0, hh, nh, hh, 1.0, l.Ks + s * np * bK, sh->ldS, bK, sh->Sb, sh->ldSM, bM, 0.0, sh->Sm,

@@ -321,11 +321,14 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     h->strassen = !(sv && sv[0] == '0') && L % 4 == 0 && N >= smin;
     if (h->strassen) {
       // two levels when K's 147 quarter operands fit 24 GB (c3: 19.7 GB, c4: 1.2 GB; c4 391 vs 401 ms
-      // per step with one level, c2 (N = 1024) is below TRAJ_STRASSEN_MIN_N), else one (c5)
+      // per step with one level, c2 (N = 1024) is below TRAJ_STRASSEN_MIN_N), else one (c5); three
+      // for one trajectory when K's 1029 eighth-size operands fit 40 GB (c3: 34.5 GB)
       const char* lv = getenv("TRAJ_STRASSEN_LEVELS");
       const bool two_ok = L % 8 == 0 && 147.0 * (L / 4) * round_up(L / 4, 16) * 8 <= 24e9;
-      h->slv = lv ? (atoi(lv) >= 2 && two_ok ? 2 : 1) : (two_ok ? 2 : 1);
-      const long long hh = L >> h->slv, ns = 3 * (h->slv == 2 ? 49 : 7);
+      const bool three_ok = T == 1 && L % 16 == 0 && 1029.0 * (L / 8) * round_up(L / 8, 16) * 8 <= 40e9;
+      const int want = lv ? atoi(lv) : 3;
+      h->slv = want >= 3 && three_ok ? 3 : (want >= 2 && two_ok ? 2 : 1);
+      const long long hh = L >> h->slv, ns = strassen_products(h->slv);
       h->ldS = round_up(hh, 16);
       h->ldM = round_up(N >> h->slv, 16);
       lay.take(h->Ks, (size_t)ns * hh * h->ldS * 8);
@@ -340,7 +343,7 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
   if (h->planar || h->planar_cqr) {
     h->ldP = round_up(N, 16);
     lay.take(h->Up, (size_t)T * std::max<long long>(6 * L * h->ldP,
-                                                     h->strassen ? 3 * (h->slv == 2 ? 49 : 7) * (L >> h->slv) * h->ldM
+                                                     h->strassen ? strassen_products(h->slv) * (L >> h->slv) * h->ldM
                                                                  : 0) * 8);
     h->Bc = h->Up;   // U's Strassen operands use the plane buffer (free during K U)
     lay.take(h->Pp, (size_t)T * 3 * L * h->ldP * 8);
@@ -1147,17 +1150,12 @@ int one_step(traj_ctx* h) {
       if (h->strassen) {
         // Strassen per planar product: U's 7^lv operands per plane, 3 7^lv leaf-size real products
         // (one batched launch for one trajectory), recombined into K U in one pass
-        const int np = 3 * (h->slv == 2 ? 49 : 7);
+        const int np = strassen_products(h->slv);
         const long long hh = h->L >> h->slv, nh = h->N >> h->slv, bK = hh * h->ldS, bM = hh * h->ldM;
         TRY(strassen_b(h->st, h->slv, Uc, h->ldN, h->sU, h->L, h->N, h->T, h->Bc, h->ldM, &h->err));
-        if (h->T == 1) {
-          TRY(dgemm(h->st, 0, hh, nh, hh, 1.0, h->Ks, h->ldS, bK, h->Bc, h->ldM, bM, 0.0, h->Ms, h->ldM, bM, np, 0,
-                    &h->err));
-        } else {
-          for (int qs = 0; qs < np; ++qs)
-            TRY(dgemm(h->st, 0, hh, nh, hh, 1.0, h->Ks + qs * bK, h->ldS, 0, h->Bc + qs * h->T * bM, h->ldM, bM, 0.0,
-                      h->Ms + qs * h->T * bM, h->ldM, bM, h->T, 0, &h->err));
-        }
+        // one launch: entry z = (plane, operand) * T + trajectory, K's operand z / T shared by the batch
+        TRY(dgemm(h->st, 0, hh, nh, hh, 1.0, h->Ks, h->ldS, bK, h->Bc, h->ldM, bM, 0.0, h->Ms, h->ldM, bM,
+                  (long long)np * h->T, 0, &h->err, 0, 0, h->T));
         TRY(strassen_c(h->st, h->slv, h->Ms, h->ldM, h->L, h->N, h->T, Un, h->ldN, h->sU, &h->err));
       } else if (h->planar) {
         // three real products on planes, then (P1 - P2) + i (P3 - P1 - P2)

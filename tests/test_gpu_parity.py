@@ -239,14 +239,14 @@ def test_c4_full_size_homodyne_mutual_information(P):
     lockstep(P, w.Lx, w.Ly, w.protocol, gams, 4, 4, [A], seed=w.seed, mi=(A, B))
 
 
-@pytest.mark.parametrize("levels", [1, 2])
-@pytest.mark.parametrize("Lx,Ly,protocol,gams", [(200, 1, "projective", [2.0]), (200, 1, "homodyne", [1.0, 0.3]),
+@pytest.mark.parametrize("levels", [1, 2, 3])
+@pytest.mark.parametrize("Lx,Ly,protocol,gams", [(208, 1, "projective", [2.0]), (208, 1, "homodyne", [1.0, 0.3]),
                                                (12, 12, "projective", [3.0, 1.0]), (12, 12, "homodyne", [1.5])])
 def test_strassen_propagator_matches_oracle(P, monkeypatch, Lx, Ly, protocol, gams, levels):
     """Strassen on each planar real product of K U (csrc/planar.cu strassen_*), one level (seven
-    half-size products) and two (49 quarter-size ones): the same state as the plain planar products
-    (1e-12) and the oracle (1e-10) -- 1d and 2d (Kronecker K), one trajectory (one batched launch)
-    and two (per-operand batched launches)."""
+    half-size products), two (49 quarter-size ones) and three (343 eighth-size ones, one trajectory;
+    with two trajectories it falls back to two): the same state as the plain planar products (1e-12)
+    and the oracle (1e-10) -- 1d and 2d (Kronecker K), one launch for all products and trajectories."""
     L, steps = Lx * Ly, 10
     monkeypatch.setenv("TRAJ_PLANAR_MIN_N", "0")
     monkeypatch.setenv("TRAJ_STRASSEN_MIN_N", "0")
