@@ -306,6 +306,55 @@ __global__ void strassen_c_kernel(const double* __restrict__ Mb, long long ldb, 
 
 }  // namespace
 
+namespace {
+
+// the three-level recombination, one plane, one top-level quadrant b1 = blockIdx.z per thread (one
+// trajectory): c = sum over the top-level products s1 feeding b1 of kSC[b1][s1] x their two-level
+// recombination -- 16 outputs and at most 4 x 49 loads per thread instead of 64 and 343
+template <int PL>
+__global__ void __launch_bounds__(256, 2) strassen_c3_kernel(const double* __restrict__ Mb, long long ldb, int h, int nh,
+                                   cplx* __restrict__ U, long long ldu, int accumulate) {
+  const int i = blockIdx.y, b1 = blockIdx.z;
+  const long long bs = (long long)h * ldb;
+  const double* m = Mb + (long long)PL * 343 * bs + (long long)i * ldb;
+  const double sr = PL == 0 ? 1.0 : (PL == 1 ? -1.0 : 0.0), si = PL == 2 ? 1.0 : -1.0;
+  const bool acc = PL > 0 || accumulate;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nh; j += gridDim.x * blockDim.x) {
+    double c[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) c[r][q] = 0.0;
+#pragma unroll 1
+    for (int s1 = 0; s1 < 7; ++s1) {
+      const double k = kSC[b1][s1];
+      if (k == 0.0) continue;
+      double ch[4][4];
+      StrassenComb<2>::run(m + (long long)s1 * 49 * bs + j, bs, ch);
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) c[r][q] += k * ch[r][q];
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int R = (b1 >> 1) * 4 + r, C = (b1 & 1) * 4 + q;
+        cplx* p = U + (long long)(R * h + i) * ldu + C * nh + j;
+        double2 v = make_double2(sr * c[r][q], si * c[r][q]);
+        if (acc) {
+          const double2 o = *p;
+          v.x += o.x;
+          v.y += o.y;
+        }
+        *p = v;
+      }
+  }
+}
+
+}  // namespace
+
 int strassen_k(cudaStream_t st, int levels, const double* Kp, long long ldk, long long pk, int L, double* Ks,
                long long ldks, std::string* err) {
   const int h = L >> levels;
@@ -343,10 +392,15 @@ int strassen_c(cudaStream_t st, int levels, const double* Mb, long long ldb, int
                long long ldu, long long sU, std::string* err, int accumulate) {
   const int h = L >> levels, nh = N >> levels;
   dim3 grid((unsigned)std::min<long long>(ceil_div(nh, 256), 16), h, T);
-  if (levels == 3) {
-    strassen_c_kernel<3, 0><<<grid, 256, 0, st>>>(Mb, ldb, h, nh, T, U, ldu, sU, accumulate);
-    strassen_c_kernel<3, 1><<<grid, 256, 0, st>>>(Mb, ldb, h, nh, T, U, ldu, sU, accumulate);
-    strassen_c_kernel<3, 2><<<grid, 256, 0, st>>>(Mb, ldb, h, nh, T, U, ldu, sU, accumulate);
+  if (levels == 3) {   // one trajectory (traj_api.cu): grid.z = the top-level quadrant
+    if (T != 1) {
+      if (err) *err = "strassen_c: three levels need one trajectory";
+      return 1;
+    }
+    dim3 g3(grid.x, h, 4);
+    strassen_c3_kernel<0><<<g3, 256, 0, st>>>(Mb, ldb, h, nh, U, ldu, accumulate);
+    strassen_c3_kernel<1><<<g3, 256, 0, st>>>(Mb, ldb, h, nh, U, ldu, accumulate);
+    strassen_c3_kernel<2><<<g3, 256, 0, st>>>(Mb, ldb, h, nh, U, ldu, accumulate);
     count_launch(2);
   } else if (levels == 2) {
     strassen_c_kernel<2, -1><<<grid, 256, 0, st>>>(Mb, ldb, h, nh, T, U, ldu, sU, accumulate);
