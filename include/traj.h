@@ -306,6 +306,30 @@ int traj_dgemm(void* stream, int64_t M, int64_t N, int64_t K, double alpha, cons
 int traj_set_zgemm_algorithm(int algo);
 int traj_get_zgemm_algorithm(void);
 
+/* traj_igemm: C_z = A_z B_z^T for z < batch on the INT8 tensor cores (tcgen05.mma kind::i8 with TMEM
+ * accumulators, operands staged by TMA; csrc/igemm.cu).  A_z: int8 M x K (row-major, lda bytes,
+ * A_z = A + z*strideA), B_z: int8 N x K (ldb, strideB), C_z: the exact int32 sums (ldc elements,
+ * strideC) -- or, with moduli != NULL (device int32[nmod], each in [2, 256]), those sums mod
+ * moduli[z % nmod] in [0, m) as uint8.  flags: 1 = only the 128 x 256 tiles that meet the upper
+ * triangle are computed, 2 = B_z[n][k] = 0 for k > n is assumed (those k-blocks are skipped).
+ * Needs 0 < K < 2^17 (so |sum| <= K 128^2 < 2^31), lda and ldb multiples of 16 >= K, ldc a multiple
+ * of 16 >= N, 16-byte aligned pointers; TRAJ_EINVAL otherwise.  Stream-ordered, asynchronous. */
+int traj_igemm(void* stream, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64_t strideA,
+               const void* B, int64_t ldb, int64_t strideB, void* C, int64_t ldc, int64_t strideC, int64_t batch,
+               const int32_t* moduli, int nmod, int flags);
+
+/* traj_zgemm_ozaki: C = op(A) B in complex128 (row-major, ld in complex elements), computed by the
+ * exact modular scheme on the INT8 tensor cores (csrc/ozaki.h: Ozaki-II; the contraction the paper
+ * states as a complex-FP64 matrix product).  opA = 0: A is M x K; opA = 1: A is stored
+ * K x M and op(A) = A^dag (the Gram form U^dag U).  B is K x N.  nmod in {4, 6, ..., 16} pairwise
+ * coprime moduli: every row of op(A) and column of B is represented to 2^-(beta+1) of its 2-norm,
+ * beta = 61 for 16 (finer than FP64 for the entries that carry the norm), and the products are
+ * exact.  flags: TRAJ_C_UPPER (only j >= i written), TRAJ_TRI_B_UPPER (B upper triangular).  The
+ * residue scratch is allocated and freed on the stream (cudaMallocAsync); TRAJ_EINVAL on a bad
+ * shape. */
+int traj_zgemm_ozaki(void* stream, int opA, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                     const void* B, int64_t ldb, void* C, int64_t ldc, int nmod, int flags);
+
 /* traj_chol_inverse: for each b, G_b (n x n Hermitian positive definite; only the
  * upper triangle is read) = R^dag R with R upper triangular; writes X_b = R^-1
  * (upper triangle; the strict lower triangle is set to zero).  G_b's strict lower

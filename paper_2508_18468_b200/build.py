@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libtraj.so")
-SOURCES = ["zgemm.cu", "dgemm.cu", "planar.cu", "cholinv.cu", "structchol.cu", "monitor.cu", "banded.cu", "qsd_rk4.cu", "pm_events.cu", "probe.cu", "small_step.cu", "shard.cu", "watchdog.cu", "traj_api.cu"]
+SOURCES = ["zgemm.cu", "dgemm.cu", "planar.cu", "cholinv.cu", "structchol.cu", "monitor.cu", "banded.cu", "qsd_rk4.cu", "pm_events.cu", "probe.cu", "small_step.cu", "shard.cu", "watchdog.cu", "igemm.cu", "ozaki.cu", "traj_api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 

@@ -1,0 +1,393 @@
+// INT8 tensor-core GEMM for sm_100a: tcgen05.mma.kind::i8, accumulators in TMEM, operands staged by
+// TMA as 128B-swizzled K-major tiles, one persistent CTA per SM.
+//
+// C_z = A_z B_z^T (A_z: M x K, B_z: N x K, both K-major int8), exact in int32.  This is the building
+// block of the modular complex-FP64 products (ozaki.cu): each residue product is one batch entry and
+// the epilogue reduces the exact int32 dot product mod that entry's modulus.
+//
+// CTA: 192 threads, warp 0 = TMA producer, warp 1 = MMA issuer (one elected lane) and TMEM owner,
+// warps 2..5 = epilogue (warp w reads TMEM lanes 32 (w % 4) .. + 31: one accumulator row per thread).
+// Tile 128 x 256 x 128 (one MMA 128 x 256 x 32 per 32 bytes of k), 4-stage smem ring of 48 KB,
+// two 256-column TMEM accumulators so the epilogue of tile t overlaps the MMAs of tile t + 1.
+#include "igemm.h"
+
+namespace traj {
+namespace {
+
+constexpr int IBM = 128, IBN = 256, IBK = 128, ISTAGES = 4;
+constexpr int IA_BYTES = IBM * IBK, IB_BYTES = IBN * IBK, ISTAGE_BYTES = IA_BYTES + IB_BYTES;
+constexpr int ITHREADS = 192;
+constexpr int ISMEM = ISTAGES * ISTAGE_BYTES + 1024 + 256;
+constexpr int IGM = 16;   // raster group: IGM m-blocks share each n-block's B tile through L2
+
+// K-major operand, 128-byte rows, 128B swizzle (8-row atoms of 1 KB): SBO = 1024 B, version 1.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+// instruction descriptor: D s32, A s8, B s8, both K-major, N >> 3 at bit 17, M >> 4 at bit 24
+__host__ __device__ constexpr uint32_t idesc_i8(int m, int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+struct KArgs {
+  int M, N, K;
+  int tiles_m, tiles_n;
+  long long tiles;       // batch * tiles_m * tiles_n
+  int a_div, b_div, a_batched, b_batched;
+  void* C;
+  long long ldc, strideC;
+  int out;
+  const int* moduli;
+  int nmod;
+  int flags;
+  int oz_s, oz_T, oz_a_traj, oz_b_traj;
+  int oz_pa[3], oz_pb[3];
+};
+
+// batch entry z -> (A entry, B entry, modulus index)
+__device__ __forceinline__ void zmap(const KArgs& a, int z, int& za, int& zb, int& q) {
+  if (a.oz_s) {
+    const int t = z % a.oz_T, pq = z / a.oz_T;
+    const int p = pq / a.oz_s;
+    q = pq - p * a.oz_s;
+    za = a.oz_a_traj ? (a.oz_pa[p] * a.oz_s + q) * a.oz_T + t : a.oz_pa[p] * a.oz_s + q;
+    zb = a.oz_b_traj ? (a.oz_pb[p] * a.oz_s + q) * a.oz_T + t : a.oz_pb[p] * a.oz_s + q;
+  } else {
+    za = a.a_batched ? z / a.a_div : 0;
+    zb = a.b_batched ? z / a.b_div : 0;
+    q = z % a.nmod;
+  }
+}
+
+struct Tile {
+  int z, mb, nb;
+};
+
+__device__ __forceinline__ Tile tile_of(const KArgs& a, long long t) {
+  const long long per = (long long)a.tiles_m * a.tiles_n;
+  Tile r;
+  r.z = (int)(t / per);
+  const int rem = (int)(t - (long long)r.z * per);
+  const int gsz = IGM * a.tiles_n;
+  const int g = rem / gsz, first = g * IGM;
+  const int h = min(IGM, a.tiles_m - first), w = rem - g * gsz;
+  r.mb = first + w % h;
+  r.nb = w / h;
+  return r;
+}
+
+__device__ __forceinline__ bool tile_live(const KArgs& a, const Tile& t) {
+  if (a.flags & IG_UPPER) return (t.nb + 1) * IBN - 1 >= t.mb * IBM;
+  return true;
+}
+
+__device__ __forceinline__ int tile_kblocks(const KArgs& a, const Tile& t) {
+  int kend = a.K;
+  if (a.flags & IG_TRI_B) kend = min(kend, (t.nb + 1) * IBN);
+  return (kend + IBK - 1) / IBK;
+}
+
+__global__ void __launch_bounds__(ITHREADS, 1)
+    igemm_i8_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const KArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  uint8_t* base = smem_raw + (base_u32 - smem_u32(smem_raw));
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + ISTAGES * ISTAGE_BYTES);
+  uint64_t* empty = full + ISTAGES;
+  uint64_t* tfull = empty + ISTAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ISTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    fence_mbar_init();
+    prefetch_tmap(&ta);
+    prefetch_tmap(&tb);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {   // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (long long t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+        const Tile tl = tile_of(a, t);
+        if (!tile_live(a, tl)) continue;
+        const int nk = tile_kblocks(a, tl);
+        int za, zb, q;
+        zmap(a, tl.z, za, zb, q);
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = base + stage * ISTAGE_BYTES;
+          mbar_arrive_expect_tx(&full[stage], ISTAGE_BYTES);
+          tma_load_3d(sa, &ta, kb * IBK, tl.mb * IBM, za, &full[stage]);
+          tma_load_3d(sa + IA_BYTES, &tb, kb * IBK, tl.nb * IBN, zb, &full[stage]);
+          if (++stage == ISTAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {   // ---------------- MMA issuer
+    constexpr uint32_t idesc = idesc_i8(IBM, IBN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (long long t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+      const Tile tl = tile_of(a, t);
+      if (!tile_live(a, tl)) continue;
+      const int nk = tile_kblocks(a, tl);
+      const int buf = it & 1;
+      const uint32_t use = (uint32_t)(it >> 1);
+      mbar_wait(&tempty[buf], (use & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t dt = tmem + buf * IBN;
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sa = base_u32 + stage * ISTAGE_BYTES, sb = sa + IA_BYTES;
+          const uint64_t da = sw128_desc(sa), db = sw128_desc(sb);
+#pragma unroll
+          for (int k = 0; k < IBK / 32; ++k)   // +32 bytes of k = +2 in the descriptor's address field
+            mma_i8(dt, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+          mma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == ISTAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (lane == 0) mma_commit(&tfull[buf]);
+      __syncwarp();
+      ++it;
+    }
+  } else {   // ---------------- epilogue: warps 2..5
+    const int q = warp & 3;
+    int it = 0;
+    for (long long t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+      const Tile tl = tile_of(a, t);
+      if (!tile_live(a, tl)) continue;
+      const int buf = it & 1;
+      const uint32_t use = (uint32_t)(it >> 1);
+      mbar_wait(&tfull[buf], use & 1);
+      tc_fence_after();
+      const int row = tl.mb * IBM + q * 32 + lane;
+      const bool row_ok = row < a.M;
+      const uint32_t taddr = tmem + buf * IBN + ((uint32_t)(q * 32) << 16);
+      int mod = 0;
+      double inv = 0.0;
+      if (a.out == IG_OUT_MOD) {
+        int za, zb, q;
+        zmap(a, tl.z, za, zb, q);
+        mod = a.moduli[q];
+        inv = 1.0 / (double)mod;
+      }
+#pragma unroll 1
+      for (int c = 0; c < IBN / 32; ++c) {
+        uint32_t v[32];
+        __syncwarp();
+        tmem_ld32(taddr + c * 32, v);
+        const int col = tl.nb * IBN + c * 32;
+        if (!row_ok || col >= a.N) {
+        } else if (a.out == IG_OUT_I32) {
+          int* p = reinterpret_cast<int*>(a.C) + tl.z * a.strideC + (long long)row * a.ldc + col;
+          if (col + 32 <= a.N) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              reinterpret_cast<int4*>(p)[j] = make_int4((int)v[4 * j], (int)v[4 * j + 1], (int)v[4 * j + 2], (int)v[4 * j + 3]);
+          } else {
+            for (int j = 0; col + j < a.N; ++j) p[j] = (int)v[j];
+          }
+        } else {
+          uint32_t w[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            uint32_t packed = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const int x = (int)v[4 * j + b];
+              int r = x - mod * (int)floor((double)x * inv);
+              r += (r < 0) ? mod : 0;
+              r -= (r >= mod) ? mod : 0;
+              packed |= (uint32_t)r << (8 * b);
+            }
+            w[j] = packed;
+          }
+          uint8_t* p = reinterpret_cast<uint8_t*>(a.C) + tl.z * a.strideC + (long long)row * a.ldc + col;
+          if (col + 32 <= a.N) {
+            reinterpret_cast<uint4*>(p)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            reinterpret_cast<uint4*>(p)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          } else {
+            for (int j = 0; col + j < a.N; ++j) p[j] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+      ++it;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
+typedef CUresult (*PFN_encode_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encode_t encode_i8() {
+  static PFN_encode_t fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encode_t>(p);
+  }
+  return fn;
+}
+
+bool map_i8(PFN_encode_t enc, CUtensorMap* m, const int8_t* p, long long K, long long rows, long long ld, long long nb,
+            long long stride, int box_rows) {
+  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)nb};
+  cuuint64_t strides[2] = {(cuuint64_t)ld, (cuuint64_t)(nb > 1 ? stride : ld * rows)};
+  cuuint32_t box[3] = {IBK, (cuuint32_t)box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(p), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+}  // namespace
+
+int igemm(cudaStream_t st, const IgemmArgs& g, std::string* err) {
+  if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return 0;
+  if (g.K <= 0 || g.K >= (1 << 17) || g.M >= (1LL << 31) || g.N >= (1LL << 31) || (g.lda & 15) || (g.ldb & 15) ||
+      g.lda < g.K || g.ldb < g.K || (g.ldc & 15) || g.ldc < g.N || g.a_div < 1 || g.b_div < 1 ||
+      g.batch % g.a_div || g.batch % g.b_div || (reinterpret_cast<uintptr_t>(g.A) & 15) ||
+      (reinterpret_cast<uintptr_t>(g.B) & 15) || (reinterpret_cast<uintptr_t>(g.C) & 15) ||
+      (g.out != IG_OUT_I32 && g.out != IG_OUT_MOD) || (g.out == IG_OUT_MOD && (!g.moduli || g.nmod < 1))) {
+    if (err) *err = "igemm: needs 0 < K < 2^17, lda/ldb multiples of 16 >= K, ldc a multiple of 16 >= N, 16-B alignment";
+    return 1;
+  }
+  PFN_encode_t enc = encode_i8();
+  if (!enc) {
+    if (err) *err = "igemm: cuTensorMapEncodeTiled unavailable";
+    return 4;
+  }
+  const long long na = g.oz_s ? g.oz_na : g.batch / g.a_div, nb = g.oz_s ? g.oz_nb : g.batch / g.b_div;
+  const bool ab = g.strideA != 0 && na > 1, bb = g.strideB != 0 && nb > 1;
+  if (g.oz_s && (g.batch != 3LL * g.oz_s * g.oz_T || g.oz_T < 1 || !g.moduli || g.out != IG_OUT_MOD)) {
+    if (err) *err = "igemm: modular batch map needs batch = 3 s T and the modular epilogue";
+    return 1;
+  }
+  CUtensorMap ma, mb;
+  if (!map_i8(enc, &ma, g.A, g.K, g.M, g.lda, ab ? na : 1, g.strideA, IBM) ||
+      !map_i8(enc, &mb, g.B, g.K, g.N, g.ldb, bb ? nb : 1, g.strideB, IBN)) {
+    if (err) *err = "igemm: tensor map";
+    return 4;
+  }
+  KArgs a;
+  a.M = (int)g.M;
+  a.N = (int)g.N;
+  a.K = (int)g.K;
+  a.tiles_m = (int)ceil_div(g.M, IBM);
+  a.tiles_n = (int)ceil_div(g.N, IBN);
+  a.tiles = g.batch * a.tiles_m * a.tiles_n;
+  a.a_div = g.a_div;
+  a.b_div = g.b_div;
+  a.a_batched = ab;
+  a.b_batched = bb;
+  a.C = g.C;
+  a.ldc = g.ldc;
+  a.strideC = g.strideC;
+  a.out = g.out;
+  a.moduli = g.moduli;
+  a.nmod = g.nmod;
+  a.flags = g.flags;
+  a.oz_s = g.oz_s;
+  a.oz_T = g.oz_T;
+  a.oz_a_traj = g.oz_a_traj;
+  a.oz_b_traj = g.oz_b_traj;
+  for (int i = 0; i < 3; ++i) {
+    a.oz_pa[i] = g.oz_pa[i];
+    a.oz_pb[i] = g.oz_pb[i];
+  }
+  if (ensure_smem((const void*)igemm_i8_kernel, ISMEM) != cudaSuccess) {
+    if (err) *err = "igemm: shared memory attribute";
+    return 4;
+  }
+  const long long grid = std::min<long long>(a.tiles, num_sms());
+  igemm_i8_kernel<<<(unsigned)grid, ITHREADS, ISMEM, st>>>(ma, mb, a);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    if (err) *err = std::string("igemm: ") + cudaGetErrorString(e);
+    return 4;
+  }
+  return 0;
+}
+
+}  // namespace traj

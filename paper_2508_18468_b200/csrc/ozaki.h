@@ -1,0 +1,77 @@
+// Internal interface of the exact modular complex-FP64 products (ozaki.cu): the Ozaki-II scheme
+// (Ozaki, Uchino, Imamura 2024) on the INT8 tensor cores of sm_100a.
+//
+// A complex product C = A B (A: M x K, B: K x N, complex128) is computed as follows.
+//  1. Each row of A (column of B) is scaled by a power of two 2^e so that the 2-norm of
+//     (|re| + |im|) over that row is < 2^beta, and rounded to integers (exact for every entry
+//     >= 2^(beta - 53) times that norm; the others lose bits below 2^-beta of it).
+//  2. The integer planes (re, im, re + im) -- and (re - im) for a conjugated operand -- are stored as
+//     their residues mod s pairwise coprime moduli m_q <= 256, int8 in [-128, 127].
+//  3. Three products per modulus (3M: P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi)) run on the
+//     INT8 tensor cores (igemm.cu), exact in int32, reduced mod m_q in the epilogue.
+//  4. Re = P1 - P2 and Im = P3 - P1 - P2 mod m_q are exact; the Chinese remainder theorem gives the
+//     integer products X (|X| < prod m_q / 2 by Cauchy-Schwarz on the scaled norms), and
+//     C_ij = X_ij 2^-(eA_i + eB_j) rounded once to FP64.
+// The only approximation is step 1's rounding: with s = 16 moduli beta = 61, i.e. every input is
+// represented to 2^-62 of its row's (column's) norm -- finer than FP64 for the entries that carry the
+// norm.  The products themselves are exact (no FP64 rounding error accumulates over k).
+#pragma once
+#include <string>
+#include "common.cuh"
+
+namespace traj {
+
+constexpr int OZ_MAXS = 16;
+
+// the bits per operand side for s moduli (floor(log2(prod m_q) / 2) - 1); 0 if s is not supported
+int oz_beta(int s);
+int oz_supported(int s);   // s in {4, 6, 8, 10, 12, 14, 16}
+
+// Residue layout: R [plane][q][t][rows][ldr] int8 (ldr = round_up(K, 16)), plane stride s*T*rows*ldr.
+inline long long oz_ld(long long K) { return round_up(K, 16); }
+
+// A operand from the rows of X (T matrices [rows][ldx], stride sX): residue row r = X row r over
+// k = X's columns; planes (re, im, re + im) (conj: im -> -im); e[t][r] (stride sE) the row exponents.
+int oz_split_rows(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T, int conj,
+                  int s, int8_t* R, int* e, long long sE, std::string* err);
+
+// B operand from the columns of X: residue row j = X column j over k = X's rows; planes
+// (re, im, re + im[, re - im]) for nplanes = 3 [4]; part: >= 8 * T * cols doubles of scratch.
+int oz_split_cols(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T, int nplanes,
+                  int s, int8_t* R, int* e, long long sE, double* part, std::string* err);
+
+enum OzFlags {
+  OZ_UPPER = 1,       // C upper triangular (only j >= i computed and written)
+  OZ_TRI_B = 2,       // B upper triangular (k > j skipped)
+  OZ_NEG_P2 = 4,      // the conjugated Gram: P2 = (-Ai) Bi is formed as Ai Bi and negated here
+  OZ_ACCUMULATE = 8,  // C += A B instead of C = A B
+};
+
+struct OzProduct {
+  int M = 0, N = 0, K = 0, T = 1, s = 16;
+  const int8_t* RA = nullptr;   // [planes][s][Ta][M][oz_ld(K)], Ta = T if a_traj else 1
+  int a_traj = 1;
+  long long a_planes = 3;       // planes in RA (for its tensor map)
+  int pa[3] = {0, 1, 2};        // RA planes of P1, P2, P3
+  const int* eA = nullptr;      // [Ta][M] (stride sEA)
+  long long sEA = 0;
+  const int8_t* RB = nullptr;   // [planes][s][T][N][oz_ld(K)]
+  long long b_planes = 3;
+  int pb[3] = {0, 1, 2};
+  const int* eB = nullptr;      // [T][N]
+  long long sEB = 0;
+  uint8_t* RC = nullptr;        // scratch [3][s][T][M][oz_ld(N)]
+  cplx* C = nullptr;
+  long long ldc = 0, sC = 0;
+  int flags = 0;
+};
+
+// the products (one batched INT8 launch) and the CRT combine into C
+int oz_product(cudaStream_t st, const OzProduct& p, std::string* err);
+
+// bytes of the scratch buffers for a product of this shape
+inline long long oz_residue_bytes(long long planes, int s, long long T, long long rows, long long K) {
+  return planes * s * T * rows * oz_ld(K);
+}
+
+}  // namespace traj

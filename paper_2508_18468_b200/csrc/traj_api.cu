@@ -24,8 +24,12 @@
 #include "banded.h"
 #include "qsd_rk4.h"
 #include "pm_events.h"
+#include "igemm.h"
+#include "ozaki.h"
 #include "probe.h"
 #include "dgemm.h"
+#include "igemm.h"
+#include "ozaki.h"
 #include "planar.h"
 #include "small_step.h"
 #include "comm_plan.h"
@@ -61,6 +65,17 @@ struct traj_ctx {
   int slv = 0;
   double *Ks = nullptr, *Bc = nullptr, *Ms = nullptr;
   long long ldS = 0, ldM = 0;
+  // exact modular complex products on the INT8 tensor cores (ozaki.h; TRAJ_OZAKI=0: the DMMA paths):
+  // oz_ku = the dense propagator K U, oz_cqr = the CholeskyQR Grams and TRMMs.  K's residues RK
+  // [3][s][L][oz_ld(L)] with row exponents eK are formed once; per product U's (or X's) residues
+  // RU / RX, the residue products RC [3][s][T][rows][oz_ld(N)] and the row / column exponents eU, eX
+  bool oz_ku = false, oz_cqr = false;
+  int oz_s = 16;
+  int8_t *RK = nullptr, *RU = nullptr, *RX = nullptr;
+  uint8_t* RC = nullptr;
+  int *eK = nullptr, *eU = nullptr, *eX = nullptr;
+  double* oz_part = nullptr;
+  size_t RC_bytes = 0;
   std::vector<cplx> band_host;     // the same on the host: passed by value to the stencil launches
   cplx* Wrk = nullptr;             // RK4 QSD scratch, shaped like U
   // event-driven PM (NEXT-4)
@@ -295,6 +310,16 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
                 !(pk && pk[0] == '0') && N >= min_n;
     const char* pc = getenv("TRAJ_PLANAR_CQR");
     h->planar_cqr = !(pc && pc[0] == '0') && N >= min_n;
+    // the modular INT8 products replace both DMMA paths from the same size on (TRAJ_OZAKI=0: off,
+    // TRAJ_OZAKI_MODULI: 4..16 even, default 16 = beta 61 bits per operand row / column)
+    const char* oz = getenv("TRAJ_OZAKI");
+    const char* om = getenv("TRAJ_OZAKI_MODULI");
+    h->oz_s = om ? atoi(om) : 16;
+    const bool oz_on = !(oz && oz[0] == '0') && oz_supported(h->oz_s) && N >= min_n && L <= 65535;
+    h->oz_cqr = oz_on;
+    h->oz_ku = oz_on && h->planar;
+    if (h->oz_ku) h->planar = false;
+    if (h->oz_cqr) h->planar_cqr = false;
   }
   if (c->protocol == TRAJ_HOMODYNE_RK4) {     // stencil generator: no K
     h->banded = false;
@@ -337,8 +362,24 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
       if (mb <= (size_t)3 * L * h->ldK * 8) h->Ms = h->Kp;
       else lay.take(h->Ms, mb);
     }
-  } else {
+  } else if (!h->oz_ku) {
     lay.take(h->K, (size_t)L * ldL * 16);
+  }
+  if (h->oz_ku || h->oz_cqr) {
+    const long long s = h->oz_s;
+    const size_t ru = (size_t)std::max(oz_residue_bytes(4, s, T, N, L), oz_residue_bytes(3, s, T, L, N));
+    h->RC_bytes = (size_t)oz_residue_bytes(3, s, T, L, N);
+    if (h->oz_ku) {
+      lay.take(h->RK, (size_t)oz_residue_bytes(3, s, 1, L, L));
+      lay.take(h->eK, (size_t)L * 4);
+      h->RC_bytes = std::max<size_t>(h->RC_bytes, (size_t)L * ldL * 16);   // K is built there before its split
+    }
+    lay.take(h->RU, ru);
+    lay.take(h->RC, h->RC_bytes);
+    if (h->oz_cqr) lay.take(h->RX, (size_t)oz_residue_bytes(3, s, T, N, N));
+    lay.take(h->eU, (size_t)T * L * 4);
+    lay.take(h->eX, (size_t)T * N * 4);
+    lay.take(h->oz_part, (size_t)8 * T * L * 8);
   }
   if (h->planar || h->planar_cqr) {
     h->ldP = round_up(N, 16);
@@ -568,6 +609,33 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
         TRY(set_identity(h->st, h->G, h->ldN, h->sG, h->N, h->T, &h->err));
         TRY(zgemm(h->st, 1, 0, h->N, h->N, lr, -1.0, 0.0, h->US, h->ldN, h->sUS, h->US, h->ldN, h->sUS, 1.0, h->G,
                   h->ldN, h->sG, h->T, TRAJ_C_UPPER_F, &h->err, 0, 0, &db));
+      } else if (h->oz_cqr) {
+        // G = U^dag U on the INT8 tensor cores: U's column residues (re, im, re + im, re - im) once,
+        // P1 = Ur^T Ur, P2' = Ui^T Ui, P3 = (Ur - Ui)^T (Ur + Ui); Re = P1 + P2', Im = P3 - P1 + P2'
+        TRY(oz_split_cols(h->st, src, h->ldN, h->sU, h->L, h->N, h->T, 4, h->oz_s, h->RU, h->eU, h->L, h->oz_part,
+                          &h->err));
+        OzProduct p;
+        p.M = h->N;
+        p.N = h->N;
+        p.K = h->L;
+        p.T = h->T;
+        p.s = h->oz_s;
+        p.RA = h->RU;
+        p.a_traj = 1;
+        p.a_planes = 4;
+        p.pa[2] = 3;
+        p.eA = h->eU;
+        p.sEA = h->L;
+        p.RB = h->RU;
+        p.b_planes = 4;
+        p.eB = h->eU;
+        p.sEB = h->L;
+        p.RC = h->RC;
+        p.C = h->G;
+        p.ldc = h->ldN;
+        p.sC = h->sG;
+        p.flags = OZ_UPPER | OZ_NEG_P2;
+        TRY(oz_product(h->st, p, &h->err));
       } else if (h->planar_cqr) {
         // G = U^dag U = (P1 + Q2) + i (P3 - P1 + Q2): P1 = Ur^T Ur, Q2 = Ui^T Ui, P3 = (Ur - Ui)^T (Ur + Ui),
         // A triple = planes 0..2, B triple = planes 3..5
@@ -606,7 +674,7 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
                            h->failed_dev, &h->err, nullptr, nullptr, h->gate));
         }
       }
-      if (full && h->chol_overlap && h->st_hi && h->N > 64) {
+      if (full && h->chol_overlap && h->st_hi && h->N > 64 && !h->oz_cqr) {
         // fork: factorise on st_hi; as each left-edge block X[0:h, 0:h] is queued, st_lo runs the
         // TRMM of the columns it completes
         CK(cudaEventRecord(h->ev_fork, h->st));
@@ -682,7 +750,32 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
     }
     {
       Phase p(&h->prof, h->st, TRAJ_PH_TRMM);
-      if (h->planar_cqr && planes_of == src) {
+      if (h->oz_cqr) {
+        // U X on the INT8 tensor cores: U's row residues, X's column residues (X upper triangular:
+        // k-blocks past each output column block skipped)
+        TRY(oz_split_rows(h->st, src, h->ldN, h->sU, h->L, h->N, h->T, 0, h->oz_s, h->RU, h->eU, h->L, &h->err));
+        TRY(oz_split_cols(h->st, h->X, h->ldN, h->sG, h->N, h->N, h->T, 3, h->oz_s, h->RX, h->eX, h->N, h->oz_part,
+                          &h->err));
+        OzProduct p;
+        p.M = h->L;
+        p.N = h->N;
+        p.K = h->N;
+        p.T = h->T;
+        p.s = h->oz_s;
+        p.RA = h->RU;
+        p.a_traj = 1;
+        p.eA = h->eU;
+        p.sEA = h->L;
+        p.RB = h->RX;
+        p.eB = h->eX;
+        p.sEB = h->N;
+        p.RC = h->RC;
+        p.C = dst;
+        p.ldc = h->ldN;
+        p.sC = h->sU;
+        p.flags = OZ_TRI_B;
+        TRY(oz_product(h->st, p, &h->err));
+      } else if (h->planar_cqr && planes_of == src) {
         // U X = (P1 - P2) + i (P3 - P1 - P2): P1 = Ur Xr, P2 = Ui Xi, P3 = (Ur + Ui)(Xr + Xi) on the
         // Gram's planes of U and X's planes (X upper triangular: k-blocks past the diagonal skipped)
         const long long tU = h->L * h->ldP, pU = h->T * tU, tX = (long long)h->N * h->ldP, pX = h->T * tX;
@@ -1147,7 +1240,27 @@ int one_step(traj_ctx* h) {
       }
     } else {
       // U <- K U  (K shared across the batch: stride 0)
-      if (h->strassen) {
+      if (h->oz_ku) {
+        TRY(oz_split_cols(h->st, Uc, h->ldN, h->sU, h->L, h->N, h->T, 3, h->oz_s, h->RU, h->eU, h->L, h->oz_part,
+                          &h->err));
+        OzProduct p;
+        p.M = h->L;
+        p.N = h->N;
+        p.K = h->L;
+        p.T = h->T;
+        p.s = h->oz_s;
+        p.RA = h->RK;
+        p.a_traj = 0;
+        p.eA = h->eK;
+        p.RB = h->RU;
+        p.eB = h->eU;
+        p.sEB = h->L;
+        p.RC = h->RC;
+        p.C = Un;
+        p.ldc = h->ldN;
+        p.sC = h->sU;
+        TRY(oz_product(h->st, p, &h->err));
+      } else if (h->strassen) {
         // Strassen per planar product: U's 7^lv operands per plane, 3 7^lv leaf-size real products
         // (one batched launch for one trajectory), recombined into K U in one pass
         const int np = strassen_products(h->slv);
@@ -1531,6 +1644,11 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
       return bail(TRAJ_ECUDA, e);
     if (h->strassen && strassen_k(h->st, h->slv, h->Kp, h->ldK, h->L * h->ldK, h->L, h->Ks, h->ldS, &e))
       return bail(TRAJ_ECUDA, e);
+  } else if (h->oz_ku) {   // K in the product scratch, then its residues (once)
+    cplx* Kt = reinterpret_cast<cplx*>(h->RC);
+    if (build_k(h->st, Kt, h->ldL, h->Lx, h->Ly, h->kcoef, h->kcoef + h->Lx, &e) ||
+        oz_split_rows(h->st, Kt, h->ldL, 0, h->L, h->L, 1, 0, h->oz_s, h->RK, h->eK, 0, &e))
+      return bail(TRAJ_ECUDA, e);
   } else if (cfg->protocol != TRAJ_HOMODYNE_RK4 && cfg->protocol != TRAJ_PROJECTIVE_EVENTS &&
              build_k(h->st, h->K, h->ldL, h->Lx, h->Ly, h->kcoef, h->kcoef + h->Lx, &e)) {
     return bail(TRAJ_ECUDA, e);
@@ -1887,6 +2005,88 @@ int traj_zgemm(void* stream, int opA, int opB, int64_t M, int64_t N, int64_t K, 
                 reinterpret_cast<const cplx*>(A), lda, strideA, reinterpret_cast<const cplx*>(B), ldb, strideB, beta,
                 reinterpret_cast<cplx*>(C), ldc, strideC, batch, flags, &e);
   return s ? fail(nullptr, s, e) : 0;
+}
+
+int traj_igemm(void* stream, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64_t strideA,
+               const void* B, int64_t ldb, int64_t strideB, void* C, int64_t ldc, int64_t strideC, int64_t batch,
+               const int32_t* moduli, int nmod, int flags) {
+  if (M < 0 || N < 0 || batch < 0 || !A || !B || !C || (flags & ~3)) return fail(nullptr, TRAJ_EINVAL, "traj_igemm: bad argument");
+  IgemmArgs g;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.batch = batch;
+  g.A = reinterpret_cast<const int8_t*>(A);
+  g.lda = lda;
+  g.strideA = strideA;
+  g.B = reinterpret_cast<const int8_t*>(B);
+  g.ldb = ldb;
+  g.strideB = strideB;
+  g.C = C;
+  g.ldc = ldc;
+  g.strideC = strideC;
+  g.out = moduli ? IG_OUT_MOD : IG_OUT_I32;
+  g.moduli = moduli;
+  g.nmod = nmod;
+  g.flags = flags;
+  std::string e;
+  const int s = igemm(reinterpret_cast<cudaStream_t>(stream), g, &e);
+  return s ? fail(nullptr, s == 1 ? TRAJ_EINVAL : TRAJ_ECUDA, e) : 0;
+}
+
+int traj_zgemm_ozaki(void* stream, int opA, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                     const void* B, int64_t ldb, void* C, int64_t ldc, int nmod, int flags) {
+  if ((opA != 0 && opA != 1) || M < 0 || N < 0 || K <= 0 || !A || !B || !C || !oz_supported(nmod) || M > 65535 ||
+      (flags & ~(TRAJ_C_UPPER | TRAJ_TRI_B_UPPER)) || lda < (opA ? M : K) || ldb < N || ldc < N)
+    return fail(nullptr, TRAJ_EINVAL, "traj_zgemm_ozaki: bad argument");
+  if (M == 0 || N == 0) return 0;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int s = nmod;
+  const long long na = opA ? 4 : 3;
+  const size_t bA = (size_t)oz_residue_bytes(na, s, 1, M, K), bB = (size_t)oz_residue_bytes(3, s, 1, N, K),
+               bC = (size_t)oz_residue_bytes(3, s, 1, M, N);
+  const size_t bE = (size_t)(M + N) * 4 + 256, bP = (size_t)8 * std::max(M, N) * 8 + 256;
+  char* w = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&w), bA + bB + bC + bE + bP + 1024, st) != cudaSuccess)
+    return fail(nullptr, TRAJ_ECUDA, "traj_zgemm_ozaki: scratch allocation");
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  int8_t* RA = reinterpret_cast<int8_t*>(w);
+  int8_t* RB = reinterpret_cast<int8_t*>(w + al(bA));
+  uint8_t* RC = reinterpret_cast<uint8_t*>(w + al(bA) + al(bB));
+  int* eA = reinterpret_cast<int*>(w + al(bA) + al(bB) + al(bC));
+  int* eB = eA + al((size_t)M * 4) / 4;
+  double* part = reinterpret_cast<double*>(w + al(bA) + al(bB) + al(bC) + al(bE));
+  std::string e;
+  const cplx* a = reinterpret_cast<const cplx*>(A);
+  const cplx* b = reinterpret_cast<const cplx*>(B);
+  int r = 0;
+  OzProduct p;
+  p.M = (int)M;
+  p.N = (int)N;
+  p.K = (int)K;
+  p.T = 1;
+  p.s = s;
+  p.RA = RA;
+  p.a_traj = 0;
+  p.eA = eA;
+  p.RB = RB;
+  p.eB = eB;
+  p.RC = RC;
+  p.C = reinterpret_cast<cplx*>(C);
+  p.ldc = ldc;
+  p.flags = ((flags & TRAJ_C_UPPER) ? OZ_UPPER : 0) | ((flags & TRAJ_TRI_B_UPPER) ? OZ_TRI_B : 0);
+  if (opA == 0) {
+    r = oz_split_rows(st, a, lda, 0, (int)M, (int)K, 1, 0, s, RA, eA, 0, &e);
+  } else {   // A^dag B = (P1 + P2') + i (P3 - P1 + P2'): P1 = Ar^T Br, P2' = Ai^T Bi, P3 = (Ar - Ai)^T (Br + Bi)
+    r = oz_split_cols(st, a, lda, 0, (int)K, (int)M, 1, 4, s, RA, eA, 0, part, &e);
+    p.a_planes = 4;
+    p.pa[2] = 3;
+    p.flags |= OZ_NEG_P2;
+  }
+  if (!r) r = oz_split_cols(st, b, ldb, 0, (int)K, (int)N, 1, 3, s, RB, eB, 0, part, &e);
+  if (!r) r = oz_product(st, p, &e);
+  cudaFreeAsync(w, st);
+  return r ? fail(nullptr, r == 1 ? TRAJ_EINVAL : TRAJ_ECUDA, e) : 0;
 }
 
 int traj_set_zgemm_algorithm(int algo) {

@@ -1,0 +1,182 @@
+"""The exact modular complex products on the INT8 tensor cores (csrc/igemm.cu, csrc/ozaki.cu) through
+the C-ABI: traj_igemm against NumPy int64 (exact, both epilogues, ragged tiles, the upper-tile and
+triangular-B skips), traj_zgemm_ozaki against an extended-precision (long double) product with the
+error bound the scheme guarantees (every input represented to 2^-beta of its row / column 2-norm,
+products exact): plain, conjugated (the Gram form U^dag U), upper-only, triangular B, rows spanning
+many decades, zero rows and a banded propagator-like operand whose entries decay to 1e-300."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+BETA = {4: 14, 6: 22, 8: 30, 10: 38, 12: 46, 14: 54, 16: 61}
+
+
+@pytest.fixture(scope="module")
+def T():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2508_18468_b200 import build
+    build.build()
+    import paper_2508_18468_b200 as P
+    P.load_library()
+    return torch
+
+
+def dev(T, a):
+    return T.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("M,N,K,batch,mod,flags", [(300, 520, 1000, 2, False, 0), (128, 256, 128, 1, False, 0),
+                                                   (300, 520, 1000, 3, True, 0), (700, 700, 700, 1, False, 1),
+                                                   (400, 700, 700, 1, False, 2), (1, 33, 16, 1, True, 0)])
+def test_igemm_exact(T, M, N, K, batch, mod, flags):
+    import paper_2508_18468_b200 as P
+    rng = np.random.default_rng(M * 7 + N + K)
+    lda = (K + 15) // 16 * 16
+    ldc = (N + 15) // 16 * 16
+    A = rng.integers(-128, 128, size=(batch, M, lda), dtype=np.int8)
+    B = rng.integers(-128, 128, size=(batch, N, lda), dtype=np.int8)
+    if flags & 2:
+        for n in range(N):
+            B[:, n, n + 1:] = 0
+    want = np.einsum("zmk,znk->zmn", A[:, :, :K].astype(np.int64), B[:, :, :K].astype(np.int64))
+    mods = np.array([251, 256, 193], dtype=np.int32)
+    dA, dB = dev(T, A), dev(T, B)
+    dC = T.zeros((batch, M, ldc), dtype=T.uint8 if mod else T.int32, device="cuda")
+    dm = dev(T, mods)
+    st = T.cuda.current_stream().cuda_stream
+    r = P.lib().traj_igemm(st, M, N, K, dA.data_ptr(), lda, M * lda, dB.data_ptr(), lda, N * lda, dC.data_ptr(), ldc,
+                           M * ldc, batch, dm.data_ptr() if mod else None, 3, flags)
+    assert r == 0
+    got = dC.cpu().numpy()[:, :, :N].astype(np.int64)
+    if mod:
+        want = np.stack([want[z] % mods[z % 3] for z in range(batch)])
+    if flags & 1:   # only tiles meeting the upper triangle are written
+        for m in range(M):
+            for z in range(batch):
+                lo = (m // 128) * 128
+                keep = np.arange(N) // 256 * 256 + 255 >= lo
+                got[z, m, ~keep] = want[z, m, ~keep]
+    assert np.array_equal(got, want)
+
+
+def test_igemm_rejects_bad_layouts(T):
+    import paper_2508_18468_b200 as P
+    st = T.cuda.current_stream().cuda_stream
+    A = T.zeros(64, 64, dtype=T.int8, device="cuda")
+    C = T.zeros(64, 64, dtype=T.int32, device="cuda")
+    lib = P.lib()
+    assert lib.traj_igemm(st, 64, 64, 64, A.data_ptr(), 40, 0, A.data_ptr(), 64, 0, C.data_ptr(), 64, 0, 1, None, 1, 0) == 1
+    assert lib.traj_igemm(st, 64, 64, 0, A.data_ptr(), 64, 0, A.data_ptr(), 64, 0, C.data_ptr(), 64, 0, 1, None, 1, 0) == 1
+    assert lib.traj_igemm(st, 64, 64, 64, A.data_ptr(), 64, 0, A.data_ptr(), 64, 0, C.data_ptr(), 8, 0, 1, None, 1, 0) == 1
+
+
+def _ld(x):
+    return x.astype(np.clongdouble)
+
+
+def _bound(opA_mat, B, C_ref, s):
+    """Error bound of the scheme: |dC_ij| <= 2^-beta (nu_a_i |b_j|_1 + nu_b_j |a_i|_1) (x4 margin for the
+    complex parts) + the final rounding of C to FP64."""
+    a = np.abs(opA_mat.real) + np.abs(opA_mat.imag)
+    b = np.abs(B.real) + np.abs(B.imag)
+    nua = np.sqrt((a ** 2).sum(1))
+    nub = np.sqrt((b ** 2).sum(0))
+    l1a = a.sum(1)
+    l1b = b.sum(0)
+    return 4.0 * 2.0 ** -BETA[s] * (nua[:, None] * l1b[None, :] + nub[None, :] * l1a[:, None]) + \
+        4.0 * 2.0 ** -53 * np.abs(C_ref).astype(np.float64)
+
+
+def _rand(rng, *shape):
+    return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+
+
+def _run(T, opA, A, B, s, flags=0, M=None):
+    import paper_2508_18468_b200 as P
+    K, N = B.shape
+    if M is None:
+        M = A.shape[1] if opA else A.shape[0]
+    dA, dB = dev(T, A), dev(T, B)
+    dC = T.full((M, N), complex(7.0, 7.0), dtype=T.complex128, device="cuda")
+    st = T.cuda.current_stream().cuda_stream
+    r = P.lib().traj_zgemm_ozaki(st, opA, M, N, K, dA.data_ptr(), A.shape[1], dB.data_ptr(), N, dC.data_ptr(), N, s,
+                                 flags)
+    assert r == 0, P.lib().traj_last_error(None)
+    return dC.cpu().numpy()
+
+
+@pytest.mark.parametrize("M,N,K", [(300, 200, 100), (129, 17, 534), (520, 300, 778), (16, 16, 16), (257, 513, 1300)])
+@pytest.mark.parametrize("s", [8, 16])
+def test_zgemm_ozaki_matches_extended_precision(T, M, N, K, s):
+    rng = np.random.default_rng(M + 3 * N + 5 * K + s)
+    A = _rand(rng, M, K) * (10.0 ** rng.integers(-6, 7, size=(M, 1)))   # rows spanning 12 decades
+    B = _rand(rng, K, N) * (10.0 ** rng.integers(-6, 7, size=(1, N)))
+    A[M // 2] = 0.0
+    ref = _ld(A) @ _ld(B)
+    got = _run(T, 0, A, B, s)
+    err = np.abs(got - ref.astype(np.complex128))
+    assert (err <= _bound(A, B, ref, s)).all()
+    assert np.all(got[M // 2] == 0)
+    if s == 16:   # at 16 moduli the result is as accurate as an FP64 GEMM's (here: within 2^-50 relative)
+        assert (err <= 2.0 ** -50 * (np.abs(A) @ np.abs(B))).all()
+
+
+@pytest.mark.parametrize("N,K", [(200, 300), (300, 1000), (64, 5000)])
+def test_zgemm_ozaki_gram_form(T, N, K):
+    """A^dag B and the Gram A^dag A (upper only) with orthonormal-ish columns, as in CholeskyQR."""
+    rng = np.random.default_rng(N + K)
+    A, _ = np.linalg.qr(_rand(rng, K, N))
+    A = A + 1e-7 * _rand(rng, K, N)
+    B = _rand(rng, K, N)
+    ref = _ld(A).conj().T @ _ld(B)
+    got = _run(T, 1, A, B, 16)
+    assert (np.abs(got - ref.astype(np.complex128)) <= _bound(A.conj().T, B, ref, 16)).all()
+    G = _run(T, 1, A, A, 16, flags=16)
+    Gref = (_ld(A).conj().T @ _ld(A)).astype(np.complex128)
+    iu = np.triu_indices(N)
+    assert np.abs(G[iu] - Gref[iu]).max() < 1e-16 * K ** 0.5
+    il = np.tril_indices(N, -1)
+    assert np.all(G[il] == complex(7.0, 7.0))   # below the diagonal untouched
+    # E = G - I to high relative accuracy (what the second CholeskyQR pass needs)
+    E = G - np.eye(N)
+    Eref = Gref - np.eye(N)
+    assert np.abs(E[iu] - Eref[iu]).max() <= 1e-3 * np.abs(Eref[iu]).max() + 1e-17
+
+
+def test_zgemm_ozaki_triangular_b(T):
+    rng = np.random.default_rng(5)
+    L, N = 700, 300
+    U = _rand(rng, L, N)
+    X = np.triu(_rand(rng, N, N))
+    ref = _ld(U) @ _ld(X)
+    got = _run(T, 0, U, X, 16, flags=4)
+    assert (np.abs(got - ref.astype(np.complex128)) <= _bound(U, X, ref, 16)).all()
+
+
+def test_zgemm_ozaki_banded_propagator_operand(T):
+    """K = exp(-i H dt) rows on a ring: entries decay from ~1 to below 1e-300 -- the fixed-point rows
+    drop what FP64 could not add anyway; the product matches at FP64 accuracy."""
+    from scipy.linalg import expm
+    L, N = 512, 256
+    H = np.zeros((L, L))
+    for i in range(L):
+        H[i, (i + 1) % L] = H[(i + 1) % L, i] = -1.0
+    Kp = expm(-1j * 0.05 * H)
+    rng = np.random.default_rng(9)
+    U, _ = np.linalg.qr(_rand(rng, L, N))
+    ref = _ld(Kp) @ _ld(U)
+    got = _run(T, 0, Kp, U, 16)
+    assert np.abs(got - ref.astype(np.complex128)).max() < 4e-17
+
+
+def test_zgemm_ozaki_rejects(T):
+    import paper_2508_18468_b200 as P
+    st = T.cuda.current_stream().cuda_stream
+    A = T.zeros(16, 16, dtype=T.complex128, device="cuda")
+    lib = P.lib()
+    assert lib.traj_zgemm_ozaki(st, 0, 16, 16, 16, A.data_ptr(), 16, A.data_ptr(), 16, A.data_ptr(), 16, 7, 0) == 1
+    assert lib.traj_zgemm_ozaki(st, 2, 16, 16, 16, A.data_ptr(), 16, A.data_ptr(), 16, A.data_ptr(), 16, 16, 0) == 1
+    assert lib.traj_zgemm_ozaki(st, 0, 16, 16, 16, A.data_ptr(), 8, A.data_ptr(), 16, A.data_ptr(), 16, 16, 0) == 1

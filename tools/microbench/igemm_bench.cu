@@ -1,0 +1,93 @@
+// Standalone check + timing of the INT8 tcgen05 GEMM (csrc/igemm.cu): exactness against a CPU
+// int64 reference on ragged shapes (both epilogues, the upper / triangular flags), then the
+// throughput of big square and K.U-shaped products.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2508_18468_b200/csrc \
+//        tools/microbench/igemm_bench.cu -o /tmp/igemm_bench -lcuda
+#include "../../paper_2508_18468_b200/csrc/igemm.cu"
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <random>
+namespace traj { std::atomic<long long> g_kernel_launches{0}; }
+using namespace traj;
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e_), __LINE__); exit(1);} } while (0)
+
+static int check(long long M, long long N, long long K, int batch, int out, int flags) {
+  const long long lda = (K + 15) / 16 * 16, ldc = (N + 15) / 16 * 16;
+  std::vector<int8_t> A(batch * M * lda), B(batch * N * lda);
+  std::mt19937 rng(1234 + M + N + K);
+  for (auto& x : A) x = (int8_t)(rng() & 255);
+  for (auto& x : B) x = (int8_t)(rng() & 255);
+  if (flags & IG_TRI_B)   // B[n][k] = 0 for k > n
+    for (int z = 0; z < batch; ++z) for (long long n = 0; n < N; ++n) for (long long k = n + 1; k < K; ++k) B[(z * N + n) * lda + k] = 0;
+  int mods[2] = {251, 256};
+  int8_t *dA, *dB; void* dC; int* dm;
+  const size_t esz = out == IG_OUT_I32 ? 4 : 1;
+  CK(cudaMalloc(&dA, A.size())); CK(cudaMalloc(&dB, B.size())); CK(cudaMalloc(&dC, batch * M * ldc * esz)); CK(cudaMalloc(&dm, 8));
+  CK(cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dB, B.data(), B.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dm, mods, 8, cudaMemcpyHostToDevice));
+  CK(cudaMemset(dC, 0x5a, batch * M * ldc * esz));
+  IgemmArgs g; g.M = M; g.N = N; g.K = K; g.batch = batch; g.A = dA; g.lda = lda; g.strideA = M * lda;
+  g.B = dB; g.ldb = lda; g.strideB = N * lda; g.C = dC; g.ldc = ldc; g.strideC = M * ldc; g.out = out; g.moduli = dm; g.nmod = 2; g.flags = flags;
+  std::string err;
+  int s = igemm(0, g, &err);
+  if (s) { printf("igemm failed %d %s\n", s, err.c_str()); return 1; }
+  CK(cudaDeviceSynchronize());
+  std::vector<uint8_t> C(batch * M * ldc * esz);
+  CK(cudaMemcpy(C.data(), dC, C.size(), cudaMemcpyDeviceToHost));
+  long long bad = 0, checked = 0;
+  for (int z = 0; z < batch; ++z) for (long long m = 0; m < M; ++m) for (long long n = 0; n < N; ++n) {
+    if ((flags & IG_UPPER) && (n / 256 + 1) * 256 - 1 < (m / 128) * 128) continue;
+    long long acc = 0;
+    for (long long k = 0; k < K; ++k) acc += (long long)A[(z * M + m) * lda + k] * B[(z * N + n) * lda + k];
+    long long got;
+    if (out == IG_OUT_I32) got = reinterpret_cast<int*>(C.data())[(z * M + m) * ldc + n];
+    else { got = C[(z * M + m) * ldc + n]; int md = mods[z % 2]; acc = ((acc % md) + md) % md; }
+    ++checked;
+    if (got != acc) { if (bad < 5) printf("  mismatch z=%d m=%lld n=%lld got %lld want %lld\n", z, m, n, got, acc); ++bad; }
+  }
+  printf("check M=%lld N=%lld K=%lld batch=%d out=%d flags=%d: %lld/%lld bad\n", M, N, K, batch, out, flags, bad, checked);
+  cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(dm);
+  return bad != 0;
+}
+
+static void timeit(long long M, long long N, long long K, int batch, int out) {
+  const long long lda = K, ldc = N;
+  int8_t *dA, *dB; void* dC; int* dm;
+  int mods[2] = {251, 256};
+  CK(cudaMalloc(&dA, batch * M * lda)); CK(cudaMalloc(&dB, batch * N * lda));
+  CK(cudaMalloc(&dC, batch * M * ldc * (out == IG_OUT_I32 ? 4 : 1))); CK(cudaMalloc(&dm, 8));
+  CK(cudaMemcpy(dm, mods, 8, cudaMemcpyHostToDevice));
+  CK(cudaMemset(dA, 3, batch * M * lda)); CK(cudaMemset(dB, 5, batch * N * lda));
+  IgemmArgs g; g.M = M; g.N = N; g.K = K; g.batch = batch; g.A = dA; g.lda = lda; g.strideA = M * lda;
+  g.B = dB; g.ldb = lda; g.strideB = N * lda; g.C = dC; g.ldc = ldc; g.strideC = M * ldc; g.out = out; g.moduli = dm; g.nmod = 2;
+  std::string err;
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  for (int i = 0; i < 3; ++i) igemm(0, g, &err);
+  CK(cudaDeviceSynchronize());
+  const int reps = 5;
+  cudaEventRecord(e0);
+  for (int i = 0; i < reps; ++i) igemm(0, g, &err);
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= reps;
+  const double ops = 2.0 * M * N * K * batch;
+  printf("time M=%lld N=%lld K=%lld batch=%d out=%d: %.3f ms  %.1f TOPS\n", M, N, K, batch, out, ms, ops / ms / 1e9);
+  cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(dm);
+}
+
+int main(int argc, char** argv) {
+  int bad = 0;
+  bad |= check(300, 520, 1000, 2, IG_OUT_I32, 0);
+  bad |= check(128, 256, 128, 1, IG_OUT_I32, 0);
+  bad |= check(300, 520, 1000, 2, IG_OUT_MOD, 0);
+  bad |= check(700, 700, 700, 1, IG_OUT_I32, IG_UPPER);
+  bad |= check(400, 700, 700, 1, IG_OUT_I32, IG_TRI_B);
+  if (bad) { printf("CHECK FAILED\n"); return 1; }
+  timeit(8192, 8192, 8192, 1, IG_OUT_I32);
+  timeit(8192, 8192, 8192, 4, IG_OUT_MOD);
+  timeit(16384, 8192, 16384, 6, IG_OUT_MOD);
+  return 0;
+}
