@@ -37,6 +37,22 @@ import workloads  # noqa: E402
 
 HBM_PEAK_GBS = 6536.7         # MEASURED_PEAKS.json hbm_gbs (copy bandwidth on this pool's B200)
 FP64_PEAK_TFLOPS = 37.1        # measured DMMA.8x8x4 issue-rate peak, profiles/r01_fp64_microbench.txt
+
+def _measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+_MP = _measured_peaks()
+# INT8 tensor peak: no measured INT8 entry, so the measured bf16 cuBLAS figure x the nominal dense ratio
+# 4.5 / 2.25 (B200_PROFILING.md); the sustained figure (power-capped seconds-long loop) for a kernel
+# timed inside a long step, the burst one for context
+INT8_PEAK_TOPS = 2.0 * float(_MP.get("bf16_tflops_sustained", 1397.9))
+INT8_PEAK_BURST_TOPS = 2.0 * float(_MP.get("bf16_tflops", 1655.2))
+INT8_PEAK_SOURCE = ("MEASURED_PEAKS.json bf16_tflops_sustained x 2 (nominal dense INT8 / bf16 = 4.5 / 2.25); "
+                    f"burst bf16_tflops x 2 = {INT8_PEAK_BURST_TOPS:.0f} TOPS")
 FP64_PEAK_SOURCE = ("measured on this pool's B200: DMMA.8x8x4 microbenchmark 37.1 TF/s (cuBLAS ZGEMM 37.0 TF/s), "
                     "profiles/r01_fp64_microbench.txt; MEASURED_PEAKS.json has no FP64 entry "
                     "(bf16 x 40/2250 nominal ratio would give 29.4)")
@@ -293,7 +309,8 @@ def run_ours(args):
     ms_max = max_over_ranks(ms, world)
     value = (1 if shard else world) * tpg * args.steps / (ms_max / 1e3)
     rows = w.L // world if shard else w.L
-    roof, executed, hbm, library = roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P)
+    oz = tr.ozaki_info() if not shard else (False, False, 0)
+    roof, executed, hbm, library = roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P, oz)
     # ---- row a4, timed separately (north star: "eigvalsh on C_A at sampled times, timed
     # separately"): the config's sampled observables once, after the timed steps
     obs = None
@@ -334,13 +351,14 @@ def run_ours(args):
         "value": value, "unit": "trajectory-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong" if shard else "weak",
         "vs_baseline": None,
-        "dtype": "c128 (f64 arithmetic)", "data": "synthetic (Neel start, Philox randoms, seed 0)",
+        "dtype": dtype_of(oz), "data": "synthetic (Neel start, Philox randoms, seed 0)",
         "config": describe(w, tpg, mode, world, args),
         "roofline": roof,
-        "step_executed_dmma": executed,
+        "step_executed": executed,
         "library_same_shape": library,
         "hbm_kernels": hbm or None,
         "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
+        "phases_nested": {"ku_mma": "propagate", "gram_mma": "gram", "trmm_mma": "trmm"},
         "phase_launches_per_step": {k: v[1] / args.steps for k, v in phases.items()},
         "gpu_launches": launches,
         "sampled_observables_ms": obs,
@@ -369,7 +387,15 @@ def strassen_levels(w, P: int = 1, T: int = 1) -> int:
     return 3 if want >= 3 and three_ok else (2 if want >= 2 and two_ok else 1)
 
 
-def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P):
+def dtype_of(oz):
+    if oz and (oz[0] or oz[1]):
+        parts = [x for x, on in (("K U", oz[0]), ("the CholeskyQR Grams / TRMMs", oz[1])) if on]
+        return (f"c128 (FP64 values; {' and '.join(parts)} as exact modular products on the INT8 tensor cores, "
+                f"{oz[2]} moduli = 61-bit operand rows/columns, CRT to FP64; the rest FP64 on DMMA / FP64 pipes)")
+    return "c128 (f64 arithmetic)"
+
+
+def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P, oz=(False, False, 0)):
     """Roofline of the dominant phase (the largest device time per step) on EXECUTED flops.
 
     Work per step in conventional 8mnk complex flops, per GPU (rows = L/P of the
@@ -474,6 +500,43 @@ def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P):
                              ("ncu dram bytes of the propagate phase (profiles/ncu_traffic.json: split, the "
                               "three real 16384x8192x16384 products as one batch-3 launch, combine) vs 8.6 GB "
                               "algorithmic")) if traffic else None}
+    oz_dom = (oz[0] and dom == "propagate") or (oz[1] and dom in ("gram", "trmm"))
+    if oz_dom:
+        # the dominant phase is an exact modular product (csrc/ozaki.h): 3 s INT8 products per complex
+        # product (3M in the residues, s moduli); algorithmic INT8 ops (2 per MAC) over the nested
+        # phase that times the INT8 tensor-core launch alone; its phase time adds the residue
+        # splits and the CRT combine
+        s_ = oz[2]
+        mma_ph = {"propagate": "ku_mma", "gram": "gram_mma", "trmm": "trmm_mma"}[dom]
+        mma_ms = phases[mma_ph][0] / args.steps
+        per = {"propagate": 2.0 * 3 * s_ * rows * w.L * w.N * tpg,
+               "gram": n_gram * 2.0 * 3 * s_ * (w.N * w.N / 2.0) * rows * tpg,
+               "trmm": n_trmm * 2.0 * 3 * s_ * rows * (w.N * w.N / 2.0) * tpg}[dom]
+        tops = per / (mma_ms / 1e3) / 1e12
+        eqp = flops8 / (kern_ms / 1e3) / 1e12
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        traffic = None
+        if os.path.exists(tp) and dom == "propagate":
+            try:
+                traffic = json.load(open(tp)).get(w.name, {}).get(f"ku_ozaki{s_}_igemm_dram_bytes")
+            except Exception:
+                traffic = None
+        roof = {"bound": "tensor", "achieved": tops, "peak": INT8_PEAK_TOPS, "unit": "TOPS (INT8)",
+                "frac": tops / INT8_PEAK_TOPS, "traffic": traffic,
+                "kernel": ("igemm_i8_kernel (tcgen05.mma.kind::i8, TMEM accumulators, TMA 128B-swizzled K-major "
+                           f"tiles, 128x256x128 CTA tile, persistent): one launch of the 3 x {s_} residue products "
+                           + {"propagate": "of U <- K U (K's residues formed once)",
+                              "gram": "of G = U^dag U (upper tiles)",
+                              "trmm": "of U <- U R^-1 (triangular k-blocks skipped)"}[dom]),
+                "kernel_ms": mma_ms, "timed": ("device time of the INT8 launch per step (CUDA events around it on "
+                                                "the handle's stream, nested phase " + mma_ph + ")"),
+                "ops_counted": (f"2 x 3 x {s_} x (the complex product's m n k; half for the Gram's and TRMM's "
+                                "triangles) INT8 multiply-adds: algorithmic, tile waste not counted"),
+                "peak_source": INT8_PEAK_SOURCE,
+                "phase_ms": kern_ms, "phase_note": "the phase adds U's residue split and the CRT combine",
+                "fp64_equiv_tflops": eqp, "fp64_equiv_frac_of_dmma_peak": eqp / FP64_PEAK_TFLOPS,
+                "fp64_equiv_note": (f"conventional 8mnk complex flops of the phase over its whole time, against the "
+                                    f"{FP64_PEAK_TFLOPS} TF/s DMMA peak: an equivalent, not a pipe fraction")}
     if w.name == "c1":
         roof["note"] = ("c1 is latency-bound (SURVEY §8(d)): L = 64, one fused launch per step with one CTA per "
                         "trajectory, whose ~140 barriers and dependent pivots set the time; the fraction is not a "
@@ -501,9 +564,18 @@ def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P):
     executed = None
     if not fused and not (args.orthonormalizer == "lowrank" and w.protocol == "projective" and not shard) \
             and w.protocol in ("projective", "homodyne"):
-        fl = sum(f * a for f, a in step8.values()) * tpg
+        # phases on the INT8 modular path leave the DMMA sum: their INT8 ops are counted apart
+        int8_ph = ({"propagate"} if oz[0] else set()) | ({"gram", "trmm"} if oz[1] else set())
+        i8 = sum(3 * oz[2] * 2.0 * (step8[k][0] / 8.0) for k in int8_ph)   # 8mnk / 8 = complex MACs
+        fl = sum(f * a for k, (f, a) in step8.items() if k not in int8_ph) * tpg
+        i8 *= tpg
         t = ms / args.steps / 1e3
         executed = {"tflops": fl / t / 1e12, "frac": fl / t / 1e12 / FP64_PEAK_TFLOPS, "flops_per_step": fl,
+                    "engine_note": ("tflops / frac: DMMA (FP64 tensor pipe) flops of the phases still on it, over the "
+                                    "whole step time" + ("; int8_*: the modular products' INT8 ops (2 x 3 s per "
+                                                         "complex m n k) over the whole step time" if int8_ph else "")),
+                    "int8_phases": sorted(int8_ph),
+                    "int8_ops_per_step": i8 or None, "int8_tops": (i8 / t / 1e12) if i8 else None,
                     "model": ("per step (and per shard, rows = L/P): K U 8 rows L N; the measured Gram(s) 4 rows N^2; "
                               "the projective update 16 rows N k1 + C_SS 8 |S|^2 N; " +
                               ("CholeskyQR pass 1 on the structure of I - V^dag V (k0 = |S| - k1 zeroed rows, "
@@ -606,7 +678,20 @@ def run_secondary(args, world, rank, P, steps=2, warmup=2):
            "unit": "trajectory-steps/s", "scaling": "strong" if shard else "weak",
            "ms_per_step": ms / steps, "steps": steps, "warmup": warmup,
            "phases_ms_per_step": {k: v[0] / steps for k, v in ph.items()}}
-    if args.propagator == "dense" and prop > 0:
+    oz = (False, False, 0)
+    if args.propagator == "dense" and prop > 0 and ph.get("ku_mma", (0.0,))[0] > 0:
+        # the modular INT8 K U (csrc/ozaki.h): the INT8 launch alone against the INT8 peak
+        oz_s = int(os.environ.get("TRAJ_OZAKI_MODULI", "16"))
+        mma = ph["ku_mma"][0] / steps
+        tops = 2.0 * 3 * oz_s * rows * w.L * w.N / (mma / 1e3) / 1e12
+        eq8 = 8.0 * rows * w.L * w.N / (prop / 1e3) / 1e12
+        out["roofline_propagate"] = {"bound": "tensor", "achieved": tops, "peak": INT8_PEAK_TOPS, "unit": "TOPS (INT8)",
+                                     "frac": tops / INT8_PEAK_TOPS, "kernel_ms": mma, "phase_ms": prop,
+                                     "kernel": f"igemm_i8_kernel: the 3 x {oz_s} residue products of K U",
+                                     "fp64_equiv_tflops": eq8, "fp64_equiv_frac_of_dmma_peak": eq8 / FP64_PEAK_TFLOPS,
+                                     "peak_source": INT8_PEAK_SOURCE}
+        oz = (True, True, oz_s)
+    elif args.propagator == "dense" and prop > 0:
         eq8 = 8.0 * rows * w.L * w.N / (prop / 1e3) / 1e12
         a = 0.75 if P.traj_get_zgemm_algorithm() == "3m" or os.environ.get("TRAJ_PLANAR_KU", "1") != "0" else 1.0
         if os.environ.get("TRAJ_PLANAR_KU", "1") != "0":

@@ -233,8 +233,16 @@ enum { TRAJ_PH_PROPAGATE = 0,  /* U <- K U                                   */
        TRAJ_PH_CHOL = 4,       /* Cholesky + triangular inverse of G         */
        TRAJ_PH_TRMM = 5,       /* U <- U R^-1                                */
        TRAJ_PH_FUSED = 6,      /* the fused small-lattice step (all rows)    */
-       TRAJ_NPHASES = 7 };
+       /* nested (not additive): the INT8 tensor-core launch of the modular products inside the
+        * propagate, Gram and TRMM phases (traj_ozaki_info) */
+       TRAJ_PH_KU_MMA = 7, TRAJ_PH_GRAM_MMA = 8, TRAJ_PH_TRMM_MMA = 9,
+       TRAJ_NPHASES = 10 };
 int traj_profile(traj_handle h, int enable);
+/* Which contractions of this handle run as exact modular products on the INT8 tensor cores
+ * (csrc/ozaki.h; environment TRAJ_OZAKI=0 selects the FP64 DMMA kernels instead):
+ * out[0] = the dense K U, out[1] = the CholeskyQR Grams and TRMMs, out[2] = the modulus count
+ * (16: every operand row / column to 2^-62 of its 2-norm). */
+int traj_ozaki_info(traj_handle h, int32_t* out3);
 int traj_phase_times(traj_handle h, double* ms, int64_t* launches);
 
 /* Row sharding: *shard_size = P, *local_shards = shards held by this handle (1, or P in

@@ -21,7 +21,8 @@ TRAJ_INIT_NEEL = 0
 TRAJ_INIT_CHECKERBOARD = 1
 TRAJ_PROP_DENSE, TRAJ_PROP_BANDED = 0, 1
 TRAJ_TRI_A_UPPER, TRAJ_TRI_A_LOWER, TRAJ_TRI_B_UPPER, TRAJ_TRI_B_LOWER, TRAJ_C_UPPER = 1, 2, 4, 8, 16
-PHASES = ("propagate", "monitor", "project", "gram", "chol", "trmm", "fused")
+PHASES = ("propagate", "monitor", "project", "gram", "chol", "trmm", "fused", "ku_mma", "gram_mma", "trmm_mma")
+NESTED_PHASES = ("ku_mma", "gram_mma", "trmm_mma")   # inside propagate / gram / trmm: not additive
 STATUS = {0: "TRAJ_OK", 1: "TRAJ_EINVAL", 2: "TRAJ_ECONFIG", 3: "TRAJ_ENUMERIC", 4: "TRAJ_ECUDA",
           5: "TRAJ_ENCCL", 6: "TRAJ_EDOMAIN"}
 
@@ -86,6 +87,7 @@ _SIGS = {
                                           ctypes.POINTER(_I64)]),
     "traj_profile": (ctypes.c_int, [_P, ctypes.c_int]),
     "traj_phase_times": (ctypes.c_int, [_P, ctypes.POINTER(_D), ctypes.POINTER(_I64)]),
+    "traj_ozaki_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int32)]),
     "traj_kernel_launches": (ctypes.c_longlong, []),
     "traj_destroy": (ctypes.c_int, [_P]),
     "traj_last_error": (ctypes.c_char_p, [_P]),
@@ -415,6 +417,12 @@ class Trajectories:
     # -- profiling
     def profile(self, enable: bool = True):
         self._c(lib().traj_profile(self._h, 1 if enable else 0))
+
+    def ozaki_info(self):
+        """(K U on the INT8 modular path, Gram/TRMM on it, modulus count)."""
+        out = (ctypes.c_int32 * 3)()
+        self._c(lib().traj_ozaki_info(self._h, out))
+        return bool(out[0]), bool(out[1]), int(out[2])
 
     def phase_times(self):
         ms = (ctypes.c_double * len(PHASES))()

@@ -71,6 +71,9 @@ struct KArgs {
   int flags;
   int oz_s, oz_T, oz_a_traj, oz_b_traj;
   int oz_pa[3], oz_pb[3];
+  const int32_t* gate;
+  const int32_t* kdev;
+  const int32_t* ndev;
 };
 
 // batch entry z -> (A entry, B entry, modulus index)
@@ -105,19 +108,24 @@ __device__ __forceinline__ Tile tile_of(const KArgs& a, long long t) {
   return r;
 }
 
+__device__ __forceinline__ int traj_of(const KArgs& a, int z) { return a.oz_s ? z % a.oz_T : z; }
+
 __device__ __forceinline__ bool tile_live(const KArgs& a, const Tile& t) {
-  if (a.flags & IG_UPPER) return (t.nb + 1) * IBN - 1 >= t.mb * IBM;
+  if ((a.flags & IG_UPPER) && (t.nb + 1) * IBN - 1 < t.mb * IBM) return false;
+  if (a.ndev && t.nb * IBN >= a.ndev[traj_of(a, t.z)]) return false;
   return true;
 }
 
 __device__ __forceinline__ int tile_kblocks(const KArgs& a, const Tile& t) {
   int kend = a.K;
   if (a.flags & IG_TRI_B) kend = min(kend, (t.nb + 1) * IBN);
+  if (a.kdev) kend = min(kend, a.kdev[traj_of(a, t.z)]);
   return (kend + IBK - 1) / IBK;
 }
 
 __global__ void __launch_bounds__(ITHREADS, 1)
     igemm_i8_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const KArgs a) {
+  if (a.gate && *a.gate == 0) return;   // uniform over the grid: no TMEM allocated, no barrier used
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* base = smem_raw + (base_u32 - smem_u32(smem_raw));
@@ -221,6 +229,7 @@ __global__ void __launch_bounds__(ITHREADS, 1)
       tc_fence_after();
       const int row = tl.mb * IBM + q * 32 + lane;
       const bool row_ok = row < a.M;
+      const bool kzero = tile_kblocks(a, tl) == 0;   // empty contraction: the accumulator was never written
       const uint32_t taddr = tmem + buf * IBN + ((uint32_t)(q * 32) << 16);
       int mod = 0;
       double inv = 0.0;
@@ -235,6 +244,10 @@ __global__ void __launch_bounds__(ITHREADS, 1)
         uint32_t v[32];
         __syncwarp();
         tmem_ld32(taddr + c * 32, v);
+        if (kzero) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0;
+        }
         const int col = tl.nb * IBN + c * 32;
         if (!row_ok || col >= a.N) {
         } else if (a.out == IG_OUT_I32) {
@@ -371,6 +384,9 @@ int igemm(cudaStream_t st, const IgemmArgs& g, std::string* err) {
   a.oz_T = g.oz_T;
   a.oz_a_traj = g.oz_a_traj;
   a.oz_b_traj = g.oz_b_traj;
+  a.gate = g.gate;
+  a.kdev = g.kdev;
+  a.ndev = g.ndev;
   for (int i = 0; i < 3; ++i) {
     a.oz_pa[i] = g.oz_pa[i];
     a.oz_pb[i] = g.oz_pb[i];

@@ -40,6 +40,12 @@ struct IgemmArgs {
   int oz_pa[3] = {0, 1, 2}, oz_pb[3] = {0, 1, 2};
   int oz_a_traj = 0, oz_b_traj = 1;
   long long oz_na = 0, oz_nb = 0;
+  const int32_t* gate = nullptr;   // device flag: when set and *gate == 0 the launch does nothing
+  // device bounds per trajectory t (modular map) or per batch entry (plain): the contraction runs over
+  // k < kdev[t] only (whole 128-k blocks; the operands must hold zeros in [kdev, round_up(kdev, 128))),
+  // and 256-column tiles at n >= ndev[t] are skipped (their outputs are not written)
+  const int32_t* kdev = nullptr;
+  const int32_t* ndev = nullptr;
 };
 
 // Needs lda, ldb multiples of 16 bytes, 16-byte aligned A/B, ldc a multiple of 16 elements and C

@@ -149,33 +149,38 @@ __device__ __forceinline__ void planes_of(long long vr, long long vi, int conj, 
 
 __device__ __forceinline__ long long to_int(double v, int e) { return __double2ll_rn(scalbn(v, e)); }
 
-template <int S, int Q = 0>
+template <int S, int NP, int Q = 0>
 struct RowStore {
   // 4 consecutive elements -> one 32-bit word per (plane, modulus)
   __device__ __forceinline__ static void run(const long long (&vr)[4], const long long (&vi)[4], int conj, int8_t* R,
                                              long long pstride, long long qstride) {
     if constexpr (Q < S) {
-      uint32_t w[3] = {0, 0, 0};
+      uint32_t w[NP];
+#pragma unroll
+      for (int p = 0; p < NP; ++p) w[p] = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         uint32_t b[4];
         planes_of<Q>(vr[k], vi[k], conj, b);
 #pragma unroll
-        for (int p = 0; p < 3; ++p) w[p] |= b[p] << (8 * k);
+        for (int p = 0; p < NP; ++p) w[p] |= b[p] << (8 * k);
       }
 #pragma unroll
-      for (int p = 0; p < 3; ++p) *reinterpret_cast<uint32_t*>(R + p * pstride + Q * qstride) = w[p];
-      RowStore<S, Q + 1>::run(vr, vi, conj, R, pstride, qstride);
+      for (int p = 0; p < NP; ++p) *reinterpret_cast<uint32_t*>(R + p * pstride + Q * qstride) = w[p];
+      RowStore<S, NP, Q + 1>::run(vr, vi, conj, R, pstride, qstride);
     }
   }
 };
 
-template <int S>
+template <int S, int NP>
 __global__ void __launch_bounds__(256) oz_split_rows_kernel(const cplx* __restrict__ X, long long ldx, long long sX,
-                                                            int rows, int cols, int T, int conj, int8_t* R, long long ldr,
-                                                            int* e, long long sE, int beta) {
+                                                            int rows, int cols_cap, int T, int conj, int8_t* R,
+                                                            long long ldr, int* e, long long sE, int beta,
+                                                            const int32_t* gate, const int32_t* cdev) {
+  if (gate && *gate == 0) return;
   const int row = blockIdx.x, t = blockIdx.y;
   const cplx* x = X + t * sX + (long long)row * ldx;
+  const int cols = cdev ? min(cols_cap, cdev[t]) : cols_cap;   // past it: zero residues
   __shared__ double red[8];
   __shared__ int ex_s;
   double acc = 0.0;
@@ -198,7 +203,7 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const cplx* __restri
   const int ex = ex_s;
   const long long qstride = (long long)T * rows * ldr, pstride = (long long)S * qstride;
   int8_t* Rrow = R + (long long)t * rows * ldr + (long long)row * ldr;
-  for (int j0 = 4 * threadIdx.x; j0 < cols; j0 += 1024) {
+  for (int j0 = 4 * threadIdx.x; j0 < cols_cap; j0 += 1024) {
     long long vr[4], vi[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -210,13 +215,15 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const cplx* __restri
         vr[k] = vi[k] = 0;
       }
     }
-    RowStore<S>::run(vr, vi, conj, Rrow + j0, pstride, qstride);
+    RowStore<S, NP>::run(vr, vi, conj, Rrow + j0, pstride, qstride);
   }
 }
 
 // per-column partial sums of (|re| + |im|)^2 over 8 row chunks: part[(c T + t) cols + j]
 __global__ void __launch_bounds__(256) oz_colnorm_kernel(const cplx* __restrict__ X, long long ldx, long long sX,
-                                                         int rows, int cols, int T, double* part) {
+                                                         int rows, int cols, int T, double* part, int subI,
+                                                         const int32_t* gate) {
+  if (gate && *gate == 0) return;
   const int j = blockIdx.x * 32 + threadIdx.x, c = blockIdx.y, t = blockIdx.z;
   const int per = (rows + 7) / 8, r0 = c * per, r1 = min(rows, r0 + per);
   double acc = 0.0;
@@ -224,7 +231,7 @@ __global__ void __launch_bounds__(256) oz_colnorm_kernel(const cplx* __restrict_
     const cplx* x = X + t * sX + j;
     for (int i = r0 + threadIdx.y; i < r1; i += 8) {
       const cplx v = x[(long long)i * ldx];
-      const double a = fabs(v.x) + fabs(v.y);
+      const double a = fabs(v.x - (subI && i == j ? 1.0 : 0.0)) + fabs(v.y);
       acc = fma(a, a, acc);
     }
   }
@@ -294,20 +301,27 @@ __device__ __forceinline__ void col_store(const Digits (&dr)[16], const Digits (
 template <int S, int NP>
 __global__ void __launch_bounds__(256) oz_split_cols_kernel(const cplx* __restrict__ X, long long ldx, long long sX,
                                                             int rows, int cols, int T, int8_t* R, long long ldr,
-                                                            int* e, long long sE, const double* part, int beta) {
+                                                            int* e, long long sE, const double* part, int beta,
+                                                            int subI, const int32_t* gate, const int32_t* cdev) {
+  if (gate && *gate == 0) return;
   extern __shared__ cplx tile[];   // [CT rows][CT + 1]
   const int j0 = blockIdx.x * CT, i0 = blockIdx.y * CT, t = blockIdx.z;
+  const int cz = cdev ? min(cols, cdev[t]) : cols;   // columns past cz are taken as zero
   const cplx* x = X + t * sX;
   for (int r = threadIdx.x / CT; r < CT; r += 256 / CT) {
     const int i = i0 + r, j = j0 + (threadIdx.x % CT);
-    tile[r * (CT + 1) + (threadIdx.x % CT)] = (i < rows && j < cols) ? x[(long long)i * ldx + j] : make_double2(0.0, 0.0);
+    cplx v = (i < rows && j < cz) ? x[(long long)i * ldx + j] : make_double2(0.0, 0.0);
+    if (subI && i == j) v.x -= 1.0;
+    tile[r * (CT + 1) + (threadIdx.x % CT)] = v;
   }
   __syncthreads();
   const int jj = threadIdx.x >> 2, ig = (threadIdx.x & 3) * 16, j = j0 + jj;
   if (j >= cols || i0 + ig >= rows) return;
   double nu2 = 0.0;
+  if (j < cz) {
 #pragma unroll
-  for (int c = 0; c < 8; ++c) nu2 += part[((long long)c * T + t) * cols + j];
+    for (int c = 0; c < 8; ++c) nu2 += part[((long long)c * T + t) * cols + j];
+  }
   const int ex = scale_exp(nu2, beta);
   if (blockIdx.y == 0 && ig == 0) e[t * sE + j] = ex;
   Digits dr[16], di[16];
@@ -369,9 +383,12 @@ template <int S>
 __global__ void __launch_bounds__(128) oz_combine_kernel(const uint8_t* __restrict__ P, long long ldp, int M, int N,
                                                          int T, const int* __restrict__ eA, long long sEA, int a_traj,
                                                          const int* __restrict__ eB, long long sEB, int flags, cplx* C,
-                                                         long long ldc, long long sC) {
+                                                         long long ldc, long long sC, const cplx* base,
+                                                         const int32_t* gate, const int32_t* ndev) {
+  if (gate && *gate == 0) return;
   const int i = blockIdx.y, t = blockIdx.z;
   const int j0 = (blockIdx.x * 128 + threadIdx.x) * 4;
+  if (ndev) N = min(N, ndev[t]);
   if (j0 >= N) return;
   if ((flags & OZ_UPPER) && j0 + 3 < i) return;
   const long long qstride = (long long)T * M * ldp, pstride = (long long)S * qstride;
@@ -387,7 +404,15 @@ __global__ void __launch_bounds__(128) oz_combine_kernel(const uint8_t* __restri
     if (j >= N || ((flags & OZ_UPPER) && j < i)) continue;
     const int sc = -(ea + eB[t * sEB + j]);
     double2 v = make_double2(scalbn(crt_value(sr[k], lr[k], Md), sc), scalbn(crt_value(si[k], li[k], Md), sc));
-    if (flags & OZ_ACCUMULATE) {
+    if (flags & OZ_NEGATE) {
+      v.x = -v.x;
+      v.y = -v.y;
+    }
+    if (base) {
+      const double2 o = base[t * sC + (long long)i * ldc + j];
+      v.x += o.x;
+      v.y += o.y;
+    } else if (flags & OZ_ACCUMULATE) {
       const double2 o = c[j];
       v.x += o.x;
       v.y += o.y;
@@ -413,8 +438,14 @@ int dispatch_s(int s, A... args) {
 template <int S>
 struct LaunchRows {
   static int go(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T, int conj,
-                int8_t* R, long long ldr, int* e, long long sE, int beta) {
-    oz_split_rows_kernel<S><<<dim3(rows, T), 256, 0, st>>>(X, ldx, sX, rows, cols, T, conj, R, ldr, e, sE, beta);
+                int8_t* R, long long ldr, int* e, long long sE, int beta, const int32_t* gate, const int32_t* cdev,
+                int np) {
+    if (np == 4)
+      oz_split_rows_kernel<S, 4><<<dim3(rows, T), 256, 0, st>>>(X, ldx, sX, rows, cols, T, conj, R, ldr, e, sE, beta,
+                                                                gate, cdev);
+    else
+      oz_split_rows_kernel<S, 3><<<dim3(rows, T), 256, 0, st>>>(X, ldx, sX, rows, cols, T, conj, R, ldr, e, sE, beta,
+                                                                gate, cdev);
     return 0;
   }
 };
@@ -422,15 +453,18 @@ struct LaunchRows {
 template <int S>
 struct LaunchCols {
   static int go(cudaStream_t st, int np, const cplx* X, long long ldx, long long sX, int rows, int cols, int T,
-                int8_t* R, long long ldr, int* e, long long sE, const double* part, int beta) {
+                int8_t* R, long long ldr, int* e, long long sE, const double* part, int beta, int subI,
+                const int32_t* gate, const int32_t* cdev) {
     const int smem = CT * (CT + 1) * 16;
     dim3 grid(ceil_div(cols, CT), ceil_div(rows, CT), T);
     if (np == 4) {
       if (ensure_smem((const void*)oz_split_cols_kernel<S, 4>, smem) != cudaSuccess) return 4;
-      oz_split_cols_kernel<S, 4><<<grid, 256, smem, st>>>(X, ldx, sX, rows, cols, T, R, ldr, e, sE, part, beta);
+      oz_split_cols_kernel<S, 4><<<grid, 256, smem, st>>>(X, ldx, sX, rows, cols, T, R, ldr, e, sE, part, beta, subI,
+                                                          gate, cdev);
     } else {
       if (ensure_smem((const void*)oz_split_cols_kernel<S, 3>, smem) != cudaSuccess) return 4;
-      oz_split_cols_kernel<S, 3><<<grid, 256, smem, st>>>(X, ldx, sX, rows, cols, T, R, ldr, e, sE, part, beta);
+      oz_split_cols_kernel<S, 3><<<grid, 256, smem, st>>>(X, ldx, sX, rows, cols, T, R, ldr, e, sE, part, beta, subI,
+                                                          gate, cdev);
     }
     return 0;
   }
@@ -441,7 +475,7 @@ struct LaunchCombine {
   static int go(cudaStream_t st, const OzProduct& p) {
     dim3 grid(ceil_div(p.N, 512), p.M, p.T);
     oz_combine_kernel<S><<<grid, 128, 0, st>>>(p.RC, oz_ld(p.N), p.M, p.N, p.T, p.eA, p.sEA, p.a_traj, p.eB, p.sEB,
-                                               p.flags, p.C, p.ldc, p.sC);
+                                               p.flags, p.C, p.ldc, p.sC, p.base, p.gate, p.ndev);
     return 0;
   }
 };
@@ -462,7 +496,8 @@ int oz_supported(int s) { return s >= 4 && s <= 16 && s % 2 == 0; }
 int oz_beta(int s) { return oz_supported(s) ? host_const().beta[s] : 0; }
 
 int oz_split_rows(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T, int conj,
-                  int s, int8_t* R, int* e, long long sE, std::string* err) {
+                  int s, int8_t* R, int* e, long long sE, std::string* err, const int32_t* gate, const int32_t* cdev,
+                  int nplanes) {
   if (rows <= 0 || cols <= 0 || T <= 0) return 0;
   const int* md;
   if (!oz_supported(s) || rows >= 65536 * 32 || T > 65535) {
@@ -470,12 +505,17 @@ int oz_split_rows(cudaStream_t st, const cplx* X, long long ldx, long long sX, i
     return 1;
   }
   if (int r = ensure_device_constants(&md, err)) return r;
-  dispatch_s<LaunchRows>(s, st, X, ldx, sX, rows, cols, T, conj, R, oz_ld(cols), e, sE, oz_beta(s));
+  if (nplanes != 3 && nplanes != 4) {
+    if (err) *err = "oz_split_rows: 3 or 4 planes";
+    return 1;
+  }
+  dispatch_s<LaunchRows>(s, st, X, ldx, sX, rows, cols, T, conj, R, oz_ld(cols), e, sE, oz_beta(s), gate, cdev, nplanes);
   return launched("oz_split_rows", err);
 }
 
 int oz_split_cols(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T, int nplanes,
-                  int s, int8_t* R, int* e, long long sE, double* part, std::string* err) {
+                  int s, int8_t* R, int* e, long long sE, double* part, std::string* err, int sub_identity,
+                  const int32_t* gate, const int32_t* cdev) {
   if (rows <= 0 || cols <= 0 || T <= 0) return 0;
   const int* md;
   if (!oz_supported(s) || (nplanes != 3 && nplanes != 4) || T > 65535 || ceil_div(rows, CT) > 65535) {
@@ -483,9 +523,11 @@ int oz_split_cols(cudaStream_t st, const cplx* X, long long ldx, long long sX, i
     return 1;
   }
   if (int r = ensure_device_constants(&md, err)) return r;
-  oz_colnorm_kernel<<<dim3(ceil_div(cols, 32), 8, T), dim3(32, 8), 0, st>>>(X, ldx, sX, rows, cols, T, part);
+  oz_colnorm_kernel<<<dim3(ceil_div(cols, 32), 8, T), dim3(32, 8), 0, st>>>(X, ldx, sX, rows, cols, T, part,
+                                                                            sub_identity, gate);
   if (int r = launched("oz_colnorm", err)) return r;
-  if (dispatch_s<LaunchCols>(s, st, nplanes, X, ldx, sX, rows, cols, T, R, oz_ld(rows), e, sE, part, oz_beta(s))) {
+  if (dispatch_s<LaunchCols>(s, st, nplanes, X, ldx, sX, rows, cols, T, R, oz_ld(rows), e, sE, part, oz_beta(s),
+                             sub_identity, gate, cdev)) {
     if (err) *err = "oz_split_cols: shared memory attribute";
     return 4;
   }
@@ -493,6 +535,17 @@ int oz_split_cols(cudaStream_t st, const cplx* X, long long ldx, long long sX, i
 }
 
 int oz_product(cudaStream_t st, const OzProduct& p, std::string* err) {
+  if (int r = oz_product_mma(st, p, err)) return r;
+  return oz_product_combine(st, p, err);
+}
+
+int oz_product_combine(cudaStream_t st, const OzProduct& p, std::string* err) {
+  if (p.M <= 0 || p.N <= 0 || p.T <= 0) return 0;
+  dispatch_s<LaunchCombine>(p.s, st, p);
+  return launched("oz_combine", err);
+}
+
+int oz_product_mma(cudaStream_t st, const OzProduct& p, std::string* err) {
   if (p.M <= 0 || p.N <= 0 || p.T <= 0) return 0;
   const int* md;
   if (!oz_supported(p.s) || p.K <= 0 || p.M > 65535 * 8 || p.T > 65535) {
@@ -531,9 +584,10 @@ int oz_product(cudaStream_t st, const OzProduct& p, std::string* err) {
   g.oz_b_traj = 1;
   g.oz_na = p.a_planes * p.s * (p.a_traj ? p.T : 1);
   g.oz_nb = p.b_planes * p.s * p.T;
-  if (int r = igemm(st, g, err)) return r;
-  dispatch_s<LaunchCombine>(p.s, st, p);
-  return launched("oz_combine", err);
+  g.gate = p.gate;
+  g.kdev = p.kdev;
+  g.ndev = p.ndev;
+  return igemm(st, g, err);
 }
 
 }  // namespace traj

@@ -32,19 +32,24 @@ inline long long oz_ld(long long K) { return round_up(K, 16); }
 
 // A operand from the rows of X (T matrices [rows][ldx], stride sX): residue row r = X row r over
 // k = X's columns; planes (re, im, re + im) (conj: im -> -im); e[t][r] (stride sE) the row exponents.
+// cdev (device, per trajectory, optional): columns j >= cdev[t] of X are taken as zero
 int oz_split_rows(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T, int conj,
-                  int s, int8_t* R, int* e, long long sE, std::string* err);
+                  int s, int8_t* R, int* e, long long sE, std::string* err, const int32_t* gate = nullptr,
+                  const int32_t* cdev = nullptr, int nplanes = 3);
 
 // B operand from the columns of X: residue row j = X column j over k = X's rows; planes
 // (re, im, re + im[, re - im]) for nplanes = 3 [4]; part: >= 8 * T * cols doubles of scratch.
+// sub_identity: the operand is X - I (square X).  gate (device, optional): skip when *gate == 0.
 int oz_split_cols(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T, int nplanes,
-                  int s, int8_t* R, int* e, long long sE, double* part, std::string* err);
+                  int s, int8_t* R, int* e, long long sE, double* part, std::string* err, int sub_identity = 0,
+                  const int32_t* gate = nullptr, const int32_t* cdev = nullptr);
 
 enum OzFlags {
   OZ_UPPER = 1,       // C upper triangular (only j >= i computed and written)
   OZ_TRI_B = 2,       // B upper triangular (k > j skipped)
   OZ_NEG_P2 = 4,      // the conjugated Gram: P2 = (-Ai) Bi is formed as Ai Bi and negated here
   OZ_ACCUMULATE = 8,  // C += A B instead of C = A B
+  OZ_NEGATE = 16,     // -A B (with base / OZ_ACCUMULATE: C = base - A B)
 };
 
 struct OzProduct {
@@ -64,10 +69,17 @@ struct OzProduct {
   cplx* C = nullptr;
   long long ldc = 0, sC = 0;
   int flags = 0;
+  const cplx* base = nullptr;   // C = base + A B (same layout as C; may alias it)
+  const int32_t* gate = nullptr;   // device flag: every launch does nothing when *gate == 0
+  const int32_t* kdev = nullptr;   // per trajectory: the contraction runs over k < kdev[t] (operands zero past it)
+  const int32_t* ndev = nullptr;   // per trajectory: only columns j < ndev[t] of C are computed and written
 };
 
 // the products (one batched INT8 launch) and the CRT combine into C
 int oz_product(cudaStream_t st, const OzProduct& p, std::string* err);
+// the same in two calls (the caller times the INT8 launch alone)
+int oz_product_mma(cudaStream_t st, const OzProduct& p, std::string* err);
+int oz_product_combine(cudaStream_t st, const OzProduct& p, std::string* err);
 
 // bytes of the scratch buffers for a product of this shape
 inline long long oz_residue_bytes(long long planes, int s, long long T, long long rows, long long K) {

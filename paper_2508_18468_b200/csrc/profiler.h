@@ -7,7 +7,7 @@
 
 namespace traj {
 
-constexpr int NPHASES = 7;
+constexpr int NPHASES = 10;
 
 struct Profiler {
   bool on = false;

@@ -71,6 +71,8 @@ struct traj_ctx {
   // RU / RX, the residue products RC [3][s][T][rows][oz_ld(N)] and the row / column exponents eU, eX
   bool oz_ku = false, oz_cqr = false;
   int oz_s = 16;
+  int oz_proj_min = 1024;   // click count from which the projective rank-k products go modular (TRAJ_OZAKI_PROJ_MIN)
+  int oz_s_corr = 10;   // moduli of the second pass's first-order correction src (X - I) (TRAJ_OZAKI_CORR_MODULI; 0: full)
   int8_t *RK = nullptr, *RU = nullptr, *RX = nullptr;
   uint8_t* RC = nullptr;
   int *eK = nullptr, *eU = nullptr, *eX = nullptr;
@@ -315,6 +317,11 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     const char* oz = getenv("TRAJ_OZAKI");
     const char* om = getenv("TRAJ_OZAKI_MODULI");
     h->oz_s = om ? atoi(om) : 16;
+    const char* opm = getenv("TRAJ_OZAKI_PROJ_MIN");
+    h->oz_proj_min = opm ? atoi(opm) : 1024;
+    const char* oc = getenv("TRAJ_OZAKI_CORR_MODULI");
+    h->oz_s_corr = oc ? atoi(oc) : 10;
+    if (h->oz_s_corr != 0 && !oz_supported(h->oz_s_corr)) h->oz_s_corr = 10;
     const bool oz_on = !(oz && oz[0] == '0') && oz_supported(h->oz_s) && N >= min_n && L <= 65535;
     h->oz_cqr = oz_on;
     h->oz_ku = oz_on && h->planar;
@@ -635,7 +642,11 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
         p.ldc = h->ldN;
         p.sC = h->sG;
         p.flags = OZ_UPPER | OZ_NEG_P2;
-        TRY(oz_product(h->st, p, &h->err));
+        {
+          Phase pm(&h->prof, h->st, TRAJ_PH_GRAM_MMA);
+          TRY(oz_product_mma(h->st, p, &h->err));
+        }
+        TRY(oz_product_combine(h->st, p, &h->err));
       } else if (h->planar_cqr) {
         // G = U^dag U = (P1 + Q2) + i (P3 - P1 + Q2): P1 = Ur^T Ur, Q2 = Ui^T Ui, P3 = (Ur - Ui)^T (Ur + Ui),
         // A triple = planes 0..2, B triple = planes 3..5
@@ -667,6 +678,8 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
                                                                h->fb_dev, &e2) ? -1 : 1;
         }
         if (h->fbg_state == 1) {
+          // the modular TRMM below keys its full-precision product on the same decision (gate)
+          if (h->oz_cqr) TRY(cqr2_decide(h->st, h->gdev, h->T, thr, h->gate, nullptr, &h->err));
           TRY(h->fbg.launch(h->st, &h->err));
         } else {   // the same decision, every kernel of the factorisation gated on it
           TRY(cqr2_decide(h->st, h->gdev, h->T, thr, h->gate, h->fb_dev, &h->err));
@@ -750,7 +763,44 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
     }
     {
       Phase p(&h->prof, h->st, TRAJ_PH_TRMM);
-      if (h->oz_cqr) {
+      if (h->oz_cqr && pass == 1 && !h->full_cqr2 && h->oz_s_corr > 0) {
+        // second pass, first-order factor X = I + D (|D| <= ~1e-9 / sqrt(N) by the device check):
+        // dst = src + src D needs only oz_s_corr moduli (D's columns carry their own exponents, so
+        // the correction is resolved to 2^-beta of |D|, far below the rounding of src); when the
+        // device decided on the full factorisation (gate), the full-precision src X overwrites it
+        for (int full = 0; full < 2; ++full) {
+          const int s = full ? h->oz_s : h->oz_s_corr;
+          const int32_t* gate = full ? h->gate : nullptr;
+          TRY(oz_split_rows(h->st, src, h->ldN, h->sU, h->L, h->N, h->T, 0, s, h->RU, h->eU, h->L, &h->err, gate));
+          TRY(oz_split_cols(h->st, h->X, h->ldN, h->sG, h->N, h->N, h->T, 3, s, h->RX, h->eX, h->N, h->oz_part,
+                            &h->err, full ? 0 : 1, gate));
+          OzProduct p;
+          p.M = h->L;
+          p.N = h->N;
+          p.K = h->N;
+          p.T = h->T;
+          p.s = s;
+          p.RA = h->RU;
+          p.a_traj = 1;
+          p.eA = h->eU;
+          p.sEA = h->L;
+          p.RB = h->RX;
+          p.eB = h->eX;
+          p.sEB = h->N;
+          p.RC = h->RC;
+          p.C = dst;
+          p.ldc = h->ldN;
+          p.sC = h->sU;
+          p.flags = OZ_TRI_B;
+          p.base = full ? nullptr : src;
+          p.gate = gate;
+          {
+            Phase pm(&h->prof, h->st, TRAJ_PH_TRMM_MMA);
+            TRY(oz_product_mma(h->st, p, &h->err));
+          }
+          TRY(oz_product_combine(h->st, p, &h->err));
+        }
+      } else if (h->oz_cqr) {
         // U X on the INT8 tensor cores: U's row residues, X's column residues (X upper triangular:
         // k-blocks past each output column block skipped)
         TRY(oz_split_rows(h->st, src, h->ldN, h->sU, h->L, h->N, h->T, 0, h->oz_s, h->RU, h->eU, h->L, &h->err));
@@ -774,7 +824,11 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
         p.ldc = h->ldN;
         p.sC = h->sU;
         p.flags = OZ_TRI_B;
-        TRY(oz_product(h->st, p, &h->err));
+        {
+          Phase pm(&h->prof, h->st, TRAJ_PH_TRMM_MMA);
+          TRY(oz_product_mma(h->st, p, &h->err));
+        }
+        TRY(oz_product_combine(h->st, p, &h->err));
       } else if (h->planar_cqr && planes_of == src) {
         // U X = (P1 - P2) + i (P3 - P1 - P2): P1 = Ur Xr, P2 = Ui Xi, P3 = (Ur + Ui)(Xr + Xi) on the
         // Gram's planes of U and X's planes (X upper triangular: k-blocks past the diagonal skipped)
@@ -877,10 +931,43 @@ int projective(traj_ctx* h, cplx* U) {
   }
   TRY(compact(h->st, h->flags, h->L, T, h->S, cap, h->count, &h->err));
   TRY(gather_rows(h->st, U, h->ldN, h->sU, h->S, cap, h->count, maxc, T, h->US, h->ldN, h->sUS, h->N, &h->err));
+  // the rank-k products on the INT8 modular path once the click count makes them large (c5:
+  // |S| ~ 3700, k1 ~ 1850); below TRAJ_OZAKI_PROJ_MIN clicks the DMMA kernels are cheaper than the
+  // residue splits of U
+  const bool ozp = h->oz_cqr && maxc >= h->oz_proj_min && maxc <= h->N;
   // C_SS = U_S U_S^dag (all trajectories padded to maxc rows; rows beyond a trajectory's
   // count are never read by the sampler)
-  TRY(zgemm(h->st, 0, 1, maxc, maxc, h->N, 1.0, 0.0, h->US, h->ldN, h->sUS, h->US, h->ldN, h->sUS, 0.0, h->D0,
-            h->ldcap, h->sD, T, 0, &h->err));
+  if (ozp) {
+    // one 4-plane row split of U_S serves both sides: C = (P1 + P2') + i (P3 - P1 + P2') with
+    // P1 = re re^T, P2' = im im^T, P3 = (re + im)(re - im)^T
+    TRY(oz_split_rows(h->st, h->US, h->ldN, h->sUS, maxc, h->N, T, 0, h->oz_s, h->RU, h->eU, h->L, &h->err, nullptr,
+                      nullptr, 4));
+    OzProduct p;
+    p.M = maxc;
+    p.N = maxc;
+    p.K = h->N;
+    p.T = T;
+    p.s = h->oz_s;
+    p.RA = h->RU;
+    p.a_traj = 1;
+    p.a_planes = 4;
+    p.eA = h->eU;
+    p.sEA = h->L;
+    p.RB = h->RU;
+    p.b_planes = 4;
+    p.pb[2] = 3;
+    p.eB = h->eU;
+    p.sEB = h->L;
+    p.RC = h->RC;
+    p.C = h->D0;
+    p.ldc = h->ldcap;
+    p.sC = h->sD;
+    p.flags = OZ_NEG_P2;
+    TRY(oz_product(h->st, p, &h->err));
+  } else {
+    TRY(zgemm(h->st, 0, 1, maxc, maxc, h->N, 1.0, 0.0, h->US, h->ldN, h->sUS, h->US, h->ldN, h->sUS, 0.0, h->D0,
+              h->ldcap, h->sD, T, 0, &h->err));
+  }
   TRY(sample_outcomes(h->st, h->D0, h->Dw, h->ldcap, h->sD, h->S, cap, h->count, maxc, T, h->step,
                       h->cfg.traj_base, h->cfg.seed, h->occ, h->Linv, h->DLinv, h->Ybuf, h->Zbuf, h->ldcap, h->pos1,
                       h->S1, h->S0, h->k1, h->k0, &h->err));
@@ -912,14 +999,69 @@ int projective(traj_ctx* h, cplx* U) {
     // W = U_{S1}^dag R^-1   (N x k1)
     TRY(zgemm(h->st, 1, 0, h->N, maxc, maxc, 1.0, 0.0, h->US, h->ldN, h->sUS, h->X11, h->ldcap, sX, 0.0, h->W,
               h->ldcap, sW, T, TRAJ_TRI_B_UPPER_F, &h->err, 0, 0, &b1));
-    // Tm = U W - E_{S1}   (L x k1)
-    TRY(skinny_gemm(h, 0, h->L, maxc, h->N, U, h->ldN, h->sU, h->W, h->ldcap, sW, h->Tm, sT, h->k1));
+    if (ozp) {
+      // Tm = U W (columns < k1), residues of U's rows and W's columns (W past k1 taken as zero)
+      TRY(oz_split_rows(h->st, U, h->ldN, h->sU, h->L, h->N, T, 0, h->oz_s, h->RU, h->eU, h->L, &h->err));
+      TRY(oz_split_cols(h->st, h->W, h->ldcap, sW, h->N, maxc, T, 3, h->oz_s, h->RX, h->eX, h->N, h->oz_part, &h->err,
+                        0, nullptr, h->k1));
+      OzProduct p;
+      p.M = h->L;
+      p.N = maxc;
+      p.K = h->N;
+      p.T = T;
+      p.s = h->oz_s;
+      p.RA = h->RU;
+      p.a_traj = 1;
+      p.eA = h->eU;
+      p.sEA = h->L;
+      p.RB = h->RX;
+      p.eB = h->eX;
+      p.sEB = h->N;
+      p.RC = h->RC;
+      p.C = h->Tm;
+      p.ldc = h->ldcap;
+      p.sC = sT;
+      p.ndev = h->k1;
+      TRY(oz_product(h->st, p, &h->err));
+    } else {
+      // Tm = U W - E_{S1}   (L x k1)
+      TRY(skinny_gemm(h, 0, h->L, maxc, h->N, U, h->ldN, h->sU, h->W, h->ldcap, sW, h->Tm, sT, h->k1));
+    }
     TRY(sub_identity_batched(h->st, h->Tm, h->ldcap, sT, h->S1, cap, h->k1, maxc, T, &h->err));
-    // U <- U - Tm W^dag  (reduction over the k1 columns)
-    DevBounds bk;
-    bk.k = h->k1;
-    TRY(zgemm(h->st, 0, 1, h->L, h->N, maxc, -1.0, 0.0, h->Tm, h->ldcap, sT, h->W, h->ldcap, sW, 1.0, U, h->ldN,
-              h->sU, T, 0, &h->err, 0, 0, &bk));
+    if (ozp) {
+      // U <- U - Tm W^dag: Tm's rows and W's rows (conjugated) over k < k1
+      TRY(oz_split_rows(h->st, h->Tm, h->ldcap, sT, h->L, maxc, T, 0, h->oz_s, h->RU, h->eU, h->L, &h->err, nullptr,
+                        h->k1));
+      TRY(oz_split_rows(h->st, h->W, h->ldcap, sW, h->N, maxc, T, 1, h->oz_s, h->RX, h->eX, h->N, &h->err, nullptr,
+                        h->k1));
+      OzProduct p;
+      p.M = h->L;
+      p.N = h->N;
+      p.K = maxc;
+      p.T = T;
+      p.s = h->oz_s;
+      p.RA = h->RU;
+      p.a_traj = 1;
+      p.eA = h->eU;
+      p.sEA = h->L;
+      p.RB = h->RX;
+      p.eB = h->eX;
+      p.sEB = h->N;
+      p.RC = h->RC;
+      p.C = U;
+      p.ldc = h->ldN;
+      p.sC = h->sU;
+      p.base = U;
+      p.flags = OZ_NEGATE;
+      p.kdev = h->k1;
+      TRY(oz_product(h->st, p, &h->err));
+    } else {
+      // U <- U - Tm W^dag  (reduction over the k1 columns)
+      DevBounds bk;
+      bk.k = h->k1;
+      TRY(zgemm(h->st, 0, 1, h->L, h->N, maxc, -1.0, 0.0, h->Tm, h->ldcap, sT, h->W, h->ldcap, sW, 1.0, U, h->ldN,
+                h->sU, T, 0, &h->err, 0, 0, &bk));
+    }
   }
   // U is orthonormal here (K unitary, the rank-k update exact), so after zeroing rows S0 the
   // first CholeskyQR Gram is I - V^dag V with V the k0 zeroed rows: keep V (zero-padded).
@@ -1259,7 +1401,11 @@ int one_step(traj_ctx* h) {
         p.C = Un;
         p.ldc = h->ldN;
         p.sC = h->sU;
-        TRY(oz_product(h->st, p, &h->err));
+        {
+          Phase pm(&h->prof, h->st, TRAJ_PH_KU_MMA);
+          TRY(oz_product_mma(h->st, p, &h->err));
+        }
+        TRY(oz_product_combine(h->st, p, &h->err));
       } else if (h->strassen) {
         // Strassen per planar product: U's 7^lv operands per plane, 3 7^lv leaf-size real products
         // (one batched launch for one trajectory), recombined into K U in one pass
@@ -1945,6 +2091,14 @@ int traj_profile(traj_handle h, int enable) {
   if (!h) return TRAJ_EINVAL;
   CK(cudaStreamSynchronize(h->st));
   h->prof.reset(enable != 0);
+  return 0;
+}
+
+int traj_ozaki_info(traj_handle h, int32_t* out3) {
+  if (!h || !out3) return TRAJ_EINVAL;
+  out3[0] = h->oz_ku ? 1 : 0;
+  out3[1] = h->oz_cqr ? 1 : 0;
+  out3[2] = (h->oz_ku || h->oz_cqr) ? h->oz_s : 0;
   return 0;
 }
 

@@ -104,6 +104,6 @@ def test_phase_names_match_the_header():
     """binding.PHASES sizes the buffers traj_phase_times fills: one name per TRAJ_PH_* entry."""
     txt = open(HEADER).read()
     n = int(re.search(r"TRAJ_NPHASES\s*=\s*(\d+)", txt).group(1))
-    ids = [int(v) for v in re.findall(r"TRAJ_PH_[A-Z]+\s*=\s*(\d+)", txt)]
+    ids = [int(v) for v in re.findall(r"TRAJ_PH_[A-Z_0-9]+\s*=\s*(\d+)", txt)]
     from paper_2508_18468_b200 import binding
     assert len(binding.PHASES) == n == len(ids) and sorted(ids) == list(range(n))

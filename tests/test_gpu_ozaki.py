@@ -180,3 +180,76 @@ def test_zgemm_ozaki_rejects(T):
     assert lib.traj_zgemm_ozaki(st, 0, 16, 16, 16, A.data_ptr(), 16, A.data_ptr(), 16, A.data_ptr(), 16, 7, 0) == 1
     assert lib.traj_zgemm_ozaki(st, 2, 16, 16, 16, A.data_ptr(), 16, A.data_ptr(), 16, A.data_ptr(), 16, 16, 0) == 1
     assert lib.traj_zgemm_ozaki(st, 0, 16, 16, 16, A.data_ptr(), 8, A.data_ptr(), 16, A.data_ptr(), 16, 16, 0) == 1
+
+
+# ---- the modular products inside the trajectory step (env thresholds lowered so small lattices take
+# ---- the path the full-size configs take), in lockstep with the oracle
+
+@pytest.fixture
+def oz_small(monkeypatch):
+    monkeypatch.setenv("TRAJ_PLANAR_MIN_N", "64")      # the modular K U / Gram / TRMM from N = 64 on
+    monkeypatch.setenv("TRAJ_OZAKI_PROJ_MIN", "1")     # the modular rank-k products at any click count
+    monkeypatch.delenv("TRAJ_OZAKI", raising=False)
+
+
+def _oz_on(P, *args, **kw):
+    g = P.Trajectories(*args, **kw)
+    assert g.ozaki_info()[:2] == (True, True)
+    return g
+
+
+def test_step_on_modular_path_projective_matches_oracle(T, oz_small):
+    import paper_2508_18468_b200 as P
+    from test_gpu_parity import lockstep
+    _oz_on(P, 300, 1, "projective", [2.0, 0.6])
+    lockstep(P, 300, 1, "projective", [2.0, 0.6], 30, 5, [np.arange(150), np.arange(37, 211)], seed=7)
+
+
+def test_step_on_modular_path_homodyne_and_2d_match_oracle(T, oz_small):
+    import paper_2508_18468_b200 as P
+    import workloads
+    from test_gpu_parity import lockstep
+    lockstep(P, 200, 1, "homodyne", [0.1, 1.0, 3.0], 60, 20, [np.arange(100), np.arange(13)], seed=3, traj_base=5)
+    A, B = workloads.strips_2d(16, 12)
+    lockstep(P, 16, 12, "projective", [2.86, 5.72], 30, 10, [workloads.columns(16, 12, 0, 8)], seed=5, mi=(A, B))
+
+
+def test_modular_cqr2_fallback_is_full_precision(T, oz_small):
+    """An ill-conditioned state (kappa ~ 1e5) makes the second pass take the full factorisation: the
+    gated 16-moduli TRMM then overwrites the cheap first-order correction."""
+    import torch
+    import paper_2508_18468_b200 as P
+    from oracle import gaussian
+    L, N = 200, 100
+    U = workloads_random(L, N, 3)
+    U[:, 1] = U[:, 0] + 1e-5 * U[:, 1]
+    c = _oz_on(P, L, 1, "homodyne", [0.0])
+    c.set_state(0, torch.from_numpy(U).cuda())
+    c.orthonormalize()
+    assert c.cqr2_fallbacks() == 1
+    Ug = c.get_state(0).cpu().numpy()
+    assert np.abs(Ug.conj().T @ Ug - np.eye(N)).max() < 1e-12
+    assert np.abs(c.correlation(0).cpu().numpy() - gaussian.correlation(gaussian.orthonormalize(U))).max() < 1e-9
+
+
+def workloads_random(L, N, seed):
+    from workloads import random_matrix
+    return random_matrix(L, N, seed)
+
+
+def test_modular_step_matches_dmma_step(T, monkeypatch):
+    """The same c3-shaped trajectory (L = 2048, projective) on the modular path and on the DMMA kernels:
+    identical clicks, C within 1e-12 after 4 steps."""
+    import paper_2508_18468_b200 as P
+    monkeypatch.setenv("TRAJ_OZAKI_PROJ_MIN", "1")
+    a = P.Trajectories(2048, 1, "projective", [0.3, 1.5], seed=1)
+    monkeypatch.setenv("TRAJ_OZAKI", "0")
+    b = P.Trajectories(2048, 1, "projective", [0.3, 1.5], seed=1)
+    assert a.ozaki_info()[0] and not b.ozaki_info()[0]
+    for _ in range(4):
+        a.step(1)
+        b.step(1)
+        for t in range(2):
+            assert a.last_clicks(t) == b.last_clicks(t)
+    for t in range(2):
+        assert np.abs(a.correlation(t).cpu().numpy() - b.correlation(t).cpu().numpy()).max() < 1e-12
