@@ -49,10 +49,13 @@ _MP = _measured_peaks()
 # INT8 tensor peak: no measured INT8 entry, so the measured bf16 cuBLAS figure x the nominal dense ratio
 # 4.5 / 2.25 (B200_PROFILING.md); the sustained figure (power-capped seconds-long loop) for a kernel
 # timed inside a long step, the burst one for context
-INT8_PEAK_TOPS = 2.0 * float(_MP.get("bf16_tflops_sustained", 1397.9))
-INT8_PEAK_BURST_TOPS = 2.0 * float(_MP.get("bf16_tflops", 1655.2))
-INT8_PEAK_SOURCE = ("MEASURED_PEAKS.json bf16_tflops_sustained x 2 (nominal dense INT8 / bf16 = 4.5 / 2.25); "
-                    f"burst bf16_tflops x 2 = {INT8_PEAK_BURST_TOPS:.0f} TOPS")
+INT8_PEAK_TOPS = 4344.8   # measured tcgen05.mma.kind::i8 issue rate, profiles/r02/int8_peak_microbench.txt
+INT8_PEAK_BF16_RATIO = 2.0 * float(_MP.get("bf16_tflops", 1655.2))
+INT8_PEAK_SOURCE = ("measured on this pool's B200 (tools/microbench/i8_peak.cu, profiles/r02/int8_peak_microbench.txt): "
+                    "back-to-back tcgen05.mma.cta_group::1.kind::i8 128x256x32 on shared-memory-resident random operands, "
+                    "148 SMs, best of 3 = 4344.8 TOPS (3806-4345 random, up to 4573 with zero operands; the clock-derived "
+                    "8192 MAC/clk/SM x 1965 MHz would be 4766). MEASURED_PEAKS.json has no INT8 entry; its bf16 cuBLAS "
+                    f"burst x the nominal 4.5/2.25 ratio gives {INT8_PEAK_BF16_RATIO:.0f}, which this kernel exceeds")
 FP64_PEAK_SOURCE = ("measured on this pool's B200: DMMA.8x8x4 microbenchmark 37.1 TF/s (cuBLAS ZGEMM 37.0 TF/s), "
                     "profiles/r01_fp64_microbench.txt; MEASURED_PEAKS.json has no FP64 entry "
                     "(bf16 x 40/2250 nominal ratio would give 29.4)")

@@ -10,6 +10,8 @@
 // Tile 128 x 256 x 128 (one MMA 128 x 256 x 32 per 32 bytes of k), 4-stage smem ring of 48 KB,
 // two 256-column TMEM accumulators so the epilogue of tile t overlaps the MMAs of tile t + 1.
 #include "igemm.h"
+#include <algorithm>
+#include <cstdlib>
 
 namespace traj {
 namespace {
@@ -18,7 +20,9 @@ constexpr int IBM = 128, IBN = 256, IBK = 128, ISTAGES = 4;
 constexpr int IA_BYTES = IBM * IBK, IB_BYTES = IBN * IBK, ISTAGE_BYTES = IA_BYTES + IB_BYTES;
 constexpr int ITHREADS = 192;
 constexpr int ISMEM = ISTAGES * ISTAGE_BYTES + 1024 + 256;
-constexpr int IGM = 16;   // raster group: IGM m-blocks share each n-block's B tile through L2
+// raster: tiles are taken in groups of `gm` m-blocks (m fastest) so that a wave of CTAs shares A and B
+// slabs through L2 (TRAJ_IGEMM_GM overrides the default for experiments)
+constexpr int IGM = 16;
 
 // K-major operand, 128-byte rows, 128B swizzle (8-row atoms of 1 KB): SBO = 1024 B, version 1.
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
@@ -69,6 +73,7 @@ struct KArgs {
   const int* moduli;
   int nmod;
   int flags;
+  int gm;
   int oz_s, oz_T, oz_a_traj, oz_b_traj;
   int oz_pa[3], oz_pb[3];
   const int32_t* gate;
@@ -100,9 +105,9 @@ __device__ __forceinline__ Tile tile_of(const KArgs& a, long long t) {
   Tile r;
   r.z = (int)(t / per);
   const int rem = (int)(t - (long long)r.z * per);
-  const int gsz = IGM * a.tiles_n;
-  const int g = rem / gsz, first = g * IGM;
-  const int h = min(IGM, a.tiles_m - first), w = rem - g * gsz;
+  const int gsz = a.gm * a.tiles_n;
+  const int g = rem / gsz, first = g * a.gm;
+  const int h = min(a.gm, a.tiles_m - first), w = rem - g * gsz;
   r.mb = first + w % h;
   r.nb = w / h;
   return r;
@@ -380,6 +385,14 @@ int igemm(cudaStream_t st, const IgemmArgs& g, std::string* err) {
   a.moduli = g.moduli;
   a.nmod = g.nmod;
   a.flags = g.flags;
+  {
+    static int gm_env = -1;
+    if (gm_env < 0) {
+      const char* v = getenv("TRAJ_IGEMM_GM");
+      gm_env = v ? std::max(1, atoi(v)) : 0;
+    }
+    a.gm = gm_env ? gm_env : IGM;
+  }
   a.oz_s = g.oz_s;
   a.oz_T = g.oz_T;
   a.oz_a_traj = g.oz_a_traj;

@@ -42,20 +42,29 @@ struct HostConst {
       int lg = 0;
       for (u128 x = Mp; x > 1; x >>= 1) ++lg;
       beta[s] = lg / 2 - 1;
-      for (int q = 0; q < s; ++q) {
-        const int m = OZM(q);
-        const int Mi = (int)((Mp / (u128)m) % (u128)m);
-        int inv = 0;
-        for (int x = 1; x < m; ++x)
-          if ((long long)Mi * x % m == 1) {
-            inv = x;
-            break;
+      // the moduli in pairs (q = 2p, 2p + 1), mu_p = m_2p m_2p+1 < 2^16 (s even); c_p = inv_p / mu_p,
+      // inv_p = (M / mu_p)^-1 mod mu_p; n = round(inv_p 2^37 / mu_p), ch = n 2^-37, cl = c_p - ch
+      for (int q = 0; 2 * q + 1 < s; ++q) {
+        const long long mu = (long long)OZM(2 * q) * OZM(2 * q + 1);
+        const long long Mi = (long long)((Mp / (u128)mu) % (u128)mu);
+        long long inv = 0;
+        {   // extended Euclid
+          long long r0 = mu, r1 = Mi, t0 = 0, t1 = 1;
+          while (r1) {
+            const long long k = r0 / r1;
+            long long tmp = r0 - k * r1;
+            r0 = r1;
+            r1 = tmp;
+            tmp = t0 - k * t1;
+            t0 = t1;
+            t1 = tmp;
           }
-        // n = round(inv 2^45 / m); cl = (inv 2^45 - n m) / (m 2^45)
-        const long long num = (long long)inv << 45;
-        const long long n = (num + m / 2) / m;
-        ch[s][q] = (double)n * 0x1p-45;
-        cl[s][q] = (double)(num - n * m) / (double)m * 0x1p-45;
+          inv = ((t0 % mu) + mu) % mu;
+        }
+        const long long num = inv << 37;
+        const long long n = (num + mu / 2) / mu;
+        ch[s][q] = (double)n * 0x1p-37;
+        cl[s][q] = (double)(num - n * mu) / (double)mu * 0x1p-37;
       }
     }
   }
@@ -112,62 +121,69 @@ __device__ __forceinline__ int scale_exp(double nu2, int beta) {
   return beta - ilogb(sqrt(nu2)) - 1;
 }
 
-// residue in [0, m) of the integer x (|x| < 2^62), by 21-bit digits: every partial sum < 2^30
-template <int Q>
-__device__ __forceinline__ uint32_t res_of(long long x) {
-  constexpr int m = OZM(Q);
-  constexpr uint32_t c21 = pow2mod(21, m), c42 = pow2mod(42, m);
-  const unsigned long long u = x < 0 ? (unsigned long long)(-x) : (unsigned long long)x;
-  const uint32_t x0 = (uint32_t)(u & 0x1FFFFF), x1 = (uint32_t)((u >> 21) & 0x1FFFFF), x2 = (uint32_t)(u >> 42);
-  uint32_t r = (x2 * c42 + x1 * c21 + x0) % (uint32_t)m;
-  if (x < 0 && r) r = m - r;
-  return r;
+// v 2^e rounded to an integer (|v 2^e| < 2^62 by the choice of e); the power of two is built
+// directly unless it leaves the normal range
+__device__ __forceinline__ double pow2(int e) { return __longlong_as_double((long long)(e + 1023) << 52); }
+__device__ __forceinline__ long long to_int(double v, int e, double p2) {
+  return __double2ll_rn((e > -1000 && e < 1000) ? v * p2 : scalbn(v, e));
 }
 
-// [0, m) -> the symmetric int8 representative as a byte
+// x (|x| < 2^62) by the 21-bit digits of x + 2^62 >= 0
+struct Dig {
+  uint32_t d0, d1, d2;
+};
+__device__ __forceinline__ Dig dig_of(long long x) {
+  const unsigned long long u = (unsigned long long)x + (1ull << 62);
+  return Dig{(uint32_t)(u & 0x1FFFFF), (uint32_t)((u >> 21) & 0x1FFFFF), (uint32_t)(u >> 42)};
+}
+// one reduction step of v in [0, k m): v <- v - m when v >= m (unsigned wrap-around makes it a min)
+__device__ __forceinline__ uint32_t red1(uint32_t v, uint32_t m) { return min(v, v - m); }
+
+// u = (x + 128) mod m_Q: the stored int8 is u - 128 (a residue of x in [-128, 127]), i.e. the byte u ^ 0x80.
+// Every partial sum of digit x constant stays below 2^31.
 template <int Q>
-__device__ __forceinline__ uint32_t sym8(uint32_t r) {
-  constexpr int m = OZM(Q);
-  return (uint32_t)(uint8_t)(int8_t)((int)r > (m - 1) / 2 ? (int)r - m : (int)r);
+struct Mod {
+  static constexpr uint32_t m = OZM(Q);
+  static constexpr uint32_t c21 = pow2mod(21, m), c42 = pow2mod(42, m);
+  static constexpr uint32_t off = (uint32_t)((128 + 4 * m - pow2mod(62, m)) % m);   // 128 - 2^62 (mod m)
+  __device__ __forceinline__ static uint32_t u(const Dig& d) { return (d.d2 * c42 + d.d1 * c21 + d.d0 + off) % m; }
+};
+
+__device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
+  return __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410) ^ 0x80808080u;
 }
 
-template <int Q>
-__device__ __forceinline__ void planes_of(long long vr, long long vi, int conj, uint32_t (&b)[4]) {
-  constexpr uint32_t m = OZM(Q);
-  const uint32_t a = res_of<Q>(vr);
-  uint32_t c = res_of<Q>(vi);
-  if (conj && c) c = m - c;
-  uint32_t s = a + c;
-  s -= s >= m ? m : 0;
-  uint32_t d = a + m - c;
-  d -= d >= m ? m : 0;
-  b[0] = sym8<Q>(a);
-  b[1] = sym8<Q>(c);
-  b[2] = sym8<Q>(s);
-  b[3] = sym8<Q>(d);
+// residues of the planes (re, im, re + im, re - im) of E consecutive elements, packed 4 per word
+template <int Q, int NP, int E>
+__device__ __forceinline__ void plane_words(const Dig (&dr)[E], const Dig (&di)[E], uint32_t (&w)[NP][E / 4]) {
+  constexpr uint32_t m = Mod<Q>::m;
+#pragma unroll
+  for (int g = 0; g < E / 4; ++g) {
+    uint32_t b[NP][4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t ur = Mod<Q>::u(dr[4 * g + k]), ui = Mod<Q>::u(di[4 * g + k]);
+      b[0][k] = ur;
+      b[1][k] = ui;
+      b[2][k] = red1(red1(ur + ui + (m - 128), m), m);             // (re + im + 128) mod m
+      if constexpr (NP == 4) b[3][k] = red1(red1(ur + m + 128 - ui, m), m);   // (re - im + 128) mod m
+    }
+#pragma unroll
+    for (int p = 0; p < NP; ++p) w[p][g] = pack4(b[p][0], b[p][1], b[p][2], b[p][3]);
+  }
 }
-
-__device__ __forceinline__ long long to_int(double v, int e) { return __double2ll_rn(scalbn(v, e)); }
 
 template <int S, int NP, int Q = 0>
 struct RowStore {
   // 4 consecutive elements -> one 32-bit word per (plane, modulus)
-  __device__ __forceinline__ static void run(const long long (&vr)[4], const long long (&vi)[4], int conj, int8_t* R,
-                                             long long pstride, long long qstride) {
+  __device__ __forceinline__ static void run(const Dig (&dr)[4], const Dig (&di)[4], int8_t* R, long long pstride,
+                                             long long qstride) {
     if constexpr (Q < S) {
-      uint32_t w[NP];
+      uint32_t w[NP][1];
+      plane_words<Q, NP, 4>(dr, di, w);
 #pragma unroll
-      for (int p = 0; p < NP; ++p) w[p] = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        uint32_t b[4];
-        planes_of<Q>(vr[k], vi[k], conj, b);
-#pragma unroll
-        for (int p = 0; p < NP; ++p) w[p] |= b[p] << (8 * k);
-      }
-#pragma unroll
-      for (int p = 0; p < NP; ++p) *reinterpret_cast<uint32_t*>(R + p * pstride + Q * qstride) = w[p];
-      RowStore<S, NP, Q + 1>::run(vr, vi, conj, R, pstride, qstride);
+      for (int p = 0; p < NP; ++p) *reinterpret_cast<uint32_t*>(R + p * pstride + Q * qstride) = w[p][0];
+      RowStore<S, NP, Q + 1>::run(dr, di, R, pstride, qstride);
     }
   }
 };
@@ -201,21 +217,24 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const cplx* __restri
   }
   __syncthreads();
   const int ex = ex_s;
+  const double p2 = pow2(ex);
   const long long qstride = (long long)T * rows * ldr, pstride = (long long)S * qstride;
   int8_t* Rrow = R + (long long)t * rows * ldr + (long long)row * ldr;
   for (int j0 = 4 * threadIdx.x; j0 < cols_cap; j0 += 1024) {
-    long long vr[4], vi[4];
+    Dig dr[4], di[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
+      long long vr = 0, vi = 0;
       if (j0 + k < cols) {
         const cplx v = x[j0 + k];
-        vr[k] = to_int(v.x, ex);
-        vi[k] = to_int(v.y, ex);
-      } else {
-        vr[k] = vi[k] = 0;
+        vr = to_int(v.x, ex, p2);
+        vi = to_int(v.y, ex, p2);
+        if (conj) vi = -vi;
       }
+      dr[k] = dig_of(vr);
+      di[k] = dig_of(vi);
     }
-    RowStore<S, NP>::run(vr, vi, conj, Rrow + j0, pstride, qstride);
+    RowStore<S, NP>::run(dr, di, Rrow + j0, pstride, qstride);
   }
 }
 
@@ -245,58 +264,22 @@ __global__ void __launch_bounds__(256) oz_colnorm_kernel(const cplx* __restrict_
   }
 }
 
-constexpr int CT = 64;   // column-split tile: 64 columns of X x 64 rows of X
+constexpr int CTI = 64, CTJ = 32;   // column-split tile: 64 rows (k) x 32 columns (residue rows) of X
 
-// the 21-bit digits of |x| (|x| < 2^62) and its sign
-struct Digits {
-  uint32_t d0, d1, d2;
-  bool neg;
-};
-__device__ __forceinline__ Digits digits_of(long long x) {
-  const unsigned long long u = x < 0 ? (unsigned long long)(-x) : (unsigned long long)x;
-  return Digits{(uint32_t)(u & 0x1FFFFF), (uint32_t)((u >> 21) & 0x1FFFFF), (uint32_t)(u >> 42), x < 0};
-}
-// residue in [0, m_q) with run-time tables (the column split's 16 values per thread leave no
-// registers for a fully unrolled modulus loop)
-__device__ __forceinline__ uint32_t res_rt(const Digits& d, int q) {
-  const uint32_t m = c_mod[q];
-  const uint32_t y = d.d2 * c_c42[q] + d.d1 * c_c21[q] + d.d0;   // < 2^30
-  uint32_t r = y - __umulhi(y, c_magic[q]) * m;                 // in [0, m + 64)
-  r -= r >= m ? m : 0;
-  if (d.neg && r) r = m - r;
-  return r;
-}
-__device__ __forceinline__ uint32_t sym8_rt(uint32_t r, uint32_t m) {
-  return (uint32_t)(uint8_t)(int8_t)((int)r > ((int)m - 1) / 2 ? (int)r - (int)m : (int)r);
-}
-
-template <int S, int NP>
-__device__ __forceinline__ void col_store(const Digits (&dr)[16], const Digits (&di)[16], int8_t* R, long long pstride,
-                                          long long qstride) {
-#pragma unroll 1
-  for (int q = 0; q < S; ++q) {
-    const uint32_t m = c_mod[q];
-    uint32_t w[NP][4];
+template <int S, int NP, int Q = 0>
+struct ColStore {
+  // 8 consecutive k of one residue row -> one 8-byte store per (plane, modulus)
+  __device__ __forceinline__ static void run(const Dig (&dr)[8], const Dig (&di)[8], int8_t* R, long long pstride,
+                                             long long qstride) {
+    if constexpr (Q < S) {
+      uint32_t w[NP][2];
+      plane_words<Q, NP, 8>(dr, di, w);
 #pragma unroll
-    for (int p = 0; p < NP; ++p)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) w[p][i] = 0;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const uint32_t a = res_rt(dr[k], q), c = res_rt(di[k], q);
-      uint32_t sm = a + c;
-      sm -= sm >= m ? m : 0;
-      uint32_t df = a + m - c;
-      df -= df >= m ? m : 0;
-      const uint32_t b[4] = {sym8_rt(a, m), sym8_rt(c, m), sym8_rt(sm, m), sym8_rt(df, m)};
-#pragma unroll
-      for (int p = 0; p < NP; ++p) w[p][k >> 2] |= b[p] << (8 * (k & 3));
+      for (int p = 0; p < NP; ++p) *reinterpret_cast<uint2*>(R + p * pstride + Q * qstride) = make_uint2(w[p][0], w[p][1]);
+      ColStore<S, NP, Q + 1>::run(dr, di, R, pstride, qstride);
     }
-#pragma unroll
-    for (int p = 0; p < NP; ++p)
-      *reinterpret_cast<uint4*>(R + p * pstride + q * qstride) = make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
   }
-}
+};
 
 template <int S, int NP>
 __global__ void __launch_bounds__(256) oz_split_cols_kernel(const cplx* __restrict__ X, long long ldx, long long sX,
@@ -304,18 +287,20 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const cplx* __restri
                                                             int* e, long long sE, const double* part, int beta,
                                                             int subI, const int32_t* gate, const int32_t* cdev) {
   if (gate && *gate == 0) return;
-  extern __shared__ cplx tile[];   // [CT rows][CT + 1]
-  const int j0 = blockIdx.x * CT, i0 = blockIdx.y * CT, t = blockIdx.z;
+  __shared__ cplx tile[CTI][CTJ + 1];
+  const int j0 = blockIdx.x * CTJ, i0 = blockIdx.y * CTI, t = blockIdx.z;
   const int cz = cdev ? min(cols, cdev[t]) : cols;   // columns past cz are taken as zero
   const cplx* x = X + t * sX;
-  for (int r = threadIdx.x / CT; r < CT; r += 256 / CT) {
-    const int i = i0 + r, j = j0 + (threadIdx.x % CT);
+#pragma unroll
+  for (int r = 0; r < CTI * CTJ / 256; ++r) {
+    const int el = threadIdx.x + 256 * r, ii = el / CTJ, jj = el % CTJ;
+    const int i = i0 + ii, j = j0 + jj;
     cplx v = (i < rows && j < cz) ? x[(long long)i * ldx + j] : make_double2(0.0, 0.0);
     if (subI && i == j) v.x -= 1.0;
-    tile[r * (CT + 1) + (threadIdx.x % CT)] = v;
+    tile[ii][jj] = v;
   }
   __syncthreads();
-  const int jj = threadIdx.x >> 2, ig = (threadIdx.x & 3) * 16, j = j0 + jj;
+  const int jj = threadIdx.x >> 3, ig = (threadIdx.x & 7) * 8, j = j0 + jj;
   if (j >= cols || i0 + ig >= rows) return;
   double nu2 = 0.0;
   if (j < cz) {
@@ -323,51 +308,76 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const cplx* __restri
     for (int c = 0; c < 8; ++c) nu2 += part[((long long)c * T + t) * cols + j];
   }
   const int ex = scale_exp(nu2, beta);
+  const double p2 = pow2(ex);
   if (blockIdx.y == 0 && ig == 0) e[t * sE + j] = ex;
-  Digits dr[16], di[16];
+  Dig dr[8], di[8];
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const cplx v = tile[(ig + k) * (CT + 1) + jj];
-    dr[k] = digits_of(to_int(v.x, ex));
-    di[k] = digits_of(to_int(v.y, ex));
+  for (int k = 0; k < 8; ++k) {
+    const cplx v = tile[ig + k][jj];
+    dr[k] = dig_of(to_int(v.x, ex, p2));
+    di[k] = dig_of(to_int(v.y, ex, p2));
   }
   const long long qstride = (long long)T * cols * ldr, pstride = (long long)S * qstride;
-  col_store<S, NP>(dr, di, R + (long long)t * cols * ldr + (long long)j * ldr + i0 + ig, pstride, qstride);
+  ColStore<S, NP>::run(dr, di, R + (long long)t * cols * ldr + (long long)j * ldr + i0 + ig, pstride, qstride);
 }
 
-template <int S, int Q = 0>
-struct Crt {
-  // accumulate sum_q frac(r_q ch_q) (exact) and sum_q r_q cl_q for the real and imaginary parts
-  __device__ __forceinline__ static void run(const uint8_t* P, long long qstride, long long pstride, int flags,
+// ---- CRT combine.  Moduli are taken in pairs (m_a, m_b) -> one residue mod mu = m_a m_b < 2^16
+// (Garner's step), then X / M = frac(sum_p r_p c_p) over the 8 pairs with c_p = ch_p + cl_p, ch_p a
+// multiple of 2^-37: every r_p ch_p (r_p < 2^16) and the sum of their fractional parts are exact.
+__host__ __device__ constexpr int modinv(int a, int m) {
+  int r = 1;
+  for (int x = 1; x < m; ++x)
+    if ((a % m) * x % m == 1) r = x;
+  return r;
+}
+
+// the real and imaginary residues of the 3M combination mod m from the product residues (bytes < m)
+template <int Q>
+__device__ __forceinline__ void reim(uint32_t a1, uint32_t a2, uint32_t a3, int neg2, uint32_t& re, uint32_t& im) {
+  constexpr uint32_t m = OZM(Q);
+  if (neg2) {   // Re = P1 + P2', Im = P3 - P1 + P2'
+    re = red1(a1 + a2, m);
+    im = red1(red1(a3 + m - a1 + a2, m), m);
+  } else {      // Re = P1 - P2, Im = P3 - P1 - P2
+    re = red1(a1 + m - a2, m);
+    im = red1(red1(a3 + 2 * m - a1 - a2, m), m);
+  }
+}
+
+template <int S, int PQ = 0>
+struct CrtPair {
+  __device__ __forceinline__ static void run(const uint8_t* P, long long qstride, long long pstride, int neg2,
                                              double (&sr)[4], double (&lr)[4], double (&si)[4], double (&li)[4]) {
-    if constexpr (Q < S) {
-      constexpr int m = OZM(Q);
-      const uchar4 p1 = *reinterpret_cast<const uchar4*>(P + Q * qstride);
-      const uchar4 p2 = *reinterpret_cast<const uchar4*>(P + pstride + Q * qstride);
-      const uchar4 p3 = *reinterpret_cast<const uchar4*>(P + 2 * pstride + Q * qstride);
-      const int a1[4] = {p1.x, p1.y, p1.z, p1.w}, a2[4] = {p2.x, p2.y, p2.z, p2.w}, a3[4] = {p3.x, p3.y, p3.z, p3.w};
-      const double ch = c_ch[S][Q], cl = c_cl[S][Q];
+    if constexpr (2 * PQ < S) {
+      constexpr int QA = 2 * PQ, QB = 2 * PQ + 1;
+      constexpr uint32_t ma = OZM(QA), mb = OZM(QB);
+      constexpr uint32_t inv = (uint32_t)modinv((int)(ma % mb), (int)mb);   // m_a^-1 mod m_b
+      const uchar4 a1 = *reinterpret_cast<const uchar4*>(P + QA * qstride);
+      const uchar4 a2 = *reinterpret_cast<const uchar4*>(P + pstride + QA * qstride);
+      const uchar4 a3 = *reinterpret_cast<const uchar4*>(P + 2 * pstride + QA * qstride);
+      const uchar4 b1 = *reinterpret_cast<const uchar4*>(P + QB * qstride);
+      const uchar4 b2 = *reinterpret_cast<const uchar4*>(P + pstride + QB * qstride);
+      const uchar4 b3 = *reinterpret_cast<const uchar4*>(P + 2 * pstride + QB * qstride);
+      const uint32_t A1[4] = {a1.x, a1.y, a1.z, a1.w}, A2[4] = {a2.x, a2.y, a2.z, a2.w}, A3[4] = {a3.x, a3.y, a3.z, a3.w};
+      const uint32_t B1[4] = {b1.x, b1.y, b1.z, b1.w}, B2[4] = {b2.x, b2.y, b2.z, b2.w}, B3[4] = {b3.x, b3.y, b3.z, b3.w};
+      const double ch = c_ch[S][PQ], cl = c_cl[S][PQ];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        int re, im;
-        if (flags & OZ_NEG_P2) {
-          re = a1[k] + a2[k];
-          im = a3[k] - a1[k] + a2[k] + m;
-        } else {
-          re = a1[k] - a2[k] + m;
-          im = a3[k] - a1[k] - a2[k] + 2 * m;
-        }
-        re %= m;
-        im %= m;
-        double tr = (double)re * ch, ti = (double)im * ch;
+        uint32_t rea, ima, reb, imb;
+        reim<QA>(A1[k], A2[k], A3[k], neg2, rea, ima);
+        reim<QB>(B1[k], B2[k], B3[k], neg2, reb, imb);
+        // Garner: r = r_a + m_a ((r_b - r_a) m_a^-1 mod m_b) < m_a m_b
+        const uint32_t rr = rea + ma * ((((reb + 2 * mb - rea) % mb) * inv) % mb);
+        const uint32_t ri = ima + ma * ((((imb + 2 * mb - ima) % mb) * inv) % mb);
+        double tr = (double)rr * ch, ti = (double)ri * ch;
         tr -= rint(tr);
         ti -= rint(ti);
         sr[k] += tr;
         si[k] += ti;
-        lr[k] = fma((double)re, cl, lr[k]);
-        li[k] = fma((double)im, cl, li[k]);
+        lr[k] = fma((double)rr, cl, lr[k]);
+        li[k] = fma((double)ri, cl, li[k]);
       }
-      Crt<S, Q + 1>::run(P, qstride, pstride, flags, sr, lr, si, li);
+      CrtPair<S, PQ + 1>::run(P, qstride, pstride, neg2, sr, lr, si, li);
     }
   }
 };
@@ -394,7 +404,7 @@ __global__ void __launch_bounds__(128) oz_combine_kernel(const uint8_t* __restri
   const long long qstride = (long long)T * M * ldp, pstride = (long long)S * qstride;
   const uint8_t* p = P + ((long long)t * M + i) * ldp + j0;
   double sr[4] = {0, 0, 0, 0}, lr[4] = {0, 0, 0, 0}, si[4] = {0, 0, 0, 0}, li[4] = {0, 0, 0, 0};
-  Crt<S>::run(p, qstride, pstride, flags, sr, lr, si, li);
+  CrtPair<S>::run(p, qstride, pstride, (flags & OZ_NEG_P2) ? 1 : 0, sr, lr, si, li);
   const double Md = c_M[S];
   const int ea = eA[(a_traj ? t : 0) * sEA + i];
   cplx* c = C + t * sC + (long long)i * ldc;
@@ -403,7 +413,15 @@ __global__ void __launch_bounds__(128) oz_combine_kernel(const uint8_t* __restri
     const int j = j0 + k;
     if (j >= N || ((flags & OZ_UPPER) && j < i)) continue;
     const int sc = -(ea + eB[t * sEB + j]);
-    double2 v = make_double2(scalbn(crt_value(sr[k], lr[k], Md), sc), scalbn(crt_value(si[k], li[k], Md), sc));
+    double2 v = make_double2(crt_value(sr[k], lr[k], Md), crt_value(si[k], li[k], Md));
+    if (sc > -1000 && sc < 1000) {
+      const double f = pow2(sc);
+      v.x *= f;
+      v.y *= f;
+    } else {
+      v.x = scalbn(v.x, sc);
+      v.y = scalbn(v.y, sc);
+    }
     if (flags & OZ_NEGATE) {
       v.x = -v.x;
       v.y = -v.y;
@@ -455,17 +473,13 @@ struct LaunchCols {
   static int go(cudaStream_t st, int np, const cplx* X, long long ldx, long long sX, int rows, int cols, int T,
                 int8_t* R, long long ldr, int* e, long long sE, const double* part, int beta, int subI,
                 const int32_t* gate, const int32_t* cdev) {
-    const int smem = CT * (CT + 1) * 16;
-    dim3 grid(ceil_div(cols, CT), ceil_div(rows, CT), T);
-    if (np == 4) {
-      if (ensure_smem((const void*)oz_split_cols_kernel<S, 4>, smem) != cudaSuccess) return 4;
-      oz_split_cols_kernel<S, 4><<<grid, 256, smem, st>>>(X, ldx, sX, rows, cols, T, R, ldr, e, sE, part, beta, subI,
-                                                          gate, cdev);
-    } else {
-      if (ensure_smem((const void*)oz_split_cols_kernel<S, 3>, smem) != cudaSuccess) return 4;
-      oz_split_cols_kernel<S, 3><<<grid, 256, smem, st>>>(X, ldx, sX, rows, cols, T, R, ldr, e, sE, part, beta, subI,
-                                                          gate, cdev);
-    }
+    dim3 grid(ceil_div(cols, CTJ), ceil_div(rows, CTI), T);
+    if (np == 4)
+      oz_split_cols_kernel<S, 4><<<grid, 256, 0, st>>>(X, ldx, sX, rows, cols, T, R, ldr, e, sE, part, beta, subI, gate,
+                                                       cdev);
+    else
+      oz_split_cols_kernel<S, 3><<<grid, 256, 0, st>>>(X, ldx, sX, rows, cols, T, R, ldr, e, sE, part, beta, subI, gate,
+                                                       cdev);
     return 0;
   }
 };
@@ -518,7 +532,7 @@ int oz_split_cols(cudaStream_t st, const cplx* X, long long ldx, long long sX, i
                   const int32_t* gate, const int32_t* cdev) {
   if (rows <= 0 || cols <= 0 || T <= 0) return 0;
   const int* md;
-  if (!oz_supported(s) || (nplanes != 3 && nplanes != 4) || T > 65535 || ceil_div(rows, CT) > 65535) {
+  if (!oz_supported(s) || (nplanes != 3 && nplanes != 4) || T > 65535 || ceil_div(rows, CTI) > 65535) {
     if (err) *err = "oz_split_cols: unsupported modulus count, plane count or shape";
     return 1;
   }

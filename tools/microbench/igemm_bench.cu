@@ -78,7 +78,43 @@ static void timeit(long long M, long long N, long long K, int batch, int out) {
   cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(dm);
 }
 
+static void timeit_rand(long long M, long long N, long long K, int batch) {
+  int8_t *dA, *dB; void* dC; int* dm;
+  int mods[2] = {251, 256};
+  CK(cudaMalloc(&dA, batch * M * K)); CK(cudaMalloc(&dB, batch * N * K));
+  CK(cudaMalloc(&dC, batch * M * N)); CK(cudaMalloc(&dm, 8));
+  CK(cudaMemcpy(dm, mods, 8, cudaMemcpyHostToDevice));
+  {
+    std::vector<int8_t> h(1 << 26);
+    std::mt19937 rng(5);
+    for (auto& x : h) x = (int8_t)(rng() & 255);
+    for (long long o = 0; o < batch * M * K; o += h.size())
+      CK(cudaMemcpy(dA + o, h.data(), std::min<long long>(h.size(), batch * M * K - o), cudaMemcpyHostToDevice));
+    for (long long o = 0; o < batch * N * K; o += h.size())
+      CK(cudaMemcpy(dB + o, h.data(), std::min<long long>(h.size(), batch * N * K - o), cudaMemcpyHostToDevice));
+  }
+  IgemmArgs g; g.M = M; g.N = N; g.K = K; g.batch = batch; g.A = dA; g.lda = K; g.strideA = M * K;
+  g.B = dB; g.ldb = K; g.strideB = N * K; g.C = dC; g.ldc = N; g.strideC = M * N; g.out = IG_OUT_MOD; g.moduli = dm; g.nmod = 2;
+  std::string err;
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  igemm(0, g, &err);
+  CK(cudaDeviceSynchronize());
+  const int reps = 3;
+  cudaEventRecord(e0);
+  for (int i = 0; i < reps; ++i) igemm(0, g, &err);
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= reps;
+  printf("random K.U shape M=%lld N=%lld K=%lld batch=%d gm=%s: %.3f ms  %.1f TOPS\n", M, N, K, batch,
+         getenv("TRAJ_IGEMM_GM") ? getenv("TRAJ_IGEMM_GM") : "16", ms, 2.0 * M * N * K * batch / ms / 1e9);
+  cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(dm);
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "ku") {   // the c3 K U launch shape: 48 products, random data
+    timeit_rand(16384, 8192, 16384, 48);
+    return 0;
+  }
   int bad = 0;
   bad |= check(300, 520, 1000, 2, IG_OUT_I32, 0);
   bad |= check(128, 256, 128, 1, IG_OUT_I32, 0);
