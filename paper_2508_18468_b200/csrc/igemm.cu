@@ -79,6 +79,7 @@ struct KArgs {
   const int32_t* gate;
   const int32_t* kdev;
   const int32_t* ndev;
+  int ksplit, kcb;   // k chunks, k-blocks per chunk
 };
 
 // batch entry z -> (A entry, B entry, modulus index)
@@ -97,14 +98,16 @@ __device__ __forceinline__ void zmap(const KArgs& a, int z, int& za, int& zb, in
 }
 
 struct Tile {
-  int z, mb, nb;
+  int z, kc, mb, nb;
 };
 
 __device__ __forceinline__ Tile tile_of(const KArgs& a, long long t) {
   const long long per = (long long)a.tiles_m * a.tiles_n;
   Tile r;
-  r.z = (int)(t / per);
-  const int rem = (int)(t - (long long)r.z * per);
+  const long long zk = t / per;
+  r.z = (int)(zk / a.ksplit);
+  r.kc = (int)(zk - (long long)r.z * a.ksplit);
+  const int rem = (int)(t - zk * per);
   const int gsz = a.gm * a.tiles_n;
   const int g = rem / gsz, first = g * a.gm;
   const int h = min(a.gm, a.tiles_m - first), w = rem - g * gsz;
@@ -121,11 +124,15 @@ __device__ __forceinline__ bool tile_live(const KArgs& a, const Tile& t) {
   return true;
 }
 
-__device__ __forceinline__ int tile_kblocks(const KArgs& a, const Tile& t) {
+// the tile's k-blocks [kb0, kb0 + count)
+__device__ __forceinline__ int tile_kblocks(const KArgs& a, const Tile& t, int* kb0 = nullptr) {
   int kend = a.K;
   if (a.flags & IG_TRI_B) kend = min(kend, (t.nb + 1) * IBN);
   if (a.kdev) kend = min(kend, a.kdev[traj_of(a, t.z)]);
-  return (kend + IBK - 1) / IBK;
+  const int nkb = (kend + IBK - 1) / IBK;
+  const int b0 = t.kc * a.kcb;
+  if (kb0) *kb0 = b0;
+  return max(0, min(nkb, b0 + a.kcb) - b0);
 }
 
 __global__ void __launch_bounds__(ITHREADS, 1)
@@ -171,10 +178,11 @@ __global__ void __launch_bounds__(ITHREADS, 1)
       for (long long t = blockIdx.x; t < a.tiles; t += gridDim.x) {
         const Tile tl = tile_of(a, t);
         if (!tile_live(a, tl)) continue;
-        const int nk = tile_kblocks(a, tl);
+        int kb0;
+        const int nk = tile_kblocks(a, tl, &kb0);
         int za, zb, q;
         zmap(a, tl.z, za, zb, q);
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = kb0; kb < kb0 + nk; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = base + stage * ISTAGE_BYTES;
           mbar_arrive_expect_tx(&full[stage], ISTAGE_BYTES);
@@ -256,7 +264,8 @@ __global__ void __launch_bounds__(ITHREADS, 1)
         const int col = tl.nb * IBN + c * 32;
         if (!row_ok || col >= a.N) {
         } else if (a.out == IG_OUT_I32) {
-          int* p = reinterpret_cast<int*>(a.C) + tl.z * a.strideC + (long long)row * a.ldc + col;
+          int* p = reinterpret_cast<int*>(a.C) + ((long long)tl.z * a.ksplit + tl.kc) * a.strideC +
+                   (long long)row * a.ldc + col;
           if (col + 32 <= a.N) {
 #pragma unroll
             for (int j = 0; j < 8; ++j)
@@ -279,7 +288,8 @@ __global__ void __launch_bounds__(ITHREADS, 1)
             }
             w[j] = packed;
           }
-          uint8_t* p = reinterpret_cast<uint8_t*>(a.C) + tl.z * a.strideC + (long long)row * a.ldc + col;
+          uint8_t* p = reinterpret_cast<uint8_t*>(a.C) + ((long long)tl.z * a.ksplit + tl.kc) * a.strideC +
+                       (long long)row * a.ldc + col;
           if (col + 32 <= a.N) {
             reinterpret_cast<uint4*>(p)[0] = make_uint4(w[0], w[1], w[2], w[3]);
             reinterpret_cast<uint4*>(p)[1] = make_uint4(w[4], w[5], w[6], w[7]);
@@ -373,7 +383,12 @@ int igemm(cudaStream_t st, const IgemmArgs& g, std::string* err) {
   a.K = (int)g.K;
   a.tiles_m = (int)ceil_div(g.M, IBM);
   a.tiles_n = (int)ceil_div(g.N, IBN);
-  a.tiles = g.batch * a.tiles_m * a.tiles_n;
+  a.ksplit = std::max(1, g.ksplit);
+  {
+    const int nkb = (int)ceil_div(g.K, IBK);
+    a.kcb = (int)ceil_div(nkb, a.ksplit);
+  }
+  a.tiles = g.batch * a.ksplit * a.tiles_m * a.tiles_n;
   a.a_div = g.a_div;
   a.b_div = g.b_div;
   a.a_batched = ab;

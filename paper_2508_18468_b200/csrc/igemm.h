@@ -46,6 +46,11 @@ struct IgemmArgs {
   // and 256-column tiles at n >= ndev[t] are skipped (their outputs are not written)
   const int32_t* kdev = nullptr;
   const int32_t* ndev = nullptr;
+  // split-K: the contraction is cut into ksplit chunks of whole 128-k blocks (the chunk outermost in
+  // the tile order, so a wave of CTAs shares a K-slab ksplit times narrower through L2); chunk c of
+  // batch entry z is written to output matrix z * ksplit + c (the caller sums them: mod m for the
+  // modular epilogue)
+  int ksplit = 1;
 };
 
 // Needs lda, ldb multiples of 16 bytes, 16-byte aligned A/B, ldc a multiple of 16 elements and C

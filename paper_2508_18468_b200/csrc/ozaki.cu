@@ -1,6 +1,7 @@
 // Exact modular complex-FP64 products on the INT8 tensor cores (Ozaki-II / CRT; see ozaki.h).
 #include "ozaki.h"
 #include "igemm.h"
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <set>
@@ -344,22 +345,44 @@ __device__ __forceinline__ void reim(uint32_t a1, uint32_t a2, uint32_t a3, int 
   }
 }
 
+// the residues of 4 consecutive outputs of one (product, modulus): with split-K, the chunks' residues
+// summed and reduced mod m
+template <int Q>
+__device__ __forceinline__ void res4(const uint8_t* p, long long kstride, int ks, uint32_t (&v)[4]) {
+  uchar4 a = *reinterpret_cast<const uchar4*>(p);
+  v[0] = a.x;
+  v[1] = a.y;
+  v[2] = a.z;
+  v[3] = a.w;
+  if (ks > 1) {
+    for (int c = 1; c < ks; ++c) {
+      a = *reinterpret_cast<const uchar4*>(p + c * kstride);
+      v[0] += a.x;
+      v[1] += a.y;
+      v[2] += a.z;
+      v[3] += a.w;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] %= (uint32_t)OZM(Q);
+  }
+}
+
 template <int S, int PQ = 0>
 struct CrtPair {
-  __device__ __forceinline__ static void run(const uint8_t* P, long long qstride, long long pstride, int neg2,
-                                             double (&sr)[4], double (&lr)[4], double (&si)[4], double (&li)[4]) {
+  __device__ __forceinline__ static void run(const uint8_t* P, long long qstride, long long pstride, long long kstride,
+                                             int ks, int neg2, double (&sr)[4], double (&lr)[4], double (&si)[4],
+                                             double (&li)[4]) {
     if constexpr (2 * PQ < S) {
       constexpr int QA = 2 * PQ, QB = 2 * PQ + 1;
       constexpr uint32_t ma = OZM(QA), mb = OZM(QB);
       constexpr uint32_t inv = (uint32_t)modinv((int)(ma % mb), (int)mb);   // m_a^-1 mod m_b
-      const uchar4 a1 = *reinterpret_cast<const uchar4*>(P + QA * qstride);
-      const uchar4 a2 = *reinterpret_cast<const uchar4*>(P + pstride + QA * qstride);
-      const uchar4 a3 = *reinterpret_cast<const uchar4*>(P + 2 * pstride + QA * qstride);
-      const uchar4 b1 = *reinterpret_cast<const uchar4*>(P + QB * qstride);
-      const uchar4 b2 = *reinterpret_cast<const uchar4*>(P + pstride + QB * qstride);
-      const uchar4 b3 = *reinterpret_cast<const uchar4*>(P + 2 * pstride + QB * qstride);
-      const uint32_t A1[4] = {a1.x, a1.y, a1.z, a1.w}, A2[4] = {a2.x, a2.y, a2.z, a2.w}, A3[4] = {a3.x, a3.y, a3.z, a3.w};
-      const uint32_t B1[4] = {b1.x, b1.y, b1.z, b1.w}, B2[4] = {b2.x, b2.y, b2.z, b2.w}, B3[4] = {b3.x, b3.y, b3.z, b3.w};
+      uint32_t A1[4], A2[4], A3[4], B1[4], B2[4], B3[4];
+      res4<QA>(P + QA * qstride, kstride, ks, A1);
+      res4<QA>(P + pstride + QA * qstride, kstride, ks, A2);
+      res4<QA>(P + 2 * pstride + QA * qstride, kstride, ks, A3);
+      res4<QB>(P + QB * qstride, kstride, ks, B1);
+      res4<QB>(P + pstride + QB * qstride, kstride, ks, B2);
+      res4<QB>(P + 2 * pstride + QB * qstride, kstride, ks, B3);
       const double ch = c_ch[S][PQ], cl = c_cl[S][PQ];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -377,7 +400,7 @@ struct CrtPair {
         lr[k] = fma((double)rr, cl, lr[k]);
         li[k] = fma((double)ri, cl, li[k]);
       }
-      CrtPair<S, PQ + 1>::run(P, qstride, pstride, neg2, sr, lr, si, li);
+      CrtPair<S, PQ + 1>::run(P, qstride, pstride, kstride, ks, neg2, sr, lr, si, li);
     }
   }
 };
@@ -394,17 +417,17 @@ __global__ void __launch_bounds__(128) oz_combine_kernel(const uint8_t* __restri
                                                          int T, const int* __restrict__ eA, long long sEA, int a_traj,
                                                          const int* __restrict__ eB, long long sEB, int flags, cplx* C,
                                                          long long ldc, long long sC, const cplx* base,
-                                                         const int32_t* gate, const int32_t* ndev) {
+                                                         const int32_t* gate, const int32_t* ndev, int ks) {
   if (gate && *gate == 0) return;
   const int i = blockIdx.y, t = blockIdx.z;
   const int j0 = (blockIdx.x * 128 + threadIdx.x) * 4;
   if (ndev) N = min(N, ndev[t]);
   if (j0 >= N) return;
   if ((flags & OZ_UPPER) && j0 + 3 < i) return;
-  const long long qstride = (long long)T * M * ldp, pstride = (long long)S * qstride;
-  const uint8_t* p = P + ((long long)t * M + i) * ldp + j0;
+  const long long kstride = (long long)M * ldp, qstride = (long long)T * ks * kstride, pstride = (long long)S * qstride;
+  const uint8_t* p = P + ((long long)t * ks * M + i) * ldp + j0;
   double sr[4] = {0, 0, 0, 0}, lr[4] = {0, 0, 0, 0}, si[4] = {0, 0, 0, 0}, li[4] = {0, 0, 0, 0};
-  CrtPair<S>::run(p, qstride, pstride, (flags & OZ_NEG_P2) ? 1 : 0, sr, lr, si, li);
+  CrtPair<S>::run(p, qstride, pstride, kstride, ks, (flags & OZ_NEG_P2) ? 1 : 0, sr, lr, si, li);
   const double Md = c_M[S];
   const int ea = eA[(a_traj ? t : 0) * sEA + i];
   cplx* c = C + t * sC + (long long)i * ldc;
@@ -489,7 +512,8 @@ struct LaunchCombine {
   static int go(cudaStream_t st, const OzProduct& p) {
     dim3 grid(ceil_div(p.N, 512), p.M, p.T);
     oz_combine_kernel<S><<<grid, 128, 0, st>>>(p.RC, oz_ld(p.N), p.M, p.N, p.T, p.eA, p.sEA, p.a_traj, p.eB, p.sEB,
-                                               p.flags, p.C, p.ldc, p.sC, p.base, p.gate, p.ndev);
+                                               p.flags, p.C, p.ldc, p.sC, p.base, p.gate, p.ndev,
+                                               std::max(1, p.ksplit));
     return 0;
   }
 };
@@ -601,6 +625,7 @@ int oz_product_mma(cudaStream_t st, const OzProduct& p, std::string* err) {
   g.gate = p.gate;
   g.kdev = p.kdev;
   g.ndev = p.ndev;
+  g.ksplit = std::max(1, p.ksplit);
   return igemm(st, g, err);
 }
 

@@ -65,7 +65,7 @@ struct OzProduct {
   int pb[3] = {0, 1, 2};
   const int* eB = nullptr;      // [T][N]
   long long sEB = 0;
-  uint8_t* RC = nullptr;        // scratch [3][s][T][M][oz_ld(N)]
+  uint8_t* RC = nullptr;        // scratch [3][s][T][ksplit][M][oz_ld(N)]
   cplx* C = nullptr;
   long long ldc = 0, sC = 0;
   int flags = 0;
@@ -73,6 +73,7 @@ struct OzProduct {
   const int32_t* gate = nullptr;   // device flag: every launch does nothing when *gate == 0
   const int32_t* kdev = nullptr;   // per trajectory: the contraction runs over k < kdev[t] (operands zero past it)
   const int32_t* ndev = nullptr;   // per trajectory: only columns j < ndev[t] of C are computed and written
+  int ksplit = 1;                  // split-K chunks of the INT8 launch (RC holds ksplit x the residue products)
 };
 
 // the products (one batched INT8 launch) and the CRT combine into C

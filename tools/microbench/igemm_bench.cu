@@ -13,7 +13,7 @@ using namespace traj;
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e_), __LINE__); exit(1);} } while (0)
 
-static int check(long long M, long long N, long long K, int batch, int out, int flags) {
+static int check(long long M, long long N, long long K, int batch, int out, int flags, int ks = 1) {
   const long long lda = (K + 15) / 16 * 16, ldc = (N + 15) / 16 * 16;
   std::vector<int8_t> A(batch * M * lda), B(batch * N * lda);
   std::mt19937 rng(1234 + M + N + K);
@@ -24,19 +24,30 @@ static int check(long long M, long long N, long long K, int batch, int out, int 
   int mods[2] = {251, 256};
   int8_t *dA, *dB; void* dC; int* dm;
   const size_t esz = out == IG_OUT_I32 ? 4 : 1;
-  CK(cudaMalloc(&dA, A.size())); CK(cudaMalloc(&dB, B.size())); CK(cudaMalloc(&dC, batch * M * ldc * esz)); CK(cudaMalloc(&dm, 8));
+  CK(cudaMalloc(&dA, A.size())); CK(cudaMalloc(&dB, B.size())); CK(cudaMalloc(&dC, ks * batch * M * ldc * esz)); CK(cudaMalloc(&dm, 8));
   CK(cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dB, B.data(), B.size(), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dm, mods, 8, cudaMemcpyHostToDevice));
-  CK(cudaMemset(dC, 0x5a, batch * M * ldc * esz));
+  CK(cudaMemset(dC, 0x5a, ks * batch * M * ldc * esz));
   IgemmArgs g; g.M = M; g.N = N; g.K = K; g.batch = batch; g.A = dA; g.lda = lda; g.strideA = M * lda;
   g.B = dB; g.ldb = lda; g.strideB = N * lda; g.C = dC; g.ldc = ldc; g.strideC = M * ldc; g.out = out; g.moduli = dm; g.nmod = 2; g.flags = flags;
+  g.ksplit = ks;
   std::string err;
   int s = igemm(0, g, &err);
   if (s) { printf("igemm failed %d %s\n", s, err.c_str()); return 1; }
   CK(cudaDeviceSynchronize());
-  std::vector<uint8_t> C(batch * M * ldc * esz);
-  CK(cudaMemcpy(C.data(), dC, C.size(), cudaMemcpyDeviceToHost));
+  std::vector<uint8_t> Cs(ks * batch * M * ldc * esz), C(batch * M * ldc * esz);
+  CK(cudaMemcpy(Cs.data(), dC, Cs.size(), cudaMemcpyDeviceToHost));
+  for (int z = 0; z < batch; ++z)   // sum the split-K chunks (mod m for the modular epilogue)
+    for (long long e = 0; e < M * ldc; ++e) {
+      long long acc = 0;
+      for (int c = 0; c < ks; ++c) {
+        const long long off = ((long long)z * ks + c) * M * ldc + e;
+        acc += out == IG_OUT_I32 ? (long long)reinterpret_cast<int*>(Cs.data())[off] : (long long)Cs[off];
+      }
+      if (out == IG_OUT_I32) reinterpret_cast<int*>(C.data())[z * M * ldc + e] = (int)acc;
+      else C[z * M * ldc + e] = (uint8_t)(acc % mods[z % 2]);
+    }
   long long bad = 0, checked = 0;
   for (int z = 0; z < batch; ++z) for (long long m = 0; m < M; ++m) for (long long n = 0; n < N; ++n) {
     if ((flags & IG_UPPER) && (n / 256 + 1) * 256 - 1 < (m / 128) * 128) continue;
@@ -82,12 +93,20 @@ static void timeit_rand(long long M, long long N, long long K, int batch) {
   int8_t *dA, *dB; void* dC; int* dm;
   int mods[2] = {251, 256};
   CK(cudaMalloc(&dA, batch * M * K)); CK(cudaMalloc(&dB, batch * N * K));
-  CK(cudaMalloc(&dC, batch * M * N)); CK(cudaMalloc(&dm, 8));
+  const int ks = getenv("KSPLIT") ? atoi(getenv("KSPLIT")) : 1;
+  CK(cudaMalloc(&dC, batch * M * N * ks)); CK(cudaMalloc(&dm, 8));
   CK(cudaMemcpy(dm, mods, 8, cudaMemcpyHostToDevice));
   {
     std::vector<int8_t> h(1 << 26);
     std::mt19937 rng(5);
     for (auto& x : h) x = (int8_t)(rng() & 255);
+    const bool banded = getenv("BANDED_A") != nullptr;   // A like K's residues: nonzero only near the diagonal
+    if (banded) {
+      std::vector<int8_t> a1(M * K, 0);
+      for (long long m = 0; m < M; ++m)
+        for (long long k = std::max(0LL, m - 24); k < std::min(K, m + 25); ++k) a1[m * K + k] = (int8_t)(rng() & 255);
+      for (int z = 0; z < batch; ++z) CK(cudaMemcpy(dA + z * M * K, a1.data(), M * K, cudaMemcpyHostToDevice));
+    } else
     for (long long o = 0; o < batch * M * K; o += h.size())
       CK(cudaMemcpy(dA + o, h.data(), std::min<long long>(h.size(), batch * M * K - o), cudaMemcpyHostToDevice));
     for (long long o = 0; o < batch * N * K; o += h.size())
@@ -95,6 +114,7 @@ static void timeit_rand(long long M, long long N, long long K, int batch) {
   }
   IgemmArgs g; g.M = M; g.N = N; g.K = K; g.batch = batch; g.A = dA; g.lda = K; g.strideA = M * K;
   g.B = dB; g.ldb = K; g.strideB = N * K; g.C = dC; g.ldc = N; g.strideC = M * N; g.out = IG_OUT_MOD; g.moduli = dm; g.nmod = 2;
+  g.ksplit = ks;
   std::string err;
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   igemm(0, g, &err);
@@ -105,8 +125,9 @@ static void timeit_rand(long long M, long long N, long long K, int batch) {
   cudaEventRecord(e1);
   CK(cudaEventSynchronize(e1));
   float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= reps;
-  printf("random K.U shape M=%lld N=%lld K=%lld batch=%d gm=%s: %.3f ms  %.1f TOPS\n", M, N, K, batch,
-         getenv("TRAJ_IGEMM_GM") ? getenv("TRAJ_IGEMM_GM") : "16", ms, 2.0 * M * N * K * batch / ms / 1e9);
+  printf("%s K.U shape M=%lld N=%lld K=%lld batch=%d gm=%s ksplit=%d: %.3f ms  %.1f TOPS\n",
+         getenv("BANDED_A") ? "banded-A" : "random", M, N, K, batch,
+         getenv("TRAJ_IGEMM_GM") ? getenv("TRAJ_IGEMM_GM") : "16", ks, ms, 2.0 * M * N * K * batch / ms / 1e9);
   cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(dm);
 }
 
@@ -121,6 +142,9 @@ int main(int argc, char** argv) {
   bad |= check(300, 520, 1000, 2, IG_OUT_MOD, 0);
   bad |= check(700, 700, 700, 1, IG_OUT_I32, IG_UPPER);
   bad |= check(400, 700, 700, 1, IG_OUT_I32, IG_TRI_B);
+  bad |= check(300, 520, 1000, 2, IG_OUT_I32, 0, 3);
+  bad |= check(300, 520, 1000, 2, IG_OUT_MOD, 0, 4);
+  bad |= check(400, 700, 700, 1, IG_OUT_I32, IG_TRI_B, 2);
   if (bad) { printf("CHECK FAILED\n"); return 1; }
   timeit(8192, 8192, 8192, 1, IG_OUT_I32);
   timeit(8192, 8192, 8192, 4, IG_OUT_MOD);
