@@ -310,6 +310,264 @@ __global__ void __launch_bounds__(ITHREADS, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
+// ---------------------------------------------------------------------------------------------
+// CTA-pair variant (tcgen05 cta_group::2): a cluster of two CTAs computes 256 x 256 tiles; each CTA
+// stages its 128 rows of A and its 128 rows (n) of B per 128-k block, the leader's elected lane
+// issues 256 x 256 x 32 MMAs that read both CTAs' shared memory, and each CTA's TMEM holds its 128
+// accumulator rows x 256 columns.  A stage is 32 KB per SM (against 48 KB unpaired), so six stages
+// hold 1.5x the k-depth of the unpaired ring and each SM reads a third fewer operand bytes per MAC.
+constexpr int PBM = 256, PBN = 256, PSTAGES = 6;
+constexpr int PA_BYTES = 128 * IBK, PB_BYTES = 128 * IBK, PSTAGE_BYTES = PA_BYTES + PB_BYTES;
+constexpr int PSMEM = PSTAGES * PSTAGE_BYTES + 1024 + 256;
+constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;   // clears the CTA-rank bit of a shared::cluster address
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair(void* smem_dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                 uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4}], [%5];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar) & PEER_MASK)
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {   // arrives at this offset in both CTAs
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {   // the rank-0 CTA's copy of this barrier
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(ra) : "r"(smem_u32(bar)));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ Tile pair_tile_of(const KArgs& a, long long t, int tiles_m2) {
+  const long long per = (long long)tiles_m2 * a.tiles_n;
+  Tile r;
+  const long long zk = t / per;
+  r.z = (int)(zk / a.ksplit);
+  r.kc = (int)(zk - (long long)r.z * a.ksplit);
+  const int rem = (int)(t - zk * per);
+  const int gm = max(1, a.gm / 2);
+  const int gsz = gm * a.tiles_n;
+  const int g = rem / gsz, first = g * gm;
+  const int h = min(gm, tiles_m2 - first), w = rem - g * gsz;
+  r.mb = first + w % h;   // in units of 256 rows
+  r.nb = w / h;
+  return r;
+}
+__device__ __forceinline__ bool pair_tile_live(const KArgs& a, const Tile& t) {
+  if ((a.flags & IG_UPPER) && (t.nb + 1) * PBN - 1 < t.mb * PBM) return false;
+  if (a.ndev && t.nb * PBN >= a.ndev[traj_of(a, t.z)]) return false;
+  return true;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ITHREADS, 1)
+    igemm_i8_pair_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const KArgs a,
+                         const int tiles_m2, const long long ptiles) {
+  if (a.gate && *a.gate == 0) return;   // uniform over the grid (both CTAs of every pair)
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  uint8_t* base = smem_raw + (base_u32 - smem_u32(smem_raw));
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + PSTAGES * PSTAGE_BYTES);
+  uint64_t* empty = full + PSTAGES;
+  uint64_t* tfull = empty + PSTAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const long long pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < PSTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);   // four epilogue warps in each CTA of the pair (used in the leader)
+    }
+    fence_mbar_init();
+    prefetch_tmap(&ta);
+    prefetch_tmap(&tb);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {   // ---------------- TMA producer (both CTAs; bytes land on the leader's barrier)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (long long t = pair; t < ptiles; t += npairs) {
+        const Tile tl = pair_tile_of(a, t, tiles_m2);
+        if (!pair_tile_live(a, tl)) continue;
+        int kb0;
+        const int nk = tile_kblocks(a, tl, &kb0);
+        int za, zb, q;
+        zmap(a, tl.z, za, zb, q);
+        for (int kb = kb0; kb < kb0 + nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = base + stage * PSTAGE_BYTES;
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * PSTAGE_BYTES);
+          tma_load_3d_pair(sa, &ta, kb * IBK, tl.mb * PBM + (int)rank * 128, za, &full[stage]);
+          tma_load_3d_pair(sa + PA_BYTES, &tb, kb * IBK, tl.nb * PBN + (int)rank * 128, zb, &full[stage]);
+          if (++stage == PSTAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {   // ---------------- MMA issuer (leader CTA only)
+      constexpr uint32_t idesc = idesc_i8(PBM, PBN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (long long t = pair; t < ptiles; t += npairs) {
+        const Tile tl = pair_tile_of(a, t, tiles_m2);
+        if (!pair_tile_live(a, tl)) continue;
+        const int nk = tile_kblocks(a, tl);
+        const int buf = it & 1;
+        const uint32_t use = (uint32_t)(it >> 1);
+        mbar_wait_cluster(&tempty[buf], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t dt = tmem + buf * PBN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t sa = base_u32 + stage * PSTAGE_BYTES, sb = sa + PA_BYTES;
+            const uint64_t da = sw128_desc(sa), db = sw128_desc(sb);
+#pragma unroll
+            for (int k = 0; k < IBK / 32; ++k) mma_i8_pair(dt, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            mma_commit_pair(&empty[stage]);
+          }
+          __syncwarp();
+          if (++stage == PSTAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (lane == 0) mma_commit_pair(&tfull[buf]);
+        __syncwarp();
+        ++it;
+      }
+    }
+  } else {   // ---------------- epilogue: warps 2..5 of each CTA, its 128 rows
+    const int q = warp & 3;
+    int it = 0;
+    for (long long t = pair; t < ptiles; t += npairs) {
+      const Tile tl = pair_tile_of(a, t, tiles_m2);
+      if (!pair_tile_live(a, tl)) continue;
+      const int buf = it & 1;
+      const uint32_t use = (uint32_t)(it >> 1);
+      mbar_wait(&tfull[buf], use & 1);
+      tc_fence_after();
+      const int row = tl.mb * PBM + (int)rank * 128 + q * 32 + lane;
+      const bool row_ok = row < a.M;
+      const bool kzero = tile_kblocks(a, tl) == 0;
+      const uint32_t taddr = tmem + buf * PBN + ((uint32_t)(q * 32) << 16);
+      int mod = 0;
+      double inv = 0.0;
+      if (a.out == IG_OUT_MOD) {
+        int za, zb, qq;
+        zmap(a, tl.z, za, zb, qq);
+        mod = a.moduli[qq];
+        inv = 1.0 / (double)mod;
+      }
+#pragma unroll 1
+      for (int c = 0; c < PBN / 32; ++c) {
+        uint32_t v[32];
+        __syncwarp();
+        tmem_ld32(taddr + c * 32, v);
+        if (kzero) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0;
+        }
+        const int col = tl.nb * PBN + c * 32;
+        if (!row_ok || col >= a.N) {
+        } else if (a.out == IG_OUT_I32) {
+          int* p = reinterpret_cast<int*>(a.C) + ((long long)tl.z * a.ksplit + tl.kc) * a.strideC +
+                   (long long)row * a.ldc + col;
+          if (col + 32 <= a.N) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              reinterpret_cast<int4*>(p)[j] = make_int4((int)v[4 * j], (int)v[4 * j + 1], (int)v[4 * j + 2], (int)v[4 * j + 3]);
+          } else {
+            for (int j = 0; col + j < a.N; ++j) p[j] = (int)v[j];
+          }
+        } else {
+          uint32_t w[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            uint32_t packed = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const int x = (int)v[4 * j + b];
+              int r = x - mod * (int)floor((double)x * inv);
+              r += (r < 0) ? mod : 0;
+              r -= (r >= mod) ? mod : 0;
+              packed |= (uint32_t)r << (8 * b);
+            }
+            w[j] = packed;
+          }
+          uint8_t* p = reinterpret_cast<uint8_t*>(a.C) + ((long long)tl.z * a.ksplit + tl.kc) * a.strideC +
+                       (long long)row * a.ldc + col;
+          if (col + 32 <= a.N) {
+            reinterpret_cast<uint4*>(p)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            reinterpret_cast<uint4*>(p)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          } else {
+            for (int j = 0; col + j < a.N; ++j) p[j] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&tempty[buf]);
+      ++it;
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
 typedef CUresult (*PFN_encode_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -371,9 +629,18 @@ int igemm(cudaStream_t st, const IgemmArgs& g, std::string* err) {
     if (err) *err = "igemm: modular batch map needs batch = 3 s T and the modular epilogue";
     return 1;
   }
+  // the CTA-pair kernel from 256 rows on (TRAJ_IGEMM_PAIR=0: always the unpaired one)
+  static int pair_env = -1;
+  if (pair_env < 0) {
+    // off by default: on the step's operands (K's residues banded) the pair kernel's wave misses L2 far
+    // more often (420 vs 98 GB of DRAM, profiles/r02/igemm_pair_vs_single.txt) and runs slower
+    const char* v = getenv("TRAJ_IGEMM_PAIR");
+    pair_env = (v && v[0] == '1') ? 1 : 0;
+  }
+  const bool use_pair = pair_env && g.M >= 256 && num_sms() >= 2;
   CUtensorMap ma, mb;
   if (!map_i8(enc, &ma, g.A, g.K, g.M, g.lda, ab ? na : 1, g.strideA, IBM) ||
-      !map_i8(enc, &mb, g.B, g.K, g.N, g.ldb, bb ? nb : 1, g.strideB, IBN)) {
+      !map_i8(enc, &mb, g.B, g.K, g.N, g.ldb, bb ? nb : 1, g.strideB, use_pair ? 128 : IBN)) {
     if (err) *err = "igemm: tensor map";
     return 4;
   }
@@ -418,6 +685,23 @@ int igemm(cudaStream_t st, const IgemmArgs& g, std::string* err) {
   for (int i = 0; i < 3; ++i) {
     a.oz_pa[i] = g.oz_pa[i];
     a.oz_pb[i] = g.oz_pb[i];
+  }
+  if (use_pair) {
+    const int tiles_m2 = (int)ceil_div(g.M, PBM);
+    const long long ptiles = g.batch * a.ksplit * (long long)tiles_m2 * a.tiles_n;
+    if (ensure_smem((const void*)igemm_i8_pair_kernel, PSMEM) != cudaSuccess) {
+      if (err) *err = "igemm: shared memory attribute (pair)";
+      return 4;
+    }
+    const long long npairs = std::min<long long>(ptiles, num_sms() / 2);
+    igemm_i8_pair_kernel<<<(unsigned)(2 * npairs), ITHREADS, PSMEM, st>>>(ma, mb, a, tiles_m2, ptiles);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      if (err) *err = std::string("igemm (pair): ") + cudaGetErrorString(e);
+      return 4;
+    }
+    return 0;
   }
   if (ensure_smem((const void*)igemm_i8_kernel, ISMEM) != cudaSuccess) {
     if (err) *err = "igemm: shared memory attribute";

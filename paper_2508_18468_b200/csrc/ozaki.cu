@@ -193,11 +193,13 @@ template <int S, int NP>
 __global__ void __launch_bounds__(256) oz_split_rows_kernel(const cplx* __restrict__ X, long long ldx, long long sX,
                                                             int rows, int cols_cap, int T, int conj, int8_t* R,
                                                             long long ldr, int* e, long long sE, int beta,
-                                                            const int32_t* gate, const int32_t* cdev) {
+                                                            const int32_t* gate, const int32_t* cdev,
+                                                            const int32_t* rdev) {
   if (gate && *gate == 0) return;
   const int row = blockIdx.x, t = blockIdx.y;
   const cplx* x = X + t * sX + (long long)row * ldx;
-  const int cols = cdev ? min(cols_cap, cdev[t]) : cols_cap;   // past it: zero residues
+  // past cdev (columns) or rdev (rows): zero residues
+  const int cols = (rdev && row >= rdev[t]) ? 0 : (cdev ? min(cols_cap, cdev[t]) : cols_cap);
   __shared__ double red[8];
   __shared__ int ex_s;
   double acc = 0.0;
@@ -242,10 +244,11 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const cplx* __restri
 // per-column partial sums of (|re| + |im|)^2 over 8 row chunks: part[(c T + t) cols + j]
 __global__ void __launch_bounds__(256) oz_colnorm_kernel(const cplx* __restrict__ X, long long ldx, long long sX,
                                                          int rows, int cols, int T, double* part, int subI,
-                                                         const int32_t* gate) {
+                                                         const int32_t* gate, const int32_t* rdev) {
   if (gate && *gate == 0) return;
   const int j = blockIdx.x * 32 + threadIdx.x, c = blockIdx.y, t = blockIdx.z;
-  const int per = (rows + 7) / 8, r0 = c * per, r1 = min(rows, r0 + per);
+  const int rz = rdev ? min(rows, rdev[t]) : rows;
+  const int per = (rows + 7) / 8, r0 = c * per, r1 = min(rz, r0 + per);
   double acc = 0.0;
   if (j < cols) {
     const cplx* x = X + t * sX + j;
@@ -286,17 +289,19 @@ template <int S, int NP>
 __global__ void __launch_bounds__(256) oz_split_cols_kernel(const cplx* __restrict__ X, long long ldx, long long sX,
                                                             int rows, int cols, int T, int8_t* R, long long ldr,
                                                             int* e, long long sE, const double* part, int beta,
-                                                            int subI, const int32_t* gate, const int32_t* cdev) {
+                                                            int subI, const int32_t* gate, const int32_t* cdev,
+                                                            const int32_t* rdev) {
   if (gate && *gate == 0) return;
   __shared__ cplx tile[CTI][CTJ + 1];
   const int j0 = blockIdx.x * CTJ, i0 = blockIdx.y * CTI, t = blockIdx.z;
   const int cz = cdev ? min(cols, cdev[t]) : cols;   // columns past cz are taken as zero
+  const int rz = rdev ? min(rows, rdev[t]) : rows;   // rows past rz too
   const cplx* x = X + t * sX;
 #pragma unroll
   for (int r = 0; r < CTI * CTJ / 256; ++r) {
     const int el = threadIdx.x + 256 * r, ii = el / CTJ, jj = el % CTJ;
     const int i = i0 + ii, j = j0 + jj;
-    cplx v = (i < rows && j < cz) ? x[(long long)i * ldx + j] : make_double2(0.0, 0.0);
+    cplx v = (i < rz && j < cz) ? x[(long long)i * ldx + j] : make_double2(0.0, 0.0);
     if (subI && i == j) v.x -= 1.0;
     tile[ii][jj] = v;
   }
@@ -347,14 +352,14 @@ __device__ __forceinline__ void reim(uint32_t a1, uint32_t a2, uint32_t a3, int 
 
 // the residues of 4 consecutive outputs of one (product, modulus): with split-K, the chunks' residues
 // summed and reduced mod m
-template <int Q>
+template <int Q, bool KS1>
 __device__ __forceinline__ void res4(const uint8_t* p, long long kstride, int ks, uint32_t (&v)[4]) {
   uchar4 a = *reinterpret_cast<const uchar4*>(p);
   v[0] = a.x;
   v[1] = a.y;
   v[2] = a.z;
   v[3] = a.w;
-  if (ks > 1) {
+  if (!KS1 && ks > 1) {
     for (int c = 1; c < ks; ++c) {
       a = *reinterpret_cast<const uchar4*>(p + c * kstride);
       v[0] += a.x;
@@ -367,7 +372,7 @@ __device__ __forceinline__ void res4(const uint8_t* p, long long kstride, int ks
   }
 }
 
-template <int S, int PQ = 0>
+template <int S, bool KS1, int PQ = 0>
 struct CrtPair {
   __device__ __forceinline__ static void run(const uint8_t* P, long long qstride, long long pstride, long long kstride,
                                              int ks, int neg2, double (&sr)[4], double (&lr)[4], double (&si)[4],
@@ -377,12 +382,12 @@ struct CrtPair {
       constexpr uint32_t ma = OZM(QA), mb = OZM(QB);
       constexpr uint32_t inv = (uint32_t)modinv((int)(ma % mb), (int)mb);   // m_a^-1 mod m_b
       uint32_t A1[4], A2[4], A3[4], B1[4], B2[4], B3[4];
-      res4<QA>(P + QA * qstride, kstride, ks, A1);
-      res4<QA>(P + pstride + QA * qstride, kstride, ks, A2);
-      res4<QA>(P + 2 * pstride + QA * qstride, kstride, ks, A3);
-      res4<QB>(P + QB * qstride, kstride, ks, B1);
-      res4<QB>(P + pstride + QB * qstride, kstride, ks, B2);
-      res4<QB>(P + 2 * pstride + QB * qstride, kstride, ks, B3);
+      res4<QA, KS1>(P + QA * qstride, kstride, ks, A1);
+      res4<QA, KS1>(P + pstride + QA * qstride, kstride, ks, A2);
+      res4<QA, KS1>(P + 2 * pstride + QA * qstride, kstride, ks, A3);
+      res4<QB, KS1>(P + QB * qstride, kstride, ks, B1);
+      res4<QB, KS1>(P + pstride + QB * qstride, kstride, ks, B2);
+      res4<QB, KS1>(P + 2 * pstride + QB * qstride, kstride, ks, B3);
       const double ch = c_ch[S][PQ], cl = c_cl[S][PQ];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -400,7 +405,7 @@ struct CrtPair {
         lr[k] = fma((double)rr, cl, lr[k]);
         li[k] = fma((double)ri, cl, li[k]);
       }
-      CrtPair<S, PQ + 1>::run(P, qstride, pstride, kstride, ks, neg2, sr, lr, si, li);
+      CrtPair<S, KS1, PQ + 1>::run(P, qstride, pstride, kstride, ks, neg2, sr, lr, si, li);
     }
   }
 };
@@ -412,7 +417,7 @@ __device__ __forceinline__ double crt_value(double s, double l, double M) {
   return f * M;
 }
 
-template <int S>
+template <int S, bool KS1>
 __global__ void __launch_bounds__(128) oz_combine_kernel(const uint8_t* __restrict__ P, long long ldp, int M, int N,
                                                          int T, const int* __restrict__ eA, long long sEA, int a_traj,
                                                          const int* __restrict__ eB, long long sEB, int flags, cplx* C,
@@ -427,7 +432,7 @@ __global__ void __launch_bounds__(128) oz_combine_kernel(const uint8_t* __restri
   const long long kstride = (long long)M * ldp, qstride = (long long)T * ks * kstride, pstride = (long long)S * qstride;
   const uint8_t* p = P + ((long long)t * ks * M + i) * ldp + j0;
   double sr[4] = {0, 0, 0, 0}, lr[4] = {0, 0, 0, 0}, si[4] = {0, 0, 0, 0}, li[4] = {0, 0, 0, 0};
-  CrtPair<S>::run(p, qstride, pstride, kstride, ks, (flags & OZ_NEG_P2) ? 1 : 0, sr, lr, si, li);
+  CrtPair<S, KS1>::run(p, qstride, pstride, kstride, ks, (flags & OZ_NEG_P2) ? 1 : 0, sr, lr, si, li);
   const double Md = c_M[S];
   const int ea = eA[(a_traj ? t : 0) * sEA + i];
   cplx* c = C + t * sC + (long long)i * ldc;
@@ -480,13 +485,13 @@ template <int S>
 struct LaunchRows {
   static int go(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T, int conj,
                 int8_t* R, long long ldr, int* e, long long sE, int beta, const int32_t* gate, const int32_t* cdev,
-                int np) {
+                int np, const int32_t* rdev) {
     if (np == 4)
       oz_split_rows_kernel<S, 4><<<dim3(rows, T), 256, 0, st>>>(X, ldx, sX, rows, cols, T, conj, R, ldr, e, sE, beta,
-                                                                gate, cdev);
+                                                                gate, cdev, rdev);
     else
       oz_split_rows_kernel<S, 3><<<dim3(rows, T), 256, 0, st>>>(X, ldx, sX, rows, cols, T, conj, R, ldr, e, sE, beta,
-                                                                gate, cdev);
+                                                                gate, cdev, rdev);
     return 0;
   }
 };
@@ -495,14 +500,14 @@ template <int S>
 struct LaunchCols {
   static int go(cudaStream_t st, int np, const cplx* X, long long ldx, long long sX, int rows, int cols, int T,
                 int8_t* R, long long ldr, int* e, long long sE, const double* part, int beta, int subI,
-                const int32_t* gate, const int32_t* cdev) {
+                const int32_t* gate, const int32_t* cdev, const int32_t* rdev) {
     dim3 grid(ceil_div(cols, CTJ), ceil_div(rows, CTI), T);
     if (np == 4)
       oz_split_cols_kernel<S, 4><<<grid, 256, 0, st>>>(X, ldx, sX, rows, cols, T, R, ldr, e, sE, part, beta, subI, gate,
-                                                       cdev);
+                                                       cdev, rdev);
     else
       oz_split_cols_kernel<S, 3><<<grid, 256, 0, st>>>(X, ldx, sX, rows, cols, T, R, ldr, e, sE, part, beta, subI, gate,
-                                                       cdev);
+                                                       cdev, rdev);
     return 0;
   }
 };
@@ -511,9 +516,13 @@ template <int S>
 struct LaunchCombine {
   static int go(cudaStream_t st, const OzProduct& p) {
     dim3 grid(ceil_div(p.N, 512), p.M, p.T);
-    oz_combine_kernel<S><<<grid, 128, 0, st>>>(p.RC, oz_ld(p.N), p.M, p.N, p.T, p.eA, p.sEA, p.a_traj, p.eB, p.sEB,
-                                               p.flags, p.C, p.ldc, p.sC, p.base, p.gate, p.ndev,
-                                               std::max(1, p.ksplit));
+    if (p.ksplit > 1)
+      oz_combine_kernel<S, false><<<grid, 128, 0, st>>>(p.RC, oz_ld(p.N), p.M, p.N, p.T, p.eA, p.sEA, p.a_traj, p.eB,
+                                                        p.sEB, p.flags, p.C, p.ldc, p.sC, p.base, p.gate, p.ndev,
+                                                        p.ksplit);
+    else
+      oz_combine_kernel<S, true><<<grid, 128, 0, st>>>(p.RC, oz_ld(p.N), p.M, p.N, p.T, p.eA, p.sEA, p.a_traj, p.eB,
+                                                       p.sEB, p.flags, p.C, p.ldc, p.sC, p.base, p.gate, p.ndev, 1);
     return 0;
   }
 };
@@ -535,7 +544,7 @@ int oz_beta(int s) { return oz_supported(s) ? host_const().beta[s] : 0; }
 
 int oz_split_rows(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T, int conj,
                   int s, int8_t* R, int* e, long long sE, std::string* err, const int32_t* gate, const int32_t* cdev,
-                  int nplanes) {
+                  int nplanes, const int32_t* rdev) {
   if (rows <= 0 || cols <= 0 || T <= 0) return 0;
   const int* md;
   if (!oz_supported(s) || rows >= 65536 * 32 || T > 65535) {
@@ -547,13 +556,14 @@ int oz_split_rows(cudaStream_t st, const cplx* X, long long ldx, long long sX, i
     if (err) *err = "oz_split_rows: 3 or 4 planes";
     return 1;
   }
-  dispatch_s<LaunchRows>(s, st, X, ldx, sX, rows, cols, T, conj, R, oz_ld(cols), e, sE, oz_beta(s), gate, cdev, nplanes);
+  dispatch_s<LaunchRows>(s, st, X, ldx, sX, rows, cols, T, conj, R, oz_ld(cols), e, sE, oz_beta(s), gate, cdev, nplanes,
+                         rdev);
   return launched("oz_split_rows", err);
 }
 
 int oz_split_cols(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T, int nplanes,
                   int s, int8_t* R, int* e, long long sE, double* part, std::string* err, int sub_identity,
-                  const int32_t* gate, const int32_t* cdev) {
+                  const int32_t* gate, const int32_t* cdev, const int32_t* rdev) {
   if (rows <= 0 || cols <= 0 || T <= 0) return 0;
   const int* md;
   if (!oz_supported(s) || (nplanes != 3 && nplanes != 4) || T > 65535 || ceil_div(rows, CTI) > 65535) {
@@ -562,10 +572,10 @@ int oz_split_cols(cudaStream_t st, const cplx* X, long long ldx, long long sX, i
   }
   if (int r = ensure_device_constants(&md, err)) return r;
   oz_colnorm_kernel<<<dim3(ceil_div(cols, 32), 8, T), dim3(32, 8), 0, st>>>(X, ldx, sX, rows, cols, T, part,
-                                                                            sub_identity, gate);
+                                                                            sub_identity, gate, rdev);
   if (int r = launched("oz_colnorm", err)) return r;
   if (dispatch_s<LaunchCols>(s, st, nplanes, X, ldx, sX, rows, cols, T, R, oz_ld(rows), e, sE, part, oz_beta(s),
-                             sub_identity, gate, cdev)) {
+                             sub_identity, gate, cdev, rdev)) {
     if (err) *err = "oz_split_cols: shared memory attribute";
     return 4;
   }
@@ -601,7 +611,7 @@ int oz_product_mma(cudaStream_t st, const OzProduct& p, std::string* err) {
   g.K = p.K;
   g.batch = 3LL * p.s * p.T;
   g.A = p.RA;
-  g.lda = oz_ld(p.K);
+  g.lda = p.lda_override ? p.lda_override : oz_ld(p.K);
   g.strideA = (long long)p.M * g.lda;
   g.B = p.RB;
   g.ldb = oz_ld(p.K);

@@ -35,14 +35,15 @@ inline long long oz_ld(long long K) { return round_up(K, 16); }
 // cdev (device, per trajectory, optional): columns j >= cdev[t] of X are taken as zero
 int oz_split_rows(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T, int conj,
                   int s, int8_t* R, int* e, long long sE, std::string* err, const int32_t* gate = nullptr,
-                  const int32_t* cdev = nullptr, int nplanes = 3);
+                  const int32_t* cdev = nullptr, int nplanes = 3, const int32_t* rdev = nullptr);
 
 // B operand from the columns of X: residue row j = X column j over k = X's rows; planes
 // (re, im, re + im[, re - im]) for nplanes = 3 [4]; part: >= 8 * T * cols doubles of scratch.
 // sub_identity: the operand is X - I (square X).  gate (device, optional): skip when *gate == 0.
 int oz_split_cols(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T, int nplanes,
                   int s, int8_t* R, int* e, long long sE, double* part, std::string* err, int sub_identity = 0,
-                  const int32_t* gate = nullptr, const int32_t* cdev = nullptr);
+                  const int32_t* gate = nullptr, const int32_t* cdev = nullptr, const int32_t* rdev = nullptr);
+// (rdev, both splits: rows r >= rdev[t] of X are taken as zero)
 
 enum OzFlags {
   OZ_UPPER = 1,       // C upper triangular (only j >= i computed and written)
@@ -74,6 +75,7 @@ struct OzProduct {
   const int32_t* kdev = nullptr;   // per trajectory: the contraction runs over k < kdev[t] (operands zero past it)
   const int32_t* ndev = nullptr;   // per trajectory: only columns j < ndev[t] of C are computed and written
   int ksplit = 1;                  // split-K chunks of the INT8 launch (RC holds ksplit x the residue products)
+  long long lda_override = 0;      // RA's row length in bytes when it is a k-range of wider residue rows
 };
 
 // the products (one batched INT8 launch) and the CRT combine into C

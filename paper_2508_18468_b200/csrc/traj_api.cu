@@ -461,7 +461,10 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
       // the GPU better and the factor has fewer sequential blocks (measured: c5 chol phase 399 ms at
       // b = 128, 306 ms at 512; c3 flat from 128 to 512)
       const char* sbv = getenv("TRAJ_STRUCT_B");
-      h->sb = sbv ? std::max(16, std::min(1024, atoi(sbv) / 16 * 16)) : (cap >= 1024 ? 512 : 128);
+      // on the modular path the solve's per-block residue splits of the L x k0 accumulator favour fewer,
+      // wider blocks (c5: 2048)
+      h->sb = sbv ? std::max(16, std::min(4096, atoi(sbv) / 16 * 16))
+                  : (cap >= 1024 ? (h->oz_cqr && cap >= h->oz_proj_min ? 2048 : 512) : 128);
       const long long b = h->sb;
       lay.take(h->sY, (size_t)T * cap * b * 16);
       lay.take(h->sC, (size_t)T * b * b * 16);
@@ -545,6 +548,91 @@ int prod3(traj_ctx* h, int opA, long long M, long long N, long long K, const dou
                &h->err, 0, n_off);
 }
 
+// The structured pass 1's solve dst = src R^-1 (structchol.h) with its products on the INT8 modular
+// path (many zeroed rows, c5: k0 ~ 1830): the block-diagonal part dst_c = src_c X_c from one row split
+// of src (each block's k-range is a byte offset into the residues), then per block c
+//   dst_c += A W_c   (A = sum_{d<c} dst_d Z_d^dag, L x k0; W_c past row k0 taken as zero)
+//   A (+)= dst_c Z_c^dag  (columns past k0 skipped)
+// with k0 bounding the INT8 launches on the device.
+int struct_chol_apply_oz(traj_ctx* h, const StructChol& s, const cplx* src, cplx* dst) {
+  const int b = s.b, N = s.N, kc = s.kc, T = s.T, L = h->L, sq = h->oz_s;
+  const long long sA = (long long)L * h->ldcap;
+  cplx* A = h->Tm;
+  const int32_t* k0 = h->lr_kdev;
+  const int nblk = (int)ceil_div(N, b);
+  auto prod = [&](int M, int Nn, int K, const int8_t* RA, const int* eA, long long sEA, const int8_t* RB, const int* eB,
+                  long long sEB, cplx* C, long long ldc, long long sC, const cplx* base, int flags,
+                  const int32_t* kdev, const int32_t* ndev) {
+    OzProduct p;
+    p.M = M;
+    p.N = Nn;
+    p.K = K;
+    p.T = T;
+    p.s = sq;
+    p.RA = RA;
+    p.a_traj = 1;
+    p.eA = eA;
+    p.sEA = sEA;
+    p.RB = RB;
+    p.eB = eB;
+    p.sEB = sEB;
+    p.RC = h->RC;
+    p.C = C;
+    p.ldc = ldc;
+    p.sC = sC;
+    p.base = base;
+    p.flags = flags;
+    p.kdev = kdev;
+    p.ndev = ndev;
+    return oz_product(h->st, p, &h->err);
+  };
+  // block-diagonal part: src's row residues once; block c's k-range starts c0 bytes into each row
+  TRY(oz_split_rows(h->st, src, h->ldN, h->sU, L, N, T, 0, sq, h->RU, h->eU, L, &h->err));
+  for (int c = 0; c < nblk; ++c) {
+    const int c0 = c * b, bc = std::min(b, N - c0);
+    const cplx* Xc = s.Xb + (long long)c0 * b;
+    TRY(oz_split_cols(h->st, Xc, b, s.sXb, bc, bc, T, 3, sq, h->RX, h->eX, N, h->oz_part, &h->err));
+    // A = src's residues at k offset c0: same planes / moduli / trajectory strides, row length oz_ld(N)
+    OzProduct p;
+    p.M = L;
+    p.N = bc;
+    p.K = bc;
+    p.T = T;
+    p.s = sq;
+    p.RA = h->RU + c0;
+    p.a_traj = 1;
+    p.lda_override = oz_ld(N);
+    p.eA = h->eU;
+    p.sEA = L;
+    p.RB = h->RX;
+    p.eB = h->eX;
+    p.sEB = N;
+    p.RC = h->RC;
+    p.C = dst + c0;
+    p.ldc = h->ldN;
+    p.sC = h->sU;
+    p.flags = OZ_TRI_B;
+    TRY(oz_product(h->st, p, &h->err));
+  }
+  // the sequential part
+  for (int c = 0; c < nblk; ++c) {
+    const int c0 = c * b, bc = std::min(b, N - c0);
+    if (c > 0) {   // dst_c += A W_c: A's rows (k < k0), W_c's columns (rows past k0 zero)
+      TRY(oz_split_rows(h->st, A, h->ldcap, sA, L, kc, T, 0, sq, h->RU, h->eU, L, &h->err, nullptr, k0));
+      TRY(oz_split_cols(h->st, s.W + c0, s.ldWZ, s.sWZ, kc, bc, T, 3, sq, h->RX, h->eX, N, h->oz_part, &h->err, 0,
+                        nullptr, nullptr, k0));
+      TRY(prod(L, bc, kc, h->RU, h->eU, L, h->RX, h->eX, N, dst + c0, h->ldN, h->sU, dst + c0, 0, k0, nullptr));
+    }
+    if (c + 1 < nblk) {   // A (+)= dst_c Z_c^dag: dst_c's rows, Z_c's rows conjugated (rows past k0 zero)
+      TRY(oz_split_rows(h->st, dst + c0, h->ldN, h->sU, L, bc, T, 0, sq, h->RU, h->eU, L, &h->err));
+      TRY(oz_split_rows(h->st, s.Z + c0, s.ldWZ, s.sWZ, kc, bc, T, 1, sq, h->RX, h->eX, N, &h->err, nullptr, nullptr, 3,
+                        k0));
+      TRY(prod(L, kc, bc, h->RU, h->eU, L, h->RX, h->eX, N, A, h->ldcap, sA, c > 0 ? A : nullptr, 0, nullptr, k0));
+    }
+  }
+  return 0;
+}
+
 // CholeskyQR pass 1 after a projective step on the structure of its Gram, G = I - V^dag V
 // (structchol.h): V = the k0 zeroed rows in US (capacity kc, zero past k0), M in Dw, A in Tm.
 int structured_pass1(traj_ctx* h, const cplx* src, cplx* dst, int kc) {
@@ -568,6 +656,7 @@ int structured_pass1(traj_ctx* h, const cplx* src, cplx* dst, int kc) {
   s.sWZ = h->sUS;
   s.chol_scratch = h->s_chol_scratch;
   TRY(struct_chol_factor(h->st, s, h->US, h->ldN, h->sUS, h->lr_kdev, h->failed_dev, &h->err));
+  if (h->oz_cqr && kc >= h->oz_proj_min) return struct_chol_apply_oz(h, s, src, dst);
   return struct_chol_apply(h->st, s, h->L, src, dst, h->ldN, h->sU, h->Tm, h->ldcap, (long long)h->L * h->ldcap,
                            h->lr_kdev, &h->err);
 }

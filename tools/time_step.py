@@ -1,0 +1,31 @@
+"""Device time per step and per phase of a config (CUDA events on the handle's stream), for A/B runs of
+environment switches: python tools/time_step.py --config c5 --warmup 1 --steps 2"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import workloads  # noqa: E402
+import paper_2508_18468_b200 as P  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c3")
+ap.add_argument("--steps", type=int, default=2)
+ap.add_argument("--warmup", type=int, default=1)
+a = ap.parse_args()
+w = workloads.CONFIGS[a.config]()
+tr = P.Trajectories(w.Lx, w.Ly, w.protocol, [w.gamma_of(0)], dt=w.dt, seed=w.seed)
+tr.step(a.warmup)
+torch.cuda.synchronize()
+tr.profile(True)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(tr.stream)
+tr.step(a.steps)
+e1.record(tr.stream)
+torch.cuda.synchronize()
+ph = tr.phase_times()
+env = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("TRAJ_"))
+print(f"{a.config} [{env}] {e0.elapsed_time(e1) / a.steps:.1f} ms/step  " +
+      " ".join(f"{k}={v[0] / a.steps:.1f}" for k, v in ph.items() if v[0] > 0), flush=True)
