@@ -23,25 +23,21 @@ namespace traj {
     if (s_) return s_;    \
   } while (0)
 
-int struct_chol_factor(cudaStream_t st, StructChol& s, const cplx* V, long long ldV, long long sV,
-                       const int32_t* k_dev, int32_t* failed, std::string* err) {
+namespace {
+
+// block c of the structured factor (see struct_chol_factor)
+int factor_block(cudaStream_t st, StructChol& s, const cplx* V, long long ldV, long long sV, const int32_t* k_dev,
+                 int32_t* failed, std::string* err, int c) {
   const int b = s.b, N = s.N, kc = s.kc, T = s.T;
-  DevBounds bk;     // reductions over the k0 rows of V, outputs with k0 rows (the rest is zero)
+  DevBounds bk;
   bk.k = k_dev;
   bk.m = k_dev;
-  DevBounds bm;     // outputs with k0 rows
+  DevBounds bm;
   bm.m = k_dev;
-  DevBounds bmn;    // k0 x k0 outputs
+  DevBounds bmn;
   bmn.m = k_dev;
   bmn.n = k_dev;
-  // M = I
-  if (cudaMemsetAsync(s.M, 0, (size_t)((T - 1) * s.sM + (long long)kc * s.ldM) * 16, st) != cudaSuccess) {
-    if (err) *err = "struct_chol: memset";
-    return 4;
-  }
-  SC_TRY(axpby_identity(st, s.M, s.ldM, s.sM, kc, T, 1.0, 1.0, err));
   const int nblk = (int)ceil_div(N, b);
-  for (int c = 0; c < nblk; ++c) {
     const int c0 = c * b, bc = std::min(b, N - c0);
     const cplx* Vc = V + c0;
     cplx* Xc = s.Xb + (long long)c0 * b;
@@ -63,7 +59,25 @@ int struct_chol_factor(cudaStream_t st, StructChol& s, const cplx* V, long long 
     if (c + 1 < nblk)
       SC_TRY(zgemm(st, 0, 1, kc, kc, bc, 1.0, 0.0, s.Z + c0, s.ldWZ, s.sWZ, s.Z + c0, s.ldWZ, s.sWZ, 1.0, s.M, s.ldM,
                    s.sM, T, 0, err, 0, 0, &bmn));
+    return 0;
+}
+
+int factor_init(cudaStream_t st, StructChol& s, std::string* err) {
+  // M = I
+  if (cudaMemsetAsync(s.M, 0, (size_t)((s.T - 1) * s.sM + (long long)s.kc * s.ldM) * 16, st) != cudaSuccess) {
+    if (err) *err = "struct_chol: memset";
+    return 4;
   }
+  return axpby_identity(st, s.M, s.ldM, s.sM, s.kc, s.T, 1.0, 1.0, err);
+}
+
+}  // namespace
+
+int struct_chol_factor(cudaStream_t st, StructChol& s, const cplx* V, long long ldV, long long sV,
+                       const int32_t* k_dev, int32_t* failed, std::string* err) {
+  SC_TRY(factor_init(st, s, err));
+  const int nblk = (int)ceil_div(s.N, s.b);
+  for (int c = 0; c < nblk; ++c) SC_TRY(factor_block(st, s, V, ldV, sV, k_dev, failed, err, c));
   return 0;
 }
 
@@ -88,6 +102,48 @@ int struct_chol_apply(cudaStream_t st, const StructChol& s, int Lr, const cplx* 
   // the sequential part: dst_c += A W_c,  A (+)= dst_c Z_c^dag
   for (int c = 0; c < nblk; ++c) {
     const int c0 = c * b, bc = std::min(b, N - c0);
+    if (c > 0)
+      SC_TRY(zgemm(st, 0, 0, Lr, bc, kc, 1.0, 0.0, A, ldA, sA, s.W + c0, s.ldWZ, s.sWZ, 1.0, dst + c0, ldU, sU, T, 0,
+                   err, 0, 0, &bk));
+    if (c + 1 < nblk)
+      SC_TRY(zgemm(st, 0, 1, Lr, kc, bc, 1.0, 0.0, dst + c0, ldU, sU, s.Z + c0, s.ldWZ, s.sWZ, c > 0 ? 1.0 : 0.0, A,
+                   ldA, sA, T, 0, err, 0, 0, &bn));
+  }
+  return 0;
+}
+
+int struct_chol_pipelined(cudaStream_t st, cudaStream_t aux, cudaEvent_t* ev, int nev, StructChol& s, const cplx* V,
+                          long long ldV, long long sV, const int32_t* k_dev, int32_t* failed, int Lr, const cplx* src,
+                          cplx* dst, long long ldU, long long sU, cplx* A, long long ldA, long long sA,
+                          std::string* err) {
+  const int b = s.b, N = s.N, kc = s.kc, T = s.T;
+  const int nblk = (int)ceil_div(N, b);
+  if (nblk > nev) {
+    if (err) *err = "struct_chol_pipelined: too few events";
+    return 1;
+  }
+  // the factor chain on aux, an event after each block
+  SC_TRY(factor_init(aux, s, err));
+  for (int c = 0; c < nblk; ++c) {
+    SC_TRY(factor_block(aux, s, V, ldV, sV, k_dev, failed, err, c));
+    if (cudaEventRecord(ev[c], aux) != cudaSuccess) {
+      if (err) *err = "struct_chol_pipelined: event record";
+      return 4;
+    }
+  }
+  // the solve on st, block c after factor block c
+  DevBounds bk, bn;
+  bk.k = k_dev;
+  bn.n = k_dev;
+  for (int c = 0; c < nblk; ++c) {
+    const int c0 = c * b, bc = std::min(b, N - c0);
+    if (cudaStreamWaitEvent(st, ev[c], 0) != cudaSuccess) {
+      if (err) *err = "struct_chol_pipelined: event wait";
+      return 4;
+    }
+    // dst_c = src_c X_c (+ A W_c), A (+)= dst_c Z_c^dag
+    SC_TRY(zgemm(st, 0, 0, Lr, bc, bc, 1.0, 0.0, src + c0, ldU, sU, s.Xb + (long long)c0 * b, b, s.sXb, 0.0, dst + c0,
+                 ldU, sU, T, TRAJ_TRI_B_UPPER_F, err));
     if (c > 0)
       SC_TRY(zgemm(st, 0, 0, Lr, bc, kc, 1.0, 0.0, A, ldA, sA, s.W + c0, s.ldWZ, s.sWZ, 1.0, dst + c0, ldU, sU, T, 0,
                    err, 0, 0, &bk));

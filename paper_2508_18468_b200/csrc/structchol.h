@@ -37,4 +37,14 @@ int struct_chol_factor(cudaStream_t st, StructChol& s, const cplx* V, long long 
 int struct_chol_apply(cudaStream_t st, const StructChol& s, int Lr, const cplx* src, cplx* dst, long long ldU,
                       long long sU, cplx* A, long long ldA, long long sA, const int32_t* k_dev, std::string* err);
 
+// The factor and the solve pipelined over two streams: block c's factor (a chain of small launches) is
+// issued on aux, and the solve of block c on st waits only for it (events ev[0..nblk), created by the
+// caller), so the latency-bound factor chain runs under the solve's L-row GEMMs.  V is read on aux:
+// the caller orders aux after V's producer; st is joined with aux on return.  Same results as
+// struct_chol_factor followed by struct_chol_apply.
+int struct_chol_pipelined(cudaStream_t st, cudaStream_t aux, cudaEvent_t* ev, int nev, StructChol& s, const cplx* V,
+                          long long ldV, long long sV, const int32_t* k_dev, int32_t* failed, int Lr, const cplx* src,
+                          cplx* dst, long long ldU, long long sU, cplx* A, long long ldA, long long sA,
+                          std::string* err);
+
 }  // namespace traj

@@ -154,6 +154,8 @@ struct traj_ctx {
   const int32_t* lr_kdev = nullptr;      // device bound of pass 1's V rows (k0), with lr_k0 its capacity
   // CholeskyQR pass 1 on the structure G = I - V^dag V (structured_pass1; TRAJ_STRUCT_CHOL=0: dense)
   bool struct_chol = true;
+  bool struct_serial = false;            // TRAJ_STRUCT_PIPELINE=0: factor and solve on one stream
+  std::vector<cudaEvent_t> sc_ev;        // per-block events of the pipelined structured pass 1
   int sb = 128;                          // column block of the structured factorisation
   cplx *sY = nullptr, *sC = nullptr, *sX = nullptr, *sW = nullptr, *sZ = nullptr;
   void* s_chol_scratch = nullptr;
@@ -655,8 +657,25 @@ int structured_pass1(traj_ctx* h, const cplx* src, cplx* dst, int kc) {
   s.ldWZ = h->ldN;
   s.sWZ = h->sUS;
   s.chol_scratch = h->s_chol_scratch;
+  const bool oz_apply = h->oz_cqr && kc >= h->oz_proj_min;
+  if (!oz_apply && h->chol_overlap && h->st_hi && !h->struct_serial) {
+    // the factor chain on the high-priority stream, each solve block after its factor block
+    const int nblk = (int)ceil_div(h->N, h->sb);
+    while ((int)h->sc_ev.size() < nblk) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      h->sc_ev.push_back(e);
+    }
+    CK(cudaEventRecord(h->ev_fork, h->st));
+    CK(cudaStreamWaitEvent(h->st_hi, h->ev_fork, 0));
+    return struct_chol_pipelined(h->st, h->st_hi, h->sc_ev.data(), (int)h->sc_ev.size(), s, h->US, h->ldN, h->sUS,
+                                 h->lr_kdev, h->failed_dev, h->L, src, dst, h->ldN, h->sU, h->Tm, h->ldcap,
+                                 (long long)h->L * h->ldcap, &h->err)
+               ? fail(h, TRAJ_ECUDA, h->err)
+               : 0;
+  }
   TRY(struct_chol_factor(h->st, s, h->US, h->ldN, h->sUS, h->lr_kdev, h->failed_dev, &h->err));
-  if (h->oz_cqr && kc >= h->oz_proj_min) return struct_chol_apply_oz(h, s, src, dst);
+  if (oz_apply) return struct_chol_apply_oz(h, s, src, dst);
   return struct_chol_apply(h->st, s, h->L, src, dst, h->ldN, h->sU, h->Tm, h->ldcap, (long long)h->L * h->ldcap,
                            h->lr_kdev, &h->err);
 }
@@ -1820,6 +1839,8 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
     if (tl) h->lowrank_tol = atof(tl);
     const char* sc = getenv("TRAJ_STRUCT_CHOL");
     h->struct_chol = !(sc && sc[0] == '0');
+    const char* sp = getenv("TRAJ_STRUCT_PIPELINE");
+    h->struct_serial = sp && sp[0] == '0';
     const char* sm = getenv("TRAJ_SMALL_STEP");
     const bool proj = cfg->protocol == TRAJ_PROJECTIVE;
     h->small = !h->sh && !h->banded && h->K && !(sm && sm[0] == '0') && !h->lowrank_orth &&
@@ -2218,6 +2239,7 @@ int traj_destroy(traj_handle h) {
     }
   for (cudaEvent_t e : {h->ev_fork, h->ev_left, h->ev_lo_done, h->ev_hi_done, h->ev_split})
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : h->sc_ev) cudaEventDestroy(e);
   if (h->solver) cusolverDnDestroy(h->solver);
   if (h->h_small) cudaFreeHost(h->h_small);
   if (h->h_dev) cudaFreeHost(h->h_dev);

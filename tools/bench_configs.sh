@@ -20,3 +20,6 @@ python bench.py --protocol homodyne --steps 5 --warmup 3 $common >> $out 2>/dev/
 python bench.py --protocol homodyne_rk4 --steps 5 --warmup 3 $common >> $out 2>/dev/null
 python bench.py --protocol projective_events --steps 3 --warmup 2 $common >> $out 2>/dev/null
 python bench.py --protocol projective_events --orthonormalizer lowrank --steps 3 --warmup 2 $common >> $out 2>/dev/null
+# the DMMA contractions instead of the modular INT8 products (A/B of the round-2 engine)
+TRAJ_OZAKI=0 python bench.py --steps 5 --warmup 3 $common >> $out 2>/dev/null
+TRAJ_OZAKI=0 python bench.py --config c5 --steps 2 --warmup 2 $common >> $out 2>/dev/null
