@@ -16,7 +16,14 @@
 namespace traj {
 namespace {
 
-constexpr int IBM = 128, IBN = 256, IBK = 128, ISTAGES = 4;
+// IGEMM_BK: bytes of k per pipeline stage (128: 128B-swizzled rows, 4 stages; 64: 64B-swizzled rows,
+// 8 stages of half the size -- finer refill granularity for the same bytes in flight)
+#ifndef IGEMM_BK
+#define IGEMM_BK 128
+#endif
+constexpr int IBM = 128, IBN = 256, IBK = IGEMM_BK, ISTAGES = 4 * 128 / IGEMM_BK;
+constexpr int SW_ROW = IGEMM_BK;                       // swizzle span = one row of a stage
+constexpr uint32_t SW_LAYOUT = IGEMM_BK == 128 ? 2 : 4;  // SWIZZLE_128B / SWIZZLE_64B descriptor codes
 constexpr int IA_BYTES = IBM * IBK, IB_BYTES = IBN * IBK, ISTAGE_BYTES = IA_BYTES + IB_BYTES;
 constexpr int ITHREADS = 192;
 constexpr int ISMEM = ISTAGES * ISTAGE_BYTES + 1024 + 256;
@@ -26,8 +33,8 @@ constexpr int IGM = 16;
 
 // K-major operand, 128-byte rows, 128B swizzle (8-row atoms of 1 KB): SBO = 1024 B, version 1.
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)((8 * SW_ROW) >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)SW_LAYOUT << 61);
 }
 
 // instruction descriptor: D s32, A s8, B s8, both K-major, N >> 3 at bit 17, M >> 4 at bit 24
@@ -316,7 +323,7 @@ __global__ void __launch_bounds__(ITHREADS, 1)
 // issues 256 x 256 x 32 MMAs that read both CTAs' shared memory, and each CTA's TMEM holds its 128
 // accumulator rows x 256 columns.  A stage is 32 KB per SM (against 48 KB unpaired), so six stages
 // hold 1.5x the k-depth of the unpaired ring and each SM reads a third fewer operand bytes per MAC.
-constexpr int PBM = 256, PBN = 256, PSTAGES = 6;
+constexpr int PBM = 256, PBN = 256, PSTAGES = 6 * 128 / IGEMM_BK;
 constexpr int PA_BYTES = 128 * IBK, PB_BYTES = 128 * IBK, PSTAGE_BYTES = PA_BYTES + PB_BYTES;
 constexpr int PSMEM = PSTAGES * PSTAGE_BYTES + 1024 + 256;
 constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;   // clears the CTA-rank bit of a shared::cluster address
@@ -591,7 +598,8 @@ bool map_i8(PFN_encode_t enc, CUtensorMap* m, const int8_t* p, long long K, long
   cuuint32_t box[3] = {IBK, (cuuint32_t)box_rows, 1};
   cuuint32_t es[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(p), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, IGEMM_BK == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 

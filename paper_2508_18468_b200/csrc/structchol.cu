@@ -112,6 +112,20 @@ int struct_chol_apply(cudaStream_t st, const StructChol& s, int Lr, const cplx* 
   return 0;
 }
 
+int struct_chol_factor_events(cudaStream_t st, StructChol& s, const cplx* V, long long ldV, long long sV,
+                              const int32_t* k_dev, int32_t* failed, cudaEvent_t* ev, std::string* err) {
+  SC_TRY(factor_init(st, s, err));
+  const int nblk = (int)ceil_div(s.N, s.b);
+  for (int c = 0; c < nblk; ++c) {
+    SC_TRY(factor_block(st, s, V, ldV, sV, k_dev, failed, err, c));
+    if (cudaEventRecord(ev[c], st) != cudaSuccess) {
+      if (err) *err = "struct_chol_factor_events: event record";
+      return 4;
+    }
+  }
+  return 0;
+}
+
 int struct_chol_pipelined(cudaStream_t st, cudaStream_t aux, cudaEvent_t* ev, int nev, StructChol& s, const cplx* V,
                           long long ldV, long long sV, const int32_t* k_dev, int32_t* failed, int Lr, const cplx* src,
                           cplx* dst, long long ldU, long long sU, cplx* A, long long ldA, long long sA,

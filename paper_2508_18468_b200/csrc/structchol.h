@@ -42,6 +42,10 @@ int struct_chol_apply(cudaStream_t st, const StructChol& s, int Lr, const cplx* 
 // caller), so the latency-bound factor chain runs under the solve's L-row GEMMs.  V is read on aux:
 // the caller orders aux after V's producer; st is joined with aux on return.  Same results as
 // struct_chol_factor followed by struct_chol_apply.
+// struct_chol_factor with an event recorded on st after each block c (ev[c], created by the caller)
+int struct_chol_factor_events(cudaStream_t st, StructChol& s, const cplx* V, long long ldV, long long sV,
+                              const int32_t* k_dev, int32_t* failed, cudaEvent_t* ev, std::string* err);
+
 int struct_chol_pipelined(cudaStream_t st, cudaStream_t aux, cudaEvent_t* ev, int nev, StructChol& s, const cplx* V,
                           long long ldV, long long sV, const int32_t* k_dev, int32_t* failed, int Lr, const cplx* src,
                           cplx* dst, long long ldU, long long sU, cplx* A, long long ldA, long long sA,

@@ -75,7 +75,7 @@ struct traj_ctx {
   int oz_s_corr = 10;   // moduli of the second pass's first-order correction src (X - I) (TRAJ_OZAKI_CORR_MODULI; 0: full)
   int8_t *RK = nullptr, *RU = nullptr, *RX = nullptr;
   uint8_t* RC = nullptr;
-  int *eK = nullptr, *eU = nullptr, *eX = nullptr;
+  int *eK = nullptr, *eU = nullptr, *eX = nullptr, *eU2 = nullptr;
   double* oz_part = nullptr;
   size_t RC_bytes = 0;
   std::vector<cplx> band_host;     // the same on the host: passed by value to the stencil launches
@@ -387,6 +387,7 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     lay.take(h->RC, h->RC_bytes);
     if (h->oz_cqr) lay.take(h->RX, (size_t)oz_residue_bytes(3, s, T, N, N));
     lay.take(h->eU, (size_t)T * L * 4);
+    lay.take(h->eU2, (size_t)T * L * 4);
     lay.take(h->eX, (size_t)T * N * 4);
     lay.take(h->oz_part, (size_t)8 * T * L * 8);
   }
@@ -556,15 +557,23 @@ int prod3(traj_ctx* h, int opA, long long M, long long N, long long K, const dou
 //   dst_c += A W_c   (A = sum_{d<c} dst_d Z_d^dag, L x k0; W_c past row k0 taken as zero)
 //   A (+)= dst_c Z_c^dag  (columns past k0 skipped)
 // with k0 bounding the INT8 launches on the device.
-int struct_chol_apply_oz(traj_ctx* h, const StructChol& s, const cplx* src, cplx* dst) {
+int struct_chol_apply_oz(traj_ctx* h, const StructChol& s, const cplx* src, cplx* dst, const cudaEvent_t* ev = nullptr) {
   const int b = s.b, N = s.N, kc = s.kc, T = s.T, L = h->L, sq = h->oz_s;
   const long long sA = (long long)L * h->ldcap;
   cplx* A = h->Tm;
   const int32_t* k0 = h->lr_kdev;
   const int nblk = (int)ceil_div(N, b);
-  auto prod = [&](int M, int Nn, int K, const int8_t* RA, const int* eA, long long sEA, const int8_t* RB, const int* eB,
-                  long long sEB, cplx* C, long long ldc, long long sC, const cplx* base, int flags,
-                  const int32_t* kdev, const int32_t* ndev) {
+  // the product scratch in two halves: outputs, and the per-block residues of A / dst_c (src's row
+  // residues stay in RU for every block's block-diagonal product)
+  const size_t half = (size_t)oz_residue_bytes(3, sq, T, L, std::max(kc, b));
+  // interleaved (block c's solve right after its factor block) when the scratch holds both halves;
+  // otherwise all block-diagonal products first, then the sequential part with its residues in RU
+  const bool inter = 2 * half + 256 <= h->RC_bytes;
+  uint8_t* RCo = h->RC;
+  int8_t* R2 = inter ? reinterpret_cast<int8_t*>(h->RC + (half + 255) / 256 * 256) : h->RU;
+  auto prod = [&](int M, int Nn, int K, const int8_t* RA, long long lda, const int* eA, const int8_t* RB,
+                  const int* eB, cplx* C, long long ldc, long long sC, const cplx* base, int flags, const int32_t* kdev,
+                  const int32_t* ndev) {
     OzProduct p;
     p.M = M;
     p.N = Nn;
@@ -573,12 +582,13 @@ int struct_chol_apply_oz(traj_ctx* h, const StructChol& s, const cplx* src, cplx
     p.s = sq;
     p.RA = RA;
     p.a_traj = 1;
+    p.lda_override = lda;
     p.eA = eA;
-    p.sEA = sEA;
+    p.sEA = L;
     p.RB = RB;
     p.eB = eB;
-    p.sEB = sEB;
-    p.RC = h->RC;
+    p.sEB = N;
+    p.RC = RCo;
     p.C = C;
     p.ldc = ldc;
     p.sC = sC;
@@ -588,48 +598,33 @@ int struct_chol_apply_oz(traj_ctx* h, const StructChol& s, const cplx* src, cplx
     p.ndev = ndev;
     return oz_product(h->st, p, &h->err);
   };
-  // block-diagonal part: src's row residues once; block c's k-range starts c0 bytes into each row
+  // src's row residues once; block c's k-range starts c0 bytes into each row
   TRY(oz_split_rows(h->st, src, h->ldN, h->sU, L, N, T, 0, sq, h->RU, h->eU, L, &h->err));
+  auto diag = [&](int c) {   // dst_c = src_c X_c
+    const int c0 = c * b, bc = std::min(b, N - c0);
+    if (ev) CK(cudaStreamWaitEvent(h->st, ev[c], 0));   // factor block c done (pipelined)
+    TRY(oz_split_cols(h->st, s.Xb + (long long)c0 * b, b, s.sXb, bc, bc, T, 3, sq, h->RX, h->eX, N, h->oz_part,
+                      &h->err));
+    TRY(prod(L, bc, bc, h->RU + c0, oz_ld(N), h->eU, h->RX, h->eX, dst + c0, h->ldN, h->sU, nullptr, OZ_TRI_B, nullptr,
+             nullptr));
+    return 0;
+  };
+  if (!inter)
+    for (int c = 0; c < nblk; ++c) TRY(diag(c));
   for (int c = 0; c < nblk; ++c) {
     const int c0 = c * b, bc = std::min(b, N - c0);
-    const cplx* Xc = s.Xb + (long long)c0 * b;
-    TRY(oz_split_cols(h->st, Xc, b, s.sXb, bc, bc, T, 3, sq, h->RX, h->eX, N, h->oz_part, &h->err));
-    // A = src's residues at k offset c0: same planes / moduli / trajectory strides, row length oz_ld(N)
-    OzProduct p;
-    p.M = L;
-    p.N = bc;
-    p.K = bc;
-    p.T = T;
-    p.s = sq;
-    p.RA = h->RU + c0;
-    p.a_traj = 1;
-    p.lda_override = oz_ld(N);
-    p.eA = h->eU;
-    p.sEA = L;
-    p.RB = h->RX;
-    p.eB = h->eX;
-    p.sEB = N;
-    p.RC = h->RC;
-    p.C = dst + c0;
-    p.ldc = h->ldN;
-    p.sC = h->sU;
-    p.flags = OZ_TRI_B;
-    TRY(oz_product(h->st, p, &h->err));
-  }
-  // the sequential part
-  for (int c = 0; c < nblk; ++c) {
-    const int c0 = c * b, bc = std::min(b, N - c0);
+    if (inter) TRY(diag(c));
     if (c > 0) {   // dst_c += A W_c: A's rows (k < k0), W_c's columns (rows past k0 zero)
-      TRY(oz_split_rows(h->st, A, h->ldcap, sA, L, kc, T, 0, sq, h->RU, h->eU, L, &h->err, nullptr, k0));
+      TRY(oz_split_rows(h->st, A, h->ldcap, sA, L, kc, T, 0, sq, R2, h->eU2, L, &h->err, nullptr, k0));
       TRY(oz_split_cols(h->st, s.W + c0, s.ldWZ, s.sWZ, kc, bc, T, 3, sq, h->RX, h->eX, N, h->oz_part, &h->err, 0,
                         nullptr, nullptr, k0));
-      TRY(prod(L, bc, kc, h->RU, h->eU, L, h->RX, h->eX, N, dst + c0, h->ldN, h->sU, dst + c0, 0, k0, nullptr));
+      TRY(prod(L, bc, kc, R2, 0, h->eU2, h->RX, h->eX, dst + c0, h->ldN, h->sU, dst + c0, 0, k0, nullptr));
     }
     if (c + 1 < nblk) {   // A (+)= dst_c Z_c^dag: dst_c's rows, Z_c's rows conjugated (rows past k0 zero)
-      TRY(oz_split_rows(h->st, dst + c0, h->ldN, h->sU, L, bc, T, 0, sq, h->RU, h->eU, L, &h->err));
+      TRY(oz_split_rows(h->st, dst + c0, h->ldN, h->sU, L, bc, T, 0, sq, R2, h->eU2, L, &h->err));
       TRY(oz_split_rows(h->st, s.Z + c0, s.ldWZ, s.sWZ, kc, bc, T, 1, sq, h->RX, h->eX, N, &h->err, nullptr, nullptr, 3,
                         k0));
-      TRY(prod(L, kc, bc, h->RU, h->eU, L, h->RX, h->eX, N, A, h->ldcap, sA, c > 0 ? A : nullptr, 0, nullptr, k0));
+      TRY(prod(L, kc, bc, R2, 0, h->eU2, h->RX, h->eX, A, h->ldcap, sA, c > 0 ? A : nullptr, 0, nullptr, k0));
     }
   }
   return 0;
@@ -658,6 +653,20 @@ int structured_pass1(traj_ctx* h, const cplx* src, cplx* dst, int kc) {
   s.sWZ = h->sUS;
   s.chol_scratch = h->s_chol_scratch;
   const bool oz_apply = h->oz_cqr && kc >= h->oz_proj_min;
+  if (oz_apply && h->chol_overlap && h->st_hi && !h->struct_serial) {
+    // the factor chain on the high-priority stream; the modular solve waits per block
+    const int nblk = (int)ceil_div(h->N, h->sb);
+    while ((int)h->sc_ev.size() < nblk) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      h->sc_ev.push_back(e);
+    }
+    CK(cudaEventRecord(h->ev_fork, h->st));
+    CK(cudaStreamWaitEvent(h->st_hi, h->ev_fork, 0));
+    TRY(struct_chol_factor_events(h->st_hi, s, h->US, h->ldN, h->sUS, h->lr_kdev, h->failed_dev, h->sc_ev.data(),
+                                  &h->err));
+    return struct_chol_apply_oz(h, s, src, dst, h->sc_ev.data());
+  }
   if (!oz_apply && h->chol_overlap && h->st_hi && !h->struct_serial) {
     // the factor chain on the high-priority stream, each solve block after its factor block
     const int nblk = (int)ceil_div(h->N, h->sb);
