@@ -44,7 +44,8 @@ struct HostConst {
       for (u128 x = Mp; x > 1; x >>= 1) ++lg;
       beta[s] = lg / 2 - 1;
       // the moduli in pairs (q = 2p, 2p + 1), mu_p = m_2p m_2p+1 < 2^16 (s even); c_p = inv_p / mu_p,
-      // inv_p = (M / mu_p)^-1 mod mu_p; n = round(inv_p 2^37 / mu_p), ch = n 2^-37, cl = c_p - ch
+      // inv_p = (M / mu_p)^-1 mod mu_p; n = round(inv_p 2^36 / mu_p), ch = n 2^-36, cl = c_p - ch (the
+      // representatives r < 2^16 + 768 keep every r ch exact in 53 bits)
       for (int q = 0; 2 * q + 1 < s; ++q) {
         const long long mu = (long long)OZM(2 * q) * OZM(2 * q + 1);
         const long long Mi = (long long)((Mp / (u128)mu) % (u128)mu);
@@ -62,10 +63,10 @@ struct HostConst {
           }
           inv = ((t0 % mu) + mu) % mu;
         }
-        const long long num = inv << 37;
+        const long long num = inv << 36;
         const long long n = (num + mu / 2) / mu;
-        ch[s][q] = (double)n * 0x1p-37;
-        cl[s][q] = (double)(num - n * mu) / (double)mu * 0x1p-37;
+        ch[s][q] = (double)n * 0x1p-36;
+        cl[s][q] = (double)(num - n * mu) / (double)mu * 0x1p-36;
       }
     }
   }
@@ -329,7 +330,7 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const cplx* __restri
 
 // ---- CRT combine.  Moduli are taken in pairs (m_a, m_b) -> one residue mod mu = m_a m_b < 2^16
 // (Garner's step), then X / M = frac(sum_p r_p c_p) over the 8 pairs with c_p = ch_p + cl_p, ch_p a
-// multiple of 2^-37: every r_p ch_p (r_p < 2^16) and the sum of their fractional parts are exact.
+// multiple of 2^-36: every r_p ch_p (r_p < 2^16) and the sum of their fractional parts are exact.
 __host__ __device__ constexpr int modinv(int a, int m) {
   int r = 1;
   for (int x = 1; x < m; ++x)
@@ -337,16 +338,17 @@ __host__ __device__ constexpr int modinv(int a, int m) {
   return r;
 }
 
-// the real and imaginary residues of the 3M combination mod m from the product residues (bytes < m)
+// representatives of the real and imaginary residues of the 3M combination from the product residues
+// (bytes < m), left unreduced in [0, 3m): the Garner step below takes any non-negative representative
 template <int Q>
 __device__ __forceinline__ void reim(uint32_t a1, uint32_t a2, uint32_t a3, int neg2, uint32_t& re, uint32_t& im) {
   constexpr uint32_t m = OZM(Q);
   if (neg2) {   // Re = P1 + P2', Im = P3 - P1 + P2'
-    re = red1(a1 + a2, m);
-    im = red1(red1(a3 + m - a1 + a2, m), m);
+    re = a1 + a2;
+    im = a3 + m - a1 + a2;
   } else {      // Re = P1 - P2, Im = P3 - P1 - P2
-    re = red1(a1 + m - a2, m);
-    im = red1(red1(a3 + 2 * m - a1 - a2, m), m);
+    re = a1 + m - a2;
+    im = a3 + 2 * m - a1 - a2;
   }
 }
 
@@ -394,9 +396,13 @@ struct CrtPair {
         uint32_t rea, ima, reb, imb;
         reim<QA>(A1[k], A2[k], A3[k], neg2, rea, ima);
         reim<QB>(B1[k], B2[k], B3[k], neg2, reb, imb);
-        // Garner: r = r_a + m_a ((r_b - r_a) m_a^-1 mod m_b) < m_a m_b
-        const uint32_t rr = rea + ma * ((((reb + 2 * mb - rea) % mb) * inv) % mb);
-        const uint32_t ri = ima + ma * ((((imb + 2 * mb - ima) % mb) * inv) % mb);
+        // Garner: r = r_a + m_a ((r_b - r_a) m_a^-1 mod m_b) in [0, mu + 2 m_a) (r_a, r_b in [0, 3m)
+        // unreduced; one modulo per component), then one step to the canonical residue in [0, mu): a zero
+        // product must come out as exactly 0 (a zero row has exponent 0, so any CRT residual of a
+        // non-canonical representative would be amplified)
+        constexpr uint32_t mu = ma * mb;
+        const uint32_t rr = red1(rea + ma * (((reb + 4 * mb - rea) * inv) % mb), mu);
+        const uint32_t ri = red1(ima + ma * (((imb + 4 * mb - ima) * inv) % mb), mu);
         double tr = (double)rr * ch, ti = (double)ri * ch;
         tr -= rint(tr);
         ti -= rint(ti);
