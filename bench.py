@@ -82,6 +82,7 @@ def parse():
                         "projective_events (NEXT-4)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-fp64-path", action="store_true", help="skip the TRAJ_OZAKI=0 (DMMA) comparison line")
     p.add_argument("--no-observables", action="store_true")
     p.add_argument("--secondary", default="c5",
                    help="also time this config (the metric is quoted at 1d L=16384 and 2d 160x160); 'none' skips")
@@ -334,6 +335,14 @@ def run_ours(args):
     # the workspace block stays in torch's caching allocator, so the e2e handle below takes it from
     # there as a user's next handle would (a fresh 29 GB cudaMalloc after a free costs ~0.4 s)
 
+    # ---- the same step on the FP64 tensor pipe (TRAJ_OZAKI=0: the DMMA kernels), for the metric's
+    # "FP64 tensor TFLOP/s vs peak" read literally: executed DMMA flops of its dominant phase over that
+    # phase's device time against the measured 37.1 TF/s DMMA peak
+    fp64_path = None
+    if oz[0] and not shard and world == 1 and not args.no_fp64_path:
+        torch.cuda.empty_cache()
+        fp64_path = run_fp64_path(args, w, tpg, P)
+
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -366,6 +375,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "sampled_observables_ms": obs,
         "secondary": secondary,
+        "fp64_tensor_path": fp64_path,
         "clocks": clk,
         "e2e": e2e,
     }
@@ -705,6 +715,47 @@ def run_secondary(args, world, rank, P, steps=2, warmup=2):
                                      "flops_counted": "executed DMMA flops (6mnk for 3M, x 7/8 with one Strassen "
                                                       "level)"}
     return out
+
+
+def run_fp64_path(args, w, tpg, P, steps=3, warmup=2):
+    """The step with every contraction on the DMMA (FP64 tensor) kernels, timed the same way."""
+    import torch
+    old = os.environ.get("TRAJ_OZAKI")
+    os.environ["TRAJ_OZAKI"] = "0"
+    try:
+        tr = open_handle(P, args, w, "traj", 0, 1, tpg)
+    finally:
+        if old is None:
+            os.environ.pop("TRAJ_OZAKI", None)
+        else:
+            os.environ["TRAJ_OZAKI"] = old
+    assert not any(tr.ozaki_info()[:2])
+    tr.step(warmup)
+    torch.cuda.synchronize()
+    tr.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(tr.stream)
+    tr.step(steps)
+    e1.record(tr.stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    ph = tr.phase_times()
+    tr.close()
+    del tr
+    torch.cuda.empty_cache()
+    prop = ph["propagate"][0] / steps
+    slv = strassen_levels(w, 1, tpg)
+    a = 0.75 * (7 / 8) ** slv   # planar 3M (6mnk) x 7/8 per Strassen level: the DMMA flops issued
+    eq8 = 8.0 * w.L * w.L * w.N * tpg / (prop / 1e3) / 1e12
+    return {"config": "the same workload with TRAJ_OZAKI=0 (planar 3M + Strassen DMMA kernels)",
+            "ms_per_step": ms, "value": tpg / (ms / 1e3), "unit": "trajectory-steps/s", "steps": steps,
+            "warmup": warmup, "phases_ms_per_step": {k: v[0] / steps for k, v in ph.items() if v[0] > 0},
+            "roofline_propagate": {"bound": "tensor", "achieved": eq8 * a, "peak": FP64_PEAK_TFLOPS,
+                                   "unit": "TFLOP/s (FP64 DMMA, executed)", "frac": eq8 * a / FP64_PEAK_TFLOPS,
+                                   "kernel_ms": prop, "achieved_8mnk_equiv": eq8,
+                                   "kernel": f"dgemm_dmma_kernel: planar 3M, {slv} Strassen level(s), split / "
+                                             "recombination passes included",
+                                   "peak_source": FP64_PEAK_SOURCE}}
 
 
 def run_e2e(args, w, tpg, mode, rank, world, P):

@@ -3,7 +3,7 @@
 # forms), appended to gpurun_out/bench_configs.jsonl.  Usage (on the GPU box): bash tools/bench_configs.sh
 out=gpurun_out/${BENCH_CONFIGS_OUT:-bench_configs.jsonl}
 : > $out
-common="--no-cpu-baseline --no-e2e --no-observables --secondary none"
+common="--no-cpu-baseline --no-e2e --no-observables --secondary none --no-fp64-path"
 python bench.py --config c1 --steps 200 --warmup 10 $common >> $out 2>/dev/null
 for c in c2 c4; do
   python bench.py --config $c --steps 10 --warmup 3 $common >> $out 2>/dev/null
