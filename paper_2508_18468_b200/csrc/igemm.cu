@@ -575,6 +575,219 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ITHREADS, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
+// ---------------------------------------------------------------------------------------------
+// B-multicast variant: a cluster of two CTAs on adjacent m-blocks of the same n-block; each CTA loads
+// its own A tile and half of the shared B tile, multicast into both CTAs' shared memory (each CTA's
+// L2 reads per stage 32 KB instead of 48 KB).  MMAs, TMEM and the epilogue stay per CTA (cta_group::1);
+// a stage is refilled only when both CTAs' MMAs have consumed it (commits multicast to both empties).
+__device__ __forceinline__ void tma_load_3d_mc(void* smem_dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                               uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, "
+      "%3, %4}], [%5], %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar) {   // arrives at this offset in both CTAs
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ITHREADS, 1)
+    igemm_i8_mc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const KArgs a,
+                       const int tiles_m2, const long long ptiles) {
+  if (a.gate && *a.gate == 0) return;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  uint8_t* base = smem_raw + (base_u32 - smem_u32(smem_raw));
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + ISTAGES * ISTAGE_BYTES);
+  uint64_t* empty = full + ISTAGES;
+  uint64_t* tfull = empty + ISTAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = (int)cluster_rank();
+  const long long pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ISTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 2);   // both CTAs' MMAs
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    fence_mbar_init();
+    prefetch_tmap(&ta);
+    prefetch_tmap(&tb);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // this CTA's tile of the pair tile: m-block 2 mb2 + rank (the pair is live when either tile is)
+  auto my_tile = [&](long long t, bool& live, bool& mine) {
+    Tile tl = pair_tile_of(a, t, tiles_m2);
+    Tile t0 = tl, t1 = tl;
+    t0.mb = 2 * tl.mb;
+    t1.mb = 2 * tl.mb + 1;
+    const bool l0 = tile_live(a, t0), l1 = t1.mb < a.tiles_m && tile_live(a, t1);
+    live = l0 || l1;
+    mine = rank ? l1 : l0;
+    return rank ? t1 : t0;
+  };
+  if (warp == 0) {
+    if (lane == 0) {   // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (long long t = pair; t < ptiles; t += npairs) {
+        bool live, mine;
+        const Tile tl = my_tile(t, live, mine);
+        if (!live) continue;
+        int kb0;
+        const int nk = tile_kblocks(a, tl, &kb0);
+        int za, zb, q;
+        zmap(a, tl.z, za, zb, q);
+        for (int kb = kb0; kb < kb0 + nk; ++kb) {
+          mbar_wait_cluster(&empty[stage], phase ^ 1);
+          uint8_t* sa = base + stage * ISTAGE_BYTES;
+          mbar_arrive_expect_tx(&full[stage], ISTAGE_BYTES);
+          tma_load_3d(sa, &ta, kb * IBK, tl.mb * IBM, za, &full[stage]);
+          tma_load_3d_mc(sa + IA_BYTES + rank * (IB_BYTES / 2), &tb, kb * IBK, tl.nb * IBN + rank * (IBN / 2), zb,
+                         &full[stage], (uint16_t)3);
+          if (++stage == ISTAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {   // ---------------- MMA issuer
+    constexpr uint32_t idesc = idesc_i8(IBM, IBN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (long long t = pair; t < ptiles; t += npairs) {
+      bool live, mine;
+      const Tile tl = my_tile(t, live, mine);
+      if (!live) continue;
+      const int nk = tile_kblocks(a, tl);
+      const int buf = it & 1;
+      const uint32_t use = (uint32_t)(it >> 1);
+      mbar_wait(&tempty[buf], (use & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t dt = tmem + buf * IBN;
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sa = base_u32 + stage * ISTAGE_BYTES, sb = sa + IA_BYTES;
+          const uint64_t da = sw128_desc(sa), db = sw128_desc(sb);
+#pragma unroll
+          for (int k = 0; k < IBK / 32; ++k) mma_i8(dt, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+          mma_commit_mc(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == ISTAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (lane == 0) mma_commit(&tfull[buf]);
+      __syncwarp();
+      ++it;
+    }
+  } else {   // ---------------- epilogue: warps 2..5
+    const int q = warp & 3;
+    int it = 0;
+    for (long long t = pair; t < ptiles; t += npairs) {
+      bool live, mine;
+      const Tile tl = my_tile(t, live, mine);
+      if (!live) continue;
+      const int buf = it & 1;
+      const uint32_t use = (uint32_t)(it >> 1);
+      mbar_wait(&tfull[buf], use & 1);
+      tc_fence_after();
+      const int row = tl.mb * IBM + q * 32 + lane;
+      const bool row_ok = mine && row < a.M;
+      const bool kzero = tile_kblocks(a, tl) == 0;
+      const uint32_t taddr = tmem + buf * IBN + ((uint32_t)(q * 32) << 16);
+      int mod = 0;
+      double inv = 0.0;
+      if (a.out == IG_OUT_MOD) {
+        int za, zb, qq;
+        zmap(a, tl.z, za, zb, qq);
+        mod = a.moduli[qq];
+        inv = 1.0 / (double)mod;
+      }
+#pragma unroll 1
+      for (int c = 0; c < IBN / 32; ++c) {
+        uint32_t v[32];
+        __syncwarp();
+        tmem_ld32(taddr + c * 32, v);
+        if (kzero) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0;
+        }
+        const int col = tl.nb * IBN + c * 32;
+        if (!row_ok || col >= a.N) {
+        } else if (a.out == IG_OUT_I32) {
+          int* p = reinterpret_cast<int*>(a.C) + ((long long)tl.z * a.ksplit + tl.kc) * a.strideC +
+                   (long long)row * a.ldc + col;
+          if (col + 32 <= a.N) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              reinterpret_cast<int4*>(p)[j] = make_int4((int)v[4 * j], (int)v[4 * j + 1], (int)v[4 * j + 2], (int)v[4 * j + 3]);
+          } else {
+            for (int j = 0; col + j < a.N; ++j) p[j] = (int)v[j];
+          }
+        } else {
+          uint32_t w[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            uint32_t packed = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const int x = (int)v[4 * j + b];
+              int r = x - mod * (int)floor((double)x * inv);
+              r += (r < 0) ? mod : 0;
+              r -= (r >= mod) ? mod : 0;
+              packed |= (uint32_t)r << (8 * b);
+            }
+            w[j] = packed;
+          }
+          uint8_t* p = reinterpret_cast<uint8_t*>(a.C) + ((long long)tl.z * a.ksplit + tl.kc) * a.strideC +
+                       (long long)row * a.ldc + col;
+          if (col + 32 <= a.N) {
+            reinterpret_cast<uint4*>(p)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            reinterpret_cast<uint4*>(p)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          } else {
+            for (int j = 0; col + j < a.N; ++j) p[j] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+      ++it;
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
 typedef CUresult (*PFN_encode_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -646,9 +859,15 @@ int igemm(cudaStream_t st, const IgemmArgs& g, std::string* err) {
     pair_env = (v && v[0] == '1') ? 1 : 0;
   }
   const bool use_pair = pair_env && g.M >= 256 && num_sms() >= 2;
+  static int mc_env = -1;
+  if (mc_env < 0) {
+    const char* v = getenv("TRAJ_IGEMM_MC");
+    mc_env = (v && v[0] == '1') ? 1 : 0;
+  }
+  const bool use_mc = !use_pair && mc_env && g.M >= 256 && num_sms() >= 2;
   CUtensorMap ma, mb;
   if (!map_i8(enc, &ma, g.A, g.K, g.M, g.lda, ab ? na : 1, g.strideA, IBM) ||
-      !map_i8(enc, &mb, g.B, g.K, g.N, g.ldb, bb ? nb : 1, g.strideB, use_pair ? 128 : IBN)) {
+      !map_i8(enc, &mb, g.B, g.K, g.N, g.ldb, bb ? nb : 1, g.strideB, (use_pair || use_mc) ? 128 : IBN)) {
     if (err) *err = "igemm: tensor map";
     return 4;
   }
@@ -707,6 +926,23 @@ int igemm(cudaStream_t st, const IgemmArgs& g, std::string* err) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
       if (err) *err = std::string("igemm (pair): ") + cudaGetErrorString(e);
+      return 4;
+    }
+    return 0;
+  }
+  if (use_mc) {
+    const int tiles_m2 = (int)ceil_div(a.tiles_m, 2);
+    const long long ptiles = g.batch * a.ksplit * (long long)tiles_m2 * a.tiles_n;
+    if (ensure_smem((const void*)igemm_i8_mc_kernel, ISMEM) != cudaSuccess) {
+      if (err) *err = "igemm: shared memory attribute (multicast)";
+      return 4;
+    }
+    const long long npairs = std::min<long long>(ptiles, num_sms() / 2);
+    igemm_i8_mc_kernel<<<(unsigned)(2 * npairs), ITHREADS, ISMEM, st>>>(ma, mb, a, tiles_m2, ptiles);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      if (err) *err = std::string("igemm (multicast): ") + cudaGetErrorString(e);
       return 4;
     }
     return 0;
