@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "zgemm.h"
 #include "cholinv.h"
+#include "ozaki.h"
 #include "comm_plan.h"
 
 namespace traj {
@@ -268,7 +269,99 @@ struct Ctx {
   DevBounds db;            // gate: every launch of the factorisation runs only if *gate != 0
   long long n_top;
   int leaf;                // 1: elimination (default), 2: register-blocked (TRAJ_CHOL_LEAF=regs)
+  const CholOzaki* oz;     // the large levels' products on the INT8 modular path (may be null)
 };
+
+// the four products of one recursion level as exact modular products (see rec below for their roles)
+int rec_level_ozaki(Ctx& c, long long n, cplx* B_blk, cplx* L_blk, cplx* C_blk, cplx* XA, cplx* XB, cplx* XC,
+                    bool before_c) {
+  const CholOzaki& z = *c.oz;
+  const long long h = split(n), r = n - h;
+  const int T = (int)c.batch, sq = z.s;
+  const int32_t* gate = c.db.gate;
+  auto prod = [&](int M, int N, int K, int a_planes, int pa2, int b_planes, int pb2, const int8_t* RB, int flags,
+                  cplx* C, long long ldc, long long sC, const cplx* base) {
+    OzProduct p;
+    p.M = M;
+    p.N = N;
+    p.K = K;
+    p.T = T;
+    p.s = sq;
+    p.RA = z.RA;
+    p.a_traj = 1;
+    p.a_planes = a_planes;
+    p.pa[2] = pa2;
+    p.eA = z.eA;
+    p.sEA = z.sE;
+    p.RB = RB;
+    p.b_planes = b_planes;
+    p.pb[2] = pb2;
+    p.eB = z.eB;
+    p.sEB = z.sE;
+    p.RC = z.RC;
+    p.C = C;
+    p.ldc = ldc;
+    p.sC = sC;
+    p.base = base;
+    p.flags = flags;
+    p.gate = gate;
+    return oz_product(c.st, p, c.err);
+  };
+  int s;
+  if (before_c) {
+    // L = B^dag X_A (r x h): B's columns conjugated (planes re, im, re - im; P2 negated), X_A's columns
+    if ((s = oz_split_cols(c.st, B_blk, c.ldg, c.sG, (int)h, (int)r, T, 4, sq, z.RA, z.eA, z.sE, z.part, c.err, 0,
+                           gate)))
+      return s;
+    if ((s = oz_split_cols(c.st, XA, c.ldx, c.sX, (int)h, (int)h, T, 3, sq, z.RB, z.eB, z.sE, z.part, c.err, 0, gate)))
+      return s;
+    if ((s = prod((int)r, (int)h, (int)h, 4, 3, 3, 2, z.RB, OZ_NEG_P2 | OZ_TRI_B, L_blk, c.ldg, c.sG, nullptr)))
+      return s;
+    // C -= L L^dag (upper): one 4-plane row split of L serves both sides
+    if ((s = oz_split_rows(c.st, L_blk, c.ldg, c.sG, (int)r, (int)h, T, 0, sq, z.RA, z.eA, z.sE, c.err, gate, nullptr,
+                           4)))
+      return s;
+    {
+      OzProduct p;
+      p.M = (int)r;
+      p.N = (int)r;
+      p.K = (int)h;
+      p.T = T;
+      p.s = sq;
+      p.RA = z.RA;
+      p.a_traj = 1;
+      p.a_planes = 4;
+      p.eA = z.eA;
+      p.sEA = z.sE;
+      p.RB = z.RA;
+      p.b_planes = 4;
+      p.pb[2] = 3;
+      p.eB = z.eA;
+      p.sEB = z.sE;
+      p.RC = z.RC;
+      p.C = C_blk;
+      p.ldc = c.ldg;
+      p.sC = c.sG;
+      p.base = C_blk;
+      p.flags = OZ_NEG_P2 | OZ_UPPER | OZ_NEGATE;
+      p.gate = gate;
+      if ((s = oz_product(c.st, p, c.err))) return s;
+    }
+    return 0;
+  }
+  // tmp = L^dag X_C (h x r): L's columns conjugated, X_C's columns
+  if ((s = oz_split_cols(c.st, L_blk, c.ldg, c.sG, (int)r, (int)h, T, 4, sq, z.RA, z.eA, z.sE, z.part, c.err, 0, gate)))
+    return s;
+  if ((s = oz_split_cols(c.st, XC, c.ldx, c.sX, (int)r, (int)r, T, 3, sq, z.RB, z.eB, z.sE, z.part, c.err, 0, gate)))
+    return s;
+  if ((s = prod((int)h, (int)r, (int)r, 4, 3, 3, 2, z.RB, OZ_NEG_P2 | OZ_TRI_B, c.tmp, c.ldt, c.sT, nullptr))) return s;
+  // X_B = -X_A tmp: X_A's rows (its zero lower triangle included), tmp's columns
+  if ((s = oz_split_rows(c.st, XA, c.ldx, c.sX, (int)h, (int)h, T, 0, sq, z.RA, z.eA, z.sE, c.err, gate)))
+    return s;
+  if ((s = oz_split_cols(c.st, c.tmp, c.ldt, c.sT, (int)h, (int)r, T, 3, sq, z.RB, z.eB, z.sE, z.part, c.err, 0, gate)))
+    return s;
+  return prod((int)h, (int)r, (int)h, 3, 2, 3, 2, z.RB, OZ_NEGATE, XB, c.ldx, c.sX, nullptr);
+}
 
 // row slice boundaries of M rows over P ranks (comm_plan.h row_slices: the schedule the ranks share)
 std::vector<long long> slices(long long M, int P, bool tri) { return row_slices(M, P, tri); }
@@ -338,6 +431,11 @@ int rec(Ctx& c, long long o, long long n) {
       return s;
     return 0;
   }
+  if (c.oz && n >= c.oz->min_n) {   // the same four products on the INT8 modular path
+    if ((s = rec_level_ozaki(c, n, B_blk, L_blk, C_blk, XA, XB, XC, true))) return s;
+    if ((s = rec(c, o + h, r))) return s;
+    return rec_level_ozaki(c, n, B_blk, L_blk, C_blk, XA, XB, XC, false);
+  }
   // R_B^dag = B^dag X_A : (r x h) = op_C(B: h x r) * X_A (h x h, upper)
   if ((s = zgemm(c.st, 1, 0, r, h, h, 1.0, 0.0, B_blk, c.ldg, c.sG, XA, c.ldx, c.sX, 0.0, L_blk, c.ldg, c.sG, c.batch,
                  TRAJ_TRI_B_UPPER_F, c.err, 0, 0, &c.db)))
@@ -368,7 +466,7 @@ size_t chol_scratch_bytes(long long n, long long batch) {
 
 int chol_inverse(cudaStream_t st, long long n, cplx* G, long long ldg, long long sG, cplx* X, long long ldx,
                  long long sX, long long batch, void* scratch, int32_t* failed, std::string* err,
-                 const CholDist* dist, const CholHook* hook, const int32_t* gate) {
+                 const CholDist* dist, const CholHook* hook, const int32_t* gate, const CholOzaki* oz) {
   if (n <= 0 || batch <= 0) return 0;
   if (batch > 65535) {
     if (err) *err = "chol_inverse: batch too large";
@@ -390,6 +488,7 @@ int chol_inverse(cudaStream_t st, long long n, cplx* G, long long ldg, long long
   c.err = err;
   c.dist = dist;
   c.hook = hook;
+  c.oz = (dist && dist->P > 1) ? nullptr : oz;
   c.db.gate = gate;
   c.n_top = n;
   {
@@ -430,7 +529,7 @@ __global__ void fallback_decide_kernel(const unsigned long long* dev, int T, dou
 
 int CholFallbackGraph::build(long long n, cplx* G, long long ldg, long long sG, cplx* X, long long ldx, long long sX,
                              long long batch, void* scratch, int32_t* failed, const unsigned long long* dev, double thr,
-                             unsigned long long* fallbacks, std::string* err) {
+                             unsigned long long* fallbacks, std::string* err, const CholOzaki* oz) {
   auto bad = [&](const char* what, cudaError_t e) {
     if (err) *err = std::string("fallback graph: ") + what + ": " + cudaGetErrorString(e);
     destroy();
@@ -464,7 +563,7 @@ int CholFallbackGraph::build(long long n, cplx* G, long long ldg, long long sG, 
     return bad("capture", e);
   }
   std::string cerr;
-  const int r = chol_inverse(cs, n, G, ldg, sG, X, ldx, sX, batch, scratch, failed, &cerr);
+  const int r = chol_inverse(cs, n, G, ldg, sG, X, ldx, sX, batch, scratch, failed, &cerr, nullptr, nullptr, nullptr, oz);
   cudaGraph_t captured = body;
   e = cudaStreamEndCapture(cs, &captured);
   cudaStreamDestroy(cs);

@@ -31,6 +31,22 @@ struct CholHook {
   void* user = nullptr;
 };
 
+// Optional workspace that runs the four products of every recursion level with n >= min_n as exact
+// modular products on the INT8 tensor cores (ozaki.h): RA >= 4 s batch n^2/2 (rounded), RB >= 3 s batch
+// n^2/2, RC >= 3 s batch n^2/2 bytes (upper bounds for the top level), eA / eB >= batch n ints each (row
+// stride n), part >= 8 batch n doubles.
+struct CholOzaki {
+  int s = 16;
+  long long min_n = 4096;
+  int8_t* RA = nullptr;
+  int8_t* RB = nullptr;
+  uint8_t* RC = nullptr;
+  int* eA = nullptr;
+  int* eB = nullptr;
+  long long sE = 0;        // exponent stride per batch entry (>= n)
+  double* part = nullptr;
+};
+
 // G_b = R^dag R (upper triangle of G_b read; strict lower triangle used as scratch),
 // X_b = R^-1 (upper; strict lower set to zero).  failed[b] = 1 on a non-positive or
 // non-finite pivot.  gate (device, may be null): every kernel of the factorisation does nothing
@@ -38,7 +54,7 @@ struct CholHook {
 // With a gate X is not touched when gated off, and must already be zero below its diagonal.
 int chol_inverse(cudaStream_t st, long long n, cplx* G, long long ldg, long long sG, cplx* X, long long ldx,
                  long long sX, long long batch, void* scratch, int32_t* failed, std::string* err,
-                 const CholDist* dist = nullptr, const CholHook* hook = nullptr, const int32_t* gate = nullptr);
+                 const CholDist* dist = nullptr, const CholHook* hook = nullptr, const int32_t* gate = nullptr, const CholOzaki* oz = nullptr);
 
 // CholeskyQR2's second-pass fallback as one CUDA graph: a decide node (any trajectory's max|G2 - I|,
 // the bit pattern in dev[t], above thr) sets the condition of an IF node whose body is the captured
@@ -50,7 +66,7 @@ struct CholFallbackGraph {
   cudaGraphExec_t exec = nullptr;
   int build(long long n, cplx* G, long long ldg, long long sG, cplx* X, long long ldx, long long sX, long long batch,
             void* scratch, int32_t* failed, const unsigned long long* dev, double thr, unsigned long long* fallbacks,
-            std::string* err);
+            std::string* err, const CholOzaki* oz = nullptr);
   int launch(cudaStream_t st, std::string* err);
   void destroy();
 };

@@ -78,6 +78,7 @@ struct traj_ctx {
   int *eK = nullptr, *eU = nullptr, *eX = nullptr, *eU2 = nullptr;
   double* oz_part = nullptr;
   size_t RC_bytes = 0;
+  CholOzaki coz;                   // chol_inverse's large levels on the modular path (RU / RX / RC as scratch)
   std::vector<cplx> band_host;     // the same on the host: passed by value to the stencil launches
   cplx* Wrk = nullptr;             // RK4 QSD scratch, shaped like U
   // event-driven PM (NEXT-4)
@@ -792,7 +793,7 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
           std::string e2;
           h->fbg_state = (fg && fg[0] == '0') || h->fbg.build(h->N, h->G, h->ldN, h->sG, h->X, h->ldN, h->sG, h->T,
                                                                h->chol_scratch, h->failed_dev, h->gdev, thr,
-                                                               h->fb_dev, &e2) ? -1 : 1;
+                                                               h->fb_dev, &e2, h->oz_cqr ? &h->coz : nullptr) ? -1 : 1;
         }
         if (h->fbg_state == 1) {
           // the modular TRMM below keys its full-precision product on the same decision (gate)
@@ -801,7 +802,7 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
         } else {   // the same decision, every kernel of the factorisation gated on it
           TRY(cqr2_decide(h->st, h->gdev, h->T, thr, h->gate, h->fb_dev, &h->err));
           TRY(chol_inverse(h->st, h->N, h->G, h->ldN, h->sG, h->X, h->ldN, h->sG, h->T, h->chol_scratch,
-                           h->failed_dev, &h->err, nullptr, nullptr, h->gate));
+                           h->failed_dev, &h->err, nullptr, nullptr, h->gate, h->oz_cqr ? &h->coz : nullptr));
         }
       }
       if (full && h->chol_overlap && h->st_hi && h->N > 64 && !h->oz_cqr) {
@@ -875,7 +876,7 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
       }
       if (full) {
         TRY(chol_inverse(h->st, h->N, h->G, h->ldN, h->sG, h->X, h->ldN, h->sG, h->T, h->chol_scratch,
-                         h->failed_dev, &h->err));
+                         h->failed_dev, &h->err, nullptr, nullptr, nullptr, h->oz_cqr ? &h->coz : nullptr));
       }
     }
     {
@@ -1796,6 +1797,7 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
   }
   h->lwork = lw;
   if (is_sharded(cfg)) {
+    // (row-sharded: chol_inverse's levels stay on DMMA)
     h->sh = new ShardedCtx();
     {
       int Wx = 0, Wy = 0;
@@ -1820,6 +1822,18 @@ int traj_init(const traj_config* cfg, traj_handle* out) {
     h->sh->prof = &h->prof;
   } else {
     carve(h, cfg, reinterpret_cast<char*>(cfg->workspace), lw);
+    if (h->oz_cqr) {   // chol_inverse's levels of n >= TRAJ_CHOL_OZAKI_MIN (default 4096) on the modular path
+      const char* cm = getenv("TRAJ_CHOL_OZAKI_MIN");
+      h->coz.s = h->oz_s;
+      h->coz.min_n = cm ? atoll(cm) : 4096;
+      h->coz.RA = h->RU;
+      h->coz.RB = h->RX;
+      h->coz.RC = h->RC;
+      h->coz.eA = h->eU;
+      h->coz.eB = h->eX;
+      h->coz.sE = h->N;
+      h->coz.part = h->oz_part;
+    }
   }
   h->last_nS.assign(h->T, 0);
   h->last_n1.assign(h->T, 0);

@@ -253,3 +253,26 @@ def test_modular_step_matches_dmma_step(T, monkeypatch):
             assert a.last_clicks(t) == b.last_clicks(t)
     for t in range(2):
         assert np.abs(a.correlation(t).cpu().numpy() - b.correlation(t).cpu().numpy()).max() < 1e-12
+
+
+def test_modular_cholesky_levels_match_oracle(T, monkeypatch):
+    """chol_inverse's large recursion levels on the modular path (threshold lowered to 128): the dense
+    CholeskyQR passes of a homodyne trajectory in lockstep with the oracle, and the ill-conditioned
+    second-pass fallback (conditional graph) at full precision."""
+    import torch
+    import paper_2508_18468_b200 as P
+    from oracle import gaussian
+    from test_gpu_parity import lockstep
+    monkeypatch.setenv("TRAJ_PLANAR_MIN_N", "64")
+    monkeypatch.setenv("TRAJ_CHOL_OZAKI_MIN", "128")
+    lockstep(P, 600, 1, "homodyne", [0.3, 2.0], 20, 5, [np.arange(300), np.arange(41, 377)], seed=13)
+    L, N = 600, 300
+    U = workloads_random(L, N, 4)
+    U[:, 7] = U[:, 3] + 1e-5 * U[:, 7]
+    c = _oz_on(P, L, 1, "homodyne", [0.0])
+    c.set_state(0, torch.from_numpy(U).cuda())
+    c.orthonormalize()
+    assert c.cqr2_fallbacks() == 1
+    Ug = c.get_state(0).cpu().numpy()
+    assert np.abs(Ug.conj().T @ Ug - np.eye(N)).max() < 1e-12
+    assert np.abs(c.correlation(0).cpu().numpy() - gaussian.correlation(gaussian.orthonormalize(U))).max() < 1e-9
