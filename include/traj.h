@@ -338,6 +338,12 @@ int traj_igemm(void* stream, int64_t M, int64_t N, int64_t K, const void* A, int
 int traj_zgemm_ozaki(void* stream, int opA, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                      const void* B, int64_t ldb, void* C, int64_t ldc, int nmod, int flags);
 
+/* The host-side constants of the modular scheme for nmod moduli (no device needed; for tests):
+ * moduli[nmod] (pairwise coprime, <= 256), *beta (operand bits: every row / column is scaled below
+ * 2^beta), ch[nmod/2], cl[nmod/2] (the CRT weights of the moduli pairs: X / M = frac(sum_p r_p (ch_p +
+ * cl_p)), ch_p a multiple of 2^-36), *M (prod m as a double).  TRAJ_EINVAL for an unsupported nmod. */
+int traj_ozaki_constants(int nmod, int32_t* moduli, int32_t* beta, double* ch, double* cl, double* M);
+
 /* traj_chol_inverse: for each b, G_b (n x n Hermitian positive definite; only the
  * upper triangle is read) = R^dag R with R upper triangular; writes X_b = R^-1
  * (upper triangle; the strict lower triangle is set to zero).  G_b's strict lower

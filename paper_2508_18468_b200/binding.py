@@ -99,6 +99,8 @@ _SIGS = {
                                   ctypes.c_int, ctypes.c_int]),
     "traj_zgemm_ozaki": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64, ctypes.c_int,
                                         ctypes.c_int]),
+    "traj_ozaki_constants": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                            ctypes.POINTER(_D), ctypes.POINTER(_D), ctypes.POINTER(_D)]),
     "traj_shard_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                        ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "traj_nccl_unique_id": (ctypes.c_int, [_P]),

@@ -546,6 +546,19 @@ int launched(const char* what, std::string* err) {
 }  // namespace
 
 int oz_supported(int s) { return s >= 4 && s <= 16 && s % 2 == 0; }
+
+int oz_constants(int s, int* moduli, int* beta, double* ch, double* cl, double* M) {
+  if (!oz_supported(s)) return 1;
+  const HostConst& h = host_const();
+  for (int q = 0; q < s; ++q) moduli[q] = OZM(q);
+  *beta = h.beta[s];
+  for (int p = 0; p < s / 2; ++p) {
+    ch[p] = h.ch[s][p];
+    cl[p] = h.cl[s][p];
+  }
+  *M = h.M[s];
+  return 0;
+}
 int oz_beta(int s) { return oz_supported(s) ? host_const().beta[s] : 0; }
 
 int oz_split_rows(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T, int conj,

@@ -26,6 +26,8 @@ constexpr int OZ_MAXS = 16;
 // the bits per operand side for s moduli (floor(log2(prod m_q) / 2) - 1); 0 if s is not supported
 int oz_beta(int s);
 int oz_supported(int s);   // s in {4, 6, 8, 10, 12, 14, 16}
+// the host constants of s moduli (for tests): the moduli, beta, the pair CRT weights ch / cl (s / 2 each), M
+int oz_constants(int s, int* moduli, int* beta, double* ch, double* cl, double* M);
 
 // Residue layout: R [plane][q][t][rows][ldr] int8 (ldr = round_up(K, 16)), plane stride s*T*rows*ldr.
 inline long long oz_ld(long long K) { return round_up(K, 16); }

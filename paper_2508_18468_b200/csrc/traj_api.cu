@@ -2377,6 +2377,12 @@ int traj_zgemm_ozaki(void* stream, int opA, int64_t M, int64_t N, int64_t K, con
   return r ? fail(nullptr, r == 1 ? TRAJ_EINVAL : TRAJ_ECUDA, e) : 0;
 }
 
+int traj_ozaki_constants(int nmod, int32_t* moduli, int32_t* beta, double* ch, double* cl, double* M) {
+  if (!moduli || !beta || !ch || !cl || !M || oz_constants(nmod, moduli, beta, ch, cl, M))
+    return fail(nullptr, TRAJ_EINVAL, "traj_ozaki_constants: nmod must be 4..16 even");
+  return 0;
+}
+
 int traj_set_zgemm_algorithm(int algo) {
   if (algo != 0 && algo != 1) return fail(nullptr, TRAJ_EINVAL, "algorithm must be 0 (4M) or 1 (3M)");
   set_zgemm_algorithm(algo);
