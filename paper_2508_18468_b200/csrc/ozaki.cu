@@ -117,8 +117,12 @@ int ensure_device_constants(const int** moduli_dev, std::string* err) {
   return 0;
 }
 
-// exponent e with nu 2^e < 2^beta (nu = the row's / column's 2-norm of |re| + |im|); 0 for a zero row
+// exponent e with nu 2^e < 2^beta (nu = the row's / column's 2-norm of |re| + |im|); 0 for a zero row;
+// OZ_NONFINITE for a row holding a NaN or an infinity: its residues are written as zeros and the combine
+// returns NaN for every output it meets (as an FP64 product would), so a failed trajectory stays failed
+constexpr int OZ_NONFINITE = 1 << 20;
 __device__ __forceinline__ int scale_exp(double nu2, int beta) {
+  if (!(nu2 <= 1.7e308)) return OZ_NONFINITE;   // NaN or infinite
   if (!(nu2 > 0.0)) return 0;
   return beta - ilogb(sqrt(nu2)) - 1;
 }
@@ -127,6 +131,7 @@ __device__ __forceinline__ int scale_exp(double nu2, int beta) {
 // directly unless it leaves the normal range
 __device__ __forceinline__ double pow2(int e) { return __longlong_as_double((long long)(e + 1023) << 52); }
 __device__ __forceinline__ long long to_int(double v, int e, double p2) {
+  if (e == OZ_NONFINITE) return 0;
   return __double2ll_rn((e > -1000 && e < 1000) ? v * p2 : scalbn(v, e));
 }
 
@@ -446,8 +451,11 @@ __global__ void __launch_bounds__(128) oz_combine_kernel(const uint8_t* __restri
   for (int k = 0; k < 4; ++k) {
     const int j = j0 + k;
     if (j >= N || ((flags & OZ_UPPER) && j < i)) continue;
-    const int sc = -(ea + eB[t * sEB + j]);
+    const int eb = eB[t * sEB + j];
+    const int sc = -(ea + eb);
     double2 v = make_double2(crt_value(sr[k], lr[k], Md), crt_value(si[k], li[k], Md));
+    if (ea == OZ_NONFINITE || eb == OZ_NONFINITE) v = make_double2(__longlong_as_double(0x7ff8000000000000LL),
+                                                                   __longlong_as_double(0x7ff8000000000000LL));
     if (sc > -1000 && sc < 1000) {
       const double f = pow2(sc);
       v.x *= f;

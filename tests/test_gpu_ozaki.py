@@ -276,3 +276,25 @@ def test_modular_cholesky_levels_match_oracle(T, monkeypatch):
     Ug = c.get_state(0).cpu().numpy()
     assert np.abs(Ug.conj().T @ Ug - np.eye(N)).max() < 1e-12
     assert np.abs(c.correlation(0).cpu().numpy() - gaussian.correlation(gaussian.orthonormalize(U))).max() < 1e-9
+
+
+@pytest.mark.parametrize("protocol", ["homodyne", "projective"])
+def test_modular_path_nan_trajectory_fails_alone(T, oz_small, protocol):
+    """A trajectory whose state holds a NaN stays failed on the modular path (non-finite rows and
+    columns come out as NaN, as an FP64 product's would) and does not disturb the other trajectory of
+    the batch, which still matches the oracle."""
+    import torch
+    import paper_2508_18468_b200 as P
+    from oracle import lattice
+    from oracle.trajectory import OracleTrajectory
+    L, gams, steps = 300, [1.0, 1.5], 6
+    gpu = _oz_on(P, L, 1, protocol, gams, seed=3)
+    U = gpu.get_state(0).cpu().numpy()
+    U[17, 5] = np.nan
+    gpu.set_state(0, torch.from_numpy(U).cuda())
+    K = lattice.propagator_lattice(L, 1, 1.0, 0.05)
+    o1 = OracleTrajectory(L, 1, protocol, gams[1], 0.05, seed=3, traj=1, K=K)
+    gpu.step(steps)
+    o1.step(steps)
+    assert gpu.failed(0) and not gpu.failed(1)
+    assert np.abs(gpu.correlation(1).cpu().numpy() - o1.correlation()).max() < 1e-10
