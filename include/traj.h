@@ -241,7 +241,9 @@ int traj_profile(traj_handle h, int enable);
 /* Which contractions of this handle run as exact modular products on the INT8 tensor cores
  * (csrc/ozaki.h; environment TRAJ_OZAKI=0 selects the FP64 DMMA kernels instead):
  * out[0] = the dense K U, out[1] = the CholeskyQR Grams and TRMMs, out[2] = the modulus count
- * (16: every operand row / column to 2^-62 of its 2-norm). */
+ * (16: every operand row / column to 2^-62 of its 2-norm).  Row-sharded handles: out[0] = out[1] =
+ * the chunked K_g U (its residues accumulated over the P chunks at U's global column exponents) and
+ * the local Grams / TRMMs; the projective rank-k products and the structured pass stay on DMMA. */
 int traj_ozaki_info(traj_handle h, int32_t* out3);
 int traj_phase_times(traj_handle h, double* ms, int64_t* launches);
 

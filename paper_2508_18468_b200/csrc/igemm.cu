@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(ITHREADS, 1)
       const uint32_t taddr = tmem + buf * IBN + ((uint32_t)(q * 32) << 16);
       int mod = 0;
       double inv = 0.0;
-      if (a.out == IG_OUT_MOD) {
+      if (a.out != IG_OUT_I32) {
         int za, zb, q;
         zmap(a, tl.z, za, zb, q);
         mod = a.moduli[q];
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(ITHREADS, 1)
             uint32_t packed = 0;
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
-              const int x = (int)v[4 * j + b];
+              int x = (int)v[4 * j + b];
               int r = x - mod * (int)floor((double)x * inv);
               r += (r < 0) ? mod : 0;
               r -= (r >= mod) ? mod : 0;
@@ -297,6 +297,28 @@ __global__ void __launch_bounds__(ITHREADS, 1)
           }
           uint8_t* p = reinterpret_cast<uint8_t*>(a.C) + ((long long)tl.z * a.ksplit + tl.kc) * a.strideC +
                        (long long)row * a.ldc + col;
+          if (a.out == IG_OUT_MOD_ACC) {   // add the residues already there (< m each), reduce once more
+            uint32_t old[8];
+            if (col + 32 <= a.N) {
+              const uint4 o0 = reinterpret_cast<const uint4*>(p)[0], o1 = reinterpret_cast<const uint4*>(p)[1];
+              old[0] = o0.x; old[1] = o0.y; old[2] = o0.z; old[3] = o0.w;
+              old[4] = o1.x; old[5] = o1.y; old[6] = o1.z; old[7] = o1.w;
+            } else {
+              for (int jj = 0; jj < 8; ++jj) old[jj] = 0;
+              for (int jj = 0; col + jj < a.N; ++jj) old[jj >> 2] |= (uint32_t)p[jj] << (8 * (jj & 3));
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              uint32_t packed = 0;
+#pragma unroll
+              for (int b = 0; b < 4; ++b) {
+                uint32_t r = ((w[j] >> (8 * b)) & 0xff) + ((old[j] >> (8 * b)) & 0xff);
+                r -= r >= (uint32_t)mod ? (uint32_t)mod : 0u;
+                packed |= r << (8 * b);
+              }
+              w[j] = packed;
+            }
+          }
           if (col + 32 <= a.N) {
             reinterpret_cast<uint4*>(p)[0] = make_uint4(w[0], w[1], w[2], w[3]);
             reinterpret_cast<uint4*>(p)[1] = make_uint4(w[4], w[5], w[6], w[7]);
@@ -835,7 +857,8 @@ int igemm(cudaStream_t st, const IgemmArgs& g, std::string* err) {
       g.lda < g.K || g.ldb < g.K || (g.ldc & 15) || g.ldc < g.N || g.a_div < 1 || g.b_div < 1 ||
       g.batch % g.a_div || g.batch % g.b_div || (reinterpret_cast<uintptr_t>(g.A) & 15) ||
       (reinterpret_cast<uintptr_t>(g.B) & 15) || (reinterpret_cast<uintptr_t>(g.C) & 15) ||
-      (g.out != IG_OUT_I32 && g.out != IG_OUT_MOD) || (g.out == IG_OUT_MOD && (!g.moduli || g.nmod < 1))) {
+      (g.out != IG_OUT_I32 && g.out != IG_OUT_MOD && g.out != IG_OUT_MOD_ACC) ||
+      (g.out != IG_OUT_I32 && (!g.moduli || g.nmod < 1))) {
     if (err) *err = "igemm: needs 0 < K < 2^17, lda/ldb multiples of 16 >= K, ldc a multiple of 16 >= N, 16-B alignment";
     return 1;
   }
@@ -846,7 +869,7 @@ int igemm(cudaStream_t st, const IgemmArgs& g, std::string* err) {
   }
   const long long na = g.oz_s ? g.oz_na : g.batch / g.a_div, nb = g.oz_s ? g.oz_nb : g.batch / g.b_div;
   const bool ab = g.strideA != 0 && na > 1, bb = g.strideB != 0 && nb > 1;
-  if (g.oz_s && (g.batch != 3LL * g.oz_s * g.oz_T || g.oz_T < 1 || !g.moduli || g.out != IG_OUT_MOD)) {
+  if (g.oz_s && (g.batch != 3LL * g.oz_s * g.oz_T || g.oz_T < 1 || !g.moduli || g.out == IG_OUT_I32)) {
     if (err) *err = "igemm: modular batch map needs batch = 3 s T and the modular epilogue";
     return 1;
   }
@@ -858,13 +881,13 @@ int igemm(cudaStream_t st, const IgemmArgs& g, std::string* err) {
     const char* v = getenv("TRAJ_IGEMM_PAIR");
     pair_env = (v && v[0] == '1') ? 1 : 0;
   }
-  const bool use_pair = pair_env && g.M >= 256 && num_sms() >= 2;
+  const bool use_pair = pair_env && g.M >= 256 && num_sms() >= 2 && g.out != IG_OUT_MOD_ACC;
   static int mc_env = -1;
   if (mc_env < 0) {
     const char* v = getenv("TRAJ_IGEMM_MC");
     mc_env = (v && v[0] == '1') ? 1 : 0;
   }
-  const bool use_mc = !use_pair && mc_env && g.M >= 256 && num_sms() >= 2;
+  const bool use_mc = !use_pair && mc_env && g.M >= 256 && num_sms() >= 2 && g.out != IG_OUT_MOD_ACC;
   CUtensorMap ma, mb;
   if (!map_i8(enc, &ma, g.A, g.K, g.M, g.lda, ab ? na : 1, g.strideA, IBM) ||
       !map_i8(enc, &mb, g.B, g.K, g.N, g.ldb, bb ? nb : 1, g.strideB, (use_pair || use_mc) ? 128 : IBN)) {

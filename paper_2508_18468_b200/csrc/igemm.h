@@ -10,6 +10,7 @@ namespace traj {
 enum IgemmOut {
   IG_OUT_I32 = 0,   // C_z[m][n] = sum_k A_z[m][k] B_z[n][k] as int32 (exact: |A|,|B| <= 128, K < 2^17)
   IG_OUT_MOD = 1,   // C_z[m][n] = that sum mod moduli[z % nmod] in [0, m) as uint8
+  IG_OUT_MOD_ACC = 2,   // C_z[m][n] = (C_z[m][n] + that sum) mod m: products of k-chunks summed in residues
 };
 
 enum IgemmFlags {

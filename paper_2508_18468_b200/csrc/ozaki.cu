@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const cplx* __restri
                                                             int rows, int cols, int T, int8_t* R, long long ldr,
                                                             int* e, long long sE, const double* part, int beta,
                                                             int subI, const int32_t* gate, const int32_t* cdev,
-                                                            const int32_t* rdev) {
+                                                            const int32_t* rdev, const int* e_in) {
   if (gate && *gate == 0) return;
   __shared__ cplx tile[CTI][CTJ + 1];
   const int j0 = blockIdx.x * CTJ, i0 = blockIdx.y * CTI, t = blockIdx.z;
@@ -314,14 +314,19 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const cplx* __restri
   __syncthreads();
   const int jj = threadIdx.x >> 3, ig = (threadIdx.x & 7) * 8, j = j0 + jj;
   if (j >= cols || i0 + ig >= rows) return;
-  double nu2 = 0.0;
-  if (j < cz) {
+  int ex;
+  if (e_in) {
+    ex = e_in[t * sE + j];
+  } else {
+    double nu2 = 0.0;
+    if (j < cz) {
 #pragma unroll
-    for (int c = 0; c < 8; ++c) nu2 += part[((long long)c * T + t) * cols + j];
+      for (int c = 0; c < 8; ++c) nu2 += part[((long long)c * T + t) * cols + j];
+    }
+    ex = scale_exp(nu2, beta);
+    if (blockIdx.y == 0 && ig == 0) e[t * sE + j] = ex;
   }
-  const int ex = scale_exp(nu2, beta);
   const double p2 = pow2(ex);
-  if (blockIdx.y == 0 && ig == 0) e[t * sE + j] = ex;
   Dig dr[8], di[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
@@ -514,14 +519,14 @@ template <int S>
 struct LaunchCols {
   static int go(cudaStream_t st, int np, const cplx* X, long long ldx, long long sX, int rows, int cols, int T,
                 int8_t* R, long long ldr, int* e, long long sE, const double* part, int beta, int subI,
-                const int32_t* gate, const int32_t* cdev, const int32_t* rdev) {
+                const int32_t* gate, const int32_t* cdev, const int32_t* rdev, const int* e_in) {
     dim3 grid(ceil_div(cols, CTJ), ceil_div(rows, CTI), T);
     if (np == 4)
       oz_split_cols_kernel<S, 4><<<grid, 256, 0, st>>>(X, ldx, sX, rows, cols, T, R, ldr, e, sE, part, beta, subI, gate,
-                                                       cdev, rdev);
+                                                       cdev, rdev, e_in);
     else
       oz_split_cols_kernel<S, 3><<<grid, 256, 0, st>>>(X, ldx, sX, rows, cols, T, R, ldr, e, sE, part, beta, subI, gate,
-                                                       cdev, rdev);
+                                                       cdev, rdev, e_in);
     return 0;
   }
 };
@@ -602,8 +607,62 @@ int oz_split_cols(cudaStream_t st, const cplx* X, long long ldx, long long sX, i
                                                                             sub_identity, gate, rdev);
   if (int r = launched("oz_colnorm", err)) return r;
   if (dispatch_s<LaunchCols>(s, st, nplanes, X, ldx, sX, rows, cols, T, R, oz_ld(rows), e, sE, part, oz_beta(s),
-                             sub_identity, gate, cdev, rdev)) {
+                             sub_identity, gate, cdev, rdev, nullptr)) {
     if (err) *err = "oz_split_cols: shared memory attribute";
+    return 4;
+  }
+  return launched("oz_split_cols", err);
+}
+
+namespace {
+__global__ void oz_colsum_kernel(const double* __restrict__ part, int cols, int T, double* nu2, long long sN, int acc) {
+  const int j = blockIdx.x * 256 + threadIdx.x, t = blockIdx.y;
+  if (j >= cols) return;
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += part[((long long)c * T + t) * cols + j];
+  nu2[t * sN + j] = acc ? nu2[t * sN + j] + s : s;
+}
+__global__ void oz_exponents_kernel(const double* __restrict__ nu2, long long sN, int cols, int beta, int* e,
+                                    long long sE) {
+  const int j = blockIdx.x * 256 + threadIdx.x, t = blockIdx.y;
+  if (j < cols) e[t * sE + j] = scale_exp(nu2[t * sN + j], beta);
+}
+}  // namespace
+
+int oz_colnorm_accumulate(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T,
+                          double* part, double* nu2, long long sN, int accumulate, std::string* err) {
+  if (cols <= 0 || T <= 0) return 0;
+  oz_colnorm_kernel<<<dim3(ceil_div(cols, 32), 8, T), dim3(32, 8), 0, st>>>(X, ldx, sX, rows, cols, T, part, 0,
+                                                                            nullptr, nullptr);
+  if (int r = launched("oz_colnorm", err)) return r;
+  oz_colsum_kernel<<<dim3(ceil_div(cols, 256), T), 256, 0, st>>>(part, cols, T, nu2, sN, accumulate);
+  return launched("oz_colsum", err);
+}
+
+int oz_exponents(cudaStream_t st, const double* nu2, long long sN, int cols, int T, int s, int* e, long long sE,
+                 std::string* err) {
+  if (cols <= 0 || T <= 0) return 0;
+  if (!oz_supported(s)) {
+    if (err) *err = "oz_exponents: unsupported modulus count";
+    return 1;
+  }
+  oz_exponents_kernel<<<dim3(ceil_div(cols, 256), T), 256, 0, st>>>(nu2, sN, cols, oz_beta(s), e, sE);
+  return launched("oz_exponents", err);
+}
+
+int oz_split_cols_e(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T,
+                    int nplanes, int s, int8_t* R, const int* e_in, long long sE, std::string* err) {
+  if (rows <= 0 || cols <= 0 || T <= 0) return 0;
+  const int* md;
+  if (!oz_supported(s) || (nplanes != 3 && nplanes != 4) || !e_in) {
+    if (err) *err = "oz_split_cols_e: unsupported modulus / plane count or no exponents";
+    return 1;
+  }
+  if (int r = ensure_device_constants(&md, err)) return r;
+  if (dispatch_s<LaunchCols>(s, st, nplanes, X, ldx, sX, rows, cols, T, R, oz_ld(rows), nullptr, sE, nullptr,
+                             oz_beta(s), 0, nullptr, nullptr, nullptr, e_in)) {
+    if (err) *err = "oz_split_cols_e: launch";
     return 4;
   }
   return launched("oz_split_cols", err);
@@ -646,7 +705,7 @@ int oz_product_mma(cudaStream_t st, const OzProduct& p, std::string* err) {
   g.C = p.RC;
   g.ldc = oz_ld(p.N);
   g.strideC = (long long)p.M * g.ldc;
-  g.out = IG_OUT_MOD;
+  g.out = p.mma_accumulate ? IG_OUT_MOD_ACC : IG_OUT_MOD;
   g.moduli = md;
   g.flags = ((p.flags & OZ_UPPER) ? IG_UPPER : 0) | ((p.flags & OZ_TRI_B) ? IG_TRI_B : 0);
   g.oz_s = p.s;

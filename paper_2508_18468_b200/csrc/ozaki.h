@@ -46,6 +46,16 @@ int oz_split_cols(cudaStream_t st, const cplx* X, long long ldx, long long sX, i
                   int s, int8_t* R, int* e, long long sE, double* part, std::string* err, int sub_identity = 0,
                   const int32_t* gate = nullptr, const int32_t* cdev = nullptr, const int32_t* rdev = nullptr);
 // (rdev, both splits: rows r >= rdev[t] of X are taken as zero)
+// e_in (optional): the columns' exponents given (e.g. global ones over all shards' rows) instead of
+// computed from X's own column norms; e is then not written
+int oz_split_cols_e(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T,
+                    int nplanes, int s, int8_t* R, const int* e_in, long long sE, std::string* err);
+// nu2[t][j] (+)= sum over X's rows of (|re| + |im|)^2 of column j (part: >= 8 T cols doubles of scratch)
+int oz_colnorm_accumulate(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T,
+                          double* part, double* nu2, long long sN, int accumulate, std::string* err);
+// e[t][j] = the column exponents for s moduli from the squared norms nu2
+int oz_exponents(cudaStream_t st, const double* nu2, long long sN, int cols, int T, int s, int* e, long long sE,
+                 std::string* err);
 
 enum OzFlags {
   OZ_UPPER = 1,       // C upper triangular (only j >= i computed and written)
@@ -78,6 +88,7 @@ struct OzProduct {
   const int32_t* ndev = nullptr;   // per trajectory: only columns j < ndev[t] of C are computed and written
   int ksplit = 1;                  // split-K chunks of the INT8 launch (RC holds ksplit x the residue products)
   long long lda_override = 0;      // RA's row length in bytes when it is a k-range of wider residue rows
+  int mma_accumulate = 0;          // oz_product_mma: add the residues to RC's (k-chunks summed) instead of writing
 };
 
 // the products (one batched INT8 launch) and the CRT combine into C

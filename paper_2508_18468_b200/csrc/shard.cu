@@ -26,6 +26,7 @@
 #include "dgemm.h"
 #include "planar.h"
 #include "comm_plan.h"
+#include "ozaki.h"
 
 namespace traj {
 
@@ -247,6 +248,17 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
     sh->planar = !banded && !(pk && pk[0] == '0') && !(pc && pc[0] == '0') && N >= min_n && (L / P) % 2 == 0;
     sh->ldKs = round_up(L, 16);
     sh->ldPs = round_up(N, 16);
+    // the modular engine replaces the planar one (K_g's chunk columns start at byte s Lp of its residue
+    // rows: TMA needs 16-byte alignment, so Lp % 16 == 0 unless P == 1)
+    const char* oz = getenv("TRAJ_OZAKI");
+    const char* om = getenv("TRAJ_OZAKI_MODULI");
+    const char* oc = getenv("TRAJ_OZAKI_CORR_MODULI");
+    sh->oz_s = om ? atoi(om) : 16;
+    sh->oz_s_corr = oc ? atoi(oc) : 10;
+    if (sh->oz_s_corr != 0 && !oz_supported(sh->oz_s_corr)) sh->oz_s_corr = 10;
+    sh->oz = !banded && !(oz && oz[0] == '0') && oz_supported(sh->oz_s) && N >= min_n && L / P <= 65535 &&
+             N <= 65535 && (P == 1 || (L / P) % 16 == 0);
+    if (sh->oz) sh->planar = false;
     if (sh->planar) {
       // the unsharded rule (traj_api.cu carve) on the Lp x Lp chunks
       const char* sv = getenv("TRAJ_STRASSEN");
@@ -274,6 +286,9 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
     l.row0 = (int)(l.g * Lp);
     if (banded) {
       lay.take(l.Uext, (size_t)(Lp + 2 * sh->H) * ldN * 16);
+    } else if (sh->oz) {
+      lay.take(l.RK, (size_t)oz_residue_bytes(3, sh->oz_s, 1, Lp, L));
+      lay.take(l.eK, (size_t)Lp * 4);
     } else if (sh->planar) {
       lay.take(l.Kp, (size_t)3 * Lp * sh->ldKs * 8);
       if (sh->slv)
@@ -305,6 +320,21 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
     lay.take(sh->Cp, (size_t)3 * Lp * sh->ldPs * 8);
     lay.take(sh->Gp, (size_t)3 * N * sh->ldPs * 8);
     lay.take(sh->Xp, (size_t)3 * N * sh->ldPs * 8);
+  }
+  if (sh->oz) {
+    const int q = sh->oz_s;
+    const long long mx = std::max(Lp, N);
+    lay.take(sh->RU, (size_t)std::max(oz_residue_bytes(4, q, 1, N, Lp), oz_residue_bytes(3, q, 1, Lp, N)));
+    lay.take(sh->RX, (size_t)oz_residue_bytes(3, q, 1, N, N));
+    // (K_g is built there, complex, before its split)
+    sh->RC_bytes = (size_t)std::max({oz_residue_bytes(3, q, 1, Lp, N), oz_residue_bytes(3, q, 1, N, N),
+                                     (long long)Lp * ldL * 16});
+    lay.take(sh->RC, sh->RC_bytes);
+    lay.take(sh->eU, (size_t)mx * 4);
+    lay.take(sh->eX, (size_t)N * 4);
+    lay.take(sh->eG, (size_t)N * 4);
+    lay.take(sh->nu2, (size_t)N * 8);
+    lay.take(sh->oz_part, (size_t)8 * mx * 8);
   }
   if (c->nccl_id && sh->planar) {   // packed, pipelined Gram allreduce: two panel buffers
     const char* gp = getenv("TRAJ_GRAM_PANEL");
@@ -506,6 +536,11 @@ int shard_build(ShardedCtx* sh, const std::vector<std::complex<double>>& kc, con
         if (strassen_k(st, sh->slv, l.Kp + (long long)c * sh->Lp, sh->ldKs, (long long)sh->Lp * sh->ldKs, sh->Lp,
                        l.Ks + c * ns * hh * sh->ldS, sh->ldS, err))
           return 4;
+    } else if (sh->oz) {   // K_g in the product scratch, then its row residues (once)
+      cplx* Kt = reinterpret_cast<cplx*>(sh->RC);
+      if (build_k(st, Kt, sh->ldL, sh->Lx, sh->Ly, sh->kcoef, sh->kcoef + sh->Lx, err, l.row0, sh->Lp) ||
+          oz_split_rows(st, Kt, sh->ldL, 0, sh->Lp, sh->L, 1, 0, sh->oz_s, l.RK, l.eK, 0, err))
+        return 4;
     } else if (!sh->banded &&
                build_k(st, l.K, sh->ldL, sh->Lx, sh->Ly, sh->kcoef, sh->kcoef + sh->Lx, err, l.row0, sh->Lp)) {
       return 4;
@@ -606,7 +641,32 @@ int cqr2(ShardedCtx* sh, int src_which, std::string* err) {
         goto gram_done;
       }
       for (auto& l : sh->loc) {
-        if (sh->planar) {
+        if (sh->oz) {
+          // local G_g = U_g^dag U_g on the INT8 tensor cores (the unsharded step's modular Gram)
+          STRY(oz_split_cols(sh->st, l.U[src], sh->ldN, 0, sh->Lp, sh->N, 1, 4, sh->oz_s, sh->RU, sh->eU, 0,
+                             sh->oz_part, err));
+          OzProduct p;
+          p.M = sh->N;
+          p.N = sh->N;
+          p.K = sh->Lp;
+          p.s = sh->oz_s;
+          p.RA = sh->RU;
+          p.a_planes = 4;
+          p.pa[2] = 3;
+          p.eA = sh->eU;
+          p.RB = sh->RU;
+          p.b_planes = 4;
+          p.eB = sh->eU;
+          p.RC = sh->RC;
+          p.C = l.Gpart;
+          p.ldc = sh->ldN;
+          p.flags = OZ_UPPER | OZ_NEG_P2;
+          {
+            Phase pm(sh->prof, sh->st, TRAJ_PH_GRAM_MMA);
+            STRY(oz_product_mma(sh->st, p, err));
+          }
+          STRY(oz_product_combine(sh->st, p, err));
+        } else if (sh->planar) {
           // local G_g = U_g^dag U_g as three real products (planes re, im, re - im | re, im, re + im)
           const long long psU = (long long)sh->Lp * sh->ldPs, psG = (long long)sh->N * sh->ldPs;
           STRY(split6_planes(sh->st, l.U[src], sh->ldN, 0, sh->Lp, sh->N, 1, l.Up6, sh->ldPs, psU, 0, err));
@@ -639,6 +699,8 @@ int cqr2(ShardedCtx* sh, int src_which, std::string* err) {
                                                                  sh->fb_dev, &e2) ? -1 : 1;
         }
         if (sh->fbg_state == 1) {
+          // the modular TRMM below keys its full-precision product on the same decision (gate)
+          if (sh->oz) STRY(cqr2_decide(sh->st, sh->gdev, 1, thr, sh->gate, nullptr, err));
           STRY(sh->fbg.launch(sh->st, err));
         } else {
           STRY(cqr2_decide(sh->st, sh->gdev, 1, thr, sh->gate, sh->fb_dev, err));
@@ -646,7 +708,7 @@ int cqr2(ShardedCtx* sh, int src_which, std::string* err) {
                             sh->failed_dev, err, nullptr, nullptr, sh->gate));
         }
       }
-      if (full && pass == 0 && sh->chol_overlap && sh->N > 64) {
+      if (full && pass == 0 && sh->chol_overlap && sh->N > 64 && !sh->oz) {
         // factorise on st_hi; each newly final left column block's TRMM runs on st_lo
         SCK(cudaEventRecord(sh->ev_fork, sh->st));
         SCK(cudaStreamWaitEvent(sh->st_hi, sh->ev_fork, 0));
@@ -698,7 +760,41 @@ int cqr2(ShardedCtx* sh, int src_which, std::string* err) {
     }
     {
       Phase p(sh->prof, sh->st, TRAJ_PH_TRMM);
-      if (sh->planar) {
+      if (sh->oz) {
+        // U_g X on the INT8 tensor cores (the unsharded step's modular TRMM): after the first-order
+        // second-pass factor X = I + D, U_g + U_g D at oz_s_corr moduli, overwritten by the full
+        // product when the device decided on the full factorisation (gate)
+        const bool corr = pass == 1 && !sh->full_cqr2 && sh->oz_s_corr > 0;
+        for (int full = corr ? 0 : 1; full < 2; ++full) {
+          const int q = full ? sh->oz_s : sh->oz_s_corr;
+          const int32_t* gate = corr && full ? sh->gate : nullptr;
+          STRY(oz_split_cols(sh->st, sh->X, sh->ldN, 0, sh->N, sh->N, 1, 3, q, sh->RX, sh->eX, 0, sh->oz_part, err,
+                             full ? 0 : 1, gate));
+          for (auto& l : sh->loc) {
+            STRY(oz_split_rows(sh->st, l.U[src], sh->ldN, 0, sh->Lp, sh->N, 1, 0, q, sh->RU, sh->eU, 0, err, gate));
+            OzProduct op;
+            op.M = sh->Lp;
+            op.N = sh->N;
+            op.K = sh->N;
+            op.s = q;
+            op.RA = sh->RU;
+            op.eA = sh->eU;
+            op.RB = sh->RX;
+            op.eB = sh->eX;
+            op.RC = sh->RC;
+            op.C = l.U[1 - src];
+            op.ldc = sh->ldN;
+            op.flags = OZ_TRI_B;
+            op.base = full ? nullptr : l.U[src];
+            op.gate = gate;
+            {
+              Phase pm(sh->prof, sh->st, TRAJ_PH_TRMM_MMA);
+              STRY(oz_product_mma(sh->st, op, err));
+            }
+            STRY(oz_product_combine(sh->st, op, err));
+          }
+        }
+      } else if (sh->planar) {
         // U_g X as three real products on the Gram's planes of U_g and X's planes
         const long long psU = (long long)sh->Lp * sh->ldPs, psX = (long long)sh->N * sh->ldPs;
         STRY(split_planes(sh->st, sh->X, sh->ldN, 0, sh->N, sh->N, 1, sh->Xp, sh->ldPs, psX, 0, err));
@@ -916,20 +1012,64 @@ int planar_finish(ShardedCtx* sh, ShardLocal& l, int nxt, std::string* err) {
   return combine_planes(sh->st, l.Pp, sh->ldPs, psC, 0, sh->Lp, sh->N, 1, l.U[nxt], sh->ldN, 0, err);
 }
 
+// modular K_g U: the GLOBAL column exponents of U (column norms summed over the shards: one N-double
+// allreduce), so that every chunk's residues U_s share one scale and their products add mod m_q
+int oz_global_exponents(ShardedCtx* sh, int cur, std::string* err) {
+  int i = 0;
+  for (auto& l : sh->loc)
+    STRY(oz_colnorm_accumulate(sh->st, l.U[cur], sh->ldN, 0, sh->Lp, sh->N, 1, sh->oz_part, sh->nu2, 0, i++ > 0,
+                               err));
+  if (sh->comm.comm && sh->P > 1) STRY(sh->comm.allreduce(sh->st, &sh->nu2, sh->nu2, (size_t)sh->N, err));
+  return oz_exponents(sh->st, sh->nu2, 0, sh->N, 1, sh->oz_s, sh->eG, 0, err);
+}
+
+OzProduct oz_ku(ShardedCtx* sh, ShardLocal& l, int nxt) {
+  OzProduct p;
+  p.M = sh->Lp;
+  p.N = sh->N;
+  p.K = sh->Lp;
+  p.T = 1;
+  p.s = sh->oz_s;
+  p.RA = l.RK;
+  p.a_traj = 0;
+  p.eA = l.eK;
+  p.RB = sh->RU;
+  p.eB = sh->eG;
+  p.RC = sh->RC;
+  p.C = l.U[nxt];
+  p.ldc = sh->ldN;
+  p.lda_override = oz_ld(sh->L);
+  return p;
+}
+
+// residues of K_g[:, s] U_s (+)= into RC: U_s's column residues at the global exponents, K_g's
+// row residues from byte s Lp of each row
+int oz_chunk(ShardedCtx* sh, ShardLocal& l, const cplx* Us, int s, bool accumulate, int nxt, std::string* err) {
+  STRY(oz_split_cols_e(sh->st, Us, sh->ldN, 0, sh->Lp, sh->N, 1, 3, sh->oz_s, sh->RU, sh->eG, 0, err));
+  OzProduct p = oz_ku(sh, l, nxt);
+  p.RA = l.RK + (long long)s * sh->Lp;
+  p.mma_accumulate = accumulate ? 1 : 0;
+  Phase pm(sh->prof, sh->st, TRAJ_PH_KU_MMA);
+  return oz_product_mma(sh->st, p, err);
+}
+
 int propagate_dense(ShardedCtx* sh, int cur, int nxt, std::string* err) {
   cudaStream_t st = sh->st;
   const long long Lp = sh->Lp, ld = sh->ldN;
   const size_t bytes = (size_t)Lp * ld * 16;
-  if (sh->planar && !(sh->comm.comm && sh->overlap && sh->P > 1)) {
+  if (sh->oz) STRY(oz_global_exponents(sh, cur, err));
+  if ((sh->planar || sh->oz) && !(sh->comm.comm && sh->overlap && sh->P > 1)) {
     // gathered first (emulation, one shard, or TRAJ_SHARD_OVERLAP=0), then the chunk products
     if (sh->P > 1) STRY(gather_full(sh, cur, err));
     for (auto& l : sh->loc) {
       for (int d = 0; d < sh->P; ++d) {
         const int s = (l.g - d + sh->P) % sh->P;
         const cplx* Us = sh->P > 1 ? sh->Ufull + (size_t)s * Lp * ld : l.U[cur];
-        STRY(planar_chunk(sh, l, Us, s, d > 0, err, nxt));
+        if (sh->oz) STRY(oz_chunk(sh, l, Us, s, d > 0, nxt, err));
+        else STRY(planar_chunk(sh, l, Us, s, d > 0, err, nxt));
       }
-      STRY(planar_finish(sh, l, nxt, err));
+      if (sh->oz) STRY(oz_product_combine(st, oz_ku(sh, l, nxt), err));
+      else STRY(planar_finish(sh, l, nxt, err));
     }
     return 0;
   }
@@ -973,12 +1113,14 @@ int propagate_dense(ShardedCtx* sh, int cur, int nxt, std::string* err) {
         SCK(cudaStreamWaitEvent(st, sh->ev_chunk[d], 0));
         Us = sh->Ufull + (size_t)s * Lp * ld;
       }
-      if (sh->planar) STRY(planar_chunk(sh, l, Us, s, d > 0, err, nxt));
+      if (sh->oz) STRY(oz_chunk(sh, l, Us, s, d > 0, nxt, err));
+      else if (sh->planar) STRY(planar_chunk(sh, l, Us, s, d > 0, err, nxt));
       else
         STRY(zgemm(st, 0, 0, Lp, sh->N, Lp, 1.0, 0.0, l.K + (size_t)s * Lp, sh->ldL, 0, Us, ld, 0, d ? 1.0 : 0.0,
                    l.U[nxt], ld, 0, 1, 0, err));
     }
-    if (sh->planar) STRY(planar_finish(sh, l, nxt, err));
+    if (sh->oz) STRY(oz_product_combine(st, oz_ku(sh, l, nxt), err));
+    else if (sh->planar) STRY(planar_finish(sh, l, nxt, err));
     return 0;
   }
   STRY(gather_full(sh, cur, err));

@@ -49,6 +49,9 @@ struct ShardLocal {
   // planar 3M (dense K): K_g's planes [3][Lp][ldKs], product planes [3][Lp][ldPs], U's six planes
   double *Kp = nullptr, *Pp = nullptr, *Up6 = nullptr;
   double* Ks = nullptr;    // Strassen: the operands of every K chunk K_g[:, s], [P][3 7^lv][Lp/2^lv][ldS]
+  // modular engine (ozaki.h): K_g's row residues [3][s][Lp][oz_ld(L)] over the full row, its row exponents
+  int8_t* RK = nullptr;
+  int* eK = nullptr;
 };
 
 struct ShardedCtx {
@@ -128,6 +131,16 @@ struct ShardedCtx {
   long long ldS = 0, ldSM = 0;
   double *Sb = nullptr, *Sm = nullptr;
   double *Cp = nullptr, *Gp = nullptr, *Xp = nullptr;   // chunk planes [3][Lp], Gram / X planes [3][N]
+  // modular engine (TRAJ_OZAKI, N >= TRAJ_PLANAR_MIN_N): K_g U as P chunk products K_g[:, s] U_s whose
+  // residues accumulate in RC (U_s split with the GLOBAL column exponents eG of U, from the column norms
+  // summed over the shards), one CRT combine; the local Grams and TRMMs as in the unsharded step
+  bool oz = false;
+  int oz_s = 16, oz_s_corr = 10;
+  int8_t *RU = nullptr, *RX = nullptr;
+  uint8_t* RC = nullptr;
+  size_t RC_bytes = 0;
+  int *eU = nullptr, *eX = nullptr, *eG = nullptr;
+  double *oz_part = nullptr, *nu2 = nullptr;
   cplx* dist_scratch = nullptr;
   size_t dist_scratch_bytes = 0;
   cudaStream_t cst = nullptr;

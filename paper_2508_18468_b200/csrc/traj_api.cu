@@ -2229,6 +2229,11 @@ int traj_profile(traj_handle h, int enable) {
 
 int traj_ozaki_info(traj_handle h, int32_t* out3) {
   if (!h || !out3) return TRAJ_EINVAL;
+  if (h->sh) {   // row-sharded: K_g U, the local Grams and TRMMs together
+    out3[0] = out3[1] = h->sh->oz ? 1 : 0;
+    out3[2] = h->sh->oz ? h->sh->oz_s : 0;
+    return 0;
+  }
   out3[0] = h->oz_ku ? 1 : 0;
   out3[1] = h->oz_cqr ? 1 : 0;
   out3[2] = (h->oz_ku || h->oz_cqr) ? h->oz_s : 0;

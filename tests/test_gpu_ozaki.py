@@ -298,3 +298,61 @@ def test_modular_path_nan_trajectory_fails_alone(T, oz_small, protocol):
     o1.step(steps)
     assert gpu.failed(0) and not gpu.failed(1)
     assert np.abs(gpu.correlation(1).cpu().numpy() - o1.correlation()).max() < 1e-10
+
+
+# ---- the row-sharded step on the modular engine: K_g U as P chunk products whose
+# ---- residues accumulate over the chunks at U's global column exponents, local modular Grams / TRMMs
+
+@pytest.mark.parametrize("L,P_shards,protocol,gam", [(480, 2, "projective", 2.0), (480, 3, "homodyne", 1.0),
+                                                     (512, 4, "projective", 0.7), (512, 8, "homodyne", 2.0),
+                                                     (512, 8, "projective", 3.0)])
+def test_row_sharded_modular_step_matches_oracle_and_dmma(T, oz_small, monkeypatch, L, P_shards, protocol, gam):
+    """Single-GPU emulation of P shards (Lp = 240, 160, 128, 64 rows: ragged against the 128-row tiles)
+    on the modular path, the same trajectory on the sharded DMMA kernels (TRAJ_OZAKI=0) and the oracle:
+    identical clicks, C within 1e-12 of the DMMA step and 1e-10 of the oracle, S_A within 1e-8."""
+    import paper_2508_18468_b200 as P
+    from oracle import lattice
+    from oracle.trajectory import OracleTrajectory
+    a = P.Trajectories(L, 1, protocol, [gam], seed=23, traj_base=1, shard_size=P_shards)
+    assert a.ozaki_info() == (True, True, 16)
+    monkeypatch.setenv("TRAJ_OZAKI", "0")
+    b = P.Trajectories(L, 1, protocol, [gam], seed=23, traj_base=1, shard_size=P_shards)
+    assert not b.ozaki_info()[0]
+    o = OracleTrajectory(L, 1, protocol, gam, 0.05, seed=23, traj=1, K=lattice.propagator_lattice(L, 1, 1.0, 0.05))
+    regions = [np.arange(L // 2), np.arange(37, 211)]
+    for s in range(12):
+        a.step(1)
+        b.step(1)
+        o.step(1)
+        if protocol == "projective":
+            assert a.last_clicks(0) == b.last_clicks(0) == (o.last_clicks[0].size, int(o.last_clicks[1].sum()))
+        if s % 4 == 3:
+            ca = a.correlation(0).cpu().numpy()
+            assert np.abs(ca - b.correlation(0).cpu().numpy()).max() < 1e-12
+            assert np.abs(ca - o.correlation()).max() < 1e-10
+            for A in regions:
+                assert abs(a.entropy(A)[0] - o.entropy(A)) < 1e-8
+    U = a.get_state(0).cpu().numpy()
+    assert np.abs(U.conj().T @ U - np.eye(L // 2)).max() < 1e-12
+    assert not a.failed(0)
+    a.close()
+    b.close()
+
+
+def test_row_sharded_modular_nccl_single_rank(T, oz_small):
+    """The NCCL code path of the sharded modular step (a one-rank communicator: the global column
+    exponents' allreduce, the chunk residues, the local Gram) against the unsharded modular handle."""
+    import paper_2508_18468_b200 as P
+    L = 232
+    uid = P.traj_nccl_unique_id()
+    a = P.Trajectories(L, 1, "projective", [3.0], seed=5, shard_size=1, shard_rank=0, nccl_id=uid)
+    b = P.Trajectories(L, 1, "projective", [3.0], seed=5)
+    assert a.ozaki_info() == b.ozaki_info() == (True, True, 16)
+    a.step(10)
+    b.step(10)
+    assert a.last_clicks(0) == b.last_clicks(0)
+    assert np.abs(a.correlation(0).cpu().numpy() - b.correlation(0).cpu().numpy()).max() < 1e-12
+    U = a.get_state(0).cpu().numpy()
+    assert np.abs(U.conj().T @ U - np.eye(L // 2)).max() < 1e-12
+    a.close()
+    b.close()

@@ -250,6 +250,7 @@ def test_strassen_propagator_matches_oracle(P, monkeypatch, Lx, Ly, protocol, ga
     L, steps = Lx * Ly, 10
     monkeypatch.setenv("TRAJ_PLANAR_MIN_N", "0")
     monkeypatch.setenv("TRAJ_STRASSEN_MIN_N", "0")
+    monkeypatch.setenv("TRAJ_OZAKI", "0")   # the DMMA planar products (the modular ones: test_gpu_ozaki.py)
     monkeypatch.setenv("TRAJ_STRASSEN_LEVELS", str(levels))
     a = P.Trajectories(Lx, Ly, protocol, gams, seed=17)
     monkeypatch.setenv("TRAJ_STRASSEN", "0")
@@ -278,6 +279,7 @@ def test_row_sharded_strassen_chunks_match_oracle(P, monkeypatch, levels, shards
     L, steps, gam = 256, 8, (3.0 if protocol == "projective" else 1.0)
     monkeypatch.setenv("TRAJ_PLANAR_MIN_N", "0")
     monkeypatch.setenv("TRAJ_STRASSEN_MIN_N", "0")
+    monkeypatch.setenv("TRAJ_OZAKI", "0")   # the DMMA planar products (the modular ones: test_gpu_ozaki.py)
     monkeypatch.setenv("TRAJ_STRASSEN_LEVELS", str(levels))
     a = P.Trajectories(L, 1, protocol, [gam], seed=19, shard_size=shards)
     monkeypatch.setenv("TRAJ_STRASSEN", "0")
@@ -470,6 +472,7 @@ def test_planar_propagator_matches_interleaved(P, Lx, Ly, protocol, gams, monkey
     and the oracle, same trajectories.  TRAJ_PLANAR_MIN_N=0 turns the planar paths on at these
     small sizes."""
     monkeypatch.setenv("TRAJ_PLANAR_MIN_N", "0")
+    monkeypatch.setenv("TRAJ_OZAKI", "0")
     monkeypatch.setenv("TRAJ_PLANAR_KU", "0")
     monkeypatch.setenv("TRAJ_PLANAR_CQR", "0")
     a = P.Trajectories(Lx, Ly, protocol, gams, seed=41)
@@ -501,6 +504,7 @@ def test_row_sharded_nccl_single_rank(P, planar, monkeypatch):
     L = 232 if planar else 128
     if planar:
         monkeypatch.setenv("TRAJ_PLANAR_MIN_N", "0")
+        monkeypatch.setenv("TRAJ_OZAKI", "0")
         monkeypatch.setenv("TRAJ_GRAM_PANEL", "64")
     uid = P.traj_nccl_unique_id()
     a = P.Trajectories(L, 1, "projective", [3.0], seed=5, shard_size=1, shard_rank=0, nccl_id=uid)
