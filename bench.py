@@ -313,7 +313,7 @@ def run_ours(args):
     ms_max = max_over_ranks(ms, world)
     value = (1 if shard else world) * tpg * args.steps / (ms_max / 1e3)
     rows = w.L // world if shard else w.L
-    oz = tr.ozaki_info() if not shard else (False, False, 0)
+    oz = tr.ozaki_info()
     roof, executed, hbm, library = roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P, oz)
     # ---- row a4, timed separately (north star: "eigvalsh on C_A at sampled times, timed
     # separately"): the config's sampled observables once, after the timed steps
@@ -540,7 +540,10 @@ def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P, oz=(False, Fal
                            f"tiles, 128x256x128 CTA tile, persistent): one launch of the 3 x {s_} residue products "
                            + {"propagate": "of U <- K U (K's residues formed once)",
                               "gram": "of G = U^dag U (upper tiles)",
-                              "trmm": "of U <- U R^-1 (triangular k-blocks skipped)"}[dom]),
+                              "trmm": "of U <- U R^-1 (triangular k-blocks skipped)"}[dom]
+                           + ("; per shard (L/P rows): the P ring-ordered K-chunk products K_g[:, s] U_s, their "
+                              "residues accumulated in the epilogue, one CRT combine" if shard and dom == "propagate"
+                              else "; per shard (L/P rows)" if shard else "")),
                 "kernel_ms": mma_ms, "timed": ("device time of the INT8 launch per step (CUDA events around it on "
                                                 "the handle's stream, nested phase " + mma_ph + ")"),
                 "ops_counted": (f"2 x 3 x {s_} x (the complex product's m n k; half for the Gram's and TRMM's "

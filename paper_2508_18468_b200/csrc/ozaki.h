@@ -91,6 +91,21 @@ struct OzProduct {
   int mma_accumulate = 0;          // oz_product_mma: add the residues to RC's (k-chunks summed) instead of writing
 };
 
+// The residue scratch of one handle's modular products (the caller sizes it for its shapes): operand
+// residues RU / RX, products RC, exponents eU / eU2 (stride sEU per trajectory) and eX (stride sEX)
+struct OzWork {
+  int s = 16;
+  int8_t* RU = nullptr;
+  int8_t* RX = nullptr;
+  uint8_t* RC = nullptr;
+  size_t RC_bytes = 0;
+  int* eU = nullptr;
+  int* eU2 = nullptr;
+  int* eX = nullptr;
+  long long sEU = 0, sEX = 0;
+  double* part = nullptr;
+};
+
 // the products (one batched INT8 launch) and the CRT combine into C
 int oz_product(cudaStream_t st, const OzProduct& p, std::string* err);
 // the same in two calls (the caller times the INT8 launch alone)

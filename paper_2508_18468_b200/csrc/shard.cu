@@ -259,6 +259,8 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
     sh->oz = !banded && !(oz && oz[0] == '0') && oz_supported(sh->oz_s) && N >= min_n && L / P <= 65535 &&
              N <= 65535 && (P == 1 || (L / P) % 16 == 0);
     if (sh->oz) sh->planar = false;
+    const char* ck = getenv("TRAJ_SHARD_OZ_CHUNKS");
+    sh->oz_chunked = ck && ck[0] == '1';
     if (sh->planar) {
       // the unsharded rule (traj_api.cu carve) on the Lp x Lp chunks
       const char* sv = getenv("TRAJ_STRASSEN");
@@ -324,13 +326,17 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
   if (sh->oz) {
     const int q = sh->oz_s;
     const long long mx = std::max(Lp, N);
-    lay.take(sh->RU, (size_t)std::max(oz_residue_bytes(4, q, 1, N, Lp), oz_residue_bytes(3, q, 1, Lp, N)));
+    // (C_SS's 4-plane row split of U_S: at most N rows on the modular path)
+    lay.take(sh->RU, (size_t)std::max({oz_residue_bytes(4, q, 1, N, Lp), oz_residue_bytes(3, q, 1, Lp, N),
+                                       oz_residue_bytes(4, q, 1, std::min<long long>(cap, N), N),
+                                       sh->oz_chunked ? 0ll : oz_residue_bytes(3, q, 1, N, L)}));
     lay.take(sh->RX, (size_t)oz_residue_bytes(3, q, 1, N, N));
     // (K_g is built there, complex, before its split)
     sh->RC_bytes = (size_t)std::max({oz_residue_bytes(3, q, 1, Lp, N), oz_residue_bytes(3, q, 1, N, N),
                                      (long long)Lp * ldL * 16});
     lay.take(sh->RC, sh->RC_bytes);
     lay.take(sh->eU, (size_t)mx * 4);
+    lay.take(sh->eU2, (size_t)mx * 4);
     lay.take(sh->eX, (size_t)N * 4);
     lay.take(sh->eG, (size_t)N * 4);
     lay.take(sh->nu2, (size_t)N * 8);
@@ -390,7 +396,11 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
     lay.take(sh->W, (size_t)N * ldcap * 16);
     // structured CholeskyQR pass 1 (structchol.h): Y [cap][b], C [b][b], X blocks [N][b], W, Z [cap][ldN]
     const char* sbv = getenv("TRAJ_STRUCT_B");
-    const int b = sbv ? std::max(16, std::min(1024, atoi(sbv) / 16 * 16)) : (cap >= 1024 ? 512 : 128);
+    const char* opm = getenv("TRAJ_OZAKI_PROJ_MIN");
+    sh->oz_proj_min = opm ? atoi(opm) : 1024;
+    // (the unsharded rule: wide blocks once the solve runs modular)
+    const int b = sbv ? std::max(16, std::min(2048, atoi(sbv) / 16 * 16))
+                      : (cap >= 1024 ? (sh->oz && cap >= sh->oz_proj_min ? 2048 : 512) : 128);
     sh->sc.b = b;
     sh->sc.N = (int)N;
     sh->sc.T = 1;
@@ -488,6 +498,8 @@ int shard_init(ShardedCtx* sh, const traj_config* c, std::string* err) {
     sh->lowrank_gram = !(lg && lg[0] == '0');
     const char* scv = getenv("TRAJ_STRUCT_CHOL");
     sh->struct_chol = !(scv && scv[0] == '0');
+    const char* sp = getenv("TRAJ_STRUCT_PIPELINE");
+    sh->struct_serial = sp && sp[0] == '0';
     const char* co = getenv("TRAJ_CHOL_OVERLAP");
     int least = 0, greatest = 0;
     sh->chol_overlap = !(co && co[0] == '0') && cudaDeviceGetStreamPriorityRange(&least, &greatest) == cudaSuccess &&
@@ -552,6 +564,46 @@ int shard_build(ShardedCtx* sh, const std::vector<std::complex<double>>& kc, con
 }
 
 namespace {
+
+OzWork oz_work(ShardedCtx* sh) {
+  OzWork w;
+  w.s = sh->oz_s;
+  w.RU = sh->RU;
+  w.RX = sh->RX;
+  w.RC = sh->RC;
+  w.RC_bytes = sh->RC_bytes;
+  w.eU = sh->eU;
+  w.eU2 = sh->eU2;
+  w.eX = sh->eX;
+  w.part = sh->oz_part;
+  return w;
+}
+
+// one modular product (T = 1) on the sharded handle's scratch
+int oz_prod1(ShardedCtx* sh, int M, int N, int K, const int8_t* RA, const int* eA, int a_planes, const int8_t* RB,
+             const int* eB, int b_planes, cplx* C, long long ldc, const cplx* base, int flags, const int32_t* kdev,
+             const int32_t* ndev, std::string* err) {
+  OzProduct p;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.s = sh->oz_s;
+  p.RA = RA;
+  p.a_planes = a_planes;
+  p.eA = eA;
+  p.RB = RB;
+  p.b_planes = b_planes;
+  p.eB = eB;
+  p.RC = sh->RC;
+  p.C = C;
+  p.ldc = ldc;
+  p.base = base;
+  p.flags = flags;
+  p.kdev = kdev;
+  p.ndev = ndev;
+  if (a_planes == 4 && b_planes == 4) p.pb[2] = 3;   // C_SS: (re + im)(re - im)^T
+  return oz_product(sh->st, p, err);
+}
 
 int gather_full(ShardedCtx* sh, int which, std::string* err) {
   std::vector<void*> send;
@@ -627,10 +679,43 @@ int cqr2(ShardedCtx* sh, int src_which, std::string* err) {
       // factor I - V^dag V from the replicated V (no collective), solve on each shard's rows
       Phase p(sh->prof, sh->st, TRAJ_PH_CHOL);
       sh->sc.kc = lr;
-      STRY(struct_chol_factor(sh->st, sh->sc, sh->USrecv, sh->ldN, 0, sh->k0, sh->failed_dev, err));
-      for (auto& l : sh->loc)
-        STRY(struct_chol_apply(sh->st, sh->sc, sh->Lp, l.U[src], l.U[1 - src], sh->ldN, 0, l.Tm, sh->ldcap, 0, sh->k0,
-                               err));
+      // the solve on the INT8 modular path once k0's capacity is large (the unsharded rule); the
+      // factor chain on the high-priority stream under the solve (TRAJ_STRUCT_PIPELINE=0: serial)
+      const bool oz_apply = sh->oz && lr >= sh->oz_proj_min;
+      const bool pipe = sh->chol_overlap && sh->st_hi && !sh->struct_serial;
+      const int nblk = (int)ceil_div(sh->N, sh->sc.b);
+      if (pipe) {
+        while ((int)sh->sc_ev.size() < nblk) {
+          cudaEvent_t e;
+          SCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+          sh->sc_ev.push_back(e);
+        }
+        SCK(cudaEventRecord(sh->ev_fork, sh->st));
+        SCK(cudaStreamWaitEvent(sh->st_hi, sh->ev_fork, 0));
+      }
+      if (pipe && !oz_apply && sh->loc.size() == 1) {
+        ShardLocal& l = sh->loc[0];
+        STRY(struct_chol_pipelined(sh->st, sh->st_hi, sh->sc_ev.data(), (int)sh->sc_ev.size(), sh->sc, sh->USrecv,
+                                   sh->ldN, 0, sh->k0, sh->failed_dev, sh->Lp, l.U[src], l.U[1 - src], sh->ldN, 0,
+                                   l.Tm, sh->ldcap, 0, err));
+      } else {
+        if (pipe)
+          STRY(struct_chol_factor_events(sh->st_hi, sh->sc, sh->USrecv, sh->ldN, 0, sh->k0, sh->failed_dev,
+                                         sh->sc_ev.data(), err));
+        else
+          STRY(struct_chol_factor(sh->st, sh->sc, sh->USrecv, sh->ldN, 0, sh->k0, sh->failed_dev, err));
+        const OzWork w = oz_work(sh);
+        for (auto& l : sh->loc) {
+          if (oz_apply) {
+            STRY(struct_chol_apply_oz(sh->st, sh->sc, w, sh->Lp, l.U[src], l.U[1 - src], sh->ldN, 0, l.Tm, sh->ldcap,
+                                      0, sh->k0, pipe ? sh->sc_ev.data() : nullptr, err));
+          } else {
+            if (pipe) SCK(cudaStreamWaitEvent(sh->st, sh->sc_ev[nblk - 1], 0));
+            STRY(struct_chol_apply(sh->st, sh->sc, sh->Lp, l.U[src], l.U[1 - src], sh->ldN, 0, l.Tm, sh->ldcap, 0,
+                                   sh->k0, err));
+          }
+        }
+      }
       src = 1 - src;
       continue;
     }
@@ -876,6 +961,9 @@ int projective(ShardedCtx* sh, int which, long long step, std::string* err) {
   // C_SS = U_S U_S^dag: with an NCCL communicator each rank computes a slice of its rows and one
   // in-place allgather replicates it (the sampling and W below stay replicated); else replicated
   const int sr = (total + P - 1) / P;
+  // the rank-k products on the INT8 modular path once the click count makes them large (the
+  // unsharded rule, TRAJ_OZAKI_PROJ_MIN)
+  const bool ozp = sh->oz && total >= sh->oz_proj_min && total <= sh->N;
   const char* css = getenv("TRAJ_SHARD_CSS_SPLIT");   // =0: replicated C_SS
   if (sh->comm.comm && P > 1 && (long long)sr * P <= sh->cap && !(css && css[0] == '0')) {
     const int me = sh->comm.rank0, r0 = me * sr, nr = std::max(0, std::min(sr, total - r0));
@@ -884,6 +972,13 @@ int projective(ShardedCtx* sh, int which, long long step, std::string* err) {
                  0.0, sh->D0 + (size_t)r0 * sh->ldcap, sh->ldcap, 0, 1, 0, err));
     void* mine = sh->D0 + (size_t)r0 * sh->ldcap;
     STRY(sh->comm.allgather(st, &mine, sh->D0, (size_t)sr * sh->ldcap * 16, err));
+  } else if (ozp) {
+    // replicated C_SS on the INT8 modular path: one 4-plane row split of U_S serves both sides
+    // (P1 = re re^T, P2' = im im^T, P3 = (re + im)(re - im)^T, OZ_NEG_P2)
+    STRY(oz_split_rows(st, sh->US, sh->ldN, 0, total, sh->N, 1, 0, sh->oz_s, sh->RU, sh->eU, 0, err, nullptr, nullptr,
+                       4));
+    STRY(oz_prod1(sh, total, total, sh->N, sh->RU, sh->eU, 4, sh->RU, sh->eU, 4, sh->D0, sh->ldcap, nullptr,
+                  OZ_NEG_P2, nullptr, nullptr, err));
   } else {
     STRY(zgemm(st, 0, 1, total, total, sh->N, 1.0, 0.0, sh->US, sh->ldN, 0, sh->US, sh->ldN, 0, 0.0, sh->D0,
                sh->ldcap, 0, 1, 0, err));
@@ -914,26 +1009,66 @@ int projective(ShardedCtx* sh, int which, long long step, std::string* err) {
   STRY(gather_rows(st, sh->US, sh->ldN, 0, sh->pos1, 0, sh->k1, total, 1, sh->USrecv, sh->ldN, 0, sh->N, err, 0, 1));
   STRY(zgemm(st, 1, 0, sh->N, total, total, 1.0, 0.0, sh->USrecv, sh->ldN, 0, sh->X11, sh->ldcap, 0, 0.0, sh->W,
              sh->ldcap, 0, 1, TRAJ_TRI_B_UPPER_F, err, 0, 0, &b1));
-  for (auto& l : sh->loc) {
-    DevBounds bn;
-    bn.n = sh->k1;
-    STRY(zgemm(st, 0, 0, sh->Lp, total, sh->N, 1.0, 0.0, l.U[which], sh->ldN, 0, sh->W, sh->ldcap, 0, 0.0, l.Tm,
-               sh->ldcap, 0, 1, 0, err, 0, 0, &bn));
-    STRY(sub_identity(st, l.Tm, sh->ldcap, sh->S1, total, err, l.row0, sh->Lp, sh->k1));
-    STRY(zgemm(st, 0, 1, sh->Lp, sh->N, total, -1.0, 0.0, l.Tm, sh->ldcap, 0, sh->W, sh->ldcap, 0, 1.0, l.U[which],
-               sh->ldN, 0, 1, 0, err, 0, 0, &bk));
+  if (ozp) {
+    // per shard Tm = U_g W (columns < k1: W's columns past k1 taken as zero), then
+    // U_g <- U_g - Tm W^dag over k < k1, on the INT8 modular path; W's column residues for the
+    // first product are shared by the shards, its conjugated row residues for the second likewise
+    // (RX holds one at a time: the shards' first products, then their second ones)
+    STRY(oz_split_cols(st, sh->W, sh->ldcap, 0, sh->N, total, 1, 3, sh->oz_s, sh->RX, sh->eX, 0, sh->oz_part, err, 0,
+                       nullptr, sh->k1));
+    for (auto& l : sh->loc) {
+      STRY(oz_split_rows(st, l.U[which], sh->ldN, 0, sh->Lp, sh->N, 1, 0, sh->oz_s, sh->RU, sh->eU, 0, err));
+      STRY(oz_prod1(sh, sh->Lp, total, sh->N, sh->RU, sh->eU, 3, sh->RX, sh->eX, 3, l.Tm, sh->ldcap, nullptr, 0,
+                    nullptr, sh->k1, err));
+      STRY(sub_identity(st, l.Tm, sh->ldcap, sh->S1, total, err, l.row0, sh->Lp, sh->k1));
+    }
+    if (sh->lowrank_gram) {   // pass 1's V (below), first product: D11 = U_S0 W (replicated rows)
+      STRY(gather_rows(st, sh->US, sh->ldN, 0, sh->pos0, 0, sh->k0, total, 1, sh->USrecv, sh->ldN, 0, sh->N, err, 0,
+                       1));
+      STRY(oz_split_rows(st, sh->USrecv, sh->ldN, 0, total, sh->N, 1, 0, sh->oz_s, sh->RU, sh->eU, 0, err));
+      STRY(oz_prod1(sh, total, total, sh->N, sh->RU, sh->eU, 3, sh->RX, sh->eX, 3, sh->D11, sh->ldcap, nullptr, 0,
+                    nullptr, sh->k1, err));
+    }
+    STRY(oz_split_rows(st, sh->W, sh->ldcap, 0, sh->N, total, 1, 1, sh->oz_s, sh->RX, sh->eX, 0, err, nullptr,
+                       sh->k1));
+    for (auto& l : sh->loc) {
+      STRY(oz_split_rows(st, l.Tm, sh->ldcap, 0, sh->Lp, total, 1, 0, sh->oz_s, sh->RU, sh->eU, 0, err, nullptr,
+                         sh->k1));
+      STRY(oz_prod1(sh, sh->Lp, sh->N, total, sh->RU, sh->eU, 3, sh->RX, sh->eX, 3, l.U[which], sh->ldN, l.U[which],
+                    OZ_NEGATE, sh->k1, nullptr, err));
+    }
+    if (sh->lowrank_gram) {   // V = U_S0 - D11 W^dag
+      STRY(oz_split_rows(st, sh->D11, sh->ldcap, 0, total, total, 1, 0, sh->oz_s, sh->RU, sh->eU, 0, err, nullptr,
+                         sh->k1));
+      STRY(oz_prod1(sh, total, sh->N, total, sh->RU, sh->eU, 3, sh->RX, sh->eX, 3, sh->USrecv, sh->ldN, sh->USrecv,
+                    OZ_NEGATE, sh->k1, nullptr, err));
+    }
+  } else {
+    for (auto& l : sh->loc) {
+      DevBounds bn;
+      bn.n = sh->k1;
+      STRY(zgemm(st, 0, 0, sh->Lp, total, sh->N, 1.0, 0.0, l.U[which], sh->ldN, 0, sh->W, sh->ldcap, 0, 0.0, l.Tm,
+                 sh->ldcap, 0, 1, 0, err, 0, 0, &bn));
+      STRY(sub_identity(st, l.Tm, sh->ldcap, sh->S1, total, err, l.row0, sh->Lp, sh->k1));
+      STRY(zgemm(st, 0, 1, sh->Lp, sh->N, total, -1.0, 0.0, l.Tm, sh->ldcap, 0, sh->W, sh->ldcap, 0, 1.0, l.U[which],
+                 sh->ldN, 0, 1, 0, err, 0, 0, &bk));
+    }
   }
   for (auto& l : sh->loc) STRY(zero_rows(st, l.U[which], sh->ldN, sh->S0, total, sh->N, err, l.row0, sh->Lp, sh->k0));
   if (sh->lowrank_gram) {
     // U was orthonormal before the rows S0 were zeroed, so pass 1's Gram is I - V^dag V with V the
     // zeroed rows after the rank-k1 update: V = U_S0 - (U_S0 W) W^dag from the gathered rows (replicated)
+    // (on the modular path V was formed with the rank-k update above)
     DevBounds bn;
     bn.n = sh->k1;
-    STRY(gather_rows(st, sh->US, sh->ldN, 0, sh->pos0, 0, sh->k0, total, 1, sh->USrecv, sh->ldN, 0, sh->N, err, 0, 1));
-    STRY(zgemm(st, 0, 0, total, total, sh->N, 1.0, 0.0, sh->USrecv, sh->ldN, 0, sh->W, sh->ldcap, 0, 0.0, sh->D11,
-               sh->ldcap, 0, 1, 0, err, 0, 0, &bn));
-    STRY(zgemm(st, 0, 1, total, sh->N, total, -1.0, 0.0, sh->D11, sh->ldcap, 0, sh->W, sh->ldcap, 0, 1.0, sh->USrecv,
-               sh->ldN, 0, 1, 0, err, 0, 0, &bk));
+    if (!ozp) {
+      STRY(gather_rows(st, sh->US, sh->ldN, 0, sh->pos0, 0, sh->k0, total, 1, sh->USrecv, sh->ldN, 0, sh->N, err, 0,
+                       1));
+      STRY(zgemm(st, 0, 0, total, total, sh->N, 1.0, 0.0, sh->USrecv, sh->ldN, 0, sh->W, sh->ldcap, 0, 0.0, sh->D11,
+                 sh->ldcap, 0, 1, 0, err, 0, 0, &bn));
+      STRY(zgemm(st, 0, 1, total, sh->N, total, -1.0, 0.0, sh->D11, sh->ldcap, 0, sh->W, sh->ldcap, 0, 1.0,
+                 sh->USrecv, sh->ldN, 0, 1, 0, err, 0, 0, &bk));
+    }
     sh->lr_k0 = total;
     if (sh->struct_chol && 2LL * total <= sh->N) {   // pass 1 on the structure of I - V^dag V (V in USrecv)
       sh->struct_pending = true;
@@ -1058,6 +1193,24 @@ int propagate_dense(ShardedCtx* sh, int cur, int nxt, std::string* err) {
   const long long Lp = sh->Lp, ld = sh->ldN;
   const size_t bytes = (size_t)Lp * ld * 16;
   if (sh->oz) STRY(oz_global_exponents(sh, cur, err));
+  if (sh->oz && !sh->oz_chunked) {
+    // the gathered U's column residues once, then ONE product K_g U per shard over k = L: the P
+    // chunk products of depth Lp run the INT8 pipe ~3x below it at P = 8 (each tile's epilogue
+    // against 16 k-blocks), more than the exchange they would hide
+    if (sh->P > 1) STRY(gather_full(sh, cur, err));
+    const cplx* Uf = sh->P > 1 ? sh->Ufull : sh->loc[0].U[cur];
+    STRY(oz_split_cols_e(st, Uf, ld, 0, sh->L, sh->N, 1, 3, sh->oz_s, sh->RU, sh->eG, 0, err));
+    for (auto& l : sh->loc) {
+      OzProduct p = oz_ku(sh, l, nxt);
+      p.K = sh->L;
+      {
+        Phase pm(sh->prof, st, TRAJ_PH_KU_MMA);
+        STRY(oz_product_mma(st, p, err));
+      }
+      STRY(oz_product_combine(st, p, err));
+    }
+    return 0;
+  }
   if ((sh->planar || sh->oz) && !(sh->comm.comm && sh->overlap && sh->P > 1)) {
     // gathered first (emulation, one shard, or TRAJ_SHARD_OVERLAP=0), then the chunk products
     if (sh->P > 1) STRY(gather_full(sh, cur, err));
@@ -1307,6 +1460,9 @@ void shard_destroy(ShardedCtx* sh) {
     if (e) cudaEventDestroy(e);
   for (auto e : sh->ev_chunk)
     if (e) cudaEventDestroy(e);
+  for (auto e : sh->sc_ev)
+    if (e) cudaEventDestroy(e);
+  sh->sc_ev.clear();
   sh->fbg.destroy();
   const bool aborted = sh->comm.wd.stop();   // an aborted communicator is already freed
   if (sh->comm.comm && !aborted) ncclCommDestroy(sh->comm.comm);

@@ -135,12 +135,19 @@ struct ShardedCtx {
   // residues accumulate in RC (U_s split with the GLOBAL column exponents eG of U, from the column norms
   // summed over the shards), one CRT combine; the local Grams and TRMMs as in the unsharded step
   bool oz = false;
+  // TRAJ_SHARD_OZ_CHUNKS=1: K_g U as the P ring-ordered chunk products (residues accumulated in the
+  // epilogue, the NCCL exchange under them); default: the gathered U, one product of depth L
+  bool oz_chunked = false;
   int oz_s = 16, oz_s_corr = 10;
   int8_t *RU = nullptr, *RX = nullptr;
   uint8_t* RC = nullptr;
   size_t RC_bytes = 0;
-  int *eU = nullptr, *eX = nullptr, *eG = nullptr;
+  int *eU = nullptr, *eU2 = nullptr, *eX = nullptr, *eG = nullptr;
   double *oz_part = nullptr, *nu2 = nullptr;
+  int oz_proj_min = 1024;   // click count from which the projective rank-k products and the structured
+                            // pass 1's solve go modular (TRAJ_OZAKI_PROJ_MIN)
+  bool struct_serial = false;           // TRAJ_STRUCT_PIPELINE=0: structured factor and solve on one stream
+  std::vector<cudaEvent_t> sc_ev;       // per-block events of the pipelined structured pass 1
   cplx* dist_scratch = nullptr;
   size_t dist_scratch_bytes = 0;
   cudaStream_t cst = nullptr;

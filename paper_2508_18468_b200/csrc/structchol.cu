@@ -168,4 +168,84 @@ int struct_chol_pipelined(cudaStream_t st, cudaStream_t aux, cudaEvent_t* ev, in
   return 0;
 }
 
+// The solve dst = src R^-1 with its products on the INT8 modular path: the block-diagonal part
+// dst_c = src_c X_c from one row split of src (each block's k-range is a byte offset into the
+// residues), then per block c
+//   dst_c += A W_c   (A = sum_{d<c} dst_d Z_d^dag, Lr x k0; W_c past row k0 taken as zero)
+//   A (+)= dst_c Z_c^dag  (columns past k0 skipped)
+// with k0 bounding the INT8 launches on the device.
+int struct_chol_apply_oz(cudaStream_t st, const StructChol& s, const OzWork& w, int Lr, const cplx* src, cplx* dst,
+                         long long ldU, long long sU, cplx* A, long long ldA, long long sA, const int32_t* k0,
+                         const cudaEvent_t* ev, std::string* err) {
+  const int b = s.b, N = s.N, kc = s.kc, T = s.T, sq = w.s;
+  const int nblk = (int)ceil_div(N, b);
+  // the product scratch in two halves: outputs, and the per-block residues of A / dst_c (src's row
+  // residues stay in RU for every block's block-diagonal product)
+  const size_t half = (size_t)oz_residue_bytes(3, sq, T, Lr, std::max(kc, b));
+  // interleaved (block c's solve right after its factor block) when the scratch holds both halves;
+  // otherwise all block-diagonal products first, then the sequential part with its residues in RU
+  const bool inter = 2 * half + 256 <= w.RC_bytes;
+  uint8_t* RCo = w.RC;
+  int8_t* R2 = inter ? reinterpret_cast<int8_t*>(w.RC + (half + 255) / 256 * 256) : w.RU;
+  auto prod = [&](int M, int Nn, int K, const int8_t* RA, long long lda, const int* eA, const int8_t* RB,
+                  const int* eB, cplx* C, long long ldc, long long sC, const cplx* base, int flags, const int32_t* kdev,
+                  const int32_t* ndev) {
+    OzProduct p;
+    p.M = M;
+    p.N = Nn;
+    p.K = K;
+    p.T = T;
+    p.s = sq;
+    p.RA = RA;
+    p.a_traj = 1;
+    p.lda_override = lda;
+    p.eA = eA;
+    p.sEA = w.sEU;
+    p.RB = RB;
+    p.eB = eB;
+    p.sEB = w.sEX;
+    p.RC = RCo;
+    p.C = C;
+    p.ldc = ldc;
+    p.sC = sC;
+    p.base = base;
+    p.flags = flags;
+    p.kdev = kdev;
+    p.ndev = ndev;
+    return oz_product(st, p, err);
+  };
+  // src's row residues once; block c's k-range starts c0 bytes into each row
+  SC_TRY(oz_split_rows(st, src, ldU, sU, Lr, N, T, 0, sq, w.RU, w.eU, w.sEU, err));
+  auto diag = [&](int c) {   // dst_c = src_c X_c
+    const int c0 = c * b, bc = std::min(b, N - c0);
+    if (ev && cudaStreamWaitEvent(st, ev[c], 0) != cudaSuccess) {   // factor block c done (pipelined)
+      if (err) *err = "struct_chol_apply_oz: event wait";
+      return 4;
+    }
+    SC_TRY(oz_split_cols(st, s.Xb + (long long)c0 * b, b, s.sXb, bc, bc, T, 3, sq, w.RX, w.eX, w.sEX, w.part, err));
+    SC_TRY(prod(Lr, bc, bc, w.RU + c0, oz_ld(N), w.eU, w.RX, w.eX, dst + c0, ldU, sU, nullptr, OZ_TRI_B, nullptr,
+                nullptr));
+    return 0;
+  };
+  if (!inter)
+    for (int c = 0; c < nblk; ++c) SC_TRY(diag(c));
+  for (int c = 0; c < nblk; ++c) {
+    const int c0 = c * b, bc = std::min(b, N - c0);
+    if (inter) SC_TRY(diag(c));
+    if (c > 0) {   // dst_c += A W_c: A's rows (k < k0), W_c's columns (rows past k0 zero)
+      SC_TRY(oz_split_rows(st, A, ldA, sA, Lr, kc, T, 0, sq, R2, w.eU2, w.sEU, err, nullptr, k0));
+      SC_TRY(oz_split_cols(st, s.W + c0, s.ldWZ, s.sWZ, kc, bc, T, 3, sq, w.RX, w.eX, w.sEX, w.part, err, 0, nullptr,
+                           nullptr, k0));
+      SC_TRY(prod(Lr, bc, kc, R2, 0, w.eU2, w.RX, w.eX, dst + c0, ldU, sU, dst + c0, 0, k0, nullptr));
+    }
+    if (c + 1 < nblk) {   // A (+)= dst_c Z_c^dag: dst_c's rows, Z_c's rows conjugated (rows past k0 zero)
+      SC_TRY(oz_split_rows(st, dst + c0, ldU, sU, Lr, bc, T, 0, sq, R2, w.eU2, w.sEU, err));
+      SC_TRY(oz_split_rows(st, s.Z + c0, s.ldWZ, s.sWZ, kc, bc, T, 1, sq, w.RX, w.eX, w.sEX, err, nullptr, nullptr, 3,
+                           k0));
+      SC_TRY(prod(Lr, kc, bc, R2, 0, w.eU2, w.RX, w.eX, A, ldA, sA, c > 0 ? A : nullptr, 0, nullptr, k0));
+    }
+  }
+  return 0;
+}
+
 }  // namespace traj

@@ -8,6 +8,7 @@
 #pragma once
 #include <string>
 #include "common.cuh"
+#include "ozaki.h"
 
 namespace traj {
 
@@ -50,5 +51,13 @@ int struct_chol_pipelined(cudaStream_t st, cudaStream_t aux, cudaEvent_t* ev, in
                           long long ldV, long long sV, const int32_t* k_dev, int32_t* failed, int Lr, const cplx* src,
                           cplx* dst, long long ldU, long long sU, cplx* A, long long ldA, long long sA,
                           std::string* err);
+
+// struct_chol_apply with its products on the INT8 modular path (ozaki.h; many zeroed rows, c5: k0 ~
+// 1830): dst_c = src_c X_c from one row split of src, then per block c dst_c += A W_c and
+// A (+)= dst_c Z_c^dag (A: Lr x k0, accumulated), k_dev bounding the launches on the device.  ev
+// (optional): block c's solve waits for ev[c] (the factor on another stream, struct_chol_factor_events).
+int struct_chol_apply_oz(cudaStream_t st, const StructChol& s, const OzWork& w, int Lr, const cplx* src, cplx* dst,
+                         long long ldU, long long sU, cplx* A, long long ldA, long long sA, const int32_t* k_dev,
+                         const cudaEvent_t* ev, std::string* err);
 
 }  // namespace traj

@@ -552,83 +552,24 @@ int prod3(traj_ctx* h, int opA, long long M, long long N, long long K, const dou
                &h->err, 0, n_off);
 }
 
-// The structured pass 1's solve dst = src R^-1 (structchol.h) with its products on the INT8 modular
-// path (many zeroed rows, c5: k0 ~ 1830): the block-diagonal part dst_c = src_c X_c from one row split
-// of src (each block's k-range is a byte offset into the residues), then per block c
-//   dst_c += A W_c   (A = sum_{d<c} dst_d Z_d^dag, L x k0; W_c past row k0 taken as zero)
-//   A (+)= dst_c Z_c^dag  (columns past k0 skipped)
-// with k0 bounding the INT8 launches on the device.
+// The structured pass 1's solve with its products on the INT8 modular path (structchol.h
+// struct_chol_apply_oz) on this handle's residue scratch
 int struct_chol_apply_oz(traj_ctx* h, const StructChol& s, const cplx* src, cplx* dst, const cudaEvent_t* ev = nullptr) {
-  const int b = s.b, N = s.N, kc = s.kc, T = s.T, L = h->L, sq = h->oz_s;
-  const long long sA = (long long)L * h->ldcap;
-  cplx* A = h->Tm;
-  const int32_t* k0 = h->lr_kdev;
-  const int nblk = (int)ceil_div(N, b);
-  // the product scratch in two halves: outputs, and the per-block residues of A / dst_c (src's row
-  // residues stay in RU for every block's block-diagonal product)
-  const size_t half = (size_t)oz_residue_bytes(3, sq, T, L, std::max(kc, b));
-  // interleaved (block c's solve right after its factor block) when the scratch holds both halves;
-  // otherwise all block-diagonal products first, then the sequential part with its residues in RU
-  const bool inter = 2 * half + 256 <= h->RC_bytes;
-  uint8_t* RCo = h->RC;
-  int8_t* R2 = inter ? reinterpret_cast<int8_t*>(h->RC + (half + 255) / 256 * 256) : h->RU;
-  auto prod = [&](int M, int Nn, int K, const int8_t* RA, long long lda, const int* eA, const int8_t* RB,
-                  const int* eB, cplx* C, long long ldc, long long sC, const cplx* base, int flags, const int32_t* kdev,
-                  const int32_t* ndev) {
-    OzProduct p;
-    p.M = M;
-    p.N = Nn;
-    p.K = K;
-    p.T = T;
-    p.s = sq;
-    p.RA = RA;
-    p.a_traj = 1;
-    p.lda_override = lda;
-    p.eA = eA;
-    p.sEA = L;
-    p.RB = RB;
-    p.eB = eB;
-    p.sEB = N;
-    p.RC = RCo;
-    p.C = C;
-    p.ldc = ldc;
-    p.sC = sC;
-    p.base = base;
-    p.flags = flags;
-    p.kdev = kdev;
-    p.ndev = ndev;
-    return oz_product(h->st, p, &h->err);
-  };
-  // src's row residues once; block c's k-range starts c0 bytes into each row
-  TRY(oz_split_rows(h->st, src, h->ldN, h->sU, L, N, T, 0, sq, h->RU, h->eU, L, &h->err));
-  auto diag = [&](int c) {   // dst_c = src_c X_c
-    const int c0 = c * b, bc = std::min(b, N - c0);
-    if (ev) CK(cudaStreamWaitEvent(h->st, ev[c], 0));   // factor block c done (pipelined)
-    TRY(oz_split_cols(h->st, s.Xb + (long long)c0 * b, b, s.sXb, bc, bc, T, 3, sq, h->RX, h->eX, N, h->oz_part,
-                      &h->err));
-    TRY(prod(L, bc, bc, h->RU + c0, oz_ld(N), h->eU, h->RX, h->eX, dst + c0, h->ldN, h->sU, nullptr, OZ_TRI_B, nullptr,
-             nullptr));
-    return 0;
-  };
-  if (!inter)
-    for (int c = 0; c < nblk; ++c) TRY(diag(c));
-  for (int c = 0; c < nblk; ++c) {
-    const int c0 = c * b, bc = std::min(b, N - c0);
-    if (inter) TRY(diag(c));
-    if (c > 0) {   // dst_c += A W_c: A's rows (k < k0), W_c's columns (rows past k0 zero)
-      TRY(oz_split_rows(h->st, A, h->ldcap, sA, L, kc, T, 0, sq, R2, h->eU2, L, &h->err, nullptr, k0));
-      TRY(oz_split_cols(h->st, s.W + c0, s.ldWZ, s.sWZ, kc, bc, T, 3, sq, h->RX, h->eX, N, h->oz_part, &h->err, 0,
-                        nullptr, nullptr, k0));
-      TRY(prod(L, bc, kc, R2, 0, h->eU2, h->RX, h->eX, dst + c0, h->ldN, h->sU, dst + c0, 0, k0, nullptr));
-    }
-    if (c + 1 < nblk) {   // A (+)= dst_c Z_c^dag: dst_c's rows, Z_c's rows conjugated (rows past k0 zero)
-      TRY(oz_split_rows(h->st, dst + c0, h->ldN, h->sU, L, bc, T, 0, sq, R2, h->eU2, L, &h->err));
-      TRY(oz_split_rows(h->st, s.Z + c0, s.ldWZ, s.sWZ, kc, bc, T, 1, sq, h->RX, h->eX, N, &h->err, nullptr, nullptr, 3,
-                        k0));
-      TRY(prod(L, kc, bc, R2, 0, h->eU2, h->RX, h->eX, A, h->ldcap, sA, c > 0 ? A : nullptr, 0, nullptr, k0));
-    }
-  }
-  return 0;
+  OzWork w;
+  w.s = h->oz_s;
+  w.RU = h->RU;
+  w.RX = h->RX;
+  w.RC = h->RC;
+  w.RC_bytes = h->RC_bytes;
+  w.eU = h->eU;
+  w.eU2 = h->eU2;
+  w.eX = h->eX;
+  w.sEU = h->L;
+  w.sEX = h->N;
+  w.part = h->oz_part;
+  const int r = struct_chol_apply_oz(h->st, s, w, h->L, src, dst, h->ldN, h->sU, h->Tm, h->ldcap,
+                                     (long long)h->L * h->ldcap, h->lr_kdev, ev, &h->err);
+  return r ? fail(h, r, h->err) : 0;
 }
 
 // CholeskyQR pass 1 after a projective step on the structure of its Gram, G = I - V^dag V

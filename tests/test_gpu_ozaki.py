@@ -303,16 +303,26 @@ def test_modular_path_nan_trajectory_fails_alone(T, oz_small, protocol):
 # ---- the row-sharded step on the modular engine: K_g U as P chunk products whose
 # ---- residues accumulate over the chunks at U's global column exponents, local modular Grams / TRMMs
 
-@pytest.mark.parametrize("L,P_shards,protocol,gam", [(480, 2, "projective", 2.0), (480, 3, "homodyne", 1.0),
-                                                     (512, 4, "projective", 0.7), (512, 8, "homodyne", 2.0),
-                                                     (512, 8, "projective", 3.0)])
-def test_row_sharded_modular_step_matches_oracle_and_dmma(T, oz_small, monkeypatch, L, P_shards, protocol, gam):
+@pytest.mark.parametrize("L,P_shards,protocol,gam,variant", [
+    (480, 2, "projective", 2.0, "one_product"), (480, 3, "homodyne", 1.0, "chunks"),
+    (512, 4, "projective", 0.7, "chunks"), (512, 8, "homodyne", 2.0, "one_product"),
+    (512, 8, "projective", 3.0, "one_product"), (512, 2, "projective", 3.0, "serial_structured")])
+def test_row_sharded_modular_step_matches_oracle_and_dmma(T, oz_small, monkeypatch, L, P_shards, protocol, gam,
+                                                          variant):
     """Single-GPU emulation of P shards (Lp = 240, 160, 128, 64 rows: ragged against the 128-row tiles)
-    on the modular path, the same trajectory on the sharded DMMA kernels (TRAJ_OZAKI=0) and the oracle:
-    identical clicks, C within 1e-12 of the DMMA step and 1e-10 of the oracle, S_A within 1e-8."""
+    on the modular path -- K_g U as one depth-L product of the gathered U's residues, or (chunks) as
+    the P ring-ordered chunk products accumulated in the residue epilogue; the projective C_SS, rank-k
+    update and structured pass-1 solve modular too (threshold lowered), the structured factor
+    pipelined or (serial_structured) not -- against the same trajectory on the sharded DMMA kernels
+    (TRAJ_OZAKI=0) and the oracle: identical clicks, C within 1e-12 of the DMMA step and 1e-10 of the
+    oracle, S_A within 1e-8."""
     import paper_2508_18468_b200 as P
     from oracle import lattice
     from oracle.trajectory import OracleTrajectory
+    if variant == "chunks":
+        monkeypatch.setenv("TRAJ_SHARD_OZ_CHUNKS", "1")
+    if variant == "serial_structured":
+        monkeypatch.setenv("TRAJ_STRUCT_PIPELINE", "0")
     a = P.Trajectories(L, 1, protocol, [gam], seed=23, traj_base=1, shard_size=P_shards)
     assert a.ozaki_info() == (True, True, 16)
     monkeypatch.setenv("TRAJ_OZAKI", "0")
