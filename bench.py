@@ -370,7 +370,8 @@ def run_ours(args):
         "library_same_shape": library,
         "hbm_kernels": hbm or None,
         "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
-        "phases_nested": {"ku_mma": "propagate", "gram_mma": "gram", "trmm_mma": "trmm"},
+        "phases_nested": {"ku_mma": "propagate", "gram_mma": "gram", "trmm_mma": "trmm",
+                          "struct_factor": "chol"},
         "phase_launches_per_step": {k: v[1] / args.steps for k, v in phases.items()},
         "gpu_launches": launches,
         "sampled_observables_ms": obs,

@@ -236,7 +236,10 @@ enum { TRAJ_PH_PROPAGATE = 0,  /* U <- K U                                   */
        /* nested (not additive): the INT8 tensor-core launch of the modular products inside the
         * propagate, Gram and TRMM phases (traj_ozaki_info) */
        TRAJ_PH_KU_MMA = 7, TRAJ_PH_GRAM_MMA = 8, TRAJ_PH_TRMM_MMA = 9,
-       TRAJ_NPHASES = 10 };
+       /* nested in chol: the structured pass 1's factor chain (on the stream it runs on; not recorded
+        * when factor and solve are interleaved on the DMMA path) */
+       TRAJ_PH_STRUCT_FACTOR = 10,
+       TRAJ_NPHASES = 11 };
 int traj_profile(traj_handle h, int enable);
 /* Which contractions of this handle run as exact modular products on the INT8 tensor cores
  * (csrc/ozaki.h; environment TRAJ_OZAKI=0 selects the FP64 DMMA kernels instead):

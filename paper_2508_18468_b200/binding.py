@@ -21,8 +21,10 @@ TRAJ_INIT_NEEL = 0
 TRAJ_INIT_CHECKERBOARD = 1
 TRAJ_PROP_DENSE, TRAJ_PROP_BANDED = 0, 1
 TRAJ_TRI_A_UPPER, TRAJ_TRI_A_LOWER, TRAJ_TRI_B_UPPER, TRAJ_TRI_B_LOWER, TRAJ_C_UPPER = 1, 2, 4, 8, 16
-PHASES = ("propagate", "monitor", "project", "gram", "chol", "trmm", "fused", "ku_mma", "gram_mma", "trmm_mma")
-NESTED_PHASES = ("ku_mma", "gram_mma", "trmm_mma")   # inside propagate / gram / trmm: not additive
+PHASES = ("propagate", "monitor", "project", "gram", "chol", "trmm", "fused", "ku_mma", "gram_mma", "trmm_mma",
+          "struct_factor")
+# inside propagate / gram / trmm / chol: not additive
+NESTED_PHASES = ("ku_mma", "gram_mma", "trmm_mma", "struct_factor")
 STATUS = {0: "TRAJ_OK", 1: "TRAJ_EINVAL", 2: "TRAJ_ECONFIG", 3: "TRAJ_ENUMERIC", 4: "TRAJ_ECUDA",
           5: "TRAJ_ENCCL", 6: "TRAJ_EDOMAIN"}
 

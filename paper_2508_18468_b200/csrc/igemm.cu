@@ -87,6 +87,7 @@ struct KArgs {
   const int32_t* kdev;
   const int32_t* ndev;
   int ksplit, kcb;   // k chunks, k-blocks per chunk
+  int barrett_kb;    // tiles of at most this many k-blocks reduce mod m in integer arithmetic (ModRed)
 };
 
 // batch entry z -> (A entry, B entry, modulus index)
@@ -141,6 +142,60 @@ __device__ __forceinline__ int tile_kblocks(const KArgs& a, const Tile& t, int* 
   if (kb0) *kb0 = b0;
   return max(0, min(nkb, b0 + a.kcb) - b0);
 }
+
+// x mod m (m <= 256) of an exact int32 accumulator (|x| <= K 2^14 < 2^30 for K <= 65536) by Barrett
+// reduction on u = x + k0 (k0 the least multiple of m >= 2^30, so 0 <= u < 2^32): q = hi32(u floor(2^32 / m))
+// is floor(u / m) or one less, r = u - q m in [0, 2m), one conditional subtract (as min(r, r - m) in
+// unsigned arithmetic).  Integer multiply-adds only: the FP64 floor it replaces ran three conversions
+// per value, which bounded the epilogue of short-K tiles.
+// The FP64 form (x - m floor(x / m)) is kept for deep tiles (more than barrett_kb k-blocks, e.g. the
+// K U product), whose epilogue hides under the MMAs anyway: measured, the integer form there costs
+// ~3% of the INT8 rate (c3 K U 59.5 -> 61.7 ms), the power of the extra ALU work under a power-limited
+// tensor pipe.
+struct ModRed {
+  uint32_t m = 1, magic = 0, k0 = 0;
+  double inv = 0.0;
+  bool barrett = true;
+  __device__ __forceinline__ void set(int mod, bool use_barrett) {
+    m = (uint32_t)mod;
+    magic = (uint32_t)(0x100000000ull / (unsigned long long)mod);
+    k0 = m * ((0x40000000u + m - 1) / m);
+    inv = 1.0 / (double)mod;
+    barrett = use_barrett;
+  }
+  __device__ __forceinline__ uint32_t operator()(int x) const {
+    const uint32_t u = (uint32_t)x + k0;
+    const uint32_t r = u - __umulhi(u, magic) * m;
+    return min(r, r - m);
+  }
+  // 32 accumulators -> 32 residue bytes packed four per word
+  __device__ __forceinline__ void pack32(const uint32_t* v, uint32_t* w) const {
+    if (barrett) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        uint32_t packed = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) packed |= (*this)((int)v[4 * j + b]) << (8 * b);
+        w[j] = packed;
+      }
+    } else {
+      const int mi = (int)m;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        uint32_t packed = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int x = (int)v[4 * j + b];
+          int r = x - mi * (int)floor((double)x * inv);
+          r += (r < 0) ? mi : 0;
+          r -= (r >= mi) ? mi : 0;
+          packed |= (uint32_t)r << (8 * b);
+        }
+        w[j] = packed;
+      }
+    }
+  }
+};
 
 __global__ void __launch_bounds__(ITHREADS, 1)
     igemm_i8_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const KArgs a) {
@@ -252,12 +307,12 @@ __global__ void __launch_bounds__(ITHREADS, 1)
       const bool kzero = tile_kblocks(a, tl) == 0;   // empty contraction: the accumulator was never written
       const uint32_t taddr = tmem + buf * IBN + ((uint32_t)(q * 32) << 16);
       int mod = 0;
-      double inv = 0.0;
+      ModRed red;
       if (a.out != IG_OUT_I32) {
         int za, zb, q;
         zmap(a, tl.z, za, zb, q);
         mod = a.moduli[q];
-        inv = 1.0 / (double)mod;
+        red.set(mod, tile_kblocks(a, tl) <= a.barrett_kb);
       }
 #pragma unroll 1
       for (int c = 0; c < IBN / 32; ++c) {
@@ -282,19 +337,7 @@ __global__ void __launch_bounds__(ITHREADS, 1)
           }
         } else {
           uint32_t w[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            uint32_t packed = 0;
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-              int x = (int)v[4 * j + b];
-              int r = x - mod * (int)floor((double)x * inv);
-              r += (r < 0) ? mod : 0;
-              r -= (r >= mod) ? mod : 0;
-              packed |= (uint32_t)r << (8 * b);
-            }
-            w[j] = packed;
-          }
+          red.pack32(v, w);
           uint8_t* p = reinterpret_cast<uint8_t*>(a.C) + ((long long)tl.z * a.ksplit + tl.kc) * a.strideC +
                        (long long)row * a.ldc + col;
           if (a.out == IG_OUT_MOD_ACC) {   // add the residues already there (< m each), reduce once more
@@ -532,12 +575,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ITHREADS, 1)
       const bool kzero = tile_kblocks(a, tl) == 0;
       const uint32_t taddr = tmem + buf * PBN + ((uint32_t)(q * 32) << 16);
       int mod = 0;
-      double inv = 0.0;
+      ModRed red;
       if (a.out == IG_OUT_MOD) {
         int za, zb, qq;
         zmap(a, tl.z, za, zb, qq);
         mod = a.moduli[qq];
-        inv = 1.0 / (double)mod;
+        red.set(mod, tile_kblocks(a, tl) <= a.barrett_kb);
       }
 #pragma unroll 1
       for (int c = 0; c < PBN / 32; ++c) {
@@ -562,19 +605,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ITHREADS, 1)
           }
         } else {
           uint32_t w[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            uint32_t packed = 0;
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-              const int x = (int)v[4 * j + b];
-              int r = x - mod * (int)floor((double)x * inv);
-              r += (r < 0) ? mod : 0;
-              r -= (r >= mod) ? mod : 0;
-              packed |= (uint32_t)r << (8 * b);
-            }
-            w[j] = packed;
-          }
+          red.pack32(v, w);
           uint8_t* p = reinterpret_cast<uint8_t*>(a.C) + ((long long)tl.z * a.ksplit + tl.kc) * a.strideC +
                        (long long)row * a.ldc + col;
           if (col + 32 <= a.N) {
@@ -745,12 +776,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ITHREADS, 1)
       const bool kzero = tile_kblocks(a, tl) == 0;
       const uint32_t taddr = tmem + buf * IBN + ((uint32_t)(q * 32) << 16);
       int mod = 0;
-      double inv = 0.0;
+      ModRed red;
       if (a.out == IG_OUT_MOD) {
         int za, zb, qq;
         zmap(a, tl.z, za, zb, qq);
         mod = a.moduli[qq];
-        inv = 1.0 / (double)mod;
+        red.set(mod, tile_kblocks(a, tl) <= a.barrett_kb);
       }
 #pragma unroll 1
       for (int c = 0; c < IBN / 32; ++c) {
@@ -775,19 +806,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ITHREADS, 1)
           }
         } else {
           uint32_t w[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            uint32_t packed = 0;
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-              const int x = (int)v[4 * j + b];
-              int r = x - mod * (int)floor((double)x * inv);
-              r += (r < 0) ? mod : 0;
-              r -= (r >= mod) ? mod : 0;
-              packed |= (uint32_t)r << (8 * b);
-            }
-            w[j] = packed;
-          }
+          red.pack32(v, w);
           uint8_t* p = reinterpret_cast<uint8_t*>(a.C) + ((long long)tl.z * a.ksplit + tl.kc) * a.strideC +
                        (long long)row * a.ldc + col;
           if (col + 32 <= a.N) {
@@ -924,6 +943,12 @@ int igemm(cudaStream_t st, const IgemmArgs& g, std::string* err) {
       gm_env = v ? std::max(1, atoi(v)) : 0;
     }
     a.gm = gm_env ? gm_env : IGM;
+    static int bk_env = -2;
+    if (bk_env == -2) {
+      const char* v = getenv("TRAJ_IGEMM_BARRETT_KB");
+      bk_env = v ? atoi(v) : -1;
+    }
+    a.barrett_kb = bk_env >= 0 ? bk_env : 64;
   }
   a.oz_s = g.oz_s;
   a.oz_T = g.oz_T;

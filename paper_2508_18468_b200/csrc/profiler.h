@@ -7,7 +7,7 @@
 
 namespace traj {
 
-constexpr int NPHASES = 10;
+constexpr int NPHASES = 11;
 
 struct Profiler {
   bool on = false;

@@ -699,11 +699,14 @@ int cqr2(ShardedCtx* sh, int src_which, std::string* err) {
                                    sh->ldN, 0, sh->k0, sh->failed_dev, sh->Lp, l.U[src], l.U[1 - src], sh->ldN, 0,
                                    l.Tm, sh->ldcap, 0, err));
       } else {
-        if (pipe)
-          STRY(struct_chol_factor_events(sh->st_hi, sh->sc, sh->USrecv, sh->ldN, 0, sh->k0, sh->failed_dev,
-                                         sh->sc_ev.data(), err));
-        else
-          STRY(struct_chol_factor(sh->st, sh->sc, sh->USrecv, sh->ldN, 0, sh->k0, sh->failed_dev, err));
+        {
+          Phase pf(sh->prof, pipe ? sh->st_hi : sh->st, TRAJ_PH_STRUCT_FACTOR);
+          if (pipe)
+            STRY(struct_chol_factor_events(sh->st_hi, sh->sc, sh->USrecv, sh->ldN, 0, sh->k0, sh->failed_dev,
+                                           sh->sc_ev.data(), err));
+          else
+            STRY(struct_chol_factor(sh->st, sh->sc, sh->USrecv, sh->ldN, 0, sh->k0, sh->failed_dev, err));
+        }
         const OzWork w = oz_work(sh);
         for (auto& l : sh->loc) {
           if (oz_apply) {

@@ -605,8 +605,11 @@ int structured_pass1(traj_ctx* h, const cplx* src, cplx* dst, int kc) {
     }
     CK(cudaEventRecord(h->ev_fork, h->st));
     CK(cudaStreamWaitEvent(h->st_hi, h->ev_fork, 0));
-    TRY(struct_chol_factor_events(h->st_hi, s, h->US, h->ldN, h->sUS, h->lr_kdev, h->failed_dev, h->sc_ev.data(),
-                                  &h->err));
+    {
+      Phase pf(&h->prof, h->st_hi, TRAJ_PH_STRUCT_FACTOR);
+      TRY(struct_chol_factor_events(h->st_hi, s, h->US, h->ldN, h->sUS, h->lr_kdev, h->failed_dev, h->sc_ev.data(),
+                                    &h->err));
+    }
     return struct_chol_apply_oz(h, s, src, dst, h->sc_ev.data());
   }
   if (!oz_apply && h->chol_overlap && h->st_hi && !h->struct_serial) {
@@ -625,7 +628,10 @@ int structured_pass1(traj_ctx* h, const cplx* src, cplx* dst, int kc) {
                ? fail(h, TRAJ_ECUDA, h->err)
                : 0;
   }
-  TRY(struct_chol_factor(h->st, s, h->US, h->ldN, h->sUS, h->lr_kdev, h->failed_dev, &h->err));
+  {
+    Phase pf(&h->prof, h->st, TRAJ_PH_STRUCT_FACTOR);
+    TRY(struct_chol_factor(h->st, s, h->US, h->ldN, h->sUS, h->lr_kdev, h->failed_dev, &h->err));
+  }
   if (oz_apply) return struct_chol_apply_oz(h, s, src, dst);
   return struct_chol_apply(h->st, s, h->L, src, dst, h->ldN, h->sU, h->Tm, h->ldcap, (long long)h->L * h->ldcap,
                            h->lr_kdev, &h->err);
