@@ -26,6 +26,14 @@ constexpr int SW_ROW = IGEMM_BK;                       // swizzle span = one row
 constexpr uint32_t SW_LAYOUT = IGEMM_BK == 128 ? 2 : 4;  // SWIZZLE_128B / SWIZZLE_64B descriptor codes
 constexpr int IA_BYTES = IBM * IBK, IB_BYTES = IBN * IBK, ISTAGE_BYTES = IA_BYTES + IB_BYTES;
 constexpr int ITHREADS = 192;
+// the unpaired kernel: IEPI epilogue warps, two per TMEM lane quarter, each taking half of the tile's
+// 256 accumulator columns -- the epilogue of a shallow tile (few k-blocks) is a serial chain of TMEM
+// loads, reductions and stores that the MMAs of the next tile no longer hide with one warp per quarter
+#ifndef IGEMM_EPI_WARPS
+#define IGEMM_EPI_WARPS 8
+#endif
+constexpr int IEPI = IGEMM_EPI_WARPS;
+constexpr int IMAIN_THREADS = 64 + 32 * IEPI;
 constexpr int ISMEM = ISTAGES * ISTAGE_BYTES + 1024 + 256;
 // raster: tiles are taken in groups of `gm` m-blocks (m fastest) so that a wave of CTAs shares A and B
 // slabs through L2 (TRAJ_IGEMM_GM overrides the default for experiments)
@@ -160,8 +168,8 @@ struct ModRed {
     m = (uint32_t)mod;
     magic = (uint32_t)(0x100000000ull / (unsigned long long)mod);
     k0 = m * ((0x40000000u + m - 1) / m);
-    inv = 1.0 / (double)mod;
     barrett = use_barrett;
+    if (!barrett) inv = 1.0 / (double)mod;
   }
   __device__ __forceinline__ uint32_t operator()(int x) const {
     const uint32_t u = (uint32_t)x + k0;
@@ -197,7 +205,7 @@ struct ModRed {
   }
 };
 
-__global__ void __launch_bounds__(ITHREADS, 1)
+__global__ void __launch_bounds__(IMAIN_THREADS, 1)
     igemm_i8_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const KArgs a) {
   if (a.gate && *a.gate == 0) return;   // uniform over the grid: no TMEM allocated, no barrier used
   extern __shared__ uint8_t smem_raw[];
@@ -217,7 +225,7 @@ __global__ void __launch_bounds__(ITHREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);
+      mbar_init(&tempty[b], IEPI);
     }
     fence_mbar_init();
     prefetch_tmap(&ta);
@@ -292,8 +300,10 @@ __global__ void __launch_bounds__(ITHREADS, 1)
       __syncwarp();
       ++it;
     }
-  } else {   // ---------------- epilogue: warps 2..5
+  } else {   // ---------------- epilogue: warps 2 .. 2 + IEPI - 1
     const int q = warp & 3;
+    constexpr int CPW = (IBN / 32) * 4 / IEPI;   // 32-column chunks per warp
+    const int c_lo = ((warp - 2) >> 2) * CPW;
     int it = 0;
     for (long long t = blockIdx.x; t < a.tiles; t += gridDim.x) {
       const Tile tl = tile_of(a, t);
@@ -315,7 +325,7 @@ __global__ void __launch_bounds__(ITHREADS, 1)
         red.set(mod, tile_kblocks(a, tl) <= a.barrett_kb);
       }
 #pragma unroll 1
-      for (int c = 0; c < IBN / 32; ++c) {
+      for (int c = c_lo; c < c_lo + CPW; ++c) {
         uint32_t v[32];
         __syncwarp();
         tmem_ld32(taddr + c * 32, v);
@@ -333,7 +343,9 @@ __global__ void __launch_bounds__(ITHREADS, 1)
             for (int j = 0; j < 8; ++j)
               reinterpret_cast<int4*>(p)[j] = make_int4((int)v[4 * j], (int)v[4 * j + 1], (int)v[4 * j + 2], (int)v[4 * j + 3]);
           } else {
-            for (int j = 0; col + j < a.N; ++j) p[j] = (int)v[j];
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col + j < a.N) p[j] = (int)v[j];
           }
         } else {
           uint32_t w[8];
@@ -348,7 +360,9 @@ __global__ void __launch_bounds__(ITHREADS, 1)
               old[4] = o1.x; old[5] = o1.y; old[6] = o1.z; old[7] = o1.w;
             } else {
               for (int jj = 0; jj < 8; ++jj) old[jj] = 0;
-              for (int jj = 0; col + jj < a.N; ++jj) old[jj >> 2] |= (uint32_t)p[jj] << (8 * (jj & 3));
+#pragma unroll
+              for (int jj = 0; jj < 32; ++jj)
+                if (col + jj < a.N) old[jj >> 2] |= (uint32_t)p[jj] << (8 * (jj & 3));
             }
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
@@ -366,7 +380,9 @@ __global__ void __launch_bounds__(ITHREADS, 1)
             reinterpret_cast<uint4*>(p)[0] = make_uint4(w[0], w[1], w[2], w[3]);
             reinterpret_cast<uint4*>(p)[1] = make_uint4(w[4], w[5], w[6], w[7]);
           } else {
-            for (int j = 0; col + j < a.N; ++j) p[j] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col + j < a.N) p[j] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
           }
         }
       }
@@ -601,7 +617,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ITHREADS, 1)
             for (int j = 0; j < 8; ++j)
               reinterpret_cast<int4*>(p)[j] = make_int4((int)v[4 * j], (int)v[4 * j + 1], (int)v[4 * j + 2], (int)v[4 * j + 3]);
           } else {
-            for (int j = 0; col + j < a.N; ++j) p[j] = (int)v[j];
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col + j < a.N) p[j] = (int)v[j];
           }
         } else {
           uint32_t w[8];
@@ -612,7 +630,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ITHREADS, 1)
             reinterpret_cast<uint4*>(p)[0] = make_uint4(w[0], w[1], w[2], w[3]);
             reinterpret_cast<uint4*>(p)[1] = make_uint4(w[4], w[5], w[6], w[7]);
           } else {
-            for (int j = 0; col + j < a.N; ++j) p[j] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col + j < a.N) p[j] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
           }
         }
       }
@@ -802,7 +822,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ITHREADS, 1)
             for (int j = 0; j < 8; ++j)
               reinterpret_cast<int4*>(p)[j] = make_int4((int)v[4 * j], (int)v[4 * j + 1], (int)v[4 * j + 2], (int)v[4 * j + 3]);
           } else {
-            for (int j = 0; col + j < a.N; ++j) p[j] = (int)v[j];
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col + j < a.N) p[j] = (int)v[j];
           }
         } else {
           uint32_t w[8];
@@ -813,7 +835,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(ITHREADS, 1)
             reinterpret_cast<uint4*>(p)[0] = make_uint4(w[0], w[1], w[2], w[3]);
             reinterpret_cast<uint4*>(p)[1] = make_uint4(w[4], w[5], w[6], w[7]);
           } else {
-            for (int j = 0; col + j < a.N; ++j) p[j] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col + j < a.N) p[j] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
           }
         }
       }
@@ -1000,7 +1024,7 @@ int igemm(cudaStream_t st, const IgemmArgs& g, std::string* err) {
     return 4;
   }
   const long long grid = std::min<long long>(a.tiles, num_sms());
-  igemm_i8_kernel<<<(unsigned)grid, ITHREADS, ISMEM, st>>>(ma, mb, a);
+  igemm_i8_kernel<<<(unsigned)grid, IMAIN_THREADS, ISMEM, st>>>(ma, mb, a);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

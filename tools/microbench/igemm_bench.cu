@@ -136,6 +136,10 @@ int main(int argc, char** argv) {
     timeit_rand(16384, 8192, 16384, 48);
     return 0;
   }
+  if (argc > 5 && std::string(argv[1]) == "shape") {   // shape M N K batch (random operands, modular epilogue)
+    timeit_rand(atoll(argv[2]), atoll(argv[3]), atoll(argv[4]), atoi(argv[5]));
+    return 0;
+  }
   int bad = 0;
   bad |= check(300, 520, 1000, 2, IG_OUT_I32, 0);
   bad |= check(128, 256, 128, 1, IG_OUT_I32, 0);
