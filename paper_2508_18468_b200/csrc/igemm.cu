@@ -966,7 +966,9 @@ int igemm(cudaStream_t st, const IgemmArgs& g, std::string* err) {
       const char* v = getenv("TRAJ_IGEMM_GM");
       gm_env = v ? std::max(1, atoi(v)) : 0;
     }
-    a.gm = gm_env ? gm_env : IGM;
+    // the upper-triangular (Gram) products: one group, column-major over all M-tiles (measured c3
+    // Gram 19.3 -> 17.4 ms; the K U product keeps groups of IGM: 58.3 vs 62.0 ms with one group)
+    a.gm = gm_env ? gm_env : ((g.flags & IG_UPPER) ? std::max(1, a.tiles_m) : IGM);
     static int bk_env = -2;
     if (bk_env == -2) {
       const char* v = getenv("TRAJ_IGEMM_BARRETT_KB");
