@@ -916,15 +916,17 @@ int igemm(cudaStream_t st, const IgemmArgs& g, std::string* err) {
     if (err) *err = "igemm: modular batch map needs batch = 3 s T and the modular epilogue";
     return 1;
   }
-  // the CTA-pair kernel from 256 rows on (TRAJ_IGEMM_PAIR=0: always the unpaired one)
-  static int pair_env = -1;
-  if (pair_env < 0) {
-    // off by default: on the step's operands (K's residues banded) the pair kernel's wave misses L2 far
-    // more often (420 vs 98 GB of DRAM, profiles/r02/igemm_pair_vs_single.txt) and runs slower
+  // the CTA-pair kernel from 256 rows on.  Default (TRAJ_IGEMM_PAIR unset): paired for the triangular
+  // products (IG_UPPER Grams, IG_TRI_B TRMMs: c3 Gram launch 17.2 -> 15.2 ms, TRMM 9.7 -> 8.1 ms), unpaired
+  // for the dense ones -- on K U the pair kernel's wave misses L2 far more often (420 vs 98 GB of DRAM,
+  // profiles/r02/igemm_pair_vs_single.txt; 56.0 -> 58.3 ms).  TRAJ_IGEMM_PAIR=1 / 0: always / never.
+  static int pair_env = -2;
+  if (pair_env == -2) {
     const char* v = getenv("TRAJ_IGEMM_PAIR");
-    pair_env = (v && v[0] == '1') ? 1 : 0;
+    pair_env = !v || !v[0] ? -1 : (v[0] == '1' ? 1 : 0);
   }
-  const bool use_pair = pair_env && g.M >= 256 && num_sms() >= 2 && g.out != IG_OUT_MOD_ACC;
+  const bool pair_wanted = pair_env == 1 || (pair_env == -1 && (g.flags & (IG_UPPER | IG_TRI_B)) != 0);
+  const bool use_pair = pair_wanted && g.M >= 256 && num_sms() >= 2 && g.out != IG_OUT_MOD_ACC;
   static int mc_env = -1;
   if (mc_env < 0) {
     const char* v = getenv("TRAJ_IGEMM_MC");

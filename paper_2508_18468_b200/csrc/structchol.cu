@@ -71,19 +71,201 @@ int factor_init(cudaStream_t st, StructChol& s, std::string* err) {
   return axpby_identity(st, s.M, s.ldM, s.sM, s.kc, s.T, 1.0, 1.0, err);
 }
 
+// S_c = I - sum_{d<c} H_d on the k0 x k0 block (identity elsewhere), upper triangle, for c < nblk:
+// one thread per (i, j), the prefix over c sequential in registers (H_d = V_d V_d^dag in H, d < nblk - 1)
+__global__ void struct_prefix_kernel(const cplx* __restrict__ H, cplx* __restrict__ S, long long ld, long long sS,
+                                     int kc, int nblk, const int32_t* __restrict__ k_dev) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= kc || j >= kc || i > j) return;
+  const int k0 = k_dev ? *k_dev : kc;
+  const bool in = i < k0 && j < k0;
+  const double d = i == j ? 1.0 : 0.0;
+  double re = 0.0, im = 0.0;
+  const long long o = (long long)i * ld + j;
+  for (int c = 0; c < nblk; ++c) {
+    S[c * sS + o] = make_double2(in ? d - re : d, in ? -im : 0.0);
+    if (c + 1 < nblk) {
+      const cplx h = H[c * sS + o];
+      re += h.x;
+      im += h.y;
+    }
+  }
+}
+
+// E_d <- sum_{d' <= d} E_d' for d < n, on the Lr x k0 block of each (the columns past k0 are never read)
+__global__ void struct_prefix_rows_kernel(cplx* __restrict__ E, long long ld, long long sE, int Lr, int kc, int n,
+                                          const int32_t* __restrict__ k_dev) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const long long i = blockIdx.y;
+  const int k0 = k_dev ? *k_dev : kc;
+  if (j >= k0 || i >= Lr) return;
+  cplx* p = E + i * ld + j;
+  double re = 0.0, im = 0.0;
+  for (int d = 0; d < n; ++d) {
+    const cplx e = p[d * sE];
+    re += e.x;
+    im += e.y;
+    p[d * sE] = make_double2(re, im);
+  }
+}
+
+// failed[0] = 1 if any of the n flags is set
+__global__ void struct_or_flags_kernel(int32_t* failed, const int32_t* __restrict__ f, int n) {
+  int any = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) any |= f[i];
+  any = __syncthreads_or(any);
+  if (threadIdx.x == 0 && any && failed) *failed = 1;
+}
+
 }  // namespace
 
 int struct_chol_factor(cudaStream_t st, StructChol& s, const cplx* V, long long ldV, long long sV,
                        const int32_t* k_dev, int32_t* failed, std::string* err) {
+  if (s.Sb) return struct_chol_factor_batched(st, s, V, ldV, sV, k_dev, failed, err);
   SC_TRY(factor_init(st, s, err));
   const int nblk = (int)ceil_div(s.N, s.b);
   for (int c = 0; c < nblk; ++c) SC_TRY(factor_block(st, s, V, ldV, sV, k_dev, failed, err, c));
   return 0;
 }
 
+int struct_chol_factor_batched(cudaStream_t st, StructChol& s, const cplx* V, long long ldV, long long sV,
+                               const int32_t* k_dev, int32_t* failed, std::string* err) {
+  const int b = s.b, N = s.N, kc = s.kc, T = s.T;
+  const int nblk = (int)ceil_div(N, b), nfull = N / b;
+  const int ct = N - nfull * b;   // the ragged last block's width (0: none)
+  const long long bb = (long long)b * b, sQ = (long long)kc * b;
+  s.Vsrc = V;
+  s.ldVsrc = ldV;
+  s.sVsrc = sV;
+  for (int t = 0; t < T; ++t) {
+    const cplx* Vt = V + t * sV;
+    cplx* Xt = s.Xb + t * s.sXb;
+    cplx* Wt = s.W + t * s.sWZ;
+    cplx* Zt = s.Z + t * s.sWZ;
+    DevBounds bmn, bk, bm;   // this trajectory's k0 for every batch entry (the blocks)
+    bmn.m = bmn.n = k_dev + t;
+    bmn.per_batch = 0;
+    bk.k = k_dev + t;
+    bk.per_batch = 0;
+    bm.m = k_dev + t;
+    bm.per_batch = 0;
+    // H_d = V_d V_d^dag (upper tiles of the k0 x k0 block), d < nblk - 1 (all full blocks)
+    if (nblk > 1)
+      SC_TRY(zgemm(st, 0, 1, kc, kc, b, 1.0, 0.0, Vt, ldV, b, Vt, ldV, b, 0.0, s.XMb, s.ldS, s.sS, nblk - 1,
+                   TRAJ_C_UPPER_F, err, 0, 0, &bmn));
+    {
+      const dim3 blk(32, 8), grd((unsigned)ceil_div(kc, 32), (unsigned)ceil_div(kc, 8));
+      struct_prefix_kernel<<<grd, blk, 0, st>>>(s.XMb, s.Sb, s.ldS, s.sS, kc, nblk, k_dev + t);
+    }
+    if (cudaMemsetAsync(s.bfail, 0, (size_t)2 * nblk * 4, st) != cudaSuccess) {
+      if (err) *err = "struct_chol_factor_batched: memset";
+      return 4;
+    }
+    // X_S,c = R_S,c^-1 (S_0 = I gives X_S,0 = I)
+    SC_TRY(chol_inverse(st, kc, s.Sb, s.ldS, s.sS, s.XMb, s.ldS, s.sS, nblk, s.bscratch, s.bfail, err));
+    // Q_c = X_S,c^dag V_c (lower-triangular op(A); rows past k0 come out zero)
+    if (nfull > 0)
+      SC_TRY(zgemm(st, 1, 0, kc, b, kc, 1.0, 0.0, s.XMb, s.ldS, s.sS, Vt, ldV, b, 0.0, s.Qb, b, sQ, nfull,
+                   TRAJ_TRI_A_LOWER_F, err, 0, 0, &bk));
+    if (ct)
+      SC_TRY(zgemm(st, 1, 0, kc, ct, kc, 1.0, 0.0, s.XMb + nfull * s.sS, s.ldS, 0, Vt + (long long)nfull * b, ldV, 0,
+                   0.0, s.Qb + nfull * sQ, b, 0, 1, TRAJ_TRI_A_LOWER_F, err, 0, 0, &bk));
+    // C_c = I - Q_c^dag Q_c (upper), X_c = R_c^-1 into the blocks of Xb
+    SC_TRY(set_identity(st, s.Cb, b, bb, b, nblk, err));
+    if (nfull > 0) {
+      SC_TRY(zgemm(st, 1, 0, b, b, kc, -1.0, 0.0, s.Qb, b, sQ, s.Qb, b, sQ, 1.0, s.Cb, b, bb, nfull, TRAJ_C_UPPER_F,
+                   err, 0, 0, &bk));
+      SC_TRY(chol_inverse(st, b, s.Cb, b, bb, Xt, b, bb, nfull, s.bscratch, s.bfail + nblk, err));
+    }
+    if (ct) {
+      SC_TRY(zgemm(st, 1, 0, ct, ct, kc, -1.0, 0.0, s.Qb + nfull * sQ, b, 0, s.Qb + nfull * sQ, b, 0, 1.0,
+                   s.Cb + nfull * bb, b, 0, 1, TRAJ_C_UPPER_F, err, 0, 0, &bk));
+      SC_TRY(chol_inverse(st, ct, s.Cb + nfull * bb, b, 0, Xt + nfull * bb, b, 0, 1, s.bscratch,
+                          s.bfail + nblk + nfull, err));
+    }
+    // W_c = V_c X_c (rows < k0), T1_c = Q_c X_c (into Sb), Z_c = X_S,c T1_c
+    auto block_products = [&](int c_first, int count, int w) -> int {
+      const long long c0 = (long long)c_first * b;
+      const long long sx = count > 1 ? bb : 0, sv = count > 1 ? b : 0, sq = count > 1 ? sQ : 0,
+                      ss = count > 1 ? s.sS : 0;
+      SC_TRY(zgemm(st, 0, 0, kc, w, w, 1.0, 0.0, Vt + c0, ldV, sv, Xt + c_first * bb, b, sx, 0.0, Wt + c0, s.ldWZ, sv,
+                   count, TRAJ_TRI_B_UPPER_F, err, 0, 0, &bm));
+      SC_TRY(zgemm(st, 0, 0, kc, w, w, 1.0, 0.0, s.Qb + c_first * sQ, b, sq, Xt + c_first * bb, b, sx, 0.0,
+                   s.Sb + c_first * s.sS, b, ss, count, TRAJ_TRI_B_UPPER_F, err));
+      SC_TRY(zgemm(st, 0, 0, kc, w, kc, 1.0, 0.0, s.XMb + c_first * s.sS, s.ldS, ss, s.Sb + c_first * s.sS, b, ss,
+                   0.0, Zt + c0, s.ldWZ, sv, count, TRAJ_TRI_A_UPPER_F, err, 0, 0, &bk));
+      return 0;
+    };
+    if (nfull > 0) SC_TRY(block_products(0, nfull, b));
+    if (ct) SC_TRY(block_products(nfull, 1, ct));
+    struct_or_flags_kernel<<<1, 256, 0, st>>>(failed ? failed + t : nullptr, s.bfail, 2 * nblk);
+    if (cudaGetLastError() != cudaSuccess) {
+      if (err) *err = "struct_chol_factor_batched: launch";
+      return 4;
+    }
+  }
+  return 0;
+}
+
+// dst = src R^-1 without the chain over blocks (structchol.h Eb).  The chain's accumulator obeys
+// A_{c+1} = A_c F_c + src_c X_c Z_c^dag with F_c = I + W_c Z_c^dag = M_c^-1 M_{c+1}, so
+// A_c = sum_{d<c} src_d X_d Z_d^dag S_{d+1} M_c, and X_d Z_d^dag S_{d+1} = X_d W_d^dag (I - M_d V_d V_d^dag)
+// = X_d (X_d^dag V_d^dag - (X_d^dag - R_d) V_d^dag) = X_d R_d V_d^dag = V_d^dag (C_d = R_d^dag R_d =
+// I - V_d^dag M_d V_d).  Hence A_c = P_c M_c with P_c = sum_{d<c} src_d V_d^dag, and A_c W_c = P_c Z_c.
+int struct_chol_apply_batched(cudaStream_t st, const StructChol& s, int Lr, const cplx* src, cplx* dst,
+                              long long ldU, long long sU, const int32_t* k_dev, std::string* err) {
+  const int b = s.b, N = s.N, kc = s.kc, T = s.T;
+  const int nblk = (int)ceil_div(N, b), nfull = N / b;
+  for (int t = 0; t < T; ++t) {
+    const cplx* st_src = src + t * sU;
+    cplx* st_dst = dst + t * sU;
+    const cplx* Vt = s.Vsrc + t * s.sVsrc;
+    const cplx* Xt = s.Xb + t * s.sXb;
+    const cplx* Zt = s.Z + t * s.sWZ;
+    DevBounds bn, bk;
+    bn.n = k_dev + t;
+    bn.per_batch = 0;
+    bk.k = k_dev + t;
+    bk.per_batch = 0;
+    // dst_c = src_c X_c for every block (the full ones batched, then the tail)
+    if (nfull > 0)
+      SC_TRY(zgemm(st, 0, 0, Lr, b, b, 1.0, 0.0, st_src, ldU, b, Xt, b, (long long)b * b, 0.0, st_dst, ldU, b, nfull,
+                   TRAJ_TRI_B_UPPER_F, err));
+    if (nfull < nblk) {
+      const int c0 = nfull * b, bc = N - c0;
+      SC_TRY(zgemm(st, 0, 0, Lr, bc, bc, 1.0, 0.0, st_src + c0, ldU, 0, Xt + (long long)c0 * b, b, 0, 0.0,
+                   st_dst + c0, ldU, 0, 1, TRAJ_TRI_B_UPPER_F, err));
+    }
+    if (nblk < 2) continue;
+    // E_d = src_d V_d^dag (d < nblk - 1: full blocks), then P_{d+1} = E_0 + ... + E_d in place
+    SC_TRY(zgemm(st, 0, 1, Lr, kc, b, 1.0, 0.0, st_src, ldU, b, Vt, s.ldVsrc, b, 0.0, s.Eb, s.ldE, s.sE, nblk - 1, 0,
+                 err, 0, 0, &bn));
+    {
+      const dim3 grd((unsigned)ceil_div(kc, 128), (unsigned)Lr);
+      struct_prefix_rows_kernel<<<grd, 128, 0, st>>>(s.Eb, s.ldE, s.sE, Lr, kc, nblk - 1, k_dev + t);
+      if (cudaGetLastError() != cudaSuccess) {
+        if (err) *err = "struct_chol_apply_batched: launch";
+        return 4;
+      }
+    }
+    // dst_c += P_c Z_c, c >= 1 (reduction over the k0 columns of P_c)
+    const int nf1 = nfull - 1;   // full blocks among c >= 1
+    if (nf1 > 0)
+      SC_TRY(zgemm(st, 0, 0, Lr, b, kc, 1.0, 0.0, s.Eb, s.ldE, s.sE, Zt + b, s.ldWZ, b, 1.0, st_dst + b, ldU, b, nf1,
+                   0, err, 0, 0, &bk));
+    if (nfull < nblk) {
+      const int c = nfull, c0 = c * b, bc = N - c0;
+      SC_TRY(zgemm(st, 0, 0, Lr, bc, kc, 1.0, 0.0, s.Eb + (c - 1) * s.sE, s.ldE, 0, Zt + c0, s.ldWZ, 0, 1.0,
+                   st_dst + c0, ldU, 0, 1, 0, err, 0, 0, &bk));
+    }
+  }
+  return 0;
+}
+
 int struct_chol_apply(cudaStream_t st, const StructChol& s, int Lr, const cplx* src, cplx* dst, long long ldU,
                       long long sU, cplx* A, long long ldA, long long sA, const int32_t* k_dev, std::string* err) {
   const int b = s.b, N = s.N, kc = s.kc, T = s.T;
+  if (s.Eb) return struct_chol_apply_batched(st, s, Lr, src, dst, ldU, sU, k_dev, err);
   DevBounds bk, bn;  // reductions over / outputs of the k0 columns of A
   bk.k = k_dev;
   bn.n = k_dev;
@@ -114,10 +296,11 @@ int struct_chol_apply(cudaStream_t st, const StructChol& s, int Lr, const cplx* 
 
 int struct_chol_factor_events(cudaStream_t st, StructChol& s, const cplx* V, long long ldV, long long sV,
                               const int32_t* k_dev, int32_t* failed, cudaEvent_t* ev, std::string* err) {
-  SC_TRY(factor_init(st, s, err));
   const int nblk = (int)ceil_div(s.N, s.b);
+  if (s.Sb) SC_TRY(struct_chol_factor_batched(st, s, V, ldV, sV, k_dev, failed, err));
+  else SC_TRY(factor_init(st, s, err));
   for (int c = 0; c < nblk; ++c) {
-    SC_TRY(factor_block(st, s, V, ldV, sV, k_dev, failed, err, c));
+    if (!s.Sb) SC_TRY(factor_block(st, s, V, ldV, sV, k_dev, failed, err, c));
     if (cudaEventRecord(ev[c], st) != cudaSuccess) {
       if (err) *err = "struct_chol_factor_events: event record";
       return 4;
@@ -137,9 +320,10 @@ int struct_chol_pipelined(cudaStream_t st, cudaStream_t aux, cudaEvent_t* ev, in
     return 1;
   }
   // the factor chain on aux, an event after each block
-  SC_TRY(factor_init(aux, s, err));
+  if (s.Sb) SC_TRY(struct_chol_factor_batched(aux, s, V, ldV, sV, k_dev, failed, err));
+  else SC_TRY(factor_init(aux, s, err));
   for (int c = 0; c < nblk; ++c) {
-    SC_TRY(factor_block(aux, s, V, ldV, sV, k_dev, failed, err, c));
+    if (!s.Sb) SC_TRY(factor_block(aux, s, V, ldV, sV, k_dev, failed, err, c));
     if (cudaEventRecord(ev[c], aux) != cudaSuccess) {
       if (err) *err = "struct_chol_pipelined: event record";
       return 4;

@@ -26,12 +26,39 @@ struct StructChol {
   cplx *W = nullptr, *Z = nullptr;      // [T][kc][ldWZ] W = V_c R_c^-1, Z = M W by column blocks
   long long ldWZ = 0, sWZ = 0;
   void* chol_scratch = nullptr;         // chol_scratch_bytes(b, T)
+  // the batched factor (struct_chol_factor_batched; null Sb: the sequential chain).  Per trajectory,
+  // for every block c of the nblk = ceil(N / b) column blocks at once:
+  cplx* Sb = nullptr;                   // [nblk][kc][ldS]  S_c = I - sum_{d<c} V_d V_d^dag, then Q_c X_c ([kc][b])
+  cplx* XMb = nullptr;                  // [nblk][kc][ldS]  the block Grams V_d V_d^dag, then R_S,c^-1
+  long long ldS = 0, sS = 0;            // ldS >= kc, sS >= kc max(ldS, b)
+  cplx* Qb = nullptr;                   // [nblk][kc][b]    Q_c = R_S,c^-dag V_c
+  cplx* Cb = nullptr;                   // [nblk][b][b]     I - Q_c^dag Q_c
+  void* bscratch = nullptr;             // max(chol_scratch_bytes(kc, nblk), chol_scratch_bytes(b, nblk))
+  int32_t* bfail = nullptr;             // [2 nblk] the batched factorisations' pivot flags
+  // the batched solve (struct_chol_apply when Eb is set): the accumulator of the chain,
+  // A_c = sum_{d<c} dst_d Z_d^dag, equals P_c M_c with P_c = sum_{d<c} src_d V_d^dag (push-through
+  // identity, structchol.cu), so dst_c = src_c X_c + P_c Z_c with every P_c a prefix sum of the blocks'
+  // src_d V_d^dag -- no product waits for another block's dst
+  cplx* Eb = nullptr;                   // [nblk - 1][Lr][ldE]  src_d V_d^dag, then the prefix sums P_{d+1}
+  long long ldE = 0, sE = 0;
+  const cplx* Vsrc = nullptr;           // V as passed to the factor (recorded by struct_chol_factor_batched)
+  long long ldVsrc = 0, sVsrc = 0;
 };
 
 // From V ([T][kc rows][ldV], rows past k_dev[t] zero): the blocks' R_c^-1, W and Z.  failed[t] is set
 // on a non-positive pivot (as the dense factorisation would).
 int struct_chol_factor(cudaStream_t st, StructChol& s, const cplx* V, long long ldV, long long sV,
                        const int32_t* k_dev, int32_t* failed, std::string* err);
+
+// The same blocks without the sequential chain over c (used by every entry point when s.Sb is set).
+// The chain's M before block c is M_c = (I - sum_{d<c} V_d V_d^dag)^-1 (each step of the chain is the
+// Woodbury update of this inverse), so with S_c = I - sum_{d<c} V_d V_d^dag = R_S^dag R_S, X_S = R_S^-1
+// (M_c = X_S X_S^dag) and Q_c = X_S^dag V_c:
+//   C_c = I - V_c^dag M_c V_c = I - Q_c^dag Q_c,  X_c = chol_inv(C_c),  W_c = V_c X_c,  Z_c = M_c W_c = X_S (Q_c X_c)
+// -- every block is independent: one batched launch per product over the nblk blocks (plus the
+// ragged last block), two batched factorisations, instead of ~8 dependent launches per block.
+int struct_chol_factor_batched(cudaStream_t st, StructChol& s, const cplx* V, long long ldV, long long sV,
+                               const int32_t* k_dev, int32_t* failed, std::string* err);
 
 // dst = src R^-1 for Lr rows of U ([T][Lr][ldU], batch stride sU); A: [T][Lr][ldA] scratch (the
 // L x k0 accumulator), ldA >= kc.

@@ -160,6 +160,12 @@ struct traj_ctx {
   int sb = 128;                          // column block of the structured factorisation
   cplx *sY = nullptr, *sC = nullptr, *sX = nullptr, *sW = nullptr, *sZ = nullptr;
   void* s_chol_scratch = nullptr;
+  bool struct_batched = true;            // the batched structured factor (structchol.h)
+  cplx *sSb = nullptr, *sXMb = nullptr, *sQb = nullptr, *sCb = nullptr;
+  long long sbS = 0, sEs = 0;
+  cplx* sEb = nullptr;
+  void* s_bscratch = nullptr;
+  int32_t* s_bfail = nullptr;
   cplx* kcoef = nullptr;
   int32_t* sites = nullptr;
   cusolverDnHandle_t solver = nullptr;
@@ -476,6 +482,25 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
       lay.take(h->sW, (size_t)T * cap * ldN * 16);
       lay.take(h->sZ, (size_t)T * cap * ldN * 16);
       lay.take(h->s_chol_scratch, chol_scratch_bytes(b, T));
+      // the batched factor (struct_chol_factor_batched; TRAJ_STRUCT_BATCHED=0: the sequential chain)
+      const char* sbat = getenv("TRAJ_STRUCT_BATCHED");
+      h->struct_batched = !(sbat && sbat[0] == '0');
+      // (DMMA solve only: with the modular solve (c5) the sequential chain pipelines each factor block
+      // under the solve on two streams, measured faster than the batched factor followed by the solve)
+      if (h->struct_batched && !(h->oz_cqr && cap >= h->oz_proj_min)) {
+        const long long nblk = ceil_div(N, b);
+        if (nblk > 1) {   // the batched solve's prefix sums
+          h->sEs = (long long)L * ldcap;
+          lay.take(h->sEb, (size_t)(nblk - 1) * h->sEs * 16);
+        }
+        h->sbS = (long long)cap * std::max<long long>(ldcap, b);
+        lay.take(h->sSb, (size_t)nblk * h->sbS * 16);
+        lay.take(h->sXMb, (size_t)nblk * h->sbS * 16);
+        lay.take(h->sQb, (size_t)nblk * cap * b * 16);
+        lay.take(h->sCb, (size_t)nblk * b * b * 16);
+        lay.take(h->s_bscratch, std::max(chol_scratch_bytes(cap, nblk), chol_scratch_bytes(b, nblk)));
+        lay.take(h->s_bfail, (size_t)2 * nblk * 4);
+      }
     }
   }
   return lay.off + 256;
@@ -595,6 +620,28 @@ int structured_pass1(traj_ctx* h, const cplx* src, cplx* dst, int kc) {
   s.sWZ = h->sUS;
   s.chol_scratch = h->s_chol_scratch;
   const bool oz_apply = h->oz_cqr && kc >= h->oz_proj_min;
+  if (h->sSb && !oz_apply) {
+    // every block at once (structchol.h): the batched factor, then the batched solve on this stream
+    s.Sb = h->sSb;
+    s.XMb = h->sXMb;
+    s.ldS = h->ldcap;
+    s.sS = h->sbS;
+    s.Qb = h->sQb;
+    s.Cb = h->sCb;
+    s.bscratch = h->s_bscratch;
+    s.bfail = h->s_bfail;
+    s.Eb = h->sEb;
+    s.ldE = h->ldcap;
+    s.sE = h->sEs;
+    {
+      Phase pf(&h->prof, h->st, TRAJ_PH_STRUCT_FACTOR);
+      TRY(struct_chol_factor_batched(h->st, s, h->US, h->ldN, h->sUS, h->lr_kdev, h->failed_dev, &h->err));
+    }
+    return struct_chol_apply(h->st, s, h->L, src, dst, h->ldN, h->sU, h->Tm, h->ldcap, (long long)h->L * h->ldcap,
+                             h->lr_kdev, &h->err)
+               ? fail(h, TRAJ_ECUDA, h->err)
+               : 0;
+  }
   if (oz_apply && h->chol_overlap && h->st_hi && !h->struct_serial) {
     // the factor chain on the high-priority stream; the modular solve waits per block
     const int nblk = (int)ceil_div(h->N, h->sb);

@@ -30,7 +30,8 @@ def dev(T, a):
 
 @pytest.mark.parametrize("M,N,K,batch,mod,flags", [(300, 520, 1000, 2, False, 0), (128, 256, 128, 1, False, 0),
                                                    (300, 520, 1000, 3, True, 0), (700, 700, 700, 1, False, 1),
-                                                   (400, 700, 700, 1, False, 2), (1, 33, 16, 1, True, 0)])
+                                                   (400, 700, 700, 1, False, 2), (1, 33, 16, 1, True, 0),
+                                                   (600, 600, 2100, 2, True, 1), (520, 600, 600, 3, True, 2)])
 def test_igemm_exact(T, M, N, K, batch, mod, flags):
     import paper_2508_18468_b200 as P
     rng = np.random.default_rng(M * 7 + N + K)

@@ -296,15 +296,18 @@ def test_row_sharded_strassen_chunks_match_oracle(P, monkeypatch, levels, shards
         assert a.last_clicks(0) == b.last_clicks(0) == (o.last_clicks[0].size, int(o.last_clicks[1].sum()))
 
 
-@pytest.mark.parametrize("block,shards", [(128, 1), (64, 1), (64, 2)])
-def test_structured_pass1_matches_dense_factorisation(P, monkeypatch, block, shards):
+@pytest.mark.parametrize("block,shards,batched", [(128, 1, "1"), (64, 1, "1"), (64, 2, "1"), (48, 1, "1"),
+                                                  (64, 1, "0"), (64, 2, "0")])
+def test_structured_pass1_matches_dense_factorisation(P, monkeypatch, block, shards, batched):
     """CholeskyQR pass 1 of a projective step on the structure of G = I - V^dag V (csrc/structchol.cu):
     the same orthonormalised state as the dense Gram / Cholesky / TRMM pass (1e-12) and the oracle
     (1e-10), batched trajectories with different click counts, column blocks with a ragged tail
-    (N = 350), and through the row-sharded emulation."""
+    (N = 350), and through the row-sharded emulation; both the batched factor (every block from its
+    own S_c = I - sum_{d<c} V_d V_d^dag) and the sequential Woodbury chain (TRAJ_STRUCT_BATCHED=0)."""
     L, steps = 700, 12
     gams = [1.5, 0.8] if shards == 1 else [1.5]
     monkeypatch.setenv("TRAJ_STRUCT_B", str(block))
+    monkeypatch.setenv("TRAJ_STRUCT_BATCHED", batched)
     a = P.Trajectories(L, 1, "projective", gams, seed=21, shard_size=shards)
     monkeypatch.setenv("TRAJ_STRUCT_CHOL", "0")
     b = P.Trajectories(L, 1, "projective", gams, seed=21, shard_size=shards)
