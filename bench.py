@@ -102,6 +102,7 @@ def workload(args):
 
 
 L2_BYTES = 126e6
+OZ_NP = 2   # real INT8 residue products per complex product and modulus (csrc/ozaki.h: the planes re +- j im)
 
 
 def resolve_mode(args, w, world: int) -> str:
@@ -405,7 +406,9 @@ def dtype_of(oz):
     if oz and (oz[0] or oz[1]):
         parts = [x for x, on in (("K U", oz[0]), ("the CholeskyQR Grams / TRMMs", oz[1])) if on]
         return (f"c128 (FP64 values; {' and '.join(parts)} as exact modular products on the INT8 tensor cores, "
-                f"{oz[2]} moduli = 61-bit operand rows/columns, CRT to FP64; the rest FP64 on DMMA / FP64 pipes)")
+                f"{oz[2]} moduli with a square root of -1 each = two real residue products per complex product and "
+                f"{ {16: 57, 18: 61}.get(oz[2], '?') }-bit operand rows/columns, CRT to FP64; the rest FP64 on DMMA / FP64 "
+                "pipes)")
     return "c128 (f64 arithmetic)"
 
 
@@ -516,16 +519,16 @@ def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P, oz=(False, Fal
                               "algorithmic")) if traffic else None}
     oz_dom = (oz[0] and dom == "propagate") or (oz[1] and dom in ("gram", "trmm"))
     if oz_dom:
-        # the dominant phase is an exact modular product (csrc/ozaki.h): 3 s INT8 products per complex
-        # product (3M in the residues, s moduli); algorithmic INT8 ops (2 per MAC) over the nested
+        # the dominant phase is an exact modular product (csrc/ozaki.h): 2 s INT8 products per complex
+        # product (the two planes re +- j im of each of the s moduli); algorithmic INT8 ops (2 per MAC) over the nested
         # phase that times the INT8 tensor-core launch alone; its phase time adds the residue
         # splits and the CRT combine
         s_ = oz[2]
         mma_ph = {"propagate": "ku_mma", "gram": "gram_mma", "trmm": "trmm_mma"}[dom]
         mma_ms = phases[mma_ph][0] / args.steps
-        per = {"propagate": 2.0 * 3 * s_ * rows * w.L * w.N * tpg,
-               "gram": n_gram * 2.0 * 3 * s_ * (w.N * w.N / 2.0) * rows * tpg,
-               "trmm": n_trmm * 2.0 * 3 * s_ * rows * (w.N * w.N / 2.0) * tpg}[dom]
+        per = {"propagate": 2.0 * OZ_NP * s_ * rows * w.L * w.N * tpg,
+               "gram": n_gram * 2.0 * OZ_NP * s_ * (w.N * w.N / 2.0) * rows * tpg,
+               "trmm": n_trmm * 2.0 * OZ_NP * s_ * rows * (w.N * w.N / 2.0) * tpg}[dom]
         tops = per / (mma_ms / 1e3) / 1e12
         eqp = flops8 / (kern_ms / 1e3) / 1e12
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -538,7 +541,7 @@ def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P, oz=(False, Fal
         roof = {"bound": "tensor", "achieved": tops, "peak": INT8_PEAK_TOPS, "unit": "TOPS (INT8)",
                 "frac": tops / INT8_PEAK_TOPS, "traffic": traffic,
                 "kernel": ("igemm_i8_kernel (tcgen05.mma.kind::i8, TMEM accumulators, TMA 128B-swizzled K-major "
-                           f"tiles, 128x256x128 CTA tile, persistent): one launch of the 3 x {s_} residue products "
+                           f"tiles, 128x256x128 CTA tile, persistent): one launch of the {OZ_NP} x {s_} residue products "
                            + {"propagate": "of U <- K U (K's residues formed once)",
                               "gram": "of G = U^dag U (upper tiles)",
                               "trmm": "of U <- U R^-1 (triangular k-blocks skipped)"}[dom]
@@ -547,7 +550,7 @@ def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P, oz=(False, Fal
                               else "; per shard (L/P rows)" if shard else "")),
                 "kernel_ms": mma_ms, "timed": ("device time of the INT8 launch per step (CUDA events around it on "
                                                 "the handle's stream, nested phase " + mma_ph + ")"),
-                "ops_counted": (f"2 x 3 x {s_} x (the complex product's m n k; half for the Gram's and TRMM's "
+                "ops_counted": (f"2 x {OZ_NP} x {s_} x (the complex product's m n k; half for the Gram's and TRMM's "
                                 "triangles) INT8 multiply-adds: algorithmic, tile waste not counted"),
                 "peak_source": INT8_PEAK_SOURCE,
                 "phase_ms": kern_ms, "phase_note": "the phase adds U's residue split and the CRT combine",
@@ -583,13 +586,13 @@ def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P, oz=(False, Fal
             and w.protocol in ("projective", "homodyne"):
         # phases on the INT8 modular path leave the DMMA sum: their INT8 ops are counted apart
         int8_ph = ({"propagate"} if oz[0] else set()) | ({"gram", "trmm"} if oz[1] else set())
-        i8 = sum(3 * oz[2] * 2.0 * (step8[k][0] / 8.0) for k in int8_ph)   # 8mnk / 8 = complex MACs
+        i8 = sum(OZ_NP * oz[2] * 2.0 * (step8[k][0] / 8.0) for k in int8_ph)   # 8mnk / 8 = complex MACs
         fl = sum(f * a for k, (f, a) in step8.items() if k not in int8_ph) * tpg
         i8 *= tpg
         t = ms / args.steps / 1e3
         executed = {"tflops": fl / t / 1e12, "frac": fl / t / 1e12 / FP64_PEAK_TFLOPS, "flops_per_step": fl,
                     "engine_note": ("tflops / frac: DMMA (FP64 tensor pipe) flops of the phases still on it, over the "
-                                    "whole step time" + ("; int8_*: the modular products' INT8 ops (2 x 3 s per "
+                                    "whole step time" + ("; int8_*: the modular products' INT8 ops (2 x 2 s per "
                                                          "complex m n k) over the whole step time" if int8_ph else "")),
                     "int8_phases": sorted(int8_ph),
                     "int8_ops_per_step": i8 or None, "int8_tops": (i8 / t / 1e12) if i8 else None,
@@ -700,11 +703,11 @@ def run_secondary(args, world, rank, P, steps=2, warmup=2):
         # the modular INT8 K U (csrc/ozaki.h): the INT8 launch alone against the INT8 peak
         oz_s = int(os.environ.get("TRAJ_OZAKI_MODULI", "16"))
         mma = ph["ku_mma"][0] / steps
-        tops = 2.0 * 3 * oz_s * rows * w.L * w.N / (mma / 1e3) / 1e12
+        tops = 2.0 * OZ_NP * oz_s * rows * w.L * w.N / (mma / 1e3) / 1e12
         eq8 = 8.0 * rows * w.L * w.N / (prop / 1e3) / 1e12
         out["roofline_propagate"] = {"bound": "tensor", "achieved": tops, "peak": INT8_PEAK_TOPS, "unit": "TOPS (INT8)",
                                      "frac": tops / INT8_PEAK_TOPS, "kernel_ms": mma, "phase_ms": prop,
-                                     "kernel": f"igemm_i8_kernel: the 3 x {oz_s} residue products of K U",
+                                     "kernel": f"igemm_i8_kernel: the {OZ_NP} x {oz_s} residue products of K U",
                                      "fp64_equiv_tflops": eq8, "fp64_equiv_frac_of_dmma_peak": eq8 / FP64_PEAK_TFLOPS,
                                      "peak_source": INT8_PEAK_SOURCE}
         oz = (True, True, oz_s)

@@ -244,7 +244,7 @@ int traj_profile(traj_handle h, int enable);
 /* Which contractions of this handle run as exact modular products on the INT8 tensor cores
  * (csrc/ozaki.h; environment TRAJ_OZAKI=0 selects the FP64 DMMA kernels instead):
  * out[0] = the dense K U, out[1] = the CholeskyQR Grams and TRMMs, out[2] = the modulus count
- * (16: every operand row / column to 2^-62 of its 2-norm).  Row-sharded handles: out[0] = out[1] =
+ * (16: every operand row / column to 2^-58 of its 2-norm).  Row-sharded handles: out[0] = out[1] =
  * the chunked K_g U (its residues accumulated over the P chunks at U's global column exponents) and
  * the local Grams / TRMMs; the projective rank-k products and the structured pass stay on DMMA. */
 int traj_ozaki_info(traj_handle h, int32_t* out3);
@@ -334,20 +334,24 @@ int traj_igemm(void* stream, int64_t M, int64_t N, int64_t K, const void* A, int
 /* traj_zgemm_ozaki: C = op(A) B in complex128 (row-major, ld in complex elements), computed by the
  * exact modular scheme on the INT8 tensor cores (csrc/ozaki.h: Ozaki-II; the contraction the paper
  * states as a complex-FP64 matrix product).  opA = 0: A is M x K; opA = 1: A is stored
- * K x M and op(A) = A^dag (the Gram form U^dag U).  B is K x N.  nmod in {4, 6, ..., 16} pairwise
- * coprime moduli: every row of op(A) and column of B is represented to 2^-(beta+1) of its 2-norm,
- * beta = 61 for 16 (finer than FP64 for the entries that carry the norm), and the products are
- * exact.  flags: TRAJ_C_UPPER (only j >= i written), TRAJ_TRI_B_UPPER (B upper triangular).  The
+ * K x M and op(A) = A^dag (the Gram form U^dag U).  B is K x N.  nmod in {4, 6, ..., 18} pairwise
+ * coprime moduli, each with a square root of -1 (so a complex product mod m is two real ones): every
+ * row of op(A) and column of B is represented to 2^-(beta+1) of its 2-norm, beta = 57 for 16 and 61
+ * for 18, and the products are exact (an FP64 GEMM's rounding errors are 2^-53 of the same norms).  flags: TRAJ_C_UPPER (only j >= i written), TRAJ_TRI_B_UPPER (B upper triangular).  The
  * residue scratch is allocated and freed on the stream (cudaMallocAsync); TRAJ_EINVAL on a bad
  * shape. */
 int traj_zgemm_ozaki(void* stream, int opA, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                      const void* B, int64_t ldb, void* C, int64_t ldc, int nmod, int flags);
 
 /* The host-side constants of the modular scheme for nmod moduli (no device needed; for tests):
- * moduli[nmod] (pairwise coprime, <= 256), *beta (operand bits: every row / column is scaled below
- * 2^beta), ch[nmod/2], cl[nmod/2] (the CRT weights of the moduli pairs: X / M = frac(sum_p r_p (ch_p +
- * cl_p)), ch_p a multiple of 2^-36), *M (prod m as a double).  TRAJ_EINVAL for an unsupported nmod. */
+ * moduli[nmod] (odd, pairwise coprime, <= 256, prime factors = 1 mod 4), *beta (operand bits: every
+ * row / column is scaled below 2^beta), ch[nmod/2], cl[nmod/2] (the CRT weights of the moduli pairs:
+ * X / M = frac(sum_p r_p (ch_p + cl_p)), ch_p a multiple of 2^-36), *M (prod m as a double).
+ * TRAJ_EINVAL for an unsupported nmod. */
 int traj_ozaki_constants(int nmod, int32_t* moduli, int32_t* beta, double* ch, double* cl, double* M);
+/* roots[q]^2 = -1 (mod moduli[q]): the image j_q of the imaginary unit in Z_m, which splits a complex
+ * residue into the two real planes re +- j_q im (csrc/ozaki.h). */
+int traj_ozaki_roots(int nmod, int32_t* roots);
 
 /* traj_chol_inverse: for each b, G_b (n x n Hermitian positive definite; only the
  * upper triangle is read) = R^dag R with R upper triangular; writes X_b = R^-1

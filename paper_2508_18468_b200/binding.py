@@ -103,6 +103,7 @@ _SIGS = {
                                         ctypes.c_int]),
     "traj_ozaki_constants": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                             ctypes.POINTER(_D), ctypes.POINTER(_D), ctypes.POINTER(_D)]),
+    "traj_ozaki_roots": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int32)]),
     "traj_shard_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                        ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "traj_nccl_unique_id": (ctypes.c_int, [_P]),

@@ -912,8 +912,8 @@ int igemm(cudaStream_t st, const IgemmArgs& g, std::string* err) {
   }
   const long long na = g.oz_s ? g.oz_na : g.batch / g.a_div, nb = g.oz_s ? g.oz_nb : g.batch / g.b_div;
   const bool ab = g.strideA != 0 && na > 1, bb = g.strideB != 0 && nb > 1;
-  if (g.oz_s && (g.batch != 3LL * g.oz_s * g.oz_T || g.oz_T < 1 || !g.moduli || g.out == IG_OUT_I32)) {
-    if (err) *err = "igemm: modular batch map needs batch = 3 s T and the modular epilogue";
+  if (g.oz_s && (g.oz_np < 1 || g.oz_np > 3 || g.batch != (long long)g.oz_np * g.oz_s * g.oz_T || g.oz_T < 1 || !g.moduli || g.out == IG_OUT_I32)) {
+    if (err) *err = "igemm: modular batch map needs batch = np s T (np <= 3) and the modular epilogue";
     return 1;
   }
   // the CTA-pair kernel from 256 rows on.  Default (TRAJ_IGEMM_PAIR unset): paired for the triangular

@@ -38,6 +38,7 @@ struct IgemmArgs {
   // oz_T when oz_a_traj, else 1 and t dropped), B_z likewise; the epilogue's modulus is moduli[q].
   // a_div / b_div / nmod are ignored; oz_na / oz_nb = the number of matrices in the A / B buffers.
   int oz_s = 0, oz_T = 1;
+  int oz_np = 3;                    // products per modulus (batch = oz_np oz_s oz_T)
   int oz_pa[3] = {0, 1, 2}, oz_pb[3] = {0, 1, 2};
   int oz_a_traj = 0, oz_b_traj = 1;
   long long oz_na = 0, oz_nb = 0;

@@ -9,12 +9,21 @@
 namespace traj {
 namespace {
 
-// pairwise coprime moduli <= 256 (the first s are used); residues are stored in [-128, 127]
+// pairwise coprime odd moduli <= 256 (the first s are used) whose prime factors are all = 1 (mod 4), so
+// that -1 is a square mod each of them (221 = 13 17, 205 = 5 41, the rest prime); residues are stored
+// in [-128, 127]
 __host__ __device__ constexpr int OZM(int q) {
-  return q == 0 ? 256 : q == 1 ? 255 : q == 2 ? 253 : q == 3 ? 251 : q == 4 ? 247 : q == 5 ? 241 : q == 6 ? 239
-       : q == 7 ? 233 : q == 8 ? 229 : q == 9 ? 227 : q == 10 ? 223 : q == 11 ? 217 : q == 12 ? 211
-       : q == 13 ? 199 : q == 14 ? 197 : 193;
+  return q == 0 ? 241 : q == 1 ? 233 : q == 2 ? 229 : q == 3 ? 221 : q == 4 ? 205 : q == 5 ? 197 : q == 6 ? 193
+       : q == 7 ? 181 : q == 8 ? 173 : q == 9 ? 157 : q == 10 ? 149 : q == 11 ? 137 : q == 12 ? 113
+       : q == 13 ? 109 : q == 14 ? 101 : q == 15 ? 97 : q == 16 ? 89 : 73;
 }
+// the smallest j with j^2 = -1 (mod m)
+__host__ __device__ constexpr int sqrt_minus_one(int m) {
+  for (int x = 1; x < m; ++x)
+    if (x * x % m == m - 1) return x;
+  return 0;
+}
+__host__ __device__ constexpr int OZJ(int q) { return sqrt_minus_one(OZM(q)); }
 __host__ __device__ constexpr int pow2mod(int e, int m) {
   int r = 1 % m;
   for (int i = 0; i < e; ++i) r = (r * 2) % m;
@@ -34,21 +43,31 @@ struct HostConst {
   double M[OZ_MAXS + 1] = {};
   int beta[OZ_MAXS + 1] = {};
   HostConst() {
-    typedef unsigned __int128 u128;
     for (int s = 1; s <= OZ_MAXS; ++s) {
-      u128 Mp = 1;
-      for (int q = 0; q < s; ++q) Mp *= (u128)OZM(q);
-      // double of M and floor(log2(M))
-      M[s] = (double)(uint64_t)(Mp >> 64) * 18446744073709551616.0 + (double)(uint64_t)Mp;
+      // M as a double (the product in 64-bit-mantissa long double, rounded once) and floor(log2(M))
+      long double Ml = 1.0L;
+      for (int q = 0; q < s; ++q) Ml *= (long double)OZM(q);
+      M[s] = (double)Ml;
       int lg = 0;
-      for (u128 x = Mp; x > 1; x >>= 1) ++lg;
-      beta[s] = lg / 2 - 1;
+      {
+        long double x = Ml;
+        while (x >= 2.0L) {
+          x *= 0.5L;
+          ++lg;
+        }
+      }
+      // both sides below 2^beta keep |2 Re|, |2 Im| (the combine reconstructs twice the product)
+      // below 2^(2 beta + 1) <= 2^(lg - 1) <= M / 2; the 21-bit digit split of the operands needs
+      // |x| < 2^62
+      beta[s] = std::min(lg / 2 - 1, 61);
       // the moduli in pairs (q = 2p, 2p + 1), mu_p = m_2p m_2p+1 < 2^16 (s even); c_p = inv_p / mu_p,
       // inv_p = (M / mu_p)^-1 mod mu_p; n = round(inv_p 2^36 / mu_p), ch = n 2^-36, cl = c_p - ch (the
       // representatives r < 2^16 + 768 keep every r ch exact in 53 bits)
       for (int q = 0; 2 * q + 1 < s; ++q) {
         const long long mu = (long long)OZM(2 * q) * OZM(2 * q + 1);
-        const long long Mi = (long long)((Mp / (u128)mu) % (u128)mu);
+        long long Mi = 1;   // (M / mu) mod mu
+        for (int r = 0; r < s; ++r)
+          if (r != 2 * q && r != 2 * q + 1) Mi = Mi * OZM(r) % mu;
         long long inv = 0;
         {   // extended Euclid
           long long r0 = mu, r1 = Mi, t0 = 0, t1 = 1;
@@ -146,13 +165,13 @@ __device__ __forceinline__ Dig dig_of(long long x) {
 // one reduction step of v in [0, k m): v <- v - m when v >= m (unsigned wrap-around makes it a min)
 __device__ __forceinline__ uint32_t red1(uint32_t v, uint32_t m) { return min(v, v - m); }
 
-// u = (x + 128) mod m_Q: the stored int8 is u - 128 (a residue of x in [-128, 127]), i.e. the byte u ^ 0x80.
-// Every partial sum of digit x constant stays below 2^31.
+// x mod m_Q in [0, m) from the digits.  Every partial sum of digit x constant stays below 2^31.
 template <int Q>
 struct Mod {
   static constexpr uint32_t m = OZM(Q);
+  static constexpr uint32_t j = OZJ(Q);   // j^2 = -1 (mod m)
   static constexpr uint32_t c21 = pow2mod(21, m), c42 = pow2mod(42, m);
-  static constexpr uint32_t off = (uint32_t)((128 + 4 * m - pow2mod(62, m)) % m);   // 128 - 2^62 (mod m)
+  static constexpr uint32_t off = (uint32_t)((4 * m - pow2mod(62, m)) % m);   // -2^62 (mod m)
   __device__ __forceinline__ static uint32_t u(const Dig& d) { return (d.d2 * c42 + d.d1 * c21 + d.d0 + off) % m; }
 };
 
@@ -160,42 +179,42 @@ __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2,
   return __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410) ^ 0x80808080u;
 }
 
-// residues of the planes (re, im, re + im, re - im) of E consecutive elements, packed 4 per word
-template <int Q, int NP, int E>
-__device__ __forceinline__ void plane_words(const Dig (&dr)[E], const Dig (&di)[E], uint32_t (&w)[NP][E / 4]) {
-  constexpr uint32_t m = Mod<Q>::m;
+// residues of the two planes z+ = re + j im and z- = re - j im (the images of re + i im under the two
+// ring homomorphisms Z[i] -> Z_m, i -> +-j) of E consecutive elements, packed 4 per word; the stored
+// int8 is ((z + 128) mod m) - 128, a residue of z in [-128, 127], i.e. the byte ((z + 128) mod m) ^ 0x80
+template <int Q, int E>
+__device__ __forceinline__ void plane_words(const Dig (&dr)[E], const Dig (&di)[E], uint32_t (&w)[2][E / 4]) {
+  constexpr uint32_t m = Mod<Q>::m, j = Mod<Q>::j;
 #pragma unroll
   for (int g = 0; g < E / 4; ++g) {
-    uint32_t b[NP][4];
+    uint32_t b[2][4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const uint32_t ur = Mod<Q>::u(dr[4 * g + k]), ui = Mod<Q>::u(di[4 * g + k]);
-      b[0][k] = ur;
-      b[1][k] = ui;
-      b[2][k] = red1(red1(ur + ui + (m - 128), m), m);             // (re + im + 128) mod m
-      if constexpr (NP == 4) b[3][k] = red1(red1(ur + m + 128 - ui, m), m);   // (re - im + 128) mod m
+      const uint32_t xr = Mod<Q>::u(dr[4 * g + k]), ji = (Mod<Q>::u(di[4 * g + k]) * j) % m;
+      b[0][k] = (xr + ji + 128) % m;
+      b[1][k] = (xr + m - ji + 128) % m;
     }
 #pragma unroll
-    for (int p = 0; p < NP; ++p) w[p][g] = pack4(b[p][0], b[p][1], b[p][2], b[p][3]);
+    for (int p = 0; p < 2; ++p) w[p][g] = pack4(b[p][0], b[p][1], b[p][2], b[p][3]);
   }
 }
 
-template <int S, int NP, int Q = 0>
+template <int S, int Q = 0>
 struct RowStore {
   // 4 consecutive elements -> one 32-bit word per (plane, modulus)
   __device__ __forceinline__ static void run(const Dig (&dr)[4], const Dig (&di)[4], int8_t* R, long long pstride,
                                              long long qstride) {
     if constexpr (Q < S) {
-      uint32_t w[NP][1];
-      plane_words<Q, NP, 4>(dr, di, w);
+      uint32_t w[2][1];
+      plane_words<Q, 4>(dr, di, w);
 #pragma unroll
-      for (int p = 0; p < NP; ++p) *reinterpret_cast<uint32_t*>(R + p * pstride + Q * qstride) = w[p][0];
-      RowStore<S, NP, Q + 1>::run(dr, di, R, pstride, qstride);
+      for (int p = 0; p < 2; ++p) *reinterpret_cast<uint32_t*>(R + p * pstride + Q * qstride) = w[p][0];
+      RowStore<S, Q + 1>::run(dr, di, R, pstride, qstride);
     }
   }
 };
 
-template <int S, int NP>
+template <int S>
 __global__ void __launch_bounds__(256) oz_split_rows_kernel(const cplx* __restrict__ X, long long ldx, long long sX,
                                                             int rows, int cols_cap, int T, int conj, int8_t* R,
                                                             long long ldr, int* e, long long sE, int beta,
@@ -243,7 +262,7 @@ __global__ void __launch_bounds__(256) oz_split_rows_kernel(const cplx* __restri
       dr[k] = dig_of(vr);
       di[k] = dig_of(vi);
     }
-    RowStore<S, NP>::run(dr, di, Rrow + j0, pstride, qstride);
+    RowStore<S>::run(dr, di, Rrow + j0, pstride, qstride);
   }
 }
 
@@ -276,22 +295,22 @@ __global__ void __launch_bounds__(256) oz_colnorm_kernel(const cplx* __restrict_
 
 constexpr int CTI = 64, CTJ = 32;   // column-split tile: 64 rows (k) x 32 columns (residue rows) of X
 
-template <int S, int NP, int Q = 0>
+template <int S, int Q = 0>
 struct ColStore {
   // 8 consecutive k of one residue row -> one 8-byte store per (plane, modulus)
   __device__ __forceinline__ static void run(const Dig (&dr)[8], const Dig (&di)[8], int8_t* R, long long pstride,
                                              long long qstride) {
     if constexpr (Q < S) {
-      uint32_t w[NP][2];
-      plane_words<Q, NP, 8>(dr, di, w);
+      uint32_t w[2][2];
+      plane_words<Q, 8>(dr, di, w);
 #pragma unroll
-      for (int p = 0; p < NP; ++p) *reinterpret_cast<uint2*>(R + p * pstride + Q * qstride) = make_uint2(w[p][0], w[p][1]);
-      ColStore<S, NP, Q + 1>::run(dr, di, R, pstride, qstride);
+      for (int p = 0; p < 2; ++p) *reinterpret_cast<uint2*>(R + p * pstride + Q * qstride) = make_uint2(w[p][0], w[p][1]);
+      ColStore<S, Q + 1>::run(dr, di, R, pstride, qstride);
     }
   }
 };
 
-template <int S, int NP>
+template <int S>
 __global__ void __launch_bounds__(256) oz_split_cols_kernel(const cplx* __restrict__ X, long long ldx, long long sX,
                                                             int rows, int cols, int T, int8_t* R, long long ldr,
                                                             int* e, long long sE, const double* part, int beta,
@@ -335,7 +354,7 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const cplx* __restri
     di[k] = dig_of(to_int(v.y, ex, p2));
   }
   const long long qstride = (long long)T * cols * ldr, pstride = (long long)S * qstride;
-  ColStore<S, NP>::run(dr, di, R + (long long)t * cols * ldr + (long long)j * ldr + i0 + ig, pstride, qstride);
+  ColStore<S>::run(dr, di, R + (long long)t * cols * ldr + (long long)j * ldr + i0 + ig, pstride, qstride);
 }
 
 // ---- CRT combine.  Moduli are taken in pairs (m_a, m_b) -> one residue mod mu = m_a m_b < 2^16
@@ -348,18 +367,15 @@ __host__ __device__ constexpr int modinv(int a, int m) {
   return r;
 }
 
-// representatives of the real and imaginary residues of the 3M combination from the product residues
-// (bytes < m), left unreduced in [0, 3m): the Garner step below takes any non-negative representative
+// residues of twice the real and imaginary parts from the two product residues a+ = P+ mod m and
+// a- = P- mod m (bytes < m; P+- = A+- B+-, the product's images under i -> +-j): 2 Re = P+ + P- is left
+// unreduced in [0, 2m) (the Garner step below takes any non-negative representative); 2 Im =
+// (P+ - P-) / j = -j (P+ - P-) takes one multiplication and one modulo
 template <int Q>
-__device__ __forceinline__ void reim(uint32_t a1, uint32_t a2, uint32_t a3, int neg2, uint32_t& re, uint32_t& im) {
-  constexpr uint32_t m = OZM(Q);
-  if (neg2) {   // Re = P1 + P2', Im = P3 - P1 + P2'
-    re = a1 + a2;
-    im = a3 + m - a1 + a2;
-  } else {      // Re = P1 - P2, Im = P3 - P1 - P2
-    re = a1 + m - a2;
-    im = a3 + 2 * m - a1 - a2;
-  }
+__device__ __forceinline__ void reim(uint32_t ap, uint32_t am, uint32_t& re, uint32_t& im) {
+  constexpr uint32_t m = OZM(Q), nj = OZM(Q) - OZJ(Q);
+  re = ap + am;
+  im = ((ap + m - am) * nj) % m;
 }
 
 // the residues of 4 consecutive outputs of one (product, modulus): with split-K, the chunks' residues
@@ -387,27 +403,26 @@ __device__ __forceinline__ void res4(const uint8_t* p, long long kstride, int ks
 template <int S, bool KS1, int PQ = 0>
 struct CrtPair {
   __device__ __forceinline__ static void run(const uint8_t* P, long long qstride, long long pstride, long long kstride,
-                                             int ks, int neg2, double (&sr)[4], double (&lr)[4], double (&si)[4],
+                                             int ks, double (&sr)[4], double (&lr)[4], double (&si)[4],
                                              double (&li)[4]) {
     if constexpr (2 * PQ < S) {
       constexpr int QA = 2 * PQ, QB = 2 * PQ + 1;
       constexpr uint32_t ma = OZM(QA), mb = OZM(QB);
       constexpr uint32_t inv = (uint32_t)modinv((int)(ma % mb), (int)mb);   // m_a^-1 mod m_b
-      uint32_t A1[4], A2[4], A3[4], B1[4], B2[4], B3[4];
+      uint32_t A1[4], A2[4], B1[4], B2[4];
       res4<QA, KS1>(P + QA * qstride, kstride, ks, A1);
       res4<QA, KS1>(P + pstride + QA * qstride, kstride, ks, A2);
-      res4<QA, KS1>(P + 2 * pstride + QA * qstride, kstride, ks, A3);
       res4<QB, KS1>(P + QB * qstride, kstride, ks, B1);
       res4<QB, KS1>(P + pstride + QB * qstride, kstride, ks, B2);
-      res4<QB, KS1>(P + 2 * pstride + QB * qstride, kstride, ks, B3);
       const double ch = c_ch[S][PQ], cl = c_cl[S][PQ];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         uint32_t rea, ima, reb, imb;
-        reim<QA>(A1[k], A2[k], A3[k], neg2, rea, ima);
-        reim<QB>(B1[k], B2[k], B3[k], neg2, reb, imb);
-        // Garner: r = r_a + m_a ((r_b - r_a) m_a^-1 mod m_b) in [0, mu + 2 m_a) (r_a, r_b in [0, 3m)
-        // unreduced; one modulo per component), then one step to the canonical residue in [0, mu): a zero
+        reim<QA>(A1[k], A2[k], rea, ima);
+        reim<QB>(B1[k], B2[k], reb, imb);
+        // Garner: r = r_a + m_a ((r_b - r_a) m_a^-1 mod m_b) in [0, mu + m_a) (r_a, r_b in [0, 2m)
+        // unreduced, 2 m_a < 4 m_b for the adjacent moduli of a pair; one modulo per component), then one
+        // step to the canonical residue in [0, mu): a zero
         // product must come out as exactly 0 (a zero row has exponent 0, so any CRT residual of a
         // non-canonical representative would be amplified)
         constexpr uint32_t mu = ma * mb;
@@ -421,7 +436,7 @@ struct CrtPair {
         lr[k] = fma((double)rr, cl, lr[k]);
         li[k] = fma((double)ri, cl, li[k]);
       }
-      CrtPair<S, KS1, PQ + 1>::run(P, qstride, pstride, kstride, ks, neg2, sr, lr, si, li);
+      CrtPair<S, KS1, PQ + 1>::run(P, qstride, pstride, kstride, ks, sr, lr, si, li);
     }
   }
 };
@@ -448,7 +463,7 @@ __global__ void __launch_bounds__(128) oz_combine_kernel(const uint8_t* __restri
   const long long kstride = (long long)M * ldp, qstride = (long long)T * ks * kstride, pstride = (long long)S * qstride;
   const uint8_t* p = P + ((long long)t * ks * M + i) * ldp + j0;
   double sr[4] = {0, 0, 0, 0}, lr[4] = {0, 0, 0, 0}, si[4] = {0, 0, 0, 0}, li[4] = {0, 0, 0, 0};
-  CrtPair<S, KS1>::run(p, qstride, pstride, kstride, ks, (flags & OZ_NEG_P2) ? 1 : 0, sr, lr, si, li);
+  CrtPair<S, KS1>::run(p, qstride, pstride, kstride, ks, sr, lr, si, li);
   const double Md = c_M[S];
   const int ea = eA[(a_traj ? t : 0) * sEA + i];
   cplx* c = C + t * sC + (long long)i * ldc;
@@ -457,7 +472,7 @@ __global__ void __launch_bounds__(128) oz_combine_kernel(const uint8_t* __restri
     const int j = j0 + k;
     if (j >= N || ((flags & OZ_UPPER) && j < i)) continue;
     const int eb = eB[t * sEB + j];
-    const int sc = -(ea + eb);
+    const int sc = -(ea + eb) - 1;   // the CRT value is twice the product
     double2 v = make_double2(crt_value(sr[k], lr[k], Md), crt_value(si[k], li[k], Md));
     if (ea == OZ_NONFINITE || eb == OZ_NONFINITE) v = make_double2(__longlong_as_double(0x7ff8000000000000LL),
                                                                    __longlong_as_double(0x7ff8000000000000LL));
@@ -496,6 +511,7 @@ int dispatch_s(int s, A... args) {
     case 12: return F<12>::go(args...);
     case 14: return F<14>::go(args...);
     case 16: return F<16>::go(args...);
+    case 18: return F<18>::go(args...);
   }
   return 1;
 }
@@ -505,12 +521,8 @@ struct LaunchRows {
   static int go(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T, int conj,
                 int8_t* R, long long ldr, int* e, long long sE, int beta, const int32_t* gate, const int32_t* cdev,
                 int np, const int32_t* rdev) {
-    if (np == 4)
-      oz_split_rows_kernel<S, 4><<<dim3(rows, T), 256, 0, st>>>(X, ldx, sX, rows, cols, T, conj, R, ldr, e, sE, beta,
-                                                                gate, cdev, rdev);
-    else
-      oz_split_rows_kernel<S, 3><<<dim3(rows, T), 256, 0, st>>>(X, ldx, sX, rows, cols, T, conj, R, ldr, e, sE, beta,
-                                                                gate, cdev, rdev);
+    oz_split_rows_kernel<S><<<dim3(rows, T), 256, 0, st>>>(X, ldx, sX, rows, cols, T, conj, R, ldr, e, sE, beta, gate,
+                                                           cdev, rdev);
     return 0;
   }
 };
@@ -521,12 +533,8 @@ struct LaunchCols {
                 int8_t* R, long long ldr, int* e, long long sE, const double* part, int beta, int subI,
                 const int32_t* gate, const int32_t* cdev, const int32_t* rdev, const int* e_in) {
     dim3 grid(ceil_div(cols, CTJ), ceil_div(rows, CTI), T);
-    if (np == 4)
-      oz_split_cols_kernel<S, 4><<<grid, 256, 0, st>>>(X, ldx, sX, rows, cols, T, R, ldr, e, sE, part, beta, subI, gate,
-                                                       cdev, rdev, e_in);
-    else
-      oz_split_cols_kernel<S, 3><<<grid, 256, 0, st>>>(X, ldx, sX, rows, cols, T, R, ldr, e, sE, part, beta, subI, gate,
-                                                       cdev, rdev, e_in);
+    oz_split_cols_kernel<S><<<grid, 256, 0, st>>>(X, ldx, sX, rows, cols, T, R, ldr, e, sE, part, beta, subI, gate,
+                                                  cdev, rdev, e_in);
     return 0;
   }
 };
@@ -558,7 +566,7 @@ int launched(const char* what, std::string* err) {
 
 }  // namespace
 
-int oz_supported(int s) { return s >= 4 && s <= 16 && s % 2 == 0; }
+int oz_supported(int s) { return s >= 4 && s <= OZ_MAXS && s % 2 == 0; }
 
 int oz_constants(int s, int* moduli, int* beta, double* ch, double* cl, double* M) {
   if (!oz_supported(s)) return 1;
@@ -573,6 +581,11 @@ int oz_constants(int s, int* moduli, int* beta, double* ch, double* cl, double* 
   return 0;
 }
 int oz_beta(int s) { return oz_supported(s) ? host_const().beta[s] : 0; }
+int oz_roots(int s, int* roots) {
+  if (!oz_supported(s)) return 1;
+  for (int q = 0; q < s; ++q) roots[q] = OZJ(q);
+  return 0;
+}
 
 int oz_split_rows(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T, int conj,
                   int s, int8_t* R, int* e, long long sE, std::string* err, const int32_t* gate, const int32_t* cdev,
@@ -584,10 +597,6 @@ int oz_split_rows(cudaStream_t st, const cplx* X, long long ldx, long long sX, i
     return 1;
   }
   if (int r = ensure_device_constants(&md, err)) return r;
-  if (nplanes != 3 && nplanes != 4) {
-    if (err) *err = "oz_split_rows: 3 or 4 planes";
-    return 1;
-  }
   dispatch_s<LaunchRows>(s, st, X, ldx, sX, rows, cols, T, conj, R, oz_ld(cols), e, sE, oz_beta(s), gate, cdev, nplanes,
                          rdev);
   return launched("oz_split_rows", err);
@@ -598,7 +607,7 @@ int oz_split_cols(cudaStream_t st, const cplx* X, long long ldx, long long sX, i
                   const int32_t* gate, const int32_t* cdev, const int32_t* rdev) {
   if (rows <= 0 || cols <= 0 || T <= 0) return 0;
   const int* md;
-  if (!oz_supported(s) || (nplanes != 3 && nplanes != 4) || T > 65535 || ceil_div(rows, CTI) > 65535) {
+  if (!oz_supported(s) || T > 65535 || ceil_div(rows, CTI) > 65535) {
     if (err) *err = "oz_split_cols: unsupported modulus count, plane count or shape";
     return 1;
   }
@@ -655,7 +664,7 @@ int oz_split_cols_e(cudaStream_t st, const cplx* X, long long ldx, long long sX,
                     int nplanes, int s, int8_t* R, const int* e_in, long long sE, std::string* err) {
   if (rows <= 0 || cols <= 0 || T <= 0) return 0;
   const int* md;
-  if (!oz_supported(s) || (nplanes != 3 && nplanes != 4) || !e_in) {
+  if (!oz_supported(s) || !e_in) {
     if (err) *err = "oz_split_cols_e: unsupported modulus / plane count or no exponents";
     return 1;
   }
@@ -695,7 +704,11 @@ int oz_product_mma(cudaStream_t st, const OzProduct& p, std::string* err) {
   g.M = p.M;
   g.N = p.N;
   g.K = p.K;
-  g.batch = 3LL * p.s * p.T;
+  // a conjugated operand (the callers' pa[2] / pb[2] == 3, the 3M scheme's (re - im) plane) swaps its two
+  // planes: conj(z)+- = z-+
+  const int ca = p.pa[2] == 3 ? 1 : 0, cb = p.pb[2] == 3 ? 1 : 0;
+  g.oz_np = 2;
+  g.batch = 2LL * p.s * p.T;
   g.A = p.RA;
   g.lda = p.lda_override ? p.lda_override : oz_ld(p.K);
   g.strideA = (long long)p.M * g.lda;
@@ -710,14 +723,15 @@ int oz_product_mma(cudaStream_t st, const OzProduct& p, std::string* err) {
   g.flags = ((p.flags & OZ_UPPER) ? IG_UPPER : 0) | ((p.flags & OZ_TRI_B) ? IG_TRI_B : 0);
   g.oz_s = p.s;
   g.oz_T = p.T;
-  for (int i = 0; i < 3; ++i) {
-    g.oz_pa[i] = p.pa[i];
-    g.oz_pb[i] = p.pb[i];
-  }
+  g.oz_pa[0] = ca;
+  g.oz_pa[1] = 1 - ca;
+  g.oz_pb[0] = cb;
+  g.oz_pb[1] = 1 - cb;
+  g.oz_pa[2] = g.oz_pb[2] = 0;
   g.oz_a_traj = p.a_traj;
   g.oz_b_traj = 1;
-  g.oz_na = p.a_planes * p.s * (p.a_traj ? p.T : 1);
-  g.oz_nb = p.b_planes * p.s * p.T;
+  g.oz_na = 2LL * p.s * (p.a_traj ? p.T : 1);
+  g.oz_nb = 2LL * p.s * p.T;
   g.gate = p.gate;
   g.kdev = p.kdev;
   g.ndev = p.ndev;

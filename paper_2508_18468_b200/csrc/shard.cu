@@ -289,7 +289,7 @@ size_t shard_carve(ShardedCtx* sh, const traj_config* c, char* base, int lwork, 
     if (banded) {
       lay.take(l.Uext, (size_t)(Lp + 2 * sh->H) * ldN * 16);
     } else if (sh->oz) {
-      lay.take(l.RK, (size_t)oz_residue_bytes(3, sh->oz_s, 1, Lp, L));
+      lay.take(l.RK, (size_t)oz_residue_bytes(2, sh->oz_s, 1, Lp, L));
       lay.take(l.eK, (size_t)Lp * 4);
     } else if (sh->planar) {
       lay.take(l.Kp, (size_t)3 * Lp * sh->ldKs * 8);

@@ -322,7 +322,7 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     const char* pc = getenv("TRAJ_PLANAR_CQR");
     h->planar_cqr = !(pc && pc[0] == '0') && N >= min_n;
     // the modular INT8 products replace both DMMA paths from the same size on (TRAJ_OZAKI=0: off,
-    // TRAJ_OZAKI_MODULI: 4..16 even, default 16 = beta 61 bits per operand row / column)
+    // TRAJ_OZAKI_MODULI: 4..18 even, default 16 = beta 57 bits per operand row / column; 18 = 61)
     const char* oz = getenv("TRAJ_OZAKI");
     const char* om = getenv("TRAJ_OZAKI_MODULI");
     h->oz_s = om ? atoi(om) : 16;
@@ -384,9 +384,9 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
   if (h->oz_ku || h->oz_cqr) {
     const long long s = h->oz_s;
     const size_t ru = (size_t)std::max(oz_residue_bytes(4, s, T, N, L), oz_residue_bytes(3, s, T, L, N));
-    h->RC_bytes = (size_t)oz_residue_bytes(3, s, T, L, N);
+    h->RC_bytes = (size_t)oz_residue_bytes(3, s, T, L, N);   // (two product planes needed; the structured solve splits it in halves)
     if (h->oz_ku) {
-      lay.take(h->RK, (size_t)oz_residue_bytes(3, s, 1, L, L));
+      lay.take(h->RK, (size_t)oz_residue_bytes(2, s, 1, L, L));
       lay.take(h->eK, (size_t)L * 4);
       h->RC_bytes = std::max<size_t>(h->RC_bytes, (size_t)L * ldL * 16);   // K is built there before its split
     }
@@ -2378,7 +2378,12 @@ int traj_zgemm_ozaki(void* stream, int opA, int64_t M, int64_t N, int64_t K, con
 
 int traj_ozaki_constants(int nmod, int32_t* moduli, int32_t* beta, double* ch, double* cl, double* M) {
   if (!moduli || !beta || !ch || !cl || !M || oz_constants(nmod, moduli, beta, ch, cl, M))
-    return fail(nullptr, TRAJ_EINVAL, "traj_ozaki_constants: nmod must be 4..16 even");
+    return fail(nullptr, TRAJ_EINVAL, "traj_ozaki_constants: nmod must be 4..18 even");
+  return 0;
+}
+
+int traj_ozaki_roots(int nmod, int32_t* roots) {
+  if (!roots || oz_roots(nmod, roots)) return fail(nullptr, TRAJ_EINVAL, "traj_ozaki_roots: nmod must be 4..18 even");
   return 0;
 }
 
