@@ -165,14 +165,27 @@ __device__ __forceinline__ Dig dig_of(long long x) {
 // one reduction step of v in [0, k m): v <- v - m when v >= m (unsigned wrap-around makes it a min)
 __device__ __forceinline__ uint32_t red1(uint32_t v, uint32_t m) { return min(v, v - m); }
 
-// x mod m_Q in [0, m) from the digits.  Every partial sum of digit x constant stays below 2^31.
+// The residues of z+ = re + j im and z- = re - j im mod m_Q straight from the digits of re + 2^62 and
+// im + 2^62: R = d2 2^42 + d1 2^21 + d0 (constants mod m) is congruent to re + 2^62 and below 2^30,
+// I = d2 (2^42 j) + d1 (2^21 j) + d0 j to j (im + 2^62) and below 3 2^29, so
+//   (z+ + 128) mod m = (R + I + offP) mod m,   (z- + 128) mod m = (R + (KM - I) + offM) mod m
+// with KM the least multiple of m >= 3 2^29 and the offsets removing the 2^62 shifts: one modulo per
+// plane, every sum below 2^32.
 template <int Q>
 struct Mod {
   static constexpr uint32_t m = OZM(Q);
   static constexpr uint32_t j = OZJ(Q);   // j^2 = -1 (mod m)
-  static constexpr uint32_t c21 = pow2mod(21, m), c42 = pow2mod(42, m);
-  static constexpr uint32_t off = (uint32_t)((4 * m - pow2mod(62, m)) % m);   // -2^62 (mod m)
-  __device__ __forceinline__ static uint32_t u(const Dig& d) { return (d.d2 * c42 + d.d1 * c21 + d.d0 + off) % m; }
+  static constexpr uint32_t c21 = pow2mod(21, m), c42 = pow2mod(42, m), p62 = pow2mod(62, m);
+  static constexpr uint32_t c21j = c21 * j % m, c42j = c42 * j % m;
+  static constexpr uint32_t offP = (128 % m + 2 * m * m - p62 * (1 + j)) % m;   // 128 - 2^62 (1 + j)
+  static constexpr uint32_t offM = (128 + m - p62 + p62 * j) % m;               // 128 - 2^62 (1 - j)
+  static constexpr uint32_t KM = m * ((3u * (1u << 29) + m - 1) / m);
+  __device__ __forceinline__ static void planes(const Dig& dr, const Dig& di, uint32_t& zp, uint32_t& zm) {
+    const uint32_t R = dr.d2 * c42 + dr.d1 * c21 + dr.d0;
+    const uint32_t I = di.d2 * c42j + di.d1 * c21j + di.d0 * j;
+    zp = (R + I + offP) % m;
+    zm = (R + (KM - I) + offM) % m;
+  }
 };
 
 __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
@@ -184,16 +197,11 @@ __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2,
 // int8 is ((z + 128) mod m) - 128, a residue of z in [-128, 127], i.e. the byte ((z + 128) mod m) ^ 0x80
 template <int Q, int E>
 __device__ __forceinline__ void plane_words(const Dig (&dr)[E], const Dig (&di)[E], uint32_t (&w)[2][E / 4]) {
-  constexpr uint32_t m = Mod<Q>::m, j = Mod<Q>::j;
 #pragma unroll
   for (int g = 0; g < E / 4; ++g) {
     uint32_t b[2][4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t xr = Mod<Q>::u(dr[4 * g + k]), ji = (Mod<Q>::u(di[4 * g + k]) * j) % m;
-      b[0][k] = (xr + ji + 128) % m;
-      b[1][k] = (xr + m - ji + 128) % m;
-    }
+    for (int k = 0; k < 4; ++k) Mod<Q>::planes(dr[4 * g + k], di[4 * g + k], b[0][k], b[1][k]);
 #pragma unroll
     for (int p = 0; p < 2; ++p) w[p][g] = pack4(b[p][0], b[p][1], b[p][2], b[p][3]);
   }
