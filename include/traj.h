@@ -204,6 +204,14 @@ int traj_last_clicks(traj_handle h, int64_t traj, int64_t* n_clicks, int64_t* n_
  * environment TRAJ_CQR2_FULL=1 forces the full factorisation every time). */
 int traj_cqr2_fallbacks(traj_handle h, int64_t* n);
 
+/* max|G2 - I| over the upper triangle of the Gram matrix G2 = U'^dag U' that the most recent
+ * CholeskyQR2 second pass measured (App. A: the QR step that keeps U orthonormal; SURVEY §8(a)
+ * a3), one double per trajectory of the handle (host array, n_traj entries; 1 for a row-sharded
+ * handle): the orthonormality left by the first pass, the quantity the first-order / full
+ * factorisation decision and the modulus count of the modular correction are keyed on.  0 before the
+ * first second pass.  Synchronises the handle's stream.  TRAJ_EINVAL for the fused small-lattice step. */
+int traj_gram_deviation(traj_handle h, double* out);
+
 /* Counters of the low-rank projective orthonormaliser (TRAJ_ORTH_LOWRANK, NEXT-1 option; SURVEY
  * §8(f) 1 "orthonormalise the projective step at low rank"), cumulative since traj_init:
  *   newton_iters  coupled Newton-Schulz iterations for (I - V V^dag)^(-1/2);

@@ -84,6 +84,7 @@ _SIGS = {
     "traj_failed": (ctypes.c_int, [_P, _I64, ctypes.POINTER(ctypes.c_int32)]),
     "traj_last_clicks": (ctypes.c_int, [_P, _I64, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     "traj_cqr2_fallbacks": (ctypes.c_int, [_P, ctypes.POINTER(_I64)]),
+    "traj_gram_deviation": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_double)]),
     "traj_probe_orthonormality": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_double)]),
     "traj_lowrank_stats": (ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I64),
                                           ctypes.POINTER(_I64)]),
@@ -404,6 +405,13 @@ class Trajectories:
         n = ctypes.c_int64(0)
         self._c(lib().traj_cqr2_fallbacks(self._h, ctypes.byref(n)))
         return n.value
+
+    def gram_deviation(self):
+        """max|G2 - I| measured by the most recent CholeskyQR2 second pass, per trajectory."""
+        import numpy as np
+        out = np.zeros(self.n_traj, dtype=np.float64)
+        self._c(lib().traj_gram_deviation(self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return out
 
     def probe_orthonormality(self):
         """Estimated ||U_t^dag U_t - I||_F per trajectory (4 random unit-modulus probes)."""

@@ -648,13 +648,39 @@ __global__ void oz_exponents_kernel(const double* __restrict__ nu2, long long sN
 }  // namespace
 
 int oz_colnorm_accumulate(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T,
-                          double* part, double* nu2, long long sN, int accumulate, std::string* err) {
+                          double* part, double* nu2, long long sN, int accumulate, std::string* err,
+                          int sub_identity) {
   if (cols <= 0 || T <= 0) return 0;
-  oz_colnorm_kernel<<<dim3(ceil_div(cols, 32), 8, T), dim3(32, 8), 0, st>>>(X, ldx, sX, rows, cols, T, part, 0,
-                                                                            nullptr, nullptr);
+  oz_colnorm_kernel<<<dim3(ceil_div(cols, 32), 8, T), dim3(32, 8), 0, st>>>(X, ldx, sX, rows, cols, T, part,
+                                                                            sub_identity, nullptr, nullptr);
   if (int r = launched("oz_colnorm", err)) return r;
   oz_colsum_kernel<<<dim3(ceil_div(cols, 256), T), 256, 0, st>>>(part, cols, T, nu2, sN, accumulate);
   return launched("oz_colsum", err);
+}
+
+namespace {
+// gate[1] = !gate[0] && max nu2 <= thr2, gate[2] = !gate[0] && !(max nu2 <= thr2); a NaN (failed
+// trajectory) does not raise the tier
+__global__ void __launch_bounds__(1024) oz_tier_decide_kernel(const double* __restrict__ nu2, long long n, double thr2,
+                                                               int32_t* gate) {
+  __shared__ int over;
+  if (threadIdx.x == 0) over = 0;
+  __syncthreads();
+  int o = 0;
+  for (long long i = threadIdx.x; i < n; i += 1024) o |= nu2[i] > thr2;
+  if (o) over = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int full = gate[0];
+    gate[1] = !full && !over;
+    gate[2] = !full && over;
+  }
+}
+}  // namespace
+
+int oz_tier_decide(cudaStream_t st, const double* nu2, long long n, double thr2, int32_t* gate, std::string* err) {
+  oz_tier_decide_kernel<<<1, 1024, 0, st>>>(nu2, n, thr2, gate);
+  return launched("oz_tier_decide", err);
 }
 
 int oz_exponents(cudaStream_t st, const double* nu2, long long sN, int cols, int T, int s, int* e, long long sE,

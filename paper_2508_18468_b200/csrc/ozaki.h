@@ -59,9 +59,14 @@ int oz_split_cols(cudaStream_t st, const cplx* X, long long ldx, long long sX, i
 // computed from X's own column norms; e is then not written
 int oz_split_cols_e(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T,
                     int nplanes, int s, int8_t* R, const int* e_in, long long sE, std::string* err);
-// nu2[t][j] (+)= sum over X's rows of (|re| + |im|)^2 of column j (part: >= 8 T cols doubles of scratch)
+// nu2[t][j] (+)= sum over X's rows of (|re| + |im|)^2 of column j (part: >= 8 T cols doubles of scratch);
+// sub_identity: of X - I
 int oz_colnorm_accumulate(cudaStream_t st, const cplx* X, long long ldx, long long sX, int rows, int cols, int T,
-                          double* part, double* nu2, long long sN, int accumulate, std::string* err);
+                          double* part, double* nu2, long long sN, int accumulate, std::string* err,
+                          int sub_identity = 0);
+// the modulus-count tier of a gated product from its operand's squared column norms nu2[0..n):
+// gate[1] = !gate[0] && max nu2 <= thr2 (the low count suffices), gate[2] = !gate[0] && !gate[1]
+int oz_tier_decide(cudaStream_t st, const double* nu2, long long n, double thr2, int32_t* gate, std::string* err);
 // e[t][j] = the column exponents for s moduli from the squared norms nu2
 int oz_exponents(cudaStream_t st, const double* nu2, long long sN, int cols, int T, int s, int* e, long long sE,
                  std::string* err);

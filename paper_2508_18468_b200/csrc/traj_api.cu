@@ -73,6 +73,7 @@ struct traj_ctx {
   int oz_s = 16;
   int oz_proj_min = 1024;   // click count from which the projective rank-k products go modular (TRAJ_OZAKI_PROJ_MIN)
   int oz_s_corr = 10;   // moduli of the second pass's first-order correction src (X - I) (TRAJ_OZAKI_CORR_MODULI; 0: full)
+  int oz_s_low = 8;     // ... when every column norm of X - I is <= 2^(beta_low - 55.5) / N (TRAJ_OZAKI_CORR_LOW; 0: no low tier)
   int8_t *RK = nullptr, *RU = nullptr, *RX = nullptr;
   uint8_t* RC = nullptr;
   int *eK = nullptr, *eU = nullptr, *eX = nullptr, *eU2 = nullptr;
@@ -331,6 +332,10 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     const char* oc = getenv("TRAJ_OZAKI_CORR_MODULI");
     h->oz_s_corr = oc ? atoi(oc) : 10;
     if (h->oz_s_corr != 0 && !oz_supported(h->oz_s_corr)) h->oz_s_corr = 10;
+    const char* ol = getenv("TRAJ_OZAKI_CORR_LOW");
+    h->oz_s_low = ol ? atoi(ol) : 8;
+    if (h->oz_s_low != 0 && (!oz_supported(h->oz_s_low) || h->oz_s_low >= h->oz_s_corr || 8 * h->L < 9 * h->N))
+      h->oz_s_low = 0;
     const bool oz_on = !(oz && oz[0] == '0') && oz_supported(h->oz_s) && N >= min_n && L <= 65535;
     h->oz_cqr = oz_on;
     h->oz_ku = oz_on && h->planar;
@@ -880,9 +885,22 @@ int cqr2(traj_ctx* h, cplx* U, cplx* tmp) {
         // dst = src + src D needs only oz_s_corr moduli (D's columns carry their own exponents, so
         // the correction is resolved to 2^-beta of |D|, far below the rounding of src); when the
         // device decided on the full factorisation (gate), the full-precision src X overwrites it
-        for (int full = 0; full < 2; ++full) {
-          const int s = full ? h->oz_s : h->oz_s_corr;
-          const int32_t* gate = full ? h->gate : nullptr;
+        // Tiers, decided on the device: src D at s moduli is resolved to 2^-beta (nu_a |b|_1 + nu_b |a|_1)
+        // <= 2^(1.5 - beta) N |D col| of a typical entry of src (2 sqrt(N) from the N-term sums, sqrt(2 N)
+        // from the (|re| + |im|) row norm against an entry), below 2^-54 when the largest column norm of D
+        // is <= 2^(beta - 55.5) / N: then the low modulus count runs (gate[1]), else the standard count
+        // (gate[2]), else the full product (gate[0]); exactly one of the three
+        const bool low = h->oz_s_low > 0;
+        if (low) {
+          double* nu2 = h->oz_part + (size_t)8 * h->T * h->N;   // past the column-norm partials (L >= N + N / 8)
+          const double dmax = ldexp(1.0, oz_beta(h->oz_s_low) - 55) / (1.4142135623730951 * (double)h->N);
+          TRY(oz_colnorm_accumulate(h->st, h->X, h->ldN, h->sG, h->N, h->N, h->T, h->oz_part, nu2, h->N, 0, &h->err, 1));
+          TRY(oz_tier_decide(h->st, nu2, (long long)h->T * h->N, dmax * dmax, h->gate, &h->err));
+        }
+        for (int tier = low ? 0 : 1; tier < 3; ++tier) {
+          const int full = tier == 2;
+          const int s = full ? h->oz_s : tier == 1 ? h->oz_s_corr : h->oz_s_low;
+          const int32_t* gate = full ? h->gate : low ? h->gate + 1 + tier : nullptr;
           TRY(oz_split_rows(h->st, src, h->ldN, h->sU, h->L, h->N, h->T, 0, s, h->RU, h->eU, h->L, &h->err, gate));
           TRY(oz_split_cols(h->st, h->X, h->ldN, h->sG, h->N, h->N, h->T, 3, s, h->RX, h->eX, h->N, h->oz_part,
                             &h->err, full ? 0 : 1, gate));
@@ -2176,6 +2194,17 @@ int traj_last_clicks(traj_handle h, int64_t traj, int64_t* n_clicks, int64_t* n_
   }
   if (n_clicks) *n_clicks = h->last_nS[traj];
   if (n_occupied) *n_occupied = h->last_n1[traj];
+  return 0;
+}
+
+int traj_gram_deviation(traj_handle h, double* out) {
+  if (!h || !out) return TRAJ_EINVAL;
+  const unsigned long long* dev = h->sh ? h->sh->gdev : (h->small ? nullptr : h->gdev);
+  if (!dev) return fail(h, TRAJ_EINVAL, "traj_gram_deviation: the fused small-lattice step keeps the Gram in shared memory");
+  const int T = h->sh ? 1 : h->T;
+  CK(cudaMemcpyAsync(h->h_dev, dev, (size_t)T * 8, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  memcpy(out, h->h_dev, (size_t)T * 8);
   return 0;
 }
 

@@ -233,6 +233,55 @@ def test_modular_cqr2_fallback_is_full_precision(T, oz_small):
     assert np.abs(c.correlation(0).cpu().numpy() - gaussian.correlation(gaussian.orthonormalize(U))).max() < 1e-9
 
 
+@pytest.mark.parametrize("low", ["8", "6", "0"])
+def test_modular_correction_tiers(T, oz_small, monkeypatch, low):
+    """The first-order second pass dst = src + src D on the modular path picks its modulus count on the
+    device from the column norms of D = X - I (low tier when all are <= 2^(beta_low - 55.5) / N, else the
+    standard count, else the full product): every tier must reproduce the full-precision src X to
+    rounding and leave U orthonormal.  Inputs with two nearly parallel columns span the well-conditioned case (low tier) to
+    deviations above the low threshold (the threshold itself is replayed here from the Gram)."""
+    import ctypes
+    import torch
+    import paper_2508_18468_b200 as P
+    L, N = 256, 128
+    rng = np.random.default_rng(11)
+    Q, _ = np.linalg.qr(rng.standard_normal((L, N)) + 1j * rng.standard_normal((L, N)))
+    mods = (ctypes.c_int32 * 32)()
+    beta = ctypes.c_int32(0)
+    ch, cl, M = (ctypes.c_double * 32)(), (ctypes.c_double * 32)(), ctypes.c_double()
+    devs = []
+    for delta in (1.0, 2e-2, 5e-3, 2.5e-3):
+        U0 = Q.copy()
+        U0[:, 1] = Q[:, 0] + delta * Q[:, 1]       # kappa ~ 2 / delta: the first pass leaves ~ kappa^2 eps
+        U0 = np.ascontiguousarray(U0)
+        out = {}
+        fell_back = False
+        for mode in ("tiered", "full"):
+            monkeypatch.setenv("TRAJ_OZAKI_CORR_LOW", low)
+            monkeypatch.setenv("TRAJ_OZAKI_CORR_MODULI", "10" if mode == "tiered" else "0")
+            c = _oz_on(P, L, 1, "homodyne", [0.0])
+            c.set_state(0, torch.from_numpy(U0).cuda())
+            c.orthonormalize()
+            fell_back |= c.cqr2_fallbacks() != 0
+            dev = float(c.gram_deviation()[0])
+            out[mode] = c.get_state(0).cpu().numpy()
+        if fell_back:        # the full factorisation's own path (test_modular_cqr2_fallback_is_full_precision)
+            continue
+        devs.append(dev)
+        print("delta", delta, "max|G2 - I|", dev)
+        Ug = out["tiered"]
+        assert np.abs(Ug.conj().T @ Ug - np.eye(N)).max() < 5e-15
+        assert np.abs(Ug - out["full"]).max() < 2e-15
+    # the sweep must straddle the low tier's threshold: |D col| <= sqrt(N) max|E| from below, >= max|E| / 2
+    # from above
+    if int(low) > 0:
+        assert P.lib().traj_ozaki_constants(int(low), mods, ctypes.byref(beta), ch, cl, ctypes.byref(M)) == 0
+        dmax = 2.0 ** (beta.value - 55.5) / N
+        assert min(devs) * np.sqrt(N) < dmax
+        if low == "6":
+            assert max(devs) / 2 > dmax
+
+
 def workloads_random(L, N, seed):
     from workloads import random_matrix
     return random_matrix(L, N, seed)

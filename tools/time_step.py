@@ -35,5 +35,9 @@ e1.record(tr.stream)
 torch.cuda.synchronize()
 ph = tr.phase_times()
 env = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("TRAJ_"))
-print(f"{a.config}{f' shards={a.shards}' if a.shards else ''} oz={tr.ozaki_info()} [{env}] {e0.elapsed_time(e1) / a.steps:.1f} ms/step  " +
+try:
+    gd = " gram_dev=" + ",".join(f"{v:.2e}" for v in tr.gram_deviation())
+except Exception:
+    gd = ""
+print(f"{a.config}{f' shards={a.shards}' if a.shards else ''}{gd} oz={tr.ozaki_info()} [{env}] {e0.elapsed_time(e1) / a.steps:.1f} ms/step  " +
       " ".join(f"{k}={v[0] / a.steps:.1f}" for k, v in ph.items() if v[0] > 0), flush=True)
