@@ -154,37 +154,51 @@ __device__ __forceinline__ long long to_int(double v, int e, double p2) {
   return __double2ll_rn((e > -1000 && e < 1000) ? v * p2 : scalbn(v, e));
 }
 
-// x (|x| < 2^62) by the 21-bit digits of x + 2^62 >= 0
+// x (|x| < 2^62) by the eight bytes of x + 2^62 >= 0 (two words: no digit extraction)
 struct Dig {
-  uint32_t d0, d1, d2;
+  uint32_t lo, hi;
 };
 __device__ __forceinline__ Dig dig_of(long long x) {
   const unsigned long long u = (unsigned long long)x + (1ull << 62);
-  return Dig{(uint32_t)(u & 0x1FFFFF), (uint32_t)((u >> 21) & 0x1FFFFF), (uint32_t)(u >> 42)};
+  return Dig{(uint32_t)u, (uint32_t)(u >> 32)};
 }
 // one reduction step of v in [0, k m): v <- v - m when v >= m (unsigned wrap-around makes it a min)
 __device__ __forceinline__ uint32_t red1(uint32_t v, uint32_t m) { return min(v, v - m); }
 
-// The residues of z+ = re + j im and z- = re - j im mod m_Q straight from the digits of re + 2^62 and
-// im + 2^62: R = d2 2^42 + d1 2^21 + d0 (constants mod m) is congruent to re + 2^62 and below 2^30,
-// I = d2 (2^42 j) + d1 (2^21 j) + d0 j to j (im + 2^62) and below 3 2^29, so
+// bytes (256^k c mod m) for k = k0 .. k0 + 3, packed for dp4a
+__host__ __device__ constexpr uint32_t pow256_word(int k0, uint32_t c, uint32_t m) {
+  uint32_t w = 0;
+  for (int k = 0; k < 4; ++k) w |= (uint32_t)((unsigned long long)pow2mod(8 * (k0 + k), (int)m) * c % m) << (8 * k);
+  return w;
+}
+
+// The residues of z+ = re + j im and z- = re - j im mod m_Q straight from the bytes b_k of re + 2^62 and
+// im + 2^62: R = sum_k b_k (256^k mod m) -- two dp4a -- is congruent to re + 2^62, I = sum_k b_k
+// (256^k j mod m) to j (im + 2^62), both <= 8 255 (m - 1) < 2^19, so
 //   (z+ + 128) mod m = (R + I + offP) mod m,   (z- + 128) mod m = (R + (KM - I) + offM) mod m
-// with KM the least multiple of m >= 3 2^29 and the offsets removing the 2^62 shifts: one modulo per
-// plane, every sum below 2^32.
+// with KM the least multiple of m >= 8 255 (m - 1) and the offsets removing the 2^62 shifts.  Every sum S is
+// below 2^21, where floor(S / m) = umulhi(S, ceil(2^32 / m)) exactly (S (ceil(2^32 / m) m - 2^32) < 2^32):
+// one multiply-high and one multiply-subtract per plane.
 template <int Q>
 struct Mod {
   static constexpr uint32_t m = OZM(Q);
   static constexpr uint32_t j = OZJ(Q);   // j^2 = -1 (mod m)
-  static constexpr uint32_t c21 = pow2mod(21, m), c42 = pow2mod(42, m), p62 = pow2mod(62, m);
-  static constexpr uint32_t c21j = c21 * j % m, c42j = c42 * j % m;
+  static constexpr uint32_t p62 = pow2mod(62, m);
+  static constexpr uint32_t cr0 = pow256_word(0, 1, m), cr1 = pow256_word(4, 1, m);
+  static constexpr uint32_t ci0 = pow256_word(0, j, m), ci1 = pow256_word(4, j, m);
   static constexpr uint32_t offP = (128 % m + 2 * m * m - p62 * (1 + j)) % m;   // 128 - 2^62 (1 + j)
   static constexpr uint32_t offM = (128 + m - p62 + p62 * j) % m;               // 128 - 2^62 (1 - j)
-  static constexpr uint32_t KM = m * ((3u * (1u << 29) + m - 1) / m);
+  static constexpr uint32_t KM = m * ((8u * 255u * (m - 1) + m - 1) / m);
+  static constexpr uint32_t magic = (uint32_t)((0x100000000ull + m - 1) / m);
+  static_assert(8ull * 255 * (m - 1) + KM + 2 * m < (1ull << 21), "sums stay below 2^21");
+  static_assert((unsigned long long)(1u << 21) * ((unsigned long long)magic * m - 0x100000000ull) < 0x100000000ull,
+                "the multiply-high quotient is exact below 2^21");
+  __device__ __forceinline__ static uint32_t mod(uint32_t v) { return v - __umulhi(v, magic) * m; }
   __device__ __forceinline__ static void planes(const Dig& dr, const Dig& di, uint32_t& zp, uint32_t& zm) {
-    const uint32_t R = dr.d2 * c42 + dr.d1 * c21 + dr.d0;
-    const uint32_t I = di.d2 * c42j + di.d1 * c21j + di.d0 * j;
-    zp = (R + I + offP) % m;
-    zm = (R + (KM - I) + offM) % m;
+    const uint32_t R = __dp4a(dr.hi, cr1, __dp4a(dr.lo, cr0, 0u));
+    const uint32_t I = __dp4a(di.hi, ci1, __dp4a(di.lo, ci0, 0u));
+    zp = mod(R + I + offP);
+    zm = mod(R + (KM - I) + offM);
   }
 };
 
@@ -325,7 +339,9 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const cplx* __restri
                                                             int subI, const int32_t* gate, const int32_t* cdev,
                                                             const int32_t* rdev, const int* e_in) {
   if (gate && *gate == 0) return;
-  __shared__ cplx tile[CTI][CTJ + 1];
+  // column index rotated by the row group (ii >> 3): the 8 threads of a 128-bit load phase (same column, rows 8
+  // apart) then fall into 8 different bank groups
+  __shared__ cplx tile[CTI][CTJ];
   const int j0 = blockIdx.x * CTJ, i0 = blockIdx.y * CTI, t = blockIdx.z;
   const int cz = cdev ? min(cols, cdev[t]) : cols;   // columns past cz are taken as zero
   const int rz = rdev ? min(rows, rdev[t]) : rows;   // rows past rz too
@@ -336,7 +352,7 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const cplx* __restri
     const int i = i0 + ii, j = j0 + jj;
     cplx v = (i < rz && j < cz) ? x[(long long)i * ldx + j] : make_double2(0.0, 0.0);
     if (subI && i == j) v.x -= 1.0;
-    tile[ii][jj] = v;
+    tile[ii][(jj + (ii >> 3)) & (CTJ - 1)] = v;
   }
   __syncthreads();
   const int jj = threadIdx.x >> 3, ig = (threadIdx.x & 7) * 8, j = j0 + jj;
@@ -357,7 +373,7 @@ __global__ void __launch_bounds__(256) oz_split_cols_kernel(const cplx* __restri
   Dig dr[8], di[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const cplx v = tile[ig + k][jj];
+    const cplx v = tile[ig + k][(jj + (ig >> 3)) & (CTJ - 1)];
     dr[k] = dig_of(to_int(v.x, ex, p2));
     di[k] = dig_of(to_int(v.y, ex, p2));
   }
@@ -408,6 +424,13 @@ __device__ __forceinline__ void res4(const uint8_t* p, long long kstride, int ks
   }
 }
 
+__device__ __forceinline__ double u32_to_double(uint32_t r) {
+  return __dadd_rn(__hiloint2double(0x43300000, (int)r), -4503599627370496.0);
+}
+__device__ __forceinline__ double round_magic(double x) {
+  return __dadd_rn(__dadd_rn(x, 6755399441055744.0), -6755399441055744.0);
+}
+
 template <int S, bool KS1, int PQ = 0>
 struct CrtPair {
   __device__ __forceinline__ static void run(const uint8_t* P, long long qstride, long long pstride, long long kstride,
@@ -436,13 +459,16 @@ struct CrtPair {
         constexpr uint32_t mu = ma * mb;
         const uint32_t rr = red1(rea + ma * (((reb + 4 * mb - rea) * inv) % mb), mu);
         const uint32_t ri = red1(ima + ma * (((imb + 4 * mb - ima) * inv) % mb), mu);
-        double tr = (double)rr * ch, ti = (double)ri * ch;
-        tr -= rint(tr);
-        ti -= rint(ti);
+        // (double)r and rint() without the conversion pipe: 2^52 + r is the double with r in its low
+        // mantissa word, and x + 1.5 2^52 - 1.5 2^52 rounds |x| < 2^51 to the nearest-even integer
+        const double dr = u32_to_double(rr), di = u32_to_double(ri);
+        double tr = dr * ch, ti = di * ch;
+        tr -= round_magic(tr);
+        ti -= round_magic(ti);
         sr[k] += tr;
         si[k] += ti;
-        lr[k] = fma((double)rr, cl, lr[k]);
-        li[k] = fma((double)ri, cl, li[k]);
+        lr[k] = fma(dr, cl, lr[k]);
+        li[k] = fma(di, cl, li[k]);
       }
       CrtPair<S, KS1, PQ + 1>::run(P, qstride, pstride, kstride, ks, sr, lr, si, li);
     }
