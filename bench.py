@@ -518,6 +518,9 @@ def roofline(args, w, tpg, shard, rows, phases, tr_clicks, ms, P, oz=(False, Fal
                               "three real 16384x8192x16384 products as one batch-3 launch, combine) vs 8.6 GB "
                               "algorithmic")) if traffic else None}
     oz_dom = (oz[0] and dom == "propagate") or (oz[1] and dom in ("gram", "trmm"))
+    # (a dominant Gram / TRMM phase whose modular launch never ran — e.g. the event-driven step's dense
+    # CholeskyQR below the modular size — keeps the DMMA roofline above)
+    oz_dom = oz_dom and phases.get({"propagate": "ku_mma", "gram": "gram_mma", "trmm": "trmm_mma"}[dom], (0.0,))[0] > 0
     if oz_dom:
         # the dominant phase is an exact modular product (csrc/ozaki.h): 2 s INT8 products per complex
         # product (the two planes re +- j im of each of the s moduli); algorithmic INT8 ops (2 per MAC) over the nested

@@ -72,6 +72,7 @@ struct traj_ctx {
   bool oz_ku = false, oz_cqr = false;
   int oz_s = 16;
   int oz_proj_min = 1024;   // click count from which the projective rank-k products go modular (TRAJ_OZAKI_PROJ_MIN)
+  int oz_struct_min = 1024; // click capacity from which the structured pass 1's solve goes modular (TRAJ_OZAKI_STRUCT_MIN; default: oz_proj_min)
   int oz_s_corr = 10;   // moduli of the second pass's first-order correction src (X - I) (TRAJ_OZAKI_CORR_MODULI; 0: full)
   int oz_s_low = 8;     // ... when every column norm of X - I is <= 2^(beta_low - 55.5) / N (TRAJ_OZAKI_CORR_LOW; 0: no low tier)
   int8_t *RK = nullptr, *RU = nullptr, *RX = nullptr;
@@ -329,6 +330,8 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     h->oz_s = om ? atoi(om) : 16;
     const char* opm = getenv("TRAJ_OZAKI_PROJ_MIN");
     h->oz_proj_min = opm ? atoi(opm) : 1024;
+    const char* osm = getenv("TRAJ_OZAKI_STRUCT_MIN");
+    h->oz_struct_min = osm ? atoi(osm) : h->oz_proj_min;
     const char* oc = getenv("TRAJ_OZAKI_CORR_MODULI");
     h->oz_s_corr = oc ? atoi(oc) : 10;
     if (h->oz_s_corr != 0 && !oz_supported(h->oz_s_corr)) h->oz_s_corr = 10;
@@ -479,7 +482,7 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
       // on the modular path the solve's per-block residue splits of the L x k0 accumulator favour fewer,
       // wider blocks (c5: 2048)
       h->sb = sbv ? std::max(16, std::min(4096, atoi(sbv) / 16 * 16))
-                  : (cap >= 1024 ? (h->oz_cqr && cap >= h->oz_proj_min ? 2048 : 512) : 128);
+                  : (cap >= 1024 ? (h->oz_cqr && cap >= h->oz_struct_min ? 2048 : 512) : 128);
       const long long b = h->sb;
       lay.take(h->sY, (size_t)T * cap * b * 16);
       lay.take(h->sC, (size_t)T * b * b * 16);
@@ -492,7 +495,7 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
       h->struct_batched = !(sbat && sbat[0] == '0');
       // (DMMA solve only: with the modular solve (c5) the sequential chain pipelines each factor block
       // under the solve on two streams, measured faster than the batched factor followed by the solve)
-      if (h->struct_batched && !(h->oz_cqr && cap >= h->oz_proj_min)) {
+      if (h->struct_batched && !(h->oz_cqr && cap >= h->oz_struct_min)) {
         const long long nblk = ceil_div(N, b);
         if (nblk > 1) {   // the batched solve's prefix sums
           h->sEs = (long long)L * ldcap;
@@ -624,7 +627,7 @@ int structured_pass1(traj_ctx* h, const cplx* src, cplx* dst, int kc) {
   s.ldWZ = h->ldN;
   s.sWZ = h->sUS;
   s.chol_scratch = h->s_chol_scratch;
-  const bool oz_apply = h->oz_cqr && kc >= h->oz_proj_min;
+  const bool oz_apply = h->oz_cqr && kc >= h->oz_struct_min;
   if (h->sSb && !oz_apply) {
     // every block at once (structchol.h): the batched factor, then the batched solve on this stream
     s.Sb = h->sSb;
