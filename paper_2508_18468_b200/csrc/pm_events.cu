@@ -542,6 +542,30 @@ __global__ void __launch_bounds__(256) ev_pass_generic_kernel(const cplx* __rest
   }
 }
 
+// Separable 2d pass: K(tau) = K_x(tau) (x) K_y(tau) on the square lattice, so the (2w+1)^2 product taps of a row
+// become 2 (2w+1): tmp = (K_x (x) 1) U, then out = (1 (x) K_y) tmp + x yhat with x from g_x = (K_x (x) 1) g.
+// Two reads and two writes of U instead of one each, against (2w+1)/2 times fewer row reads through L2.
+__device__ cplx ev_unit_tap = {1.0, 0.0};
+
+__global__ void __launch_bounds__(256) ev_vec_axis_kernel(const double2* __restrict__ g, double2* __restrict__ gx,
+                                                          int Lx, int Ly, DevTaps tx) {
+  const int m = blockIdx.x * 256 + threadIdx.x;
+  if (m >= Lx * Ly) return;
+  double re = 0.0, im = 0.0;
+  for (int q = 0; q < tx.n; ++q) {
+    const double2 c = tx.c[q], v = g[nb_site(m, Lx, Ly, tx.lo + q, 0)];
+    re += c.x * v.x - c.y * v.y;
+    im += c.x * v.y + c.y * v.x;
+  }
+  gx[m] = make_double2(re, im);
+}
+
+// TRAJ_EV_SEPARABLE=0: the 2d pass with the product taps in one kernel
+bool ev_separable() {
+  const char* e = getenv("TRAJ_EV_SEPARABLE");
+  return !(e && e[0] == '0');
+}
+
 // TRAJ_EV_ALT_TAPS=0: always the general four-FMA taps
 bool ev_alt_taps() {
   const char* e = getenv("TRAJ_EV_ALT_TAPS");
@@ -602,7 +626,7 @@ int ev_gemv(cudaStream_t st, const cplx* U, long long ld, int N, int L, const cp
 int ev_pass(cudaStream_t st, const cplx* U, cplx* out, long long ld, int N, int Lx, int Ly, const cplx* cx_dev,
             const cplx* cx_host, int xlo, int xn, const cplx* cy_dev, int ylo, int yn_taps, const cplx* y,
             const double* coef, const double2* g, int j, const cplx* yn, const double* coefn, double2* gn,
-            std::string* err) {
+            cplx* tmp, double2* gx, std::string* err) {
   const int w = (xn - 1) / 2;
   cudaError_t e;
   if (Ly == 1 && xlo == -w && w <= 9 && xn + 16 <= Lx && cx_host) {
@@ -614,6 +638,20 @@ int ev_pass(cudaStream_t st, const cplx* U, cplx* out, long long ld, int N, int 
       e = launch_pass_1d<6>(st, U, out, ld, N, Lx, cx_host, w, y, coef, g, j, yn, coefn, gn);
     else
       e = launch_pass_1d<9>(st, U, out, ld, N, Lx, cx_host, w, y, coef, g, j, yn, coefn, gn);
+  } else if (Ly > 1 && xn > 1 && yn_taps > 1 && tmp && gx && xn <= EVG_MAXTAPS && yn_taps <= EVG_MAXTAPS &&
+             ev_separable()) {
+    const cplx* one = nullptr;
+    e = cudaGetSymbolAddress((void**)&one, ev_unit_tap);
+    if (e == cudaSuccess) {
+      const DevTaps tx{cx_dev, xlo, xn}, ty{cy_dev, ylo, yn_taps}, id{one, 0, 1};
+      ev_pass_generic_kernel<<<Lx * Ly, 256, 0, st>>>(U, tmp, ld, N, Lx, Ly, tx, id, nullptr, nullptr, nullptr, -1,
+                                                      nullptr, nullptr, nullptr);
+      if (coef) ev_vec_axis_kernel<<<(unsigned)ceil_div(Lx * Ly, 256), 256, 0, st>>>(g, gx, Lx, Ly, tx);
+      ev_pass_generic_kernel<<<Lx * Ly, 256, 0, st>>>(tmp, out, ld, N, Lx, Ly, id, ty, y, coef, coef ? gx : g, j, yn,
+                                                      coefn, gn);
+      count_launch(coef ? 2 : 1);
+      e = cudaGetLastError();
+    }
   } else {
     if (xn * yn_taps > EVG_MAXTAPS) {
       if (err) *err = "ev_pass: more than 1024 taps";

@@ -30,10 +30,12 @@ int ev_gemv(cudaStream_t st, const cplx* U, long long ld, int N, int L, const cp
             std::string* err);
 // out = K(tau) U + x y s (x_i = alpha (K g)_i + beta delta_ij; coef == nullptr: propagation only), and
 // gn_i = sn <out_i, yn> when yn != nullptr.  1d bands of half-width <= 9 use the row-blocked
-// kernel with the HOST taps cx_host passed by value; otherwise the device taps, one CTA per row.
+// kernel with the HOST taps cx_host passed by value; otherwise the device taps, one CTA per row.  On a 2d lattice
+// with tmp (L x ld) and gx (L) given, the pass is separable: the x-axis taps into tmp (and g into gx), then the
+// y-axis taps with the rank-1 term into out (TRAJ_EV_SEPARABLE=0: the (2w+1)^2 product taps in one kernel).
 int ev_pass(cudaStream_t st, const cplx* U, cplx* out, long long ld, int N, int Lx, int Ly, const cplx* cx_dev,
             const cplx* cx_host, int xlo, int xn, const cplx* cy_dev, int ylo, int yn_taps, const cplx* y,
             const double* coef, const double2* g, int j, const cplx* yn, const double* coefn, double2* gn,
-            std::string* err);
+            cplx* tmp, double2* gx, std::string* err);
 
 }  // namespace traj

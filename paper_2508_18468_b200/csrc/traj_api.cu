@@ -91,6 +91,8 @@ struct traj_ctx {
   cplx* ev_y2 = nullptr;           // one-pass events: [2][N] unnormalised yhat
   double* ev_c2 = nullptr;         // [2][8] coef
   double2* ev_g2 = nullptr;        // [2][L] g = U yhat^dag
+  cplx* ev_tmp = nullptr;          // 2d lattices: [L][ldN] the x-axis half of the separable pass
+  double2* ev_gx = nullptr;        // ... and [L] the x-axis half of K g
   double* ev_part = nullptr;       // [64] prep partials
   bool ev_onepass = true;          // TRAJ_EVENTS_ONEPASS=0: two-pass event updates
   int32_t* occ_count = nullptr;
@@ -356,6 +358,10 @@ size_t carve(traj_ctx* h, const traj_config* c, char* base, int lwork) {
     lay.take(h->ev_y2, (size_t)2 * N * 16);
     lay.take(h->ev_c2, 2 * 8 * 8);
     lay.take(h->ev_g2, (size_t)2 * L * 16);
+    if (h->Ly > 1) {
+      lay.take(h->ev_tmp, (size_t)L * ldN * 16);
+      lay.take(h->ev_gx, (size_t)L * 16);
+    }
     lay.take(h->ev_part, 64 * 8);
     lay.take(h->occ_count, (size_t)T * 4);
     lay.take(h->taps_dev, (size_t)EV_TAPCAP * 16);
@@ -1424,7 +1430,8 @@ int event_window_onepass(traj_ctx* h) {
         }
         TRY(ev_pass(h->st, src, dst, h->ldN, h->N, h->Lx, h->Ly, cx, reinterpret_cast<const cplx*>(p.x.c.data()),
                     p.x.lo, p.x.n, cy, p.y.lo, p.y.n, ev ? Y[cur] : nullptr, ev ? C[cur] : nullptr, G[cur], p.j,
-                    next_ev ? Y[1 - cur] : nullptr, next_ev ? C[1 - cur] : nullptr, G[1 - cur], &h->err));
+                    next_ev ? Y[1 - cur] : nullptr, next_ev ? C[1 - cur] : nullptr, G[1 - cur], h->ev_tmp, h->ev_gx,
+                    &h->err));
         std::swap(src, dst);
         if (ev) cur = 1 - cur;
       }

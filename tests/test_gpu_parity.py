@@ -626,6 +626,36 @@ def test_event_driven_pm_matches_oracle(P, Lx, Ly, gam, orth):
     assert events > 50
 
 
+def test_event_driven_pm_2d_separable_pass_matches_product_taps_and_oracle(P, monkeypatch):
+    """NEXT-4 on a 2d lattice: the separable pass (x-axis taps into a scratch copy, then y-axis taps
+    with the rank-1 term; the default) and the (2w+1)^2 product taps in one kernel
+    (TRAJ_EV_SEPARABLE=0) give the same trajectory, and both follow the oracle's literal L x L
+    algorithm on a non-square lattice."""
+    from oracle.pm_events import EventPM
+    Lx, Ly, gam = 12, 10, 3.0
+    A = np.arange(Lx * Ly // 2)
+    res = {}
+    for sep in ("1", "0"):
+        monkeypatch.setenv("TRAJ_EV_SEPARABLE", sep)
+        g = P.Trajectories(Lx, Ly, "projective_events", [gam], seed=5)
+        o = EventPM(Lx, Ly, gam, 0.05, seed=5, traj=0)
+        events = 0
+        for s in range(20):
+            g.step(1)
+            n0 = len(o.log)
+            o.step(1)
+            nev, nocc = g.last_clicks(0)
+            assert nev == len(o.log) - n0
+            assert nocc == sum(1 for e in o.log[n0:] if e[3])
+            events += nev
+        assert events > 100
+        C = g.correlation(0).cpu().numpy()
+        assert np.abs(C - o.correlation()).max() < C_TOL
+        assert abs(g.entropy(A)[0] - o.entropy(A)) < S_TOL
+        res[sep] = C
+    assert np.abs(res["1"] - res["0"]).max() < 1e-12
+
+
 @pytest.mark.parametrize("Lx,Ly,P_shards,protocol", [(256, 1, 4, "projective"), (240, 1, 2, "homodyne"),
                                                      (12, 12, 3, "projective"), (10, 8, 2, "homodyne")])
 def test_row_sharded_banded_halo_matches_oracle(P, Lx, Ly, P_shards, protocol):
