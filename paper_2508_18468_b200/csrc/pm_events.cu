@@ -250,32 +250,57 @@ __device__ __forceinline__ double2 stencil_vec(const double2* g, int Lx, int Ly,
   return make_double2(re, im);
 }
 
-// r_k = (K(tau + tau') U)_{j', k} + X yprev_k sprev,  X = sum_{q'} c'_{q'} x_{m_q'} (prev event);
+// r_k = (K(tau + tau') U)_{j', k} + X yprev_k sprev,  X = (K(tau') x)_{j'} with x_m = alpha (K(tau) g)_m + beta delta_{m,jprev}
+// (prev event), i.e. X = alpha (K(tau + tau') g)_{j'} + beta K(tau')_{j', jprev}: the combined taps c on g and the
+// one entry of the own taps o that reaches jprev (K(tau') K(tau) = K(tau + tau')), summed over the block's threads.
 // part[b] = sum over this block's k of |r_k|^2.  Without a previous event: r = (K(tau') U)_{j'}.
 constexpr int EVP_THREADS = 256;
 __global__ void __launch_bounds__(EVP_THREADS) ev_prep_kernel(const cplx* U, long long ld, int N, int Lx, int Ly, int j,
                                                              DevTaps cx, DevTaps cy, DevTaps ox, DevTaps oy,
-                                                             DevTaps ix, DevTaps iy, const double* coef_prev,
-                                                             const double2* g_prev, const cplx* y_prev, int j_prev,
-                                                             cplx* y_out, double* part) {
+                                                             const double* coef_prev, const double2* g_prev,
+                                                             const cplx* y_prev, int j_prev, cplx* y_out,
+                                                             double* part) {
   __shared__ double red[EVP_THREADS / 32];
+  __shared__ double redx[2][EVP_THREADS / 32];
   __shared__ double2 Xs;
+  if (coef_prev) {
+    const double alpha = coef_prev[0], beta = coef_prev[1];
+    double xr = 0.0, xi = 0.0;
+    for (int q = threadIdx.x; q < cx.n * cy.n; q += EVP_THREADS) {
+      const int qy = q / cx.n, qx = q % cx.n;
+      const double2 a = cx.c[qx], b = cy.c[qy];
+      const double cr = a.x * b.x - a.y * b.y, ci = a.x * b.y + a.y * b.x;
+      const double2 v = g_prev[nb_site(j, Lx, Ly, cx.lo + qx, cy.lo + qy)];
+      xr += alpha * (cr * v.x - ci * v.y);
+      xi += alpha * (cr * v.y + ci * v.x);
+    }
+    for (int q = threadIdx.x; q < ox.n * oy.n; q += EVP_THREADS) {
+      const int qy = q / ox.n, qx = q % ox.n;
+      if (nb_site(j, Lx, Ly, ox.lo + qx, oy.lo + qy) != j_prev) continue;
+      const double2 a = ox.c[qx], b = oy.c[qy];
+      xr += beta * (a.x * b.x - a.y * b.y);
+      xi += beta * (a.x * b.y + a.y * b.x);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      xr += __shfl_xor_sync(0xffffffffu, xr, o);
+      xi += __shfl_xor_sync(0xffffffffu, xi, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      redx[0][threadIdx.x >> 5] = xr;
+      redx[1][threadIdx.x >> 5] = xi;
+    }
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     double2 X = make_double2(0.0, 0.0);
     if (coef_prev) {
-      const double alpha = coef_prev[0], beta = coef_prev[1], s = coef_prev[4];
-      for (int qy = 0; qy < oy.n; ++qy)
-        for (int qx = 0; qx < ox.n; ++qx) {
-          const int m = nb_site(j, Lx, Ly, ox.lo + qx, oy.lo + qy);
-          const double2 v = stencil_vec(g_prev, Lx, Ly, m, ix, iy);
-          double xr = alpha * v.x + (m == j_prev ? beta : 0.0), xi = alpha * v.y;
-          const double2 a = ox.c[qx], b = oy.c[qy];
-          const double cr = a.x * b.x - a.y * b.y, ci = a.x * b.y + a.y * b.x;
-          X.x += cr * xr - ci * xi;
-          X.y += cr * xi + ci * xr;
-        }
-      X.x *= s;
-      X.y *= s;
+      for (int w = 0; w < EVP_THREADS / 32; ++w) {
+        X.x += redx[0][w];
+        X.y += redx[1][w];
+      }
+      X.x *= coef_prev[4];
+      X.y *= coef_prev[4];
     }
     Xs = X;
   }
@@ -373,7 +398,15 @@ __global__ void __launch_bounds__(256) ev_pass_1d_kernel(const cplx* __restrict_
                                                          const cplx* __restrict__ y, const double* __restrict__ coef,
                                                          const double2* __restrict__ g, int j,
                                                          const cplx* __restrict__ yn, const double* __restrict__ coefn,
-                                                         double2* __restrict__ gn) {
+                                                         double2* __restrict__ gn, int bstride, int pstride) {
+  // ring blockIdx.y of a 2d lattice's axis: its site p is row blockIdx.y * bstride + p * pstride of U, g, gn
+  // (x axis: bstride = Lx, pstride = 1; y axis: 1, Lx; the 1d ring: 0, 1)
+  U += (long long)blockIdx.y * bstride * ld;
+  out += (long long)blockIdx.y * bstride * ld;
+  g += (long long)blockIdx.y * bstride;
+  gn += (long long)blockIdx.y * bstride;
+  j -= blockIdx.y * bstride;
+  const long long ldp = ld * pstride;
   __shared__ double2 xs[EV_R];
   __shared__ double red[8][2 * EV_R];
   const int i0 = blockIdx.x * EV_R;
@@ -386,12 +419,12 @@ __global__ void __launch_bounds__(256) ev_pass_1d_kernel(const cplx* __restrict_
       for (int d = 0; d < 2 * W + 1; ++d) {
         int p = i - W + d;
         p = p < 0 ? p + L : (p >= L ? p - L : p);
-        const double2 v = g[p];
+        const double2 v = g[(long long)p * pstride];
         vr += taps.c[d][0] * v.x - taps.c[d][1] * v.y;
         vi += taps.c[d][0] * v.y + taps.c[d][1] * v.x;
       }
       const double s = coef[4];
-      x = make_double2(s * (coef[0] * vr + (i == j ? coef[1] : 0.0)), s * coef[0] * vi);
+      x = make_double2(s * (coef[0] * vr + (i * pstride == j ? coef[1] : 0.0)), s * coef[0] * vi);
     }
     xs[threadIdx.x] = x;
   }
@@ -411,7 +444,7 @@ __global__ void __launch_bounds__(256) ev_pass_1d_kernel(const cplx* __restrict_
     for (int q = 0; q < EV_R + 2 * W; ++q) {
       int p = i0 - W + q;
       if (wraps) p = p < 0 ? p + L : (p >= L ? p - L : p);
-      in[q] = U[(long long)p * ld + k];
+      in[q] = U[p * ldp + k];
     }
     const double2 yk = coef ? y[k] : make_double2(0.0, 0.0);
     const double2 ynk = yn ? yn[k] : make_double2(0.0, 0.0);
@@ -434,7 +467,7 @@ __global__ void __launch_bounds__(256) ev_pass_1d_kernel(const cplx* __restrict_
           im = fma(taps.c[d][1], b.x, im);
         }
       }
-      if (i0 + r < L) out[(long long)(i0 + r) * ld + k] = make_double2(re, im);
+      if (i0 + r < L) out[(i0 + r) * ldp + k] = make_double2(re, im);
       ar[r] += re * ynk.x + im * ynk.y;
       ai[r] += im * ynk.x - re * ynk.y;
     }
@@ -459,7 +492,7 @@ __global__ void __launch_bounds__(256) ev_pass_1d_kernel(const cplx* __restrict_
       a += red[w][2 * threadIdx.x];
       b += red[w][2 * threadIdx.x + 1];
     }
-    gn[i0 + threadIdx.x] = make_double2(sn * a, sn * b);
+    gn[(long long)(i0 + threadIdx.x) * pstride] = make_double2(sn * a, sn * b);
   }
 }
 
@@ -575,7 +608,8 @@ bool ev_alt_taps() {
 template <int W>
 cudaError_t launch_pass_1d(cudaStream_t st, const cplx* U, cplx* out, long long ld, int N, int L,
                            const cplx* taps_host, int w, const cplx* y, const double* coef, const double2* g, int j,
-                           const cplx* yn, const double* coefn, double2* gn) {
+                           const cplx* yn, const double* coefn, double2* gn, int rings = 1, int bstride = 0,
+                           int pstride = 1) {
   constexpr int R = W <= 6 ? 8 : 4;
   EvTaps<W> t;
   for (int d = 0; d < 2 * W + 1; ++d) t.c[d][0] = t.c[d][1] = t.c[d][2] = 0.0;
@@ -586,12 +620,13 @@ cudaError_t launch_pass_1d(cudaStream_t st, const cplx* U, cplx* out, long long 
     t.c[W - w + d][2] = -taps_host[d].y;
     alt = alt && (((d - w) & 1) == 0 ? taps_host[d].y == 0.0 : taps_host[d].x == 0.0);
   }
+  const dim3 grid((unsigned)ceil_div(L, R), (unsigned)rings);
   if (alt && ev_alt_taps())
-    ev_pass_1d_kernel<W, R, true><<<(unsigned)ceil_div(L, R), 256, 0, st>>>(U, out, ld, N, L, t, y, coef, g, j, yn,
-                                                                            coefn, gn);
+    ev_pass_1d_kernel<W, R, true><<<grid, 256, 0, st>>>(U, out, ld, N, L, t, y, coef, g, j, yn, coefn, gn, bstride,
+                                                        pstride);
   else
-    ev_pass_1d_kernel<W, R, false><<<(unsigned)ceil_div(L, R), 256, 0, st>>>(U, out, ld, N, L, t, y, coef, g, j, yn,
-                                                                             coefn, gn);
+    ev_pass_1d_kernel<W, R, false><<<grid, 256, 0, st>>>(U, out, ld, N, L, t, y, coef, g, j, yn, coefn, gn, bstride,
+                                                         pstride);
   return cudaGetLastError();
 }
 
@@ -599,13 +634,11 @@ cudaError_t launch_pass_1d(cudaStream_t st, const cplx* U, cplx* out, long long 
 
 int ev_prep(cudaStream_t st, const cplx* U, long long ld, int N, int Lx, int Ly, int j, const cplx* cxc, int cxlo,
             int cxn, const cplx* cyc, int cylo, int cyn, const cplx* oxc, int oxlo, int oxn, const cplx* oyc, int oylo,
-            int oyn, const cplx* ixc, int ixlo, int ixn, const cplx* iyc, int iylo, int iyn, const double* coef_prev,
-            const double2* g_prev, const cplx* y_prev, int j_prev, double pc, cplx* y_out, double* part,
-            double* coef_out, int32_t* occ_count, std::string* err) {
+            int oyn, const double* coef_prev, const double2* g_prev, const cplx* y_prev, int j_prev, double pc,
+            cplx* y_out, double* part, double* coef_out, int32_t* occ_count, std::string* err) {
   const int nb = (int)std::min<long long>(ceil_div(N, EVP_THREADS), 64);
   ev_prep_kernel<<<nb, EVP_THREADS, 0, st>>>(U, ld, N, Lx, Ly, j, DevTaps{cxc, cxlo, cxn}, DevTaps{cyc, cylo, cyn},
-                                             DevTaps{oxc, oxlo, oxn}, DevTaps{oyc, oylo, oyn},
-                                             DevTaps{ixc, ixlo, ixn}, DevTaps{iyc, iylo, iyn}, coef_prev, g_prev,
+                                             DevTaps{oxc, oxlo, oxn}, DevTaps{oyc, oylo, oyn}, coef_prev, g_prev,
                                              y_prev, j_prev, y_out, part);
   ev_decide_kernel<<<1, 32, 0, st>>>(part, nb, pc, coef_out, occ_count);
   count_launch(2);
@@ -623,34 +656,50 @@ int ev_gemv(cudaStream_t st, const cplx* U, long long ld, int N, int L, const cp
   return e == cudaSuccess ? 0 : 4;
 }
 
+namespace {
+// one axis of the pass on the row-blocked kernel (the band [-w, w], w <= 9, on rings of extent >= 2w + 17)
+bool ring_ok(int lo, int n, int extent) { return lo == -(n - 1) / 2 && (n - 1) / 2 <= 9 && n + 16 <= extent; }
+
+cudaError_t launch_ring(cudaStream_t st, const cplx* U, cplx* out, long long ld, int N, int L, const cplx* taps_host,
+                        int w, const cplx* y, const double* coef, const double2* g, int j, const cplx* yn,
+                        const double* coefn, double2* gn, int rings, int bstride, int pstride) {
+  if (w <= 2) return launch_pass_1d<2>(st, U, out, ld, N, L, taps_host, w, y, coef, g, j, yn, coefn, gn, rings, bstride, pstride);
+  if (w <= 4) return launch_pass_1d<4>(st, U, out, ld, N, L, taps_host, w, y, coef, g, j, yn, coefn, gn, rings, bstride, pstride);
+  if (w <= 6) return launch_pass_1d<6>(st, U, out, ld, N, L, taps_host, w, y, coef, g, j, yn, coefn, gn, rings, bstride, pstride);
+  return launch_pass_1d<9>(st, U, out, ld, N, L, taps_host, w, y, coef, g, j, yn, coefn, gn, rings, bstride, pstride);
+}
+}  // namespace
+
 int ev_pass(cudaStream_t st, const cplx* U, cplx* out, long long ld, int N, int Lx, int Ly, const cplx* cx_dev,
-            const cplx* cx_host, int xlo, int xn, const cplx* cy_dev, int ylo, int yn_taps, const cplx* y,
-            const double* coef, const double2* g, int j, const cplx* yn, const double* coefn, double2* gn,
-            cplx* tmp, double2* gx, std::string* err) {
+            const cplx* cx_host, int xlo, int xn, const cplx* cy_dev, const cplx* cy_host, int ylo, int yn_taps,
+            const cplx* y, const double* coef, const double2* g, int j, const cplx* yn, const double* coefn,
+            double2* gn, cplx* tmp, double2* gx, std::string* err) {
   const int w = (xn - 1) / 2;
   cudaError_t e;
-  if (Ly == 1 && xlo == -w && w <= 9 && xn + 16 <= Lx && cx_host) {
-    if (w <= 2)
-      e = launch_pass_1d<2>(st, U, out, ld, N, Lx, cx_host, w, y, coef, g, j, yn, coefn, gn);
-    else if (w <= 4)
-      e = launch_pass_1d<4>(st, U, out, ld, N, Lx, cx_host, w, y, coef, g, j, yn, coefn, gn);
-    else if (w <= 6)
-      e = launch_pass_1d<6>(st, U, out, ld, N, Lx, cx_host, w, y, coef, g, j, yn, coefn, gn);
-    else
-      e = launch_pass_1d<9>(st, U, out, ld, N, Lx, cx_host, w, y, coef, g, j, yn, coefn, gn);
+  if (Ly == 1 && cx_host && ring_ok(xlo, xn, Lx)) {
+    e = launch_ring(st, U, out, ld, N, Lx, cx_host, w, y, coef, g, j, yn, coefn, gn, 1, 0, 1);
   } else if (Ly > 1 && xn > 1 && yn_taps > 1 && tmp && gx && xn <= EVG_MAXTAPS && yn_taps <= EVG_MAXTAPS &&
              ev_separable()) {
     const cplx* one = nullptr;
     e = cudaGetSymbolAddress((void**)&one, ev_unit_tap);
     if (e == cudaSuccess) {
       const DevTaps tx{cx_dev, xlo, xn}, ty{cy_dev, ylo, yn_taps}, id{one, 0, 1};
-      ev_pass_generic_kernel<<<Lx * Ly, 256, 0, st>>>(U, tmp, ld, N, Lx, Ly, tx, id, nullptr, nullptr, nullptr, -1,
-                                                      nullptr, nullptr, nullptr);
+      // x axis: tmp = (K_x (x) 1) U on the Ly lattice lines (consecutive rows), g_x = (K_x (x) 1) g
+      if (cx_host && ring_ok(xlo, xn, Lx))
+        e = launch_ring(st, U, tmp, ld, N, Lx, cx_host, w, nullptr, nullptr, g, -1, nullptr, nullptr, gn, Ly, Lx, 1);
+      else
+        ev_pass_generic_kernel<<<Lx * Ly, 256, 0, st>>>(U, tmp, ld, N, Lx, Ly, tx, id, nullptr, nullptr, nullptr, -1,
+                                                        nullptr, nullptr, nullptr);
       if (coef) ev_vec_axis_kernel<<<(unsigned)ceil_div(Lx * Ly, 256), 256, 0, st>>>(g, gx, Lx, Ly, tx);
-      ev_pass_generic_kernel<<<Lx * Ly, 256, 0, st>>>(tmp, out, ld, N, Lx, Ly, id, ty, y, coef, coef ? gx : g, j, yn,
-                                                      coefn, gn);
+      // y axis: out = (1 (x) K_y) tmp + x yhat on the Lx lattice columns (rows Lx apart), and the next event's g
+      if (e == cudaSuccess && cy_host && ring_ok(ylo, yn_taps, Ly))
+        e = launch_ring(st, tmp, out, ld, N, Ly, cy_host, (yn_taps - 1) / 2, y, coef, coef ? gx : g, j, yn, coefn, gn,
+                        Lx, 1, Lx);
+      else if (e == cudaSuccess)
+        ev_pass_generic_kernel<<<Lx * Ly, 256, 0, st>>>(tmp, out, ld, N, Lx, Ly, id, ty, y, coef, coef ? gx : g, j, yn,
+                                                        coefn, gn);
       count_launch(coef ? 2 : 1);
-      e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaGetLastError();
     }
   } else {
     if (xn * yn_taps > EVG_MAXTAPS) {

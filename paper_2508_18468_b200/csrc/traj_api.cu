@@ -1413,8 +1413,8 @@ int event_window_onepass(traj_ctx* h) {
         const bool ev = p.j >= 0;
         if (ev && q == 0) {
           TRY(ev_prep(h->st, src, h->ldN, h->N, h->Lx, h->Ly, p.j, cx, p.x.lo, p.x.n, cy, p.y.lo, p.y.n, nullptr, 0, 0,
-                      nullptr, 0, 0, nullptr, 0, 0, nullptr, 0, 0, nullptr, nullptr, nullptr, -1, p.pc, Y[cur],
-                      h->ev_part, C[cur], h->occ_count + t, &h->err));
+                      nullptr, 0, 0, nullptr, nullptr, nullptr, -1, p.pc, Y[cur], h->ev_part, C[cur], h->occ_count + t,
+                      &h->err));
           TRY(ev_gemv(h->st, src, h->ldN, h->N, h->L, Y[cur], C[cur], G[cur], &h->err));
         }
         const bool next_ev = ev && q + 1 < passes.size() && passes[q + 1].j >= 0;
@@ -1425,11 +1425,12 @@ int event_window_onepass(traj_ctx* h) {
           const cplx* ccx = h->taps_dev + pn.offc;
           const cplx* ccy = ccx + pn.cx.n;
           TRY(ev_prep(h->st, src, h->ldN, h->N, h->Lx, h->Ly, pn.j, ccx, pn.cx.lo, pn.cx.n, ccy, pn.cy.lo, pn.cy.n, ncx,
-                      pn.x.lo, pn.x.n, ncy, pn.y.lo, pn.y.n, cx, p.x.lo, p.x.n, cy, p.y.lo, p.y.n, C[cur], G[cur],
-                      Y[cur], p.j, pn.pc, Y[1 - cur], h->ev_part, C[1 - cur], h->occ_count + t, &h->err));
+                      pn.x.lo, pn.x.n, ncy, pn.y.lo, pn.y.n, C[cur], G[cur], Y[cur], p.j, pn.pc, Y[1 - cur],
+                      h->ev_part, C[1 - cur], h->occ_count + t, &h->err));
         }
         TRY(ev_pass(h->st, src, dst, h->ldN, h->N, h->Lx, h->Ly, cx, reinterpret_cast<const cplx*>(p.x.c.data()),
-                    p.x.lo, p.x.n, cy, p.y.lo, p.y.n, ev ? Y[cur] : nullptr, ev ? C[cur] : nullptr, G[cur], p.j,
+                    p.x.lo, p.x.n, cy, reinterpret_cast<const cplx*>(p.y.c.data()), p.y.lo, p.y.n,
+                    ev ? Y[cur] : nullptr, ev ? C[cur] : nullptr, G[cur], p.j,
                     next_ev ? Y[1 - cur] : nullptr, next_ev ? C[1 - cur] : nullptr, G[1 - cur], h->ev_tmp, h->ev_gx,
                     &h->err));
         std::swap(src, dst);

@@ -626,13 +626,16 @@ def test_event_driven_pm_matches_oracle(P, Lx, Ly, gam, orth):
     assert events > 50
 
 
-def test_event_driven_pm_2d_separable_pass_matches_product_taps_and_oracle(P, monkeypatch):
+@pytest.mark.parametrize("Lx,Ly,gam,steps,min_events", [(12, 10, 3.0, 20, 100), (28, 27, 10.0, 2, 200)])
+def test_event_driven_pm_2d_separable_pass_matches_product_taps_and_oracle(P, monkeypatch, Lx, Ly, gam, steps,
+                                                                           min_events):
     """NEXT-4 on a 2d lattice: the separable pass (x-axis taps into a scratch copy, then y-axis taps
     with the rank-1 term; the default) and the (2w+1)^2 product taps in one kernel
     (TRAJ_EV_SEPARABLE=0) give the same trajectory, and both follow the oracle's literal L x L
-    algorithm on a non-square lattice."""
+    algorithm on a non-square lattice.  12 x 10: both halves one CTA per row (the rings
+    are too short for the row-blocked kernel); 28 x 27 at a high event rate (short waiting times,
+    narrow bands): both halves on the row-blocked ring kernel, ragged last row blocks on both axes."""
     from oracle.pm_events import EventPM
-    Lx, Ly, gam = 12, 10, 3.0
     A = np.arange(Lx * Ly // 2)
     res = {}
     for sep in ("1", "0"):
@@ -640,7 +643,7 @@ def test_event_driven_pm_2d_separable_pass_matches_product_taps_and_oracle(P, mo
         g = P.Trajectories(Lx, Ly, "projective_events", [gam], seed=5)
         o = EventPM(Lx, Ly, gam, 0.05, seed=5, traj=0)
         events = 0
-        for s in range(20):
+        for s in range(steps):
             g.step(1)
             n0 = len(o.log)
             o.step(1)
@@ -648,7 +651,7 @@ def test_event_driven_pm_2d_separable_pass_matches_product_taps_and_oracle(P, mo
             assert nev == len(o.log) - n0
             assert nocc == sum(1 for e in o.log[n0:] if e[3])
             events += nev
-        assert events > 100
+        assert events > min_events
         C = g.correlation(0).cpu().numpy()
         assert np.abs(C - o.correlation()).max() < C_TOL
         assert abs(g.entropy(A)[0] - o.entropy(A)) < S_TOL
